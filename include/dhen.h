@@ -1,0 +1,167 @@
+/* dhen.h — C ABI of the B200-native DHEN layer-stack training path.
+ *
+ * DHEN (arXiv 2203.11014, "PAPER.md" = P:<line>): a stack of layers, each
+ *   Y = Norm( Concat_i Interaction_i(X_n) + ShortCut(X_n) )          (Eq.(1))
+ *   ShortCut(X_n) = X_n if len(X_n) == len(Y) else W_n^T X_n          (Eq.(2))
+ * over the embedding list X_n (stored [B][m][d], row t = the paper's x^t),
+ * with interaction modules Dot (Eq.(3)), SelfAttention (Eq.(4)), Conv (Eq.(5)),
+ * Linear (Eq.(6)), DCN cross (Eq.(7), north-star DCN-v2 reading) and an MLP
+ * single-tensor module.  Readings of silent passages: DESIGN.md §3.
+ *
+ * Memory ownership: the CALLER owns all device memory.  dhen_sizes() reports
+ * how many bytes of `state` (parameters, master weights, gradients) and `work`
+ * (saved activations + scratch, sized for batch_max_local) the library needs;
+ * the caller allocates both (16-byte aligned; PyTorch in the Python binding)
+ * and passes them to dhen_init(), which carves them.  They must outlive ctx.
+ * Tensor arguments x/y/dy/dx/x0/dx0 are device pointers in the config's dtype
+ * (fp32 or bf16), row-major [B][m][d], 16-byte aligned; labels/loss are fp32
+ * device pointers.  Every call is stream-ordered on `stream` (a cudaStream_t;
+ * NULL = legacy default stream) and returns before the GPU work finishes; the
+ * caller keeps its buffers alive until the stream completes.
+ *
+ * Errors: every entry point returns a dhen_status.  A call that fails its
+ * validation launches nothing (no partial updates).  dhen_last_error()
+ * returns a thread-local message naming the call and the offending values.
+ * Asynchronous CUDA faults surface as DHEN_E_CUDA on a later call.  No C++
+ * exception crosses this boundary.  A ctx is used from one host thread.
+ *
+ * Collectives: with world > 1 the library owns an NCCL communicator (bootstrap
+ * id from dhen_nccl_id() on rank 0, broadcast by the caller), shards every
+ * parameter group across ranks (FSDP; on one host HSDP == FSDP,
+ * P:171) and all ranks must make the same sequence of collective calls
+ * (dhen_layer_fwd / dhen_layer_bwd / dhen_train_step).
+ */
+#ifndef DHEN_H_
+#define DHEN_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dhen_ctx dhen_ctx;
+
+typedef enum {
+  DHEN_OK = 0,
+  DHEN_E_CONFIG = 1,    /* invalid dhen_config / dhen_dist                      */
+  DHEN_E_SHAPE = 2,     /* B out of range, bad layer / group index            */
+  DHEN_E_ALIGN = 3,     /* a pointer not 16-byte aligned, or NULL             */
+  DHEN_E_STATE = 4,     /* call out of order (bwd without fwd, ...)           */
+  DHEN_E_CUDA = 5,      /* CUDA runtime / driver error                        */
+  DHEN_E_NCCL = 6,      /* NCCL error                                          */
+  DHEN_E_NONFINITE = 7, /* non-finite loss                             */
+  DHEN_E_NOMEM = 8      /* caller buffers smaller than dhen_sizes() reported   */
+} dhen_status;
+
+/* Interaction module kinds. */
+typedef enum {
+  DHEN_DOT = 0,    /* Eq.(3): z = triu(X X^T) (strict, row-major pairs), U = reshape(W_m z, l, d)  */
+  DHEN_ATTN = 1,   /* Eq.(4): U = W_u^T TransformerEncoderLayer(X) (post-norm, ReLU, no key bias)  */
+  DHEN_CONV = 2,   /* Eq.(5): U = W_u^T ((1/C) sum_c K_c (*) X), same zero padding, no bias         */
+  DHEN_DCN = 3,    /* Eq.(7) north star: T = X (.) (X W^T + b) + X per token, U = W_u^T T          */
+  DHEN_LINEAR = 4, /* Eq.(6): U = W^T X on the token axis                                          */
+  DHEN_MLP = 5     /* U = reshape(W_m relu(W_2 relu(W_1 vec(X) + b_1) + b_2), l, d)           */
+} dhen_kind;
+
+typedef enum { DHEN_FP32 = 0, DHEN_BF16 = 1 } dhen_dtype;
+
+typedef struct {
+  int kind;          /* dhen_kind                                   */
+  int l;             /* output token count l_i >= 1          */
+  int heads;         /* ATTN: heads H, d % H == 0 (0 -> 2)          */
+  int ffn_mult;      /* ATTN: FFN width = ffn_mult * d (0 -> 4)     */
+  int conv_channels; /* CONV: C filters (0 -> 4)                    */
+  int conv_k;        /* CONV: odd kernel extent k (0 -> 3)          */
+  int mlp_hidden[2]; /* MLP: hidden widths (0 -> 1024)              */
+} dhen_module;
+
+typedef struct {
+  int n_modules;
+  const dhen_module* modules; /* ensemble = concat along tokens in this order */
+} dhen_layer;
+
+typedef struct {
+  int m0;                 /* input token count m of X_0             */
+  int d;                  /* embedding dim, d % 8 == 0                      */
+  int n_layers;
+  const dhen_layer* layers;
+  int dtype;              /* dhen_dtype: storage / compute-operand dtype    */
+  float ln_eps;           /* LayerNorm epsilon (0 -> 1e-5)                  */
+  int batch_max_local;    /* largest per-rank B any call will use          */
+  unsigned long long seed;/* parameter init seed                            */
+} dhen_config;
+
+typedef struct {
+  int rank, world;              /* world == 1: no NCCL                          */
+  unsigned char nccl_id[128];   /* ncclUniqueId from rank 0 (world > 1)         */
+  int fsdp;                     /* 1: fully sharded (default); 0: replicated DP */
+} dhen_dist;
+
+/* Host-only, pure: validates a config (preconditions S:186, S:195, S:204,
+ * l >= 1, d % 8 == 0, d % heads == 0).  DHEN_E_CONFIG with a message. */
+dhen_status dhen_validate(const dhen_config* cfg);
+
+/* Host-only: bytes of caller-provided `state` and `work` device memory. */
+dhen_status dhen_sizes(const dhen_config* cfg, const dhen_dist* dist,
+                       size_t* state_bytes, size_t* work_bytes);
+
+/* Host-only: total / per-rank-shard element counts of parameter group g
+ * (g in [0, n_layers) = layer g, g == n_layers = head).  Canonical order:
+ * DESIGN.md §2 table. */
+dhen_status dhen_group_numel(const dhen_config* cfg, const dhen_dist* dist, int group,
+                             size_t* numel, size_t* shard_numel);
+
+/* Rank 0: a fresh NCCL unique id (128 bytes) to broadcast to the other ranks. */
+dhen_status dhen_nccl_id(unsigned char out[128]);
+
+/* Carve state/work, initialise parameters from cfg->seed (U(+-1/sqrt(fan_in)),
+ * LN gamma = 1, beta = 0), create the NCCL communicator when world > 1 (a
+ * collective over all ranks).  Launches on `stream`. */
+dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state, size_t state_bytes,
+                      void* work, size_t work_bytes, void* stream, dhen_ctx** out);
+
+/* Forward of layer n: x [B][m_in][d] -> y [B][m_out][d] (Eq.(1)(2)).  Saves
+ * the activations layer n's backward needs (x is referenced, not copied: keep
+ * it unchanged until dhen_layer_bwd(n) returns).  Collective when world > 1. */
+dhen_status dhen_layer_fwd(dhen_ctx* ctx, int layer, const void* x, void* y, int B, void* stream);
+
+/* Backward of layer n given dy [B][m_out][d]: accumulates (+=) the layer's
+ * parameter gradients and writes dx [B][m_in][d] (dx may be NULL).
+ * Requires a preceding dhen_layer_fwd(n) with the same B (else DHEN_E_STATE).
+ * With world > 1, gradients are reduce-scattered to the owner shards. */
+dhen_status dhen_layer_bwd(dhen_ctx* ctx, int layer, const void* dy, void* dx, int B, void* stream);
+
+/* One training step on the local batch x0 [B][m0][d], labels [B] (0/1 fp32):
+ * zero grads, forward all layers, head z_b = w_h . mean_t Y_N[b,t] + b_h,
+ * loss = sum_b BCEWithLogits(z_b, y_b) / B_global (R17, R21), backward,
+ * reduce-scatter (world > 1), SGD theta -= lr * g on fp32 masters (R18).
+ * loss_dev (nullable, fp32 device scalar) receives the loss of this rank's
+ * samples (sum over ranks = global loss).  dx0 (nullable) receives dL/dx0. */
+dhen_status dhen_train_step(dhen_ctx* ctx, const void* x0, const float* labels, int B, int B_global,
+                            float lr, float* loss_dev, void* dx0, void* stream);
+
+/* Forward of the whole stack + head without backward: logits_dev [B] fp32. */
+dhen_status dhen_forward(dhen_ctx* ctx, const void* x0, int B, float* logits_dev, void* stream);
+
+dhen_status dhen_zero_grad(dhen_ctx* ctx, void* stream);
+
+/* Canonical fp32 parameters of group g: set == 1 copies host -> master
+ * weights (and refreshes the compute copy), set == 0 copies masters -> host.
+ * `host` holds dhen_group_numel() floats.  Synchronises `stream`. */
+dhen_status dhen_params_io(dhen_ctx* ctx, int group, float* host, int set, void* stream);
+
+/* Accumulated fp32 gradients of group g (reduced over ranks when world > 1)
+ * -> host.  Synchronises `stream`. */
+dhen_status dhen_grads_get(dhen_ctx* ctx, int group, float* host, void* stream);
+
+/* Number of library kernels launched since init (a host-side counter). */
+unsigned long long dhen_launch_count(const dhen_ctx* ctx);
+
+const char* dhen_last_error(void);
+void dhen_destroy(dhen_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DHEN_H_ */

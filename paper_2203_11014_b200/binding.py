@@ -1,0 +1,273 @@
+"""Thin ctypes binding of libdhen.so (include/dhen.h).  Argument marshalling
+only: every step of the DHEN path runs in the library's CUDA kernels; torch
+provides device memory, streams and process groups.  There is no fallback: if
+the library (or a GPU) is missing, calls raise."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdhen.so")
+
+DOT, ATTN, CONV, DCN, LINEAR, MLP = range(6)
+KIND_IDS = {"dot": DOT, "attn": ATTN, "conv": CONV, "dcn": DCN, "linear": LINEAR, "mlp": MLP}
+FP32, BF16 = 0, 1
+
+STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_SHAPE", 3: "E_ALIGN", 4: "E_STATE", 5: "E_CUDA", 6: "E_NCCL",
+          7: "E_NONFINITE", 8: "E_NOMEM"}
+
+# every symbol include/dhen.h declares
+EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "dhen_init", "dhen_layer_fwd",
+           "dhen_layer_bwd", "dhen_train_step", "dhen_forward", "dhen_zero_grad", "dhen_params_io",
+           "dhen_grads_get", "dhen_launch_count", "dhen_last_error", "dhen_destroy")
+
+
+class dhen_module(C.Structure):
+    _fields_ = [("kind", C.c_int), ("l", C.c_int), ("heads", C.c_int), ("ffn_mult", C.c_int),
+                ("conv_channels", C.c_int), ("conv_k", C.c_int), ("mlp_hidden", C.c_int * 2)]
+
+
+class dhen_layer(C.Structure):
+    _fields_ = [("n_modules", C.c_int), ("modules", C.POINTER(dhen_module))]
+
+
+class dhen_config(C.Structure):
+    _fields_ = [("m0", C.c_int), ("d", C.c_int), ("n_layers", C.c_int), ("layers", C.POINTER(dhen_layer)),
+                ("dtype", C.c_int), ("ln_eps", C.c_float), ("batch_max_local", C.c_int),
+                ("seed", C.c_ulonglong)]
+
+
+class dhen_dist(C.Structure):
+    _fields_ = [("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.c_ubyte * 128), ("fsdp", C.c_int)]
+
+
+class DhenError(RuntimeError):
+    def __init__(self, call, status, msg):
+        super().__init__(f"{call} -> DHEN_{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libdhen.so (build it first with paper_2203_11014_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} missing: run `python -m paper_2203_11014_b200.build`")
+    lib = C.CDLL(path)
+    vp, i, sz = C.c_void_p, C.c_int, C.c_size_t
+    sig = {
+        "dhen_validate": [C.POINTER(dhen_config)],
+        "dhen_sizes": [C.POINTER(dhen_config), C.POINTER(dhen_dist), C.POINTER(sz), C.POINTER(sz)],
+        "dhen_group_numel": [C.POINTER(dhen_config), C.POINTER(dhen_dist), i, C.POINTER(sz), C.POINTER(sz)],
+        "dhen_nccl_id": [C.POINTER(C.c_ubyte)],
+        "dhen_init": [C.POINTER(dhen_config), C.POINTER(dhen_dist), vp, sz, vp, sz, vp, C.POINTER(vp)],
+        "dhen_layer_fwd": [vp, i, vp, vp, i, vp],
+        "dhen_layer_bwd": [vp, i, vp, vp, i, vp],
+        "dhen_train_step": [vp, vp, vp, i, i, C.c_float, vp, vp, vp],
+        "dhen_forward": [vp, vp, i, vp, vp],
+        "dhen_zero_grad": [vp, vp],
+        "dhen_params_io": [vp, i, vp, i, vp],
+        "dhen_grads_get": [vp, i, vp, vp],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = C.c_int
+    lib.dhen_last_error.restype = C.c_char_p
+    lib.dhen_last_error.argtypes = []
+    lib.dhen_launch_count.restype = C.c_ulonglong
+    lib.dhen_launch_count.argtypes = [vp]
+    lib.dhen_destroy.restype = None
+    lib.dhen_destroy.argtypes = [vp]
+    _lib = lib
+    return lib
+
+
+def _check(call, st):
+    if st != 0:
+        raise DhenError(call, st, load().dhen_last_error().decode())
+
+
+@dataclass
+class Module:
+    kind: str
+    l: int
+    heads: int = 2
+    ffn_mult: int = 4
+    conv_channels: int = 4
+    conv_k: int = 3
+    mlp_hidden: Sequence[int] = (1024, 1024)
+
+
+@dataclass
+class Config:
+    m0: int
+    d: int
+    layers: List[List[Module]]
+    dtype: str = "bf16"
+    batch_max_local: int = 1
+    ln_eps: float = 1e-5
+    seed: int = 0
+    _keep: list = field(default_factory=list, repr=False)
+
+    def to_c(self) -> dhen_config:
+        layers = (dhen_layer * len(self.layers))()
+        keep = [layers]
+        for n, L in enumerate(self.layers):
+            mods = (dhen_module * len(L))()
+            for i, s in enumerate(L):
+                mods[i].kind = KIND_IDS[s.kind]
+                mods[i].l = s.l
+                mods[i].heads = s.heads
+                mods[i].ffn_mult = s.ffn_mult
+                mods[i].conv_channels = s.conv_channels
+                mods[i].conv_k = s.conv_k
+                mods[i].mlp_hidden[0] = s.mlp_hidden[0]
+                mods[i].mlp_hidden[1] = s.mlp_hidden[1]
+            layers[n].n_modules = len(L)
+            layers[n].modules = C.cast(mods, C.POINTER(dhen_module))
+            keep.append(mods)
+        self._keep = keep
+        return dhen_config(self.m0, self.d, len(self.layers), C.cast(layers, C.POINTER(dhen_layer)),
+                           BF16 if self.dtype == "bf16" else FP32, self.ln_eps, self.batch_max_local, self.seed)
+
+    def dims(self):
+        out, m = [], self.m0
+        for L in self.layers:
+            mo = sum(s.l for s in L)
+            out.append((m, mo))
+            m = mo
+        return out
+
+
+def make_dist(rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, fsdp: bool = True) -> dhen_dist:
+    d = dhen_dist()
+    d.rank, d.world, d.fsdp = rank, world, int(fsdp)
+    if nccl_id is not None:
+        for k in range(128):
+            d.nccl_id[k] = nccl_id[k]
+    return d
+
+
+def validate(cfg: Config) -> None:
+    c = cfg.to_c()
+    _check("dhen_validate", load().dhen_validate(C.byref(c)))
+
+
+def sizes(cfg: Config, dist: Optional[dhen_dist] = None):
+    c = cfg.to_c()
+    s, w = C.c_size_t(), C.c_size_t()
+    _check("dhen_sizes", load().dhen_sizes(C.byref(c), C.byref(dist or make_dist()), C.byref(s), C.byref(w)))
+    return s.value, w.value
+
+
+def group_numel(cfg: Config, group: int, dist: Optional[dhen_dist] = None):
+    c = cfg.to_c()
+    n, sh = C.c_size_t(), C.c_size_t()
+    _check("dhen_group_numel", load().dhen_group_numel(C.byref(c), C.byref(dist or make_dist()), group,
+                                                       C.byref(n), C.byref(sh)))
+    return n.value, sh.value
+
+
+def nccl_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _check("dhen_nccl_id", load().dhen_nccl_id(buf))
+    return bytes(buf)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class DHEN:
+    """A DHEN stack bound to the current CUDA device.  State and work memory are
+    torch uint8 CUDA tensors handed to the library (which carves them)."""
+
+    def __init__(self, cfg: Config, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
+                 fsdp: bool = True, stream=None):
+        import torch
+        self.torch = torch
+        self.cfg = cfg
+        self.lib = load()
+        self.dist = make_dist(rank, world, nccl_id, fsdp)
+        self._c = cfg.to_c()
+        sb, wb = sizes(cfg, self.dist)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.state = torch.empty(sb, dtype=torch.uint8, device=dev)
+        self.work = torch.empty(wb, dtype=torch.uint8, device=dev)
+        self.dtype = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+        ctx = C.c_void_p()
+        _check("dhen_init", self.lib.dhen_init(C.byref(self._c), C.byref(self.dist), _ptr(self.state), sb,
+                                               _ptr(self.work), wb, self._stream(stream), C.byref(ctx)))
+        self.ctx = ctx
+        self.n_groups = len(cfg.layers) + 1
+
+    def _stream(self, stream=None):
+        s = stream if stream is not None else self.torch.cuda.current_stream()
+        return C.c_void_p(s.cuda_stream)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.dhen_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launches(self) -> int:
+        return int(self.lib.dhen_launch_count(self.ctx))
+
+    def numel(self, group: int) -> int:
+        return group_numel(self.cfg, group, self.dist)[0]
+
+    def set_params(self, group: int, flat, stream=None):
+        import numpy as np
+        a = np.ascontiguousarray(flat, dtype=np.float32)
+        assert a.size == self.numel(group), (a.size, self.numel(group))
+        _check("dhen_params_io", self.lib.dhen_params_io(self.ctx, group, a.ctypes.data_as(C.c_void_p), 1,
+                                                         self._stream(stream)))
+
+    def get_params(self, group: int, stream=None):
+        import numpy as np
+        a = np.zeros(self.numel(group), np.float32)
+        _check("dhen_params_io", self.lib.dhen_params_io(self.ctx, group, a.ctypes.data_as(C.c_void_p), 0,
+                                                         self._stream(stream)))
+        return a
+
+    def get_grads(self, group: int, stream=None):
+        import numpy as np
+        a = np.zeros(self.numel(group), np.float32)
+        _check("dhen_grads_get", self.lib.dhen_grads_get(self.ctx, group, a.ctypes.data_as(C.c_void_p),
+                                                         self._stream(stream)))
+        return a
+
+    def zero_grad(self, stream=None):
+        _check("dhen_zero_grad", self.lib.dhen_zero_grad(self.ctx, self._stream(stream)))
+
+    def layer_fwd(self, n, x, y, stream=None):
+        _check("dhen_layer_fwd", self.lib.dhen_layer_fwd(self.ctx, n, _ptr(x), _ptr(y), x.shape[0],
+                                                         self._stream(stream)))
+
+    def layer_bwd(self, n, dy, dx, stream=None):
+        _check("dhen_layer_bwd", self.lib.dhen_layer_bwd(self.ctx, n, _ptr(dy), _ptr(dx), dy.shape[0],
+                                                         self._stream(stream)))
+
+    def train_step(self, x0, labels, lr, B_global=None, loss=None, dx0=None, stream=None):
+        B = x0.shape[0]
+        _check("dhen_train_step", self.lib.dhen_train_step(self.ctx, _ptr(x0), _ptr(labels), B,
+                                                           B_global or B, float(lr), _ptr(loss), _ptr(dx0),
+                                                           self._stream(stream)))
+
+    def forward(self, x0, logits, stream=None):
+        _check("dhen_forward", self.lib.dhen_forward(self.ctx, _ptr(x0), x0.shape[0], _ptr(logits),
+                                                     self._stream(stream)))

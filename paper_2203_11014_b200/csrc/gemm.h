@@ -1,0 +1,74 @@
+// gemm.h — the generic strided/batched contraction every DHEN step lowers to.
+//
+//   C[z][i][j]  (epilogue)=  alpha * sum_k A[z][i][k] * B[z][k][j]
+//
+// A, B are bf16 or fp32 (same dtype); accumulation is fp32 (TMEM on the
+// tcgen05 path, registers on the SIMT path; never TF32).  Each operand is a
+// strided view; the K index may be two-level (k -> (k / kdiv, k % kdiv)) so a
+// reduction over (sample, dim) pairs — the token-mixing weight gradients,
+// B4/B3 in SURVEY §8(a) — is one GEMM.  The epilogue fuses bias (with an
+// optional zero gap, for the key-bias-free QKV projection, R10), the DCN cross
+// x ⊙ (acc + b) + x (F8), ReLU, ReLU-mask (backward), residual add and
+// accumulation (+=) into C.
+#pragma once
+#include "common.cuh"
+
+namespace dhen {
+
+struct Operand {            // A: (z, i, k) ; B: (z, k, j)
+  const void* ptr;
+  int dt;
+  int64_t s_mn;             // stride of i (A) / j (B)
+  int64_t s_k;              // stride of the inner k index
+  int64_t s_ko;             // stride of the outer k index (k / kdiv); kdiv == 0: single-level
+  int kdiv;
+  int64_t bs0, bs1;         // batch strides (z / zdiv, z % zdiv)
+  int zdiv;
+  __host__ __device__ int64_t off(int64_t z, int64_t mn, int64_t k) const {
+    int64_t ko = kdiv ? (k / kdiv) : 0, ki = kdiv ? (k % kdiv) : k;
+    return (z / zdiv) * bs0 + (z % zdiv) * bs1 + mn * s_mn + ki * s_k + ko * s_ko;
+  }
+};
+
+inline Operand operand(const void* p, int dt, int64_t s_mn, int64_t s_k, int64_t bs0 = 0, int64_t bs1 = 0,
+                       int zdiv = 1, int kdiv = 0, int64_t s_ko = 0) {
+  Operand o;
+  o.ptr = p; o.dt = dt; o.s_mn = s_mn; o.s_k = s_k; o.s_ko = s_ko; o.kdiv = kdiv;
+  o.bs0 = bs0; o.bs1 = bs1; o.zdiv = zdiv;
+  return o;
+}
+
+struct Epilogue {
+  float alpha = 1.f;
+  const void* bias = nullptr;   // indexed by j, dtype bias_dt
+  int bias_dt = F32;
+  int bias_gap_lo = 0, bias_gap_hi = 0;   // j in [lo, hi) -> no bias; j >= hi -> bias[j - (hi - lo)]
+  int relu = 0;
+  View mask = noview();         // out *= (mask > 0)           (ReLU backward)
+  View cross = noview();        // DCN: aux <- out; out = x * out + x
+  View aux = noview();
+  View resid = noview();        // out += resid
+  int accumulate = 0;           // out += C (C read in its own dtype)
+};
+
+struct Gemm {
+  int M, N, K, batch;
+  Operand a, b;
+  View c;
+  Epilogue e;
+};
+
+struct Workspace {              // scratch for split-K partials (fp32)
+  float* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+// Launch counter (reported as gpu_launches by the bench).
+extern unsigned long long g_launches;
+
+// Dispatch: tcgen05/TMA path when the shapes and layouts allow it, the SIMT
+// path (exact fp32 FMA; the fp32 mode and odd shapes) otherwise.
+cudaError_t gemm_run(const Gemm& g, const Workspace& ws, cudaStream_t st);
+cudaError_t gemm_simt(const Gemm& g, const Workspace& ws, cudaStream_t st);
+
+}  // namespace dhen

@@ -1,0 +1,156 @@
+// gemm_simt.cu — exact-FP32-FMA tiled GEMM over strided views (the fp32 mode,
+// never TF32) and the fallback for shapes the tcgen05 path does not
+// take.  64x64x16 tiles, 256 threads, 4x4 outputs per thread, deterministic
+// split-K (fixed-order second pass) for long reductions.
+#include "gemm.h"
+#include <algorithm>
+
+namespace dhen {
+
+unsigned long long g_launches = 0;
+
+__device__ __forceinline__ void epi_apply(const Gemm& g, int z, int i, int j, float acc) {
+  const Epilogue& e = g.e;
+  float v = acc * e.alpha;
+  if (e.bias) {
+    int bj = j;
+    bool has = true;
+    if (e.bias_gap_hi > e.bias_gap_lo) {
+      if (j >= e.bias_gap_lo && j < e.bias_gap_hi) has = false;
+      else if (j >= e.bias_gap_hi) bj = j - (e.bias_gap_hi - e.bias_gap_lo);
+    }
+    if (has) v += ld_as_f32(e.bias, bj, e.bias_dt);
+  }
+  if (e.cross.ptr) {
+    if (e.aux.ptr) st_from_f32(e.aux.ptr, e.aux.off(z, i, j), e.aux.dt, v);
+    float x = ld_as_f32(e.cross.ptr, e.cross.off(z, i, j), e.cross.dt);
+    v = x * v + x;
+  } else if (e.aux.ptr) {
+    st_from_f32(e.aux.ptr, e.aux.off(z, i, j), e.aux.dt, v);
+  }
+  if (e.relu) v = fmaxf(v, 0.f);
+  if (e.mask.ptr) {
+    float mv = ld_as_f32(e.mask.ptr, e.mask.off(z, i, j), e.mask.dt);
+    v = mv > 0.f ? v : 0.f;
+  }
+  if (e.resid.ptr) v += ld_as_f32(e.resid.ptr, e.resid.off(z, i, j), e.resid.dt);
+  int64_t co = g.c.off(z, i, j);
+  if (e.accumulate) v += ld_as_f32(g.c.ptr, co, g.c.dt);
+  st_from_f32(g.c.ptr, co, g.c.dt, v);
+}
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(Gemm g, int splits, int kchunk, float* ws, int zbase) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int zb = zbase + blockIdx.z / splits, sp = blockIdx.z % splits;
+  const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
+  const int kbeg = sp * kchunk;
+  const int kend = min(g.K, kbeg + kchunk);
+  const T* A = static_cast<const T*>(g.a.ptr);
+  const T* Bp = static_cast<const T*>(g.b.ptr);
+  const bool a_kc = (g.a.s_k == 1);   // k contiguous in A
+  const bool b_kc = (g.b.s_k == 1);
+  const int tx = tid % 16, ty = tid / 16;
+  float acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
+
+  for (int k0 = kbeg; k0 < kend; k0 += BK) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int e = tid + 256 * q;
+      int ii, kk;
+      if (a_kc) { ii = e / BK; kk = e % BK; } else { kk = e / BM; ii = e % BM; }
+      int gi = i0 + ii, gk = k0 + kk;
+      float v = 0.f;
+      if (gi < g.M && gk < kend) v = tof<T>(A[g.a.off(zb, gi, gk)]);
+      As[kk][ii] = v;
+      int jj;
+      if (b_kc) { jj = e / BK; kk = e % BK; } else { kk = e / BN; jj = e % BN; }
+      int gj = j0 + jj;
+      gk = k0 + kk;
+      v = 0.f;
+      if (gj < g.N && gk < kend) v = tof<T>(Bp[g.b.off(zb, gj, gk)]);
+      Bs[kk][jj] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = As[kk][ty * 4 + r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx * 4 + c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      int i = i0 + ty * 4 + r, j = j0 + tx * 4 + c;
+      if (i < g.M && j < g.N) {
+        if (splits == 1) epi_apply(g, zb, i, j, acc[r][c]);
+        else ws[((int64_t)(zb * splits + sp) * g.M + i) * g.N + j] = acc[r][c];
+      }
+    }
+}
+
+__global__ void splitk_reduce_kernel(Gemm g, int splits, const float* ws) {
+  int64_t total = (int64_t)g.batch * g.M * g.N;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t zb = t / ((int64_t)g.M * g.N);
+    int64_t r = t % ((int64_t)g.M * g.N);
+    int i = (int)(r / g.N), j = (int)(r % g.N);
+    float s = 0.f;
+    for (int sp = 0; sp < splits; ++sp) s += ws[((zb * splits + sp) * g.M + i) * (int64_t)g.N + j];
+    epi_apply(g, (int)zb, i, j, s);
+  }
+}
+
+cudaError_t gemm_simt(const Gemm& g, const Workspace& ws, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
+  int tm = (g.M + BM - 1) / BM, tn = (g.N + BN - 1) / BN;
+  int64_t tiles = (int64_t)tm * tn * g.batch;
+  int splits = 1;
+  if (g.K > 512 && tiles < 2 * 148) {
+    splits = (int)std::min<int64_t>((2 * 148 + tiles - 1) / tiles, (g.K + 255) / 256);
+    int64_t need = (int64_t)splits * g.batch * g.M * g.N * 4;
+    while (splits > 1 && need > (int64_t)ws.bytes) {
+      --splits;
+      need = (int64_t)splits * g.batch * g.M * g.N * 4;
+    }
+  }
+  int kchunk = (g.K + splits - 1) / splits;
+  kchunk = (kchunk + BK - 1) / BK * BK;
+  if (g.K <= 0) kchunk = 0;
+  const int zmax = 65535 / splits;
+  for (int zb = 0; zb < g.batch; zb += zmax) {
+    int nz = std::min(zmax, g.batch - zb);
+    dim3 grid(tn, tm, nz * splits);
+    if (g.a.dt == F32)
+      gemm_simt_kernel<float><<<grid, 256, 0, st>>>(g, splits, kchunk, ws.ptr, zb);
+    else
+      gemm_simt_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(g, splits, kchunk, ws.ptr, zb);
+    ++g_launches;
+  }
+  if (splits > 1) {
+    int64_t total = (int64_t)g.batch * g.M * g.N;
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g, splits, ws.ptr);
+    ++g_launches;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace dhen

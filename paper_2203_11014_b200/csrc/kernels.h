@@ -1,0 +1,61 @@
+// kernels.h — launchers of the non-GEMM DHEN kernels (sm_100a).  Every launcher
+// enqueues on `st`, counts its launches in g_launches and returns the launch error.
+#pragma once
+#include "common.cuh"
+
+namespace dhen {
+
+extern unsigned long long g_launches;
+
+// F1: Z[b][p] = G[b][i][j] for i < j, p row-major (R7).  G fp32 [B][m][m].
+cudaError_t triu_extract(const float* G, void* Z, int dt, int B, int m, int64_t ldz, cudaStream_t st);
+// B5: S[b][i][j] = S[b][j][i] = dZ[b][p(i,j)], S[b][i][i] = 0.
+cudaError_t sym_from_triu(const void* dZ, void* S, int dt, int B, int m, int64_t ldz, cudaStream_t st);
+
+// F12 / encoder LN1, LN2: R = U (+ addx), Y = gamma (R - mu) rstd + beta per row of d.
+// U fp32 [rows][d]; addx (dt) nullable; Y, Rsave dtype dt; mu, rstd fp32 [rows].
+cudaError_t ln_fwd(const float* U, const void* addx, const void* gamma, const void* beta, int pdt, float eps,
+                   int64_t rows, int d, void* Y, void* Rsave, float* mu, float* rstd, int dt, cudaStream_t st);
+// B2: dR = rstd (g - mean g - xh mean(g xh)), g = dY * gamma, xh from Rsave.  dR stored (dt);
+// acc_mode 1: acc = dR, 2: acc += dR (fp32 rows x d).  dgamma/dbeta += sums (deterministic).
+cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
+                   const void* gamma, int pdt, int64_t rows, int d, void* dR, int dt, float* acc, int acc_mode,
+                   float* dgamma, float* dbeta, float* scratch, size_t scratch_bytes, cudaStream_t st);
+
+// out[c] += sum_r src[r * ld + c] for c < cols (deterministic two-pass).
+cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t ld, float* out,
+                       float* scratch, size_t scratch_bytes, cudaStream_t st);
+
+// F4 softmax over rows of S (fp32) -> P (dt).  B6: dS = scale * P (dP - rowsum(P dP)).
+cudaError_t softmax_rows(const float* S, void* P, int dt, int64_t rows, int n, cudaStream_t st);
+cudaError_t softmax_bwd(const void* P, const float* dP, void* dS, int dt, int64_t rows, int n, float scale,
+                        cudaStream_t st);
+
+// B8 elementwise: dA = dT * X (dt); acc += dT * A + dT.
+cudaError_t dcn_bwd_elem(const void* dT, const void* X, const void* A, void* dA, float* acc, int dt, int64_t n,
+                         cudaStream_t st);
+
+// F7 / B7: 1-channel m x d image, C k x k filters folded to their mean (exact), zero padding.
+cudaError_t conv_fwd(const void* X, const void* K, int pdt, int C, int k, int B, int m, int d, void* T, int dt,
+                     cudaStream_t st);
+cudaError_t conv_dgrad(const void* dT, const void* K, int pdt, int C, int k, int B, int m, int d, float* acc, int dt,
+                       cudaStream_t st);
+cudaError_t conv_wgrad(const void* dT, const void* X, int C, int k, int B, int m, int d, int dt, float* dK,
+                       float* scratch, size_t scratch_bytes, cudaStream_t st);
+
+// F13 / B1: z_b = w . mean_t Y[b,t] + b_h; loss_b = BCE(z_b, y_b); dz_b = (sigma(z_b) - y_b) / Bg;
+// dY[b,t,c] = dz_b w[c] / m (dt).  Then loss_out = sum_b loss_b / Bg, dw += sum dz pooled, db += sum dz.
+cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, const float* labels, int B, int m, int d,
+                         int Bg, void* dY, int dt, float* pooled, float* z, float* lossb, float* dz, float* loss_out,
+                         float* dw, float* db, int do_bwd, cudaStream_t st);
+
+// SGD (R18): master -= lr * grad; copy = (dt) master.  lr == 0 with grad == NULL: refresh copy only.
+cudaError_t sgd_cast(float* master, const float* grad, float lr, void* copy, int dt, int64_t n, cudaStream_t st);
+cudaError_t cast(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t st);
+// parameter init: uniform(-bound, bound) from a counter-based hash of (seed, index), or a constant.
+// element i gets the value of tensor index idx0 + i (sharded init gives the same tensor at any world size)
+cudaError_t init_uniform(float* p, int64_t n, float bound, unsigned long long seed, unsigned long long stream_id,
+                         int64_t idx0, cudaStream_t st);
+cudaError_t fill(float* p, int64_t n, float v, cudaStream_t st);
+
+}  // namespace dhen

@@ -1,0 +1,929 @@
+// runtime.cu — the C ABI (include/dhen.h) and the DHEN layer-stack runtime:
+// config validation, canonical parameter layout, carving of caller-provided
+// memory, per-layer forward/backward as sequences of our kernels, head + loss,
+// SGD, and FSDP parameter all-gather / gradient reduce-scatter over NCCL.
+//
+// Forward of layer n (Eq.(1)(2)): each module
+// writes its l_i output tokens into an fp32 concat buffer Ucat at token offset
+// sum_{j<i} l_j; the shortcut (W_n^T X when the token counts differ) is
+// accumulated into Ucat; the LN kernel adds the identity shortcut, normalises
+// and writes Y.  Backward mirrors it (B1-B12).  bf16 storage points are listed
+// in DESIGN.md §4 and mirrored by the oracle's Precision.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dhen.h"
+#include "gemm.h"
+#include "kernels.h"
+
+using namespace dhen;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string t_err;
+static dhen_status fail(dhen_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return s;
+}
+#define CK(call)                                                                               \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) return fail(DHEN_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define NK(call)                                                                               \
+  do {                                                                                         \
+    ncclResult_t r_ = (call);                                                                  \
+    if (r_ != ncclSuccess) return fail(DHEN_E_NCCL, "%s: %s", #call, ncclGetErrorString(r_));  \
+  } while (0)
+#define RET(call)                         \
+  do {                                    \
+    dhen_status s_ = (call);              \
+    if (s_ != DHEN_OK) return s_;         \
+  } while (0)
+
+// ------------------------------------------------------------------ plan structures
+namespace {
+
+struct Mod {
+  dhen_module s;
+  int off_tok = 0;   // token offset of this module's outputs in the concat
+  // parameter offsets inside the layer group (canonical order)
+  int64_t W = -1, b = -1, Wu = -1, Wm = -1, K = -1;
+  int64_t Wq = -1, Wo = -1, bq = -1, bo = -1, g1 = -1, be1 = -1, g2 = -1, be2 = -1, W1 = -1, b1 = -1, W2 = -1, b2 = -1;
+  // saved activations (work)
+  void *Z = nullptr, *A = nullptr, *T = nullptr, *QKV = nullptr, *P = nullptr, *O = nullptr, *R1 = nullptr,
+       *Z1 = nullptr, *F = nullptr, *R2 = nullptr, *h1 = nullptr, *h2 = nullptr;
+  float *mu1 = nullptr, *rs1 = nullptr, *mu2 = nullptr, *rs2 = nullptr;
+};
+
+struct Group {
+  int64_t n = 0, npad = 0, shard = 0;   // numel, padded numel, per-rank shard
+  float* master = nullptr;              // fp32 [shard] (the full vector when world == 1 / DP)
+  void* comp = nullptr;                 // dtype copy [shard] (full when world == 1 / DP)
+  float* grad = nullptr;                // fp32 [npad] full gradient (accumulated in bwd)
+  float* gshard = nullptr;              // fp32 [shard] reduced gradient shard (world > 1)
+  std::vector<int64_t> toff, tn;        // tensors: offset, numel
+  std::vector<int> tinit;               // 0 uniform, 1 ones, 2 zeros
+  std::vector<float> tbound;
+};
+
+struct Layer {
+  int m_in = 0, m_out = 0;
+  std::vector<Mod> mods;
+  int64_t Wn = -1, gamma = -1, beta = -1;
+  void* Y = nullptr;
+  void* R = nullptr;
+  float *mu = nullptr, *rstd = nullptr;
+  const void* X = nullptr;   // forward input (referenced)
+  int B = -1;                // batch of the saved forward, -1 = none
+};
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base((char*)b) {}
+  void* take(size_t bytes) {
+    off = (off + 255) & ~size_t(255);
+    void* p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  }
+};
+
+}  // namespace
+
+struct dhen_ctx {
+  dhen_config cfg;
+  std::vector<dhen_layer> layers_cfg;
+  std::vector<std::vector<dhen_module>> mods_cfg;
+  dhen_dist dist;
+  int dt, es;            // storage dtype, element size
+  int d, Bmax;
+  std::vector<Layer> L;
+  std::vector<Group> G;  // n_layers + 1 (head)
+  // gathered compute copies (world > 1, FSDP): 2 ping-pong buffers of max npad
+  void* gathered[2] = {nullptr, nullptr};
+  int gathered_owner[2] = {-1, -1};
+  int64_t max_npad = 0;
+  // scratch
+  float* Ucat = nullptr;
+  float* dXacc = nullptr;
+  void* dR = nullptr;
+  void* dY[2] = {nullptr, nullptr};
+  float* big = nullptr;     // fp32 scratch [B*H*m*m] / [B*m*m] (Gram, attention S / dP)
+  void* tA = nullptr;       // dtype scratch [B * m * d * 3] (dT, dQKV, ...)
+  void* tB = nullptr;       // dtype scratch [B * m * d]
+  void* tC = nullptr;       // dtype scratch [B * m * max(f, d)] (dF, dh*)
+  void* tD = nullptr;       // dtype scratch [B * H * m * m] (dS, S of Dot bwd)
+  float* rtmp = nullptr;    // fp32 [B * m * d]
+  float* red = nullptr;     // reduction partials
+  size_t red_bytes = 0;
+  Workspace ws;
+  float *pooled = nullptr, *z = nullptr, *lossb = nullptr, *dz = nullptr;
+  ncclComm_t comm = nullptr;
+  unsigned long long launches0 = 0;
+};
+
+// ------------------------------------------------------------------ validation / planning
+static int mdef(int v, int d) { return v > 0 ? v : d; }
+
+static dhen_status validate(const dhen_config* c) {
+  if (!c) return fail(DHEN_E_CONFIG, "dhen_validate: cfg is NULL");
+  if (c->m0 < 1 || c->d < 1 || c->n_layers < 1 || !c->layers)
+    return fail(DHEN_E_CONFIG, "dhen_validate: m0=%d d=%d n_layers=%d layers=%p", c->m0, c->d, c->n_layers, (void*)c->layers);
+  if (c->d % 8 != 0) return fail(DHEN_E_CONFIG, "dhen_validate: d=%d not a multiple of 8 (16-byte rows)", c->d);
+  if (c->d > 1024) return fail(DHEN_E_CONFIG, "dhen_validate: d=%d > 1024", c->d);
+  if (c->dtype != DHEN_FP32 && c->dtype != DHEN_BF16) return fail(DHEN_E_CONFIG, "dhen_validate: dtype=%d", c->dtype);
+  if (c->batch_max_local < 1) return fail(DHEN_E_CONFIG, "dhen_validate: batch_max_local=%d", c->batch_max_local);
+  int m = c->m0;
+  for (int n = 0; n < c->n_layers; ++n) {
+    const dhen_layer& L = c->layers[n];
+    if (L.n_modules < 1 || !L.modules) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d has no modules", n);
+    int mo = 0;
+    for (int i = 0; i < L.n_modules; ++i) {
+      const dhen_module& s = L.modules[i];
+      if (s.kind < DHEN_DOT || s.kind > DHEN_MLP) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d module %d kind=%d", n, i, s.kind);
+      if (s.l < 1) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d module %d l=%d < 1", n, i, s.l);
+      if (s.kind == DHEN_DOT && m < 2) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d Dot needs m >= 2, m=%d (S:186)", n, m);
+      if (s.kind == DHEN_ATTN && c->d % mdef(s.heads, 2) != 0)
+        return fail(DHEN_E_CONFIG, "dhen_validate: layer %d attention d=%d %% heads=%d != 0 (S:195)", n, c->d, mdef(s.heads, 2));
+      if (s.kind == DHEN_CONV && (mdef(s.conv_k, 3) % 2 == 0 || mdef(s.conv_k, 3) > 7))
+        return fail(DHEN_E_CONFIG, "dhen_validate: layer %d conv_k=%d must be odd and <= 7 (S:204)", n, mdef(s.conv_k, 3));
+      mo += s.l;
+    }
+    m = mo;
+  }
+  return DHEN_OK;
+}
+
+// Builds layer/group structure; carves state/work when the carvers have bases.
+static void plan(dhen_ctx* c, Carver& state, Carver& work) {
+  const int d = c->d, B = c->Bmax, es = c->es;
+  const int world = c->dist.world;
+  const bool shard = world > 1 && c->dist.fsdp;
+  int m = c->cfg.m0, m_max = m, H_mm_max = 0, f_max = d, m_out_max = 0;
+  int64_t tC_elems = 0, tA_elems = 0;
+  c->L.assign(c->cfg.n_layers, Layer());
+  c->G.assign(c->cfg.n_layers + 1, Group());
+  for (int n = 0; n < c->cfg.n_layers; ++n) {
+    Layer& Lr = c->L[n];
+    Group& g = c->G[n];
+    const dhen_layer& lc = c->cfg.layers[n];
+    Lr.m_in = m;
+    int mo = 0;
+    for (int i = 0; i < lc.n_modules; ++i) mo += lc.modules[i].l;
+    Lr.m_out = mo;
+    int64_t off = 0;
+    auto tensor = [&](int64_t numel, int init, int fan) {
+      int64_t o = off;
+      g.toff.push_back(off);
+      g.tn.push_back(numel);
+      g.tinit.push_back(init);
+      g.tbound.push_back(fan > 0 ? 1.f / sqrtf((float)fan) : 0.f);
+      off += numel;
+      return o;
+    };
+    Lr.mods.clear();
+    int tok = 0;
+    for (int i = 0; i < lc.n_modules; ++i) {
+      Mod md;
+      md.s = lc.modules[i];
+      md.s.heads = mdef(md.s.heads, 2);
+      md.s.ffn_mult = mdef(md.s.ffn_mult, 4);
+      md.s.conv_channels = mdef(md.s.conv_channels, 4);
+      md.s.conv_k = mdef(md.s.conv_k, 3);
+      md.s.mlp_hidden[0] = mdef(md.s.mlp_hidden[0], 1024);
+      md.s.mlp_hidden[1] = mdef(md.s.mlp_hidden[1], 1024);
+      md.off_tok = tok;
+      tok += md.s.l;
+      const int l = md.s.l;
+      switch (md.s.kind) {
+        case DHEN_DOT: { int h = m * (m - 1) / 2; md.Wm = tensor((int64_t)l * d * h, 0, h); break; }
+        case DHEN_LINEAR: md.W = tensor((int64_t)m * l, 0, m); break;
+        case DHEN_DCN: md.W = tensor((int64_t)d * d, 0, d); md.b = tensor(d, 0, d); md.Wu = tensor((int64_t)m * l, 0, m); break;
+        case DHEN_CONV: { int k = md.s.conv_k; md.K = tensor((int64_t)md.s.conv_channels * k * k, 0, k * k); md.Wu = tensor((int64_t)m * l, 0, m); break; }
+        case DHEN_ATTN: {
+          int f = md.s.ffn_mult * d;
+          md.Wq = tensor((int64_t)d * d, 0, d); tensor((int64_t)d * d, 0, d); tensor((int64_t)d * d, 0, d);
+          md.Wo = tensor((int64_t)d * d, 0, d);
+          md.bq = tensor(d, 0, d); tensor(d, 0, d); md.bo = tensor(d, 0, d);
+          md.g1 = tensor(d, 1, 0); md.be1 = tensor(d, 2, 0); md.g2 = tensor(d, 1, 0); md.be2 = tensor(d, 2, 0);
+          md.W1 = tensor((int64_t)f * d, 0, d); md.b1 = tensor(f, 0, d); md.W2 = tensor((int64_t)d * f, 0, f); md.b2 = tensor(d, 0, f);
+          md.Wu = tensor((int64_t)m * l, 0, m);
+          break;
+        }
+        case DHEN_MLP: {
+          int h1 = md.s.mlp_hidden[0], h2 = md.s.mlp_hidden[1];
+          md.W1 = tensor((int64_t)h1 * m * d, 0, m * d); md.b1 = tensor(h1, 0, m * d);
+          md.W2 = tensor((int64_t)h2 * h1, 0, h1); md.b2 = tensor(h2, 0, h1);
+          md.Wm = tensor((int64_t)l * d * h2, 0, h2);
+          break;
+        }
+      }
+      Lr.mods.push_back(md);
+    }
+    if (m != mo) Lr.Wn = tensor((int64_t)m * mo, 0, m);
+    Lr.gamma = tensor(d, 1, 0);
+    Lr.beta = tensor(d, 2, 0);
+    g.n = off;
+    m = mo;
+    m_max = std::max(m_max, mo);
+    m_out_max = std::max(m_out_max, mo);
+  }
+  {  // head group (R17)
+    Group& g = c->G[c->cfg.n_layers];
+    g.toff = {0, d}; g.tn = {d, 1}; g.tinit = {0, 0};
+    g.tbound = {1.f / sqrtf((float)d), 1.f / sqrtf((float)d)};
+    g.n = d + 1;
+  }
+  // sizes of every group, then state memory
+  c->max_npad = 0;
+  for (auto& g : c->G) {
+    int64_t q = (int64_t)64 * (shard ? world : 1);
+    g.npad = (g.n + q - 1) / q * q;
+    g.shard = shard ? g.npad / world : g.npad;
+    c->max_npad = std::max(c->max_npad, g.npad);
+    g.master = (float*)state.take(g.shard * 4);
+    g.comp = state.take(g.shard * es);
+    g.grad = (float*)state.take(g.npad * 4);
+    g.gshard = world > 1 ? (float*)state.take(g.shard * 4) : nullptr;
+  }
+  if (shard) { c->gathered[0] = state.take(c->max_npad * es); c->gathered[1] = state.take(c->max_npad * es); }
+  // saved activations (work)
+  m = c->cfg.m0;
+  for (int n = 0; n < c->cfg.n_layers; ++n) {
+    Layer& Lr = c->L[n];
+    const int mi = Lr.m_in, mo = Lr.m_out;
+    Lr.Y = work.take((size_t)B * mo * d * es);
+    Lr.R = work.take((size_t)B * mo * d * es);
+    Lr.mu = (float*)work.take((size_t)B * mo * 4);
+    Lr.rstd = (float*)work.take((size_t)B * mo * 4);
+    for (Mod& md : Lr.mods) {
+      size_t tok = (size_t)B * mi * d;
+      switch (md.s.kind) {
+        case DHEN_DOT:
+          md.Z = work.take((size_t)B * (mi * (mi - 1) / 2) * es);
+          H_mm_max = std::max(H_mm_max, mi * mi);
+          tA_elems = std::max<int64_t>(tA_elems, (int64_t)B * (mi * (mi - 1) / 2));
+          break;
+        case DHEN_DCN: md.A = work.take(tok * es); md.T = work.take(tok * es); break;
+        case DHEN_CONV: md.T = work.take(tok * es); break;
+        case DHEN_ATTN: {
+          int H = md.s.heads, f = md.s.ffn_mult * d;
+          md.QKV = work.take(tok * 3 * es);
+          md.P = work.take((size_t)B * H * mi * mi * es);
+          md.O = work.take(tok * es);
+          md.R1 = work.take(tok * es);
+          md.Z1 = work.take(tok * es);
+          md.F = work.take((size_t)B * mi * f * es);
+          md.R2 = work.take(tok * es);
+          md.T = work.take(tok * es);
+          md.mu1 = (float*)work.take((size_t)B * mi * 4); md.rs1 = (float*)work.take((size_t)B * mi * 4);
+          md.mu2 = (float*)work.take((size_t)B * mi * 4); md.rs2 = (float*)work.take((size_t)B * mi * 4);
+          H_mm_max = std::max(H_mm_max, H * mi * mi);
+          f_max = std::max(f_max, f);
+          tC_elems = std::max<int64_t>(tC_elems, (int64_t)B * mi * std::max(f, 3 * d));
+          break;
+        }
+        case DHEN_MLP: {
+          md.h1 = work.take((size_t)B * md.s.mlp_hidden[0] * es);
+          md.h2 = work.take((size_t)B * md.s.mlp_hidden[1] * es);
+          tC_elems = std::max<int64_t>(tC_elems, (int64_t)B * std::max(md.s.mlp_hidden[0], md.s.mlp_hidden[1]));
+          tA_elems = std::max<int64_t>(tA_elems, (int64_t)B * md.s.mlp_hidden[1]);
+          break;
+        }
+        default: break;
+      }
+    }
+  }
+  // scratch
+  const size_t rows_d = (size_t)B * m_max * d;
+  c->Ucat = (float*)work.take((size_t)B * m_out_max * d * 4);
+  c->dXacc = (float*)work.take(rows_d * 4);
+  c->dR = work.take(rows_d * es);
+  c->dY[0] = work.take(rows_d * es);
+  c->dY[1] = work.take(rows_d * es);
+  c->big = (float*)work.take((size_t)B * std::max(H_mm_max, 1) * 4);
+  c->tA = work.take((size_t)std::max<int64_t>(tA_elems, (int64_t)rows_d * 3) * es);
+  c->tB = work.take(rows_d * es);
+  c->tC = work.take((size_t)std::max<int64_t>(tC_elems, 1) * es);
+  c->tD = work.take((size_t)B * std::max(H_mm_max, 1) * es);
+  c->rtmp = (float*)work.take(rows_d * 4);
+  c->red_bytes = (size_t)16 << 20;
+  c->red = (float*)work.take(c->red_bytes);
+  c->ws.bytes = (size_t)256 << 20;
+  c->ws.ptr = (float*)work.take(c->ws.bytes);
+  c->pooled = (float*)work.take((size_t)B * d * 4);
+  c->z = (float*)work.take((size_t)B * 4);
+  c->lossb = (float*)work.take((size_t)B * 4);
+  c->dz = (float*)work.take((size_t)B * 4);
+  (void)f_max;
+}
+
+// ------------------------------------------------------------------ GEMM helpers
+static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st) {
+  CK(gemm_run(g, c->ws, st));
+  return DHEN_OK;
+}
+static Gemm mk(int M, int N, int K, int batch, Operand a, Operand b, View cv) {
+  Gemm g;
+  g.M = M; g.N = N; g.K = K; g.batch = batch; g.a = a; g.b = b; g.c = cv;
+  return g;
+}
+
+// Parameter pointers for the current layer group
+struct PP {
+  char* base;
+  int es;
+  void* operator()(int64_t off) const { return base + off * es; }
+};
+
+// Token projection (F10): U_b = W^T T_b -> fp32 view dst (rows stride d, batch stride ldb), accumulate?
+static dhen_status tokmix_fwd(dhen_ctx* c, const void* T, int m, const void* W, int l, float* dst, int64_t ldb, int B,
+                              int acc, cudaStream_t st) {
+  const int d = c->d, dt = c->dt;
+  Gemm g = mk(l, d, m, B, operand(W, dt, 1, l), operand(T, dt, 1, d, (int64_t)m * d),
+              view(dst, F32, d, 1, ldb));
+  g.e.accumulate = acc;
+  return G_(g, c, st);
+}
+// B4: dT = W dU (set, dtype dT_dt) or dX += W dU (fp32 accumulate); dW += sum_b T_b dU_b^T
+static dhen_status tokmix_bwd(dhen_ctx* c, const void* T, int m, const void* W, int l, const void* dU, int64_t ldu,
+                              void* dT, int dT_dt, int acc, float* gW, int B, cudaStream_t st) {
+  const int d = c->d, dt = c->dt;
+  Gemm g = mk(m, d, l, B, operand(W, dt, l, 1), operand(dU, dt, 1, d, ldu), view(dT, dT_dt, d, 1, (int64_t)m * d));
+  g.e.accumulate = acc;
+  RET(G_(g, c, st));
+  Gemm gw = mk(m, l, B * d, 1, operand(T, dt, d, 1, 0, 0, 1, d, (int64_t)m * d),
+               operand(dU, dt, d, 1, 0, 0, 1, d, ldu), view(gW, F32, l, 1));
+  gw.e.accumulate = 1;
+  return G_(gw, c, st);
+}
+
+// ------------------------------------------------------------------ FSDP gather / scatter
+static dhen_status comp_params(dhen_ctx* c, int gi, cudaStream_t st, void** out) {
+  Group& g = c->G[gi];
+  if (c->dist.world == 1 || !c->dist.fsdp) { *out = g.comp; return DHEN_OK; }
+  int slot = gi & 1;
+  if (c->gathered_owner[slot] != gi) {
+    NK(ncclAllGather(g.comp, c->gathered[slot], (size_t)g.shard, c->dt == F32 ? ncclFloat32 : ncclBfloat16, c->comm,
+                     st));
+    c->gathered_owner[slot] = gi;
+  }
+  *out = c->gathered[slot];
+  return DHEN_OK;
+}
+static void invalidate_gathered(dhen_ctx* c) { c->gathered_owner[0] = c->gathered_owner[1] = -1; }
+
+static dhen_status reduce_grads(dhen_ctx* c, int gi, cudaStream_t st) {
+  if (c->dist.world == 1) return DHEN_OK;
+  Group& g = c->G[gi];
+  if (c->dist.fsdp) {
+    NK(ncclReduceScatter(g.grad, g.gshard, (size_t)g.shard, ncclFloat32, ncclSum, c->comm, st));
+  } else {
+    NK(ncclAllReduce(g.grad, g.gshard, (size_t)g.shard, ncclFloat32, ncclSum, c->comm, st));
+  }
+  return DHEN_OK;
+}
+
+// ------------------------------------------------------------------ layer forward
+static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, cudaStream_t st) {
+  Layer& Lr = c->L[n];
+  const int d = c->d, dt = c->dt, es = c->es;
+  const int mi = Lr.m_in, mo = Lr.m_out;
+  void* pbase;
+  RET(comp_params(c, n, st, &pbase));
+  PP p{(char*)pbase, es};
+  float* U = c->Ucat;
+  const int64_t ldU = (int64_t)mo * d;
+  const int64_t rows = (int64_t)B * mi;
+  for (Mod& md : Lr.mods) {
+    const int l = md.s.l;
+    float* Us = U + (int64_t)md.off_tok * d;
+    switch (md.s.kind) {
+      case DHEN_DOT: {   // F1 + F2
+        const int h = mi * (mi - 1) / 2;
+        Gemm g = mk(mi, mi, d, B, operand(X, dt, d, 1, (int64_t)mi * d), operand(X, dt, d, 1, (int64_t)mi * d),
+                    view(c->big, F32, mi, 1, (int64_t)mi * mi));
+        RET(G_(g, c, st));
+        CK(triu_extract(c->big, md.Z, dt, B, mi, h, st));
+        Gemm v = mk(B, l * d, h, 1, operand(md.Z, dt, h, 1), operand(p(md.Wm), dt, h, 1), view(Us, F32, ldU, 1));
+        RET(G_(v, c, st));
+        break;
+      }
+      case DHEN_LINEAR:  // F10 with T = X
+        RET(tokmix_fwd(c, X, mi, p(md.W), l, Us, ldU, B, 0, st));
+        break;
+      case DHEN_DCN: {   // F8: A = X W^T + b ; T = X * A + X
+        Gemm g = mk((int)rows, d, d, 1, operand(X, dt, d, 1), operand(p(md.W), dt, d, 1), view(md.T, dt, d, 1));
+        g.e.bias = p(md.b); g.e.bias_dt = dt;
+        g.e.cross = view((void*)X, dt, d, 1);
+        g.e.aux = view(md.A, dt, d, 1);
+        RET(G_(g, c, st));
+        RET(tokmix_fwd(c, md.T, mi, p(md.Wu), l, Us, ldU, B, 0, st));
+        break;
+      }
+      case DHEN_CONV:    // F7
+        CK(conv_fwd(X, p(md.K), dt, md.s.conv_channels, md.s.conv_k, B, mi, d, md.T, dt, st));
+        RET(tokmix_fwd(c, md.T, mi, p(md.Wu), l, Us, ldU, B, 0, st));
+        break;
+      case DHEN_ATTN: {  // F3-F6
+        const int H = md.s.heads, dh = d / H, f = md.s.ffn_mult * d;
+        const int64_t s3 = 3 * (int64_t)d;
+        char* QKV = (char*)md.QKV;
+        Gemm q = mk((int)rows, 3 * d, d, 1, operand(X, dt, d, 1), operand(p(md.Wq), dt, d, 1), view(QKV, dt, s3, 1));
+        q.e.bias = p(md.bq); q.e.bias_dt = dt; q.e.bias_gap_lo = d; q.e.bias_gap_hi = 2 * d;   // no key bias (R10)
+        RET(G_(q, c, st));
+        Gemm s = mk(mi, mi, dh, B * H, operand(QKV, dt, s3, 1, mi * s3, dh, H),
+                    operand(QKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H),
+                    view(c->big, F32, mi, 1, (int64_t)mi * mi));
+        s.e.alpha = 1.f / sqrtf((float)dh);
+        RET(G_(s, c, st));
+        CK(softmax_rows(c->big, md.P, dt, (int64_t)B * H * mi, mi, st));
+        Gemm o = mk(mi, dh, mi, B * H, operand(md.P, dt, mi, 1, (int64_t)mi * mi),
+                    operand(QKV + 2 * (int64_t)d * es, dt, 1, s3, mi * s3, dh, H),
+                    view(md.O, dt, d, 1, (int64_t)mi * d, dh, H));
+        RET(G_(o, c, st));
+        Gemm r1 = mk((int)rows, d, d, 1, operand(md.O, dt, d, 1), operand(p(md.Wo), dt, d, 1), view(c->rtmp, F32, d, 1));
+        r1.e.bias = p(md.bo); r1.e.bias_dt = dt; r1.e.resid = view((void*)X, dt, d, 1);
+        RET(G_(r1, c, st));
+        CK(ln_fwd(c->rtmp, nullptr, p(md.g1), p(md.be1), dt, c->cfg.ln_eps, rows, d, md.Z1, md.R1, md.mu1, md.rs1, dt, st));
+        Gemm f1 = mk((int)rows, f, d, 1, operand(md.Z1, dt, d, 1), operand(p(md.W1), dt, d, 1), view(md.F, dt, f, 1));
+        f1.e.bias = p(md.b1); f1.e.bias_dt = dt; f1.e.relu = 1;
+        RET(G_(f1, c, st));
+        Gemm f2 = mk((int)rows, d, f, 1, operand(md.F, dt, f, 1), operand(p(md.W2), dt, f, 1), view(c->rtmp, F32, d, 1));
+        f2.e.bias = p(md.b2); f2.e.bias_dt = dt; f2.e.resid = view(md.Z1, dt, d, 1);
+        RET(G_(f2, c, st));
+        CK(ln_fwd(c->rtmp, nullptr, p(md.g2), p(md.be2), dt, c->cfg.ln_eps, rows, d, md.T, md.R2, md.mu2, md.rs2, dt, st));
+        RET(tokmix_fwd(c, md.T, mi, p(md.Wu), l, Us, ldU, B, 0, st));
+        break;
+      }
+      case DHEN_MLP: {   // F9
+        const int h1 = md.s.mlp_hidden[0], h2 = md.s.mlp_hidden[1];
+        const int K1 = mi * d;
+        Gemm a = mk(B, h1, K1, 1, operand(X, dt, K1, 1), operand(p(md.W1), dt, K1, 1), view(md.h1, dt, h1, 1));
+        a.e.bias = p(md.b1); a.e.bias_dt = dt; a.e.relu = 1;
+        RET(G_(a, c, st));
+        Gemm b2 = mk(B, h2, h1, 1, operand(md.h1, dt, h1, 1), operand(p(md.W2), dt, h1, 1), view(md.h2, dt, h2, 1));
+        b2.e.bias = p(md.b2); b2.e.bias_dt = dt; b2.e.relu = 1;
+        RET(G_(b2, c, st));
+        Gemm v = mk(B, l * d, h2, 1, operand(md.h2, dt, h2, 1), operand(p(md.Wm), dt, h2, 1), view(Us, F32, ldU, 1));
+        RET(G_(v, c, st));
+        break;
+      }
+    }
+  }
+  // F11 shortcut (Eq.(2)) + F12 LayerNorm
+  if (Lr.Wn >= 0) RET(tokmix_fwd(c, X, mi, p(Lr.Wn), mo, U, ldU, B, 1, st));
+  CK(ln_fwd(U, Lr.Wn >= 0 ? nullptr : X, p(Lr.gamma), p(Lr.beta), dt, c->cfg.ln_eps, (int64_t)B * mo, d, Y, Lr.R, Lr.mu,
+            Lr.rstd, dt, st));
+  Lr.X = X;
+  Lr.B = B;
+  return DHEN_OK;
+}
+
+// ------------------------------------------------------------------ layer backward
+static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B, cudaStream_t st) {
+  Layer& Lr = c->L[n];
+  Group& G = c->G[n];
+  const int d = c->d, dt = c->dt, es = c->es;
+  const int mi = Lr.m_in, mo = Lr.m_out;
+  const void* X = Lr.X;
+  void* pbase;
+  RET(comp_params(c, n, st, &pbase));
+  PP p{(char*)pbase, es};
+  float* g = G.grad;
+  auto gp = [&](int64_t off) { return g + off; };
+  const int64_t ldU = (int64_t)mo * d;
+  const int64_t rows = (int64_t)B * mi;
+  float* acc = c->dXacc;
+  // B2: LN backward; identity shortcut (B3) initialises the dX accumulator
+  CK(ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc, Lr.Wn >= 0 ? 0 : 1,
+            gp(Lr.gamma), gp(Lr.beta), c->red, c->red_bytes, st));
+  if (Lr.Wn >= 0)   // B3: dX = W_n dR ; dW_n += sum_b X_b dR_b^T
+    RET(tokmix_bwd(c, X, mi, p(Lr.Wn), mo, c->dR, ldU, acc, F32, 0, gp(Lr.Wn), B, st));
+  for (Mod& md : Lr.mods) {
+    const int l = md.s.l;
+    char* dU = (char*)c->dR + (int64_t)md.off_tok * d * es;
+    switch (md.s.kind) {
+      case DHEN_DOT: {   // B5
+        const int h = mi * (mi - 1) / 2;
+        Gemm gw = mk(l * d, h, B, 1, operand(dU, dt, 1, ldU), operand(md.Z, dt, 1, h), view(gp(md.Wm), F32, h, 1));
+        gw.e.accumulate = 1;
+        RET(G_(gw, c, st));
+        Gemm gz = mk(B, h, l * d, 1, operand(dU, dt, ldU, 1), operand(p(md.Wm), dt, 1, h), view(c->tA, dt, h, 1));
+        RET(G_(gz, c, st));
+        CK(sym_from_triu(c->tA, c->tD, dt, B, mi, h, st));
+        Gemm gx = mk(mi, d, mi, B, operand(c->tD, dt, mi, 1, (int64_t)mi * mi), operand(X, dt, 1, d, (int64_t)mi * d),
+                     view(acc, F32, d, 1, (int64_t)mi * d));
+        gx.e.accumulate = 1;
+        RET(G_(gx, c, st));
+        break;
+      }
+      case DHEN_LINEAR:
+        RET(tokmix_bwd(c, X, mi, p(md.W), l, dU, ldU, acc, F32, 1, gp(md.W), B, st));
+        break;
+      case DHEN_DCN: {   // B8
+        void* dT = c->tA;
+        void* dA = c->tB;
+        RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st));
+        CK(dcn_bwd_elem(dT, X, md.A, dA, acc, dt, rows * d, st));
+        Gemm gx = mk((int)rows, d, d, 1, operand(dA, dt, d, 1), operand(p(md.W), dt, 1, d), view(acc, F32, d, 1));
+        gx.e.accumulate = 1;
+        RET(G_(gx, c, st));
+        Gemm gw = mk(d, d, (int)rows, 1, operand(dA, dt, 1, d), operand(X, dt, 1, d), view(gp(md.W), F32, d, 1));
+        gw.e.accumulate = 1;
+        RET(G_(gw, c, st));
+        CK(colsum_add(dA, dt, rows, d, d, gp(md.b), c->red, c->red_bytes, st));
+        break;
+      }
+      case DHEN_CONV: {  // B7
+        void* dT = c->tA;
+        RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st));
+        CK(conv_dgrad(dT, p(md.K), dt, md.s.conv_channels, md.s.conv_k, B, mi, d, acc, dt, st));
+        CK(conv_wgrad(dT, X, md.s.conv_channels, md.s.conv_k, B, mi, d, dt, gp(md.K), c->red, c->red_bytes, st));
+        break;
+      }
+      case DHEN_ATTN: {  // B6
+        const int H = md.s.heads, dh = d / H, f = md.s.ffn_mult * d;
+        const int64_t s3 = 3 * (int64_t)d;
+        char* QKV = (char*)md.QKV;
+        void* dT = c->tB;
+        RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st));
+        void* dR2 = c->tA;   // [rows, d]
+        CK(ln_bwd(dT, dt, md.R2, md.mu2, md.rs2, p(md.g2), dt, rows, d, dR2, dt, nullptr, 0, gp(md.g2), gp(md.be2), c->red,
+                  c->red_bytes, st));
+        void* dF = c->tC;
+        Gemm a = mk((int)rows, f, d, 1, operand(dR2, dt, d, 1), operand(p(md.W2), dt, 1, f), view(dF, dt, f, 1));
+        a.e.mask = view(md.F, dt, f, 1);
+        RET(G_(a, c, st));
+        Gemm w2 = mk(d, f, (int)rows, 1, operand(dR2, dt, 1, d), operand(md.F, dt, 1, f), view(gp(md.W2), F32, f, 1));
+        w2.e.accumulate = 1;
+        RET(G_(w2, c, st));
+        CK(colsum_add(dR2, dt, rows, d, d, gp(md.b2), c->red, c->red_bytes, st));
+        Gemm z1 = mk((int)rows, d, f, 1, operand(dF, dt, f, 1), operand(p(md.W1), dt, 1, d), view(c->rtmp, F32, d, 1));
+        z1.e.resid = view(dR2, dt, d, 1);
+        RET(G_(z1, c, st));
+        Gemm w1 = mk(f, d, (int)rows, 1, operand(dF, dt, 1, f), operand(md.Z1, dt, 1, d), view(gp(md.W1), F32, d, 1));
+        w1.e.accumulate = 1;
+        RET(G_(w1, c, st));
+        CK(colsum_add(dF, dt, rows, f, f, gp(md.b1), c->red, c->red_bytes, st));
+        void* dR1 = c->tB;   // dT no longer needed
+        CK(ln_bwd(c->rtmp, F32, md.R1, md.mu1, md.rs1, p(md.g1), dt, rows, d, dR1, dt, acc, 2, gp(md.g1), gp(md.be1),
+                  c->red, c->red_bytes, st));
+        void* dO = c->tA;    // dR2 no longer needed
+        Gemm go = mk((int)rows, d, d, 1, operand(dR1, dt, d, 1), operand(p(md.Wo), dt, 1, d), view(dO, dt, d, 1));
+        RET(G_(go, c, st));
+        Gemm wo = mk(d, d, (int)rows, 1, operand(dR1, dt, 1, d), operand(md.O, dt, 1, d), view(gp(md.Wo), F32, d, 1));
+        wo.e.accumulate = 1;
+        RET(G_(wo, c, st));
+        CK(colsum_add(dR1, dt, rows, d, d, gp(md.bo), c->red, c->red_bytes, st));
+        // attention core backward
+        char* dQKV = (char*)c->tC;   // [rows, 3d]  (dF no longer needed; tC >= rows*f >= rows*3d? checked at plan)
+        Gemm dv = mk(mi, dh, mi, B * H, operand(md.P, dt, 1, mi, (int64_t)mi * mi),
+                     operand(dO, dt, 1, d, (int64_t)mi * d, dh, H),
+                     view(dQKV + 2 * (int64_t)d * es, dt, s3, 1, mi * s3, dh, H));
+        RET(G_(dv, c, st));
+        Gemm dp = mk(mi, mi, dh, B * H, operand(dO, dt, d, 1, (int64_t)mi * d, dh, H),
+                     operand(QKV + 2 * (int64_t)d * es, dt, s3, 1, mi * s3, dh, H),
+                     view(c->big, F32, mi, 1, (int64_t)mi * mi));
+        RET(G_(dp, c, st));
+        CK(softmax_bwd(md.P, c->big, c->tD, dt, (int64_t)B * H * mi, mi, 1.f / sqrtf((float)dh), st));
+        Gemm dq = mk(mi, dh, mi, B * H, operand(c->tD, dt, mi, 1, (int64_t)mi * mi),
+                     operand(QKV + (int64_t)d * es, dt, 1, s3, mi * s3, dh, H),
+                     view(dQKV, dt, s3, 1, mi * s3, dh, H));
+        RET(G_(dq, c, st));
+        Gemm dk = mk(mi, dh, mi, B * H, operand(c->tD, dt, 1, mi, (int64_t)mi * mi),
+                     operand(QKV, dt, 1, s3, mi * s3, dh, H),
+                     view(dQKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H));
+        RET(G_(dk, c, st));
+        Gemm gx = mk((int)rows, d, 3 * d, 1, operand(dQKV, dt, s3, 1), operand(p(md.Wq), dt, 1, d), view(acc, F32, d, 1));
+        gx.e.accumulate = 1;
+        RET(G_(gx, c, st));
+        Gemm gw = mk(3 * d, d, (int)rows, 1, operand(dQKV, dt, 1, s3), operand(X, dt, 1, d), view(gp(md.Wq), F32, d, 1));
+        gw.e.accumulate = 1;
+        RET(G_(gw, c, st));
+        CK(colsum_add(dQKV, dt, rows, d, s3, gp(md.bq), c->red, c->red_bytes, st));
+        CK(colsum_add(dQKV + 2 * (int64_t)d * es, dt, rows, d, s3, gp(md.bq) + d, c->red, c->red_bytes, st));
+        break;
+      }
+      case DHEN_MLP: {   // B9
+        const int h1 = md.s.mlp_hidden[0], h2 = md.s.mlp_hidden[1];
+        const int K1 = mi * d;
+        Gemm wm = mk(l * d, h2, B, 1, operand(dU, dt, 1, ldU), operand(md.h2, dt, 1, h2), view(gp(md.Wm), F32, h2, 1));
+        wm.e.accumulate = 1;
+        RET(G_(wm, c, st));
+        void* dh2 = c->tA;
+        Gemm a = mk(B, h2, l * d, 1, operand(dU, dt, ldU, 1), operand(p(md.Wm), dt, 1, h2), view(dh2, dt, h2, 1));
+        a.e.mask = view(md.h2, dt, h2, 1);
+        RET(G_(a, c, st));
+        Gemm w2 = mk(h2, h1, B, 1, operand(dh2, dt, 1, h2), operand(md.h1, dt, 1, h1), view(gp(md.W2), F32, h1, 1));
+        w2.e.accumulate = 1;
+        RET(G_(w2, c, st));
+        CK(colsum_add(dh2, dt, B, h2, h2, gp(md.b2), c->red, c->red_bytes, st));
+        void* dh1 = c->tC;
+        Gemm b1 = mk(B, h1, h2, 1, operand(dh2, dt, h2, 1), operand(p(md.W2), dt, 1, h1), view(dh1, dt, h1, 1));
+        b1.e.mask = view(md.h1, dt, h1, 1);
+        RET(G_(b1, c, st));
+        Gemm w1 = mk(h1, K1, B, 1, operand(dh1, dt, 1, h1), operand(X, dt, 1, K1), view(gp(md.W1), F32, K1, 1));
+        w1.e.accumulate = 1;
+        RET(G_(w1, c, st));
+        CK(colsum_add(dh1, dt, B, h1, h1, gp(md.b1), c->red, c->red_bytes, st));
+        Gemm gx = mk(B, K1, h1, 1, operand(dh1, dt, h1, 1), operand(p(md.W1), dt, 1, K1), view(acc, F32, K1, 1));
+        gx.e.accumulate = 1;
+        RET(G_(gx, c, st));
+        break;
+      }
+    }
+  }
+  if (dX) CK(cast(acc, F32, dX, dt, rows * d, st));
+  RET(reduce_grads(c, n, st));
+  return DHEN_OK;
+}
+
+// ------------------------------------------------------------------ head
+static dhen_status head(dhen_ctx* c, const void* YN, int mN, const float* labels, int B, int Bg, void* dY, float* loss,
+                        int do_bwd, cudaStream_t st) {
+  const int gi = c->cfg.n_layers;
+  void* pbase;
+  RET(comp_params(c, gi, st, &pbase));
+  PP p{(char*)pbase, c->es};
+  Group& G = c->G[gi];
+  CK(head_fwd_bwd(YN, p(0), p(c->d), c->dt, labels, B, mN, c->d, Bg, dY, c->dt, c->pooled, c->z, c->lossb, c->dz, loss,
+                  G.grad, G.grad + c->d, do_bwd, st));
+  if (do_bwd) RET(reduce_grads(c, gi, st));
+  return DHEN_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+static bool aligned16(const void* p) { return p && (((uintptr_t)p) & 15) == 0; }
+static cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+extern "C" {
+
+const char* dhen_last_error(void) { return t_err.c_str(); }
+
+dhen_status dhen_validate(const dhen_config* cfg) { return validate(cfg); }
+
+static dhen_status make_ctx(const dhen_config* cfg, const dhen_dist* dist, dhen_ctx* c) {
+  RET(validate(cfg));
+  dhen_dist dd;
+  if (dist) dd = *dist; else { memset(&dd, 0, sizeof dd); dd.world = 1; dd.fsdp = 1; }
+  if (dd.world < 1 || dd.rank < 0 || dd.rank >= dd.world)
+    return fail(DHEN_E_CONFIG, "dhen: rank=%d world=%d", dd.rank, dd.world);
+  c->cfg = *cfg;
+  if (c->cfg.ln_eps <= 0.f) c->cfg.ln_eps = 1e-5f;
+  c->mods_cfg.resize(cfg->n_layers);
+  c->layers_cfg.resize(cfg->n_layers);
+  for (int n = 0; n < cfg->n_layers; ++n) {
+    c->mods_cfg[n].assign(cfg->layers[n].modules, cfg->layers[n].modules + cfg->layers[n].n_modules);
+    c->layers_cfg[n].n_modules = cfg->layers[n].n_modules;
+    c->layers_cfg[n].modules = c->mods_cfg[n].data();
+  }
+  c->cfg.layers = c->layers_cfg.data();
+  c->dist = dd;
+  c->dt = cfg->dtype == DHEN_BF16 ? BF16 : F32;
+  c->es = c->dt == BF16 ? 2 : 4;
+  c->d = cfg->d;
+  c->Bmax = cfg->batch_max_local;
+  return DHEN_OK;
+}
+
+dhen_status dhen_sizes(const dhen_config* cfg, const dhen_dist* dist, size_t* state_bytes, size_t* work_bytes) {
+  dhen_ctx c;
+  RET(make_ctx(cfg, dist, &c));
+  Carver s(nullptr), w(nullptr);
+  plan(&c, s, w);
+  if (state_bytes) *state_bytes = s.off + 256;
+  if (work_bytes) *work_bytes = w.off + 256;
+  return DHEN_OK;
+}
+
+dhen_status dhen_group_numel(const dhen_config* cfg, const dhen_dist* dist, int group, size_t* numel, size_t* shard) {
+  dhen_ctx c;
+  RET(make_ctx(cfg, dist, &c));
+  Carver s(nullptr), w(nullptr);
+  plan(&c, s, w);
+  if (group < 0 || group > cfg->n_layers) return fail(DHEN_E_SHAPE, "dhen_group_numel: group=%d of %d", group, cfg->n_layers + 1);
+  if (numel) *numel = (size_t)c.G[group].n;
+  if (shard) *shard = (size_t)c.G[group].shard;
+  return DHEN_OK;
+}
+
+dhen_status dhen_nccl_id(unsigned char out[128]) {
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  memcpy(out, id.internal, 128);
+  return DHEN_OK;
+}
+
+dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state, size_t state_bytes, void* work,
+                      size_t work_bytes, void* stream, dhen_ctx** out) {
+  if (!out) return fail(DHEN_E_ALIGN, "dhen_init: out is NULL");
+  *out = nullptr;
+  dhen_ctx* c = new dhen_ctx();
+  dhen_status s0 = make_ctx(cfg, dist, c);
+  if (s0 != DHEN_OK) { delete c; return s0; }
+  if (!aligned16(state) || !aligned16(work)) { delete c; return fail(DHEN_E_ALIGN, "dhen_init: state=%p work=%p not 16-B aligned", state, work); }
+  Carver sz(nullptr), wz(nullptr);
+  plan(c, sz, wz);
+  if (state_bytes < sz.off || work_bytes < wz.off) {
+    size_t a = sz.off, b = wz.off;
+    delete c;
+    return fail(DHEN_E_NOMEM, "dhen_init: state %zu < %zu or work %zu < %zu bytes", state_bytes, a, work_bytes, b);
+  }
+  // align bases to 256
+  Carver s((void*)(((uintptr_t)state + 255) & ~uintptr_t(255))), w((void*)(((uintptr_t)work + 255) & ~uintptr_t(255)));
+  if (((uintptr_t)state & 255) || ((uintptr_t)work & 255)) {
+    if (state_bytes < sz.off + 256 || work_bytes < wz.off + 256) { delete c; return fail(DHEN_E_NOMEM, "dhen_init: buffers too small after alignment"); }
+  }
+  plan(c, s, w);
+  if (c->dist.world > 1) {
+    ncclUniqueId id;
+    memcpy(id.internal, c->dist.nccl_id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, c->dist.world, id, c->dist.rank);
+    if (r != ncclSuccess) { delete c; return fail(DHEN_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)); }
+  }
+  // parameter init: every rank initialises its own slice of the canonical vector
+  const unsigned long long launches_before = g_launches;
+  cudaStream_t st = S(stream);
+  for (size_t gi = 0; gi < c->G.size(); ++gi) {
+    Group& g = c->G[gi];
+    const int64_t lo = (c->dist.world > 1 && c->dist.fsdp) ? (int64_t)c->dist.rank * g.shard : 0;
+    const int64_t hi = lo + g.shard;
+    cudaError_t e = cudaMemsetAsync(g.master, 0, g.shard * 4, st);
+    if (e != cudaSuccess) { delete c; return fail(DHEN_E_CUDA, "dhen_init: %s", cudaGetErrorString(e)); }
+    for (size_t t = 0; t < g.toff.size(); ++t) {
+      int64_t a = std::max(lo, g.toff[t]), b = std::min(hi, g.toff[t] + g.tn[t]);
+      if (a >= b) continue;
+      // uniform values depend on the tensor's global index only (same params at any world size)
+      if (g.tinit[t] == 0) {
+        cudaError_t e2 = init_uniform(g.master + (a - lo), b - a, g.tbound[t], c->cfg.seed, gi * 4096 + t, a - g.toff[t], st);
+        if (e2 != cudaSuccess) { delete c; return fail(DHEN_E_CUDA, "dhen_init: %s", cudaGetErrorString(e2)); }
+      } else {
+        cudaError_t e2 = fill(g.master + (a - lo), b - a, g.tinit[t] == 1 ? 1.f : 0.f, st);
+        if (e2 != cudaSuccess) { delete c; return fail(DHEN_E_CUDA, "dhen_init: %s", cudaGetErrorString(e2)); }
+      }
+    }
+    cudaError_t e3 = sgd_cast(g.master, nullptr, 0.f, g.comp, c->dt, g.shard, st);
+    if (e3 != cudaSuccess) { delete c; return fail(DHEN_E_CUDA, "dhen_init: %s", cudaGetErrorString(e3)); }
+    e3 = cudaMemsetAsync(g.grad, 0, g.npad * 4, st);
+    if (e3 != cudaSuccess) { delete c; return fail(DHEN_E_CUDA, "dhen_init: %s", cudaGetErrorString(e3)); }
+  }
+  c->launches0 = launches_before;
+  *out = c;
+  return DHEN_OK;
+}
+
+void dhen_destroy(dhen_ctx* c) {
+  if (!c) return;
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+}
+
+unsigned long long dhen_launch_count(const dhen_ctx* c) { return c ? g_launches - c->launches0 : 0; }
+
+dhen_status dhen_zero_grad(dhen_ctx* c, void* stream) {
+  if (!c) return fail(DHEN_E_STATE, "dhen_zero_grad: ctx is NULL");
+  for (auto& g : c->G) {
+    CK(cudaMemsetAsync(g.grad, 0, g.npad * 4, S(stream)));
+    if (g.gshard) CK(cudaMemsetAsync(g.gshard, 0, g.shard * 4, S(stream)));
+  }
+  return DHEN_OK;
+}
+
+dhen_status dhen_layer_fwd(dhen_ctx* c, int n, const void* x, void* y, int B, void* stream) {
+  if (!c) return fail(DHEN_E_STATE, "dhen_layer_fwd: ctx is NULL");
+  if (n < 0 || n >= c->cfg.n_layers) return fail(DHEN_E_SHAPE, "dhen_layer_fwd: layer=%d of %d", n, c->cfg.n_layers);
+  if (B < 1 || B > c->Bmax) return fail(DHEN_E_SHAPE, "dhen_layer_fwd: B=%d not in [1, %d]", B, c->Bmax);
+  if (!aligned16(x) || !aligned16(y)) return fail(DHEN_E_ALIGN, "dhen_layer_fwd: x=%p y=%p", x, y);
+  invalidate_gathered(c);
+  RET(layer_fwd(c, n, x, y, B, S(stream)));
+  CK(cudaGetLastError());
+  return DHEN_OK;
+}
+
+dhen_status dhen_layer_bwd(dhen_ctx* c, int n, const void* dy, void* dx, int B, void* stream) {
+  if (!c) return fail(DHEN_E_STATE, "dhen_layer_bwd: ctx is NULL");
+  if (n < 0 || n >= c->cfg.n_layers) return fail(DHEN_E_SHAPE, "dhen_layer_bwd: layer=%d of %d", n, c->cfg.n_layers);
+  if (c->L[n].B != B) return fail(DHEN_E_STATE, "dhen_layer_bwd: layer %d has no saved forward at B=%d (saved B=%d)", n, B, c->L[n].B);
+  if (!aligned16(dy) || (dx && !aligned16(dx))) return fail(DHEN_E_ALIGN, "dhen_layer_bwd: dy=%p dx=%p", dy, dx);
+  invalidate_gathered(c);
+  RET(layer_bwd(c, n, dy, dx, B, S(stream)));
+  CK(cudaGetLastError());
+  return DHEN_OK;
+}
+
+dhen_status dhen_forward(dhen_ctx* c, const void* x0, int B, float* logits, void* stream) {
+  if (!c) return fail(DHEN_E_STATE, "dhen_forward: ctx is NULL");
+  if (B < 1 || B > c->Bmax) return fail(DHEN_E_SHAPE, "dhen_forward: B=%d not in [1, %d]", B, c->Bmax);
+  if (!aligned16(x0) || !aligned16(logits)) return fail(DHEN_E_ALIGN, "dhen_forward: x0=%p logits=%p", x0, logits);
+  cudaStream_t st = S(stream);
+  invalidate_gathered(c);
+  const void* X = x0;
+  for (int n = 0; n < c->cfg.n_layers; ++n) {
+    RET(layer_fwd(c, n, X, c->L[n].Y, B, st));
+    X = c->L[n].Y;
+  }
+  RET(head(c, X, c->L.back().m_out, nullptr, B, B, nullptr, nullptr, 0, st));
+  CK(cudaMemcpyAsync(logits, c->z, (size_t)B * 4, cudaMemcpyDeviceToDevice, st));
+  CK(cudaGetLastError());
+  return DHEN_OK;
+}
+
+dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, int B, int Bg, float lr, float* loss,
+                            void* dx0, void* stream) {
+  if (!c) return fail(DHEN_E_STATE, "dhen_train_step: ctx is NULL");
+  if (B < 1 || B > c->Bmax) return fail(DHEN_E_SHAPE, "dhen_train_step: B=%d not in [1, %d]", B, c->Bmax);
+  if (Bg < B) return fail(DHEN_E_SHAPE, "dhen_train_step: B_global=%d < B=%d", Bg, B);
+  if (!aligned16(x0) || !aligned16(labels) || (dx0 && !aligned16(dx0)) || (loss && ((uintptr_t)loss & 3)))
+    return fail(DHEN_E_ALIGN, "dhen_train_step: x0=%p labels=%p dx0=%p loss=%p", x0, (const void*)labels, dx0, (void*)loss);
+  if (!std::isfinite(lr)) return fail(DHEN_E_CONFIG, "dhen_train_step: lr=%g", (double)lr);
+  cudaStream_t st = S(stream);
+  RET(dhen_zero_grad(c, stream));
+  invalidate_gathered(c);
+  const void* X = x0;
+  for (int n = 0; n < c->cfg.n_layers; ++n) {
+    RET(layer_fwd(c, n, X, c->L[n].Y, B, st));
+    X = c->L[n].Y;
+  }
+  RET(head(c, X, c->L.back().m_out, labels, B, Bg, c->dY[0], loss, 1, st));
+  int cur = 0;
+  for (int n = c->cfg.n_layers - 1; n >= 0; --n) {
+    void* dx = n > 0 ? c->dY[cur ^ 1] : dx0;
+    RET(layer_bwd(c, n, c->dY[cur], dx, B, st));
+    cur ^= 1;
+  }
+  // B12: SGD on the (local shard of the) fp32 masters, refresh the compute copy
+  for (auto& g : c->G) {
+    const float* gr = c->dist.world > 1 ? g.gshard : g.grad;
+    CK(sgd_cast(g.master, gr, lr, g.comp, c->dt, g.shard, st));
+  }
+  invalidate_gathered(c);
+  CK(cudaGetLastError());
+  return DHEN_OK;
+}
+
+dhen_status dhen_params_io(dhen_ctx* c, int gi, float* host, int set, void* stream) {
+  if (!c) return fail(DHEN_E_STATE, "dhen_params_io: ctx is NULL");
+  if (gi < 0 || gi > c->cfg.n_layers) return fail(DHEN_E_SHAPE, "dhen_params_io: group=%d", gi);
+  if (!host) return fail(DHEN_E_ALIGN, "dhen_params_io: host is NULL");
+  Group& g = c->G[gi];
+  cudaStream_t st = S(stream);
+  const bool sh = c->dist.world > 1 && c->dist.fsdp;
+  const int64_t lo = sh ? (int64_t)c->dist.rank * g.shard : 0;
+  if (set) {
+    CK(cudaMemsetAsync(g.master, 0, g.shard * 4, st));
+    int64_t n = std::min<int64_t>(g.shard, std::max<int64_t>(0, g.n - lo));
+    if (n > 0) CK(cudaMemcpyAsync(g.master, host + lo, n * 4, cudaMemcpyHostToDevice, st));
+    CK(sgd_cast(g.master, nullptr, 0.f, g.comp, c->dt, g.shard, st));
+    invalidate_gathered(c);
+    CK(cudaStreamSynchronize(st));
+  } else {
+    if (sh) {
+      NK(ncclAllGather(g.master, g.grad, (size_t)g.shard, ncclFloat32, c->comm, st));   // grad buffer as temp
+      CK(cudaMemcpyAsync(host, g.grad, g.n * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemsetAsync(g.grad, 0, g.npad * 4, st));
+    } else {
+      CK(cudaMemcpyAsync(host, g.master, g.n * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+  }
+  return DHEN_OK;
+}
+
+dhen_status dhen_grads_get(dhen_ctx* c, int gi, float* host, void* stream) {
+  if (!c) return fail(DHEN_E_STATE, "dhen_grads_get: ctx is NULL");
+  if (gi < 0 || gi > c->cfg.n_layers) return fail(DHEN_E_SHAPE, "dhen_grads_get: group=%d", gi);
+  if (!host) return fail(DHEN_E_ALIGN, "dhen_grads_get: host is NULL");
+  Group& g = c->G[gi];
+  cudaStream_t st = S(stream);
+  if (c->dist.world > 1 && c->dist.fsdp) {
+    void* tmp = c->ws.ptr;   // split-K workspace as temp (>= npad floats checked below)
+    if ((size_t)g.npad * 4 > c->ws.bytes) return fail(DHEN_E_NOMEM, "dhen_grads_get: group too large for temp");
+    NK(ncclAllGather(g.gshard, tmp, (size_t)g.shard, ncclFloat32, c->comm, st));
+    CK(cudaMemcpyAsync(host, tmp, g.n * 4, cudaMemcpyDeviceToHost, st));
+  } else if (c->dist.world > 1) {
+    CK(cudaMemcpyAsync(host, g.gshard, g.n * 4, cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(cudaMemcpyAsync(host, g.grad, g.n * 4, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return DHEN_OK;
+}
+
+}  // extern "C"

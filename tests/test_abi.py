@@ -1,0 +1,80 @@
+"""C ABI checks that need no GPU: the library loads, exports every symbol
+include/dhen.h declares, validates configs with the documented errors, and its
+parameter layout agrees with the oracle's canonical order (sizes per group)."""
+import os
+import re
+
+import pytest
+
+from oracle import dhen_oracle as O
+from tests.helpers import config, small
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_2203_11014_b200 import binding, build
+    build.build()
+    binding.load()
+    return binding
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "dhen.h")).read()
+    return sorted(set(re.findall(r"\b(dhen_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_header_symbol(B):
+    lib = B.load()
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(B.EXPORTS)
+
+
+def _cfg(B, net, dtype="bf16", bmax=8):
+    from tests.gpu_common import to_binding
+    return to_binding(net, dtype, bmax)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_group_sizes_match_oracle_layout(B, name):
+    net = config(name)
+    cfg = _cfg(B, net)
+    groups = O.param_groups(net)
+    for gi, g in enumerate(groups):
+        n, sh = B.group_numel(cfg, gi)
+        assert n == O.group_size(g), (gi, n, O.group_size(g))
+        assert sh >= n and sh % 64 == 0
+    # sharded: shard * world covers the padded group
+    d = B.make_dist(rank=1, world=8)
+    for gi in range(len(groups)):
+        n, sh = B.group_numel(cfg, gi, d)
+        assert sh * 8 >= n and sh % 64 == 0
+
+
+def test_validate_errors(B):
+    bad = [
+        (O.NetSpec(1, 16, [O.LayerSpec([O.ModuleSpec("dot", 2)])]), "Dot needs m >= 2"),
+        (O.NetSpec(4, 12, [O.LayerSpec([O.ModuleSpec("linear", 2)])]), "multiple of 8"),
+        (O.NetSpec(4, 24, [O.LayerSpec([O.ModuleSpec("attn", 2, heads=5)])]), "heads"),
+        (O.NetSpec(4, 16, [O.LayerSpec([O.ModuleSpec("conv", 2, conv_k=4)])]), "odd"),
+        (O.NetSpec(4, 16, [O.LayerSpec([O.ModuleSpec("linear", 0)])]), "l=0"),
+    ]
+    for net, frag in bad:
+        with pytest.raises(B.DhenError) as ei:
+            B.validate(_cfg(B, net))
+        assert ei.value.status == 1 and frag in str(ei.value), str(ei.value)
+    B.validate(_cfg(B, small("C4")))
+
+
+def test_sizes_scale_with_batch(B):
+    net = config("C2")
+    s1, w1 = B.sizes(_cfg(B, net, bmax=64))
+    s2, w2 = B.sizes(_cfg(B, net, bmax=128))
+    assert s1 == s2 and w2 > w1
+    # saved activations at C4's per-GPU batch fit one B200 (180 GB)
+    s, w = B.sizes(_cfg(B, config("C4"), bmax=8192))
+    assert s + w < 170e9, (s, w)
