@@ -1,0 +1,330 @@
+"""DHEN training-step benchmark (BASELINE.json metric: train samples/s, fwd + bwd).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step is one `dhen_train_step` (forward of every layer, head + BCE loss,
+backward, reduce-scatter when N > 1, SGD) over one synthetic batch of the
+config's per-GPU size.  N > 1 runs one process per GPU (torchrun), batch-sharded
+with fully sharded parameters (weak scaling: per-GPU batch fixed).
+
+value:   device time (CUDA events on the launch stream) of K steps, inputs
+         resident in HBM, L2 flushed (256 MiB write) before every timed step,
+         max over ranks;  samples/s = N * B_local * K / time.
+e2e:     the same through the public API with pinned HOST buffers: every step
+         copies X0 + labels host->device and the loss device->host inside the
+         timed region.
+roofline: the op with the largest device time in a separate profiled pass of K
+         steps (per-op CUDA events from dhen_profile), algorithmic FLOPs or bytes
+         per launch / its mean launch time, against MEASURED_PEAKS.json.
+cpu_baseline: the fp64 oracle (test infrastructure) on a bounded sample of the
+         same workload on this host's cores (rank 0, N = 1 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return {"hbm": j["hbm_gbs"], "tc": j["bf16_tflops"], "tc_sus": j["bf16_tflops_sustained"],
+                "sm_max_mhz": j.get("sm_max_mhz", 1965.0), "src": "measured"}
+    return {"hbm": 6650.0, "tc": 1590.0, "tc_sus": 1400.0, "sm_max_mhz": 1965.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8:
+                self.rows.append(f)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(self.rows[0][1]),
+                "samples": len(self.rows), "reasons": reasons}
+
+
+def cpu_baseline(cfg_name: str, target_s: float = 12.0):
+    """The fp64 oracle (as it stands) on a bounded sample of the workload."""
+    import numpy as np
+    import synth
+    from oracle import dhen_oracle as O
+    from tests.helpers import config, make_flat_params, oracle_params
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([t.get("num_threads", 1) for t in threadpool_info()] or [1])
+    except Exception:
+        cores = os.cpu_count() or 1
+    net = config(cfg_name)
+    params = oracle_params(net, make_flat_params(net, 1))
+    Bo = {"C1": 32, "C2": 16, "C3": 4, "C4": 2, "C5": 8}[cfg_name]
+    X0 = synth.make_x0(1, Bo, net.m0, net.d, bf16=True).astype(np.float64)
+    y = synth.make_labels(1, Bo).astype(np.float64)
+    t0 = time.perf_counter()
+    steps = 0
+    while True:
+        O.train_step(net, params, X0, y, 0.01)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= target_s or (steps >= 1 and el * (steps + 1) / steps > 3 * target_s):
+            break
+    return {"value": steps * Bo / el, "unit": "samples/s", "cores": int(cores), "kind": "oracle",
+            "sample": f"{steps} fp64 oracle train steps of {Bo} samples of {cfg_name} "
+                      f"({el:.1f} s; cost is linear in B)", "seconds": round(el, 2)}
+
+
+def run_reference(args):
+    """--impl reference: the oracle is this tier's reference arm (host cores)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import synth
+    from oracle import dhen_oracle as O
+    from tests.helpers import config, make_flat_params, oracle_params
+    net = config(args.config)
+    params = oracle_params(net, make_flat_params(net, 1))
+    Bo = {"C1": 32, "C2": 8, "C3": 2, "C4": 1, "C5": 4}[args.config]
+    X0 = synth.make_x0(1, Bo, net.m0, net.d, bf16=True).astype(np.float64)
+    y = synth.make_labels(1, Bo).astype(np.float64)
+    for _ in range(args.warmup):
+        O.train_step(net, params, X0, y, 0.01)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.train_step(net, params, X0, y, 0.01)
+    el = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([t.get("num_threads", 1) for t in threadpool_info()] or [1])
+    except Exception:
+        cores = os.cpu_count() or 1
+    v = args.steps * Bo / el
+    from paper_2203_11014_b200 import configs
+    print(json.dumps({
+        "impl": "reference", "metric": "DHEN train samples/sec (fwd+bwd)", "value": v, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {configs.DESCR[args.config]}", "global_batch": Bo,
+                   "sample_of_batch": configs.BATCH[args.config]},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": int(cores), "kind": "oracle",
+                         "sample": f"{args.steps} steps x {Bo} samples of {args.config} (fp64 oracle)"},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the config's)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-json", default="")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2203_11014_b200 import binding, configs, flops
+    from paper_2203_11014_b200 import build as _build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0 and not os.path.exists(binding.LIB_PATH):
+        _build.build()
+    if world > 1:
+        dist.barrier()
+
+    cfg = configs.make(args.config, args.batch or None)
+    B = cfg.batch_max_local
+    nid = None
+    if world > 1:
+        obj = [binding.nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    model = binding.DHEN(cfg, rank=rank, world=world, nccl_id=nid)
+    tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    X0 = synth.make_x0(synth.SEED_BASE + 100 + rank, B, cfg.m0, cfg.d, bf16=(cfg.dtype == "bf16"))
+    y = synth.make_labels(synth.SEED_BASE + 100 + rank, B)
+    x0 = torch.tensor(X0, device="cuda").to(tdt).contiguous()
+    lab = torch.tensor(y, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    Bg = B * world
+    lr = 0.01
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+
+    def step():
+        model.train_step(x0, lab, lr, B_global=Bg, loss=loss)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device time, L2 flushed before each step)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = model.launches()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(st)
+            step()
+            ev[k][1].record(st)
+        torch.cuda.synchronize()
+    launches = model.launches() - l0 - 0
+    if world > 1:
+        dist.barrier()
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([dev_ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms = float(t.item())
+    value = Bg * args.steps / (dev_ms / 1e3)
+    loss_val = float(loss.item())
+
+    # ---------------- e2e: public API with pinned host buffers, copies inside the timed region
+    hx = torch.tensor(X0).to(tdt).pin_memory()
+    hy = torch.tensor(y).pin_memory()
+    hl = torch.zeros(1).pin_memory()
+    dx = torch.empty_like(x0)
+    dy = torch.empty_like(lab)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(args.steps):
+        dx.copy_(hx, non_blocking=True)
+        dy.copy_(hy, non_blocking=True)
+        model.train_step(dx, dy, lr, B_global=Bg, loss=loss)
+        hl.copy_(loss, non_blocking=True)
+    e1.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    e2e = {"value": Bg * args.steps / (e2e_ms / 1e3), "unit": "samples/s",
+           "h2d_bytes_per_step": int(hx.numel() * hx.element_size() + hy.numel() * 4), "d2h_bytes_per_step": 4}
+
+    # ---------------- profiled pass: per-op device time (roofline of the dominant op)
+    model.profile(True)
+    for _ in range(args.steps):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    ops = model.profile_read()
+    model.profile(False)
+    tot_ms = sum(o["ms"] for o in ops)
+    top = max(ops, key=lambda o: o["ms"])
+    pk = peaks()
+    per_launch_ms = top["ms"] / top["launches"]
+    ai = top["flops"] / max(top["bytes"], 1.0)
+    ridge = pk["tc_sus"] * 1e12 / (pk["hbm"] * 1e9)
+    is_gemm = top["flops"] > 0 and not top["name"].startswith(("conv", "head", "layer", "attn.soft"))
+    tc_path = top.get("tc_launches", 0) > 0
+    if is_gemm and ai >= ridge and tc_path:
+        bound, unit, achieved, peak = "tensor", "TFLOP/s", top["flops"] / top["ms"] / 1e9, pk["tc_sus"]
+    elif is_gemm and not tc_path:
+        # exact-FP32 SIMT FMA path: 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz
+        bound, unit, achieved, peak = "alu", "TFLOP/s", top["flops"] / top["ms"] / 1e9, 148 * 128 * 2 * 1.965e-3
+    else:
+        bound, unit, achieved, peak = "hbm", "GB/s", top["bytes"] / top["ms"] / 1e6, pk["hbm"]
+    roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+            "traffic": None, "kernel": top["name"], "share_of_step": top["ms"] / tot_ms,
+            "per_launch_ms": per_launch_ms, "launches_per_step": top["launches"] / args.steps,
+            "peak_source": pk["src"] + (" sustained bf16" if bound == "tensor" else "")}
+    if args.profile_json and rank == 0:
+        json.dump({"ops": ops, "steps": args.steps}, open(args.profile_json, "w"), indent=1)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    tf = flops.train_flops_per_sample(cfg)
+    out = {
+        "metric": "DHEN train samples/sec (fwd+bwd)", "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+        "config": {"workload": f"{args.config}: {configs.DESCR[args.config]}", "global_batch": Bg, "batch_per_gpu": B,
+                   "m0": cfg.m0, "d": cfg.d, "layers": len(cfg.layers),
+                   "parallelism": f"fsdp{world}" if world > 1 else "single",
+                   "l2": "flushed (256 MiB write) before every timed step"},
+        "mfu": {"train_flops_per_sample": tf, "vs_burst": value * tf / (world * pk["tc"] * 1e12),
+                "vs_sustained": value * tf / (world * pk["tc_sus"] * 1e12)},
+        "loss": loss_val,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / args.steps,
+        "clocks": clk.summary(),
+        "roofline": roof,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.config)
+    print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -155,6 +155,36 @@ dhen_status dhen_params_io(dhen_ctx* ctx, int group, float* host, int set, void*
  * -> host.  Synchronises `stream`. */
 dhen_status dhen_grads_get(dhen_ctx* ctx, int group, float* host, void* stream);
 
+/* Per-op device timing: enable != 0 clears and starts recording a CUDA event
+ * pair around every op the library launches (on the op's stream); 0 stops.
+ * Adds two event records per op: for measurement passes, not the timed step. */
+dhen_status dhen_profile(dhen_ctx* ctx, int enable);
+
+typedef struct {
+  char name[40];                /* op tag, e.g. "dot.proj", "layer.ln"           */
+  unsigned long long launches;  /* recorded launches of this op                   */
+  double ms;                    /* summed device time (CUDA events)               */
+  double flops;                 /* summed algorithmic FLOPs (2 M N K per GEMM)    */
+  double bytes;                 /* summed algorithmic HBM bytes (operands once)   */
+  unsigned long long tc_launches; /* launches that ran on the tcgen05 tensor-core path */
+} dhen_op_stat;
+
+/* Aggregate the recorded ops by tag (synchronises on the recorded events):
+ * writes min(cap, *n) entries to out, *n = number of distinct tags. */
+dhen_status dhen_profile_read(dhen_ctx* ctx, dhen_op_stat* out, int cap, int* n);
+
+/* Test hook (tests/test_gpu_gemm.py): one strided / batched contraction
+ *   C[z][i][j] (+)= sum_k A[z][i][k] B[z][k][j]
+ * through the library's GEMM dispatcher.  q = int64[24]: M, N, K, batch,
+ * A{s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko}, B{s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko},
+ * C{rs, cs, bs0, bs1, zdiv}, accumulate.  ab_dtype/c_dtype: dhen_dtype.
+ * path: 0 auto, 1 SIMT only, 2 tcgen05 only (DHEN_E_CONFIG if not expressible).
+ * ws: fp32 device scratch for split-K partials. */
+dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* B, void* C, int ab_dtype, int c_dtype,
+                            int path, void* ws, size_t ws_bytes, void* stream);
+/* 1 if the last GEMM ran on the tcgen05 path. */
+int dhen_debug_last_gemm_tc(void);
+
 /* Number of library kernels launched since init (a host-side counter). */
 unsigned long long dhen_launch_count(const dhen_ctx* ctx);
 

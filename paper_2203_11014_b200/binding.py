@@ -22,7 +22,8 @@ STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_SHAPE", 3: "E_ALIGN", 4: "E_STATE", 5: "
 # every symbol include/dhen.h declares
 EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "dhen_init", "dhen_layer_fwd",
            "dhen_layer_bwd", "dhen_train_step", "dhen_forward", "dhen_zero_grad", "dhen_params_io",
-           "dhen_grads_get", "dhen_launch_count", "dhen_last_error", "dhen_destroy")
+           "dhen_grads_get", "dhen_launch_count", "dhen_last_error", "dhen_destroy", "dhen_profile",
+           "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_last_gemm_tc")
 
 
 class dhen_module(C.Structure):
@@ -42,6 +43,11 @@ class dhen_config(C.Structure):
 
 class dhen_dist(C.Structure):
     _fields_ = [("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.c_ubyte * 128), ("fsdp", C.c_int)]
+
+
+class dhen_op_stat(C.Structure):
+    _fields_ = [("name", C.c_char * 40), ("launches", C.c_ulonglong), ("ms", C.c_double), ("flops", C.c_double),
+                ("bytes", C.c_double), ("tc_launches", C.c_ulonglong)]
 
 
 class DhenError(RuntimeError):
@@ -75,6 +81,9 @@ def load(path: str = LIB_PATH):
         "dhen_zero_grad": [vp, vp],
         "dhen_params_io": [vp, i, vp, i, vp],
         "dhen_grads_get": [vp, i, vp, vp],
+        "dhen_profile": [vp, i],
+        "dhen_profile_read": [vp, C.POINTER(dhen_op_stat), i, C.POINTER(i)],
+        "dhen_debug_gemm": [C.POINTER(C.c_longlong), vp, vp, vp, i, i, i, vp, sz, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -84,6 +93,8 @@ def load(path: str = LIB_PATH):
     lib.dhen_last_error.argtypes = []
     lib.dhen_launch_count.restype = C.c_ulonglong
     lib.dhen_launch_count.argtypes = [vp]
+    lib.dhen_debug_last_gemm_tc.restype = C.c_int
+    lib.dhen_debug_last_gemm_tc.argtypes = []
     lib.dhen_destroy.restype = None
     lib.dhen_destroy.argtypes = [vp]
     _lib = lib
@@ -182,6 +193,22 @@ def nccl_id() -> bytes:
     return bytes(buf)
 
 
+def debug_gemm(q, A, B, Cm, path=0, ws=None, stream=None):
+    """Test hook: one contraction through the library's GEMM dispatcher (see dhen.h).
+    Returns True if it ran on the tcgen05 path."""
+    import torch
+    arr = (C.c_longlong * 24)(*[int(v) for v in q])
+    abt = BF16 if A.dtype == torch.bfloat16 else FP32
+    ct = BF16 if Cm.dtype == torch.bfloat16 else FP32
+    if ws is None:
+        ws = torch.empty(64 << 20, dtype=torch.uint8, device=A.device)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check("dhen_debug_gemm", load().dhen_debug_gemm(arr, C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()),
+                                                     C.c_void_p(Cm.data_ptr()), abt, ct, path,
+                                                     C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(s.cuda_stream)))
+    return bool(load().dhen_debug_last_gemm_tc())
+
+
 def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
@@ -267,6 +294,19 @@ class DHEN:
         _check("dhen_train_step", self.lib.dhen_train_step(self.ctx, _ptr(x0), _ptr(labels), B,
                                                            B_global or B, float(lr), _ptr(loss), _ptr(dx0),
                                                            self._stream(stream)))
+
+    def profile(self, enable: bool):
+        _check("dhen_profile", self.lib.dhen_profile(self.ctx, int(enable)))
+
+    def profile_read(self):
+        """[{name, launches, ms, flops, bytes}] aggregated per op tag."""
+        cap = 256
+        arr = (dhen_op_stat * cap)()
+        n = C.c_int()
+        _check("dhen_profile_read", self.lib.dhen_profile_read(self.ctx, arr, cap, C.byref(n)))
+        return [{"name": arr[k].name.decode(), "launches": arr[k].launches, "ms": arr[k].ms,
+                 "flops": arr[k].flops, "bytes": arr[k].bytes,
+                 "tc_launches": arr[k].tc_launches} for k in range(min(n.value, cap))]
 
     def forward(self, x0, logits, stream=None):
         _check("dhen_forward", self.lib.dhen_forward(self.ctx, _ptr(x0), x0.shape[0], _ptr(logits),

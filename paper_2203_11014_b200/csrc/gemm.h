@@ -65,10 +65,18 @@ struct Workspace {              // scratch for split-K partials (fp32)
 
 // Launch counter (reported as gpu_launches by the bench).
 extern unsigned long long g_launches;
+// 1 if the last gemm_run took the tcgen05 path (profiling attribution).
+extern int g_last_gemm_tc;
+// path override: -1 env/auto, 0 auto, 1 SIMT only, 2 tcgen05 only (test hook)
+extern int g_gemm_force;
 
 // Dispatch: tcgen05/TMA path when the shapes and layouts allow it, the SIMT
 // path (exact fp32 FMA; the fp32 mode and odd shapes) otherwise.
 cudaError_t gemm_run(const Gemm& g, const Workspace& ws, cudaStream_t st);
 cudaError_t gemm_simt(const Gemm& g, const Workspace& ws, cudaStream_t st);
+// tcgen05 path; returns cudaErrorNotSupported (nothing launched) when the GEMM does not qualify.
+cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st);
+// sums split-K partials ws[(z*splits+sp)][M][N] in fixed order and applies the epilogue.
+cudaError_t splitk_reduce(const Gemm& g, int splits, const float* ws, cudaStream_t st);
 
 }  // namespace dhen

@@ -3,41 +3,12 @@
 // take.  64x64x16 tiles, 256 threads, 4x4 outputs per thread, deterministic
 // split-K (fixed-order second pass) for long reductions.
 #include "gemm.h"
+#include "gemm_epi.cuh"
 #include <algorithm>
 
 namespace dhen {
 
 unsigned long long g_launches = 0;
-
-__device__ __forceinline__ void epi_apply(const Gemm& g, int z, int i, int j, float acc) {
-  const Epilogue& e = g.e;
-  float v = acc * e.alpha;
-  if (e.bias) {
-    int bj = j;
-    bool has = true;
-    if (e.bias_gap_hi > e.bias_gap_lo) {
-      if (j >= e.bias_gap_lo && j < e.bias_gap_hi) has = false;
-      else if (j >= e.bias_gap_hi) bj = j - (e.bias_gap_hi - e.bias_gap_lo);
-    }
-    if (has) v += ld_as_f32(e.bias, bj, e.bias_dt);
-  }
-  if (e.cross.ptr) {
-    if (e.aux.ptr) st_from_f32(e.aux.ptr, e.aux.off(z, i, j), e.aux.dt, v);
-    float x = ld_as_f32(e.cross.ptr, e.cross.off(z, i, j), e.cross.dt);
-    v = x * v + x;
-  } else if (e.aux.ptr) {
-    st_from_f32(e.aux.ptr, e.aux.off(z, i, j), e.aux.dt, v);
-  }
-  if (e.relu) v = fmaxf(v, 0.f);
-  if (e.mask.ptr) {
-    float mv = ld_as_f32(e.mask.ptr, e.mask.off(z, i, j), e.mask.dt);
-    v = mv > 0.f ? v : 0.f;
-  }
-  if (e.resid.ptr) v += ld_as_f32(e.resid.ptr, e.resid.off(z, i, j), e.resid.dt);
-  int64_t co = g.c.off(z, i, j);
-  if (e.accumulate) v += ld_as_f32(g.c.ptr, co, g.c.dt);
-  st_from_f32(g.c.ptr, co, g.c.dt, v);
-}
 
 constexpr int BM = 64, BN = 64, BK = 16;
 
@@ -107,6 +78,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(Gemm g, int splits, int 
 }
 
 __global__ void splitk_reduce_kernel(Gemm g, int splits, const float* ws) {
+  // partial tiles ws[(z * splits + sp)][M][N] summed in fixed split order, then the epilogue
   int64_t total = (int64_t)g.batch * g.M * g.N;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t zb = t / ((int64_t)g.M * g.N);
@@ -144,12 +116,15 @@ cudaError_t gemm_simt(const Gemm& g, const Workspace& ws, cudaStream_t st) {
       gemm_simt_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(g, splits, kchunk, ws.ptr, zb);
     ++g_launches;
   }
-  if (splits > 1) {
-    int64_t total = (int64_t)g.batch * g.M * g.N;
-    int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g, splits, ws.ptr);
-    ++g_launches;
-  }
+  if (splits > 1) return splitk_reduce(g, splits, ws.ptr, st);
+  return cudaGetLastError();
+}
+
+cudaError_t splitk_reduce(const Gemm& g, int splits, const float* ws, cudaStream_t st) {
+  int64_t total = (int64_t)g.batch * g.M * g.N;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g, splits, ws);
+  ++g_launches;
   return cudaGetLastError();
 }
 

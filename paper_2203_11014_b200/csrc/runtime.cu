@@ -135,7 +135,41 @@ struct dhen_ctx {
   float *pooled = nullptr, *z = nullptr, *lossb = nullptr, *dz = nullptr;
   ncclComm_t comm = nullptr;
   unsigned long long launches0 = 0;
+  // per-op device timing (dhen_profile): event pairs on the launch stream
+  struct Rec { const char* tag; int e0, e1; double flops, bytes; int tc; };
+  bool prof = false;
+  std::vector<cudaEvent_t> events;
+  int next_event = 0;
+  std::vector<Rec> recs;
 };
+
+// RAII scope recording a CUDA event pair around one op when profiling is on.
+struct ProfScope {
+  dhen_ctx* c;
+  cudaStream_t st;
+  int rec = -1;
+  ProfScope(dhen_ctx* c_, const char* tag, double flops, double bytes, cudaStream_t st_) : c(c_), st(st_) {
+    if (!c->prof) return;
+    if (c->next_event + 2 > (int)c->events.size()) {
+      if (c->events.size() >= (1u << 16)) return;   // pool exhausted: stop recording
+      size_t n0 = c->events.size();
+      c->events.resize(n0 + 1024);
+      for (size_t i = n0; i < c->events.size(); ++i) cudaEventCreate(&c->events[i]);
+    }
+    int e0 = c->next_event++, e1 = c->next_event++;
+    cudaEventRecord(c->events[e0], st);
+    c->recs.push_back({tag, e0, e1, flops, bytes, 0});
+    rec = (int)c->recs.size() - 1;
+  }
+  ~ProfScope() {
+    if (rec >= 0) cudaEventRecord(c->events[c->recs[rec].e1], st);
+  }
+};
+#define KT(tag, flops, bytes, call)                          \
+  do {                                                       \
+    ProfScope ps_(c, tag, (double)(flops), (double)(bytes), st); \
+    CK(call);                                                \
+  } while (0)
 
 // ------------------------------------------------------------------ validation / planning
 static int mdef(int v, int d) { return v > 0 ? v : d; }
@@ -334,8 +368,18 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
 }
 
 // ------------------------------------------------------------------ GEMM helpers
-static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st) {
+static double vbytes(const View& v, double n) { return v.ptr ? n * (v.dt == F32 ? 4 : 2) : 0; }
+static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const char* tag) {
+  // algorithmic traffic: each operand read once (shared operands once), C written (and read if +=)
+  const double es = g.a.dt == F32 ? 4 : 2;
+  const double mn = (double)g.M * g.N * g.batch;
+  double bytes = (double)g.M * g.K * es * (g.a.bs0 || g.a.bs1 ? g.batch : 1) +
+                 (double)g.N * g.K * es * (g.b.bs0 || g.b.bs1 ? g.batch : 1) +
+                 vbytes(g.c, mn) * (g.e.accumulate ? 2 : 1) + vbytes(g.e.resid, mn) + vbytes(g.e.mask, mn) +
+                 vbytes(g.e.cross, mn) + vbytes(g.e.aux, mn);
+  ProfScope ps(c, tag, 2.0 * (double)g.M * g.N * g.K * g.batch, bytes, st);
   CK(gemm_run(g, c->ws, st));
+  if (ps.rec >= 0) c->recs[ps.rec].tc = g_last_gemm_tc;
   return DHEN_OK;
 }
 static Gemm mk(int M, int N, int K, int batch, Operand a, Operand b, View cv) {
@@ -358,7 +402,7 @@ static dhen_status tokmix_fwd(dhen_ctx* c, const void* T, int m, const void* W, 
   Gemm g = mk(l, d, m, B, operand(W, dt, 1, l), operand(T, dt, 1, d, (int64_t)m * d),
               view(dst, F32, d, 1, ldb));
   g.e.accumulate = acc;
-  return G_(g, c, st);
+  return G_(g, c, st, "tokmix.fwd");
 }
 // B4: dT = W dU (set, dtype dT_dt) or dX += W dU (fp32 accumulate); dW += sum_b T_b dU_b^T
 static dhen_status tokmix_bwd(dhen_ctx* c, const void* T, int m, const void* W, int l, const void* dU, int64_t ldu,
@@ -366,11 +410,11 @@ static dhen_status tokmix_bwd(dhen_ctx* c, const void* T, int m, const void* W, 
   const int d = c->d, dt = c->dt;
   Gemm g = mk(m, d, l, B, operand(W, dt, l, 1), operand(dU, dt, 1, d, ldu), view(dT, dT_dt, d, 1, (int64_t)m * d));
   g.e.accumulate = acc;
-  RET(G_(g, c, st));
+  RET(G_(g, c, st, "tokmix.dgrad"));
   Gemm gw = mk(m, l, B * d, 1, operand(T, dt, d, 1, 0, 0, 1, d, (int64_t)m * d),
                operand(dU, dt, d, 1, 0, 0, 1, d, ldu), view(gW, F32, l, 1));
   gw.e.accumulate = 1;
-  return G_(gw, c, st);
+  return G_(gw, c, st, "tokmix.wgrad");
 }
 
 // ------------------------------------------------------------------ FSDP gather / scatter
@@ -418,10 +462,10 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         const int h = mi * (mi - 1) / 2;
         Gemm g = mk(mi, mi, d, B, operand(X, dt, d, 1, (int64_t)mi * d), operand(X, dt, d, 1, (int64_t)mi * d),
                     view(c->big, F32, mi, 1, (int64_t)mi * mi));
-        RET(G_(g, c, st));
-        CK(triu_extract(c->big, md.Z, dt, B, mi, h, st));
+        RET(G_(g, c, st, "dot.gram"));
+        KT("dot.triu", 0, (double)B * h * (4 + es), triu_extract(c->big, md.Z, dt, B, mi, h, st));
         Gemm v = mk(B, l * d, h, 1, operand(md.Z, dt, h, 1), operand(p(md.Wm), dt, h, 1), view(Us, F32, ldU, 1));
-        RET(G_(v, c, st));
+        RET(G_(v, c, st, "dot.proj"));
         break;
       }
       case DHEN_LINEAR:  // F10 with T = X
@@ -432,12 +476,12 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         g.e.bias = p(md.b); g.e.bias_dt = dt;
         g.e.cross = view((void*)X, dt, d, 1);
         g.e.aux = view(md.A, dt, d, 1);
-        RET(G_(g, c, st));
+        RET(G_(g, c, st, "dcn.cross"));
         RET(tokmix_fwd(c, md.T, mi, p(md.Wu), l, Us, ldU, B, 0, st));
         break;
       }
       case DHEN_CONV:    // F7
-        CK(conv_fwd(X, p(md.K), dt, md.s.conv_channels, md.s.conv_k, B, mi, d, md.T, dt, st));
+        KT("conv.fwd", 2.0 * rows * d * md.s.conv_k * md.s.conv_k, 2.0 * rows * d * es, conv_fwd(X, p(md.K), dt, md.s.conv_channels, md.s.conv_k, B, mi, d, md.T, dt, st));
         RET(tokmix_fwd(c, md.T, mi, p(md.Wu), l, Us, ldU, B, 0, st));
         break;
       case DHEN_ATTN: {  // F3-F6
@@ -446,28 +490,28 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         char* QKV = (char*)md.QKV;
         Gemm q = mk((int)rows, 3 * d, d, 1, operand(X, dt, d, 1), operand(p(md.Wq), dt, d, 1), view(QKV, dt, s3, 1));
         q.e.bias = p(md.bq); q.e.bias_dt = dt; q.e.bias_gap_lo = d; q.e.bias_gap_hi = 2 * d;   // no key bias (R10)
-        RET(G_(q, c, st));
+        RET(G_(q, c, st, "attn.qkv"));
         Gemm s = mk(mi, mi, dh, B * H, operand(QKV, dt, s3, 1, mi * s3, dh, H),
                     operand(QKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H),
                     view(c->big, F32, mi, 1, (int64_t)mi * mi));
         s.e.alpha = 1.f / sqrtf((float)dh);
-        RET(G_(s, c, st));
-        CK(softmax_rows(c->big, md.P, dt, (int64_t)B * H * mi, mi, st));
+        RET(G_(s, c, st, "attn.qk"));
+        KT("attn.softmax", 0, (double)B * H * mi * mi * (4 + es), softmax_rows(c->big, md.P, dt, (int64_t)B * H * mi, mi, st));
         Gemm o = mk(mi, dh, mi, B * H, operand(md.P, dt, mi, 1, (int64_t)mi * mi),
                     operand(QKV + 2 * (int64_t)d * es, dt, 1, s3, mi * s3, dh, H),
                     view(md.O, dt, d, 1, (int64_t)mi * d, dh, H));
-        RET(G_(o, c, st));
+        RET(G_(o, c, st, "attn.pv"));
         Gemm r1 = mk((int)rows, d, d, 1, operand(md.O, dt, d, 1), operand(p(md.Wo), dt, d, 1), view(c->rtmp, F32, d, 1));
         r1.e.bias = p(md.bo); r1.e.bias_dt = dt; r1.e.resid = view((void*)X, dt, d, 1);
-        RET(G_(r1, c, st));
-        CK(ln_fwd(c->rtmp, nullptr, p(md.g1), p(md.be1), dt, c->cfg.ln_eps, rows, d, md.Z1, md.R1, md.mu1, md.rs1, dt, st));
+        RET(G_(r1, c, st, "attn.out"));
+        KT("attn.ln1", 0, (double)rows * d * (4 + 2 * es), ln_fwd(c->rtmp, nullptr, p(md.g1), p(md.be1), dt, c->cfg.ln_eps, rows, d, md.Z1, md.R1, md.mu1, md.rs1, dt, st));
         Gemm f1 = mk((int)rows, f, d, 1, operand(md.Z1, dt, d, 1), operand(p(md.W1), dt, d, 1), view(md.F, dt, f, 1));
         f1.e.bias = p(md.b1); f1.e.bias_dt = dt; f1.e.relu = 1;
-        RET(G_(f1, c, st));
+        RET(G_(f1, c, st, "attn.ffn1"));
         Gemm f2 = mk((int)rows, d, f, 1, operand(md.F, dt, f, 1), operand(p(md.W2), dt, f, 1), view(c->rtmp, F32, d, 1));
         f2.e.bias = p(md.b2); f2.e.bias_dt = dt; f2.e.resid = view(md.Z1, dt, d, 1);
-        RET(G_(f2, c, st));
-        CK(ln_fwd(c->rtmp, nullptr, p(md.g2), p(md.be2), dt, c->cfg.ln_eps, rows, d, md.T, md.R2, md.mu2, md.rs2, dt, st));
+        RET(G_(f2, c, st, "attn.ffn2"));
+        KT("attn.ln2", 0, (double)rows * d * (4 + 2 * es), ln_fwd(c->rtmp, nullptr, p(md.g2), p(md.be2), dt, c->cfg.ln_eps, rows, d, md.T, md.R2, md.mu2, md.rs2, dt, st));
         RET(tokmix_fwd(c, md.T, mi, p(md.Wu), l, Us, ldU, B, 0, st));
         break;
       }
@@ -476,19 +520,19 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         const int K1 = mi * d;
         Gemm a = mk(B, h1, K1, 1, operand(X, dt, K1, 1), operand(p(md.W1), dt, K1, 1), view(md.h1, dt, h1, 1));
         a.e.bias = p(md.b1); a.e.bias_dt = dt; a.e.relu = 1;
-        RET(G_(a, c, st));
+        RET(G_(a, c, st, "mlp.fc1"));
         Gemm b2 = mk(B, h2, h1, 1, operand(md.h1, dt, h1, 1), operand(p(md.W2), dt, h1, 1), view(md.h2, dt, h2, 1));
         b2.e.bias = p(md.b2); b2.e.bias_dt = dt; b2.e.relu = 1;
-        RET(G_(b2, c, st));
+        RET(G_(b2, c, st, "mlp.fc2"));
         Gemm v = mk(B, l * d, h2, 1, operand(md.h2, dt, h2, 1), operand(p(md.Wm), dt, h2, 1), view(Us, F32, ldU, 1));
-        RET(G_(v, c, st));
+        RET(G_(v, c, st, "mlp.proj"));
         break;
       }
     }
   }
   // F11 shortcut (Eq.(2)) + F12 LayerNorm
   if (Lr.Wn >= 0) RET(tokmix_fwd(c, X, mi, p(Lr.Wn), mo, U, ldU, B, 1, st));
-  CK(ln_fwd(U, Lr.Wn >= 0 ? nullptr : X, p(Lr.gamma), p(Lr.beta), dt, c->cfg.ln_eps, (int64_t)B * mo, d, Y, Lr.R, Lr.mu,
+  KT("layer.ln", 0, (double)B * mo * d * (4 + 2 * es) + (Lr.Wn >= 0 ? 0.0 : (double)B * mo * d * es), ln_fwd(U, Lr.Wn >= 0 ? nullptr : X, p(Lr.gamma), p(Lr.beta), dt, c->cfg.ln_eps, (int64_t)B * mo, d, Y, Lr.R, Lr.mu,
             Lr.rstd, dt, st));
   Lr.X = X;
   Lr.B = B;
@@ -511,7 +555,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   const int64_t rows = (int64_t)B * mi;
   float* acc = c->dXacc;
   // B2: LN backward; identity shortcut (B3) initialises the dX accumulator
-  CK(ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc, Lr.Wn >= 0 ? 0 : 1,
+  KT("layer.ln_bwd", 0, (double)B * mo * d * (3 * es + 4), ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc, Lr.Wn >= 0 ? 0 : 1,
             gp(Lr.gamma), gp(Lr.beta), c->red, c->red_bytes, st));
   if (Lr.Wn >= 0)   // B3: dX = W_n dR ; dW_n += sum_b X_b dR_b^T
     RET(tokmix_bwd(c, X, mi, p(Lr.Wn), mo, c->dR, ldU, acc, F32, 0, gp(Lr.Wn), B, st));
@@ -523,14 +567,14 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         const int h = mi * (mi - 1) / 2;
         Gemm gw = mk(l * d, h, B, 1, operand(dU, dt, 1, ldU), operand(md.Z, dt, 1, h), view(gp(md.Wm), F32, h, 1));
         gw.e.accumulate = 1;
-        RET(G_(gw, c, st));
+        RET(G_(gw, c, st, "dot.proj_wgrad"));
         Gemm gz = mk(B, h, l * d, 1, operand(dU, dt, ldU, 1), operand(p(md.Wm), dt, 1, h), view(c->tA, dt, h, 1));
-        RET(G_(gz, c, st));
-        CK(sym_from_triu(c->tA, c->tD, dt, B, mi, h, st));
+        RET(G_(gz, c, st, "dot.proj_dgrad"));
+        KT("dot.sym", 0, (double)B * (h + mi * mi) * es, sym_from_triu(c->tA, c->tD, dt, B, mi, h, st));
         Gemm gx = mk(mi, d, mi, B, operand(c->tD, dt, mi, 1, (int64_t)mi * mi), operand(X, dt, 1, d, (int64_t)mi * d),
                      view(acc, F32, d, 1, (int64_t)mi * d));
         gx.e.accumulate = 1;
-        RET(G_(gx, c, st));
+        RET(G_(gx, c, st, "dot.gram_bwd"));
         break;
       }
       case DHEN_LINEAR:
@@ -540,21 +584,21 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         void* dT = c->tA;
         void* dA = c->tB;
         RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st));
-        CK(dcn_bwd_elem(dT, X, md.A, dA, acc, dt, rows * d, st));
+        KT("dcn.bwd_elem", 0, (double)rows * d * (4 * es + 8), dcn_bwd_elem(dT, X, md.A, dA, acc, dt, rows * d, st));
         Gemm gx = mk((int)rows, d, d, 1, operand(dA, dt, d, 1), operand(p(md.W), dt, 1, d), view(acc, F32, d, 1));
         gx.e.accumulate = 1;
-        RET(G_(gx, c, st));
+        RET(G_(gx, c, st, "dcn.dgrad"));
         Gemm gw = mk(d, d, (int)rows, 1, operand(dA, dt, 1, d), operand(X, dt, 1, d), view(gp(md.W), F32, d, 1));
         gw.e.accumulate = 1;
-        RET(G_(gw, c, st));
-        CK(colsum_add(dA, dt, rows, d, d, gp(md.b), c->red, c->red_bytes, st));
+        RET(G_(gw, c, st, "dcn.wgrad"));
+        KT("dcn.bias_grad", 0, (double)rows * d * es, colsum_add(dA, dt, rows, d, d, gp(md.b), c->red, c->red_bytes, st));
         break;
       }
       case DHEN_CONV: {  // B7
         void* dT = c->tA;
         RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st));
-        CK(conv_dgrad(dT, p(md.K), dt, md.s.conv_channels, md.s.conv_k, B, mi, d, acc, dt, st));
-        CK(conv_wgrad(dT, X, md.s.conv_channels, md.s.conv_k, B, mi, d, dt, gp(md.K), c->red, c->red_bytes, st));
+        KT("conv.dgrad", 2.0 * rows * d * md.s.conv_k * md.s.conv_k, (double)rows * d * (es + 8), conv_dgrad(dT, p(md.K), dt, md.s.conv_channels, md.s.conv_k, B, mi, d, acc, dt, st));
+        KT("conv.wgrad", 2.0 * rows * d * md.s.conv_k * md.s.conv_k, 2.0 * rows * d * es, conv_wgrad(dT, X, md.s.conv_channels, md.s.conv_k, B, mi, d, dt, gp(md.K), c->red, c->red_bytes, st));
         break;
       }
       case DHEN_ATTN: {  // B6
@@ -564,60 +608,60 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         void* dT = c->tB;
         RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st));
         void* dR2 = c->tA;   // [rows, d]
-        CK(ln_bwd(dT, dt, md.R2, md.mu2, md.rs2, p(md.g2), dt, rows, d, dR2, dt, nullptr, 0, gp(md.g2), gp(md.be2), c->red,
+        KT("attn.ln2_bwd", 0, (double)rows * d * 3 * es, ln_bwd(dT, dt, md.R2, md.mu2, md.rs2, p(md.g2), dt, rows, d, dR2, dt, nullptr, 0, gp(md.g2), gp(md.be2), c->red,
                   c->red_bytes, st));
         void* dF = c->tC;
         Gemm a = mk((int)rows, f, d, 1, operand(dR2, dt, d, 1), operand(p(md.W2), dt, 1, f), view(dF, dt, f, 1));
         a.e.mask = view(md.F, dt, f, 1);
-        RET(G_(a, c, st));
+        RET(G_(a, c, st, "attn.ffn2_dgrad"));
         Gemm w2 = mk(d, f, (int)rows, 1, operand(dR2, dt, 1, d), operand(md.F, dt, 1, f), view(gp(md.W2), F32, f, 1));
         w2.e.accumulate = 1;
-        RET(G_(w2, c, st));
-        CK(colsum_add(dR2, dt, rows, d, d, gp(md.b2), c->red, c->red_bytes, st));
+        RET(G_(w2, c, st, "attn.ffn2_wgrad"));
+        KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dR2, dt, rows, d, d, gp(md.b2), c->red, c->red_bytes, st));
         Gemm z1 = mk((int)rows, d, f, 1, operand(dF, dt, f, 1), operand(p(md.W1), dt, 1, d), view(c->rtmp, F32, d, 1));
         z1.e.resid = view(dR2, dt, d, 1);
-        RET(G_(z1, c, st));
+        RET(G_(z1, c, st, "attn.ffn1_dgrad"));
         Gemm w1 = mk(f, d, (int)rows, 1, operand(dF, dt, 1, f), operand(md.Z1, dt, 1, d), view(gp(md.W1), F32, d, 1));
         w1.e.accumulate = 1;
-        RET(G_(w1, c, st));
-        CK(colsum_add(dF, dt, rows, f, f, gp(md.b1), c->red, c->red_bytes, st));
+        RET(G_(w1, c, st, "attn.ffn1_wgrad"));
+        KT("attn.bias_grad", 0, (double)rows * f * es, colsum_add(dF, dt, rows, f, f, gp(md.b1), c->red, c->red_bytes, st));
         void* dR1 = c->tB;   // dT no longer needed
-        CK(ln_bwd(c->rtmp, F32, md.R1, md.mu1, md.rs1, p(md.g1), dt, rows, d, dR1, dt, acc, 2, gp(md.g1), gp(md.be1),
+        KT("attn.ln1_bwd", 0, (double)rows * d * (2 * es + 12), ln_bwd(c->rtmp, F32, md.R1, md.mu1, md.rs1, p(md.g1), dt, rows, d, dR1, dt, acc, 2, gp(md.g1), gp(md.be1),
                   c->red, c->red_bytes, st));
         void* dO = c->tA;    // dR2 no longer needed
         Gemm go = mk((int)rows, d, d, 1, operand(dR1, dt, d, 1), operand(p(md.Wo), dt, 1, d), view(dO, dt, d, 1));
-        RET(G_(go, c, st));
+        RET(G_(go, c, st, "attn.out_dgrad"));
         Gemm wo = mk(d, d, (int)rows, 1, operand(dR1, dt, 1, d), operand(md.O, dt, 1, d), view(gp(md.Wo), F32, d, 1));
         wo.e.accumulate = 1;
-        RET(G_(wo, c, st));
-        CK(colsum_add(dR1, dt, rows, d, d, gp(md.bo), c->red, c->red_bytes, st));
+        RET(G_(wo, c, st, "attn.out_wgrad"));
+        KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dR1, dt, rows, d, d, gp(md.bo), c->red, c->red_bytes, st));
         // attention core backward
         char* dQKV = (char*)c->tC;   // [rows, 3d]  (dF no longer needed; tC >= rows*f >= rows*3d? checked at plan)
         Gemm dv = mk(mi, dh, mi, B * H, operand(md.P, dt, 1, mi, (int64_t)mi * mi),
                      operand(dO, dt, 1, d, (int64_t)mi * d, dh, H),
                      view(dQKV + 2 * (int64_t)d * es, dt, s3, 1, mi * s3, dh, H));
-        RET(G_(dv, c, st));
+        RET(G_(dv, c, st, "attn.dv"));
         Gemm dp = mk(mi, mi, dh, B * H, operand(dO, dt, d, 1, (int64_t)mi * d, dh, H),
                      operand(QKV + 2 * (int64_t)d * es, dt, s3, 1, mi * s3, dh, H),
                      view(c->big, F32, mi, 1, (int64_t)mi * mi));
-        RET(G_(dp, c, st));
-        CK(softmax_bwd(md.P, c->big, c->tD, dt, (int64_t)B * H * mi, mi, 1.f / sqrtf((float)dh), st));
+        RET(G_(dp, c, st, "attn.dp"));
+        KT("attn.softmax_bwd", 0, (double)B * H * mi * mi * (4 + 2 * es), softmax_bwd(md.P, c->big, c->tD, dt, (int64_t)B * H * mi, mi, 1.f / sqrtf((float)dh), st));
         Gemm dq = mk(mi, dh, mi, B * H, operand(c->tD, dt, mi, 1, (int64_t)mi * mi),
                      operand(QKV + (int64_t)d * es, dt, 1, s3, mi * s3, dh, H),
                      view(dQKV, dt, s3, 1, mi * s3, dh, H));
-        RET(G_(dq, c, st));
+        RET(G_(dq, c, st, "attn.dq"));
         Gemm dk = mk(mi, dh, mi, B * H, operand(c->tD, dt, 1, mi, (int64_t)mi * mi),
                      operand(QKV, dt, 1, s3, mi * s3, dh, H),
                      view(dQKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H));
-        RET(G_(dk, c, st));
+        RET(G_(dk, c, st, "attn.dk"));
         Gemm gx = mk((int)rows, d, 3 * d, 1, operand(dQKV, dt, s3, 1), operand(p(md.Wq), dt, 1, d), view(acc, F32, d, 1));
         gx.e.accumulate = 1;
-        RET(G_(gx, c, st));
+        RET(G_(gx, c, st, "attn.qkv_dgrad"));
         Gemm gw = mk(3 * d, d, (int)rows, 1, operand(dQKV, dt, 1, s3), operand(X, dt, 1, d), view(gp(md.Wq), F32, d, 1));
         gw.e.accumulate = 1;
-        RET(G_(gw, c, st));
-        CK(colsum_add(dQKV, dt, rows, d, s3, gp(md.bq), c->red, c->red_bytes, st));
-        CK(colsum_add(dQKV + 2 * (int64_t)d * es, dt, rows, d, s3, gp(md.bq) + d, c->red, c->red_bytes, st));
+        RET(G_(gw, c, st, "attn.qkv_wgrad"));
+        KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dQKV, dt, rows, d, s3, gp(md.bq), c->red, c->red_bytes, st));
+        KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dQKV + 2 * (int64_t)d * es, dt, rows, d, s3, gp(md.bq) + d, c->red, c->red_bytes, st));
         break;
       }
       case DHEN_MLP: {   // B9
@@ -625,31 +669,31 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         const int K1 = mi * d;
         Gemm wm = mk(l * d, h2, B, 1, operand(dU, dt, 1, ldU), operand(md.h2, dt, 1, h2), view(gp(md.Wm), F32, h2, 1));
         wm.e.accumulate = 1;
-        RET(G_(wm, c, st));
+        RET(G_(wm, c, st, "mlp.proj_wgrad"));
         void* dh2 = c->tA;
         Gemm a = mk(B, h2, l * d, 1, operand(dU, dt, ldU, 1), operand(p(md.Wm), dt, 1, h2), view(dh2, dt, h2, 1));
         a.e.mask = view(md.h2, dt, h2, 1);
-        RET(G_(a, c, st));
+        RET(G_(a, c, st, "mlp.proj_dgrad"));
         Gemm w2 = mk(h2, h1, B, 1, operand(dh2, dt, 1, h2), operand(md.h1, dt, 1, h1), view(gp(md.W2), F32, h1, 1));
         w2.e.accumulate = 1;
-        RET(G_(w2, c, st));
-        CK(colsum_add(dh2, dt, B, h2, h2, gp(md.b2), c->red, c->red_bytes, st));
+        RET(G_(w2, c, st, "mlp.fc2_wgrad"));
+        KT("mlp.bias_grad", 0, (double)B * h2 * es, colsum_add(dh2, dt, B, h2, h2, gp(md.b2), c->red, c->red_bytes, st));
         void* dh1 = c->tC;
         Gemm b1 = mk(B, h1, h2, 1, operand(dh2, dt, h2, 1), operand(p(md.W2), dt, 1, h1), view(dh1, dt, h1, 1));
         b1.e.mask = view(md.h1, dt, h1, 1);
-        RET(G_(b1, c, st));
+        RET(G_(b1, c, st, "mlp.fc2_dgrad"));
         Gemm w1 = mk(h1, K1, B, 1, operand(dh1, dt, 1, h1), operand(X, dt, 1, K1), view(gp(md.W1), F32, K1, 1));
         w1.e.accumulate = 1;
-        RET(G_(w1, c, st));
-        CK(colsum_add(dh1, dt, B, h1, h1, gp(md.b1), c->red, c->red_bytes, st));
+        RET(G_(w1, c, st, "mlp.fc1_wgrad"));
+        KT("mlp.bias_grad", 0, (double)B * h1 * es, colsum_add(dh1, dt, B, h1, h1, gp(md.b1), c->red, c->red_bytes, st));
         Gemm gx = mk(B, K1, h1, 1, operand(dh1, dt, h1, 1), operand(p(md.W1), dt, 1, K1), view(acc, F32, K1, 1));
         gx.e.accumulate = 1;
-        RET(G_(gx, c, st));
+        RET(G_(gx, c, st, "mlp.fc1_dgrad"));
         break;
       }
     }
   }
-  if (dX) CK(cast(acc, F32, dX, dt, rows * d, st));
+  if (dX) KT("layer.dx_cast", 0, (double)rows * d * (4 + es), cast(acc, F32, dX, dt, rows * d, st));
   RET(reduce_grads(c, n, st));
   return DHEN_OK;
 }
@@ -662,7 +706,7 @@ static dhen_status head(dhen_ctx* c, const void* YN, int mN, const float* labels
   RET(comp_params(c, gi, st, &pbase));
   PP p{(char*)pbase, c->es};
   Group& G = c->G[gi];
-  CK(head_fwd_bwd(YN, p(0), p(c->d), c->dt, labels, B, mN, c->d, Bg, dY, c->dt, c->pooled, c->z, c->lossb, c->dz, loss,
+  KT("head", 0, (double)B * mN * c->d * c->es * (do_bwd ? 2 : 1), head_fwd_bwd(YN, p(0), p(c->d), c->dt, labels, B, mN, c->d, Bg, dY, c->dt, c->pooled, c->z, c->lossb, c->dz, loss,
                   G.grad, G.grad + c->d, do_bwd, st));
   if (do_bwd) RET(reduce_grads(c, gi, st));
   return DHEN_OK;
@@ -790,11 +834,68 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
 
 void dhen_destroy(dhen_ctx* c) {
   if (!c) return;
+  for (auto e : c->events) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
 }
 
 unsigned long long dhen_launch_count(const dhen_ctx* c) { return c ? g_launches - c->launches0 : 0; }
+
+dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* Bp, void* Cp, int ab_dt, int c_dt, int path,
+                            void* ws, size_t ws_bytes, void* stream) {
+  if (!q || !A || !Bp || !Cp) return fail(DHEN_E_ALIGN, "dhen_debug_gemm: NULL argument");
+  const int abt = ab_dt == DHEN_BF16 ? BF16 : F32, ct = c_dt == DHEN_BF16 ? BF16 : F32;
+  Gemm g = mk((int)q[0], (int)q[1], (int)q[2], (int)q[3],
+              operand(A, abt, q[4], q[5], q[6], q[7], (int)q[8], (int)q[9], q[10]),
+              operand(Bp, abt, q[11], q[12], q[13], q[14], (int)q[15], (int)q[16], q[17]),
+              view(Cp, ct, q[18], q[19], q[20], q[21], (int)q[22]));
+  g.e.accumulate = (int)q[23];
+  Workspace w;
+  w.ptr = (float*)ws;
+  w.bytes = ws_bytes;
+  dhen::g_gemm_force = path;
+  cudaError_t e = gemm_run(g, w, S(stream));
+  const int used_tc = g_last_gemm_tc;
+  dhen::g_gemm_force = -1;
+  if (e == cudaErrorNotSupported) return fail(DHEN_E_CONFIG, "dhen_debug_gemm: layout not supported on this path");
+  CK(e);
+  return used_tc ? DHEN_OK : DHEN_OK;
+}
+
+int dhen_debug_last_gemm_tc(void) { return g_last_gemm_tc; }
+
+dhen_status dhen_profile(dhen_ctx* c, int enable) {
+  if (!c) return fail(DHEN_E_STATE, "dhen_profile: ctx is NULL");
+  c->prof = enable != 0;
+  if (enable) { c->recs.clear(); c->next_event = 0; }
+  return DHEN_OK;
+}
+
+dhen_status dhen_profile_read(dhen_ctx* c, dhen_op_stat* out, int cap, int* n) {
+  if (!c || !n) return fail(DHEN_E_STATE, "dhen_profile_read: ctx or n is NULL");
+  std::vector<dhen_op_stat> agg;
+  for (auto& r : c->recs) {
+    CK(cudaEventSynchronize(c->events[r.e1]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->events[r.e0], c->events[r.e1]));
+    size_t k = 0;
+    for (; k < agg.size(); ++k) if (!strncmp(agg[k].name, r.tag, sizeof agg[k].name)) break;
+    if (k == agg.size()) {
+      dhen_op_stat z;
+      memset(&z, 0, sizeof z);
+      strncpy(z.name, r.tag, sizeof z.name - 1);
+      agg.push_back(z);
+    }
+    agg[k].launches += 1;
+    agg[k].ms += ms;
+    agg[k].flops += r.flops;
+    agg[k].bytes += r.bytes;
+    agg[k].tc_launches += r.tc ? 1 : 0;
+  }
+  *n = (int)agg.size();
+  for (int k = 0; k < (int)agg.size() && k < cap; ++k) out[k] = agg[k];
+  return DHEN_OK;
+}
 
 dhen_status dhen_zero_grad(dhen_ctx* c, void* stream) {
   if (!c) return fail(DHEN_E_STATE, "dhen_zero_grad: ctx is NULL");
@@ -870,7 +971,7 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
   // B12: SGD on the (local shard of the) fp32 masters, refresh the compute copy
   for (auto& g : c->G) {
     const float* gr = c->dist.world > 1 ? g.gshard : g.grad;
-    CK(sgd_cast(g.master, gr, lr, g.comp, c->dt, g.shard, st));
+    KT("sgd", 0, (double)g.shard * (12 + c->es), sgd_cast(g.master, gr, lr, g.comp, c->dt, g.shard, st));
   }
   invalidate_gathered(c);
   CK(cudaGetLastError());

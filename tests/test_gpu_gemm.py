@@ -1,0 +1,116 @@
+"""The GEMM kernels (tcgen05/TMA path and the exact SIMT path) through the C ABI
+test hook dhen_debug_gemm, against a plain fp64 matmul of the same bf16 / fp32
+values.  Covers every operand layout the DHEN path uses: K-major / MN-major A and
+B, two-level batch (attention heads), two-level K (token-mixing wgrad), split-K,
+accumulate, ragged tails."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _offsets(z, r, K, s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko):
+    zz = torch.arange(z).view(z, 1, 1)
+    rr = torch.arange(r).view(1, r, 1)
+    kk = torch.arange(K).view(1, 1, K)
+    if kdiv:
+        ki, ko = kk % kdiv, kk // kdiv
+    else:
+        ki, ko = kk, torch.zeros_like(kk)
+    return (zz // zdiv) * bs0 + (zz % zdiv) * bs1 + rr * s_mn + ki * s_k + ko * s_ko
+
+
+def _run(M, N, K, batch, a, b, c, acc=0, path=2, dt=torch.bfloat16, expect_tc=True):
+    from paper_2203_11014_b200.binding import debug_gemm
+    g = torch.Generator().manual_seed(M * 7 + N * 3 + K)
+    offA = _offsets(batch, M, K, *a)
+    offB = _offsets(batch, N, K, *b)
+    A = torch.randn(int(offA.max()) + 1, generator=g).to(dt)
+    B = torch.randn(int(offB.max()) + 1, generator=g).to(dt)
+    rs, cs, cb0, cb1, czdiv = c
+    zz = torch.arange(batch).view(batch, 1, 1)
+    offC = (zz // czdiv) * cb0 + (zz % czdiv) * cb1 + torch.arange(M).view(1, M, 1) * rs + \
+        torch.arange(N).view(1, 1, N) * cs
+    Cm = torch.randn(int(offC.max()) + 1, generator=g)
+    C0 = Cm.clone()
+    Ad = A.double()[offA]                 # [z, M, K]
+    Bd = B.double()[offB]                 # [z, N, K]
+    ref = torch.einsum("zik,zjk->zij", Ad, Bd)
+    if acc:
+        ref = ref + C0.double()[offC]
+    q = [M, N, K, batch] + list(a) + list(b) + list(c) + [acc]
+    Cg = Cm.cuda()
+    used_tc = debug_gemm(q, A.cuda(), B.cuda(), Cg, path=path)
+    torch.cuda.synchronize()
+    out = Cg.cpu().double()[offC]
+    err = (out - ref).abs().max().item() / max(1.0, ref.abs().max().item())
+    assert used_tc == expect_tc
+    # untouched elements outside the view stay as they were
+    mask = torch.ones_like(Cm, dtype=torch.bool)
+    mask[offC.reshape(-1)] = False
+    assert torch.equal(Cg.cpu()[mask], C0[mask])
+    return err
+
+
+# (s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko)
+def KM(ld, bs0=0, bs1=0, zdiv=1):
+    return (ld, 1, bs0, bs1, zdiv, 0, 0)
+
+
+def MNM(ld, bs0=0, bs1=0, zdiv=1):
+    return (1, ld, bs0, bs1, zdiv, 0, 0)
+
+
+@pytest.mark.parametrize("path", [2, 1])
+@pytest.mark.parametrize("M,N,K", [(300, 200, 160), (128, 128, 64), (2048, 4096, 2016), (77, 48, 40)])
+def test_nt_kmajor(path, M, N, K):
+    err = _run(M, N, K, 1, KM(K), KM(K), (N, 1, 0, 0, 1), path=path, expect_tc=(path == 2))
+    assert err < 2e-5, err
+
+
+@pytest.mark.parametrize("amn,bmn", [(1, 0), (0, 1), (1, 1)])
+def test_mn_major_operands(amn, bmn):
+    M, N, K = 320, 192, 1000
+    a = MNM(M) if amn else KM(K)
+    b = MNM(N) if bmn else KM(K)
+    err = _run(M, N, K, 1, a, b, (N, 1, 0, 0, 1))
+    assert err < 2e-5, err
+
+
+def test_batched_heads_like_attention():
+    # Q K^T per (b, h): Q/K live in a [B, m, 3d] QKV buffer; head h at column h*dh
+    Bn, m, d, H = 5, 100, 128, 2
+    dh = d // H
+    s3 = 3 * d
+    a = (s3, 1, m * s3, dh, H, 0, 0)
+    b = (s3, 1, m * s3, dh, H, 0, 0)
+    err = _run(m, m, dh, Bn * H, a, b, (m, 1, m * m, 0, 1))
+    assert err < 2e-5, err
+    # P V: A = P [z, m, m] K-major, B(k, j) = V[b, k, h*dh + j] MN-major; C into [B, m, d] at head offset
+    for mm, tc in ((128, True), (100, False)):   # m = 100: P rows are 200 B, not TMA-expressible -> SIMT
+        a = (mm, 1, mm * mm, 0, 1, 0, 0)
+        b = (1, s3, mm * s3, dh, H, 0, 0)
+        err = _run(mm, dh, mm, Bn * H, a, b, (d, 1, mm * d, dh, H), path=0, expect_tc=tc)
+        assert err < 2e-5, err
+
+
+def test_two_level_k_token_mix_wgrad():
+    # dW[i][t] = sum_b sum_c T[b,i,c] dU[b,t,c]   (K = B * d, kdiv = d)
+    Bn, m, l, d = 40, 64, 32, 128
+    a = (d, 1, 0, 0, 1, d, m * d)
+    b = (d, 1, 0, 0, 1, d, 96 * d)        # dU rows inside a [B, 96, d] concat buffer
+    err = _run(m, l, Bn * d, 1, a, b, (l, 1, 0, 0, 1), acc=1)
+    assert err < 2e-5, err
+
+
+def test_split_k_wgrad():
+    # dW = dA^T X with K = B*m rows (both operands MN-major), few output tiles -> split-K
+    M, N, K = 128, 128, 65536
+    err = _run(M, N, K, 1, MNM(M), MNM(N), (N, 1, 0, 0, 1), acc=1)
+    assert err < 2e-5, err
+
+
+def test_fp32_simt_exact():
+    M, N, K = 70, 90, 130
+    err = _run(M, N, K, 1, KM(K), MNM(N), (N, 1, 0, 0, 1), path=0, dt=torch.float32, expect_tc=False)
+    assert err < 1e-6, err
