@@ -175,9 +175,10 @@ dhen_status dhen_profile_read(dhen_ctx* ctx, dhen_op_stat* out, int cap, int* n)
 
 /* Test hook (tests/test_gpu_gemm.py): one strided / batched contraction
  *   C[z][i][j] (+)= sum_k A[z][i][k] B[z][k][j]
- * through the library's GEMM dispatcher.  q = int64[24]: M, N, K, batch,
+ * through the library's GEMM dispatcher.  q = int64[30]: M, N, K, batch,
  * A{s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko}, B{s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko},
- * C{rs, cs, bs0, bs1, zdiv}, accumulate.  ab_dtype/c_dtype: dhen_dtype.
+ * C{rs, cs, bs0, bs1, zdiv}, accumulate, A{mdiv, s_mo}, B{mdiv, s_mo}, C{rdiv, rs_o}
+ * (two-level row index r -> (r / div) * s_o + (r % div) * s; div 0 = single level).  ab_dtype/c_dtype: dhen_dtype.
  * path: 0 auto, 1 SIMT only, 2 tcgen05 only (DHEN_E_CONFIG if not expressible).
  * ws: fp32 device scratch for split-K partials. */
 dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* B, void* C, int ab_dtype, int c_dtype,

@@ -197,7 +197,8 @@ def debug_gemm(q, A, B, Cm, path=0, ws=None, stream=None):
     """Test hook: one contraction through the library's GEMM dispatcher (see dhen.h).
     Returns True if it ran on the tcgen05 path."""
     import torch
-    arr = (C.c_longlong * 24)(*[int(v) for v in q])
+    q = list(q) + [0] * (30 - len(q))
+    arr = (C.c_longlong * 30)(*[int(v) for v in q])
     abt = BF16 if A.dtype == torch.bfloat16 else FP32
     ct = BF16 if Cm.dtype == torch.bfloat16 else FP32
     if ws is None:

@@ -36,20 +36,33 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 // A strided (optionally doubly-batched) matrix view: element (z, r, c) lives at
-// ptr + (z / zdiv) * bs0 + (z % zdiv) * bs1 + r * rs + c * cs   (elements).
+// ptr + (z / zdiv) * bs0 + (z % zdiv) * bs1 + R(r) + c * cs   (elements),
+// R(r) = r * rs, or with a two-level row index (rdiv > 0): (r / rdiv) * rs_o + (r % rdiv) * rs.
 struct View {
   void* ptr;
   int64_t rs, cs, bs0, bs1;
   int zdiv;
   int dt;
+  int rdiv;
+  int64_t rs_o;
   __host__ __device__ int64_t off(int64_t z, int64_t r, int64_t c) const {
-    return (z / zdiv) * bs0 + (z % zdiv) * bs1 + r * rs + c * cs;
+    int64_t o = c * cs;
+    if (zdiv == 1) o += z * bs0; else o += (z / zdiv) * bs0 + (z % zdiv) * bs1;
+    if (rdiv) o += (r / rdiv) * rs_o + (r % rdiv) * rs; else o += r * rs;
+    return o;
   }
 };
 
 inline View view(void* p, int dt, int64_t rs, int64_t cs, int64_t bs0 = 0, int64_t bs1 = 0, int zdiv = 1) {
   View v;
   v.ptr = p; v.rs = rs; v.cs = cs; v.bs0 = bs0; v.bs1 = bs1; v.zdiv = zdiv; v.dt = dt;
+  v.rdiv = 0; v.rs_o = 0;
+  return v;
+}
+// two-level rows: r -> (r / rdiv) * rs_o + (r % rdiv) * rs
+inline View view2(void* p, int dt, int rdiv, int64_t rs_o, int64_t rs, int64_t cs) {
+  View v = view(p, dt, rs, cs);
+  v.rdiv = rdiv; v.rs_o = rs_o;
   return v;
 }
 inline View noview() { return view(nullptr, F32, 0, 0); }

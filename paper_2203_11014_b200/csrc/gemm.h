@@ -18,15 +18,20 @@ namespace dhen {
 struct Operand {            // A: (z, i, k) ; B: (z, k, j)
   const void* ptr;
   int dt;
-  int64_t s_mn;             // stride of i (A) / j (B)
+  int64_t s_mn;             // stride of i (A) / j (B)  (inner index when mdiv > 0)
   int64_t s_k;              // stride of the inner k index
   int64_t s_ko;             // stride of the outer k index (k / kdiv); kdiv == 0: single-level
   int kdiv;
   int64_t bs0, bs1;         // batch strides (z / zdiv, z % zdiv)
   int zdiv;
+  int mdiv;                 // two-level i / j: (i / mdiv) * s_mo + (i % mdiv) * s_mn; 0: single-level
+  int64_t s_mo;
   __host__ __device__ int64_t off(int64_t z, int64_t mn, int64_t k) const {
     int64_t ko = kdiv ? (k / kdiv) : 0, ki = kdiv ? (k % kdiv) : k;
-    return (z / zdiv) * bs0 + (z % zdiv) * bs1 + mn * s_mn + ki * s_k + ko * s_ko;
+    int64_t o = ki * s_k + ko * s_ko;
+    if (zdiv == 1) o += z * bs0; else o += (z / zdiv) * bs0 + (z % zdiv) * bs1;
+    if (mdiv) o += (mn / mdiv) * s_mo + (mn % mdiv) * s_mn; else o += mn * s_mn;
+    return o;
   }
 };
 
@@ -35,6 +40,13 @@ inline Operand operand(const void* p, int dt, int64_t s_mn, int64_t s_k, int64_t
   Operand o;
   o.ptr = p; o.dt = dt; o.s_mn = s_mn; o.s_k = s_k; o.s_ko = s_ko; o.kdiv = kdiv;
   o.bs0 = bs0; o.bs1 = bs1; o.zdiv = zdiv;
+  o.mdiv = 0; o.s_mo = 0;
+  return o;
+}
+// operand with a two-level row index (i -> (i / mdiv, i % mdiv))
+inline Operand operand2(const void* p, int dt, int mdiv, int64_t s_mo, int64_t s_mn, int64_t s_k) {
+  Operand o = operand(p, dt, s_mn, s_k);
+  o.mdiv = mdiv; o.s_mo = s_mo;
   return o;
 }
 

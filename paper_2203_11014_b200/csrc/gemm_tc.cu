@@ -28,6 +28,8 @@ struct OpMap {
   int mn_major;   // 1: MN contiguous (boxes of 64 MN x 64 K), 0: K contiguous (box 64 K x tile rows)
   int has_ko;     // coordinate slot 2 holds k / kdiv
   int kdiv;
+  int mo;         // coordinate slot of row / mdiv (-1: single-level rows)
+  int mdiv;
   int z1, z0;     // coordinate slots of z % zdiv and z / zdiv (-1: operand not batched there)
   int zdiv;
 };
@@ -38,6 +40,7 @@ struct Params {
   int tiles_m, tiles_n;
   int kblocks, splits, kb_per_split;
   int zbase;
+  int lanes_rows;   // epilogue: consecutive lanes on consecutive rows (output column-contiguous)
   float* ws;
   uint32_t idesc;
 };
@@ -92,6 +95,7 @@ __device__ __forceinline__ void load_operand(const CUtensorMap* map, const OpMap
   int c[5] = {0, 0, 0, 0, 0};
   const int kin = om.has_ko ? k % om.kdiv : k;
   if (om.has_ko) c[2] = k / om.kdiv;
+  if (om.mo >= 0) { c[om.mo] = mn0 / om.mdiv; mn0 = mn0 % om.mdiv; }
   if (om.z1 >= 0) c[om.z1] = z % om.zdiv;
   if (om.z0 >= 0) c[om.z0] = z / om.zdiv;
   if (!om.mn_major) {
@@ -179,11 +183,15 @@ __global__ void __launch_bounds__(128, 1)
   }
   __syncwarp();
 
-  // ---------------- epilogue: TMEM -> registers -> fused epilogue -> global
+  // ---------------- epilogue: TMEM -> registers -> smem (the idle ring) -> fused epilogue -> global.
+  // Each warp owns TMEM lanes / tile rows [32w, 32w+32).  Pass 1 parks its rows in shared memory
+  // (row stride BN+1: conflict-free both ways); pass 2 walks them with consecutive lanes on
+  // consecutive memory (columns, or rows when the output is column-contiguous) so every global
+  // access of the epilogue is coalesced.
   if (nk > 0) mbar_wait(smem_u32(bars + 2 * STAGES), 0);
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const int row = m0 + warp * 32 + lane;
-  const Gemm& g = p.g;
+  constexpr int SROW = BN + 1;
+  float* stage = reinterpret_cast<float*>(smem) + warp * 32 * SROW;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 16) {
     uint32_t v[16];
@@ -194,15 +202,35 @@ __global__ void __launch_bounds__(128, 1)
           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < g.M && n0 + c0 < g.N) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = n0 + c0 + j;
-        const float acc = nk > 0 ? __uint_as_float(v[j]) : 0.f;
+    for (int j = 0; j < 16; ++j) stage[lane * SROW + c0 + j] = nk > 0 ? __uint_as_float(v[j]) : 0.f;
+  }
+  __syncwarp();
+  const Gemm& g = p.g;
+  const int rbase = m0 + warp * 32;
+  if (!p.lanes_rows) {
+#pragma unroll 1
+    for (int r = 0; r < 32; ++r) {
+      const int row = rbase + r;
+      if (row >= g.M) break;
+#pragma unroll
+      for (int q = 0; q < BN / 32; ++q) {
+        const int col = n0 + lane + 32 * q;
         if (col < g.N) {
+          const float acc = stage[r * SROW + lane + 32 * q];
           if (p.splits == 1) epi_apply(g, z, row, col, acc);
           else p.ws[((int64_t)(z * p.splits + sp) * g.M + row) * g.N + col] = acc;
         }
+      }
+    }
+  } else {
+    const int row = rbase + lane;
+    if (row < g.M) {
+#pragma unroll 4
+      for (int cc = 0; cc < BN; ++cc) {
+        const int col = n0 + cc;
+        if (col >= g.N) break;
+        epi_apply(g, z, row, col, stage[lane * SROW + cc]);
       }
     }
   }
@@ -241,25 +269,33 @@ static bool make_map(CUtensorMap* map, OpMap* om, const Operand& o, int rows, in
   om->has_ko = o.kdiv ? 1 : 0;
   om->kdiv = o.kdiv ? o.kdiv : 1;
   om->zdiv = o.zdiv;
-  om->z0 = om->z1 = -1;
+  om->z0 = om->z1 = om->mo = -1;
+  om->mdiv = o.mdiv ? o.mdiv : 1;
   if (o.kdiv && (o.kdiv % BK != 0 || K % o.kdiv != 0)) return false;
+  if (o.mdiv && (o.mdiv % tile_rows != 0 || rows % o.mdiv != 0)) return false;
   cuuint64_t dims[5] = {1, 1, 1, 1, 1}, strides[4] = {0, 0, 0, 0};
   cuuint32_t box[5] = {1, 1, 1, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
   const int kin = o.kdiv ? o.kdiv : K;
   int64_t s1;
+  const int rin = o.mdiv ? o.mdiv : rows;
   if (!om->mn_major) {
-    dims[0] = kin; dims[1] = rows; s1 = o.s_mn;
+    dims[0] = kin; dims[1] = rin; s1 = o.s_mn;
     box[0] = BK; box[1] = tile_rows;
   } else {
-    dims[0] = rows; dims[1] = kin; s1 = o.s_k;
+    dims[0] = rin; dims[1] = kin; s1 = o.s_k;
     box[0] = 64; box[1] = BK;
   }
   strides[0] = s1 * es;
   int r = 2;
   if (o.kdiv) { dims[r] = K / o.kdiv; strides[r - 1] = o.s_ko * es; ++r; }
+  if (o.mdiv) { dims[r] = rows / o.mdiv; strides[r - 1] = o.s_mo * es; om->mo = r; ++r; }
   if (o.zdiv > 1 && o.bs1 != 0) { dims[r] = o.zdiv; strides[r - 1] = o.bs1 * es; om->z1 = r; ++r; }
   const int nb0 = (batch + o.zdiv - 1) / o.zdiv;
-  if (nb0 > 1 && o.bs0 != 0) { dims[r] = nb0; strides[r - 1] = o.bs0 * es; om->z0 = r; ++r; }
+  if (nb0 > 1 && o.bs0 != 0) {
+    if (r >= 5) return false;
+    dims[r] = nb0; strides[r - 1] = o.bs0 * es; om->z0 = r; ++r;
+  }
+  if (r > 5) return false;
   for (int i = 0; i < 4; ++i) {
     if (i + 1 >= r) strides[i] = (i == 0 ? 16 : strides[i - 1]) ;
     if (strides[i] % 16 != 0 || strides[i] == 0 || strides[i] >= (1ull << 40)) return false;
@@ -317,6 +353,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   p.splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;   // no empty splits
   p.ws = ws.ptr;
   p.zbase = 0;
+  p.lanes_rows = (g.c.cs != 1 && g.c.rs == 1 && splits == 1) ? 1 : 0;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a.mn_major << 15) | ((uint32_t)p.b.mn_major << 16) |
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   cudaError_t e = BN == 64 ? launch<64, 4>(p, ma, mb, st) : launch<128, 3>(p, ma, mb, st);

@@ -395,20 +395,24 @@ struct PP {
   void* operator()(int64_t off) const { return base + off * es; }
 };
 
-// Token projection (F10): U_b = W^T T_b -> fp32 view dst (rows stride d, batch stride ldb), accumulate?
+// Token projection (F10): U_b = W^T T_b, as ONE GEMM over rows r = (b, c) (M = B*d, two-level row
+// index), N = l, K = m:  U[b,t,c] = sum_i T[b,i,c] W[i,t].  T_b is read MN-major (c contiguous) and
+// the output is column-contiguous (lanes along rows in the epilogue).
 static dhen_status tokmix_fwd(dhen_ctx* c, const void* T, int m, const void* W, int l, float* dst, int64_t ldb, int B,
                               int acc, cudaStream_t st) {
   const int d = c->d, dt = c->dt;
-  Gemm g = mk(l, d, m, B, operand(W, dt, 1, l), operand(T, dt, 1, d, (int64_t)m * d),
-              view(dst, F32, d, 1, ldb));
+  Gemm g = mk(B * d, l, m, 1, operand2(T, dt, d, (int64_t)m * d, 1, d), operand(W, dt, 1, l),
+              view2(dst, F32, d, ldb, 1, d));
   g.e.accumulate = acc;
   return G_(g, c, st, "tokmix.fwd");
 }
-// B4: dT = W dU (set, dtype dT_dt) or dX += W dU (fp32 accumulate); dW += sum_b T_b dU_b^T
+// B4: dT[b,i,c] = sum_t W[i,t] dU[b,t,c] (rows (b,c), N = m, K = l) stored (dT_dt) or accumulated
+// into fp32; dW[i,t] += sum_(b,c) T[b,i,c] dU[b,t,c] (K = B*d, two-level K).
 static dhen_status tokmix_bwd(dhen_ctx* c, const void* T, int m, const void* W, int l, const void* dU, int64_t ldu,
                               void* dT, int dT_dt, int acc, float* gW, int B, cudaStream_t st) {
   const int d = c->d, dt = c->dt;
-  Gemm g = mk(m, d, l, B, operand(W, dt, l, 1), operand(dU, dt, 1, d, ldu), view(dT, dT_dt, d, 1, (int64_t)m * d));
+  Gemm g = mk(B * d, m, l, 1, operand2(dU, dt, d, ldu, 1, d), operand(W, dt, l, 1),
+              view2(dT, dT_dt, d, (int64_t)m * d, 1, d));
   g.e.accumulate = acc;
   RET(G_(g, c, st, "tokmix.dgrad"));
   Gemm gw = mk(m, l, B * d, 1, operand(T, dt, d, 1, 0, 0, 1, d, (int64_t)m * d),
@@ -850,6 +854,9 @@ dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* Bp, v
               operand(Bp, abt, q[11], q[12], q[13], q[14], (int)q[15], (int)q[16], q[17]),
               view(Cp, ct, q[18], q[19], q[20], q[21], (int)q[22]));
   g.e.accumulate = (int)q[23];
+  g.a.mdiv = (int)q[24]; g.a.s_mo = q[25];
+  g.b.mdiv = (int)q[26]; g.b.s_mo = q[27];
+  g.c.rdiv = (int)q[28]; g.c.rs_o = q[29];
   Workspace w;
   w.ptr = (float*)ws;
   w.bytes = ws_bytes;

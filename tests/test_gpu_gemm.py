@@ -9,7 +9,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _offsets(z, r, K, s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko):
+def _offsets(z, r, K, s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko, mdiv=0, s_mo=0):
     zz = torch.arange(z).view(z, 1, 1)
     rr = torch.arange(r).view(1, r, 1)
     kk = torch.arange(K).view(1, 1, K)
@@ -17,20 +17,23 @@ def _offsets(z, r, K, s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko):
         ki, ko = kk % kdiv, kk // kdiv
     else:
         ki, ko = kk, torch.zeros_like(kk)
-    return (zz // zdiv) * bs0 + (zz % zdiv) * bs1 + rr * s_mn + ki * s_k + ko * s_ko
+    rows = (rr // mdiv) * s_mo + (rr % mdiv) * s_mn if mdiv else rr * s_mn
+    return (zz // zdiv) * bs0 + (zz % zdiv) * bs1 + rows + ki * s_k + ko * s_ko
 
 
-def _run(M, N, K, batch, a, b, c, acc=0, path=2, dt=torch.bfloat16, expect_tc=True):
+def _run(M, N, K, batch, a, b, c, acc=0, path=2, dt=torch.bfloat16, expect_tc=True, a2=(0, 0), b2=(0, 0),
+         c2=(0, 0)):
     from paper_2203_11014_b200.binding import debug_gemm
     g = torch.Generator().manual_seed(M * 7 + N * 3 + K)
-    offA = _offsets(batch, M, K, *a)
-    offB = _offsets(batch, N, K, *b)
+    offA = _offsets(batch, M, K, *a, *a2)
+    offB = _offsets(batch, N, K, *b, *b2)
     A = torch.randn(int(offA.max()) + 1, generator=g).to(dt)
     B = torch.randn(int(offB.max()) + 1, generator=g).to(dt)
     rs, cs, cb0, cb1, czdiv = c
     zz = torch.arange(batch).view(batch, 1, 1)
-    offC = (zz // czdiv) * cb0 + (zz % czdiv) * cb1 + torch.arange(M).view(1, M, 1) * rs + \
-        torch.arange(N).view(1, 1, N) * cs
+    rr = torch.arange(M).view(1, M, 1)
+    crow = (rr // c2[0]) * c2[1] + (rr % c2[0]) * rs if c2[0] else rr * rs
+    offC = (zz // czdiv) * cb0 + (zz % czdiv) * cb1 + crow + torch.arange(N).view(1, 1, N) * cs
     Cm = torch.randn(int(offC.max()) + 1, generator=g)
     C0 = Cm.clone()
     Ad = A.double()[offA]                 # [z, M, K]
@@ -38,7 +41,7 @@ def _run(M, N, K, batch, a, b, c, acc=0, path=2, dt=torch.bfloat16, expect_tc=Tr
     ref = torch.einsum("zik,zjk->zij", Ad, Bd)
     if acc:
         ref = ref + C0.double()[offC]
-    q = [M, N, K, batch] + list(a) + list(b) + list(c) + [acc]
+    q = [M, N, K, batch] + list(a) + list(b) + list(c) + [acc] + list(a2) + list(b2) + list(c2)
     Cg = Cm.cuda()
     used_tc = debug_gemm(q, A.cuda(), B.cuda(), Cg, path=path)
     torch.cuda.synchronize()
@@ -114,3 +117,18 @@ def test_fp32_simt_exact():
     M, N, K = 70, 90, 130
     err = _run(M, N, K, 1, KM(K), MNM(N), (N, 1, 0, 0, 1), path=0, dt=torch.float32, expect_tc=False)
     assert err < 1e-6, err
+
+
+@pytest.mark.parametrize("path", [2, 1])
+def test_two_level_rows_token_mix(path):
+    """Token projection as one GEMM over rows (b, c): U[b,t,c] = sum_i T[b,i,c] W[i,t]
+    (A MN-major with two-level rows, column-contiguous output), and its dgrad."""
+    Bn, m, l, d, mo = 37, 64, 32, 128, 96
+    # fwd: A(r=(b,c), i) = T[b,i,c]; B(i, t) = W[i][t]; C(r, t) = U[b, off + t, c]
+    err = _run(Bn * d, l, m, 1, (1, d, 0, 0, 1, 0, 0), (1, l, 0, 0, 1, 0, 0), (1, d, 0, 0, 1),
+               a2=(d, m * d), c2=(d, mo * d), path=path, expect_tc=(path == 2))
+    assert err < 2e-5, err
+    # dgrad: A(r=(b,c), t) = dU[b,t,c]; B(t, i) = W[i][t] (K-major); C(r, i) = dT[b,i,c]
+    err = _run(Bn * d, m, l, 1, (1, d, 0, 0, 1, 0, 0), (l, 1, 0, 0, 1, 0, 0), (1, d, 0, 0, 1),
+               a2=(d, mo * d), c2=(d, m * d), acc=1, path=path, expect_tc=(path == 2))
+    assert err < 2e-5, err
