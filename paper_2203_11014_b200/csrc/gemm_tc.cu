@@ -39,8 +39,9 @@ struct Params {
   OpMap a, b;
   int tiles_m, tiles_n;
   int kblocks, splits, kb_per_split;
-  int zbase;
+  int zbase, nz;    // batch indices [zbase, zbase + nz) in this launch
   int lanes_rows;   // epilogue: consecutive lanes on consecutive rows (output column-contiguous)
+  int fast;         // vectorised epilogue: 4 consecutive columns per lane (all views row-major, aligned)
   float* ws;
   uint32_t idesc;
 };
@@ -89,6 +90,111 @@ __device__ __forceinline__ void mma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
 }
 
+__device__ __forceinline__ void ld4(const void* p, int64_t off, int dt, float* o) {
+  if (dt == F32) {
+    const float4 v = *reinterpret_cast<const float4*>(static_cast<const float*>(p) + off);
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  } else {
+    const uint2 v = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(p) + off);
+    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&v.x);
+    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&v.y);
+    const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+    o[0] = fa.x; o[1] = fa.y; o[2] = fb.x; o[3] = fb.y;
+  }
+}
+__device__ __forceinline__ void st4(void* p, int64_t off, int dt, const float* v) {
+  if (dt == F32) {
+    *reinterpret_cast<float4*>(static_cast<float*>(p) + off) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p) + off) = u;
+  }
+}
+// Per-row base offsets of every epilogue view (the column term is added per element).
+struct RowBase {
+  int64_t c, cross, aux, mask, resid;
+};
+__device__ __forceinline__ RowBase row_base(const Gemm& g, int z, int row) {
+  RowBase rb;
+  rb.c = g.c.off(z, row, 0);
+  rb.cross = g.e.cross.ptr ? g.e.cross.off(z, row, 0) : 0;
+  rb.aux = g.e.aux.ptr ? g.e.aux.off(z, row, 0) : 0;
+  rb.mask = g.e.mask.ptr ? g.e.mask.off(z, row, 0) : 0;
+  rb.resid = g.e.resid.ptr ? g.e.resid.off(z, row, 0) : 0;
+  return rb;
+}
+__device__ __forceinline__ float bias_at(const Epilogue& e, int j) {
+  if (!e.bias) return 0.f;
+  if (e.bias_gap_hi > e.bias_gap_lo) {
+    if (j >= e.bias_gap_lo && j < e.bias_gap_hi) return 0.f;
+    if (j >= e.bias_gap_hi) j -= e.bias_gap_hi - e.bias_gap_lo;
+  }
+  return ld_as_f32(e.bias, j, e.bias_dt);
+}
+// The fused epilogue of one element given its row bases (same math as epi_apply).
+__device__ __forceinline__ void epi_elem(const Gemm& g, const RowBase& rb, int col, float acc) {
+  const Epilogue& e = g.e;
+  float v = acc * e.alpha + bias_at(e, col);
+  if (e.cross.ptr) {
+    if (e.aux.ptr) st_from_f32(e.aux.ptr, rb.aux + col * e.aux.cs, e.aux.dt, v);
+    const float x = ld_as_f32(e.cross.ptr, rb.cross + col * e.cross.cs, e.cross.dt);
+    v = x * v + x;
+  } else if (e.aux.ptr) {
+    st_from_f32(e.aux.ptr, rb.aux + col * e.aux.cs, e.aux.dt, v);
+  }
+  if (e.relu) v = fmaxf(v, 0.f);
+  if (e.mask.ptr) v = ld_as_f32(e.mask.ptr, rb.mask + col * e.mask.cs, e.mask.dt) > 0.f ? v : 0.f;
+  if (e.resid.ptr) v += ld_as_f32(e.resid.ptr, rb.resid + col * e.resid.cs, e.resid.dt);
+  const int64_t co = rb.c + col * g.c.cs;
+  if (e.accumulate) v += ld_as_f32(g.c.ptr, co, g.c.dt);
+  st_from_f32(g.c.ptr, co, g.c.dt, v);
+}
+
+// Vectorised epilogue of 4 consecutive columns [col, col + 4) of one row (all views cs == 1).
+// Operands of a 4-column chunk are loaded first (epi4_load) for several rows, then combined and
+// stored (epi4_store): keeps several independent global loads in flight per lane.
+struct Chunk4 {
+  float x[4], m[4], r[4], c[4];
+};
+__device__ __forceinline__ void epi4_load(const Gemm& g, const RowBase& rb, int col, Chunk4& k) {
+  const Epilogue& e = g.e;
+  if (e.cross.ptr) ld4(e.cross.ptr, rb.cross + col, e.cross.dt, k.x);
+  if (e.mask.ptr) ld4(e.mask.ptr, rb.mask + col, e.mask.dt, k.m);
+  if (e.resid.ptr) ld4(e.resid.ptr, rb.resid + col, e.resid.dt, k.r);
+  if (e.accumulate) ld4(g.c.ptr, rb.c + col, g.c.dt, k.c);
+}
+__device__ __forceinline__ void epi4_store(const Gemm& g, const RowBase& rb, int col, float* a, const float* bias4,
+                                           const Chunk4& k) {
+  const Epilogue& e = g.e;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) a[t] = a[t] * e.alpha + bias4[t];
+  if (e.aux.ptr) st4(e.aux.ptr, rb.aux + col, e.aux.dt, a);
+  if (e.cross.ptr) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] = k.x[t] * a[t] + k.x[t];
+  }
+  if (e.relu) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] = fmaxf(a[t], 0.f);
+  }
+  if (e.mask.ptr) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] = k.m[t] > 0.f ? a[t] : 0.f;
+  }
+  if (e.resid.ptr) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] += k.r[t];
+  }
+  if (e.accumulate) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] += k.c[t];
+  }
+  st4(g.c.ptr, rb.c + col, g.c.dt, a);
+}
+
 template <int TILE>
 __device__ __forceinline__ void load_operand(const CUtensorMap* map, const OpMap& om, uint32_t dst, int mn0, int k,
                                              int z, uint32_t mbar) {
@@ -112,35 +218,42 @@ __device__ __forceinline__ void load_operand(const CUtensorMap* map, const OpMap
   }
 }
 
+// Persistent, warp-specialised kernel: warp 0 = TMA producer, warp 1 = MMA issuer,
+// warps 2-9 = epilogue.  Work items (tile, batch index, K split) are strided over
+// the grid.  The TMEM accumulator is double-buffered (2 x BN columns) so the
+// epilogue of item i overlaps the MMAs of item i+1 and the loads of item i+2.
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    const __grid_constant__ Params p) {
   constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
+  constexpr int SC = BN / 2 < 64 ? BN / 2 : 64;   // columns staged per epilogue pass
+  constexpr int SROW = SC + 4;              // float4 rows; 16-B granules conflict-free both ways
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* bars = (uint64_t*)(sB + STAGES * B_BYTES);   // full[STAGES], empty[STAGES], tfull
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 1);
+  float* stage_all = (float*)(sB + STAGES * B_BYTES);
+  uint64_t* bars = (uint64_t*)(stage_all + 8 * 32 * SROW);   // full[S], empty[S], tfull[2], tempty[2]
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  const int tile = blockIdx.x;
-  const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
-  const int z = p.zbase + blockIdx.y / p.splits, sp = blockIdx.y % p.splits;
-  const int m0 = tm * BM, n0 = tn * BN;
-  const int kb0 = sp * p.kb_per_split;
-  const int nk = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
+  const int ntiles = p.tiles_m * p.tiles_n;
+  const int total = ntiles * p.nz * p.splits;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
-    for (int s = 0; s < 2 * STAGES + 1; ++s) mbar_init(smem_u32(bars + s), 1);
+    for (int s = 0; s < 2 * STAGES + 2; ++s) mbar_init(smem_u32(bars + s), 1);
+    for (int s = 0; s < 2; ++s) mbar_init(smem_u32(tempty + s), 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -148,95 +261,210 @@ __global__ void __launch_bounds__(128, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer
-    for (int i = 0; i < nk; ++i) {
-      const int s = i % STAGES;
-      const uint32_t ph = (i / STAGES) & 1;
-      mbar_wait(smem_u32(bars + STAGES + s), ph ^ 1);
-      const uint32_t fb = smem_u32(bars + s);
-      mbar_expect_tx(fb, A_BYTES + B_BYTES);
-      const int k = (kb0 + i) * BK;
-      load_operand<BM>(&tma_a, p.a, smem_u32(sA + s * A_BYTES), m0, k, z, fb);
-      load_operand<BN>(&tma_b, p.b, smem_u32(sB + s * B_BYTES), n0, k, z, fb);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread)
-    const uint32_t a_step = p.a.mn_major ? 16 * 128 : 32;   // bytes per K = 16 slice
-    const uint32_t b_step = p.b.mn_major ? 16 * 128 : 32;
-    const uint32_t a_lbo = p.a.mn_major ? 64 * BK * 2 : 16, b_lbo = p.b.mn_major ? 64 * BK * 2 : 16;
-    for (int i = 0; i < nk; ++i) {
-      const int s = i % STAGES;
-      const uint32_t ph = (i / STAGES) & 1;
-      mbar_wait(smem_u32(bars + s), ph);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t ab = smem_u32(sA + s * A_BYTES), bb = smem_u32(sB + s * B_BYTES);
-#pragma unroll
-      for (int kk = 0; kk < BK / 16; ++kk) {
-        const uint64_t ad = sdesc(ab + kk * a_step, a_lbo, 1024);
-        const uint64_t bd = sdesc(bb + kk * b_step, b_lbo, 1024);
-        mma_f16(tmem, ad, bd, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
-      }
-      mma_commit(smem_u32(bars + STAGES + s));   // slot free once these MMAs complete
-    }
-    mma_commit(smem_u32(bars + 2 * STAGES));     // accumulator complete
-  }
-  __syncwarp();
+  auto decode = [&](int item, int& m0, int& n0, int& z, int& sp, int& kb0, int& nk) {
+    const int tile = item % ntiles;
+    const int zs = item / ntiles;
+    sp = zs % p.splits;
+    z = p.zbase + zs / p.splits;
+    m0 = (tile % p.tiles_m) * BM;
+    n0 = (tile / p.tiles_m) * BN;
+    kb0 = sp * p.kb_per_split;
+    nk = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
+  };
 
-  // ---------------- epilogue: TMEM -> registers -> smem (the idle ring) -> fused epilogue -> global.
-  // Each warp owns TMEM lanes / tile rows [32w, 32w+32).  Pass 1 parks its rows in shared memory
-  // (row stride BN+1: conflict-free both ways); pass 2 walks them with consecutive lanes on
-  // consecutive memory (columns, or rows when the output is column-contiguous) so every global
-  // access of the epilogue is coalesced.
-  if (nk > 0) mbar_wait(smem_u32(bars + 2 * STAGES), 0);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  constexpr int SROW = BN + 1;
-  float* stage = reinterpret_cast<float*>(smem) + warp * 32 * SROW;
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    uint32_t v[16];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int j = 0; j < 16; ++j) stage[lane * SROW + c0 + j] = nk > 0 ? __uint_as_float(v[j]) : 0.f;
-  }
-  __syncwarp();
-  const Gemm& g = p.g;
-  const int rbase = m0 + warp * 32;
-  if (!p.lanes_rows) {
-#pragma unroll 1
-    for (int r = 0; r < 32; ++r) {
-      const int row = rbase + r;
-      if (row >= g.M) break;
-#pragma unroll
-      for (int q = 0; q < BN / 32; ++q) {
-        const int col = n0 + lane + 32 * q;
-        if (col < g.N) {
-          const float acc = stage[r * SROW + lane + 32 * q];
-          if (p.splits == 1) epi_apply(g, z, row, col, acc);
-          else p.ws[((int64_t)(z * p.splits + sp) * g.M + row) * g.N + col] = acc;
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int it = 0;
+      for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        int m0, n0, z, sp, kb0, nk;
+        decode(item, m0, n0, z, sp, kb0, nk);
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(smem_u32(empty + s), ph ^ 1);
+          const uint32_t fb = smem_u32(full + s);
+          mbar_expect_tx(fb, A_BYTES + B_BYTES);
+          const int k = (kb0 + i) * BK;
+          load_operand<BM>(&tma_a, p.a, smem_u32(sA + s * A_BYTES), m0, k, z, fb);
+          load_operand<BN>(&tma_b, p.b, smem_u32(sB + s * B_BYTES), n0, k, z, fb);
         }
       }
     }
-  } else {
-    const int row = rbase + lane;
-    if (row < g.M) {
-#pragma unroll 4
-      for (int cc = 0; cc < BN; ++cc) {
-        const int col = n0 + cc;
-        if (col >= g.N) break;
-        epi_apply(g, z, row, col, stage[lane * SROW + cc]);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread)
+      const uint32_t a_step = p.a.mn_major ? 16 * 128 : 32;   // bytes per K = 16 slice
+      const uint32_t b_step = p.b.mn_major ? 16 * 128 : 32;
+      const uint32_t a_lbo = p.a.mn_major ? 64 * BK * 2 : 16, b_lbo = p.b.mn_major ? 64 * BK * 2 : 16;
+      int it = 0, li = 0;
+      for (int item = blockIdx.x; item < total; item += gridDim.x, ++li) {
+        int m0, n0, z, sp, kb0, nk;
+        decode(item, m0, n0, z, sp, kb0, nk);
+        const int ab = li & 1;
+        const uint32_t aph = (li >> 1) & 1;
+        mbar_wait(smem_u32(tempty + ab), aph ^ 1);      // epilogue drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t dacc = tmem + (uint32_t)(ab * BN);
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(smem_u32(full + s), ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t ab_ = smem_u32(sA + s * A_BYTES), bb_ = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = sdesc(ab_ + kk * a_step, a_lbo, 1024);
+            const uint64_t bd = sdesc(bb_ + kk * b_step, b_lbo, 1024);
+            mma_f16(dacc, ad, bd, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(smem_u32(empty + s));               // ring slot free once these MMAs complete
+        }
+        mma_commit(smem_u32(tfull + ab));                // accumulator ready for the epilogue
       }
+    }
+  } else {
+    // ---------------- epilogue warps 2..9: warp w reads TMEM lanes [32 (w % 4), +32) (hardware rule)
+    // and column half hh of the accumulator; 8 warps give the epilogue enough loads in flight.
+    const int q4 = warp & 3;
+    const int hh = (warp - 2) >> 2;
+    constexpr int HC = BN / 2;                 // columns per warp
+    float* stage = stage_all + (warp - 2) * 32 * SROW;
+    const Gemm& g = p.g;
+    int li = 0;
+    for (int item = blockIdx.x; item < total; item += gridDim.x, ++li) {
+      int m0, n0, z, sp, kb0, nk;
+      decode(item, m0, n0, z, sp, kb0, nk);
+      const int ab = li & 1;
+      const uint32_t aph = (li >> 1) & 1;
+      mbar_wait(smem_u32(tfull + ab), aph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int rbase = m0 + q4 * 32;
+      if (p.lanes_rows) {
+        // column-contiguous output: row per lane straight from TMEM; consecutive lanes = consecutive addresses
+        const int row = rbase + lane;
+        const bool rok = row < g.M;
+        RowBase rb;
+        if (rok) rb = row_base(g, z, row);
+#pragma unroll 1
+        for (int c0 = hh * HC; c0 < hh * HC + HC; c0 += 16) {
+          uint32_t v[16];
+          const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                "=r"(v[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (c0 + 16 >= hh * HC + HC) {
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty + ab)) : "memory");
+          }
+          if (rok && n0 + c0 < g.N) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int col = n0 + c0 + j;
+              if (col < g.N) epi_elem(g, rb, col, __uint_as_float(v[j]));
+            }
+          }
+        }
+        continue;
+      }
+      // row-major output: park this warp's 32 x SC block in smem, then walk it with lanes on columns
+#pragma unroll 1
+      for (int pc = 0; pc < HC; pc += SC) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < SC; c0 += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC + pc + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float4* dst = reinterpret_cast<float4*>(stage + lane * SROW + c0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
+                               __uint_as_float(v[4 * j + 3]));
+      }
+      if (pc + SC >= HC) {
+        // accumulator fully read: hand it back to the MMA warp
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty + ab)) : "memory");
+      }
+      __syncwarp();
+      const int cbase = n0 + hh * HC + pc;
+      if (p.fast) {
+        constexpr int LPR = SC / 4;            // lanes per row (4 columns each)
+        constexpr int RPP = 32 / LPR;          // rows per pass
+        constexpr int U = 2;                   // passes whose loads are in flight together
+        const int sub = lane / LPR, cl = lane % LPR;
+        const int col = cbase + 4 * cl;
+        float bias4[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) bias4[t] = (col + t < g.N) ? bias_at(g.e, col + t) : 0.f;
+        const bool full4 = col + 3 < g.N;
+#pragma unroll 1
+        for (int r0 = 0; r0 < 32; r0 += RPP * U) {
+          RowBase rb[U];
+          Chunk4 k[U];
+          bool ok[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int r = r0 + u * RPP + sub;
+            const int row = rbase + r;
+            ok[u] = (r < 32) && (row < g.M) && (col < g.N);
+            if (ok[u]) {
+              rb[u] = row_base(g, z, row);
+              if (full4) epi4_load(g, rb[u], col, k[u]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+            const int r = r0 + u * RPP + sub;
+            const float4 a4 = *reinterpret_cast<const float4*>(stage + r * SROW + 4 * cl);
+            float a[4] = {a4.x, a4.y, a4.z, a4.w};
+            if (full4) {
+              epi4_store(g, rb[u], col, a, bias4, k[u]);
+            } else {
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                if (col + t < g.N) epi_elem(g, rb[u], col + t, a[t]);
+            }
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int r = 0; r < 32; ++r) {
+          const int row = rbase + r;
+          if (row >= g.M) break;
+          RowBase rb;
+          if (p.splits == 1) rb = row_base(g, z, row);
+#pragma unroll
+          for (int q = 0; q < SC / 32; ++q) {
+            const int col = cbase + lane + 32 * q;
+            if (col < g.N) {
+              const float acc = stage[r * SROW + lane + 32 * q];
+              if (p.splits == 1) epi_elem(g, rb, col, acc);
+              else p.ws[((int64_t)(z * p.splits + sp) * g.M + row) * g.N + col] = acc;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      }
+      __syncwarp();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
 }
 
 // ------------------------------------------------------------------ host side
@@ -308,21 +536,36 @@ static bool make_map(CUtensorMap* map, OpMap* om, const Operand& o, int rows, in
   return res == CUDA_SUCCESS;
 }
 
+// a view can take 4-wide vector accesses: column-contiguous rows, every row / batch offset a multiple of 4
+// elements and a base aligned to 4 elements of its dtype
+static bool vec_ok(const View& v) {
+  if (!v.ptr) return true;
+  const int es = v.dt == F32 ? 4 : 2;
+  if (v.cs != 1) return false;
+  if (((uintptr_t)v.ptr) % (4 * es)) return false;
+  if (v.rs % 4 || v.bs0 % 4 || v.bs1 % 4 || v.rs_o % 4) return false;
+  return true;
+}
+
 template <int BN, int STAGES>
 static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st) {
-  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 1) * 8 + 16 + 1024;
+  constexpr int SC = BN / 2 < 64 ? BN / 2 : 64;
+  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + 8 * 32 * (SC + 4) * 4 + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static_assert(SMEM <= 227 * 1024, "smem");
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr = true;
   }
   const int ntiles = p0.tiles_m * p0.tiles_n;
-  const int zmax = 65535 / p0.splits;
+  const int zmax = std::max(1, (int)std::min<int64_t>(p0.g.batch, (int64_t)(1 << 30) / ((int64_t)ntiles * p0.splits)));
   for (int zb = 0; zb < p0.g.batch; zb += zmax) {
     Params p = p0;
     p.zbase = zb;
-    const int nz = std::min(zmax, p0.g.batch - zb);
-    gemm_tc_kernel<BN, STAGES><<<dim3(ntiles, nz * p.splits), 128, SMEM, st>>>(ma, mb, p);
+    p.nz = std::min(zmax, p0.g.batch - zb);
+    const int64_t items = (int64_t)ntiles * p.nz * p.splits;
+    const int grid = (int)std::min<int64_t>(items, 148);
+    gemm_tc_kernel<BN, STAGES><<<grid, 320, SMEM, st>>>(ma, mb, p);
     ++g_launches;
   }
   return cudaGetLastError();
@@ -334,7 +577,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   using namespace tc;
   if (g.a.dt != BF16 || g.b.dt != BF16 || g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return cudaErrorNotSupported;
   if (g.N < 16) return cudaErrorNotSupported;
-  const int BN = g.N <= 64 ? 64 : 128;
+  const int BN = g.N <= 64 ? 64 : g.N <= 128 ? 128 : 256;
   Params p;
   p.g = g;
   CUtensorMap ma, mb;
@@ -345,7 +588,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   p.kblocks = (g.K + BK - 1) / BK;
   const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n * g.batch;
   int splits = 1;
-  if (tiles < 148 && p.kblocks >= 8) {
+  if (tiles < 148 && p.kblocks >= 8) {   // few output tiles, long K: split K across CTAs
     splits = (int)std::min<int64_t>((2 * 148 + tiles - 1) / tiles, p.kblocks / 4);
     while (splits > 1 && (int64_t)splits * g.batch * g.M * g.N * 4 > (int64_t)ws.bytes) --splits;
   }
@@ -353,10 +596,14 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   p.splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;   // no empty splits
   p.ws = ws.ptr;
   p.zbase = 0;
+  p.nz = g.batch;
   p.lanes_rows = (g.c.cs != 1 && g.c.rs == 1 && splits == 1) ? 1 : 0;
+  p.fast = (!p.lanes_rows && splits == 1 && vec_ok(g.c) && vec_ok(g.e.cross) && vec_ok(g.e.aux) &&
+            vec_ok(g.e.resid) && vec_ok(g.e.mask)) ? 1 : 0;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a.mn_major << 15) | ((uint32_t)p.b.mn_major << 16) |
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-  cudaError_t e = BN == 64 ? launch<64, 4>(p, ma, mb, st) : launch<128, 3>(p, ma, mb, st);
+  cudaError_t e = BN == 64 ? launch<64, 6>(p, ma, mb, st) : BN == 128 ? launch<128, 4>(p, ma, mb, st)
+                                                      : launch<256, 3>(p, ma, mb, st);
   if (e != cudaSuccess) return e;
   if (p.splits > 1) return splitk_reduce(g, p.splits, ws.ptr, st);
   return cudaSuccess;

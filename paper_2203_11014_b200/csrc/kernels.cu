@@ -428,7 +428,7 @@ __global__ void head_k(const void* Y, const void* w, const void* bh, int pdt, co
   part = warp_sum(part);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = part;
   __syncthreads();
-  __shared__ float zs, dzs;
+  __shared__ float dzs;
   if (threadIdx.x == 0) {
     float s = 0.f;
     for (int q = 0; q < (int)(blockDim.x / 32); ++q) s += red[q];
@@ -441,7 +441,6 @@ __global__ void head_k(const void* Y, const void* w, const void* bh, int pdt, co
       dzs = (sg - y) / (float)Bg;
       dz[b] = dzs;
     }
-    zs = zz;
   }
   __syncthreads();
   if (!do_bwd) return;
@@ -451,27 +450,26 @@ __global__ void head_k(const void* Y, const void* w, const void* bh, int pdt, co
     st_from_f32(dY, (int64_t)b * m * d + e, dt, g * ld_as_f32(w, c, pdt));
   }
 }
-__global__ void head_red_k(const float* pooled, const float* dz, const float* lossb, int B, int d, int Bg,
-                           float* loss_out, float* dw, float* db) {
-  __shared__ float red[32];
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+// two-pass deterministic reduction of the head gradients over samples:
+// part[blk] = (sum_b dz_b pooled_b[0..d), sum_b dz_b, sum_b loss_b) over the block's sample chunk
+__global__ void head_part_k(const float* pooled, const float* dz, const float* lossb, int B, int d, int per,
+                            float* part) {
+  const int b0 = blockIdx.x * per, b1 = min(B, b0 + per);
+  for (int c = threadIdx.x; c < d + 2; c += blockDim.x) {
     float s = 0.f;
-    for (int b = 0; b < B; ++b) s += dz[b] * pooled[(int64_t)b * d + c];
-    dw[c] += s;
+    for (int b = b0; b < b1; ++b) {
+      s += c < d ? dz[b] * pooled[(int64_t)b * d + c] : (c == d ? dz[b] : lossb[b]);
+    }
+    part[(int64_t)blockIdx.x * (d + 2) + c] = s;
   }
-  float l = 0.f, g = 0.f;
-  // fixed assignment of samples to threads, then fixed-order combination
-  for (int b = threadIdx.x; b < B; b += blockDim.x) { l += lossb[b]; g += dz[b]; }
-  l = warp_sum(l);
-  g = warp_sum(g);
-  __shared__ float redg[32];
-  if ((threadIdx.x & 31) == 0) { red[threadIdx.x / 32] = l; redg[threadIdx.x / 32] = g; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float a = 0.f, bb = 0.f;
-    for (int q = 0; q < (int)(blockDim.x / 32); ++q) { a += red[q]; bb += redg[q]; }
-    if (loss_out) *loss_out = a / (float)Bg;
-    db[0] += bb;
+}
+__global__ void head_fin_k(const float* part, int nparts, int d, int Bg, float* loss_out, float* dw, float* db) {
+  for (int c = threadIdx.x; c < d + 2; c += blockDim.x) {
+    float s = 0.f;
+    for (int q = 0; q < nparts; ++q) s += part[(int64_t)q * (d + 2) + c];
+    if (c < d) dw[c] += s;
+    else if (c == d) db[0] += s;
+    else if (loss_out) *loss_out = s / (float)Bg;
   }
 }
 cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, const float* labels, int B, int m, int d,
@@ -480,8 +478,11 @@ cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, 
   head_k<<<B, 256, 0, st>>>(Y, w, bh, pdt, labels, m, d, Bg, dY, dt, pooled, z, lossb, dz, do_bwd);
   ++g_launches;
   if (do_bwd) {
-    head_red_k<<<1, 256, 0, st>>>(pooled, dz, lossb, B, d, Bg, loss_out, dw, db);
-    ++g_launches;
+    const int per = 32, nparts = (B + per - 1) / per;
+    float* part = pooled + (int64_t)B * d;   // scratch after pooled (sized by the runtime)
+    head_part_k<<<nparts, 128, 0, st>>>(pooled, dz, lossb, B, d, per, part);
+    head_fin_k<<<1, 256, 0, st>>>(part, nparts, d, Bg, loss_out, dw, db);
+    g_launches += 2;
   }
   return cudaGetLastError();
 }

@@ -360,7 +360,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   c->red = (float*)work.take(c->red_bytes);
   c->ws.bytes = (size_t)256 << 20;
   c->ws.ptr = (float*)work.take(c->ws.bytes);
-  c->pooled = (float*)work.take((size_t)B * d * 4);
+  c->pooled = (float*)work.take(((size_t)B * d + (size_t)((B + 31) / 32) * (d + 2)) * 4);   // + head partials
   c->z = (float*)work.take((size_t)B * 4);
   c->lossb = (float*)work.take((size_t)B * 4);
   c->dz = (float*)work.take((size_t)B * 4);

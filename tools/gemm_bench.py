@@ -1,0 +1,91 @@
+"""Time single library GEMMs of the DHEN step's shapes through the C-ABI test hook
+(CUDA events, L2 flushed before each launch).  Usage:
+    python tools/gemm_bench.py [--cfg C2] [--only name] [--iters 20]
+Prints one line per shape: ms, TFLOP/s, GB/s (algorithmic bytes)."""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2203_11014_b200.binding import debug_gemm  # noqa: E402
+
+
+def shapes(cfg):
+    # (name, M, N, K, batch, A(s_mn,s_k,bs0,bs1,zdiv,kdiv,s_ko), B(...), C(rs,cs,bs0,bs1,zdiv), acc, a2, b2, c2, cdt)
+    if cfg == "C2":
+        B, m, d, l, mo = 2048, 64, 128, 32, 64
+        h = m * (m - 1) // 2
+    else:
+        B, m, d, l, mo = 8192, 128, 256, 32, 128
+        h = m * (m - 1) // 2
+    R = B * m
+    f32, bf = torch.float32, torch.bfloat16
+    return [
+        ("dot.gram", m, m, d, B, (d, 1, m * d, 0, 1, 0, 0), (d, 1, m * d, 0, 1, 0, 0), (m, 1, m * m, 0, 1), 0,
+         (0, 0), (0, 0), (0, 0), f32),
+        ("dot.proj", B, l * d, h, 1, (h, 1, 0, 0, 1, 0, 0), (h, 1, 0, 0, 1, 0, 0), (mo * d, 1, 0, 0, 1), 0,
+         (0, 0), (0, 0), (0, 0), f32),
+        ("dot.proj_dgrad", B, h, l * d, 1, (mo * d, 1, 0, 0, 1, 0, 0), (1, h, 0, 0, 1, 0, 0), (h, 1, 0, 0, 1), 0,
+         (0, 0), (0, 0), (0, 0), bf),
+        ("dot.proj_wgrad", l * d, h, B, 1, (1, mo * d, 0, 0, 1, 0, 0), (1, h, 0, 0, 1, 0, 0), (h, 1, 0, 0, 1), 1,
+         (0, 0), (0, 0), (0, 0), f32),
+        ("dot.gram_bwd", m, d, m, B, (m, 1, m * m, 0, 1, 0, 0), (1, d, m * d, 0, 1, 0, 0), (d, 1, m * d, 0, 1), 1,
+         (0, 0), (0, 0), (0, 0), f32),
+        ("dcn.cross", R, d, d, 1, (d, 1, 0, 0, 1, 0, 0), (d, 1, 0, 0, 1, 0, 0), (d, 1, 0, 0, 1), 0,
+         (0, 0), (0, 0), (0, 0), bf),
+        ("dcn.wgrad", d, d, R, 1, (1, d, 0, 0, 1, 0, 0), (1, d, 0, 0, 1, 0, 0), (d, 1, 0, 0, 1), 1,
+         (0, 0), (0, 0), (0, 0), f32),
+        ("tokmix.fwd", B * d, l, m, 1, (1, d, 0, 0, 1, 0, 0), (1, l, 0, 0, 1, 0, 0), (1, d, 0, 0, 1), 0,
+         (d, m * d), (0, 0), (d, mo * d), f32),
+        ("tokmix.dgrad", B * d, m, l, 1, (1, d, 0, 0, 1, 0, 0), (l, 1, 0, 0, 1, 0, 0), (1, d, 0, 0, 1), 0,
+         (d, mo * d), (0, 0), (d, m * d), bf),
+        ("tokmix.wgrad", m, l, B * d, 1, (d, 1, 0, 0, 1, d, m * d), (d, 1, 0, 0, 1, d, mo * d), (l, 1, 0, 0, 1), 1,
+         (0, 0), (0, 0), (0, 0), f32),
+    ]
+
+
+def extent(r, K, z, s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko, mdiv=0, s_mo=0):
+    rows = ((r - 1) // mdiv) * s_mo + ((r - 1) % mdiv) * s_mn if mdiv else (r - 1) * s_mn
+    kk = ((K - 1) % kdiv) * s_k + ((K - 1) // kdiv) * s_ko if kdiv else (K - 1) * s_k
+    zz = ((z - 1) // zdiv) * bs0 + ((z - 1) % zdiv) * bs1
+    return rows + kk + zz + 1
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cfg", default="C2")
+    ap.add_argument("--only", default="")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--path", type=int, default=0)
+    args = ap.parse_args()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for (name, M, N, K, Z, a, b, c, acc, a2, b2, c2, cdt) in shapes(args.cfg):
+        if args.only and args.only not in name:
+            continue
+        A = torch.randn(extent(M, K, Z, *a, *a2), device="cuda").to(torch.bfloat16)
+        Bm = torch.randn(extent(N, K, Z, *b, *b2), device="cuda").to(torch.bfloat16)
+        rs, cs, cb0, cb1, czd = c
+        cext = extent(M, N, Z, rs, cs, cb0, cb1, czd, 0, 0, *c2)
+        Cm = torch.zeros(cext, device="cuda", dtype=cdt)
+        q = [M, N, K, Z] + list(a) + list(b) + list(c) + [acc] + list(a2) + list(b2) + list(c2)
+        tc = debug_gemm(q, A, Bm, Cm, path=args.path, ws=ws)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.iters)]
+        for e0, e1 in ev:
+            flush.zero_()
+            e0.record()
+            debug_gemm(q, A, Bm, Cm, path=args.path, ws=ws)
+            e1.record()
+        torch.cuda.synchronize()
+        ms = sorted(e0.elapsed_time(e1) for e0, e1 in ev)[len(ev) // 2]
+        fl = 2.0 * M * N * K * Z
+        es_c = 4 if cdt == torch.float32 else 2
+        byts = A.numel() * 2 + Bm.numel() * 2 + M * N * Z * es_c * (2 if acc else 1)
+        print(f"{name:16s} tc={int(tc)} M={M:7d} N={N:5d} K={K:6d} Z={Z:5d} {ms * 1e3:9.1f} us "
+              f"{fl / ms / 1e9:8.1f} TF/s {byts / ms / 1e6:8.1f} GB/s", flush=True)
+
+
+if __name__ == "__main__":
+    main()
