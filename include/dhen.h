@@ -185,6 +185,9 @@ dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* B, vo
                             int path, void* ws, size_t ws_bytes, void* stream);
 /* 1 if the last GEMM ran on the tcgen05 path. */
 int dhen_debug_last_gemm_tc(void);
+/* Debug: device buffer (>= 448 int64) receiving clock64 timestamps of CTA 0 of every following
+ * tcgen05 GEMM (producer issue, MMA start, data ready, epilogue start, epilogue end); NULL = off. */
+void dhen_debug_gemm_trace(void* dev_buf);
 
 /* Number of library kernels launched since init (a host-side counter). */
 unsigned long long dhen_launch_count(const dhen_ctx* ctx);

@@ -23,7 +23,8 @@ STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_SHAPE", 3: "E_ALIGN", 4: "E_STATE", 5: "
 EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "dhen_init", "dhen_layer_fwd",
            "dhen_layer_bwd", "dhen_train_step", "dhen_forward", "dhen_zero_grad", "dhen_params_io",
            "dhen_grads_get", "dhen_launch_count", "dhen_last_error", "dhen_destroy", "dhen_profile",
-           "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_last_gemm_tc")
+           "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_last_gemm_tc",
+           "dhen_debug_gemm_trace")
 
 
 class dhen_module(C.Structure):
@@ -93,6 +94,8 @@ def load(path: str = LIB_PATH):
     lib.dhen_last_error.argtypes = []
     lib.dhen_launch_count.restype = C.c_ulonglong
     lib.dhen_launch_count.argtypes = [vp]
+    lib.dhen_debug_gemm_trace.restype = None
+    lib.dhen_debug_gemm_trace.argtypes = [vp]
     lib.dhen_debug_last_gemm_tc.restype = C.c_int
     lib.dhen_debug_last_gemm_tc.argtypes = []
     lib.dhen_destroy.restype = None
@@ -199,6 +202,9 @@ def debug_gemm(q, A, B, Cm, path=0, ws=None, stream=None):
     import torch
     q = list(q) + [0] * (30 - len(q))
     arr = (C.c_longlong * 30)(*[int(v) for v in q])
+    for t_ in (A, B, Cm):
+        if t_.dtype not in (torch.bfloat16, torch.float32):
+            raise TypeError(f"debug_gemm: unsupported dtype {t_.dtype}")
     abt = BF16 if A.dtype == torch.bfloat16 else FP32
     ct = BF16 if Cm.dtype == torch.bfloat16 else FP32
     if ws is None:

@@ -81,6 +81,8 @@ extern unsigned long long g_launches;
 extern int g_last_gemm_tc;
 // path override: -1 env/auto, 0 auto, 1 SIMT only, 2 tcgen05 only (test hook)
 extern int g_gemm_force;
+// debug: device buffer of >= 448 int64 for a clock64 trace of CTA 0 of the next tcgen05 GEMMs
+extern long long* g_gemm_trace;
 
 // Dispatch: tcgen05/TMA path when the shapes and layouts allow it, the SIMT
 // path (exact fp32 FMA; the fp32 mode and odd shapes) otherwise.

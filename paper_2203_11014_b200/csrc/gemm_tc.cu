@@ -15,11 +15,13 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemm.h"
 #include "gemm_epi.cuh"
 
 namespace dhen {
+long long* g_gemm_trace = nullptr;
 namespace tc {
 
 constexpr int BM = 128, BK = 64;
@@ -34,16 +36,38 @@ struct OpMap {
   int zdiv;
 };
 
+// Compact, host-resolved epilogue plan: every present view shares one row geometry
+// (offset = row term + batch term + col * cs), operands other than C are bf16.
+enum { EF_ACC = 1, EF_RELU = 2, EF_MASK = 4, EF_CROSS = 8, EF_AUX = 16, EF_RESID = 32, EF_BIAS = 64 };
+struct Lean {
+  void* c;
+  const void* x;
+  void* aux;
+  const void* mask;
+  const void* resid;
+  const void* bias;
+  int64_t rs, rs_o, bs0, bs1, cs;
+  int rdiv, zdiv;
+  int c_f32, flags, gap_lo, gap_hi;
+  float alpha;
+};
+
 struct Params {
   Gemm g;
+  Lean ep;
+  int lean;         // 1: use the lean epilogue plan
+  int lean_id;      // >0: compile-time specialised pass (8 columns per lane / 16 per row-lane)
   OpMap a, b;
   int tiles_m, tiles_n;
   int kblocks, splits, kb_per_split;
   int zbase, nz;    // batch indices [zbase, zbase + nz) in this launch
   int lanes_rows;   // epilogue: consecutive lanes on consecutive rows (output column-contiguous)
   int fast;         // vectorised epilogue: 4 consecutive columns per lane (all views row-major, aligned)
+  int fast8;        // 8 consecutive columns per lane (N % 8 == 0, 16-B aligned rows)
   float* ws;
   uint32_t idesc;
+  long long* trace;   // debug: CTA 0 records clock64 timestamps (nullptr = off)
+  int dbg;            // debug: 1 = skip the global epilogue pass (timing experiments only)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -59,10 +83,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(a),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)   // suspend-time hint (ns): sleep until the phase completes instead of spinning
       : "memory");
 }
 __device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap* map, const int c[5], uint32_t mbar) {
@@ -195,6 +219,258 @@ __device__ __forceinline__ void epi4_store(const Gemm& g, const RowBase& rb, int
   st4(g.c.ptr, rb.c + col, g.c.dt, a);
 }
 
+// ---- explicit-state-space memory helpers for the epilogue (no generic addressing)
+__device__ __forceinline__ void sts4(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void ldg_bf4(const void* base, int64_t off, float* o) {
+  uint32_t u0, u1;
+  asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(u0), "=r"(u1) : "l"((const __nv_bfloat16*)base + off));
+  o[0] = __uint_as_float(u0 << 16); o[1] = __uint_as_float(u0 & 0xffff0000u);
+  o[2] = __uint_as_float(u1 << 16); o[3] = __uint_as_float(u1 & 0xffff0000u);
+}
+__device__ __forceinline__ void ldg_c4(const void* base, int64_t off, int f32, float* o) {
+  if (f32) {
+    asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3])
+                 : "l"((const float*)base + off));
+  } else {
+    uint32_t u0, u1;
+    asm volatile("ld.global.v2.u32 {%0, %1}, [%2];" : "=r"(u0), "=r"(u1) : "l"((const __nv_bfloat16*)base + off));
+    o[0] = __uint_as_float(u0 << 16); o[1] = __uint_as_float(u0 & 0xffff0000u);
+    o[2] = __uint_as_float(u1 << 16); o[3] = __uint_as_float(u1 & 0xffff0000u);
+  }
+}
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void stg4(void* base, int64_t off, int f32, const float* v) {
+  if (f32) {
+    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"((float*)base + off), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                 "f"(v[3]) : "memory");
+  } else {
+    asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"((__nv_bfloat16*)base + off), "r"(pack_bf2(v[0], v[1])),
+                 "r"(pack_bf2(v[2], v[3])) : "memory");
+  }
+}
+__device__ __forceinline__ float ldg_bf1(const void* base, int64_t off) {
+  unsigned short u;
+  asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(u) : "l"((const __nv_bfloat16*)base + off));
+  return __uint_as_float(((uint32_t)u) << 16);
+}
+__device__ __forceinline__ float ldg_c1(const void* base, int64_t off, int f32) {
+  if (f32) {
+    float v;
+    asm volatile("ld.global.f32 %0, [%1];" : "=f"(v) : "l"((const float*)base + off));
+    return v;
+  }
+  unsigned short u;
+  asm volatile("ld.global.u16 %0, [%1];" : "=h"(u) : "l"((const __nv_bfloat16*)base + off));
+  return __uint_as_float(((uint32_t)u) << 16);
+}
+__device__ __forceinline__ void stg1(void* base, int64_t off, int f32, float v) {
+  if (f32) {
+    asm volatile("st.global.f32 [%0], %1;" ::"l"((float*)base + off), "f"(v) : "memory");
+  } else {
+    __nv_bfloat16 h = __float2bfloat16_rn(v);
+    asm volatile("st.global.u16 [%0], %1;" ::"l"((__nv_bfloat16*)base + off), "h"(*reinterpret_cast<unsigned short*>(&h))
+                 : "memory");
+  }
+}
+__device__ __forceinline__ int64_t lean_row(const Lean& e, int z, int row) {
+  int64_t o;
+  if (e.rdiv) {
+    const unsigned q = (unsigned)row / (unsigned)e.rdiv;
+    o = (int64_t)q * e.rs_o + (int64_t)((unsigned)row - q * (unsigned)e.rdiv) * e.rs;
+  } else {
+    o = (int64_t)row * e.rs;
+  }
+  if (e.zdiv == 1) {
+    o += (int64_t)z * e.bs0;
+  } else {
+    const unsigned q = (unsigned)z / (unsigned)e.zdiv;
+    o += (int64_t)q * e.bs0 + (int64_t)((unsigned)z - q * (unsigned)e.zdiv) * e.bs1;
+  }
+  return o;
+}
+__device__ __forceinline__ float lean_bias(const Lean& e, int j) {
+  if (e.gap_hi > e.gap_lo) {
+    if (j >= e.gap_lo && j < e.gap_hi) return 0.f;
+    if (j >= e.gap_hi) j -= e.gap_hi - e.gap_lo;
+  }
+  return ldg_bf1(e.bias, j);
+}
+// one element of the lean epilogue
+__device__ __forceinline__ void lean1(const Lean& e, int64_t o, float v, float bias) {
+  const int f = e.flags;
+  v = v * e.alpha + bias;
+  if (f & EF_AUX) stg1(e.aux, o, 0, v);
+  if (f & EF_CROSS) { const float x = ldg_bf1(e.x, o); v = x * v + x; }
+  if (f & EF_RELU) v = fmaxf(v, 0.f);
+  if (f & EF_MASK) v = ldg_bf1(e.mask, o) > 0.f ? v : 0.f;
+  if (f & EF_RESID) v += ldg_bf1(e.resid, o);
+  if (f & EF_ACC) v += ldg_c1(e.c, o, e.c_f32);
+  stg1(e.c, o, e.c_f32, v);
+}
+
+// ---- compile-time specialised epilogue passes (one per (flags, C dtype) in use; see lean_variant())
+__device__ __forceinline__ void ldg_bf8(const void* base, int64_t off, float* o) {
+  uint32_t u[4];
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
+               : "l"((const __nv_bfloat16*)base + off));
+#pragma unroll
+  for (int t = 0; t < 4; ++t) { o[2 * t] = __uint_as_float(u[t] << 16); o[2 * t + 1] = __uint_as_float(u[t] & 0xffff0000u); }
+}
+template <bool CF32>
+__device__ __forceinline__ void ldg_c8(const void* base, int64_t off, float* o) {
+  if (CF32) {
+    asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3])
+                 : "l"((const float*)base + off));
+    asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(o[4]), "=f"(o[5]), "=f"(o[6]), "=f"(o[7])
+                 : "l"((const float*)base + off + 4));
+  } else {
+    uint32_t u[4];
+    asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
+                 : "l"((const __nv_bfloat16*)base + off));
+#pragma unroll
+    for (int t = 0; t < 4; ++t) { o[2 * t] = __uint_as_float(u[t] << 16); o[2 * t + 1] = __uint_as_float(u[t] & 0xffff0000u); }
+  }
+}
+template <bool CF32>
+__device__ __forceinline__ void stg8(void* base, int64_t off, const float* v) {
+  if (CF32) {
+    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"((float*)base + off), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                 "f"(v[3]) : "memory");
+    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"((float*)base + off + 4), "f"(v[4]), "f"(v[5]),
+                 "f"(v[6]), "f"(v[7]) : "memory");
+  } else {
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"((__nv_bfloat16*)base + off), "r"(pack_bf2(v[0], v[1])),
+                 "r"(pack_bf2(v[2], v[3])), "r"(pack_bf2(v[4], v[5])), "r"(pack_bf2(v[6], v[7])) : "memory");
+  }
+}
+__device__ __forceinline__ int64_t shfl64(int64_t v, int src) {
+  const int lo = __shfl_sync(0xffffffffu, (int)(v & 0xffffffff), src);
+  const int hi = __shfl_sync(0xffffffffu, (int)(v >> 32), src);
+  return ((int64_t)hi << 32) | (uint32_t)lo;
+}
+// Row-major output, 8 consecutive columns per lane (N % 8 == 0, 16-B aligned rows).
+template <int F, bool CF32, int SC>
+__device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int M, int N, int cbase, uint32_t stage,
+                                           int lane) {
+  constexpr int LPR = SC / 8, RPP = 32 / LPR, SROW = SC + 4;
+  const int sub = lane / LPR, cl = lane % LPR;
+  const int col = cbase + 8 * cl;
+  const int64_t my_off = (rbase + lane < M) ? lean_row(e, z, rbase + lane) : 0;   // row offset of row `lane`
+  float bias8[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) bias8[t] = 0.f;
+  if ((F & EF_BIAS) && col < N) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) bias8[t] = lean_bias(e, col + t);
+  }
+  const float alpha = e.alpha;
+#pragma unroll 4
+  for (int r = sub; r < 32; r += RPP) {
+    const int64_t o = shfl64(my_off, r) + col;
+    if (rbase + r >= M || col >= N) continue;
+    const uint32_t sa = stage + (uint32_t)((r * SROW + 8 * cl) * 4);
+    const float4 x0 = lds4(sa), x1 = lds4(sa + 16);
+    float a[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) a[t] = a[t] * alpha + bias8[t];
+    float t8[8];
+    if (F & EF_AUX) stg8<false>(e.aux, o, a);
+    if (F & EF_CROSS) {
+      ldg_bf8(e.x, o, t8);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] = t8[t] * a[t] + t8[t];
+    }
+    if (F & EF_RELU) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] = fmaxf(a[t], 0.f);
+    }
+    if (F & EF_MASK) {
+      ldg_bf8(e.mask, o, t8);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] = t8[t] > 0.f ? a[t] : 0.f;
+    }
+    if (F & EF_RESID) {
+      ldg_bf8(e.resid, o, t8);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] += t8[t];
+    }
+    if (F & EF_ACC) {
+      ldg_c8<CF32>(e.c, o, t8);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] += t8[t];
+    }
+    stg8<CF32>(e.c, o, a);
+  }
+}
+// Column-contiguous output (cs != 1, rs == 1): one row per lane, 16 accumulator columns in registers.
+template <int F, bool CF32>
+__device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0, int N, const uint32_t* v) {
+  const float alpha = e.alpha;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int col = col0 + j;
+    if (col >= N) break;
+    const int64_t o = lo + (int64_t)col * e.cs;
+    float a = __uint_as_float(v[j]) * alpha;
+    if (F & EF_BIAS) a += lean_bias(e, col);
+    if (F & EF_AUX) stg1(e.aux, o, 0, a);
+    if (F & EF_CROSS) { const float x = ldg_bf1(e.x, o); a = x * a + x; }
+    if (F & EF_RELU) a = fmaxf(a, 0.f);
+    if (F & EF_MASK) a = ldg_bf1(e.mask, o) > 0.f ? a : 0.f;
+    if (F & EF_RESID) a += ldg_bf1(e.resid, o);
+    if (F & EF_ACC) a += ldg_c1(e.c, o, CF32);
+    stg1(e.c, o, CF32, a);
+  }
+}
+// The (flags, C dtype) combinations the DHEN step uses get a specialised loop; id 0 = none.
+#define LEAN_VARIANTS(X)                          \
+  X(1, 0, true)                                   \
+  X(2, 0, false)                                  \
+  X(3, EF_ACC, true)                              \
+  X(4, EF_BIAS | EF_RELU, false)                  \
+  X(5, EF_BIAS | EF_RESID, true)                  \
+  X(6, EF_RESID, true)                            \
+  X(7, EF_MASK, false)                            \
+  X(8, EF_BIAS | EF_CROSS | EF_AUX, false)        \
+  X(9, EF_BIAS, false)                            \
+  X(10, EF_BIAS, true)                            \
+  X(11, EF_ACC, false)
+static inline int lean_variant(int flags, bool cf32) {
+#define LV_ID(id, f, c) if (flags == (f) && cf32 == (c)) return id;
+  LEAN_VARIANTS(LV_ID)
+#undef LV_ID
+  return 0;
+}
+template <int SC>
+__device__ __forceinline__ void lean_pass8_dispatch(int id, const Lean& e, int z, int rbase, int M, int N, int cbase,
+                                                    uint32_t stage, int lane) {
+  switch (id) {
+#define LV_CASE(i, f, c) case i: lean_pass8<(f), (c), SC>(e, z, rbase, M, N, cbase, stage, lane); break;
+    LEAN_VARIANTS(LV_CASE)
+#undef LV_CASE
+    default: break;
+  }
+}
+__device__ __forceinline__ void lean_rows16_dispatch(int id, const Lean& e, int64_t lo, int col0, int N,
+                                                     const uint32_t* v) {
+  switch (id) {
+#define LV_CASE(i, f, c) case i: lean_rows16<(f), (c)>(e, lo, col0, N, v); break;
+    LEAN_VARIANTS(LV_CASE)
+#undef LV_CASE
+    default: break;
+  }
+}
+
 template <int TILE>
 __device__ __forceinline__ void load_operand(const CUtensorMap* map, const OpMap& om, uint32_t dst, int mn0, int k,
                                              int z, uint32_t mbar) {
@@ -283,6 +559,7 @@ __global__ void __launch_bounds__(320, 1)
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(smem_u32(empty + s), ph ^ 1);
+          if (p.trace && blockIdx.x == 0 && it < 64) p.trace[it] = clock64();
           const uint32_t fb = smem_u32(full + s);
           mbar_expect_tx(fb, A_BYTES + B_BYTES);
           const int k = (kb0 + i) * BK;
@@ -305,12 +582,14 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t aph = (li >> 1) & 1;
         mbar_wait(smem_u32(tempty + ab), aph ^ 1);      // epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;");
+        if (p.trace && blockIdx.x == 0 && li < 64) p.trace[64 + li] = clock64();
         const uint32_t dacc = tmem + (uint32_t)(ab * BN);
         for (int i = 0; i < nk; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(smem_u32(full + s), ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
+          if (p.trace && blockIdx.x == 0 && it < 64) p.trace[128 + it] = clock64();
           const uint32_t ab_ = smem_u32(sA + s * A_BYTES), bb_ = smem_u32(sB + s * B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
@@ -325,12 +604,13 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else {
     // ---------------- epilogue warps 2..9: warp w reads TMEM lanes [32 (w % 4), +32) (hardware rule)
-    // and column half hh of the accumulator; 8 warps give the epilogue enough loads in flight.
+    // and column half hh of the accumulator; 8 warps keep enough stores / loads in flight.
     const int q4 = warp & 3;
     const int hh = (warp - 2) >> 2;
     constexpr int HC = BN / 2;                 // columns per warp
-    float* stage = stage_all + (warp - 2) * 32 * SROW;
+    const uint32_t stage = smem_u32(stage_all) + (uint32_t)((warp - 2) * 32 * SROW * 4);
     const Gemm& g = p.g;
+    const Lean& e = p.ep;
     int li = 0;
     for (int item = blockIdx.x; item < total; item += gridDim.x, ++li) {
       int m0, n0, z, sp, kb0, nk;
@@ -339,13 +619,15 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t aph = (li >> 1) & 1;
       mbar_wait(smem_u32(tfull + ab), aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
+      if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[192 + li] = clock64();
       const int rbase = m0 + q4 * 32;
       if (p.lanes_rows) {
         // column-contiguous output: row per lane straight from TMEM; consecutive lanes = consecutive addresses
         const int row = rbase + lane;
         const bool rok = row < g.M;
         RowBase rb;
-        if (rok) rb = row_base(g, z, row);
+        int64_t lo = 0;
+        if (rok) { if (p.lean) lo = lean_row(e, z, row); else rb = row_base(g, z, row); }
 #pragma unroll 1
         for (int c0 = hh * HC; c0 < hh * HC + HC; c0 += 16) {
           uint32_t v[16];
@@ -360,13 +642,24 @@ __global__ void __launch_bounds__(320, 1)
           if (c0 + 16 >= hh * HC + HC) {
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty + ab)) : "memory");
+            if (lane == 0) asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty + ab)) : "memory");
           }
           if (rok && n0 + c0 < g.N) {
+            if (p.lean_id > 0) {
+              lean_rows16_dispatch(p.lean_id, e, lo, n0 + c0, g.N, v);
+            } else if (p.lean) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int col = n0 + c0 + j;
-              if (col < g.N) epi_elem(g, rb, col, __uint_as_float(v[j]));
+              for (int j = 0; j < 16; ++j) {
+                const int col = n0 + c0 + j;
+                if (col < g.N)
+                  lean1(e, lo + (int64_t)col * e.cs, __uint_as_float(v[j]), (e.flags & EF_BIAS) ? lean_bias(e, col) : 0.f);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const int col = n0 + c0 + j;
+                if (col < g.N) epi_elem(g, rb, col, __uint_as_float(v[j]));
+              }
             }
           }
         }
@@ -376,90 +669,120 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll 1
       for (int pc = 0; pc < HC; pc += SC) {
 #pragma unroll 1
-      for (int c0 = 0; c0 < SC; c0 += 16) {
-        uint32_t v[16];
-        const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC + pc + c0);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        float4* dst = reinterpret_cast<float4*>(stage + lane * SROW + c0);
+        for (int c0 = 0; c0 < SC; c0 += 16) {
+          uint32_t v[16];
+          const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC + pc + c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                "=r"(v[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          const uint32_t dst = stage + (uint32_t)((lane * SROW + c0) * 4);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
-                               __uint_as_float(v[4 * j + 3]));
-      }
-      if (pc + SC >= HC) {
-        // accumulator fully read: hand it back to the MMA warp
-        asm volatile("tcgen05.fence::before_thread_sync;");
+          for (int j = 0; j < 4; ++j)
+            sts4(dst + 16 * j, __uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
+                 __uint_as_float(v[4 * j + 3]));
+        }
+        if (pc + SC >= HC) {
+          if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[256 + li] = clock64();
+          // accumulator fully read: hand it back to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty + ab)) : "memory");
+        }
         __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty + ab)) : "memory");
-      }
-      __syncwarp();
-      const int cbase = n0 + hh * HC + pc;
-      if (p.fast) {
-        constexpr int LPR = SC / 4;            // lanes per row (4 columns each)
-        constexpr int RPP = 32 / LPR;          // rows per pass
-        constexpr int U = 2;                   // passes whose loads are in flight together
-        const int sub = lane / LPR, cl = lane % LPR;
-        const int col = cbase + 4 * cl;
-        float bias4[4];
+        const int cbase = n0 + hh * HC + pc;
+        if (p.dbg == 1) {
+        } else if (p.lean_id > 0 && p.fast8) {
+          lean_pass8_dispatch<SC>(p.lean_id, e, z, rbase, g.M, g.N, cbase, stage, lane);
+        } else if (p.lean && p.fast) {
+          constexpr int LPR = SC / 4;          // lanes per row (4 columns each)
+          constexpr int RPP = 32 / LPR;        // rows per pass
+          const int sub = lane / LPR, cl = lane % LPR;
+          const int col = cbase + 4 * cl;
+          if (col < g.N) {                     // N % 4 == 0 in lean/fast mode: the 4 columns are all valid
+            float bias4[4] = {0.f, 0.f, 0.f, 0.f};
+            if (e.flags & EF_BIAS) {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) bias4[t] = (col + t < g.N) ? bias_at(g.e, col + t) : 0.f;
-        const bool full4 = col + 3 < g.N;
+              for (int t = 0; t < 4; ++t) bias4[t] = lean_bias(e, col + t);
+            }
+            const int f = e.flags;
+#pragma unroll 4
+            for (int r = sub; r < 32; r += RPP) {
+              const int row = rbase + r;
+              if (row >= g.M) break;
+              const int64_t o = lean_row(e, z, row) + col;
+              const float4 a4 = lds4(stage + (uint32_t)((r * SROW + 4 * cl) * 4));
+              float a[4] = {a4.x * e.alpha + bias4[0], a4.y * e.alpha + bias4[1], a4.z * e.alpha + bias4[2],
+                            a4.w * e.alpha + bias4[3]};
+              float t4[4];
+              if (f & EF_AUX) stg4(e.aux, o, 0, a);
+              if (f & EF_CROSS) {
+                ldg_bf4(e.x, o, t4);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) a[t] = t4[t] * a[t] + t4[t];
+              }
+              if (f & EF_RELU) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) a[t] = fmaxf(a[t], 0.f);
+              }
+              if (f & EF_MASK) {
+                ldg_bf4(e.mask, o, t4);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) a[t] = t4[t] > 0.f ? a[t] : 0.f;
+              }
+              if (f & EF_RESID) {
+                ldg_bf4(e.resid, o, t4);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) a[t] += t4[t];
+              }
+              if (f & EF_ACC) {
+                ldg_c4(e.c, o, e.c_f32, t4);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) a[t] += t4[t];
+              }
+              if (p.dbg == 2) { if (a[0] == 12345.f) stg4(e.c, o, e.c_f32, a); }
+              else stg4(e.c, o, e.c_f32, a);
+            }
+          }
+        } else if (p.dbg == 3) {
+          // debug: stores only
+          constexpr int LPR = SC / 4;
+          constexpr int RPP = 32 / LPR;
+          const int sub = lane / LPR, cl = lane % LPR;
+          const int col = cbase + 4 * cl;
+          float a[4] = {0.f, 0.f, 0.f, 0.f};
+          if (col < g.N)
+            for (int r = sub; r < 32; r += RPP) {
+              const int row = rbase + r;
+              if (row >= g.M) break;
+              stg4(e.c, (int64_t)row * e.rs + col, e.c_f32, a);
+            }
+        } else {
+          // generic path (split-K partials, irregular views)
+          const float* stg = stage_all + (warp - 2) * 32 * SROW;
 #pragma unroll 1
-        for (int r0 = 0; r0 < 32; r0 += RPP * U) {
-          RowBase rb[U];
-          Chunk4 k[U];
-          bool ok[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int r = r0 + u * RPP + sub;
+          for (int r = 0; r < 32; ++r) {
             const int row = rbase + r;
-            ok[u] = (r < 32) && (row < g.M) && (col < g.N);
-            if (ok[u]) {
-              rb[u] = row_base(g, z, row);
-              if (full4) epi4_load(g, rb[u], col, k[u]);
-            }
-          }
+            if (row >= g.M) break;
+            RowBase rb;
+            if (p.splits == 1) rb = row_base(g, z, row);
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (!ok[u]) continue;
-            const int r = r0 + u * RPP + sub;
-            const float4 a4 = *reinterpret_cast<const float4*>(stage + r * SROW + 4 * cl);
-            float a[4] = {a4.x, a4.y, a4.z, a4.w};
-            if (full4) {
-              epi4_store(g, rb[u], col, a, bias4, k[u]);
-            } else {
-#pragma unroll
-              for (int t = 0; t < 4; ++t)
-                if (col + t < g.N) epi_elem(g, rb[u], col + t, a[t]);
+            for (int q = 0; q < SC / 32; ++q) {
+              const int col = cbase + lane + 32 * q;
+              if (col < g.N) {
+                const float acc = stg[r * SROW + lane + 32 * q];
+                if (p.splits == 1) epi_elem(g, rb, col, acc);
+                else p.ws[((int64_t)(z * p.splits + sp) * g.M + row) * g.N + col] = acc;
+              }
             }
           }
         }
-      } else {
-#pragma unroll 1
-        for (int r = 0; r < 32; ++r) {
-          const int row = rbase + r;
-          if (row >= g.M) break;
-          RowBase rb;
-          if (p.splits == 1) rb = row_base(g, z, row);
-#pragma unroll
-          for (int q = 0; q < SC / 32; ++q) {
-            const int col = cbase + lane + 32 * q;
-            if (col < g.N) {
-              const float acc = stage[r * SROW + lane + 32 * q];
-              if (p.splits == 1) epi_elem(g, rb, col, acc);
-              else p.ws[((int64_t)(z * p.splits + sp) * g.M + row) * g.N + col] = acc;
-            }
-          }
-        }
+        __syncwarp();
       }
-      __syncwarp();
-      }
-      __syncwarp();
+      if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[320 + li] = clock64();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -536,6 +859,35 @@ static bool make_map(CUtensorMap* map, OpMap* om, const Operand& o, int rows, in
   return res == CUDA_SUCCESS;
 }
 
+static bool same_geom(const View& a, const View& c) {
+  return !a.ptr || (a.rs == c.rs && a.cs == c.cs && a.bs0 == c.bs0 && a.bs1 == c.bs1 && a.zdiv == c.zdiv &&
+                    a.rdiv == c.rdiv && a.rs_o == c.rs_o && a.dt == BF16);
+}
+// Resolve the epilogue to a Lean plan: all present views share C's geometry, operands other than C
+// are bf16, and row-major outputs have N % 4 == 0 with 4-element-aligned rows (vector accesses).
+static bool make_lean(const Gemm& g, Lean* e) {
+  const Epilogue& x = g.e;
+  if (!same_geom(x.cross, g.c) || !same_geom(x.aux, g.c) || !same_geom(x.mask, g.c) || !same_geom(x.resid, g.c))
+    return false;
+  if (x.bias && x.bias_dt != BF16) return false;
+  if (g.c.cs == 1 && (g.N % 4 || g.c.rs % 4 || g.c.bs0 % 4 || g.c.bs1 % 4 || g.c.rs_o % 4)) return false;
+  auto al = [](const void* p, int b) { return !p || ((uintptr_t)p % b) == 0; };
+  if (g.c.cs == 1 && (!al(g.c.ptr, g.c.dt == F32 ? 16 : 8) || !al(x.cross.ptr, 8) || !al(x.aux.ptr, 8) ||
+                      !al(x.mask.ptr, 8) || !al(x.resid.ptr, 8)))
+    return false;
+  e->c = g.c.ptr; e->x = x.cross.ptr; e->aux = x.aux.ptr; e->mask = x.mask.ptr; e->resid = x.resid.ptr;
+  e->bias = x.bias;
+  e->rs = g.c.rs; e->rs_o = g.c.rs_o; e->bs0 = g.c.bs0; e->bs1 = g.c.bs1; e->cs = g.c.cs;
+  e->rdiv = g.c.rdiv; e->zdiv = g.c.zdiv;
+  e->c_f32 = g.c.dt == F32;
+  e->alpha = x.alpha;
+  e->gap_lo = x.bias_gap_lo; e->gap_hi = x.bias_gap_hi;
+  e->flags = (x.accumulate ? EF_ACC : 0) | (x.relu ? EF_RELU : 0) | (x.mask.ptr ? EF_MASK : 0) |
+             (x.cross.ptr ? EF_CROSS : 0) | (x.aux.ptr ? EF_AUX : 0) | (x.resid.ptr ? EF_RESID : 0) |
+             (x.bias ? EF_BIAS : 0);
+  return true;
+}
+
 // a view can take 4-wide vector accesses: column-contiguous rows, every row / batch offset a multiple of 4
 // elements and a base aligned to 4 elements of its dtype
 static bool vec_ok(const View& v) {
@@ -595,9 +947,22 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   p.kb_per_split = (p.kblocks + splits - 1) / splits;
   p.splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;   // no empty splits
   p.ws = ws.ptr;
+  p.trace = g_gemm_trace;
+  { const char* e = getenv("DHEN_DBG_EPI"); p.dbg = e ? atoi(e) : 0; }
   p.zbase = 0;
   p.nz = g.batch;
   p.lanes_rows = (g.c.cs != 1 && g.c.rs == 1 && splits == 1) ? 1 : 0;
+  p.lean = (splits == 1 && make_lean(g, &p.ep)) ? 1 : 0;
+  p.lean_id = p.lean ? lean_variant(p.ep.flags, p.ep.c_f32 != 0) : 0;
+  p.fast8 = 0;
+  if (p.lean && g.c.cs == 1 && g.N % 8 == 0) {
+    auto al16 = [](const void* q) { return !q || ((uintptr_t)q % 16) == 0; };
+    const View* vs[5] = {&g.c, &g.e.cross, &g.e.aux, &g.e.mask, &g.e.resid};
+    bool ok = true;
+    for (const View* v : vs)
+      if (v->ptr && (!al16(v->ptr) || v->rs % 8 || v->bs0 % 8 || v->bs1 % 8 || v->rs_o % 8)) ok = false;
+    p.fast8 = ok ? 1 : 0;
+  }
   p.fast = (!p.lanes_rows && splits == 1 && vec_ok(g.c) && vec_ok(g.e.cross) && vec_ok(g.e.aux) &&
             vec_ok(g.e.resid) && vec_ok(g.e.mask)) ? 1 : 0;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a.mn_major << 15) | ((uint32_t)p.b.mn_major << 16) |

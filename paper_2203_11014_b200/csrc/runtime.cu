@@ -871,6 +871,8 @@ dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* Bp, v
 
 int dhen_debug_last_gemm_tc(void) { return g_last_gemm_tc; }
 
+void dhen_debug_gemm_trace(void* dev_buf) { g_gemm_trace = (long long*)dev_buf; }
+
 dhen_status dhen_profile(dhen_ctx* c, int enable) {
   if (!c) return fail(DHEN_E_STATE, "dhen_profile: ctx is NULL");
   c->prof = enable != 0;

@@ -11,7 +11,7 @@ import torch.nn.functional as F
 
 from oracle import dhen_oracle as O
 
-torch.set_default_dtype(torch.float64)
+
 RNG = np.random.default_rng(0)
 
 

@@ -43,6 +43,15 @@ def shapes(cfg):
          (d, mo * d), (0, 0), (d, m * d), bf),
         ("tokmix.wgrad", m, l, B * d, 1, (d, 1, 0, 0, 1, d, m * d), (d, 1, 0, 0, 1, d, mo * d), (l, 1, 0, 0, 1), 1,
          (0, 0), (0, 0), (0, 0), f32),
+        # experiments: same M, N, K as tokmix.fwd with plain layouts
+        ("x.kmaj_rowmajor", B * d, l, m, 1, (m, 1, 0, 0, 1, 0, 0), (m, 1, 0, 0, 1, 0, 0), (l, 1, 0, 0, 1), 0,
+         (0, 0), (0, 0), (0, 0), f32),
+        ("x.kmaj_n128", B * d, 128, m, 1, (m, 1, 0, 0, 1, 0, 0), (m, 1, 0, 0, 1, 0, 0), (128, 1, 0, 0, 1), 0,
+         (0, 0), (0, 0), (0, 0), bf),
+        ("x.kmaj_k256", B * d // 4, 128, 256, 1, (256, 1, 0, 0, 1, 0, 0), (256, 1, 0, 0, 1, 0, 0), (128, 1, 0, 0, 1), 0,
+         (0, 0), (0, 0), (0, 0), bf),
+        ("x.mnA_rowmajor", B * d, l, m, 1, (1, d, 0, 0, 1, 0, 0), (1, l, 0, 0, 1, 0, 0), (l, 1, 0, 0, 1), 0,
+         (d, m * d), (0, 0), (0, 0), f32),
     ]
 
 
@@ -59,6 +68,8 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--path", type=int, default=0)
+    ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--flush", default="write", choices=["write", "read", "none"])
     args = ap.parse_args()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -74,12 +85,30 @@ def main():
         tc = debug_gemm(q, A, Bm, Cm, path=args.path, ws=ws)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.iters)]
         for e0, e1 in ev:
-            flush.zero_()
+            if args.flush == "write":
+                flush.zero_()
+            elif args.flush == "read":
+                flush_sum = flush.view(torch.int32).sum()  # noqa: F841  (read-only flush: clean lines)
             e0.record()
             debug_gemm(q, A, Bm, Cm, path=args.path, ws=ws)
             e1.record()
         torch.cuda.synchronize()
         ms = sorted(e0.elapsed_time(e1) for e0, e1 in ev)[len(ev) // 2]
+        if args.trace:
+            from paper_2203_11014_b200.binding import load
+            import ctypes
+            tr = torch.zeros(512, dtype=torch.int64, device="cuda")
+            load().dhen_debug_gemm_trace(ctypes.c_void_p(tr.data_ptr()))
+            flush.zero_()
+            debug_gemm(q, A, Bm, Cm, path=args.path, ws=ws)
+            torch.cuda.synchronize()
+            load().dhen_debug_gemm_trace(None)
+            t = tr.cpu().tolist()
+            t0 = min(x for x in t if x > 0)
+            names = ["load_issue", "mma_start", "data_ready", "epi_start", "tmem_read", "epi_end", "arrived"]
+            for i in range(16):
+                print("  item/iter %2d: " % i + " ".join(f"{nm}={(t[64 * k + i] - t0) if t[64 * k + i] else -1:7d}"
+                                                      for k, nm in enumerate(names)))
         fl = 2.0 * M * N * K * Z
         es_c = 4 if cdt == torch.float32 else 2
         byts = A.numel() * 2 + Bm.numel() * 2 + M * N * Z * es_c * (2 if acc else 1)
