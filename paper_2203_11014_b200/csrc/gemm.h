@@ -54,7 +54,8 @@ struct Epilogue {
   float alpha = 1.f;
   const void* bias = nullptr;   // indexed by j, dtype bias_dt
   int bias_dt = F32;
-  int bias_gap_lo = 0, bias_gap_hi = 0;   // j in [lo, hi) -> no bias; j >= hi -> bias[j - (hi - lo)]
+  int bias_gap_lo = 0, bias_gap_hi = 0;   // j in [lo, hi) -> no bias; j >= hi -> bias[j - hi + bias_hi_off]
+  int bias_hi_off = 0;                    // where column hi's bias lives (relative to bias)
   int relu = 0;
   View mask = noview();         // out *= (mask > 0)           (ReLU backward)
   View cross = noview();        // DCN: aux <- out; out = x * out + x

@@ -13,7 +13,7 @@ static __device__ __forceinline__ void epi_apply(const Gemm& g, int z, int i, in
     bool has = true;
     if (e.bias_gap_hi > e.bias_gap_lo) {
       if (j >= e.bias_gap_lo && j < e.bias_gap_hi) has = false;
-      else if (j >= e.bias_gap_hi) bj = j - (e.bias_gap_hi - e.bias_gap_lo);
+      else if (j >= e.bias_gap_hi) bj = j - e.bias_gap_hi + e.bias_hi_off;
     }
     if (has) v += ld_as_f32(e.bias, bj, e.bias_dt);
   }

@@ -48,7 +48,7 @@ struct Lean {
   const void* bias;
   int64_t rs, rs_o, bs0, bs1, cs;
   int rdiv, zdiv;
-  int c_f32, flags, gap_lo, gap_hi;
+  int c_f32, flags, gap_lo, gap_hi, hi_off;
   float alpha;
 };
 
@@ -154,7 +154,7 @@ __device__ __forceinline__ float bias_at(const Epilogue& e, int j) {
   if (!e.bias) return 0.f;
   if (e.bias_gap_hi > e.bias_gap_lo) {
     if (j >= e.bias_gap_lo && j < e.bias_gap_hi) return 0.f;
-    if (j >= e.bias_gap_hi) j -= e.bias_gap_hi - e.bias_gap_lo;
+    if (j >= e.bias_gap_hi) j = j - e.bias_gap_hi + e.bias_hi_off;
   }
   return ld_as_f32(e.bias, j, e.bias_dt);
 }
@@ -301,7 +301,7 @@ __device__ __forceinline__ int64_t lean_row(const Lean& e, int z, int row) {
 __device__ __forceinline__ float lean_bias(const Lean& e, int j) {
   if (e.gap_hi > e.gap_lo) {
     if (j >= e.gap_lo && j < e.gap_hi) return 0.f;
-    if (j >= e.gap_hi) j -= e.gap_hi - e.gap_lo;
+    if (j >= e.gap_hi) j = j - e.gap_hi + e.hi_off;
   }
   return ldg_bf1(e.bias, j);
 }
@@ -881,7 +881,7 @@ static bool make_lean(const Gemm& g, Lean* e) {
   e->rdiv = g.c.rdiv; e->zdiv = g.c.zdiv;
   e->c_f32 = g.c.dt == F32;
   e->alpha = x.alpha;
-  e->gap_lo = x.bias_gap_lo; e->gap_hi = x.bias_gap_hi;
+  e->gap_lo = x.bias_gap_lo; e->gap_hi = x.bias_gap_hi; e->hi_off = x.bias_hi_off;
   e->flags = (x.accumulate ? EF_ACC : 0) | (x.relu ? EF_RELU : 0) | (x.mask.ptr ? EF_MASK : 0) |
              (x.cross.ptr ? EF_CROSS : 0) | (x.aux.ptr ? EF_AUX : 0) | (x.resid.ptr ? EF_RESID : 0) |
              (x.bias ? EF_BIAS : 0);

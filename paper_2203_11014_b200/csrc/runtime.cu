@@ -62,7 +62,7 @@ struct Mod {
   int off_tok = 0;   // token offset of this module's outputs in the concat
   // parameter offsets inside the layer group (canonical order)
   int64_t W = -1, b = -1, Wu = -1, Wm = -1, K = -1;
-  int64_t Wq = -1, Wo = -1, bq = -1, bo = -1, g1 = -1, be1 = -1, g2 = -1, be2 = -1, W1 = -1, b1 = -1, W2 = -1, b2 = -1;
+  int64_t Wq = -1, Wo = -1, bq = -1, bv = -1, bo = -1, g1 = -1, be1 = -1, g2 = -1, be2 = -1, W1 = -1, b1 = -1, W2 = -1, b2 = -1;
   // saved activations (work)
   void *Z = nullptr, *A = nullptr, *T = nullptr, *QKV = nullptr, *P = nullptr, *O = nullptr, *R1 = nullptr,
        *Z1 = nullptr, *F = nullptr, *R2 = nullptr, *h1 = nullptr, *h2 = nullptr;
@@ -75,7 +75,9 @@ struct Group {
   void* comp = nullptr;                 // dtype copy [shard] (full when world == 1 / DP)
   float* grad = nullptr;                // fp32 [npad] full gradient (accumulated in bwd)
   float* gshard = nullptr;              // fp32 [shard] reduced gradient shard (world > 1)
-  std::vector<int64_t> toff, tn;        // tensors: offset, numel
+  std::vector<int64_t> toff, tn;        // tensors: internal offset (64-element aligned), numel
+  std::vector<int64_t> tcanon;          // tensors: offset in the dense canonical order (params_io)
+  int64_t ncanon = 0;                   // canonical (dense) numel
   std::vector<int> tinit;               // 0 uniform, 1 ones, 2 zeros
   std::vector<float> tbound;
 };
@@ -133,6 +135,7 @@ struct dhen_ctx {
   size_t red_bytes = 0;
   Workspace ws;
   float *pooled = nullptr, *z = nullptr, *lossb = nullptr, *dz = nullptr;
+  float* gtmp = nullptr;    // fp32 [max_npad]: all-gather target of params_io / grads_get (world > 1)
   ncclComm_t comm = nullptr;
   unsigned long long launches0 = 0;
   // per-op device timing (dhen_profile): event pairs on the launch stream
@@ -221,9 +224,13 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
     for (int i = 0; i < lc.n_modules; ++i) mo += lc.modules[i].l;
     Lr.m_out = mo;
     int64_t off = 0;
+    int64_t coff = 0;
     auto tensor = [&](int64_t numel, int init, int fan) {
+      off = (off + 63) / 64 * 64;   // every tensor starts 128-B aligned (TMA / vector access)
       int64_t o = off;
       g.toff.push_back(off);
+      g.tcanon.push_back(coff);
+      coff += numel;
       g.tn.push_back(numel);
       g.tinit.push_back(init);
       g.tbound.push_back(fan > 0 ? 1.f / sqrtf((float)fan) : 0.f);
@@ -253,7 +260,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
           int f = md.s.ffn_mult * d;
           md.Wq = tensor((int64_t)d * d, 0, d); tensor((int64_t)d * d, 0, d); tensor((int64_t)d * d, 0, d);
           md.Wo = tensor((int64_t)d * d, 0, d);
-          md.bq = tensor(d, 0, d); tensor(d, 0, d); md.bo = tensor(d, 0, d);
+          md.bq = tensor(d, 0, d); md.bv = tensor(d, 0, d); md.bo = tensor(d, 0, d);
           md.g1 = tensor(d, 1, 0); md.be1 = tensor(d, 2, 0); md.g2 = tensor(d, 1, 0); md.be2 = tensor(d, 2, 0);
           md.W1 = tensor((int64_t)f * d, 0, d); md.b1 = tensor(f, 0, d); md.W2 = tensor((int64_t)d * f, 0, f); md.b2 = tensor(d, 0, f);
           md.Wu = tensor((int64_t)m * l, 0, m);
@@ -273,15 +280,18 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
     Lr.gamma = tensor(d, 1, 0);
     Lr.beta = tensor(d, 2, 0);
     g.n = off;
+    g.ncanon = coff;
     m = mo;
     m_max = std::max(m_max, mo);
     m_out_max = std::max(m_out_max, mo);
   }
   {  // head group (R17)
     Group& g = c->G[c->cfg.n_layers];
-    g.toff = {0, d}; g.tn = {d, 1}; g.tinit = {0, 0};
+    const int64_t bo = (d + 63) / 64 * 64;
+    g.toff = {0, bo}; g.tn = {d, 1}; g.tinit = {0, 0}; g.tcanon = {0, d};
     g.tbound = {1.f / sqrtf((float)d), 1.f / sqrtf((float)d)};
-    g.n = d + 1;
+    g.n = bo + 1;
+    g.ncanon = d + 1;
   }
   // sizes of every group, then state memory
   c->max_npad = 0;
@@ -296,6 +306,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
     g.gshard = world > 1 ? (float*)state.take(g.shard * 4) : nullptr;
   }
   if (shard) { c->gathered[0] = state.take(c->max_npad * es); c->gathered[1] = state.take(c->max_npad * es); }
+  if (world > 1) c->gtmp = (float*)state.take(c->max_npad * 4);
   // saved activations (work)
   m = c->cfg.m0;
   for (int n = 0; n < c->cfg.n_layers; ++n) {
@@ -494,6 +505,7 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         char* QKV = (char*)md.QKV;
         Gemm q = mk((int)rows, 3 * d, d, 1, operand(X, dt, d, 1), operand(p(md.Wq), dt, d, 1), view(QKV, dt, s3, 1));
         q.e.bias = p(md.bq); q.e.bias_dt = dt; q.e.bias_gap_lo = d; q.e.bias_gap_hi = 2 * d;   // no key bias (R10)
+        q.e.bias_hi_off = (int)(md.bv - md.bq);
         RET(G_(q, c, st, "attn.qkv"));
         Gemm s = mk(mi, mi, dh, B * H, operand(QKV, dt, s3, 1, mi * s3, dh, H),
                     operand(QKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H),
@@ -665,7 +677,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         gw.e.accumulate = 1;
         RET(G_(gw, c, st, "attn.qkv_wgrad"));
         KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dQKV, dt, rows, d, s3, gp(md.bq), c->red, c->red_bytes, st));
-        KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dQKV + 2 * (int64_t)d * es, dt, rows, d, s3, gp(md.bq) + d, c->red, c->red_bytes, st));
+        KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dQKV + 2 * (int64_t)d * es, dt, rows, d, s3, gp(md.bv), c->red, c->red_bytes, st));
         break;
       }
       case DHEN_MLP: {   // B9
@@ -710,8 +722,8 @@ static dhen_status head(dhen_ctx* c, const void* YN, int mN, const float* labels
   RET(comp_params(c, gi, st, &pbase));
   PP p{(char*)pbase, c->es};
   Group& G = c->G[gi];
-  KT("head", 0, (double)B * mN * c->d * c->es * (do_bwd ? 2 : 1), head_fwd_bwd(YN, p(0), p(c->d), c->dt, labels, B, mN, c->d, Bg, dY, c->dt, c->pooled, c->z, c->lossb, c->dz, loss,
-                  G.grad, G.grad + c->d, do_bwd, st));
+  KT("head", 0, (double)B * mN * c->d * c->es * (do_bwd ? 2 : 1), head_fwd_bwd(YN, p(0), p(G.toff[1]), c->dt, labels, B, mN, c->d, Bg, dY, c->dt, c->pooled, c->z, c->lossb, c->dz, loss,
+                  G.grad, G.grad + G.toff[1], do_bwd, st));
   if (do_bwd) RET(reduce_grads(c, gi, st));
   return DHEN_OK;
 }
@@ -766,7 +778,7 @@ dhen_status dhen_group_numel(const dhen_config* cfg, const dhen_dist* dist, int 
   Carver s(nullptr), w(nullptr);
   plan(&c, s, w);
   if (group < 0 || group > cfg->n_layers) return fail(DHEN_E_SHAPE, "dhen_group_numel: group=%d of %d", group, cfg->n_layers + 1);
-  if (numel) *numel = (size_t)c.G[group].n;
+  if (numel) *numel = (size_t)c.G[group].ncanon;
   if (shard) *shard = (size_t)c.G[group].shard;
   return DHEN_OK;
 }
@@ -987,6 +999,31 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
   return DHEN_OK;
 }
 
+// The library keeps every tensor 128-B aligned inside its group (internal layout); the
+// caller sees the dense canonical order.  These copy between the two through a host buffer.
+static void to_internal(const Group& g, const float* canon, std::vector<float>& pad) {
+  pad.assign((size_t)g.npad, 0.f);
+  for (size_t t = 0; t < g.toff.size(); ++t)
+    memcpy(pad.data() + g.toff[t], canon + g.tcanon[t], (size_t)g.tn[t] * 4);
+}
+static void to_canonical(const Group& g, const float* pad, float* canon) {
+  for (size_t t = 0; t < g.toff.size(); ++t)
+    memcpy(canon + g.tcanon[t], pad + g.toff[t], (size_t)g.tn[t] * 4);
+}
+// full (all ranks) internal vector of a sharded fp32 buffer -> host
+static dhen_status gather_f32(dhen_ctx* c, Group& g, const float* shard_or_full, std::vector<float>& pad,
+                              cudaStream_t st) {
+  pad.assign((size_t)g.npad, 0.f);
+  if (c->dist.world > 1 && c->dist.fsdp) {
+    NK(ncclAllGather(shard_or_full, c->gtmp, (size_t)g.shard, ncclFloat32, c->comm, st));
+    CK(cudaMemcpyAsync(pad.data(), c->gtmp, (size_t)g.npad * 4, cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(cudaMemcpyAsync(pad.data(), shard_or_full, (size_t)g.n * 4, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return DHEN_OK;
+}
+
 dhen_status dhen_params_io(dhen_ctx* c, int gi, float* host, int set, void* stream) {
   if (!c) return fail(DHEN_E_STATE, "dhen_params_io: ctx is NULL");
   if (gi < 0 || gi > c->cfg.n_layers) return fail(DHEN_E_SHAPE, "dhen_params_io: group=%d", gi);
@@ -995,23 +1032,16 @@ dhen_status dhen_params_io(dhen_ctx* c, int gi, float* host, int set, void* stre
   cudaStream_t st = S(stream);
   const bool sh = c->dist.world > 1 && c->dist.fsdp;
   const int64_t lo = sh ? (int64_t)c->dist.rank * g.shard : 0;
+  std::vector<float> pad;
   if (set) {
-    CK(cudaMemsetAsync(g.master, 0, g.shard * 4, st));
-    int64_t n = std::min<int64_t>(g.shard, std::max<int64_t>(0, g.n - lo));
-    if (n > 0) CK(cudaMemcpyAsync(g.master, host + lo, n * 4, cudaMemcpyHostToDevice, st));
+    to_internal(g, host, pad);
+    CK(cudaMemcpyAsync(g.master, pad.data() + lo, (size_t)g.shard * 4, cudaMemcpyHostToDevice, st));
     CK(sgd_cast(g.master, nullptr, 0.f, g.comp, c->dt, g.shard, st));
     invalidate_gathered(c);
     CK(cudaStreamSynchronize(st));
   } else {
-    if (sh) {
-      NK(ncclAllGather(g.master, g.grad, (size_t)g.shard, ncclFloat32, c->comm, st));   // grad buffer as temp
-      CK(cudaMemcpyAsync(host, g.grad, g.n * 4, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      CK(cudaMemsetAsync(g.grad, 0, g.npad * 4, st));
-    } else {
-      CK(cudaMemcpyAsync(host, g.master, g.n * 4, cudaMemcpyDeviceToHost, st));
-    }
-    CK(cudaStreamSynchronize(st));
+    RET(gather_f32(c, g, g.master, pad, st));
+    to_canonical(g, pad.data(), host);
   }
   return DHEN_OK;
 }
@@ -1022,17 +1052,9 @@ dhen_status dhen_grads_get(dhen_ctx* c, int gi, float* host, void* stream) {
   if (!host) return fail(DHEN_E_ALIGN, "dhen_grads_get: host is NULL");
   Group& g = c->G[gi];
   cudaStream_t st = S(stream);
-  if (c->dist.world > 1 && c->dist.fsdp) {
-    void* tmp = c->ws.ptr;   // split-K workspace as temp (>= npad floats checked below)
-    if ((size_t)g.npad * 4 > c->ws.bytes) return fail(DHEN_E_NOMEM, "dhen_grads_get: group too large for temp");
-    NK(ncclAllGather(g.gshard, tmp, (size_t)g.shard, ncclFloat32, c->comm, st));
-    CK(cudaMemcpyAsync(host, tmp, g.n * 4, cudaMemcpyDeviceToHost, st));
-  } else if (c->dist.world > 1) {
-    CK(cudaMemcpyAsync(host, g.gshard, g.n * 4, cudaMemcpyDeviceToHost, st));
-  } else {
-    CK(cudaMemcpyAsync(host, g.grad, g.n * 4, cudaMemcpyDeviceToHost, st));
-  }
-  CK(cudaStreamSynchronize(st));
+  std::vector<float> pad;
+  RET(gather_f32(c, g, c->dist.world > 1 ? g.gshard : g.grad, pad, st));
+  to_canonical(g, pad.data(), host);
   return DHEN_OK;
 }
 
