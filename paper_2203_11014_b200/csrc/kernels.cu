@@ -52,6 +52,209 @@ cudaError_t sym_from_triu(const void* dZ, void* S, int dt, int B, int m, int64_t
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ vector IO helpers
+template <int VEC, typename T> struct VIO;
+template <> struct VIO<8, __nv_bfloat16> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16* p, float* o) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) { o[2 * t] = __uint_as_float(w[t] << 16); o[2 * t + 1] = __uint_as_float(w[t] & 0xffff0000u); }
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float* v) {
+    uint4 u;
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]),
+                   h2 = __floats2bfloat162_rn(v[4], v[5]), h3 = __floats2bfloat162_rn(v[6], v[7]);
+    u.x = *reinterpret_cast<uint32_t*>(&h0); u.y = *reinterpret_cast<uint32_t*>(&h1);
+    u.z = *reinterpret_cast<uint32_t*>(&h2); u.w = *reinterpret_cast<uint32_t*>(&h3);
+    *reinterpret_cast<uint4*>(p) = u;
+  }
+};
+template <> struct VIO<4, __nv_bfloat16> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16* p, float* o) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    o[0] = __uint_as_float(u.x << 16); o[1] = __uint_as_float(u.x & 0xffff0000u);
+    o[2] = __uint_as_float(u.y << 16); o[3] = __uint_as_float(u.y & 0xffff0000u);
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float* v) {
+    uint2 u;
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]);
+    u.x = *reinterpret_cast<uint32_t*>(&h0); u.y = *reinterpret_cast<uint32_t*>(&h1);
+    *reinterpret_cast<uint2*>(p) = u;
+  }
+};
+template <> struct VIO<2, __nv_bfloat16> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16* p, float* o) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
+    o[0] = __uint_as_float(u << 16); o[1] = __uint_as_float(u & 0xffff0000u);
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float* v) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v[0], v[1]);
+    *reinterpret_cast<__nv_bfloat162*>(p) = h;
+  }
+};
+template <> struct VIO<1, __nv_bfloat16> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16* p, float* o) { o[0] = __bfloat162float(*p); }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float* v) { *p = __float2bfloat16_rn(v[0]); }
+};
+template <int VEC> struct VIO<VEC, float> {
+  static __device__ __forceinline__ void ld(const float* p, float* o) {
+    if constexpr (VEC % 4 == 0) {
+#pragma unroll
+      for (int t = 0; t < VEC; t += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(p + t);
+        o[t] = v.x; o[t + 1] = v.y; o[t + 2] = v.z; o[t + 3] = v.w;
+      }
+    } else if constexpr (VEC == 2) {
+      const float2 v = *reinterpret_cast<const float2*>(p);
+      o[0] = v.x; o[1] = v.y;
+    } else {
+      o[0] = *p;
+    }
+  }
+  static __device__ __forceinline__ void st(float* p, const float* v) {
+    if constexpr (VEC % 4 == 0) {
+#pragma unroll
+      for (int t = 0; t < VEC; t += 4) *reinterpret_cast<float4*>(p + t) = make_float4(v[t], v[t + 1], v[t + 2], v[t + 3]);
+    } else if constexpr (VEC == 2) {
+      *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    } else {
+      *p = v[0];
+    }
+  }
+};
+
+// ------------------------------------------------------------------ LayerNorm (vectorised)
+// One warp per row of d; lane owns NCH chunks of VEC consecutive elements: element (j*32 + lane)*VEC.
+template <typename T, int VEC, int NCH>
+__global__ void __launch_bounds__(256) ln_fwd_v(const float* __restrict__ U, const T* __restrict__ addx,
+                                                const T* __restrict__ gamma, const T* __restrict__ beta, float eps,
+                                                int64_t rows, int d, T* __restrict__ Y, T* __restrict__ Rsave,
+                                                float* __restrict__ mu, float* __restrict__ rstd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
+    float v[NCH][VEC];
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c = (j * 32 + lane) * VEC;
+      VIO<VEC, float>::ld(U + r * d + c, v[j]);
+      if (addx) {
+        float x[VEC];
+        VIO<VEC, T>::ld(addx + r * d + c, x);
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) v[j][t] += x[t];
+      }
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) s += v[j][t];
+    }
+    const float mean = warp_sum(s) / d;
+    float s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j)
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) { const float q = v[j][t] - mean; s2 += q * q; }
+    const float rs = rsqrtf(warp_sum(s2) / d + eps);
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c = (j * 32 + lane) * VEC;
+      float g[VEC], b[VEC], y[VEC];
+      VIO<VEC, T>::ld(gamma + c, g);
+      VIO<VEC, T>::ld(beta + c, b);
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) y[t] = (v[j][t] - mean) * rs * g[t] + b[t];
+      VIO<VEC, T>::st(Y + r * d + c, y);
+      if (Rsave) VIO<VEC, T>::st(Rsave + r * d + c, v[j]);
+    }
+    if (lane == 0) { mu[r] = mean; rstd[r] = rs; }
+  }
+}
+
+template <typename TD, typename T, int VEC, int NCH>
+__global__ void __launch_bounds__(256) ln_bwd_v(const TD* __restrict__ dY, const T* __restrict__ Rsave,
+                                                const float* __restrict__ mu, const float* __restrict__ rstd,
+                                                const T* __restrict__ gamma, int64_t rows, int d, T* __restrict__ dR,
+                                                float* __restrict__ acc, int acc_mode, float* __restrict__ part,
+                                                int64_t rows_per_block) {
+  extern __shared__ float sred[];   // [8 warps][2][d]
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  const int64_t r0 = blockIdx.x * rows_per_block, r1 = min(rows, r0 + rows_per_block);
+  float pg[NCH][VEC], pb[NCH][VEC], g[NCH][VEC];
+#pragma unroll
+  for (int j = 0; j < NCH; ++j) {
+    VIO<VEC, T>::ld(gamma + (j * 32 + lane) * VEC, g[j]);
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) { pg[j][t] = 0.f; pb[j][t] = 0.f; }
+  }
+  for (int64_t r = r0 + w; r < r1; r += 8) {
+    float xh[NCH][VEC], gy[NCH][VEC];
+    float s1 = 0.f, s2 = 0.f;
+    const float m_ = mu[r], rs = rstd[r];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c = (j * 32 + lane) * VEC;
+      float dy[VEC], x[VEC];
+      VIO<VEC, TD>::ld(dY + r * d + c, dy);
+      VIO<VEC, T>::ld(Rsave + r * d + c, x);
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) {
+        xh[j][t] = (x[t] - m_) * rs;
+        gy[j][t] = dy[t] * g[j][t];
+        pg[j][t] += dy[t] * xh[j][t];
+        pb[j][t] += dy[t];
+        s1 += gy[j][t];
+        s2 += gy[j][t] * xh[j][t];
+      }
+    }
+    s1 = warp_sum(s1) / d;
+    s2 = warp_sum(s2) / d;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c = (j * 32 + lane) * VEC;
+      float o[VEC];
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) o[t] = rs * (gy[j][t] - s1 - xh[j][t] * s2);
+      VIO<VEC, T>::st(dR + r * d + c, o);
+      if (acc_mode) {
+        float q[VEC];
+        VIO<VEC, T>::ld(dR + r * d + c, q);   // the stored (rounded) value feeds the residual path
+        if (acc_mode == 2) {
+          float a[VEC];
+          VIO<VEC, float>::ld(acc + r * d + c, a);
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) q[t] += a[t];
+        }
+        VIO<VEC, float>::st(acc + r * d + c, q);
+      }
+    }
+  }
+  // block reduction of the dgamma / dbeta partials in fixed warp order
+#pragma unroll
+  for (int j = 0; j < NCH; ++j) {
+    const int c = (j * 32 + lane) * VEC;
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) { sred[(w * 2) * d + c + t] = pg[j][t]; sred[(w * 2 + 1) * d + c + t] = pb[j][t]; }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float a = 0.f, b = 0.f;
+    for (int ww = 0; ww < 8; ++ww) { a += sred[(ww * 2) * d + c]; b += sred[(ww * 2 + 1) * d + c]; }
+    part[(int64_t)blockIdx.x * 2 * d + c] = a;
+    part[(int64_t)blockIdx.x * 2 * d + d + c] = b;
+  }
+}
+
+// (VEC, NCH) for a row length d; {0,0} = no vectorised variant (generic kernels)
+static inline void ln_shape(int d, int& vec, int& nch) {
+  vec = 0; nch = 0;
+  if (d % 256 == 0 && d / 256 <= 4) { vec = 8; nch = d / 256; }
+  else if (d % 128 == 0 && d / 128 <= 3) { vec = 4; nch = d / 128; }
+  else if (d % 64 == 0 && d / 64 <= 3) { vec = 2; nch = d / 64; }
+  else if (d % 32 == 0 && d / 32 <= 2) { vec = 1; nch = d / 32; }
+}
+#define LN_SHAPES(X) X(8, 1) X(8, 2) X(8, 3) X(8, 4) X(4, 1) X(4, 3) X(2, 1) X(2, 3) X(1, 1) X(1, 2)
+
 // ------------------------------------------------------------------ LayerNorm
 constexpr int LN_MAXQ_ALL = 32;  // d <= 1024
 
@@ -94,7 +297,7 @@ __global__ void ln_fwd_k(const float* U, const void* addx, const void* gamma, co
     if (lane == 0) { mu[r] = mean; rstd[r] = rs; }
   }
 }
-cudaError_t ln_fwd(const float* U, const void* addx, const void* gamma, const void* beta, int pdt, float eps,
+static cudaError_t ln_fwd_generic(const float* U, const void* addx, const void* gamma, const void* beta, int pdt, float eps,
                    int64_t rows, int d, void* Y, void* Rsave, float* mu, float* rstd, int dt, cudaStream_t st) {
   if (d > 32 * LN_MAXQ_ALL) return cudaErrorInvalidValue;
   const int nb = nblocks(rows, 8, 148 * 64);
@@ -175,7 +378,7 @@ __global__ void reduce_parts_k(const float* part, int nparts, int n, float* out0
   }
 }
 
-cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
+static cudaError_t ln_bwd_generic(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
                    const void* gamma, int pdt, int64_t rows, int d, void* dR, int dt, float* acc, int acc_mode,
                    float* dgamma, float* dbeta, float* scratch, size_t scratch_bytes, cudaStream_t st) {
   if (d > 32 * LN_MAXQ_ALL) return cudaErrorInvalidValue;
@@ -190,6 +393,67 @@ cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu,
     ln_bwd_k<8><<<nb, 256, 0, st>>>(dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, scratch, rpb);
   else
     ln_bwd_k<32><<<nb, 256, 0, st>>>(dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, scratch, rpb);
+  reduce_parts_k<<<nblocks(2 * d), 256, 0, st>>>(scratch, nb, d, dgamma, dbeta);
+  g_launches += 2;
+  return cudaGetLastError();
+}
+
+
+cudaError_t ln_fwd(const float* U, const void* addx, const void* gamma, const void* beta, int pdt, float eps,
+                   int64_t rows, int d, void* Y, void* Rsave, float* mu, float* rstd, int dt, cudaStream_t st) {
+  int vec, nch;
+  ln_shape(d, vec, nch);
+  if (!vec || pdt != dt) return ln_fwd_generic(U, addx, gamma, beta, pdt, eps, rows, d, Y, Rsave, mu, rstd, dt, st);
+  const int nb = nblocks(rows, 8, 148 * 64);
+#define LNF(V, N)                                                                                               \
+  if (vec == V && nch == N) {                                                                                   \
+    if (dt == BF16)                                                                                             \
+      ln_fwd_v<__nv_bfloat16, V, N><<<nb, 256, 0, st>>>(U, (const __nv_bfloat16*)addx, (const __nv_bfloat16*)gamma, \
+          (const __nv_bfloat16*)beta, eps, rows, d, (__nv_bfloat16*)Y, (__nv_bfloat16*)Rsave, mu, rstd);       \
+    else                                                                                                        \
+      ln_fwd_v<float, V, N><<<nb, 256, 0, st>>>(U, (const float*)addx, (const float*)gamma, (const float*)beta, eps, \
+          rows, d, (float*)Y, (float*)Rsave, mu, rstd);                                                        \
+  }
+  LN_SHAPES(LNF)
+#undef LNF
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
+                   const void* gamma, int pdt, int64_t rows, int d, void* dR, int dt, float* acc, int acc_mode,
+                   float* dgamma, float* dbeta, float* scratch, size_t scratch_bytes, cudaStream_t st) {
+  int vec, nch;
+  ln_shape(d, vec, nch);
+  if (!vec || pdt != dt)
+    return ln_bwd_generic(dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, dgamma, dbeta,
+                          scratch, scratch_bytes, st);
+  int nb = (int)std::min<int64_t>((rows + 63) / 64, 148 * 4);
+  nb = (int)std::min<int64_t>(nb, (int64_t)(scratch_bytes / (sizeof(float) * 2 * d)));
+  if (nb < 1) return cudaErrorInvalidValue;
+  int64_t rpb = (rows + nb - 1) / nb;
+  nb = (int)((rows + rpb - 1) / rpb);
+  const size_t sm = (size_t)16 * d * sizeof(float);
+  if (sm > 48 * 1024)
+    return ln_bwd_generic(dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, dgamma, dbeta,
+                          scratch, scratch_bytes, st);
+#define LNB(V, N)                                                                                                   \
+  if (vec == V && nch == N) {                                                                                       \
+    if (dt == BF16) {                                                                                               \
+      if (dydt == BF16)                                                                                             \
+        ln_bwd_v<__nv_bfloat16, __nv_bfloat16, V, N><<<nb, 256, sm, st>>>((const __nv_bfloat16*)dY,                 \
+            (const __nv_bfloat16*)Rsave, mu, rstd, (const __nv_bfloat16*)gamma, rows, d, (__nv_bfloat16*)dR, acc,   \
+            acc_mode, scratch, rpb);                                                                                \
+      else                                                                                                          \
+        ln_bwd_v<float, __nv_bfloat16, V, N><<<nb, 256, sm, st>>>((const float*)dY, (const __nv_bfloat16*)Rsave,    \
+            mu, rstd, (const __nv_bfloat16*)gamma, rows, d, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb);       \
+    } else {                                                                                                        \
+      ln_bwd_v<float, float, V, N><<<nb, 256, sm, st>>>((const float*)dY, (const float*)Rsave, mu, rstd,            \
+          (const float*)gamma, rows, d, (float*)dR, acc, acc_mode, scratch, rpb);                                   \
+    }                                                                                                               \
+  }
+  LN_SHAPES(LNB)
+#undef LNB
   reduce_parts_k<<<nblocks(2 * d), 256, 0, st>>>(scratch, nb, d, dgamma, dbeta);
   g_launches += 2;
   return cudaGetLastError();
@@ -219,8 +483,65 @@ __global__ void colsum_fin_k(const float* part, int nparts, int cols, float* out
     out[c] += s;
   }
 }
+// vectorised: thread (tx, ty) owns 8 consecutive columns tx*8.. of a 256-column slab and rows ty, ty+8, ...
+template <typename T>
+__global__ void __launch_bounds__(256) colsum8_part_k(const T* __restrict__ src, int64_t rows, int cols, int64_t ld,
+                                                      int64_t rpc, float* __restrict__ part) {
+  __shared__ float sm[8][257];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const int c = blockIdx.x * 256 + tx * 8;
+  const int64_t r0 = blockIdx.y * rpc, r1 = min(rows, r0 + rpc);
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c < cols) {
+    int64_t r = r0 + ty;
+    for (; r + 24 < r1; r += 32) {     // 4 independent loads in flight
+      float v0[8], v1[8], v2[8], v3[8];
+      VIO<8, T>::ld(src + r * ld + c, v0);
+      VIO<8, T>::ld(src + (r + 8) * ld + c, v1);
+      VIO<8, T>::ld(src + (r + 16) * ld + c, v2);
+      VIO<8, T>::ld(src + (r + 24) * ld + c, v3);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] += (v0[t] + v1[t]) + (v2[t] + v3[t]);
+    }
+    for (; r < r1; r += 8) {
+      float v0[8];
+      VIO<8, T>::ld(src + r * ld + c, v0);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] += v0[t];
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 8; ++t) sm[ty][tx * 8 + t] = a[t];
+  __syncthreads();
+  const int cc = blockIdx.x * 256 + threadIdx.x;
+  if (cc < cols) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += sm[k][threadIdx.x];
+    part[(int64_t)blockIdx.y * cols + cc] = t;
+  }
+}
+
 cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t ld, float* out, float* scratch,
                        size_t scratch_bytes, cudaStream_t st) {
+  const int es = dt == F32 ? 4 : 2;
+  if (cols % 8 == 0 && ld % 8 == 0 && ((uintptr_t)src % (8 * es)) == 0) {
+    const int cb = (cols + 255) / 256;
+    int64_t nch = std::max<int64_t>(1, std::min<int64_t>(rows / 64, std::max(1, 4 * 148 / cb)));
+    nch = std::min<int64_t>(nch, (int64_t)(scratch_bytes / (sizeof(float) * cols)));
+    if (nch >= 1) {
+      int64_t rpc = (rows + nch - 1) / nch;
+      nch = (rows + rpc - 1) / rpc;
+      if (nch < 1) nch = 1;
+      if (dt == F32)
+        colsum8_part_k<float><<<dim3(cb, (unsigned)nch), 256, 0, st>>>((const float*)src, rows, cols, ld, rpc, scratch);
+      else
+        colsum8_part_k<__nv_bfloat16><<<dim3(cb, (unsigned)nch), 256, 0, st>>>((const __nv_bfloat16*)src, rows, cols,
+                                                                                ld, rpc, scratch);
+      colsum_fin_k<<<nblocks(cols), 256, 0, st>>>(scratch, (int)nch, cols, out);
+      g_launches += 2;
+      return cudaGetLastError();
+    }
+  }
   int cb = (cols + 31) / 32;
   int64_t nch = std::max<int64_t>(1, std::min<int64_t>(rows / 256, std::max(1, 296 / cb)));
   nch = std::min<int64_t>(nch, (int64_t)(scratch_bytes / (sizeof(float) * cols)));
@@ -289,6 +610,141 @@ cudaError_t dcn_bwd_elem(const void* dT, const void* X, const void* A, void* dA,
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ conv, banded shared-memory stencils
+// Block = one sample b and a band of RB = 8 output rows; the band + halo rows of the input live in smem
+// (zero padded), each thread computes 8 consecutive outputs of one row.  d % 8 == 0, d <= 1024.
+constexpr int CV_RB = 8;
+template <typename T, int K, bool FLIP>
+__global__ void __launch_bounds__(256) conv_band_k(const T* __restrict__ in, const T* __restrict__ Kp, int C, int m,
+                                                   int d, T* __restrict__ outT, float* __restrict__ outAcc) {
+  constexpr int R = (K - 1) / 2;
+  extern __shared__ float band[];          // [(RB + 2R) rows][d + 2R]
+  __shared__ float kb[K * K];
+  const int b = blockIdx.y, i0 = blockIdx.x * CV_RB;
+  const int W = d + 2 * R;
+  for (int t = threadIdx.x; t < K * K; t += blockDim.x) {
+    float sacc = 0.f;
+    for (int c = 0; c < C; ++c) sacc += tof<T>(Kp[c * K * K + t]);
+    kb[t] = sacc / C;
+  }
+  const int rows_in = CV_RB + 2 * R;
+  for (int e = threadIdx.x; e < rows_in * (d / 8); e += blockDim.x) {
+    const int rr = e / (d / 8), cc = (e % (d / 8)) * 8;
+    const int gi = i0 - R + rr;
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (gi >= 0 && gi < m) VIO<8, T>::ld(in + ((int64_t)b * m + gi) * d + cc, v);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) band[rr * W + R + cc + t] = v[t];
+  }
+  for (int e = threadIdx.x; e < rows_in * 2 * R; e += blockDim.x) {   // zero the left / right halo columns
+    const int rr = e / (2 * R), q = e % (2 * R);
+    band[rr * W + (q < R ? q : d + q)] = 0.f;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < CV_RB * (d / 8); e += blockDim.x) {
+    const int ri = e / (d / 8), j0 = (e % (d / 8)) * 8;
+    const int gi = i0 + ri;
+    if (gi >= m) continue;
+    float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      const float* row = band + (ri + (FLIP ? 2 * R - a : a)) * W + j0;
+      float x[8 + 2 * R];
+#pragma unroll
+      for (int q = 0; q < 8 + 2 * R; ++q) x[q] = row[q];
+#pragma unroll
+      for (int e2 = 0; e2 < K; ++e2) {
+        const float kv = FLIP ? kb[a * K + e2] : kb[a * K + e2];
+        const int sh = FLIP ? 2 * R - e2 : e2;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) o[t] += kv * x[t + sh];
+      }
+    }
+    const int64_t off = ((int64_t)b * m + gi) * d + j0;
+    if (outAcc) {
+      float a8[8];
+      VIO<8, float>::ld(outAcc + off, a8);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a8[t] += o[t];
+      VIO<8, float>::st(outAcc + off, a8);
+    } else {
+      VIO<8, T>::st(outT + off, o);
+    }
+  }
+}
+
+// dK[a][e] partials: block = (band of sample b): sum over its outputs of dT[i][j] * X[i+a-R][j+e-R]
+template <typename T, int K>
+__global__ void __launch_bounds__(256) conv_wgrad_band_k(const T* __restrict__ dT, const T* __restrict__ X, int m,
+                                                         int d, float* __restrict__ part) {
+  constexpr int R = (K - 1) / 2;
+  extern __shared__ float band[];          // X band [(RB + 2R)][d + 2R]
+  __shared__ float red[K * K][8];
+  const int b = blockIdx.y, i0 = blockIdx.x * CV_RB;
+  const int W = d + 2 * R, rows_in = CV_RB + 2 * R;
+  for (int e = threadIdx.x; e < rows_in * (d / 8); e += blockDim.x) {
+    const int rr = e / (d / 8), cc = (e % (d / 8)) * 8;
+    const int gi = i0 - R + rr;
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (gi >= 0 && gi < m) VIO<8, T>::ld(X + ((int64_t)b * m + gi) * d + cc, v);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) band[rr * W + R + cc + t] = v[t];
+  }
+  for (int e = threadIdx.x; e < rows_in * 2 * R; e += blockDim.x) {
+    const int rr = e / (2 * R), q = e % (2 * R);
+    band[rr * W + (q < R ? q : d + q)] = 0.f;
+  }
+  __syncthreads();
+  float acc[K * K];
+#pragma unroll
+  for (int q = 0; q < K * K; ++q) acc[q] = 0.f;
+  for (int e = threadIdx.x; e < CV_RB * (d / 8); e += blockDim.x) {
+    const int ri = e / (d / 8), j0 = (e % (d / 8)) * 8;
+    const int gi = i0 + ri;
+    if (gi >= m) continue;
+    float g[8];
+    VIO<8, T>::ld(dT + ((int64_t)b * m + gi) * d + j0, g);
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      const float* row = band + (ri + a) * W + j0;
+      float x[8 + 2 * R];
+#pragma unroll
+      for (int q = 0; q < 8 + 2 * R; ++q) x[q] = row[q];
+#pragma unroll
+      for (int e2 = 0; e2 < K; ++e2)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[a * K + e2] += g[t] * x[t + e2];
+    }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+#pragma unroll
+  for (int q = 0; q < K * K; ++q) {
+    const float v = warp_sum(acc[q]);
+    if (lane == 0) red[q][w] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < K * K) {
+    float v = 0.f;
+    for (int ww = 0; ww < 8; ++ww) v += red[threadIdx.x][ww];
+    part[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * K * K + threadIdx.x] = v;
+  }
+}
+
+template <typename T, int K>
+static cudaError_t conv_band_launch(const void* in, const void* Kp, int C, int B, int m, int d, void* outT, float* outAcc,
+                                    bool flip, cudaStream_t st) {
+  constexpr int R = (K - 1) / 2;
+  const size_t sm = (size_t)(CV_RB + 2 * R) * (d + 2 * R) * sizeof(float);
+  dim3 grid((m + CV_RB - 1) / CV_RB, B);
+  if (flip)
+    conv_band_k<T, K, true><<<grid, 256, sm, st>>>((const T*)in, (const T*)Kp, C, m, d, (T*)outT, outAcc);
+  else
+    conv_band_k<T, K, false><<<grid, 256, sm, st>>>((const T*)in, (const T*)Kp, C, m, d, (T*)outT, outAcc);
+  ++g_launches;
+  return cudaGetLastError();
+}
+static bool conv_band_ok(int k, int d, int B) { return (k == 3 || k == 5) && d % 8 == 0 && d <= 1024 && B <= 65535; }
+
 // ------------------------------------------------------------------ conv (folded channel mean)
 constexpr int CONV_MAXK = 7;
 __device__ void load_kbar(const void* K, int pdt, int C, int k, float* kb) {
@@ -323,6 +779,12 @@ __global__ void conv_fwd_k(const void* X, const void* K, int pdt, int C, int k, 
 cudaError_t conv_fwd(const void* X, const void* K, int pdt, int C, int k, int B, int m, int d, void* T, int dt,
                      cudaStream_t st) {
   if (k > CONV_MAXK) return cudaErrorInvalidValue;
+  if (conv_band_ok(k, d, B) && pdt == dt) {
+    if (dt == BF16) return k == 3 ? conv_band_launch<__nv_bfloat16, 3>(X, K, C, B, m, d, T, nullptr, false, st)
+                                  : conv_band_launch<__nv_bfloat16, 5>(X, K, C, B, m, d, T, nullptr, false, st);
+    return k == 3 ? conv_band_launch<float, 3>(X, K, C, B, m, d, T, nullptr, false, st)
+                  : conv_band_launch<float, 5>(X, K, C, B, m, d, T, nullptr, false, st);
+  }
   conv_fwd_k<<<nblocks((int64_t)B * m * d), 256, 0, st>>>(X, K, pdt, C, k, B, m, d, T, dt);
   ++g_launches;
   return cudaGetLastError();
@@ -352,6 +814,12 @@ __global__ void conv_dgrad_k(const void* dT, const void* K, int pdt, int C, int 
 cudaError_t conv_dgrad(const void* dT, const void* K, int pdt, int C, int k, int B, int m, int d, float* acc, int dt,
                        cudaStream_t st) {
   if (k > CONV_MAXK) return cudaErrorInvalidValue;
+  if (conv_band_ok(k, d, B) && pdt == dt) {
+    if (dt == BF16) return k == 3 ? conv_band_launch<__nv_bfloat16, 3>(dT, K, C, B, m, d, nullptr, acc, true, st)
+                                  : conv_band_launch<__nv_bfloat16, 5>(dT, K, C, B, m, d, nullptr, acc, true, st);
+    return k == 3 ? conv_band_launch<float, 3>(dT, K, C, B, m, d, nullptr, acc, true, st)
+                  : conv_band_launch<float, 5>(dT, K, C, B, m, d, nullptr, acc, true, st);
+  }
   conv_dgrad_k<<<nblocks((int64_t)B * m * d), 256, 0, st>>>(dT, K, pdt, C, k, B, m, d, acc, dt);
   ++g_launches;
   return cudaGetLastError();
@@ -401,6 +869,22 @@ __global__ void conv_wgrad_fin_k(const float* part, int nparts, int C, int kk, f
 cudaError_t conv_wgrad(const void* dT, const void* X, int C, int k, int B, int m, int d, int dt, float* dK,
                        float* scratch, size_t scratch_bytes, cudaStream_t st) {
   if (k > CONV_MAXK) return cudaErrorInvalidValue;
+  const int nbx = (m + CV_RB - 1) / CV_RB;
+  if (conv_band_ok(k, d, B) && (size_t)nbx * B * k * k * sizeof(float) <= scratch_bytes) {
+    const int R = (k - 1) / 2;
+    const size_t sm = (size_t)(CV_RB + 2 * R) * (d + 2 * R) * sizeof(float);
+    dim3 grid(nbx, B);
+    if (dt == BF16) {
+      if (k == 3) conv_wgrad_band_k<__nv_bfloat16, 3><<<grid, 256, sm, st>>>((const __nv_bfloat16*)dT, (const __nv_bfloat16*)X, m, d, scratch);
+      else conv_wgrad_band_k<__nv_bfloat16, 5><<<grid, 256, sm, st>>>((const __nv_bfloat16*)dT, (const __nv_bfloat16*)X, m, d, scratch);
+    } else {
+      if (k == 3) conv_wgrad_band_k<float, 3><<<grid, 256, sm, st>>>((const float*)dT, (const float*)X, m, d, scratch);
+      else conv_wgrad_band_k<float, 5><<<grid, 256, sm, st>>>((const float*)dT, (const float*)X, m, d, scratch);
+    }
+    conv_wgrad_fin_k<<<1, 64, 0, st>>>(scratch, nbx * B, C, k * k, dK);
+    g_launches += 2;
+    return cudaGetLastError();
+  }
   int64_t total = (int64_t)B * m * d;
   int nb = (int)std::min<int64_t>(std::max<int64_t>(1, total / 4096), 148 * 4);
   nb = (int)std::min<int64_t>(nb, (int64_t)(scratch_bytes / (sizeof(float) * k * k)));

@@ -422,8 +422,8 @@ static dhen_status tokmix_fwd(dhen_ctx* c, const void* T, int m, const void* W, 
 static dhen_status tokmix_bwd(dhen_ctx* c, const void* T, int m, const void* W, int l, const void* dU, int64_t ldu,
                               void* dT, int dT_dt, int acc, float* gW, int B, cudaStream_t st) {
   const int d = c->d, dt = c->dt;
-  Gemm g = mk(B * d, m, l, 1, operand2(dU, dt, d, ldu, 1, d), operand(W, dt, l, 1),
-              view2(dT, dT_dt, d, (int64_t)m * d, 1, d));
+  // per-sample batched: dT_b = W dU_b (M = m rows i, N = d, K = l), row-major output
+  Gemm g = mk(m, d, l, B, operand(W, dt, l, 1), operand(dU, dt, 1, d, ldu), view(dT, dT_dt, d, 1, (int64_t)m * d));
   g.e.accumulate = acc;
   RET(G_(g, c, st, "tokmix.dgrad"));
   Gemm gw = mk(m, l, B * d, 1, operand(T, dt, d, 1, 0, 0, 1, d, (int64_t)m * d),

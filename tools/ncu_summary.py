@@ -1,0 +1,49 @@
+"""Summarise ncu outputs for profiles/.
+    python tools/ncu_summary.py launches <launches.csv>      -> per-kernel share of device time
+    python tools/ncu_summary.py full <report.ncu-rep>        -> key metrics of a --set full capture"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+
+def launches(path):
+    rows = [r for r in csv.reader(open(path)) if r]
+    hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[hdr_i]
+    ik, iv, im = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
+    agg = defaultdict(lambda: [0, 0.0])
+    for r in rows[hdr_i + 1:]:
+        if len(r) <= iv or r[im] != "gpu__time_duration.sum":
+            continue
+        name = r[ik].split("(")[0].replace("void ", "")
+        agg[name][0] += 1
+        agg[name][1] += float(r[iv].replace(",", ""))
+    tot = sum(v[1] for v in agg.values())
+    print(f"# ncu launch list (gpu__time_duration.sum, cold-cache, serialised): {sum(v[0] for v in agg.values())} launches, {tot/1e3:.1f} us total")
+    print(f"{'kernel':60s} {'launches':>8s} {'total_us':>10s} {'share':>7s}")
+    for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        print(f"{k[:60]:60s} {n:8d} {t/1e3:10.1f} {100*t/tot:6.1f}%")
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+            "sm__inst_executed_pipe_tensor.sum", "launch__registers_per_thread", "launch__grid_size",
+            "launch__block_size", "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "lts__t_bytes.sum", "smsp__inst_executed.sum"]
+    for r in rows[2:]:
+        print("---")
+        for h, u, v in zip(hdr, units, r):
+            if h in want or h.startswith("sm__pipe_tensor") and "pct" in h:
+                print(f"{h} [{u}] = {v}")
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
