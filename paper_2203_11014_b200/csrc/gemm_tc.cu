@@ -59,6 +59,7 @@ struct Params {
   int lean_id;      // >0: compile-time specialised pass (8 columns per lane / 16 per row-lane)
   OpMap a, b;
   int tiles_m, tiles_n;
+  int n_fast;       // raster: N tiles fastest (tiles_n small) or M tiles fastest
   int kblocks, splits, kb_per_split;
   int zbase, nz;    // batch indices [zbase, zbase + nz) in this launch
   int lanes_rows;   // epilogue: consecutive lanes on consecutive rows (output column-contiguous)
@@ -542,8 +543,13 @@ __global__ void __launch_bounds__(320, 1)
     const int zs = item / ntiles;
     sp = zs % p.splits;
     z = p.zbase + zs / p.splits;
-    m0 = (tile % p.tiles_m) * BM;
-    n0 = (tile / p.tiles_m) * BN;
+    if (p.n_fast) {   // tall-skinny: the N tiles of one M row-block run together (A read once from DRAM)
+      m0 = (tile / p.tiles_n) * BM;
+      n0 = (tile % p.tiles_n) * BN;
+    } else {
+      m0 = (tile % p.tiles_m) * BM;
+      n0 = (tile / p.tiles_m) * BN;
+    }
     kb0 = sp * p.kb_per_split;
     nk = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
   };
@@ -937,6 +943,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   if (!make_map(&mb, &p.b, g.b, g.N, g.K, g.batch, BN)) return cudaErrorNotSupported;
   p.tiles_m = (g.M + BM - 1) / BM;
   p.tiles_n = (g.N + BN - 1) / BN;
+  p.n_fast = (p.tiles_n <= 16 && p.tiles_m >= p.tiles_n) ? 1 : 0;
   p.kblocks = (g.K + BK - 1) / BK;
   const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n * g.batch;
   int splits = 1;

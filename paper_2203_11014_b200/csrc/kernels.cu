@@ -556,41 +556,42 @@ cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t 
 }
 
 // ------------------------------------------------------------------ softmax
-__global__ void softmax_rows_k(const float* S, void* P, int dt, int64_t rows, int n) {
+__global__ void softmax_rows_k(const float* S, void* P, int dt, int64_t rows, int n, int ld) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
-    const float* s = S + r * n;
+    const float* s = S + r * ld;
     float mx = -INFINITY;
     for (int c = lane; c < n; c += 32) mx = fmaxf(mx, s[c]);
     mx = warp_max(mx);
     float sum = 0.f;
     for (int c = lane; c < n; c += 32) sum += __expf(s[c] - mx);
     const float inv = 1.f / warp_sum(sum);
-    for (int c = lane; c < n; c += 32) st_from_f32(P, r * n + c, dt, __expf(s[c] - mx) * inv);
+    for (int c = lane; c < n; c += 32) st_from_f32(P, r * ld + c, dt, __expf(s[c] - mx) * inv);
   }
 }
-cudaError_t softmax_rows(const float* S, void* P, int dt, int64_t rows, int n, cudaStream_t st) {
-  softmax_rows_k<<<nblocks(rows, 8, 148 * 64), 256, 0, st>>>(S, P, dt, rows, n);
+cudaError_t softmax_rows(const float* S, void* P, int dt, int64_t rows, int n, int ld, cudaStream_t st) {
+  softmax_rows_k<<<nblocks(rows, 8, 148 * 64), 256, 0, st>>>(S, P, dt, rows, n, ld);
   ++g_launches;
   return cudaGetLastError();
 }
-__global__ void softmax_bwd_k(const void* P, const float* dP, void* dS, int dt, int64_t rows, int n, float scale) {
+__global__ void softmax_bwd_k(const void* P, const float* dP, void* dS, int dt, int64_t rows, int n, int ld,
+                              float scale) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
     float s = 0.f;
-    for (int c = lane; c < n; c += 32) s += ld_as_f32(P, r * n + c, dt) * dP[r * n + c];
+    for (int c = lane; c < n; c += 32) s += ld_as_f32(P, r * ld + c, dt) * dP[r * ld + c];
     s = warp_sum(s);
     for (int c = lane; c < n; c += 32) {
-      float p = ld_as_f32(P, r * n + c, dt);
-      st_from_f32(dS, r * n + c, dt, scale * p * (dP[r * n + c] - s));
+      float p = ld_as_f32(P, r * ld + c, dt);
+      st_from_f32(dS, r * ld + c, dt, scale * p * (dP[r * ld + c] - s));
     }
   }
 }
-cudaError_t softmax_bwd(const void* P, const float* dP, void* dS, int dt, int64_t rows, int n, float scale,
+cudaError_t softmax_bwd(const void* P, const float* dP, void* dS, int dt, int64_t rows, int n, int ld, float scale,
                         cudaStream_t st) {
-  softmax_bwd_k<<<nblocks(rows, 8, 148 * 64), 256, 0, st>>>(P, dP, dS, dt, rows, n, scale);
+  softmax_bwd_k<<<nblocks(rows, 8, 148 * 64), 256, 0, st>>>(P, dP, dS, dt, rows, n, ld, scale);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -616,11 +617,10 @@ cudaError_t dcn_bwd_elem(const void* dT, const void* X, const void* A, void* dA,
 constexpr int CV_RB = 8;
 template <typename T, int K, bool FLIP>
 __global__ void __launch_bounds__(256) conv_band_k(const T* __restrict__ in, const T* __restrict__ Kp, int C, int m,
-                                                   int d, T* __restrict__ outT, float* __restrict__ outAcc) {
+                                                   int d, T* __restrict__ outT, float* __restrict__ outAcc, int nbatch) {
   constexpr int R = (K - 1) / 2;
   extern __shared__ float band[];          // [(RB + 2R) rows][d + 2R]
   __shared__ float kb[K * K];
-  const int b = blockIdx.y, i0 = blockIdx.x * CV_RB;
   const int W = d + 2 * R;
   for (int t = threadIdx.x; t < K * K; t += blockDim.x) {
     float sacc = 0.f;
@@ -628,6 +628,10 @@ __global__ void __launch_bounds__(256) conv_band_k(const T* __restrict__ in, con
     kb[t] = sacc / C;
   }
   const int rows_in = CV_RB + 2 * R;
+  const int nbm = (m + CV_RB - 1) / CV_RB;
+  for (int64_t band_i = blockIdx.x; band_i < (int64_t)nbm * nbatch; band_i += gridDim.x) {
+  const int b = (int)(band_i / nbm), i0 = (int)(band_i % nbm) * CV_RB;
+  __syncthreads();
   for (int e = threadIdx.x; e < rows_in * (d / 8); e += blockDim.x) {
     const int rr = e / (d / 8), cc = (e % (d / 8)) * 8;
     const int gi = i0 - R + rr;
@@ -671,17 +675,24 @@ __global__ void __launch_bounds__(256) conv_band_k(const T* __restrict__ in, con
       VIO<8, T>::st(outT + off, o);
     }
   }
+  }
 }
 
 // dK[a][e] partials: block = (band of sample b): sum over its outputs of dT[i][j] * X[i+a-R][j+e-R]
 template <typename T, int K>
 __global__ void __launch_bounds__(256) conv_wgrad_band_k(const T* __restrict__ dT, const T* __restrict__ X, int m,
-                                                         int d, float* __restrict__ part) {
+                                                         int d, float* __restrict__ part, int nbatch) {
   constexpr int R = (K - 1) / 2;
   extern __shared__ float band[];          // X band [(RB + 2R)][d + 2R]
   __shared__ float red[K * K][8];
-  const int b = blockIdx.y, i0 = blockIdx.x * CV_RB;
   const int W = d + 2 * R, rows_in = CV_RB + 2 * R;
+  const int nbm = (m + CV_RB - 1) / CV_RB;
+  float acc[K * K];
+#pragma unroll
+  for (int q = 0; q < K * K; ++q) acc[q] = 0.f;
+  for (int64_t band_i = blockIdx.x; band_i < (int64_t)nbm * nbatch; band_i += gridDim.x) {
+  const int b = (int)(band_i / nbm), i0 = (int)(band_i % nbm) * CV_RB;
+  __syncthreads();
   for (int e = threadIdx.x; e < rows_in * (d / 8); e += blockDim.x) {
     const int rr = e / (d / 8), cc = (e % (d / 8)) * 8;
     const int gi = i0 - R + rr;
@@ -695,9 +706,6 @@ __global__ void __launch_bounds__(256) conv_wgrad_band_k(const T* __restrict__ d
     band[rr * W + (q < R ? q : d + q)] = 0.f;
   }
   __syncthreads();
-  float acc[K * K];
-#pragma unroll
-  for (int q = 0; q < K * K; ++q) acc[q] = 0.f;
   for (int e = threadIdx.x; e < CV_RB * (d / 8); e += blockDim.x) {
     const int ri = e / (d / 8), j0 = (e % (d / 8)) * 8;
     const int gi = i0 + ri;
@@ -716,6 +724,7 @@ __global__ void __launch_bounds__(256) conv_wgrad_band_k(const T* __restrict__ d
         for (int t = 0; t < 8; ++t) acc[a * K + e2] += g[t] * x[t + e2];
     }
   }
+  }
   const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
 #pragma unroll
   for (int q = 0; q < K * K; ++q) {
@@ -726,7 +735,7 @@ __global__ void __launch_bounds__(256) conv_wgrad_band_k(const T* __restrict__ d
   if (threadIdx.x < K * K) {
     float v = 0.f;
     for (int ww = 0; ww < 8; ++ww) v += red[threadIdx.x][ww];
-    part[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * K * K + threadIdx.x] = v;
+    part[(int64_t)blockIdx.x * K * K + threadIdx.x] = v;
   }
 }
 
@@ -735,15 +744,16 @@ static cudaError_t conv_band_launch(const void* in, const void* Kp, int C, int B
                                     bool flip, cudaStream_t st) {
   constexpr int R = (K - 1) / 2;
   const size_t sm = (size_t)(CV_RB + 2 * R) * (d + 2 * R) * sizeof(float);
-  dim3 grid((m + CV_RB - 1) / CV_RB, B);
+  const int64_t bands = (int64_t)((m + CV_RB - 1) / CV_RB) * B;
+  const int grid = (int)std::min<int64_t>(bands, 148 * 8);
   if (flip)
-    conv_band_k<T, K, true><<<grid, 256, sm, st>>>((const T*)in, (const T*)Kp, C, m, d, (T*)outT, outAcc);
+    conv_band_k<T, K, true><<<grid, 256, sm, st>>>((const T*)in, (const T*)Kp, C, m, d, (T*)outT, outAcc, B);
   else
-    conv_band_k<T, K, false><<<grid, 256, sm, st>>>((const T*)in, (const T*)Kp, C, m, d, (T*)outT, outAcc);
+    conv_band_k<T, K, false><<<grid, 256, sm, st>>>((const T*)in, (const T*)Kp, C, m, d, (T*)outT, outAcc, B);
   ++g_launches;
   return cudaGetLastError();
 }
-static bool conv_band_ok(int k, int d, int B) { return (k == 3 || k == 5) && d % 8 == 0 && d <= 1024 && B <= 65535; }
+static bool conv_band_ok(int k, int d, int B) { return (k == 3 || k == 5) && d % 8 == 0 && d <= 1024 && B >= 1; }
 
 // ------------------------------------------------------------------ conv (folded channel mean)
 constexpr int CONV_MAXK = 7;
@@ -869,19 +879,19 @@ __global__ void conv_wgrad_fin_k(const float* part, int nparts, int C, int kk, f
 cudaError_t conv_wgrad(const void* dT, const void* X, int C, int k, int B, int m, int d, int dt, float* dK,
                        float* scratch, size_t scratch_bytes, cudaStream_t st) {
   if (k > CONV_MAXK) return cudaErrorInvalidValue;
-  const int nbx = (m + CV_RB - 1) / CV_RB;
-  if (conv_band_ok(k, d, B) && (size_t)nbx * B * k * k * sizeof(float) <= scratch_bytes) {
+  const int64_t bands = (int64_t)((m + CV_RB - 1) / CV_RB) * B;
+  const int grid = (int)std::min<int64_t>(bands, 148 * 4);
+  if (conv_band_ok(k, d, B) && (size_t)grid * k * k * sizeof(float) <= scratch_bytes) {
     const int R = (k - 1) / 2;
     const size_t sm = (size_t)(CV_RB + 2 * R) * (d + 2 * R) * sizeof(float);
-    dim3 grid(nbx, B);
     if (dt == BF16) {
-      if (k == 3) conv_wgrad_band_k<__nv_bfloat16, 3><<<grid, 256, sm, st>>>((const __nv_bfloat16*)dT, (const __nv_bfloat16*)X, m, d, scratch);
-      else conv_wgrad_band_k<__nv_bfloat16, 5><<<grid, 256, sm, st>>>((const __nv_bfloat16*)dT, (const __nv_bfloat16*)X, m, d, scratch);
+      if (k == 3) conv_wgrad_band_k<__nv_bfloat16, 3><<<grid, 256, sm, st>>>((const __nv_bfloat16*)dT, (const __nv_bfloat16*)X, m, d, scratch, B);
+      else conv_wgrad_band_k<__nv_bfloat16, 5><<<grid, 256, sm, st>>>((const __nv_bfloat16*)dT, (const __nv_bfloat16*)X, m, d, scratch, B);
     } else {
-      if (k == 3) conv_wgrad_band_k<float, 3><<<grid, 256, sm, st>>>((const float*)dT, (const float*)X, m, d, scratch);
-      else conv_wgrad_band_k<float, 5><<<grid, 256, sm, st>>>((const float*)dT, (const float*)X, m, d, scratch);
+      if (k == 3) conv_wgrad_band_k<float, 3><<<grid, 256, sm, st>>>((const float*)dT, (const float*)X, m, d, scratch, B);
+      else conv_wgrad_band_k<float, 5><<<grid, 256, sm, st>>>((const float*)dT, (const float*)X, m, d, scratch, B);
     }
-    conv_wgrad_fin_k<<<1, 64, 0, st>>>(scratch, nbx * B, C, k * k, dK);
+    conv_wgrad_fin_k<<<1, 64, 0, st>>>(scratch, grid, C, k * k, dK);
     g_launches += 2;
     return cudaGetLastError();
   }

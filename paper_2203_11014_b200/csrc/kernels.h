@@ -26,9 +26,10 @@ cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu,
 cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t ld, float* out,
                        float* scratch, size_t scratch_bytes, cudaStream_t st);
 
-// F4 softmax over rows of S (fp32) -> P (dt).  B6: dS = scale * P (dP - rowsum(P dP)).
-cudaError_t softmax_rows(const float* S, void* P, int dt, int64_t rows, int n, cudaStream_t st);
-cudaError_t softmax_bwd(const void* P, const float* dP, void* dS, int dt, int64_t rows, int n, float scale,
+// F4 softmax over rows (n valid columns, row pitch ld) of S (fp32) -> P (dt).
+// B6: dS = scale * P (dP - rowsum(P dP)).
+cudaError_t softmax_rows(const float* S, void* P, int dt, int64_t rows, int n, int ld, cudaStream_t st);
+cudaError_t softmax_bwd(const void* P, const float* dP, void* dS, int dt, int64_t rows, int n, int ld, float scale,
                         cudaStream_t st);
 
 // B8 elementwise: dA = dT * X (dt); acc += dT * A + dT.

@@ -329,7 +329,8 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
         case DHEN_ATTN: {
           int H = md.s.heads, f = md.s.ffn_mult * d;
           md.QKV = work.take(tok * 3 * es);
-          md.P = work.take((size_t)B * H * mi * mi * es);
+          const int mp = (mi + 7) / 8 * 8;   // score rows padded to 16 B (TMA pitch)
+          md.P = work.take((size_t)B * H * mi * mp * es);
           md.O = work.take(tok * es);
           md.R1 = work.take(tok * es);
           md.Z1 = work.take(tok * es);
@@ -338,7 +339,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
           md.T = work.take(tok * es);
           md.mu1 = (float*)work.take((size_t)B * mi * 4); md.rs1 = (float*)work.take((size_t)B * mi * 4);
           md.mu2 = (float*)work.take((size_t)B * mi * 4); md.rs2 = (float*)work.take((size_t)B * mi * 4);
-          H_mm_max = std::max(H_mm_max, H * mi * mi);
+          H_mm_max = std::max(H_mm_max, H * mi * mp);
           f_max = std::max(f_max, f);
           tC_elems = std::max<int64_t>(tC_elems, (int64_t)B * mi * std::max(f, 3 * d));
           break;
@@ -507,13 +508,14 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         q.e.bias = p(md.bq); q.e.bias_dt = dt; q.e.bias_gap_lo = d; q.e.bias_gap_hi = 2 * d;   // no key bias (R10)
         q.e.bias_hi_off = (int)(md.bv - md.bq);
         RET(G_(q, c, st, "attn.qkv"));
+        const int mp = (mi + 7) / 8 * 8;   // padded score-row pitch
         Gemm s = mk(mi, mi, dh, B * H, operand(QKV, dt, s3, 1, mi * s3, dh, H),
                     operand(QKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H),
-                    view(c->big, F32, mi, 1, (int64_t)mi * mi));
+                    view(c->big, F32, mp, 1, (int64_t)mi * mp));
         s.e.alpha = 1.f / sqrtf((float)dh);
         RET(G_(s, c, st, "attn.qk"));
-        KT("attn.softmax", 0, (double)B * H * mi * mi * (4 + es), softmax_rows(c->big, md.P, dt, (int64_t)B * H * mi, mi, st));
-        Gemm o = mk(mi, dh, mi, B * H, operand(md.P, dt, mi, 1, (int64_t)mi * mi),
+        KT("attn.softmax", 0, (double)B * H * mi * mi * (4 + es), softmax_rows(c->big, md.P, dt, (int64_t)B * H * mi, mi, mp, st));
+        Gemm o = mk(mi, dh, mi, B * H, operand(md.P, dt, mp, 1, (int64_t)mi * mp),
                     operand(QKV + 2 * (int64_t)d * es, dt, 1, s3, mi * s3, dh, H),
                     view(md.O, dt, d, 1, (int64_t)mi * d, dh, H));
         RET(G_(o, c, st, "attn.pv"));
@@ -653,20 +655,21 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dR1, dt, rows, d, d, gp(md.bo), c->red, c->red_bytes, st));
         // attention core backward
         char* dQKV = (char*)c->tC;   // [rows, 3d]  (dF no longer needed; tC >= rows*f >= rows*3d? checked at plan)
-        Gemm dv = mk(mi, dh, mi, B * H, operand(md.P, dt, 1, mi, (int64_t)mi * mi),
+        const int mp = (mi + 7) / 8 * 8;
+        Gemm dv = mk(mi, dh, mi, B * H, operand(md.P, dt, 1, mp, (int64_t)mi * mp),
                      operand(dO, dt, 1, d, (int64_t)mi * d, dh, H),
                      view(dQKV + 2 * (int64_t)d * es, dt, s3, 1, mi * s3, dh, H));
         RET(G_(dv, c, st, "attn.dv"));
         Gemm dp = mk(mi, mi, dh, B * H, operand(dO, dt, d, 1, (int64_t)mi * d, dh, H),
                      operand(QKV + 2 * (int64_t)d * es, dt, s3, 1, mi * s3, dh, H),
-                     view(c->big, F32, mi, 1, (int64_t)mi * mi));
+                     view(c->big, F32, mp, 1, (int64_t)mi * mp));
         RET(G_(dp, c, st, "attn.dp"));
-        KT("attn.softmax_bwd", 0, (double)B * H * mi * mi * (4 + 2 * es), softmax_bwd(md.P, c->big, c->tD, dt, (int64_t)B * H * mi, mi, 1.f / sqrtf((float)dh), st));
-        Gemm dq = mk(mi, dh, mi, B * H, operand(c->tD, dt, mi, 1, (int64_t)mi * mi),
+        KT("attn.softmax_bwd", 0, (double)B * H * mi * mi * (4 + 2 * es), softmax_bwd(md.P, c->big, c->tD, dt, (int64_t)B * H * mi, mi, mp, 1.f / sqrtf((float)dh), st));
+        Gemm dq = mk(mi, dh, mi, B * H, operand(c->tD, dt, mp, 1, (int64_t)mi * mp),
                      operand(QKV + (int64_t)d * es, dt, 1, s3, mi * s3, dh, H),
                      view(dQKV, dt, s3, 1, mi * s3, dh, H));
         RET(G_(dq, c, st, "attn.dq"));
-        Gemm dk = mk(mi, dh, mi, B * H, operand(c->tD, dt, 1, mi, (int64_t)mi * mi),
+        Gemm dk = mk(mi, dh, mi, B * H, operand(c->tD, dt, 1, mp, (int64_t)mi * mp),
                      operand(QKV, dt, 1, s3, mi * s3, dh, H),
                      view(dQKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H));
         RET(G_(dk, c, st, "attn.dk"));

@@ -43,6 +43,12 @@ def shapes(cfg):
          (d, mo * d), (0, 0), (d, m * d), bf),
         ("tokmix.wgrad", m, l, B * d, 1, (d, 1, 0, 0, 1, d, m * d), (d, 1, 0, 0, 1, d, mo * d), (l, 1, 0, 0, 1), 1,
          (0, 0), (0, 0), (0, 0), f32),
+        ("attn.ffn1", R, 4 * d, d, 1, (d, 1, 0, 0, 1, 0, 0), (d, 1, 0, 0, 1, 0, 0), (4 * d, 1, 0, 0, 1), 0,
+         (0, 0), (0, 0), (0, 0), bf),
+        ("attn.ffn2_dgrad", R, 4 * d, d, 1, (d, 1, 0, 0, 1, 0, 0), (1, 4 * d, 0, 0, 1, 0, 0), (4 * d, 1, 0, 0, 1), 0,
+         (0, 0), (0, 0), (0, 0), bf),
+        ("attn.ffn2", R, d, 4 * d, 1, (4 * d, 1, 0, 0, 1, 0, 0), (4 * d, 1, 0, 0, 1, 0, 0), (d, 1, 0, 0, 1), 0,
+         (0, 0), (0, 0), (0, 0), f32),
         # experiments: same M, N, K as tokmix.fwd with plain layouts
         ("x.kmaj_rowmajor", B * d, l, m, 1, (m, 1, 0, 0, 1, 0, 0), (m, 1, 0, 0, 1, 0, 0), (l, 1, 0, 0, 1), 0,
          (0, 0), (0, 0), (0, 0), f32),
