@@ -25,7 +25,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -44,47 +43,57 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons polled through NVML every 2 ms during the timed region (the region of a
+    short step can be far shorter than nvidia-smi's 200 ms interval); nvidia-smi CSV as a fallback."""
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, gpu: int):
-        self.gpu, self.rows, self.proc = gpu, [], None
+        self.gpu, self.sm, self.reasons, self.max_mhz = gpu, [], set(), None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis else self.gpu
+            self.h = N.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+            self.th = threading.Thread(target=self._poll, daemon=True)
             self.th.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # pragma: no cover
+            self.err = repr(e)
+            self.N = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            f = [x.strip() for x in line.split(",")]
-            if len(f) >= 8:
-                self.rows.append(f)
+    def _poll(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.REASONS:
+                    if r & getattr(N, attr, 0):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.N is not None:
+            self.th.join(timeout=1)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(self.rows[0][1]),
-                "samples": len(self.rows), "reasons": reasons}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "samples": len(self.sm),
+                "source": "nvml", "reasons": sorted(self.reasons)}
 
 
 def cpu_baseline(cfg_name: str, target_s: float = 12.0):
@@ -165,6 +174,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default="")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph (launch every kernel from the host)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -208,8 +218,13 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
 
+    graphed = not args.eager
+
     def step():
-        model.train_step(x0, lab, lr, B_global=Bg, loss=loss)
+        if graphed:
+            model.train_step_graphed(x0, lab, lr, B_global=Bg, loss=loss)
+        else:
+            model.train_step(x0, lab, lr, B_global=Bg, loss=loss)
 
     for _ in range(args.warmup):
         step()
@@ -246,6 +261,11 @@ def main():
     dx = torch.empty_like(x0)
     dy = torch.empty_like(lab)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dx.copy_(hx)
+    dy.copy_(hy)
+    for _ in range(2):   # capture the graph for these buffers outside the timed region
+        step_e2e_warm = model.train_step_graphed if graphed else model.train_step
+        step_e2e_warm(dx, dy, lr, B_global=Bg, loss=loss)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -253,7 +273,10 @@ def main():
     for _ in range(args.steps):
         dx.copy_(hx, non_blocking=True)
         dy.copy_(hy, non_blocking=True)
-        model.train_step(dx, dy, lr, B_global=Bg, loss=loss)
+        if graphed:
+            model.train_step_graphed(dx, dy, lr, B_global=Bg, loss=loss)
+        else:
+            model.train_step(dx, dy, lr, B_global=Bg, loss=loss)
         hl.copy_(loss, non_blocking=True)
     e1.record(st)
     torch.cuda.synchronize()
@@ -314,6 +337,7 @@ def main():
         "loss": loss_val,
         "e2e": e2e,
         "gpu_launches": int(launches),
+        "cuda_graph": graphed and world == 1,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk.summary(),
         "roofline": roof,

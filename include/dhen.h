@@ -141,6 +141,13 @@ dhen_status dhen_layer_bwd(dhen_ctx* ctx, int layer, const void* dy, void* dx, i
 dhen_status dhen_train_step(dhen_ctx* ctx, const void* x0, const float* labels, int B, int B_global,
                             float lr, float* loss_dev, void* dx0, void* stream);
 
+/* dhen_train_step through a CUDA graph: the first call with a given argument set runs the step
+ * eagerly and captures it; later calls with the same (x0, labels, B, B_global, lr, loss_dev, dx0)
+ * replay the graph (one cudaGraphLaunch on `stream`).  Buffer contents may change between calls,
+ * pointers may not (a change re-captures).  world > 1 or profiling: plain dhen_train_step. */
+dhen_status dhen_train_step_graphed(dhen_ctx* ctx, const void* x0, const float* labels, int B, int B_global,
+                                    float lr, float* loss_dev, void* dx0, void* stream);
+
 /* Forward of the whole stack + head without backward: logits_dev [B] fp32. */
 dhen_status dhen_forward(dhen_ctx* ctx, const void* x0, int B, float* logits_dev, void* stream);
 

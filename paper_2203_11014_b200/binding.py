@@ -21,7 +21,7 @@ STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_SHAPE", 3: "E_ALIGN", 4: "E_STATE", 5: "
 
 # every symbol include/dhen.h declares
 EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "dhen_init", "dhen_layer_fwd",
-           "dhen_layer_bwd", "dhen_train_step", "dhen_forward", "dhen_zero_grad", "dhen_params_io",
+           "dhen_layer_bwd", "dhen_train_step", "dhen_train_step_graphed", "dhen_forward", "dhen_zero_grad", "dhen_params_io",
            "dhen_grads_get", "dhen_launch_count", "dhen_last_error", "dhen_destroy", "dhen_profile",
            "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_last_gemm_tc",
            "dhen_debug_gemm_trace")
@@ -78,6 +78,7 @@ def load(path: str = LIB_PATH):
         "dhen_layer_fwd": [vp, i, vp, vp, i, vp],
         "dhen_layer_bwd": [vp, i, vp, vp, i, vp],
         "dhen_train_step": [vp, vp, vp, i, i, C.c_float, vp, vp, vp],
+        "dhen_train_step_graphed": [vp, vp, vp, i, i, C.c_float, vp, vp, vp],
         "dhen_forward": [vp, vp, i, vp, vp],
         "dhen_zero_grad": [vp, vp],
         "dhen_params_io": [vp, i, vp, i, vp],
@@ -314,6 +315,13 @@ class DHEN:
         return [{"name": arr[k].name.decode(), "launches": arr[k].launches, "ms": arr[k].ms,
                  "flops": arr[k].flops, "bytes": arr[k].bytes,
                  "tc_launches": arr[k].tc_launches} for k in range(min(n.value, cap))]
+
+    def train_step_graphed(self, x0, labels, lr, B_global=None, loss=None, dx0=None, stream=None):
+        """train_step replayed from a CUDA graph (captured on the first call with these buffers)."""
+        B = x0.shape[0]
+        _check("dhen_train_step_graphed", self.lib.dhen_train_step_graphed(
+            self.ctx, _ptr(x0), _ptr(labels), B, B_global or B, float(lr), _ptr(loss), _ptr(dx0),
+            self._stream(stream)))
 
     def forward(self, x0, logits, stream=None):
         _check("dhen_forward", self.lib.dhen_forward(self.ctx, _ptr(x0), x0.shape[0], _ptr(logits),

@@ -137,6 +137,16 @@ struct dhen_ctx {
   float *pooled = nullptr, *z = nullptr, *lossb = nullptr, *dz = nullptr;
   float* gtmp = nullptr;    // fp32 [max_npad]: all-gather target of params_io / grads_get (world > 1)
   ncclComm_t comm = nullptr;
+  // CUDA graph of dhen_train_step (dhen_train_step_graphed), keyed by its arguments
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap_st = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  const void* gkey[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  int gkey_B = 0, gkey_Bg = 0;
+  float gkey_lr = 0.f;
+  unsigned long long graph_launches = 0;   // kernels inside the captured step
+  cudaStream_t comm_st = nullptr;     // collectives (world > 1)
+  cudaEvent_t ev_ag[2] = {nullptr, nullptr}, ev_use[2] = {nullptr, nullptr}, ev_grad = nullptr, ev_comm = nullptr;
   unsigned long long launches0 = 0;
   // per-op device timing (dhen_profile): event pairs on the launch stream
   struct Rec { const char* tag; int e0, e1; double flops, bytes; int tc; };
@@ -434,28 +444,67 @@ static dhen_status tokmix_bwd(dhen_ctx* c, const void* T, int m, const void* W, 
 }
 
 // ------------------------------------------------------------------ FSDP gather / scatter
+// Two gathered-parameter slots (slot = group & 1).  All collectives run on the communication stream:
+//   prefetch(g): comm waits ev_use[slot] (the compute stream is done with the slot's previous owner),
+//                all-gathers group g into the slot, records ev_ag[slot];
+//   comp_params(g): prefetch if needed, then the compute stream waits ev_ag[slot];
+//   release(g):  the compute stream records ev_use[slot] after the last kernel reading the slot;
+//   reduce_grads(g): comm waits ev_grad (recorded on compute after g's backward), reduce-scatters the
+//                fp32 gradient into the local shard (all-reduce in replicated DP mode).
+// world == 1: parameters are local, nothing is launched.
+static bool sharded(const dhen_ctx* c) { return c->dist.world > 1 && c->dist.fsdp; }
+
+static dhen_status prefetch(dhen_ctx* c, int gi) {
+  if (!sharded(c) || gi < 0 || gi > c->cfg.n_layers) return DHEN_OK;
+  const int slot = gi & 1;
+  if (c->gathered_owner[slot] == gi) return DHEN_OK;
+  Group& g = c->G[gi];
+  CK(cudaStreamWaitEvent(c->comm_st, c->ev_use[slot], 0));
+  NK(ncclAllGather(g.comp, c->gathered[slot], (size_t)g.shard, c->dt == F32 ? ncclFloat32 : ncclBfloat16, c->comm,
+                   c->comm_st));
+  CK(cudaEventRecord(c->ev_ag[slot], c->comm_st));
+  c->gathered_owner[slot] = gi;
+  return DHEN_OK;
+}
 static dhen_status comp_params(dhen_ctx* c, int gi, cudaStream_t st, void** out) {
   Group& g = c->G[gi];
-  if (c->dist.world == 1 || !c->dist.fsdp) { *out = g.comp; return DHEN_OK; }
-  int slot = gi & 1;
-  if (c->gathered_owner[slot] != gi) {
-    NK(ncclAllGather(g.comp, c->gathered[slot], (size_t)g.shard, c->dt == F32 ? ncclFloat32 : ncclBfloat16, c->comm,
-                     st));
-    c->gathered_owner[slot] = gi;
-  }
-  *out = c->gathered[slot];
+  if (!sharded(c)) { *out = g.comp; return DHEN_OK; }
+  RET(prefetch(c, gi));
+  CK(cudaStreamWaitEvent(st, c->ev_ag[gi & 1], 0));
+  *out = c->gathered[gi & 1];
+  return DHEN_OK;
+}
+static dhen_status release(dhen_ctx* c, int gi, cudaStream_t st) {
+  if (!sharded(c)) return DHEN_OK;
+  CK(cudaEventRecord(c->ev_use[gi & 1], st));
   return DHEN_OK;
 }
 static void invalidate_gathered(dhen_ctx* c) { c->gathered_owner[0] = c->gathered_owner[1] = -1; }
+// parameters (compute copies) were rewritten on `st`: later all-gathers must wait for that
+static dhen_status fence_params(dhen_ctx* c, cudaStream_t st) {
+  invalidate_gathered(c);
+  if (!sharded(c)) return DHEN_OK;
+  for (int k = 0; k < 2; ++k) CK(cudaEventRecord(c->ev_use[k], st));
+  return DHEN_OK;
+}
 
 static dhen_status reduce_grads(dhen_ctx* c, int gi, cudaStream_t st) {
   if (c->dist.world == 1) return DHEN_OK;
   Group& g = c->G[gi];
+  CK(cudaEventRecord(c->ev_grad, st));
+  CK(cudaStreamWaitEvent(c->comm_st, c->ev_grad, 0));
   if (c->dist.fsdp) {
-    NK(ncclReduceScatter(g.grad, g.gshard, (size_t)g.shard, ncclFloat32, ncclSum, c->comm, st));
+    NK(ncclReduceScatter(g.grad, g.gshard, (size_t)g.shard, ncclFloat32, ncclSum, c->comm, c->comm_st));
   } else {
-    NK(ncclAllReduce(g.grad, g.gshard, (size_t)g.shard, ncclFloat32, ncclSum, c->comm, st));
+    NK(ncclAllReduce(g.grad, g.gshard, (size_t)g.shard, ncclFloat32, ncclSum, c->comm, c->comm_st));
   }
+  return DHEN_OK;
+}
+// the compute stream waits for every collective issued so far
+static dhen_status join_comm(dhen_ctx* c, cudaStream_t st) {
+  if (c->dist.world == 1) return DHEN_OK;
+  CK(cudaEventRecord(c->ev_comm, c->comm_st));
+  CK(cudaStreamWaitEvent(st, c->ev_comm, 0));
   return DHEN_OK;
 }
 
@@ -554,6 +603,7 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
             Lr.rstd, dt, st));
   Lr.X = X;
   Lr.B = B;
+  RET(release(c, n, st));
   return DHEN_OK;
 }
 
@@ -713,6 +763,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
     }
   }
   if (dX) KT("layer.dx_cast", 0, (double)rows * d * (4 + es), cast(acc, F32, dX, dt, rows * d, st));
+  RET(release(c, n, st));
   RET(reduce_grads(c, n, st));
   return DHEN_OK;
 }
@@ -727,6 +778,7 @@ static dhen_status head(dhen_ctx* c, const void* YN, int mN, const float* labels
   Group& G = c->G[gi];
   KT("head", 0, (double)B * mN * c->d * c->es * (do_bwd ? 2 : 1), head_fwd_bwd(YN, p(0), p(G.toff[1]), c->dt, labels, B, mN, c->d, Bg, dY, c->dt, c->pooled, c->z, c->lossb, c->dz, loss,
                   G.grad, G.grad + G.toff[1], do_bwd, st));
+  RET(release(c, gi, st));
   if (do_bwd) RET(reduce_grads(c, gi, st));
   return DHEN_OK;
 }
@@ -819,6 +871,14 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
     memcpy(id.internal, c->dist.nccl_id, 128);
     ncclResult_t r = ncclCommInitRank(&c->comm, c->dist.world, id, c->dist.rank);
     if (r != ncclSuccess) { delete c; return fail(DHEN_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)); }
+    bool ok = cudaStreamCreateWithFlags(&c->comm_st, cudaStreamNonBlocking) == cudaSuccess;
+    for (int k = 0; k < 2; ++k) {
+      ok = ok && cudaEventCreateWithFlags(&c->ev_ag[k], cudaEventDisableTiming) == cudaSuccess;
+      ok = ok && cudaEventCreateWithFlags(&c->ev_use[k], cudaEventDisableTiming) == cudaSuccess;
+    }
+    ok = ok && cudaEventCreateWithFlags(&c->ev_grad, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) { dhen_destroy(c); return fail(DHEN_E_CUDA, "dhen_init: stream/event creation failed"); }
   }
   // parameter init: every rank initialises its own slice of the canonical vector
   const unsigned long long launches_before = g_launches;
@@ -847,6 +907,7 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
     if (e3 != cudaSuccess) { delete c; return fail(DHEN_E_CUDA, "dhen_init: %s", cudaGetErrorString(e3)); }
   }
   c->launches0 = launches_before;
+  if (fence_params(c, st) != DHEN_OK) { dhen_destroy(c); return DHEN_E_CUDA; }
   *out = c;
   return DHEN_OK;
 }
@@ -854,6 +915,17 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
 void dhen_destroy(dhen_ctx* c) {
   if (!c) return;
   for (auto e : c->events) cudaEventDestroy(e);
+  for (int k = 0; k < 2; ++k) {
+    if (c->ev_ag[k]) cudaEventDestroy(c->ev_ag[k]);
+    if (c->ev_use[k]) cudaEventDestroy(c->ev_use[k]);
+  }
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->cap_st) cudaStreamDestroy(c->cap_st);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_grad) cudaEventDestroy(c->ev_grad);
+  if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+  if (c->comm_st) cudaStreamDestroy(c->comm_st);
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
 }
@@ -948,6 +1020,7 @@ dhen_status dhen_layer_bwd(dhen_ctx* c, int n, const void* dy, void* dx, int B, 
   if (!aligned16(dy) || (dx && !aligned16(dx))) return fail(DHEN_E_ALIGN, "dhen_layer_bwd: dy=%p dx=%p", dy, dx);
   invalidate_gathered(c);
   RET(layer_bwd(c, n, dy, dx, B, S(stream)));
+  RET(join_comm(c, S(stream)));
   CK(cudaGetLastError());
   return DHEN_OK;
 }
@@ -960,6 +1033,8 @@ dhen_status dhen_forward(dhen_ctx* c, const void* x0, int B, float* logits, void
   invalidate_gathered(c);
   const void* X = x0;
   for (int n = 0; n < c->cfg.n_layers; ++n) {
+    RET(prefetch(c, n));
+    RET(prefetch(c, n + 1));          // overlap the next group's all-gather with this layer
     RET(layer_fwd(c, n, X, c->L[n].Y, B, st));
     X = c->L[n].Y;
   }
@@ -982,6 +1057,8 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
   invalidate_gathered(c);
   const void* X = x0;
   for (int n = 0; n < c->cfg.n_layers; ++n) {
+    RET(prefetch(c, n));
+    RET(prefetch(c, n + 1));          // overlap the next group's all-gather with this layer (F0)
     RET(layer_fwd(c, n, X, c->L[n].Y, B, st));
     X = c->L[n].Y;
   }
@@ -989,15 +1066,18 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
   int cur = 0;
   for (int n = c->cfg.n_layers - 1; n >= 0; --n) {
     void* dx = n > 0 ? c->dY[cur ^ 1] : dx0;
+    RET(prefetch(c, n));
+    RET(prefetch(c, n - 1));          // re-gather for backward ahead of use; RS of n runs behind (B11)
     RET(layer_bwd(c, n, c->dY[cur], dx, B, st));
     cur ^= 1;
   }
+  RET(join_comm(c, st));
   // B12: SGD on the (local shard of the) fp32 masters, refresh the compute copy
   for (auto& g : c->G) {
     const float* gr = c->dist.world > 1 ? g.gshard : g.grad;
     KT("sgd", 0, (double)g.shard * (12 + c->es), sgd_cast(g.master, gr, lr, g.comp, c->dt, g.shard, st));
   }
-  invalidate_gathered(c);
+  RET(fence_params(c, st));
   CK(cudaGetLastError());
   return DHEN_OK;
 }
@@ -1027,6 +1107,43 @@ static dhen_status gather_f32(dhen_ctx* c, Group& g, const float* shard_or_full,
   return DHEN_OK;
 }
 
+dhen_status dhen_train_step_graphed(dhen_ctx* c, const void* x0, const float* labels, int B, int Bg, float lr,
+                                    float* loss, void* dx0, void* stream) {
+  if (!c) return fail(DHEN_E_STATE, "dhen_train_step_graphed: ctx is NULL");
+  if (c->dist.world > 1 || c->prof) return dhen_train_step(c, x0, labels, B, Bg, lr, loss, dx0, stream);
+  cudaStream_t st = S(stream);
+  const bool same = c->gexec && c->gkey[0] == x0 && c->gkey[1] == labels && c->gkey[2] == loss &&
+                    c->gkey[3] == dx0 && c->gkey_B == B && c->gkey_Bg == Bg && c->gkey_lr == lr;
+  if (!same) {
+    if (c->gexec) { CK(cudaGraphExecDestroy(c->gexec)); c->gexec = nullptr; }
+    if (!c->cap_st) {
+      CK(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    // validate + warm (attribute setup, TMA-descriptor paths) eagerly once, then capture
+    RET(dhen_train_step(c, x0, labels, B, Bg, lr, loss, dx0, stream));
+    CK(cudaStreamSynchronize(st));
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(c->cap_st, cudaStreamCaptureModeThreadLocal));
+    const unsigned long long l0 = g_launches;
+    dhen_status s0 = dhen_train_step(c, x0, labels, B, Bg, lr, loss, dx0, c->cap_st);
+    c->graph_launches = g_launches - l0;
+    cudaError_t e = cudaStreamEndCapture(c->cap_st, &graph);
+    if (s0 != DHEN_OK) { if (graph) cudaGraphDestroy(graph); return s0; }
+    CK(e);
+    e = cudaGraphInstantiate(&c->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(e);
+    c->gkey[0] = x0; c->gkey[1] = labels; c->gkey[2] = loss; c->gkey[3] = dx0;
+    c->gkey_B = B; c->gkey_Bg = Bg; c->gkey_lr = lr;
+    return DHEN_OK;   // this call's step already ran eagerly
+  }
+  CK(cudaGraphLaunch(c->gexec, st));
+  g_launches += c->graph_launches;
+  return DHEN_OK;
+}
+
 dhen_status dhen_params_io(dhen_ctx* c, int gi, float* host, int set, void* stream) {
   if (!c) return fail(DHEN_E_STATE, "dhen_params_io: ctx is NULL");
   if (gi < 0 || gi > c->cfg.n_layers) return fail(DHEN_E_SHAPE, "dhen_params_io: group=%d", gi);
@@ -1040,7 +1157,7 @@ dhen_status dhen_params_io(dhen_ctx* c, int gi, float* host, int set, void* stre
     to_internal(g, host, pad);
     CK(cudaMemcpyAsync(g.master, pad.data() + lo, (size_t)g.shard * 4, cudaMemcpyHostToDevice, st));
     CK(sgd_cast(g.master, nullptr, 0.f, g.comp, c->dt, g.shard, st));
-    invalidate_gathered(c);
+    RET(fence_params(c, st));
     CK(cudaStreamSynchronize(st));
   } else {
     RET(gather_f32(c, g, g.master, pad, st));

@@ -205,3 +205,25 @@ def test_bf16_full_dims_layer_local(name, B, layers):
         errs = {k: norm_err(gg[k], v) for k, v in go.items()}
         bad = {k: e for k, e in errs.items() if e > (5e-2 if _gated(k) else 2e-2)}
         assert not bad, (n, bad, errs)
+
+
+def test_graphed_step_matches_eager_bitwise():
+    """dhen_train_step_graphed (CUDA graph replay) == dhen_train_step, bit for bit, over 3 steps."""
+    import torch
+    net = small("C4")
+    outs = []
+    for graphed in (False, True):
+        case = Case(net, 13, "bf16", seed=99)
+        loss = torch.zeros(1, device="cuda")
+        losses = []
+        for _ in range(3):
+            if graphed:
+                case.model.train_step_graphed(case.x0, case.labels, 0.05, loss=loss)
+            else:
+                case.model.train_step(case.x0, case.labels, 0.05, loss=loss)
+            torch.cuda.synchronize()
+            losses.append(loss.item())
+        outs.append((losses, [case.model.get_params(g) for g in range(len(case.flats))]))
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)
