@@ -188,10 +188,15 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
     return np.ldexp(r, e - 8)
 
 
+# Where the CUDA path stores bf16.  dcn.dT is not one: the DCN backward is fused into
+# the token-projection dgrad epilogue, which keeps dT in fp32 registers.
+GPU_POINTS = tuple(p for p in STORAGE_POINTS if p != "dcn.dT")
+
+
 @dataclass
 class Precision:
     bf16: bool = False
-    points: Sequence[str] = STORAGE_POINTS
+    points: Sequence[str] = GPU_POINTS
 
     def q(self, name: str, x: np.ndarray) -> np.ndarray:
         assert name in STORAGE_POINTS, name
@@ -302,7 +307,7 @@ def dcn_fwd(X, p, s, pr):
 
 def dcn_bwd(X, p, s, c, dU, pr):
     dT, dWu = tokmix_bwd(c["T"], p["W_u"], dU)
-    dT = pr.q("dcn.dT", dT)
+    dT = pr.q("dcn.dT", dT)          # not a storage point of the fused GPU path (kept for emulation studies)
     dA = pr.q("dcn.dA", dT * X)
     dX = dT * c["A"] + dT + dA @ p["W"]
     dW = dA.reshape(-1, dA.shape[-1]).T @ X.reshape(-1, X.shape[-1])

@@ -62,6 +62,12 @@ struct Epilogue {
   View aux = noview();
   View resid = noview();        // out += resid
   int accumulate = 0;           // out += C (C read in its own dtype)
+  // DCN backward fused into the token-mixing dgrad (B8): v = acc (= dT); aux <- v * x (dA, x = cross view);
+  // C += v * a + v (a = mask view holds A; C is the fp32 dX accumulator)
+  int dcn_bwd = 0;
+  // Gram triangle (F1): element (i, j) of sample z is stored iff j > i, at C + z * c.bs0 +
+  // i * triu_m - i (i + 1) / 2 + (j - i - 1)  (strict upper triangle, row-major pairs, R7)
+  int triu_m = 0;
 };
 
 struct Gemm {

@@ -7,6 +7,21 @@ namespace dhen {
 
 static __device__ __forceinline__ void epi_apply(const Gemm& g, int z, int i, int j, float acc) {
   const Epilogue& e = g.e;
+  if (e.triu_m) {
+    if (j <= i) return;
+    const int64_t o = (int64_t)z * g.c.bs0 + (int64_t)i * e.triu_m - (int64_t)i * (i + 1) / 2 + (j - i - 1);
+    st_from_f32(g.c.ptr, o, g.c.dt, acc * e.alpha);
+    return;
+  }
+  if (e.dcn_bwd) {
+    const float v = acc * e.alpha;
+    const float x = ld_as_f32(e.cross.ptr, e.cross.off(z, i, j), e.cross.dt);
+    const float a = ld_as_f32(e.mask.ptr, e.mask.off(z, i, j), e.mask.dt);
+    st_from_f32(e.aux.ptr, e.aux.off(z, i, j), e.aux.dt, v * x);
+    const int64_t co = g.c.off(z, i, j);
+    st_from_f32(g.c.ptr, co, g.c.dt, ld_as_f32(g.c.ptr, co, g.c.dt) + v * a + v);
+    return;
+  }
   float v = acc * e.alpha;
   if (e.bias) {
     int bj = j;

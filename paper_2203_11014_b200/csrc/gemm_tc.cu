@@ -38,7 +38,8 @@ struct OpMap {
 
 // Compact, host-resolved epilogue plan: every present view shares one row geometry
 // (offset = row term + batch term + col * cs), operands other than C are bf16.
-enum { EF_ACC = 1, EF_RELU = 2, EF_MASK = 4, EF_CROSS = 8, EF_AUX = 16, EF_RESID = 32, EF_BIAS = 64 };
+enum { EF_ACC = 1, EF_RELU = 2, EF_MASK = 4, EF_CROSS = 8, EF_AUX = 16, EF_RESID = 32, EF_BIAS = 64,
+       EF_DCNB = 128, EF_TRIU = 256 };
 struct Lean {
   void* c;
   const void* x;
@@ -49,6 +50,7 @@ struct Lean {
   int64_t rs, rs_o, bs0, bs1, cs;
   int rdiv, zdiv;
   int c_f32, flags, gap_lo, gap_hi, hi_off;
+  int triu_m;
   float alpha;
 };
 
@@ -382,6 +384,32 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
     const uint32_t sa = stage + (uint32_t)((r * SROW + 8 * cl) * 4);
     const float4 x0 = lds4(sa), x1 = lds4(sa + 16);
     float a[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    if (F & EF_TRIU) {
+      // strict upper triangle of the per-sample Gram: pairs (i, j > i) row-major (R7)
+      const int i = rbase + r;
+      const int64_t zb = o - col - (int64_t)i * e.rs;     // = z * bs0 (rs = 0 for this view)
+      const int64_t base = zb + (int64_t)i * e.triu_m - (int64_t)i * (i + 1) / 2 - i - 1;
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (col + t > i) stg1(e.c, base + col + t, CF32, a[t] * alpha);
+      continue;
+    }
+    if (F & EF_DCNB) {
+      // B8 fused: dA = dT * X (bf16, aux), dX_acc += dT * A + dT  (dT = the fp32 accumulator)
+      float xv[8], av[8], cv[8], da[8];
+      ldg_bf8(e.x, o, xv);
+      ldg_bf8(e.mask, o, av);
+      ldg_c8<true>(e.c, o, cv);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const float v = a[t] * alpha;
+        da[t] = v * xv[t];
+        cv[t] += v * av[t] + v;
+      }
+      stg8<false>(e.aux, o, da);
+      stg8<true>(e.c, o, cv);
+      continue;
+    }
 #pragma unroll
     for (int t = 0; t < 8; ++t) a[t] = a[t] * alpha + bias8[t];
     float t8[8];
@@ -416,6 +444,7 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
 // Column-contiguous output (cs != 1, rs == 1): one row per lane, 16 accumulator columns in registers.
 template <int F, bool CF32>
 __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0, int N, const uint32_t* v) {
+  if constexpr ((F & (EF_DCNB | EF_TRIU)) != 0) return;   // host never selects these in column-contiguous mode
   const float alpha = e.alpha;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
@@ -445,7 +474,10 @@ __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0,
   X(8, EF_BIAS | EF_CROSS | EF_AUX, false)        \
   X(9, EF_BIAS, false)                            \
   X(10, EF_BIAS, true)                            \
-  X(11, EF_ACC, false)
+  X(11, EF_ACC, false)                            \
+  X(12, EF_DCNB, true)                            \
+  X(13, EF_TRIU, false)                           \
+  X(14, EF_TRIU, true)
 static inline int lean_variant(int flags, bool cf32) {
 #define LV_ID(id, f, c) if (flags == (f) && cf32 == (c)) return id;
   LEAN_VARIANTS(LV_ID)
@@ -780,7 +812,10 @@ __global__ void __launch_bounds__(320, 1)
               const int col = cbase + lane + 32 * q;
               if (col < g.N) {
                 const float acc = stg[r * SROW + lane + 32 * q];
-                if (p.splits == 1) epi_elem(g, rb, col, acc);
+                if (p.splits == 1) {
+                  if (g.e.triu_m || g.e.dcn_bwd) epi_apply(g, z, row, col, acc);
+                  else epi_elem(g, rb, col, acc);
+                }
                 else p.ws[((int64_t)(z * p.splits + sp) * g.M + row) * g.N + col] = acc;
               }
             }
@@ -876,9 +911,9 @@ static bool make_lean(const Gemm& g, Lean* e) {
   if (!same_geom(x.cross, g.c) || !same_geom(x.aux, g.c) || !same_geom(x.mask, g.c) || !same_geom(x.resid, g.c))
     return false;
   if (x.bias && x.bias_dt != BF16) return false;
-  if (g.c.cs == 1 && (g.N % 4 || g.c.rs % 4 || g.c.bs0 % 4 || g.c.bs1 % 4 || g.c.rs_o % 4)) return false;
+  if (g.c.cs == 1 && !x.triu_m && (g.N % 4 || g.c.rs % 4 || g.c.bs0 % 4 || g.c.bs1 % 4 || g.c.rs_o % 4)) return false;
   auto al = [](const void* p, int b) { return !p || ((uintptr_t)p % b) == 0; };
-  if (g.c.cs == 1 && (!al(g.c.ptr, g.c.dt == F32 ? 16 : 8) || !al(x.cross.ptr, 8) || !al(x.aux.ptr, 8) ||
+  if (g.c.cs == 1 && !x.triu_m && (!al(g.c.ptr, g.c.dt == F32 ? 16 : 8) || !al(x.cross.ptr, 8) || !al(x.aux.ptr, 8) ||
                       !al(x.mask.ptr, 8) || !al(x.resid.ptr, 8)))
     return false;
   e->c = g.c.ptr; e->x = x.cross.ptr; e->aux = x.aux.ptr; e->mask = x.mask.ptr; e->resid = x.resid.ptr;
@@ -891,6 +926,17 @@ static bool make_lean(const Gemm& g, Lean* e) {
   e->flags = (x.accumulate ? EF_ACC : 0) | (x.relu ? EF_RELU : 0) | (x.mask.ptr ? EF_MASK : 0) |
              (x.cross.ptr ? EF_CROSS : 0) | (x.aux.ptr ? EF_AUX : 0) | (x.resid.ptr ? EF_RESID : 0) |
              (x.bias ? EF_BIAS : 0);
+  e->triu_m = x.triu_m;
+  if (x.dcn_bwd) {
+    if (g.c.dt != F32 || !x.cross.ptr || !x.mask.ptr || !x.aux.ptr || g.c.cs != 1 || x.bias || x.accumulate) return false;
+    e->flags = EF_DCNB;
+  }
+  if (x.triu_m) {
+    if (g.c.rs != 0 || g.c.rdiv || g.c.zdiv != 1 || x.bias || x.accumulate || x.cross.ptr || x.mask.ptr ||
+        x.resid.ptr || x.aux.ptr || x.relu)
+      return false;
+    e->flags = EF_TRIU;
+  }
   return true;
 }
 
@@ -961,6 +1007,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   p.lanes_rows = (g.c.cs != 1 && g.c.rs == 1 && splits == 1) ? 1 : 0;
   p.lean = (splits == 1 && make_lean(g, &p.ep)) ? 1 : 0;
   p.lean_id = p.lean ? lean_variant(p.ep.flags, p.ep.c_f32 != 0) : 0;
+  const bool special = p.lean && (p.ep.flags & (EF_DCNB | EF_TRIU));
   p.fast8 = 0;
   if (p.lean && g.c.cs == 1 && g.N % 8 == 0) {
     auto al16 = [](const void* q) { return !q || ((uintptr_t)q % 16) == 0; };
@@ -968,10 +1015,13 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
     bool ok = true;
     for (const View* v : vs)
       if (v->ptr && (!al16(v->ptr) || v->rs % 8 || v->bs0 % 8 || v->bs1 % 8 || v->rs_o % 8)) ok = false;
+    if (g.e.triu_m) ok = true;   // scalar stores into the packed triangle
     p.fast8 = ok ? 1 : 0;
   }
+  if (special && !(p.fast8 && p.lean_id > 0 && !p.lanes_rows)) { p.lean = 0; p.lean_id = 0; }   // generic epi_apply
   p.fast = (!p.lanes_rows && splits == 1 && vec_ok(g.c) && vec_ok(g.e.cross) && vec_ok(g.e.aux) &&
             vec_ok(g.e.resid) && vec_ok(g.e.mask)) ? 1 : 0;
+  if (special || g.e.triu_m || g.e.dcn_bwd) p.fast = 0;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a.mn_major << 15) | ((uint32_t)p.b.mn_major << 16) |
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   cudaError_t e = BN == 64 ? launch<64, 6>(p, ma, mb, st) : BN == 128 ? launch<128, 4>(p, ma, mb, st)

@@ -525,10 +525,11 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
     switch (md.s.kind) {
       case DHEN_DOT: {   // F1 + F2
         const int h = mi * (mi - 1) / 2;
+        // Gram X X^T per sample; the epilogue writes the strict upper triangle Z directly (F1, R7)
         Gemm g = mk(mi, mi, d, B, operand(X, dt, d, 1, (int64_t)mi * d), operand(X, dt, d, 1, (int64_t)mi * d),
-                    view(c->big, F32, mi, 1, (int64_t)mi * mi));
+                    view(md.Z, dt, 0, 1, h));
+        g.e.triu_m = mi;
         RET(G_(g, c, st, "dot.gram"));
-        KT("dot.triu", 0, (double)B * h * (4 + es), triu_extract(c->big, md.Z, dt, B, mi, h, st));
         Gemm v = mk(B, l * d, h, 1, operand(md.Z, dt, h, 1), operand(p(md.Wm), dt, h, 1), view(Us, F32, ldU, 1));
         RET(G_(v, c, st, "dot.proj"));
         break;
@@ -649,10 +650,19 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         RET(tokmix_bwd(c, X, mi, p(md.W), l, dU, ldU, acc, F32, 1, gp(md.W), B, st));
         break;
       case DHEN_DCN: {   // B8
-        void* dT = c->tA;
         void* dA = c->tB;
-        RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st));
-        KT("dcn.bwd_elem", 0, (double)rows * d * (4 * es + 8), dcn_bwd_elem(dT, X, md.A, dA, acc, dt, rows * d, st));
+        // dT = W_u dU (never stored): the epilogue forms dA = dT (.) X and dX += dT (.) A + dT (B8)
+        Gemm gt = mk(mi, d, l, B, operand(p(md.Wu), dt, l, 1), operand(dU, dt, 1, d, ldU),
+                     view(acc, F32, d, 1, (int64_t)mi * d));
+        gt.e.dcn_bwd = 1;
+        gt.e.cross = view((void*)X, dt, d, 1, (int64_t)mi * d);
+        gt.e.mask = view(md.A, dt, d, 1, (int64_t)mi * d);
+        gt.e.aux = view(dA, dt, d, 1, (int64_t)mi * d);
+        RET(G_(gt, c, st, "dcn.dT_fused"));
+        Gemm gw_u = mk(mi, l, B * d, 1, operand(md.T, dt, d, 1, 0, 0, 1, d, (int64_t)mi * d),
+                       operand(dU, dt, d, 1, 0, 0, 1, d, ldU), view(gp(md.Wu), F32, l, 1));
+        gw_u.e.accumulate = 1;
+        RET(G_(gw_u, c, st, "tokmix.wgrad"));
         Gemm gx = mk((int)rows, d, d, 1, operand(dA, dt, d, 1), operand(p(md.W), dt, 1, d), view(acc, F32, d, 1));
         gx.e.accumulate = 1;
         RET(G_(gx, c, st, "dcn.dgrad"));
