@@ -190,6 +190,12 @@ dhen_status dhen_profile_read(dhen_ctx* ctx, dhen_op_stat* out, int cap, int* n)
  * ws: fp32 device scratch for split-K partials. */
 dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* B, void* C, int ab_dtype, int c_dtype,
                             int path, void* ws, size_t ws_bytes, void* stream);
+/* Test hook: as dhen_debug_gemm plus one fused epilogue: mode 1 ReLU-mask by E (> 0), 2 residual
+ * + E, 3 DCN cross E (.) (acc + bias) + E with the pre-cross value stored to aux, 4 ReLU; E / aux are bf16
+ * with C's geometry; bias (bf16, nullable) is indexed by column. */
+dhen_status dhen_debug_gemm_epi(const long long* q, const void* A, const void* B, void* C, int ab_dtype, int c_dtype,
+                                int path, void* ws, size_t ws_bytes, int mode, const void* E, const void* bias,
+                                void* aux, void* stream);
 /* 1 if the last GEMM ran on the tcgen05 path. */
 int dhen_debug_last_gemm_tc(void);
 /* Debug: device buffer (>= 448 int64) receiving clock64 timestamps of CTA 0 of every following

@@ -23,7 +23,7 @@ STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_SHAPE", 3: "E_ALIGN", 4: "E_STATE", 5: "
 EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "dhen_init", "dhen_layer_fwd",
            "dhen_layer_bwd", "dhen_train_step", "dhen_train_step_graphed", "dhen_forward", "dhen_zero_grad", "dhen_params_io",
            "dhen_grads_get", "dhen_launch_count", "dhen_last_error", "dhen_destroy", "dhen_profile",
-           "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_last_gemm_tc",
+           "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_gemm_epi", "dhen_debug_last_gemm_tc",
            "dhen_debug_gemm_trace")
 
 
@@ -86,6 +86,7 @@ def load(path: str = LIB_PATH):
         "dhen_profile": [vp, i],
         "dhen_profile_read": [vp, C.POINTER(dhen_op_stat), i, C.POINTER(i)],
         "dhen_debug_gemm": [C.POINTER(C.c_longlong), vp, vp, vp, i, i, i, vp, sz, vp],
+        "dhen_debug_gemm_epi": [C.POINTER(C.c_longlong), vp, vp, vp, i, i, i, vp, sz, i, vp, vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -214,6 +215,23 @@ def debug_gemm(q, A, B, Cm, path=0, ws=None, stream=None):
     _check("dhen_debug_gemm", load().dhen_debug_gemm(arr, C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()),
                                                      C.c_void_p(Cm.data_ptr()), abt, ct, path,
                                                      C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(s.cuda_stream)))
+    return bool(load().dhen_debug_last_gemm_tc())
+
+
+def debug_gemm_epi(q, A, B, Cm, mode, E=None, bias=None, aux=None, path=0, ws=None, stream=None):
+    """Test hook: contraction + one fused epilogue (see dhen_debug_gemm_epi).  Returns True if tcgen05."""
+    import torch
+    q = list(q) + [0] * (30 - len(q))
+    arr = (C.c_longlong * 30)(*[int(v) for v in q])
+    abt = BF16 if A.dtype == torch.bfloat16 else FP32
+    ct = BF16 if Cm.dtype == torch.bfloat16 else FP32
+    if ws is None:
+        ws = torch.empty(64 << 20, dtype=torch.uint8, device=A.device)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    vp = lambda t: None if t is None else C.c_void_p(t.data_ptr())  # noqa: E731
+    _check("dhen_debug_gemm_epi", load().dhen_debug_gemm_epi(arr, vp(A), vp(B), vp(Cm), abt, ct, path, vp(ws),
+                                                             ws.numel(), mode, vp(E), vp(bias), vp(aux),
+                                                             C.c_void_p(s.cuda_stream)))
     return bool(load().dhen_debug_last_gemm_tc())
 
 

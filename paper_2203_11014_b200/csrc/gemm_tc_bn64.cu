@@ -1,0 +1,10 @@
+// gemm_tc_bn64.cu — instantiations of the tcgen05 GEMM kernel for BN = 64 (all epilogue variants).
+#include "gemm_tc_kernel.cuh"
+
+namespace dhen {
+namespace tc {
+cudaError_t launch_bn64(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st, int var) {
+  return launch_var<64, 6>(p, ma, mb, st, var);
+}
+}  // namespace tc
+}  // namespace dhen

@@ -1,0 +1,906 @@
+// gemm_tc_kernel.cuh — device side of the tcgen05 GEMM (see gemm_tc.cu for the host side and the
+// design notes).  Included by gemm_tc.cu and by the three per-tile-width instantiation units.
+#pragma once
+// bf16 GEMM on the 5th-generation tensor cores (sm_100a):
+// TMA (cp.async.bulk.tensor, 128B swizzle) fills a multi-stage shared-memory
+// ring guarded by mbarriers; one elected thread issues tcgen05.mma
+// (kind::f16, M = 128, N = BN, K = 16 per instruction) accumulating in TMEM;
+// tcgen05.commit releases ring slots and finally signals the epilogue; four
+// warps read the fp32 accumulator back with tcgen05.ld and apply the fused
+// epilogue (bias / DCN cross / ReLU / mask / residual / +=).
+//
+// Operands may be K-major or MN-major (transposed views of row-major tensors,
+// so dgrad / wgrad need no transpose kernels), batched through up to two
+// batch strides, and may have a two-level K (k -> (k / kdiv, k % kdiv)) so the
+// token-mixing weight gradients reduce over (sample, dim) in one GEMM.  Long K
+// with few output tiles is split across CTAs with a deterministic fixed-order
+// second pass.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "gemm.h"
+#include "gemm_epi.cuh"
+
+namespace dhen {
+namespace tc {
+
+constexpr int BM = 128, BK = 64;
+
+struct OpMap {
+  int mn_major;   // 1: MN contiguous (boxes of 64 MN x 64 K), 0: K contiguous (box 64 K x tile rows)
+  int has_ko;     // coordinate slot 2 holds k / kdiv
+  int kdiv;
+  int mo;         // coordinate slot of row / mdiv (-1: single-level rows)
+  int mdiv;
+  int z1, z0;     // coordinate slots of z % zdiv and z / zdiv (-1: operand not batched there)
+  int zdiv;
+};
+
+// Compact, host-resolved epilogue plan: every present view shares one row geometry
+// (offset = row term + batch term + col * cs), operands other than C are bf16.
+enum { EF_ACC = 1, EF_RELU = 2, EF_MASK = 4, EF_CROSS = 8, EF_AUX = 16, EF_RESID = 32, EF_BIAS = 64,
+       EF_DCNB = 128, EF_TRIU = 256 };
+struct Lean {
+  void* c;
+  const void* x;
+  void* aux;
+  const void* mask;
+  const void* resid;
+  const void* bias;
+  int64_t rs, rs_o, bs0, bs1, cs;
+  int rdiv, zdiv;
+  int c_f32, flags, gap_lo, gap_hi, hi_off;
+  int triu_m;
+  float alpha;
+};
+
+struct Params {
+  Gemm g;
+  Lean ep;
+  int lean;         // 1: use the lean epilogue plan
+  int lean_id;      // >0: compile-time specialised pass (8 columns per lane / 16 per row-lane)
+  OpMap a, b;
+  int tiles_m, tiles_n;
+  int n_fast;       // raster: N tiles fastest (tiles_n small) or M tiles fastest
+  int kblocks, splits, kb_per_split;
+  int zbase, nz;    // batch indices [zbase, zbase + nz) in this launch
+  int lanes_rows;   // epilogue: consecutive lanes on consecutive rows (output column-contiguous)
+  int fast;         // vectorised epilogue: 4 consecutive columns per lane (all views row-major, aligned)
+  int fast8;        // 8 consecutive columns per lane (N % 8 == 0, 16-B aligned rows)
+  float* ws;
+  uint32_t idesc;
+  long long* trace;   // debug: CTA 0 records clock64 timestamps (nullptr = off)
+  int dbg;            // debug: 1 = skip the global epilogue pass (timing experiments only)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity), "r"(0x989680)   // suspend-time hint (ns): sleep until the phase completes instead of spinning
+      : "memory");
+}
+__device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap* map, const int c[5], uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;   // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
+}
+
+__device__ __forceinline__ void ld4(const void* p, int64_t off, int dt, float* o) {
+  if (dt == F32) {
+    const float4 v = *reinterpret_cast<const float4*>(static_cast<const float*>(p) + off);
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  } else {
+    const uint2 v = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(p) + off);
+    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&v.x);
+    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&v.y);
+    const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+    o[0] = fa.x; o[1] = fa.y; o[2] = fb.x; o[3] = fb.y;
+  }
+}
+__device__ __forceinline__ void st4(void* p, int64_t off, int dt, const float* v) {
+  if (dt == F32) {
+    *reinterpret_cast<float4*>(static_cast<float*>(p) + off) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p) + off) = u;
+  }
+}
+// Per-row base offsets of every epilogue view (the column term is added per element).
+struct RowBase {
+  int64_t c, cross, aux, mask, resid;
+};
+__device__ __forceinline__ RowBase row_base(const Gemm& g, int z, int row) {
+  RowBase rb;
+  rb.c = g.c.off(z, row, 0);
+  rb.cross = g.e.cross.ptr ? g.e.cross.off(z, row, 0) : 0;
+  rb.aux = g.e.aux.ptr ? g.e.aux.off(z, row, 0) : 0;
+  rb.mask = g.e.mask.ptr ? g.e.mask.off(z, row, 0) : 0;
+  rb.resid = g.e.resid.ptr ? g.e.resid.off(z, row, 0) : 0;
+  return rb;
+}
+__device__ __forceinline__ float bias_at(const Epilogue& e, int j) {
+  if (!e.bias) return 0.f;
+  if (e.bias_gap_hi > e.bias_gap_lo) {
+    if (j >= e.bias_gap_lo && j < e.bias_gap_hi) return 0.f;
+    if (j >= e.bias_gap_hi) j = j - e.bias_gap_hi + e.bias_hi_off;
+  }
+  return ld_as_f32(e.bias, j, e.bias_dt);
+}
+// The fused epilogue of one element given its row bases (same math as epi_apply).
+__device__ __forceinline__ void epi_elem(const Gemm& g, const RowBase& rb, int col, float acc) {
+  const Epilogue& e = g.e;
+  float v = acc * e.alpha + bias_at(e, col);
+  if (e.cross.ptr) {
+    if (e.aux.ptr) st_from_f32(e.aux.ptr, rb.aux + col * e.aux.cs, e.aux.dt, v);
+    const float x = ld_as_f32(e.cross.ptr, rb.cross + col * e.cross.cs, e.cross.dt);
+    v = x * v + x;
+  } else if (e.aux.ptr) {
+    st_from_f32(e.aux.ptr, rb.aux + col * e.aux.cs, e.aux.dt, v);
+  }
+  if (e.relu) v = fmaxf(v, 0.f);
+  if (e.mask.ptr) v = ld_as_f32(e.mask.ptr, rb.mask + col * e.mask.cs, e.mask.dt) > 0.f ? v : 0.f;
+  if (e.resid.ptr) v += ld_as_f32(e.resid.ptr, rb.resid + col * e.resid.cs, e.resid.dt);
+  const int64_t co = rb.c + col * g.c.cs;
+  if (e.accumulate) v += ld_as_f32(g.c.ptr, co, g.c.dt);
+  st_from_f32(g.c.ptr, co, g.c.dt, v);
+}
+
+// Vectorised epilogue of 4 consecutive columns [col, col + 4) of one row (all views cs == 1).
+// Operands of a 4-column chunk are loaded first (epi4_load) for several rows, then combined and
+// stored (epi4_store): keeps several independent global loads in flight per lane.
+struct Chunk4 {
+  float x[4], m[4], r[4], c[4];
+};
+__device__ __forceinline__ void epi4_load(const Gemm& g, const RowBase& rb, int col, Chunk4& k) {
+  const Epilogue& e = g.e;
+  if (e.cross.ptr) ld4(e.cross.ptr, rb.cross + col, e.cross.dt, k.x);
+  if (e.mask.ptr) ld4(e.mask.ptr, rb.mask + col, e.mask.dt, k.m);
+  if (e.resid.ptr) ld4(e.resid.ptr, rb.resid + col, e.resid.dt, k.r);
+  if (e.accumulate) ld4(g.c.ptr, rb.c + col, g.c.dt, k.c);
+}
+__device__ __forceinline__ void epi4_store(const Gemm& g, const RowBase& rb, int col, float* a, const float* bias4,
+                                           const Chunk4& k) {
+  const Epilogue& e = g.e;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) a[t] = a[t] * e.alpha + bias4[t];
+  if (e.aux.ptr) st4(e.aux.ptr, rb.aux + col, e.aux.dt, a);
+  if (e.cross.ptr) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] = k.x[t] * a[t] + k.x[t];
+  }
+  if (e.relu) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] = fmaxf(a[t], 0.f);
+  }
+  if (e.mask.ptr) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] = k.m[t] > 0.f ? a[t] : 0.f;
+  }
+  if (e.resid.ptr) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] += k.r[t];
+  }
+  if (e.accumulate) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] += k.c[t];
+  }
+  st4(g.c.ptr, rb.c + col, g.c.dt, a);
+}
+
+// ---- explicit-state-space memory helpers for the epilogue (no generic addressing)
+__device__ __forceinline__ void sts4(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void unpack_bf4(const uint2 u, float* o) {
+  o[0] = __uint_as_float(u.x << 16); o[1] = __uint_as_float(u.x & 0xffff0000u);
+  o[2] = __uint_as_float(u.y << 16); o[3] = __uint_as_float(u.y & 0xffff0000u);
+}
+__device__ __forceinline__ void ldg_bf4(const void* base, int64_t off, float* o) {
+  unpack_bf4(__ldg(reinterpret_cast<const uint2*>((const __nv_bfloat16*)base + off)), o);
+}
+__device__ __forceinline__ void ldg_c4(const void* base, int64_t off, int f32, float* o) {
+  if (f32) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>((const float*)base + off));
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  } else {
+    unpack_bf4(__ldcg(reinterpret_cast<const uint2*>((const __nv_bfloat16*)base + off)), o);
+  }
+}
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void stg4(void* base, int64_t off, int f32, const float* v) {
+  if (f32) {
+    __stwb(reinterpret_cast<float4*>((float*)base + off), make_float4(v[0], v[1], v[2], v[3]));
+  } else {
+    uint2 u;
+    u.x = pack_bf2(v[0], v[1]);
+    u.y = pack_bf2(v[2], v[3]);
+    __stwb(reinterpret_cast<uint2*>((__nv_bfloat16*)base + off), u);
+  }
+}
+__device__ __forceinline__ float ldg_bf1(const void* base, int64_t off) {
+  const unsigned short u = __ldg(reinterpret_cast<const unsigned short*>((const __nv_bfloat16*)base + off));
+  return __uint_as_float(((uint32_t)u) << 16);
+}
+__device__ __forceinline__ float ldg_c1(const void* base, int64_t off, int f32) {
+  if (f32) return __ldcg((const float*)base + off);
+  const unsigned short u = __ldcg(reinterpret_cast<const unsigned short*>((const __nv_bfloat16*)base + off));
+  return __uint_as_float(((uint32_t)u) << 16);
+}
+__device__ __forceinline__ void stg1(void* base, int64_t off, int f32, float v) {
+  if (f32) {
+    __stwb((float*)base + off, v);
+  } else {
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    __stwb(reinterpret_cast<unsigned short*>((__nv_bfloat16*)base + off), *reinterpret_cast<const unsigned short*>(&h));
+  }
+}
+__device__ __forceinline__ int64_t lean_row(const Lean& e, int z, int row) {
+  int64_t o;
+  if (e.rdiv) {
+    const unsigned q = (unsigned)row / (unsigned)e.rdiv;
+    o = (int64_t)q * e.rs_o + (int64_t)((unsigned)row - q * (unsigned)e.rdiv) * e.rs;
+  } else {
+    o = (int64_t)row * e.rs;
+  }
+  if (e.zdiv == 1) {
+    o += (int64_t)z * e.bs0;
+  } else {
+    const unsigned q = (unsigned)z / (unsigned)e.zdiv;
+    o += (int64_t)q * e.bs0 + (int64_t)((unsigned)z - q * (unsigned)e.zdiv) * e.bs1;
+  }
+  return o;
+}
+__device__ __forceinline__ float lean_bias(const Lean& e, int j) {
+  if (e.gap_hi > e.gap_lo) {
+    if (j >= e.gap_lo && j < e.gap_hi) return 0.f;
+    if (j >= e.gap_hi) j = j - e.gap_hi + e.hi_off;
+  }
+  return ldg_bf1(e.bias, j);
+}
+// one element of the lean epilogue
+__device__ __forceinline__ void lean1(const Lean& e, int64_t o, float v, float bias) {
+  const int f = e.flags;
+  v = v * e.alpha + bias;
+  if (f & EF_AUX) stg1(e.aux, o, 0, v);
+  if (f & EF_CROSS) { const float x = ldg_bf1(e.x, o); v = x * v + x; }
+  if (f & EF_RELU) v = fmaxf(v, 0.f);
+  if (f & EF_MASK) v = ldg_bf1(e.mask, o) > 0.f ? v : 0.f;
+  if (f & EF_RESID) v += ldg_bf1(e.resid, o);
+  if (f & EF_ACC) v += ldg_c1(e.c, o, e.c_f32);
+  stg1(e.c, o, e.c_f32, v);
+}
+
+// ---- compile-time specialised epilogue passes (one per (flags, C dtype) in use; see lean_variant())
+// Global accesses through intrinsics (no asm volatile / memory clobbers) so the compiler can issue
+// the loads of several rows ahead of earlier stores.
+__device__ __forceinline__ void unpack_bf8(const uint4 u, float* o) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int t = 0; t < 4; ++t) { o[2 * t] = __uint_as_float(w[t] << 16); o[2 * t + 1] = __uint_as_float(w[t] & 0xffff0000u); }
+}
+__device__ __forceinline__ void ldg_bf8(const void* base, int64_t off, float* o) {
+  unpack_bf8(__ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)base + off)), o);
+}
+template <bool CF32>
+__device__ __forceinline__ void ldg_c8(const void* base, int64_t off, float* o) {
+  if (CF32) {
+    const float4* q = reinterpret_cast<const float4*>((const float*)base + off);
+    const float4 a = __ldcg(q), b = __ldcg(q + 1);
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+  } else {
+    unpack_bf8(__ldcg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)base + off)), o);
+  }
+}
+template <bool CF32>
+__device__ __forceinline__ void stg8(void* base, int64_t off, const float* v) {
+  if (CF32) {
+    float4* q = reinterpret_cast<float4*>((float*)base + off);
+    __stwb(q, make_float4(v[0], v[1], v[2], v[3]));
+    __stwb(q + 1, make_float4(v[4], v[5], v[6], v[7]));
+  } else {
+    uint4 u;
+    u.x = pack_bf2(v[0], v[1]); u.y = pack_bf2(v[2], v[3]); u.z = pack_bf2(v[4], v[5]); u.w = pack_bf2(v[6], v[7]);
+    __stwb(reinterpret_cast<uint4*>((__nv_bfloat16*)base + off), u);
+  }
+}
+__device__ __forceinline__ int64_t shfl64(int64_t v, int src) {
+  const int lo = __shfl_sync(0xffffffffu, (int)(v & 0xffffffff), src);
+  const int hi = __shfl_sync(0xffffffffu, (int)(v >> 32), src);
+  return ((int64_t)hi << 32) | (uint32_t)lo;
+}
+// Row-major output, 8 consecutive columns per lane (N % 8 == 0, 16-B aligned rows).  Rows are handled
+// in groups of G: first every extra operand of the group is loaded (all loads in flight together),
+// then the group is combined and stored -- one memory latency per group instead of per row.
+template <int F, bool CF32, int SC>
+__device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int M, int N, int cbase, uint32_t stage,
+                                           int lane) {
+  constexpr int LPR = SC / 8, RPP = 32 / LPR, SROW = SC + 4;
+  constexpr int NR = 32 / RPP;                               // rows per lane in this pass
+  // operands to prefetch per row: bf16 uint4 slots (X / A / mask / resid / bf16 C) and fp32 C
+  constexpr int NB = ((F & (EF_CROSS | EF_DCNB)) ? 1 : 0) + ((F & (EF_MASK | EF_DCNB)) ? 1 : 0) +
+                     ((F & EF_RESID) ? 1 : 0) + (((F & EF_ACC) && !CF32) ? 1 : 0);
+  constexpr bool F32C = ((F & EF_ACC) && CF32) || (F & EF_DCNB);
+  constexpr int REGS = NB * 4 + (F32C ? 8 : 0);               // registers per prefetched row
+  constexpr int SLX = 0;                                                     // compile-time slot indices
+  constexpr int SLM = SLX + ((F & (EF_CROSS | EF_DCNB)) ? 1 : 0);
+  constexpr int SLR = SLM + ((F & (EF_MASK | EF_DCNB)) ? 1 : 0);
+  constexpr int SLC = SLR + ((F & EF_RESID) ? 1 : 0);
+  constexpr int G0 = REGS == 0 ? NR : (REGS <= 4 ? 8 : REGS <= 8 ? 4 : 2);
+  constexpr int G = G0 < NR ? G0 : NR;                          // rows per load group
+  const int sub = lane / LPR, cl = lane % LPR;
+  const int col = cbase + 8 * cl;
+  const bool cok = col < N;
+  const int64_t my_off = (rbase + lane < M) ? lean_row(e, z, rbase + lane) : 0;   // row offset of row `lane`
+  float bias8[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) bias8[t] = 0.f;
+  if ((F & EF_BIAS) && cok) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) bias8[t] = lean_bias(e, col + t);
+  }
+  const float alpha = e.alpha;
+#pragma unroll
+  for (int g0 = 0; g0 < NR; g0 += G) {
+    int64_t o[G];
+    bool ok[G];
+    uint4 ub[G][NB > 0 ? NB : 1];
+    float cv[G][F32C ? 8 : 1];
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const int r = sub + (g0 + k) * RPP;
+      o[k] = shfl64(my_off, r) + col;
+      ok[k] = cok && (rbase + r < M);
+      if (ok[k]) {
+        if constexpr ((F & (EF_CROSS | EF_DCNB)) != 0)
+          ub[k][SLX] = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.x + o[k]));
+        if constexpr ((F & (EF_MASK | EF_DCNB)) != 0)
+          ub[k][SLM] = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.mask + o[k]));
+        if constexpr ((F & EF_RESID) != 0)
+          ub[k][SLR] = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.resid + o[k]));
+        if constexpr ((F & EF_ACC) != 0 && !CF32)
+          ub[k][SLC] = __ldcg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.c + o[k]));
+        if constexpr (F32C) ldg_c8<true>(e.c, o[k], cv[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      if (!ok[k]) continue;
+      const int r = sub + (g0 + k) * RPP;
+      const uint32_t sa = stage + (uint32_t)((r * SROW + 8 * cl) * 4);
+      const float4 x0 = lds4(sa), x1 = lds4(sa + 16);
+      float a[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+      if (F & EF_TRIU) {
+        // strict upper triangle of the per-sample Gram: pairs (i, j > i) row-major (R7)
+        const int i = rbase + r;
+        const int64_t zb = o[k] - col - (int64_t)i * e.rs;     // = z * bs0 (rs = 0 for this view)
+        const int64_t base = zb + (int64_t)i * e.triu_m - (int64_t)i * (i + 1) / 2 - i - 1;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (col + t > i) stg1(e.c, base + col + t, CF32, a[t] * alpha);
+        continue;
+      }
+      if (F & EF_DCNB) {
+        // B8 fused: dA = dT * X (bf16, aux), dX_acc += dT * A + dT  (dT = the fp32 accumulator)
+        float xv[8], av[8], da[8];
+        unpack_bf8(ub[k][SLX], xv);
+        unpack_bf8(ub[k][SLM], av);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const float v = a[t] * alpha;
+          da[t] = v * xv[t];
+          cv[k][t] += v * av[t] + v;
+        }
+        stg8<false>(e.aux, o[k], da);
+        stg8<true>(e.c, o[k], cv[k]);
+        continue;
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] = a[t] * alpha + bias8[t];
+      float t8[8];
+      if (F & EF_AUX) stg8<false>(e.aux, o[k], a);
+      if constexpr ((F & EF_CROSS) != 0) {
+        unpack_bf8(ub[k][SLX], t8);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) a[t] = t8[t] * a[t] + t8[t];
+      }
+      if (F & EF_RELU) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) a[t] = fmaxf(a[t], 0.f);
+      }
+      if constexpr ((F & EF_MASK) != 0) {
+        unpack_bf8(ub[k][SLM], t8);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) a[t] = t8[t] > 0.f ? a[t] : 0.f;
+      }
+      if constexpr ((F & EF_RESID) != 0) {
+        unpack_bf8(ub[k][SLR], t8);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) a[t] += t8[t];
+      }
+      if (F & EF_ACC) {
+        if (CF32) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) a[t] += cv[k][t];
+        } else {
+          unpack_bf8(ub[k][SLC], t8);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) a[t] += t8[t];
+        }
+      }
+      stg8<CF32>(e.c, o[k], a);
+    }
+  }
+}
+// Column-contiguous output (cs != 1, rs == 1): one row per lane, 16 accumulator columns in registers.
+template <int F, bool CF32>
+__device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0, int N, const uint32_t* v) {
+  if constexpr ((F & (EF_DCNB | EF_TRIU)) != 0) return;   // host never selects these in column-contiguous mode
+  const float alpha = e.alpha;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int col = col0 + j;
+    if (col >= N) break;
+    const int64_t o = lo + (int64_t)col * e.cs;
+    float a = __uint_as_float(v[j]) * alpha;
+    if (F & EF_BIAS) a += lean_bias(e, col);
+    if (F & EF_AUX) stg1(e.aux, o, 0, a);
+    if (F & EF_CROSS) { const float x = ldg_bf1(e.x, o); a = x * a + x; }
+    if (F & EF_RELU) a = fmaxf(a, 0.f);
+    if (F & EF_MASK) a = ldg_bf1(e.mask, o) > 0.f ? a : 0.f;
+    if (F & EF_RESID) a += ldg_bf1(e.resid, o);
+    if (F & EF_ACC) a += ldg_c1(e.c, o, CF32);
+    stg1(e.c, o, CF32, a);
+  }
+}
+// The (flags, C dtype) combinations the DHEN step uses get a specialised loop; id 0 = none.
+#define LEAN_VARIANTS(X)                          \
+  X(1, 0, true)                                   \
+  X(2, 0, false)                                  \
+  X(3, EF_ACC, true)                              \
+  X(4, EF_BIAS | EF_RELU, false)                  \
+  X(5, EF_BIAS | EF_RESID, true)                  \
+  X(6, EF_RESID, true)                            \
+  X(7, EF_MASK, false)                            \
+  X(8, EF_BIAS | EF_CROSS | EF_AUX, false)        \
+  X(9, EF_BIAS, false)                            \
+  X(10, EF_BIAS, true)                            \
+  X(11, EF_ACC, false)                            \
+  X(12, EF_DCNB, true)                            \
+  X(13, EF_TRIU, false)                           \
+  X(14, EF_TRIU, true)                            \
+  X(15, EF_RELU, false)                           \
+  X(16, EF_RESID, false)                          \
+  X(17, EF_MASK, true)                            \
+  X(18, EF_BIAS | EF_CROSS, false)
+static inline int lean_variant(int flags, bool cf32) {
+#define LV_ID(id, f, c) if (flags == (f) && cf32 == (c)) return id;
+  LEAN_VARIANTS(LV_ID)
+#undef LV_ID
+  return 0;
+}
+template <int V> struct VarF {   // variant id -> (flags, fp32 C)
+  static constexpr int F = 0;
+  static constexpr bool C = false;
+};
+#define LV_SPEC(i, f, c)                    \
+  template <> struct VarF<i> {              \
+    static constexpr int F = (f);           \
+    static constexpr bool C = (c);          \
+  };
+LEAN_VARIANTS(LV_SPEC)
+#undef LV_SPEC
+
+template <int TILE>
+__device__ __forceinline__ void load_operand(const CUtensorMap* map, const OpMap& om, uint32_t dst, int mn0, int k,
+                                             int z, uint32_t mbar) {
+  int c[5] = {0, 0, 0, 0, 0};
+  const int kin = om.has_ko ? k % om.kdiv : k;
+  if (om.has_ko) c[2] = k / om.kdiv;
+  if (om.mo >= 0) { c[om.mo] = mn0 / om.mdiv; mn0 = mn0 % om.mdiv; }
+  if (om.z1 >= 0) c[om.z1] = z % om.zdiv;
+  if (om.z0 >= 0) c[om.z0] = z / om.zdiv;
+  if (!om.mn_major) {
+    c[0] = kin;
+    c[1] = mn0;
+    tma_load5(dst, map, c, mbar);
+  } else {
+#pragma unroll
+    for (int j = 0; j < TILE / 64; ++j) {
+      c[0] = mn0 + 64 * j;
+      c[1] = kin;
+      tma_load5(dst + j * 64 * BK * 2, map, c, mbar);
+    }
+  }
+}
+
+// Persistent, warp-specialised kernel: warp 0 = TMA producer, warp 1 = MMA issuer,
+// warps 2-9 = epilogue.  Work items (tile, batch index, K split) are strided over
+// the grid.  The TMEM accumulator is double-buffered (2 x BN columns) so the
+// epilogue of item i overlaps the MMAs of item i+1 and the loads of item i+2.
+template <int BN, int STAGES, int VAR>
+__global__ void __launch_bounds__(320, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                   const __grid_constant__ Params p) {
+  constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
+  constexpr int SC = BN / 2 < 64 ? BN / 2 : 64;   // columns staged per epilogue pass
+  constexpr int SROW = SC + 4;              // float4 rows; 16-B granules conflict-free both ways
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  float* stage_all = (float*)(sB + STAGES * B_BYTES);
+  uint64_t* bars = (uint64_t*)(stage_all + 8 * 32 * SROW);   // full[S], empty[S], tfull[2], tempty[2]
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = p.tiles_m * p.tiles_n;
+  const int total = ntiles * p.nz * p.splits;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+    for (int s = 0; s < 2 * STAGES + 2; ++s) mbar_init(smem_u32(bars + s), 1);
+    for (int s = 0; s < 2; ++s) mbar_init(smem_u32(tempty + s), 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  auto decode = [&](int item, int& m0, int& n0, int& z, int& sp, int& kb0, int& nk) {
+    const int tile = item % ntiles;
+    const int zs = item / ntiles;
+    sp = zs % p.splits;
+    z = p.zbase + zs / p.splits;
+    if (p.n_fast) {   // tall-skinny: the N tiles of one M row-block run together (A read once from DRAM)
+      m0 = (tile / p.tiles_n) * BM;
+      n0 = (tile % p.tiles_n) * BN;
+    } else {
+      m0 = (tile % p.tiles_m) * BM;
+      n0 = (tile / p.tiles_m) * BN;
+    }
+    kb0 = sp * p.kb_per_split;
+    nk = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int it = 0;
+      for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        int m0, n0, z, sp, kb0, nk;
+        decode(item, m0, n0, z, sp, kb0, nk);
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(smem_u32(empty + s), ph ^ 1);
+          if (p.trace && blockIdx.x == 0 && it < 64) p.trace[it] = clock64();
+          const uint32_t fb = smem_u32(full + s);
+          mbar_expect_tx(fb, A_BYTES + B_BYTES);
+          const int k = (kb0 + i) * BK;
+          load_operand<BM>(&tma_a, p.a, smem_u32(sA + s * A_BYTES), m0, k, z, fb);
+          load_operand<BN>(&tma_b, p.b, smem_u32(sB + s * B_BYTES), n0, k, z, fb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread)
+      const uint32_t a_step = p.a.mn_major ? 16 * 128 : 32;   // bytes per K = 16 slice
+      const uint32_t b_step = p.b.mn_major ? 16 * 128 : 32;
+      const uint32_t a_lbo = p.a.mn_major ? 64 * BK * 2 : 16, b_lbo = p.b.mn_major ? 64 * BK * 2 : 16;
+      int it = 0, li = 0;
+      for (int item = blockIdx.x; item < total; item += gridDim.x, ++li) {
+        int m0, n0, z, sp, kb0, nk;
+        decode(item, m0, n0, z, sp, kb0, nk);
+        const int ab = li & 1;
+        const uint32_t aph = (li >> 1) & 1;
+        mbar_wait(smem_u32(tempty + ab), aph ^ 1);      // epilogue drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (p.trace && blockIdx.x == 0 && li < 64) p.trace[64 + li] = clock64();
+        const uint32_t dacc = tmem + (uint32_t)(ab * BN);
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(smem_u32(full + s), ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (p.trace && blockIdx.x == 0 && it < 64) p.trace[128 + it] = clock64();
+          const uint32_t ab_ = smem_u32(sA + s * A_BYTES), bb_ = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = sdesc(ab_ + kk * a_step, a_lbo, 1024);
+            const uint64_t bd = sdesc(bb_ + kk * b_step, b_lbo, 1024);
+            mma_f16(dacc, ad, bd, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(smem_u32(empty + s));               // ring slot free once these MMAs complete
+        }
+        mma_commit(smem_u32(tfull + ab));                // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..9: warp w reads TMEM lanes [32 (w % 4), +32) (hardware rule)
+    // and column half hh of the accumulator; 8 warps keep enough stores / loads in flight.
+    const int q4 = warp & 3;
+    const int hh = (warp - 2) >> 2;
+    constexpr int HC = BN / 2;                 // columns per warp
+    const uint32_t stage = smem_u32(stage_all) + (uint32_t)((warp - 2) * 32 * SROW * 4);
+    const Gemm& g = p.g;
+    const Lean& e = p.ep;
+    int li = 0;
+    for (int item = blockIdx.x; item < total; item += gridDim.x, ++li) {
+      int m0, n0, z, sp, kb0, nk;
+      decode(item, m0, n0, z, sp, kb0, nk);
+      const int ab = li & 1;
+      const uint32_t aph = (li >> 1) & 1;
+      mbar_wait(smem_u32(tfull + ab), aph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[192 + li] = clock64();
+      const int rbase = m0 + q4 * 32;
+      if (p.lanes_rows) {
+        // column-contiguous output: row per lane straight from TMEM; consecutive lanes = consecutive addresses
+        const int row = rbase + lane;
+        const bool rok = row < g.M;
+        RowBase rb;
+        int64_t lo = 0;
+        if (rok) { if (p.lean) lo = lean_row(e, z, row); else rb = row_base(g, z, row); }
+#pragma unroll 1
+        for (int c0 = hh * HC; c0 < hh * HC + HC; c0 += 16) {
+          uint32_t v[16];
+          const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                "=r"(v[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (c0 + 16 >= hh * HC + HC) {
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty + ab)) : "memory");
+          }
+          if (rok && n0 + c0 < g.N) {
+            if constexpr (VAR > 0) {
+              lean_rows16<VarF<VAR>::F, VarF<VAR>::C>(e, lo, n0 + c0, g.N, v);
+            } else if (p.lean) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const int col = n0 + c0 + j;
+                if (col < g.N)
+                  lean1(e, lo + (int64_t)col * e.cs, __uint_as_float(v[j]), (e.flags & EF_BIAS) ? lean_bias(e, col) : 0.f);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const int col = n0 + c0 + j;
+                if (col < g.N) epi_elem(g, rb, col, __uint_as_float(v[j]));
+              }
+            }
+          }
+        }
+        continue;
+      }
+      // row-major output: park this warp's 32 x SC block in smem, then walk it with lanes on columns
+#pragma unroll 1
+      for (int pc = 0; pc < HC; pc += SC) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < SC; c0 += 16) {
+          uint32_t v[16];
+          const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC + pc + c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                "=r"(v[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          const uint32_t dst = stage + (uint32_t)((lane * SROW + c0) * 4);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            sts4(dst + 16 * j, __uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
+                 __uint_as_float(v[4 * j + 3]));
+        }
+        if (pc + SC >= HC) {
+          if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[256 + li] = clock64();
+          // accumulator fully read: hand it back to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty + ab)) : "memory");
+        }
+        __syncwarp();
+        const int cbase = n0 + hh * HC + pc;
+        if (p.dbg == 1) {
+        } else if (VAR > 0) {
+          if constexpr (VAR > 0) lean_pass8<VarF<VAR>::F, VarF<VAR>::C, SC>(e, z, rbase, g.M, g.N, cbase, stage, lane);
+        } else if (p.lean && p.fast) {
+          constexpr int LPR = SC / 4;          // lanes per row (4 columns each)
+          constexpr int RPP = 32 / LPR;        // rows per pass
+          const int sub = lane / LPR, cl = lane % LPR;
+          const int col = cbase + 4 * cl;
+          if (col < g.N) {                     // N % 4 == 0 in lean/fast mode: the 4 columns are all valid
+            float bias4[4] = {0.f, 0.f, 0.f, 0.f};
+            if (e.flags & EF_BIAS) {
+#pragma unroll
+              for (int t = 0; t < 4; ++t) bias4[t] = lean_bias(e, col + t);
+            }
+            const int f = e.flags;
+#pragma unroll 4
+            for (int r = sub; r < 32; r += RPP) {
+              const int row = rbase + r;
+              if (row >= g.M) break;
+              const int64_t o = lean_row(e, z, row) + col;
+              const float4 a4 = lds4(stage + (uint32_t)((r * SROW + 4 * cl) * 4));
+              float a[4] = {a4.x * e.alpha + bias4[0], a4.y * e.alpha + bias4[1], a4.z * e.alpha + bias4[2],
+                            a4.w * e.alpha + bias4[3]};
+              float t4[4];
+              if (f & EF_AUX) stg4(e.aux, o, 0, a);
+              if (f & EF_CROSS) {
+                ldg_bf4(e.x, o, t4);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) a[t] = t4[t] * a[t] + t4[t];
+              }
+              if (f & EF_RELU) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) a[t] = fmaxf(a[t], 0.f);
+              }
+              if (f & EF_MASK) {
+                ldg_bf4(e.mask, o, t4);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) a[t] = t4[t] > 0.f ? a[t] : 0.f;
+              }
+              if (f & EF_RESID) {
+                ldg_bf4(e.resid, o, t4);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) a[t] += t4[t];
+              }
+              if (f & EF_ACC) {
+                ldg_c4(e.c, o, e.c_f32, t4);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) a[t] += t4[t];
+              }
+              if (p.dbg == 2) { if (a[0] == 12345.f) stg4(e.c, o, e.c_f32, a); }
+              else stg4(e.c, o, e.c_f32, a);
+            }
+          }
+        } else if (p.dbg == 3) {
+          // debug: stores only
+          constexpr int LPR = SC / 4;
+          constexpr int RPP = 32 / LPR;
+          const int sub = lane / LPR, cl = lane % LPR;
+          const int col = cbase + 4 * cl;
+          float a[4] = {0.f, 0.f, 0.f, 0.f};
+          if (col < g.N)
+            for (int r = sub; r < 32; r += RPP) {
+              const int row = rbase + r;
+              if (row >= g.M) break;
+              stg4(e.c, (int64_t)row * e.rs + col, e.c_f32, a);
+            }
+        } else {
+          // generic path (split-K partials, irregular views)
+          const float* stg = stage_all + (warp - 2) * 32 * SROW;
+#pragma unroll 1
+          for (int r = 0; r < 32; ++r) {
+            const int row = rbase + r;
+            if (row >= g.M) break;
+            RowBase rb;
+            if (p.splits == 1) rb = row_base(g, z, row);
+#pragma unroll
+            for (int q = 0; q < SC / 32; ++q) {
+              const int col = cbase + lane + 32 * q;
+              if (col < g.N) {
+                const float acc = stg[r * SROW + lane + 32 * q];
+                if (p.splits == 1) {
+                  if (g.e.triu_m || g.e.dcn_bwd) epi_apply(g, z, row, col, acc);
+                  else epi_elem(g, rb, col, acc);
+                }
+                else p.ws[((int64_t)(z * p.splits + sp) * g.M + row) * g.N + col] = acc;
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[320 + li] = clock64();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+}
+
+template <int BN, int STAGES, int VAR>
+static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st) {
+  constexpr int SC = BN / 2 < 64 ? BN / 2 : 64;
+  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + 8 * 32 * (SC + 4) * 4 + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static_assert(SMEM <= 227 * 1024, "smem");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  const int ntiles = p0.tiles_m * p0.tiles_n;
+  const int zmax = std::max(1, (int)std::min<int64_t>(p0.g.batch, (int64_t)(1 << 30) / ((int64_t)ntiles * p0.splits)));
+  for (int zb = 0; zb < p0.g.batch; zb += zmax) {
+    Params p = p0;
+    p.zbase = zb;
+    p.nz = std::min(zmax, p0.g.batch - zb);
+    const int64_t items = (int64_t)ntiles * p.nz * p.splits;
+    const int grid = (int)std::min<int64_t>(items, 148);
+    gemm_tc_kernel<BN, STAGES, VAR><<<grid, 320, SMEM, st>>>(ma, mb, p);
+    ++g_launches;
+  }
+  return cudaGetLastError();
+}
+
+// Launch with the epilogue variant as a template argument (one variant per kernel instantiation).
+template <int BN, int STAGES>
+cudaError_t launch_var(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st, int var) {
+  switch (var) {
+#define LV_L(i, f, c) \
+  case i: return launch<BN, STAGES, i>(p, ma, mb, st);
+    LEAN_VARIANTS(LV_L)
+#undef LV_L
+    default: return launch<BN, STAGES, 0>(p, ma, mb, st);
+  }
+}
+// defined in gemm_tc_bn{64,128,256}.cu (parallel compilation of the instantiations)
+cudaError_t launch_bn64(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st, int var);
+cudaError_t launch_bn128(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st, int var);
+cudaError_t launch_bn256(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st, int var);
+
+}  // namespace tc
+}  // namespace dhen

@@ -968,6 +968,41 @@ dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* Bp, v
 
 int dhen_debug_last_gemm_tc(void) { return g_last_gemm_tc; }
 
+dhen_status dhen_debug_gemm_epi(const long long* q, const void* A, const void* Bp, void* Cp, int ab_dt, int c_dt,
+                                int path, void* ws, size_t ws_bytes, int mode, const void* E, const void* bias,
+                                void* aux, void* stream) {
+  if (!q || !A || !Bp || !Cp) return fail(DHEN_E_ALIGN, "dhen_debug_gemm_epi: NULL argument");
+  const int abt = ab_dt == DHEN_BF16 ? BF16 : F32, ct = c_dt == DHEN_BF16 ? BF16 : F32;
+  Gemm g = mk((int)q[0], (int)q[1], (int)q[2], (int)q[3],
+              operand(A, abt, q[4], q[5], q[6], q[7], (int)q[8], (int)q[9], q[10]),
+              operand(Bp, abt, q[11], q[12], q[13], q[14], (int)q[15], (int)q[16], q[17]),
+              view(Cp, ct, q[18], q[19], q[20], q[21], (int)q[22]));
+  g.e.accumulate = (int)q[23];
+  g.a.mdiv = (int)q[24]; g.a.s_mo = q[25];
+  g.b.mdiv = (int)q[26]; g.b.s_mo = q[27];
+  g.c.rdiv = (int)q[28]; g.c.rs_o = q[29];
+  View ev = g.c;   // the extra operand shares C's geometry, in bf16
+  ev.dt = BF16;
+  ev.ptr = const_cast<void*>(E);
+  if (bias) { g.e.bias = bias; g.e.bias_dt = BF16; }
+  switch (mode) {   // 1 mask, 2 residual, 3 DCN cross (+ aux), 4 relu, 0 none
+    case 1: g.e.mask = ev; break;
+    case 2: g.e.resid = ev; break;
+    case 3: g.e.cross = ev; if (aux) { g.e.aux = ev; g.e.aux.ptr = aux; } break;
+    case 4: g.e.relu = 1; break;
+    default: break;
+  }
+  Workspace w;
+  w.ptr = (float*)ws;
+  w.bytes = ws_bytes;
+  dhen::g_gemm_force = path;
+  cudaError_t e = gemm_run(g, w, S(stream));
+  dhen::g_gemm_force = -1;
+  if (e == cudaErrorNotSupported) return fail(DHEN_E_CONFIG, "dhen_debug_gemm_epi: layout not supported on this path");
+  CK(e);
+  return DHEN_OK;
+}
+
 void dhen_debug_gemm_trace(void* dev_buf) { g_gemm_trace = (long long*)dev_buf; }
 
 dhen_status dhen_profile(dhen_ctx* c, int enable) {

@@ -9,7 +9,6 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2203_11014_b200.binding import debug_gemm  # noqa: E402
 
 
 def shapes(cfg):
@@ -76,6 +75,7 @@ def main():
     ap.add_argument("--path", type=int, default=0)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--flush", default="write", choices=["write", "read", "none"])
+    ap.add_argument("--epi", type=int, default=0, help="fused epilogue mode (1 mask, 2 resid, 3 cross, 4 relu)")
     args = ap.parse_args()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -88,6 +88,15 @@ def main():
         cext = extent(M, N, Z, rs, cs, cb0, cb1, czd, 0, 0, *c2)
         Cm = torch.zeros(cext, device="cuda", dtype=cdt)
         q = [M, N, K, Z] + list(a) + list(b) + list(c) + [acc] + list(a2) + list(b2) + list(c2)
+        E = torch.randn(cext, device="cuda").to(torch.bfloat16) if args.epi else None
+        aux = torch.empty(cext, device="cuda", dtype=torch.bfloat16) if args.epi == 3 else None
+        if args.epi:
+            from paper_2203_11014_b200.binding import debug_gemm_epi
+
+            def debug_gemm(q, A, Bm, Cm, path=0, ws=None):  # noqa: F811
+                return debug_gemm_epi(q, A, Bm, Cm, args.epi, E=E, aux=aux, path=path, ws=ws)
+        else:
+            from paper_2203_11014_b200.binding import debug_gemm
         tc = debug_gemm(q, A, Bm, Cm, path=args.path, ws=ws)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.iters)]
         for e0, e1 in ev:
