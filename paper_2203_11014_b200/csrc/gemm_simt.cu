@@ -77,16 +77,34 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(Gemm g, int splits, int 
     }
 }
 
-__global__ void splitk_reduce_kernel(Gemm g, int splits, const float* ws) {
-  // partial tiles ws[(z * splits + sp)][M][N] summed in fixed split order, then the epilogue
-  int64_t total = (int64_t)g.batch * g.M * g.N;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t zb = t / ((int64_t)g.M * g.N);
-    int64_t r = t % ((int64_t)g.M * g.N);
-    int i = (int)(r / g.N), j = (int)(r % g.N);
-    float s = 0.f;
-    for (int sp = 0; sp < splits; ++sp) s += ws[((zb * splits + sp) * g.M + i) * (int64_t)g.N + j];
-    epi_apply(g, (int)zb, i, j, s);
+// Split-K reduction: block = 32 consecutive output elements (tx) x 8 split lanes (ty); split lane ty
+// sums splits ty, ty+8, ... (two independent chains), then the 8 lane sums are combined in fixed order
+// -> deterministic, and ~splits/8 dependent loads per thread instead of splits.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(Gemm g, int splits, const float* ws) {
+  __shared__ float red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t mn = (int64_t)g.M * g.N;
+  const int64_t total = (int64_t)g.batch * mn;
+  for (int64_t e0 = (int64_t)blockIdx.x * 32; e0 < total; e0 += (int64_t)gridDim.x * 32) {
+    const int64_t e = e0 + tx;
+    float s0 = 0.f, s1 = 0.f;
+    if (e < total) {
+      const int64_t zb = e / mn, r = e % mn;
+      const float* base = ws + zb * splits * mn + r;
+      int sp = ty;
+      for (; sp + 8 < splits; sp += 16) { s0 += base[(int64_t)sp * mn]; s1 += base[(int64_t)(sp + 8) * mn]; }
+      if (sp < splits) s0 += base[(int64_t)sp * mn];
+    }
+    red[ty][tx] = s0 + s1;
+    __syncthreads();
+    if (ty == 0 && e < total) {
+      float v = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v += red[k][tx];
+      const int64_t zb = e / mn, r = e % mn;
+      epi_apply(g, (int)zb, (int)(r / g.N), (int)(r % g.N), v);
+    }
+    __syncthreads();
   }
 }
 
@@ -122,7 +140,7 @@ cudaError_t gemm_simt(const Gemm& g, const Workspace& ws, cudaStream_t st) {
 
 cudaError_t splitk_reduce(const Gemm& g, int splits, const float* ws, cudaStream_t st) {
   int64_t total = (int64_t)g.batch * g.M * g.N;
-  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  int blocks = (int)std::min<int64_t>((total + 31) / 32, 148 * 8);
   splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g, splits, ws);
   ++g_launches;
   return cudaGetLastError();

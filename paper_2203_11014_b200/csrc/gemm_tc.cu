@@ -162,7 +162,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n * g.batch;
   int splits = 1;
   if (tiles * 2 <= 148 && p.kblocks >= 8) {   // output fills < half the SMs, long K: split K across CTAs
-    splits = (int)std::min<int64_t>((2 * 148 + tiles - 1) / tiles, p.kblocks / 4);
+    splits = (int)std::min<int64_t>((148 + tiles - 1) / tiles, p.kblocks / 4);   // one item per SM
     while (splits > 1 && (int64_t)splits * g.batch * g.M * g.N * 4 > (int64_t)ws.bytes) --splits;
   }
   p.kb_per_split = (p.kblocks + splits - 1) / splits;

@@ -535,24 +535,33 @@ template <int V> struct VarF {   // variant id -> (flags, fp32 C)
 LEAN_VARIANTS(LV_SPEC)
 #undef LV_SPEC
 
-template <int TILE>
-__device__ __forceinline__ void load_operand(const CUtensorMap* map, const OpMap& om, uint32_t dst, int mn0, int k,
-                                             int z, uint32_t mbar) {
+// Per-item TMA coordinates of one operand: everything except the K position is fixed for the
+// item (computed once, with the divisions); the k-loop only advances (kin, ko) by additions.
+struct OpCoords {
+  int mn;          // inner-row coordinate of the tile start (row % mdiv when two-level)
+  int c2, c3, c4;  // slots 2..4 with the K-independent parts filled in (ko added to slot 2 per k-block)
+};
+__device__ __forceinline__ OpCoords op_coords(const OpMap& om, int mn0, int z) {
   int c[5] = {0, 0, 0, 0, 0};
-  const int kin = om.has_ko ? k % om.kdiv : k;
-  if (om.has_ko) c[2] = k / om.kdiv;
   if (om.mo >= 0) { c[om.mo] = mn0 / om.mdiv; mn0 = mn0 % om.mdiv; }
   if (om.z1 >= 0) c[om.z1] = z % om.zdiv;
   if (om.z0 >= 0) c[om.z0] = z / om.zdiv;
-  if (!om.mn_major) {
-    c[0] = kin;
-    c[1] = mn0;
+  OpCoords r;
+  r.mn = mn0; r.c2 = c[2]; r.c3 = c[3]; r.c4 = c[4];
+  return r;
+}
+template <int TILE>
+__device__ __forceinline__ void load_tile(const CUtensorMap* map, bool mn_major, const OpCoords& q, int kin, int ko,
+                                          uint32_t dst, uint32_t mbar) {
+  int c[5];
+  c[2] = q.c2 + ko; c[3] = q.c3; c[4] = q.c4;
+  if (!mn_major) {
+    c[0] = kin; c[1] = q.mn;
     tma_load5(dst, map, c, mbar);
   } else {
 #pragma unroll
     for (int j = 0; j < TILE / 64; ++j) {
-      c[0] = mn0 + 64 * j;
-      c[1] = kin;
+      c[0] = q.mn + 64 * j; c[1] = kin;
       tma_load5(dst + j * 64 * BK * 2, map, c, mbar);
     }
   }
@@ -624,16 +633,24 @@ __global__ void __launch_bounds__(320, 1)
       for (int item = blockIdx.x; item < total; item += gridDim.x) {
         int m0, n0, z, sp, kb0, nk;
         decode(item, m0, n0, z, sp, kb0, nk);
+        const OpCoords qa = op_coords(p.a, m0, z), qb = op_coords(p.b, n0, z);
+        // K position: (kin, ko) per operand; both operands share k, but each has its own kdiv
+        const int k0 = kb0 * BK;
+        int ka = p.a.has_ko ? k0 % p.a.kdiv : k0, koa = p.a.has_ko ? k0 / p.a.kdiv : 0;
+        int kbk = p.b.has_ko ? k0 % p.b.kdiv : k0, kob = p.b.has_ko ? k0 / p.b.kdiv : 0;
+        const int kda = p.a.has_ko ? p.a.kdiv : 0x7fffffff, kdb = p.b.has_ko ? p.b.kdiv : 0x7fffffff;
+        const bool amn = p.a.mn_major != 0, bmn = p.b.mn_major != 0;
+        uint32_t s = (uint32_t)(it % STAGES), ph = (uint32_t)((it / STAGES) & 1);
         for (int i = 0; i < nk; ++i, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(smem_u32(empty + s), ph ^ 1);
           if (p.trace && blockIdx.x == 0 && it < 64) p.trace[it] = clock64();
           const uint32_t fb = smem_u32(full + s);
           mbar_expect_tx(fb, A_BYTES + B_BYTES);
-          const int k = (kb0 + i) * BK;
-          load_operand<BM>(&tma_a, p.a, smem_u32(sA + s * A_BYTES), m0, k, z, fb);
-          load_operand<BN>(&tma_b, p.b, smem_u32(sB + s * B_BYTES), n0, k, z, fb);
+          load_tile<BM>(&tma_a, amn, qa, ka, koa, smem_u32(sA) + s * A_BYTES, fb);
+          load_tile<BN>(&tma_b, bmn, qb, kbk, kob, smem_u32(sB) + s * B_BYTES, fb);
+          ka += BK; if (ka >= kda) { ka = 0; ++koa; }
+          kbk += BK; if (kbk >= kdb) { kbk = 0; ++kob; }
+          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
     }

@@ -645,34 +645,28 @@ __global__ void __launch_bounds__(256) conv_band_k(const T* __restrict__ in, con
     band[rr * W + (q < R ? q : d + q)] = 0.f;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < CV_RB * (d / 8); e += blockDim.x) {
-    const int ri = e / (d / 8), j0 = (e % (d / 8)) * 8;
-    const int gi = i0 + ri;
-    if (gi >= m) continue;
-    float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  // thread <-> output column j (consecutive threads, consecutive smem words: conflict-free); each thread
+  // walks down the band's rows (RPT rows per thread when d < blockDim)
+  const int cpb = d < (int)blockDim.x ? d : (int)blockDim.x;      // columns per pass
+  const int rgroups = (int)blockDim.x / cpb;                       // row groups (d < 256)
+  const int rpt = (CV_RB + rgroups - 1) / rgroups;
+  const int rg = threadIdx.x / cpb;
+  for (int j = threadIdx.x % cpb; j < d; j += cpb) {
+    if (rg >= rgroups) break;
+    const int r0 = rg * rpt, r1 = min(CV_RB, r0 + rpt);
+    for (int ri = r0; ri < r1; ++ri) {
+      const int gi = i0 + ri;
+      if (gi >= m) break;
+      float o = 0.f;
 #pragma unroll
-    for (int a = 0; a < K; ++a) {
-      const float* row = band + (ri + (FLIP ? 2 * R - a : a)) * W + j0;
-      float x[8 + 2 * R];
+      for (int a = 0; a < K; ++a) {
+        const float* row = band + (ri + (FLIP ? 2 * R - a : a)) * W + j;
 #pragma unroll
-      for (int q = 0; q < 8 + 2 * R; ++q) x[q] = row[q];
-#pragma unroll
-      for (int e2 = 0; e2 < K; ++e2) {
-        const float kv = FLIP ? kb[a * K + e2] : kb[a * K + e2];
-        const int sh = FLIP ? 2 * R - e2 : e2;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) o[t] += kv * x[t + sh];
+        for (int e2 = 0; e2 < K; ++e2) o += kb[a * K + e2] * row[FLIP ? 2 * R - e2 : e2];
       }
-    }
-    const int64_t off = ((int64_t)b * m + gi) * d + j0;
-    if (outAcc) {
-      float a8[8];
-      VIO<8, float>::ld(outAcc + off, a8);
-#pragma unroll
-      for (int t = 0; t < 8; ++t) a8[t] += o[t];
-      VIO<8, float>::st(outAcc + off, a8);
-    } else {
-      VIO<8, T>::st(outT + off, o);
+      const int64_t off = ((int64_t)b * m + gi) * d + j;
+      if (outAcc) outAcc[off] += o;
+      else outT[off] = fromf<T>(o);
     }
   }
   }
@@ -706,22 +700,22 @@ __global__ void __launch_bounds__(256) conv_wgrad_band_k(const T* __restrict__ d
     band[rr * W + (q < R ? q : d + q)] = 0.f;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < CV_RB * (d / 8); e += blockDim.x) {
-    const int ri = e / (d / 8), j0 = (e % (d / 8)) * 8;
-    const int gi = i0 + ri;
-    if (gi >= m) continue;
-    float g[8];
-    VIO<8, T>::ld(dT + ((int64_t)b * m + gi) * d + j0, g);
+  const int cpb = d < (int)blockDim.x ? d : (int)blockDim.x;
+  const int rgroups = (int)blockDim.x / cpb;
+  const int rpt = (CV_RB + rgroups - 1) / rgroups;
+  const int rg = threadIdx.x / cpb;
+  for (int j = threadIdx.x % cpb; j < d && rg < rgroups; j += cpb) {
+    const int r0 = rg * rpt, r1 = min(CV_RB, r0 + rpt);
+    for (int ri = r0; ri < r1; ++ri) {
+      const int gi = i0 + ri;
+      if (gi >= m) break;
+      const float g = tof<T>(dT[((int64_t)b * m + gi) * d + j]);
 #pragma unroll
-    for (int a = 0; a < K; ++a) {
-      const float* row = band + (ri + a) * W + j0;
-      float x[8 + 2 * R];
+      for (int a = 0; a < K; ++a) {
+        const float* row = band + (ri + a) * W + j;
 #pragma unroll
-      for (int q = 0; q < 8 + 2 * R; ++q) x[q] = row[q];
-#pragma unroll
-      for (int e2 = 0; e2 < K; ++e2)
-#pragma unroll
-        for (int t = 0; t < 8; ++t) acc[a * K + e2] += g[t] * x[t + e2];
+        for (int e2 = 0; e2 < K; ++e2) acc[a * K + e2] += g * row[e2];
+      }
     }
   }
   }
@@ -737,6 +731,153 @@ __global__ void __launch_bounds__(256) conv_wgrad_band_k(const T* __restrict__ d
     for (int ww = 0; ww < 8; ++ww) v += red[threadIdx.x][ww];
     part[(int64_t)blockIdx.x * K * K + threadIdx.x] = v;
   }
+}
+
+// Whole-sample variant: the sample's m x d image (+ zero halo) is staged in shared memory (as T) with all
+// 16-B loads in flight; thread <-> column j, a K-row register window slides down the rows.
+// MODE 0: T_out = Kbar (*) X;  1: acc += flip(Kbar) (*) dT;  2: dK partials += sum dT[i][j] X[i+a-R][j+e-R].
+template <typename T, int K, int MODE>
+__global__ void __launch_bounds__(256) conv_sample_k(const T* __restrict__ img, const T* __restrict__ other,
+                                                     const T* __restrict__ Kp, int C, int B, int m, int d,
+                                                     T* __restrict__ outT, float* __restrict__ outAcc,
+                                                     float* __restrict__ part) {
+  constexpr int R = (K - 1) / 2;
+  extern __shared__ __align__(16) unsigned char conv_smem[];
+  T* S = reinterpret_cast<T*>(conv_smem);            // [(m + 2R)][W]
+  __shared__ float kb[K * K];
+  __shared__ float red[K * K][8];
+  const int W = d + 2 * R;
+  if (MODE != 2) {
+    for (int t = threadIdx.x; t < K * K; t += blockDim.x) {
+      float sacc = 0.f;
+      for (int c = 0; c < C; ++c) sacc += tof<T>(Kp[c * K * K + t]);
+      kb[t] = sacc / C;
+    }
+  }
+  // zero the halo once (rows 0..R-1, m+R..m+2R-1, and columns 0..R-1, d+R..d+2R-1 of every row)
+  for (int e = threadIdx.x; e < (m + 2 * R) * W; e += blockDim.x) {
+    const int rr = e / W, cc = e % W;
+    if (rr < R || rr >= m + R || cc < R || cc >= d + R) S[e] = fromf<T>(0.f);
+  }
+  float wacc[K * K];
+#pragma unroll
+  for (int q = 0; q < K * K; ++q) wacc[q] = 0.f;
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
+    __syncthreads();
+    // stage the sample (8 elements per 16-B load); interior only
+    const T* src = img + (int64_t)b * m * d;
+    for (int e = threadIdx.x; e < m * (d / 8); e += blockDim.x) {
+      const int rr = e / (d / 8), cc = (e % (d / 8)) * 8;
+      float v[8];
+      VIO<8, T>::ld(src + (int64_t)rr * d + cc, v);
+      T* dst = S + (rr + R) * W + R + cc;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) dst[t] = fromf<T>(v[t]);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      // window rows: w[a][e] = S[i + a][j + e] (padded coordinates)
+      float w[K][K];
+#pragma unroll
+      for (int a = 0; a < K - 1; ++a)
+#pragma unroll
+        for (int e = 0; e < K; ++e) w[a + 1][e] = tof<T>(S[a * W + j + e]);
+      if (MODE == 1) {
+        // dgrad: 8 rows of outputs in registers, then their 8 accumulator loads in flight together
+        for (int i0 = 0; i0 < m; i0 += 8) {
+          float o8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u;
+            o8[u] = 0.f;
+            if (i < m) {
+#pragma unroll
+              for (int a = 0; a < K - 1; ++a)
+#pragma unroll
+                for (int e = 0; e < K; ++e) w[a][e] = w[a + 1][e];
+#pragma unroll
+              for (int e = 0; e < K; ++e) w[K - 1][e] = tof<T>(S[(i + K - 1) * W + j + e]);
+#pragma unroll
+              for (int a = 0; a < K; ++a)
+#pragma unroll
+                for (int e = 0; e < K; ++e) o8[u] += kb[(K - 1 - a) * K + (K - 1 - e)] * w[a][e];
+            }
+          }
+          float c8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            c8[u] = (i0 + u < m) ? __ldcg(outAcc + ((int64_t)b * m + i0 + u) * d + j) : 0.f;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (i0 + u < m) outAcc[((int64_t)b * m + i0 + u) * d + j] = c8[u] + o8[u];
+        }
+        continue;
+      }
+      for (int i = 0; i < m; ++i) {
+#pragma unroll
+        for (int a = 0; a < K - 1; ++a)
+#pragma unroll
+          for (int e = 0; e < K; ++e) w[a][e] = w[a + 1][e];
+#pragma unroll
+        for (int e = 0; e < K; ++e) w[K - 1][e] = tof<T>(S[(i + K - 1) * W + j + e]);
+        const int64_t off = ((int64_t)b * m + i) * d + j;
+        if (MODE == 0) {
+          float o = 0.f;
+#pragma unroll
+          for (int a = 0; a < K; ++a)
+#pragma unroll
+            for (int e = 0; e < K; ++e) o += kb[a * K + e] * w[a][e];
+          outT[off] = fromf<T>(o);
+        } else if (MODE == 1) {
+          float o = 0.f;
+#pragma unroll
+          for (int a = 0; a < K; ++a)
+#pragma unroll
+            for (int e = 0; e < K; ++e) o += kb[(K - 1 - a) * K + (K - 1 - e)] * w[a][e];
+          outAcc[off] += o;
+        } else {
+          const float g = tof<T>(other[off]);
+#pragma unroll
+          for (int a = 0; a < K; ++a)
+#pragma unroll
+            for (int e = 0; e < K; ++e) wacc[a * K + e] += g * w[a][e];
+        }
+      }
+    }
+  }
+  if (MODE == 2) {
+    const int lane = threadIdx.x & 31, wi = threadIdx.x / 32;
+#pragma unroll
+    for (int q = 0; q < K * K; ++q) {
+      const float v = warp_sum(wacc[q]);
+      if (lane == 0) red[q][wi] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < K * K) {
+      float v = 0.f;
+      for (int ww = 0; ww < (int)(blockDim.x / 32); ++ww) v += red[threadIdx.x][ww];
+      part[(int64_t)blockIdx.x * K * K + threadIdx.x] = v;
+    }
+  }
+}
+
+template <typename T, int K, int MODE>
+static cudaError_t conv_sample_launch(const void* img, const void* other, const void* Kp, int C, int B, int m, int d,
+                                      void* outT, float* outAcc, float* part, int grid, cudaStream_t st) {
+  constexpr int R = (K - 1) / 2;
+  const size_t sm = (size_t)(m + 2 * R) * (d + 2 * R) * sizeof(T);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv_sample_k<T, K, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  conv_sample_k<T, K, MODE><<<grid, 256, sm, st>>>((const T*)img, (const T*)other, (const T*)Kp, C, B, m, d, (T*)outT,
+                                                   outAcc, part);
+  ++g_launches;
+  return cudaGetLastError();
+}
+static bool conv_sample_ok(int k, int m, int d, int es) {
+  return k == 3 && d % 8 == 0 && (size_t)(m + 2) * (d + 2) * es <= 200 * 1024;
 }
 
 template <typename T, int K>
@@ -789,6 +930,11 @@ __global__ void conv_fwd_k(const void* X, const void* K, int pdt, int C, int k, 
 cudaError_t conv_fwd(const void* X, const void* K, int pdt, int C, int k, int B, int m, int d, void* T, int dt,
                      cudaStream_t st) {
   if (k > CONV_MAXK) return cudaErrorInvalidValue;
+  if (conv_sample_ok(k, m, d, dt == BF16 ? 2 : 4) && pdt == dt) {
+    const int grid = std::min(B, 148 * 2);
+    if (dt == BF16) return conv_sample_launch<__nv_bfloat16, 3, 0>(X, nullptr, K, C, B, m, d, T, nullptr, nullptr, grid, st);
+    return conv_sample_launch<float, 3, 0>(X, nullptr, K, C, B, m, d, T, nullptr, nullptr, grid, st);
+  }
   if (conv_band_ok(k, d, B) && pdt == dt) {
     if (dt == BF16) return k == 3 ? conv_band_launch<__nv_bfloat16, 3>(X, K, C, B, m, d, T, nullptr, false, st)
                                   : conv_band_launch<__nv_bfloat16, 5>(X, K, C, B, m, d, T, nullptr, false, st);
@@ -824,6 +970,11 @@ __global__ void conv_dgrad_k(const void* dT, const void* K, int pdt, int C, int 
 cudaError_t conv_dgrad(const void* dT, const void* K, int pdt, int C, int k, int B, int m, int d, float* acc, int dt,
                        cudaStream_t st) {
   if (k > CONV_MAXK) return cudaErrorInvalidValue;
+  if (conv_sample_ok(k, m, d, dt == BF16 ? 2 : 4) && pdt == dt) {
+    const int grid = std::min(B, 148 * 2);
+    if (dt == BF16) return conv_sample_launch<__nv_bfloat16, 3, 1>(dT, nullptr, K, C, B, m, d, nullptr, acc, nullptr, grid, st);
+    return conv_sample_launch<float, 3, 1>(dT, nullptr, K, C, B, m, d, nullptr, acc, nullptr, grid, st);
+  }
   if (conv_band_ok(k, d, B) && pdt == dt) {
     if (dt == BF16) return k == 3 ? conv_band_launch<__nv_bfloat16, 3>(dT, K, C, B, m, d, nullptr, acc, true, st)
                                   : conv_band_launch<__nv_bfloat16, 5>(dT, K, C, B, m, d, nullptr, acc, true, st);
@@ -879,6 +1030,17 @@ __global__ void conv_wgrad_fin_k(const float* part, int nparts, int C, int kk, f
 cudaError_t conv_wgrad(const void* dT, const void* X, int C, int k, int B, int m, int d, int dt, float* dK,
                        float* scratch, size_t scratch_bytes, cudaStream_t st) {
   if (k > CONV_MAXK) return cudaErrorInvalidValue;
+  if (conv_sample_ok(k, m, d, dt == BF16 ? 2 : 4)) {
+    const int grid = std::min(B, 148 * 2);
+    if ((size_t)grid * k * k * sizeof(float) <= scratch_bytes) {
+      cudaError_t e = dt == BF16 ? conv_sample_launch<__nv_bfloat16, 3, 2>(X, dT, nullptr, C, B, m, d, nullptr, nullptr, scratch, grid, st)
+                                 : conv_sample_launch<float, 3, 2>(X, dT, nullptr, C, B, m, d, nullptr, nullptr, scratch, grid, st);
+      if (e != cudaSuccess) return e;
+      conv_wgrad_fin_k<<<1, 64, 0, st>>>(scratch, grid, C, k * k, dK);
+      ++g_launches;
+      return cudaGetLastError();
+    }
+  }
   const int64_t bands = (int64_t)((m + CV_RB - 1) / CV_RB) * B;
   const int grid = (int)std::min<int64_t>(bands, 148 * 4);
   if (conv_band_ok(k, d, B) && (size_t)grid * k * k * sizeof(float) <= scratch_bytes) {
