@@ -186,7 +186,8 @@ dhen_status dhen_profile_read(dhen_ctx* ctx, dhen_op_stat* out, int cap, int* n)
  * A{s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko}, B{s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko},
  * C{rs, cs, bs0, bs1, zdiv}, accumulate, A{mdiv, s_mo}, B{mdiv, s_mo}, C{rdiv, rs_o}
  * (two-level row index r -> (r / div) * s_o + (r % div) * s; div 0 = single level).  ab_dtype/c_dtype: dhen_dtype.
- * path: 0 auto, 1 SIMT only, 2 tcgen05 only (DHEN_E_CONFIG if not expressible).
+ * path: 0 auto, 1 SIMT only, 2 tcgen05 only (DHEN_E_CONFIG if not expressible), 3 tcgen05 with CTA pairs
+ * (cta_group::2, 256-row tiles) wherever the tile width allows, 4 tcgen05 without CTA pairs.
  * ws: fp32 device scratch for split-K partials. */
 dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* B, void* C, int ab_dtype, int c_dtype,
                             int path, void* ws, size_t ws_bytes, void* stream);
@@ -196,7 +197,7 @@ dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* B, vo
 dhen_status dhen_debug_gemm_epi(const long long* q, const void* A, const void* B, void* C, int ab_dtype, int c_dtype,
                                 int path, void* ws, size_t ws_bytes, int mode, const void* E, const void* bias,
                                 void* aux, void* stream);
-/* 1 if the last GEMM ran on the tcgen05 path. */
+/* 0: the last GEMM ran on the SIMT path, 1: tcgen05 (one CTA per tile), 2: tcgen05 with CTA pairs. */
 int dhen_debug_last_gemm_tc(void);
 /* Debug: device buffer (>= 448 int64) receiving clock64 timestamps of CTA 0 of every following
  * tcgen05 GEMM (producer issue, MMA start, data ready, epilogue start, epilogue end); NULL = off. */

@@ -200,7 +200,7 @@ def nccl_id() -> bytes:
 
 def debug_gemm(q, A, B, Cm, path=0, ws=None, stream=None):
     """Test hook: one contraction through the library's GEMM dispatcher (see dhen.h).
-    Returns True if it ran on the tcgen05 path."""
+    Returns 0 (SIMT), 1 (tcgen05) or 2 (tcgen05 with CTA pairs); path 3 / 4 force pairs on / off."""
     import torch
     q = list(q) + [0] * (30 - len(q))
     arr = (C.c_longlong * 30)(*[int(v) for v in q])
@@ -215,7 +215,7 @@ def debug_gemm(q, A, B, Cm, path=0, ws=None, stream=None):
     _check("dhen_debug_gemm", load().dhen_debug_gemm(arr, C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()),
                                                      C.c_void_p(Cm.data_ptr()), abt, ct, path,
                                                      C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(s.cuda_stream)))
-    return bool(load().dhen_debug_last_gemm_tc())
+    return int(load().dhen_debug_last_gemm_tc())
 
 
 def debug_gemm_epi(q, A, B, Cm, mode, E=None, bias=None, aux=None, path=0, ws=None, stream=None):
@@ -232,7 +232,7 @@ def debug_gemm_epi(q, A, B, Cm, mode, E=None, bias=None, aux=None, path=0, ws=No
     _check("dhen_debug_gemm_epi", load().dhen_debug_gemm_epi(arr, vp(A), vp(B), vp(Cm), abt, ct, path, vp(ws),
                                                              ws.numel(), mode, vp(E), vp(bias), vp(aux),
                                                              C.c_void_p(s.cuda_stream)))
-    return bool(load().dhen_debug_last_gemm_tc())
+    return int(load().dhen_debug_last_gemm_tc())
 
 
 def _ptr(t):

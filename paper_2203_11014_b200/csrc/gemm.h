@@ -86,6 +86,8 @@ struct Workspace {              // scratch for split-K partials (fp32)
 extern unsigned long long g_launches;
 // 1 if the last gemm_run took the tcgen05 path (profiling attribution).
 extern int g_last_gemm_tc;
+extern int g_gemm_pair;
+extern int g_last_gemm_pair;
 // path override: -1 env/auto, 0 auto, 1 SIMT only, 2 tcgen05 only (test hook)
 extern int g_gemm_force;
 // debug: device buffer of >= 448 int64 for a clock64 trace of CTA 0 of the next tcgen05 GEMMs

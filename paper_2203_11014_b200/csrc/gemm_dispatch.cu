@@ -10,6 +10,7 @@ namespace dhen {
 
 int g_last_gemm_tc = 0;
 int g_gemm_force = -1;   // -1: env / auto, 0: auto, 1: SIMT only, 2: tcgen05 only
+int g_gemm_pair = -1;    // -1: env DHEN_PAIR / auto, 0: no CTA pairs, 1: CTA pairs wherever expressible
 
 static int force_mode() {
   if (g_gemm_force >= 0) return g_gemm_force;
@@ -22,7 +23,7 @@ cudaError_t gemm_run(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   const int mode = force_mode();
   if (mode != 1) {
     cudaError_t e = gemm_tc(g, ws, st);
-    if (e == cudaSuccess) { g_last_gemm_tc = 1; return e; }
+    if (e == cudaSuccess) { g_last_gemm_tc = g_last_gemm_pair ? 2 : 1; return e; }
     if (e != cudaErrorNotSupported || mode == 2) return e;
   }
   return gemm_simt(g, ws, st);

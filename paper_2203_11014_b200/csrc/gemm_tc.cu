@@ -21,6 +21,7 @@
 
 namespace dhen {
 long long* g_gemm_trace = nullptr;
+int g_last_gemm_pair = 0;
 namespace tc {
 
 // ------------------------------------------------------------------ host side
@@ -152,12 +153,8 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   const int BN = g.N <= 64 ? 64 : g.N <= 128 ? 128 : 256;
   Params p;
   p.g = g;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, &p.a, g.a, g.M, g.K, g.batch, BM)) return cudaErrorNotSupported;
-  if (!make_map(&mb, &p.b, g.b, g.N, g.K, g.batch, BN)) return cudaErrorNotSupported;
   p.tiles_m = (g.M + BM - 1) / BM;
   p.tiles_n = (g.N + BN - 1) / BN;
-  p.n_fast = (p.tiles_n <= 16 && p.tiles_m >= p.tiles_n) ? 1 : 0;
   p.kblocks = (g.K + BK - 1) / BK;
   const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n * g.batch;
   int splits = 1;
@@ -165,6 +162,23 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
     splits = (int)std::min<int64_t>((148 + tiles - 1) / tiles, p.kblocks / 4);   // one item per SM
     while (splits > 1 && (int64_t)splits * g.batch * g.M * g.N * 4 > (int64_t)ws.bytes) --splits;
   }
+  // CTA pairs (cta_group::2, 256 x BN tiles, each CTA loads BN / 2 rows of B): halves the B traffic per
+  // output row.  Measured (tools/gemm_bench.py, DHEN_PAIR=0/1): +3-4 % on the long-K dot.proj family, but
+  // slower on the short-K, store-bound shapes (the pair's epilogues run in lock step), so the default
+  // takes pairs only for K >= 4096 with enough 256-row tiles to fill every SM pair.
+  {
+    static int env_mode = -2;
+    if (env_mode == -2) { const char* ev = getenv("DHEN_PAIR"); env_mode = ev ? atoi(ev) : -1; }
+    const int mode = g_gemm_pair >= 0 ? g_gemm_pair : env_mode;
+    const int64_t pitems = (int64_t)((g.M + 2 * BM - 1) / (2 * BM)) * p.tiles_n * g.batch;
+    p.pair = (BN >= 128 && splits == 1 && mode != 0 && (mode == 1 ? g.M > BM : (pitems >= 74 && g.K >= 4096))) ? 1 : 0;
+  }
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, &p.a, g.a, g.M, g.K, g.batch, BM)) return cudaErrorNotSupported;
+  if (!make_map(&mb, &p.b, g.b, g.N, g.K, g.batch, p.pair ? BN / 2 : BN)) return cudaErrorNotSupported;
+  if (p.pair) p.tiles_m = (g.M + 2 * BM - 1) / (2 * BM);
+  g_last_gemm_pair = p.pair;
+  p.n_fast = (p.tiles_n <= 16 && p.tiles_m >= p.tiles_n) ? 1 : 0;
   p.kb_per_split = (p.kblocks + splits - 1) / splits;
   p.splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;   // no empty splits
   p.ws = ws.ptr;
@@ -191,7 +205,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
             vec_ok(g.e.resid) && vec_ok(g.e.mask)) ? 1 : 0;
   if (special || g.e.triu_m || g.e.dcn_bwd) p.fast = 0;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a.mn_major << 15) | ((uint32_t)p.b.mn_major << 16) |
-            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((p.pair ? 2 * BM : BM) >> 4) << 24);
   const int var = (p.lean_id > 0 && (p.fast8 || p.lanes_rows)) ? p.lean_id : 0;
   cudaError_t e = BN == 64 ? launch_bn64(p, ma, mb, st, var) : BN == 128 ? launch_bn128(p, ma, mb, st, var)
                                                            : launch_bn256(p, ma, mb, st, var);

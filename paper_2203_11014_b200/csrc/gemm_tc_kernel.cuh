@@ -71,6 +71,7 @@ struct Params {
   int fast8;        // 8 consecutive columns per lane (N % 8 == 0, 16-B aligned rows)
   float* ws;
   uint32_t idesc;
+  int pair;           // 1: CTA pairs (cluster of 2) compute 256-row tiles with cta_group::2 MMAs
   long long* trace;   // debug: CTA 0 records clock64 timestamps (nullptr = off)
   int dbg;            // debug: 1 = skip the global epilogue pass (timing experiments only)
 };
@@ -99,6 +100,56 @@ __device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap* map, 
       "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
       "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(mbar)
       : "memory");
+}
+// --- CTA-pair (cta_group::2) helpers: the pair shares one 256 x BN accumulator tile; each CTA holds
+// 128 rows of A and BN / 2 rows of B in its own shared memory and 128 accumulator lanes in its own TMEM.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {   // same offset in CTA `rank` of the cluster
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load5_pair(uint32_t dst, const CUtensorMap* map, const int c[5], uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_pair(uint32_t mbar) {   // arrive on the barrier at this offset in both CTAs
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(mbar),
+               "h"((uint16_t)3)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t a) {   // a: shared::cluster address (possibly the peer's)
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
+__device__ __forceinline__ void tempty_arrive(uint32_t a, bool pair) {   // accumulator drained (rank 0 counts both CTAs)
+  if (pair) mbar_arrive_cluster(mapa_u32(a, 0));
+  else asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -390,6 +441,17 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
     bool ok[G];
     uint4 ub[G][NB > 0 ? NB : 1];
     float cv[G][F32C ? 8 : 1];
+    float4 st0[G], st1[G];
+    // the 8 lanes of a quarter-warp read one staged row: lanes 4-7 take their two 16-B chunks in the
+    // opposite order so each instruction touches 8 distinct bank groups (no 2-way conflict)
+    const uint32_t sw = (uint32_t)((cl >> 2) & 1) << 4;
+#pragma unroll
+    for (int k = 0; k < G; ++k) {   // staged accumulator rows of the group: all shared loads in flight together
+      const int r = sub + (g0 + k) * RPP;
+      const uint32_t sa = stage + (uint32_t)((r * SROW + 8 * cl) * 4);
+      st0[k] = lds4(sa + sw);
+      st1[k] = lds4(sa + (sw ^ 16u));
+    }
 #pragma unroll
     for (int k = 0; k < G; ++k) {
       const int r = sub + (g0 + k) * RPP;
@@ -411,8 +473,7 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
     for (int k = 0; k < G; ++k) {
       if (!ok[k]) continue;
       const int r = sub + (g0 + k) * RPP;
-      const uint32_t sa = stage + (uint32_t)((r * SROW + 8 * cl) * 4);
-      const float4 x0 = lds4(sa), x1 = lds4(sa + 16);
+      const float4 x0 = sw ? st1[k] : st0[k], x1 = sw ? st0[k] : st1[k];
       float a[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
       if (F & EF_TRIU) {
         // strict upper triangle of the per-sample Gram: pairs (i, j > i) row-major (R7)
@@ -550,19 +611,17 @@ __device__ __forceinline__ OpCoords op_coords(const OpMap& om, int mn0, int z) {
   r.mn = mn0; r.c2 = c[2]; r.c3 = c[3]; r.c4 = c[4];
   return r;
 }
-template <int TILE>
 __device__ __forceinline__ void load_tile(const CUtensorMap* map, bool mn_major, const OpCoords& q, int kin, int ko,
-                                          uint32_t dst, uint32_t mbar) {
+                                          uint32_t dst, uint32_t mbar, int chunks, bool pair) {
   int c[5];
   c[2] = q.c2 + ko; c[3] = q.c3; c[4] = q.c4;
   if (!mn_major) {
     c[0] = kin; c[1] = q.mn;
-    tma_load5(dst, map, c, mbar);
+    if (pair) tma_load5_pair(dst, map, c, mbar); else tma_load5(dst, map, c, mbar);
   } else {
-#pragma unroll
-    for (int j = 0; j < TILE / 64; ++j) {
+    for (int j = 0; j < chunks; ++j) {   // 64-column boxes (MN-major, 128B swizzle)
       c[0] = q.mn + 64 * j; c[1] = kin;
-      tma_load5(dst + j * 64 * BK * 2, map, c, mbar);
+      if (pair) tma_load5_pair(dst + j * 64 * BK * 2, map, c, mbar); else tma_load5(dst + j * 64 * BK * 2, map, c, mbar);
     }
   }
 }
@@ -571,7 +630,7 @@ __device__ __forceinline__ void load_tile(const CUtensorMap* map, bool mn_major,
 // warps 2-9 = epilogue.  Work items (tile, batch index, K split) are strided over
 // the grid.  The TMEM accumulator is double-buffered (2 x BN columns) so the
 // epilogue of item i overlaps the MMAs of item i+1 and the loads of item i+2.
-template <int BN, int STAGES, int VAR>
+template <int BN, int STAGES, int VAR, bool PAIR>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    const __grid_constant__ Params p) {
@@ -592,21 +651,34 @@ __global__ void __launch_bounds__(320, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = p.tiles_m * p.tiles_n;
   const int total = ntiles * p.nz * p.splits;
+  // CTA-pair mode: both CTAs of a cluster walk the same items (256-row tiles); rank 0 issues the MMAs
+  constexpr bool pair = PAIR;   // separate instantiation: cta_group::2 code requires a cluster launch
+  const uint32_t crank = pair ? cluster_rank() : 0u;
+  const int wid = pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nwk = pair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int BMP = pair ? 2 * BM : BM;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
     for (int s = 0; s < 2 * STAGES + 2; ++s) mbar_init(smem_u32(bars + s), 1);
-    for (int s = 0; s < 2; ++s) mbar_init(smem_u32(tempty + s), 8);
+    for (int s = 0; s < 2; ++s) mbar_init(smem_u32(tempty + s), pair ? 16 : 8);   // epilogue warps of both CTAs
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (pair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (pair) cluster_sync_all();   // the peer's barriers are initialised before any remote arrive / TMA
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
@@ -616,10 +688,10 @@ __global__ void __launch_bounds__(320, 1)
     sp = zs % p.splits;
     z = p.zbase + zs / p.splits;
     if (p.n_fast) {   // tall-skinny: the N tiles of one M row-block run together (A read once from DRAM)
-      m0 = (tile / p.tiles_n) * BM;
+      m0 = (tile / p.tiles_n) * BMP;
       n0 = (tile % p.tiles_n) * BN;
     } else {
-      m0 = (tile % p.tiles_m) * BM;
+      m0 = (tile % p.tiles_m) * BMP;
       n0 = (tile / p.tiles_m) * BN;
     }
     kb0 = sp * p.kb_per_split;
@@ -630,10 +702,10 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       // ---------------- TMA producer
       int it = 0;
-      for (int item = blockIdx.x; item < total; item += gridDim.x) {
+      for (int item = wid; item < total; item += nwk) {
         int m0, n0, z, sp, kb0, nk;
         decode(item, m0, n0, z, sp, kb0, nk);
-        const OpCoords qa = op_coords(p.a, m0, z), qb = op_coords(p.b, n0, z);
+        const OpCoords qa = op_coords(p.a, m0 + (int)crank * BM, z), qb = op_coords(p.b, n0 + (int)crank * (BN / 2), z);
         // K position: (kin, ko) per operand; both operands share k, but each has its own kdiv
         const int k0 = kb0 * BK;
         int ka = p.a.has_ko ? k0 % p.a.kdiv : k0, koa = p.a.has_ko ? k0 / p.a.kdiv : 0;
@@ -644,10 +716,15 @@ __global__ void __launch_bounds__(320, 1)
         for (int i = 0; i < nk; ++i, ++it) {
           mbar_wait(smem_u32(empty + s), ph ^ 1);
           if (p.trace && blockIdx.x == 0 && it < 64) p.trace[it] = clock64();
-          const uint32_t fb = smem_u32(full + s);
-          mbar_expect_tx(fb, A_BYTES + B_BYTES);
-          load_tile<BM>(&tma_a, amn, qa, ka, koa, smem_u32(sA) + s * A_BYTES, fb);
-          load_tile<BN>(&tma_b, bmn, qb, kbk, kob, smem_u32(sB) + s * B_BYTES, fb);
+          uint32_t fb = smem_u32(full + s);
+          if (!pair) {
+            mbar_expect_tx(fb, A_BYTES + B_BYTES);
+          } else {
+            if (crank == 0) mbar_expect_tx(fb, 2 * (A_BYTES + B_BYTES / 2));   // both CTAs' halves land on rank 0's barrier
+            fb = mapa_u32(fb, 0);
+          }
+          load_tile(&tma_a, amn, qa, ka, koa, smem_u32(sA) + s * A_BYTES, fb, BM / 64, pair);
+          load_tile(&tma_b, bmn, qb, kbk, kob, smem_u32(sB) + s * B_BYTES, fb, pair ? BN / 128 : BN / 64, pair);
           ka += BK; if (ka >= kda) { ka = 0; ++koa; }
           kbk += BK; if (kbk >= kdb) { kbk = 0; ++kob; }
           if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -655,18 +732,19 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && crank == 0) {
       // ---------------- MMA issuer (single thread)
       const uint32_t a_step = p.a.mn_major ? 16 * 128 : 32;   // bytes per K = 16 slice
       const uint32_t b_step = p.b.mn_major ? 16 * 128 : 32;
       const uint32_t a_lbo = p.a.mn_major ? 64 * BK * 2 : 16, b_lbo = p.b.mn_major ? 64 * BK * 2 : 16;
       int it = 0, li = 0;
-      for (int item = blockIdx.x; item < total; item += gridDim.x, ++li) {
+      for (int item = wid; item < total; item += nwk, ++li) {
         int m0, n0, z, sp, kb0, nk;
         decode(item, m0, n0, z, sp, kb0, nk);
         const int ab = li & 1;
         const uint32_t aph = (li >> 1) & 1;
-        mbar_wait(smem_u32(tempty + ab), aph ^ 1);      // epilogue drained this accumulator
+        if (pair) mbar_wait_cluster(smem_u32(tempty + ab), aph ^ 1);   // both CTAs' epilogues drained it
+        else mbar_wait(smem_u32(tempty + ab), aph ^ 1);      // epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (p.trace && blockIdx.x == 0 && li < 64) p.trace[64 + li] = clock64();
         const uint32_t dacc = tmem + (uint32_t)(ab * BN);
@@ -681,11 +759,14 @@ __global__ void __launch_bounds__(320, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = sdesc(ab_ + kk * a_step, a_lbo, 1024);
             const uint64_t bd = sdesc(bb_ + kk * b_step, b_lbo, 1024);
-            mma_f16(dacc, ad, bd, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+            if (pair) mma_f16_pair(dacc, ad, bd, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+            else mma_f16(dacc, ad, bd, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(smem_u32(empty + s));               // ring slot free once these MMAs complete
+          // ring slot free once these MMAs complete
+          if (pair) mma_commit_pair(smem_u32(empty + s)); else mma_commit(smem_u32(empty + s));
         }
-        mma_commit(smem_u32(tfull + ab));                // accumulator ready for the epilogue
+        // accumulator ready for the epilogue
+        if (pair) mma_commit_pair(smem_u32(tfull + ab)); else mma_commit(smem_u32(tfull + ab));
       }
     }
   } else {
@@ -698,7 +779,7 @@ __global__ void __launch_bounds__(320, 1)
     const Gemm& g = p.g;
     const Lean& e = p.ep;
     int li = 0;
-    for (int item = blockIdx.x; item < total; item += gridDim.x, ++li) {
+    for (int item = wid; item < total; item += nwk, ++li) {
       int m0, n0, z, sp, kb0, nk;
       decode(item, m0, n0, z, sp, kb0, nk);
       const int ab = li & 1;
@@ -706,7 +787,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(smem_u32(tfull + ab), aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[192 + li] = clock64();
-      const int rbase = m0 + q4 * 32;
+      const int rbase = m0 + (int)crank * BM + q4 * 32;
       if (p.lanes_rows) {
         // column-contiguous output: row per lane straight from TMEM; consecutive lanes = consecutive addresses
         const int row = rbase + lane;
@@ -728,7 +809,7 @@ __global__ void __launch_bounds__(320, 1)
           if (c0 + 16 >= hh * HC + HC) {
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty + ab)) : "memory");
+            if (lane == 0) tempty_arrive(smem_u32(tempty + ab), pair);
           }
           if (rok && n0 + c0 < g.N) {
             if constexpr (VAR > 0) {
@@ -754,20 +835,23 @@ __global__ void __launch_bounds__(320, 1)
       // row-major output: park this warp's 32 x SC block in smem, then walk it with lanes on columns
 #pragma unroll 1
       for (int pc = 0; pc < HC; pc += SC) {
-#pragma unroll 1
-        for (int c0 = 0; c0 < SC; c0 += 16) {
-          uint32_t v[16];
-          const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC + pc + c0);
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                "=r"(v[15])
-              : "r"(taddr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          const uint32_t dst = stage + (uint32_t)((lane * SROW + c0) * 4);
+        {
+          // all TMEM loads of the pass in flight under one wait, then the staging stores
+          uint32_t v[SC];
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int c0 = 0; c0 < SC; c0 += 16) {
+            const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC + pc + c0);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(v[c0 + 0]), "=r"(v[c0 + 1]), "=r"(v[c0 + 2]), "=r"(v[c0 + 3]), "=r"(v[c0 + 4]), "=r"(v[c0 + 5]),
+                  "=r"(v[c0 + 6]), "=r"(v[c0 + 7]), "=r"(v[c0 + 8]), "=r"(v[c0 + 9]), "=r"(v[c0 + 10]), "=r"(v[c0 + 11]),
+                  "=r"(v[c0 + 12]), "=r"(v[c0 + 13]), "=r"(v[c0 + 14]), "=r"(v[c0 + 15])
+                : "r"(taddr));
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          const uint32_t dst = stage + (uint32_t)(lane * SROW * 4);
+#pragma unroll
+          for (int j = 0; j < SC / 4; ++j)
             sts4(dst + 16 * j, __uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
                  __uint_as_float(v[4 * j + 3]));
         }
@@ -776,7 +860,7 @@ __global__ void __launch_bounds__(320, 1)
           // accumulator fully read: hand it back to the MMA warp
           asm volatile("tcgen05.fence::before_thread_sync;");
           __syncwarp();
-          if (lane == 0) asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty + ab)) : "memory");
+          if (lane == 0) tempty_arrive(smem_u32(tempty + ab), pair);
         }
         __syncwarp();
         const int cbase = n0 + hh * HC + pc;
@@ -876,7 +960,13 @@ __global__ void __launch_bounds__(320, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  if (pair) {
+    cluster_sync_all();   // no CTA leaves while its peer may still touch its barriers, smem or TMEM
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  } else {
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  }
 }
 
 template <int BN, int STAGES, int VAR>
@@ -886,7 +976,9 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
   static_assert(SMEM <= 227 * 1024, "smem");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, VAR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if constexpr (BN >= 128)
+      cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, VAR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr = true;
   }
   const int ntiles = p0.tiles_m * p0.tiles_n;
@@ -896,8 +988,31 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
     p.zbase = zb;
     p.nz = std::min(zmax, p0.g.batch - zb);
     const int64_t items = (int64_t)ntiles * p.nz * p.splits;
-    const int grid = (int)std::min<int64_t>(items, 148);
-    gemm_tc_kernel<BN, STAGES, VAR><<<grid, 320, SMEM, st>>>(ma, mb, p);
+    if constexpr (BN >= 128) if (p.pair) {
+      static int max_clusters = 0;
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.blockDim = dim3(320); cfg.dynamicSmemBytes = SMEM; cfg.stream = st; cfg.attrs = at; cfg.numAttrs = 1;
+      if (!max_clusters) {   // SM pairs the GPC layout can co-schedule (<= 74 on 148 SMs)
+        cfg.gridDim = dim3(148);
+        if (cudaOccupancyMaxActiveClusters(&max_clusters, gemm_tc_kernel<BN, STAGES, VAR, true>, &cfg) != cudaSuccess ||
+            max_clusters <= 0) {
+          (void)cudaGetLastError();
+          max_clusters = 64;
+        }
+      }
+      cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(items, max_clusters)));
+      cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, VAR, true>, ma, mb, p);
+      if (e != cudaSuccess) return e;
+      ++g_launches;
+      continue;
+    }
+    {
+      const int grid = (int)std::min<int64_t>(items, 148);
+      gemm_tc_kernel<BN, STAGES, VAR, false><<<grid, 320, SMEM, st>>>(ma, mb, p);
+    }
     ++g_launches;
   }
   return cudaGetLastError();

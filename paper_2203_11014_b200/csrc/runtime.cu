@@ -957,10 +957,12 @@ dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* Bp, v
   Workspace w;
   w.ptr = (float*)ws;
   w.bytes = ws_bytes;
-  dhen::g_gemm_force = path;
+  dhen::g_gemm_force = path >= 3 ? 2 : path;
+  dhen::g_gemm_pair = path == 3 ? 1 : path == 4 ? 0 : -1;
   cudaError_t e = gemm_run(g, w, S(stream));
   const int used_tc = g_last_gemm_tc;
   dhen::g_gemm_force = -1;
+  dhen::g_gemm_pair = -1;
   if (e == cudaErrorNotSupported) return fail(DHEN_E_CONFIG, "dhen_debug_gemm: layout not supported on this path");
   CK(e);
   return used_tc ? DHEN_OK : DHEN_OK;
@@ -995,9 +997,11 @@ dhen_status dhen_debug_gemm_epi(const long long* q, const void* A, const void* B
   Workspace w;
   w.ptr = (float*)ws;
   w.bytes = ws_bytes;
-  dhen::g_gemm_force = path;
+  dhen::g_gemm_force = path >= 3 ? 2 : path;
+  dhen::g_gemm_pair = path == 3 ? 1 : path == 4 ? 0 : -1;
   cudaError_t e = gemm_run(g, w, S(stream));
   dhen::g_gemm_force = -1;
+  dhen::g_gemm_pair = -1;
   if (e == cudaErrorNotSupported) return fail(DHEN_E_CONFIG, "dhen_debug_gemm_epi: layout not supported on this path");
   CK(e);
   return DHEN_OK;

@@ -47,7 +47,9 @@ def _run(M, N, K, batch, a, b, c, acc=0, path=2, dt=torch.bfloat16, expect_tc=Tr
     torch.cuda.synchronize()
     out = Cg.cpu().double()[offC]
     err = (out - ref).abs().max().item() / max(1.0, ref.abs().max().item())
-    assert used_tc == expect_tc
+    assert bool(used_tc) == expect_tc
+    if path == 3:
+        assert used_tc == 2   # CTA-pair kernel
     # untouched elements outside the view stay as they were
     mask = torch.ones_like(Cm, dtype=torch.bool)
     mask[offC.reshape(-1)] = False
@@ -132,3 +134,50 @@ def test_two_level_rows_token_mix(path):
     err = _run(Bn * d, m, l, 1, (1, d, 0, 0, 1, 0, 0), (l, 1, 0, 0, 1, 0, 0), (1, d, 0, 0, 1),
                a2=(d, mo * d), c2=(d, m * d), acc=1, path=path, expect_tc=(path == 2))
     assert err < 2e-5, err
+
+
+@pytest.mark.parametrize("amn,bmn", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(1024, 256, 256), (304, 200, 160), (640, 384, 320), (520, 128, 64)])
+def test_cta_pairs(amn, bmn, M, N, K):
+    """cta_group::2 kernel (256-row tiles split over a CTA pair, each CTA loading half of B): every
+    operand layout, ragged M / N / K tails, N tiles of 128 and 256."""
+    a = MNM(M) if amn else KM(K)
+    b = MNM(N) if bmn else KM(K)
+    err = _run(M, N, K, 1, a, b, (N, 1, 0, 0, 1), path=3)
+    assert err < 2e-5, err
+
+
+def test_cta_pairs_batched_twolevel():
+    """CTA pairs with a batched (heads) problem and with the two-level K of the token-mixing wgrad."""
+    z, M, N, K = 6, 512, 256, 128
+    err = _run(M, N, K, z, KM(K, bs0=M * K), KM(K, bs0=N * K), (N, 1, M * N, 0, 1), path=3)
+    assert err < 2e-5, err
+    m, d, l, Bn = 256, 128, 256, 3   # K = 384: 6 k-blocks, no split-K
+    err = _run(m, l, Bn * d, 1, (d, 1, 0, 0, 1, d, m * d), (d, 1, 0, 0, 1, d, l * d), (l, 1, 0, 0, 1), acc=1,
+               path=3)
+    assert err < 2e-5, err
+
+
+def test_cta_pairs_epilogue():
+    """CTA pairs with a fused epilogue (DCN cross + aux) on a ragged M."""
+    from paper_2203_11014_b200.binding import debug_gemm_epi
+    g = torch.Generator().manual_seed(5)
+    M, N, K = 777, 256, 256
+    A = torch.randn(M, K, generator=g).bfloat16()
+    W = torch.randn(N, K, generator=g).bfloat16()
+    E = torch.randn(M, N, generator=g).bfloat16()
+    bias = torch.randn(N, generator=g).bfloat16()
+    q = [M, N, K, 1] + list(KM(K)) + list(KM(K)) + [N, 1, 0, 0, 1] + [0]
+    outs = []
+    for path in (3, 4):
+        Cg = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+        aux = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+        tc = debug_gemm_epi(q, A.cuda(), W.cuda(), Cg, 3, E=E.cuda(), bias=bias.cuda(), aux=aux, path=path)
+        assert tc == (2 if path == 3 else 1)
+        outs.append((Cg.cpu(), aux.cpu()))
+    u = A.double() @ W.double().T + bias.double()
+    ref = E.double() * u + E.double()
+    assert (outs[0][1].double() - u).abs().max() <= 2e-2 * u.abs().max()
+    assert (outs[0][0].double() - ref).abs().max() <= 2e-2 * ref.abs().max()
+    # same fp32 accumulation order per element: pairs and single CTAs agree bit for bit
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
