@@ -31,23 +31,45 @@ cudaError_t triu_extract(const float* G, void* Z, int dt, int B, int m, int64_t 
   return cudaGetLastError();
 }
 
-__global__ void sym_from_triu_k(const void* dZ, void* S, int dt, int B, int m, int64_t ldz) {
-  int64_t total = (int64_t)B * m * m;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int b = (int)(t / ((int64_t)m * m));
-    int r = (int)(t % ((int64_t)m * m));
-    int i = r / m, j = r % m;
-    float v = 0.f;
-    if (i != j) {
-      int a = min(i, j), c = max(i, j);
-      int p = a * m - a * (a + 1) / 2 + (c - a - 1);
-      v = ld_as_f32(dZ, (int64_t)b * ldz + p, dt);
+// One block per sample: the packed triangle (h values, contiguous) is staged in shared memory, then the m x m
+// matrix is written row-major with 8-element vector stores (m % 8 == 0) or scalars.
+__global__ void __launch_bounds__(256) sym_from_triu_k(const void* dZ, void* S, int dt, int m, int64_t ldz) {
+  extern __shared__ float tri[];
+  const int h = m * (m - 1) / 2;
+  const int b = blockIdx.x;
+  for (int p = threadIdx.x; p < h; p += blockDim.x) tri[p] = ld_as_f32(dZ, (int64_t)b * ldz + p, dt);
+  __syncthreads();
+  const int64_t base = (int64_t)b * m * m;
+  auto val = [&](int i, int j) -> float {
+    if (i == j) return 0.f;
+    const int a = min(i, j), c = max(i, j);
+    return tri[a * m - a * (a + 1) / 2 + (c - a - 1)];
+  };
+  if (dt == BF16 && (m % 8) == 0) {
+    const int cpr = m / 8;
+    for (int q = threadIdx.x; q < m * cpr; q += blockDim.x) {
+      const int i = q / cpr, j0 = (q - i * cpr) * 8;
+      uint32_t w[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(val(i, j0 + 2 * t), val(i, j0 + 2 * t + 1));
+        w[t] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+      *reinterpret_cast<uint4*>((__nv_bfloat16*)S + base + (int64_t)i * m + j0) = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    st_from_f32(S, t, dt, v);
+  } else {
+    for (int q = threadIdx.x; q < m * m; q += blockDim.x) st_from_f32(S, base + q, dt, val(q / m, q % m));
   }
 }
 cudaError_t sym_from_triu(const void* dZ, void* S, int dt, int B, int m, int64_t ldz, cudaStream_t st) {
-  sym_from_triu_k<<<nblocks((int64_t)B * m * m), 256, 0, st>>>(dZ, S, dt, B, m, ldz);
+  const size_t sm = (size_t)m * (m - 1) / 2 * sizeof(float);
+  if (sm > 200 * 1024) return cudaErrorInvalidValue;
+  static size_t attr = 48 * 1024;
+  if (sm > attr) {
+    cudaFuncSetAttribute(sym_from_triu_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = sm;
+  }
+  sym_from_triu_k<<<B, 256, sm, st>>>(dZ, S, dt, m, ldz);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -369,13 +391,40 @@ __global__ void ln_bwd_k(const void* dY, int dydt, const void* Rsave, const floa
   }
 }
 
-__global__ void reduce_parts_k(const float* part, int nparts, int n, float* out0, float* out1) {
-  // part [nparts][2n] -> out0 += sum part[:, :n], out1 += sum part[:, n:]
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < 2 * n; c += gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * 2 * n + c];
-    if (c < n) { if (out0) out0[c] += s; } else { if (out1) out1[c - n] += s; }
+// Deterministic column sums of a partials matrix part[nparts][n]: block (32 cols x 32 part-strides); thread
+// (x, y) sums parts y, y + 32, ... in order, then warp 0 adds the 32 strides in order.  Fixed order at any grid.
+__global__ void __launch_bounds__(1024) part_sum_k(const float* __restrict__ part, int nparts, int n,
+                                                   float* __restrict__ out0, int n0, float* __restrict__ out1,
+                                                   int n1, float* __restrict__ out2, float out2_scale) {
+  __shared__ float sm[32][33];
+  const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + x;
+  float s = 0.f;
+  if (c < n) {
+    int p = y;
+    for (; p + 96 < nparts; p += 128) {   // 4 independent loads in flight, summed in index order
+      const float a = part[(int64_t)p * n + c], b = part[(int64_t)(p + 32) * n + c];
+      const float d = part[(int64_t)(p + 64) * n + c], e = part[(int64_t)(p + 96) * n + c];
+      s = (((s + a) + b) + d) + e;
+    }
+    for (; p < nparts; p += 32) s += part[(int64_t)p * n + c];
   }
+  sm[y][x] = s;
+  __syncthreads();
+  if (y == 0 && c < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) t += sm[k][x];
+    // columns [0, n0) -> out0 +=, [n0, n0 + n1) -> out1 +=, column n0 + n1 -> *out2 = scale * sum
+    if (c < n0) { if (out0) out0[c] += t; }
+    else if (c < n0 + n1) { if (out1) out1[c - n0] += t; }
+    else if (c == n0 + n1 && out2) *out2 = t * out2_scale;
+  }
+}
+static void part_sum(const float* part, int nparts, int n, float* out0, int n0, float* out1, int n1, float* out2,
+                     float out2_scale, cudaStream_t st) {
+  part_sum_k<<<(n + 31) / 32, 1024, 0, st>>>(part, nparts, n, out0, n0, out1, n1, out2, out2_scale);
+  ++g_launches;
 }
 
 static cudaError_t ln_bwd_generic(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
@@ -393,8 +442,8 @@ static cudaError_t ln_bwd_generic(const void* dY, int dydt, const void* Rsave, c
     ln_bwd_k<8><<<nb, 256, 0, st>>>(dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, scratch, rpb);
   else
     ln_bwd_k<32><<<nb, 256, 0, st>>>(dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, scratch, rpb);
-  reduce_parts_k<<<nblocks(2 * d), 256, 0, st>>>(scratch, nb, d, dgamma, dbeta);
-  g_launches += 2;
+  ++g_launches;
+  part_sum(scratch, nb, 2 * d, dgamma, d, dbeta, d, nullptr, 0.f, st);
   return cudaGetLastError();
 }
 
@@ -454,8 +503,8 @@ cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu,
   }
   LN_SHAPES(LNB)
 #undef LNB
-  reduce_parts_k<<<nblocks(2 * d), 256, 0, st>>>(scratch, nb, d, dgamma, dbeta);
-  g_launches += 2;
+  ++g_launches;
+  part_sum(scratch, nb, 2 * d, dgamma, d, dbeta, d, nullptr, 0.f, st);
   return cudaGetLastError();
 }
 
@@ -474,13 +523,6 @@ __global__ void colsum_part_k(const void* src, int dt, int64_t rows, int cols, i
     float t = 0.f;
     for (int k = 0; k < 8; ++k) t += sm[k][cx];
     part[(int64_t)blockIdx.y * cols + c] = t;
-  }
-}
-__global__ void colsum_fin_k(const float* part, int nparts, int cols, float* out) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * cols + c];
-    out[c] += s;
   }
 }
 // vectorised: thread (tx, ty) owns 8 consecutive columns tx*8.. of a 256-column slab and rows ty, ty+8, ...
@@ -537,8 +579,8 @@ cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t 
       else
         colsum8_part_k<__nv_bfloat16><<<dim3(cb, (unsigned)nch), 256, 0, st>>>((const __nv_bfloat16*)src, rows, cols,
                                                                                 ld, rpc, scratch);
-      colsum_fin_k<<<nblocks(cols), 256, 0, st>>>(scratch, (int)nch, cols, out);
-      g_launches += 2;
+      ++g_launches;
+      part_sum(scratch, (int)nch, cols, out, cols, nullptr, 0, nullptr, 0.f, st);
       return cudaGetLastError();
     }
   }
@@ -550,8 +592,8 @@ cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t 
   nch = (rows + rpc - 1) / rpc;
   if (nch < 1) nch = 1;
   colsum_part_k<<<dim3(cb, (unsigned)nch), 256, 0, st>>>(src, dt, rows, cols, ld, rpc, scratch);
-  colsum_fin_k<<<nblocks(cols), 256, 0, st>>>(scratch, (int)nch, cols, out);
-  g_launches += 2;
+  ++g_launches;
+  part_sum(scratch, (int)nch, cols, out, cols, nullptr, 0, nullptr, 0.f, st);
   return cudaGetLastError();
 }
 
@@ -1069,6 +1111,75 @@ cudaError_t conv_wgrad(const void* dT, const void* X, int C, int k, int B, int m
 }
 
 // ------------------------------------------------------------------ head + loss
+// One block per sample.  Pooling: thread (ry, cx) sums rows ry, ry + RY, ... of column chunk cx (VEC
+// consecutive columns), then the RY partials are added in fixed order.  dY[b] = (dz_b / m) w broadcast.
+template <int VEC>
+__global__ void __launch_bounds__(256) head_v(const __nv_bfloat16* __restrict__ Y, const __nv_bfloat16* __restrict__ w,
+                                              const __nv_bfloat16* __restrict__ bh, const float* __restrict__ labels,
+                                              int m, int d, int Bg, __nv_bfloat16* __restrict__ dY, float* pooled,
+                                              float* z, float* lossb, float* dz, int do_bwd) {
+  extern __shared__ float hs[];   // [RY][d] partial column sums
+  __shared__ float red[8];
+  __shared__ float dzs;
+  const int b = blockIdx.x;
+  const int CX = d / VEC, RY = blockDim.x / CX;
+  const int cx = threadIdx.x % CX, ry = threadIdx.x / CX;
+  const __nv_bfloat16* Yb = Y + (int64_t)b * m * d;
+  if (ry < RY) {
+    float a[VEC];
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) a[t] = 0.f;
+    for (int r = ry; r < m; r += RY) {
+      const uint4 u = *reinterpret_cast<const uint4*>(Yb + (int64_t)r * d + cx * VEC);
+      const uint32_t q[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) { a[2 * t] += __uint_as_float(q[t] << 16); a[2 * t + 1] += __uint_as_float(q[t] & 0xffff0000u); }
+    }
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) hs[ry * d + cx * VEC + t] = a[t];
+  }
+  __syncthreads();
+  float part = 0.f;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < RY; ++k) s += hs[k * d + c];
+    s /= m;
+    pooled[(int64_t)b * d + c] = s;
+    part += s * __bfloat162float(w[c]);
+  }
+  part = warp_sum(part);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int q = 0; q < (int)(blockDim.x / 32); ++q) s += red[q];
+    const float zz = s + __bfloat162float(bh[0]);
+    z[b] = zz;
+    if (do_bwd) {
+      const float y = labels[b];
+      lossb[b] = fmaxf(zz, 0.f) - y * zz + log1pf(expf(-fabsf(zz)));
+      const float sg = 1.f / (1.f + expf(-zz));
+      dzs = (sg - y) / (float)Bg;
+      dz[b] = dzs;
+    }
+  }
+  __syncthreads();
+  if (!do_bwd) return;
+  const float g = dzs / m;
+  // every row of dY[b] is the same vector g * w
+  for (int q = threadIdx.x; q < m * CX; q += blockDim.x) {
+    const int r = q / CX, c0 = (q - r * CX) * VEC;
+    const uint4 wu = *reinterpret_cast<const uint4*>(w + c0);
+    const uint32_t wq[4] = {wu.x, wu.y, wu.z, wu.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(g * __uint_as_float(wq[t] << 16), g * __uint_as_float(wq[t] & 0xffff0000u));
+      o[t] = *reinterpret_cast<uint32_t*>(&h2);
+    }
+    *reinterpret_cast<uint4*>(dY + (int64_t)b * m * d + (int64_t)r * d + c0) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
 __global__ void head_k(const void* Y, const void* w, const void* bh, int pdt, const float* labels, int m, int d, int Bg,
                        void* dY, int dt, float* pooled, float* z, float* lossb, float* dz, int do_bwd) {
   __shared__ float red[32];
@@ -1119,26 +1230,24 @@ __global__ void head_part_k(const float* pooled, const float* dz, const float* l
     part[(int64_t)blockIdx.x * (d + 2) + c] = s;
   }
 }
-__global__ void head_fin_k(const float* part, int nparts, int d, int Bg, float* loss_out, float* dw, float* db) {
-  for (int c = threadIdx.x; c < d + 2; c += blockDim.x) {
-    float s = 0.f;
-    for (int q = 0; q < nparts; ++q) s += part[(int64_t)q * (d + 2) + c];
-    if (c < d) dw[c] += s;
-    else if (c == d) db[0] += s;
-    else if (loss_out) *loss_out = s / (float)Bg;
-  }
-}
 cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, const float* labels, int B, int m, int d,
                          int Bg, void* dY, int dt, float* pooled, float* z, float* lossb, float* dz, float* loss_out,
                          float* dw, float* db, int do_bwd, cudaStream_t st) {
-  head_k<<<B, 256, 0, st>>>(Y, w, bh, pdt, labels, m, d, Bg, dY, dt, pooled, z, lossb, dz, do_bwd);
+  if (dt == BF16 && pdt == BF16 && d % 8 == 0 && d / 8 <= 256 && ((uintptr_t)Y % 16) == 0 && ((uintptr_t)w % 16) == 0 &&
+      (!do_bwd || ((uintptr_t)dY % 16) == 0)) {
+    const int RY = 256 / (d / 8);
+    head_v<8><<<B, 256, (size_t)RY * d * sizeof(float), st>>>((const __nv_bfloat16*)Y, (const __nv_bfloat16*)w,
+        (const __nv_bfloat16*)bh, labels, m, d, Bg, (__nv_bfloat16*)dY, pooled, z, lossb, dz, do_bwd);
+  } else {
+    head_k<<<B, 256, 0, st>>>(Y, w, bh, pdt, labels, m, d, Bg, dY, dt, pooled, z, lossb, dz, do_bwd);
+  }
   ++g_launches;
   if (do_bwd) {
     const int per = 32, nparts = (B + per - 1) / per;
     float* part = pooled + (int64_t)B * d;   // scratch after pooled (sized by the runtime)
     head_part_k<<<nparts, 128, 0, st>>>(pooled, dz, lossb, B, d, per, part);
-    head_fin_k<<<1, 256, 0, st>>>(part, nparts, d, Bg, loss_out, dw, db);
-    g_launches += 2;
+    ++g_launches;
+    part_sum(part, nparts, d + 2, dw, d, db, 1, loss_out, 1.f / (float)Bg, st);
   }
   return cudaGetLastError();
 }
@@ -1151,9 +1260,30 @@ __global__ void sgd_cast_k(float* master, const float* grad, float lr, void* cop
     if (copy) st_from_f32(copy, t, dt, v);
   }
 }
+// 4 elements per thread (n % 4 == 0, 16-B aligned fp32 arrays, 8-B aligned bf16 copy)
+__global__ void sgd_cast4_k(float4* __restrict__ master, const float4* __restrict__ grad, float lr, uint2* __restrict__ copy,
+                            int64_t n4) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n4; t += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = master[t];
+    if (grad) {
+      const float4 g = grad[t];
+      v.x -= lr * g.x; v.y -= lr * g.y; v.z -= lr * g.z; v.w -= lr * g.w;
+      master[t] = v;
+    }
+    if (copy) {
+      __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+      copy[t] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+    }
+  }
+}
 cudaError_t sgd_cast(float* master, const float* grad, float lr, void* copy, int dt, int64_t n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  sgd_cast_k<<<nblocks(n), 256, 0, st>>>(master, grad, lr, copy, dt, n);
+  if (n % 4 == 0 && (!copy || dt == BF16) && ((uintptr_t)master % 16) == 0 && ((uintptr_t)grad % 16) == 0 &&
+      ((uintptr_t)copy % 8) == 0) {
+    sgd_cast4_k<<<nblocks(n / 4, 256, 148 * 16), 256, 0, st>>>((float4*)master, (const float4*)grad, lr, (uint2*)copy, n / 4);
+  } else {
+    sgd_cast_k<<<nblocks(n), 256, 0, st>>>(master, grad, lr, copy, dt, n);
+  }
   ++g_launches;
   return cudaGetLastError();
 }
@@ -1161,9 +1291,22 @@ __global__ void cast_k(const void* src, int sdt, void* dst, int ddt, int64_t n) 
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
     st_from_f32(dst, t, ddt, ld_as_f32(src, t, sdt));
 }
+// fp32 -> bf16, 8 elements per thread
+__global__ void cast8_k(const float4* __restrict__ src, uint4* __restrict__ dst, int64_t n8) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n8; t += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = __ldcs(src + 2 * t), b = __ldcs(src + 2 * t + 1);
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w);
+    __nv_bfloat162 h2 = __floats2bfloat162_rn(b.x, b.y), h3 = __floats2bfloat162_rn(b.z, b.w);
+    dst[t] = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                        *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+  }
+}
 cudaError_t cast(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  cast_k<<<nblocks(n), 256, 0, st>>>(src, sdt, dst, ddt, n);
+  if (sdt == F32 && ddt == BF16 && n % 8 == 0 && ((uintptr_t)src % 16) == 0 && ((uintptr_t)dst % 16) == 0)
+    cast8_k<<<nblocks(n / 8, 256, 148 * 16), 256, 0, st>>>((const float4*)src, (uint4*)dst, n / 8);
+  else
+    cast_k<<<nblocks(n), 256, 0, st>>>(src, sdt, dst, ddt, n);
   ++g_launches;
   return cudaGetLastError();
 }
