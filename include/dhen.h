@@ -203,6 +203,11 @@ int dhen_debug_last_gemm_tc(void);
  * tcgen05 GEMM (producer issue, MMA start, data ready, epilogue start, epilogue end); NULL = off. */
 void dhen_debug_gemm_trace(void* dev_buf);
 
+/* Test hook: the attention core path (F4 / B6).  mode 1 (default, or env DHEN_ATTN_FUSED) = the fused
+ * per-(sample, head) tcgen05 kernels where m <= 128 and d / heads is 64 or 128 (bf16); 0 = the two batched
+ * GEMMs + softmax kernels everywhere.  Returns the previous mode.  Process-wide; not thread-safe. */
+int dhen_debug_attn_fused(int mode);
+
 /* Number of library kernels launched since init (a host-side counter). */
 unsigned long long dhen_launch_count(const dhen_ctx* ctx);
 

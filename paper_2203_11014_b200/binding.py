@@ -24,7 +24,7 @@ EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "d
            "dhen_layer_bwd", "dhen_train_step", "dhen_train_step_graphed", "dhen_forward", "dhen_zero_grad", "dhen_params_io",
            "dhen_grads_get", "dhen_launch_count", "dhen_last_error", "dhen_destroy", "dhen_profile",
            "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_gemm_epi", "dhen_debug_last_gemm_tc",
-           "dhen_debug_gemm_trace")
+           "dhen_debug_gemm_trace", "dhen_debug_attn_fused")
 
 
 class dhen_module(C.Structure):
@@ -100,6 +100,8 @@ def load(path: str = LIB_PATH):
     lib.dhen_debug_gemm_trace.argtypes = [vp]
     lib.dhen_debug_last_gemm_tc.restype = C.c_int
     lib.dhen_debug_last_gemm_tc.argtypes = []
+    lib.dhen_debug_attn_fused.restype = C.c_int
+    lib.dhen_debug_attn_fused.argtypes = [C.c_int]
     lib.dhen_destroy.restype = None
     lib.dhen_destroy.argtypes = [vp]
     _lib = lib
@@ -216,6 +218,11 @@ def debug_gemm(q, A, B, Cm, path=0, ws=None, stream=None):
                                                      C.c_void_p(Cm.data_ptr()), abt, ct, path,
                                                      C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(s.cuda_stream)))
     return int(load().dhen_debug_last_gemm_tc())
+
+
+def debug_attn_fused(mode: int) -> int:
+    """Test hook: select the fused attention core (1) or the two-GEMM path (0); returns the previous mode."""
+    return int(load().dhen_debug_attn_fused(int(mode)))
 
 
 def debug_gemm_epi(q, A, B, Cm, mode, E=None, bias=None, aux=None, path=0, ws=None, stream=None):

@@ -1,0 +1,537 @@
+// attn_tc.cu — fused self-attention core for short feature-token sequences (F4 / B6 of SURVEY §8(a)):
+//
+//   forward   (Eq.(4)):  S = Q_h K_h^T,  P = softmax_row(S / sqrt(dh)),  O_h = P V_h
+//   backward  (B6):  dV = P^T dO,  dP = dO V^T,  dS = P (dP - rowsum(P dP)) / sqrt(dh),
+//                    dQ = dS K,  dK = dS^T Q
+//
+// One CTA owns one (sample, head) item at a time: m <= 128 tokens, dh in {64, 128}.  Q, K, V (and dO) of
+// the item arrive by TMA (2-D maps over the [B*m][3d] / [B*m][d] activations; a tile's rows m..127 are
+// ignored), every contraction is one chain of tcgen05.mma (M = 128, K = 16 steps) into
+// TMEM, and the softmax runs on the accumulator rows straight out of TMEM (one thread = one query row,
+// no cross-thread reduction).  P (and dS) never leave the SM: they are written to shared memory in the
+// 128-B-swizzled K-major layout the next MMA reads, as the A operand (P V, dS K) or, through the same
+// bytes read as an MN-major operand, as the transposed A operand (P^T dO, dS^T Q).  The backward
+// recomputes S and P from Q, K (bit-identical to the forward: same MMA chain, same softmax code) instead
+// of storing P, so per item the forward moves Q, K, V in and O out, the backward Q, K, V, dO in and
+// dQ, dK, dV out — the attention's algorithmic bytes.
+//
+// Warp roles (persistent CTAs, items strided over the grid): warp 0 = TMA producer, warp 1 = MMA issuer
+// (also owns the TMEM allocation), warps 2-5 = softmax / epilogue (warp w reads TMEM lanes 32 (w % 4) ..).
+// Numerics follow the oracle's storage points: P and dS are rounded to bf16 (they are MMA
+// operands), dS carries the 1/sqrt(dh) scale, O and dQKV are stored bf16, all accumulation is fp32.
+#include <cuda.h>
+
+#include "attn.h"
+#include "gemm_tc_kernel.cuh"
+
+namespace dhen {
+namespace attn {
+
+using namespace tc;
+
+constexpr int ROWS = 128;          // MMA M / padded token count
+constexpr int CHUNK = ROWS * 128;  // one 64-column (128-B) swizzled chunk of 128 rows: 16 KB
+
+struct Params {
+  int items, H, m, d;
+  float scale;                 // 1 / sqrt(dh)
+  __nv_bfloat16* out;          // fwd: O [B][m][d];  bwd: dQKV [B][m][3d]
+};
+
+__device__ __forceinline__ void tma_load2(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ uint4 lds16(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+// 32 consecutive fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// Row `row` of a 128-row, 128-B swizzled K-major operand: 16-B granule g (8 bf16) of 64-column chunk c.
+__device__ __forceinline__ uint32_t swz(uint32_t base, int row, int c, int g) {
+  return base + (uint32_t)(c * CHUNK + row * 128 + ((g ^ (row & 7)) << 4));
+}
+__device__ __forceinline__ uint32_t idesc(int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
+}
+// D (+)= A B over K = 16 * ksteps.  A / B are 128-row (or dh-row) swizzled tiles in shared memory:
+//   K-major operand: k-step kk at chunk kk / 4, byte offset (kk % 4) * 32 (SBO 1024 = 8 rows)
+//   MN-major operand (the transposed read of a row-major tile): k-step kk = 16 rows -> + kk * 2048,
+//   the 64-wide MN chunks are CHUNK apart (LBO)
+__device__ __forceinline__ void mma_chain(uint32_t d, uint32_t a, bool a_mn, uint32_t b, bool b_mn, uint32_t id,
+                                          int ksteps) {
+  for (int kk = 0; kk < ksteps; ++kk) {
+    const uint32_t ao = a_mn ? (uint32_t)kk * 2048u : (uint32_t)((kk >> 2) * CHUNK + (kk & 3) * 32);
+    const uint32_t bo = b_mn ? (uint32_t)kk * 2048u : (uint32_t)((kk >> 2) * CHUNK + (kk & 3) * 32);
+    const uint64_t ad = sdesc(a + ao, a_mn ? CHUNK : 16, 1024);
+    const uint64_t bd = sdesc(b + bo, b_mn ? CHUNK : 16, 1024);
+    mma_f16(d, ad, bd, id, kk > 0 ? 1u : 0u);
+  }
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+// Softmax of this thread's S row (TMEM lane) into bf16 P, packed two per word (p[j/2]); rows >= m and
+// columns >= m give 0.  Three passes over the row in 32-column chunks (max; exp written back to TMEM and
+// summed; normalise and pack) keep 32 values live instead of 128.  The same code runs in the forward and
+// in the backward recompute, so both see bit-identical P.
+__device__ __forceinline__ void softmax_row(uint32_t tS, int m, bool row_ok, float scale, uint32_t* p) {
+  float v[32];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < ROWS / 32; ++c) {
+    tmem_ld32(tS + c * 32, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) mx = (c * 32 + j) < m ? fmaxf(mx, v[j]) : mx;
+  }
+  const float k2 = scale * 1.4426950408889634f;   // exp(x) = exp2(x log2 e)
+  const float off = mx * k2;
+  float sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < ROWS / 32; ++c) {
+    tmem_ld32(tS + c * 32, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float e = (c * 32 + j) < m ? exp2f(fmaf(v[j], k2, -off)) : 0.f;
+      v[j] = e;
+      sum += e;
+    }
+    tmem_st32(tS + c * 32, v);
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  const float inv = row_ok ? 1.f / sum : 0.f;
+#pragma unroll
+  for (int c = 0; c < ROWS / 32; ++c) {
+    tmem_ld32(tS + c * 32, v);
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) p[(c * 32 + j) / 2] = pack_bf2(v[j] * inv, v[j + 1] * inv);
+  }
+}
+// bf16 pairs of a row into the swizzled K-major tile at `base`
+__device__ __forceinline__ void store_row_tile(uint32_t base, int row, const uint32_t* p) {
+#pragma unroll
+  for (int g = 0; g < ROWS / 8; ++g)
+    sts16(swz(base, row, g >> 3, g & 7), p[4 * g], p[4 * g + 1], p[4 * g + 2], p[4 * g + 3]);
+}
+// DH accumulator columns of this thread's lane -> bf16 global row (16-B stores) if `ok`.  The TMEM loads
+// are warp-collective (.sync.aligned): every lane executes them, only the stores are predicated.
+template <int DH>
+__device__ __forceinline__ void store_acc_row(uint32_t taddr, __nv_bfloat16* dst, bool ok) {
+#pragma unroll
+  for (int c = 0; c < DH / 32; ++c) {
+    float v[32];
+    tmem_ld32(taddr + c * 32, v);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      u.x = pack_bf2(v[8 * q], v[8 * q + 1]); u.y = pack_bf2(v[8 * q + 2], v[8 * q + 3]);
+      u.z = pack_bf2(v[8 * q + 4], v[8 * q + 5]); u.w = pack_bf2(v[8 * q + 6], v[8 * q + 7]);
+      if (ok) *reinterpret_cast<uint4*>(dst + c * 32 + q * 8) = u;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ forward
+// smem: Q | K | V  (DH / 64 chunks each); P overlays Q (and K when DH = 64) once S is in TMEM.
+// TMEM (256 cols): S [0, 128), O [128, 128 + DH).
+template <int DH>
+__global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant__ CUtensorMap qkv, const __grid_constant__ Params p) {
+  constexpr int NCH = DH / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sQ = smem_u32(smem), sK = sQ + NCH * CHUNK, sV = sK + NCH * CHUNK, sP = sQ;
+  uint64_t* bars = (uint64_t*)(smem + 3 * NCH * CHUNK);
+  const uint32_t b_qk = smem_u32(bars + 0), b_v = smem_u32(bars + 1), b_s = smem_u32(bars + 2),
+                 b_p = smem_u32(bars + 3), b_o = smem_u32(bars + 4), b_oe = smem_u32(bars + 5);
+  uint32_t* tslot = (uint32_t*)(bars + 6);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&qkv) : "memory");
+    mbar_init(b_qk, 1); mbar_init(b_v, 1); mbar_init(b_s, 1); mbar_init(b_p, 4); mbar_init(b_o, 1); mbar_init(b_oe, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  const int H = p.H, d = p.d;
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer
+      int it = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+        const int b = item / H, h = item - (item / H) * H;
+        if (it > 0) mbar_wait(b_o, (it - 1) & 1);   // previous item's P V done: Q, K, V, P free
+        mbar_expect_tx(b_qk, 2 * NCH * CHUNK);
+        for (int c = 0; c < NCH; ++c) {
+          tma_load2(sQ + c * CHUNK, &qkv, h * DH + 64 * c, b * p.m, b_qk);
+          tma_load2(sK + c * CHUNK, &qkv, d + h * DH + 64 * c, b * p.m, b_qk);
+        }
+        mbar_expect_tx(b_v, NCH * CHUNK);
+        for (int c = 0; c < NCH; ++c) tma_load2(sV + c * CHUNK, &qkv, 2 * d + h * DH + 64 * c, b * p.m, b_v);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // ---------------- MMA issuer
+      const uint32_t id_s = idesc(ROWS, false, false), id_o = idesc(DH, false, true);
+      int it = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+        const uint32_t ph = it & 1;
+        mbar_wait(b_qk, ph);
+        tc_after();
+        mma_chain(tmem, sQ, false, sK, false, id_s, DH / 16);            // S = Q K^T
+        mma_commit(b_s);
+        mbar_wait(b_p, ph);
+        mbar_wait(b_v, ph);
+        if (it > 0) mbar_wait(b_oe, (it - 1) & 1);                          // O columns drained
+        tc_after();
+        mma_chain(tmem + ROWS, sP, false, sV, true, id_o, ROWS / 16);     // O = P V
+        mma_commit(b_o);
+      }
+    }
+  } else {             // ---------------- softmax + epilogue (warps 2..5)
+    const int q4 = warp & 3, row = q4 * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
+    const bool row_ok = row < p.m;
+    int it = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+      const int b = item / H, h = item - (item / H) * H;
+      const uint32_t ph = it & 1;
+      mbar_wait(b_s, ph);
+      tc_after();
+      uint32_t pk[ROWS / 2];
+      softmax_row(tl, p.m, row_ok, p.scale, pk);
+      store_row_tile(sP, row, pk);
+      fence_async_smem();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(b_p);
+      mbar_wait(b_o, ph);
+      tc_after();
+      store_acc_row<DH>(tl + ROWS, p.out + ((int64_t)b * p.m + row) * d + h * DH, row_ok);
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(b_oe);
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+// ------------------------------------------------------------------ backward
+// smem: Q | K | V | dO (DH / 64 chunks each) | P / dS (2 chunks): dS overwrites P once dV = P^T dO is done.
+// TMEM: S [0,128) -> dV [0, DH);  dP [128, 256) -> dK [128, 128 + DH);  dQ [64, 128) (DH = 64) or
+// [256, 384) (DH = 128).  Allocation 256 / 512 columns.
+template <int DH>
+__global__ void __launch_bounds__(192, DH == 64 ? 2 : 1) attn_bwd_kernel(const __grid_constant__ CUtensorMap qkv,
+                                                                     const __grid_constant__ CUtensorMap dom,
+                                                                     const __grid_constant__ Params p) {
+  constexpr int NCH = DH / 64;
+  constexpr int TCOLS = DH == 64 ? 256 : 512;
+  constexpr uint32_t C_S = 0, C_DP = 128, C_DV = 0, C_DK = 128, C_DQ = DH == 64 ? 64 : 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sQ = smem_u32(smem), sK = sQ + NCH * CHUNK, sV = sK + NCH * CHUNK, sdO = sV + NCH * CHUNK,
+                 sP = sdO + NCH * CHUNK;
+  uint64_t* bars = (uint64_t*)(smem + 4 * NCH * CHUNK + 2 * CHUNK);
+  const uint32_t b_qk = smem_u32(bars + 0), b_vdo = smem_u32(bars + 1), b_s = smem_u32(bars + 2),
+                 b_dp = smem_u32(bars + 3), b_p = smem_u32(bars + 4), b_dv = smem_u32(bars + 5),
+                 b_ds = smem_u32(bars + 6), b_dqk = smem_u32(bars + 7), b_tf = smem_u32(bars + 8);
+  uint32_t* tslot = (uint32_t*)(bars + 9);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&qkv) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&dom) : "memory");
+    mbar_init(b_qk, 1); mbar_init(b_vdo, 1); mbar_init(b_s, 1); mbar_init(b_dp, 1); mbar_init(b_p, 4);
+    mbar_init(b_dv, 1); mbar_init(b_ds, 4); mbar_init(b_dqk, 1); mbar_init(b_tf, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  const int H = p.H, d = p.d;
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer: each buffer reloaded as soon as its last reader is done
+      int it = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+        const int b = item / H, h = item - (item / H) * H;
+        const uint32_t pp = (it - 1) & 1;
+        // arm the next phase only after the previous one completed (dP(it - 1) consumed V and dO of it - 1)
+        if (it > 0) mbar_wait(b_dp, pp);     // V last read by dP
+        mbar_expect_tx(b_vdo, 2 * NCH * CHUNK);
+        for (int c = 0; c < NCH; ++c) tma_load2(sV + c * CHUNK, &qkv, 2 * d + h * DH + 64 * c, b * p.m, b_vdo);
+        if (it > 0) mbar_wait(b_dv, pp);     // dO last read by dV
+        for (int c = 0; c < NCH; ++c) tma_load2(sdO + c * CHUNK, &dom, h * DH + 64 * c, b * p.m, b_vdo);
+        if (it > 0) mbar_wait(b_dqk, pp);    // Q, K last read by dQ / dK
+        mbar_expect_tx(b_qk, 2 * NCH * CHUNK);
+        for (int c = 0; c < NCH; ++c) {
+          tma_load2(sQ + c * CHUNK, &qkv, h * DH + 64 * c, b * p.m, b_qk);
+          tma_load2(sK + c * CHUNK, &qkv, d + h * DH + 64 * c, b * p.m, b_qk);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // ---------------- MMA issuer
+      const uint32_t id_sq = idesc(ROWS, false, false);   // S, dP: both operands K-major
+      const uint32_t id_t = idesc(DH, true, true);         // dV = P^T dO, dK = dS^T Q
+      const uint32_t id_q = idesc(DH, false, true);        // dQ = dS K
+      int it = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+        const uint32_t ph = it & 1;
+        if (it > 0) mbar_wait(b_tf, (it - 1) & 1);         // previous item's accumulators drained
+        mbar_wait(b_vdo, ph);
+        tc_after();
+        mma_chain(tmem + C_DP, sdO, false, sV, false, id_sq, DH / 16);   // dP = dO V^T
+        mma_commit(b_dp);
+        mbar_wait(b_qk, ph);
+        tc_after();
+        mma_chain(tmem + C_S, sQ, false, sK, false, id_sq, DH / 16);     // S = Q K^T
+        mma_commit(b_s);
+        mbar_wait(b_p, ph);
+        tc_after();
+        mma_chain(tmem + C_DV, sP, true, sdO, true, id_t, ROWS / 16);    // dV = P^T dO
+        mma_commit(b_dv);
+        mbar_wait(b_ds, ph);
+        tc_after();
+        mma_chain(tmem + C_DQ, sP, false, sK, true, id_q, ROWS / 16);    // dQ = dS K
+        mma_chain(tmem + C_DK, sP, true, sQ, true, id_t, ROWS / 16);     // dK = dS^T Q
+        mma_commit(b_dqk);
+      }
+    }
+  } else {             // ---------------- softmax recompute, dS, epilogues (warps 2..5)
+    const int q4 = warp & 3, row = q4 * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
+    const bool row_ok = row < p.m;
+    const int64_t ld = 3 * (int64_t)d;
+    int it = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+      const int b = item / H, h = item - (item / H) * H;
+      const uint32_t ph = it & 1;
+      __nv_bfloat16* orow = p.out + ((int64_t)b * p.m + row) * ld + h * DH;
+      mbar_wait(b_s, ph);
+      tc_after();
+      {
+        uint32_t pk[ROWS / 2];
+        softmax_row(tl + C_S, p.m, row_ok, p.scale, pk);
+        store_row_tile(sP, row, pk);
+      }
+      fence_async_smem();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(b_p);
+      // D = sum_j P_j dP_j (bf16 P as stored: read back from this thread's row of the tile, fp32 dP)
+      mbar_wait(b_dp, ph);
+      tc_after();
+      float D = 0.f;
+#pragma unroll
+      for (int c = 0; c < ROWS / 32; ++c) {
+        float v[32];
+        tmem_ld32(tl + C_DP + c * 32, v);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int gg = c * 4 + g;   // 16-B granule index along the row (8 columns each)
+          const uint4 u = lds16(swz(sP, row, gg >> 3, gg & 7));
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            D = fmaf(__uint_as_float(w[t] << 16), v[8 * g + 2 * t], D);
+            D = fmaf(__uint_as_float(w[t] & 0xffff0000u), v[8 * g + 2 * t + 1], D);
+          }
+        }
+      }
+      // dV (rows = keys) is ready once P^T dO is done; then P's bytes may be overwritten by dS
+      mbar_wait(b_dv, ph);
+      tc_after();
+      store_acc_row<DH>(tl + C_DV, orow + 2 * d, row_ok);
+      // dS = scale * P (dP - D), bf16, over P in the same tile (each thread rewrites its own row)
+#pragma unroll
+      for (int c = 0; c < ROWS / 32; ++c) {
+        float v[32];
+        tmem_ld32(tl + C_DP + c * 32, v);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int gg = c * 4 + g;
+          const uint32_t a = swz(sP, row, gg >> 3, gg & 7);
+          const uint4 u = lds16(a);
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+          uint32_t q[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            q[t] = pack_bf2(p.scale * __uint_as_float(w[t] << 16) * (v[8 * g + 2 * t] - D),
+                            p.scale * __uint_as_float(w[t] & 0xffff0000u) * (v[8 * g + 2 * t + 1] - D));
+          sts16(a, q[0], q[1], q[2], q[3]);
+        }
+      }
+      fence_async_smem();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(b_ds);
+      mbar_wait(b_dqk, ph);
+      tc_after();
+      store_acc_row<DH>(tl + C_DQ, orow, row_ok);
+      store_acc_row<DH>(tl + C_DK, orow + d, row_ok);
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(b_tf);
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeFn)f;
+  }
+  return fn;
+}
+// [B * m][cols] bf16 -> 2-D map, box 64 columns x 128 rows, 128-B swizzle.  An item's tile starts at row
+// b * m; its rows m..127 hold the next samples' (finite) rows, or the zero fill past the tensor end, and
+// the kernels never let them reach a result (columns >= m of P and dS are 0, rows >= m are not stored).
+// (A 3-D [B][m][cols] map with the box taller than m, i.e. out-of-bounds rows inside the tensor, hung
+// the forward on B200 — measured; the 2-D form keeps every out-of-bounds box at the tensor end.)
+static bool map2(CUtensorMap* map, const void* ptr, int cols, int64_t rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn || ((uintptr_t)ptr & 15) || (cols * 2) % 16 || rows < ROWS) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)ROWS}, es[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int g_mode = -1;   // DHEN_ATTN_FUSED: 0 = off (two batched GEMMs + softmax kernels), default on
+int set_mode(int mode) {
+  if (g_mode < 0) { const char* e = getenv("DHEN_ATTN_FUSED"); g_mode = e ? atoi(e) : 1; }
+  const int old = g_mode;
+  g_mode = mode;
+  return old;
+}
+
+bool fused_ok(int dt, int B, int H, int m, int d) {
+  if (g_mode < 0) { const char* e = getenv("DHEN_ATTN_FUSED"); g_mode = e ? atoi(e) : 1; }
+  if (!g_mode || dt != BF16 || H <= 0 || d % H) return false;
+  const int dh = d / H;
+  return (dh == 64 || dh == 128) && m >= 1 && m <= ROWS && (int64_t)B * m >= ROWS && (int64_t)B * H < (1ll << 31) &&
+         (int64_t)B * m < (1ll << 31);
+}
+
+template <typename K>
+static int grid_for(K kern, int smem, int items) {
+  static int sms = 0;
+  if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
+  int per = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 192, smem) != cudaSuccess || per < 1) {
+    (void)cudaGetLastError();
+    per = 1;
+  }
+  return (int)std::min<int64_t>(items, (int64_t)sms * per);
+}
+
+cudaError_t core_fwd(const void* QKV, void* O, int B, int H, int m, int d, cudaStream_t st) {
+  if (!fused_ok(BF16, B, H, m, d)) return cudaErrorNotSupported;
+  const int dh = d / H;
+  CUtensorMap mq;
+  if (!map2(&mq, QKV, 3 * d, (int64_t)B * m)) return cudaErrorNotSupported;
+  Params p;
+  p.items = B * H; p.H = H; p.m = m; p.d = d; p.scale = 1.f / sqrtf((float)dh); p.out = (__nv_bfloat16*)O;
+  const int nch = dh / 64;
+  const int smem = 3 * nch * CHUNK + 1024 + 128;
+  if (dh == 64) {
+    static bool a = false;
+    if (!a) { cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+    attn_fwd_kernel<64><<<grid_for(attn_fwd_kernel<64>, smem, p.items), 192, smem, st>>>(mq, p);
+  } else {
+    static bool a = false;
+    if (!a) { cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+    attn_fwd_kernel<128><<<grid_for(attn_fwd_kernel<128>, smem, p.items), 192, smem, st>>>(mq, p);
+  }
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t core_bwd(const void* QKV, const void* dO, void* dQKV, int B, int H, int m, int d, cudaStream_t st) {
+  if (!fused_ok(BF16, B, H, m, d)) return cudaErrorNotSupported;
+  const int dh = d / H;
+  CUtensorMap mq, mo;
+  if (!map2(&mq, QKV, 3 * d, (int64_t)B * m) || !map2(&mo, dO, d, (int64_t)B * m)) return cudaErrorNotSupported;
+  Params p;
+  p.items = B * H; p.H = H; p.m = m; p.d = d; p.scale = 1.f / sqrtf((float)dh); p.out = (__nv_bfloat16*)dQKV;
+  const int nch = dh / 64;
+  const int smem = 4 * nch * CHUNK + 2 * CHUNK + 1024 + 128;
+  if (dh == 64) {
+    static bool a = false;
+    if (!a) { cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+    attn_bwd_kernel<64><<<grid_for(attn_bwd_kernel<64>, smem, p.items), 192, smem, st>>>(mq, mo, p);
+  } else {
+    static bool a = false;
+    if (!a) { cudaFuncSetAttribute(attn_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+    attn_bwd_kernel<128><<<grid_for(attn_bwd_kernel<128>, smem, p.items), 192, smem, st>>>(mq, mo, p);
+  }
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace attn
+}  // namespace dhen

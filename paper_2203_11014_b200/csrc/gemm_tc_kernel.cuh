@@ -435,50 +435,59 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
     for (int t = 0; t < 8; ++t) bias8[t] = lean_bias(e, col + t);
   }
   const float alpha = e.alpha;
+  // operand loads of row group q (rows sub + (q * G + k) * RPP) into register buffer `buf`; the loads of
+  // group q + 1 are issued before group q is combined and stored (two groups in flight per lane)
+  constexpr int NG = NR / G;
+  int64_t o[2][G];
+  bool ok[2][G];
+  uint4 ub[2][G][NB > 0 ? NB : 1];
+  float cv[2][G][F32C ? 8 : 1];
+  auto prefetch = [&](int q, int buf) {
 #pragma unroll
-  for (int g0 = 0; g0 < NR; g0 += G) {
-    int64_t o[G];
-    bool ok[G];
-    uint4 ub[G][NB > 0 ? NB : 1];
-    float cv[G][F32C ? 8 : 1];
+    for (int k = 0; k < G; ++k) {
+      const int r = sub + (q * G + k) * RPP;
+      o[buf][k] = shfl64(my_off, r) + col;
+      ok[buf][k] = cok && (rbase + r < M);
+      if (ok[buf][k]) {
+        if constexpr ((F & (EF_CROSS | EF_DCNB)) != 0)
+          ub[buf][k][SLX] = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.x + o[buf][k]));
+        if constexpr ((F & (EF_MASK | EF_DCNB)) != 0)
+          ub[buf][k][SLM] = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.mask + o[buf][k]));
+        if constexpr ((F & EF_RESID) != 0)
+          ub[buf][k][SLR] = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.resid + o[buf][k]));
+        if constexpr ((F & EF_ACC) != 0 && !CF32)
+          ub[buf][k][SLC] = __ldcg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.c + o[buf][k]));
+        if constexpr (F32C) ldg_c8<true>(e.c, o[buf][k], cv[buf][k]);
+      }
+    }
+  };
+  // the 8 lanes of a quarter-warp read one staged row: lanes 4-7 take their two 16-B chunks in the
+  // opposite order so each instruction touches 8 distinct bank groups (no 2-way conflict)
+  const uint32_t sw = (uint32_t)((cl >> 2) & 1) << 4;
+  prefetch(0, 0);
+#pragma unroll
+  for (int q = 0; q < NG; ++q) {
+    const int cb = q & 1;
+    if (q + 1 < NG) prefetch(q + 1, cb ^ 1);
     float4 st0[G], st1[G];
-    // the 8 lanes of a quarter-warp read one staged row: lanes 4-7 take their two 16-B chunks in the
-    // opposite order so each instruction touches 8 distinct bank groups (no 2-way conflict)
-    const uint32_t sw = (uint32_t)((cl >> 2) & 1) << 4;
 #pragma unroll
-    for (int k = 0; k < G; ++k) {   // staged accumulator rows of the group: all shared loads in flight together
-      const int r = sub + (g0 + k) * RPP;
+    for (int k = 0; k < G; ++k) {   // staged accumulator rows of the group
+      const int r = sub + (q * G + k) * RPP;
       const uint32_t sa = stage + (uint32_t)((r * SROW + 8 * cl) * 4);
       st0[k] = lds4(sa + sw);
       st1[k] = lds4(sa + (sw ^ 16u));
     }
 #pragma unroll
     for (int k = 0; k < G; ++k) {
-      const int r = sub + (g0 + k) * RPP;
-      o[k] = shfl64(my_off, r) + col;
-      ok[k] = cok && (rbase + r < M);
-      if (ok[k]) {
-        if constexpr ((F & (EF_CROSS | EF_DCNB)) != 0)
-          ub[k][SLX] = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.x + o[k]));
-        if constexpr ((F & (EF_MASK | EF_DCNB)) != 0)
-          ub[k][SLM] = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.mask + o[k]));
-        if constexpr ((F & EF_RESID) != 0)
-          ub[k][SLR] = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.resid + o[k]));
-        if constexpr ((F & EF_ACC) != 0 && !CF32)
-          ub[k][SLC] = __ldcg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.c + o[k]));
-        if constexpr (F32C) ldg_c8<true>(e.c, o[k], cv[k]);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < G; ++k) {
-      if (!ok[k]) continue;
-      const int r = sub + (g0 + k) * RPP;
+      if (!ok[cb][k]) continue;
+      const int r = sub + (q * G + k) * RPP;
+      const int64_t ok_ = o[cb][k];
       const float4 x0 = sw ? st1[k] : st0[k], x1 = sw ? st0[k] : st1[k];
       float a[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
       if (F & EF_TRIU) {
         // strict upper triangle of the per-sample Gram: pairs (i, j > i) row-major (R7)
         const int i = rbase + r;
-        const int64_t zb = o[k] - col - (int64_t)i * e.rs;     // = z * bs0 (rs = 0 for this view)
+        const int64_t zb = ok_ - col - (int64_t)i * e.rs;     // = z * bs0 (rs = 0 for this view)
         const int64_t base = zb + (int64_t)i * e.triu_m - (int64_t)i * (i + 1) / 2 - i - 1;
 #pragma unroll
         for (int t = 0; t < 8; ++t)
@@ -488,24 +497,24 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
       if (F & EF_DCNB) {
         // B8 fused: dA = dT * X (bf16, aux), dX_acc += dT * A + dT  (dT = the fp32 accumulator)
         float xv[8], av[8], da[8];
-        unpack_bf8(ub[k][SLX], xv);
-        unpack_bf8(ub[k][SLM], av);
+        unpack_bf8(ub[cb][k][SLX], xv);
+        unpack_bf8(ub[cb][k][SLM], av);
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
           const float v = a[t] * alpha;
           da[t] = v * xv[t];
-          cv[k][t] += v * av[t] + v;
+          cv[cb][k][t] += v * av[t] + v;
         }
-        stg8<false>(e.aux, o[k], da);
-        stg8<true>(e.c, o[k], cv[k]);
+        stg8<false>(e.aux, ok_, da);
+        stg8<true>(e.c, ok_, cv[cb][k]);
         continue;
       }
 #pragma unroll
       for (int t = 0; t < 8; ++t) a[t] = a[t] * alpha + bias8[t];
       float t8[8];
-      if (F & EF_AUX) stg8<false>(e.aux, o[k], a);
+      if (F & EF_AUX) stg8<false>(e.aux, ok_, a);
       if constexpr ((F & EF_CROSS) != 0) {
-        unpack_bf8(ub[k][SLX], t8);
+        unpack_bf8(ub[cb][k][SLX], t8);
 #pragma unroll
         for (int t = 0; t < 8; ++t) a[t] = t8[t] * a[t] + t8[t];
       }
@@ -514,26 +523,26 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
         for (int t = 0; t < 8; ++t) a[t] = fmaxf(a[t], 0.f);
       }
       if constexpr ((F & EF_MASK) != 0) {
-        unpack_bf8(ub[k][SLM], t8);
+        unpack_bf8(ub[cb][k][SLM], t8);
 #pragma unroll
         for (int t = 0; t < 8; ++t) a[t] = t8[t] > 0.f ? a[t] : 0.f;
       }
       if constexpr ((F & EF_RESID) != 0) {
-        unpack_bf8(ub[k][SLR], t8);
+        unpack_bf8(ub[cb][k][SLR], t8);
 #pragma unroll
         for (int t = 0; t < 8; ++t) a[t] += t8[t];
       }
       if (F & EF_ACC) {
         if (CF32) {
 #pragma unroll
-          for (int t = 0; t < 8; ++t) a[t] += cv[k][t];
+          for (int t = 0; t < 8; ++t) a[t] += cv[cb][k][t];
         } else {
-          unpack_bf8(ub[k][SLC], t8);
+          unpack_bf8(ub[cb][k][SLC], t8);
 #pragma unroll
           for (int t = 0; t < 8; ++t) a[t] += t8[t];
         }
       }
-      stg8<CF32>(e.c, o[k], a);
+      stg8<CF32>(e.c, ok_, a);
     }
   }
 }

@@ -24,6 +24,7 @@
 #include "../../include/dhen.h"
 #include "gemm.h"
 #include "kernels.h"
+#include "attn.h"
 
 using namespace dhen;
 
@@ -558,17 +559,24 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         q.e.bias = p(md.bq); q.e.bias_dt = dt; q.e.bias_gap_lo = d; q.e.bias_gap_hi = 2 * d;   // no key bias (R10)
         q.e.bias_hi_off = (int)(md.bv - md.bq);
         RET(G_(q, c, st, "attn.qkv"));
-        const int mp = (mi + 7) / 8 * 8;   // padded score-row pitch
-        Gemm s = mk(mi, mi, dh, B * H, operand(QKV, dt, s3, 1, mi * s3, dh, H),
-                    operand(QKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H),
-                    view(c->big, F32, mp, 1, (int64_t)mi * mp));
-        s.e.alpha = 1.f / sqrtf((float)dh);
-        RET(G_(s, c, st, "attn.qk"));
-        KT("attn.softmax", 0, (double)B * H * mi * mi * (4 + es), softmax_rows(c->big, md.P, dt, (int64_t)B * H * mi, mi, mp, st));
-        Gemm o = mk(mi, dh, mi, B * H, operand(md.P, dt, mp, 1, (int64_t)mi * mp),
-                    operand(QKV + 2 * (int64_t)d * es, dt, 1, s3, mi * s3, dh, H),
-                    view(md.O, dt, d, 1, (int64_t)mi * d, dh, H));
-        RET(G_(o, c, st, "attn.pv"));
+        if (attn::fused_ok(dt, B, H, mi, d)) {
+          // F4 fused: S, softmax and P V per (sample, head) on one SM, P never leaves shared memory
+          ProfScope ps(c, "attn.core", 4.0 * B * H * (double)mi * mi * dh, (double)B * mi * 4 * d * es, st);
+          CK(attn::core_fwd(QKV, md.O, B, H, mi, d, st));
+          if (ps.rec >= 0) c->recs[ps.rec].tc = 1;
+        } else {
+          const int mp = (mi + 7) / 8 * 8;   // padded score-row pitch
+          Gemm s = mk(mi, mi, dh, B * H, operand(QKV, dt, s3, 1, mi * s3, dh, H),
+                      operand(QKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H),
+                      view(c->big, F32, mp, 1, (int64_t)mi * mp));
+          s.e.alpha = 1.f / sqrtf((float)dh);
+          RET(G_(s, c, st, "attn.qk"));
+          KT("attn.softmax", 0, (double)B * H * mi * mi * (4 + es), softmax_rows(c->big, md.P, dt, (int64_t)B * H * mi, mi, mp, st));
+          Gemm o = mk(mi, dh, mi, B * H, operand(md.P, dt, mp, 1, (int64_t)mi * mp),
+                      operand(QKV + 2 * (int64_t)d * es, dt, 1, s3, mi * s3, dh, H),
+                      view(md.O, dt, d, 1, (int64_t)mi * d, dh, H));
+          RET(G_(o, c, st, "attn.pv"));
+        }
         Gemm r1 = mk((int)rows, d, d, 1, operand(md.O, dt, d, 1), operand(p(md.Wo), dt, d, 1), view(c->rtmp, F32, d, 1));
         r1.e.bias = p(md.bo); r1.e.bias_dt = dt; r1.e.resid = view((void*)X, dt, d, 1);
         RET(G_(r1, c, st, "attn.out"));
@@ -715,24 +723,31 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dR1, dt, rows, d, d, gp(md.bo), c->red, c->red_bytes, st));
         // attention core backward
         char* dQKV = (char*)c->tC;   // [rows, 3d]  (dF no longer needed; tC >= rows*f >= rows*3d? checked at plan)
-        const int mp = (mi + 7) / 8 * 8;
-        Gemm dv = mk(mi, dh, mi, B * H, operand(md.P, dt, 1, mp, (int64_t)mi * mp),
-                     operand(dO, dt, 1, d, (int64_t)mi * d, dh, H),
-                     view(dQKV + 2 * (int64_t)d * es, dt, s3, 1, mi * s3, dh, H));
-        RET(G_(dv, c, st, "attn.dv"));
-        Gemm dp = mk(mi, mi, dh, B * H, operand(dO, dt, d, 1, (int64_t)mi * d, dh, H),
-                     operand(QKV + 2 * (int64_t)d * es, dt, s3, 1, mi * s3, dh, H),
-                     view(c->big, F32, mp, 1, (int64_t)mi * mp));
-        RET(G_(dp, c, st, "attn.dp"));
-        KT("attn.softmax_bwd", 0, (double)B * H * mi * mi * (4 + 2 * es), softmax_bwd(md.P, c->big, c->tD, dt, (int64_t)B * H * mi, mi, mp, 1.f / sqrtf((float)dh), st));
-        Gemm dq = mk(mi, dh, mi, B * H, operand(c->tD, dt, mp, 1, (int64_t)mi * mp),
-                     operand(QKV + (int64_t)d * es, dt, 1, s3, mi * s3, dh, H),
-                     view(dQKV, dt, s3, 1, mi * s3, dh, H));
-        RET(G_(dq, c, st, "attn.dq"));
-        Gemm dk = mk(mi, dh, mi, B * H, operand(c->tD, dt, 1, mp, (int64_t)mi * mp),
-                     operand(QKV, dt, 1, s3, mi * s3, dh, H),
-                     view(dQKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H));
-        RET(G_(dk, c, st, "attn.dk"));
+        if (attn::fused_ok(dt, B, H, mi, d)) {
+          // B6 core fused: S and P recomputed on chip, dV, dP, dS, dQ, dK per (sample, head)
+          ProfScope ps(c, "attn.core_bwd", 10.0 * B * H * (double)mi * mi * dh, (double)B * mi * 7 * d * es, st);
+          CK(attn::core_bwd(QKV, dO, dQKV, B, H, mi, d, st));
+          if (ps.rec >= 0) c->recs[ps.rec].tc = 1;
+        } else {
+          const int mp = (mi + 7) / 8 * 8;
+          Gemm dv = mk(mi, dh, mi, B * H, operand(md.P, dt, 1, mp, (int64_t)mi * mp),
+                       operand(dO, dt, 1, d, (int64_t)mi * d, dh, H),
+                       view(dQKV + 2 * (int64_t)d * es, dt, s3, 1, mi * s3, dh, H));
+          RET(G_(dv, c, st, "attn.dv"));
+          Gemm dp = mk(mi, mi, dh, B * H, operand(dO, dt, d, 1, (int64_t)mi * d, dh, H),
+                       operand(QKV + 2 * (int64_t)d * es, dt, s3, 1, mi * s3, dh, H),
+                       view(c->big, F32, mp, 1, (int64_t)mi * mp));
+          RET(G_(dp, c, st, "attn.dp"));
+          KT("attn.softmax_bwd", 0, (double)B * H * mi * mi * (4 + 2 * es), softmax_bwd(md.P, c->big, c->tD, dt, (int64_t)B * H * mi, mi, mp, 1.f / sqrtf((float)dh), st));
+          Gemm dq = mk(mi, dh, mi, B * H, operand(c->tD, dt, mp, 1, (int64_t)mi * mp),
+                       operand(QKV + (int64_t)d * es, dt, 1, s3, mi * s3, dh, H),
+                       view(dQKV, dt, s3, 1, mi * s3, dh, H));
+          RET(G_(dq, c, st, "attn.dq"));
+          Gemm dk = mk(mi, dh, mi, B * H, operand(c->tD, dt, 1, mp, (int64_t)mi * mp),
+                       operand(QKV, dt, 1, s3, mi * s3, dh, H),
+                       view(dQKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H));
+          RET(G_(dk, c, st, "attn.dk"));
+        }
         Gemm gx = mk((int)rows, d, 3 * d, 1, operand(dQKV, dt, s3, 1), operand(p(md.Wq), dt, 1, d), view(acc, F32, d, 1));
         gx.e.accumulate = 1;
         RET(G_(gx, c, st, "attn.qkv_dgrad"));
@@ -969,6 +984,7 @@ dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* Bp, v
 }
 
 int dhen_debug_last_gemm_tc(void) { return g_last_gemm_tc; }
+int dhen_debug_attn_fused(int mode) { return attn::set_mode(mode); }
 
 dhen_status dhen_debug_gemm_epi(const long long* q, const void* A, const void* Bp, void* Cp, int ab_dt, int c_dt,
                                 int path, void* ws, size_t ws_bytes, int mode, const void* E, const void* bias,
