@@ -68,6 +68,10 @@ struct Epilogue {
   // Gram triangle (F1): element (i, j) of sample z is stored iff j > i, at C + z * c.bs0 +
   // i * triu_m - i (i + 1) / 2 + (j - i - 1)  (strict upper triangle, row-major pairs, R7)
   int triu_m = 0;
+  // several samples per tile (M = triu_spt * triu_m rows, batch item z = samples z*spt .. z*spt+spt-1, c.bs0 =
+  // spt * triu_ld): only the diagonal triu_m x triu_m blocks are stored, sample s at C + s * triu_ld
+  int triu_spt = 1;
+  int64_t triu_ld = 0;
 };
 
 struct Gemm {

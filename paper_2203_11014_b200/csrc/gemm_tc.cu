@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "gemm_tc_kernel.cuh"
 
@@ -120,8 +121,10 @@ static bool make_lean(const Gemm& g, Lean* e) {
              (x.cross.ptr ? EF_CROSS : 0) | (x.aux.ptr ? EF_AUX : 0) | (x.resid.ptr ? EF_RESID : 0) |
              (x.bias ? EF_BIAS : 0);
   e->triu_m = x.triu_m;
+  e->triu_spt = x.triu_spt;
+  e->triu_ld = x.triu_ld;
   if (x.dcn_bwd) {
-    if (g.c.dt != F32 || !x.cross.ptr || !x.mask.ptr || !x.aux.ptr || g.c.cs != 1 || x.bias || x.accumulate) return false;
+    if (g.c.dt != F32 || !x.cross.ptr || !x.mask.ptr || !x.aux.ptr || x.bias || x.accumulate) return false;
     e->flags = EF_DCNB;
   }
   if (x.triu_m) {
@@ -200,15 +203,46 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
     if (g.e.triu_m) ok = true;   // scalar stores into the packed triangle
     p.fast8 = ok ? 1 : 0;
   }
-  if (special && !(p.fast8 && p.lean_id > 0 && !p.lanes_rows)) { p.lean = 0; p.lean_id = 0; }   // generic epi_apply
+  // specialised passes for the DCN-backward / triangle epilogues: row-major (fast8), or DCN backward with a
+  // column-contiguous C (lanes on rows); anything else takes the generic epi_apply
+  if (special && !(p.fast8 && p.lean_id > 0 && !p.lanes_rows) &&
+      !((p.ep.flags & EF_DCNB) && p.lanes_rows && p.lean_id > 0)) { p.lean = 0; p.lean_id = 0; }
   p.fast = (!p.lanes_rows && splits == 1 && vec_ok(g.c) && vec_ok(g.e.cross) && vec_ok(g.e.aux) &&
             vec_ok(g.e.resid) && vec_ok(g.e.mask)) ? 1 : 0;
   if (special || g.e.triu_m || g.e.dcn_bwd) p.fast = 0;
+  // TMA-store epilogue: row-major C (single-level rows, one batch stride), a variant within TS_FLAGS
+  // (fp32 += as a TMA reduce-add), 128-B passes that fit the warp's column half
+  CUtensorMap mc;
+  memset(&mc, 0, sizeof mc);
+  p.tstore = 0;
+  {
+    static int env = -1;
+    if (env < 0) { const char* ev = getenv("DHEN_TSTORE"); env = ev ? atoi(ev) : 1; }
+    const int es = g.c.dt == F32 ? 4 : 2;
+    const int fl = p.lean ? p.ep.flags : -1;
+    const bool flags_ok = fl >= 0 && (fl & ~TS_FLAGS) == 0 && (!(fl & EF_ACC) || g.c.dt == F32) && p.lean_id > 0;
+    const bool geom_ok = g.c.cs == 1 && g.c.rdiv == 0 && (g.c.zdiv == 1 || g.c.bs1 == 0) && !p.lanes_rows &&
+                         splits == 1 && ((uintptr_t)g.c.ptr % 16) == 0 && (g.c.rs * es) % 16 == 0 &&
+                         (g.c.bs0 * es) % 16 == 0 && (g.c.dt == F32 || BN >= 128) && g.c.rs >= g.N;
+    EncodeFn fn = encode_fn();
+    if (env && flags_ok && geom_ok && fn) {
+      const int64_t bstride = (g.batch > 1 && g.c.bs0) ? g.c.bs0 : (int64_t)g.c.rs * g.M;
+      cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)g.batch};
+      cuuint64_t strides[2] = {(cuuint64_t)(g.c.rs * es), (cuuint64_t)(bstride * es)};
+      cuuint32_t box[3] = {(cuuint32_t)(128 / es), 32, 1}, estr[3] = {1, 1, 1};
+      if (strides[1] % 16 == 0 && strides[1] > 0 &&
+          fn(&mc, g.c.dt == F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, g.c.ptr, dims,
+             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        p.tstore = 1;
+    }
+  }
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a.mn_major << 15) | ((uint32_t)p.b.mn_major << 16) |
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((p.pair ? 2 * BM : BM) >> 4) << 24);
   const int var = (p.lean_id > 0 && (p.fast8 || p.lanes_rows)) ? p.lean_id : 0;
-  cudaError_t e = BN == 64 ? launch_bn64(p, ma, mb, st, var) : BN == 128 ? launch_bn128(p, ma, mb, st, var)
-                                                           : launch_bn256(p, ma, mb, st, var);
+  if (p.tstore && var != p.lean_id) p.tstore = 0;
+  cudaError_t e = BN == 64 ? launch_bn64(p, ma, mb, mc, st, var) : BN == 128 ? launch_bn128(p, ma, mb, mc, st, var)
+                                                               : launch_bn256(p, ma, mb, mc, st, var);
   if (e != cudaSuccess) return e;
   if (p.splits > 1) return splitk_reduce(g, p.splits, ws.ptr, st);
   return cudaSuccess;

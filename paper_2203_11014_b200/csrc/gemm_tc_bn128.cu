@@ -3,8 +3,9 @@
 
 namespace dhen {
 namespace tc {
-cudaError_t launch_bn128(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st, int var) {
-  return launch_var<128, 4>(p, ma, mb, st, var);
+cudaError_t launch_bn128(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                        cudaStream_t st, int var) {
+  return launch_var<128, 4>(p, ma, mb, mc, st, var);
 }
 }  // namespace tc
 }  // namespace dhen

@@ -52,7 +52,8 @@ struct Lean {
   int64_t rs, rs_o, bs0, bs1, cs;
   int rdiv, zdiv;
   int c_f32, flags, gap_lo, gap_hi, hi_off;
-  int triu_m;
+  int triu_m, triu_spt;
+  int64_t triu_ld;
   float alpha;
 };
 
@@ -74,7 +75,10 @@ struct Params {
   int pair;           // 1: CTA pairs (cluster of 2) compute 256-row tiles with cta_group::2 MMAs
   long long* trace;   // debug: CTA 0 records clock64 timestamps (nullptr = off)
   int dbg;            // debug: 1 = skip the global epilogue pass (timing experiments only)
+  int tstore;         // 1: TMA-store epilogue (row-major C, flags within TS_FLAGS; fp32 += is a TMA reduce-add)
 };
+// epilogue flags the TMA-store path implements (any subset; EF_ACC only with fp32 C, as cp.reduce .add)
+constexpr int TS_FLAGS = EF_BIAS | EF_RELU | EF_ACC;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -168,6 +172,35 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t ad, uint64_t b
 }
 __device__ __forceinline__ void mma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
+}
+
+// ---- TMA-store epilogue helpers
+__device__ __forceinline__ void tma_store3(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(c2), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add3(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void sts4u(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ void ld_tmem32(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
 }
 
 __device__ __forceinline__ void ld4(const void* p, int64_t off, int dt, float* o) {
@@ -486,12 +519,19 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
       float a[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
       if (F & EF_TRIU) {
         // strict upper triangle of the per-sample Gram: pairs (i, j > i) row-major (R7)
-        const int i = rbase + r;
-        const int64_t zb = ok_ - col - (int64_t)i * e.rs;     // = z * bs0 (rs = 0 for this view)
+        int i = rbase + r, c0 = col;
+        int64_t zb = ok_ - col - (int64_t)i * e.rs;     // = z * bs0 (rs = 0 for this view)
+        if (e.triu_spt > 1) {                            // several samples per tile: diagonal blocks only
+          const int blk = i / e.triu_m;
+          if (col / e.triu_m != blk) continue;
+          zb += (int64_t)blk * e.triu_ld;
+          i -= blk * e.triu_m;
+          c0 -= blk * e.triu_m;
+        }
         const int64_t base = zb + (int64_t)i * e.triu_m - (int64_t)i * (i + 1) / 2 - i - 1;
 #pragma unroll
         for (int t = 0; t < 8; ++t)
-          if (col + t > i) stg1(e.c, base + col + t, CF32, a[t] * alpha);
+          if (c0 + t > i) stg1(e.c, base + c0 + t, CF32, a[t] * alpha);
         continue;
       }
       if (F & EF_DCNB) {
@@ -547,23 +587,46 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
   }
 }
 // Column-contiguous output (cs != 1, rs == 1): one row per lane, 16 accumulator columns in registers.
+// Every operand of the 16 columns is loaded before the first store (the stores may alias C's loads, so
+// the compiler could not hoist them itself): 16 x (operands) independent loads in flight per lane.
 template <int F, bool CF32>
 __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0, int N, const uint32_t* v) {
-  if constexpr ((F & (EF_DCNB | EF_TRIU)) != 0) return;   // host never selects these in column-contiguous mode
+  if constexpr ((F & EF_TRIU) != 0) return;   // host never selects the triangle in column-contiguous mode
+  constexpr bool LX = (F & (EF_CROSS | EF_DCNB)) != 0, LM = (F & (EF_MASK | EF_DCNB)) != 0;
+  constexpr bool LR = (F & EF_RESID) != 0, LC = (F & (EF_ACC | EF_DCNB)) != 0;
+  constexpr bool C32 = CF32 || (F & EF_DCNB) != 0;
   const float alpha = e.alpha;
+  float xs[16], ms[16], rv[16], cv[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int col = col0 + j;
+    if (col < N) {
+      const int64_t o = lo + (int64_t)col * e.cs;
+      if constexpr (LX) xs[j] = ldg_bf1(e.x, o);
+      if constexpr (LM) ms[j] = ldg_bf1(e.mask, o);
+      if constexpr (LR) rv[j] = ldg_bf1(e.resid, o);
+      if constexpr (LC) cv[j] = ldg_c1(e.c, o, C32);
+    }
+  }
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int col = col0 + j;
     if (col >= N) break;
     const int64_t o = lo + (int64_t)col * e.cs;
     float a = __uint_as_float(v[j]) * alpha;
+    if constexpr ((F & EF_DCNB) != 0) {
+      // B8 fused: dA = dT * X (bf16 aux), dX_acc += dT * A + dT
+      stg1(e.aux, o, 0, a * xs[j]);
+      stg1(e.c, o, 1, cv[j] + a * ms[j] + a);
+      continue;
+    }
     if (F & EF_BIAS) a += lean_bias(e, col);
     if (F & EF_AUX) stg1(e.aux, o, 0, a);
-    if (F & EF_CROSS) { const float x = ldg_bf1(e.x, o); a = x * a + x; }
+    if constexpr ((F & EF_CROSS) != 0) a = xs[j] * a + xs[j];
     if (F & EF_RELU) a = fmaxf(a, 0.f);
-    if (F & EF_MASK) a = ldg_bf1(e.mask, o) > 0.f ? a : 0.f;
-    if (F & EF_RESID) a += ldg_bf1(e.resid, o);
-    if (F & EF_ACC) a += ldg_c1(e.c, o, CF32);
+    if constexpr ((F & EF_MASK) != 0) a = ms[j] > 0.f ? a : 0.f;
+    if constexpr (LR) a += rv[j];
+    if constexpr ((F & EF_ACC) != 0) a += cv[j];
     stg1(e.c, o, CF32, a);
   }
 }
@@ -639,19 +702,28 @@ __device__ __forceinline__ void load_tile(const CUtensorMap* map, bool mn_major,
 // warps 2-9 = epilogue.  Work items (tile, batch index, K split) are strided over
 // the grid.  The TMEM accumulator is double-buffered (2 x BN columns) so the
 // epilogue of item i overlaps the MMAs of item i+1 and the loads of item i+2.
+template <int BN> struct EpiSmem {
+  static constexpr int SC = BN / 2 < 64 ? BN / 2 : 64;   // columns staged per epilogue pass
+  static constexpr int SROW = SC + 4;                     // float4 rows; 16-B granules conflict-free both ways
+  static constexpr int STAGE = 8 * 32 * SROW * 4;         // fp32 staging of the 8 epilogue warps
+  static constexpr int TBOX = 8 * 2 * 4096;               // TMA-store boxes: 2 x (32 rows x 128 B) per warp
+  static constexpr int BYTES = STAGE > TBOX ? STAGE : TBOX;
+};
+
 template <int BN, int STAGES, int VAR, bool PAIR>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                   const __grid_constant__ Params p) {
+                   const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ Params p) {
   constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
-  constexpr int SC = BN / 2 < 64 ? BN / 2 : 64;   // columns staged per epilogue pass
-  constexpr int SROW = SC + 4;              // float4 rows; 16-B granules conflict-free both ways
+  constexpr int SC = EpiSmem<BN>::SC;
+  constexpr int SROW = EpiSmem<BN>::SROW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  float* stage_all = (float*)(sB + STAGES * B_BYTES);
-  uint64_t* bars = (uint64_t*)(stage_all + 8 * 32 * SROW);   // full[S], empty[S], tfull[2], tempty[2]
+  float* stage_all = (float*)(sB + STAGES * B_BYTES);   // fp32 staging, or the TMA-store boxes (1024-B aligned)
+  float* sbias = (float*)((uint8_t*)stage_all + EpiSmem<BN>::BYTES);   // [2][BN] bias of the current tiles
+  uint64_t* bars = (uint64_t*)(sbias + 2 * BN);   // full[S], empty[S], tfull[2], tempty[2]
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
@@ -797,6 +869,71 @@ __global__ void __launch_bounds__(320, 1)
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[192 + li] = clock64();
       const int rbase = m0 + (int)crank * BM + q4 * 32;
+      if constexpr (VAR > 0 && ((VarF<VAR>::F & ~TS_FLAGS) == 0) && (!(VarF<VAR>::F & EF_ACC) || VarF<VAR>::C)) {
+        if (p.tstore && p.dbg != 1) {
+          // ---- TMA-store epilogue: lane = row; a pass takes 128 B of the row (64 bf16 / 32 fp32 columns) from
+          // TMEM, applies alpha / bias / ReLU, writes it into a 128-B-swizzled box (32 rows x 128 B) and one lane
+          // stores the box with cp.async.bulk.tensor (fp32 +=: cp.reduce.async.bulk .add).  Two boxes per warp.
+          constexpr int F = VarF<VAR>::F;
+          constexpr bool CF = VarF<VAR>::C;
+          constexpr int CW = CF ? 32 : 64;
+          float* sb = sbias + ab * BN;
+          if constexpr ((F & EF_BIAS) != 0) {
+            asm volatile("bar.sync 1, 256;" ::: "memory");   // every epilogue warp finished the tile that used sb
+            const int t = threadIdx.x - 64;
+            for (int j = t; j < BN; j += 256) sb[j] = (n0 + j < g.N) ? lean_bias(e, n0 + j) : 0.f;
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+          }
+          const uint32_t boxes = smem_u32(stage_all) + (uint32_t)((warp - 2) * 2 * 4096);
+          const float alpha = e.alpha;
+#pragma unroll 1
+          for (int pc = 0; pc < HC; pc += CW) {
+            uint32_t v[CW];
+            const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC + pc);
+            ld_tmem32(taddr, v);
+            if constexpr (CW == 64) ld_tmem32(taddr + 32, v + 32);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (pc + CW >= HC) {   // accumulator fully read: hand it back to the MMA warp
+              asm volatile("tcgen05.fence::before_thread_sync;");
+              __syncwarp();
+              if (lane == 0) tempty_arrive(smem_u32(tempty + ab), pair);
+            }
+            const int cl0 = hh * HC + pc;   // tile-local column of v[0]
+#pragma unroll
+            for (int j = 0; j < CW; ++j) {
+              float a = __uint_as_float(v[j]) * alpha;
+              if constexpr ((F & EF_BIAS) != 0) a += sb[cl0 + j];
+              if constexpr ((F & EF_RELU) != 0) a = fmaxf(a, 0.f);
+              v[j] = __float_as_uint(a);
+            }
+            const int bsel = (pc / CW) & 1;
+            const uint32_t box = boxes + (uint32_t)(bsel * 4096);
+            if (lane == 0) bulk_wait_read<1>();   // the store that last read this box is done with it
+            __syncwarp();
+            const uint32_t rowa = box + (uint32_t)(lane * 128);
+#pragma unroll
+            for (int gq = 0; gq < 8; ++gq) {   // 16-B granule gq of the row -> swizzled slot gq ^ (row & 7)
+              const uint32_t a = rowa + (uint32_t)(((gq ^ (lane & 7)) & 7) << 4);
+              if constexpr (CF) {
+                sts4u(a, v[4 * gq], v[4 * gq + 1], v[4 * gq + 2], v[4 * gq + 3]);
+              } else {
+                sts4u(a, pack_bf2(__uint_as_float(v[8 * gq]), __uint_as_float(v[8 * gq + 1])),
+                      pack_bf2(__uint_as_float(v[8 * gq + 2]), __uint_as_float(v[8 * gq + 3])),
+                      pack_bf2(__uint_as_float(v[8 * gq + 4]), __uint_as_float(v[8 * gq + 5])),
+                      pack_bf2(__uint_as_float(v[8 * gq + 6]), __uint_as_float(v[8 * gq + 7])));
+              }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr ((F & EF_ACC) != 0) tma_reduce_add3(&tma_c, box, n0 + cl0, rbase, z);
+              else tma_store3(&tma_c, box, n0 + cl0, rbase, z);
+              bulk_commit();
+            }
+          }
+          continue;
+        }
+      }
       if (p.lanes_rows) {
         // column-contiguous output: row per lane straight from TMEM; consecutive lanes = consecutive addresses
         const int row = rbase + lane;
@@ -967,6 +1104,7 @@ __global__ void __launch_bounds__(320, 1)
       if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[320 + li] = clock64();
     }
   }
+  if (p.tstore && warp >= 2 && lane == 0) bulk_wait_all();   // TMA stores done reading smem and written
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (pair) {
@@ -979,9 +1117,10 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 template <int BN, int STAGES, int VAR>
-static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st) {
-  constexpr int SC = BN / 2 < 64 ? BN / 2 : 64;
-  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + 8 * 32 * (SC + 4) * 4 + (2 * STAGES + 4) * 8 + 16 + 1024;
+static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                          cudaStream_t st) {
+  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + EpiSmem<BN>::BYTES + 2 * BN * 4 + (2 * STAGES + 4) * 8 +
+                       16 + 1024;
   static_assert(SMEM <= 227 * 1024, "smem");
   static bool attr = false;
   if (!attr) {
@@ -1013,14 +1152,14 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
         }
       }
       cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(items, max_clusters)));
-      cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, VAR, true>, ma, mb, p);
+      cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, VAR, true>, ma, mb, mc, p);
       if (e != cudaSuccess) return e;
       ++g_launches;
       continue;
     }
     {
       const int grid = (int)std::min<int64_t>(items, 148);
-      gemm_tc_kernel<BN, STAGES, VAR, false><<<grid, 320, SMEM, st>>>(ma, mb, p);
+      gemm_tc_kernel<BN, STAGES, VAR, false><<<grid, 320, SMEM, st>>>(ma, mb, mc, p);
     }
     ++g_launches;
   }
@@ -1029,19 +1168,23 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
 
 // Launch with the epilogue variant as a template argument (one variant per kernel instantiation).
 template <int BN, int STAGES>
-cudaError_t launch_var(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st, int var) {
+cudaError_t launch_var(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                       cudaStream_t st, int var) {
   switch (var) {
 #define LV_L(i, f, c) \
-  case i: return launch<BN, STAGES, i>(p, ma, mb, st);
+  case i: return launch<BN, STAGES, i>(p, ma, mb, mc, st);
     LEAN_VARIANTS(LV_L)
 #undef LV_L
-    default: return launch<BN, STAGES, 0>(p, ma, mb, st);
+    default: return launch<BN, STAGES, 0>(p, ma, mb, mc, st);
   }
 }
 // defined in gemm_tc_bn{64,128,256}.cu (parallel compilation of the instantiations)
-cudaError_t launch_bn64(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st, int var);
-cudaError_t launch_bn128(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st, int var);
-cudaError_t launch_bn256(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st, int var);
+cudaError_t launch_bn64(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                        cudaStream_t st, int var);
+cudaError_t launch_bn128(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                         cudaStream_t st, int var);
+cudaError_t launch_bn256(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                         cudaStream_t st, int var);
 
 }  // namespace tc
 }  // namespace dhen

@@ -126,6 +126,9 @@ struct dhen_ctx {
   float* dXacc = nullptr;
   void* dR = nullptr;
   void* dY[2] = {nullptr, nullptr};
+  // layout experiments (env DHEN_GRAM_SPT, DHEN_TR_SMALL_M; measured slower on C2, default off): several
+  // samples per Gram tile; transposed (column-contiguous C) Gram-backward / DCN dT for m < 128
+  int gram_spt = 0, tr_small_m = 0;
   float* big = nullptr;     // fp32 scratch [B*H*m*m] / [B*m*m] (Gram, attention S / dP)
   void* tA = nullptr;       // dtype scratch [B * m * d * 3] (dT, dQKV, ...)
   void* tB = nullptr;       // dtype scratch [B * m * d]
@@ -526,10 +529,15 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
     switch (md.s.kind) {
       case DHEN_DOT: {   // F1 + F2
         const int h = mi * (mi - 1) / 2;
-        // Gram X X^T per sample; the epilogue writes the strict upper triangle Z directly (F1, R7)
-        Gemm g = mk(mi, mi, d, B, operand(X, dt, d, 1, (int64_t)mi * d), operand(X, dt, d, 1, (int64_t)mi * d),
-                    view(md.Z, dt, 0, 1, h));
+        // Gram X X^T per sample; the epilogue writes the strict upper triangle Z directly (F1, R7).  For
+        // m <= 64 (dividing 128) spt = 128 / m samples share one 128-row tile: the tile is the Gram of the
+        // stacked samples and only its diagonal blocks are stored (full MMA rows, one tile per spt samples).
+        const int spt = (c->gram_spt && dt == BF16 && mi <= 64 && 128 % mi == 0 && B % (128 / mi) == 0) ? 128 / mi : 1;
+        Gemm g = mk(spt * mi, spt * mi, d, B / spt, operand(X, dt, d, 1, (int64_t)spt * mi * d),
+                    operand(X, dt, d, 1, (int64_t)spt * mi * d), view(md.Z, dt, 0, 1, (int64_t)spt * h));
         g.e.triu_m = mi;
+        g.e.triu_spt = spt;
+        g.e.triu_ld = h;
         RET(G_(g, c, st, "dot.gram"));
         Gemm v = mk(B, l * d, h, 1, operand(md.Z, dt, h, 1), operand(p(md.Wm), dt, h, 1), view(Us, F32, ldU, 1));
         RET(G_(v, c, st, "dot.proj"));
@@ -648,8 +656,13 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         Gemm gz = mk(B, h, l * d, 1, operand(dU, dt, ldU, 1), operand(p(md.Wm), dt, 1, h), view(c->tA, dt, h, 1));
         RET(G_(gz, c, st, "dot.proj_dgrad"));
         KT("dot.sym", 0, (double)B * (h + mi * mi) * es, sym_from_triu(c->tA, c->tD, dt, B, mi, h, st));
-        Gemm gx = mk(mi, d, mi, B, operand(c->tD, dt, mi, 1, (int64_t)mi * mi), operand(X, dt, 1, d, (int64_t)mi * d),
-                     view(acc, F32, d, 1, (int64_t)mi * d));
+        // dX_b += S_b X_b.  m < 128: as its transpose dX_b^T += X_b^T S_b (M = d rows fill the 128-row MMA
+        // tile; S symmetric, K-major), C column-contiguous
+        Gemm gx = c->tr_small_m && mi < 128 && dt == BF16
+                      ? mk(d, mi, mi, B, operand(X, dt, 1, d, (int64_t)mi * d), operand(c->tD, dt, mi, 1, (int64_t)mi * mi),
+                           view(acc, F32, 1, d, (int64_t)mi * d))
+                      : mk(mi, d, mi, B, operand(c->tD, dt, mi, 1, (int64_t)mi * mi), operand(X, dt, 1, d, (int64_t)mi * d),
+                           view(acc, F32, d, 1, (int64_t)mi * d));
         gx.e.accumulate = 1;
         RET(G_(gx, c, st, "dot.gram_bwd"));
         break;
@@ -660,12 +673,17 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
       case DHEN_DCN: {   // B8
         void* dA = c->tB;
         // dT = W_u dU (never stored): the epilogue forms dA = dT (.) X and dX += dT (.) A + dT (B8)
-        Gemm gt = mk(mi, d, l, B, operand(p(md.Wu), dt, l, 1), operand(dU, dt, 1, d, ldU),
-                     view(acc, F32, d, 1, (int64_t)mi * d));
+        // m < 128: as its transpose dT_b^T = dU_b^T W_u^T (M = d rows fill the MMA tile), C column-contiguous
+        const bool tr = c->tr_small_m && mi < 128 && dt == BF16;
+        Gemm gt = tr ? mk(d, mi, l, B, operand(dU, dt, 1, d, ldU), operand(p(md.Wu), dt, l, 1),
+                          view(acc, F32, 1, d, (int64_t)mi * d))
+                     : mk(mi, d, l, B, operand(p(md.Wu), dt, l, 1), operand(dU, dt, 1, d, ldU),
+                          view(acc, F32, d, 1, (int64_t)mi * d));
+        const int64_t vr = tr ? 1 : d, vc = tr ? d : 1;
         gt.e.dcn_bwd = 1;
-        gt.e.cross = view((void*)X, dt, d, 1, (int64_t)mi * d);
-        gt.e.mask = view(md.A, dt, d, 1, (int64_t)mi * d);
-        gt.e.aux = view(dA, dt, d, 1, (int64_t)mi * d);
+        gt.e.cross = view((void*)X, dt, vr, vc, (int64_t)mi * d);
+        gt.e.mask = view(md.A, dt, vr, vc, (int64_t)mi * d);
+        gt.e.aux = view(dA, dt, vr, vc, (int64_t)mi * d);
         RET(G_(gt, c, st, "dcn.dT_fused"));
         Gemm gw_u = mk(mi, l, B * d, 1, operand(md.T, dt, d, 1, 0, 0, 1, d, (int64_t)mi * d),
                        operand(dU, dt, d, 1, 0, 0, 1, d, ldU), view(gp(md.Wu), F32, l, 1));
@@ -825,6 +843,8 @@ static dhen_status make_ctx(const dhen_config* cfg, const dhen_dist* dist, dhen_
   if (dd.world < 1 || dd.rank < 0 || dd.rank >= dd.world)
     return fail(DHEN_E_CONFIG, "dhen: rank=%d world=%d", dd.rank, dd.world);
   c->cfg = *cfg;
+  { const char* e = getenv("DHEN_GRAM_SPT"); c->gram_spt = e ? atoi(e) : 0; }
+  { const char* e = getenv("DHEN_TR_SMALL_M"); c->tr_small_m = e ? atoi(e) : 0; }
   if (c->cfg.ln_eps <= 0.f) c->cfg.ln_eps = 1e-5f;
   c->mods_cfg.resize(cfg->n_layers);
   c->layers_cfg.resize(cfg->n_layers);

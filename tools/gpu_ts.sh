@@ -1,0 +1,8 @@
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { echo build failed; exit 1; }
+for pr in 0 1; do
+  echo "== DHEN_PAIR=$pr"
+  DHEN_PAIR=$pr timeout 120 python tools/gemm_bench.py --cfg C4 --only attn.ffn 2>&1 | grep -v Warn
+  DHEN_PAIR=$pr timeout 120 python tools/gemm_bench.py --cfg C4 --only dcn 2>&1 | grep -v Warn
+  DHEN_PAIR=$pr DHEN_DBG_EPI=1 timeout 120 python tools/gemm_bench.py --cfg C4 --only attn.ffn1 2>&1 | grep -v Warn
+done
