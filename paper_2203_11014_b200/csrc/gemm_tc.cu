@@ -57,7 +57,10 @@ static bool make_map(CUtensorMap* map, OpMap* om, const Operand& o, int rows, in
   om->zdiv = o.zdiv;
   om->z0 = om->z1 = om->mo = -1;
   om->mdiv = o.mdiv ? o.mdiv : 1;
-  if (o.kdiv && (o.kdiv % BK != 0 || K % o.kdiv != 0)) return false;
+  // two-level K: kdiv a multiple of BK (a k-block inside one outer index), or, MN-major only, kdiv dividing BK
+  // (the box spans BK / kdiv outer indices: k-rows land in smem in (outer, inner) = k order)
+  const bool ko_in_box = o.kdiv && o.kdiv < BK && BK % o.kdiv == 0 && mnmaj && !kmaj;
+  if (o.kdiv && ((o.kdiv % BK != 0 && !ko_in_box) || K % o.kdiv != 0)) return false;
   if (o.mdiv && (o.mdiv % tile_rows != 0 || rows % o.mdiv != 0)) return false;
   cuuint64_t dims[5] = {1, 1, 1, 1, 1}, strides[4] = {0, 0, 0, 0};
   cuuint32_t box[5] = {1, 1, 1, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
@@ -73,7 +76,11 @@ static bool make_map(CUtensorMap* map, OpMap* om, const Operand& o, int rows, in
   }
   strides[0] = s1 * es;
   int r = 2;
-  if (o.kdiv) { dims[r] = K / o.kdiv; strides[r - 1] = o.s_ko * es; ++r; }
+  if (o.kdiv) {
+    dims[r] = K / o.kdiv; strides[r - 1] = o.s_ko * es;
+    if (ko_in_box) { box[1] = o.kdiv; box[r] = BK / o.kdiv; }
+    ++r;
+  }
   if (o.mdiv) { dims[r] = rows / o.mdiv; strides[r - 1] = o.s_mo * es; om->mo = r; ++r; }
   if (o.zdiv > 1 && o.bs1 != 0) { dims[r] = o.zdiv; strides[r - 1] = o.bs1 * es; om->z1 = r; ++r; }
   const int nb0 = (batch + o.zdiv - 1) / o.zdiv;

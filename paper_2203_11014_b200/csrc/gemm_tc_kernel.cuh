@@ -806,8 +806,8 @@ __global__ void __launch_bounds__(320, 1)
           }
           load_tile(&tma_a, amn, qa, ka, koa, smem_u32(sA) + s * A_BYTES, fb, BM / 64, pair);
           load_tile(&tma_b, bmn, qb, kbk, kob, smem_u32(sB) + s * B_BYTES, fb, pair ? BN / 128 : BN / 64, pair);
-          ka += BK; if (ka >= kda) { ka = 0; ++koa; }
-          kbk += BK; if (kbk >= kdb) { kbk = 0; ++kob; }
+          ka += BK; while (ka >= kda) { ka -= kda; ++koa; }     // kdiv < BK: several outer indices per k-block
+          kbk += BK; while (kbk >= kdb) { kbk -= kdb; ++kob; }
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -859,6 +859,7 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t stage = smem_u32(stage_all) + (uint32_t)((warp - 2) * 32 * SROW * 4);
     const Gemm& g = p.g;
     const Lean& e = p.ep;
+    uint32_t tsel = 0;   // TMA-store box parity of this warp (running over all passes of all tiles)
     int li = 0;
     for (int item = wid; item < total; item += nwk, ++li) {
       int m0, n0, z, sp, kb0, nk;
@@ -906,8 +907,8 @@ __global__ void __launch_bounds__(320, 1)
               if constexpr ((F & EF_RELU) != 0) a = fmaxf(a, 0.f);
               v[j] = __float_as_uint(a);
             }
-            const int bsel = (pc / CW) & 1;
-            const uint32_t box = boxes + (uint32_t)(bsel * 4096);
+            const uint32_t box = boxes + (uint32_t)((tsel & 1) * 4096);   // alternate across passes AND tiles
+            ++tsel;
             if (lane == 0) bulk_wait_read<1>();   // the store that last read this box is done with it
             __syncwarp();
             const uint32_t rowa = box + (uint32_t)(lane * 128);

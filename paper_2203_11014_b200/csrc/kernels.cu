@@ -1252,6 +1252,22 @@ cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, 
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ block-diagonal token map
+// out[i][k] (bf16, [spt m][spt l]) = W[i % m][k % l] if i / m == k / l else 0; W bf16 [m][l]
+__global__ void blockdiag_k(const __nv_bfloat16* W, int m, int l, int spt, __nv_bfloat16* out) {
+  const int n = spt * m * spt * l;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int i = t / (spt * l), k = t - i * (spt * l);
+    out[t] = (i / m == k / l) ? W[(i % m) * l + (k % l)] : __float2bfloat16_rn(0.f);
+  }
+}
+cudaError_t blockdiag(const void* W, int m, int l, int spt, void* out, cudaStream_t st) {
+  const int n = spt * m * spt * l;
+  blockdiag_k<<<(n + 255) / 256, 256, 0, st>>>((const __nv_bfloat16*)W, m, l, spt, (__nv_bfloat16*)out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ SGD, casts, init
 __global__ void sgd_cast_k(float* master, const float* grad, float lr, void* copy, int dt, int64_t n) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {

@@ -134,6 +134,7 @@ struct dhen_ctx {
   void* tB = nullptr;       // dtype scratch [B * m * d]
   void* tC = nullptr;       // dtype scratch [B * m * max(f, d)] (dF, dh*)
   void* tD = nullptr;       // dtype scratch [B * H * m * m] (dS, S of Dot bwd)
+  void* bdiag = nullptr;    // bf16 [128][128]: blockdiag(W_u, ..) for several samples per 128-row tile
   float* rtmp = nullptr;    // fp32 [B * m * d]
   float* red = nullptr;     // reduction partials
   size_t red_bytes = 0;
@@ -382,6 +383,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   c->tC = work.take((size_t)std::max<int64_t>(tC_elems, 1) * es);
   c->tD = work.take((size_t)B * std::max(H_mm_max, 1) * es);
   c->rtmp = (float*)work.take(rows_d * 4);
+  c->bdiag = work.take((size_t)128 * 128 * 2);   // block-diagonal token map (DCN backward, m <= 64)
   c->red_bytes = (size_t)16 << 20;
   c->red = (float*)work.take(c->red_bytes);
   c->ws.bytes = (size_t)256 << 20;
@@ -673,6 +675,22 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
       case DHEN_DCN: {   // B8
         void* dA = c->tB;
         // dT = W_u dU (never stored): the epilogue forms dA = dT (.) X and dX += dT (.) A + dT (B8)
+        // m <= 64 (dividing 128), l dividing 64: spt = 128 / m samples per 128-row tile, as one GEMM with the
+        // block-diagonal token map blockdiag(W_u, .., W_u) [spt m][spt l] against spt stacked dU_b (the B
+        // operand's two-level K: k -> (sample, t)), so every MMA row and epilogue warp carries data.
+        const int spt = 128 / std::max(mi, 1);
+        const bool pack = !c->tr_small_m && dt == BF16 && mi <= 64 && 128 % mi == 0 && l <= 64 && 64 % l == 0 &&
+                          (spt * l) % 64 == 0 && B % spt == 0;
+        if (pack) {
+          KT("dcn.bdiag", 0, 2.0 * 128 * 128 * es, blockdiag(p(md.Wu), mi, l, spt, c->bdiag, st));
+          Gemm gt = mk(spt * mi, d, spt * l, B / spt, operand(c->bdiag, dt, spt * l, 1),
+                       operand(dU, dt, 1, d, spt * ldU, 0, 1, l, ldU), view(acc, F32, d, 1, (int64_t)spt * mi * d));
+          gt.e.dcn_bwd = 1;
+          gt.e.cross = view((void*)X, dt, d, 1, (int64_t)spt * mi * d);
+          gt.e.mask = view(md.A, dt, d, 1, (int64_t)spt * mi * d);
+          gt.e.aux = view(dA, dt, d, 1, (int64_t)spt * mi * d);
+          RET(G_(gt, c, st, "dcn.dT_fused"));
+        } else {
         // m < 128: as its transpose dT_b^T = dU_b^T W_u^T (M = d rows fill the MMA tile), C column-contiguous
         const bool tr = c->tr_small_m && mi < 128 && dt == BF16;
         Gemm gt = tr ? mk(d, mi, l, B, operand(dU, dt, 1, d, ldU), operand(p(md.Wu), dt, l, 1),
@@ -685,6 +703,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         gt.e.mask = view(md.A, dt, vr, vc, (int64_t)mi * d);
         gt.e.aux = view(dA, dt, vr, vc, (int64_t)mi * d);
         RET(G_(gt, c, st, "dcn.dT_fused"));
+        }
         Gemm gw_u = mk(mi, l, B * d, 1, operand(md.T, dt, d, 1, 0, 0, 1, d, (int64_t)mi * d),
                        operand(dU, dt, d, 1, 0, 0, 1, d, ldU), view(gp(md.Wu), F32, l, 1));
         gw_u.e.accumulate = 1;

@@ -108,6 +108,19 @@ def test_two_level_k_token_mix_wgrad():
     assert err < 2e-5, err
 
 
+@pytest.mark.parametrize("path", [2, 1])
+def test_two_level_k_inside_one_k_block(path):
+    """B operand MN-major with a two-level K whose inner extent (kdiv = 32) divides the 64-wide k-block: the
+    DCN-backward packing (two samples' dU rows stacked along K against a block-diagonal token map)."""
+    Bn, m, l, d, mo = 6, 64, 32, 128, 96
+    spt = 2
+    a = (spt * l, 1, 0, 0, 1, 0, 0)                       # blockdiag map [spt m][spt l], shared by the batch
+    b = (1, d, spt * mo * d, 0, 1, l, mo * d)             # B(z, c, k) = dU[spt z + k / l][k % l][c]
+    err = _run(spt * m, d, spt * l, Bn // spt, a, b, (d, 1, spt * m * d, 0, 1), acc=1, path=path,
+               expect_tc=(path == 2))
+    assert err < 2e-5, err
+
+
 def test_split_k_wgrad():
     # dW = dA^T X with K = B*m rows (both operands MN-major), few output tiles -> split-K
     M, N, K = 128, 128, 65536
