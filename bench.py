@@ -311,8 +311,19 @@ def main():
         bound, unit, achieved, peak = "alu", "TFLOP/s", top["flops"] / top["ms"] / 1e9, 148 * 128 * 2 * 1.965e-3
     else:
         bound, unit, achieved, peak = "hbm", "GB/s", top["bytes"] / top["ms"] / 1e6, pk["hbm"]
+    # traffic: DRAM bytes per launch of this op's kernel from the committed ncu --set full capture
+    # (profiles/ncu_traffic.json, written by tools/ncu_summary.py traffic), when one exists for this op
+    traffic, traffic_src = None, None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        ent = json.load(open(tp)).get(args.config, {}).get(top["name"])
+        if ent:
+            traffic, traffic_src = ent["traffic_bytes_per_launch"], ent["summary"]
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-            "traffic": None, "kernel": top["name"], "share_of_step": top["ms"] / tot_ms,
+            "traffic": traffic, "traffic_source": traffic_src,
+            "algorithmic_bytes_per_launch": top["bytes"] / top["launches"],
+            "algorithmic_flops_per_launch": top["flops"] / top["launches"],
+            "kernel": top["name"], "share_of_step": top["ms"] / tot_ms,
             "per_launch_ms": per_launch_ms, "launches_per_step": top["launches"] / args.steps,
             "peak_source": pk["src"] + (" sustained bf16" if bound == "tensor" else "")}
     if args.profile_json and rank == 0:

@@ -185,6 +185,11 @@ __device__ __forceinline__ void tma_reduce_add3(const CUtensorMap* map, uint32_t
                "r"(c0), "r"(c1), "r"(c2), "r"(src)
                : "memory");
 }
+// fp32 += of 4 consecutive elements in L2 (REDG.ADD.F32x4; subnormal addends flush to zero)
+__device__ __forceinline__ void red_add4(float* p, const float* v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3])
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
@@ -448,7 +453,7 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
   // operands to prefetch per row: bf16 uint4 slots (X / A / mask / resid / bf16 C) and fp32 C
   constexpr int NB = ((F & (EF_CROSS | EF_DCNB)) ? 1 : 0) + ((F & (EF_MASK | EF_DCNB)) ? 1 : 0) +
                      ((F & EF_RESID) ? 1 : 0) + (((F & EF_ACC) && !CF32) ? 1 : 0);
-  constexpr bool F32C = ((F & EF_ACC) && CF32) || (F & EF_DCNB);
+  constexpr bool F32C = (F & EF_ACC) && CF32;   // DCN backward adds into C with red.global (no load)
   constexpr int REGS = NB * 4 + (F32C ? 8 : 0);               // registers per prefetched row
   constexpr int SLX = 0;                                                     // compile-time slot indices
   constexpr int SLM = SLX + ((F & (EF_CROSS | EF_DCNB)) ? 1 : 0);
@@ -536,17 +541,19 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
       }
       if (F & EF_DCNB) {
         // B8 fused: dA = dT * X (bf16, aux), dX_acc += dT * A + dT  (dT = the fp32 accumulator)
-        float xv[8], av[8], da[8];
+        // (the fp32 dX accumulator is updated in L2 by vector reductions: one adder per element, fixed order)
+        float xv[8], av[8], da[8], dx[8];
         unpack_bf8(ub[cb][k][SLX], xv);
         unpack_bf8(ub[cb][k][SLM], av);
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
           const float v = a[t] * alpha;
           da[t] = v * xv[t];
-          cv[cb][k][t] += v * av[t] + v;
+          dx[t] = v * av[t] + v;
         }
         stg8<false>(e.aux, ok_, da);
-        stg8<true>(e.c, ok_, cv[cb][k]);
+        red_add4((float*)e.c + ok_, dx);
+        red_add4((float*)e.c + ok_ + 4, dx + 4);
         continue;
       }
 #pragma unroll
@@ -593,7 +600,7 @@ template <int F, bool CF32>
 __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0, int N, const uint32_t* v) {
   if constexpr ((F & EF_TRIU) != 0) return;   // host never selects the triangle in column-contiguous mode
   constexpr bool LX = (F & (EF_CROSS | EF_DCNB)) != 0, LM = (F & (EF_MASK | EF_DCNB)) != 0;
-  constexpr bool LR = (F & EF_RESID) != 0, LC = (F & (EF_ACC | EF_DCNB)) != 0;
+  constexpr bool LR = (F & EF_RESID) != 0, LC = (F & EF_ACC) != 0;
   constexpr bool C32 = CF32 || (F & EF_DCNB) != 0;
   const float alpha = e.alpha;
   float xs[16], ms[16], rv[16], cv[16];
@@ -617,7 +624,7 @@ __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0,
     if constexpr ((F & EF_DCNB) != 0) {
       // B8 fused: dA = dT * X (bf16 aux), dX_acc += dT * A + dT
       stg1(e.aux, o, 0, a * xs[j]);
-      stg1(e.c, o, 1, cv[j] + a * ms[j] + a);
+      asm volatile("red.global.add.f32 [%0], %1;" ::"l"((float*)e.c + o), "f"(a * ms[j] + a) : "memory");
       continue;
     }
     if (F & EF_BIAS) a += lean_bias(e, col);

@@ -403,7 +403,7 @@ static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const 
   const double mn = (double)g.M * g.N * g.batch;
   double bytes = (double)g.M * g.K * es * (g.a.bs0 || g.a.bs1 ? g.batch : 1) +
                  (double)g.N * g.K * es * (g.b.bs0 || g.b.bs1 ? g.batch : 1) +
-                 vbytes(g.c, mn) * (g.e.accumulate ? 2 : 1) + vbytes(g.e.resid, mn) + vbytes(g.e.mask, mn) +
+                 vbytes(g.c, mn) * (g.e.accumulate || g.e.dcn_bwd ? 2 : 1) + vbytes(g.e.resid, mn) + vbytes(g.e.mask, mn) +
                  vbytes(g.e.cross, mn) + vbytes(g.e.aux, mn);
   ProfScope ps(c, tag, 2.0 * (double)g.M * g.N * g.K * g.batch, bytes, st);
   CK(gemm_run(g, c->ws, st));

@@ -1,6 +1,11 @@
 """Summarise ncu outputs for profiles/.
     python tools/ncu_summary.py launches <launches.csv>      -> per-kernel share of device time
-    python tools/ncu_summary.py full <report.ncu-rep>        -> key metrics of a --set full capture"""
+    python tools/ncu_summary.py full <report.ncu-rep>        -> key metrics of a --set full capture
+    python tools/ncu_summary.py traffic <report.ncu-rep> <config> <op> <summary.txt>
+        -> add {config: {op: dram bytes per launch, ncu duration}} to profiles/ncu_traffic.json (read by bench.py
+           to fill roofline.traffic for that op)"""
+import json
+import os
 import csv
 import io
 import subprocess
@@ -45,5 +50,31 @@ def full(path):
                 print(f"{h} [{u}] = {v}")
 
 
+def traffic(path, cfg, op, summary):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    r = rows[2]
+    get = lambda k: r[hdr.index(k)]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    nbytes = sum(float(get(k).replace(",", "")) * scale[units[hdr.index(k)]]
+                 for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    dur = float(get("gpu__time_duration.sum").replace(",", ""))
+    dur_us = dur * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+                    "second": 1e6, "s": 1e6}[units[hdr.index("gpu__time_duration.sum")]]
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
+    j = json.load(open(p)) if os.path.exists(p) else {}
+    j.setdefault(cfg, {})[op] = {"kernel": get("Kernel Name"), "traffic_bytes_per_launch": nbytes,
+                                 "ncu_duration_us": dur_us, "summary": summary,
+                                 "how": "ncu --set full --clock-control none, one launch after warm-up; "
+                                        "dram__bytes_read.sum + dram__bytes_write.sum (writes still dirty in the "
+                                        "126 MB L2 when the kernel ends are not counted)"}
+    json.dump(j, open(p, "w"), indent=1, sort_keys=True)
+    print(f"{cfg} {op}: {nbytes / 1e6:.1f} MB per launch, {dur_us:.1f} us under ncu")
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    if sys.argv[1] == "traffic":
+        traffic(*sys.argv[2:6])
+    else:
+        {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
