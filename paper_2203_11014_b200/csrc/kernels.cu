@@ -448,8 +448,215 @@ static cudaError_t ln_bwd_generic(const void* dY, int dydt, const void* Rsave, c
 }
 
 
+// ------------------------------------------------------------------ LayerNorm, several rows per warp (bf16, d = 8 LPR)
+// A row is LPR lanes x 8 columns (16-B bf16 / 32-B fp32 accesses); a warp holds 32 / LPR rows per pass and
+// UR passes per iteration, so UR * 32 / LPR rows of loads are in flight per warp.  Row reductions are
+// shuffles inside the LPR-lane segment (fixed order: deterministic).
+template <int LPR>
+__device__ __forceinline__ float seg_sum(float v) {
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ void ld8f(const float* p, float* o) {
+  const float4 a = __ldcs(reinterpret_cast<const float4*>(p)), b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
+__device__ __forceinline__ void ld8b(const __nv_bfloat16* p, float* o) { VIO<8, __nv_bfloat16>::ld(p, o); }
+template <typename TD> __device__ __forceinline__ void ld8(const TD* p, float* o);
+template <> __device__ __forceinline__ void ld8<float>(const float* p, float* o) { ld8f(p, o); }
+template <> __device__ __forceinline__ void ld8<__nv_bfloat16>(const __nv_bfloat16* p, float* o) { ld8b(p, o); }
+
+template <int LPR, int UR>
+__global__ void __launch_bounds__(256) ln_fwd_r(const float* __restrict__ U, const __nv_bfloat16* __restrict__ addx,
+                                                const __nv_bfloat16* __restrict__ gamma,
+                                                const __nv_bfloat16* __restrict__ beta, float eps, int64_t rows,
+                                                __nv_bfloat16* __restrict__ Y, __nv_bfloat16* __restrict__ Rsave,
+                                                float* __restrict__ mu, float* __restrict__ rstd) {
+  constexpr int d = 8 * LPR, RPW = 32 / LPR, RPI = RPW * UR;
+  const int lane = threadIdx.x & 31, sub = lane / LPR, c = (lane % LPR) * 8;
+  float g[8], b[8];
+  ld8b(gamma + c, g);
+  ld8b(beta + c, b);
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t r0 = ((int64_t)blockIdx.x * 8 + threadIdx.x / 32) * RPI; r0 < rows; r0 += nw * RPI) {
+    float v[UR][8];
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      const int64_t r = r0 + u * RPW + sub;
+      if (r < rows) {
+        ld8f(U + r * d + c, v[u]);
+        if (addx) {
+          float x[8];
+          ld8b(addx + r * d + c, x);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) v[u][t] += x[t];
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[u][t] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      const int64_t r = r0 + u * RPW + sub;
+      float s = 0.f;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) s += v[u][t];
+      const float mean = seg_sum<LPR>(s) / d;
+      float s2 = 0.f;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { const float q = v[u][t] - mean; s2 += q * q; }
+      const float rs = rsqrtf(seg_sum<LPR>(s2) / d + eps);
+      if (r < rows) {
+        float y[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) y[t] = (v[u][t] - mean) * rs * g[t] + b[t];
+        VIO<8, __nv_bfloat16>::st(Y + r * d + c, y);
+        if (Rsave) VIO<8, __nv_bfloat16>::st(Rsave + r * d + c, v[u]);
+        if (c == 0) { mu[r] = mean; rstd[r] = rs; }
+      }
+    }
+  }
+}
+
+template <int LPR, int UR, typename TD>
+__global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const __nv_bfloat16* __restrict__ Rsave,
+                                                const float* __restrict__ mu, const float* __restrict__ rstd,
+                                                const __nv_bfloat16* __restrict__ gamma, int64_t rows,
+                                                __nv_bfloat16* __restrict__ dR, float* __restrict__ acc, int acc_mode,
+                                                float* __restrict__ part, int64_t rows_per_block) {
+  constexpr int d = 8 * LPR, RPW = 32 / LPR, RPI = RPW * UR;
+  __shared__ float sred[8][2][d];
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32, sub = lane / LPR, c = (lane % LPR) * 8;
+  const int64_t rb0 = blockIdx.x * rows_per_block, rb1 = min(rows, rb0 + rows_per_block);
+  float g[8], pg[8], pb[8];
+  ld8b(gamma + c, g);
+#pragma unroll
+  for (int t = 0; t < 8; ++t) { pg[t] = 0.f; pb[t] = 0.f; }
+  for (int64_t r0 = rb0 + (int64_t)w * RPI; r0 < rb1; r0 += 8 * RPI) {
+    float dy[UR][8], x[UR][8], mr[UR], rr[UR];
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {   // every load of the iteration issued before the first use
+      const int64_t r = r0 + u * RPW + sub;
+      if (r < rb1) {
+        ld8<TD>(dY + r * d + c, dy[u]);
+        ld8b(Rsave + r * d + c, x[u]);
+        mr[u] = mu[r];
+        rr[u] = rstd[r];
+      } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) { dy[u][t] = 0.f; x[u][t] = 0.f; }
+        mr[u] = 0.f; rr[u] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      const int64_t r = r0 + u * RPW + sub;
+      const bool ok = r < rb1;
+      const float m_ = mr[u], rs = rr[u];
+      float xh[8], gy[8], s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        xh[t] = (x[u][t] - m_) * rs;
+        gy[t] = dy[u][t] * g[t];
+        pg[t] += dy[u][t] * xh[t];
+        pb[t] += dy[u][t];
+        s1 += gy[t];
+        s2 += gy[t] * xh[t];
+      }
+      s1 = seg_sum<LPR>(s1) / d;
+      s2 = seg_sum<LPR>(s2) / d;
+      if (ok) {
+        float o[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) o[t] = rs * (gy[t] - s1 - xh[t] * s2);
+        uint4 q;
+        {
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]),
+                         h2 = __floats2bfloat162_rn(o[4], o[5]), h3 = __floats2bfloat162_rn(o[6], o[7]);
+          q = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                         *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+        }
+        *reinterpret_cast<uint4*>(dR + r * d + c) = q;
+        if (acc_mode) {   // the stored (rounded) value feeds the residual path
+          const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+          float qf[8];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) { qf[2 * t] = __uint_as_float(qw[t] << 16); qf[2 * t + 1] = __uint_as_float(qw[t] & 0xffff0000u); }
+          float* ap = acc + r * d + c;
+          if (acc_mode == 1) {
+            reinterpret_cast<float4*>(ap)[0] = make_float4(qf[0], qf[1], qf[2], qf[3]);
+            reinterpret_cast<float4*>(ap)[1] = make_float4(qf[4], qf[5], qf[6], qf[7]);
+          } else {   // acc += dR in L2 (one adder per element)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ap), "f"(qf[0]), "f"(qf[1]), "f"(qf[2]), "f"(qf[3]) : "memory");
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ap + 4), "f"(qf[4]), "f"(qf[5]), "f"(qf[6]), "f"(qf[7]) : "memory");
+          }
+        }
+      }
+    }
+  }
+  // dgamma / dbeta: lanes with equal columns (xor offsets >= LPR), then the 8 warps in order
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      pg[t] += __shfl_xor_sync(0xffffffffu, pg[t], o);
+      pb[t] += __shfl_xor_sync(0xffffffffu, pb[t], o);
+    }
+  if (sub == 0) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) { sred[w][0][c + t] = pg[t]; sred[w][1][c + t] = pb[t]; }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) {
+    const int which = j / d, cc = j - which * d;
+    float s = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) s += sred[ww][which][cc];
+    part[(int64_t)blockIdx.x * 2 * d + j] = s;
+  }
+}
+
+// one resident wave: SMs x blocks per SM at the kernel's register / smem occupancy
+template <typename K>
+static int resident_blocks(K kern, int threads, size_t smem) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem) != cudaSuccess || per < 1) {
+    (void)cudaGetLastError();
+    per = 1;
+  }
+  return sms * per;
+}
+static int ln_bwd_grid(int lpr, int dydt) {
+  static int cache[2][6] = {{0}};
+  const int li = lpr == 4 ? 0 : lpr == 8 ? 1 : lpr == 16 ? 2 : 3, ti = dydt == BF16 ? 0 : 1;
+  int& v = cache[ti][li];
+  if (!v) {
+#define LG(L, I) if (li == I) v = ti == 0 ? resident_blocks(ln_bwd_r<L, 2, __nv_bfloat16>, 256, 0) : resident_blocks(ln_bwd_r<L, 2, float>, 256, 0);
+    LG(4, 0) LG(8, 1) LG(16, 2) LG(32, 3)
+#undef LG
+  }
+  return v;
+}
+static int ln_lpr(int d) { return (d % 8 == 0 && (d / 8) <= 32 && ((d / 8) & (d / 8 - 1)) == 0) ? d / 8 : 0; }
+
 cudaError_t ln_fwd(const float* U, const void* addx, const void* gamma, const void* beta, int pdt, float eps,
                    int64_t rows, int d, void* Y, void* Rsave, float* mu, float* rstd, int dt, cudaStream_t st) {
+  const int lpr = ln_lpr(d);
+  if (dt == BF16 && pdt == BF16 && lpr >= 4) {
+    const int rpi = (32 / lpr) * 2;   // rows per warp iteration (UR = 2)
+    const int nb = nblocks((rows + rpi - 1) / rpi, 8, 148 * 8);
+#define LNR(L)                                                                                                    \
+    if (lpr == L) ln_fwd_r<L, 2><<<nb, 256, 0, st>>>(U, (const __nv_bfloat16*)addx, (const __nv_bfloat16*)gamma, \
+        (const __nv_bfloat16*)beta, eps, rows, (__nv_bfloat16*)Y, (__nv_bfloat16*)Rsave, mu, rstd);
+    LNR(4) LNR(8) LNR(16) LNR(32)
+#undef LNR
+    ++g_launches;
+    return cudaGetLastError();
+  }
   int vec, nch;
   ln_shape(d, vec, nch);
   if (!vec || pdt != dt) return ln_fwd_generic(U, addx, gamma, beta, pdt, eps, rows, d, Y, Rsave, mu, rstd, dt, st);
@@ -472,6 +679,30 @@ cudaError_t ln_fwd(const float* U, const void* addx, const void* gamma, const vo
 cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
                    const void* gamma, int pdt, int64_t rows, int d, void* dR, int dt, float* acc, int acc_mode,
                    float* dgamma, float* dbeta, float* scratch, size_t scratch_bytes, cudaStream_t st) {
+  const int lpr = ln_lpr(d);
+  if (dt == BF16 && pdt == BF16 && lpr >= 4) {
+    const int rpi = (32 / lpr) * 2;
+    int nb = (int)std::min<int64_t>((rows + 8 * rpi - 1) / (8 * rpi), ln_bwd_grid(lpr, dydt));
+    nb = (int)std::min<int64_t>(nb, (int64_t)(scratch_bytes / (sizeof(float) * 2 * d)));
+    if (nb >= 1) {
+      int64_t rpb = (rows + nb - 1) / nb;
+      nb = (int)((rows + rpb - 1) / rpb);
+#define LNB2(L)                                                                                                        \
+      if (lpr == L) {                                                                                                  \
+        if (dydt == BF16)                                                                                              \
+          ln_bwd_r<L, 2, __nv_bfloat16><<<nb, 256, 0, st>>>((const __nv_bfloat16*)dY, (const __nv_bfloat16*)Rsave, mu, \
+              rstd, (const __nv_bfloat16*)gamma, rows, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb);               \
+        else                                                                                                           \
+          ln_bwd_r<L, 2, float><<<nb, 256, 0, st>>>((const float*)dY, (const __nv_bfloat16*)Rsave, mu, rstd,           \
+              (const __nv_bfloat16*)gamma, rows, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb);                     \
+      }
+      LNB2(4) LNB2(8) LNB2(16) LNB2(32)
+#undef LNB2
+      ++g_launches;
+      part_sum(scratch, nb, 2 * d, dgamma, d, dbeta, d, nullptr, 0.f, st);
+      return cudaGetLastError();
+    }
+  }
   int vec, nch;
   ln_shape(d, vec, nch);
   if (!vec || pdt != dt)
@@ -563,9 +794,61 @@ __global__ void __launch_bounds__(256) colsum8_part_k(const T* __restrict__ src,
   }
 }
 
+// cols <= 2048, cols % 8 == 0: one block covers every column: CT = cols / 8 column-threads (8 columns each, 16-B
+// loads) x RT = 256 / CT row-threads; the RT partial rows are added in fixed order through shared memory.
+__global__ void __launch_bounds__(256) colsum_all_k(const __nv_bfloat16* __restrict__ src, int64_t rows, int cols,
+                                                    int64_t ld, int64_t rpc, float* __restrict__ part) {
+  extern __shared__ float csm[];   // [RT][cols]
+  const int CT = cols / 8, RT = 256 / CT;
+  const int ct = threadIdx.x % CT, ry = threadIdx.x / CT, c = ct * 8;
+  const int64_t r0 = blockIdx.x * rpc, r1 = min(rows, r0 + rpc);
+  if (ry < RT) {
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int64_t r = r0 + ry;
+    for (; r + 3 * RT < r1; r += 4 * RT) {   // 4 independent 16-B loads in flight
+      float v0[8], v1[8], v2[8], v3[8];
+      VIO<8, __nv_bfloat16>::ld(src + r * ld + c, v0);
+      VIO<8, __nv_bfloat16>::ld(src + (r + RT) * ld + c, v1);
+      VIO<8, __nv_bfloat16>::ld(src + (r + 2 * RT) * ld + c, v2);
+      VIO<8, __nv_bfloat16>::ld(src + (r + 3 * RT) * ld + c, v3);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] += (v0[t] + v1[t]) + (v2[t] + v3[t]);
+    }
+    for (; r < r1; r += RT) {
+      float v0[8];
+      VIO<8, __nv_bfloat16>::ld(src + r * ld + c, v0);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] += v0[t];
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) csm[ry * cols + c + t] = a[t];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < cols; j += blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < RT; ++k) s += csm[k * cols + j];
+    part[(int64_t)blockIdx.x * cols + j] = s;
+  }
+}
+
 cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t ld, float* out, float* scratch,
                        size_t scratch_bytes, cudaStream_t st) {
   const int es = dt == F32 ? 4 : 2;
+  if (dt == BF16 && cols % 8 == 0 && cols <= 2048 && ld % 8 == 0 && ((uintptr_t)src % 16) == 0) {
+    const int CT = cols / 8, RT = 256 / CT;
+    int64_t nch = std::max<int64_t>(1, std::min<int64_t>(rows / (4 * RT), 4 * 148));
+    nch = std::min<int64_t>(nch, (int64_t)(scratch_bytes / (sizeof(float) * cols)));
+    if (nch >= 1) {
+      int64_t rpc = (rows + nch - 1) / nch;
+      nch = (rows + rpc - 1) / rpc;
+      if (nch < 1) nch = 1;
+      colsum_all_k<<<(unsigned)nch, 256, (size_t)RT * cols * sizeof(float), st>>>((const __nv_bfloat16*)src, rows, cols,
+                                                                                   ld, rpc, scratch);
+      ++g_launches;
+      part_sum(scratch, (int)nch, cols, out, cols, nullptr, 0, nullptr, 0.f, st);
+      return cudaGetLastError();
+    }
+  }
   if (cols % 8 == 0 && ld % 8 == 0 && ((uintptr_t)src % (8 * es)) == 0) {
     const int cb = (cols + 255) / 256;
     int64_t nch = std::max<int64_t>(1, std::min<int64_t>(rows / 64, std::max(1, 4 * 148 / cb)));
