@@ -139,6 +139,12 @@ struct dhen_ctx {
   float* red = nullptr;     // reduction partials
   size_t red_bytes = 0;
   Workspace ws;
+  // weight-gradient side stream (B4/B5/B7/B8/B9 wgrads overlap the same module's dgrads; joined per module)
+  int overlap = 1;                    // env DHEN_OVERLAP
+  cudaStream_t side_st = nullptr;
+  cudaEvent_t ev_sf = nullptr, ev_sx = nullptr, ev_sj = nullptr;
+  Workspace ws2;                      // split-K scratch of the side stream
+  float* red2 = nullptr;              // reduction scratch of the side stream
   float *pooled = nullptr, *z = nullptr, *lossb = nullptr, *dz = nullptr;
   float* gtmp = nullptr;    // fp32 [max_npad]: all-gather target of params_io / grads_get (world > 1)
   ncclComm_t comm = nullptr;
@@ -186,6 +192,12 @@ struct ProfScope {
 #define KT(tag, flops, bytes, call)                          \
   do {                                                       \
     ProfScope ps_(c, tag, (double)(flops), (double)(bytes), st); \
+    CK(call);                                                \
+  } while (0)
+// the same on an explicit stream (the weight-gradient side stream)
+#define KTS(strm, tag, flops, bytes, call)                   \
+  do {                                                       \
+    ProfScope ps_(c, tag, (double)(flops), (double)(bytes), strm); \
     CK(call);                                                \
   } while (0)
 
@@ -388,6 +400,9 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   c->red = (float*)work.take(c->red_bytes);
   c->ws.bytes = (size_t)256 << 20;
   c->ws.ptr = (float*)work.take(c->ws.bytes);
+  c->ws2.bytes = (size_t)256 << 20;
+  c->ws2.ptr = (float*)work.take(c->ws2.bytes);
+  c->red2 = (float*)work.take(c->red_bytes);
   c->pooled = (float*)work.take(((size_t)B * d + (size_t)((B + 31) / 32) * (d + 2)) * 4);   // + head partials
   c->z = (float*)work.take((size_t)B * 4);
   c->lossb = (float*)work.take((size_t)B * 4);
@@ -397,7 +412,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
 
 // ------------------------------------------------------------------ GEMM helpers
 static double vbytes(const View& v, double n) { return v.ptr ? n * (v.dt == F32 ? 4 : 2) : 0; }
-static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const char* tag) {
+static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const char* tag, const Workspace* ws = nullptr) {
   // algorithmic traffic: each operand read once (shared operands once), C written (and read if +=)
   const double es = g.a.dt == F32 ? 4 : 2;
   const double mn = (double)g.M * g.N * g.batch;
@@ -406,7 +421,7 @@ static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const 
                  vbytes(g.c, mn) * (g.e.accumulate || g.e.dcn_bwd ? 2 : 1) + vbytes(g.e.resid, mn) + vbytes(g.e.mask, mn) +
                  vbytes(g.e.cross, mn) + vbytes(g.e.aux, mn);
   ProfScope ps(c, tag, 2.0 * (double)g.M * g.N * g.K * g.batch, bytes, st);
-  CK(gemm_run(g, c->ws, st));
+  CK(gemm_run(g, ws ? *ws : c->ws, st));
   if (ps.rec >= 0) c->recs[ps.rec].tc = g_last_gemm_tc;
   return DHEN_OK;
 }
@@ -436,8 +451,10 @@ static dhen_status tokmix_fwd(dhen_ctx* c, const void* T, int m, const void* W, 
 }
 // B4: dT[b,i,c] = sum_t W[i,t] dU[b,t,c] (rows (b,c), N = m, K = l) stored (dT_dt) or accumulated
 // into fp32; dW[i,t] += sum_(b,c) T[b,i,c] dU[b,t,c] (K = B*d, two-level K).
+// ... dgrad on `st`, wgrad on `sw` with workspace `wsw` (the weight-gradient side stream, or st itself)
 static dhen_status tokmix_bwd(dhen_ctx* c, const void* T, int m, const void* W, int l, const void* dU, int64_t ldu,
-                              void* dT, int dT_dt, int acc, float* gW, int B, cudaStream_t st) {
+                              void* dT, int dT_dt, int acc, float* gW, int B, cudaStream_t st, cudaStream_t sw = nullptr,
+                              const Workspace* wsw = nullptr) {
   const int d = c->d, dt = c->dt;
   // per-sample batched: dT_b = W dU_b (M = m rows i, N = d, K = l), row-major output
   Gemm g = mk(m, d, l, B, operand(W, dt, l, 1), operand(dU, dt, 1, d, ldu), view(dT, dT_dt, d, 1, (int64_t)m * d));
@@ -446,7 +463,7 @@ static dhen_status tokmix_bwd(dhen_ctx* c, const void* T, int m, const void* W, 
   Gemm gw = mk(m, l, B * d, 1, operand(T, dt, d, 1, 0, 0, 1, d, (int64_t)m * d),
                operand(dU, dt, d, 1, 0, 0, 1, d, ldu), view(gW, F32, l, 1));
   gw.e.accumulate = 1;
-  return G_(gw, c, st, "tokmix.wgrad");
+  return G_(gw, c, sw ? sw : st, "tokmix.wgrad", wsw);
 }
 
 // ------------------------------------------------------------------ FSDP gather / scatter
@@ -646,15 +663,31 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
             gp(Lr.gamma), gp(Lr.beta), c->red, c->red_bytes, st));
   if (Lr.Wn >= 0)   // B3: dX = W_n dR ; dW_n += sum_b X_b dR_b^T
     RET(tokmix_bwd(c, X, mi, p(Lr.Wn), mo, c->dR, ldU, acc, F32, 0, gp(Lr.Wn), B, st));
+  // Weight gradients of a module run on the side stream `sd` (own split-K / reduction scratch) while its
+  // data gradients run on `st`; `fork` hands the side stream everything enqueued on st so far, `join`
+  // makes st wait for the side stream at the end of the module (shared scratch is reused by the next one).
+  // (the profiled pass runs serialised so every op's event-timed duration is its own)
+  cudaStream_t sd = (c->overlap && !c->prof) ? c->side_st : st;
+  const Workspace* ws2 = &c->ws2;
+  float* red2 = c->red2;
+  auto fork = [&]() -> dhen_status {
+    if (sd != st) { CK(cudaEventRecord(c->ev_sf, st)); CK(cudaStreamWaitEvent(sd, c->ev_sf, 0)); }
+    return DHEN_OK;
+  };
+  auto join = [&]() -> dhen_status {
+    if (sd != st) { CK(cudaEventRecord(c->ev_sj, sd)); CK(cudaStreamWaitEvent(st, c->ev_sj, 0)); }
+    return DHEN_OK;
+  };
   for (Mod& md : Lr.mods) {
     const int l = md.s.l;
     char* dU = (char*)c->dR + (int64_t)md.off_tok * d * es;
     switch (md.s.kind) {
       case DHEN_DOT: {   // B5
         const int h = mi * (mi - 1) / 2;
+        RET(fork());
         Gemm gw = mk(l * d, h, B, 1, operand(dU, dt, 1, ldU), operand(md.Z, dt, 1, h), view(gp(md.Wm), F32, h, 1));
         gw.e.accumulate = 1;
-        RET(G_(gw, c, st, "dot.proj_wgrad"));
+        RET(G_(gw, c, sd, "dot.proj_wgrad", ws2));
         Gemm gz = mk(B, h, l * d, 1, operand(dU, dt, ldU, 1), operand(p(md.Wm), dt, 1, h), view(c->tA, dt, h, 1));
         RET(G_(gz, c, st, "dot.proj_dgrad"));
         KT("dot.sym", 0, (double)B * (h + mi * mi) * es, sym_from_triu(c->tA, c->tD, dt, B, mi, h, st));
@@ -667,13 +700,23 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
                            view(acc, F32, d, 1, (int64_t)mi * d));
         gx.e.accumulate = 1;
         RET(G_(gx, c, st, "dot.gram_bwd"));
+        RET(join());
         break;
       }
       case DHEN_LINEAR:
-        RET(tokmix_bwd(c, X, mi, p(md.W), l, dU, ldU, acc, F32, 1, gp(md.W), B, st));
+        RET(fork());
+        RET(tokmix_bwd(c, X, mi, p(md.W), l, dU, ldU, acc, F32, 1, gp(md.W), B, st, sd, ws2));
+        RET(join());
         break;
       case DHEN_DCN: {   // B8
         void* dA = c->tB;
+        RET(fork());
+        {   // dW_u += sum T dU (side stream; needs only saved T and dU)
+          Gemm gw_u = mk(mi, l, B * d, 1, operand(md.T, dt, d, 1, 0, 0, 1, d, (int64_t)mi * d),
+                         operand(dU, dt, d, 1, 0, 0, 1, d, ldU), view(gp(md.Wu), F32, l, 1));
+          gw_u.e.accumulate = 1;
+          RET(G_(gw_u, c, sd, "tokmix.wgrad", ws2));
+        }
         // dT = W_u dU (never stored): the epilogue forms dA = dT (.) X and dX += dT (.) A + dT (B8)
         // m <= 64 (dividing 128), l dividing 64: spt = 128 / m samples per 128-row tile, as one GEMM with the
         // block-diagonal token map blockdiag(W_u, .., W_u) [spt m][spt l] against spt stacked dU_b (the B
@@ -704,24 +747,25 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         gt.e.aux = view(dA, dt, vr, vc, (int64_t)mi * d);
         RET(G_(gt, c, st, "dcn.dT_fused"));
         }
-        Gemm gw_u = mk(mi, l, B * d, 1, operand(md.T, dt, d, 1, 0, 0, 1, d, (int64_t)mi * d),
-                       operand(dU, dt, d, 1, 0, 0, 1, d, ldU), view(gp(md.Wu), F32, l, 1));
-        gw_u.e.accumulate = 1;
-        RET(G_(gw_u, c, st, "tokmix.wgrad"));
+        if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dA ready
         Gemm gx = mk((int)rows, d, d, 1, operand(dA, dt, d, 1), operand(p(md.W), dt, 1, d), view(acc, F32, d, 1));
         gx.e.accumulate = 1;
         RET(G_(gx, c, st, "dcn.dgrad"));
         Gemm gw = mk(d, d, (int)rows, 1, operand(dA, dt, 1, d), operand(X, dt, 1, d), view(gp(md.W), F32, d, 1));
         gw.e.accumulate = 1;
-        RET(G_(gw, c, st, "dcn.wgrad"));
-        KT("dcn.bias_grad", 0, (double)rows * d * es, colsum_add(dA, dt, rows, d, d, gp(md.b), c->red, c->red_bytes, st));
+        RET(G_(gw, c, sd, "dcn.wgrad", ws2));
+        KTS(sd, "dcn.bias_grad", 0, (double)rows * d * es, colsum_add(dA, dt, rows, d, d, gp(md.b), red2, c->red_bytes, sd));
+        RET(join());
         break;
       }
       case DHEN_CONV: {  // B7
         void* dT = c->tA;
-        RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st));
+        RET(fork());
+        RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st, sd, ws2));
+        if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dT ready
         KT("conv.dgrad", 2.0 * rows * d * md.s.conv_k * md.s.conv_k, (double)rows * d * (es + 8), conv_dgrad(dT, p(md.K), dt, md.s.conv_channels, md.s.conv_k, B, mi, d, acc, dt, st));
-        KT("conv.wgrad", 2.0 * rows * d * md.s.conv_k * md.s.conv_k, 2.0 * rows * d * es, conv_wgrad(dT, X, md.s.conv_channels, md.s.conv_k, B, mi, d, dt, gp(md.K), c->red, c->red_bytes, st));
+        KTS(sd, "conv.wgrad", 2.0 * rows * d * md.s.conv_k * md.s.conv_k, 2.0 * rows * d * es, conv_wgrad(dT, X, md.s.conv_channels, md.s.conv_k, B, mi, d, dt, gp(md.K), red2, c->red_bytes, sd));
+        RET(join());
         break;
       }
       case DHEN_ATTN: {  // B6
@@ -798,28 +842,32 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
       case DHEN_MLP: {   // B9
         const int h1 = md.s.mlp_hidden[0], h2 = md.s.mlp_hidden[1];
         const int K1 = mi * d;
+        RET(fork());
         Gemm wm = mk(l * d, h2, B, 1, operand(dU, dt, 1, ldU), operand(md.h2, dt, 1, h2), view(gp(md.Wm), F32, h2, 1));
         wm.e.accumulate = 1;
-        RET(G_(wm, c, st, "mlp.proj_wgrad"));
+        RET(G_(wm, c, sd, "mlp.proj_wgrad", ws2));
         void* dh2 = c->tA;
         Gemm a = mk(B, h2, l * d, 1, operand(dU, dt, ldU, 1), operand(p(md.Wm), dt, 1, h2), view(dh2, dt, h2, 1));
         a.e.mask = view(md.h2, dt, h2, 1);
         RET(G_(a, c, st, "mlp.proj_dgrad"));
+        if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dh2 ready
         Gemm w2 = mk(h2, h1, B, 1, operand(dh2, dt, 1, h2), operand(md.h1, dt, 1, h1), view(gp(md.W2), F32, h1, 1));
         w2.e.accumulate = 1;
-        RET(G_(w2, c, st, "mlp.fc2_wgrad"));
-        KT("mlp.bias_grad", 0, (double)B * h2 * es, colsum_add(dh2, dt, B, h2, h2, gp(md.b2), c->red, c->red_bytes, st));
+        RET(G_(w2, c, sd, "mlp.fc2_wgrad", ws2));
+        KTS(sd, "mlp.bias_grad", 0, (double)B * h2 * es, colsum_add(dh2, dt, B, h2, h2, gp(md.b2), red2, c->red_bytes, sd));
         void* dh1 = c->tC;
         Gemm b1 = mk(B, h1, h2, 1, operand(dh2, dt, h2, 1), operand(p(md.W2), dt, 1, h1), view(dh1, dt, h1, 1));
         b1.e.mask = view(md.h1, dt, h1, 1);
         RET(G_(b1, c, st, "mlp.fc2_dgrad"));
+        if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dh1 ready
         Gemm w1 = mk(h1, K1, B, 1, operand(dh1, dt, 1, h1), operand(X, dt, 1, K1), view(gp(md.W1), F32, K1, 1));
         w1.e.accumulate = 1;
-        RET(G_(w1, c, st, "mlp.fc1_wgrad"));
-        KT("mlp.bias_grad", 0, (double)B * h1 * es, colsum_add(dh1, dt, B, h1, h1, gp(md.b1), c->red, c->red_bytes, st));
+        RET(G_(w1, c, sd, "mlp.fc1_wgrad", ws2));
+        KTS(sd, "mlp.bias_grad", 0, (double)B * h1 * es, colsum_add(dh1, dt, B, h1, h1, gp(md.b1), red2, c->red_bytes, sd));
         Gemm gx = mk(B, K1, h1, 1, operand(dh1, dt, h1, 1), operand(p(md.W1), dt, 1, K1), view(acc, F32, K1, 1));
         gx.e.accumulate = 1;
         RET(G_(gx, c, st, "mlp.fc1_dgrad"));
+        RET(join());
         break;
       }
     }
@@ -930,6 +978,15 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
     if (state_bytes < sz.off + 256 || work_bytes < wz.off + 256) { delete c; return fail(DHEN_E_NOMEM, "dhen_init: buffers too small after alignment"); }
   }
   plan(c, s, w);
+  {
+    const char* ev = getenv("DHEN_OVERLAP");
+    c->overlap = ev ? atoi(ev) : 1;
+    bool ok = cudaStreamCreateWithFlags(&c->side_st, cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_sf, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_sx, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_sj, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) { dhen_destroy(c); return fail(DHEN_E_CUDA, "dhen_init: side stream creation failed"); }
+  }
   if (c->dist.world > 1) {
     ncclUniqueId id;
     memcpy(id.internal, c->dist.nccl_id, 128);
@@ -987,6 +1044,10 @@ void dhen_destroy(dhen_ctx* c) {
   if (c->cap_st) cudaStreamDestroy(c->cap_st);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_sf) cudaEventDestroy(c->ev_sf);
+  if (c->ev_sx) cudaEventDestroy(c->ev_sx);
+  if (c->ev_sj) cudaEventDestroy(c->ev_sj);
+  if (c->side_st) cudaStreamDestroy(c->side_st);
   if (c->ev_grad) cudaEventDestroy(c->ev_grad);
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
   if (c->comm_st) cudaStreamDestroy(c->comm_st);
