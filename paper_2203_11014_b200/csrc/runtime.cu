@@ -421,7 +421,7 @@ static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const 
                  vbytes(g.c, mn) * (g.e.accumulate || g.e.dcn_bwd ? 2 : 1) + vbytes(g.e.resid, mn) + vbytes(g.e.mask, mn) +
                  vbytes(g.e.cross, mn) + vbytes(g.e.aux, mn);
   ProfScope ps(c, tag, 2.0 * (double)g.M * g.N * g.K * g.batch, bytes, st);
-  CK(gemm_run(g, ws ? *ws : c->ws, st));
+  CK(gemm_run(g, ws ? *ws : (st == c->side_st ? c->ws2 : c->ws), st));   // each stream its own split-K scratch
   if (ps.rec >= 0) c->recs[ps.rec].tc = g_last_gemm_tc;
   return DHEN_OK;
 }
@@ -542,9 +542,22 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
   float* U = c->Ucat;
   const int64_t ldU = (int64_t)mo * d;
   const int64_t rows = (int64_t)B * mi;
+  // Module branches are independent until the concat (each writes its own token rows of Ucat): with a
+  // self-attention module in the layer it runs on the layer stream and every other module on the side
+  // stream; otherwise modules alternate.  Attention modules always stay on the layer stream (rtmp/big
+  // scratch).  The profiled pass runs serialised.
+  const cudaStream_t st0 = st;
+  const bool use_side = c->overlap && !c->prof && Lr.mods.size() > 1;
+  bool has_attn = false;
+  for (const Mod& m_ : Lr.mods) has_attn |= m_.s.kind == DHEN_ATTN;
+  if (use_side) { CK(cudaEventRecord(c->ev_sf, st0)); CK(cudaStreamWaitEvent(c->side_st, c->ev_sf, 0)); }
+  int mod_idx = 0;
   for (Mod& md : Lr.mods) {
     const int l = md.s.l;
     float* Us = U + (int64_t)md.off_tok * d;
+    const bool on_side = use_side && md.s.kind != DHEN_ATTN && (has_attn || (mod_idx & 1));
+    ++mod_idx;
+    cudaStream_t st = on_side ? c->side_st : st0;   // this module's stream (shadows the layer stream)
     switch (md.s.kind) {
       case DHEN_DOT: {   // F1 + F2
         const int h = mi * (mi - 1) / 2;
@@ -633,6 +646,7 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
       }
     }
   }
+  if (use_side) { CK(cudaEventRecord(c->ev_sj, c->side_st)); CK(cudaStreamWaitEvent(st0, c->ev_sj, 0)); }
   // F11 shortcut (Eq.(2)) + F12 LayerNorm
   if (Lr.Wn >= 0) RET(tokmix_fwd(c, X, mi, p(Lr.Wn), mo, U, ldU, B, 1, st));
   KT("layer.ln", 0, (double)B * mo * d * (4 + 2 * es) + (Lr.Wn >= 0 ? 0.0 : (double)B * mo * d * es), ln_fwd(U, Lr.Wn >= 0 ? nullptr : X, p(Lr.gamma), p(Lr.beta), dt, c->cfg.ln_eps, (int64_t)B * mo, d, Y, Lr.R, Lr.mu,
