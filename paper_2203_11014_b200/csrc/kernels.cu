@@ -1221,6 +1221,165 @@ static cudaError_t conv_band_launch(const void* in, const void* Kp, int C, int B
 }
 static bool conv_band_ok(int k, int d, int B) { return (k == 3 || k == 5) && d % 8 == 0 && d <= 1024 && B >= 1; }
 
+// ------------------------------------------------------------------ conv, double-buffered whole-sample stencils
+// (bf16, 3x3).  One persistent block per SM; sample b's m x d image arrives with one cp.async.bulk copy into
+// rows 1..m of a zero-bordered smem image (rows 0 and m+1 stay zero) while the block computes the previous
+// sample from the other buffer.  Thread t owns column j = t % d for the rows of its row group; the window
+// slides down the rows in registers (three smem loads per output).  MODE 0: T = K * X (bf16).  MODE 1: dX +=
+// K^flip * dT by fp32 reductions in L2 (one adder per element).  MODE 2: dK partials sum dT[i][j] X[i+a][j+e]
+// (dT read from global, 8 rows in flight).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init1(uint32_t a, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait1(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+template <int MODE>
+__global__ void __launch_bounds__(512, 1) conv_db_k(const __nv_bfloat16* __restrict__ img, const __nv_bfloat16* __restrict__ other,
+                                                    const __nv_bfloat16* __restrict__ Kp, int C, int B, int m, int d,
+                                                    __nv_bfloat16* __restrict__ outT, float* __restrict__ outAcc,
+                                                    float* __restrict__ part) {
+  extern __shared__ __align__(128) unsigned char cdb_smem[];
+  __shared__ __align__(8) uint64_t full[2];
+  __shared__ float kb[9];
+  __shared__ float red[9][16];
+  const int S = (m + 2) * d;   // elements per buffer
+  __nv_bfloat16* buf0 = reinterpret_cast<__nv_bfloat16*>(cdb_smem);
+  if (MODE != 2 && threadIdx.x < 9) {
+    float s = 0.f;
+    for (int c = 0; c < C; ++c) s += __bfloat162float(Kp[c * 9 + threadIdx.x]);
+    kb[threadIdx.x] = s / C;
+  }
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {   // zero border rows of both buffers
+    buf0[e] = buf0[(m + 1) * d + e] = __float2bfloat16_rn(0.f);
+    buf0[S + e] = buf0[S + (m + 1) * d + e] = __float2bfloat16_rn(0.f);
+  }
+  const uint32_t f0 = (uint32_t)__cvta_generic_to_shared(&full[0]), f1 = (uint32_t)__cvta_generic_to_shared(&full[1]);
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(buf0);
+  const uint32_t bytes = (uint32_t)m * d * 2;
+  if (threadIdx.x == 0) {
+    mbar_init1(f0, 1);
+    mbar_init1(f1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if ((int)blockIdx.x < B) {
+      mbar_expect(f0, bytes);
+      bulk_g2s(sb + d * 2, img + (int64_t)blockIdx.x * m * d, bytes, f0);
+    }
+  }
+  __syncthreads();
+  const int j = threadIdx.x % d, groups = (int)blockDim.x / d, rg = threadIdx.x / d;
+  const int rpg = (m + groups - 1) / groups, i0 = rg * rpg, i1 = min(m, i0 + rpg);
+  float wacc[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) wacc[q] = 0.f;
+  float kf[9];
+  if (MODE == 0) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) kf[q] = kb[q];
+  } else if (MODE == 1) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) kf[q] = kb[8 - q];   // flipped
+  }
+  int it = 0;
+  for (int b = blockIdx.x; b < B; b += gridDim.x, ++it) {
+    const int s = it & 1;
+    if (threadIdx.x == 0 && b + (int)gridDim.x < B) {   // prefetch the next sample into the other buffer
+      const uint32_t fn = s ? f0 : f1;
+      mbar_expect(fn, bytes);
+      bulk_g2s(sb + (uint32_t)((s ^ 1) * S + d) * 2, img + (int64_t)(b + gridDim.x) * m * d, bytes, fn);
+    }
+    mbar_wait1(s ? f1 : f0, (it >> 1) & 1);
+    if (rg < groups && i0 < i1) {
+      const __nv_bfloat16* Sb = buf0 + s * S;
+      auto at = [&](int r, int c) -> float { return (c >= 0 && c < d) ? __bfloat162float(Sb[r * d + c]) : 0.f; };
+      // window rows (padded coordinates): rows i0, i0 + 1 of the buffer = input rows i0 - 1, i0
+      float w[3][3];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int e = 0; e < 3; ++e) w[a + 1][e] = at(i0 + a, j + e - 1);
+      const int64_t base = (int64_t)b * m * d + j;
+      for (int i = i0; i < i1; i += 8) {
+        float g8[8];
+        if (MODE == 2) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) g8[u] = (i + u < i1) ? __bfloat162float(other[base + (int64_t)(i + u) * d]) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int ii = i + u;
+          if (ii >= i1) break;
+#pragma unroll
+          for (int e = 0; e < 3; ++e) { w[0][e] = w[1][e]; w[1][e] = w[2][e]; w[2][e] = at(ii + 2, j + e - 1); }
+          if (MODE == 2) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int e = 0; e < 3; ++e) wacc[a * 3 + e] += g8[u] * w[a][e];
+          } else {
+            float o = 0.f;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int e = 0; e < 3; ++e) o += kf[a * 3 + e] * w[a][e];
+            const int64_t off = base + (int64_t)ii * d;
+            if (MODE == 0) outT[off] = __float2bfloat16_rn(o);
+            else asm volatile("red.global.add.f32 [%0], %1;" ::"l"(outAcc + off), "f"(o) : "memory");
+          }
+        }
+      }
+    }
+    __syncthreads();   // every thread is done with buffer s before it is refilled (two samples ahead)
+  }
+  if (MODE == 2) {
+    const int lane = threadIdx.x & 31, wi = threadIdx.x / 32;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const float v = warp_sum(wacc[q]);
+      if (lane == 0) red[q][wi] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 9) {
+      float v = 0.f;
+      for (int ww = 0; ww < (int)(blockDim.x / 32); ++ww) v += red[threadIdx.x][ww];
+      part[(int64_t)blockIdx.x * 9 + threadIdx.x] = v;
+    }
+  }
+}
+static bool conv_db_ok(int k, int m, int d, int dt, int pdt) {
+  return k == 3 && dt == BF16 && pdt == BF16 && d % 8 == 0 && d <= 512 && 512 % d == 0 && (int64_t)m * d * 2 < (1 << 20) &&
+         (size_t)2 * (m + 2) * d * 2 <= 200 * 1024;
+}
+template <int MODE>
+static cudaError_t conv_db_launch(const void* img, const void* other, const void* Kp, int C, int B, int m, int d,
+                                  void* outT, float* outAcc, float* part, int* grid_out, cudaStream_t st) {
+  const size_t sm = (size_t)2 * (m + 2) * d * 2;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv_db_k<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  static int sms = 0;
+  if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
+  const int grid = std::min(B, sms);
+  if (grid_out) *grid_out = grid;
+  conv_db_k<MODE><<<grid, 512, sm, st>>>((const __nv_bfloat16*)img, (const __nv_bfloat16*)other,
+                                         (const __nv_bfloat16*)Kp, C, B, m, d, (__nv_bfloat16*)outT, outAcc, part);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ conv (folded channel mean)
 constexpr int CONV_MAXK = 7;
 __device__ void load_kbar(const void* K, int pdt, int C, int k, float* kb) {
@@ -1255,6 +1414,7 @@ __global__ void conv_fwd_k(const void* X, const void* K, int pdt, int C, int k, 
 cudaError_t conv_fwd(const void* X, const void* K, int pdt, int C, int k, int B, int m, int d, void* T, int dt,
                      cudaStream_t st) {
   if (k > CONV_MAXK) return cudaErrorInvalidValue;
+  if (conv_db_ok(k, m, d, dt, pdt)) return conv_db_launch<0>(X, nullptr, K, C, B, m, d, T, nullptr, nullptr, nullptr, st);
   if (conv_sample_ok(k, m, d, dt == BF16 ? 2 : 4) && pdt == dt) {
     const int grid = std::min(B, 148 * 2);
     if (dt == BF16) return conv_sample_launch<__nv_bfloat16, 3, 0>(X, nullptr, K, C, B, m, d, T, nullptr, nullptr, grid, st);
@@ -1295,6 +1455,7 @@ __global__ void conv_dgrad_k(const void* dT, const void* K, int pdt, int C, int 
 cudaError_t conv_dgrad(const void* dT, const void* K, int pdt, int C, int k, int B, int m, int d, float* acc, int dt,
                        cudaStream_t st) {
   if (k > CONV_MAXK) return cudaErrorInvalidValue;
+  if (conv_db_ok(k, m, d, dt, pdt)) return conv_db_launch<1>(dT, nullptr, K, C, B, m, d, nullptr, acc, nullptr, nullptr, st);
   if (conv_sample_ok(k, m, d, dt == BF16 ? 2 : 4) && pdt == dt) {
     const int grid = std::min(B, 148 * 2);
     if (dt == BF16) return conv_sample_launch<__nv_bfloat16, 3, 1>(dT, nullptr, K, C, B, m, d, nullptr, acc, nullptr, grid, st);
@@ -1355,6 +1516,14 @@ __global__ void conv_wgrad_fin_k(const float* part, int nparts, int C, int kk, f
 cudaError_t conv_wgrad(const void* dT, const void* X, int C, int k, int B, int m, int d, int dt, float* dK,
                        float* scratch, size_t scratch_bytes, cudaStream_t st) {
   if (k > CONV_MAXK) return cudaErrorInvalidValue;
+  if (conv_db_ok(k, m, d, dt, dt) && (size_t)std::min(B, 148) * 9 * sizeof(float) <= scratch_bytes) {
+    int grid = 0;
+    cudaError_t e = conv_db_launch<2>(X, dT, nullptr, C, B, m, d, nullptr, nullptr, scratch, &grid, st);
+    if (e != cudaSuccess) return e;
+    conv_wgrad_fin_k<<<1, 64, 0, st>>>(scratch, grid, C, k * k, dK);
+    ++g_launches;
+    return cudaGetLastError();
+  }
   if (conv_sample_ok(k, m, d, dt == BF16 ? 2 : 4)) {
     const int grid = std::min(B, 148 * 2);
     if ((size_t)grid * k * k * sizeof(float) <= scratch_bytes) {
