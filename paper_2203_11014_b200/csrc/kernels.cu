@@ -1250,92 +1250,107 @@ __global__ void __launch_bounds__(512, 1) conv_db_k(const __nv_bfloat16* __restr
                                                     const __nv_bfloat16* __restrict__ Kp, int C, int B, int m, int d,
                                                     __nv_bfloat16* __restrict__ outT, float* __restrict__ outAcc,
                                                     float* __restrict__ part) {
+  // smem image: rows 0..m+1 (0 and m+1 zero), dense rows (pitch d): the sample lands with ONE bulk copy;
+  // the two edge column-quads read their out-of-image neighbour as 0.
   extern __shared__ __align__(128) unsigned char cdb_smem[];
   __shared__ __align__(8) uint64_t full[2];
   __shared__ float kb[9];
   __shared__ float red[9][16];
-  const int S = (m + 2) * d;   // elements per buffer
+  const int P = d;
+  const int S = (m + 2) * P;   // elements per buffer
   __nv_bfloat16* buf0 = reinterpret_cast<__nv_bfloat16*>(cdb_smem);
   if (MODE != 2 && threadIdx.x < 9) {
     float s = 0.f;
     for (int c = 0; c < C; ++c) s += __bfloat162float(Kp[c * 9 + threadIdx.x]);
     kb[threadIdx.x] = s / C;
   }
-  for (int e = threadIdx.x; e < d; e += blockDim.x) {   // zero border rows of both buffers
-    buf0[e] = buf0[(m + 1) * d + e] = __float2bfloat16_rn(0.f);
-    buf0[S + e] = buf0[S + (m + 1) * d + e] = __float2bfloat16_rn(0.f);
-  }
+  for (int e = threadIdx.x; e < 2 * S; e += blockDim.x) buf0[e] = __float2bfloat16_rn(0.f);   // borders stay 0
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the zero fill before the async (bulk) writes
+  __syncthreads();
   const uint32_t f0 = (uint32_t)__cvta_generic_to_shared(&full[0]), f1 = (uint32_t)__cvta_generic_to_shared(&full[1]);
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(buf0);
   const uint32_t bytes = (uint32_t)m * d * 2;
+  // one thread issues the sample's single bulk copy into rows 1..m
+  auto issue = [&](int b, int s, uint32_t fb) {
+    mbar_expect(fb, bytes);
+    bulk_g2s(sb + (uint32_t)(s * S + P) * 2, img + (int64_t)b * m * d, bytes, fb);
+  };
   if (threadIdx.x == 0) {
     mbar_init1(f0, 1);
     mbar_init1(f1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if ((int)blockIdx.x < B) {
-      mbar_expect(f0, bytes);
-      bulk_g2s(sb + d * 2, img + (int64_t)blockIdx.x * m * d, bytes, f0);
-    }
   }
   __syncthreads();
-  const int j = threadIdx.x % d, groups = (int)blockDim.x / d, rg = threadIdx.x / d;
+  if (threadIdx.x == 0 && (int)blockIdx.x < B) issue(blockIdx.x, 0, f0);
+  const int TPR = d / 4, groups = (int)blockDim.x / TPR, rg = threadIdx.x / TPR;
+  const int c0 = (threadIdx.x % TPR) * 4;   // this thread's 4 output columns
   const int rpg = (m + groups - 1) / groups, i0 = rg * rpg, i1 = min(m, i0 + rpg);
   float wacc[9];
 #pragma unroll
   for (int q = 0; q < 9; ++q) wacc[q] = 0.f;
   float kf[9];
-  if (MODE == 0) {
 #pragma unroll
-    for (int q = 0; q < 9; ++q) kf[q] = kb[q];
-  } else if (MODE == 1) {
-#pragma unroll
-    for (int q = 0; q < 9; ++q) kf[q] = kb[8 - q];   // flipped
-  }
+  for (int q = 0; q < 9; ++q) kf[q] = MODE == 0 ? kb[q] : MODE == 1 ? kb[8 - q] : 0.f;   // dgrad: flipped
   int it = 0;
   for (int b = blockIdx.x; b < B; b += gridDim.x, ++it) {
     const int s = it & 1;
-    if (threadIdx.x == 0 && b + (int)gridDim.x < B) {   // prefetch the next sample into the other buffer
-      const uint32_t fn = s ? f0 : f1;
-      mbar_expect(fn, bytes);
-      bulk_g2s(sb + (uint32_t)((s ^ 1) * S + d) * 2, img + (int64_t)(b + gridDim.x) * m * d, bytes, fn);
-    }
+    if (threadIdx.x == 0 && b + (int)gridDim.x < B) issue(b + gridDim.x, s ^ 1, s ? f0 : f1);   // next sample
     mbar_wait1(s ? f1 : f0, (it >> 1) & 1);
     if (rg < groups && i0 < i1) {
-      const __nv_bfloat16* Sb = buf0 + s * S;
-      auto at = [&](int r, int c) -> float { return (c >= 0 && c < d) ? __bfloat162float(Sb[r * d + c]) : 0.f; };
-      // window rows (padded coordinates): rows i0, i0 + 1 of the buffer = input rows i0 - 1, i0
-      float w[3][3];
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int e = 0; e < 3; ++e) w[a + 1][e] = at(i0 + a, j + e - 1);
-      const int64_t base = (int64_t)b * m * d + j;
+      const __nv_bfloat16* Sb = buf0 + s * S + c0;   // column c0 of padded row 0
+      const bool lft = c0 > 0, rgt = c0 + 4 < d;
+      // window: 3 rows x 6 columns (c0 - 1 .. c0 + 4) from three 8-B loads per row
+      auto load_row = [&](int r, float* o6) {
+        const uint2 a = lft ? *reinterpret_cast<const uint2*>(Sb + r * P - 4) : make_uint2(0u, 0u);
+        const uint2 bq = *reinterpret_cast<const uint2*>(Sb + r * P);
+        const uint2 c = rgt ? *reinterpret_cast<const uint2*>(Sb + r * P + 4) : make_uint2(0u, 0u);
+        o6[0] = __uint_as_float(a.y & 0xffff0000u);   // column c0 - 1
+        o6[1] = __uint_as_float(bq.x << 16); o6[2] = __uint_as_float(bq.x & 0xffff0000u);
+        o6[3] = __uint_as_float(bq.y << 16); o6[4] = __uint_as_float(bq.y & 0xffff0000u);
+        o6[5] = __uint_as_float(c.x << 16);            // column c0 + 4
+      };
+      float w[3][6];
+      load_row(i0, w[1]);
+      load_row(i0 + 1, w[2]);
+      const int64_t base = (int64_t)b * m * d + c0;
       for (int i = i0; i < i1; i += 8) {
-        float g8[8];
+        uint2 g8[8];
         if (MODE == 2) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) g8[u] = (i + u < i1) ? __bfloat162float(other[base + (int64_t)(i + u) * d]) : 0.f;
+          for (int u = 0; u < 8; ++u)
+            g8[u] = (i + u < i1) ? __ldcs(reinterpret_cast<const uint2*>(other + base + (int64_t)(i + u) * d)) : make_uint2(0u, 0u);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int ii = i + u;
           if (ii >= i1) break;
 #pragma unroll
-          for (int e = 0; e < 3; ++e) { w[0][e] = w[1][e]; w[1][e] = w[2][e]; w[2][e] = at(ii + 2, j + e - 1); }
+          for (int e = 0; e < 6; ++e) { w[0][e] = w[1][e]; w[1][e] = w[2][e]; }
+          load_row(ii + 2, w[2]);
           if (MODE == 2) {
+            const float g[4] = {__uint_as_float(g8[u].x << 16), __uint_as_float(g8[u].x & 0xffff0000u),
+                                __uint_as_float(g8[u].y << 16), __uint_as_float(g8[u].y & 0xffff0000u)};
 #pragma unroll
             for (int a = 0; a < 3; ++a)
 #pragma unroll
-              for (int e = 0; e < 3; ++e) wacc[a * 3 + e] += g8[u] * w[a][e];
+              for (int e = 0; e < 3; ++e)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) wacc[a * 3 + e] += g[t] * w[a][t + e];
           } else {
-            float o = 0.f;
+            float o[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int a = 0; a < 3; ++a)
 #pragma unroll
-              for (int e = 0; e < 3; ++e) o += kf[a * 3 + e] * w[a][e];
+              for (int e = 0; e < 3; ++e)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) o[t] += kf[a * 3 + e] * w[a][t + e];
             const int64_t off = base + (int64_t)ii * d;
-            if (MODE == 0) outT[off] = __float2bfloat16_rn(o);
-            else asm volatile("red.global.add.f32 [%0], %1;" ::"l"(outAcc + off), "f"(o) : "memory");
+            if (MODE == 0) {
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
+              *reinterpret_cast<uint2*>(outT + off) = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+            } else {
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(outAcc + off), "f"(o[0]), "f"(o[1]), "f"(o[2]), "f"(o[3]) : "memory");
+            }
           }
         }
       }
@@ -1358,7 +1373,7 @@ __global__ void __launch_bounds__(512, 1) conv_db_k(const __nv_bfloat16* __restr
   }
 }
 static bool conv_db_ok(int k, int m, int d, int dt, int pdt) {
-  return k == 3 && dt == BF16 && pdt == BF16 && d % 8 == 0 && d <= 512 && 512 % d == 0 && (int64_t)m * d * 2 < (1 << 20) &&
+  return k == 3 && dt == BF16 && pdt == BF16 && d % 8 == 0 && d <= 2048 && 2048 % d == 0 && (int64_t)m * d * 2 < (1 << 20) &&
          (size_t)2 * (m + 2) * d * 2 <= 200 * 1024;
 }
 template <int MODE>
