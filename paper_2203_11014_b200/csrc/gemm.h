@@ -72,6 +72,13 @@ struct Epilogue {
   // spt * triu_ld): only the diagonal triu_m x triu_m blocks are stored, sample s at C + s * triu_ld
   int triu_spt = 1;
   int64_t triu_ld = 0;
+  // LayerNorm over the output row (F5 / F6 / F12 fused, N = the whole row): v = alpha acc + bias + resid;
+  // aux <- v (bf16, the saved pre-norm sum); C = gamma (v - mu) rstd + beta; mu / rstd (fp32 per row) saved
+  const void* ln_gamma = nullptr;
+  const void* ln_beta = nullptr;
+  float* ln_mu = nullptr;
+  float* ln_rstd = nullptr;
+  float ln_eps = 1e-5f;
 };
 
 struct Gemm {

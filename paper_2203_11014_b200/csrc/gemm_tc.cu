@@ -127,6 +127,13 @@ static bool make_lean(const Gemm& g, Lean* e) {
   e->flags = (x.accumulate ? EF_ACC : 0) | (x.relu ? EF_RELU : 0) | (x.mask.ptr ? EF_MASK : 0) |
              (x.cross.ptr ? EF_CROSS : 0) | (x.aux.ptr ? EF_AUX : 0) | (x.resid.ptr ? EF_RESID : 0) |
              (x.bias ? EF_BIAS : 0);
+  e->ln_gamma = x.ln_gamma; e->ln_beta = x.ln_beta; e->ln_mu = x.ln_mu; e->ln_rstd = x.ln_rstd; e->ln_eps = x.ln_eps;
+  if (x.ln_gamma) {   // LayerNorm epilogue: whole rows in one tile, bf16 output, bias + residual, pre-norm sum to aux
+    if (g.c.dt != BF16 || g.c.cs != 1 || !x.bias || !x.resid.ptr || !x.aux.ptr || !x.ln_beta || !x.ln_mu || !x.ln_rstd ||
+        x.accumulate || x.relu || x.mask.ptr || x.cross.ptr || x.triu_m || x.dcn_bwd)
+      return false;
+    e->flags |= EF_LN;
+  }
   e->triu_m = x.triu_m;
   e->triu_spt = x.triu_spt;
   e->triu_ld = x.triu_ld;
@@ -161,6 +168,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   if (g.a.dt != BF16 || g.b.dt != BF16 || g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return cudaErrorNotSupported;
   if (g.N < 16) return cudaErrorNotSupported;
   const int BN = g.N <= 64 ? 64 : g.N <= 128 ? 128 : 256;
+  if (g.e.ln_gamma && (g.N != BN || BN < 128)) return cudaErrorNotSupported;   // LN needs whole rows per tile
   Params p;
   p.g = g;
   p.tiles_m = (g.M + BM - 1) / BM;
@@ -168,7 +176,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   p.kblocks = (g.K + BK - 1) / BK;
   const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n * g.batch;
   int splits = 1;
-  if (tiles * 2 <= 148 && p.kblocks >= 8) {   // output fills < half the SMs, long K: split K across CTAs
+  if (tiles * 2 <= 148 && p.kblocks >= 8 && !g.e.ln_gamma) {   // output fills < half the SMs, long K: split K
     splits = (int)std::min<int64_t>((148 + tiles - 1) / tiles, p.kblocks / 4);   // one item per SM
     while (splits > 1 && (int64_t)splits * g.batch * g.M * g.N * 4 > (int64_t)ws.bytes) --splits;
   }
@@ -181,7 +189,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
     if (env_mode == -2) { const char* ev = getenv("DHEN_PAIR"); env_mode = ev ? atoi(ev) : -1; }
     const int mode = g_gemm_pair >= 0 ? g_gemm_pair : env_mode;
     const int64_t pitems = (int64_t)((g.M + 2 * BM - 1) / (2 * BM)) * p.tiles_n * g.batch;
-    p.pair = (BN >= 128 && splits == 1 && mode != 0 && (mode == 1 ? g.M > BM : (pitems >= 74 && g.K >= 4096))) ? 1 : 0;
+    p.pair = (BN >= 128 && splits == 1 && mode != 0 && !g.e.ln_gamma && (mode == 1 ? g.M > BM : (pitems >= 74 && g.K >= 4096))) ? 1 : 0;
   }
   CUtensorMap ma, mb;
   if (!make_map(&ma, &p.a, g.a, g.M, g.K, g.batch, BM)) return cudaErrorNotSupported;
@@ -248,6 +256,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((p.pair ? 2 * BM : BM) >> 4) << 24);
   const int var = (p.lean_id > 0 && (p.fast8 || p.lanes_rows)) ? p.lean_id : 0;
   if (p.tstore && var != p.lean_id) p.tstore = 0;
+  if (g.e.ln_gamma && (!p.lean || var != p.lean_id || (p.ep.flags & EF_LN) == 0 || p.lanes_rows)) return cudaErrorNotSupported;
   cudaError_t e = BN == 64 ? launch_bn64(p, ma, mb, mc, st, var) : BN == 128 ? launch_bn128(p, ma, mb, mc, st, var)
                                                                : launch_bn256(p, ma, mb, mc, st, var);
   if (e != cudaSuccess) return e;

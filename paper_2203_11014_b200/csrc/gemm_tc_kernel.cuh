@@ -41,7 +41,7 @@ struct OpMap {
 // Compact, host-resolved epilogue plan: every present view shares one row geometry
 // (offset = row term + batch term + col * cs), operands other than C are bf16.
 enum { EF_ACC = 1, EF_RELU = 2, EF_MASK = 4, EF_CROSS = 8, EF_AUX = 16, EF_RESID = 32, EF_BIAS = 64,
-       EF_DCNB = 128, EF_TRIU = 256 };
+       EF_DCNB = 128, EF_TRIU = 256, EF_LN = 512 };
 struct Lean {
   void* c;
   const void* x;
@@ -55,6 +55,11 @@ struct Lean {
   int triu_m, triu_spt;
   int64_t triu_ld;
   float alpha;
+  const void* ln_gamma;
+  const void* ln_beta;
+  float* ln_mu;
+  float* ln_rstd;
+  float ln_eps;
 };
 
 struct Params {
@@ -174,6 +179,16 @@ __device__ __forceinline__ void mma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
 }
 
+__device__ __forceinline__ void tmem_st32f(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
 // ---- TMA-store epilogue helpers
 __device__ __forceinline__ void tma_store3(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(c0),
@@ -656,7 +671,8 @@ __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0,
   X(15, EF_RELU, false)                           \
   X(16, EF_RESID, false)                          \
   X(17, EF_MASK, true)                            \
-  X(18, EF_BIAS | EF_CROSS, false)
+  X(18, EF_BIAS | EF_CROSS, false)                \
+  X(19, EF_BIAS | EF_RESID | EF_AUX | EF_LN, false)
 static inline int lean_variant(int flags, bool cf32) {
 #define LV_ID(id, f, c) if (flags == (f) && cf32 == (c)) return id;
   LEAN_VARIANTS(LV_ID)
@@ -877,6 +893,85 @@ __global__ void __launch_bounds__(320, 1)
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[192 + li] = clock64();
       const int rbase = m0 + (int)crank * BM + q4 * 32;
+      if constexpr (VAR > 0 && (VarF<VAR>::F & EF_LN) != 0) {
+        // ---- LayerNorm epilogue (N == BN: the tile holds whole rows).  Lane = row; the two warps of a TMEM
+        // lane quadrant (hh = 0, 1) own the two column halves and exchange row partial sums through shared
+        // memory (named barrier per quadrant).  Pass 1: v = alpha acc + bias + resid -> written back to TMEM,
+        // R = bf16(v) stored, sum(v); pass 2: sum((v - mu)^2); pass 3: Y = gamma (v - mu) rstd + beta.
+        const int row = rbase + lane;
+        const bool rok = row < g.M;
+        const int64_t ro = rok ? lean_row(e, z, row) : 0;
+        const uint32_t tq = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC);
+        float* xch = sbias + q4 * 64;   // [quadrant][hh][32 lanes] row partial sums (the bias scratch)
+        const int cb0 = n0 + hh * HC;
+        float s1 = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < HC; c += 32) {
+          uint32_t v[32];
+          ld_tmem32(tq + c, v);
+          float rv[32], bv[32];
+          if (rok) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ldg_bf8(e.resid, ro + cb0 + c + 8 * q, rv + 8 * q);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) rv[q] = 0.f;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ldg_bf8(e.bias, cb0 + c + 8 * q, bv + 8 * q);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float f[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) { f[q] = __uint_as_float(v[q]) * e.alpha + bv[q] + rv[q]; s1 += f[q]; }
+          if (rok) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) stg8<false>(e.aux, ro + cb0 + c + 8 * q, f + 8 * q);
+          }
+          tmem_st32f(tq + c, f);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        const uint32_t bar_id = 2 + q4;
+        xch[hh * 32 + lane] = s1;
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        const float mean = (xch[lane] + xch[32 + lane]) / (float)g.N;
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        float s2 = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < HC; c += 32) {
+          uint32_t v[32];
+          ld_tmem32(tq + c, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int q = 0; q < 32; ++q) { const float t = __uint_as_float(v[q]) - mean; s2 += t * t; }
+        }
+        xch[hh * 32 + lane] = s2;
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        const float rs = rsqrtf((xch[lane] + xch[32 + lane]) / (float)g.N + e.ln_eps);
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        if (rok && hh == 0) { e.ln_mu[row] = mean; e.ln_rstd[row] = rs; }
+#pragma unroll 1
+        for (int c = 0; c < HC; c += 32) {
+          uint32_t v[32];
+          ld_tmem32(tq + c, v);
+          float gv[32], be[32];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) { ldg_bf8(e.ln_gamma, cb0 + c + 8 * q, gv + 8 * q); ldg_bf8(e.ln_beta, cb0 + c + 8 * q, be + 8 * q); }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (c + 32 >= HC) {   // accumulator fully read: hand it back to the MMA warp
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) tempty_arrive(smem_u32(tempty + ab), pair);
+          }
+          float y[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) y[q] = (__uint_as_float(v[q]) - mean) * rs * gv[q] + be[q];
+          if (rok) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) stg8<false>(e.c, ro + cb0 + c + 8 * q, y + 8 * q);
+          }
+        }
+        continue;
+      }
       if constexpr (VAR > 0 && ((VarF<VAR>::F & ~TS_FLAGS) == 0) && (!(VarF<VAR>::F & EF_ACC) || VarF<VAR>::C)) {
         if (p.tstore && p.dbg != 1) {
           // ---- TMA-store epilogue: lane = row; a pass takes 128 B of the row (64 bf16 / 32 fp32 columns) from

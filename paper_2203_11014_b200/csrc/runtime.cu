@@ -129,6 +129,7 @@ struct dhen_ctx {
   // layout experiments (env DHEN_GRAM_SPT, DHEN_TR_SMALL_M; measured slower on C2, default off): several
   // samples per Gram tile; transposed (column-contiguous C) Gram-backward / DCN dT for m < 128
   int gram_spt = 0, tr_small_m = 0;
+  int ln_fuse = 1;   // env DHEN_LN_FUSE: LayerNorm in the attention out-proj / FFN2 GEMM epilogues
   float* big = nullptr;     // fp32 scratch [B*H*m*m] / [B*m*m] (Gram, attention S / dP)
   void* tA = nullptr;       // dtype scratch [B * m * d * 3] (dT, dQKV, ...)
   void* tB = nullptr;       // dtype scratch [B * m * d]
@@ -617,17 +618,39 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
                       view(md.O, dt, d, 1, (int64_t)mi * d, dh, H));
           RET(G_(o, c, st, "attn.pv"));
         }
-        Gemm r1 = mk((int)rows, d, d, 1, operand(md.O, dt, d, 1), operand(p(md.Wo), dt, d, 1), view(c->rtmp, F32, d, 1));
-        r1.e.bias = p(md.bo); r1.e.bias_dt = dt; r1.e.resid = view((void*)X, dt, d, 1);
-        RET(G_(r1, c, st, "attn.out"));
-        KT("attn.ln1", 0, (double)rows * d * (4 + 2 * es), ln_fwd(c->rtmp, nullptr, p(md.g1), p(md.be1), dt, c->cfg.ln_eps, rows, d, md.Z1, md.R1, md.mu1, md.rs1, dt, st));
+        // F5: Z1 = LN1(X + O W_o^T + b_o) -- with whole rows per tile (bf16, d = 128 / 256) the LayerNorm runs
+        // in the GEMM epilogue (R1 and the row statistics saved for B6), else GEMM into fp32 + LN kernel
+        const bool ln_fused = c->ln_fuse && dt == BF16 && (d == 128 || d == 256);
+        if (ln_fused) {
+          Gemm r1 = mk((int)rows, d, d, 1, operand(md.O, dt, d, 1), operand(p(md.Wo), dt, d, 1), view(md.Z1, dt, d, 1));
+          r1.e.bias = p(md.bo); r1.e.bias_dt = dt; r1.e.resid = view((void*)X, dt, d, 1);
+          r1.e.aux = view(md.R1, dt, d, 1);
+          r1.e.ln_gamma = p(md.g1); r1.e.ln_beta = p(md.be1); r1.e.ln_mu = md.mu1; r1.e.ln_rstd = md.rs1;
+          r1.e.ln_eps = c->cfg.ln_eps;
+          RET(G_(r1, c, st, "attn.out_ln1"));
+        } else {
+          Gemm r1 = mk((int)rows, d, d, 1, operand(md.O, dt, d, 1), operand(p(md.Wo), dt, d, 1), view(c->rtmp, F32, d, 1));
+          r1.e.bias = p(md.bo); r1.e.bias_dt = dt; r1.e.resid = view((void*)X, dt, d, 1);
+          RET(G_(r1, c, st, "attn.out"));
+          KT("attn.ln1", 0, (double)rows * d * (4 + 2 * es), ln_fwd(c->rtmp, nullptr, p(md.g1), p(md.be1), dt, c->cfg.ln_eps, rows, d, md.Z1, md.R1, md.mu1, md.rs1, dt, st));
+        }
         Gemm f1 = mk((int)rows, f, d, 1, operand(md.Z1, dt, d, 1), operand(p(md.W1), dt, d, 1), view(md.F, dt, f, 1));
         f1.e.bias = p(md.b1); f1.e.bias_dt = dt; f1.e.relu = 1;
         RET(G_(f1, c, st, "attn.ffn1"));
-        Gemm f2 = mk((int)rows, d, f, 1, operand(md.F, dt, f, 1), operand(p(md.W2), dt, f, 1), view(c->rtmp, F32, d, 1));
-        f2.e.bias = p(md.b2); f2.e.bias_dt = dt; f2.e.resid = view(md.Z1, dt, d, 1);
-        RET(G_(f2, c, st, "attn.ffn2"));
-        KT("attn.ln2", 0, (double)rows * d * (4 + 2 * es), ln_fwd(c->rtmp, nullptr, p(md.g2), p(md.be2), dt, c->cfg.ln_eps, rows, d, md.T, md.R2, md.mu2, md.rs2, dt, st));
+        // F6: T = LN2(Z1 + F W_2^T + b_2), fused the same way
+        if (ln_fused) {
+          Gemm f2 = mk((int)rows, d, f, 1, operand(md.F, dt, f, 1), operand(p(md.W2), dt, f, 1), view(md.T, dt, d, 1));
+          f2.e.bias = p(md.b2); f2.e.bias_dt = dt; f2.e.resid = view(md.Z1, dt, d, 1);
+          f2.e.aux = view(md.R2, dt, d, 1);
+          f2.e.ln_gamma = p(md.g2); f2.e.ln_beta = p(md.be2); f2.e.ln_mu = md.mu2; f2.e.ln_rstd = md.rs2;
+          f2.e.ln_eps = c->cfg.ln_eps;
+          RET(G_(f2, c, st, "attn.ffn2_ln2"));
+        } else {
+          Gemm f2 = mk((int)rows, d, f, 1, operand(md.F, dt, f, 1), operand(p(md.W2), dt, f, 1), view(c->rtmp, F32, d, 1));
+          f2.e.bias = p(md.b2); f2.e.bias_dt = dt; f2.e.resid = view(md.Z1, dt, d, 1);
+          RET(G_(f2, c, st, "attn.ffn2"));
+          KT("attn.ln2", 0, (double)rows * d * (4 + 2 * es), ln_fwd(c->rtmp, nullptr, p(md.g2), p(md.be2), dt, c->cfg.ln_eps, rows, d, md.T, md.R2, md.mu2, md.rs2, dt, st));
+        }
         RET(tokmix_fwd(c, md.T, mi, p(md.Wu), l, Us, ldU, B, 0, st));
         break;
       }
@@ -926,6 +949,7 @@ static dhen_status make_ctx(const dhen_config* cfg, const dhen_dist* dist, dhen_
   c->cfg = *cfg;
   { const char* e = getenv("DHEN_GRAM_SPT"); c->gram_spt = e ? atoi(e) : 0; }
   { const char* e = getenv("DHEN_TR_SMALL_M"); c->tr_small_m = e ? atoi(e) : 0; }
+  { const char* e = getenv("DHEN_LN_FUSE"); c->ln_fuse = e ? atoi(e) : 1; }
   if (c->cfg.ln_eps <= 0.f) c->cfg.ln_eps = 1e-5f;
   c->mods_cfg.resize(cfg->n_layers);
   c->layers_cfg.resize(cfg->n_layers);

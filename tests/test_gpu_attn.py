@@ -88,3 +88,25 @@ def test_fused_attention_deterministic():
     assert np.array_equal(t2np(y1), t2np(y2))
     assert np.array_equal(t2np(dx1), t2np(dx2))
     assert np.array_equal(g1, g2)
+
+
+@pytest.mark.parametrize("m,d,B", [(128, 128, 200), (100, 256, 90)])
+def test_layernorm_epilogue_matches_ln_kernel(m, d, B, monkeypatch):
+    """F5 / F6: LayerNorm fused into the out-projection / FFN2 GEMM epilogue (whole rows per tile) against
+    the GEMM-into-fp32 + LayerNorm-kernel path on the same inputs (same bf16 storage points)."""
+    from paper_2203_11014_b200.binding import debug_attn_fused
+    debug_attn_fused(1)
+    net = _net(m, d)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("DHEN_LN_FUSE", mode)
+        case = Case(net, B, "bf16", seed=123)
+        y, dy, dx, gg = _layer(case, net)
+        out[mode] = (t2np(y), t2np(dx), gg)
+    (y0, dx0, g0), (y1, dx1, g1) = out["0"], out["1"]
+    assert elem_err(y1, y0) <= 1e-2
+    assert norm_err(dx1, dx0) <= 1e-2
+    t0, t1 = per_tensor(net, 0, g0), per_tensor(net, 0, g1)
+    for k in t0:
+        tol = 5e-2 if k.endswith(("W_1", "b_1")) else 1e-2
+        assert norm_err(t1[k], t0[k]) <= tol, (k, norm_err(t1[k], t0[k]))
