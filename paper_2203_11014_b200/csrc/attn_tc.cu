@@ -21,6 +21,9 @@
 // operands), dS carries the 1/sqrt(dh) scale, O and dQKV are stored bf16, all accumulation is fp32.
 #include <cuda.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "attn.h"
 #include "gemm_tc_kernel.cuh"
 
@@ -428,6 +431,285 @@ __global__ void __launch_bounds__(192, DH == 64 ? 2 : 1) attn_bwd_kernel(const _
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
 }
 
+// ------------------------------------------------------------------ ping-pong variants (one CTA per SM)
+// Two consumer groups of four warps (warps 2-5: group 0, 6-9: group 1) take alternate items, so one group's
+// softmax / epilogue overlaps the other's, and an NS-deep ring of item stages lets the TMA producer run
+// NS items ahead.  Item it of a CTA uses stage it % NS and group it & 1; each group owns a 128-column TMEM
+// region (the output accumulators overlay S once P has left it).
+__device__ __forceinline__ int cta_items(int items) {
+  return (int)blockIdx.x < items ? (items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+}
+
+// forward: stage = Q | K | V (DH / 64 chunks each), P overlays Q (and K when DH = 64).
+template <int DH, int NS>
+__global__ void __launch_bounds__(320, 1) attn_fwd_pp(const __grid_constant__ CUtensorMap qkv, const __grid_constant__ Params p) {
+  constexpr int NCH = DH / 64, STG = 3 * NCH * CHUNK;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bars = (uint64_t*)(smem + NS * STG);
+  auto B_ = [&](int i) { return smem_u32(bars + i); };
+  // [0, NS) qk_full, [NS, 2NS) v_full, [2NS, 3NS) stage free, then per group: s_full, p_full, o_full, t_free
+  const int GB = 3 * NS;
+  uint32_t* tslot = (uint32_t*)(bars + GB + 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&qkv) : "memory");
+    for (int i = 0; i < 3 * NS; ++i) mbar_init(B_(i), 1);
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(B_(GB + 4 * g + 0), 1); mbar_init(B_(GB + 4 * g + 1), 4);
+      mbar_init(B_(GB + 4 * g + 2), 1); mbar_init(B_(GB + 4 * g + 3), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  const int H = p.H, d = p.d, n = cta_items(p.items);
+  auto sQ = [&](int s) { return sbase + (uint32_t)(s * STG); };
+  auto sK = [&](int s) { return sbase + (uint32_t)(s * STG + NCH * CHUNK); };
+  auto sV = [&](int s) { return sbase + (uint32_t)(s * STG + 2 * NCH * CHUNK); };
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer
+      for (int it = 0; it < n; ++it) {
+        const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS;
+        if (it >= NS) mbar_wait(B_(2 * NS + s), ((it / NS) - 1) & 1);   // P V of item it - NS done
+        mbar_expect_tx(B_(s), 2 * NCH * CHUNK);
+        for (int c = 0; c < NCH; ++c) {
+          tma_load2(sQ(s) + c * CHUNK, &qkv, h * DH + 64 * c, b * p.m, B_(s));
+          tma_load2(sK(s) + c * CHUNK, &qkv, d + h * DH + 64 * c, b * p.m, B_(s));
+        }
+        mbar_expect_tx(B_(NS + s), NCH * CHUNK);
+        for (int c = 0; c < NCH; ++c) tma_load2(sV(s) + c * CHUNK, &qkv, 2 * d + h * DH + 64 * c, b * p.m, B_(NS + s));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // ---------------- MMA issuer
+      const uint32_t id_s = idesc(ROWS, false, false), id_o = idesc(DH, false, true);
+      auto issueS = [&](int it) {
+        const int s = it % NS, g = it & 1;
+        if (it >= 2) mbar_wait(B_(GB + 4 * g + 3), ((it >> 1) - 1) & 1);   // group's O of item it - 2 drained
+        mbar_wait(B_(s), (it / NS) & 1);
+        tc_after();
+        mma_chain(tmem + g * 128, sQ(s), false, sK(s), false, id_s, DH / 16);   // S = Q K^T
+        mma_commit(B_(GB + 4 * g + 0));
+      };
+      if (n > 0) issueS(0);
+      for (int it = 0; it < n; ++it) {
+        if (it + 1 < n) issueS(it + 1);
+        const int s = it % NS, g = it & 1;
+        mbar_wait(B_(GB + 4 * g + 1), (it >> 1) & 1);   // P written
+        mbar_wait(B_(NS + s), (it / NS) & 1);            // V landed
+        tc_after();
+        mma_chain(tmem + g * 128, sQ(s), false, sV(s), true, id_o, ROWS / 16);   // O = P V (P overlays Q)
+        mma_commit(B_(GB + 4 * g + 2));
+        mma_commit(B_(2 * NS + s));
+      }
+    }
+  } else {             // ---------------- two softmax / epilogue groups
+    const int g = (warp - 2) >> 2, q4 = warp & 3, row = q4 * 32 + lane;
+    const uint32_t tl = tmem + (uint32_t)(g * 128) + ((uint32_t)(q4 * 32) << 16);
+    const bool row_ok = row < p.m;
+    for (int it = g; it < n; it += 2) {
+      const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS;
+      const uint32_t ph = (it >> 1) & 1;
+      mbar_wait(B_(GB + 4 * g + 0), ph);
+      tc_after();
+      {
+        uint32_t pk[ROWS / 2];
+        softmax_row(tl, p.m, row_ok, p.scale, pk);
+        store_row_tile(sQ(s), row, pk);
+      }
+      fence_async_smem();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B_(GB + 4 * g + 1));
+      mbar_wait(B_(GB + 4 * g + 2), ph);
+      tc_after();
+      store_acc_row<DH>(tl, p.out + ((int64_t)b * p.m + row) * d + h * DH, row_ok);
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B_(GB + 4 * g + 3));
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+// backward (DH = 64): stage = Q | K | V | dO | P/dS (96 KB), two stages.  TMEM per group (256 columns):
+// S [0,128) -> dV [0,64) and dQ [64,128);  dP [128,256) -> dK [128,192).
+template <int NS>
+__global__ void __launch_bounds__(320, 1) attn_bwd_pp(const __grid_constant__ CUtensorMap qkv,
+                                                      const __grid_constant__ CUtensorMap dom,
+                                                      const __grid_constant__ Params p) {
+  constexpr int DH = 64, STG = 6 * CHUNK;
+  constexpr uint32_t C_S = 0, C_DP = 128, C_DV = 0, C_DK = 128, C_DQ = 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bars = (uint64_t*)(smem + NS * STG);
+  auto B_ = [&](int i) { return smem_u32(bars + i); };
+  // [0,NS) qk_full, [NS,2NS) vdo_full, [2NS,3NS) stage free; per group (8 each): s, dp, p, dv, ds, dqk, tfree
+  const int GB = 3 * NS;
+  uint32_t* tslot = (uint32_t*)(bars + GB + 16);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&qkv) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&dom) : "memory");
+    for (int i = 0; i < 3 * NS; ++i) mbar_init(B_(i), 1);
+    for (int g = 0; g < 2; ++g) {
+      const int o = GB + 8 * g;
+      mbar_init(B_(o + 0), 1); mbar_init(B_(o + 1), 1); mbar_init(B_(o + 2), 4); mbar_init(B_(o + 3), 1);
+      mbar_init(B_(o + 4), 4); mbar_init(B_(o + 5), 1); mbar_init(B_(o + 6), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  const int H = p.H, d = p.d, n = cta_items(p.items);
+  auto sQ = [&](int s) { return sbase + (uint32_t)(s * STG); };
+  auto sK = [&](int s) { return sbase + (uint32_t)(s * STG + CHUNK); };
+  auto sV = [&](int s) { return sbase + (uint32_t)(s * STG + 2 * CHUNK); };
+  auto sdO = [&](int s) { return sbase + (uint32_t)(s * STG + 3 * CHUNK); };
+  auto sP = [&](int s) { return sbase + (uint32_t)(s * STG + 4 * CHUNK); };
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer
+      for (int it = 0; it < n; ++it) {
+        const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS;
+        if (it >= NS) mbar_wait(B_(2 * NS + s), ((it / NS) - 1) & 1);   // item it - NS fully done with the stage
+        mbar_expect_tx(B_(NS + s), 2 * CHUNK);
+        tma_load2(sV(s), &qkv, 2 * d + h * DH, b * p.m, B_(NS + s));
+        tma_load2(sdO(s), &dom, h * DH, b * p.m, B_(NS + s));
+        mbar_expect_tx(B_(s), 2 * CHUNK);
+        tma_load2(sQ(s), &qkv, h * DH, b * p.m, B_(s));
+        tma_load2(sK(s), &qkv, d + h * DH, b * p.m, B_(s));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // ---------------- MMA issuer
+      const uint32_t id_sq = idesc(ROWS, false, false), id_t = idesc(DH, true, true), id_q = idesc(DH, false, true);
+      auto issueF = [&](int it) {
+        const int s = it % NS, g = it & 1, o = GB + 8 * g;
+        const uint32_t tg = tmem + (uint32_t)(g * 256);
+        if (it >= 2) mbar_wait(B_(o + 6), ((it >> 1) - 1) & 1);   // group's accumulators of item it - 2 drained
+        mbar_wait(B_(NS + s), (it / NS) & 1);
+        tc_after();
+        mma_chain(tg + C_DP, sdO(s), false, sV(s), false, id_sq, DH / 16);   // dP = dO V^T
+        mma_commit(B_(o + 1));
+        mbar_wait(B_(s), (it / NS) & 1);
+        tc_after();
+        mma_chain(tg + C_S, sQ(s), false, sK(s), false, id_sq, DH / 16);     // S = Q K^T
+        mma_commit(B_(o + 0));
+      };
+      if (n > 0) issueF(0);
+      for (int it = 0; it < n; ++it) {
+        if (it + 1 < n) issueF(it + 1);
+        const int s = it % NS, g = it & 1, o = GB + 8 * g;
+        const uint32_t tg = tmem + (uint32_t)(g * 256), ph = (it >> 1) & 1;
+        mbar_wait(B_(o + 2), ph);   // P written
+        tc_after();
+        mma_chain(tg + C_DV, sP(s), true, sdO(s), true, id_t, ROWS / 16);    // dV = P^T dO
+        mma_commit(B_(o + 3));
+        mbar_wait(B_(o + 4), ph);   // dS written
+        tc_after();
+        mma_chain(tg + C_DQ, sP(s), false, sK(s), true, id_q, ROWS / 16);    // dQ = dS K
+        mma_chain(tg + C_DK, sP(s), true, sQ(s), true, id_t, ROWS / 16);     // dK = dS^T Q
+        mma_commit(B_(o + 5));
+        mma_commit(B_(2 * NS + s));
+      }
+    }
+  } else {             // ---------------- two consumer groups
+    const int g = (warp - 2) >> 2, q4 = warp & 3, row = q4 * 32 + lane, o = GB + 8 * g;
+    const uint32_t tl = tmem + (uint32_t)(g * 256) + ((uint32_t)(q4 * 32) << 16);
+    const bool row_ok = row < p.m;
+    const int64_t ld = 3 * (int64_t)d;
+    for (int it = g; it < n; it += 2) {
+      const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS;
+      const uint32_t ph = (it >> 1) & 1, pt = sP(s);
+      __nv_bfloat16* orow = p.out + ((int64_t)b * p.m + row) * ld + h * DH;
+      mbar_wait(B_(o + 0), ph);
+      tc_after();
+      {
+        uint32_t pk[ROWS / 2];
+        softmax_row(tl + C_S, p.m, row_ok, p.scale, pk);
+        store_row_tile(pt, row, pk);
+      }
+      fence_async_smem();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B_(o + 2));
+      mbar_wait(B_(o + 1), ph);
+      tc_after();
+      float D = 0.f;
+#pragma unroll
+      for (int c = 0; c < ROWS / 32; ++c) {
+        float v[32];
+        tmem_ld32(tl + C_DP + c * 32, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int gg = c * 4 + q;
+          const uint4 u = lds16(swz(pt, row, gg >> 3, gg & 7));
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            D = fmaf(__uint_as_float(w[t] << 16), v[8 * q + 2 * t], D);
+            D = fmaf(__uint_as_float(w[t] & 0xffff0000u), v[8 * q + 2 * t + 1], D);
+          }
+        }
+      }
+      mbar_wait(B_(o + 3), ph);   // dV done: P may be overwritten
+      tc_after();
+      store_acc_row<DH>(tl + C_DV, orow + 2 * d, row_ok);
+#pragma unroll
+      for (int c = 0; c < ROWS / 32; ++c) {
+        float v[32];
+        tmem_ld32(tl + C_DP + c * 32, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int gg = c * 4 + q;
+          const uint32_t a_ = swz(pt, row, gg >> 3, gg & 7);
+          const uint4 u = lds16(a_);
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+          uint32_t qq[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            qq[t] = pack_bf2(p.scale * __uint_as_float(w[t] << 16) * (v[8 * q + 2 * t] - D),
+                             p.scale * __uint_as_float(w[t] & 0xffff0000u) * (v[8 * q + 2 * t + 1] - D));
+          sts16(a_, qq[0], qq[1], qq[2], qq[3]);
+        }
+      }
+      fence_async_smem();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B_(o + 4));
+      mbar_wait(B_(o + 5), ph);
+      tc_after();
+      store_acc_row<DH>(tl + C_DQ, orow, row_ok);
+      store_acc_row<DH>(tl + C_DK, orow + d, row_ok);
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B_(o + 6));
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -462,6 +744,7 @@ static bool map2(CUtensorMap* map, const void* ptr, int cols, int64_t rows) {
 }
 
 static int g_mode = -1;   // DHEN_ATTN_FUSED: 0 = off (two batched GEMMs + softmax kernels), default on
+static int g_pp = [] { const char* e = getenv("DHEN_ATTN_PP"); return e ? atoi(e) : 1; }();   // ping-pong kernels
 int set_mode(int mode) {
   if (g_mode < 0) { const char* e = getenv("DHEN_ATTN_FUSED"); g_mode = e ? atoi(e) : 1; }
   const int old = g_mode;
@@ -497,6 +780,24 @@ cudaError_t core_fwd(const void* QKV, void* O, int B, int H, int m, int d, cudaS
   Params p;
   p.items = B * H; p.H = H; p.m = m; p.d = d; p.scale = 1.f / sqrtf((float)dh); p.out = (__nv_bfloat16*)O;
   const int nch = dh / 64;
+  if (g_pp) {   // ping-pong: one CTA per SM, two consumer groups, 192 KB of item stages
+    const int ns = dh == 64 ? 4 : 2;
+    const int smem = ns * 3 * nch * CHUNK + 1024 + 256;
+    static int sms = 0;
+    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
+    const int grid = std::min(p.items, sms);
+    if (dh == 64) {
+      static bool a = false;
+      if (!a) { cudaFuncSetAttribute(attn_fwd_pp<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+      attn_fwd_pp<64, 4><<<grid, 320, smem, st>>>(mq, p);
+    } else {
+      static bool a = false;
+      if (!a) { cudaFuncSetAttribute(attn_fwd_pp<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+      attn_fwd_pp<128, 2><<<grid, 320, smem, st>>>(mq, p);
+    }
+    ++g_launches;
+    return cudaGetLastError();
+  }
   const int smem = 3 * nch * CHUNK + 1024 + 128;
   if (dh == 64) {
     static bool a = false;
@@ -519,6 +820,16 @@ cudaError_t core_bwd(const void* QKV, const void* dO, void* dQKV, int B, int H, 
   Params p;
   p.items = B * H; p.H = H; p.m = m; p.d = d; p.scale = 1.f / sqrtf((float)dh); p.out = (__nv_bfloat16*)dQKV;
   const int nch = dh / 64;
+  if (g_pp && dh == 64) {   // ping-pong backward (two 96-KB stages, two consumer groups)
+    const int smem = 2 * 6 * CHUNK + 1024 + 256;
+    static int sms = 0;
+    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
+    static bool a = false;
+    if (!a) { cudaFuncSetAttribute(attn_bwd_pp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+    attn_bwd_pp<2><<<std::min(p.items, sms), 320, smem, st>>>(mq, mo, p);
+    ++g_launches;
+    return cudaGetLastError();
+  }
   const int smem = 4 * nch * CHUNK + 2 * CHUNK + 1024 + 128;
   if (dh == 64) {
     static bool a = false;
