@@ -79,6 +79,7 @@ struct Epilogue {
   float* ln_mu = nullptr;
   float* ln_rstd = nullptr;
   float ln_eps = 1e-5f;
+  int ln_d = 0;   // segment (token) length: N (one token per row) or a divisor of N (several tokens per row)
 };
 
 struct Gemm {

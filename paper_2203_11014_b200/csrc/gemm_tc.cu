@@ -128,8 +128,9 @@ static bool make_lean(const Gemm& g, Lean* e) {
              (x.cross.ptr ? EF_CROSS : 0) | (x.aux.ptr ? EF_AUX : 0) | (x.resid.ptr ? EF_RESID : 0) |
              (x.bias ? EF_BIAS : 0);
   e->ln_gamma = x.ln_gamma; e->ln_beta = x.ln_beta; e->ln_mu = x.ln_mu; e->ln_rstd = x.ln_rstd; e->ln_eps = x.ln_eps;
-  if (x.ln_gamma) {   // LayerNorm epilogue: whole rows in one tile, bf16 output, bias + residual, pre-norm sum to aux
-    if (g.c.dt != BF16 || g.c.cs != 1 || !x.bias || !x.resid.ptr || !x.aux.ptr || !x.ln_beta || !x.ln_mu || !x.ln_rstd ||
+  e->ln_d = x.ln_d ? x.ln_d : g.N;
+  if (x.ln_gamma) {   // LayerNorm epilogue: token segments in one tile, bf16 output, residual, pre-norm sum to aux
+    if (g.c.dt != BF16 || g.c.cs != 1 || !x.resid.ptr || !x.aux.ptr || !x.ln_beta || !x.ln_mu || !x.ln_rstd ||
         x.accumulate || x.relu || x.mask.ptr || x.cross.ptr || x.triu_m || x.dcn_bwd)
       return false;
     e->flags |= EF_LN;
@@ -168,7 +169,10 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   if (g.a.dt != BF16 || g.b.dt != BF16 || g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return cudaErrorNotSupported;
   if (g.N < 16) return cudaErrorNotSupported;
   const int BN = g.N <= 64 ? 64 : g.N <= 128 ? 128 : 256;
-  if (g.e.ln_gamma && (g.N != BN || BN < 128)) return cudaErrorNotSupported;   // LN needs whole rows per tile
+  if (g.e.ln_gamma) {   // LN segments must be whole warp halves or whole tiles, and tiles must be full
+    const int ld_ = g.e.ln_d ? g.e.ln_d : g.N;
+    if (BN < 128 || g.N % BN != 0 || (ld_ != BN && ld_ != BN / 2)) return cudaErrorNotSupported;
+  }
   Params p;
   p.g = g;
   p.tiles_m = (g.M + BM - 1) / BM;

@@ -60,6 +60,7 @@ struct Lean {
   float* ln_mu;
   float* ln_rstd;
   float ln_eps;
+  int ln_d;
 };
 
 struct Params {
@@ -672,7 +673,8 @@ __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0,
   X(16, EF_RESID, false)                          \
   X(17, EF_MASK, true)                            \
   X(18, EF_BIAS | EF_CROSS, false)                \
-  X(19, EF_BIAS | EF_RESID | EF_AUX | EF_LN, false)
+  X(19, EF_BIAS | EF_RESID | EF_AUX | EF_LN, false)      \
+  X(20, EF_RESID | EF_AUX | EF_LN, false)
 static inline int lean_variant(int flags, bool cf32) {
 #define LV_ID(id, f, c) if (flags == (f) && cf32 == (c)) return id;
   LEAN_VARIANTS(LV_ID)
@@ -894,16 +896,24 @@ __global__ void __launch_bounds__(320, 1)
       if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[192 + li] = clock64();
       const int rbase = m0 + (int)crank * BM + q4 * 32;
       if constexpr (VAR > 0 && (VarF<VAR>::F & EF_LN) != 0) {
-        // ---- LayerNorm epilogue (N == BN: the tile holds whole rows).  Lane = row; the two warps of a TMEM
-        // lane quadrant (hh = 0, 1) own the two column halves and exchange row partial sums through shared
-        // memory (named barrier per quadrant).  Pass 1: v = alpha acc + bias + resid -> written back to TMEM,
-        // R = bf16(v) stored, sum(v); pass 2: sum((v - mu)^2); pass 3: Y = gamma (v - mu) rstd + beta.
+        // ---- LayerNorm epilogue over row segments of ln_d columns (each segment one token of d features).
+        // Lane = row.  ln_d == HC: a warp's column half is one whole segment; ln_d == BN: the two warps of a
+        // TMEM lane quadrant (hh = 0, 1) own the two halves of the segment and exchange row partial sums through
+        // shared memory (named barrier per quadrant).  Pass 1: v = alpha acc (+ bias) + resid -> TMEM, R = bf16(v)
+        // stored, sum(v); pass 2: sum((v - mu)^2); pass 3: Y = gamma (v - mu) rstd + beta.  The segment's
+        // statistics index is (element offset of its first column) / ln_d, relative to ln_mu / ln_rstd.
+        constexpr int F = VarF<VAR>::F;
         const int row = rbase + lane;
         const bool rok = row < g.M;
         const int64_t ro = rok ? lean_row(e, z, row) : 0;
         const uint32_t tq = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC);
+        const bool xch_mode = e.ln_d != HC;
         float* xch = sbias + q4 * 64;   // [quadrant][hh][32 lanes] row partial sums (the bias scratch)
-        const int cb0 = n0 + hh * HC;
+        const int cb0 = n0 + hh * HC;                       // first column of this warp's half
+        const int seg0 = xch_mode ? n0 : cb0;               // first column of the segment
+        const int gofs = cb0 - seg0;                        // gamma / beta index of column cb0
+        const float inv_d = 1.f / (float)e.ln_d;
+        const uint32_t bar_id = 2 + q4;
         float s1 = 0.f;
 #pragma unroll 1
         for (int c = 0; c < HC; c += 32) {
@@ -917,8 +927,13 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
             for (int q = 0; q < 32; ++q) rv[q] = 0.f;
           }
+          if constexpr ((F & EF_BIAS) != 0) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) ldg_bf8(e.bias, cb0 + c + 8 * q, bv + 8 * q);
+            for (int q = 0; q < 4; ++q) ldg_bf8(e.bias, cb0 + c + 8 * q, bv + 8 * q);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) bv[q] = 0.f;
+          }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           float f[32];
 #pragma unroll
@@ -930,11 +945,13 @@ __global__ void __launch_bounds__(320, 1)
           tmem_st32f(tq + c, f);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        const uint32_t bar_id = 2 + q4;
-        xch[hh * 32 + lane] = s1;
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-        const float mean = (xch[lane] + xch[32 + lane]) / (float)g.N;
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        if (xch_mode) {
+          xch[hh * 32 + lane] = s1;
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+          s1 = xch[lane] + xch[32 + lane];
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        }
+        const float mean = s1 * inv_d;
         float s2 = 0.f;
 #pragma unroll 1
         for (int c = 0; c < HC; c += 32) {
@@ -944,18 +961,28 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int q = 0; q < 32; ++q) { const float t = __uint_as_float(v[q]) - mean; s2 += t * t; }
         }
-        xch[hh * 32 + lane] = s2;
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-        const float rs = rsqrtf((xch[lane] + xch[32 + lane]) / (float)g.N + e.ln_eps);
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-        if (rok && hh == 0) { e.ln_mu[row] = mean; e.ln_rstd[row] = rs; }
+        if (xch_mode) {
+          xch[hh * 32 + lane] = s2;
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+          s2 = xch[lane] + xch[32 + lane];
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        }
+        const float rs = rsqrtf(s2 * inv_d + e.ln_eps);
+        if (rok && (!xch_mode || hh == 0)) {
+          const int64_t tok = (ro + seg0) / e.ln_d;
+          e.ln_mu[tok] = mean;
+          e.ln_rstd[tok] = rs;
+        }
 #pragma unroll 1
         for (int c = 0; c < HC; c += 32) {
           uint32_t v[32];
           ld_tmem32(tq + c, v);
           float gv[32], be[32];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) { ldg_bf8(e.ln_gamma, cb0 + c + 8 * q, gv + 8 * q); ldg_bf8(e.ln_beta, cb0 + c + 8 * q, be + 8 * q); }
+          for (int q = 0; q < 4; ++q) {
+            ldg_bf8(e.ln_gamma, gofs + c + 8 * q, gv + 8 * q);
+            ldg_bf8(e.ln_beta, gofs + c + 8 * q, be + 8 * q);
+          }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           if (c + 32 >= HC) {   // accumulator fully read: hand it back to the MMA warp
             asm volatile("tcgen05.fence::before_thread_sync;");

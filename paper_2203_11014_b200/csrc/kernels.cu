@@ -1584,7 +1584,7 @@ template <int VEC>
 __global__ void __launch_bounds__(256) head_v(const __nv_bfloat16* __restrict__ Y, const __nv_bfloat16* __restrict__ w,
                                               const __nv_bfloat16* __restrict__ bh, const float* __restrict__ labels,
                                               int m, int d, int Bg, __nv_bfloat16* __restrict__ dY, float* pooled,
-                                              float* z, float* lossb, float* dz, int do_bwd) {
+                                              float* z, float* lossb, float* dz, int do_bwd, float* __restrict__ hpart) {
   extern __shared__ float hs[];   // [RY][d] partial column sums
   __shared__ float red[8];
   __shared__ float dzs;
@@ -1632,6 +1632,10 @@ __global__ void __launch_bounds__(256) head_v(const __nv_bfloat16* __restrict__ 
   }
   __syncthreads();
   if (!do_bwd) return;
+  if (hpart) {   // this sample's row of the head-gradient / loss partials: [dz pooled (d), dz, loss]
+    for (int c = threadIdx.x; c < d; c += blockDim.x) hpart[(int64_t)b * (d + 2) + c] = dzs * pooled[(int64_t)b * d + c];
+    if (threadIdx.x == 0) { hpart[(int64_t)b * (d + 2) + d] = dzs; hpart[(int64_t)b * (d + 2) + d + 1] = lossb[b]; }
+  }
   const float g = dzs / m;
   // every row of dY[b] is the same vector g * w
   for (int q = threadIdx.x; q < m * CX; q += blockDim.x) {
@@ -1703,8 +1707,13 @@ cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, 
   if (dt == BF16 && pdt == BF16 && d % 8 == 0 && d / 8 <= 256 && ((uintptr_t)Y % 16) == 0 && ((uintptr_t)w % 16) == 0 &&
       (!do_bwd || ((uintptr_t)dY % 16) == 0)) {
     const int RY = 256 / (d / 8);
+    float* hpart = pooled + (int64_t)B * d;   // [B][d + 2] (sized by the runtime)
     head_v<8><<<B, 256, (size_t)RY * d * sizeof(float), st>>>((const __nv_bfloat16*)Y, (const __nv_bfloat16*)w,
-        (const __nv_bfloat16*)bh, labels, m, d, Bg, (__nv_bfloat16*)dY, pooled, z, lossb, dz, do_bwd);
+        (const __nv_bfloat16*)bh, labels, m, d, Bg, (__nv_bfloat16*)dY, pooled, z, lossb, dz, do_bwd,
+        do_bwd ? hpart : nullptr);
+    ++g_launches;
+    if (do_bwd) part_sum(hpart, B, d + 2, dw, d, db, 1, loss_out, 1.f / (float)Bg, st);   // fixed order over samples
+    return cudaGetLastError();
   } else {
     head_k<<<B, 256, 0, st>>>(Y, w, bh, pdt, labels, m, d, Bg, dY, dt, pooled, z, lossb, dz, do_bwd);
   }
@@ -1731,6 +1740,21 @@ __global__ void blockdiag_k(const __nv_bfloat16* W, int m, int l, int spt, __nv_
 cudaError_t blockdiag(const void* W, int m, int l, int spt, void* out, cudaStream_t st) {
   const int n = spt * m * spt * l;
   blockdiag_k<<<(n + 255) / 256, 256, 0, st>>>((const __nv_bfloat16*)W, m, l, spt, (__nv_bfloat16*)out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// out[i][k] (bf16, [spt l][spt m]) = W[k % m][i % l] if i / l == k / m else 0: blockdiag(W^T, .., W^T)
+__global__ void blockdiag_t_k(const __nv_bfloat16* W, int m, int l, int spt, __nv_bfloat16* out) {
+  const int n = spt * l * spt * m;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int i = t / (spt * m), k = t - i * (spt * m);
+    out[t] = (i / l == k / m) ? W[(k % m) * l + (i % l)] : __float2bfloat16_rn(0.f);
+  }
+}
+cudaError_t blockdiag_t(const void* W, int m, int l, int spt, void* out, cudaStream_t st) {
+  const int n = spt * l * spt * m;
+  blockdiag_t_k<<<(n + 255) / 256, 256, 0, st>>>((const __nv_bfloat16*)W, m, l, spt, (__nv_bfloat16*)out);
   ++g_launches;
   return cudaGetLastError();
 }

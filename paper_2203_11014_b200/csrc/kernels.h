@@ -52,6 +52,8 @@ cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, 
 
 // out (bf16 [spt m][spt l]) = blockdiag(W, .., W) of the bf16 token map W [m][l] (DCN backward packing)
 cudaError_t blockdiag(const void* W, int m, int l, int spt, void* out, cudaStream_t st);
+// out (bf16 [spt l][spt m]) = blockdiag(W^T, .., W^T) (packed token projection)
+cudaError_t blockdiag_t(const void* W, int m, int l, int spt, void* out, cudaStream_t st);
 
 // SGD (R18): master -= lr * grad; copy = (dt) master.  lr == 0 with grad == NULL: refresh copy only.
 cudaError_t sgd_cast(float* master, const float* grad, float lr, void* copy, int dt, int64_t n, cudaStream_t st);

@@ -68,6 +68,7 @@ struct Mod {
   void *Z = nullptr, *A = nullptr, *T = nullptr, *QKV = nullptr, *P = nullptr, *O = nullptr, *R1 = nullptr,
        *Z1 = nullptr, *F = nullptr, *R2 = nullptr, *h1 = nullptr, *h2 = nullptr;
   float *mu1 = nullptr, *rs1 = nullptr, *mu2 = nullptr, *rs2 = nullptr;
+  void* bdT = nullptr;   // bf16 [128][spt m]: blockdiag(W_u^T, ..) for the packed token projection (layer LN fused)
 };
 
 struct Group {
@@ -381,6 +382,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
         }
         default: break;
       }
+      md.bdT = work.take((size_t)128 * 128 * 8 * 2);   // spt m <= 1024 columns
     }
   }
   // scratch
@@ -404,7 +406,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   c->ws2.bytes = (size_t)256 << 20;
   c->ws2.ptr = (float*)work.take(c->ws2.bytes);
   c->red2 = (float*)work.take(c->red_bytes);
-  c->pooled = (float*)work.take(((size_t)B * d + (size_t)((B + 31) / 32) * (d + 2)) * 4);   // + head partials
+  c->pooled = (float*)work.take(((size_t)B * d + (size_t)B * (d + 2)) * 4);   // + head partials [B][d + 2]
   c->z = (float*)work.take((size_t)B * 4);
   c->lossb = (float*)work.take((size_t)B * 4);
   c->dz = (float*)work.take((size_t)B * 4);
@@ -547,6 +549,21 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
   // self-attention module in the layer it runs on the layer stream and every other module on the side
   // stream; otherwise modules alternate.  Attention modules always stay on the layer stream (rtmp/big
   // scratch).  The profiled pass runs serialised.
+  // F12 fused (identity shortcut, bf16, d = 128 / 256): every module's producing GEMM writes its token rows of
+  // Y = LN(U_i + X) directly -- the LayerNorm runs in its epilogue over d-column segments (R, mu, rstd saved),
+  // so neither the fp32 concat buffer nor the LayerNorm kernel is touched.  Token-mixing outputs use the packed
+  // form U[(b, t)] = blockdiag(W_u^T, ..) x [T_b; T_b+1; ..] (rows = tokens of 128 / l samples per tile).
+  bool lnf = c->ln_fuse && dt == BF16 && Lr.Wn < 0 && mi == mo && (d == 128 || d == 256);
+  for (const Mod& m_ : Lr.mods) {
+    if (!lnf) break;
+    const int l_ = m_.s.l;
+    if (m_.s.kind == DHEN_DOT || m_.s.kind == DHEN_MLP) {
+      const int N = l_ * d, BN = N <= 64 ? 64 : N <= 128 ? 128 : 256;
+      lnf = BN >= 128 && N % BN == 0 && (d == BN || 2 * d == BN);
+    } else {
+      lnf = l_ <= 128 && 128 % l_ == 0 && B % (128 / l_) == 0 && mi % 64 == 0 && (128 / l_) * mi <= 1024;
+    }
+  }
   const cudaStream_t st0 = st;
   const bool use_side = c->overlap && !c->prof && Lr.mods.size() > 1;
   bool has_attn = false;
@@ -559,6 +576,28 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
     const bool on_side = use_side && md.s.kind != DHEN_ATTN && (has_attn || (mod_idx & 1));
     ++mod_idx;
     cudaStream_t st = on_side ? c->side_st : st0;   // this module's stream (shadows the layer stream)
+    const int64_t so = (int64_t)mo * d;               // sample stride of Y / R / X (mi == mo when lnf)
+    char* Yo = (char*)Y + (int64_t)md.off_tok * d * es;
+    char* Ro = (char*)Lr.R + (int64_t)md.off_tok * d * es;
+    const char* Xo = (const char*)X + (int64_t)md.off_tok * d * es;
+    auto set_ln = [&](Gemm& gm) {
+      gm.e.ln_gamma = p(Lr.gamma); gm.e.ln_beta = p(Lr.beta);
+      gm.e.ln_mu = Lr.mu + md.off_tok; gm.e.ln_rstd = Lr.rstd + md.off_tok;
+      gm.e.ln_eps = c->cfg.ln_eps; gm.e.ln_d = d;
+    };
+    // token projection U = W^T T of this module: into the concat buffer, or packed with the layer LN fused
+    auto emit_tm = [&](const void* T_, const void* W_) -> dhen_status {
+      if (!lnf) return tokmix_fwd(c, T_, mi, W_, l, Us, ldU, B, 0, st);
+      const int spt = 128 / l;
+      KT("tokmix.bdiagT", 0, 0.0, blockdiag_t(W_, mi, l, spt, md.bdT, st));
+      auto rows2 = [&](void* ptr) { View v = view2(ptr, dt, l, so, d, 1); v.bs0 = spt * so; return v; };
+      Gemm gm = mk(spt * l, d, spt * mi, B / spt, operand(md.bdT, dt, spt * mi, 1),
+                   operand(T_, dt, 1, d, (int64_t)spt * mi * d, 0, 1, mi, (int64_t)mi * d), rows2(Yo));
+      gm.e.resid = rows2((void*)Xo);
+      gm.e.aux = rows2(Ro);
+      set_ln(gm);
+      return G_(gm, c, st, "tokmix.fwd_ln");
+    };
     switch (md.s.kind) {
       case DHEN_DOT: {   // F1 + F2
         const int h = mi * (mi - 1) / 2;
@@ -572,12 +611,20 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         g.e.triu_spt = spt;
         g.e.triu_ld = h;
         RET(G_(g, c, st, "dot.gram"));
-        Gemm v = mk(B, l * d, h, 1, operand(md.Z, dt, h, 1), operand(p(md.Wm), dt, h, 1), view(Us, F32, ldU, 1));
-        RET(G_(v, c, st, "dot.proj"));
+        if (lnf) {   // F2 + F12: the projection's rows are samples, its columns l tokens x d (LN per d segment)
+          Gemm v = mk(B, l * d, h, 1, operand(md.Z, dt, h, 1), operand(p(md.Wm), dt, h, 1), view(Yo, dt, so, 1));
+          v.e.resid = view((void*)Xo, dt, so, 1);
+          v.e.aux = view(Ro, dt, so, 1);
+          set_ln(v);
+          RET(G_(v, c, st, "dot.proj_ln"));
+        } else {
+          Gemm v = mk(B, l * d, h, 1, operand(md.Z, dt, h, 1), operand(p(md.Wm), dt, h, 1), view(Us, F32, ldU, 1));
+          RET(G_(v, c, st, "dot.proj"));
+        }
         break;
       }
       case DHEN_LINEAR:  // F10 with T = X
-        RET(tokmix_fwd(c, X, mi, p(md.W), l, Us, ldU, B, 0, st));
+        RET(emit_tm(X, p(md.W)));
         break;
       case DHEN_DCN: {   // F8: A = X W^T + b ; T = X * A + X
         Gemm g = mk((int)rows, d, d, 1, operand(X, dt, d, 1), operand(p(md.W), dt, d, 1), view(md.T, dt, d, 1));
@@ -585,12 +632,12 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         g.e.cross = view((void*)X, dt, d, 1);
         g.e.aux = view(md.A, dt, d, 1);
         RET(G_(g, c, st, "dcn.cross"));
-        RET(tokmix_fwd(c, md.T, mi, p(md.Wu), l, Us, ldU, B, 0, st));
+        RET(emit_tm(md.T, p(md.Wu)));
         break;
       }
       case DHEN_CONV:    // F7
         KT("conv.fwd", 2.0 * rows * d * md.s.conv_k * md.s.conv_k, 2.0 * rows * d * es, conv_fwd(X, p(md.K), dt, md.s.conv_channels, md.s.conv_k, B, mi, d, md.T, dt, st));
-        RET(tokmix_fwd(c, md.T, mi, p(md.Wu), l, Us, ldU, B, 0, st));
+        RET(emit_tm(md.T, p(md.Wu)));
         break;
       case DHEN_ATTN: {  // F3-F6
         const int H = md.s.heads, dh = d / H, f = md.s.ffn_mult * d;
@@ -651,7 +698,7 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
           RET(G_(f2, c, st, "attn.ffn2"));
           KT("attn.ln2", 0, (double)rows * d * (4 + 2 * es), ln_fwd(c->rtmp, nullptr, p(md.g2), p(md.be2), dt, c->cfg.ln_eps, rows, d, md.T, md.R2, md.mu2, md.rs2, dt, st));
         }
-        RET(tokmix_fwd(c, md.T, mi, p(md.Wu), l, Us, ldU, B, 0, st));
+        RET(emit_tm(md.T, p(md.Wu)));
         break;
       }
       case DHEN_MLP: {   // F9
@@ -663,8 +710,16 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         Gemm b2 = mk(B, h2, h1, 1, operand(md.h1, dt, h1, 1), operand(p(md.W2), dt, h1, 1), view(md.h2, dt, h2, 1));
         b2.e.bias = p(md.b2); b2.e.bias_dt = dt; b2.e.relu = 1;
         RET(G_(b2, c, st, "mlp.fc2"));
-        Gemm v = mk(B, l * d, h2, 1, operand(md.h2, dt, h2, 1), operand(p(md.Wm), dt, h2, 1), view(Us, F32, ldU, 1));
-        RET(G_(v, c, st, "mlp.proj"));
+        if (lnf) {
+          Gemm v = mk(B, l * d, h2, 1, operand(md.h2, dt, h2, 1), operand(p(md.Wm), dt, h2, 1), view(Yo, dt, so, 1));
+          v.e.resid = view((void*)Xo, dt, so, 1);
+          v.e.aux = view(Ro, dt, so, 1);
+          set_ln(v);
+          RET(G_(v, c, st, "mlp.proj_ln"));
+        } else {
+          Gemm v = mk(B, l * d, h2, 1, operand(md.h2, dt, h2, 1), operand(p(md.Wm), dt, h2, 1), view(Us, F32, ldU, 1));
+          RET(G_(v, c, st, "mlp.proj"));
+        }
         break;
       }
     }
@@ -672,8 +727,9 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
   if (use_side) { CK(cudaEventRecord(c->ev_sj, c->side_st)); CK(cudaStreamWaitEvent(st0, c->ev_sj, 0)); }
   // F11 shortcut (Eq.(2)) + F12 LayerNorm
   if (Lr.Wn >= 0) RET(tokmix_fwd(c, X, mi, p(Lr.Wn), mo, U, ldU, B, 1, st));
-  KT("layer.ln", 0, (double)B * mo * d * (4 + 2 * es) + (Lr.Wn >= 0 ? 0.0 : (double)B * mo * d * es), ln_fwd(U, Lr.Wn >= 0 ? nullptr : X, p(Lr.gamma), p(Lr.beta), dt, c->cfg.ln_eps, (int64_t)B * mo, d, Y, Lr.R, Lr.mu,
-            Lr.rstd, dt, st));
+  if (!lnf)
+    KT("layer.ln", 0, (double)B * mo * d * (4 + 2 * es) + (Lr.Wn >= 0 ? 0.0 : (double)B * mo * d * es), ln_fwd(U, Lr.Wn >= 0 ? nullptr : X, p(Lr.gamma), p(Lr.beta), dt, c->cfg.ln_eps, (int64_t)B * mo, d, Y, Lr.R, Lr.mu,
+              Lr.rstd, dt, st));
   Lr.X = X;
   Lr.B = B;
   RET(release(c, n, st));
