@@ -80,6 +80,12 @@ struct Epilogue {
   float* ln_rstd = nullptr;
   float ln_eps = 1e-5f;
   int ln_d = 0;   // segment (token) length: N (one token per row) or a divisor of N (several tokens per row)
+  // ReLU bitmask, word-major [N / 32][bits_ld >= M] (bit j of word (w, r) = column 32 w + j of row r; a warp's
+  // lanes = consecutive rows touch consecutive words): bits_mode 1 writes (stored value > 0)
+  // next to C (the FFN1 forward), 2 multiplies by it (the FFN2 data gradient) instead of reading the bf16 mask
+  uint32_t* bits = nullptr;
+  int bits_mode = 0;
+  int64_t bits_ld = 0;
 };
 
 struct Gemm {

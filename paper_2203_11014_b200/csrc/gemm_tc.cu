@@ -129,6 +129,11 @@ static bool make_lean(const Gemm& g, Lean* e) {
              (x.bias ? EF_BIAS : 0);
   e->ln_gamma = x.ln_gamma; e->ln_beta = x.ln_beta; e->ln_mu = x.ln_mu; e->ln_rstd = x.ln_rstd; e->ln_eps = x.ln_eps;
   e->ln_d = x.ln_d ? x.ln_d : g.N;
+  e->bits = x.bits; e->bits_ld = x.bits_ld;
+  if (x.bits_mode) {
+    if (g.c.dt != BF16 || g.N % 64 || g.batch != 1 || x.mask.ptr || (x.bits_mode == 1 && !x.relu)) return false;
+    e->flags |= x.bits_mode == 1 ? EF_BITS : EF_BMASK;
+  }
   if (x.ln_gamma) {   // LayerNorm epilogue: token segments in one tile, bf16 output, residual, pre-norm sum to aux
     if (g.c.dt != BF16 || g.c.cs != 1 || !x.resid.ptr || !x.aux.ptr || !x.ln_beta || !x.ln_mu || !x.ln_rstd ||
         x.accumulate || x.relu || x.mask.ptr || x.cross.ptr || x.triu_m || x.dcn_bwd)
@@ -261,6 +266,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   const int var = (p.lean_id > 0 && (p.fast8 || p.lanes_rows)) ? p.lean_id : 0;
   if (p.tstore && var != p.lean_id) p.tstore = 0;
   if (g.e.ln_gamma && (!p.lean || var != p.lean_id || (p.ep.flags & EF_LN) == 0 || p.lanes_rows)) return cudaErrorNotSupported;
+  if (g.e.bits_mode && !p.tstore) return cudaErrorNotSupported;   // bitmask epilogues exist on the TMA-store path
   cudaError_t e = BN == 64 ? launch_bn64(p, ma, mb, mc, st, var) : BN == 128 ? launch_bn128(p, ma, mb, mc, st, var)
                                                                : launch_bn256(p, ma, mb, mc, st, var);
   if (e != cudaSuccess) return e;

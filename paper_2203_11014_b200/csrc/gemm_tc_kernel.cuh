@@ -41,7 +41,7 @@ struct OpMap {
 // Compact, host-resolved epilogue plan: every present view shares one row geometry
 // (offset = row term + batch term + col * cs), operands other than C are bf16.
 enum { EF_ACC = 1, EF_RELU = 2, EF_MASK = 4, EF_CROSS = 8, EF_AUX = 16, EF_RESID = 32, EF_BIAS = 64,
-       EF_DCNB = 128, EF_TRIU = 256, EF_LN = 512 };
+       EF_DCNB = 128, EF_TRIU = 256, EF_LN = 512, EF_BITS = 1024, EF_BMASK = 2048 };
 struct Lean {
   void* c;
   const void* x;
@@ -61,6 +61,8 @@ struct Lean {
   float* ln_rstd;
   float ln_eps;
   int ln_d;
+  uint32_t* bits;     // ReLU bitmask, word-major [N / 32][bits_ld = M]: EF_BITS writes (value > 0), EF_BMASK masks
+  int64_t bits_ld;
 };
 
 struct Params {
@@ -84,7 +86,7 @@ struct Params {
   int tstore;         // 1: TMA-store epilogue (row-major C, flags within TS_FLAGS; fp32 += is a TMA reduce-add)
 };
 // epilogue flags the TMA-store path implements (any subset; EF_ACC only with fp32 C, as cp.reduce .add)
-constexpr int TS_FLAGS = EF_BIAS | EF_RELU | EF_ACC;
+constexpr int TS_FLAGS = EF_BIAS | EF_RELU | EF_ACC | EF_BITS | EF_BMASK;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -674,7 +676,9 @@ __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0,
   X(17, EF_MASK, true)                            \
   X(18, EF_BIAS | EF_CROSS, false)                \
   X(19, EF_BIAS | EF_RESID | EF_AUX | EF_LN, false)      \
-  X(20, EF_RESID | EF_AUX | EF_LN, false)
+  X(20, EF_RESID | EF_AUX | EF_LN, false)               \
+  X(21, EF_BIAS | EF_RELU | EF_BITS, false)              \
+  X(22, EF_BMASK, false)
 static inline int lean_variant(int flags, bool cf32) {
 #define LV_ID(id, f, c) if (flags == (f) && cf32 == (c)) return id;
   LEAN_VARIANTS(LV_ID)
@@ -1029,12 +1033,36 @@ __global__ void __launch_bounds__(320, 1)
               if (lane == 0) tempty_arrive(smem_u32(tempty + ab), pair);
             }
             const int cl0 = hh * HC + pc;   // tile-local column of v[0]
+            const int brow = rbase + lane;
+            uint32_t mw[CW / 32];            // ReLU bitmask words of these CW columns (EF_BMASK: read)
+            if constexpr ((F & EF_BMASK) != 0) {
+              const uint32_t* bp = e.bits + (int64_t)((n0 + cl0) / 32) * e.bits_ld + brow;   // word-major: lanes coalesce
+#pragma unroll
+              for (int q = 0; q < CW / 32; ++q) mw[q] = brow < g.M ? __ldg(bp + (int64_t)q * e.bits_ld) : 0u;
+            }
 #pragma unroll
             for (int j = 0; j < CW; ++j) {
               float a = __uint_as_float(v[j]) * alpha;
               if constexpr ((F & EF_BIAS) != 0) a += sb[cl0 + j];
               if constexpr ((F & EF_RELU) != 0) a = fmaxf(a, 0.f);
+              if constexpr ((F & EF_BMASK) != 0) a = ((mw[j >> 5] >> (j & 31)) & 1u) ? a : 0.f;
               v[j] = __float_as_uint(a);
+            }
+            if constexpr ((F & EF_BITS) != 0 && !CF) {
+              // bit j = the STORED bf16 value is > 0: round-to-nearest-even maps a float > 0 to a bf16 > 0 exactly
+              // when it exceeds half the smallest bf16 subnormal, 2^-134 (R22, R24)
+#pragma unroll
+              for (int q = 0; q < CW / 32; ++q) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int t = 0; t < 32; ++t) w |= (__uint_as_float(v[32 * q + t]) > 0x1p-134f ? 1u : 0u) << t;
+                mw[q] = w;
+              }
+              if (brow < g.M) {
+                uint32_t* bp = e.bits + (int64_t)((n0 + cl0) / 32) * e.bits_ld + brow;
+#pragma unroll
+                for (int q = 0; q < CW / 32; ++q) bp[(int64_t)q * e.bits_ld] = mw[q];
+              }
             }
             const uint32_t box = boxes + (uint32_t)((tsel & 1) * 4096);   // alternate across passes AND tiles
             ++tsel;

@@ -69,6 +69,7 @@ struct Mod {
        *Z1 = nullptr, *F = nullptr, *R2 = nullptr, *h1 = nullptr, *h2 = nullptr;
   float *mu1 = nullptr, *rs1 = nullptr, *mu2 = nullptr, *rs2 = nullptr;
   void* bdT = nullptr;   // bf16 [128][spt m]: blockdiag(W_u^T, ..) for the packed token projection (layer LN fused)
+  uint32_t* Fbits = nullptr;   // attention FFN ReLU bitmask [f / 32][B m] (FFN2 data gradient reads it, not F)
 };
 
 struct Group {
@@ -131,6 +132,7 @@ struct dhen_ctx {
   // samples per Gram tile; transposed (column-contiguous C) Gram-backward / DCN dT for m < 128
   int gram_spt = 0, tr_small_m = 0;
   int ln_fuse = 1;   // env DHEN_LN_FUSE: LayerNorm in the attention out-proj / FFN2 GEMM epilogues
+  int relu_bits = 1; // env DHEN_RELU_BITS: FFN ReLU mask as a bitmask (FFN1 writes it, FFN2 dgrad reads it)
   float* big = nullptr;     // fp32 scratch [B*H*m*m] / [B*m*m] (Gram, attention S / dP)
   void* tA = nullptr;       // dtype scratch [B * m * d * 3] (dT, dQKV, ...)
   void* tB = nullptr;       // dtype scratch [B * m * d]
@@ -364,6 +366,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
           md.R1 = work.take(tok * es);
           md.Z1 = work.take(tok * es);
           md.F = work.take((size_t)B * mi * f * es);
+          md.Fbits = (uint32_t*)work.take((size_t)B * mi * ((f + 31) / 32) * 4);
           md.R2 = work.take(tok * es);
           md.T = work.take(tok * es);
           md.mu1 = (float*)work.take((size_t)B * mi * 4); md.rs1 = (float*)work.take((size_t)B * mi * 4);
@@ -683,6 +686,8 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         }
         Gemm f1 = mk((int)rows, f, d, 1, operand(md.Z1, dt, d, 1), operand(p(md.W1), dt, d, 1), view(md.F, dt, f, 1));
         f1.e.bias = p(md.b1); f1.e.bias_dt = dt; f1.e.relu = 1;
+        const bool fbits = c->relu_bits && dt == BF16 && f % 64 == 0 && f >= 128;
+        if (fbits) { f1.e.bits = md.Fbits; f1.e.bits_mode = 1; f1.e.bits_ld = rows; }
         RET(G_(f1, c, st, "attn.ffn1"));
         // F6: T = LN2(Z1 + F W_2^T + b_2), fused the same way
         if (ln_fused) {
@@ -872,7 +877,11 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
                   c->red_bytes, st));
         void* dF = c->tC;
         Gemm a = mk((int)rows, f, d, 1, operand(dR2, dt, d, 1), operand(p(md.W2), dt, 1, f), view(dF, dt, f, 1));
-        a.e.mask = view(md.F, dt, f, 1);
+        if (c->relu_bits && dt == BF16 && f % 64 == 0 && f >= 128) {   // ReLU'(0) = 0 from the forward's bitmask
+          a.e.bits = md.Fbits; a.e.bits_mode = 2; a.e.bits_ld = rows;
+        } else {
+          a.e.mask = view(md.F, dt, f, 1);
+        }
         RET(G_(a, c, st, "attn.ffn2_dgrad"));
         Gemm w2 = mk(d, f, (int)rows, 1, operand(dR2, dt, 1, d), operand(md.F, dt, 1, f), view(gp(md.W2), F32, f, 1));
         w2.e.accumulate = 1;
@@ -1006,6 +1015,7 @@ static dhen_status make_ctx(const dhen_config* cfg, const dhen_dist* dist, dhen_
   { const char* e = getenv("DHEN_GRAM_SPT"); c->gram_spt = e ? atoi(e) : 0; }
   { const char* e = getenv("DHEN_TR_SMALL_M"); c->tr_small_m = e ? atoi(e) : 0; }
   { const char* e = getenv("DHEN_LN_FUSE"); c->ln_fuse = e ? atoi(e) : 1; }
+  { const char* e = getenv("DHEN_RELU_BITS"); c->relu_bits = e ? atoi(e) : 1; }
   if (c->cfg.ln_eps <= 0.f) c->cfg.ln_eps = 1e-5f;
   c->mods_cfg.resize(cfg->n_layers);
   c->layers_cfg.resize(cfg->n_layers);

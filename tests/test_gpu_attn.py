@@ -110,3 +110,21 @@ def test_layernorm_epilogue_matches_ln_kernel(m, d, B, monkeypatch):
     for k in t0:
         tol = 5e-2 if k.endswith(("W_1", "b_1")) else 1e-2
         assert norm_err(t1[k], t0[k]) <= tol, (k, norm_err(t1[k], t0[k]))
+
+
+@pytest.mark.parametrize("m,d,B", [(128, 128, 160), (100, 256, 70)])
+def test_relu_bitmask_matches_bf16_mask(m, d, B, monkeypatch):
+    """B6 FFN: the ReLU derivative taken from the forward's bitmask (bit = stored bf16 F > 0, R22) gives the
+    same data and weight gradients, bit for bit, as reading F itself."""
+    from paper_2203_11014_b200.binding import debug_attn_fused
+    debug_attn_fused(1)
+    net = _net(m, d)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("DHEN_RELU_BITS", mode)
+        case = Case(net, B, "bf16", seed=321)
+        y, dy, dx, gg = _layer(case, net)
+        out[mode] = (t2np(y), t2np(dx), gg)
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert np.array_equal(out["0"][1], out["1"][1])
+    assert np.array_equal(out["0"][2], out["1"][2])
