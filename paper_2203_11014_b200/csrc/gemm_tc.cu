@@ -186,7 +186,8 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n * g.batch;
   int splits = 1;
   if (tiles * 2 <= 148 && p.kblocks >= 8 && !g.e.ln_gamma) {   // output fills < half the SMs, long K: split K
-    splits = (int)std::min<int64_t>((148 + tiles - 1) / tiles, p.kblocks / 4);   // one item per SM
+    // one item per SM: floor, so tiles x splits never exceeds the SM count (a 149th item doubles the time)
+    splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / tiles, p.kblocks / 4));
     while (splits > 1 && (int64_t)splits * g.batch * g.M * g.N * 4 > (int64_t)ws.bytes) --splits;
   }
   // CTA pairs (cta_group::2, 256 x BN tiles, each CTA loads BN / 2 rows of B): halves the B traffic per
@@ -198,7 +199,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
     if (env_mode == -2) { const char* ev = getenv("DHEN_PAIR"); env_mode = ev ? atoi(ev) : -1; }
     const int mode = g_gemm_pair >= 0 ? g_gemm_pair : env_mode;
     const int64_t pitems = (int64_t)((g.M + 2 * BM - 1) / (2 * BM)) * p.tiles_n * g.batch;
-    p.pair = (BN >= 128 && splits == 1 && mode != 0 && !g.e.ln_gamma && (mode == 1 ? g.M > BM : (pitems >= 74 && g.K >= 4096))) ? 1 : 0;
+    p.pair = (BN >= 128 && (splits == 1 || mode == 1 || (splits > 1 && g.M >= 2 * BM)) && mode != 0 && !g.e.ln_gamma && (mode == 1 ? g.M > BM : (pitems >= 74 && g.K >= 4096))) ? 1 : 0;
   }
   CUtensorMap ma, mb;
   if (!make_map(&ma, &p.a, g.a, g.M, g.K, g.batch, BM)) return cudaErrorNotSupported;

@@ -48,6 +48,11 @@ def shapes(cfg):
          (0, 0), (0, 0), (0, 0), bf),
         ("attn.ffn2", R, d, 4 * d, 1, (4 * d, 1, 0, 0, 1, 0, 0), (4 * d, 1, 0, 0, 1, 0, 0), (d, 1, 0, 0, 1), 0,
          (0, 0), (0, 0), (0, 0), f32),
+        # weight gradients (K = B m rows, both operands MN-major, split-K)
+        ("attn.ffn1_wgrad", 4 * d, d, R, 1, (1, 4 * d, 0, 0, 1, 0, 0), (1, d, 0, 0, 1, 0, 0), (d, 1, 0, 0, 1), 1,
+         (0, 0), (0, 0), (0, 0), f32),
+        ("attn.ffn2_wgrad", d, 4 * d, R, 1, (1, d, 0, 0, 1, 0, 0), (1, 4 * d, 0, 0, 1, 0, 0), (4 * d, 1, 0, 0, 1), 1,
+         (0, 0), (0, 0), (0, 0), f32),
         # experiments: same M, N, K as tokmix.fwd with plain layouts
         ("x.kmaj_rowmajor", B * d, l, m, 1, (m, 1, 0, 0, 1, 0, 0), (m, 1, 0, 0, 1, 0, 0), (l, 1, 0, 0, 1), 0,
          (0, 0), (0, 0), (0, 0), f32),
