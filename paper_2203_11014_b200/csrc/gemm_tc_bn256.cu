@@ -3,7 +3,7 @@
 
 namespace dhen {
 namespace tc {
-cudaError_t launch_bn256(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+cudaError_t launch_bn256(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                         cudaStream_t st, int var) {
   return launch_var<256, 3>(p, ma, mb, mc, st, var);
 }

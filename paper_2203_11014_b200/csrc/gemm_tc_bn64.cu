@@ -3,7 +3,7 @@
 
 namespace dhen {
 namespace tc {
-cudaError_t launch_bn64(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+cudaError_t launch_bn64(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                         cudaStream_t st, int var) {
   return launch_var<64, 6>(p, ma, mb, mc, st, var);
 }

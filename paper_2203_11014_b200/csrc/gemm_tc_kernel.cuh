@@ -65,6 +65,12 @@ struct Lean {
   int64_t bits_ld;
 };
 
+// TMA maps of the epilogue outputs: c = C, d = the aux output (the LayerNorm epilogue's pre-norm sum R)
+struct OutMaps {
+  CUtensorMap c;
+  CUtensorMap d;
+};
+
 struct Params {
   Gemm g;
   Lean ep;
@@ -84,6 +90,8 @@ struct Params {
   long long* trace;   // debug: CTA 0 records clock64 timestamps (nullptr = off)
   int dbg;            // debug: 1 = skip the global epilogue pass (timing experiments only)
   int tstore;         // 1: TMA-store epilogue (row-major C, flags within TS_FLAGS; fp32 += is a TMA reduce-add)
+  int lnst;           // LayerNorm epilogue: 1 = Y and R leave through TMA stores (tma_o.c / tma_o.d)
+  int ln_rdiv;        // 0: 3-D maps {N, M, batch}; l > 0: 4-D maps {N, l, M / l, batch} (two-level rows)
 };
 // epilogue flags the TMA-store path implements (any subset; EF_ACC only with fp32 C, as cp.reduce .add)
 constexpr int TS_FLAGS = EF_BIAS | EF_RELU | EF_ACC | EF_BITS | EF_BMASK;
@@ -196,6 +204,11 @@ __device__ __forceinline__ void tmem_st32f(uint32_t taddr, const float* v) {
 __device__ __forceinline__ void tma_store3(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(c0),
                "r"(c1), "r"(c2), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store4(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(c2), "r"(c3), "r"(src)
                : "memory");
 }
 __device__ __forceinline__ void tma_reduce_add3(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
@@ -742,7 +755,7 @@ template <int BN> struct EpiSmem {
 template <int BN, int STAGES, int VAR, bool PAIR>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                   const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ Params p) {
+                   const __grid_constant__ OutMaps tma_o, const __grid_constant__ Params p) {
   constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
   constexpr int SC = EpiSmem<BN>::SC;
   constexpr int SROW = EpiSmem<BN>::SROW;
@@ -919,6 +932,28 @@ __global__ void __launch_bounds__(320, 1)
         const float inv_d = 1.f / (float)e.ln_d;
         const uint32_t bar_id = 2 + q4;
         float s1 = 0.f;
+        const uint32_t boxes = smem_u32(stage_all) + (uint32_t)((warp - 2) * 2 * 4096);
+        // one 32-row x 64-column bf16 chunk of this warp -> box -> TMA store (R: map d, Y: map c)
+        auto box_store = [&](const CUtensorMap* map, const float* vals, int col) {
+          const uint32_t box = boxes + (uint32_t)((tsel & 1) * 4096);
+          ++tsel;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          const uint32_t rowa = box + (uint32_t)(lane * 128);
+#pragma unroll
+          for (int gq = 0; gq < 8; ++gq)
+            sts4u(rowa + (uint32_t)(((gq ^ (lane & 7)) & 7) << 4), pack_bf2(vals[8 * gq], vals[8 * gq + 1]),
+                  pack_bf2(vals[8 * gq + 2], vals[8 * gq + 3]), pack_bf2(vals[8 * gq + 4], vals[8 * gq + 5]),
+                  pack_bf2(vals[8 * gq + 6], vals[8 * gq + 7]));
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            if (p.ln_rdiv) tma_store4(map, box, col, rbase % p.ln_rdiv, rbase / p.ln_rdiv, z);
+            else tma_store3(map, box, col, rbase, z);
+            bulk_commit();
+          }
+        };
+        float f64[64];   // a 64-column chunk of R or Y on its way to a box (TMA path)
 #pragma unroll 1
         for (int c = 0; c < HC; c += 32) {
           uint32_t v[32];
@@ -942,7 +977,11 @@ __global__ void __launch_bounds__(320, 1)
           float f[32];
 #pragma unroll
           for (int q = 0; q < 32; ++q) { f[q] = __uint_as_float(v[q]) * e.alpha + bv[q] + rv[q]; s1 += f[q]; }
-          if (rok) {
+          if (p.lnst) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) f64[(c & 32) + q] = f[q];
+            if (c & 32) box_store(&tma_o.d, f64, cb0 + c - 32);
+          } else if (rok) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) stg8<false>(e.aux, ro + cb0 + c + 8 * q, f + 8 * q);
           }
@@ -996,7 +1035,11 @@ __global__ void __launch_bounds__(320, 1)
           float y[32];
 #pragma unroll
           for (int q = 0; q < 32; ++q) y[q] = (__uint_as_float(v[q]) - mean) * rs * gv[q] + be[q];
-          if (rok) {
+          if (p.lnst) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) f64[(c & 32) + q] = y[q];
+            if (c & 32) box_store(&tma_o.c, f64, cb0 + c - 32);
+          } else if (rok) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) stg8<false>(e.c, ro + cb0 + c + 8 * q, y + 8 * q);
           }
@@ -1084,8 +1127,8 @@ __global__ void __launch_bounds__(320, 1)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
-              if constexpr ((F & EF_ACC) != 0) tma_reduce_add3(&tma_c, box, n0 + cl0, rbase, z);
-              else tma_store3(&tma_c, box, n0 + cl0, rbase, z);
+              if constexpr ((F & EF_ACC) != 0) tma_reduce_add3(&tma_o.c, box, n0 + cl0, rbase, z);
+              else tma_store3(&tma_o.c, box, n0 + cl0, rbase, z);
               bulk_commit();
             }
           }
@@ -1262,7 +1305,7 @@ __global__ void __launch_bounds__(320, 1)
       if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[320 + li] = clock64();
     }
   }
-  if (p.tstore && warp >= 2 && lane == 0) bulk_wait_all();   // TMA stores done reading smem and written
+  if ((p.tstore || p.lnst) && warp >= 2 && lane == 0) bulk_wait_all();   // TMA stores done reading smem and written
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (pair) {
@@ -1275,7 +1318,7 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 template <int BN, int STAGES, int VAR>
-static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                           cudaStream_t st) {
   constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + EpiSmem<BN>::BYTES + 2 * BN * 4 + (2 * STAGES + 4) * 8 +
                        16 + 1024;
@@ -1326,7 +1369,7 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
 
 // Launch with the epilogue variant as a template argument (one variant per kernel instantiation).
 template <int BN, int STAGES>
-cudaError_t launch_var(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+cudaError_t launch_var(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                        cudaStream_t st, int var) {
   switch (var) {
 #define LV_L(i, f, c) \
@@ -1337,11 +1380,11 @@ cudaError_t launch_var(const Params& p, const CUtensorMap& ma, const CUtensorMap
   }
 }
 // defined in gemm_tc_bn{64,128,256}.cu (parallel compilation of the instantiations)
-cudaError_t launch_bn64(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+cudaError_t launch_bn64(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                         cudaStream_t st, int var);
-cudaError_t launch_bn128(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+cudaError_t launch_bn128(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                          cudaStream_t st, int var);
-cudaError_t launch_bn256(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+cudaError_t launch_bn256(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                          cudaStream_t st, int var);
 
 }  // namespace tc
