@@ -262,43 +262,8 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
         p.tstore = 1;
     }
   }
-  // LayerNorm epilogue outputs (Y = C, R = aux) through TMA stores: bf16, 64-column x 32-row boxes over single-level
-  // rows with one batch stride, or two-level rows (row -> (row / l, row % l)) with 32 % l == 0 or l % 32 == 0
-  p.lnst = 0;
+  p.lnst = 0;   // (TMA-store outputs for the LayerNorm epilogue were measured 2-3 % slower than direct stores)
   p.ln_rdiv = 0;
-  if (p.lean && (p.ep.flags & EF_LN) && !p.lanes_rows) {
-    static int env = -1;
-    if (env < 0) { const char* ev = getenv("DHEN_LN_TSTORE"); env = ev ? atoi(ev) : 0; }   // measured slower: off
-    EncodeFn fn = encode_fn();
-    const View* vs[2] = {&g.c, &g.e.aux};
-    CUtensorMap* ms[2] = {&mc.c, &mc.d};
-    bool ok = env && fn && (g.c.zdiv == 1 || g.c.bs1 == 0);
-    const int l = g.c.rdiv;
-    if (l && !(32 % l == 0 || l % 32 == 0)) ok = false;
-    if (l && g.M % l) ok = false;
-    for (int t = 0; t < 2 && ok; ++t) {
-      const View& v = *vs[t];
-      if (((uintptr_t)v.ptr % 16) || (v.rs * 2) % 16 || (v.bs0 * 2) % 16 || (v.rs_o * 2) % 16) { ok = false; break; }
-      const int64_t bstride = (g.batch > 1 && v.bs0) ? v.bs0 : (l ? v.rs_o * (g.M / l) : v.rs * g.M);
-      cuuint32_t estr[4] = {1, 1, 1, 1};
-      CUresult res;
-      if (!l) {
-        cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)g.batch};
-        cuuint64_t strides[2] = {(cuuint64_t)(v.rs * 2), (cuuint64_t)(bstride * 2)};
-        cuuint32_t box[3] = {64, 32, 1};
-        res = fn(ms[t], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, v.ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      } else {
-        cuuint64_t dims[4] = {(cuuint64_t)g.N, (cuuint64_t)l, (cuuint64_t)(g.M / l), (cuuint64_t)g.batch};
-        cuuint64_t strides[3] = {(cuuint64_t)(v.rs * 2), (cuuint64_t)(v.rs_o * 2), (cuuint64_t)(bstride * 2)};
-        cuuint32_t box[4] = {64, (cuuint32_t)std::min(32, l), (cuuint32_t)std::max(1, 32 / l), 1};
-        res = fn(ms[t], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      }
-      if (res != CUDA_SUCCESS) ok = false;
-    }
-    if (ok) { p.lnst = 1; p.ln_rdiv = l; }
-  }
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a.mn_major << 15) | ((uint32_t)p.b.mn_major << 16) |
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((p.pair ? 2 * BM : BM) >> 4) << 24);
   const int var = (p.lean_id > 0 && (p.fast8 || p.lanes_rows)) ? p.lean_id : 0;

@@ -908,6 +908,21 @@ __global__ void __launch_bounds__(320, 1)
       decode(item, m0, n0, z, sp, kb0, nk);
       const int ab = li & 1;
       const uint32_t aph = (li >> 1) & 1;
+      // LayerNorm epilogue: this thread's residual row slice (HC bf16) is loaded BEFORE the accumulator is
+      // ready, so its latency hides under the tile's MMAs (it is the epilogue's only global read)
+      constexpr bool LNV = VAR > 0 && (VarF<VAR>::F & EF_LN) != 0;
+      uint4 rpre[LNV ? HC / 8 : 1];
+      if constexpr (LNV) {
+        const int row_ = m0 + (int)crank * BM + q4 * 32 + lane;
+        if (row_ < g.M) {
+          const __nv_bfloat16* rp = (const __nv_bfloat16*)e.resid + lean_row(e, z, row_) + n0 + hh * HC;
+#pragma unroll
+          for (int q = 0; q < HC / 8; ++q) rpre[q] = __ldg(reinterpret_cast<const uint4*>(rp) + q);
+        } else {
+#pragma unroll
+          for (int q = 0; q < HC / 8; ++q) rpre[q] = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
       mbar_wait(smem_u32(tfull + ab), aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[192 + li] = clock64();
@@ -932,40 +947,13 @@ __global__ void __launch_bounds__(320, 1)
         const float inv_d = 1.f / (float)e.ln_d;
         const uint32_t bar_id = 2 + q4;
         float s1 = 0.f;
-        const uint32_t boxes = smem_u32(stage_all) + (uint32_t)((warp - 2) * 2 * 4096);
-        // one 32-row x 64-column bf16 chunk of this warp -> box -> TMA store (R: map d, Y: map c)
-        auto box_store = [&](const CUtensorMap* map, const float* vals, int col) {
-          const uint32_t box = boxes + (uint32_t)((tsel & 1) * 4096);
-          ++tsel;
-          if (lane == 0) bulk_wait_read<1>();
-          __syncwarp();
-          const uint32_t rowa = box + (uint32_t)(lane * 128);
 #pragma unroll
-          for (int gq = 0; gq < 8; ++gq)
-            sts4u(rowa + (uint32_t)(((gq ^ (lane & 7)) & 7) << 4), pack_bf2(vals[8 * gq], vals[8 * gq + 1]),
-                  pack_bf2(vals[8 * gq + 2], vals[8 * gq + 3]), pack_bf2(vals[8 * gq + 4], vals[8 * gq + 5]),
-                  pack_bf2(vals[8 * gq + 6], vals[8 * gq + 7]));
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) {
-            if (p.ln_rdiv) tma_store4(map, box, col, rbase % p.ln_rdiv, rbase / p.ln_rdiv, z);
-            else tma_store3(map, box, col, rbase, z);
-            bulk_commit();
-          }
-        };
-        float f64[64];   // a 64-column chunk of R or Y on its way to a box (TMA path)
-#pragma unroll 1
-        for (int c = 0; c < HC; c += 32) {
+        for (int c = 0; c < HC; c += 32) {   // unrolled: rpre is indexed with compile-time offsets
           uint32_t v[32];
           ld_tmem32(tq + c, v);
           float rv[32], bv[32];
-          if (rok) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) ldg_bf8(e.resid, ro + cb0 + c + 8 * q, rv + 8 * q);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) rv[q] = 0.f;
-          }
+          for (int q = 0; q < 4; ++q) unpack_bf8(rpre[c / 8 + q], rv + 8 * q);   // prefetched residual
           if constexpr ((F & EF_BIAS) != 0) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) ldg_bf8(e.bias, cb0 + c + 8 * q, bv + 8 * q);
@@ -977,11 +965,7 @@ __global__ void __launch_bounds__(320, 1)
           float f[32];
 #pragma unroll
           for (int q = 0; q < 32; ++q) { f[q] = __uint_as_float(v[q]) * e.alpha + bv[q] + rv[q]; s1 += f[q]; }
-          if (p.lnst) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) f64[(c & 32) + q] = f[q];
-            if (c & 32) box_store(&tma_o.d, f64, cb0 + c - 32);
-          } else if (rok) {
+          if (rok) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) stg8<false>(e.aux, ro + cb0 + c + 8 * q, f + 8 * q);
           }
@@ -1035,11 +1019,7 @@ __global__ void __launch_bounds__(320, 1)
           float y[32];
 #pragma unroll
           for (int q = 0; q < 32; ++q) y[q] = (__uint_as_float(v[q]) - mean) * rs * gv[q] + be[q];
-          if (p.lnst) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) f64[(c & 32) + q] = y[q];
-            if (c & 32) box_store(&tma_o.c, f64, cb0 + c - 32);
-          } else if (rok) {
+          if (rok) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) stg8<false>(e.c, ro + cb0 + c + 8 * q, y + 8 * q);
           }
