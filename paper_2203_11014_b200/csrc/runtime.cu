@@ -11,6 +11,7 @@
 // in DESIGN.md §4 and mirrored by the oracle's Precision.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -172,11 +173,14 @@ struct dhen_ctx {
 };
 
 // RAII scope recording a CUDA event pair around one op when profiling is on.
+// Per-op scope: an NVTX range named after the op (so `ncu --nvtx --nvtx-include "<op>/"` captures exactly that
+// op's kernels; a no-op without an attached tool) and, in profiling mode, CUDA events around the op.
 struct ProfScope {
   dhen_ctx* c;
   cudaStream_t st;
   int rec = -1;
   ProfScope(dhen_ctx* c_, const char* tag, double flops, double bytes, cudaStream_t st_) : c(c_), st(st_) {
+    nvtxRangePushA(tag);
     if (!c->prof) return;
     if (c->next_event + 2 > (int)c->events.size()) {
       if (c->events.size() >= (1u << 16)) return;   // pool exhausted: stop recording
@@ -191,6 +195,7 @@ struct ProfScope {
   }
   ~ProfScope() {
     if (rec >= 0) cudaEventRecord(c->events[c->recs[rec].e1], st);
+    nvtxRangePop();
   }
 };
 #define KT(tag, flops, bytes, call)                          \

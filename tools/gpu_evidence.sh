@@ -1,6 +1,7 @@
 #!/bin/bash
-# Round evidence: bench lines (all configs), per-op profiles, C2 ncu launch list, ncu --set full of the
-# dominant kernel of each config.  Outputs in gpurun_out/ev_*; summarise with tools/ncu_summary.py.
+# Round evidence: bench lines (all configs), per-op profiles, C2 ncu launch list, and one ncu --set full
+# capture of each config's dominant op (selected by its NVTX range).  Outputs in gpurun_out/ev_*;
+# copy into profiles/ with tools/ev_collect.sh.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { echo build failed; exit 1; }
 nproc > gpurun_out/ev_host.txt; lscpu | grep -E "Model name|^CPU\(s\)|Thread" >> gpurun_out/ev_host.txt
@@ -14,14 +15,11 @@ timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/ev_launches_C2.csv \
    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ev_ncu_launch.log 2>&1
 echo "launch list rc=$?"
-# dominant kernels (skip the warm-up launches, capture one)
-cap() {  # config regex skip tag
-  timeout 300 python bench.py --config $1 --steps 2 --warmup 3 --no-cpu-baseline --eager > gpurun_out/ev_plain_$4.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$2" -s $3 -c 1 \
-    -o gpurun_out/ev_ncu_$4 -f python bench.py --config $1 --steps 2 --warmup 3 --no-cpu-baseline --eager > gpurun_out/ev_ncu_$4.log 2>&1
-  echo "ncu $4 rc=$?"
-}
-cap C2 "gemm_tc_kernel<.int.128, .int.4, .int.12" 6 c2_dcn_dT
-cap C5 "gemm_tc_kernel<.int.256, .int.3, .int.12" 20 c5_dcn_dT
-cap C3 "attn_bwd_kernel" 8 c3_attn_bwd
-cap C4 "attn_bwd_kernel" 16 c4_attn_bwd
+for c in C2 C3 C4 C5; do
+  op=$(python -c "import json; print(json.loads(open('gpurun_out/ev_bench_$c.json').read().strip().splitlines()[-1])['roofline']['kernel'])")
+  echo "$c dominant op: $op" > gpurun_out/ev_dom_$c.txt
+  timeout 300 python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --eager > gpurun_out/ev_plain_$c.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "$op/" -s 2 -c 1 \
+    -o gpurun_out/ev_ncu_$c -f python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --eager > gpurun_out/ev_ncu_$c.log 2>&1
+  echo "ncu $c $op rc=$?"
+done
