@@ -26,7 +26,9 @@ static __device__ __forceinline__ void epi_apply(const Gemm& g, int z, int i, in
     const float a = ld_as_f32(e.mask.ptr, e.mask.off(z, i, j), e.mask.dt);
     st_from_f32(e.aux.ptr, e.aux.off(z, i, j), e.aux.dt, v * x);
     const int64_t co = g.c.off(z, i, j);
-    st_from_f32(g.c.ptr, co, g.c.dt, ld_as_f32(g.c.ptr, co, g.c.dt) + v * a + v);
+    const float base = e.resid.ptr ? ld_as_f32(e.resid.ptr, e.resid.off(z, i, j), e.resid.dt)   // first writer
+                                   : ld_as_f32(g.c.ptr, co, g.c.dt);
+    st_from_f32(g.c.ptr, co, g.c.dt, base + v * a + v);
     return;
   }
   float v = acc * e.alpha;

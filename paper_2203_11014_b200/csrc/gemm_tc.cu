@@ -145,7 +145,7 @@ static bool make_lean(const Gemm& g, Lean* e) {
   e->triu_ld = x.triu_ld;
   if (x.dcn_bwd) {
     if (g.c.dt != F32 || !x.cross.ptr || !x.mask.ptr || !x.aux.ptr || x.bias || x.accumulate) return false;
-    e->flags = EF_DCNB;
+    e->flags = EF_DCNB | (x.resid.ptr ? EF_RESID : 0);   // with a residual: first writer (C = resid + ...)
   }
   if (x.triu_m) {
     if (g.c.rs != 0 || g.c.rdiv || g.c.zdiv != 1 || x.bias || x.accumulate || x.cross.ptr || x.mask.ptr ||

@@ -583,8 +583,17 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
           dx[t] = v * av[t] + v;
         }
         stg8<false>(e.aux, ok_, da);
-        red_add4((float*)e.c + ok_, dx);
-        red_add4((float*)e.c + ok_ + 4, dx + 4);
+        if constexpr ((F & EF_RESID) != 0) {
+          // first writer of the dX accumulator: dX = dR (identity shortcut, B3) + dT A + dT, a plain store
+          float rv8[8];
+          unpack_bf8(ub[cb][k][SLR], rv8);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) dx[t] += rv8[t];
+          stg8<true>(e.c, ok_, dx);
+        } else {
+          red_add4((float*)e.c + ok_, dx);
+          red_add4((float*)e.c + ok_ + 4, dx + 4);
+        }
         continue;
       }
 #pragma unroll
@@ -655,7 +664,8 @@ __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0,
     if constexpr ((F & EF_DCNB) != 0) {
       // B8 fused: dA = dT * X (bf16 aux), dX_acc += dT * A + dT
       stg1(e.aux, o, 0, a * xs[j]);
-      asm volatile("red.global.add.f32 [%0], %1;" ::"l"((float*)e.c + o), "f"(a * ms[j] + a) : "memory");
+      if constexpr (LR) stg1(e.c, o, 1, rv[j] + a * ms[j] + a);   // first writer of dX
+      else asm volatile("red.global.add.f32 [%0], %1;" ::"l"((float*)e.c + o), "f"(a * ms[j] + a) : "memory");
       continue;
     }
     if (F & EF_BIAS) a += lean_bias(e, col);
@@ -691,7 +701,8 @@ __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0,
   X(19, EF_BIAS | EF_RESID | EF_AUX | EF_LN, false)      \
   X(20, EF_RESID | EF_AUX | EF_LN, false)               \
   X(21, EF_BIAS | EF_RELU | EF_BITS, false)              \
-  X(22, EF_BMASK, false)
+  X(22, EF_BMASK, false)                                 \
+  X(23, EF_DCNB | EF_RESID, true)
 static inline int lean_variant(int flags, bool cf32) {
 #define LV_ID(id, f, c) if (flags == (f) && cf32 == (c)) return id;
   LEAN_VARIANTS(LV_ID)

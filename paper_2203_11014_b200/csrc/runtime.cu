@@ -134,6 +134,7 @@ struct dhen_ctx {
   int gram_spt = 0, tr_small_m = 0;
   int ln_fuse = 1;   // env DHEN_LN_FUSE: LayerNorm in the attention out-proj / FFN2 GEMM epilogues
   int relu_bits = 1; // env DHEN_RELU_BITS: FFN ReLU mask as a bitmask (FFN1 writes it, FFN2 dgrad reads it)
+  int first_writer = 1;   // env DHEN_FIRST_WRITER: the first module's dX GEMM adds the shortcut's dR (B3)
   float* big = nullptr;     // fp32 scratch [B*H*m*m] / [B*m*m] (Gram, attention S / dP)
   void* tA = nullptr;       // dtype scratch [B * m * d * 3] (dT, dQKV, ...)
   void* tB = nullptr;       // dtype scratch [B * m * d]
@@ -465,11 +466,13 @@ static dhen_status tokmix_fwd(dhen_ctx* c, const void* T, int m, const void* W, 
 // ... dgrad on `st`, wgrad on `sw` with workspace `wsw` (the weight-gradient side stream, or st itself)
 static dhen_status tokmix_bwd(dhen_ctx* c, const void* T, int m, const void* W, int l, const void* dU, int64_t ldu,
                               void* dT, int dT_dt, int acc, float* gW, int B, cudaStream_t st, cudaStream_t sw = nullptr,
-                              const Workspace* wsw = nullptr) {
+                              const Workspace* wsw = nullptr, const void* resid = nullptr) {
   const int d = c->d, dt = c->dt;
-  // per-sample batched: dT_b = W dU_b (M = m rows i, N = d, K = l), row-major output
+  // per-sample batched: dT_b = W dU_b (M = m rows i, N = d, K = l), row-major output; with `resid` (the
+  // identity shortcut's dR, same [B][m][d] layout) it is the first writer: dT = resid + W dU_b
   Gemm g = mk(m, d, l, B, operand(W, dt, l, 1), operand(dU, dt, 1, d, ldu), view(dT, dT_dt, d, 1, (int64_t)m * d));
-  g.e.accumulate = acc;
+  g.e.accumulate = resid ? 0 : acc;
+  if (resid) g.e.resid = view((void*)resid, dt, d, 1, (int64_t)m * d);
   RET(G_(g, c, st, "tokmix.dgrad"));
   Gemm gw = mk(m, l, B * d, 1, operand(T, dt, d, 1, 0, 0, 1, d, (int64_t)m * d),
                operand(dU, dt, d, 1, 0, 0, 1, d, ldu), view(gW, F32, l, 1));
@@ -762,7 +765,27 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   const int64_t rows = (int64_t)B * mi;
   float* acc = c->dXacc;
   // B2: LN backward; identity shortcut (B3) initialises the dX accumulator
-  KT("layer.ln_bwd", 0, (double)B * mo * d * (3 * es + 4), ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc, Lr.Wn >= 0 ? 0 : 1,
+  // B3 identity shortcut: dX starts as dR.  When the first module's first dX-writing GEMM can add dR in its
+  // epilogue (Dot: Gram backward, DCN: dT, Linear: token dgrad, MLP: fc1 dgrad) it initialises the fp32
+  // accumulator itself and LN backward does not write it (one fp32 write + one read-modify-write saved).
+  // Module order of the backward: the best first-writer candidate goes first (its epilogue adds dR most
+  // cheaply: DCN > Linear > MLP > Dot), the others follow in declaration order (a fixed order: deterministic).
+  std::vector<Mod*> order;
+  {
+    int best = -1, best_rank = 99;
+    const int rank_of[6] = {3 /*DOT*/, 99 /*ATTN*/, 99 /*CONV*/, 0 /*DCN*/, 1 /*LINEAR*/, 2 /*MLP*/};
+    for (int i = 0; i < (int)Lr.mods.size(); ++i) {
+      const int rk = rank_of[Lr.mods[i].s.kind];
+      if (rk < best_rank) { best_rank = rk; best = i; }
+    }
+    if (best >= 0 && c->first_writer) order.push_back(&Lr.mods[best]);
+    for (int i = 0; i < (int)Lr.mods.size(); ++i)
+      if (!(c->first_writer && i == best)) order.push_back(&Lr.mods[i]);
+  }
+  const int first_kind = order.empty() ? -1 : order[0]->s.kind;
+  const bool first_dR = c->first_writer && Lr.Wn < 0 && mi == mo &&
+                        (first_kind == DHEN_DOT || first_kind == DHEN_DCN || first_kind == DHEN_LINEAR || first_kind == DHEN_MLP);
+  KT("layer.ln_bwd", 0, (double)B * mo * d * (3 * es + (first_dR ? 0 : 4)), ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc, (Lr.Wn >= 0 || first_dR) ? 0 : 1,
             gp(Lr.gamma), gp(Lr.beta), c->red, c->red_bytes, st));
   if (Lr.Wn >= 0)   // B3: dX = W_n dR ; dW_n += sum_b X_b dR_b^T
     RET(tokmix_bwd(c, X, mi, p(Lr.Wn), mo, c->dR, ldU, acc, F32, 0, gp(Lr.Wn), B, st));
@@ -781,9 +804,13 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
     if (sd != st) { CK(cudaEventRecord(c->ev_sj, sd)); CK(cudaStreamWaitEvent(st, c->ev_sj, 0)); }
     return DHEN_OK;
   };
-  for (Mod& md : Lr.mods) {
+  bool first_mod = true;
+  for (Mod* mdp : order) {
+    Mod& md = *mdp;
     const int l = md.s.l;
     char* dU = (char*)c->dR + (int64_t)md.off_tok * d * es;
+    const bool take_dR = first_dR && first_mod;   // this module's first dX write adds the shortcut's dR
+    first_mod = false;
     switch (md.s.kind) {
       case DHEN_DOT: {   // B5
         const int h = mi * (mi - 1) / 2;
@@ -802,13 +829,14 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
                       : mk(mi, d, mi, B, operand(c->tD, dt, mi, 1, (int64_t)mi * mi), operand(X, dt, 1, d, (int64_t)mi * d),
                            view(acc, F32, d, 1, (int64_t)mi * d));
         gx.e.accumulate = 1;
+        if (take_dR) { gx.e.accumulate = 0; gx.e.resid = gx.c; gx.e.resid.ptr = c->dR; gx.e.resid.dt = dt; }
         RET(G_(gx, c, st, "dot.gram_bwd"));
         RET(join());
         break;
       }
       case DHEN_LINEAR:
         RET(fork());
-        RET(tokmix_bwd(c, X, mi, p(md.W), l, dU, ldU, acc, F32, 1, gp(md.W), B, st, sd, ws2));
+        RET(tokmix_bwd(c, X, mi, p(md.W), l, dU, ldU, acc, F32, 1, gp(md.W), B, st, sd, ws2, take_dR ? c->dR : nullptr));
         RET(join());
         break;
       case DHEN_DCN: {   // B8
@@ -835,6 +863,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
           gt.e.cross = view((void*)X, dt, d, 1, (int64_t)spt * mi * d);
           gt.e.mask = view(md.A, dt, d, 1, (int64_t)spt * mi * d);
           gt.e.aux = view(dA, dt, d, 1, (int64_t)spt * mi * d);
+          if (take_dR) gt.e.resid = view(c->dR, dt, d, 1, (int64_t)spt * mi * d);
           RET(G_(gt, c, st, "dcn.dT_fused"));
         } else {
         // m < 128: as its transpose dT_b^T = dU_b^T W_u^T (M = d rows fill the MMA tile), C column-contiguous
@@ -848,6 +877,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         gt.e.cross = view((void*)X, dt, vr, vc, (int64_t)mi * d);
         gt.e.mask = view(md.A, dt, vr, vc, (int64_t)mi * d);
         gt.e.aux = view(dA, dt, vr, vc, (int64_t)mi * d);
+        if (take_dR) gt.e.resid = view(c->dR, dt, vr, vc, (int64_t)mi * d);
         RET(G_(gt, c, st, "dcn.dT_fused"));
         }
         if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dA ready
@@ -973,6 +1003,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         KTS(sd, "mlp.bias_grad", 0, (double)B * h1 * es, colsum_add(dh1, dt, B, h1, h1, gp(md.b1), red2, c->red_bytes, sd));
         Gemm gx = mk(B, K1, h1, 1, operand(dh1, dt, h1, 1), operand(p(md.W1), dt, 1, K1), view(acc, F32, K1, 1));
         gx.e.accumulate = 1;
+        if (take_dR) { gx.e.accumulate = 0; gx.e.resid = view(c->dR, dt, K1, 1); }
         RET(G_(gx, c, st, "mlp.fc1_dgrad"));
         RET(join());
         break;
@@ -1021,6 +1052,7 @@ static dhen_status make_ctx(const dhen_config* cfg, const dhen_dist* dist, dhen_
   { const char* e = getenv("DHEN_TR_SMALL_M"); c->tr_small_m = e ? atoi(e) : 0; }
   { const char* e = getenv("DHEN_LN_FUSE"); c->ln_fuse = e ? atoi(e) : 1; }
   { const char* e = getenv("DHEN_RELU_BITS"); c->relu_bits = e ? atoi(e) : 1; }
+  { const char* e = getenv("DHEN_FIRST_WRITER"); c->first_writer = e ? atoi(e) : 1; }
   if (c->cfg.ln_eps <= 0.f) c->cfg.ln_eps = 1e-5f;
   c->mods_cfg.resize(cfg->n_layers);
   c->layers_cfg.resize(cfg->n_layers);
