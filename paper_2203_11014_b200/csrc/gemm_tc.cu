@@ -101,15 +101,20 @@ static bool make_map(CUtensorMap* map, OpMap* om, const Operand& o, int rows, in
   return res == CUDA_SUCCESS;
 }
 
-static bool same_geom(const View& a, const View& c) {
+static bool same_geom(const View& a, const View& c, bool allow_f32 = false) {
   return !a.ptr || (a.rs == c.rs && a.cs == c.cs && a.bs0 == c.bs0 && a.bs1 == c.bs1 && a.zdiv == c.zdiv &&
-                    a.rdiv == c.rdiv && a.rs_o == c.rs_o && a.dt == BF16);
+                    a.rdiv == c.rdiv && a.rs_o == c.rs_o && (a.dt == BF16 || (allow_f32 && a.dt == F32)));
 }
 // Resolve the epilogue to a Lean plan: all present views share C's geometry, operands other than C
 // are bf16, and row-major outputs have N % 4 == 0 with 4-element-aligned rows (vector accesses).
 static bool make_lean(const Gemm& g, Lean* e) {
   const Epilogue& x = g.e;
-  if (!same_geom(x.cross, g.c) || !same_geom(x.aux, g.c) || !same_geom(x.mask, g.c) || !same_geom(x.resid, g.c))
+  // an fp32 residual is the dX accumulator read by its last writer (bf16 C, no other fused operand)
+  const bool r32 = x.resid.ptr && x.resid.dt == F32;
+  if (r32 && (g.c.dt != BF16 || x.cross.ptr || x.mask.ptr || x.aux.ptr || x.bias || x.accumulate || x.relu ||
+              x.dcn_bwd || x.triu_m || x.ln_gamma || x.bits_mode))
+    return false;
+  if (!same_geom(x.cross, g.c) || !same_geom(x.aux, g.c) || !same_geom(x.mask, g.c) || !same_geom(x.resid, g.c, r32))
     return false;
   if (x.bias && x.bias_dt != BF16) return false;
   if (g.c.cs == 1 && !x.triu_m && (g.N % 4 || g.c.rs % 4 || g.c.bs0 % 4 || g.c.bs1 % 4 || g.c.rs_o % 4)) return false;
@@ -126,7 +131,7 @@ static bool make_lean(const Gemm& g, Lean* e) {
   e->gap_lo = x.bias_gap_lo; e->gap_hi = x.bias_gap_hi; e->hi_off = x.bias_hi_off;
   e->flags = (x.accumulate ? EF_ACC : 0) | (x.relu ? EF_RELU : 0) | (x.mask.ptr ? EF_MASK : 0) |
              (x.cross.ptr ? EF_CROSS : 0) | (x.aux.ptr ? EF_AUX : 0) | (x.resid.ptr ? EF_RESID : 0) |
-             (x.bias ? EF_BIAS : 0);
+             (x.bias ? EF_BIAS : 0) | (r32 ? EF_R32 : 0);
   e->ln_gamma = x.ln_gamma; e->ln_beta = x.ln_beta; e->ln_mu = x.ln_mu; e->ln_rstd = x.ln_rstd; e->ln_eps = x.ln_eps;
   e->ln_d = x.ln_d ? x.ln_d : g.N;
   e->bits = x.bits; e->bits_ld = x.bits_ld;

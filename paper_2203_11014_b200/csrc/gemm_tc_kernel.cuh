@@ -41,7 +41,8 @@ struct OpMap {
 // Compact, host-resolved epilogue plan: every present view shares one row geometry
 // (offset = row term + batch term + col * cs), operands other than C are bf16.
 enum { EF_ACC = 1, EF_RELU = 2, EF_MASK = 4, EF_CROSS = 8, EF_AUX = 16, EF_RESID = 32, EF_BIAS = 64,
-       EF_DCNB = 128, EF_TRIU = 256, EF_LN = 512, EF_BITS = 1024, EF_BMASK = 2048 };
+       EF_DCNB = 128, EF_TRIU = 256, EF_LN = 512, EF_BITS = 1024, EF_BMASK = 2048,
+       EF_R32 = 4096 /* the residual view is fp32 (the dX accumulator; its last writer emits bf16 dX) */ };
 struct Lean {
   void* c;
   const void* x;
@@ -483,8 +484,9 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
   constexpr int NR = 32 / RPP;                               // rows per lane in this pass
   // operands to prefetch per row: bf16 uint4 slots (X / A / mask / resid / bf16 C) and fp32 C
   constexpr int NB = ((F & (EF_CROSS | EF_DCNB)) ? 1 : 0) + ((F & (EF_MASK | EF_DCNB)) ? 1 : 0) +
-                     ((F & EF_RESID) ? 1 : 0) + (((F & EF_ACC) && !CF32) ? 1 : 0);
-  constexpr bool F32C = (F & EF_ACC) && CF32;   // DCN backward adds into C with red.global (no load)
+                     (((F & EF_RESID) && !(F & EF_R32)) ? 1 : 0) + (((F & EF_ACC) && !CF32) ? 1 : 0);
+  // fp32 operand per row: C itself (+=, fp32 C) or an fp32 residual (EF_R32); DCN backward adds with red.global
+  constexpr bool F32C = ((F & EF_ACC) && CF32) || ((F & EF_R32) != 0);
   constexpr int REGS = NB * 4 + (F32C ? 8 : 0);               // registers per prefetched row
   constexpr int SLX = 0;                                                     // compile-time slot indices
   constexpr int SLM = SLX + ((F & (EF_CROSS | EF_DCNB)) ? 1 : 0);
@@ -526,7 +528,7 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
           ub[buf][k][SLR] = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.resid + o[buf][k]));
         if constexpr ((F & EF_ACC) != 0 && !CF32)
           ub[buf][k][SLC] = __ldcg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.c + o[buf][k]));
-        if constexpr (F32C) ldg_c8<true>(e.c, o[buf][k], cv[buf][k]);
+        if constexpr (F32C) ldg_c8<true>((F & EF_R32) ? e.resid : e.c, o[buf][k], cv[buf][k]);
       }
     }
   };
@@ -614,7 +616,10 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
 #pragma unroll
         for (int t = 0; t < 8; ++t) a[t] = t8[t] > 0.f ? a[t] : 0.f;
       }
-      if constexpr ((F & EF_RESID) != 0) {
+      if constexpr ((F & EF_RESID) != 0 && (F & EF_R32) != 0) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) a[t] += cv[cb][k][t];
+      } else if constexpr ((F & EF_RESID) != 0) {
         unpack_bf8(ub[cb][k][SLR], t8);
 #pragma unroll
         for (int t = 0; t < 8; ++t) a[t] += t8[t];
@@ -651,7 +656,7 @@ __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0,
       const int64_t o = lo + (int64_t)col * e.cs;
       if constexpr (LX) xs[j] = ldg_bf1(e.x, o);
       if constexpr (LM) ms[j] = ldg_bf1(e.mask, o);
-      if constexpr (LR) rv[j] = ldg_bf1(e.resid, o);
+      if constexpr (LR) rv[j] = (F & EF_R32) ? ldg_c1(e.resid, o, 1) : ldg_bf1(e.resid, o);
       if constexpr (LC) cv[j] = ldg_c1(e.c, o, C32);
     }
   }
@@ -702,7 +707,8 @@ __device__ __forceinline__ void lean_rows16(const Lean& e, int64_t lo, int col0,
   X(20, EF_RESID | EF_AUX | EF_LN, false)               \
   X(21, EF_BIAS | EF_RELU | EF_BITS, false)              \
   X(22, EF_BMASK, false)                                 \
-  X(23, EF_DCNB | EF_RESID, true)
+  X(23, EF_DCNB | EF_RESID, true)                       \
+  X(24, EF_RESID | EF_R32, false)
 static inline int lean_variant(int flags, bool cf32) {
 #define LV_ID(id, f, c) if (flags == (f) && cf32 == (c)) return id;
   LEAN_VARIANTS(LV_ID)

@@ -466,13 +466,13 @@ static dhen_status tokmix_fwd(dhen_ctx* c, const void* T, int m, const void* W, 
 // ... dgrad on `st`, wgrad on `sw` with workspace `wsw` (the weight-gradient side stream, or st itself)
 static dhen_status tokmix_bwd(dhen_ctx* c, const void* T, int m, const void* W, int l, const void* dU, int64_t ldu,
                               void* dT, int dT_dt, int acc, float* gW, int B, cudaStream_t st, cudaStream_t sw = nullptr,
-                              const Workspace* wsw = nullptr, const void* resid = nullptr) {
+                              const Workspace* wsw = nullptr, const void* resid = nullptr, int resid_dt = -1) {
   const int d = c->d, dt = c->dt;
   // per-sample batched: dT_b = W dU_b (M = m rows i, N = d, K = l), row-major output; with `resid` (the
   // identity shortcut's dR, same [B][m][d] layout) it is the first writer: dT = resid + W dU_b
   Gemm g = mk(m, d, l, B, operand(W, dt, l, 1), operand(dU, dt, 1, d, ldu), view(dT, dT_dt, d, 1, (int64_t)m * d));
   g.e.accumulate = resid ? 0 : acc;
-  if (resid) g.e.resid = view((void*)resid, dt, d, 1, (int64_t)m * d);
+  if (resid) g.e.resid = view((void*)resid, resid_dt >= 0 ? resid_dt : dt, d, 1, (int64_t)m * d);
   RET(G_(g, c, st, "tokmix.dgrad"));
   Gemm gw = mk(m, l, B * d, 1, operand(T, dt, d, 1, 0, 0, 1, d, (int64_t)m * d),
                operand(dU, dt, d, 1, 0, 0, 1, d, ldu), view(gW, F32, l, 1));
@@ -804,12 +804,18 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
     if (sd != st) { CK(cudaEventRecord(c->ev_sj, sd)); CK(cudaStreamWaitEvent(st, c->ev_sj, 0)); }
     return DHEN_OK;
   };
+  // The last module's last dX-writing GEMM emits dX (layer dtype) = accumulator + its contribution: the fp32
+  // accumulator is read once and never written back, and no cast kernel runs.
+  const int last_kind = order.empty() ? -1 : order.back()->s.kind;
+  const bool last_dX = dX && c->first_writer &&
+                       (last_kind == DHEN_DOT || last_kind == DHEN_DCN || last_kind == DHEN_LINEAR || last_kind == DHEN_MLP);
   bool first_mod = true;
   for (Mod* mdp : order) {
     Mod& md = *mdp;
     const int l = md.s.l;
     char* dU = (char*)c->dR + (int64_t)md.off_tok * d * es;
     const bool take_dR = first_dR && first_mod;   // this module's first dX write adds the shortcut's dR
+    const bool emit_dX = last_dX && mdp == order.back();   // this module's last dX write emits dX
     first_mod = false;
     switch (md.s.kind) {
       case DHEN_DOT: {   // B5
@@ -830,13 +836,22 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
                            view(acc, F32, d, 1, (int64_t)mi * d));
         gx.e.accumulate = 1;
         if (take_dR) { gx.e.accumulate = 0; gx.e.resid = gx.c; gx.e.resid.ptr = c->dR; gx.e.resid.dt = dt; }
+        if (emit_dX) {   // dX = (dR | acc) + S X
+          if (!take_dR) { gx.e.resid = gx.c; }   // fp32 accumulator view
+          gx.e.accumulate = 0;
+          gx.c.ptr = dX; gx.c.dt = dt;
+        }
         RET(G_(gx, c, st, "dot.gram_bwd"));
         RET(join());
         break;
       }
       case DHEN_LINEAR:
         RET(fork());
-        RET(tokmix_bwd(c, X, mi, p(md.W), l, dU, ldU, acc, F32, 1, gp(md.W), B, st, sd, ws2, take_dR ? c->dR : nullptr));
+        if (emit_dX)   // dX = (dR | acc) + W dU
+          RET(tokmix_bwd(c, X, mi, p(md.W), l, dU, ldU, dX, dt, 0, gp(md.W), B, st, sd, ws2,
+                         take_dR ? (const void*)c->dR : (const void*)acc, take_dR ? dt : F32));
+        else
+          RET(tokmix_bwd(c, X, mi, p(md.W), l, dU, ldU, acc, F32, 1, gp(md.W), B, st, sd, ws2, take_dR ? c->dR : nullptr));
         RET(join());
         break;
       case DHEN_DCN: {   // B8
@@ -883,6 +898,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dA ready
         Gemm gx = mk((int)rows, d, d, 1, operand(dA, dt, d, 1), operand(p(md.W), dt, 1, d), view(acc, F32, d, 1));
         gx.e.accumulate = 1;
+        if (emit_dX) { gx.e.accumulate = 0; gx.e.resid = view(acc, F32, d, 1); gx.c = view(dX, dt, d, 1); }   // dX = acc + dA W
         RET(G_(gx, c, st, "dcn.dgrad"));
         Gemm gw = mk(d, d, (int)rows, 1, operand(dA, dt, 1, d), operand(X, dt, 1, d), view(gp(md.W), F32, d, 1));
         gw.e.accumulate = 1;
@@ -1004,13 +1020,18 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         Gemm gx = mk(B, K1, h1, 1, operand(dh1, dt, h1, 1), operand(p(md.W1), dt, 1, K1), view(acc, F32, K1, 1));
         gx.e.accumulate = 1;
         if (take_dR) { gx.e.accumulate = 0; gx.e.resid = view(c->dR, dt, K1, 1); }
+        if (emit_dX) {   // dX = (dR | acc) + dh1 W1
+          if (!take_dR) gx.e.resid = view(acc, F32, K1, 1);
+          gx.e.accumulate = 0;
+          gx.c = view(dX, dt, K1, 1);
+        }
         RET(G_(gx, c, st, "mlp.fc1_dgrad"));
         RET(join());
         break;
       }
     }
   }
-  if (dX) KT("layer.dx_cast", 0, (double)rows * d * (4 + es), cast(acc, F32, dX, dt, rows * d, st));
+  if (dX && !last_dX) KT("layer.dx_cast", 0, (double)rows * d * (4 + es), cast(acc, F32, dX, dt, rows * d, st));
   RET(release(c, n, st));
   RET(reduce_grads(c, n, st));
   return DHEN_OK;
