@@ -105,7 +105,11 @@ __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t cnt) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
 }
+#ifndef DHEN_MBAR_SLEEP
+#define DHEN_MBAR_SLEEP 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+#if DHEN_MBAR_SLEEP
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -115,6 +119,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
       "}\n" ::"r"(a),
       "r"(parity), "r"(0x989680)   // suspend-time hint (ns): sleep until the phase completes instead of spinning
       : "memory");
+#else
+  // no suspend-time hint: try_wait blocks for a hardware-defined window and the loop re-polls, so a waiter
+  // (the MMA issuer above all) resumes as soon as the phase completes
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap* map, const int c[5], uint32_t mbar) {
   asm volatile(
