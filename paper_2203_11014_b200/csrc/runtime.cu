@@ -139,6 +139,8 @@ struct dhen_ctx {
   void* tA = nullptr;       // dtype scratch [B * m * d * 3] (dT, dQKV, ...)
   void* tB = nullptr;       // dtype scratch [B * m * d]
   void* tC = nullptr;       // dtype scratch [B * m * max(f, d)] (dF, dh*)
+  void* tE = nullptr;       // dtype scratch [B * m * d]: attention dO (its own buffer: side-stream readers of dR2)
+  void* tF = nullptr;       // dtype scratch [B * m * 3d]: attention dQKV (its own buffer: side-stream readers of dF)
   void* tD = nullptr;       // dtype scratch [B * H * m * m] (dS, S of Dot bwd)
   void* bdiag = nullptr;    // bf16 [128][128]: blockdiag(W_u, ..) for several samples per 128-row tile
   float* rtmp = nullptr;    // fp32 [B * m * d]
@@ -250,6 +252,9 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   const bool shard = world > 1 && c->dist.fsdp;
   int m = c->cfg.m0, m_max = m, H_mm_max = 0, f_max = d, m_out_max = 0;
   int64_t tC_elems = 0, tA_elems = 0;
+  bool has_attn_any = false;
+  for (int n = 0; n < c->cfg.n_layers; ++n)
+    for (int i = 0; i < c->cfg.layers[n].n_modules; ++i) has_attn_any |= c->cfg.layers[n].modules[i].kind == DHEN_ATTN;
   c->L.assign(c->cfg.n_layers, Layer());
   c->G.assign(c->cfg.n_layers + 1, Group());
   for (int n = 0; n < c->cfg.n_layers; ++n) {
@@ -405,6 +410,10 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   c->tA = work.take((size_t)std::max<int64_t>(tA_elems, (int64_t)rows_d * 3) * es);
   c->tB = work.take(rows_d * es);
   c->tC = work.take((size_t)std::max<int64_t>(tC_elems, 1) * es);
+  if (has_attn_any) {
+    c->tE = work.take(rows_d * es);
+    c->tF = work.take(rows_d * 3 * es);
+  }
   c->tD = work.take((size_t)B * std::max(H_mm_max, 1) * es);
   c->rtmp = (float*)work.take(rows_d * 4);
   c->bdiag = work.take((size_t)128 * 128 * 2);   // block-diagonal token map (DCN backward, m <= 64)
@@ -922,10 +931,24 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         const int64_t s3 = 3 * (int64_t)d;
         char* QKV = (char*)md.QKV;
         void* dT = c->tB;
-        RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st));
+        // weight gradients and bias column sums run on the side stream as their inputs become ready
+        // (dO and dQKV have their own buffers, so nothing the side stream reads is overwritten)
+        auto ready = [&]() -> dhen_status {
+          if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }
+          return DHEN_OK;
+        };
+        RET(fork());
+        RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st, sd, ws2));
         void* dR2 = c->tA;   // [rows, d]
         KT("attn.ln2_bwd", 0, (double)rows * d * 3 * es, ln_bwd(dT, dt, md.R2, md.mu2, md.rs2, p(md.g2), dt, rows, d, dR2, dt, nullptr, 0, gp(md.g2), gp(md.be2), c->red,
                   c->red_bytes, st));
+        RET(ready());   // dR2
+        {
+          Gemm w2 = mk(d, f, (int)rows, 1, operand(dR2, dt, 1, d), operand(md.F, dt, 1, f), view(gp(md.W2), F32, f, 1));
+          w2.e.accumulate = 1;
+          RET(G_(w2, c, sd, "attn.ffn2_wgrad", ws2));
+          KTS(sd, "attn.bias_grad", 0, (double)rows * d * es, colsum_add(dR2, dt, rows, d, d, gp(md.b2), red2, c->red_bytes, sd));
+        }
         void* dF = c->tC;
         Gemm a = mk((int)rows, f, d, 1, operand(dR2, dt, d, 1), operand(p(md.W2), dt, 1, f), view(dF, dt, f, 1));
         if (c->relu_bits && dt == BF16 && f % 64 == 0 && f >= 128) {   // ReLU'(0) = 0 from the forward's bitmask
@@ -934,29 +957,31 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
           a.e.mask = view(md.F, dt, f, 1);
         }
         RET(G_(a, c, st, "attn.ffn2_dgrad"));
-        Gemm w2 = mk(d, f, (int)rows, 1, operand(dR2, dt, 1, d), operand(md.F, dt, 1, f), view(gp(md.W2), F32, f, 1));
-        w2.e.accumulate = 1;
-        RET(G_(w2, c, st, "attn.ffn2_wgrad"));
-        KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dR2, dt, rows, d, d, gp(md.b2), c->red, c->red_bytes, st));
+        RET(ready());   // dF
+        {
+          Gemm w1 = mk(f, d, (int)rows, 1, operand(dF, dt, 1, f), operand(md.Z1, dt, 1, d), view(gp(md.W1), F32, d, 1));
+          w1.e.accumulate = 1;
+          RET(G_(w1, c, sd, "attn.ffn1_wgrad", ws2));
+          KTS(sd, "attn.bias_grad", 0, (double)rows * f * es, colsum_add(dF, dt, rows, f, f, gp(md.b1), red2, c->red_bytes, sd));
+        }
         Gemm z1 = mk((int)rows, d, f, 1, operand(dF, dt, f, 1), operand(p(md.W1), dt, 1, d), view(c->rtmp, F32, d, 1));
         z1.e.resid = view(dR2, dt, d, 1);
         RET(G_(z1, c, st, "attn.ffn1_dgrad"));
-        Gemm w1 = mk(f, d, (int)rows, 1, operand(dF, dt, 1, f), operand(md.Z1, dt, 1, d), view(gp(md.W1), F32, d, 1));
-        w1.e.accumulate = 1;
-        RET(G_(w1, c, st, "attn.ffn1_wgrad"));
-        KT("attn.bias_grad", 0, (double)rows * f * es, colsum_add(dF, dt, rows, f, f, gp(md.b1), c->red, c->red_bytes, st));
         void* dR1 = c->tB;   // dT no longer needed
         KT("attn.ln1_bwd", 0, (double)rows * d * (2 * es + 12), ln_bwd(c->rtmp, F32, md.R1, md.mu1, md.rs1, p(md.g1), dt, rows, d, dR1, dt, acc, 2, gp(md.g1), gp(md.be1),
                   c->red, c->red_bytes, st));
-        void* dO = c->tA;    // dR2 no longer needed
+        RET(ready());   // dR1
+        {
+          Gemm wo = mk(d, d, (int)rows, 1, operand(dR1, dt, 1, d), operand(md.O, dt, 1, d), view(gp(md.Wo), F32, d, 1));
+          wo.e.accumulate = 1;
+          RET(G_(wo, c, sd, "attn.out_wgrad", ws2));
+          KTS(sd, "attn.bias_grad", 0, (double)rows * d * es, colsum_add(dR1, dt, rows, d, d, gp(md.bo), red2, c->red_bytes, sd));
+        }
+        void* dO = c->tE;
         Gemm go = mk((int)rows, d, d, 1, operand(dR1, dt, d, 1), operand(p(md.Wo), dt, 1, d), view(dO, dt, d, 1));
         RET(G_(go, c, st, "attn.out_dgrad"));
-        Gemm wo = mk(d, d, (int)rows, 1, operand(dR1, dt, 1, d), operand(md.O, dt, 1, d), view(gp(md.Wo), F32, d, 1));
-        wo.e.accumulate = 1;
-        RET(G_(wo, c, st, "attn.out_wgrad"));
-        KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dR1, dt, rows, d, d, gp(md.bo), c->red, c->red_bytes, st));
         // attention core backward
-        char* dQKV = (char*)c->tC;   // [rows, 3d]  (dF no longer needed; tC >= rows*f >= rows*3d? checked at plan)
+        char* dQKV = (char*)c->tF;   // [rows, 3d]
         if (attn::fused_ok(dt, B, H, mi, d)) {
           // B6 core fused: S and P recomputed on chip, dV, dP, dS, dQ, dK per (sample, head)
           ProfScope ps(c, "attn.core_bwd", 10.0 * B * H * (double)mi * mi * dh, (double)B * mi * 7 * d * es, st);
@@ -982,14 +1007,18 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
                        view(dQKV + (int64_t)d * es, dt, s3, 1, mi * s3, dh, H));
           RET(G_(dk, c, st, "attn.dk"));
         }
+        RET(ready());   // dQKV
+        {
+          Gemm gw = mk(3 * d, d, (int)rows, 1, operand(dQKV, dt, 1, s3), operand(X, dt, 1, d), view(gp(md.Wq), F32, d, 1));
+          gw.e.accumulate = 1;
+          RET(G_(gw, c, sd, "attn.qkv_wgrad", ws2));
+          KTS(sd, "attn.bias_grad", 0, (double)rows * d * es, colsum_add(dQKV, dt, rows, d, s3, gp(md.bq), red2, c->red_bytes, sd));
+          KTS(sd, "attn.bias_grad", 0, (double)rows * d * es, colsum_add(dQKV + 2 * (int64_t)d * es, dt, rows, d, s3, gp(md.bv), red2, c->red_bytes, sd));
+        }
         Gemm gx = mk((int)rows, d, 3 * d, 1, operand(dQKV, dt, s3, 1), operand(p(md.Wq), dt, 1, d), view(acc, F32, d, 1));
         gx.e.accumulate = 1;
         RET(G_(gx, c, st, "attn.qkv_dgrad"));
-        Gemm gw = mk(3 * d, d, (int)rows, 1, operand(dQKV, dt, 1, s3), operand(X, dt, 1, d), view(gp(md.Wq), F32, d, 1));
-        gw.e.accumulate = 1;
-        RET(G_(gw, c, st, "attn.qkv_wgrad"));
-        KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dQKV, dt, rows, d, s3, gp(md.bq), c->red, c->red_bytes, st));
-        KT("attn.bias_grad", 0, (double)rows * d * es, colsum_add(dQKV + 2 * (int64_t)d * es, dt, rows, d, s3, gp(md.bv), c->red, c->red_bytes, st));
+        RET(join());
         break;
       }
       case DHEN_MLP: {   // B9
