@@ -108,6 +108,20 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(Gemm g, int splits, 
   }
 }
 
+// Split-K reduction for many output elements and few splits: one thread per element, the splits added in
+// index order (deterministic), then the fused epilogue.
+__global__ void __launch_bounds__(256) splitk_reduce_elem_kernel(Gemm g, int splits, const float* ws) {
+  const int64_t mn = (int64_t)g.M * g.N;
+  const int64_t total = (int64_t)g.batch * mn;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t zb = e / mn, r = e - zb * mn;
+    const float* base = ws + zb * splits * mn + r;
+    float v = 0.f;
+    for (int sp = 0; sp < splits; ++sp) v += __ldcs(base + (int64_t)sp * mn);
+    epi_apply(g, (int)zb, (int)(r / g.N), (int)(r % g.N), v);
+  }
+}
+
 cudaError_t gemm_simt(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
   if (g.e.ln_gamma || g.e.bits_mode) return cudaErrorNotSupported;   // tcgen05-path-only epilogues
@@ -141,6 +155,12 @@ cudaError_t gemm_simt(const Gemm& g, const Workspace& ws, cudaStream_t st) {
 
 cudaError_t splitk_reduce(const Gemm& g, int splits, const float* ws, cudaStream_t st) {
   int64_t total = (int64_t)g.batch * g.M * g.N;
+  if (total >= (int64_t)148 * 256 && splits <= 32) {   // enough elements to fill the machine one per thread
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    splitk_reduce_elem_kernel<<<blocks, 256, 0, st>>>(g, splits, ws);
+    ++g_launches;
+    return cudaGetLastError();
+  }
   int blocks = (int)std::min<int64_t>((total + 31) / 32, 148 * 8);
   splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g, splits, ws);
   ++g_launches;

@@ -48,6 +48,8 @@ def shapes(cfg):
          (0, 0), (0, 0), (0, 0), bf),
         ("attn.ffn2", R, d, 4 * d, 1, (4 * d, 1, 0, 0, 1, 0, 0), (4 * d, 1, 0, 0, 1, 0, 0), (d, 1, 0, 0, 1), 0,
          (0, 0), (0, 0), (0, 0), f32),
+        ("mlp.fc2_wgrad", 1024, 1024, 8192, 1, (1, 1024, 0, 0, 1, 0, 0), (1, 1024, 0, 0, 1, 0, 0), (1024, 1, 0, 0, 1), 1,
+         (0, 0), (0, 0), (0, 0), f32),
         # weight gradients (K = B m rows, both operands MN-major, split-K)
         ("attn.ffn1_wgrad", 4 * d, d, R, 1, (1, 4 * d, 0, 0, 1, 0, 0), (1, d, 0, 0, 1, 0, 0), (d, 1, 0, 0, 1), 1,
          (0, 0), (0, 0), (0, 0), f32),
