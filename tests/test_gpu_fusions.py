@@ -1,0 +1,72 @@
+"""A/B tests of the fusions and schedules that are switchable at context creation (env read by dhen_init):
+each variant must reproduce the reference schedule on the same inputs -- bit for bit where the arithmetic
+is the same, within bf16 rounding where a fusion changes where a value is rounded.
+
+DHEN_OVERLAP      weight gradients / module branches on a second stream        -> bitwise identical
+DHEN_LN_FUSE      LayerNorm in the producing GEMM epilogues (F5, F6, F12)      -> same storage points
+DHEN_FIRST_WRITER first / last dX writer (B3, B10) instead of LN-bwd init + cast -> same fp32 sums, other order
+DHEN_RELU_BITS    FFN ReLU derivative from a bitmask                            -> bitwise identical
+"""
+import numpy as np
+import pytest
+
+from oracle import dhen_oracle as O
+from tests.gpu_common import Case, per_tensor
+from tests.helpers import config, norm_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _step(net, B, seed, env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    case = Case(net, B, "bf16", seed=seed)
+    out = case.gpu_step(lr=0.01)
+    for k in env:
+        monkeypatch.delenv(k, raising=False)
+    return out
+
+
+def _cmp(a, b, net, tol):
+    if tol == 0:
+        assert a["loss"] == b["loss"]
+        assert np.array_equal(a["dX0"], b["dX0"])
+        for ga, gb in zip(a["grads"], b["grads"]):
+            assert np.array_equal(ga, gb)
+        return
+    assert abs(a["loss"] - b["loss"]) <= tol * max(1.0, abs(b["loss"]))
+    assert norm_err(a["dX0"], b["dX0"]) <= tol
+    for gi, (ga, gb) in enumerate(zip(a["grads"], b["grads"])):
+        ta, tb = per_tensor(net, gi, ga), per_tensor(net, gi, gb)
+        for k in tb:
+            gated = k.endswith(("W_1", "b_1", "W_2", "b_2")) and (".mlp." in k or ".attn." in k)
+            assert norm_err(ta[k], tb[k]) <= (5e-2 if gated else tol), (gi, k, norm_err(ta[k], tb[k]))
+
+
+def _net(name, layers):
+    net = config(name)
+    return O.NetSpec(net.m0, net.d, net.layers[:layers])
+
+
+@pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2), ("C3", 32, 2), ("C5", 16, 2)])
+def test_side_streams_bitwise(name, B, layers, monkeypatch):
+    net = _net(name, layers)
+    a = _step(net, B, 11, {"DHEN_OVERLAP": "0"}, monkeypatch)
+    b = _step(net, B, 11, {"DHEN_OVERLAP": "1"}, monkeypatch)
+    _cmp(a, b, net, 0)
+
+
+@pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2), ("C5", 16, 2)])
+def test_fused_layernorm_matches_kernel(name, B, layers, monkeypatch):
+    net = _net(name, layers)
+    a = _step(net, B, 12, {"DHEN_LN_FUSE": "0"}, monkeypatch)
+    b = _step(net, B, 12, {"DHEN_LN_FUSE": "1"}, monkeypatch)
+    _cmp(a, b, net, 1e-2)
+
+
+@pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2), ("C5", 16, 2), ("C3", 32, 2)])
+def test_first_last_dx_writer(name, B, layers, monkeypatch):
+    net = _net(name, layers)
+    a = _step(net, B, 13, {"DHEN_FIRST_WRITER": "0"}, monkeypatch)
+    b = _step(net, B, 13, {"DHEN_FIRST_WRITER": "1"}, monkeypatch)
+    _cmp(a, b, net, 1e-2)
