@@ -630,12 +630,15 @@ static int resident_blocks(K kern, int threads, size_t smem) {
   }
   return sms * per;
 }
+#ifndef LNB_UR
+#define LNB_UR 2   // rows per lane segment per iteration of the LayerNorm backward (loads in flight)
+#endif
 static int ln_bwd_grid(int lpr, int dydt) {
   static int cache[2][6] = {{0}};
   const int li = lpr == 4 ? 0 : lpr == 8 ? 1 : lpr == 16 ? 2 : 3, ti = dydt == BF16 ? 0 : 1;
   int& v = cache[ti][li];
   if (!v) {
-#define LG(L, I) if (li == I) v = ti == 0 ? resident_blocks(ln_bwd_r<L, 2, __nv_bfloat16>, 256, 0) : resident_blocks(ln_bwd_r<L, 2, float>, 256, 0);
+#define LG(L, I) if (li == I) v = ti == 0 ? resident_blocks(ln_bwd_r<L, LNB_UR, __nv_bfloat16>, 256, 0) : resident_blocks(ln_bwd_r<L, LNB_UR, float>, 256, 0);
     LG(4, 0) LG(8, 1) LG(16, 2) LG(32, 3)
 #undef LG
   }
@@ -681,7 +684,7 @@ cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu,
                    float* dgamma, float* dbeta, float* scratch, size_t scratch_bytes, cudaStream_t st) {
   const int lpr = ln_lpr(d);
   if (dt == BF16 && pdt == BF16 && lpr >= 4) {
-    const int rpi = (32 / lpr) * 2;
+    const int rpi = (32 / lpr) * LNB_UR;
     int nb = (int)std::min<int64_t>((rows + 8 * rpi - 1) / (8 * rpi), ln_bwd_grid(lpr, dydt));
     nb = (int)std::min<int64_t>(nb, (int64_t)(scratch_bytes / (sizeof(float) * 2 * d)));
     if (nb >= 1) {
@@ -690,10 +693,10 @@ cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu,
 #define LNB2(L)                                                                                                        \
       if (lpr == L) {                                                                                                  \
         if (dydt == BF16)                                                                                              \
-          ln_bwd_r<L, 2, __nv_bfloat16><<<nb, 256, 0, st>>>((const __nv_bfloat16*)dY, (const __nv_bfloat16*)Rsave, mu, \
+          ln_bwd_r<L, LNB_UR, __nv_bfloat16><<<nb, 256, 0, st>>>((const __nv_bfloat16*)dY, (const __nv_bfloat16*)Rsave, mu, \
               rstd, (const __nv_bfloat16*)gamma, rows, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb);               \
         else                                                                                                           \
-          ln_bwd_r<L, 2, float><<<nb, 256, 0, st>>>((const float*)dY, (const __nv_bfloat16*)Rsave, mu, rstd,           \
+          ln_bwd_r<L, LNB_UR, float><<<nb, 256, 0, st>>>((const float*)dY, (const __nv_bfloat16*)Rsave, mu, rstd,           \
               (const __nv_bfloat16*)gamma, rows, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb);                     \
       }
       LNB2(4) LNB2(8) LNB2(16) LNB2(32)
