@@ -243,6 +243,11 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ uint4 lds16_(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ void sts4u(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
@@ -980,6 +985,29 @@ __global__ void __launch_bounds__(320, 1)
         const int gofs = cb0 - seg0;                        // gamma / beta index of column cb0
         const float inv_d = 1.f / (float)e.ln_d;
         const uint32_t bar_id = 2 + q4;
+        // R and Y leave through the warp's staging area (bf16 rows of HC columns, 16-B padded pitch) and are
+        // stored with lanes along columns (coalesced 16-B stores) instead of one row per lane
+        constexpr int PB = HC * 2 + 16;
+        const uint32_t stgw = smem_u32(stage_all) + (uint32_t)((warp - 2) * 32 * SROW * 4);
+        static_assert(32 * PB <= 32 * SROW * 4, "LN staging fits the warp's staging area");
+        auto stage8 = [&](int col, const float* vals) {   // 8 values of this lane's row at warp-local column col
+          sts4u(stgw + (uint32_t)(lane * PB + col * 2), pack_bf2(vals[0], vals[1]), pack_bf2(vals[2], vals[3]),
+                pack_bf2(vals[4], vals[5]), pack_bf2(vals[6], vals[7]));
+        };
+        auto flush = [&](void* base) {   // staged 32 x HC block -> rows rbase.., columns cb0..
+          __syncwarp();
+          constexpr int LPRr = HC / 8, RPI = 32 / LPRr;
+          const int cl = lane % LPRr, sr = lane / LPRr;
+#pragma unroll 4
+          for (int r0 = 0; r0 < 32; r0 += RPI) {
+            const int r = r0 + sr;
+            const int64_t orow = shfl64(ro, r);
+            const uint4 u = lds16_(stgw + (uint32_t)(r * PB + cl * 16));
+            if (rbase + r < g.M)
+              *reinterpret_cast<uint4*>((__nv_bfloat16*)base + orow + cb0 + cl * 8) = u;
+          }
+          __syncwarp();
+        };
         float s1 = 0.f;
 #pragma unroll
         for (int c = 0; c < HC; c += 32) {   // unrolled: rpre is indexed with compile-time offsets
@@ -999,12 +1027,11 @@ __global__ void __launch_bounds__(320, 1)
           float f[32];
 #pragma unroll
           for (int q = 0; q < 32; ++q) { f[q] = __uint_as_float(v[q]) * e.alpha + bv[q] + rv[q]; s1 += f[q]; }
-          if (rok) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) stg8<false>(e.aux, ro + cb0 + c + 8 * q, f + 8 * q);
-          }
+          for (int q = 0; q < 4; ++q) stage8(c + 8 * q, f + 8 * q);
           tmem_st32f(tq + c, f);
         }
+        flush(e.aux);   // R
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         if (xch_mode) {
           xch[hh * 32 + lane] = s1;
@@ -1053,11 +1080,10 @@ __global__ void __launch_bounds__(320, 1)
           float y[32];
 #pragma unroll
           for (int q = 0; q < 32; ++q) y[q] = (__uint_as_float(v[q]) - mean) * rs * gv[q] + be[q];
-          if (rok) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) stg8<false>(e.c, ro + cb0 + c + 8 * q, y + 8 * q);
-          }
+          for (int q = 0; q < 4; ++q) stage8(c + 8 * q, y + 8 * q);
         }
+        flush(e.c);     // Y
         continue;
       }
       if constexpr (VAR > 0 && ((VarF<VAR>::F & ~TS_FLAGS) == 0) && (!(VarF<VAR>::F & EF_ACC) || VarF<VAR>::C)) {
