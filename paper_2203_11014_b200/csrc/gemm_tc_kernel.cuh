@@ -947,20 +947,42 @@ __global__ void __launch_bounds__(320, 1)
       decode(item, m0, n0, z, sp, kb0, nk);
       const int ab = li & 1;
       const uint32_t aph = (li >> 1) & 1;
-      // LayerNorm epilogue: this thread's residual row slice (HC bf16) is loaded BEFORE the accumulator is
-      // ready, so its latency hides under the tile's MMAs (it is the epilogue's only global read)
+      // LayerNorm epilogue: the warp's residual block (32 rows x HC bf16) is loaded BEFORE the accumulator is
+      // ready -- with lanes along columns (coalesced 16-B loads) into the warp's staging area, where pass 1
+      // reads its row back and overwrites it with R -- so its latency hides under the tile's MMAs
       constexpr bool LNV = VAR > 0 && (VarF<VAR>::F & EF_LN) != 0;
+      // (measured: the coalesced staging pre-load wins when a warp half is a whole LN segment, ln_d == HC;
+      // with the warp-pair exchange, ln_d == BN, a per-row register prefetch is faster)
+      const bool ln_stage_x = LNV && e.ln_d == HC;
       uint4 rpre[LNV ? HC / 8 : 1];
-      if constexpr (LNV) {
+      if (LNV && !ln_stage_x) {
         const int row_ = m0 + (int)crank * BM + q4 * 32 + lane;
         if (row_ < g.M) {
           const __nv_bfloat16* rp = (const __nv_bfloat16*)e.resid + lean_row(e, z, row_) + n0 + hh * HC;
 #pragma unroll
-          for (int q = 0; q < HC / 8; ++q) rpre[q] = __ldg(reinterpret_cast<const uint4*>(rp) + q);
+          for (int q = 0; q < (LNV ? HC / 8 : 1); ++q) rpre[q] = __ldg(reinterpret_cast<const uint4*>(rp) + q);
         } else {
 #pragma unroll
-          for (int q = 0; q < HC / 8; ++q) rpre[q] = make_uint4(0u, 0u, 0u, 0u);
+          for (int q = 0; q < (LNV ? HC / 8 : 1); ++q) rpre[q] = make_uint4(0u, 0u, 0u, 0u);
         }
+      }
+      if (ln_stage_x) {
+        constexpr int PBr = HC * 2 + 16, LPRr = HC / 8, RPIr = 32 / LPRr;
+        const uint32_t stgw_ = smem_u32(stage_all) + (uint32_t)((warp - 2) * 32 * SROW * 4);
+        const int row_ = m0 + (int)crank * BM + q4 * 32 + lane;
+        const int64_t my_ro = row_ < g.M ? lean_row(e, z, row_) : 0;
+        const int cl = lane % LPRr, sr = lane / LPRr;
+        __syncwarp();   // the previous tile's Y flush has read the staging area
+#pragma unroll 4
+        for (int r0 = 0; r0 < 32; r0 += RPIr) {
+          const int r = r0 + sr;
+          const int64_t orow = shfl64(my_ro, r);
+          uint4 u = make_uint4(0u, 0u, 0u, 0u);
+          if (m0 + (int)crank * BM + q4 * 32 + r < g.M)
+            u = __ldg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)e.resid + orow + n0 + hh * HC + cl * 8));
+          sts4u(stgw_ + (uint32_t)(r * PBr + cl * 16), u.x, u.y, u.z, u.w);
+        }
+        __syncwarp();
       }
       mbar_wait(smem_u32(tfull + ab), aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -1015,7 +1037,8 @@ __global__ void __launch_bounds__(320, 1)
           ld_tmem32(tq + c, v);
           float rv[32], bv[32];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) unpack_bf8(rpre[c / 8 + q], rv + 8 * q);   // prefetched residual
+          for (int q = 0; q < 4; ++q)
+            unpack_bf8(ln_stage_x ? lds16_(stgw + (uint32_t)(lane * PB + (c + 8 * q) * 2)) : rpre[c / 8 + q], rv + 8 * q);
           if constexpr ((F & EF_BIAS) != 0) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) ldg_bf8(e.bias, cb0 + c + 8 * q, bv + 8 * q);
