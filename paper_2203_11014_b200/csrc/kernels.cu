@@ -34,17 +34,25 @@ cudaError_t triu_extract(const float* G, void* Z, int dt, int B, int m, int64_t 
 // One block per sample: the packed triangle (h values, contiguous) is staged in shared memory, then the m x m
 // matrix is written row-major with 8-element vector stores (m % 8 == 0) or scalars.
 __global__ void __launch_bounds__(256) sym_from_triu_k(const void* dZ, void* S, int dt, int m, int64_t ldz) {
-  extern __shared__ float tri[];
+  extern __shared__ float tri[];          // [h] triangle values, then [m] row bases
   const int h = m * (m - 1) / 2;
+  int* rb = reinterpret_cast<int*>(tri + h);   // rb[i] + j = index of pair (i, j > i)
   const int b = blockIdx.x;
-  for (int p = threadIdx.x; p < h; p += blockDim.x) tri[p] = ld_as_f32(dZ, (int64_t)b * ldz + p, dt);
+  if (dt == BF16 && (ldz % 8) == 0 && (h % 8) == 0) {   // 16-B loads of 8 bf16
+    const uint4* src = reinterpret_cast<const uint4*>((const __nv_bfloat16*)dZ + (int64_t)b * ldz);
+    for (int q = threadIdx.x; q < h / 8; q += blockDim.x) {
+      const uint4 u = __ldg(src + q);
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) { tri[8 * q + 2 * t] = __uint_as_float(w[t] << 16); tri[8 * q + 2 * t + 1] = __uint_as_float(w[t] & 0xffff0000u); }
+    }
+  } else {
+    for (int p = threadIdx.x; p < h; p += blockDim.x) tri[p] = ld_as_f32(dZ, (int64_t)b * ldz + p, dt);
+  }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) rb[i] = i * m - i * (i + 1) / 2 - i - 1;
   __syncthreads();
   const int64_t base = (int64_t)b * m * m;
-  auto val = [&](int i, int j) -> float {
-    if (i == j) return 0.f;
-    const int a = min(i, j), c = max(i, j);
-    return tri[a * m - a * (a + 1) / 2 + (c - a - 1)];
-  };
+  auto val = [&](int i, int j) -> float { return j > i ? tri[rb[i] + j] : (j < i ? tri[rb[j] + i] : 0.f); };
   if (dt == BF16 && (m % 8) == 0) {
     const int cpr = m / 8;
     for (int q = threadIdx.x; q < m * cpr; q += blockDim.x) {
@@ -62,7 +70,7 @@ __global__ void __launch_bounds__(256) sym_from_triu_k(const void* dZ, void* S, 
   }
 }
 cudaError_t sym_from_triu(const void* dZ, void* S, int dt, int B, int m, int64_t ldz, cudaStream_t st) {
-  const size_t sm = (size_t)m * (m - 1) / 2 * sizeof(float);
+  const size_t sm = ((size_t)m * (m - 1) / 2 + m) * sizeof(float);
   if (sm > 200 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 48 * 1024;
   if (sm > attr) {
@@ -1794,6 +1802,35 @@ cudaError_t sgd_cast(float* master, const float* grad, float lr, void* copy, int
   } else {
     sgd_cast_k<<<nblocks(n), 256, 0, st>>>(master, grad, lr, copy, dt, n);
   }
+  ++g_launches;
+  return cudaGetLastError();
+}
+// Multi-tensor SGD: every parameter group of the step in ONE launch (segments concatenated in 4-element units)
+__global__ void __launch_bounds__(256) sgd_multi_k(SgdSegs segs, float lr) {
+  int64_t tot = 0;
+  for (int s = 0; s < segs.n; ++s) tot += segs.n4[s];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int s = 0;
+    int64_t u = t;
+    while (u >= segs.n4[s]) { u -= segs.n4[s]; ++s; }
+    float4* master = reinterpret_cast<float4*>(segs.master[s]);
+    float4 v = master[u];
+    const float4 g = reinterpret_cast<const float4*>(segs.grad[s])[u];
+    v.x -= lr * g.x; v.y -= lr * g.y; v.z -= lr * g.z; v.w -= lr * g.w;
+    master[u] = v;
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    reinterpret_cast<uint2*>(segs.copy[s])[u] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+}
+cudaError_t sgd_multi(const SgdSegs& segs, float lr, cudaStream_t st) {
+  int64_t tot = 0;
+  for (int s = 0; s < segs.n; ++s) {
+    if ((uintptr_t)segs.master[s] % 16 || (uintptr_t)segs.grad[s] % 16 || (uintptr_t)segs.copy[s] % 8)
+      return cudaErrorInvalidValue;
+    tot += segs.n4[s];
+  }
+  if (tot == 0) return cudaSuccess;
+  sgd_multi_k<<<nblocks(tot, 256, 148 * 16), 256, 0, st>>>(segs, lr);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -58,6 +58,15 @@ cudaError_t blockdiag_t(const void* W, int m, int l, int spt, void* out, cudaStr
 // SGD (R18): master -= lr * grad; copy = (dt) master.  lr == 0 with grad == NULL: refresh copy only.
 cudaError_t sgd_cast(float* master, const float* grad, float lr, void* copy, int dt, int64_t n, cudaStream_t st);
 cudaError_t cast(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t st);
+// multi-tensor SGD (bf16 compute copies): segment s = n4[s] float4 groups of master / grad / copy (<= 32 segments)
+struct SgdSegs {
+  int n;
+  float* master[32];
+  const float* grad[32];
+  void* copy[32];
+  int64_t n4[32];
+};
+cudaError_t sgd_multi(const SgdSegs& segs, float lr, cudaStream_t st);
 // parameter init: uniform(-bound, bound) from a counter-based hash of (seed, index), or a constant.
 // element i gets the value of tensor index idx0 + i (sharded init gives the same tensor at any world size)
 cudaError_t init_uniform(float* p, int64_t n, float bound, unsigned long long seed, unsigned long long stream_id,

@@ -1429,9 +1429,26 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
   }
   RET(join_comm(c, st));
   // B12: SGD on the (local shard of the) fp32 masters, refresh the compute copy
-  for (auto& g : c->G) {
-    const float* gr = c->dist.world > 1 ? g.gshard : g.grad;
-    KT("sgd", 0, (double)g.shard * (12 + c->es), sgd_cast(g.master, gr, lr, g.comp, c->dt, g.shard, st));
+  bool multi = c->dt == BF16 && c->G.size() <= 32;
+  for (auto& g : c->G) multi = multi && g.shard % 4 == 0;
+  if (multi) {   // every group in one launch
+    SgdSegs segs;
+    segs.n = 0;
+    double bytes = 0;
+    for (auto& g : c->G) {
+      segs.master[segs.n] = g.master;
+      segs.grad[segs.n] = c->dist.world > 1 ? g.gshard : g.grad;
+      segs.copy[segs.n] = g.comp;
+      segs.n4[segs.n] = g.shard / 4;
+      ++segs.n;
+      bytes += (double)g.shard * (12 + c->es);
+    }
+    KT("sgd", 0, bytes, sgd_multi(segs, lr, st));
+  } else {
+    for (auto& g : c->G) {
+      const float* gr = c->dist.world > 1 ? g.gshard : g.grad;
+      KT("sgd", 0, (double)g.shard * (12 + c->es), sgd_cast(g.master, gr, lr, g.comp, c->dt, g.shard, st));
+    }
   }
   RET(fence_params(c, st));
   CK(cudaGetLastError());
