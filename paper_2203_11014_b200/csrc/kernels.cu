@@ -4,6 +4,7 @@
 // reduction is a fixed-order two-pass (deterministic).
 #include "kernels.h"
 #include <algorithm>
+#include <type_traits>
 
 namespace dhen {
 
@@ -542,21 +543,45 @@ __global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const
   ld8b(gamma + c, g);
 #pragma unroll
   for (int t = 0; t < 8; ++t) { pg[t] = 0.f; pb[t] = 0.f; }
-  for (int64_t r0 = rb0 + (int64_t)w * RPI; r0 < rb1; r0 += 8 * RPI) {
+  // raw operands of one iteration (bf16 dY and R as 16-B words): the next iteration's are loaded while this
+  // one is computed (software pipelining: two iterations of loads in flight per warp)
+  constexpr bool RAWP = std::is_same<TD, __nv_bfloat16>::value;
+  uint4 ry[2][UR], rx[2][UR];
+  float rm[2][UR], rq[2][UR];
+  auto fetch = [&](int64_t r0_, int bsl) {
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      const int64_t r = r0_ + u * RPW + sub;
+      if (r < rb1) {
+        if constexpr (RAWP) ry[bsl][u] = __ldg(reinterpret_cast<const uint4*>(dY + r * d + c));
+        rx[bsl][u] = __ldg(reinterpret_cast<const uint4*>(Rsave + r * d + c));
+        rm[bsl][u] = mu[r];
+        rq[bsl][u] = rstd[r];
+      } else {
+        ry[bsl][u] = make_uint4(0u, 0u, 0u, 0u); rx[bsl][u] = make_uint4(0u, 0u, 0u, 0u);
+        rm[bsl][u] = 0.f; rq[bsl][u] = 0.f;
+      }
+    }
+  };
+  auto body = [&](int64_t r0, auto BSC) {
+    constexpr int BS = decltype(BSC)::value;
+    if (r0 + 8 * RPI < rb1) fetch(r0 + 8 * RPI, BS ^ 1);   // next iteration's operands in flight
     float dy[UR][8], x[UR][8], mr[UR], rr[UR];
 #pragma unroll
-    for (int u = 0; u < UR; ++u) {   // every load of the iteration issued before the first use
+    for (int u = 0; u < UR; ++u) {
       const int64_t r = r0 + u * RPW + sub;
-      if (r < rb1) {
-        ld8<TD>(dY + r * d + c, dy[u]);
-        ld8b(Rsave + r * d + c, x[u]);
-        mr[u] = mu[r];
-        rr[u] = rstd[r];
+      if constexpr (RAWP) {
+        VIO<8, __nv_bfloat16>::ld(reinterpret_cast<const __nv_bfloat16*>(&ry[BS][u]), dy[u]);
       } else {
+        if (r < rb1) ld8<TD>(dY + r * d + c, dy[u]);
+        else {
 #pragma unroll
-        for (int t = 0; t < 8; ++t) { dy[u][t] = 0.f; x[u][t] = 0.f; }
-        mr[u] = 0.f; rr[u] = 0.f;
+          for (int t = 0; t < 8; ++t) dy[u][t] = 0.f;
+        }
       }
+      VIO<8, __nv_bfloat16>::ld(reinterpret_cast<const __nv_bfloat16*>(&rx[BS][u]), x[u]);
+      mr[u] = rm[BS][u];
+      rr[u] = rq[BS][u];
     }
 #pragma unroll
     for (int u = 0; u < UR; ++u) {
@@ -603,6 +628,12 @@ __global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const
         }
       }
     }
+    };
+  const int64_t rs0 = rb0 + (int64_t)w * RPI;
+  if (rs0 < rb1) fetch(rs0, 0);
+  for (int64_t r0 = rs0; r0 < rb1; r0 += 16 * RPI) {   // two iterations per trip: buffer indices compile-time
+    body(r0, std::integral_constant<int, 0>{});
+    if (r0 + 8 * RPI < rb1) body(r0 + 8 * RPI, std::integral_constant<int, 1>{});
   }
   // dgamma / dbeta: lanes with equal columns (xor offsets >= LPR), then the 8 warps in order
 #pragma unroll
