@@ -545,20 +545,27 @@ __global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const
   for (int t = 0; t < 8; ++t) { pg[t] = 0.f; pb[t] = 0.f; }
   // raw operands of one iteration (bf16 dY and R as 16-B words): the next iteration's are loaded while this
   // one is computed (software pipelining: two iterations of loads in flight per warp)
-  constexpr bool RAWP = std::is_same<TD, __nv_bfloat16>::value;
-  uint4 ry[2][UR], rx[2][UR];
+  constexpr bool RAWP = true;   // bf16 dY: one 16-B word; fp32 dY: two (ry, ry2)
+  constexpr bool F32DY = std::is_same<TD, float>::value;
+  uint4 ry[2][UR], rx[2][UR], ry2[2][F32DY ? UR : 1];
   float rm[2][UR], rq[2][UR];
   auto fetch = [&](int64_t r0_, int bsl) {
 #pragma unroll
     for (int u = 0; u < UR; ++u) {
       const int64_t r = r0_ + u * RPW + sub;
       if (r < rb1) {
-        if constexpr (RAWP) ry[bsl][u] = __ldg(reinterpret_cast<const uint4*>(dY + r * d + c));
+        if constexpr (F32DY) {
+          ry[bsl][u] = __ldcs(reinterpret_cast<const uint4*>(dY + r * d + c));
+          ry2[bsl][u] = __ldcs(reinterpret_cast<const uint4*>(dY + r * d + c) + 1);
+        } else {
+          ry[bsl][u] = __ldg(reinterpret_cast<const uint4*>(dY + r * d + c));
+        }
         rx[bsl][u] = __ldg(reinterpret_cast<const uint4*>(Rsave + r * d + c));
         rm[bsl][u] = mu[r];
         rq[bsl][u] = rstd[r];
       } else {
         ry[bsl][u] = make_uint4(0u, 0u, 0u, 0u); rx[bsl][u] = make_uint4(0u, 0u, 0u, 0u);
+        if constexpr (F32DY) ry2[bsl][u] = make_uint4(0u, 0u, 0u, 0u);
         rm[bsl][u] = 0.f; rq[bsl][u] = 0.f;
       }
     }
@@ -570,7 +577,12 @@ __global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const
 #pragma unroll
     for (int u = 0; u < UR; ++u) {
       const int64_t r = r0 + u * RPW + sub;
-      if constexpr (RAWP) {
+      if constexpr (F32DY) {
+        const uint4 a = ry[BS][u], b = ry2[BS][u];
+        dy[u][0] = __uint_as_float(a.x); dy[u][1] = __uint_as_float(a.y); dy[u][2] = __uint_as_float(a.z);
+        dy[u][3] = __uint_as_float(a.w); dy[u][4] = __uint_as_float(b.x); dy[u][5] = __uint_as_float(b.y);
+        dy[u][6] = __uint_as_float(b.z); dy[u][7] = __uint_as_float(b.w);
+      } else if constexpr (RAWP) {
         VIO<8, __nv_bfloat16>::ld(reinterpret_cast<const __nv_bfloat16*>(&ry[BS][u]), dy[u]);
       } else {
         if (r < rb1) ld8<TD>(dY + r * d + c, dy[u]);
