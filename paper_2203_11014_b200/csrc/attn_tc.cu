@@ -174,6 +174,7 @@ __device__ __forceinline__ void store_acc_row(uint32_t taddr, __nv_bfloat16* dst
 // TMEM (256 cols): S [0, 128), O [128, 128 + DH).
 template <int DH>
 __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant__ CUtensorMap qkv, const __grid_constant__ Params p) {
+  pdl_release();
   constexpr int NCH = DH / 64;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tslot;
+  pdl_wait();   // prerequisites complete (setup above overlapped the previous kernel's tail)
   const int H = p.H, d = p.d;
 
   if (warp == 0) {
@@ -270,6 +272,7 @@ template <int DH>
 __global__ void __launch_bounds__(192, DH == 64 ? 2 : 1) attn_bwd_kernel(const __grid_constant__ CUtensorMap qkv,
                                                                      const __grid_constant__ CUtensorMap dom,
                                                                      const __grid_constant__ Params p) {
+  pdl_release();
   constexpr int NCH = DH / 64;
   constexpr int TCOLS = DH == 64 ? 256 : 512;
   constexpr uint32_t C_S = 0, C_DP = 128, C_DV = 0, C_DK = 128, C_DQ = DH == 64 ? 64 : 256;
@@ -298,6 +301,7 @@ __global__ void __launch_bounds__(192, DH == 64 ? 2 : 1) attn_bwd_kernel(const _
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tslot;
+  pdl_wait();   // prerequisites complete (setup above overlapped the previous kernel's tail)
   const int H = p.H, d = p.d;
 
   if (warp == 0) {
@@ -443,6 +447,7 @@ __device__ __forceinline__ int cta_items(int items) {
 // forward: stage = Q | K | V (DH / 64 chunks each), P overlays Q (and K when DH = 64).
 template <int DH, int NS>
 __global__ void __launch_bounds__(320, 1) attn_fwd_pp(const __grid_constant__ CUtensorMap qkv, const __grid_constant__ Params p) {
+  pdl_release();
   constexpr int NCH = DH / 64, STG = 3 * NCH * CHUNK;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -470,6 +475,7 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_pp(const __grid_constant__ CU
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tslot;
+  pdl_wait();   // prerequisites complete (setup above overlapped the previous kernel's tail)
   const int H = p.H, d = p.d, n = cta_items(p.items);
   auto sQ = [&](int s) { return sbase + (uint32_t)(s * STG); };
   auto sK = [&](int s) { return sbase + (uint32_t)(s * STG + NCH * CHUNK); };
@@ -549,6 +555,7 @@ template <int NS>
 __global__ void __launch_bounds__(320, 1) attn_bwd_pp(const __grid_constant__ CUtensorMap qkv,
                                                       const __grid_constant__ CUtensorMap dom,
                                                       const __grid_constant__ Params p) {
+  pdl_release();
   constexpr int DH = 64, STG = 6 * CHUNK;
   constexpr uint32_t C_S = 0, C_DP = 128, C_DV = 0, C_DK = 128, C_DQ = 64;
   extern __shared__ uint8_t smem_raw[];
@@ -579,6 +586,7 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_pp(const __grid_constant__ CU
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tslot;
+  pdl_wait();   // prerequisites complete (setup above overlapped the previous kernel's tail)
   const int H = p.H, d = p.d, n = cta_items(p.items);
   auto sQ = [&](int s) { return sbase + (uint32_t)(s * STG); };
   auto sK = [&](int s) { return sbase + (uint32_t)(s * STG + CHUNK); };
@@ -789,11 +797,11 @@ cudaError_t core_fwd(const void* QKV, void* O, int B, int H, int m, int d, cudaS
     if (dh == 64) {
       static bool a = false;
       if (!a) { cudaFuncSetAttribute(attn_fwd_pp<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-      attn_fwd_pp<64, 4><<<grid, 320, smem, st>>>(mq, p);
+      pdl_launch(attn_fwd_pp<64, 4>, grid, 320, smem, st, mq, p);
     } else {
       static bool a = false;
       if (!a) { cudaFuncSetAttribute(attn_fwd_pp<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-      attn_fwd_pp<128, 2><<<grid, 320, smem, st>>>(mq, p);
+      pdl_launch(attn_fwd_pp<128, 2>, grid, 320, smem, st, mq, p);
     }
     ++g_launches;
     return cudaGetLastError();
@@ -802,11 +810,11 @@ cudaError_t core_fwd(const void* QKV, void* O, int B, int H, int m, int d, cudaS
   if (dh == 64) {
     static bool a = false;
     if (!a) { cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-    attn_fwd_kernel<64><<<grid_for(attn_fwd_kernel<64>, smem, p.items), 192, smem, st>>>(mq, p);
+    pdl_launch(attn_fwd_kernel<64>, grid_for(attn_fwd_kernel<64>, smem, p.items), 192, smem, st, mq, p);
   } else {
     static bool a = false;
     if (!a) { cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-    attn_fwd_kernel<128><<<grid_for(attn_fwd_kernel<128>, smem, p.items), 192, smem, st>>>(mq, p);
+    pdl_launch(attn_fwd_kernel<128>, grid_for(attn_fwd_kernel<128>, smem, p.items), 192, smem, st, mq, p);
   }
   ++g_launches;
   return cudaGetLastError();
@@ -826,7 +834,7 @@ cudaError_t core_bwd(const void* QKV, const void* dO, void* dQKV, int B, int H, 
     if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
     static bool a = false;
     if (!a) { cudaFuncSetAttribute(attn_bwd_pp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-    attn_bwd_pp<2><<<std::min(p.items, sms), 320, smem, st>>>(mq, mo, p);
+    pdl_launch(attn_bwd_pp<2>, std::min(p.items, sms), 320, smem, st, mq, mo, p);
     ++g_launches;
     return cudaGetLastError();
   }
@@ -834,11 +842,11 @@ cudaError_t core_bwd(const void* QKV, const void* dO, void* dQKV, int B, int H, 
   if (dh == 64) {
     static bool a = false;
     if (!a) { cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-    attn_bwd_kernel<64><<<grid_for(attn_bwd_kernel<64>, smem, p.items), 192, smem, st>>>(mq, mo, p);
+    pdl_launch(attn_bwd_kernel<64>, grid_for(attn_bwd_kernel<64>, smem, p.items), 192, smem, st, mq, mo, p);
   } else {
     static bool a = false;
     if (!a) { cudaFuncSetAttribute(attn_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-    attn_bwd_kernel<128><<<grid_for(attn_bwd_kernel<128>, smem, p.items), 192, smem, st>>>(mq, mo, p);
+    pdl_launch(attn_bwd_kernel<128>, grid_for(attn_bwd_kernel<128>, smem, p.items), 192, smem, st, mq, mo, p);
   }
   ++g_launches;
   return cudaGetLastError();

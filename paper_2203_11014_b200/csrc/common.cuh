@@ -8,6 +8,34 @@ namespace dhen {
 
 enum Dt : int { F32 = 0, BF16 = 1 };
 
+// Programmatic dependent launch (PDL).  Every library kernel is launched with pdl_launch (the launch attribute
+// lets it start while the previous kernel on the stream drains) and calls pdl_entry() before touching global
+// memory: it releases its own dependents at once, then waits until its prerequisite grid has completed and its
+// writes are visible (griddepcontrol.wait; a no-op for a launch without the attribute).  A dependent grid only
+// launches after every CTA of its primary has triggered, so a primary's CTAs are never starved of SMs.
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_entry() {
+  pdl_release();
+  pdl_wait();
+}
+int pdl_enabled();   // env DHEN_PDL (default 0): 1 launches with programmatic stream serialization (measured: C2 neutral, C3 -2%)
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ float ld_as_f32(const void* p, int64_t i, int dt) {
   return dt == F32 ? static_cast<const float*>(p)[i]
                    : __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);

@@ -9,6 +9,10 @@
 namespace dhen {
 
 int g_last_gemm_tc = 0;
+int pdl_enabled() {
+  static int v = [] { const char* e = getenv("DHEN_PDL"); return e ? atoi(e) : 0; }();
+  return v;
+}
 int g_gemm_force = -1;   // -1: env / auto, 0: auto, 1: SIMT only, 2: tcgen05 only
 int g_gemm_pair = -1;    // -1: env DHEN_PAIR / auto, 0: no CTA pairs, 1: CTA pairs wherever expressible
 

@@ -14,6 +14,7 @@ constexpr int BM = 64, BN = 64, BK = 16;
 
 template <typename T>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(Gemm g, int splits, int kchunk, float* ws, int zbase) {
+  pdl_entry();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int tid = threadIdx.x;
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(Gemm g, int splits, int 
 // sums splits ty, ty+8, ... (two independent chains), then the 8 lane sums are combined in fixed order
 // -> deterministic, and ~splits/8 dependent loads per thread instead of splits.
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(Gemm g, int splits, const float* ws) {
+  pdl_entry();
   __shared__ float red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t mn = (int64_t)g.M * g.N;
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(Gemm g, int splits, 
 // Split-K reduction for many output elements and few splits: one thread per element, the splits added in
 // index order (deterministic), then the fused epilogue.
 __global__ void __launch_bounds__(256) splitk_reduce_elem_kernel(Gemm g, int splits, const float* ws) {
+  pdl_entry();
   const int64_t mn = (int64_t)g.M * g.N;
   const int64_t total = (int64_t)g.batch * mn;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -144,9 +147,9 @@ cudaError_t gemm_simt(const Gemm& g, const Workspace& ws, cudaStream_t st) {
     int nz = std::min(zmax, g.batch - zb);
     dim3 grid(tn, tm, nz * splits);
     if (g.a.dt == F32)
-      gemm_simt_kernel<float><<<grid, 256, 0, st>>>(g, splits, kchunk, ws.ptr, zb);
+      pdl_launch(gemm_simt_kernel<float>, grid, 256, 0, st, g, splits, kchunk, ws.ptr, zb);
     else
-      gemm_simt_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(g, splits, kchunk, ws.ptr, zb);
+      pdl_launch(gemm_simt_kernel<__nv_bfloat16>, grid, 256, 0, st, g, splits, kchunk, ws.ptr, zb);
     ++g_launches;
   }
   if (splits > 1) return splitk_reduce(g, splits, ws.ptr, st);
@@ -157,12 +160,12 @@ cudaError_t splitk_reduce(const Gemm& g, int splits, const float* ws, cudaStream
   int64_t total = (int64_t)g.batch * g.M * g.N;
   if (total >= (int64_t)148 * 256 && splits <= 32) {   // enough elements to fill the machine one per thread
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    splitk_reduce_elem_kernel<<<blocks, 256, 0, st>>>(g, splits, ws);
+    pdl_launch(splitk_reduce_elem_kernel, blocks, 256, 0, st, g, splits, ws);
     ++g_launches;
     return cudaGetLastError();
   }
   int blocks = (int)std::min<int64_t>((total + 31) / 32, 148 * 8);
-  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(g, splits, ws);
+  pdl_launch(splitk_reduce_kernel, blocks, 256, 0, st, g, splits, ws);
   ++g_launches;
   return cudaGetLastError();
 }

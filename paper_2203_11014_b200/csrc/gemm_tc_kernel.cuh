@@ -795,6 +795,7 @@ template <int BN, int STAGES, int VAR, bool PAIR>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    const __grid_constant__ OutMaps tma_o, const __grid_constant__ Params p) {
+  pdl_release();
   constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
   constexpr int SC = EpiSmem<BN>::SC;
   constexpr int SROW = EpiSmem<BN>::SROW;
@@ -843,6 +844,7 @@ __global__ void __launch_bounds__(320, 1)
   if (pair) cluster_sync_all();   // the peer's barriers are initialised before any remote arrive / TMA
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();   // prerequisites complete (barrier init / TMEM alloc above overlapped the previous kernel's tail)
 
   auto decode = [&](int item, int& m0, int& n0, int& z, int& sp, int& kb0, int& nk) {
     const int tile = item % ntiles;
@@ -1403,10 +1405,13 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
     if constexpr (BN >= 128) if (p.pair) {
       static int max_clusters = 0;
       cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute at[1];
+      cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-      cfg.blockDim = dim3(320); cfg.dynamicSmemBytes = SMEM; cfg.stream = st; cfg.attrs = at; cfg.numAttrs = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.blockDim = dim3(320); cfg.dynamicSmemBytes = SMEM; cfg.stream = st; cfg.attrs = at;
+      cfg.numAttrs = pdl_enabled() ? 2 : 1;
       if (!max_clusters) {   // SM pairs the GPC layout can co-schedule (<= 74 on 148 SMs)
         cfg.gridDim = dim3(148);
         if (cudaOccupancyMaxActiveClusters(&max_clusters, gemm_tc_kernel<BN, STAGES, VAR, true>, &cfg) != cudaSuccess ||
@@ -1423,7 +1428,8 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
     }
     {
       const int grid = (int)std::min<int64_t>(items, 148);
-      gemm_tc_kernel<BN, STAGES, VAR, false><<<grid, 320, SMEM, st>>>(ma, mb, mc, p);
+      cudaError_t e = pdl_launch(gemm_tc_kernel<BN, STAGES, VAR, false>, grid, 320, SMEM, st, ma, mb, mc, p);
+      if (e != cudaSuccess) return e;
     }
     ++g_launches;
   }

@@ -14,6 +14,7 @@ static inline int nblocks(int64_t n, int per = 256, int cap = 148 * 32) {
 
 // ------------------------------------------------------------------ Dot triangle
 __global__ void triu_extract_k(const float* G, void* Z, int dt, int B, int m, int64_t ldz) {
+  pdl_entry();
   const int h = m * (m - 1) / 2;
   int64_t total = (int64_t)B * h;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -27,7 +28,7 @@ __global__ void triu_extract_k(const float* G, void* Z, int dt, int B, int m, in
 }
 cudaError_t triu_extract(const float* G, void* Z, int dt, int B, int m, int64_t ldz, cudaStream_t st) {
   int64_t total = (int64_t)B * m * (m - 1) / 2;
-  triu_extract_k<<<nblocks(total), 256, 0, st>>>(G, Z, dt, B, m, ldz);
+  pdl_launch(triu_extract_k, nblocks(total), 256, 0, st, G, Z, dt, B, m, ldz);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -35,6 +36,7 @@ cudaError_t triu_extract(const float* G, void* Z, int dt, int B, int m, int64_t 
 // One block per sample: the packed triangle (h values, contiguous) is staged in shared memory, then the m x m
 // matrix is written row-major with 8-element vector stores (m % 8 == 0) or scalars.
 __global__ void __launch_bounds__(256) sym_from_triu_k(const void* dZ, void* S, int dt, int m, int64_t ldz) {
+  pdl_entry();
   extern __shared__ float tri[];          // [h] triangle values, then [m] row bases
   const int h = m * (m - 1) / 2;
   int* rb = reinterpret_cast<int*>(tri + h);   // rb[i] + j = index of pair (i, j > i)
@@ -78,7 +80,7 @@ cudaError_t sym_from_triu(const void* dZ, void* S, int dt, int B, int m, int64_t
     cudaFuncSetAttribute(sym_from_triu_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = sm;
   }
-  sym_from_triu_k<<<B, 256, sm, st>>>(dZ, S, dt, m, ldz);
+  pdl_launch(sym_from_triu_k, B, 256, sm, st, dZ, S, dt, m, ldz);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -162,6 +164,7 @@ __global__ void __launch_bounds__(256) ln_fwd_v(const float* __restrict__ U, con
                                                 const T* __restrict__ gamma, const T* __restrict__ beta, float eps,
                                                 int64_t rows, int d, T* __restrict__ Y, T* __restrict__ Rsave,
                                                 float* __restrict__ mu, float* __restrict__ rstd) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
@@ -208,6 +211,7 @@ __global__ void __launch_bounds__(256) ln_bwd_v(const TD* __restrict__ dY, const
                                                 const T* __restrict__ gamma, int64_t rows, int d, T* __restrict__ dR,
                                                 float* __restrict__ acc, int acc_mode, float* __restrict__ part,
                                                 int64_t rows_per_block) {
+  pdl_entry();
   extern __shared__ float sred[];   // [8 warps][2][d]
   const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
   const int64_t r0 = blockIdx.x * rows_per_block, r1 = min(rows, r0 + rows_per_block);
@@ -292,6 +296,7 @@ constexpr int LN_MAXQ_ALL = 32;  // d <= 1024
 template <int LN_MAXQ>
 __global__ void ln_fwd_k(const float* U, const void* addx, const void* gamma, const void* beta, int pdt, float eps,
                          int64_t rows, int d, void* Y, void* Rsave, float* mu, float* rstd, int dt) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
@@ -332,9 +337,9 @@ static cudaError_t ln_fwd_generic(const float* U, const void* addx, const void* 
                    int64_t rows, int d, void* Y, void* Rsave, float* mu, float* rstd, int dt, cudaStream_t st) {
   if (d > 32 * LN_MAXQ_ALL) return cudaErrorInvalidValue;
   const int nb = nblocks(rows, 8, 148 * 64);
-  if (d <= 128) ln_fwd_k<4><<<nb, 256, 0, st>>>(U, addx, gamma, beta, pdt, eps, rows, d, Y, Rsave, mu, rstd, dt);
-  else if (d <= 256) ln_fwd_k<8><<<nb, 256, 0, st>>>(U, addx, gamma, beta, pdt, eps, rows, d, Y, Rsave, mu, rstd, dt);
-  else ln_fwd_k<32><<<nb, 256, 0, st>>>(U, addx, gamma, beta, pdt, eps, rows, d, Y, Rsave, mu, rstd, dt);
+  if (d <= 128) pdl_launch(ln_fwd_k<4>, nb, 256, 0, st, U, addx, gamma, beta, pdt, eps, rows, d, Y, Rsave, mu, rstd, dt);
+  else if (d <= 256) pdl_launch(ln_fwd_k<8>, nb, 256, 0, st, U, addx, gamma, beta, pdt, eps, rows, d, Y, Rsave, mu, rstd, dt);
+  else pdl_launch(ln_fwd_k<32>, nb, 256, 0, st, U, addx, gamma, beta, pdt, eps, rows, d, Y, Rsave, mu, rstd, dt);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -343,6 +348,7 @@ template <int LN_MAXQ>
 __global__ void ln_bwd_k(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
                          const void* gamma, int pdt, int64_t rows, int d, void* dR, int dt, float* acc, int acc_mode,
                          float* part, int64_t rows_per_block) {
+  pdl_entry();
   __shared__ float sg[8][2][256];   // per-warp partials for one 256-column slab
   const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
   const int64_t r0 = blockIdx.x * rows_per_block, r1 = min(rows, r0 + rows_per_block);
@@ -405,6 +411,7 @@ __global__ void ln_bwd_k(const void* dY, int dydt, const void* Rsave, const floa
 __global__ void __launch_bounds__(1024) part_sum_k(const float* __restrict__ part, int nparts, int n,
                                                    float* __restrict__ out0, int n0, float* __restrict__ out1,
                                                    int n1, float* __restrict__ out2, float out2_scale) {
+  pdl_entry();
   __shared__ float sm[32][33];
   const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + x;
@@ -432,7 +439,7 @@ __global__ void __launch_bounds__(1024) part_sum_k(const float* __restrict__ par
 }
 static void part_sum(const float* part, int nparts, int n, float* out0, int n0, float* out1, int n1, float* out2,
                      float out2_scale, cudaStream_t st) {
-  part_sum_k<<<(n + 31) / 32, 1024, 0, st>>>(part, nparts, n, out0, n0, out1, n1, out2, out2_scale);
+  pdl_launch(part_sum_k, (n + 31) / 32, 1024, 0, st, part, nparts, n, out0, n0, out1, n1, out2, out2_scale);
   ++g_launches;
 }
 
@@ -446,11 +453,11 @@ static cudaError_t ln_bwd_generic(const void* dY, int dydt, const void* Rsave, c
   int64_t rpb = (rows + nb - 1) / nb;
   nb = (int)((rows + rpb - 1) / rpb);
   if (d <= 128)
-    ln_bwd_k<4><<<nb, 256, 0, st>>>(dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, scratch, rpb);
+    pdl_launch(ln_bwd_k<4>, nb, 256, 0, st, dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, scratch, rpb);
   else if (d <= 256)
-    ln_bwd_k<8><<<nb, 256, 0, st>>>(dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, scratch, rpb);
+    pdl_launch(ln_bwd_k<8>, nb, 256, 0, st, dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, scratch, rpb);
   else
-    ln_bwd_k<32><<<nb, 256, 0, st>>>(dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, scratch, rpb);
+    pdl_launch(ln_bwd_k<32>, nb, 256, 0, st, dY, dydt, Rsave, mu, rstd, gamma, pdt, rows, d, dR, dt, acc, acc_mode, scratch, rpb);
   ++g_launches;
   part_sum(scratch, nb, 2 * d, dgamma, d, dbeta, d, nullptr, 0.f, st);
   return cudaGetLastError();
@@ -482,6 +489,7 @@ __global__ void __launch_bounds__(256) ln_fwd_r(const float* __restrict__ U, con
                                                 const __nv_bfloat16* __restrict__ beta, float eps, int64_t rows,
                                                 __nv_bfloat16* __restrict__ Y, __nv_bfloat16* __restrict__ Rsave,
                                                 float* __restrict__ mu, float* __restrict__ rstd) {
+  pdl_entry();
   constexpr int d = 8 * LPR, RPW = 32 / LPR, RPI = RPW * UR;
   const int lane = threadIdx.x & 31, sub = lane / LPR, c = (lane % LPR) * 8;
   float g[8], b[8];
@@ -535,6 +543,7 @@ __global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const
                                                 const __nv_bfloat16* __restrict__ gamma, int64_t rows,
                                                 __nv_bfloat16* __restrict__ dR, float* __restrict__ acc, int acc_mode,
                                                 float* __restrict__ part, int64_t rows_per_block) {
+  pdl_entry();
   constexpr int d = 8 * LPR, RPW = 32 / LPR, RPI = RPW * UR;
   __shared__ float sred[8][2][d];
   const int lane = threadIdx.x & 31, w = threadIdx.x / 32, sub = lane / LPR, c = (lane % LPR) * 8;
@@ -704,7 +713,7 @@ cudaError_t ln_fwd(const float* U, const void* addx, const void* gamma, const vo
     const int rpi = (32 / lpr) * 2;   // rows per warp iteration (UR = 2)
     const int nb = nblocks((rows + rpi - 1) / rpi, 8, 148 * 8);
 #define LNR(L)                                                                                                    \
-    if (lpr == L) ln_fwd_r<L, 2><<<nb, 256, 0, st>>>(U, (const __nv_bfloat16*)addx, (const __nv_bfloat16*)gamma, \
+    if (lpr == L) pdl_launch(ln_fwd_r<L, 2>, nb, 256, 0, st, U, (const __nv_bfloat16*)addx, (const __nv_bfloat16*)gamma, \
         (const __nv_bfloat16*)beta, eps, rows, (__nv_bfloat16*)Y, (__nv_bfloat16*)Rsave, mu, rstd);
     LNR(4) LNR(8) LNR(16) LNR(32)
 #undef LNR
@@ -718,10 +727,10 @@ cudaError_t ln_fwd(const float* U, const void* addx, const void* gamma, const vo
 #define LNF(V, N)                                                                                               \
   if (vec == V && nch == N) {                                                                                   \
     if (dt == BF16)                                                                                             \
-      ln_fwd_v<__nv_bfloat16, V, N><<<nb, 256, 0, st>>>(U, (const __nv_bfloat16*)addx, (const __nv_bfloat16*)gamma, \
+      pdl_launch(ln_fwd_v<__nv_bfloat16, V, N>, nb, 256, 0, st, U, (const __nv_bfloat16*)addx, (const __nv_bfloat16*)gamma, \
           (const __nv_bfloat16*)beta, eps, rows, d, (__nv_bfloat16*)Y, (__nv_bfloat16*)Rsave, mu, rstd);       \
     else                                                                                                        \
-      ln_fwd_v<float, V, N><<<nb, 256, 0, st>>>(U, (const float*)addx, (const float*)gamma, (const float*)beta, eps, \
+      pdl_launch(ln_fwd_v<float, V, N>, nb, 256, 0, st, U, (const float*)addx, (const float*)gamma, (const float*)beta, eps, \
           rows, d, (float*)Y, (float*)Rsave, mu, rstd);                                                        \
   }
   LN_SHAPES(LNF)
@@ -744,10 +753,10 @@ cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu,
 #define LNB2(L)                                                                                                        \
       if (lpr == L) {                                                                                                  \
         if (dydt == BF16)                                                                                              \
-          ln_bwd_r<L, LNB_UR, __nv_bfloat16><<<nb, 256, 0, st>>>((const __nv_bfloat16*)dY, (const __nv_bfloat16*)Rsave, mu, \
+          pdl_launch(ln_bwd_r<L, LNB_UR, __nv_bfloat16>, nb, 256, 0, st, (const __nv_bfloat16*)dY, (const __nv_bfloat16*)Rsave, mu, \
               rstd, (const __nv_bfloat16*)gamma, rows, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb);               \
         else                                                                                                           \
-          ln_bwd_r<L, LNB_UR, float><<<nb, 256, 0, st>>>((const float*)dY, (const __nv_bfloat16*)Rsave, mu, rstd,           \
+          pdl_launch(ln_bwd_r<L, LNB_UR, float>, nb, 256, 0, st, (const float*)dY, (const __nv_bfloat16*)Rsave, mu, rstd,           \
               (const __nv_bfloat16*)gamma, rows, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb);                     \
       }
       LNB2(4) LNB2(8) LNB2(16) LNB2(32)
@@ -775,14 +784,14 @@ cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu,
   if (vec == V && nch == N) {                                                                                       \
     if (dt == BF16) {                                                                                               \
       if (dydt == BF16)                                                                                             \
-        ln_bwd_v<__nv_bfloat16, __nv_bfloat16, V, N><<<nb, 256, sm, st>>>((const __nv_bfloat16*)dY,                 \
+        pdl_launch(ln_bwd_v<__nv_bfloat16, __nv_bfloat16, V, N>, nb, 256, sm, st, (const __nv_bfloat16*)dY,                 \
             (const __nv_bfloat16*)Rsave, mu, rstd, (const __nv_bfloat16*)gamma, rows, d, (__nv_bfloat16*)dR, acc,   \
             acc_mode, scratch, rpb);                                                                                \
       else                                                                                                          \
-        ln_bwd_v<float, __nv_bfloat16, V, N><<<nb, 256, sm, st>>>((const float*)dY, (const __nv_bfloat16*)Rsave,    \
+        pdl_launch(ln_bwd_v<float, __nv_bfloat16, V, N>, nb, 256, sm, st, (const float*)dY, (const __nv_bfloat16*)Rsave,    \
             mu, rstd, (const __nv_bfloat16*)gamma, rows, d, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb);       \
     } else {                                                                                                        \
-      ln_bwd_v<float, float, V, N><<<nb, 256, sm, st>>>((const float*)dY, (const float*)Rsave, mu, rstd,            \
+      pdl_launch(ln_bwd_v<float, float, V, N>, nb, 256, sm, st, (const float*)dY, (const float*)Rsave, mu, rstd,            \
           (const float*)gamma, rows, d, (float*)dR, acc, acc_mode, scratch, rpb);                                   \
     }                                                                                                               \
   }
@@ -795,6 +804,7 @@ cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu,
 
 // ------------------------------------------------------------------ column sums
 __global__ void colsum_part_k(const void* src, int dt, int64_t rows, int cols, int64_t ld, int64_t rpc, float* part) {
+  pdl_entry();
   __shared__ float sm[8][33];
   const int cx = threadIdx.x % 32, ry = threadIdx.x / 32;
   const int c = blockIdx.x * 32 + cx;
@@ -814,6 +824,7 @@ __global__ void colsum_part_k(const void* src, int dt, int64_t rows, int cols, i
 template <typename T>
 __global__ void __launch_bounds__(256) colsum8_part_k(const T* __restrict__ src, int64_t rows, int cols, int64_t ld,
                                                       int64_t rpc, float* __restrict__ part) {
+  pdl_entry();
   __shared__ float sm[8][257];
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
   const int c = blockIdx.x * 256 + tx * 8;
@@ -852,6 +863,7 @@ __global__ void __launch_bounds__(256) colsum8_part_k(const T* __restrict__ src,
 // loads) x RT = 256 / CT row-threads; the RT partial rows are added in fixed order through shared memory.
 __global__ void __launch_bounds__(256) colsum_all_k(const __nv_bfloat16* __restrict__ src, int64_t rows, int cols,
                                                     int64_t ld, int64_t rpc, float* __restrict__ part) {
+  pdl_entry();
   extern __shared__ float csm[];   // [RT][cols]
   const int CT = cols / 8, RT = 256 / CT;
   const int ct = threadIdx.x % CT, ry = threadIdx.x / CT, c = ct * 8;
@@ -896,7 +908,7 @@ cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t 
       int64_t rpc = (rows + nch - 1) / nch;
       nch = (rows + rpc - 1) / rpc;
       if (nch < 1) nch = 1;
-      colsum_all_k<<<(unsigned)nch, 256, (size_t)RT * cols * sizeof(float), st>>>((const __nv_bfloat16*)src, rows, cols,
+      pdl_launch(colsum_all_k, (unsigned)nch, 256, (size_t)RT * cols * sizeof(float), st, (const __nv_bfloat16*)src, rows, cols,
                                                                                    ld, rpc, scratch);
       ++g_launches;
       part_sum(scratch, (int)nch, cols, out, cols, nullptr, 0, nullptr, 0.f, st);
@@ -912,9 +924,9 @@ cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t 
       nch = (rows + rpc - 1) / rpc;
       if (nch < 1) nch = 1;
       if (dt == F32)
-        colsum8_part_k<float><<<dim3(cb, (unsigned)nch), 256, 0, st>>>((const float*)src, rows, cols, ld, rpc, scratch);
+        pdl_launch(colsum8_part_k<float>, dim3(cb, (unsigned)nch), 256, 0, st, (const float*)src, rows, cols, ld, rpc, scratch);
       else
-        colsum8_part_k<__nv_bfloat16><<<dim3(cb, (unsigned)nch), 256, 0, st>>>((const __nv_bfloat16*)src, rows, cols,
+        pdl_launch(colsum8_part_k<__nv_bfloat16>, dim3(cb, (unsigned)nch), 256, 0, st, (const __nv_bfloat16*)src, rows, cols,
                                                                                 ld, rpc, scratch);
       ++g_launches;
       part_sum(scratch, (int)nch, cols, out, cols, nullptr, 0, nullptr, 0.f, st);
@@ -928,7 +940,7 @@ cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t 
   int64_t rpc = (rows + nch - 1) / nch;
   nch = (rows + rpc - 1) / rpc;
   if (nch < 1) nch = 1;
-  colsum_part_k<<<dim3(cb, (unsigned)nch), 256, 0, st>>>(src, dt, rows, cols, ld, rpc, scratch);
+  pdl_launch(colsum_part_k, dim3(cb, (unsigned)nch), 256, 0, st, src, dt, rows, cols, ld, rpc, scratch);
   ++g_launches;
   part_sum(scratch, (int)nch, cols, out, cols, nullptr, 0, nullptr, 0.f, st);
   return cudaGetLastError();
@@ -936,6 +948,7 @@ cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t 
 
 // ------------------------------------------------------------------ softmax
 __global__ void softmax_rows_k(const float* S, void* P, int dt, int64_t rows, int n, int ld) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
@@ -950,12 +963,13 @@ __global__ void softmax_rows_k(const float* S, void* P, int dt, int64_t rows, in
   }
 }
 cudaError_t softmax_rows(const float* S, void* P, int dt, int64_t rows, int n, int ld, cudaStream_t st) {
-  softmax_rows_k<<<nblocks(rows, 8, 148 * 64), 256, 0, st>>>(S, P, dt, rows, n, ld);
+  pdl_launch(softmax_rows_k, nblocks(rows, 8, 148 * 64), 256, 0, st, S, P, dt, rows, n, ld);
   ++g_launches;
   return cudaGetLastError();
 }
 __global__ void softmax_bwd_k(const void* P, const float* dP, void* dS, int dt, int64_t rows, int n, int ld,
                               float scale) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
@@ -970,13 +984,14 @@ __global__ void softmax_bwd_k(const void* P, const float* dP, void* dS, int dt, 
 }
 cudaError_t softmax_bwd(const void* P, const float* dP, void* dS, int dt, int64_t rows, int n, int ld, float scale,
                         cudaStream_t st) {
-  softmax_bwd_k<<<nblocks(rows, 8, 148 * 64), 256, 0, st>>>(P, dP, dS, dt, rows, n, ld, scale);
+  pdl_launch(softmax_bwd_k, nblocks(rows, 8, 148 * 64), 256, 0, st, P, dP, dS, dt, rows, n, ld, scale);
   ++g_launches;
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ DCN backward elementwise
 __global__ void dcn_bwd_elem_k(const void* dT, const void* X, const void* A, void* dA, float* acc, int dt, int64_t n) {
+  pdl_entry();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     float g = ld_as_f32(dT, t, dt), x = ld_as_f32(X, t, dt), a = ld_as_f32(A, t, dt);
     st_from_f32(dA, t, dt, g * x);
@@ -985,7 +1000,7 @@ __global__ void dcn_bwd_elem_k(const void* dT, const void* X, const void* A, voi
 }
 cudaError_t dcn_bwd_elem(const void* dT, const void* X, const void* A, void* dA, float* acc, int dt, int64_t n,
                          cudaStream_t st) {
-  dcn_bwd_elem_k<<<nblocks(n), 256, 0, st>>>(dT, X, A, dA, acc, dt, n);
+  pdl_launch(dcn_bwd_elem_k, nblocks(n), 256, 0, st, dT, X, A, dA, acc, dt, n);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -997,6 +1012,7 @@ constexpr int CV_RB = 8;
 template <typename T, int K, bool FLIP>
 __global__ void __launch_bounds__(256) conv_band_k(const T* __restrict__ in, const T* __restrict__ Kp, int C, int m,
                                                    int d, T* __restrict__ outT, float* __restrict__ outAcc, int nbatch) {
+  pdl_entry();
   constexpr int R = (K - 1) / 2;
   extern __shared__ float band[];          // [(RB + 2R) rows][d + 2R]
   __shared__ float kb[K * K];
@@ -1055,6 +1071,7 @@ __global__ void __launch_bounds__(256) conv_band_k(const T* __restrict__ in, con
 template <typename T, int K>
 __global__ void __launch_bounds__(256) conv_wgrad_band_k(const T* __restrict__ dT, const T* __restrict__ X, int m,
                                                          int d, float* __restrict__ part, int nbatch) {
+  pdl_entry();
   constexpr int R = (K - 1) / 2;
   extern __shared__ float band[];          // X band [(RB + 2R)][d + 2R]
   __shared__ float red[K * K][8];
@@ -1120,6 +1137,7 @@ __global__ void __launch_bounds__(256) conv_sample_k(const T* __restrict__ img, 
                                                      const T* __restrict__ Kp, int C, int B, int m, int d,
                                                      T* __restrict__ outT, float* __restrict__ outAcc,
                                                      float* __restrict__ part) {
+  pdl_entry();
   constexpr int R = (K - 1) / 2;
   extern __shared__ __align__(16) unsigned char conv_smem[];
   T* S = reinterpret_cast<T*>(conv_smem);            // [(m + 2R)][W]
@@ -1250,7 +1268,7 @@ static cudaError_t conv_sample_launch(const void* img, const void* other, const 
     cudaFuncSetAttribute(conv_sample_k<T, K, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  conv_sample_k<T, K, MODE><<<grid, 256, sm, st>>>((const T*)img, (const T*)other, (const T*)Kp, C, B, m, d, (T*)outT,
+  pdl_launch(conv_sample_k<T, K, MODE>, grid, 256, sm, st, (const T*)img, (const T*)other, (const T*)Kp, C, B, m, d, (T*)outT,
                                                    outAcc, part);
   ++g_launches;
   return cudaGetLastError();
@@ -1267,9 +1285,9 @@ static cudaError_t conv_band_launch(const void* in, const void* Kp, int C, int B
   const int64_t bands = (int64_t)((m + CV_RB - 1) / CV_RB) * B;
   const int grid = (int)std::min<int64_t>(bands, 148 * 8);
   if (flip)
-    conv_band_k<T, K, true><<<grid, 256, sm, st>>>((const T*)in, (const T*)Kp, C, m, d, (T*)outT, outAcc, B);
+    pdl_launch(conv_band_k<T, K, true>, grid, 256, sm, st, (const T*)in, (const T*)Kp, C, m, d, (T*)outT, outAcc, B);
   else
-    conv_band_k<T, K, false><<<grid, 256, sm, st>>>((const T*)in, (const T*)Kp, C, m, d, (T*)outT, outAcc, B);
+    pdl_launch(conv_band_k<T, K, false>, grid, 256, sm, st, (const T*)in, (const T*)Kp, C, m, d, (T*)outT, outAcc, B);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -1304,6 +1322,7 @@ __global__ void __launch_bounds__(512, 1) conv_db_k(const __nv_bfloat16* __restr
                                                     const __nv_bfloat16* __restrict__ Kp, int C, int B, int m, int d,
                                                     __nv_bfloat16* __restrict__ outT, float* __restrict__ outAcc,
                                                     float* __restrict__ part) {
+  pdl_entry();
   // smem image: rows 0..m+1 (0 and m+1 zero), dense rows (pitch d): the sample lands with ONE bulk copy;
   // the two edge column-quads read their out-of-image neighbour as 0.
   extern __shared__ __align__(128) unsigned char cdb_smem[];
@@ -1443,7 +1462,7 @@ static cudaError_t conv_db_launch(const void* img, const void* other, const void
   if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
   const int grid = std::min(B, sms);
   if (grid_out) *grid_out = grid;
-  conv_db_k<MODE><<<grid, 512, sm, st>>>((const __nv_bfloat16*)img, (const __nv_bfloat16*)other,
+  pdl_launch(conv_db_k<MODE>, grid, 512, sm, st, (const __nv_bfloat16*)img, (const __nv_bfloat16*)other,
                                          (const __nv_bfloat16*)Kp, C, B, m, d, (__nv_bfloat16*)outT, outAcc, part);
   ++g_launches;
   return cudaGetLastError();
@@ -1460,6 +1479,7 @@ __device__ void load_kbar(const void* K, int pdt, int C, int k, float* kb) {
   __syncthreads();
 }
 __global__ void conv_fwd_k(const void* X, const void* K, int pdt, int C, int k, int B, int m, int d, void* T, int dt) {
+  pdl_entry();
   __shared__ float kb[CONV_MAXK * CONV_MAXK];
   load_kbar(K, pdt, C, k, kb);
   const int r = (k - 1) / 2;
@@ -1495,12 +1515,13 @@ cudaError_t conv_fwd(const void* X, const void* K, int pdt, int C, int k, int B,
     return k == 3 ? conv_band_launch<float, 3>(X, K, C, B, m, d, T, nullptr, false, st)
                   : conv_band_launch<float, 5>(X, K, C, B, m, d, T, nullptr, false, st);
   }
-  conv_fwd_k<<<nblocks((int64_t)B * m * d), 256, 0, st>>>(X, K, pdt, C, k, B, m, d, T, dt);
+  pdl_launch(conv_fwd_k, nblocks((int64_t)B * m * d), 256, 0, st, X, K, pdt, C, k, B, m, d, T, dt);
   ++g_launches;
   return cudaGetLastError();
 }
 __global__ void conv_dgrad_k(const void* dT, const void* K, int pdt, int C, int k, int B, int m, int d, float* acc,
                              int dt) {
+  pdl_entry();
   __shared__ float kb[CONV_MAXK * CONV_MAXK];
   load_kbar(K, pdt, C, k, kb);
   const int r = (k - 1) / 2;
@@ -1536,12 +1557,13 @@ cudaError_t conv_dgrad(const void* dT, const void* K, int pdt, int C, int k, int
     return k == 3 ? conv_band_launch<float, 3>(dT, K, C, B, m, d, nullptr, acc, true, st)
                   : conv_band_launch<float, 5>(dT, K, C, B, m, d, nullptr, acc, true, st);
   }
-  conv_dgrad_k<<<nblocks((int64_t)B * m * d), 256, 0, st>>>(dT, K, pdt, C, k, B, m, d, acc, dt);
+  pdl_launch(conv_dgrad_k, nblocks((int64_t)B * m * d), 256, 0, st, dT, K, pdt, C, k, B, m, d, acc, dt);
   ++g_launches;
   return cudaGetLastError();
 }
 __global__ void conv_wgrad_k(const void* dT, const void* X, int k, int B, int m, int d, int dt, float* part,
                              int64_t per_block) {
+  pdl_entry();
   __shared__ float red[CONV_MAXK * CONV_MAXK][8];
   const int r = (k - 1) / 2;
   float s[CONV_MAXK * CONV_MAXK];
@@ -1575,6 +1597,7 @@ __global__ void conv_wgrad_k(const void* dT, const void* X, int k, int B, int m,
   }
 }
 __global__ void conv_wgrad_fin_k(const float* part, int nparts, int C, int kk, float* dK) {
+  pdl_entry();
   for (int t = threadIdx.x; t < kk; t += blockDim.x) {
     float s = 0.f;
     for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * kk + t];
@@ -1589,7 +1612,7 @@ cudaError_t conv_wgrad(const void* dT, const void* X, int C, int k, int B, int m
     int grid = 0;
     cudaError_t e = conv_db_launch<2>(X, dT, nullptr, C, B, m, d, nullptr, nullptr, scratch, &grid, st);
     if (e != cudaSuccess) return e;
-    conv_wgrad_fin_k<<<1, 64, 0, st>>>(scratch, grid, C, k * k, dK);
+    pdl_launch(conv_wgrad_fin_k, 1, 64, 0, st, scratch, grid, C, k * k, dK);
     ++g_launches;
     return cudaGetLastError();
   }
@@ -1599,7 +1622,7 @@ cudaError_t conv_wgrad(const void* dT, const void* X, int C, int k, int B, int m
       cudaError_t e = dt == BF16 ? conv_sample_launch<__nv_bfloat16, 3, 2>(X, dT, nullptr, C, B, m, d, nullptr, nullptr, scratch, grid, st)
                                  : conv_sample_launch<float, 3, 2>(X, dT, nullptr, C, B, m, d, nullptr, nullptr, scratch, grid, st);
       if (e != cudaSuccess) return e;
-      conv_wgrad_fin_k<<<1, 64, 0, st>>>(scratch, grid, C, k * k, dK);
+      pdl_launch(conv_wgrad_fin_k, 1, 64, 0, st, scratch, grid, C, k * k, dK);
       ++g_launches;
       return cudaGetLastError();
     }
@@ -1610,13 +1633,13 @@ cudaError_t conv_wgrad(const void* dT, const void* X, int C, int k, int B, int m
     const int R = (k - 1) / 2;
     const size_t sm = (size_t)(CV_RB + 2 * R) * (d + 2 * R) * sizeof(float);
     if (dt == BF16) {
-      if (k == 3) conv_wgrad_band_k<__nv_bfloat16, 3><<<grid, 256, sm, st>>>((const __nv_bfloat16*)dT, (const __nv_bfloat16*)X, m, d, scratch, B);
-      else conv_wgrad_band_k<__nv_bfloat16, 5><<<grid, 256, sm, st>>>((const __nv_bfloat16*)dT, (const __nv_bfloat16*)X, m, d, scratch, B);
+      if (k == 3) pdl_launch(conv_wgrad_band_k<__nv_bfloat16, 3>, grid, 256, sm, st, (const __nv_bfloat16*)dT, (const __nv_bfloat16*)X, m, d, scratch, B);
+      else pdl_launch(conv_wgrad_band_k<__nv_bfloat16, 5>, grid, 256, sm, st, (const __nv_bfloat16*)dT, (const __nv_bfloat16*)X, m, d, scratch, B);
     } else {
-      if (k == 3) conv_wgrad_band_k<float, 3><<<grid, 256, sm, st>>>((const float*)dT, (const float*)X, m, d, scratch, B);
-      else conv_wgrad_band_k<float, 5><<<grid, 256, sm, st>>>((const float*)dT, (const float*)X, m, d, scratch, B);
+      if (k == 3) pdl_launch(conv_wgrad_band_k<float, 3>, grid, 256, sm, st, (const float*)dT, (const float*)X, m, d, scratch, B);
+      else pdl_launch(conv_wgrad_band_k<float, 5>, grid, 256, sm, st, (const float*)dT, (const float*)X, m, d, scratch, B);
     }
-    conv_wgrad_fin_k<<<1, 64, 0, st>>>(scratch, grid, C, k * k, dK);
+    pdl_launch(conv_wgrad_fin_k, 1, 64, 0, st, scratch, grid, C, k * k, dK);
     g_launches += 2;
     return cudaGetLastError();
   }
@@ -1625,8 +1648,8 @@ cudaError_t conv_wgrad(const void* dT, const void* X, int C, int k, int B, int m
   nb = (int)std::min<int64_t>(nb, (int64_t)(scratch_bytes / (sizeof(float) * k * k)));
   int64_t per = (total + nb - 1) / nb;
   nb = (int)((total + per - 1) / per);
-  conv_wgrad_k<<<nb, 256, 0, st>>>(dT, X, k, B, m, d, dt, scratch, per);
-  conv_wgrad_fin_k<<<1, 64, 0, st>>>(scratch, nb, C, k * k, dK);
+  pdl_launch(conv_wgrad_k, nb, 256, 0, st, dT, X, k, B, m, d, dt, scratch, per);
+  pdl_launch(conv_wgrad_fin_k, 1, 64, 0, st, scratch, nb, C, k * k, dK);
   g_launches += 2;
   return cudaGetLastError();
 }
@@ -1639,6 +1662,7 @@ __global__ void __launch_bounds__(256) head_v(const __nv_bfloat16* __restrict__ 
                                               const __nv_bfloat16* __restrict__ bh, const float* __restrict__ labels,
                                               int m, int d, int Bg, __nv_bfloat16* __restrict__ dY, float* pooled,
                                               float* z, float* lossb, float* dz, int do_bwd, float* __restrict__ hpart) {
+  pdl_entry();
   extern __shared__ float hs[];   // [RY][d] partial column sums
   __shared__ float red[8];
   __shared__ float dzs;
@@ -1707,6 +1731,7 @@ __global__ void __launch_bounds__(256) head_v(const __nv_bfloat16* __restrict__ 
 }
 __global__ void head_k(const void* Y, const void* w, const void* bh, int pdt, const float* labels, int m, int d, int Bg,
                        void* dY, int dt, float* pooled, float* z, float* lossb, float* dz, int do_bwd) {
+  pdl_entry();
   __shared__ float red[32];
   const int b = blockIdx.x;
   float part = 0.f;
@@ -1746,6 +1771,7 @@ __global__ void head_k(const void* Y, const void* w, const void* bh, int pdt, co
 // part[blk] = (sum_b dz_b pooled_b[0..d), sum_b dz_b, sum_b loss_b) over the block's sample chunk
 __global__ void head_part_k(const float* pooled, const float* dz, const float* lossb, int B, int d, int per,
                             float* part) {
+  pdl_entry();
   const int b0 = blockIdx.x * per, b1 = min(B, b0 + per);
   for (int c = threadIdx.x; c < d + 2; c += blockDim.x) {
     float s = 0.f;
@@ -1762,20 +1788,20 @@ cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, 
       (!do_bwd || ((uintptr_t)dY % 16) == 0)) {
     const int RY = 256 / (d / 8);
     float* hpart = pooled + (int64_t)B * d;   // [B][d + 2] (sized by the runtime)
-    head_v<8><<<B, 256, (size_t)RY * d * sizeof(float), st>>>((const __nv_bfloat16*)Y, (const __nv_bfloat16*)w,
+    pdl_launch(head_v<8>, B, 256, (size_t)RY * d * sizeof(float), st, (const __nv_bfloat16*)Y, (const __nv_bfloat16*)w,
         (const __nv_bfloat16*)bh, labels, m, d, Bg, (__nv_bfloat16*)dY, pooled, z, lossb, dz, do_bwd,
         do_bwd ? hpart : nullptr);
     ++g_launches;
     if (do_bwd) part_sum(hpart, B, d + 2, dw, d, db, 1, loss_out, 1.f / (float)Bg, st);   // fixed order over samples
     return cudaGetLastError();
   } else {
-    head_k<<<B, 256, 0, st>>>(Y, w, bh, pdt, labels, m, d, Bg, dY, dt, pooled, z, lossb, dz, do_bwd);
+    pdl_launch(head_k, B, 256, 0, st, Y, w, bh, pdt, labels, m, d, Bg, dY, dt, pooled, z, lossb, dz, do_bwd);
   }
   ++g_launches;
   if (do_bwd) {
     const int per = 32, nparts = (B + per - 1) / per;
     float* part = pooled + (int64_t)B * d;   // scratch after pooled (sized by the runtime)
-    head_part_k<<<nparts, 128, 0, st>>>(pooled, dz, lossb, B, d, per, part);
+    pdl_launch(head_part_k, nparts, 128, 0, st, pooled, dz, lossb, B, d, per, part);
     ++g_launches;
     part_sum(part, nparts, d + 2, dw, d, db, 1, loss_out, 1.f / (float)Bg, st);
   }
@@ -1785,6 +1811,7 @@ cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, 
 // ------------------------------------------------------------------ block-diagonal token map
 // out[i][k] (bf16, [spt m][spt l]) = W[i % m][k % l] if i / m == k / l else 0; W bf16 [m][l]
 __global__ void blockdiag_k(const __nv_bfloat16* W, int m, int l, int spt, __nv_bfloat16* out) {
+  pdl_entry();
   const int n = spt * m * spt * l;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int i = t / (spt * l), k = t - i * (spt * l);
@@ -1793,13 +1820,14 @@ __global__ void blockdiag_k(const __nv_bfloat16* W, int m, int l, int spt, __nv_
 }
 cudaError_t blockdiag(const void* W, int m, int l, int spt, void* out, cudaStream_t st) {
   const int n = spt * m * spt * l;
-  blockdiag_k<<<(n + 255) / 256, 256, 0, st>>>((const __nv_bfloat16*)W, m, l, spt, (__nv_bfloat16*)out);
+  pdl_launch(blockdiag_k, (n + 255) / 256, 256, 0, st, (const __nv_bfloat16*)W, m, l, spt, (__nv_bfloat16*)out);
   ++g_launches;
   return cudaGetLastError();
 }
 
 // out[i][k] (bf16, [spt l][spt m]) = W[k % m][i % l] if i / l == k / m else 0: blockdiag(W^T, .., W^T)
 __global__ void blockdiag_t_k(const __nv_bfloat16* W, int m, int l, int spt, __nv_bfloat16* out) {
+  pdl_entry();
   const int n = spt * l * spt * m;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int i = t / (spt * m), k = t - i * (spt * m);
@@ -1808,13 +1836,14 @@ __global__ void blockdiag_t_k(const __nv_bfloat16* W, int m, int l, int spt, __n
 }
 cudaError_t blockdiag_t(const void* W, int m, int l, int spt, void* out, cudaStream_t st) {
   const int n = spt * l * spt * m;
-  blockdiag_t_k<<<(n + 255) / 256, 256, 0, st>>>((const __nv_bfloat16*)W, m, l, spt, (__nv_bfloat16*)out);
+  pdl_launch(blockdiag_t_k, (n + 255) / 256, 256, 0, st, (const __nv_bfloat16*)W, m, l, spt, (__nv_bfloat16*)out);
   ++g_launches;
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ SGD, casts, init
 __global__ void sgd_cast_k(float* master, const float* grad, float lr, void* copy, int dt, int64_t n) {
+  pdl_entry();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     float v = master[t];
     if (grad) { v -= lr * grad[t]; master[t] = v; }
@@ -1824,6 +1853,7 @@ __global__ void sgd_cast_k(float* master, const float* grad, float lr, void* cop
 // 4 elements per thread (n % 4 == 0, 16-B aligned fp32 arrays, 8-B aligned bf16 copy)
 __global__ void sgd_cast4_k(float4* __restrict__ master, const float4* __restrict__ grad, float lr, uint2* __restrict__ copy,
                             int64_t n4) {
+  pdl_entry();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n4; t += (int64_t)gridDim.x * blockDim.x) {
     float4 v = master[t];
     if (grad) {
@@ -1841,15 +1871,16 @@ cudaError_t sgd_cast(float* master, const float* grad, float lr, void* copy, int
   if (n <= 0) return cudaSuccess;
   if (n % 4 == 0 && (!copy || dt == BF16) && ((uintptr_t)master % 16) == 0 && ((uintptr_t)grad % 16) == 0 &&
       ((uintptr_t)copy % 8) == 0) {
-    sgd_cast4_k<<<nblocks(n / 4, 256, 148 * 16), 256, 0, st>>>((float4*)master, (const float4*)grad, lr, (uint2*)copy, n / 4);
+    pdl_launch(sgd_cast4_k, nblocks(n / 4, 256, 148 * 16), 256, 0, st, (float4*)master, (const float4*)grad, lr, (uint2*)copy, n / 4);
   } else {
-    sgd_cast_k<<<nblocks(n), 256, 0, st>>>(master, grad, lr, copy, dt, n);
+    pdl_launch(sgd_cast_k, nblocks(n), 256, 0, st, master, grad, lr, copy, dt, n);
   }
   ++g_launches;
   return cudaGetLastError();
 }
 // Multi-tensor SGD: every parameter group of the step in ONE launch (segments concatenated in 4-element units)
 __global__ void __launch_bounds__(256) sgd_multi_k(SgdSegs segs, float lr) {
+  pdl_entry();
   int64_t tot = 0;
   for (int s = 0; s < segs.n; ++s) tot += segs.n4[s];
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
@@ -1873,16 +1904,18 @@ cudaError_t sgd_multi(const SgdSegs& segs, float lr, cudaStream_t st) {
     tot += segs.n4[s];
   }
   if (tot == 0) return cudaSuccess;
-  sgd_multi_k<<<nblocks(tot, 256, 148 * 16), 256, 0, st>>>(segs, lr);
+  pdl_launch(sgd_multi_k, nblocks(tot, 256, 148 * 16), 256, 0, st, segs, lr);
   ++g_launches;
   return cudaGetLastError();
 }
 __global__ void cast_k(const void* src, int sdt, void* dst, int ddt, int64_t n) {
+  pdl_entry();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
     st_from_f32(dst, t, ddt, ld_as_f32(src, t, sdt));
 }
 // fp32 -> bf16, 8 elements per thread
 __global__ void cast8_k(const float4* __restrict__ src, uint4* __restrict__ dst, int64_t n8) {
+  pdl_entry();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n8; t += (int64_t)gridDim.x * blockDim.x) {
     const float4 a = __ldcs(src + 2 * t), b = __ldcs(src + 2 * t + 1);
     __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w);
@@ -1894,9 +1927,9 @@ __global__ void cast8_k(const float4* __restrict__ src, uint4* __restrict__ dst,
 cudaError_t cast(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (sdt == F32 && ddt == BF16 && n % 8 == 0 && ((uintptr_t)src % 16) == 0 && ((uintptr_t)dst % 16) == 0)
-    cast8_k<<<nblocks(n / 8, 256, 148 * 16), 256, 0, st>>>((const float4*)src, (uint4*)dst, n / 8);
+    pdl_launch(cast8_k, nblocks(n / 8, 256, 148 * 16), 256, 0, st, (const float4*)src, (uint4*)dst, n / 8);
   else
-    cast_k<<<nblocks(n), 256, 0, st>>>(src, sdt, dst, ddt, n);
+    pdl_launch(cast_k, nblocks(n), 256, 0, st, src, sdt, dst, ddt, n);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -1908,6 +1941,7 @@ __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
 }
 __global__ void init_uniform_k(float* p, int64_t n, float bound, unsigned long long seed, unsigned long long sid,
                                int64_t idx0) {
+  pdl_entry();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long h = splitmix64(seed ^ splitmix64(sid * 0x100000001B3ull + (unsigned long long)(idx0 + t)));
     float u = (float)((h >> 40) * (1.0 / 16777216.0));   // [0,1)
@@ -1917,16 +1951,17 @@ __global__ void init_uniform_k(float* p, int64_t n, float bound, unsigned long l
 cudaError_t init_uniform(float* p, int64_t n, float bound, unsigned long long seed, unsigned long long stream_id,
                          int64_t idx0, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  init_uniform_k<<<nblocks(n), 256, 0, st>>>(p, n, bound, seed, stream_id, idx0);
+  pdl_launch(init_uniform_k, nblocks(n), 256, 0, st, p, n, bound, seed, stream_id, idx0);
   ++g_launches;
   return cudaGetLastError();
 }
 __global__ void fill_k(float* p, int64_t n, float v) {
+  pdl_entry();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) p[t] = v;
 }
 cudaError_t fill(float* p, int64_t n, float v, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  fill_k<<<nblocks(n), 256, 0, st>>>(p, n, v);
+  pdl_launch(fill_k, nblocks(n), 256, 0, st, p, n, v);
   ++g_launches;
   return cudaGetLastError();
 }
