@@ -111,8 +111,9 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
 }
 // Softmax of this thread's S row (TMEM lane) into bf16 P, packed two per word (p[j/2]); rows >= m and
 // columns >= m give 0.  Three passes over the row in 32-column chunks (max; exp written back to TMEM and
-// summed; normalise and pack) keep 32 values live instead of 128.  The same code runs in the forward and
-// in the backward recompute, so both see bit-identical P.
+// summed; normalise and pack) keep 32 values live instead of 128.  The same arithmetic, in the same order
+// (the row sum as two 64-column halves), runs in the forward and in every backward recompute (including
+// the split-row one in attn_bwd_ws), so all see bit-identical P.
 __device__ __forceinline__ void softmax_row(uint32_t tS, int m, bool row_ok, float scale, uint32_t* p) {
   float v[32];
   float mx = -INFINITY;
@@ -124,7 +125,7 @@ __device__ __forceinline__ void softmax_row(uint32_t tS, int m, bool row_ok, flo
   }
   const float k2 = scale * 1.4426950408889634f;   // exp(x) = exp2(x log2 e)
   const float off = mx * k2;
-  float sum = 0.f;
+  float sh[2] = {0.f, 0.f};   // the row sum is (columns 0..63 in order) + (columns 64..127 in order)
 #pragma unroll
   for (int c = 0; c < ROWS / 32; ++c) {
     tmem_ld32(tS + c * 32, v);
@@ -132,10 +133,11 @@ __device__ __forceinline__ void softmax_row(uint32_t tS, int m, bool row_ok, flo
     for (int j = 0; j < 32; ++j) {
       const float e = (c * 32 + j) < m ? exp2f(fmaf(v[j], k2, -off)) : 0.f;
       v[j] = e;
-      sum += e;
+      sh[c >> 1] += e;
     }
     tmem_st32(tS + c * 32, v);
   }
+  const float sum = sh[0] + sh[1];
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   const float inv = row_ok ? 1.f / sum : 0.f;
 #pragma unroll
@@ -718,6 +720,253 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_pp(const __grid_constant__ CU
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ------------------------------------------------------------------ backward, dh = 128, store group
+// One CTA per SM (224 KB of shared memory), items pipelined instead of ping-ponged (two item stages of
+// Q | K | V | dO | P would need 320 KB):
+//   smem   Q | K  x 2 stages (the next item's Q, K arrive while this one runs), V, dO, P / dS.  The outputs
+//          are staged in the bytes of the inputs that are dead by then: dV in V (read by dP), dQ and dK in
+//          the item's Q and K (read by dQ / dK); each buffer is reloaded once its stores have read it.
+//   TMEM   two 256-column halves, item it in half it & 1:  S [0,128) -> dV -> dQ,  dP [128,256) -> dK.
+//          dQ overlays dV, so the dQ MMA waits until dV has been read out.
+//   warps  0 TMA producer, 1 MMA issuer, 2-9 softmax recompute + D + dS (two threads per query row, one
+//          per 64-column half; S and dP are read from TMEM once and kept in registers),
+//          10-13 output group: dV, dQ, dK rows out of TMEM -> bf16 -> swizzled staging -> TMA store
+//          (box 64 columns x m rows, so a ragged m never writes past its sample).
+__device__ __forceinline__ void tma_store2(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bar_sync_out() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void bar_sync_rows() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
+
+__global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CUtensorMap qkv,
+                                                      const __grid_constant__ CUtensorMap dom,
+                                                      const __grid_constant__ CUtensorMap dst,
+                                                      const __grid_constant__ Params p) {
+  pdl_release();
+  constexpr int DH = 128, NCH = 2;
+  constexpr uint32_t C_S = 0, C_DP = 128, C_DV = 0, C_DK = 128, C_DQ = 0;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = smem_u32(smem);
+  auto sQ = [&](int s) { return sbase + (uint32_t)(s * 4 * CHUNK); };
+  auto sK = [&](int s) { return sbase + (uint32_t)(s * 4 * CHUNK + 2 * CHUNK); };
+  const uint32_t sV = sbase + 8 * CHUNK, sdO = sV + 2 * CHUNK, sP = sdO + 2 * CHUNK;
+  uint64_t* bars = (uint64_t*)(smem + 14 * CHUNK);
+  auto B_ = [&](int i) { return smem_u32(bars + i); };
+  // 0,1 qk_full[s]  2,3 qk_free[s] (stores read)  4 vdo_full  5 s  6 dp  7 p(4)  8 dv  9 ds(4)
+  // 10 dv_drained(4)  11 dqk  12,13 tfree[half](4)  14 v_free (dV stores read)
+  uint32_t* tslot = (uint32_t*)(bars + 16);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&qkv) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&dom) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&dst) : "memory");
+    for (int i = 0; i < 15; ++i)
+      mbar_init(B_(i), (i == 7 || i == 9) ? 8 : (i == 10 || i == 12 || i == 13) ? 4 : 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  pdl_wait();
+  const int H = p.H, d = p.d, n = cta_items(p.items);
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer
+      for (int it = 0; it < n; ++it) {
+        const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it & 1;
+        if (it >= 2) mbar_wait(B_(2 + s), ((it >> 1) - 1) & 1);   // item it - 2's dQ / dK stores read Q, K
+        mbar_expect_tx(B_(s), 2 * NCH * CHUNK);
+        for (int c = 0; c < NCH; ++c) {
+          tma_load2(sQ(s) + c * CHUNK, &qkv, h * DH + 64 * c, b * p.m, B_(s));
+          tma_load2(sK(s) + c * CHUNK, &qkv, d + h * DH + 64 * c, b * p.m, B_(s));
+        }
+        if (it >= 1) mbar_wait(B_(8), (it - 1) & 1);   // dO of item it - 1 read by dV
+        mbar_expect_tx(B_(4), 2 * NCH * CHUNK);
+        for (int c = 0; c < NCH; ++c) tma_load2(sdO + c * CHUNK, &dom, h * DH + 64 * c, b * p.m, B_(4));
+        if (it >= 1) mbar_wait(B_(14), (it - 1) & 1);  // item it - 1's dV stores read V's bytes
+        for (int c = 0; c < NCH; ++c) tma_load2(sV + c * CHUNK, &qkv, 2 * d + h * DH + 64 * c, b * p.m, B_(4));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // ---------------- MMA issuer
+      const uint32_t id_sq = idesc(ROWS, false, false), id_t = idesc(DH, true, true), id_q = idesc(DH, false, true);
+      auto issueS = [&](int it) {
+        const int s = it & 1;
+        const uint32_t tg = tmem + (uint32_t)(s * 256);
+        if (it >= 2) mbar_wait(B_(12 + s), ((it >> 1) - 1) & 1);   // half drained (item it - 2)
+        mbar_wait(B_(s), (it >> 1) & 1);
+        tc_after();
+        mma_chain(tg + C_S, sQ(s), false, sK(s), false, id_sq, DH / 16);   // S = Q K^T
+        mma_commit(B_(5));
+      };
+      if (n > 0) issueS(0);
+      for (int it = 0; it < n; ++it) {
+        const int s = it & 1;
+        const uint32_t tg = tmem + (uint32_t)(s * 256), ph = it & 1;
+        mbar_wait(B_(4), ph);
+        tc_after();
+        mma_chain(tg + C_DP, sdO, false, sV, false, id_sq, DH / 16);   // dP = dO V^T
+        mma_commit(B_(6));
+        mbar_wait(B_(7), ph);   // P written
+        tc_after();
+        mma_chain(tg + C_DV, sP, true, sdO, true, id_t, ROWS / 16);    // dV = P^T dO
+        mma_commit(B_(8));
+        mbar_wait(B_(9), ph);   // dS written
+        if (it + 1 < n) issueS(it + 1);   // the next item's softmax input goes first
+        tc_after();
+        mma_chain(tg + C_DK, sP, true, sQ(s), true, id_t, ROWS / 16);  // dK = dS^T Q
+        mbar_wait(B_(10), ph);  // dV read out of TMEM (dQ overlays it)
+        tc_after();
+        mma_chain(tg + C_DQ, sP, false, sK(s), true, id_q, ROWS / 16); // dQ = dS K
+        mma_commit(B_(11));
+      }
+    }
+  } else if (warp < 10) {  // ---------------- softmax recompute, D, dS: two threads per query row
+    // warp w and w + 4 share TMEM lanes 32 (w % 4) ..; half hf owns columns [64 hf, 64 hf + 64) of S, P,
+    // dP, dS.  Row max, row sum and D = sum_j P_j dP_j are exchanged through xch[2][128].
+    const int hf = (warp - 2) >> 2, q4 = warp & 3, row = q4 * 32 + lane, c0 = 64 * hf;
+    const bool row_ok = row < p.m;
+    const float k2 = p.scale * 1.4426950408889634f;
+    float* xch = (float*)(smem + 14 * CHUNK + 256);
+    auto exchange = [&](float part) -> float2 {
+      bar_sync_rows();                 // the partner has read the previous exchange
+      xch[hf * ROWS + row] = part;
+      bar_sync_rows();
+      return make_float2(xch[row], xch[ROWS + row]);
+    };
+    for (int it = 0; it < n; ++it) {
+      const uint32_t ph = it & 1;
+      const uint32_t tl = tmem + (uint32_t)((it & 1) * 256) + ((uint32_t)(q4 * 32) << 16);
+      uint32_t pk[32];
+      float v[64];
+      mbar_wait(B_(5), ph);
+      tc_after();
+      tmem_ld32(tl + C_S + c0, v);
+      tmem_ld32(tl + C_S + c0 + 32, v + 32);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) mx = (c0 + j) < p.m ? fmaxf(mx, v[j]) : mx;
+      const float2 xm = exchange(mx);
+      const float off = fmaxf(xm.x, xm.y) * k2;
+      float sp = 0.f;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        v[j] = (c0 + j) < p.m ? exp2f(fmaf(v[j], k2, -off)) : 0.f;
+        sp += v[j];
+      }
+      const float2 xs = exchange(sp);
+      const float inv = row_ok ? 1.f / (xs.x + xs.y) : 0.f;
+#pragma unroll
+      for (int j = 0; j < 64; j += 2) pk[j / 2] = pack_bf2(v[j] * inv, v[j + 1] * inv);
+      if (it >= 1) mbar_wait(B_(11), (it - 1) & 1);   // dS of item it - 1 read by dQ / dK
+#pragma unroll
+      for (int g = 0; g < 8; ++g) sts16(swz(sP, row, hf, g), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+      fence_async_smem();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B_(7));
+      mbar_wait(B_(6), ph);
+      tc_after();
+      float Dp = 0.f;   // dP (fp32) is read from TMEM in 32-column pieces, twice: for D, then for dS
+#pragma unroll
+      for (int hc = 0; hc < 2; ++hc) {
+        tmem_ld32(tl + C_DP + c0 + 32 * hc, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          Dp = fmaf(__uint_as_float(pk[16 * hc + j] << 16), v[2 * j], Dp);
+          Dp = fmaf(__uint_as_float(pk[16 * hc + j] & 0xffff0000u), v[2 * j + 1], Dp);
+        }
+      }
+      const float2 xd = exchange(Dp);
+      const float D = xd.x + xd.y;
+      mbar_wait(B_(8), ph);   // dV done: P may be overwritten
+      tc_after();
+#pragma unroll
+      for (int hc = 0; hc < 2; ++hc) {
+        tmem_ld32(tl + C_DP + c0 + 32 * hc, v);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t qq[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint32_t w = pk[16 * hc + 4 * g + t];
+            qq[t] = pack_bf2(p.scale * __uint_as_float(w << 16) * (v[8 * g + 2 * t] - D),
+                             p.scale * __uint_as_float(w & 0xffff0000u) * (v[8 * g + 2 * t + 1] - D));
+          }
+          sts16(swz(sP, row, hf, 4 * hc + g), qq[0], qq[1], qq[2], qq[3]);
+        }
+      }
+      fence_async_smem();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B_(9));
+    }
+  } else {                 // ---------------- output group: TMEM -> staging -> TMA store
+    const int q4 = warp & 3, row = q4 * 32 + lane;
+    const bool leader = warp == 10 && lane == 0;
+    // 64 accumulator columns of this thread's row -> bf16 -> 128-B swizzled rows of the staging chunk
+    auto stage_chunk = [&](uint32_t taddr, uint32_t slot) {
+      float v[64];
+      tmem_ld32(taddr, v);
+      tmem_ld32(taddr + 32, v + 32);
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+        sts16(swz(slot, row, 0, g), pack_bf2(v[8 * g], v[8 * g + 1]), pack_bf2(v[8 * g + 2], v[8 * g + 3]),
+              pack_bf2(v[8 * g + 4], v[8 * g + 5]), pack_bf2(v[8 * g + 6], v[8 * g + 7]));
+    };
+    for (int it = 0; it < n; ++it) {
+      const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it & 1;
+      const uint32_t ph = it & 1;
+      const uint32_t tl = tmem + (uint32_t)((it & 1) * 256) + ((uint32_t)(q4 * 32) << 16);
+      const int row0 = b * p.m;
+      mbar_wait(B_(8), ph);   // dV done (and dP before it: V is dead)
+      tc_after();
+      for (int c = 0; c < NCH; ++c) stage_chunk(tl + C_DV + 64 * c, sV + c * CHUNK);
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B_(10));
+      fence_async_smem();
+      bar_sync_out();
+      if (leader) {
+        for (int c = 0; c < NCH; ++c) tma_store2(&dst, sV + c * CHUNK, 2 * d + h * DH + 64 * c, row0);
+        bulk_commit();
+        bulk_wait_read<0>();
+        mbar_arrive(B_(14));
+      }
+      mbar_wait(B_(11), ph);   // dQ, dK done (Q, K of this item are dead)
+      tc_after();
+      for (int c = 0; c < NCH; ++c) stage_chunk(tl + C_DQ + 64 * c, sQ(s) + c * CHUNK);
+      for (int c = 0; c < NCH; ++c) stage_chunk(tl + C_DK + 64 * c, sK(s) + c * CHUNK);
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B_(12 + (it & 1)));
+      fence_async_smem();
+      bar_sync_out();
+      if (leader) {
+        for (int c = 0; c < NCH; ++c) {
+          tma_store2(&dst, sQ(s) + c * CHUNK, h * DH + 64 * c, row0);
+          tma_store2(&dst, sK(s) + c * CHUNK, d + h * DH + 64 * c, row0);
+        }
+        bulk_commit();
+        bulk_wait_read<0>();
+        mbar_arrive(B_(2 + s));
+      }
+    }
+    if (leader) bulk_wait_all();
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -751,8 +1000,21 @@ static bool map2(CUtensorMap* map, const void* ptr, int cols, int64_t rows) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Store map over the same [B * m][cols] tensor with box 64 columns x m rows (one sample's rows exactly).
+static bool map2_store(CUtensorMap* map, const void* ptr, int cols, int64_t rows, int m) {
+  EncodeFn fn = encode_fn();
+  if (!fn || ((uintptr_t)ptr & 15) || (cols * 2) % 16 || m < 1 || m > ROWS) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)m}, es[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int g_mode = -1;   // DHEN_ATTN_FUSED: 0 = off (two batched GEMMs + softmax kernels), default on
 static int g_pp = [] { const char* e = getenv("DHEN_ATTN_PP"); return e ? atoi(e) : 1; }();   // ping-pong kernels
+static int g_ws = [] { const char* e = getenv("DHEN_ATTN_WS"); return e ? atoi(e) : 1; }();   // dh = 128 backward
 int set_mode(int mode) {
   if (g_mode < 0) { const char* e = getenv("DHEN_ATTN_FUSED"); g_mode = e ? atoi(e) : 1; }
   const int old = g_mode;
@@ -835,6 +1097,18 @@ cudaError_t core_bwd(const void* QKV, const void* dO, void* dQKV, int B, int H, 
     static bool a = false;
     if (!a) { cudaFuncSetAttribute(attn_bwd_pp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
     pdl_launch(attn_bwd_pp<2>, std::min(p.items, sms), 320, smem, st, mq, mo, p);
+    ++g_launches;
+    return cudaGetLastError();
+  }
+  if (g_ws && dh == 128) {   // pipelined items + TMA-store output group
+    CUtensorMap ms;
+    if (!map2_store(&ms, dQKV, 3 * d, (int64_t)B * m, m)) return cudaErrorNotSupported;
+    const int smem = 14 * CHUNK + 1024 + 256 + 2 * ROWS * 4;   // + row exchange
+    static int sms = 0;
+    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
+    static bool a = false;
+    if (!a) { cudaFuncSetAttribute(attn_bwd_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+    pdl_launch(attn_bwd_ws, std::min(p.items, sms), 448, smem, st, mq, mo, ms, p);
     ++g_launches;
     return cudaGetLastError();
   }
