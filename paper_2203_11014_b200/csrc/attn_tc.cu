@@ -740,20 +740,21 @@ __device__ __forceinline__ void tma_store2(const CUtensorMap* map, uint32_t src,
 __device__ __forceinline__ void bar_sync_out() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 __device__ __forceinline__ void bar_sync_rows() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
 
+template <int DH>
 __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CUtensorMap qkv,
                                                       const __grid_constant__ CUtensorMap dom,
                                                       const __grid_constant__ CUtensorMap dst,
                                                       const __grid_constant__ Params p) {
   pdl_release();
-  constexpr int DH = 128, NCH = 2;
-  constexpr uint32_t C_S = 0, C_DP = 128, C_DV = 0, C_DK = 128, C_DQ = 0;
+  constexpr int NCH = DH / 64, NB = 6 * NCH + 2;   // NB: 16-KB chunks of shared memory
+  constexpr uint32_t C_S = 0, C_DP = 128, C_DV = 0, C_DK = 128, C_DQ = DH == 64 ? 64 : 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
-  auto sQ = [&](int s) { return sbase + (uint32_t)(s * 4 * CHUNK); };
-  auto sK = [&](int s) { return sbase + (uint32_t)(s * 4 * CHUNK + 2 * CHUNK); };
-  const uint32_t sV = sbase + 8 * CHUNK, sdO = sV + 2 * CHUNK, sP = sdO + 2 * CHUNK;
-  uint64_t* bars = (uint64_t*)(smem + 14 * CHUNK);
+  auto sQ = [&](int s) { return sbase + (uint32_t)(s * 2 * NCH * CHUNK); };
+  auto sK = [&](int s) { return sbase + (uint32_t)(s * 2 * NCH * CHUNK + NCH * CHUNK); };
+  const uint32_t sV = sbase + 4 * NCH * CHUNK, sdO = sV + NCH * CHUNK, sP = sdO + NCH * CHUNK;
+  uint64_t* bars = (uint64_t*)(smem + NB * CHUNK);
   auto B_ = [&](int i) { return smem_u32(bars + i); };
   // 0,1 qk_full[s]  2,3 qk_free[s] (stores read)  4 vdo_full  5 s  6 dp  7 p(4)  8 dv  9 ds(4)
   // 10 dv_drained(4)  11 dqk  12,13 tfree[half](4)  14 v_free (dV stores read)
@@ -822,7 +823,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
         if (it + 1 < n) issueS(it + 1);   // the next item's softmax input goes first
         tc_after();
         mma_chain(tg + C_DK, sP, true, sQ(s), true, id_t, ROWS / 16);  // dK = dS^T Q
-        mbar_wait(B_(10), ph);  // dV read out of TMEM (dQ overlays it)
+        if (DH == 128) mbar_wait(B_(10), ph);  // dV read out of TMEM (dQ overlays it)
         tc_after();
         mma_chain(tg + C_DQ, sP, false, sK(s), true, id_q, ROWS / 16); // dQ = dS K
         mma_commit(B_(11));
@@ -834,7 +835,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
     const int hf = (warp - 2) >> 2, q4 = warp & 3, row = q4 * 32 + lane, c0 = 64 * hf;
     const bool row_ok = row < p.m;
     const float k2 = p.scale * 1.4426950408889634f;
-    float* xch = (float*)(smem + 14 * CHUNK + 256);
+    float* xch = (float*)(smem + NB * CHUNK + 256);
     auto exchange = [&](float part) -> float2 {
       bar_sync_rows();                 // the partner has read the previous exchange
       xch[hf * ROWS + row] = part;
@@ -1090,6 +1091,24 @@ cudaError_t core_bwd(const void* QKV, const void* dO, void* dQKV, int B, int H, 
   Params p;
   p.items = B * H; p.H = H; p.m = m; p.d = d; p.scale = 1.f / sqrtf((float)dh); p.out = (__nv_bfloat16*)dQKV;
   const int nch = dh / 64;
+  if (g_ws) {   // pipelined items + split-row softmax + TMA-store output group
+    CUtensorMap ms;
+    if (!map2_store(&ms, dQKV, 3 * d, (int64_t)B * m, m)) return cudaErrorNotSupported;
+    const int smem = (6 * nch + 2) * CHUNK + 1024 + 256 + 2 * ROWS * 4;   // + row exchange
+    static int sms = 0;
+    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
+    if (dh == 64) {
+      static bool a = false;
+      if (!a) { cudaFuncSetAttribute(attn_bwd_ws<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+      pdl_launch(attn_bwd_ws<64>, std::min(p.items, sms), 448, smem, st, mq, mo, ms, p);
+    } else {
+      static bool a = false;
+      if (!a) { cudaFuncSetAttribute(attn_bwd_ws<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+      pdl_launch(attn_bwd_ws<128>, std::min(p.items, sms), 448, smem, st, mq, mo, ms, p);
+    }
+    ++g_launches;
+    return cudaGetLastError();
+  }
   if (g_pp && dh == 64) {   // ping-pong backward (two 96-KB stages, two consumer groups)
     const int smem = 2 * 6 * CHUNK + 1024 + 256;
     static int sms = 0;
@@ -1097,18 +1116,6 @@ cudaError_t core_bwd(const void* QKV, const void* dO, void* dQKV, int B, int H, 
     static bool a = false;
     if (!a) { cudaFuncSetAttribute(attn_bwd_pp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
     pdl_launch(attn_bwd_pp<2>, std::min(p.items, sms), 320, smem, st, mq, mo, p);
-    ++g_launches;
-    return cudaGetLastError();
-  }
-  if (g_ws && dh == 128) {   // pipelined items + TMA-store output group
-    CUtensorMap ms;
-    if (!map2_store(&ms, dQKV, 3 * d, (int64_t)B * m, m)) return cudaErrorNotSupported;
-    const int smem = 14 * CHUNK + 1024 + 256 + 2 * ROWS * 4;   // + row exchange
-    static int sms = 0;
-    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
-    static bool a = false;
-    if (!a) { cudaFuncSetAttribute(attn_bwd_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-    pdl_launch(attn_bwd_ws, std::min(p.items, sms), 448, smem, st, mq, mo, ms, p);
     ++g_launches;
     return cudaGetLastError();
   }
