@@ -739,6 +739,51 @@ __device__ __forceinline__ void tma_store2(const CUtensorMap* map, uint32_t src,
 }
 __device__ __forceinline__ void bar_sync_out() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 __device__ __forceinline__ void bar_sync_rows() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
+// Row partials of the two threads that share a query row (warps w, w + 4 of the 8-warp row group):
+// returns (half 0's, half 1's).  The leading barrier keeps a partner from overwriting a value not yet read.
+__device__ __forceinline__ float2 row_exchange(float* xch, int hf, int row, float part) {
+  bar_sync_rows();
+  xch[hf * ROWS + row] = part;
+  bar_sync_rows();
+  return make_float2(xch[row], xch[ROWS + row]);
+}
+// 64 fp32 accumulator columns of this thread's TMEM lane -> bf16 -> row `row` of a 128-B swizzled
+// staging chunk (the layout a SWIZZLE_128B TMA store reads)
+__device__ __forceinline__ void stage_row64(uint32_t taddr, uint32_t slot, int row) {
+  float v[64];
+  tmem_ld32(taddr, v);
+  tmem_ld32(taddr + 32, v + 32);
+#pragma unroll
+  for (int g = 0; g < 8; ++g)
+    sts16(swz(slot, row, 0, g), pack_bf2(v[8 * g], v[8 * g + 1]), pack_bf2(v[8 * g + 2], v[8 * g + 3]),
+          pack_bf2(v[8 * g + 4], v[8 * g + 5]), pack_bf2(v[8 * g + 6], v[8 * g + 7]));
+}
+// Split-row softmax: this thread's 64-column half (c0 = 64 hf) of its S row (TMEM, tS = the row's lane
+// base) into bf16 P pairs pk[32].  Same arithmetic and order as softmax_row: max over the row, e =
+// exp2(S k2 - max k2), sum = (half 0 in order) + (half 1 in order), P = e * (1 / sum).
+__device__ __forceinline__ void split_softmax(uint32_t tS, int hf, int row, int m, float scale, float* xch,
+                                              uint32_t* pk) {
+  const int c0 = 64 * hf;
+  const float k2 = scale * 1.4426950408889634f;
+  float v[64];
+  tmem_ld32(tS + c0, v);
+  tmem_ld32(tS + c0 + 32, v + 32);
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 64; ++j) mx = (c0 + j) < m ? fmaxf(mx, v[j]) : mx;
+  const float2 xm = row_exchange(xch, hf, row, mx);
+  const float off = fmaxf(xm.x, xm.y) * k2;
+  float sp = 0.f;
+#pragma unroll
+  for (int j = 0; j < 64; ++j) {
+    v[j] = (c0 + j) < m ? exp2f(fmaf(v[j], k2, -off)) : 0.f;
+    sp += v[j];
+  }
+  const float2 xs = row_exchange(xch, hf, row, sp);
+  const float inv = row < m ? 1.f / (xs.x + xs.y) : 0.f;
+#pragma unroll
+  for (int j = 0; j < 64; j += 2) pk[j / 2] = pack_bf2(v[j] * inv, v[j + 1] * inv);
+}
 
 template <int DH>
 __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CUtensorMap qkv,
@@ -833,39 +878,15 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
     // warp w and w + 4 share TMEM lanes 32 (w % 4) ..; half hf owns columns [64 hf, 64 hf + 64) of S, P,
     // dP, dS.  Row max, row sum and D = sum_j P_j dP_j are exchanged through xch[2][128].
     const int hf = (warp - 2) >> 2, q4 = warp & 3, row = q4 * 32 + lane, c0 = 64 * hf;
-    const bool row_ok = row < p.m;
-    const float k2 = p.scale * 1.4426950408889634f;
     float* xch = (float*)(smem + NB * CHUNK + 256);
-    auto exchange = [&](float part) -> float2 {
-      bar_sync_rows();                 // the partner has read the previous exchange
-      xch[hf * ROWS + row] = part;
-      bar_sync_rows();
-      return make_float2(xch[row], xch[ROWS + row]);
-    };
     for (int it = 0; it < n; ++it) {
       const uint32_t ph = it & 1;
       const uint32_t tl = tmem + (uint32_t)((it & 1) * 256) + ((uint32_t)(q4 * 32) << 16);
       uint32_t pk[32];
-      float v[64];
+      float v[32];
       mbar_wait(B_(5), ph);
       tc_after();
-      tmem_ld32(tl + C_S + c0, v);
-      tmem_ld32(tl + C_S + c0 + 32, v + 32);
-      float mx = -INFINITY;
-#pragma unroll
-      for (int j = 0; j < 64; ++j) mx = (c0 + j) < p.m ? fmaxf(mx, v[j]) : mx;
-      const float2 xm = exchange(mx);
-      const float off = fmaxf(xm.x, xm.y) * k2;
-      float sp = 0.f;
-#pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        v[j] = (c0 + j) < p.m ? exp2f(fmaf(v[j], k2, -off)) : 0.f;
-        sp += v[j];
-      }
-      const float2 xs = exchange(sp);
-      const float inv = row_ok ? 1.f / (xs.x + xs.y) : 0.f;
-#pragma unroll
-      for (int j = 0; j < 64; j += 2) pk[j / 2] = pack_bf2(v[j] * inv, v[j + 1] * inv);
+      split_softmax(tl + C_S, hf, row, p.m, p.scale, xch, pk);
       if (it >= 1) mbar_wait(B_(11), (it - 1) & 1);   // dS of item it - 1 read by dQ / dK
 #pragma unroll
       for (int g = 0; g < 8; ++g) sts16(swz(sP, row, hf, g), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
@@ -885,7 +906,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
           Dp = fmaf(__uint_as_float(pk[16 * hc + j] & 0xffff0000u), v[2 * j + 1], Dp);
         }
       }
-      const float2 xd = exchange(Dp);
+      const float2 xd = row_exchange(xch, hf, row, Dp);
       const float D = xd.x + xd.y;
       mbar_wait(B_(8), ph);   // dV done: P may be overwritten
       tc_after();
@@ -912,16 +933,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
   } else {                 // ---------------- output group: TMEM -> staging -> TMA store
     const int q4 = warp & 3, row = q4 * 32 + lane;
     const bool leader = warp == 10 && lane == 0;
-    // 64 accumulator columns of this thread's row -> bf16 -> 128-B swizzled rows of the staging chunk
-    auto stage_chunk = [&](uint32_t taddr, uint32_t slot) {
-      float v[64];
-      tmem_ld32(taddr, v);
-      tmem_ld32(taddr + 32, v + 32);
-#pragma unroll
-      for (int g = 0; g < 8; ++g)
-        sts16(swz(slot, row, 0, g), pack_bf2(v[8 * g], v[8 * g + 1]), pack_bf2(v[8 * g + 2], v[8 * g + 3]),
-              pack_bf2(v[8 * g + 4], v[8 * g + 5]), pack_bf2(v[8 * g + 6], v[8 * g + 7]));
-    };
+    auto stage_chunk = [&](uint32_t taddr, uint32_t slot) { stage_row64(taddr, slot, row); };
     for (int it = 0; it < n; ++it) {
       const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it & 1;
       const uint32_t ph = it & 1;
@@ -966,6 +978,131 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
   __syncthreads();
   tc_after();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+
+// ------------------------------------------------------------------ forward, store group
+// Same roles as attn_bwd_ws: warps 0 TMA, 1 MMA, 2-9 split-row softmax, 10-13 O out of TMEM -> staging ->
+// TMA store.  NS stages of Q | K | V; P overlays Q (and K when dh = 64) once S is done, and O is staged
+// in the same bytes once P V is done, so a stage is free again when O's store has read it.  TMEM: two
+// 128-column halves (item it in half it & 1), S [0,128) then O [0, dh) over it.
+template <int DH, int NS>
+__global__ void __launch_bounds__(448, 1) attn_fwd_ws(const __grid_constant__ CUtensorMap qkv,
+                                                      const __grid_constant__ CUtensorMap ost,
+                                                      const __grid_constant__ Params p) {
+  pdl_release();
+  constexpr int NCH = DH / 64, STG = 3 * NCH * CHUNK;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bars = (uint64_t*)(smem + NS * STG);
+  auto B_ = [&](int i) { return smem_u32(bars + i); };
+  // [0,NS) qk_full  [NS,2NS) v_full  [2NS,3NS) stage free (O stored)  then per half h:
+  // 3NS+h s_full, 3NS+2+h p_full(8), 3NS+4+h o_full, 3NS+6+h tfree(4)
+  const int GB = 3 * NS;
+  uint32_t* tslot = (uint32_t*)(bars + GB + 8);
+  float* xch = (float*)(smem + NS * STG + 256);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&qkv) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&ost) : "memory");
+    for (int i = 0; i < GB; ++i) mbar_init(B_(i), 1);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(B_(GB + h), 1); mbar_init(B_(GB + 2 + h), 8); mbar_init(B_(GB + 4 + h), 1); mbar_init(B_(GB + 6 + h), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  pdl_wait();
+  const int H = p.H, d = p.d, n = cta_items(p.items);
+  auto sQ = [&](int s) { return sbase + (uint32_t)(s * STG); };
+  auto sK = [&](int s) { return sbase + (uint32_t)(s * STG + NCH * CHUNK); };
+  auto sV = [&](int s) { return sbase + (uint32_t)(s * STG + 2 * NCH * CHUNK); };
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer
+      for (int it = 0; it < n; ++it) {
+        const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS;
+        if (it >= NS) mbar_wait(B_(2 * NS + s), ((it / NS) - 1) & 1);   // item it - NS's O store read the stage
+        mbar_expect_tx(B_(s), 2 * NCH * CHUNK);
+        for (int c = 0; c < NCH; ++c) {
+          tma_load2(sQ(s) + c * CHUNK, &qkv, h * DH + 64 * c, b * p.m, B_(s));
+          tma_load2(sK(s) + c * CHUNK, &qkv, d + h * DH + 64 * c, b * p.m, B_(s));
+        }
+        mbar_expect_tx(B_(NS + s), NCH * CHUNK);
+        for (int c = 0; c < NCH; ++c) tma_load2(sV(s) + c * CHUNK, &qkv, 2 * d + h * DH + 64 * c, b * p.m, B_(NS + s));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // ---------------- MMA issuer
+      const uint32_t id_s = idesc(ROWS, false, false), id_o = idesc(DH, false, true);
+      auto issueS = [&](int it) {
+        const int s = it % NS, hh = it & 1;
+        if (it >= 2) mbar_wait(B_(GB + 6 + hh), ((it >> 1) - 1) & 1);   // O of item it - 2 read out
+        mbar_wait(B_(s), (it / NS) & 1);
+        tc_after();
+        mma_chain(tmem + hh * 128, sQ(s), false, sK(s), false, id_s, DH / 16);   // S = Q K^T
+        mma_commit(B_(GB + hh));
+      };
+      if (n > 0) issueS(0);
+      for (int it = 0; it < n; ++it) {
+        if (it + 1 < n) issueS(it + 1);
+        const int s = it % NS, hh = it & 1;
+        mbar_wait(B_(GB + 2 + hh), (it >> 1) & 1);   // P written
+        mbar_wait(B_(NS + s), (it / NS) & 1);        // V landed
+        tc_after();
+        mma_chain(tmem + hh * 128, sQ(s), false, sV(s), true, id_o, ROWS / 16);   // O = P V (P overlays Q)
+        mma_commit(B_(GB + 4 + hh));
+      }
+    }
+  } else if (warp < 10) {  // ---------------- split-row softmax
+    const int hf = (warp - 2) >> 2, q4 = warp & 3, row = q4 * 32 + lane;
+    for (int it = 0; it < n; ++it) {
+      const int s = it % NS, hh = it & 1;
+      mbar_wait(B_(GB + hh), (it >> 1) & 1);
+      tc_after();
+      uint32_t pk[32];
+      split_softmax(tmem + (uint32_t)(hh * 128) + ((uint32_t)(q4 * 32) << 16), hf, row, p.m, p.scale, xch, pk);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) sts16(swz(sQ(s), row, hf, g), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+      fence_async_smem();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B_(GB + 2 + hh));
+    }
+  } else {                 // ---------------- output group
+    const int q4 = warp & 3, row = q4 * 32 + lane;
+    const bool leader = warp == 10 && lane == 0;
+    for (int it = 0; it < n; ++it) {
+      const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS, hh = it & 1;
+      mbar_wait(B_(GB + 4 + hh), (it >> 1) & 1);   // O done (P, i.e. Q's bytes, dead)
+      tc_after();
+      const uint32_t tl = tmem + (uint32_t)(hh * 128) + ((uint32_t)(q4 * 32) << 16);
+      for (int c = 0; c < NCH; ++c) stage_row64(tl + 64 * c, sQ(s) + c * CHUNK, row);
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B_(GB + 6 + hh));
+      fence_async_smem();
+      bar_sync_out();
+      if (leader) {
+        for (int c = 0; c < NCH; ++c) tma_store2(&ost, sQ(s) + c * CHUNK, h * DH + 64 * c, b * p.m);
+        bulk_commit();
+        bulk_wait_read<0>();
+        mbar_arrive(B_(2 * NS + s));
+      }
+    }
+    if (leader) bulk_wait_all();
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
 // ------------------------------------------------------------------ host side
@@ -1051,6 +1188,26 @@ cudaError_t core_fwd(const void* QKV, void* O, int B, int H, int m, int d, cudaS
   Params p;
   p.items = B * H; p.H = H; p.m = m; p.d = d; p.scale = 1.f / sqrtf((float)dh); p.out = (__nv_bfloat16*)O;
   const int nch = dh / 64;
+  if (g_ws) {   // split-row softmax + TMA-store output group, 192 KB of item stages
+    CUtensorMap ms;
+    if (!map2_store(&ms, O, d, (int64_t)B * m, m)) return cudaErrorNotSupported;
+    const int ns = dh == 64 ? 4 : 2;
+    const int smem = ns * 3 * nch * CHUNK + 1024 + 256 + 2 * ROWS * 4;
+    static int sms = 0;
+    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
+    const int grid = std::min(p.items, sms);
+    if (dh == 64) {
+      static bool a = false;
+      if (!a) { cudaFuncSetAttribute(attn_fwd_ws<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+      pdl_launch(attn_fwd_ws<64, 4>, grid, 448, smem, st, mq, ms, p);
+    } else {
+      static bool a = false;
+      if (!a) { cudaFuncSetAttribute(attn_fwd_ws<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+      pdl_launch(attn_fwd_ws<128, 2>, grid, 448, smem, st, mq, ms, p);
+    }
+    ++g_launches;
+    return cudaGetLastError();
+  }
   if (g_pp) {   // ping-pong: one CTA per SM, two consumer groups, 192 KB of item stages
     const int ns = dh == 64 ? 4 : 2;
     const int smem = ns * 3 * nch * CHUNK + 1024 + 256;
