@@ -109,11 +109,36 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
       "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
       : "memory");
 }
-// Softmax of this thread's S row (TMEM lane) into bf16 P, packed two per word (p[j/2]); rows >= m and
-// columns >= m give 0.  Three passes over the row in 32-column chunks (max; exp written back to TMEM and
-// summed; normalise and pack) keep 32 values live instead of 128.  The same arithmetic, in the same order
-// (the row sum as two 64-column halves), runs in the forward and in every backward recompute (including
-// the split-row one in attn_bwd_ws), so all see bit-identical P.
+// Packed fp32 pairs (FFMA2 / FADD2 / FMUL2 on sm_100): each lane is an ordinary rounded fma / add / mul.
+__device__ __forceinline__ uint64_t f2u(float2 a) { return *reinterpret_cast<uint64_t*>(&a); }
+__device__ __forceinline__ float2 u2f(uint64_t a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+  return u2f(r);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+__device__ __forceinline__ float ex2(float x) {   // 2^x, MUFU.EX2 (ex2(-inf) = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// The softmax arithmetic, fixed so that every kernel that forms P (forward, and each backward recompute)
+// gets bit-identical values:  columns >= m read as -inf;  mx = row max;  e_j = ex2(fma(S_j, k2, -mx k2))
+// with k2 = scale log2(e);  per 64-column half, two running sums over the even and odd columns in order,
+// half sum = even + odd, row sum = half 0 + half 1;  P_j = e_j * (1 / sum)  (0 for rows >= m).
+//
+// Whole row per thread (the older kernels): three passes over 32-column chunks (max; exp written back
+// to TMEM and summed; normalise and pack) keep 32 values live instead of 128.
 __device__ __forceinline__ void softmax_row(uint32_t tS, int m, bool row_ok, float scale, uint32_t* p) {
   float v[32];
   float mx = -INFINITY;
@@ -125,19 +150,19 @@ __device__ __forceinline__ void softmax_row(uint32_t tS, int m, bool row_ok, flo
   }
   const float k2 = scale * 1.4426950408889634f;   // exp(x) = exp2(x log2 e)
   const float off = mx * k2;
-  float sh[2] = {0.f, 0.f};   // the row sum is (columns 0..63 in order) + (columns 64..127 in order)
+  float se[2] = {0.f, 0.f}, so[2] = {0.f, 0.f};
 #pragma unroll
   for (int c = 0; c < ROWS / 32; ++c) {
     tmem_ld32(tS + c * 32, v);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const float e = (c * 32 + j) < m ? exp2f(fmaf(v[j], k2, -off)) : 0.f;
+      const float e = ex2(fmaf((c * 32 + j) < m ? v[j] : -INFINITY, k2, -off));
       v[j] = e;
-      sh[c >> 1] += e;
+      if (j & 1) so[c >> 1] += e; else se[c >> 1] += e;
     }
     tmem_st32(tS + c * 32, v);
   }
-  const float sum = sh[0] + sh[1];
+  const float sum = (se[0] + so[0]) + (se[1] + so[1]);
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   const float inv = row_ok ? 1.f / sum : 0.f;
 #pragma unroll
@@ -739,14 +764,6 @@ __device__ __forceinline__ void tma_store2(const CUtensorMap* map, uint32_t src,
 }
 __device__ __forceinline__ void bar_sync_out() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 __device__ __forceinline__ void bar_sync_rows() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
-// Row partials of the two threads that share a query row (warps w, w + 4 of the 8-warp row group):
-// returns (half 0's, half 1's).  The leading barrier keeps a partner from overwriting a value not yet read.
-__device__ __forceinline__ float2 row_exchange(float* xch, int hf, int row, float part) {
-  bar_sync_rows();
-  xch[hf * ROWS + row] = part;
-  bar_sync_rows();
-  return make_float2(xch[row], xch[ROWS + row]);
-}
 // 64 fp32 accumulator columns of this thread's TMEM lane -> bf16 -> row `row` of a 128-B swizzled
 // staging chunk (the layout a SWIZZLE_128B TMA store reads)
 __device__ __forceinline__ void stage_row64(uint32_t taddr, uint32_t slot, int row) {
@@ -758,31 +775,53 @@ __device__ __forceinline__ void stage_row64(uint32_t taddr, uint32_t slot, int r
     sts16(swz(slot, row, 0, g), pack_bf2(v[8 * g], v[8 * g + 1]), pack_bf2(v[8 * g + 2], v[8 * g + 3]),
           pack_bf2(v[8 * g + 4], v[8 * g + 5]), pack_bf2(v[8 * g + 6], v[8 * g + 7]));
 }
+// Row partials of the two threads that share a query row (warps w, w + 4 of the 8-warp row group),
+// through xch[2][128] (shared-window address): returns (half 0's, half 1's).  The leading barrier keeps a
+// partner from overwriting a value not yet read.
+__device__ __forceinline__ float2 row_exchange(uint32_t xch, int hf, int row, float part) {
+  bar_sync_rows();
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(xch + (uint32_t)(hf * ROWS + row) * 4), "f"(part) : "memory");
+  bar_sync_rows();
+  float2 r;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r.x) : "r"(xch + (uint32_t)row * 4) : "memory");
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r.y) : "r"(xch + (uint32_t)(ROWS + row) * 4) : "memory");
+  return r;
+}
 // Split-row softmax: this thread's 64-column half (c0 = 64 hf) of its S row (TMEM, tS = the row's lane
-// base) into bf16 P pairs pk[32].  Same arithmetic and order as softmax_row: max over the row, e =
-// exp2(S k2 - max k2), sum = (half 0 in order) + (half 1 in order), P = e * (1 / sum).
-__device__ __forceinline__ void split_softmax(uint32_t tS, int hf, int row, int m, float scale, float* xch,
+// base) into bf16 P pairs pk[32], with softmax_row's arithmetic (above).
+__device__ __forceinline__ void split_softmax(uint32_t tS, int hf, int row, int m, float scale, uint32_t xch,
                                               uint32_t* pk) {
-  const int c0 = 64 * hf;
+  const int c0 = 64 * hf, L = m - c0;
   const float k2 = scale * 1.4426950408889634f;
   float v[64];
   tmem_ld32(tS + c0, v);
   tmem_ld32(tS + c0 + 32, v + 32);
-  float mx = -INFINITY;
+  if (L < 64) {
 #pragma unroll
-  for (int j = 0; j < 64; ++j) mx = (c0 + j) < m ? fmaxf(mx, v[j]) : mx;
+    for (int j = 0; j < 64; ++j) v[j] = j < L ? v[j] : -INFINITY;
+  }
+  float mx = v[0];
+#pragma unroll
+  for (int j = 1; j < 64; ++j) mx = fmaxf(mx, v[j]);
   const float2 xm = row_exchange(xch, hf, row, mx);
   const float off = fmaxf(xm.x, xm.y) * k2;
-  float sp = 0.f;
+  const float2 kk = make_float2(k2, k2), oo = make_float2(-off, -off);
+  float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int j = 0; j < 64; ++j) {
-    v[j] = (c0 + j) < m ? exp2f(fmaf(v[j], k2, -off)) : 0.f;
-    sp += v[j];
+  for (int j = 0; j < 64; j += 2) {
+    const float2 t = fma2(make_float2(v[j], v[j + 1]), kk, oo);
+    v[j] = ex2(t.x);
+    v[j + 1] = ex2(t.y);
+    acc = add2(acc, make_float2(v[j], v[j + 1]));
   }
-  const float2 xs = row_exchange(xch, hf, row, sp);
+  const float2 xs = row_exchange(xch, hf, row, acc.x + acc.y);
   const float inv = row < m ? 1.f / (xs.x + xs.y) : 0.f;
+  const float2 ii = make_float2(inv, inv);
 #pragma unroll
-  for (int j = 0; j < 64; j += 2) pk[j / 2] = pack_bf2(v[j] * inv, v[j + 1] * inv);
+  for (int j = 0; j < 64; j += 2) {
+    const float2 q = mul2(make_float2(v[j], v[j + 1]), ii);
+    pk[j / 2] = pack_bf2(q.x, q.y);
+  }
 }
 
 template <int DH>
@@ -878,7 +917,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
     // warp w and w + 4 share TMEM lanes 32 (w % 4) ..; half hf owns columns [64 hf, 64 hf + 64) of S, P,
     // dP, dS.  Row max, row sum and D = sum_j P_j dP_j are exchanged through xch[2][128].
     const int hf = (warp - 2) >> 2, q4 = warp & 3, row = q4 * 32 + lane, c0 = 64 * hf;
-    float* xch = (float*)(smem + NB * CHUNK + 256);
+    const uint32_t xch = smem_u32(smem + NB * CHUNK + 256);
     for (int it = 0; it < n; ++it) {
       const uint32_t ph = it & 1;
       const uint32_t tl = tmem + (uint32_t)((it & 1) * 256) + ((uint32_t)(q4 * 32) << 16);
@@ -896,18 +935,21 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
       if (lane == 0) mbar_arrive(B_(7));
       mbar_wait(B_(6), ph);
       tc_after();
-      float Dp = 0.f;   // dP (fp32) is read from TMEM in 32-column pieces, twice: for D, then for dS
+      float2 Dp2 = make_float2(0.f, 0.f);   // dP (fp32) is read from TMEM in 32-column pieces, twice: for D, then dS
 #pragma unroll
       for (int hc = 0; hc < 2; ++hc) {
         tmem_ld32(tl + C_DP + c0 + 32 * hc, v);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          Dp = fmaf(__uint_as_float(pk[16 * hc + j] << 16), v[2 * j], Dp);
-          Dp = fmaf(__uint_as_float(pk[16 * hc + j] & 0xffff0000u), v[2 * j + 1], Dp);
+          const uint32_t w = pk[16 * hc + j];
+          Dp2 = fma2(make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u)),
+                     make_float2(v[2 * j], v[2 * j + 1]), Dp2);
         }
       }
+      const float Dp = Dp2.x + Dp2.y;
       const float2 xd = row_exchange(xch, hf, row, Dp);
       const float D = xd.x + xd.y;
+      const float2 sc2 = make_float2(p.scale, p.scale), nD2 = make_float2(-D, -D);
       mbar_wait(B_(8), ph);   // dV done: P may be overwritten
       tc_after();
 #pragma unroll
@@ -917,10 +959,11 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
         for (int g = 0; g < 4; ++g) {
           uint32_t qq[4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
+          for (int t = 0; t < 4; ++t) {   // dS = (scale P) (dP - D)
             const uint32_t w = pk[16 * hc + 4 * g + t];
-            qq[t] = pack_bf2(p.scale * __uint_as_float(w << 16) * (v[8 * g + 2 * t] - D),
-                             p.scale * __uint_as_float(w & 0xffff0000u) * (v[8 * g + 2 * t + 1] - D));
+            const float2 sp = mul2(make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u)), sc2);
+            const float2 q = mul2(sp, add2(make_float2(v[8 * g + 2 * t], v[8 * g + 2 * t + 1]), nD2));
+            qq[t] = pack_bf2(q.x, q.y);
           }
           sts16(swz(sP, row, hf, 4 * hc + g), qq[0], qq[1], qq[2], qq[3]);
         }
@@ -983,8 +1026,8 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
 
 // ------------------------------------------------------------------ forward, store group
 // Same roles as attn_bwd_ws: warps 0 TMA, 1 MMA, 2-9 split-row softmax, 10-13 O out of TMEM -> staging ->
-// TMA store.  NS stages of Q | K | V; P overlays Q (and K when dh = 64) once S is done, and O is staged
-// in the same bytes once P V is done, so a stage is free again when O's store has read it.  TMEM: two
+// TMA store.  NS stages of Q | K | V; P overlays Q (and K when dh = 64) once S is done, and a stage is
+// free again as soon as P V is done; O goes through its own staging buffer (dh / 64 chunks).  TMEM: two
 // 128-column halves (item it in half it & 1), S [0,128) then O [0, dh) over it.
 template <int DH, int NS>
 __global__ void __launch_bounds__(448, 1) attn_fwd_ws(const __grid_constant__ CUtensorMap qkv,
@@ -995,13 +1038,14 @@ __global__ void __launch_bounds__(448, 1) attn_fwd_ws(const __grid_constant__ CU
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
-  uint64_t* bars = (uint64_t*)(smem + NS * STG);
+  const uint32_t sO = sbase + (uint32_t)(NS * STG);
+  uint64_t* bars = (uint64_t*)(smem + NS * STG + NCH * CHUNK);
   auto B_ = [&](int i) { return smem_u32(bars + i); };
-  // [0,NS) qk_full  [NS,2NS) v_full  [2NS,3NS) stage free (O stored)  then per half h:
+  // [0,NS) qk_full  [NS,2NS) v_full  [2NS,3NS) stage free (P V done)  then per half h:
   // 3NS+h s_full, 3NS+2+h p_full(8), 3NS+4+h o_full, 3NS+6+h tfree(4)
   const int GB = 3 * NS;
   uint32_t* tslot = (uint32_t*)(bars + GB + 8);
-  float* xch = (float*)(smem + NS * STG + 256);
+  const uint32_t xch = smem_u32(smem + NS * STG + NCH * CHUNK + 256);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&qkv) : "memory");
@@ -1029,7 +1073,7 @@ __global__ void __launch_bounds__(448, 1) attn_fwd_ws(const __grid_constant__ CU
     if (lane == 0) {   // ---------------- TMA producer
       for (int it = 0; it < n; ++it) {
         const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS;
-        if (it >= NS) mbar_wait(B_(2 * NS + s), ((it / NS) - 1) & 1);   // item it - NS's O store read the stage
+        if (it >= NS) mbar_wait(B_(2 * NS + s), ((it / NS) - 1) & 1);   // P V of item it - NS done
         mbar_expect_tx(B_(s), 2 * NCH * CHUNK);
         for (int c = 0; c < NCH; ++c) {
           tma_load2(sQ(s) + c * CHUNK, &qkv, h * DH + 64 * c, b * p.m, B_(s));
@@ -1059,6 +1103,7 @@ __global__ void __launch_bounds__(448, 1) attn_fwd_ws(const __grid_constant__ CU
         tc_after();
         mma_chain(tmem + hh * 128, sQ(s), false, sV(s), true, id_o, ROWS / 16);   // O = P V (P overlays Q)
         mma_commit(B_(GB + 4 + hh));
+        mma_commit(B_(2 * NS + s));
       }
     }
   } else if (warp < 10) {  // ---------------- split-row softmax
@@ -1080,21 +1125,21 @@ __global__ void __launch_bounds__(448, 1) attn_fwd_ws(const __grid_constant__ CU
     const int q4 = warp & 3, row = q4 * 32 + lane;
     const bool leader = warp == 10 && lane == 0;
     for (int it = 0; it < n; ++it) {
-      const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS, hh = it & 1;
-      mbar_wait(B_(GB + 4 + hh), (it >> 1) & 1);   // O done (P, i.e. Q's bytes, dead)
+      const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, hh = it & 1;
+      mbar_wait(B_(GB + 4 + hh), (it >> 1) & 1);   // O done
       tc_after();
+      if (leader) bulk_wait_read<0>();   // the previous item's O store has read the staging buffer
+      bar_sync_out();
       const uint32_t tl = tmem + (uint32_t)(hh * 128) + ((uint32_t)(q4 * 32) << 16);
-      for (int c = 0; c < NCH; ++c) stage_row64(tl + 64 * c, sQ(s) + c * CHUNK, row);
+      for (int c = 0; c < NCH; ++c) stage_row64(tl + 64 * c, sO + c * CHUNK, row);
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(B_(GB + 6 + hh));
       fence_async_smem();
       bar_sync_out();
       if (leader) {
-        for (int c = 0; c < NCH; ++c) tma_store2(&ost, sQ(s) + c * CHUNK, h * DH + 64 * c, b * p.m);
+        for (int c = 0; c < NCH; ++c) tma_store2(&ost, sO + c * CHUNK, h * DH + 64 * c, b * p.m);
         bulk_commit();
-        bulk_wait_read<0>();
-        mbar_arrive(B_(2 * NS + s));
       }
     }
     if (leader) bulk_wait_all();
@@ -1192,7 +1237,7 @@ cudaError_t core_fwd(const void* QKV, void* O, int B, int H, int m, int d, cudaS
     CUtensorMap ms;
     if (!map2_store(&ms, O, d, (int64_t)B * m, m)) return cudaErrorNotSupported;
     const int ns = dh == 64 ? 4 : 2;
-    const int smem = ns * 3 * nch * CHUNK + 1024 + 256 + 2 * ROWS * 4;
+    const int smem = (ns * 3 + 1) * nch * CHUNK + 1024 + 256 + 2 * ROWS * 4;
     static int sms = 0;
     if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
     const int grid = std::min(p.items, sms);
