@@ -986,6 +986,15 @@ __global__ void __launch_bounds__(320, 1)
         }
         __syncwarp();
       }
+      // ReLU-bitmask words of the warp's rows x HC columns, also fetched before the accumulator is ready
+      constexpr bool BMV = VAR > 0 && (VarF<VAR>::F & EF_BMASK) != 0;
+      uint32_t bpre[BMV ? HC / 32 : 1];
+      if constexpr (BMV) {
+        const int row_ = m0 + (int)crank * BM + q4 * 32 + lane;
+        const uint32_t* bp = e.bits + (int64_t)((n0 + hh * HC) / 32) * e.bits_ld + row_;   // word-major: lanes coalesce
+#pragma unroll
+        for (int q = 0; q < HC / 32; ++q) bpre[q] = row_ < g.M ? __ldg(bp + (int64_t)q * e.bits_ld) : 0u;
+      }
       mbar_wait(smem_u32(tfull + ab), aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[192 + li] = clock64();
@@ -1143,10 +1152,11 @@ __global__ void __launch_bounds__(320, 1)
             const int cl0 = hh * HC + pc;   // tile-local column of v[0]
             const int brow = rbase + lane;
             uint32_t mw[CW / 32];            // ReLU bitmask words of these CW columns (EF_BMASK: read)
-            if constexpr ((F & EF_BMASK) != 0) {
-              const uint32_t* bp = e.bits + (int64_t)((n0 + cl0) / 32) * e.bits_ld + brow;   // word-major: lanes coalesce
+            if constexpr ((F & EF_BMASK) != 0) {   // this pass's words from the prefetch, then shift it down
 #pragma unroll
-              for (int q = 0; q < CW / 32; ++q) mw[q] = brow < g.M ? __ldg(bp + (int64_t)q * e.bits_ld) : 0u;
+              for (int q = 0; q < CW / 32; ++q) mw[q] = bpre[q];
+#pragma unroll
+              for (int q = 0; q + CW / 32 < HC / 32; ++q) bpre[q] = bpre[q + CW / 32];
             }
 #pragma unroll
             for (int j = 0; j < CW; ++j) {

@@ -1294,11 +1294,13 @@ dhen_status dhen_debug_gemm_epi(const long long* q, const void* A, const void* B
   ev.dt = BF16;
   ev.ptr = const_cast<void*>(E);
   if (bias) { g.e.bias = bias; g.e.bias_dt = BF16; }
-  switch (mode) {   // 1 mask, 2 residual, 3 DCN cross (+ aux), 4 relu, 0 none
+  switch (mode) {   // 1 mask, 2 residual, 3 DCN cross (+ aux), 4 relu, 5 relu + bitmask out (aux), 6 bitmask in (aux)
     case 1: g.e.mask = ev; break;
     case 2: g.e.resid = ev; break;
     case 3: g.e.cross = ev; if (aux) { g.e.aux = ev; g.e.aux.ptr = aux; } break;
     case 4: g.e.relu = 1; break;
+    case 5: g.e.relu = 1; g.e.bits = (uint32_t*)aux; g.e.bits_mode = 1; g.e.bits_ld = g.M; break;
+    case 6: g.e.bits = (uint32_t*)aux; g.e.bits_mode = 2; g.e.bits_ld = g.M; break;
     default: break;
   }
   Workspace w;

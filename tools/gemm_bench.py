@@ -82,7 +82,7 @@ def main():
     ap.add_argument("--path", type=int, default=0)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--flush", default="write", choices=["write", "read", "none"])
-    ap.add_argument("--epi", type=int, default=0, help="fused epilogue mode (1 mask, 2 resid, 3 cross, 4 relu)")
+    ap.add_argument("--epi", type=int, default=0, help="fused epilogue mode (1 mask, 2 resid, 3 cross, 4 relu, 5 relu+bits out, 6 bits in)")
     args = ap.parse_args()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -97,6 +97,8 @@ def main():
         q = [M, N, K, Z] + list(a) + list(b) + list(c) + [acc] + list(a2) + list(b2) + list(c2)
         E = torch.randn(cext, device="cuda").to(torch.bfloat16) if args.epi else None
         aux = torch.empty(cext, device="cuda", dtype=torch.bfloat16) if args.epi == 3 else None
+        if args.epi in (5, 6):   # ReLU bitmask [N / 32][M] words
+            aux = torch.randint(-2**31, 2**31 - 1, (((N + 31) // 32) * M * Z,), device="cuda", dtype=torch.int32)
         if args.epi:
             from paper_2203_11014_b200.binding import debug_gemm_epi
 
