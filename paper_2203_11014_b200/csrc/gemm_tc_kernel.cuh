@@ -791,26 +791,35 @@ template <int BN> struct EpiSmem {
   static constexpr int BYTES = STAGE > TBOX ? STAGE : TBOX;
 };
 
+template <int BN, int STAGES, bool PAIR>
+constexpr int ring_stages() {
+  return PAIR ? (STAGES * (BM * BK * 2 + BN * BK * 2)) / (BM * BK * 2 + BN * BK) : STAGES;
+}
+
 template <int BN, int STAGES, int VAR, bool PAIR>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    const __grid_constant__ OutMaps tma_o, const __grid_constant__ Params p) {
   pdl_release();
-  constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
+  constexpr int A_BYTES = BM * BK * 2;
+  // B bytes per ring slot in this CTA (a pair CTA loads BN / 2 rows), and the ring depth the same shared
+  // memory holds: a pair kernel gets the deeper ring (BN = 256: 4 slots instead of 3)
+  constexpr int B_BYTES = PAIR ? BN * BK : BN * BK * 2;
+  constexpr int NST = ring_stages<BN, STAGES, PAIR>();
   constexpr int SC = EpiSmem<BN>::SC;
   constexpr int SROW = EpiSmem<BN>::SROW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  float* stage_all = (float*)(sB + STAGES * B_BYTES);   // fp32 staging, or the TMA-store boxes (1024-B aligned)
+  uint8_t* sB = smem + NST * A_BYTES;
+  float* stage_all = (float*)(sB + NST * B_BYTES);   // fp32 staging, or the TMA-store boxes (1024-B aligned)
   float* sbias = (float*)((uint8_t*)stage_all + EpiSmem<BN>::BYTES);   // [2][BN] bias of the current tiles
   uint64_t* bars = (uint64_t*)(sbias + 2 * BN);   // full[S], empty[S], tfull[2], tempty[2]
   uint64_t* full = bars;
-  uint64_t* empty = bars + STAGES;
-  uint64_t* tfull = bars + 2 * STAGES;
-  uint64_t* tempty = bars + 2 * STAGES + 2;
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+  uint64_t* empty = bars + NST;
+  uint64_t* tfull = bars + 2 * NST;
+  uint64_t* tempty = bars + 2 * NST + 2;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * NST + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = p.tiles_m * p.tiles_n;
   const int total = ntiles * p.nz * p.splits;
@@ -824,7 +833,7 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
-    for (int s = 0; s < 2 * STAGES + 2; ++s) mbar_init(smem_u32(bars + s), 1);
+    for (int s = 0; s < 2 * NST + 2; ++s) mbar_init(smem_u32(bars + s), 1);
     for (int s = 0; s < 2; ++s) mbar_init(smem_u32(tempty + s), pair ? 16 : 8);   // epilogue warps of both CTAs
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -876,7 +885,7 @@ __global__ void __launch_bounds__(320, 1)
         int kbk = p.b.has_ko ? k0 % p.b.kdiv : k0, kob = p.b.has_ko ? k0 / p.b.kdiv : 0;
         const int kda = p.a.has_ko ? p.a.kdiv : 0x7fffffff, kdb = p.b.has_ko ? p.b.kdiv : 0x7fffffff;
         const bool amn = p.a.mn_major != 0, bmn = p.b.mn_major != 0;
-        uint32_t s = (uint32_t)(it % STAGES), ph = (uint32_t)((it / STAGES) & 1);
+        uint32_t s = (uint32_t)(it % NST), ph = (uint32_t)((it / NST) & 1);
         for (int i = 0; i < nk; ++i, ++it) {
           mbar_wait(smem_u32(empty + s), ph ^ 1);
           if (p.trace && blockIdx.x == 0 && it < 64) p.trace[it] = clock64();
@@ -884,14 +893,14 @@ __global__ void __launch_bounds__(320, 1)
           if (!pair) {
             mbar_expect_tx(fb, A_BYTES + B_BYTES);
           } else {
-            if (crank == 0) mbar_expect_tx(fb, 2 * (A_BYTES + B_BYTES / 2));   // both CTAs' halves land on rank 0's barrier
+            if (crank == 0) mbar_expect_tx(fb, 2 * (A_BYTES + B_BYTES));   // both CTAs' halves land on rank 0's barrier
             fb = mapa_u32(fb, 0);
           }
           load_tile(&tma_a, amn, qa, ka, koa, smem_u32(sA) + s * A_BYTES, fb, BM / 64, pair);
           load_tile(&tma_b, bmn, qb, kbk, kob, smem_u32(sB) + s * B_BYTES, fb, pair ? BN / 128 : BN / 64, pair);
           ka += BK; while (ka >= kda) { ka -= kda; ++koa; }     // kdiv < BK: several outer indices per k-block
           kbk += BK; while (kbk >= kdb) { kbk -= kdb; ++kob; }
-          if (++s == STAGES) { s = 0; ph ^= 1; }
+          if (++s == NST) { s = 0; ph ^= 1; }
         }
       }
     }
@@ -913,8 +922,8 @@ __global__ void __launch_bounds__(320, 1)
         if (p.trace && blockIdx.x == 0 && li < 64) p.trace[64 + li] = clock64();
         const uint32_t dacc = tmem + (uint32_t)(ab * BN);
         for (int i = 0; i < nk; ++i, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
+          const int s = it % NST;
+          const uint32_t ph = (it / NST) & 1;
           mbar_wait(smem_u32(full + s), ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (p.trace && blockIdx.x == 0 && it < 64) p.trace[128 + it] = clock64();
@@ -1395,8 +1404,8 @@ __global__ void __launch_bounds__(320, 1)
 template <int BN, int STAGES, int VAR>
 static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                           cudaStream_t st) {
-  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + EpiSmem<BN>::BYTES + 2 * BN * 4 + (2 * STAGES + 4) * 8 +
-                       16 + 1024;
+  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + EpiSmem<BN>::BYTES + 2 * BN * 4 +
+                       (2 * ring_stages<BN, STAGES, true>() + 4) * 8 + 16 + 1024;
   static_assert(SMEM <= 227 * 1024, "smem");
   static bool attr = false;
   if (!attr) {

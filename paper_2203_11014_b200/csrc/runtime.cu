@@ -168,7 +168,7 @@ struct dhen_ctx {
   cudaEvent_t ev_ag[2] = {nullptr, nullptr}, ev_use[2] = {nullptr, nullptr}, ev_grad = nullptr, ev_comm = nullptr;
   unsigned long long launches0 = 0;
   // per-op device timing (dhen_profile): event pairs on the launch stream
-  struct Rec { const char* tag; int e0, e1; double flops, bytes; int tc; };
+  struct Rec { const char* tag; int e0, e1; double flops, bytes; int tc; cudaStream_t st; };
   bool prof = false;
   std::vector<cudaEvent_t> events;
   int next_event = 0;
@@ -193,7 +193,7 @@ struct ProfScope {
     }
     int e0 = c->next_event++, e1 = c->next_event++;
     cudaEventRecord(c->events[e0], st);
-    c->recs.push_back({tag, e0, e1, flops, bytes, 0});
+    c->recs.push_back({tag, e0, e1, flops, bytes, 0, st});
     rec = (int)c->recs.size() - 1;
   }
   ~ProfScope() {
@@ -1348,6 +1348,22 @@ dhen_status dhen_profile_read(dhen_ctx* c, dhen_op_stat* out, int cap, int* n) {
   }
   *n = (int)agg.size();
   for (int k = 0; k < (int)agg.size() && k < cap; ++k) out[k] = agg[k];
+  // DHEN_PROF_TRACE=<file>: also dump every record (op, stream, start and end in ms from the first record)
+  if (const char* tf = getenv("DHEN_PROF_TRACE")) {
+    if (FILE* fp = fopen(tf, "w")) {
+      std::vector<cudaStream_t> sts;
+      for (auto& r : c->recs) {
+        float t0 = 0.f, t1 = 0.f;
+        cudaEventElapsedTime(&t0, c->events[c->recs[0].e0], c->events[r.e0]);
+        cudaEventElapsedTime(&t1, c->events[c->recs[0].e0], c->events[r.e1]);
+        size_t si = 0;
+        for (; si < sts.size(); ++si) if (sts[si] == r.st) break;
+        if (si == sts.size()) sts.push_back(r.st);
+        fprintf(fp, "%s,%zu,%.4f,%.4f\n", r.tag, si, t0, t1);
+      }
+      fclose(fp);
+    }
+  }
   return DHEN_OK;
 }
 
