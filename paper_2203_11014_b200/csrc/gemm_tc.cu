@@ -199,15 +199,16 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   // slot, so the same shared memory holds a deeper ring (BN = 256: 4 slots instead of 3).  Measured
   // (tools/gemm_bench.py, DHEN_PAIR=0/1): +7-18 % on the long-K dot.proj family (C4 945 -> 802 us, 1360
   // TF/s), but slower on the short-K, store-bound shapes (the pair's epilogues run in lock step), so the
-  // default takes pairs for K >= 2048 with at least 64 pair items (split-K items included: +13 % on the
-  // C4 attention FFN weight gradients).
+  // default takes pairs for K >= 1024 (DHEN_PAIR_K; 512 measured slower) with at least 64 pair items
+  // (split-K items included: +13 % on the C4 attention FFN weight gradients).
   {
     static int env_mode = -2;
     if (env_mode == -2) { const char* ev = getenv("DHEN_PAIR"); env_mode = ev ? atoi(ev) : -1; }
+    static int pair_k = [] { const char* e = getenv("DHEN_PAIR_K"); return e ? atoi(e) : 1024; }();
     const int mode = g_gemm_pair >= 0 ? g_gemm_pair : env_mode;
     const int64_t pitems = (int64_t)((g.M + 2 * BM - 1) / (2 * BM)) * p.tiles_n * g.batch;
     p.pair = (BN >= 128 && (splits == 1 || mode == 1 || (splits > 1 && g.M >= 2 * BM)) && mode != 0 &&
-              (mode == 1 ? g.M > BM : (pitems * splits >= 64 && g.K >= 2048))) ? 1 : 0;
+              (mode == 1 ? g.M > BM : (pitems * splits >= 64 && g.K >= pair_k))) ? 1 : 0;
   }
   CUtensorMap ma, mb;
   if (!make_map(&ma, &p.a, g.a, g.M, g.K, g.batch, BM)) return cudaErrorNotSupported;
