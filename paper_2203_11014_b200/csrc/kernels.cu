@@ -741,7 +741,8 @@ cudaError_t ln_fwd(const float* U, const void* addx, const void* gamma, const vo
 
 cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
                    const void* gamma, int pdt, int64_t rows, int d, void* dR, int dt, float* acc, int acc_mode,
-                   float* dgamma, float* dbeta, float* scratch, size_t scratch_bytes, cudaStream_t st) {
+                   float* dgamma, float* dbeta, float* scratch, size_t scratch_bytes, cudaStream_t st,
+                   cudaStream_t st_red, cudaEvent_t ev_red) {
   const int lpr = ln_lpr(d);
   if (dt == BF16 && pdt == BF16 && lpr >= 4) {
     const int rpi = (32 / lpr) * LNB_UR;
@@ -762,7 +763,13 @@ cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu,
       LNB2(4) LNB2(8) LNB2(16) LNB2(32)
 #undef LNB2
       ++g_launches;
-      part_sum(scratch, nb, 2 * d, dgamma, d, dbeta, d, nullptr, 0.f, st);
+      cudaStream_t sr = st;
+      if (st_red && ev_red && st_red != st) {   // dR is what st needs next; the parameter sums can trail
+        cudaEventRecord(ev_red, st);
+        cudaStreamWaitEvent(st_red, ev_red, 0);
+        sr = st_red;
+      }
+      part_sum(scratch, nb, 2 * d, dgamma, d, dbeta, d, nullptr, 0.f, sr);
       return cudaGetLastError();
     }
   }
@@ -1783,7 +1790,8 @@ __global__ void head_part_k(const float* pooled, const float* dz, const float* l
 }
 cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, const float* labels, int B, int m, int d,
                          int Bg, void* dY, int dt, float* pooled, float* z, float* lossb, float* dz, float* loss_out,
-                         float* dw, float* db, int do_bwd, cudaStream_t st) {
+                         float* dw, float* db, int do_bwd, cudaStream_t st, cudaStream_t st_red,
+                         cudaEvent_t ev_red) {
   if (dt == BF16 && pdt == BF16 && d % 8 == 0 && d / 8 <= 256 && ((uintptr_t)Y % 16) == 0 && ((uintptr_t)w % 16) == 0 &&
       (!do_bwd || ((uintptr_t)dY % 16) == 0)) {
     const int RY = 256 / (d / 8);
@@ -1792,7 +1800,15 @@ cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, 
         (const __nv_bfloat16*)bh, labels, m, d, Bg, (__nv_bfloat16*)dY, pooled, z, lossb, dz, do_bwd,
         do_bwd ? hpart : nullptr);
     ++g_launches;
-    if (do_bwd) part_sum(hpart, B, d + 2, dw, d, db, 1, loss_out, 1.f / (float)Bg, st);   // fixed order over samples
+    if (do_bwd) {
+      cudaStream_t sr = st;
+      if (st_red && ev_red && st_red != st) {   // dY is what st needs next; the head sums can trail
+        cudaEventRecord(ev_red, st);
+        cudaStreamWaitEvent(st_red, ev_red, 0);
+        sr = st_red;
+      }
+      part_sum(hpart, B, d + 2, dw, d, db, 1, loss_out, 1.f / (float)Bg, sr);   // fixed order over samples
+    }
     return cudaGetLastError();
   } else {
     pdl_launch(head_k, B, 256, 0, st, Y, w, bh, pdt, labels, m, d, Bg, dY, dt, pooled, z, lossb, dz, do_bwd);

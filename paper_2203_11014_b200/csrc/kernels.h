@@ -20,7 +20,10 @@ cudaError_t ln_fwd(const float* U, const void* addx, const void* gamma, const vo
 // acc_mode 1: acc = dR, 2: acc += dR (fp32 rows x d).  dgamma/dbeta += sums (deterministic).
 cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
                    const void* gamma, int pdt, int64_t rows, int d, void* dR, int dt, float* acc, int acc_mode,
-                   float* dgamma, float* dbeta, float* scratch, size_t scratch_bytes, cudaStream_t st);
+                   float* dgamma, float* dbeta, float* scratch, size_t scratch_bytes, cudaStream_t st,
+                   cudaStream_t st_red = nullptr, cudaEvent_t ev_red = nullptr);
+// (st_red: the final fixed-order reduction of the dgamma / dbeta partials runs there, after ev_red is
+//  recorded on st; scratch must then stay untouched on st until st_red is joined back)
 
 // out[c] += sum_r src[r * ld + c] for c < cols (deterministic two-pass).
 cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t ld, float* out,
@@ -48,7 +51,8 @@ cudaError_t conv_wgrad(const void* dT, const void* X, int C, int k, int B, int m
 // dY[b,t,c] = dz_b w[c] / m (dt).  Then loss_out = sum_b loss_b / Bg, dw += sum dz pooled, db += sum dz.
 cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, const float* labels, int B, int m, int d,
                          int Bg, void* dY, int dt, float* pooled, float* z, float* lossb, float* dz, float* loss_out,
-                         float* dw, float* db, int do_bwd, cudaStream_t st);
+                         float* dw, float* db, int do_bwd, cudaStream_t st, cudaStream_t st_red = nullptr,
+                         cudaEvent_t ev_red = nullptr);
 
 // out (bf16 [spt m][spt l]) = blockdiag(W, .., W) of the bf16 token map W [m][l] (DCN backward packing)
 cudaError_t blockdiag(const void* W, int m, int l, int spt, void* out, cudaStream_t st);

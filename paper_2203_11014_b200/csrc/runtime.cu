@@ -150,9 +150,11 @@ struct dhen_ctx {
   // weight-gradient side stream (B4/B5/B7/B8/B9 wgrads overlap the same module's dgrads; joined per module)
   int overlap = 1;                    // env DHEN_OVERLAP
   cudaStream_t side_st = nullptr;
-  cudaEvent_t ev_sf = nullptr, ev_sx = nullptr, ev_sj = nullptr;
+  cudaEvent_t ev_sf = nullptr, ev_sx = nullptr, ev_sj = nullptr, ev_red = nullptr;
   Workspace ws2;                      // split-K scratch of the side stream
   float* red2 = nullptr;              // reduction scratch of the side stream
+  float* red3 = nullptr;              // layer-LN parameter partials (their final sum trails on the side stream)
+  int trail = 1;                      // DHEN_TRAIL: parameter-sum reductions of LN / head trail on the side stream
   float *pooled = nullptr, *z = nullptr, *lossb = nullptr, *dz = nullptr;
   float* gtmp = nullptr;    // fp32 [max_npad]: all-gather target of params_io / grads_get (world > 1)
   ncclComm_t comm = nullptr;
@@ -424,6 +426,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   c->ws2.bytes = (size_t)256 << 20;
   c->ws2.ptr = (float*)work.take(c->ws2.bytes);
   c->red2 = (float*)work.take(c->red_bytes);
+  c->red3 = (float*)work.take(c->red_bytes);
   c->pooled = (float*)work.take(((size_t)B * d + (size_t)B * (d + 2)) * 4);   // + head partials [B][d + 2]
   c->z = (float*)work.take((size_t)B * 4);
   c->lossb = (float*)work.take((size_t)B * 4);
@@ -794,15 +797,16 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   const int first_kind = order.empty() ? -1 : order[0]->s.kind;
   const bool first_dR = c->first_writer && Lr.Wn < 0 && mi == mo &&
                         (first_kind == DHEN_DOT || first_kind == DHEN_DCN || first_kind == DHEN_LINEAR || first_kind == DHEN_MLP);
-  KT("layer.ln_bwd", 0, (double)B * mo * d * (3 * es + (first_dR ? 0 : 4)), ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc, (Lr.Wn >= 0 || first_dR) ? 0 : 1,
-            gp(Lr.gamma), gp(Lr.beta), c->red, c->red_bytes, st));
-  if (Lr.Wn >= 0)   // B3: dX = W_n dR ; dW_n += sum_b X_b dR_b^T
-    RET(tokmix_bwd(c, X, mi, p(Lr.Wn), mo, c->dR, ldU, acc, F32, 0, gp(Lr.Wn), B, st));
   // Weight gradients of a module run on the side stream `sd` (own split-K / reduction scratch) while its
   // data gradients run on `st`; `fork` hands the side stream everything enqueued on st so far, `join`
   // makes st wait for the side stream at the end of the module (shared scratch is reused by the next one).
   // (the profiled pass runs serialised so every op's event-timed duration is its own)
   cudaStream_t sd = (c->overlap && !c->prof) ? c->side_st : st;
+  // the LN parameter sums trail on sd (own scratch red3; the modules' joins below order its reuse)
+  KT("layer.ln_bwd", 0, (double)B * mo * d * (3 * es + (first_dR ? 0 : 4)), ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc, (Lr.Wn >= 0 || first_dR) ? 0 : 1,
+            gp(Lr.gamma), gp(Lr.beta), c->red3, c->red_bytes, st, c->trail ? sd : st, c->ev_red));
+  if (Lr.Wn >= 0)   // B3: dX = W_n dR ; dW_n += sum_b X_b dR_b^T
+    RET(tokmix_bwd(c, X, mi, p(Lr.Wn), mo, c->dR, ldU, acc, F32, 0, gp(Lr.Wn), B, st));
   const Workspace* ws2 = &c->ws2;
   float* red2 = c->red2;
   auto fork = [&]() -> dhen_status {
@@ -1074,8 +1078,11 @@ static dhen_status head(dhen_ctx* c, const void* YN, int mN, const float* labels
   RET(comp_params(c, gi, st, &pbase));
   PP p{(char*)pbase, c->es};
   Group& G = c->G[gi];
+  // single GPU: the head's parameter / loss sums trail on the side stream (the first backward layer's
+  // module joins bring it back before anything reads them); with collectives they stay on st
+  cudaStream_t sr = (c->overlap && c->trail && !c->prof && c->dist.world == 1) ? c->side_st : st;
   KT("head", 0, (double)B * mN * c->d * c->es * (do_bwd ? 2 : 1), head_fwd_bwd(YN, p(0), p(G.toff[1]), c->dt, labels, B, mN, c->d, Bg, dY, c->dt, c->pooled, c->z, c->lossb, c->dz, loss,
-                  G.grad, G.grad + G.toff[1], do_bwd, st));
+                  G.grad, G.grad + G.toff[1], do_bwd, st, sr, c->ev_red));
   RET(release(c, gi, st));
   if (do_bwd) RET(reduce_grads(c, gi, st));
   return DHEN_OK;
@@ -1172,10 +1179,13 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
   {
     const char* ev = getenv("DHEN_OVERLAP");
     c->overlap = ev ? atoi(ev) : 1;
+    const char* et = getenv("DHEN_TRAIL");
+    c->trail = et ? atoi(et) : 1;
     bool ok = cudaStreamCreateWithFlags(&c->side_st, cudaStreamNonBlocking) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_sf, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_sx, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_sj, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_red, cudaEventDisableTiming) == cudaSuccess;
     if (!ok) { dhen_destroy(c); return fail(DHEN_E_CUDA, "dhen_init: side stream creation failed"); }
   }
   if (c->dist.world > 1) {
@@ -1238,6 +1248,7 @@ void dhen_destroy(dhen_ctx* c) {
   if (c->ev_sf) cudaEventDestroy(c->ev_sf);
   if (c->ev_sx) cudaEventDestroy(c->ev_sx);
   if (c->ev_sj) cudaEventDestroy(c->ev_sj);
+  if (c->ev_red) cudaEventDestroy(c->ev_red);
   if (c->side_st) cudaStreamDestroy(c->side_st);
   if (c->ev_grad) cudaEventDestroy(c->ev_grad);
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
