@@ -789,6 +789,7 @@ template <int BN> struct EpiSmem {
   static constexpr int STAGE = 8 * 32 * SROW * 4;         // fp32 staging of the 8 epilogue warps
   static constexpr int TBOX = 8 * 2 * 4096;               // TMA-store boxes: 2 x (32 rows x 128 B) per warp
   static constexpr int BYTES = STAGE > TBOX ? STAGE : TBOX;
+  static constexpr int SBIAS = 2 * BN > 512 ? 2 * BN : 512;   // floats: [2][BN] bias, or the LN (s1, s2) exchange
 };
 
 template <int BN, int STAGES, bool PAIR>
@@ -814,7 +815,7 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* sB = smem + NST * A_BYTES;
   float* stage_all = (float*)(sB + NST * B_BYTES);   // fp32 staging, or the TMA-store boxes (1024-B aligned)
   float* sbias = (float*)((uint8_t*)stage_all + EpiSmem<BN>::BYTES);   // [2][BN] bias of the current tiles
-  uint64_t* bars = (uint64_t*)(sbias + 2 * BN);   // full[S], empty[S], tfull[2], tempty[2]
+  uint64_t* bars = (uint64_t*)(sbias + EpiSmem<BN>::SBIAS);   // full[S], empty[S], tfull[2], tempty[2]
   uint64_t* full = bars;
   uint64_t* empty = bars + NST;
   uint64_t* tfull = bars + 2 * NST;
@@ -1013,7 +1014,7 @@ __global__ void __launch_bounds__(320, 1)
         // Lane = row.  ln_d == HC: a warp's column half is one whole segment; ln_d == BN: the two warps of a
         // TMEM lane quadrant (hh = 0, 1) own the two halves of the segment and exchange row partial sums through
         // shared memory (named barrier per quadrant).  Pass 1: v = alpha acc (+ bias) + resid -> TMEM, R = bf16(v)
-        // stored, sum(v); pass 2: sum((v - mu)^2); pass 3: Y = gamma (v - mu) rstd + beta.  The segment's
+        // stored, sum(v) and sum(v^2) (var = E[v^2] - mu^2); pass 2: Y = gamma (v - mu) rstd + beta.  The segment's
         // statistics index is (element offset of its first column) / ln_d, relative to ln_mu / ln_rstd.
         constexpr int F = VarF<VAR>::F;
         const int row = rbase + lane;
@@ -1021,7 +1022,7 @@ __global__ void __launch_bounds__(320, 1)
         const int64_t ro = rok ? lean_row(e, z, row) : 0;
         const uint32_t tq = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC);
         const bool xch_mode = e.ln_d != HC;
-        float* xch = sbias + q4 * 64;   // [quadrant][hh][32 lanes] row partial sums (the bias scratch)
+        float* xch = sbias + q4 * 128;  // [quadrant][hh][32 lanes] row partial (s1, s2) pairs (the bias scratch)
         const int cb0 = n0 + hh * HC;                       // first column of this warp's half
         const int seg0 = xch_mode ? n0 : cb0;               // first column of the segment
         const int gofs = cb0 - seg0;                        // gamma / beta index of column cb0
@@ -1050,7 +1051,7 @@ __global__ void __launch_bounds__(320, 1)
           }
           __syncwarp();
         };
-        float s1 = 0.f;
+        float s1 = 0.f, s2 = 0.f;   // sum and sum of squares of v (one pass; fp32 is ample for LN rows)
 #pragma unroll
         for (int c = 0; c < HC; c += 32) {   // unrolled: rpre is indexed with compile-time offsets
           uint32_t v[32];
@@ -1069,36 +1070,29 @@ __global__ void __launch_bounds__(320, 1)
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           float f[32];
 #pragma unroll
-          for (int q = 0; q < 32; ++q) { f[q] = __uint_as_float(v[q]) * e.alpha + bv[q] + rv[q]; s1 += f[q]; }
+          for (int q = 0; q < 32; ++q) { f[q] = __uint_as_float(v[q]) * e.alpha + bv[q] + rv[q]; s1 += f[q]; s2 = fmaf(f[q], f[q], s2); }
 #pragma unroll
           for (int q = 0; q < 4; ++q) stage8(c + 8 * q, f + 8 * q);
           tmem_st32f(tq + c, f);
         }
         flush(e.aux);   // R
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        if (xch_mode) {
-          xch[hh * 32 + lane] = s1;
+        if (xch_mode) {   // [quadrant][hh][32 lanes] of (s1, s2) pairs through the bias scratch
+          const uint32_t xa = smem_u32(xch);
+          asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(xa + (uint32_t)((hh * 32 + lane) * 8)), "f"(s1), "f"(s2)
+                       : "memory");
           asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-          s1 = xch[lane] + xch[32 + lane];
+          float a1, a2, b1, b2;
+          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a1), "=f"(a2) : "r"(xa + (uint32_t)(lane * 8)) : "memory");
+          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(b1), "=f"(b2) : "r"(xa + (uint32_t)((32 + lane) * 8))
+                       : "memory");
+          s1 = a1 + b1;
+          s2 = a2 + b2;
           asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
         }
         const float mean = s1 * inv_d;
-        float s2 = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < HC; c += 32) {
-          uint32_t v[32];
-          ld_tmem32(tq + c, v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int q = 0; q < 32; ++q) { const float t = __uint_as_float(v[q]) - mean; s2 += t * t; }
-        }
-        if (xch_mode) {
-          xch[hh * 32 + lane] = s2;
-          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-          s2 = xch[lane] + xch[32 + lane];
-          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-        }
-        const float rs = rsqrtf(s2 * inv_d + e.ln_eps);
+        const float var = fmaxf(fmaf(-mean, mean, s2 * inv_d), 0.f);
+        const float rs = rsqrtf(var + e.ln_eps);
         if (rok && (!xch_mode || hh == 0)) {
           const int64_t tok = (ro + seg0) / e.ln_d;
           e.ln_mu[tok] = mean;
@@ -1404,7 +1398,7 @@ __global__ void __launch_bounds__(320, 1)
 template <int BN, int STAGES, int VAR>
 static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                           cudaStream_t st) {
-  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + EpiSmem<BN>::BYTES + 2 * BN * 4 +
+  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + EpiSmem<BN>::BYTES + EpiSmem<BN>::SBIAS * 4 +
                        (2 * ring_stages<BN, STAGES, true>() + 4) * 8 + 16 + 1024;
   static_assert(SMEM <= 227 * 1024, "smem");
   static bool attr = false;
