@@ -1857,6 +1857,32 @@ cudaError_t blockdiag_t(const void* W, int m, int l, int spt, void* out, cudaStr
   return cudaGetLastError();
 }
 
+// All of a step's block-diagonal token maps in one launch (blockIdx.y = job): jobs with tr = 1 build
+// blockdiag_t (the forward's packed token projection), tr = 0 blockdiag (the DCN backward's packed dT).
+__global__ void blockdiag_multi_k(BdJobs jobs) {
+  pdl_entry();
+  const BdJob& j = jobs.job[blockIdx.y];
+  const int m = j.m, l = j.l, spt = j.spt;
+  const int n = spt * m * spt * l;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    __nv_bfloat16 v = __float2bfloat16_rn(0.f);
+    if (j.tr) {
+      const int i = t / (spt * m), k = t - i * (spt * m);
+      if (i / l == k / m) v = j.W[(k % m) * l + (i % l)];
+    } else {
+      const int i = t / (spt * l), k = t - i * (spt * l);
+      if (i / m == k / l) v = j.W[(i % m) * l + (k % l)];
+    }
+    j.out[t] = v;
+  }
+}
+cudaError_t blockdiag_multi(const BdJobs& jobs, cudaStream_t st) {
+  if (jobs.n <= 0) return cudaSuccess;
+  pdl_launch(blockdiag_multi_k, dim3(64, jobs.n), 256, 0, st, jobs);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ SGD, casts, init
 __global__ void sgd_cast_k(float* master, const float* grad, float lr, void* copy, int dt, int64_t n) {
   pdl_entry();

@@ -54,6 +54,17 @@ cudaError_t head_fwd_bwd(const void* Y, const void* w, const void* bh, int pdt, 
                          float* dw, float* db, int do_bwd, cudaStream_t st, cudaStream_t st_red = nullptr,
                          cudaEvent_t ev_red = nullptr);
 
+// Several block-diagonal maps in one launch (a training step builds every layer's up front).
+struct BdJob {
+  const __nv_bfloat16* W;
+  __nv_bfloat16* out;
+  int m, l, spt, tr;   // tr = 1: blockdiag_t layout, 0: blockdiag layout
+};
+struct BdJobs {
+  int n;
+  BdJob job[32];
+};
+cudaError_t blockdiag_multi(const BdJobs& jobs, cudaStream_t st);
 // out (bf16 [spt m][spt l]) = blockdiag(W, .., W) of the bf16 token map W [m][l] (DCN backward packing)
 cudaError_t blockdiag(const void* W, int m, int l, int spt, void* out, cudaStream_t st);
 // out (bf16 [spt l][spt m]) = blockdiag(W^T, .., W^T) (packed token projection)

@@ -70,6 +70,8 @@ struct Mod {
        *Z1 = nullptr, *F = nullptr, *R2 = nullptr, *h1 = nullptr, *h2 = nullptr;
   float *mu1 = nullptr, *rs1 = nullptr, *mu2 = nullptr, *rs2 = nullptr;
   void* bdT = nullptr;   // bf16 [128][spt m]: blockdiag(W_u^T, ..) for the packed token projection (layer LN fused)
+  void* bdg = nullptr;   // bf16 [128][128]: blockdiag(W_u, ..) for the packed DCN backward dT
+  bool bdT_pre = false, bdg_pre = false;   // built for this step by prebuild_bd (train_step, one launch)
   uint32_t* Fbits = nullptr;   // attention FFN ReLU bitmask [f / 32][B m] (FFN2 data gradient reads it, not F)
 };
 
@@ -399,6 +401,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
         default: break;
       }
       md.bdT = work.take((size_t)128 * 128 * 8 * 2);   // spt m <= 1024 columns
+      if (md.s.kind == DHEN_DCN) md.bdg = work.take((size_t)128 * 128 * 2);
     }
   }
   // scratch
@@ -557,6 +560,30 @@ static dhen_status join_comm(dhen_ctx* c, cudaStream_t st) {
   return DHEN_OK;
 }
 
+// Whether layer n's forward takes the LayerNorm-fused form (F12 in the producing GEMMs' epilogues).
+static bool layer_lnf(const dhen_ctx* c, int n, int B) {
+  const Layer& Lr = c->L[n];
+  const int d = c->d, mi = Lr.m_in, mo = Lr.m_out;
+  bool lnf = c->ln_fuse && c->dt == BF16 && Lr.Wn < 0 && mi == mo && (d == 128 || d == 256);
+  for (const Mod& m_ : Lr.mods) {
+    if (!lnf) break;
+    const int l_ = m_.s.l;
+    if (m_.s.kind == DHEN_DOT || m_.s.kind == DHEN_MLP) {
+      const int N = l_ * d, BN = N <= 64 ? 64 : N <= 128 ? 128 : 256;
+      lnf = BN >= 128 && N % BN == 0 && (d == BN || 2 * d == BN);
+    } else {
+      lnf = l_ <= 128 && 128 % l_ == 0 && B % (128 / l_) == 0 && mi % 64 == 0 && (128 / l_) * mi <= 1024;
+    }
+  }
+  return lnf;
+}
+// Whether the DCN backward's token-map dgrad packs 128 / m samples per tile (block-diagonal W_u).
+static bool dcn_pack(const dhen_ctx* c, int mi, int l, int B) {
+  const int spt = 128 / std::max(mi, 1);
+  return !c->tr_small_m && c->dt == BF16 && mi <= 64 && 128 % mi == 0 && l <= 64 && 64 % l == 0 &&
+         (spt * l) % 64 == 0 && B % spt == 0;
+}
+
 // ------------------------------------------------------------------ layer forward
 static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, cudaStream_t st) {
   Layer& Lr = c->L[n];
@@ -576,17 +603,7 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
   // Y = LN(U_i + X) directly -- the LayerNorm runs in its epilogue over d-column segments (R, mu, rstd saved),
   // so neither the fp32 concat buffer nor the LayerNorm kernel is touched.  Token-mixing outputs use the packed
   // form U[(b, t)] = blockdiag(W_u^T, ..) x [T_b; T_b+1; ..] (rows = tokens of 128 / l samples per tile).
-  bool lnf = c->ln_fuse && dt == BF16 && Lr.Wn < 0 && mi == mo && (d == 128 || d == 256);
-  for (const Mod& m_ : Lr.mods) {
-    if (!lnf) break;
-    const int l_ = m_.s.l;
-    if (m_.s.kind == DHEN_DOT || m_.s.kind == DHEN_MLP) {
-      const int N = l_ * d, BN = N <= 64 ? 64 : N <= 128 ? 128 : 256;
-      lnf = BN >= 128 && N % BN == 0 && (d == BN || 2 * d == BN);
-    } else {
-      lnf = l_ <= 128 && 128 % l_ == 0 && B % (128 / l_) == 0 && mi % 64 == 0 && (128 / l_) * mi <= 1024;
-    }
-  }
+  const bool lnf = layer_lnf(c, n, B);
   const cudaStream_t st0 = st;
   const bool use_side = c->overlap && !c->prof && Lr.mods.size() > 1;
   bool has_attn = false;
@@ -612,7 +629,7 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
     auto emit_tm = [&](const void* T_, const void* W_) -> dhen_status {
       if (!lnf) return tokmix_fwd(c, T_, mi, W_, l, Us, ldU, B, 0, st);
       const int spt = 128 / l;
-      KT("tokmix.bdiagT", 0, 0.0, blockdiag_t(W_, mi, l, spt, md.bdT, st));
+      if (!md.bdT_pre) KT("tokmix.bdiagT", 0, 0.0, blockdiag_t(W_, mi, l, spt, md.bdT, st));
       auto rows2 = [&](void* ptr) { View v = view2(ptr, dt, l, so, d, 1); v.bs0 = spt * so; return v; };
       Gemm gm = mk(spt * l, d, spt * mi, B / spt, operand(md.bdT, dt, spt * mi, 1),
                    operand(T_, dt, 1, d, (int64_t)spt * mi * d, 0, 1, mi, (int64_t)mi * d), rows2(Yo));
@@ -881,11 +898,11 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         // block-diagonal token map blockdiag(W_u, .., W_u) [spt m][spt l] against spt stacked dU_b (the B
         // operand's two-level K: k -> (sample, t)), so every MMA row and epilogue warp carries data.
         const int spt = 128 / std::max(mi, 1);
-        const bool pack = !c->tr_small_m && dt == BF16 && mi <= 64 && 128 % mi == 0 && l <= 64 && 64 % l == 0 &&
-                          (spt * l) % 64 == 0 && B % spt == 0;
+        const bool pack = dcn_pack(c, mi, l, B);
         if (pack) {
-          KT("dcn.bdiag", 0, 2.0 * 128 * 128 * es, blockdiag(p(md.Wu), mi, l, spt, c->bdiag, st));
-          Gemm gt = mk(spt * mi, d, spt * l, B / spt, operand(c->bdiag, dt, spt * l, 1),
+          void* bdg = md.bdg_pre ? md.bdg : c->bdiag;
+          if (!md.bdg_pre) KT("dcn.bdiag", 0, 2.0 * 128 * 128 * es, blockdiag(p(md.Wu), mi, l, spt, bdg, st));
+          Gemm gt = mk(spt * mi, d, spt * l, B / spt, operand(bdg, dt, spt * l, 1),
                        operand(dU, dt, 1, d, spt * ldU, 0, 1, l, ldU), view(acc, F32, d, 1, (int64_t)spt * mi * d));
           gt.e.dcn_bwd = 1;
           gt.e.cross = view((void*)X, dt, d, 1, (int64_t)spt * mi * d);
@@ -1068,6 +1085,44 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   RET(release(c, n, st));
   RET(reduce_grads(c, n, st));
   return DHEN_OK;
+}
+
+// ------------------------------------------------------------------ block-diagonal token maps, per step
+// Single GPU, bf16: the compute weights are fixed for the whole step, so every layer's block-diagonal maps
+// (forward packed token projection, DCN backward packed dT) are built up front in ONE launch instead of one
+// small launch per module and direction.  The flags are cleared when the step ends (SGD changes W_u).
+static dhen_status prebuild_bd(dhen_ctx* c, int B, cudaStream_t st) {
+  static int on = [] { const char* e = getenv("DHEN_BD_PRE"); return e ? atoi(e) : 1; }();
+  if (!on || c->dist.world != 1 || c->dt != BF16) return DHEN_OK;
+  BdJobs jobs;
+  jobs.n = 0;
+  for (int n = 0; n < c->cfg.n_layers; ++n) {
+    Layer& Lr = c->L[n];
+    const int mi = Lr.m_in;
+    void* pbase;
+    RET(comp_params(c, n, st, &pbase));
+    PP p{(char*)pbase, c->es};
+    const bool lnf = layer_lnf(c, n, B);
+    for (Mod& md : Lr.mods) {
+      const int l = md.s.l;
+      const int64_t wu = md.s.kind == DHEN_LINEAR ? md.W : md.Wu;
+      const bool tm = md.s.kind == DHEN_LINEAR || md.s.kind == DHEN_DCN || md.s.kind == DHEN_CONV || md.s.kind == DHEN_ATTN;
+      if (tm && lnf && md.bdT && jobs.n < 32) {
+        jobs.job[jobs.n++] = {(const __nv_bfloat16*)p(wu), (__nv_bfloat16*)md.bdT, mi, l, 128 / l, 1};
+        md.bdT_pre = true;
+      }
+      if (md.s.kind == DHEN_DCN && md.bdg && dcn_pack(c, mi, l, B) && jobs.n < 32) {
+        jobs.job[jobs.n++] = {(const __nv_bfloat16*)p(md.Wu), (__nv_bfloat16*)md.bdg, mi, l, 128 / std::max(mi, 1), 0};
+        md.bdg_pre = true;
+      }
+    }
+  }
+  KT("bdiag.all", 0, 0.0, blockdiag_multi(jobs, st));
+  return DHEN_OK;
+}
+static void clear_bd(dhen_ctx* c) {
+  for (Layer& Lr : c->L)
+    for (Mod& md : Lr.mods) md.bdT_pre = md.bdg_pre = false;
 }
 
 // ------------------------------------------------------------------ head
@@ -1393,6 +1448,7 @@ dhen_status dhen_layer_fwd(dhen_ctx* c, int n, const void* x, void* y, int B, vo
   if (B < 1 || B > c->Bmax) return fail(DHEN_E_SHAPE, "dhen_layer_fwd: B=%d not in [1, %d]", B, c->Bmax);
   if (!aligned16(x) || !aligned16(y)) return fail(DHEN_E_ALIGN, "dhen_layer_fwd: x=%p y=%p", x, y);
   invalidate_gathered(c);
+  clear_bd(c);
   RET(layer_fwd(c, n, x, y, B, S(stream)));
   CK(cudaGetLastError());
   return DHEN_OK;
@@ -1404,6 +1460,7 @@ dhen_status dhen_layer_bwd(dhen_ctx* c, int n, const void* dy, void* dx, int B, 
   if (c->L[n].B != B) return fail(DHEN_E_STATE, "dhen_layer_bwd: layer %d has no saved forward at B=%d (saved B=%d)", n, B, c->L[n].B);
   if (!aligned16(dy) || (dx && !aligned16(dx))) return fail(DHEN_E_ALIGN, "dhen_layer_bwd: dy=%p dx=%p", dy, dx);
   invalidate_gathered(c);
+  clear_bd(c);
   RET(layer_bwd(c, n, dy, dx, B, S(stream)));
   RET(join_comm(c, S(stream)));
   CK(cudaGetLastError());
@@ -1441,6 +1498,8 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
   RET(dhen_zero_grad(c, stream));
   invalidate_gathered(c);
   const void* X = x0;
+  clear_bd(c);
+  RET(prebuild_bd(c, B, st));
   for (int n = 0; n < c->cfg.n_layers; ++n) {
     RET(prefetch(c, n));
     RET(prefetch(c, n + 1));          // overlap the next group's all-gather with this layer (F0)
@@ -1480,6 +1539,7 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
     }
   }
   RET(fence_params(c, st));
+  clear_bd(c);
   CK(cudaGetLastError());
   return DHEN_OK;
 }
