@@ -208,6 +208,11 @@ void dhen_debug_gemm_trace(void* dev_buf);
  * GEMMs + softmax kernels everywhere.  Returns the previous mode.  Process-wide; not thread-safe. */
 int dhen_debug_attn_fused(int mode);
 
+/* Test hook: CTA-pair (cta_group::2) selection of the tcgen05 GEMMs.  mode -1 (default) = the size rule
+ * (K >= 1024 and >= 64 pair items, env DHEN_PAIR / DHEN_PAIR_K), 0 = never, 1 = wherever expressible.
+ * Returns the previous mode.  Process-wide; not thread-safe. */
+int dhen_debug_gemm_pair(int mode);
+
 /* Number of library kernels launched since init (a host-side counter). */
 unsigned long long dhen_launch_count(const dhen_ctx* ctx);
 

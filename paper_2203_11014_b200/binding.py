@@ -24,7 +24,7 @@ EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "d
            "dhen_layer_bwd", "dhen_train_step", "dhen_train_step_graphed", "dhen_forward", "dhen_zero_grad", "dhen_params_io",
            "dhen_grads_get", "dhen_launch_count", "dhen_last_error", "dhen_destroy", "dhen_profile",
            "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_gemm_epi", "dhen_debug_last_gemm_tc",
-           "dhen_debug_gemm_trace", "dhen_debug_attn_fused")
+           "dhen_debug_gemm_trace", "dhen_debug_attn_fused", "dhen_debug_gemm_pair")
 
 
 class dhen_module(C.Structure):
@@ -102,6 +102,8 @@ def load(path: str = LIB_PATH):
     lib.dhen_debug_last_gemm_tc.argtypes = []
     lib.dhen_debug_attn_fused.restype = C.c_int
     lib.dhen_debug_attn_fused.argtypes = [C.c_int]
+    lib.dhen_debug_gemm_pair.restype = C.c_int
+    lib.dhen_debug_gemm_pair.argtypes = [C.c_int]
     lib.dhen_destroy.restype = None
     lib.dhen_destroy.argtypes = [vp]
     _lib = lib
@@ -218,6 +220,11 @@ def debug_gemm(q, A, B, Cm, path=0, ws=None, stream=None):
                                                      C.c_void_p(Cm.data_ptr()), abt, ct, path,
                                                      C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(s.cuda_stream)))
     return int(load().dhen_debug_last_gemm_tc())
+
+
+def debug_gemm_pair(mode: int) -> int:
+    """Test hook: CTA-pair GEMM selection (-1 size rule, 0 never, 1 wherever expressible); returns the previous mode."""
+    return int(load().dhen_debug_gemm_pair(int(mode)))
 
 
 def debug_attn_fused(mode: int) -> int:

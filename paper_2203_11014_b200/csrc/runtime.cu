@@ -1330,11 +1330,12 @@ dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* Bp, v
   w.ptr = (float*)ws;
   w.bytes = ws_bytes;
   dhen::g_gemm_force = path >= 3 ? 2 : path;
-  dhen::g_gemm_pair = path == 3 ? 1 : path == 4 ? 0 : -1;
+  const int pair_prev = dhen::g_gemm_pair;
+  dhen::g_gemm_pair = path == 3 ? 1 : path == 4 ? 0 : pair_prev;
   cudaError_t e = gemm_run(g, w, S(stream));
   const int used_tc = g_last_gemm_tc;
   dhen::g_gemm_force = -1;
-  dhen::g_gemm_pair = -1;
+  dhen::g_gemm_pair = pair_prev;
   if (e == cudaErrorNotSupported) return fail(DHEN_E_CONFIG, "dhen_debug_gemm: layout not supported on this path");
   CK(e);
   return used_tc ? DHEN_OK : DHEN_OK;
@@ -1342,6 +1343,11 @@ dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* Bp, v
 
 int dhen_debug_last_gemm_tc(void) { return g_last_gemm_tc; }
 int dhen_debug_attn_fused(int mode) { return attn::set_mode(mode); }
+int dhen_debug_gemm_pair(int mode) {
+  const int old = dhen::g_gemm_pair;
+  dhen::g_gemm_pair = mode < 0 ? -1 : mode > 0 ? 1 : 0;
+  return old;
+}
 
 dhen_status dhen_debug_gemm_epi(const long long* q, const void* A, const void* Bp, void* Cp, int ab_dt, int c_dt,
                                 int path, void* ws, size_t ws_bytes, int mode, const void* E, const void* bias,
@@ -1373,10 +1379,11 @@ dhen_status dhen_debug_gemm_epi(const long long* q, const void* A, const void* B
   w.ptr = (float*)ws;
   w.bytes = ws_bytes;
   dhen::g_gemm_force = path >= 3 ? 2 : path;
-  dhen::g_gemm_pair = path == 3 ? 1 : path == 4 ? 0 : -1;
+  const int pair_prev = dhen::g_gemm_pair;
+  dhen::g_gemm_pair = path == 3 ? 1 : path == 4 ? 0 : pair_prev;
   cudaError_t e = gemm_run(g, w, S(stream));
   dhen::g_gemm_force = -1;
-  dhen::g_gemm_pair = -1;
+  dhen::g_gemm_pair = pair_prev;
   if (e == cudaErrorNotSupported) return fail(DHEN_E_CONFIG, "dhen_debug_gemm_epi: layout not supported on this path");
   CK(e);
   return DHEN_OK;

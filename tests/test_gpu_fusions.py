@@ -6,6 +6,7 @@ DHEN_OVERLAP      weight gradients / module branches on a second stream        -
 DHEN_LN_FUSE      LayerNorm in the producing GEMM epilogues (F5, F6, F12)      -> same storage points
 DHEN_FIRST_WRITER first / last dX writer (B3, B10) instead of LN-bwd init + cast -> same fp32 sums, other order
 DHEN_RELU_BITS    FFN ReLU derivative from a bitmask                            -> bitwise identical
+dhen_debug_gemm_pair CTA-pair GEMMs vs single-CTA tiles                       -> same sums up to split grouping
 """
 import numpy as np
 import pytest
@@ -69,4 +70,22 @@ def test_first_last_dx_writer(name, B, layers, monkeypatch):
     net = _net(name, layers)
     a = _step(net, B, 13, {"DHEN_FIRST_WRITER": "0"}, monkeypatch)
     b = _step(net, B, 13, {"DHEN_FIRST_WRITER": "1"}, monkeypatch)
+    _cmp(a, b, net, 1e-2)
+
+
+@pytest.mark.parametrize("name,B,layers", [("C2", 2048, 2), ("C4", 128, 2)])
+def test_cta_pairs_match_single_cta(name, B, layers, monkeypatch):
+    """CTA-pair GEMMs (cta_group::2, deeper ring; LayerNorm epilogues included) against single-CTA tiles on
+    the same step, at batch sizes where the size rule takes pairs (C2: the dot projection family at the
+    bench's B = 2048; C4: FFN2 and the long-K weight gradients).  Same MMA chain per output row, so the
+    results agree to rounding of the split-K reduction grouping."""
+    from paper_2203_11014_b200.binding import debug_gemm_pair
+    net = _net(name, layers)
+    old = debug_gemm_pair(0)
+    try:
+        a = _step(net, B, 14, {}, monkeypatch)
+        debug_gemm_pair(-1)
+        b = _step(net, B, 14, {}, monkeypatch)
+    finally:
+        debug_gemm_pair(old)
     _cmp(a, b, net, 1e-2)
