@@ -65,6 +65,9 @@ struct Epilogue {
   // DCN backward fused into the token-mixing dgrad (B8): v = acc (= dT); aux <- v * x (dA, x = cross view);
   // C += v * a + v (a = mask view holds A; C is the fp32 dX accumulator)
   int dcn_bwd = 0;
+  // with dcn_bwd (tcgen05 path, N <= 256): column sums of dA, one fixed-order partial row per CTA into
+  // bsum[blockIdx][N] (the bias gradient's partials; g_last_gemm_grid rows are written)
+  float* bsum = nullptr;
   // Gram triangle (F1): element (i, j) of sample z is stored iff j > i, at C + z * c.bs0 +
   // i * triu_m - i (i + 1) / 2 + (j - i - 1)  (strict upper triangle, row-major pairs, R7)
   int triu_m = 0;
@@ -104,6 +107,7 @@ struct Workspace {              // scratch for split-K partials (fp32)
 extern unsigned long long g_launches;
 // 1 if the last gemm_run took the tcgen05 path (profiling attribution).
 extern int g_last_gemm_tc;
+extern int g_last_gemm_grid;   // CTAs of the last tcgen05 GEMM launch (rows of an Epilogue::bsum partial)
 extern int g_gemm_pair;
 extern int g_last_gemm_pair;
 // path override: -1 env/auto, 0 auto, 1 SIMT only, 2 tcgen05 only (test hook)

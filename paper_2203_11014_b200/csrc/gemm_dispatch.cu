@@ -9,6 +9,7 @@
 namespace dhen {
 
 int g_last_gemm_tc = 0;
+int g_last_gemm_grid = 0;
 int pdl_enabled() {
   static int v = [] { const char* e = getenv("DHEN_PDL"); return e ? atoi(e) : 0; }();
   return v;

@@ -148,6 +148,7 @@ static bool make_lean(const Gemm& g, Lean* e) {
   e->triu_m = x.triu_m;
   e->triu_spt = x.triu_spt;
   e->triu_ld = x.triu_ld;
+  e->bsum = x.dcn_bwd ? x.bsum : nullptr;
   if (x.dcn_bwd) {
     if (g.c.dt != F32 || !x.cross.ptr || !x.mask.ptr || !x.aux.ptr || x.bias || x.accumulate) return false;
     e->flags = EF_DCNB | (x.resid.ptr ? EF_RESID : 0);   // with a residual: first writer (C = resid + ...)
@@ -279,6 +280,10 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   if (p.tstore && var != p.lean_id) p.tstore = 0;
   if (g.e.ln_gamma && (!p.lean || var != p.lean_id || (p.ep.flags & EF_LN) == 0 || p.lanes_rows)) return cudaErrorNotSupported;
   if (g.e.bits_mode && !p.tstore) return cudaErrorNotSupported;   // bitmask epilogues exist on the TMA-store path
+  // fused dA column sums exist in the row-major DCN-backward pass only (single CTAs, N <= 256)
+  if (g.e.bsum && (!g.e.dcn_bwd || var == 0 || !p.fast8 || p.lanes_rows || p.pair || g.N > 256 ||
+                   (p.ep.flags & EF_DCNB) == 0))
+    return cudaErrorNotSupported;
   cudaError_t e = BN == 64 ? launch_bn64(p, ma, mb, mc, st, var) : BN == 128 ? launch_bn128(p, ma, mb, mc, st, var)
                                                                : launch_bn256(p, ma, mb, mc, st, var);
   if (e != cudaSuccess) return e;

@@ -64,6 +64,7 @@ struct Lean {
   int ln_d;
   uint32_t* bits;     // ReLU bitmask, word-major [N / 32][bits_ld = M]: EF_BITS writes (value > 0), EF_BMASK masks
   int64_t bits_ld;
+  float* bsum;        // EF_DCNB: per-CTA column sums of dA -> bsum[blockIdx][N] (N <= 256), or nullptr
 };
 
 // TMA maps of the epilogue outputs: c = C, d = the aux output (the LayerNorm epilogue's pre-norm sum R)
@@ -501,7 +502,7 @@ __device__ __forceinline__ int64_t shfl64(int64_t v, int src) {
 // then the group is combined and stored -- one memory latency per group instead of per row.
 template <int F, bool CF32, int SC>
 __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int M, int N, int cbase, uint32_t stage,
-                                           int lane) {
+                                           int lane, uint32_t csw = 0u) {
   constexpr int LPR = SC / 8, RPP = 32 / LPR, SROW = SC + 4;
   constexpr int NR = 32 / RPP;                               // rows per lane in this pass
   // operands to prefetch per row: bf16 uint4 slots (X / A / mask / resid / bf16 C) and fp32 C
@@ -528,6 +529,9 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
     for (int t = 0; t < 8; ++t) bias8[t] = lean_bias(e, col + t);
   }
   const float alpha = e.alpha;
+  float dsum[(F & EF_DCNB) ? 8 : 1];   // EF_DCNB with csw: this lane's column sums of dA over its rows
+#pragma unroll
+  for (int t = 0; t < ((F & EF_DCNB) ? 8 : 1); ++t) dsum[t] = 0.f;
   // operand loads of row group q (rows sub + (q * G + k) * RPP) into register buffer `buf`; the loads of
   // group q + 1 are issued before group q is combined and stored (two groups in flight per lane)
   constexpr int NG = NR / G;
@@ -607,6 +611,10 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
           dx[t] = v * av[t] + v;
         }
         stg8<false>(e.aux, ok_, da);
+        if constexpr ((F & EF_DCNB) != 0) {   // the bias gradient sums dA as STORED (bf16), in row order
+#pragma unroll
+          for (int t = 0; t < 8; ++t) dsum[t] += __bfloat162float(__float2bfloat16_rn(da[t]));
+        }
         if constexpr ((F & EF_RESID) != 0) {
           // first writer of the dX accumulator: dX = dR (identity shortcut, B3) + dT A + dT, a plain store
           float rv8[8];
@@ -657,6 +665,23 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
         }
       }
       stg8<CF32>(e.c, ok_, a);
+    }
+  }
+  if constexpr ((F & EF_DCNB) != 0) {
+    if (csw) {   // fold the lanes of one column group (fixed xor tree), then one lane adds to the warp's row
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) dsum[t] += __shfl_xor_sync(0xffffffffu, dsum[t], o);
+      if (sub == 0 && cok) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const uint32_t a_ = csw + (uint32_t)((col + t) * 4);
+          float s_;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(s_) : "r"(a_) : "memory");
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(a_), "f"(s_ + dsum[t]) : "memory");
+        }
+      }
     }
   }
 }
@@ -821,6 +846,9 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* tfull = bars + 2 * NST;
   uint64_t* tempty = bars + 2 * NST + 2;
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * NST + 4);
+  // DCN-backward variants: [8 epilogue warps][256 columns] fp32 column sums of dA (Lean::bsum)
+  constexpr bool BSV = VAR > 0 && (VarF<VAR>::F & EF_DCNB) != 0;
+  float* csum = (float*)(bars + 2 * NST + 6);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = p.tiles_m * p.tiles_n;
   const int total = ntiles * p.nz * p.splits;
@@ -848,6 +876,9 @@ __global__ void __launch_bounds__(320, 1)
                    "r"(2 * BN));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+  }
+  if constexpr (BSV) {
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) csum[i] = 0.f;
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -1291,7 +1322,10 @@ __global__ void __launch_bounds__(320, 1)
         const int cbase = n0 + hh * HC + pc;
         if (p.dbg == 1) {
         } else if (VAR > 0) {
-          if constexpr (VAR > 0) lean_pass8<VarF<VAR>::F, VarF<VAR>::C, SC>(e, z, rbase, g.M, g.N, cbase, stage, lane);
+          if constexpr (VAR > 0)
+            lean_pass8<VarF<VAR>::F, VarF<VAR>::C, SC>(
+                e, z, rbase, g.M, g.N, cbase, stage, lane,
+                (BSV && e.bsum) ? smem_u32(csum) + (uint32_t)((warp - 2) * 256 * 4) : 0u);
         } else if (p.lean && p.fast) {
           constexpr int LPR = SC / 4;          // lanes per row (4 columns each)
           constexpr int RPP = 32 / LPR;        // rows per pass
@@ -1386,6 +1420,16 @@ __global__ void __launch_bounds__(320, 1)
   if ((p.tstore || p.lnst) && warp >= 2 && lane == 0) bulk_wait_all();   // TMA stores done reading smem and written
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if constexpr (BSV) {   // this CTA's partial row of the dA column sums: warps summed in a fixed order
+    if (p.ep.bsum) {
+      for (int col = threadIdx.x; col < p.g.N; col += blockDim.x) {
+        float s_ = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s_ += csum[w * 256 + col];
+        p.ep.bsum[(int64_t)blockIdx.x * p.g.N + col] = s_;
+      }
+    }
+  }
   if (pair) {
     cluster_sync_all();   // no CTA leaves while its peer may still touch its barriers, smem or TMEM
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -1399,7 +1443,8 @@ template <int BN, int STAGES, int VAR>
 static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                           cudaStream_t st) {
   constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + EpiSmem<BN>::BYTES + EpiSmem<BN>::SBIAS * 4 +
-                       (2 * ring_stages<BN, STAGES, true>() + 4) * 8 + 16 + 1024;
+                       (2 * ring_stages<BN, STAGES, true>() + 4) * 8 + 16 + 1024 +
+                       ((VarF<VAR>::F & EF_DCNB) != 0 ? 8 * 256 * 4 : 0);
   static_assert(SMEM <= 227 * 1024, "smem");
   static bool attr = false;
   if (!attr) {
@@ -1434,6 +1479,7 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
         }
       }
       cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(items, max_clusters)));
+      g_last_gemm_grid = (int)cfg.gridDim.x;
       cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, VAR, true>, ma, mb, mc, p);
       if (e != cudaSuccess) return e;
       ++g_launches;
@@ -1441,6 +1487,7 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
     }
     {
       const int grid = (int)std::min<int64_t>(items, 148);
+      g_last_gemm_grid = grid;
       cudaError_t e = pdl_launch(gemm_tc_kernel<BN, STAGES, VAR, false>, grid, 320, SMEM, st, ma, mb, mc, p);
       if (e != cudaSuccess) return e;
     }

@@ -442,6 +442,10 @@ static void part_sum(const float* part, int nparts, int n, float* out0, int n0, 
   pdl_launch(part_sum_k, (n + 31) / 32, 1024, 0, st, part, nparts, n, out0, n0, out1, n1, out2, out2_scale);
   ++g_launches;
 }
+cudaError_t rows_sum_add(const float* part, int nparts, int n, float* out, cudaStream_t st) {
+  part_sum(part, nparts, n, out, n, nullptr, 0, nullptr, 0.f, st);
+  return cudaGetLastError();
+}
 
 static cudaError_t ln_bwd_generic(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
                    const void* gamma, int pdt, int64_t rows, int d, void* dR, int dt, float* acc, int acc_mode,

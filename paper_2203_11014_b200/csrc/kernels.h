@@ -25,6 +25,8 @@ cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu,
 // (st_red: the final fixed-order reduction of the dgamma / dbeta partials runs there, after ev_red is
 //  recorded on st; scratch must then stay untouched on st until st_red is joined back)
 
+// out[c] += sum_p part[p * n + c] over p < nparts, in index order (partial rows -> a gradient)
+cudaError_t rows_sum_add(const float* part, int nparts, int n, float* out, cudaStream_t st);
 // out[c] += sum_r src[r * ld + c] for c < cols (deterministic two-pass).
 cudaError_t colsum_add(const void* src, int dt, int64_t rows, int cols, int64_t ld, float* out,
                        float* scratch, size_t scratch_bytes, cudaStream_t st);

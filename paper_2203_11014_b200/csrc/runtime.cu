@@ -156,7 +156,9 @@ struct dhen_ctx {
   Workspace ws2;                      // split-K scratch of the side stream
   float* red2 = nullptr;              // reduction scratch of the side stream
   float* red3 = nullptr;              // layer-LN parameter partials (their final sum trails on the side stream)
+  float* bsum = nullptr;              // DCN backward: per-CTA column sums of dA from the dT GEMM epilogue
   int trail = 1;                      // DHEN_TRAIL: parameter-sum reductions of LN / head trail on the side stream
+  int fuse_db = 1;                    // DHEN_FUSE_DB: DCN bias gradient from the dT GEMM epilogue's column sums
   float *pooled = nullptr, *z = nullptr, *lossb = nullptr, *dz = nullptr;
   float* gtmp = nullptr;    // fp32 [max_npad]: all-gather target of params_io / grads_get (world > 1)
   ncclComm_t comm = nullptr;
@@ -430,6 +432,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   c->ws2.ptr = (float*)work.take(c->ws2.bytes);
   c->red2 = (float*)work.take(c->red_bytes);
   c->red3 = (float*)work.take(c->red_bytes);
+  c->bsum = (float*)work.take((size_t)2 * 148 * 256 * 4);   // DCN bias partial rows [<= 296 CTAs][d <= 256]
   c->pooled = (float*)work.take(((size_t)B * d + (size_t)B * (d + 2)) * 4);   // + head partials [B][d + 2]
   c->z = (float*)work.take((size_t)B * 4);
   c->lossb = (float*)work.take((size_t)B * 4);
@@ -451,6 +454,24 @@ static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const 
   CK(gemm_run(g, ws ? *ws : (st == c->side_st ? c->ws2 : c->ws), st));   // each stream its own split-K scratch
   if (ps.rec >= 0) c->recs[ps.rec].tc = g_last_gemm_tc;
   return DHEN_OK;
+}
+// The DCN backward dT GEMM with the fused dA column sums (Epilogue::bsum) when its tcgen05 pass can take
+// them; otherwise the same GEMM without (and *rows = 0: the caller sums dA with colsum_add instead).
+static dhen_status G_dT(Gemm& g, dhen_ctx* c, cudaStream_t st, int* rows) {
+  *rows = 0;
+  if (g.e.bsum) {
+    cudaError_t e;
+    {
+      ProfScope ps(c, "dcn.dT_fused", 2.0 * (double)g.M * g.N * g.K * g.batch, 0.0, st);
+      e = gemm_run(g, c->ws, st);
+      if (ps.rec >= 0) c->recs[ps.rec].tc = g_last_gemm_tc;
+    }
+    if (e == cudaSuccess) { *rows = g_last_gemm_grid; return DHEN_OK; }
+    if (e != cudaErrorNotSupported) CK(e);
+    (void)cudaGetLastError();
+    g.e.bsum = nullptr;
+  }
+  return G_(g, c, st, "dcn.dT_fused");
 }
 static Gemm mk(int M, int N, int K, int batch, Operand a, Operand b, View cv) {
   Gemm g;
@@ -899,6 +920,9 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         // operand's two-level K: k -> (sample, t)), so every MMA row and epilogue warp carries data.
         const int spt = 128 / std::max(mi, 1);
         const bool pack = dcn_pack(c, mi, l, B);
+        // the bias gradient's column sums of dA come out of the dT GEMM's epilogue (one partial row per CTA)
+        const bool fuse_db = c->fuse_db && dt == BF16 && d <= 256;
+        int bsum_rows = 0;
         if (pack) {
           void* bdg = md.bdg_pre ? md.bdg : c->bdiag;
           if (!md.bdg_pre) KT("dcn.bdiag", 0, 2.0 * 128 * 128 * es, blockdiag(p(md.Wu), mi, l, spt, bdg, st));
@@ -909,7 +933,8 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
           gt.e.mask = view(md.A, dt, d, 1, (int64_t)spt * mi * d);
           gt.e.aux = view(dA, dt, d, 1, (int64_t)spt * mi * d);
           if (take_dR) gt.e.resid = view(c->dR, dt, d, 1, (int64_t)spt * mi * d);
-          RET(G_(gt, c, st, "dcn.dT_fused"));
+          if (fuse_db) gt.e.bsum = c->bsum;
+          RET(G_dT(gt, c, st, &bsum_rows));
         } else {
         // m < 128: as its transpose dT_b^T = dU_b^T W_u^T (M = d rows fill the MMA tile), C column-contiguous
         const bool tr = c->tr_small_m && mi < 128 && dt == BF16;
@@ -923,7 +948,8 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         gt.e.mask = view(md.A, dt, vr, vc, (int64_t)mi * d);
         gt.e.aux = view(dA, dt, vr, vc, (int64_t)mi * d);
         if (take_dR) gt.e.resid = view(c->dR, dt, vr, vc, (int64_t)mi * d);
-        RET(G_(gt, c, st, "dcn.dT_fused"));
+        if (fuse_db && !tr) gt.e.bsum = c->bsum;
+        RET(G_dT(gt, c, st, &bsum_rows));
         }
         if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dA ready
         Gemm gx = mk((int)rows, d, d, 1, operand(dA, dt, d, 1), operand(p(md.W), dt, 1, d), view(acc, F32, d, 1));
@@ -933,7 +959,10 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         Gemm gw = mk(d, d, (int)rows, 1, operand(dA, dt, 1, d), operand(X, dt, 1, d), view(gp(md.W), F32, d, 1));
         gw.e.accumulate = 1;
         RET(G_(gw, c, sd, "dcn.wgrad", ws2));
-        KTS(sd, "dcn.bias_grad", 0, (double)rows * d * es, colsum_add(dA, dt, rows, d, d, gp(md.b), red2, c->red_bytes, sd));
+        if (bsum_rows > 0)
+          KTS(sd, "dcn.bias_grad", 0, (double)bsum_rows * d * 4, rows_sum_add(c->bsum, bsum_rows, d, gp(md.b), sd));
+        else
+          KTS(sd, "dcn.bias_grad", 0, (double)rows * d * es, colsum_add(dA, dt, rows, d, d, gp(md.b), red2, c->red_bytes, sd));
         RET(join());
         break;
       }
@@ -1236,6 +1265,8 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
     c->overlap = ev ? atoi(ev) : 1;
     const char* et = getenv("DHEN_TRAIL");
     c->trail = et ? atoi(et) : 1;
+    const char* ef = getenv("DHEN_FUSE_DB");
+    c->fuse_db = ef ? atoi(ef) : 1;
     bool ok = cudaStreamCreateWithFlags(&c->side_st, cudaStreamNonBlocking) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_sf, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_sx, cudaEventDisableTiming) == cudaSuccess;
