@@ -68,6 +68,9 @@ struct Epilogue {
   // with dcn_bwd (tcgen05 path, N <= 256): column sums of dA, one fixed-order partial row per CTA into
   // bsum[blockIdx][N] (the bias gradient's partials; g_last_gemm_grid rows are written)
   float* bsum = nullptr;
+  // bf16 C on the TMA-store path: column sums of the STORED C over each 32-row block, written to
+  // csum[(z * ceil(M / 32) + row / 32) * N + col] (a bias gradient's partial rows)
+  float* csum = nullptr;
   // Gram triangle (F1): element (i, j) of sample z is stored iff j > i, at C + z * c.bs0 +
   // i * triu_m - i (i + 1) / 2 + (j - i - 1)  (strict upper triangle, row-major pairs, R7)
   int triu_m = 0;

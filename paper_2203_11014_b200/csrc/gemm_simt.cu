@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_elem_kernel(Gemm g, int spl
 
 cudaError_t gemm_simt(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
-  if (g.e.ln_gamma || g.e.bits_mode || g.e.bsum) return cudaErrorNotSupported;   // tcgen05-path-only epilogues
+  if (g.e.ln_gamma || g.e.bits_mode || g.e.bsum || g.e.csum) return cudaErrorNotSupported;   // tcgen05-path-only epilogues
   int tm = (g.M + BM - 1) / BM, tn = (g.N + BN - 1) / BN;
   int64_t tiles = (int64_t)tm * tn * g.batch;
   int splits = 1;

@@ -149,6 +149,7 @@ static bool make_lean(const Gemm& g, Lean* e) {
   e->triu_spt = x.triu_spt;
   e->triu_ld = x.triu_ld;
   e->bsum = x.dcn_bwd ? x.bsum : nullptr;
+  e->csum = x.csum;
   if (x.dcn_bwd) {
     if (g.c.dt != F32 || !x.cross.ptr || !x.mask.ptr || !x.aux.ptr || x.bias || x.accumulate) return false;
     e->flags = EF_DCNB | (x.resid.ptr ? EF_RESID : 0);   // with a residual: first writer (C = resid + ...)
@@ -280,6 +281,8 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   if (p.tstore && var != p.lean_id) p.tstore = 0;
   if (g.e.ln_gamma && (!p.lean || var != p.lean_id || (p.ep.flags & EF_LN) == 0 || p.lanes_rows)) return cudaErrorNotSupported;
   if (g.e.bits_mode && !p.tstore) return cudaErrorNotSupported;   // bitmask epilogues exist on the TMA-store path
+  // column sums of the stored C exist on the bf16 TMA-store path only (rows = M / 32 blocks per batch item)
+  if (g.e.csum && (!p.tstore || g.c.dt != BF16 || g.e.accumulate)) return cudaErrorNotSupported;
   // fused dA column sums exist in the row-major DCN-backward pass only (single CTAs, N <= 256)
   if (g.e.bsum && (!g.e.dcn_bwd || var == 0 || !p.fast8 || p.lanes_rows || p.pair || g.N > 256 ||
                    (p.ep.flags & EF_DCNB) == 0))

@@ -65,6 +65,7 @@ struct Lean {
   uint32_t* bits;     // ReLU bitmask, word-major [N / 32][bits_ld = M]: EF_BITS writes (value > 0), EF_BMASK masks
   int64_t bits_ld;
   float* bsum;        // EF_DCNB: per-CTA column sums of dA -> bsum[blockIdx][N] (N <= 256), or nullptr
+  float* csum;        // TMA-store bf16 C: column sums of the stored C per 32-row block -> csum[row / 32][N]
 };
 
 // TMA maps of the epilogue outputs: c = C, d = the aux output (the LayerNorm epilogue's pre-norm sum R)
@@ -1239,6 +1240,27 @@ __global__ void __launch_bounds__(320, 1)
               if constexpr ((F & EF_ACC) != 0) tma_reduce_add3(&tma_o.c, box, n0 + cl0, rbase, z);
               else tma_store3(&tma_o.c, box, n0 + cl0, rbase, z);
               bulk_commit();
+            }
+            if constexpr (!CF && (F & EF_ACC) == 0) {
+              if (e.csum) {   // column sums of the 32 stored (bf16) rows: lane = 2 columns, read down the box
+                float s0 = 0.f, s1 = 0.f;
+                const int nr = min(32, g.M - rbase);
+#pragma unroll 4
+                for (int r = 0; r < nr; ++r) {
+                  uint32_t w;
+                  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w)
+                               : "r"(box + (uint32_t)(r * 128 + ((((lane >> 2) ^ (r & 7)) & 7) << 4) + (lane & 3) * 4))
+                               : "memory");
+                  s0 += __uint_as_float(w << 16);
+                  s1 += __uint_as_float(w & 0xffff0000u);
+                }
+                const int cg = n0 + cl0 + 2 * lane;
+                if (cg < g.N) {
+                  float* cp = e.csum + ((int64_t)z * ((g.M + 31) / 32) + rbase / 32) * g.N + cg;
+                  cp[0] = s0;
+                  if (cg + 1 < g.N) cp[1] = s1;
+                }
+              }
             }
           }
           continue;

@@ -157,6 +157,7 @@ struct dhen_ctx {
   float* red2 = nullptr;              // reduction scratch of the side stream
   float* red3 = nullptr;              // layer-LN parameter partials (their final sum trails on the side stream)
   float* bsum = nullptr;              // DCN backward: per-CTA column sums of dA from the dT GEMM epilogue
+  float* csum = nullptr;              // attention FFN: 32-row column sums of dF from the FFN2 dgrad epilogue
   int trail = 1;                      // DHEN_TRAIL: parameter-sum reductions of LN / head trail on the side stream
   int fuse_db = 1;                    // DHEN_FUSE_DB: DCN bias gradient from the dT GEMM epilogue's column sums
   float *pooled = nullptr, *z = nullptr, *lossb = nullptr, *dz = nullptr;
@@ -257,7 +258,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   const int world = c->dist.world;
   const bool shard = world > 1 && c->dist.fsdp;
   int m = c->cfg.m0, m_max = m, H_mm_max = 0, f_max = d, m_out_max = 0;
-  int64_t tC_elems = 0, tA_elems = 0;
+  int64_t tC_elems = 0, tA_elems = 0, csum_elems = 0;
   bool has_attn_any = false;
   for (int n = 0; n < c->cfg.n_layers; ++n)
     for (int i = 0; i < c->cfg.layers[n].n_modules; ++i) has_attn_any |= c->cfg.layers[n].modules[i].kind == DHEN_ATTN;
@@ -391,6 +392,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
           H_mm_max = std::max(H_mm_max, H * mi * mp);
           f_max = std::max(f_max, f);
           tC_elems = std::max<int64_t>(tC_elems, (int64_t)B * mi * std::max(f, 3 * d));
+          csum_elems = std::max<int64_t>(csum_elems, ((int64_t)B * mi + 31) / 32 * f);
           break;
         }
         case DHEN_MLP: {
@@ -433,6 +435,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   c->red2 = (float*)work.take(c->red_bytes);
   c->red3 = (float*)work.take(c->red_bytes);
   c->bsum = (float*)work.take((size_t)2 * 148 * 256 * 4);   // DCN bias partial rows [<= 296 CTAs][d <= 256]
+  if (csum_elems) c->csum = (float*)work.take((size_t)csum_elems * 4);   // attention db_1 partial rows
   c->pooled = (float*)work.take(((size_t)B * d + (size_t)B * (d + 2)) * 4);   // + head partials [B][d + 2]
   c->z = (float*)work.take((size_t)B * 4);
   c->lossb = (float*)work.take((size_t)B * 4);
@@ -472,6 +475,24 @@ static dhen_status G_dT(Gemm& g, dhen_ctx* c, cudaStream_t st, int* rows) {
     g.e.bsum = nullptr;
   }
   return G_(g, c, st, "dcn.dT_fused");
+}
+// A GEMM with fused column sums of its stored output (Epilogue::csum) when its TMA-store pass can take
+// them; otherwise the same GEMM without (*ok = false: the caller sums the output itself).
+static dhen_status G_csum(Gemm& g, dhen_ctx* c, cudaStream_t st, const char* tag, bool* ok) {
+  *ok = false;
+  if (g.e.csum) {
+    cudaError_t e;
+    {
+      ProfScope ps(c, tag, 2.0 * (double)g.M * g.N * g.K * g.batch, 0.0, st);
+      e = gemm_run(g, c->ws, st);
+      if (ps.rec >= 0) c->recs[ps.rec].tc = g_last_gemm_tc;
+    }
+    if (e == cudaSuccess) { *ok = true; return DHEN_OK; }
+    if (e != cudaErrorNotSupported) CK(e);
+    (void)cudaGetLastError();
+    g.e.csum = nullptr;
+  }
+  return G_(g, c, st, tag);
 }
 static Gemm mk(int M, int N, int K, int batch, Operand a, Operand b, View cv) {
   Gemm g;
@@ -1006,13 +1027,20 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         } else {
           a.e.mask = view(md.F, dt, f, 1);
         }
-        RET(G_(a, c, st, "attn.ffn2_dgrad"));
+        // db_1 = column sums of dF: 32-row partial sums folded in the dgrad's TMA-store epilogue
+        bool db1_fused = false;
+        if (c->fuse_db && dt == BF16 && c->csum) a.e.csum = c->csum;
+        RET(G_csum(a, c, st, "attn.ffn2_dgrad", &db1_fused));
         RET(ready());   // dF
         {
           Gemm w1 = mk(f, d, (int)rows, 1, operand(dF, dt, 1, f), operand(md.Z1, dt, 1, d), view(gp(md.W1), F32, d, 1));
           w1.e.accumulate = 1;
           RET(G_(w1, c, sd, "attn.ffn1_wgrad", ws2));
-          KTS(sd, "attn.bias_grad", 0, (double)rows * f * es, colsum_add(dF, dt, rows, f, f, gp(md.b1), red2, c->red_bytes, sd));
+          if (db1_fused)
+            KTS(sd, "attn.bias_grad", 0, (double)((rows + 31) / 32) * f * 4,
+                colsum_add(c->csum, F32, (rows + 31) / 32, f, f, gp(md.b1), red2, c->red_bytes, sd));
+          else
+            KTS(sd, "attn.bias_grad", 0, (double)rows * f * es, colsum_add(dF, dt, rows, f, f, gp(md.b1), red2, c->red_bytes, sd));
         }
         Gemm z1 = mk((int)rows, d, f, 1, operand(dF, dt, f, 1), operand(p(md.W1), dt, 1, d), view(c->rtmp, F32, d, 1));
         z1.e.resid = view(dR2, dt, d, 1);

@@ -115,10 +115,12 @@ def test_layernorm_epilogue_matches_ln_kernel(m, d, B, monkeypatch):
 @pytest.mark.parametrize("m,d,B", [(128, 128, 160), (100, 256, 70)])
 def test_relu_bitmask_matches_bf16_mask(m, d, B, monkeypatch):
     """B6 FFN: the ReLU derivative taken from the forward's bitmask (bit = stored bf16 F > 0, R22) gives the
-    same data and weight gradients, bit for bit, as reading F itself."""
+    same data and weight gradients, bit for bit, as reading F itself.  (db_1's in-epilogue column sums exist
+    on the bitmask's TMA-store path only, so both arms take the separate column-sum kernel here.)"""
     from paper_2203_11014_b200.binding import debug_attn_fused
     debug_attn_fused(1)
     net = _net(m, d)
+    monkeypatch.setenv("DHEN_FUSE_DB", "0")
     out = {}
     for mode in ("0", "1"):
         monkeypatch.setenv("DHEN_RELU_BITS", mode)

@@ -7,7 +7,7 @@ DHEN_LN_FUSE      LayerNorm in the producing GEMM epilogues (F5, F6, F12)      -
 DHEN_FIRST_WRITER first / last dX writer (B3, B10) instead of LN-bwd init + cast -> same fp32 sums, other order
 DHEN_RELU_BITS    FFN ReLU derivative from a bitmask                            -> bitwise identical
 dhen_debug_gemm_pair CTA-pair GEMMs vs single-CTA tiles                       -> same sums up to split grouping
-DHEN_FUSE_DB      DCN bias gradient from the dT GEMM epilogue (column sums)     -> same values, other grouping
+DHEN_FUSE_DB      bias gradients from GEMM epilogue column sums (DCN db, FFN db_1) -> same values, other grouping
 """
 import numpy as np
 import pytest
@@ -92,10 +92,11 @@ def test_cta_pairs_match_single_cta(name, B, layers, monkeypatch):
     _cmp(a, b, net, 1e-2)
 
 
-@pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C5", 16, 2)])
-def test_fused_dcn_bias_grad(name, B, layers, monkeypatch):
-    """B8 db = sum over rows of the stored dA: column sums folded in the dT GEMM epilogue (per-CTA partial
-    rows, fixed order) against the separate column-sum kernel (same bf16 dA values, other grouping)."""
+@pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C5", 16, 2), ("C3", 32, 2), ("C4", 16, 2)])
+def test_fused_bias_grads(name, B, layers, monkeypatch):
+    """Bias gradients summed inside the producing GEMM epilogues against the separate column-sum kernel
+    (same stored bf16 values, other grouping): B8 db = sum of dA (per-CTA partial rows from the DCN dT GEMM)
+    and B6 db_1 = sum of dF (32-row partial rows from the FFN2 dgrad's TMA-store epilogue)."""
     net = _net(name, layers)
     a = _step(net, B, 15, {"DHEN_FUSE_DB": "0"}, monkeypatch)
     b = _step(net, B, 15, {"DHEN_FUSE_DB": "1"}, monkeypatch)
