@@ -546,14 +546,19 @@ __global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const
                                                 const float* __restrict__ mu, const float* __restrict__ rstd,
                                                 const __nv_bfloat16* __restrict__ gamma, int64_t rows,
                                                 __nv_bfloat16* __restrict__ dR, float* __restrict__ acc, int acc_mode,
-                                                float* __restrict__ part, int64_t rows_per_block) {
+                                                float* __restrict__ part, int64_t rows_per_block,
+                                                const float* __restrict__ vdz = nullptr,
+                                                const __nv_bfloat16* __restrict__ vw = nullptr, int vm = 1) {
   pdl_entry();
   constexpr int d = 8 * LPR, RPW = 32 / LPR, RPI = RPW * UR;
   __shared__ float sred[8][2][d];
   const int lane = threadIdx.x & 31, w = threadIdx.x / 32, sub = lane / LPR, c = (lane % LPR) * 8;
   const int64_t rb0 = blockIdx.x * rows_per_block, rb1 = min(rows, rb0 + rows_per_block);
-  float g[8], pg[8], pb[8];
+  float g[8], pg[8], pb[8], wv[8];
   ld8b(gamma + c, g);
+  // vdz: the head's upstream gradient is never stored -- row r of dY is bf16(dz_b / m * w) with b = r / m
+  // (F13 / B1, the same arithmetic as head_v), formed here from the per-sample dz and the head weight
+  if (vdz) ld8b(vw + c, wv);
 #pragma unroll
   for (int t = 0; t < 8; ++t) { pg[t] = 0.f; pb[t] = 0.f; }
   // raw operands of one iteration (bf16 dY and R as 16-B words): the next iteration's are loaded while this
@@ -571,7 +576,18 @@ __global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const
           ry[bsl][u] = __ldcs(reinterpret_cast<const uint4*>(dY + r * d + c));
           ry2[bsl][u] = __ldcs(reinterpret_cast<const uint4*>(dY + r * d + c) + 1);
         } else {
-          ry[bsl][u] = __ldg(reinterpret_cast<const uint4*>(dY + r * d + c));
+          if (vdz) {
+            const float gv = vdz[r / vm] / vm;
+            uint32_t o[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(gv * wv[2 * t], gv * wv[2 * t + 1]);
+              o[t] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            ry[bsl][u] = make_uint4(o[0], o[1], o[2], o[3]);
+          } else {
+            ry[bsl][u] = __ldg(reinterpret_cast<const uint4*>(dY + r * d + c));
+          }
         }
         rx[bsl][u] = __ldg(reinterpret_cast<const uint4*>(Rsave + r * d + c));
         rm[bsl][u] = mu[r];
@@ -746,8 +762,9 @@ cudaError_t ln_fwd(const float* U, const void* addx, const void* gamma, const vo
 cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
                    const void* gamma, int pdt, int64_t rows, int d, void* dR, int dt, float* acc, int acc_mode,
                    float* dgamma, float* dbeta, float* scratch, size_t scratch_bytes, cudaStream_t st,
-                   cudaStream_t st_red, cudaEvent_t ev_red) {
+                   cudaStream_t st_red, cudaEvent_t ev_red, const float* vdz, const void* vw, int vm) {
   const int lpr = ln_lpr(d);
+  if (vdz && !(dt == BF16 && pdt == BF16 && lpr >= 4 && dydt == BF16 && vw && vm > 0)) return cudaErrorNotSupported;
   if (dt == BF16 && pdt == BF16 && lpr >= 4) {
     const int rpi = (32 / lpr) * LNB_UR;
     int nb = (int)std::min<int64_t>((rows + 8 * rpi - 1) / (8 * rpi), ln_bwd_grid(lpr, dydt));
@@ -759,10 +776,12 @@ cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu,
       if (lpr == L) {                                                                                                  \
         if (dydt == BF16)                                                                                              \
           pdl_launch(ln_bwd_r<L, LNB_UR, __nv_bfloat16>, nb, 256, 0, st, (const __nv_bfloat16*)dY, (const __nv_bfloat16*)Rsave, mu, \
-              rstd, (const __nv_bfloat16*)gamma, rows, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb);               \
+              rstd, (const __nv_bfloat16*)gamma, rows, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb, vdz,        \
+              (const __nv_bfloat16*)vw, vm);                                                                   \
         else                                                                                                           \
           pdl_launch(ln_bwd_r<L, LNB_UR, float>, nb, 256, 0, st, (const float*)dY, (const __nv_bfloat16*)Rsave, mu, rstd,           \
-              (const __nv_bfloat16*)gamma, rows, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb);                     \
+              (const __nv_bfloat16*)gamma, rows, (__nv_bfloat16*)dR, acc, acc_mode, scratch, rpb,                   \
+              (const float*)nullptr, (const __nv_bfloat16*)nullptr, 1);                                         \
       }
       LNB2(4) LNB2(8) LNB2(16) LNB2(32)
 #undef LNB2
@@ -1725,6 +1744,7 @@ __global__ void __launch_bounds__(256) head_v(const __nv_bfloat16* __restrict__ 
     for (int c = threadIdx.x; c < d; c += blockDim.x) hpart[(int64_t)b * (d + 2) + c] = dzs * pooled[(int64_t)b * d + c];
     if (threadIdx.x == 0) { hpart[(int64_t)b * (d + 2) + d] = dzs; hpart[(int64_t)b * (d + 2) + d + 1] = lossb[b]; }
   }
+  if (!dY) return;   // dY formed by the last layer's LayerNorm backward instead (ln_bwd vdz)
   const float g = dzs / m;
   // every row of dY[b] is the same vector g * w
   for (int q = threadIdx.x; q < m * CX; q += blockDim.x) {

@@ -21,7 +21,9 @@ cudaError_t ln_fwd(const float* U, const void* addx, const void* gamma, const vo
 cudaError_t ln_bwd(const void* dY, int dydt, const void* Rsave, const float* mu, const float* rstd,
                    const void* gamma, int pdt, int64_t rows, int d, void* dR, int dt, float* acc, int acc_mode,
                    float* dgamma, float* dbeta, float* scratch, size_t scratch_bytes, cudaStream_t st,
-                   cudaStream_t st_red = nullptr, cudaEvent_t ev_red = nullptr);
+                   cudaStream_t st_red = nullptr, cudaEvent_t ev_red = nullptr, const float* vdz = nullptr,
+                   const void* vw = nullptr, int vm = 0);
+// (vdz: dY is not read; row r of dY is bf16(vdz[r / vm] / vm * vw) -- the head's gradient, formed in place)
 // (st_red: the final fixed-order reduction of the dgamma / dbeta partials runs there, after ev_red is
 //  recorded on st; scratch must then stay untouched on st until st_red is joined back)
 

@@ -160,6 +160,8 @@ struct dhen_ctx {
   float* csum = nullptr;              // attention FFN: 32-row column sums of dF from the FFN2 dgrad epilogue
   int trail = 1;                      // DHEN_TRAIL: parameter-sum reductions of LN / head trail on the side stream
   int fuse_db = 1;                    // DHEN_FUSE_DB: DCN bias gradient from the dT GEMM epilogue's column sums
+  int vdy = 1;                        // DHEN_VDY: the head's dY is formed inside the last layer's LN backward
+  bool vdy_now = false;               // set by train_step for the last layer's backward
   float *pooled = nullptr, *z = nullptr, *lossb = nullptr, *dz = nullptr;
   float* gtmp = nullptr;    // fp32 [max_npad]: all-gather target of params_io / grads_get (world > 1)
   ncclComm_t comm = nullptr;
@@ -863,7 +865,9 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   cudaStream_t sd = (c->overlap && !c->prof) ? c->side_st : st;
   // the LN parameter sums trail on sd (own scratch red3; the modules' joins below order its reuse)
   KT("layer.ln_bwd", 0, (double)B * mo * d * (3 * es + (first_dR ? 0 : 4)), ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc, (Lr.Wn >= 0 || first_dR) ? 0 : 1,
-            gp(Lr.gamma), gp(Lr.beta), c->red3, c->red_bytes, st, c->trail ? sd : st, c->ev_red));
+            gp(Lr.gamma), gp(Lr.beta), c->red3, c->red_bytes, st, c->trail ? sd : st, c->ev_red,
+            c->vdy_now ? c->dz : nullptr, c->vdy_now ? c->G[c->cfg.n_layers].comp : nullptr, mo));
+  c->vdy_now = false;
   if (Lr.Wn >= 0)   // B3: dX = W_n dR ; dW_n += sum_b X_b dR_b^T
     RET(tokmix_bwd(c, X, mi, p(Lr.Wn), mo, c->dR, ldU, acc, F32, 0, gp(Lr.Wn), B, st));
   const Workspace* ws2 = &c->ws2;
@@ -1295,6 +1299,8 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
     c->trail = et ? atoi(et) : 1;
     const char* ef = getenv("DHEN_FUSE_DB");
     c->fuse_db = ef ? atoi(ef) : 1;
+    const char* ev2 = getenv("DHEN_VDY");
+    c->vdy = ev2 ? atoi(ev2) : 1;
     bool ok = cudaStreamCreateWithFlags(&c->side_st, cudaStreamNonBlocking) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_sf, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_sx, cudaEventDisableTiming) == cudaSuccess;
@@ -1572,7 +1578,11 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
     RET(layer_fwd(c, n, X, c->L[n].Y, B, st));
     X = c->L[n].Y;
   }
-  RET(head(c, X, c->L.back().m_out, labels, B, Bg, c->dY[0], loss, 1, st));
+  // single GPU, bf16: the head writes only dz; the last layer's LN backward forms dY = dz w / m itself
+  const bool vdy = c->vdy && c->dist.world == 1 && c->dt == BF16 && c->d % 8 == 0 && c->d >= 32 && c->d <= 256 &&
+                   (c->d & (c->d - 1)) == 0;
+  RET(head(c, X, c->L.back().m_out, labels, B, Bg, vdy ? nullptr : c->dY[0], loss, 1, st));
+  c->vdy_now = vdy;
   int cur = 0;
   for (int n = c->cfg.n_layers - 1; n >= 0; --n) {
     void* dx = n > 0 ? c->dY[cur ^ 1] : dx0;

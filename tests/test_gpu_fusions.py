@@ -8,6 +8,7 @@ DHEN_FIRST_WRITER first / last dX writer (B3, B10) instead of LN-bwd init + cast
 DHEN_RELU_BITS    FFN ReLU derivative from a bitmask                            -> bitwise identical
 dhen_debug_gemm_pair CTA-pair GEMMs vs single-CTA tiles                       -> same sums up to split grouping
 DHEN_FUSE_DB      bias gradients from GEMM epilogue column sums (DCN db, FFN db_1) -> same values, other grouping
+DHEN_VDY          head dY formed inside the last LayerNorm backward (not stored) -> bitwise identical
 """
 import numpy as np
 import pytest
@@ -101,3 +102,13 @@ def test_fused_bias_grads(name, B, layers, monkeypatch):
     a = _step(net, B, 15, {"DHEN_FUSE_DB": "0"}, monkeypatch)
     b = _step(net, B, 15, {"DHEN_FUSE_DB": "1"}, monkeypatch)
     _cmp(a, b, net, 1e-3)
+
+
+@pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2)])
+def test_head_gradient_formed_in_ln_backward(name, B, layers, monkeypatch):
+    """B1 -> B2: the head's dY = bf16(dz_b / m w) formed inside the last layer's LayerNorm backward (never
+    stored) is bit-identical to the head kernel writing it and the LayerNorm backward reading it."""
+    net = _net(name, layers)
+    a = _step(net, B, 16, {"DHEN_VDY": "0"}, monkeypatch)
+    b = _step(net, B, 16, {"DHEN_VDY": "1"}, monkeypatch)
+    _cmp(a, b, net, 0)
