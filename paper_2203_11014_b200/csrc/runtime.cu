@@ -184,6 +184,12 @@ struct dhen_ctx {
   std::vector<Rec> recs;
 };
 
+// The profiled pass runs serialised (every op's event-timed duration is its own) unless DHEN_PROF_OVERLAP=1
+// keeps the side stream (the DHEN_PROF_TRACE timeline then shows the real concurrency).
+static bool serial_prof(const dhen_ctx* c) {
+  static int keep = [] { const char* e = getenv("DHEN_PROF_OVERLAP"); return e ? atoi(e) : 0; }();
+  return c->prof && !keep;
+}
 // RAII scope recording a CUDA event pair around one op when profiling is on.
 // Per-op scope: an NVTX range named after the op (so `ncu --nvtx --nvtx-include "<op>/"` captures exactly that
 // op's kernels; a no-op without an attached tool) and, in profiling mode, CUDA events around the op.
@@ -649,7 +655,7 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
   // form U[(b, t)] = blockdiag(W_u^T, ..) x [T_b; T_b+1; ..] (rows = tokens of 128 / l samples per tile).
   const bool lnf = layer_lnf(c, n, B);
   const cudaStream_t st0 = st;
-  const bool use_side = c->overlap && !c->prof && Lr.mods.size() > 1;
+  const bool use_side = c->overlap && !serial_prof(c) && Lr.mods.size() > 1;
   bool has_attn = false;
   for (const Mod& m_ : Lr.mods) has_attn |= m_.s.kind == DHEN_ATTN;
   if (use_side) { CK(cudaEventRecord(c->ev_sf, st0)); CK(cudaStreamWaitEvent(c->side_st, c->ev_sf, 0)); }
@@ -859,10 +865,10 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   const bool first_dR = c->first_writer && Lr.Wn < 0 && mi == mo &&
                         (first_kind == DHEN_DOT || first_kind == DHEN_DCN || first_kind == DHEN_LINEAR || first_kind == DHEN_MLP);
   // Weight gradients of a module run on the side stream `sd` (own split-K / reduction scratch) while its
-  // data gradients run on `st`; `fork` hands the side stream everything enqueued on st so far, `join`
-  // makes st wait for the side stream at the end of the module (shared scratch is reused by the next one).
+  // data gradients run on `st`; `fork` hands the side stream everything enqueued on st so far, and st waits
+  // for the side stream before it overwrites a shared buffer that pending side work reads (and at layer end).
   // (the profiled pass runs serialised so every op's event-timed duration is its own)
-  cudaStream_t sd = (c->overlap && !c->prof) ? c->side_st : st;
+  cudaStream_t sd = (c->overlap && !serial_prof(c)) ? c->side_st : st;
   // the LN parameter sums trail on sd (own scratch red3; the modules' joins below order its reuse)
   KT("layer.ln_bwd", 0, (double)B * mo * d * (3 * es + (first_dR ? 0 : 4)), ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc, (Lr.Wn >= 0 || first_dR) ? 0 : 1,
             gp(Lr.gamma), gp(Lr.beta), c->red3, c->red_bytes, st, c->trail ? sd : st, c->ev_red,
@@ -876,9 +882,39 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
     if (sd != st) { CK(cudaEventRecord(c->ev_sf, st)); CK(cudaStreamWaitEvent(sd, c->ev_sf, 0)); }
     return DHEN_OK;
   };
-  auto join = [&]() -> dhen_status {
+  // Joins are deferred: a module's side-stream work only has to finish before later st work overwrites a
+  // shared buffer it reads.  Bits: 1 tA, 2 tB, 4 tC, 8 tD, 16 bsum; everything else (attention) = all.
+  auto st_writes = [](int k) -> uint32_t {
+    switch (k) {
+      case DHEN_DOT: return 1u | 8u;      // dZ (tA), S (tD)
+      case DHEN_DCN: return 2u | 16u;     // dA (tB), dA column sums (bsum)
+      case DHEN_CONV: return 1u;          // dT (tA)
+      case DHEN_MLP: return 1u | 4u;      // dh2 (tA), dh1 (tC)
+      case DHEN_LINEAR: return 0u;        // the dX accumulator only
+      default: return ~0u;
+    }
+  };
+  auto side_reads = [](int k) -> uint32_t {
+    switch (k) {
+      case DHEN_DOT: return 0u;           // dU and the saved Z
+      case DHEN_DCN: return 2u | 16u;     // dA, its column sums
+      case DHEN_CONV: return 1u;          // dT
+      case DHEN_MLP: return 1u | 4u;      // dh2, dh1
+      case DHEN_LINEAR: return 0u;        // X and dU
+      default: return ~0u;
+    }
+  };
+  uint32_t side_pending = 0;
+  int cur_kind = -1;
+  auto real_join = [&]() -> dhen_status {
     if (sd != st) { CK(cudaEventRecord(c->ev_sj, sd)); CK(cudaStreamWaitEvent(st, c->ev_sj, 0)); }
+    side_pending = 0;
     return DHEN_OK;
+  };
+  static int defer = [] { const char* e = getenv("DHEN_DEFER_JOIN"); return e ? atoi(e) : 1; }();
+  auto join = [&]() -> dhen_status {   // end of a module: record what its side work still reads
+    side_pending |= side_reads(cur_kind);
+    return defer ? DHEN_OK : real_join();
   };
   // The last module's last dX-writing GEMM emits dX (layer dtype) = accumulator + its contribution: the fp32
   // accumulator is read once and never written back, and no cast kernel runs.
@@ -893,6 +929,8 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
     const bool take_dR = first_dR && first_mod;   // this module's first dX write adds the shortcut's dR
     const bool emit_dX = last_dX && mdp == order.back();   // this module's last dX write emits dX
     first_mod = false;
+    cur_kind = md.s.kind;
+    if (side_pending & st_writes(cur_kind)) RET(real_join());
     switch (md.s.kind) {
       case DHEN_DOT: {   // B5
         const int h = mi * (mi - 1) / 2;
@@ -1142,6 +1180,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
       }
     }
   }
+  RET(real_join());   // the layer's side-stream work is done before anything after the layer
   if (dX && !last_dX) KT("layer.dx_cast", 0, (double)rows * d * (4 + es), cast(acc, F32, dX, dt, rows * d, st));
   RET(release(c, n, st));
   RET(reduce_grads(c, n, st));
@@ -1196,7 +1235,7 @@ static dhen_status head(dhen_ctx* c, const void* YN, int mN, const float* labels
   Group& G = c->G[gi];
   // single GPU: the head's parameter / loss sums trail on the side stream (the first backward layer's
   // module joins bring it back before anything reads them); with collectives they stay on st
-  cudaStream_t sr = (c->overlap && c->trail && !c->prof && c->dist.world == 1) ? c->side_st : st;
+  cudaStream_t sr = (c->overlap && c->trail && !serial_prof(c) && c->dist.world == 1) ? c->side_st : st;
   KT("head", 0, (double)B * mN * c->d * c->es * (do_bwd ? 2 : 1), head_fwd_bwd(YN, p(0), p(G.toff[1]), c->dt, labels, B, mN, c->d, Bg, dY, c->dt, c->pooled, c->z, c->lossb, c->dz, loss,
                   G.grad, G.grad + G.toff[1], do_bwd, st, sr, c->ev_red));
   RET(release(c, gi, st));

@@ -1,11 +1,12 @@
-"""Print one step of a DHEN_PROF_TRACE dump (op, stream, start, end) as a timeline.
+"""Print one step of a DHEN_PROF_TRACE dump (op, stream, start, end) as a timeline, ops sorted by start;
+gap_us = idle time of that op's stream before it.  With DHEN_PROF_OVERLAP=1 the side stream is kept.
 Usage: timeline.py trace.csv steps"""
 import sys
 
 rows = [l.strip().split(",") for l in open(sys.argv[1]) if l.strip()]
 steps = int(sys.argv[2])
 per = len(rows) // steps
-last = rows[-per:]
+last = sorted(rows[-per:], key=lambda r: float(r[2]))
 t00 = float(last[0][2])
 busy = {}
 prev_end = {}
@@ -16,5 +17,5 @@ for op, st, t0, t1 in last:
     prev_end[st] = t1
     busy[st] = busy.get(st, 0.0) + (t1 - t0)
     print(f"{op:22s} {st:>2s} {t0:9.1f} {t1 - t0:8.1f} {gap:7.1f}")
-span = (float(last[-1][3]) - t00) * 1e3
+span = (max(float(r[3]) for r in last) - t00) * 1e3
 print(f"span {span:.1f} us; busy per stream: " + ", ".join(f"{k}: {v:.1f}" for k, v in sorted(busy.items())))
