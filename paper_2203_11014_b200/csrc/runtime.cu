@@ -71,6 +71,9 @@ struct Mod {
   float *mu1 = nullptr, *rs1 = nullptr, *mu2 = nullptr, *rs2 = nullptr;
   void* bdT = nullptr;   // bf16 [128][spt m]: blockdiag(W_u^T, ..) for the packed token projection (layer LN fused)
   void* bdg = nullptr;   // bf16 [128][128]: blockdiag(W_u, ..) for the packed DCN backward dT
+  // backward scratch of its own (not the shared tA / tC), so the module's data gradients never wait for an
+  // earlier module's side-stream weight gradients: MLP dh2 / dh1, Conv dT
+  void *dh2 = nullptr, *dh1 = nullptr, *dT = nullptr;
   bool bdT_pre = false, bdg_pre = false;   // built for this step by prebuild_bd (train_step, one launch)
   uint32_t* Fbits = nullptr;   // attention FFN ReLU bitmask [f / 32][B m] (FFN2 data gradient reads it, not F)
 };
@@ -382,7 +385,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
           tA_elems = std::max<int64_t>(tA_elems, (int64_t)B * (mi * (mi - 1) / 2));
           break;
         case DHEN_DCN: md.A = work.take(tok * es); md.T = work.take(tok * es); break;
-        case DHEN_CONV: md.T = work.take(tok * es); break;
+        case DHEN_CONV: md.T = work.take(tok * es); md.dT = work.take(tok * es); break;
         case DHEN_ATTN: {
           int H = md.s.heads, f = md.s.ffn_mult * d;
           md.QKV = work.take(tok * 3 * es);
@@ -406,6 +409,8 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
         case DHEN_MLP: {
           md.h1 = work.take((size_t)B * md.s.mlp_hidden[0] * es);
           md.h2 = work.take((size_t)B * md.s.mlp_hidden[1] * es);
+          md.dh2 = work.take((size_t)B * md.s.mlp_hidden[1] * es);
+          md.dh1 = work.take((size_t)B * md.s.mlp_hidden[0] * es);
           tC_elems = std::max<int64_t>(tC_elems, (int64_t)B * std::max(md.s.mlp_hidden[0], md.s.mlp_hidden[1]));
           tA_elems = std::max<int64_t>(tA_elems, (int64_t)B * md.s.mlp_hidden[1]);
           break;
@@ -883,24 +888,22 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
     return DHEN_OK;
   };
   // Joins are deferred: a module's side-stream work only has to finish before later st work overwrites a
-  // shared buffer it reads.  Bits: 1 tA, 2 tB, 4 tC, 8 tD, 16 bsum; everything else (attention) = all.
+  // shared buffer it reads.  Bits: 1 tA, 2 tB, 4 tC, 8 tD, 16 bsum, 32 tE, 64 tF, 128 rtmp, 256 big, 512 csum.
+  // (Conv and MLP backward scratch is per module, so they share nothing.)
   auto st_writes = [](int k) -> uint32_t {
     switch (k) {
       case DHEN_DOT: return 1u | 8u;      // dZ (tA), S (tD)
       case DHEN_DCN: return 2u | 16u;     // dA (tB), dA column sums (bsum)
-      case DHEN_CONV: return 1u;          // dT (tA)
-      case DHEN_MLP: return 1u | 4u;      // dh2 (tA), dh1 (tC)
-      case DHEN_LINEAR: return 0u;        // the dX accumulator only
+      case DHEN_ATTN: return 1u | 2u | 4u | 8u | 32u | 64u | 128u | 256u | 512u;
+      case DHEN_CONV: case DHEN_MLP: case DHEN_LINEAR: return 0u;   // own scratch / the dX accumulator
       default: return ~0u;
     }
   };
   auto side_reads = [](int k) -> uint32_t {
     switch (k) {
-      case DHEN_DOT: return 0u;           // dU and the saved Z
       case DHEN_DCN: return 2u | 16u;     // dA, its column sums
-      case DHEN_CONV: return 1u;          // dT
-      case DHEN_MLP: return 1u | 4u;      // dh2, dh1
-      case DHEN_LINEAR: return 0u;        // X and dU
+      case DHEN_ATTN: return 1u | 2u | 4u | 64u | 512u;   // dR2 (tA), dR1 (tB), dF (tC), dQKV (tF), db1 partials
+      case DHEN_DOT: case DHEN_CONV: case DHEN_MLP: case DHEN_LINEAR: return 0u;   // saved / own buffers
       default: return ~0u;
     }
   };
@@ -1030,7 +1033,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         break;
       }
       case DHEN_CONV: {  // B7
-        void* dT = c->tA;
+        void* dT = md.dT;
         RET(fork());
         RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st, sd, ws2));
         if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dT ready
@@ -1148,7 +1151,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         Gemm wm = mk(l * d, h2, B, 1, operand(dU, dt, 1, ldU), operand(md.h2, dt, 1, h2), view(gp(md.Wm), F32, h2, 1));
         wm.e.accumulate = 1;
         RET(G_(wm, c, sd, "mlp.proj_wgrad", ws2));
-        void* dh2 = c->tA;
+        void* dh2 = md.dh2;
         Gemm a = mk(B, h2, l * d, 1, operand(dU, dt, ldU, 1), operand(p(md.Wm), dt, 1, h2), view(dh2, dt, h2, 1));
         a.e.mask = view(md.h2, dt, h2, 1);
         RET(G_(a, c, st, "mlp.proj_dgrad"));
@@ -1157,7 +1160,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         w2.e.accumulate = 1;
         RET(G_(w2, c, sd, "mlp.fc2_wgrad", ws2));
         KTS(sd, "mlp.bias_grad", 0, (double)B * h2 * es, colsum_add(dh2, dt, B, h2, h2, gp(md.b2), red2, c->red_bytes, sd));
-        void* dh1 = c->tC;
+        void* dh1 = md.dh1;
         Gemm b1 = mk(B, h1, h2, 1, operand(dh2, dt, h2, 1), operand(p(md.W2), dt, 1, h1), view(dh1, dt, h1, 1));
         b1.e.mask = view(md.h1, dt, h1, 1);
         RET(G_(b1, c, st, "mlp.fc2_dgrad"));
