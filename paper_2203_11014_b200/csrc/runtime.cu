@@ -458,14 +458,17 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
 
 // ------------------------------------------------------------------ GEMM helpers
 static double vbytes(const View& v, double n) { return v.ptr ? n * (v.dt == F32 ? 4 : 2) : 0; }
-static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const char* tag, const Workspace* ws = nullptr) {
-  // algorithmic traffic: each operand read once (shared operands once), C written (and read if +=)
+// algorithmic traffic of a GEMM: each operand read once (shared operands once), C written (and read if +=)
+static double gemm_bytes(const Gemm& g) {
   const double es = g.a.dt == F32 ? 4 : 2;
   const double mn = (double)g.M * g.N * g.batch;
-  double bytes = (double)g.M * g.K * es * (g.a.bs0 || g.a.bs1 ? g.batch : 1) +
-                 (double)g.N * g.K * es * (g.b.bs0 || g.b.bs1 ? g.batch : 1) +
-                 vbytes(g.c, mn) * (g.e.accumulate || g.e.dcn_bwd ? 2 : 1) + vbytes(g.e.resid, mn) + vbytes(g.e.mask, mn) +
-                 vbytes(g.e.cross, mn) + vbytes(g.e.aux, mn);
+  return (double)g.M * g.K * es * (g.a.bs0 || g.a.bs1 ? g.batch : 1) +
+         (double)g.N * g.K * es * (g.b.bs0 || g.b.bs1 ? g.batch : 1) +
+         vbytes(g.c, mn) * (g.e.accumulate || g.e.dcn_bwd ? 2 : 1) + vbytes(g.e.resid, mn) + vbytes(g.e.mask, mn) +
+         vbytes(g.e.cross, mn) + vbytes(g.e.aux, mn);
+}
+static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const char* tag, const Workspace* ws = nullptr) {
+  const double bytes = gemm_bytes(g);
   ProfScope ps(c, tag, 2.0 * (double)g.M * g.N * g.K * g.batch, bytes, st);
   CK(gemm_run(g, ws ? *ws : (st == c->side_st ? c->ws2 : c->ws), st));   // each stream its own split-K scratch
   if (ps.rec >= 0) c->recs[ps.rec].tc = g_last_gemm_tc;
@@ -478,7 +481,7 @@ static dhen_status G_dT(Gemm& g, dhen_ctx* c, cudaStream_t st, int* rows) {
   if (g.e.bsum) {
     cudaError_t e;
     {
-      ProfScope ps(c, "dcn.dT_fused", 2.0 * (double)g.M * g.N * g.K * g.batch, 0.0, st);
+      ProfScope ps(c, "dcn.dT_fused", 2.0 * (double)g.M * g.N * g.K * g.batch, gemm_bytes(g), st);
       e = gemm_run(g, c->ws, st);
       if (ps.rec >= 0) c->recs[ps.rec].tc = g_last_gemm_tc;
     }
@@ -496,7 +499,7 @@ static dhen_status G_csum(Gemm& g, dhen_ctx* c, cudaStream_t st, const char* tag
   if (g.e.csum) {
     cudaError_t e;
     {
-      ProfScope ps(c, tag, 2.0 * (double)g.M * g.N * g.K * g.batch, 0.0, st);
+      ProfScope ps(c, tag, 2.0 * (double)g.M * g.N * g.K * g.batch, gemm_bytes(g), st);
       e = gemm_run(g, c->ws, st);
       if (ps.rec >= 0) c->recs[ps.rec].tc = g_last_gemm_tc;
     }
