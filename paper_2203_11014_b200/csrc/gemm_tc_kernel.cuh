@@ -1243,17 +1243,21 @@ __global__ void __launch_bounds__(320, 1)
             }
             if constexpr (!CF && (F & EF_ACC) == 0) {
               if (e.csum) {   // column sums of the 32 stored (bf16) rows: lane = 2 columns, read down the box
-                float s0 = 0.f, s1 = 0.f;
+                // 32 independent loads, four running pairs (rows r % 4) summed at the end: a fixed order
                 const int nr = min(32, g.M - rbase);
-#pragma unroll 4
-                for (int r = 0; r < nr; ++r) {
+                float2 sp[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+                for (int r = 0; r < 32; ++r) {
                   uint32_t w;
                   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w)
                                : "r"(box + (uint32_t)(r * 128 + ((((lane >> 2) ^ (r & 7)) & 7) << 4) + (lane & 3) * 4))
                                : "memory");
-                  s0 += __uint_as_float(w << 16);
-                  s1 += __uint_as_float(w & 0xffff0000u);
+                  if (r >= nr) w = 0u;
+                  sp[r & 3].x += __uint_as_float(w << 16);
+                  sp[r & 3].y += __uint_as_float(w & 0xffff0000u);
                 }
+                const float s0 = (sp[0].x + sp[1].x) + (sp[2].x + sp[3].x);
+                const float s1 = (sp[0].y + sp[1].y) + (sp[2].y + sp[3].y);
                 const int cg = n0 + cl0 + 2 * lane;
                 if (cg < g.N) {
                   float* cp = e.csum + ((int64_t)z * ((g.M + 31) / 32) + rbase / 32) * g.N + cg;
