@@ -1193,9 +1193,13 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
               for (int q = 0; q + CW / 32 < HC / 32; ++q) bpre[q] = bpre[q + CW / 32];
             }
+            if (alpha != 1.f) {   // (a uniform branch: the plain GEMMs skip the multiply)
+#pragma unroll
+              for (int j = 0; j < CW; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
+            }
 #pragma unroll
             for (int j = 0; j < CW; ++j) {
-              float a = __uint_as_float(v[j]) * alpha;
+              float a = __uint_as_float(v[j]);
               if constexpr ((F & EF_BIAS) != 0) a += sb[cl0 + j];
               if constexpr ((F & EF_RELU) != 0) a = fmaxf(a, 0.f);
               if constexpr ((F & EF_BMASK) != 0) a = ((mw[j >> 5] >> (j & 31)) & 1u) ? a : 0.f;
