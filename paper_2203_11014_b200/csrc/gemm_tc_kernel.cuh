@@ -1197,10 +1197,20 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
               for (int j = 0; j < CW; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
             }
+            if constexpr ((F & EF_BIAS) != 0) {   // the tile's bias row from shared memory, 16 B at a time
+              const uint32_t sba = smem_u32(sb + cl0);
+#pragma unroll
+              for (int j = 0; j < CW; j += 4) {
+                const float4 b4 = lds4(sba + (uint32_t)(j * 4));
+                v[j] = __float_as_uint(__uint_as_float(v[j]) + b4.x);
+                v[j + 1] = __float_as_uint(__uint_as_float(v[j + 1]) + b4.y);
+                v[j + 2] = __float_as_uint(__uint_as_float(v[j + 2]) + b4.z);
+                v[j + 3] = __float_as_uint(__uint_as_float(v[j + 3]) + b4.w);
+              }
+            }
 #pragma unroll
             for (int j = 0; j < CW; ++j) {
               float a = __uint_as_float(v[j]);
-              if constexpr ((F & EF_BIAS) != 0) a += sb[cl0 + j];
               if constexpr ((F & EF_RELU) != 0) a = fmaxf(a, 0.f);
               if constexpr ((F & EF_BMASK) != 0) a = ((mw[j >> 5] >> (j & 31)) & 1u) ? a : 0.f;
               v[j] = __float_as_uint(a);
