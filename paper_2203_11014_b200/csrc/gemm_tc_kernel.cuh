@@ -530,6 +530,7 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
     for (int t = 0; t < 8; ++t) bias8[t] = lean_bias(e, col + t);
   }
   const float alpha = e.alpha;
+  const bool alpha1 = alpha == 1.f;
   float dsum[(F & EF_DCNB) ? 8 : 1];   // EF_DCNB with csw: this lane's column sums of dA over its rows
 #pragma unroll
   for (int t = 0; t < ((F & EF_DCNB) ? 8 : 1); ++t) dsum[t] = 0.f;
@@ -607,14 +608,21 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
         unpack_bf8(ub[cb][k][SLM], av);
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
-          const float v = a[t] * alpha;
+          const float v = alpha1 ? a[t] : a[t] * alpha;
           da[t] = v * xv[t];
           dx[t] = v * av[t] + v;
         }
-        stg8<false>(e.aux, ok_, da);
-        if constexpr ((F & EF_DCNB) != 0) {   // the bias gradient sums dA as STORED (bf16), in row order
+        uint4 dau;   // dA as stored (bf16 pairs); the bias gradient sums exactly these values, in row order
+        dau.x = pack_bf2(da[0], da[1]); dau.y = pack_bf2(da[2], da[3]);
+        dau.z = pack_bf2(da[4], da[5]); dau.w = pack_bf2(da[6], da[7]);
+        __stwb(reinterpret_cast<uint4*>((__nv_bfloat16*)e.aux + ok_), dau);
+        if constexpr ((F & EF_DCNB) != 0) {
+          const uint32_t dw[4] = {dau.x, dau.y, dau.z, dau.w};
 #pragma unroll
-          for (int t = 0; t < 8; ++t) dsum[t] += __bfloat162float(__float2bfloat16_rn(da[t]));
+          for (int t = 0; t < 4; ++t) {
+            dsum[2 * t] += __uint_as_float(dw[t] << 16);
+            dsum[2 * t + 1] += __uint_as_float(dw[t] & 0xffff0000u);
+          }
         }
         if constexpr ((F & EF_RESID) != 0) {
           // first writer of the dX accumulator: dX = dR (identity shortcut, B3) + dT A + dT, a plain store
