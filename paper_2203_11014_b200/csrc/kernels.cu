@@ -4,6 +4,7 @@
 // reduction is a fixed-order two-pass (deterministic).
 #include "kernels.h"
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 namespace dhen {
@@ -72,7 +73,59 @@ __global__ void __launch_bounds__(256) sym_from_triu_k(const void* dZ, void* S, 
     for (int q = threadIdx.x; q < m * m; q += blockDim.x) st_from_f32(S, base + q, dt, val(q / m, q % m));
   }
 }
+// bf16, m % 8 == 0: one warp per triangle row i scatters its pairs into a dense bf16 m x (m+2) shared image,
+// both (i, j) and (j, i); the +2 pad makes the transposed column writes and the 4-byte row reads of the
+// store phase conflict-free.  Values are copied, not re-rounded, so the result equals sym_from_triu_k's.
+__global__ void __launch_bounds__(256) sym_from_triu_bf16_k(const __nv_bfloat16* __restrict__ dZ,
+                                                             __nv_bfloat16* __restrict__ S, int m, int64_t ldz, int stage) {
+  pdl_entry();
+  extern __shared__ __align__(16) unsigned char sym_raw[];
+  __nv_bfloat16* D = reinterpret_cast<__nv_bfloat16*>(sym_raw);   // [m][m + 2], then the staged triangle [h]
+  const int P = m + 2, b = blockIdx.x, lane = threadIdx.x & 31, nw = blockDim.x >> 5, h = m * (m - 1) / 2;
+  const __nv_bfloat16* z = dZ + (int64_t)b * ldz;
+  if (stage) {   // all of the triangle in flight at once (16-B loads), then scattered from shared memory
+    uint4* t = reinterpret_cast<uint4*>(D + m * P);
+    const uint4* src = reinterpret_cast<const uint4*>(z);
+    for (int q = threadIdx.x; q < h / 8; q += blockDim.x) t[q] = __ldg(src + q);
+    z = D + m * P;
+    __syncthreads();
+  }
+  for (int i = threadIdx.x >> 5; i < m; i += nw) {
+    const int rbi = i * m - i * (i + 1) / 2 - i - 1;               // rbi + j = index of pair (i, j > i)
+    if (lane == 0) D[i * P + i] = __float2bfloat16(0.f);
+    for (int j = i + 1 + lane; j < m; j += 32) {
+      const __nv_bfloat16 v = z[rbi + j];   // shared (staged) or global
+      D[i * P + j] = v;
+      D[j * P + i] = v;
+    }
+  }
+  __syncthreads();
+  const int cpr = m / 8;
+  const int64_t base = (int64_t)b * m * m;
+  for (int q = threadIdx.x; q < m * cpr; q += blockDim.x) {
+    const int i = q / cpr, j0 = (q - i * cpr) * 8;
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(D + i * P + j0);
+    *reinterpret_cast<uint4*>(S + base + (int64_t)i * m + j0) = make_uint4(r[0], r[1], r[2], r[3]);
+  }
+}
 cudaError_t sym_from_triu(const void* dZ, void* S, int dt, int B, int m, int64_t ldz, cudaStream_t st) {
+  // DHEN_SYM (A/B switch): 0 the staged-triangle kernel; 1 the dense image, triangle staged in shared memory;
+  // 2 the dense image read from global.  Default by measurement (tools/gpu_sym.sh, one B200): dense for
+  // m >= 128 (C4 1.60 -> 1.14 ms/step), staged triangle at m = 64 (C2 29.8 vs 32.0 us/step).
+  const char* e = getenv("DHEN_SYM");
+  const int mode = e ? atoi(e) : (m >= 128 ? 1 : 0);
+  const int stage = mode == 1 && (ldz % 8) == 0 && ((m * (m - 1) / 2) % 8) == 0;
+  if (mode && dt == BF16 && (m % 8) == 0 && (size_t)m * (m + 2) * 2 + (size_t)m * m <= 200 * 1024) {
+    const size_t sm = (size_t)m * (m + 2) * 2 + (stage ? (size_t)m * (m - 1) : 0);
+    static size_t attr_d = 48 * 1024;
+    if (sm > attr_d) {
+      cudaFuncSetAttribute(sym_from_triu_bf16_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr_d = sm;
+    }
+    pdl_launch(sym_from_triu_bf16_k, B, 256, sm, st, (const __nv_bfloat16*)dZ, (__nv_bfloat16*)S, m, ldz, stage);
+    ++g_launches;
+    return cudaGetLastError();
+  }
   const size_t sm = ((size_t)m * (m - 1) / 2 + m) * sizeof(float);
   if (sm > 200 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 48 * 1024;

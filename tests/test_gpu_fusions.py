@@ -9,6 +9,7 @@ DHEN_RELU_BITS    FFN ReLU derivative from a bitmask                            
 dhen_debug_gemm_pair CTA-pair GEMMs vs single-CTA tiles                       -> same sums up to split grouping
 DHEN_FUSE_DB      bias gradients from GEMM epilogue column sums (DCN db, FFN db_1) -> same values, other grouping
 DHEN_VDY          head dY formed inside the last LayerNorm backward (not stored) -> bitwise identical
+DHEN_SYM          dot backward symmetrisation through a dense shared image       -> bitwise identical
 """
 import numpy as np
 import pytest
@@ -111,4 +112,16 @@ def test_head_gradient_formed_in_ln_backward(name, B, layers, monkeypatch):
     net = _net(name, layers)
     a = _step(net, B, 16, {"DHEN_VDY": "0"}, monkeypatch)
     b = _step(net, B, 16, {"DHEN_VDY": "1"}, monkeypatch)
+    _cmp(a, b, net, 0)
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+@pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2)])
+def test_dense_symmetrisation_bitwise(name, B, layers, mode, monkeypatch):
+    """B-dot: S = sym(dZ) scattered through a dense bf16 m x (m+2) shared image (one warp per triangle row)
+    is bit-identical to the staged-triangle kernel (both copy the stored bf16 values); mode 1 stages the
+    triangle in shared memory first, mode 2 reads it from global memory."""
+    net = _net(name, layers)
+    a = _step(net, B, 17, {"DHEN_SYM": "0"}, monkeypatch)
+    b = _step(net, B, 17, {"DHEN_SYM": mode}, monkeypatch)
     _cmp(a, b, net, 0)
