@@ -1,11 +1,15 @@
 """DHEN training-step benchmark (BASELINE.json metric: train samples/s, fwd + bwd).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
 A step is one `dhen_train_step` (forward of every layer, head + BCE loss,
 backward, reduce-scatter when N > 1, SGD) over one synthetic batch of the
-config's per-GPU size.  N > 1 runs one process per GPU (torchrun), batch-sharded
-with fully sharded parameters (weak scaling: per-GPU batch fixed).
+config's per-GPU size.  Default workload: C4, the north-star 8-layer
+full-module DHEN (BASELINE configs[3]) at its per-GPU shard of 8192 samples.
+N > 1 runs one process per GPU, batch-sharded with fully sharded parameters
+(weak scaling: per-GPU batch fixed; N = 8 is configs[3]'s global 65536): under
+torchrun the ranks come from the environment, otherwise `--gpus N` re-launches
+itself through torch.distributed.run with N local ranks.
 
 value:   device time (CUDA events on the launch stream) of K steps, inputs
          resident in HBM, L2 flushed (256 MiB write) before every timed step,
@@ -96,33 +100,44 @@ class ClockSampler:
                 "source": "nvml", "reasons": sorted(self.reasons)}
 
 
-def cpu_baseline(cfg_name: str, target_s: float = 12.0):
-    """The fp64 oracle (as it stands) on a bounded sample of the workload."""
+def cpu_baseline(cfg_name: str, target_s: float = 8.0):
+    """The fp64 oracle (as it stands) on a bounded sample of the workload, with all of the host's BLAS
+    threads and again with one (1-thread and all-core samples/s)."""
     import numpy as np
     import synth
     from oracle import dhen_oracle as O
     from tests.helpers import config, make_flat_params, oracle_params
     try:
-        from threadpoolctl import threadpool_info
+        from threadpoolctl import threadpool_info, threadpool_limits
         cores = max([t.get("num_threads", 1) for t in threadpool_info()] or [1])
     except Exception:
+        threadpool_limits = None
         cores = os.cpu_count() or 1
     net = config(cfg_name)
     params = oracle_params(net, make_flat_params(net, 1))
     Bo = {"C1": 32, "C2": 16, "C3": 4, "C4": 2, "C5": 8}[cfg_name]
     X0 = synth.make_x0(1, Bo, net.m0, net.d, bf16=True).astype(np.float64)
     y = synth.make_labels(1, Bo).astype(np.float64)
-    t0 = time.perf_counter()
-    steps = 0
-    while True:
-        O.train_step(net, params, X0, y, 0.01)
-        steps += 1
-        el = time.perf_counter() - t0
-        if el >= target_s or (steps >= 1 and el * (steps + 1) / steps > 3 * target_s):
-            break
-    return {"value": steps * Bo / el, "unit": "samples/s", "cores": int(cores), "kind": "oracle",
-            "sample": f"{steps} fp64 oracle train steps of {Bo} samples of {cfg_name} "
-                      f"({el:.1f} s; cost is linear in B)", "seconds": round(el, 2)}
+
+    def timed():
+        t0 = time.perf_counter()
+        steps = 0
+        while True:
+            O.train_step(net, params, X0, y, 0.01)
+            steps += 1
+            el = time.perf_counter() - t0
+            if el >= target_s or (steps >= 1 and el * (steps + 1) / steps > 3 * target_s):
+                return steps, el
+    steps, el = timed()
+    out = {"value": steps * Bo / el, "unit": "samples/s", "cores": int(cores), "kind": "oracle",
+           "sample": f"{steps} fp64 oracle train steps of {Bo} samples of {cfg_name} "
+                     f"({el:.1f} s; cost is linear in B)", "seconds": round(el, 2)}
+    if threadpool_limits is not None and cores > 1:
+        with threadpool_limits(limits=1):
+            s1, e1 = timed()
+        out["one_thread"] = {"value": s1 * Bo / e1, "cores": 1, "seconds": round(e1, 2),
+                             "sample": f"{s1} steps of {Bo} samples, BLAS limited to 1 thread"}
+    return out
 
 
 def run_reference(args):
@@ -164,21 +179,47 @@ def run_reference(args):
     }))
 
 
+def relaunch(n: int):
+    """--gpus N without a launcher: one process per GPU through torch.distributed.run (rank 0 prints the
+    line).  NCCL_DEBUG=INFO goes to stderr so the communicator size (comm nranks) can be checked."""
+    import socket
+    import subprocess
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        raise SystemExit(f"bench.py: --gpus {n} but only {have} CUDA device(s) visible")
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd, env=env))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default="")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph (launch every kernel from the host)")
+    ap.add_argument("--watchdog", action="store_true",
+                    help="debug: run the libdhen_wd.so build (bounded mbarrier waits that report and trap)")
+    ap.add_argument("--lib", default="", help="debug: load this library build instead (A/B experiments)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}")
 
     import numpy as np
     import torch
@@ -196,6 +237,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if rank == 0 and not os.path.exists(binding.LIB_PATH):
         _build.build()
+    if args.watchdog or args.lib:
+        binding.load(args.lib or binding.WD_LIB_PATH)
     if world > 1:
         dist.barrier()
 

@@ -93,9 +93,13 @@ typedef struct {
 } dhen_config;
 
 typedef struct {
-  int rank, world;              /* world == 1: no NCCL                          */
-  unsigned char nccl_id[128];   /* ncclUniqueId from rank 0 (world > 1)         */
+  int rank, world;              /* world == 1: no collectives                   */
+  unsigned char nccl_id[128];   /* backend 0: ncclUniqueId from rank 0 (world > 1); backend 1: dhen_loopback_id() */
   int fsdp;                     /* 1: fully sharded (default); 0: replicated DP */
+  int backend;                  /* 0: NCCL (one process per GPU, the product path); 1: loopback -- `world` virtual
+                                   ranks in ONE process on one GPU, one host thread and ctx per rank, collectives
+                                   = host rendezvous + stream/event-ordered copies and fixed-order sums (a test
+                                   backend for the FSDP path on a one-GPU machine; no CUDA-graph capture) */
 } dhen_dist;
 
 /* Host-only, pure: validates a config (preconditions S:186, S:195, S:204,
@@ -114,6 +118,15 @@ dhen_status dhen_group_numel(const dhen_config* cfg, const dhen_dist* dist, int 
 
 /* Rank 0: a fresh NCCL unique id (128 bytes) to broadcast to the other ranks. */
 dhen_status dhen_nccl_id(unsigned char out[128]);
+
+/* A fresh loopback-group id (dhen_dist.backend = 1): every virtual rank of the group passes the same id. */
+dhen_status dhen_loopback_id(unsigned char out[128]);
+
+/* Bytes this rank's collectives have moved since init (ring convention: an all-gather of n elements per rank
+ * receives (world - 1) n, a reduce-scatter to n per rank sends (world - 1) n, fp32 = 4 B, bf16 = 2 B).  One
+ * FSDP training step moves (world - 1) / world x (2 x 2 B per gathered copy + 4 B) per padded parameter
+ * (DESIGN.md §10 gives the exact per-step formula).  0 when world == 1. */
+unsigned long long dhen_comm_bytes(const dhen_ctx* ctx);
 
 /* Carve state/work, initialise parameters from cfg->seed (U(+-1/sqrt(fan_in)),
  * LN gamma = 1, beta = 0), create the NCCL communicator when world > 1 (a
@@ -164,6 +177,8 @@ dhen_status dhen_grads_get(dhen_ctx* ctx, int group, float* host, void* stream);
 
 /* Per-op device timing: enable != 0 clears and starts recording a CUDA event
  * pair around every op the library launches (on the op's stream); 0 stops.
+ * enable == 1 serialises the side stream onto the layer stream (every op's time is its own);
+ * enable == 2 keeps the concurrency (the timeline of dhen_debug_profile_trace shows it).
  * Adds two event records per op: for measurement passes, not the timed step. */
 dhen_status dhen_profile(dhen_ctx* ctx, int enable);
 
@@ -179,39 +194,6 @@ typedef struct {
 /* Aggregate the recorded ops by tag (synchronises on the recorded events):
  * writes min(cap, *n) entries to out, *n = number of distinct tags. */
 dhen_status dhen_profile_read(dhen_ctx* ctx, dhen_op_stat* out, int cap, int* n);
-
-/* Test hook (tests/test_gpu_gemm.py): one strided / batched contraction
- *   C[z][i][j] (+)= sum_k A[z][i][k] B[z][k][j]
- * through the library's GEMM dispatcher.  q = int64[30]: M, N, K, batch,
- * A{s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko}, B{s_mn, s_k, bs0, bs1, zdiv, kdiv, s_ko},
- * C{rs, cs, bs0, bs1, zdiv}, accumulate, A{mdiv, s_mo}, B{mdiv, s_mo}, C{rdiv, rs_o}
- * (two-level row index r -> (r / div) * s_o + (r % div) * s; div 0 = single level).  ab_dtype/c_dtype: dhen_dtype.
- * path: 0 auto, 1 SIMT only, 2 tcgen05 only (DHEN_E_CONFIG if not expressible), 3 tcgen05 with CTA pairs
- * (cta_group::2, 256-row tiles) wherever the tile width allows, 4 tcgen05 without CTA pairs.
- * ws: fp32 device scratch for split-K partials. */
-dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* B, void* C, int ab_dtype, int c_dtype,
-                            int path, void* ws, size_t ws_bytes, void* stream);
-/* Test hook: as dhen_debug_gemm plus one fused epilogue: mode 1 ReLU-mask by E (> 0), 2 residual
- * + E, 3 DCN cross E (.) (acc + bias) + E with the pre-cross value stored to aux, 4 ReLU; E / aux are bf16
- * with C's geometry; bias (bf16, nullable) is indexed by column. */
-dhen_status dhen_debug_gemm_epi(const long long* q, const void* A, const void* B, void* C, int ab_dtype, int c_dtype,
-                                int path, void* ws, size_t ws_bytes, int mode, const void* E, const void* bias,
-                                void* aux, void* stream);
-/* 0: the last GEMM ran on the SIMT path, 1: tcgen05 (one CTA per tile), 2: tcgen05 with CTA pairs. */
-int dhen_debug_last_gemm_tc(void);
-/* Debug: device buffer (>= 448 int64) receiving clock64 timestamps of CTA 0 of every following
- * tcgen05 GEMM (producer issue, MMA start, data ready, epilogue start, epilogue end); NULL = off. */
-void dhen_debug_gemm_trace(void* dev_buf);
-
-/* Test hook: the attention core path (F4 / B6).  mode 1 (default, or env DHEN_ATTN_FUSED) = the fused
- * per-(sample, head) tcgen05 kernels where m <= 128 and d / heads is 64 or 128 (bf16); 0 = the two batched
- * GEMMs + softmax kernels everywhere.  Returns the previous mode.  Process-wide; not thread-safe. */
-int dhen_debug_attn_fused(int mode);
-
-/* Test hook: CTA-pair (cta_group::2) selection of the tcgen05 GEMMs.  mode -1 (default) = the size rule
- * (K >= 1024 and >= 64 pair items, env DHEN_PAIR / DHEN_PAIR_K), 0 = never, 1 = wherever expressible.
- * Returns the previous mode.  Process-wide; not thread-safe. */
-int dhen_debug_gemm_pair(int mode);
 
 /* Number of library kernels launched since init (a host-side counter). */
 unsigned long long dhen_launch_count(const dhen_ctx* ctx);

@@ -11,6 +11,7 @@ from typing import List, Optional, Sequence
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdhen.so")
+WD_LIB_PATH = os.path.join(HERE, "libdhen_wd.so")   # debug build: bounded mbarrier waits (build.py --watchdog)
 
 DOT, ATTN, CONV, DCN, LINEAR, MLP = range(6)
 KIND_IDS = {"dot": DOT, "attn": ATTN, "conv": CONV, "dcn": DCN, "linear": LINEAR, "mlp": MLP}
@@ -19,12 +20,14 @@ FP32, BF16 = 0, 1
 STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_SHAPE", 3: "E_ALIGN", 4: "E_STATE", 5: "E_CUDA", 6: "E_NCCL",
           7: "E_NONFINITE", 8: "E_NOMEM"}
 
-# every symbol include/dhen.h declares
-EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "dhen_init", "dhen_layer_fwd",
+# every symbol include/dhen.h and include/dhen_debug.h declare
+EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "dhen_loopback_id", "dhen_comm_bytes",
+           "dhen_init", "dhen_layer_fwd",
            "dhen_layer_bwd", "dhen_train_step", "dhen_train_step_graphed", "dhen_forward", "dhen_zero_grad", "dhen_params_io",
            "dhen_grads_get", "dhen_launch_count", "dhen_last_error", "dhen_destroy", "dhen_profile",
            "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_gemm_epi", "dhen_debug_last_gemm_tc",
-           "dhen_debug_gemm_trace", "dhen_debug_attn_fused", "dhen_debug_gemm_pair")
+           "dhen_debug_gemm_trace", "dhen_tuning_default", "dhen_set_tuning", "dhen_get_tuning",
+           "dhen_debug_profile_trace")
 
 
 class dhen_module(C.Structure):
@@ -43,12 +46,23 @@ class dhen_config(C.Structure):
 
 
 class dhen_dist(C.Structure):
-    _fields_ = [("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.c_ubyte * 128), ("fsdp", C.c_int)]
+    _fields_ = [("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.c_ubyte * 128), ("fsdp", C.c_int),
+                ("backend", C.c_int)]
+
+
+NCCL, LOOPBACK = 0, 1   # dhen_dist.backend
 
 
 class dhen_op_stat(C.Structure):
     _fields_ = [("name", C.c_char * 40), ("launches", C.c_ulonglong), ("ms", C.c_double), ("flops", C.c_double),
                 ("bytes", C.c_double), ("tc_launches", C.c_ulonglong)]
+
+
+class dhen_tuning(C.Structure):
+    """Schedule / fusion switches of one context (include/dhen_debug.h); defaults = measured best."""
+    _fields_ = [(n, C.c_int) for n in ("overlap", "defer_join", "ln_fuse", "first_writer", "relu_bits", "fuse_db",
+                                         "vdy", "trail", "bd_pre", "sym", "tstore", "pair", "pair_k", "attn_fused",
+                                         "pdl", "gemm_simt")]
 
 
 class DhenError(RuntimeError):
@@ -74,6 +88,7 @@ def load(path: str = LIB_PATH):
         "dhen_sizes": [C.POINTER(dhen_config), C.POINTER(dhen_dist), C.POINTER(sz), C.POINTER(sz)],
         "dhen_group_numel": [C.POINTER(dhen_config), C.POINTER(dhen_dist), i, C.POINTER(sz), C.POINTER(sz)],
         "dhen_nccl_id": [C.POINTER(C.c_ubyte)],
+        "dhen_loopback_id": [C.POINTER(C.c_ubyte)],
         "dhen_init": [C.POINTER(dhen_config), C.POINTER(dhen_dist), vp, sz, vp, sz, vp, C.POINTER(vp)],
         "dhen_layer_fwd": [vp, i, vp, vp, i, vp],
         "dhen_layer_bwd": [vp, i, vp, vp, i, vp],
@@ -87,23 +102,30 @@ def load(path: str = LIB_PATH):
         "dhen_profile_read": [vp, C.POINTER(dhen_op_stat), i, C.POINTER(i)],
         "dhen_debug_gemm": [C.POINTER(C.c_longlong), vp, vp, vp, i, i, i, vp, sz, vp],
         "dhen_debug_gemm_epi": [C.POINTER(C.c_longlong), vp, vp, vp, i, i, i, vp, sz, i, vp, vp, vp, vp],
+        "dhen_set_tuning": [vp, C.POINTER(dhen_tuning)],
+        "dhen_get_tuning": [vp, C.POINTER(dhen_tuning)],
+        "dhen_debug_profile_trace": [vp, C.c_char_p],
     }
     for name, args in sig.items():
-        f = getattr(lib, name)
+        f = getattr(lib, name, None)
+        if f is None:   # (an older library build loaded for an A/B experiment; test_abi checks the exports)
+            continue
         f.argtypes = args
         f.restype = C.c_int
     lib.dhen_last_error.restype = C.c_char_p
     lib.dhen_last_error.argtypes = []
     lib.dhen_launch_count.restype = C.c_ulonglong
     lib.dhen_launch_count.argtypes = [vp]
+    if hasattr(lib, "dhen_comm_bytes"):
+        lib.dhen_comm_bytes.restype = C.c_ulonglong
+        lib.dhen_comm_bytes.argtypes = [vp]
     lib.dhen_debug_gemm_trace.restype = None
     lib.dhen_debug_gemm_trace.argtypes = [vp]
     lib.dhen_debug_last_gemm_tc.restype = C.c_int
     lib.dhen_debug_last_gemm_tc.argtypes = []
-    lib.dhen_debug_attn_fused.restype = C.c_int
-    lib.dhen_debug_attn_fused.argtypes = [C.c_int]
-    lib.dhen_debug_gemm_pair.restype = C.c_int
-    lib.dhen_debug_gemm_pair.argtypes = [C.c_int]
+    if hasattr(lib, "dhen_tuning_default"):
+        lib.dhen_tuning_default.restype = None
+        lib.dhen_tuning_default.argtypes = [C.POINTER(dhen_tuning)]
     lib.dhen_destroy.restype = None
     lib.dhen_destroy.argtypes = [vp]
     _lib = lib
@@ -167,9 +189,10 @@ class Config:
         return out
 
 
-def make_dist(rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, fsdp: bool = True) -> dhen_dist:
+def make_dist(rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, fsdp: bool = True,
+              backend: int = NCCL) -> dhen_dist:
     d = dhen_dist()
-    d.rank, d.world, d.fsdp = rank, world, int(fsdp)
+    d.rank, d.world, d.fsdp, d.backend = rank, world, int(fsdp), int(backend)
     if nccl_id is not None:
         for k in range(128):
             d.nccl_id[k] = nccl_id[k]
@@ -202,6 +225,13 @@ def nccl_id() -> bytes:
     return bytes(buf)
 
 
+def loopback_id() -> bytes:
+    """A fresh id for a loopback group (backend=LOOPBACK): `world` virtual ranks in this process."""
+    buf = (C.c_ubyte * 128)()
+    _check("dhen_loopback_id", load().dhen_loopback_id(buf))
+    return bytes(buf)
+
+
 def debug_gemm(q, A, B, Cm, path=0, ws=None, stream=None):
     """Test hook: one contraction through the library's GEMM dispatcher (see dhen.h).
     Returns 0 (SIMT), 1 (tcgen05) or 2 (tcgen05 with CTA pairs); path 3 / 4 force pairs on / off."""
@@ -222,14 +252,11 @@ def debug_gemm(q, A, B, Cm, path=0, ws=None, stream=None):
     return int(load().dhen_debug_last_gemm_tc())
 
 
-def debug_gemm_pair(mode: int) -> int:
-    """Test hook: CTA-pair GEMM selection (-1 size rule, 0 never, 1 wherever expressible); returns the previous mode."""
-    return int(load().dhen_debug_gemm_pair(int(mode)))
-
-
-def debug_attn_fused(mode: int) -> int:
-    """Test hook: select the fused attention core (1) or the two-GEMM path (0); returns the previous mode."""
-    return int(load().dhen_debug_attn_fused(int(mode)))
+def tuning_default() -> dict:
+    """The default (measured-best) schedule / fusion switches as a dict."""
+    t = dhen_tuning()
+    load().dhen_tuning_default(C.byref(t))
+    return {n: getattr(t, n) for n, _ in dhen_tuning._fields_}
 
 
 def debug_gemm_epi(q, A, B, Cm, mode, E=None, bias=None, aux=None, path=0, ws=None, stream=None):
@@ -258,12 +285,12 @@ class DHEN:
     torch uint8 CUDA tensors handed to the library (which carves them)."""
 
     def __init__(self, cfg: Config, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
-                 fsdp: bool = True, stream=None):
+                 fsdp: bool = True, stream=None, backend: int = NCCL):
         import torch
         self.torch = torch
         self.cfg = cfg
         self.lib = load()
-        self.dist = make_dist(rank, world, nccl_id, fsdp)
+        self.dist = make_dist(rank, world, nccl_id, fsdp, backend)
         self._c = cfg.to_c()
         sb, wb = sizes(cfg, self.dist)
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -293,6 +320,10 @@ class DHEN:
 
     def launches(self) -> int:
         return int(self.lib.dhen_launch_count(self.ctx))
+
+    def comm_bytes(self) -> int:
+        """Bytes this rank's collectives moved since init (dhen_comm_bytes)."""
+        return int(self.lib.dhen_comm_bytes(self.ctx))
 
     def numel(self, group: int) -> int:
         return group_numel(self.cfg, group, self.dist)[0]
@@ -335,8 +366,28 @@ class DHEN:
                                                            B_global or B, float(lr), _ptr(loss), _ptr(dx0),
                                                            self._stream(stream)))
 
-    def profile(self, enable: bool):
-        _check("dhen_profile", self.lib.dhen_profile(self.ctx, int(enable)))
+    def profile(self, enable, keep_overlap: bool = False):
+        """Per-op CUDA-event timing on (serialised side stream, or concurrency kept) / off."""
+        _check("dhen_profile", self.lib.dhen_profile(self.ctx, (2 if keep_overlap else 1) if enable else 0))
+
+    def profile_trace(self, path: str):
+        """Per-op timeline (tag, stream, start, end ms) of the last profiled pass -> CSV (tools/timeline.py)."""
+        _check("dhen_debug_profile_trace", self.lib.dhen_debug_profile_trace(self.ctx, path.encode()))
+
+    def tuning(self) -> dict:
+        t = dhen_tuning()
+        _check("dhen_get_tuning", self.lib.dhen_get_tuning(self.ctx, C.byref(t)))
+        return {n: getattr(t, n) for n, _ in dhen_tuning._fields_}
+
+    def set_tuning(self, **kw):
+        """Change this context's schedule / fusion switches (dhen_debug.h dhen_tuning): set_tuning(overlap=0)."""
+        t = dhen_tuning()
+        _check("dhen_get_tuning", self.lib.dhen_get_tuning(self.ctx, C.byref(t)))
+        for k, v in kw.items():
+            if not hasattr(t, k):
+                raise KeyError(k)
+            setattr(t, k, int(v))
+        _check("dhen_set_tuning", self.lib.dhen_set_tuning(self.ctx, C.byref(t)))
 
     def profile_read(self):
         """[{name, launches, ms, flops, bytes}] aggregated per op tag."""

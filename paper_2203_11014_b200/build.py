@@ -1,9 +1,12 @@
 """Build libdhen.so in-tree with nvcc for sm_100a (no torch extension machinery).
 
-    python -m paper_2203_11014_b200.build [--force]
+    python -m paper_2203_11014_b200.build [--force] [--watchdog]
 
 Objects go to paper_2203_11014_b200/build/, the library to
 paper_2203_11014_b200/libdhen.so (git-ignored, travels to the GPU box).
+--watchdog builds the debug variant libdhen_wd.so (objects in build_wd/):
+every mbarrier wait is bounded and reports its call site before trapping
+(common.cuh); load it with binding.load(binding.WD_LIB_PATH).
 """
 from __future__ import annotations
 
@@ -18,6 +21,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libdhen.so")
+WD_LIB = os.path.join(HERE, "libdhen_wd.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -44,17 +48,20 @@ def _deps_newer(obj: str, src: str) -> bool:
         return True
     t = os.path.getmtime(obj)
     hdrs = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
-        [os.path.join(ROOT, "include", "dhen.h")]
+        glob.glob(os.path.join(ROOT, "include", "*.h"))
     return any(os.path.getmtime(p) > t for p in [src] + hdrs)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, watchdog: bool = False) -> str:
+    bdir, lib_out = (BUILD + "_wd", WD_LIB) if watchdog else (BUILD, LIB)
+    os.makedirs(bdir, exist_ok=True)
     flags, nd = _flags()
+    if watchdog:
+        flags = flags + ["-DDHEN_WATCHDOG=1"]
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     jobs = []
     for s in srcs:
-        o = os.path.join(BUILD, os.path.basename(s) + ".o")
+        o = os.path.join(bdir, os.path.basename(s) + ".o")
         if force or _deps_newer(o, s):
             jobs.append((s, o))
 
@@ -74,16 +81,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 print(f"{os.path.basename(s)}: {out}")
     if failed:
         raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
-    objs = [os.path.join(BUILD, os.path.basename(s) + ".o") for s in srcs]
-    if force or jobs or not os.path.exists(LIB):
+    objs = [os.path.join(bdir, os.path.basename(s) + ".o") for s in srcs]
+    if force or jobs or not os.path.exists(lib_out):
         lib = os.path.join(nd, "lib")
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + \
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib_out] + objs + \
             ["-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}", "-lcuda"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
-    return LIB
+    return lib_out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, watchdog="--watchdog" in sys.argv))

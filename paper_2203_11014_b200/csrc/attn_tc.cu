@@ -7,16 +7,17 @@
 // One CTA owns one (sample, head) item at a time: m <= 128 tokens, dh in {64, 128}.  Q, K, V (and dO) of
 // the item arrive by TMA (2-D maps over the [B*m][3d] / [B*m][d] activations; a tile's rows m..127 are
 // ignored), every contraction is one chain of tcgen05.mma (M = 128, K = 16 steps) into
-// TMEM, and the softmax runs on the accumulator rows straight out of TMEM (one thread = one query row,
-// no cross-thread reduction).  P (and dS) never leave the SM: they are written to shared memory in the
+// TMEM, and the softmax runs on the accumulator rows straight out of TMEM (two threads per query row,
+// one per 64-column half, exchanging row max / sum / D through shared memory).  P (and dS) never leave the SM: they are written to shared memory in the
 // 128-B-swizzled K-major layout the next MMA reads, as the A operand (P V, dS K) or, through the same
 // bytes read as an MN-major operand, as the transposed A operand (P^T dO, dS^T Q).  The backward
 // recomputes S and P from Q, K (bit-identical to the forward: same MMA chain, same softmax code) instead
 // of storing P, so per item the forward moves Q, K, V in and O out, the backward Q, K, V, dO in and
 // dQ, dK, dV out — the attention's algorithmic bytes.
 //
-// Warp roles (persistent CTAs, items strided over the grid): warp 0 = TMA producer, warp 1 = MMA issuer
-// (also owns the TMEM allocation), warps 2-5 = softmax / epilogue (warp w reads TMEM lanes 32 (w % 4) ..).
+// Warp roles (persistent CTAs, one per SM, items strided over the grid): warp 0 = TMA producer, warp 1 =
+// MMA issuer (also owns the TMEM allocation), warps 2-9 = split-row softmax / dS (warp w reads TMEM lanes
+// 32 (w % 4) ..), warps 10-13 = output group (TMEM -> bf16 -> swizzled staging -> TMA store).
 // Numerics follow the oracle's storage points: P and dS are rounded to bf16 (they are MMA
 // operands), dS carries the 1/sqrt(dh) scale, O and dQKV are stored bf16, all accumulation is fp32.
 #include <cuda.h>
@@ -26,6 +27,7 @@
 
 #include "attn.h"
 #include "gemm_tc_kernel.cuh"
+#include "tuning.h"
 
 namespace dhen {
 namespace attn {
@@ -136,616 +138,13 @@ __device__ __forceinline__ float ex2(float x) {   // 2^x, MUFU.EX2 (ex2(-inf) = 
 // gets bit-identical values:  columns >= m read as -inf;  mx = row max;  e_j = ex2(fma(S_j, k2, -mx k2))
 // with k2 = scale log2(e);  per 64-column half, two running sums over the even and odd columns in order,
 // half sum = even + odd, row sum = half 0 + half 1;  P_j = e_j * (1 / sum)  (0 for rows >= m).
-//
-// Whole row per thread (the older kernels): three passes over 32-column chunks (max; exp written back
-// to TMEM and summed; normalise and pack) keep 32 values live instead of 128.
-__device__ __forceinline__ void softmax_row(uint32_t tS, int m, bool row_ok, float scale, uint32_t* p) {
-  float v[32];
-  float mx = -INFINITY;
-#pragma unroll
-  for (int c = 0; c < ROWS / 32; ++c) {
-    tmem_ld32(tS + c * 32, v);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) mx = (c * 32 + j) < m ? fmaxf(mx, v[j]) : mx;
-  }
-  const float k2 = scale * 1.4426950408889634f;   // exp(x) = exp2(x log2 e)
-  const float off = mx * k2;
-  float se[2] = {0.f, 0.f}, so[2] = {0.f, 0.f};
-#pragma unroll
-  for (int c = 0; c < ROWS / 32; ++c) {
-    tmem_ld32(tS + c * 32, v);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float e = ex2(fmaf((c * 32 + j) < m ? v[j] : -INFINITY, k2, -off));
-      v[j] = e;
-      if (j & 1) so[c >> 1] += e; else se[c >> 1] += e;
-    }
-    tmem_st32(tS + c * 32, v);
-  }
-  const float sum = (se[0] + so[0]) + (se[1] + so[1]);
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  const float inv = row_ok ? 1.f / sum : 0.f;
-#pragma unroll
-  for (int c = 0; c < ROWS / 32; ++c) {
-    tmem_ld32(tS + c * 32, v);
-#pragma unroll
-    for (int j = 0; j < 32; j += 2) p[(c * 32 + j) / 2] = pack_bf2(v[j] * inv, v[j + 1] * inv);
-  }
-}
-// bf16 pairs of a row into the swizzled K-major tile at `base`
-__device__ __forceinline__ void store_row_tile(uint32_t base, int row, const uint32_t* p) {
-#pragma unroll
-  for (int g = 0; g < ROWS / 8; ++g)
-    sts16(swz(base, row, g >> 3, g & 7), p[4 * g], p[4 * g + 1], p[4 * g + 2], p[4 * g + 3]);
-}
-// DH accumulator columns of this thread's lane -> bf16 global row (16-B stores) if `ok`.  The TMEM loads
-// are warp-collective (.sync.aligned): every lane executes them, only the stores are predicated.
-template <int DH>
-__device__ __forceinline__ void store_acc_row(uint32_t taddr, __nv_bfloat16* dst, bool ok) {
-#pragma unroll
-  for (int c = 0; c < DH / 32; ++c) {
-    float v[32];
-    tmem_ld32(taddr + c * 32, v);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 u;
-      u.x = pack_bf2(v[8 * q], v[8 * q + 1]); u.y = pack_bf2(v[8 * q + 2], v[8 * q + 3]);
-      u.z = pack_bf2(v[8 * q + 4], v[8 * q + 5]); u.w = pack_bf2(v[8 * q + 6], v[8 * q + 7]);
-      if (ok) *reinterpret_cast<uint4*>(dst + c * 32 + q * 8) = u;
-    }
-  }
-}
 
-// ------------------------------------------------------------------ forward
-// smem: Q | K | V  (DH / 64 chunks each); P overlays Q (and K when DH = 64) once S is in TMEM.
-// TMEM (256 cols): S [0, 128), O [128, 128 + DH).
-template <int DH>
-__global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant__ CUtensorMap qkv, const __grid_constant__ Params p) {
-  pdl_release();
-  constexpr int NCH = DH / 64;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t sQ = smem_u32(smem), sK = sQ + NCH * CHUNK, sV = sK + NCH * CHUNK, sP = sQ;
-  uint64_t* bars = (uint64_t*)(smem + 3 * NCH * CHUNK);
-  const uint32_t b_qk = smem_u32(bars + 0), b_v = smem_u32(bars + 1), b_s = smem_u32(bars + 2),
-                 b_p = smem_u32(bars + 3), b_o = smem_u32(bars + 4), b_oe = smem_u32(bars + 5);
-  uint32_t* tslot = (uint32_t*)(bars + 6);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&qkv) : "memory");
-    mbar_init(b_qk, 1); mbar_init(b_v, 1); mbar_init(b_s, 1); mbar_init(b_p, 4); mbar_init(b_o, 1); mbar_init(b_oe, 4);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(256));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  const uint32_t tmem = *tslot;
-  pdl_wait();   // prerequisites complete (setup above overlapped the previous kernel's tail)
-  const int H = p.H, d = p.d;
-
-  if (warp == 0) {
-    if (lane == 0) {   // ---------------- TMA producer
-      int it = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
-        const int b = item / H, h = item - (item / H) * H;
-        if (it > 0) mbar_wait(b_o, (it - 1) & 1);   // previous item's P V done: Q, K, V, P free
-        mbar_expect_tx(b_qk, 2 * NCH * CHUNK);
-        for (int c = 0; c < NCH; ++c) {
-          tma_load2(sQ + c * CHUNK, &qkv, h * DH + 64 * c, b * p.m, b_qk);
-          tma_load2(sK + c * CHUNK, &qkv, d + h * DH + 64 * c, b * p.m, b_qk);
-        }
-        mbar_expect_tx(b_v, NCH * CHUNK);
-        for (int c = 0; c < NCH; ++c) tma_load2(sV + c * CHUNK, &qkv, 2 * d + h * DH + 64 * c, b * p.m, b_v);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {   // ---------------- MMA issuer
-      const uint32_t id_s = idesc(ROWS, false, false), id_o = idesc(DH, false, true);
-      int it = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
-        const uint32_t ph = it & 1;
-        mbar_wait(b_qk, ph);
-        tc_after();
-        mma_chain(tmem, sQ, false, sK, false, id_s, DH / 16);            // S = Q K^T
-        mma_commit(b_s);
-        mbar_wait(b_p, ph);
-        mbar_wait(b_v, ph);
-        if (it > 0) mbar_wait(b_oe, (it - 1) & 1);                          // O columns drained
-        tc_after();
-        mma_chain(tmem + ROWS, sP, false, sV, true, id_o, ROWS / 16);     // O = P V
-        mma_commit(b_o);
-      }
-    }
-  } else {             // ---------------- softmax + epilogue (warps 2..5)
-    const int q4 = warp & 3, row = q4 * 32 + lane;
-    const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
-    const bool row_ok = row < p.m;
-    int it = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
-      const int b = item / H, h = item - (item / H) * H;
-      const uint32_t ph = it & 1;
-      mbar_wait(b_s, ph);
-      tc_after();
-      uint32_t pk[ROWS / 2];
-      softmax_row(tl, p.m, row_ok, p.scale, pk);
-      store_row_tile(sP, row, pk);
-      fence_async_smem();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(b_p);
-      mbar_wait(b_o, ph);
-      tc_after();
-      store_acc_row<DH>(tl + ROWS, p.out + ((int64_t)b * p.m + row) * d + h * DH, row_ok);
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(b_oe);
-    }
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
-}
-
-// ------------------------------------------------------------------ backward
-// smem: Q | K | V | dO (DH / 64 chunks each) | P / dS (2 chunks): dS overwrites P once dV = P^T dO is done.
-// TMEM: S [0,128) -> dV [0, DH);  dP [128, 256) -> dK [128, 128 + DH);  dQ [64, 128) (DH = 64) or
-// [256, 384) (DH = 128).  Allocation 256 / 512 columns.
-template <int DH>
-__global__ void __launch_bounds__(192, DH == 64 ? 2 : 1) attn_bwd_kernel(const __grid_constant__ CUtensorMap qkv,
-                                                                     const __grid_constant__ CUtensorMap dom,
-                                                                     const __grid_constant__ Params p) {
-  pdl_release();
-  constexpr int NCH = DH / 64;
-  constexpr int TCOLS = DH == 64 ? 256 : 512;
-  constexpr uint32_t C_S = 0, C_DP = 128, C_DV = 0, C_DK = 128, C_DQ = DH == 64 ? 64 : 256;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t sQ = smem_u32(smem), sK = sQ + NCH * CHUNK, sV = sK + NCH * CHUNK, sdO = sV + NCH * CHUNK,
-                 sP = sdO + NCH * CHUNK;
-  uint64_t* bars = (uint64_t*)(smem + 4 * NCH * CHUNK + 2 * CHUNK);
-  const uint32_t b_qk = smem_u32(bars + 0), b_vdo = smem_u32(bars + 1), b_s = smem_u32(bars + 2),
-                 b_dp = smem_u32(bars + 3), b_p = smem_u32(bars + 4), b_dv = smem_u32(bars + 5),
-                 b_ds = smem_u32(bars + 6), b_dqk = smem_u32(bars + 7), b_tf = smem_u32(bars + 8);
-  uint32_t* tslot = (uint32_t*)(bars + 9);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&qkv) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&dom) : "memory");
-    mbar_init(b_qk, 1); mbar_init(b_vdo, 1); mbar_init(b_s, 1); mbar_init(b_dp, 1); mbar_init(b_p, 4);
-    mbar_init(b_dv, 1); mbar_init(b_ds, 4); mbar_init(b_dqk, 1); mbar_init(b_tf, 4);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(TCOLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  const uint32_t tmem = *tslot;
-  pdl_wait();   // prerequisites complete (setup above overlapped the previous kernel's tail)
-  const int H = p.H, d = p.d;
-
-  if (warp == 0) {
-    if (lane == 0) {   // ---------------- TMA producer: each buffer reloaded as soon as its last reader is done
-      int it = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
-        const int b = item / H, h = item - (item / H) * H;
-        const uint32_t pp = (it - 1) & 1;
-        // arm the next phase only after the previous one completed (dP(it - 1) consumed V and dO of it - 1)
-        if (it > 0) mbar_wait(b_dp, pp);     // V last read by dP
-        mbar_expect_tx(b_vdo, 2 * NCH * CHUNK);
-        for (int c = 0; c < NCH; ++c) tma_load2(sV + c * CHUNK, &qkv, 2 * d + h * DH + 64 * c, b * p.m, b_vdo);
-        if (it > 0) mbar_wait(b_dv, pp);     // dO last read by dV
-        for (int c = 0; c < NCH; ++c) tma_load2(sdO + c * CHUNK, &dom, h * DH + 64 * c, b * p.m, b_vdo);
-        if (it > 0) mbar_wait(b_dqk, pp);    // Q, K last read by dQ / dK
-        mbar_expect_tx(b_qk, 2 * NCH * CHUNK);
-        for (int c = 0; c < NCH; ++c) {
-          tma_load2(sQ + c * CHUNK, &qkv, h * DH + 64 * c, b * p.m, b_qk);
-          tma_load2(sK + c * CHUNK, &qkv, d + h * DH + 64 * c, b * p.m, b_qk);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {   // ---------------- MMA issuer
-      const uint32_t id_sq = idesc(ROWS, false, false);   // S, dP: both operands K-major
-      const uint32_t id_t = idesc(DH, true, true);         // dV = P^T dO, dK = dS^T Q
-      const uint32_t id_q = idesc(DH, false, true);        // dQ = dS K
-      int it = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
-        const uint32_t ph = it & 1;
-        if (it > 0) mbar_wait(b_tf, (it - 1) & 1);         // previous item's accumulators drained
-        mbar_wait(b_vdo, ph);
-        tc_after();
-        mma_chain(tmem + C_DP, sdO, false, sV, false, id_sq, DH / 16);   // dP = dO V^T
-        mma_commit(b_dp);
-        mbar_wait(b_qk, ph);
-        tc_after();
-        mma_chain(tmem + C_S, sQ, false, sK, false, id_sq, DH / 16);     // S = Q K^T
-        mma_commit(b_s);
-        mbar_wait(b_p, ph);
-        tc_after();
-        mma_chain(tmem + C_DV, sP, true, sdO, true, id_t, ROWS / 16);    // dV = P^T dO
-        mma_commit(b_dv);
-        mbar_wait(b_ds, ph);
-        tc_after();
-        mma_chain(tmem + C_DQ, sP, false, sK, true, id_q, ROWS / 16);    // dQ = dS K
-        mma_chain(tmem + C_DK, sP, true, sQ, true, id_t, ROWS / 16);     // dK = dS^T Q
-        mma_commit(b_dqk);
-      }
-    }
-  } else {             // ---------------- softmax recompute, dS, epilogues (warps 2..5)
-    const int q4 = warp & 3, row = q4 * 32 + lane;
-    const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
-    const bool row_ok = row < p.m;
-    const int64_t ld = 3 * (int64_t)d;
-    int it = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
-      const int b = item / H, h = item - (item / H) * H;
-      const uint32_t ph = it & 1;
-      __nv_bfloat16* orow = p.out + ((int64_t)b * p.m + row) * ld + h * DH;
-      mbar_wait(b_s, ph);
-      tc_after();
-      {
-        uint32_t pk[ROWS / 2];
-        softmax_row(tl + C_S, p.m, row_ok, p.scale, pk);
-        store_row_tile(sP, row, pk);
-      }
-      fence_async_smem();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(b_p);
-      // D = sum_j P_j dP_j (bf16 P as stored: read back from this thread's row of the tile, fp32 dP)
-      mbar_wait(b_dp, ph);
-      tc_after();
-      float D = 0.f;
-#pragma unroll
-      for (int c = 0; c < ROWS / 32; ++c) {
-        float v[32];
-        tmem_ld32(tl + C_DP + c * 32, v);
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int gg = c * 4 + g;   // 16-B granule index along the row (8 columns each)
-          const uint4 u = lds16(swz(sP, row, gg >> 3, gg & 7));
-          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            D = fmaf(__uint_as_float(w[t] << 16), v[8 * g + 2 * t], D);
-            D = fmaf(__uint_as_float(w[t] & 0xffff0000u), v[8 * g + 2 * t + 1], D);
-          }
-        }
-      }
-      // dV (rows = keys) is ready once P^T dO is done; then P's bytes may be overwritten by dS
-      mbar_wait(b_dv, ph);
-      tc_after();
-      store_acc_row<DH>(tl + C_DV, orow + 2 * d, row_ok);
-      // dS = scale * P (dP - D), bf16, over P in the same tile (each thread rewrites its own row)
-#pragma unroll
-      for (int c = 0; c < ROWS / 32; ++c) {
-        float v[32];
-        tmem_ld32(tl + C_DP + c * 32, v);
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int gg = c * 4 + g;
-          const uint32_t a = swz(sP, row, gg >> 3, gg & 7);
-          const uint4 u = lds16(a);
-          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-          uint32_t q[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            q[t] = pack_bf2(p.scale * __uint_as_float(w[t] << 16) * (v[8 * g + 2 * t] - D),
-                            p.scale * __uint_as_float(w[t] & 0xffff0000u) * (v[8 * g + 2 * t + 1] - D));
-          sts16(a, q[0], q[1], q[2], q[3]);
-        }
-      }
-      fence_async_smem();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(b_ds);
-      mbar_wait(b_dqk, ph);
-      tc_after();
-      store_acc_row<DH>(tl + C_DQ, orow, row_ok);
-      store_acc_row<DH>(tl + C_DK, orow + d, row_ok);
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(b_tf);
-    }
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
-}
-
-// ------------------------------------------------------------------ ping-pong variants (one CTA per SM)
-// Two consumer groups of four warps (warps 2-5: group 0, 6-9: group 1) take alternate items, so one group's
-// softmax / epilogue overlaps the other's, and an NS-deep ring of item stages lets the TMA producer run
-// NS items ahead.  Item it of a CTA uses stage it % NS and group it & 1; each group owns a 128-column TMEM
-// region (the output accumulators overlay S once P has left it).
+// Items of this CTA (persistent CTAs, items strided over the grid).
 __device__ __forceinline__ int cta_items(int items) {
   return (int)blockIdx.x < items ? (items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
 }
 
-// forward: stage = Q | K | V (DH / 64 chunks each), P overlays Q (and K when DH = 64).
-template <int DH, int NS>
-__global__ void __launch_bounds__(320, 1) attn_fwd_pp(const __grid_constant__ CUtensorMap qkv, const __grid_constant__ Params p) {
-  pdl_release();
-  constexpr int NCH = DH / 64, STG = 3 * NCH * CHUNK;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t sbase = smem_u32(smem);
-  uint64_t* bars = (uint64_t*)(smem + NS * STG);
-  auto B_ = [&](int i) { return smem_u32(bars + i); };
-  // [0, NS) qk_full, [NS, 2NS) v_full, [2NS, 3NS) stage free, then per group: s_full, p_full, o_full, t_free
-  const int GB = 3 * NS;
-  uint32_t* tslot = (uint32_t*)(bars + GB + 8);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&qkv) : "memory");
-    for (int i = 0; i < 3 * NS; ++i) mbar_init(B_(i), 1);
-    for (int g = 0; g < 2; ++g) {
-      mbar_init(B_(GB + 4 * g + 0), 1); mbar_init(B_(GB + 4 * g + 1), 4);
-      mbar_init(B_(GB + 4 * g + 2), 1); mbar_init(B_(GB + 4 * g + 3), 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(256));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  const uint32_t tmem = *tslot;
-  pdl_wait();   // prerequisites complete (setup above overlapped the previous kernel's tail)
-  const int H = p.H, d = p.d, n = cta_items(p.items);
-  auto sQ = [&](int s) { return sbase + (uint32_t)(s * STG); };
-  auto sK = [&](int s) { return sbase + (uint32_t)(s * STG + NCH * CHUNK); };
-  auto sV = [&](int s) { return sbase + (uint32_t)(s * STG + 2 * NCH * CHUNK); };
-  if (warp == 0) {
-    if (lane == 0) {   // ---------------- TMA producer
-      for (int it = 0; it < n; ++it) {
-        const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS;
-        if (it >= NS) mbar_wait(B_(2 * NS + s), ((it / NS) - 1) & 1);   // P V of item it - NS done
-        mbar_expect_tx(B_(s), 2 * NCH * CHUNK);
-        for (int c = 0; c < NCH; ++c) {
-          tma_load2(sQ(s) + c * CHUNK, &qkv, h * DH + 64 * c, b * p.m, B_(s));
-          tma_load2(sK(s) + c * CHUNK, &qkv, d + h * DH + 64 * c, b * p.m, B_(s));
-        }
-        mbar_expect_tx(B_(NS + s), NCH * CHUNK);
-        for (int c = 0; c < NCH; ++c) tma_load2(sV(s) + c * CHUNK, &qkv, 2 * d + h * DH + 64 * c, b * p.m, B_(NS + s));
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {   // ---------------- MMA issuer
-      const uint32_t id_s = idesc(ROWS, false, false), id_o = idesc(DH, false, true);
-      auto issueS = [&](int it) {
-        const int s = it % NS, g = it & 1;
-        if (it >= 2) mbar_wait(B_(GB + 4 * g + 3), ((it >> 1) - 1) & 1);   // group's O of item it - 2 drained
-        mbar_wait(B_(s), (it / NS) & 1);
-        tc_after();
-        mma_chain(tmem + g * 128, sQ(s), false, sK(s), false, id_s, DH / 16);   // S = Q K^T
-        mma_commit(B_(GB + 4 * g + 0));
-      };
-      if (n > 0) issueS(0);
-      for (int it = 0; it < n; ++it) {
-        if (it + 1 < n) issueS(it + 1);
-        const int s = it % NS, g = it & 1;
-        mbar_wait(B_(GB + 4 * g + 1), (it >> 1) & 1);   // P written
-        mbar_wait(B_(NS + s), (it / NS) & 1);            // V landed
-        tc_after();
-        mma_chain(tmem + g * 128, sQ(s), false, sV(s), true, id_o, ROWS / 16);   // O = P V (P overlays Q)
-        mma_commit(B_(GB + 4 * g + 2));
-        mma_commit(B_(2 * NS + s));
-      }
-    }
-  } else {             // ---------------- two softmax / epilogue groups
-    const int g = (warp - 2) >> 2, q4 = warp & 3, row = q4 * 32 + lane;
-    const uint32_t tl = tmem + (uint32_t)(g * 128) + ((uint32_t)(q4 * 32) << 16);
-    const bool row_ok = row < p.m;
-    for (int it = g; it < n; it += 2) {
-      const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS;
-      const uint32_t ph = (it >> 1) & 1;
-      mbar_wait(B_(GB + 4 * g + 0), ph);
-      tc_after();
-      {
-        uint32_t pk[ROWS / 2];
-        softmax_row(tl, p.m, row_ok, p.scale, pk);
-        store_row_tile(sQ(s), row, pk);
-      }
-      fence_async_smem();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(B_(GB + 4 * g + 1));
-      mbar_wait(B_(GB + 4 * g + 2), ph);
-      tc_after();
-      store_acc_row<DH>(tl, p.out + ((int64_t)b * p.m + row) * d + h * DH, row_ok);
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(B_(GB + 4 * g + 3));
-    }
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
-}
-
-// backward (DH = 64): stage = Q | K | V | dO | P/dS (96 KB), two stages.  TMEM per group (256 columns):
-// S [0,128) -> dV [0,64) and dQ [64,128);  dP [128,256) -> dK [128,192).
-template <int NS>
-__global__ void __launch_bounds__(320, 1) attn_bwd_pp(const __grid_constant__ CUtensorMap qkv,
-                                                      const __grid_constant__ CUtensorMap dom,
-                                                      const __grid_constant__ Params p) {
-  pdl_release();
-  constexpr int DH = 64, STG = 6 * CHUNK;
-  constexpr uint32_t C_S = 0, C_DP = 128, C_DV = 0, C_DK = 128, C_DQ = 64;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t sbase = smem_u32(smem);
-  uint64_t* bars = (uint64_t*)(smem + NS * STG);
-  auto B_ = [&](int i) { return smem_u32(bars + i); };
-  // [0,NS) qk_full, [NS,2NS) vdo_full, [2NS,3NS) stage free; per group (8 each): s, dp, p, dv, ds, dqk, tfree
-  const int GB = 3 * NS;
-  uint32_t* tslot = (uint32_t*)(bars + GB + 16);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&qkv) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&dom) : "memory");
-    for (int i = 0; i < 3 * NS; ++i) mbar_init(B_(i), 1);
-    for (int g = 0; g < 2; ++g) {
-      const int o = GB + 8 * g;
-      mbar_init(B_(o + 0), 1); mbar_init(B_(o + 1), 1); mbar_init(B_(o + 2), 4); mbar_init(B_(o + 3), 1);
-      mbar_init(B_(o + 4), 4); mbar_init(B_(o + 5), 1); mbar_init(B_(o + 6), 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  const uint32_t tmem = *tslot;
-  pdl_wait();   // prerequisites complete (setup above overlapped the previous kernel's tail)
-  const int H = p.H, d = p.d, n = cta_items(p.items);
-  auto sQ = [&](int s) { return sbase + (uint32_t)(s * STG); };
-  auto sK = [&](int s) { return sbase + (uint32_t)(s * STG + CHUNK); };
-  auto sV = [&](int s) { return sbase + (uint32_t)(s * STG + 2 * CHUNK); };
-  auto sdO = [&](int s) { return sbase + (uint32_t)(s * STG + 3 * CHUNK); };
-  auto sP = [&](int s) { return sbase + (uint32_t)(s * STG + 4 * CHUNK); };
-  if (warp == 0) {
-    if (lane == 0) {   // ---------------- TMA producer
-      for (int it = 0; it < n; ++it) {
-        const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS;
-        if (it >= NS) mbar_wait(B_(2 * NS + s), ((it / NS) - 1) & 1);   // item it - NS fully done with the stage
-        mbar_expect_tx(B_(NS + s), 2 * CHUNK);
-        tma_load2(sV(s), &qkv, 2 * d + h * DH, b * p.m, B_(NS + s));
-        tma_load2(sdO(s), &dom, h * DH, b * p.m, B_(NS + s));
-        mbar_expect_tx(B_(s), 2 * CHUNK);
-        tma_load2(sQ(s), &qkv, h * DH, b * p.m, B_(s));
-        tma_load2(sK(s), &qkv, d + h * DH, b * p.m, B_(s));
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {   // ---------------- MMA issuer
-      const uint32_t id_sq = idesc(ROWS, false, false), id_t = idesc(DH, true, true), id_q = idesc(DH, false, true);
-      auto issueF = [&](int it) {
-        const int s = it % NS, g = it & 1, o = GB + 8 * g;
-        const uint32_t tg = tmem + (uint32_t)(g * 256);
-        if (it >= 2) mbar_wait(B_(o + 6), ((it >> 1) - 1) & 1);   // group's accumulators of item it - 2 drained
-        mbar_wait(B_(NS + s), (it / NS) & 1);
-        tc_after();
-        mma_chain(tg + C_DP, sdO(s), false, sV(s), false, id_sq, DH / 16);   // dP = dO V^T
-        mma_commit(B_(o + 1));
-        mbar_wait(B_(s), (it / NS) & 1);
-        tc_after();
-        mma_chain(tg + C_S, sQ(s), false, sK(s), false, id_sq, DH / 16);     // S = Q K^T
-        mma_commit(B_(o + 0));
-      };
-      if (n > 0) issueF(0);
-      for (int it = 0; it < n; ++it) {
-        if (it + 1 < n) issueF(it + 1);
-        const int s = it % NS, g = it & 1, o = GB + 8 * g;
-        const uint32_t tg = tmem + (uint32_t)(g * 256), ph = (it >> 1) & 1;
-        mbar_wait(B_(o + 2), ph);   // P written
-        tc_after();
-        mma_chain(tg + C_DV, sP(s), true, sdO(s), true, id_t, ROWS / 16);    // dV = P^T dO
-        mma_commit(B_(o + 3));
-        mbar_wait(B_(o + 4), ph);   // dS written
-        tc_after();
-        mma_chain(tg + C_DQ, sP(s), false, sK(s), true, id_q, ROWS / 16);    // dQ = dS K
-        mma_chain(tg + C_DK, sP(s), true, sQ(s), true, id_t, ROWS / 16);     // dK = dS^T Q
-        mma_commit(B_(o + 5));
-        mma_commit(B_(2 * NS + s));
-      }
-    }
-  } else {             // ---------------- two consumer groups
-    const int g = (warp - 2) >> 2, q4 = warp & 3, row = q4 * 32 + lane, o = GB + 8 * g;
-    const uint32_t tl = tmem + (uint32_t)(g * 256) + ((uint32_t)(q4 * 32) << 16);
-    const bool row_ok = row < p.m;
-    const int64_t ld = 3 * (int64_t)d;
-    for (int it = g; it < n; it += 2) {
-      const int item = blockIdx.x + it * gridDim.x, b = item / H, h = item - b * H, s = it % NS;
-      const uint32_t ph = (it >> 1) & 1, pt = sP(s);
-      __nv_bfloat16* orow = p.out + ((int64_t)b * p.m + row) * ld + h * DH;
-      mbar_wait(B_(o + 0), ph);
-      tc_after();
-      {
-        uint32_t pk[ROWS / 2];
-        softmax_row(tl + C_S, p.m, row_ok, p.scale, pk);
-        store_row_tile(pt, row, pk);
-      }
-      fence_async_smem();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(B_(o + 2));
-      mbar_wait(B_(o + 1), ph);
-      tc_after();
-      float D = 0.f;
-#pragma unroll
-      for (int c = 0; c < ROWS / 32; ++c) {
-        float v[32];
-        tmem_ld32(tl + C_DP + c * 32, v);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int gg = c * 4 + q;
-          const uint4 u = lds16(swz(pt, row, gg >> 3, gg & 7));
-          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            D = fmaf(__uint_as_float(w[t] << 16), v[8 * q + 2 * t], D);
-            D = fmaf(__uint_as_float(w[t] & 0xffff0000u), v[8 * q + 2 * t + 1], D);
-          }
-        }
-      }
-      mbar_wait(B_(o + 3), ph);   // dV done: P may be overwritten
-      tc_after();
-      store_acc_row<DH>(tl + C_DV, orow + 2 * d, row_ok);
-#pragma unroll
-      for (int c = 0; c < ROWS / 32; ++c) {
-        float v[32];
-        tmem_ld32(tl + C_DP + c * 32, v);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int gg = c * 4 + q;
-          const uint32_t a_ = swz(pt, row, gg >> 3, gg & 7);
-          const uint4 u = lds16(a_);
-          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-          uint32_t qq[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            qq[t] = pack_bf2(p.scale * __uint_as_float(w[t] << 16) * (v[8 * q + 2 * t] - D),
-                             p.scale * __uint_as_float(w[t] & 0xffff0000u) * (v[8 * q + 2 * t + 1] - D));
-          sts16(a_, qq[0], qq[1], qq[2], qq[3]);
-        }
-      }
-      fence_async_smem();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(B_(o + 4));
-      mbar_wait(B_(o + 5), ph);
-      tc_after();
-      store_acc_row<DH>(tl + C_DQ, orow, row_ok);
-      store_acc_row<DH>(tl + C_DK, orow + d, row_ok);
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(B_(o + 6));
-    }
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
-}
-
-// ------------------------------------------------------------------ backward, dh = 128, store group
+// ------------------------------------------------------------------ backward, store group
 // One CTA per SM (224 KB of shared memory), items pipelined instead of ping-ponged (two item stages of
 // Q | K | V | dO | P would need 320 KB):
 //   smem   Q | K  x 2 stages (the next item's Q, K arrive while this one runs), V, dO, P / dS.  The outputs
@@ -1195,141 +594,66 @@ static bool map2_store(CUtensorMap* map, const void* ptr, int cols, int64_t rows
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int g_mode = -1;   // DHEN_ATTN_FUSED: 0 = off (two batched GEMMs + softmax kernels), default on
-static int g_pp = [] { const char* e = getenv("DHEN_ATTN_PP"); return e ? atoi(e) : 1; }();   // ping-pong kernels
-static int g_ws = [] { const char* e = getenv("DHEN_ATTN_WS"); return e ? atoi(e) : 1; }();   // dh = 128 backward
-int set_mode(int mode) {
-  if (g_mode < 0) { const char* e = getenv("DHEN_ATTN_FUSED"); g_mode = e ? atoi(e) : 1; }
-  const int old = g_mode;
-  g_mode = mode;
-  return old;
-}
-
 bool fused_ok(int dt, int B, int H, int m, int d) {
-  if (g_mode < 0) { const char* e = getenv("DHEN_ATTN_FUSED"); g_mode = e ? atoi(e) : 1; }
-  if (!g_mode || dt != BF16 || H <= 0 || d % H) return false;
+  if (!tune().attn_fused || dt != BF16 || H <= 0 || d % H) return false;
   const int dh = d / H;
   return (dh == 64 || dh == 128) && m >= 1 && m <= ROWS && (int64_t)B * m >= ROWS && (int64_t)B * H < (1ll << 31) &&
          (int64_t)B * m < (1ll << 31);
 }
 
-template <typename K>
-static int grid_for(K kern, int smem, int items) {
+static int sm_count() {
   static int sms = 0;
   if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
-  int per = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 192, smem) != cudaSuccess || per < 1) {
-    (void)cudaGetLastError();
-    per = 1;
-  }
-  return (int)std::min<int64_t>(items, (int64_t)sms * per);
+  return sms;
 }
 
+// Forward: warp-specialised store-group kernel, one CTA per SM, NS item stages of Q | K | V (NS = 4 / 2 for
+// dh = 64 / 128: 192 KB), split-row softmax, O through a TMA store with a box of m rows.
 cudaError_t core_fwd(const void* QKV, void* O, int B, int H, int m, int d, cudaStream_t st) {
   if (!fused_ok(BF16, B, H, m, d)) return cudaErrorNotSupported;
   const int dh = d / H;
-  CUtensorMap mq;
-  if (!map2(&mq, QKV, 3 * d, (int64_t)B * m)) return cudaErrorNotSupported;
+  CUtensorMap mq, ms;
+  if (!map2(&mq, QKV, 3 * d, (int64_t)B * m) || !map2_store(&ms, O, d, (int64_t)B * m, m)) return cudaErrorNotSupported;
   Params p;
   p.items = B * H; p.H = H; p.m = m; p.d = d; p.scale = 1.f / sqrtf((float)dh); p.out = (__nv_bfloat16*)O;
-  const int nch = dh / 64;
-  if (g_ws) {   // split-row softmax + TMA-store output group, 192 KB of item stages
-    CUtensorMap ms;
-    if (!map2_store(&ms, O, d, (int64_t)B * m, m)) return cudaErrorNotSupported;
-    const int ns = dh == 64 ? 4 : 2;
-    const int smem = (ns * 3 + 1) * nch * CHUNK + 1024 + 256 + 2 * ROWS * 4;
-    static int sms = 0;
-    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
-    const int grid = std::min(p.items, sms);
-    if (dh == 64) {
-      static bool a = false;
-      if (!a) { cudaFuncSetAttribute(attn_fwd_ws<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-      pdl_launch(attn_fwd_ws<64, 4>, grid, 448, smem, st, mq, ms, p);
-    } else {
-      static bool a = false;
-      if (!a) { cudaFuncSetAttribute(attn_fwd_ws<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-      pdl_launch(attn_fwd_ws<128, 2>, grid, 448, smem, st, mq, ms, p);
-    }
-    ++g_launches;
-    return cudaGetLastError();
-  }
-  if (g_pp) {   // ping-pong: one CTA per SM, two consumer groups, 192 KB of item stages
-    const int ns = dh == 64 ? 4 : 2;
-    const int smem = ns * 3 * nch * CHUNK + 1024 + 256;
-    static int sms = 0;
-    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
-    const int grid = std::min(p.items, sms);
-    if (dh == 64) {
-      static bool a = false;
-      if (!a) { cudaFuncSetAttribute(attn_fwd_pp<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-      pdl_launch(attn_fwd_pp<64, 4>, grid, 320, smem, st, mq, p);
-    } else {
-      static bool a = false;
-      if (!a) { cudaFuncSetAttribute(attn_fwd_pp<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-      pdl_launch(attn_fwd_pp<128, 2>, grid, 320, smem, st, mq, p);
-    }
-    ++g_launches;
-    return cudaGetLastError();
-  }
-  const int smem = 3 * nch * CHUNK + 1024 + 128;
+  const int nch = dh / 64, ns = dh == 64 ? 4 : 2;
+  const int smem = (ns * 3 + 1) * nch * CHUNK + 1024 + 256 + 2 * ROWS * 4;
+  const int grid = std::min(p.items, sm_count());
   if (dh == 64) {
     static bool a = false;
-    if (!a) { cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-    pdl_launch(attn_fwd_kernel<64>, grid_for(attn_fwd_kernel<64>, smem, p.items), 192, smem, st, mq, p);
+    if (!a) { cudaFuncSetAttribute(attn_fwd_ws<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+    pdl_launch(attn_fwd_ws<64, 4>, grid, 448, smem, st, mq, ms, p);
   } else {
     static bool a = false;
-    if (!a) { cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-    pdl_launch(attn_fwd_kernel<128>, grid_for(attn_fwd_kernel<128>, smem, p.items), 192, smem, st, mq, p);
+    if (!a) { cudaFuncSetAttribute(attn_fwd_ws<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+    pdl_launch(attn_fwd_ws<128, 2>, grid, 448, smem, st, mq, ms, p);
   }
   ++g_launches;
   return cudaGetLastError();
 }
 
+// Backward: pipelined items (Q | K double-buffered), split-row softmax recompute, outputs staged in dead input
+// bytes and stored by TMA.
 cudaError_t core_bwd(const void* QKV, const void* dO, void* dQKV, int B, int H, int m, int d, cudaStream_t st) {
   if (!fused_ok(BF16, B, H, m, d)) return cudaErrorNotSupported;
   const int dh = d / H;
-  CUtensorMap mq, mo;
-  if (!map2(&mq, QKV, 3 * d, (int64_t)B * m) || !map2(&mo, dO, d, (int64_t)B * m)) return cudaErrorNotSupported;
+  CUtensorMap mq, mo, ms;
+  if (!map2(&mq, QKV, 3 * d, (int64_t)B * m) || !map2(&mo, dO, d, (int64_t)B * m) ||
+      !map2_store(&ms, dQKV, 3 * d, (int64_t)B * m, m))
+    return cudaErrorNotSupported;
   Params p;
   p.items = B * H; p.H = H; p.m = m; p.d = d; p.scale = 1.f / sqrtf((float)dh); p.out = (__nv_bfloat16*)dQKV;
   const int nch = dh / 64;
-  if (g_ws) {   // pipelined items + split-row softmax + TMA-store output group
-    CUtensorMap ms;
-    if (!map2_store(&ms, dQKV, 3 * d, (int64_t)B * m, m)) return cudaErrorNotSupported;
-    const int smem = (6 * nch + 2) * CHUNK + 1024 + 256 + 2 * ROWS * 4;   // + row exchange
-    static int sms = 0;
-    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
-    if (dh == 64) {
-      static bool a = false;
-      if (!a) { cudaFuncSetAttribute(attn_bwd_ws<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-      pdl_launch(attn_bwd_ws<64>, std::min(p.items, sms), 448, smem, st, mq, mo, ms, p);
-    } else {
-      static bool a = false;
-      if (!a) { cudaFuncSetAttribute(attn_bwd_ws<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-      pdl_launch(attn_bwd_ws<128>, std::min(p.items, sms), 448, smem, st, mq, mo, ms, p);
-    }
-    ++g_launches;
-    return cudaGetLastError();
-  }
-  if (g_pp && dh == 64) {   // ping-pong backward (two 96-KB stages, two consumer groups)
-    const int smem = 2 * 6 * CHUNK + 1024 + 256;
-    static int sms = 0;
-    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
-    static bool a = false;
-    if (!a) { cudaFuncSetAttribute(attn_bwd_pp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-    pdl_launch(attn_bwd_pp<2>, std::min(p.items, sms), 320, smem, st, mq, mo, p);
-    ++g_launches;
-    return cudaGetLastError();
-  }
-  const int smem = 4 * nch * CHUNK + 2 * CHUNK + 1024 + 128;
+  const int smem = (6 * nch + 2) * CHUNK + 1024 + 256 + 2 * ROWS * 4;   // + row exchange
+  const int grid = std::min(p.items, sm_count());
   if (dh == 64) {
     static bool a = false;
-    if (!a) { cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-    pdl_launch(attn_bwd_kernel<64>, grid_for(attn_bwd_kernel<64>, smem, p.items), 192, smem, st, mq, mo, p);
+    if (!a) { cudaFuncSetAttribute(attn_bwd_ws<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+    pdl_launch(attn_bwd_ws<64>, grid, 448, smem, st, mq, mo, ms, p);
   } else {
     static bool a = false;
-    if (!a) { cudaFuncSetAttribute(attn_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
-    pdl_launch(attn_bwd_kernel<128>, grid_for(attn_bwd_kernel<128>, smem, p.items), 192, smem, st, mq, mo, p);
+    if (!a) { cudaFuncSetAttribute(attn_bwd_ws<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a = true; }
+    pdl_launch(attn_bwd_ws<128>, grid, 448, smem, st, mq, mo, ms, p);
   }
   ++g_launches;
   return cudaGetLastError();

@@ -4,6 +4,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <cstdio>
+
 namespace dhen {
 
 enum Dt : int { F32 = 0, BF16 = 1 };
@@ -34,6 +36,78 @@ inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// mbarrier phase waits.  Every kernel's waits go through these.  Built with -DDHEN_WATCHDOG=1 (the
+// `python -m paper_2203_11014_b200.build --watchdog` library, libdhen_wd.so) a wait that has not completed
+// after DHEN_WATCHDOG_NS of wall time prints the block, thread, barrier address, expected parity, the
+// mbarrier's raw state and the call site, then traps: a lost arrive or a phase mismatch becomes a reported
+// launch failure instead of a silent hang.  The default build spins without a bound (no extra instructions).
+#ifndef DHEN_WATCHDOG
+#define DHEN_WATCHDOG 0
+#endif
+#ifndef DHEN_WATCHDOG_NS
+#define DHEN_WATCHDOG_NS 4000000000ull
+#endif
+__device__ __forceinline__ uint32_t mbar_try_parity(uint32_t a, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  return ok;
+}
+__device__ __forceinline__ uint32_t mbar_try_parity_cluster(uint32_t a, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  return ok;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __noinline__ inline void mbar_timeout(uint32_t a, uint32_t parity, const char* file, int line) {
+  uint64_t raw;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(raw) : "r"(a) : "memory");
+  uint32_t dsm;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm));
+  printf("DHEN watchdog: %s:%d block (%d,%d) of %d thread %d: mbarrier smem+0x%x parity %u not completed; raw 0x%016llx "
+         "(dynamic smem %u)\n",
+         file, line, blockIdx.x, blockIdx.y, gridDim.x, threadIdx.x, a, parity, (unsigned long long)raw, dsm);
+  __trap();
+}
+template <bool CLUSTER>
+__device__ __forceinline__ void mbar_wait_impl(uint32_t a, uint32_t parity, const char* file, int line) {
+#if DHEN_WATCHDOG
+  if (CLUSTER ? mbar_try_parity_cluster(a, parity) : mbar_try_parity(a, parity)) return;
+  const uint64_t t0 = global_ns();
+  for (uint32_t n = 1;; ++n) {
+    if (CLUSTER ? mbar_try_parity_cluster(a, parity) : mbar_try_parity(a, parity)) return;
+    if ((n & 255u) == 0u && global_ns() - t0 > DHEN_WATCHDOG_NS) mbar_timeout(a, parity, file, line);
+  }
+#else
+  (void)file; (void)line;
+  if (CLUSTER) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAITC_%=:\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITC_%=;\n}\n" ::"r"(a),
+        "r"(parity), "r"(0x989680)
+        : "memory");
+  } else {
+    // no suspend-time hint: try_wait blocks for a hardware-defined window and the loop re-polls, so a waiter
+    // (the MMA issuer above all) resumes as soon as the phase completes
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT_%=;\n}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+  }
+#endif
 }
 
 __device__ __forceinline__ float ld_as_f32(const void* p, int64_t i, int dt) {

@@ -74,10 +74,6 @@ struct Epilogue {
   // Gram triangle (F1): element (i, j) of sample z is stored iff j > i, at C + z * c.bs0 +
   // i * triu_m - i (i + 1) / 2 + (j - i - 1)  (strict upper triangle, row-major pairs, R7)
   int triu_m = 0;
-  // several samples per tile (M = triu_spt * triu_m rows, batch item z = samples z*spt .. z*spt+spt-1, c.bs0 =
-  // spt * triu_ld): only the diagonal triu_m x triu_m blocks are stored, sample s at C + s * triu_ld
-  int triu_spt = 1;
-  int64_t triu_ld = 0;
   // LayerNorm over the output row (F5 / F6 / F12 fused, N = the whole row): v = alpha acc + bias + resid;
   // aux <- v (bf16, the saved pre-norm sum); C = gamma (v - mu) rstd + beta; mu / rstd (fp32 per row) saved
   const void* ln_gamma = nullptr;
@@ -111,10 +107,10 @@ extern unsigned long long g_launches;
 // 1 if the last gemm_run took the tcgen05 path (profiling attribution).
 extern int g_last_gemm_tc;
 extern int g_last_gemm_grid;   // CTAs of the last tcgen05 GEMM launch (rows of an Epilogue::bsum partial)
-extern int g_gemm_pair;
+extern thread_local int g_gemm_pair;
 extern int g_last_gemm_pair;
-// path override: -1 env/auto, 0 auto, 1 SIMT only, 2 tcgen05 only (test hook)
-extern int g_gemm_force;
+// path override of dhen_debug_gemm: -1 the switches, 0 auto, 1 SIMT only, 2 tcgen05 only
+extern thread_local int g_gemm_force;
 // debug: device buffer of >= 448 int64 for a clock64 trace of CTA 0 of the next tcgen05 GEMMs
 extern long long* g_gemm_trace;
 

@@ -8,13 +8,7 @@ namespace dhen {
 static __device__ __forceinline__ void epi_apply(const Gemm& g, int z, int i, int j, float acc) {
   const Epilogue& e = g.e;
   if (e.triu_m) {
-    int64_t zb = (int64_t)z * g.c.bs0;
-    if (e.triu_spt > 1) {   // diagonal blocks only: sample z * spt + i / m
-      if (i / e.triu_m != j / e.triu_m) return;
-      zb += (int64_t)(i / e.triu_m) * e.triu_ld;
-      j -= (i / e.triu_m) * e.triu_m;
-      i -= (i / e.triu_m) * e.triu_m;
-    }
+    const int64_t zb = (int64_t)z * g.c.bs0;
     if (j <= i) return;
     const int64_t o = zb + (int64_t)i * e.triu_m - (int64_t)i * (i + 1) / 2 + (j - i - 1);
     st_from_f32(g.c.ptr, o, g.c.dt, acc * e.alpha);

@@ -19,6 +19,7 @@
 #include <cstring>
 
 #include "gemm_tc_kernel.cuh"
+#include "tuning.h"
 
 namespace dhen {
 long long* g_gemm_trace = nullptr;
@@ -146,8 +147,6 @@ static bool make_lean(const Gemm& g, Lean* e) {
     e->flags |= EF_LN;
   }
   e->triu_m = x.triu_m;
-  e->triu_spt = x.triu_spt;
-  e->triu_ld = x.triu_ld;
   e->bsum = x.dcn_bwd ? x.bsum : nullptr;
   e->csum = x.csum;
   if (x.dcn_bwd) {
@@ -199,15 +198,13 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   }
   // CTA pairs (cta_group::2, 256 x BN tiles, each CTA loads BN / 2 rows of B): halves the B bytes per ring
   // slot, so the same shared memory holds a deeper ring (BN = 256: 4 slots instead of 3).  Measured
-  // (tools/gemm_bench.py, DHEN_PAIR=0/1): +7-18 % on the long-K dot.proj family (C4 945 -> 802 us, 1360
+  // (tools/gemm_bench.py, dhen_tuning.pair 0 / 1): +7-18 % on the long-K dot.proj family (C4 945 -> 802 us, 1360
   // TF/s), but slower on the short-K, store-bound shapes (the pair's epilogues run in lock step), so the
-  // default takes pairs for K >= 1024 (DHEN_PAIR_K; 512 measured slower) with at least 64 pair items
+  // default takes pairs for K >= 1024 (dhen_tuning.pair_k; 512 measured slower) with at least 64 pair items
   // (split-K items included: +13 % on the C4 attention FFN weight gradients).
   {
-    static int env_mode = -2;
-    if (env_mode == -2) { const char* ev = getenv("DHEN_PAIR"); env_mode = ev ? atoi(ev) : -1; }
-    static int pair_k = [] { const char* e = getenv("DHEN_PAIR_K"); return e ? atoi(e) : 1024; }();
-    const int mode = g_gemm_pair >= 0 ? g_gemm_pair : env_mode;
+    const int pair_k = tune().pair_k;
+    const int mode = g_gemm_pair >= 0 ? g_gemm_pair : tune().pair;
     const int64_t pitems = (int64_t)((g.M + 2 * BM - 1) / (2 * BM)) * p.tiles_n * g.batch;
     p.pair = (BN >= 128 && (splits == 1 || mode == 1 || (splits > 1 && g.M >= 2 * BM)) && mode != 0 &&
               (mode == 1 ? g.M > BM : (pitems * splits >= 64 && g.K >= pair_k))) ? 1 : 0;
@@ -222,7 +219,6 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   p.splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;   // no empty splits
   p.ws = ws.ptr;
   p.trace = g_gemm_trace;
-  { const char* e = getenv("DHEN_DBG_EPI"); p.dbg = e ? atoi(e) : 0; }
   p.zbase = 0;
   p.nz = g.batch;
   p.lanes_rows = (g.c.cs != 1 && g.c.rs == 1 && splits == 1) ? 1 : 0;
@@ -252,8 +248,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   memset(&mc, 0, sizeof mc);
   p.tstore = 0;
   {
-    static int env = -1;
-    if (env < 0) { const char* ev = getenv("DHEN_TSTORE"); env = ev ? atoi(ev) : 1; }
+    const int env = tune().tstore;
     const int es = g.c.dt == F32 ? 4 : 2;
     const int fl = p.lean ? p.ep.flags : -1;
     const bool flags_ok = fl >= 0 && (fl & ~TS_FLAGS) == 0 && (!(fl & EF_ACC) || g.c.dt == F32) && p.lean_id > 0;

@@ -53,8 +53,7 @@ struct Lean {
   int64_t rs, rs_o, bs0, bs1, cs;
   int rdiv, zdiv;
   int c_f32, flags, gap_lo, gap_hi, hi_off;
-  int triu_m, triu_spt;
-  int64_t triu_ld;
+  int triu_m;
   float alpha;
   const void* ln_gamma;
   const void* ln_beta;
@@ -91,7 +90,6 @@ struct Params {
   uint32_t idesc;
   int pair;           // 1: CTA pairs (cluster of 2) compute 256-row tiles with cta_group::2 MMAs
   long long* trace;   // debug: CTA 0 records clock64 timestamps (nullptr = off)
-  int dbg;            // debug: 1 = skip the global epilogue pass (timing experiments only)
   int tstore;         // 1: TMA-store epilogue (row-major C, flags within TS_FLAGS; fp32 += is a TMA reduce-add)
   int lnst;           // LayerNorm epilogue: 1 = Y and R leave through TMA stores (tma_o.c / tma_o.d)
   int ln_rdiv;        // 0: 3-D maps {N, M, batch}; l > 0: 4-D maps {N, l, M / l, batch} (two-level rows)
@@ -107,34 +105,8 @@ __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t cnt) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
 }
-#ifndef DHEN_MBAR_SLEEP
-#define DHEN_MBAR_SLEEP 0
-#endif
-__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
-#if DHEN_MBAR_SLEEP
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(parity), "r"(0x989680)   // suspend-time hint (ns): sleep until the phase completes instead of spinning
-      : "memory");
-#else
-  // no suspend-time hint: try_wait blocks for a hardware-defined window and the loop re-polls, so a waiter
-  // (the MMA issuer above all) resumes as soon as the phase completes
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(parity)
-      : "memory");
-#endif
-}
+// phase wait (common.cuh: unbounded spin, or the watchdog build's bounded one reporting the call site)
+#define mbar_wait(a, parity) mbar_wait_impl<false>((a), (parity), __FILE__, __LINE__)
 __device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap* map, const int c[5], uint32_t mbar) {
   asm volatile(
       "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
@@ -176,17 +148,7 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t mbar) {   // arrive on 
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t a) {   // a: shared::cluster address (possibly the peer's)
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
 }
-__device__ __forceinline__ void mbar_wait_cluster(uint32_t a, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAITC_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAITC_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(parity), "r"(0x989680)
-      : "memory");
-}
+#define mbar_wait_cluster(a, parity) mbar_wait_impl<true>((a), (parity), __FILE__, __LINE__)
 __device__ __forceinline__ void tempty_arrive(uint32_t a, bool pair) {   // accumulator drained (rank 0 counts both CTAs)
   if (pair) mbar_arrive_cluster(mapa_u32(a, 0));
   else asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
@@ -585,15 +547,8 @@ __device__ __forceinline__ void lean_pass8(const Lean& e, int z, int rbase, int 
       float a[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
       if (F & EF_TRIU) {
         // strict upper triangle of the per-sample Gram: pairs (i, j > i) row-major (R7)
-        int i = rbase + r, c0 = col;
-        int64_t zb = ok_ - col - (int64_t)i * e.rs;     // = z * bs0 (rs = 0 for this view)
-        if (e.triu_spt > 1) {                            // several samples per tile: diagonal blocks only
-          const int blk = i / e.triu_m;
-          if (col / e.triu_m != blk) continue;
-          zb += (int64_t)blk * e.triu_ld;
-          i -= blk * e.triu_m;
-          c0 -= blk * e.triu_m;
-        }
+        const int i = rbase + r, c0 = col;
+        const int64_t zb = ok_ - col - (int64_t)i * e.rs;   // = z * bs0 (rs = 0 for this view)
         const int64_t base = zb + (int64_t)i * e.triu_m - (int64_t)i * (i + 1) / 2 - i - 1;
 #pragma unroll
         for (int t = 0; t < 8; ++t)
@@ -823,7 +778,7 @@ template <int BN> struct EpiSmem {
   static constexpr int STAGE = 8 * 32 * SROW * 4;         // fp32 staging of the 8 epilogue warps
   static constexpr int TBOX = 8 * 2 * 4096;               // TMA-store boxes: 2 x (32 rows x 128 B) per warp
   static constexpr int BYTES = STAGE > TBOX ? STAGE : TBOX;
-  static constexpr int SBIAS = 2 * BN > 512 ? 2 * BN : 512;   // floats: [2][BN] bias, or the LN (s1, s2) exchange
+  static constexpr int SBIAS = 2 * BN > 512 ? 2 * BN : 512;   // floats: [2][BN] bias, or the LN (mean, M2) exchange
 };
 
 template <int BN, int STAGES, bool PAIR>
@@ -1054,7 +1009,7 @@ __global__ void __launch_bounds__(320, 1)
         // Lane = row.  ln_d == HC: a warp's column half is one whole segment; ln_d == BN: the two warps of a
         // TMEM lane quadrant (hh = 0, 1) own the two halves of the segment and exchange row partial sums through
         // shared memory (named barrier per quadrant).  Pass 1: v = alpha acc (+ bias) + resid -> TMEM, R = bf16(v)
-        // stored, sum(v) and sum(v^2) (var = E[v^2] - mu^2); pass 2: Y = gamma (v - mu) rstd + beta.  The segment's
+        // stored, mean and M2 of v (chunked, Chan-merged); pass 2: Y = gamma (v - mu) rstd + beta.  The segment's
         // statistics index is (element offset of its first column) / ln_d, relative to ln_mu / ln_rstd.
         constexpr int F = VarF<VAR>::F;
         const int row = rbase + lane;
@@ -1062,7 +1017,7 @@ __global__ void __launch_bounds__(320, 1)
         const int64_t ro = rok ? lean_row(e, z, row) : 0;
         const uint32_t tq = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC);
         const bool xch_mode = e.ln_d != HC;
-        float* xch = sbias + q4 * 128;  // [quadrant][hh][32 lanes] row partial (s1, s2) pairs (the bias scratch)
+        float* xch = sbias + q4 * 128;  // [quadrant][hh][32 lanes] row partial (mean, M2) pairs (the bias scratch)
         const int cb0 = n0 + hh * HC;                       // first column of this warp's half
         const int seg0 = xch_mode ? n0 : cb0;               // first column of the segment
         const int gofs = cb0 - seg0;                        // gamma / beta index of column cb0
@@ -1091,7 +1046,10 @@ __global__ void __launch_bounds__(320, 1)
           }
           __syncwarp();
         };
-        float s1 = 0.f, s2 = 0.f;   // sum and sum of squares of v (one pass; fp32 is ample for LN rows)
+        // Row statistics without cancellation: per 32-column chunk the mean and the sum of squared deviations
+        // from it (two passes over the chunk's registers), merged chunk by chunk with Chan's pairwise update, and
+        // across the quadrant warp pair the same way -- a large common offset |mean| >> std costs no precision.
+        float s1 = 0.f, s2 = 0.f;   // running mean and M2 (sum of squared deviations) of this thread's columns
 #pragma unroll
         for (int c = 0; c < HC; c += 32) {   // unrolled: rpre is indexed with compile-time offsets
           uint32_t v[32];
@@ -1109,15 +1067,27 @@ __global__ void __launch_bounds__(320, 1)
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           float f[32];
+          float cs_ = 0.f;
 #pragma unroll
-          for (int q = 0; q < 32; ++q) { f[q] = __uint_as_float(v[q]) * e.alpha + bv[q] + rv[q]; s1 += f[q]; s2 = fmaf(f[q], f[q], s2); }
+          for (int q = 0; q < 32; ++q) { f[q] = __uint_as_float(v[q]) * e.alpha + bv[q] + rv[q]; cs_ += f[q]; }
+          const float cm = cs_ * (1.f / 32.f);
+          float cm2 = 0.f;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) { const float t_ = f[q] - cm; cm2 = fmaf(t_, t_, cm2); }
+          if (c == 0) {
+            s1 = cm; s2 = cm2;
+          } else {   // merge (c columns: s1, s2) with (32 columns: cm, cm2)
+            const float w_ = 32.f / (float)(c + 32), dl = cm - s1;
+            s1 = fmaf(dl, w_, s1);
+            s2 += cm2 + dl * dl * ((float)c * w_);
+          }
 #pragma unroll
           for (int q = 0; q < 4; ++q) stage8(c + 8 * q, f + 8 * q);
           tmem_st32f(tq + c, f);
         }
         flush(e.aux);   // R
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        if (xch_mode) {   // [quadrant][hh][32 lanes] of (s1, s2) pairs through the bias scratch
+        if (xch_mode) {   // [quadrant][hh][32 lanes] of (mean, M2) pairs through the bias scratch
           const uint32_t xa = smem_u32(xch);
           asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(xa + (uint32_t)((hh * 32 + lane) * 8)), "f"(s1), "f"(s2)
                        : "memory");
@@ -1126,12 +1096,13 @@ __global__ void __launch_bounds__(320, 1)
           asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a1), "=f"(a2) : "r"(xa + (uint32_t)(lane * 8)) : "memory");
           asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(b1), "=f"(b2) : "r"(xa + (uint32_t)((32 + lane) * 8))
                        : "memory");
-          s1 = a1 + b1;
-          s2 = a2 + b2;
+          const float dl = b1 - a1;   // two halves of HC columns each
+          s1 = 0.5f * (a1 + b1);
+          s2 = (a2 + b2) + dl * dl * (0.5f * (float)HC);
           asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
         }
-        const float mean = s1 * inv_d;
-        const float var = fmaxf(fmaf(-mean, mean, s2 * inv_d), 0.f);
+        const float mean = s1;
+        const float var = s2 * inv_d;
         const float rs = rsqrtf(var + e.ln_eps);
         if (rok && (!xch_mode || hh == 0)) {
           const int64_t tok = (ro + seg0) / e.ln_d;
@@ -1164,7 +1135,7 @@ __global__ void __launch_bounds__(320, 1)
         continue;
       }
       if constexpr (VAR > 0 && ((VarF<VAR>::F & ~TS_FLAGS) == 0) && (!(VarF<VAR>::F & EF_ACC) || VarF<VAR>::C)) {
-        if (p.tstore && p.dbg != 1) {
+        if (p.tstore) {
           // ---- TMA-store epilogue: lane = row; a pass takes 128 B of the row (64 bf16 / 32 fp32 columns) from
           // TMEM, applies alpha / bias / ReLU, writes it into a 128-B-swizzled box (32 rows x 128 B) and one lane
           // stores the box with cp.async.bulk.tensor (fp32 +=: cp.reduce.async.bulk .add).  Two boxes per warp.
@@ -1368,8 +1339,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         __syncwarp();
         const int cbase = n0 + hh * HC + pc;
-        if (p.dbg == 1) {
-        } else if (VAR > 0) {
+        if (VAR > 0) {
           if constexpr (VAR > 0)
             lean_pass8<VarF<VAR>::F, VarF<VAR>::C, SC>(
                 e, z, rbase, g.M, g.N, cbase, stage, lane,
@@ -1420,23 +1390,9 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
                 for (int t = 0; t < 4; ++t) a[t] += t4[t];
               }
-              if (p.dbg == 2) { if (a[0] == 12345.f) stg4(e.c, o, e.c_f32, a); }
-              else stg4(e.c, o, e.c_f32, a);
+              stg4(e.c, o, e.c_f32, a);
             }
           }
-        } else if (p.dbg == 3) {
-          // debug: stores only
-          constexpr int LPR = SC / 4;
-          constexpr int RPP = 32 / LPR;
-          const int sub = lane / LPR, cl = lane % LPR;
-          const int col = cbase + 4 * cl;
-          float a[4] = {0.f, 0.f, 0.f, 0.f};
-          if (col < g.N)
-            for (int r = sub; r < 32; r += RPP) {
-              const int row = rbase + r;
-              if (row >= g.M) break;
-              stg4(e.c, (int64_t)row * e.rs + col, e.c_f32, a);
-            }
         } else {
           // generic path (split-K partials, irregular views)
           const float* stg = stage_all + (warp - 2) * 32 * SROW;

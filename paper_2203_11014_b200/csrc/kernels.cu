@@ -3,6 +3,7 @@
 // head + BCE loss, SGD.  Warp-per-row reductions via shuffles; every cross-block
 // reduction is a fixed-order two-pass (deterministic).
 #include "kernels.h"
+#include "tuning.h"
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
@@ -109,11 +110,10 @@ __global__ void __launch_bounds__(256) sym_from_triu_bf16_k(const __nv_bfloat16*
   }
 }
 cudaError_t sym_from_triu(const void* dZ, void* S, int dt, int B, int m, int64_t ldz, cudaStream_t st) {
-  // DHEN_SYM (A/B switch): 0 the staged-triangle kernel; 1 the dense image, triangle staged in shared memory;
-  // 2 the dense image read from global.  Default by measurement (tools/gpu_sym.sh, one B200): dense for
+  // dhen_tuning.sym: 0 the staged-triangle kernel; 1 the dense image, triangle staged in shared memory;
+  // 2 the dense image read from global.  Default (-1) by measurement (tools/gpu_sym.sh, one B200): dense for
   // m >= 128 (C4 1.60 -> 1.14 ms/step), staged triangle at m = 64 (C2 29.8 vs 32.0 us/step).
-  const char* e = getenv("DHEN_SYM");
-  const int mode = e ? atoi(e) : (m >= 128 ? 1 : 0);
+  const int mode = tune().sym >= 0 ? tune().sym : (m >= 128 ? 1 : 0);
   const int stage = mode == 1 && (ldz % 8) == 0 && ((m * (m - 1) / 2) % 8) == 0;
   if (mode && dt == BF16 && (m % 8) == 0 && (size_t)m * (m + 2) * 2 + (size_t)m * m <= 200 * 1024) {
     const size_t sm = (size_t)m * (m + 2) * 2 + (stage ? (size_t)m * (m - 1) : 0);
@@ -1394,12 +1394,7 @@ __device__ __forceinline__ void mbar_init1(uint32_t a, uint32_t cnt) {
 __device__ __forceinline__ void mbar_expect(uint32_t a, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait1(uint32_t a, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
+#define mbar_wait1(a, parity) mbar_wait_impl<false>((a), (parity), __FILE__, __LINE__)
 template <int MODE>
 __global__ void __launch_bounds__(512, 1) conv_db_k(const __nv_bfloat16* __restrict__ img, const __nv_bfloat16* __restrict__ other,
                                                     const __nv_bfloat16* __restrict__ Kp, int C, int B, int m, int d,

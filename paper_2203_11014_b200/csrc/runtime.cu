@@ -23,9 +23,12 @@
 #include <vector>
 
 #include "../../include/dhen.h"
+#include "../../include/dhen_debug.h"
 #include "gemm.h"
 #include "kernels.h"
 #include "attn.h"
+#include "comm.h"
+#include "tuning.h"
 
 using namespace dhen;
 
@@ -134,12 +137,7 @@ struct dhen_ctx {
   float* dXacc = nullptr;
   void* dR = nullptr;
   void* dY[2] = {nullptr, nullptr};
-  // layout experiments (env DHEN_GRAM_SPT, DHEN_TR_SMALL_M; measured slower on C2, default off): several
-  // samples per Gram tile; transposed (column-contiguous C) Gram-backward / DCN dT for m < 128
-  int gram_spt = 0, tr_small_m = 0;
-  int ln_fuse = 1;   // env DHEN_LN_FUSE: LayerNorm in the attention out-proj / FFN2 GEMM epilogues
-  int relu_bits = 1; // env DHEN_RELU_BITS: FFN ReLU mask as a bitmask (FFN1 writes it, FFN2 dgrad reads it)
-  int first_writer = 1;   // env DHEN_FIRST_WRITER: the first module's dX GEMM adds the shortcut's dR (B3)
+  dhen_tuning tune = tuning_default();   // schedule / fusion switches of this context (dhen_debug.h)
   float* big = nullptr;     // fp32 scratch [B*H*m*m] / [B*m*m] (Gram, attention S / dP)
   void* tA = nullptr;       // dtype scratch [B * m * d * 3] (dT, dQKV, ...)
   void* tB = nullptr;       // dtype scratch [B * m * d]
@@ -153,7 +151,6 @@ struct dhen_ctx {
   size_t red_bytes = 0;
   Workspace ws;
   // weight-gradient side stream (B4/B5/B7/B8/B9 wgrads overlap the same module's dgrads; joined per module)
-  int overlap = 1;                    // env DHEN_OVERLAP
   cudaStream_t side_st = nullptr;
   cudaEvent_t ev_sf = nullptr, ev_sx = nullptr, ev_sj = nullptr, ev_red = nullptr;
   Workspace ws2;                      // split-K scratch of the side stream
@@ -161,13 +158,11 @@ struct dhen_ctx {
   float* red3 = nullptr;              // layer-LN parameter partials (their final sum trails on the side stream)
   float* bsum = nullptr;              // DCN backward: per-CTA column sums of dA from the dT GEMM epilogue
   float* csum = nullptr;              // attention FFN: 32-row column sums of dF from the FFN2 dgrad epilogue
-  int trail = 1;                      // DHEN_TRAIL: parameter-sum reductions of LN / head trail on the side stream
-  int fuse_db = 1;                    // DHEN_FUSE_DB: DCN bias gradient from the dT GEMM epilogue's column sums
-  int vdy = 1;                        // DHEN_VDY: the head's dY is formed inside the last layer's LN backward
   bool vdy_now = false;               // set by train_step for the last layer's backward
   float *pooled = nullptr, *z = nullptr, *lossb = nullptr, *dz = nullptr;
+  void* headw = nullptr;    // FSDP: the gathered head weight w_h, kept for the last layer's in-LN dY (vdy)
   float* gtmp = nullptr;    // fp32 [max_npad]: all-gather target of params_io / grads_get (world > 1)
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;                // collectives (world > 1): NCCL or the in-process loopback (comm.h)
   // CUDA graph of dhen_train_step (dhen_train_step_graphed), keyed by its arguments
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap_st = nullptr;
@@ -178,21 +173,21 @@ struct dhen_ctx {
   unsigned long long graph_launches = 0;   // kernels inside the captured step
   cudaStream_t comm_st = nullptr;     // collectives (world > 1)
   cudaEvent_t ev_ag[2] = {nullptr, nullptr}, ev_use[2] = {nullptr, nullptr}, ev_grad = nullptr, ev_comm = nullptr;
+  cudaEvent_t ev_grad2 = nullptr, ev_cfork = nullptr;
+  bool graph_off = false;             // world > 1: capturing the step failed once -> eager steps from then on
   unsigned long long launches0 = 0;
   // per-op device timing (dhen_profile): event pairs on the launch stream
   struct Rec { const char* tag; int e0, e1; double flops, bytes; int tc; cudaStream_t st; };
   bool prof = false;
+  int prof_mode = 1;   // dhen_profile: 1 serialised side stream, 2 concurrency kept
   std::vector<cudaEvent_t> events;
   int next_event = 0;
   std::vector<Rec> recs;
 };
 
-// The profiled pass runs serialised (every op's event-timed duration is its own) unless DHEN_PROF_OVERLAP=1
-// keeps the side stream (the DHEN_PROF_TRACE timeline then shows the real concurrency).
-static bool serial_prof(const dhen_ctx* c) {
-  static int keep = [] { const char* e = getenv("DHEN_PROF_OVERLAP"); return e ? atoi(e) : 0; }();
-  return c->prof && !keep;
-}
+// The profiled pass runs serialised (every op's event-timed duration is its own) unless dhen_profile(ctx, 2)
+// keeps the side stream (the dhen_debug_profile_trace timeline then shows the real concurrency).
+static bool serial_prof(const dhen_ctx* c) { return c->prof && c->prof_mode != 2; }
 // RAII scope recording a CUDA event pair around one op when profiling is on.
 // Per-op scope: an NVTX range named after the op (so `ncu --nvtx --nvtx-include "<op>/"` captures exactly that
 // op's kernels; a no-op without an attached tool) and, in profiling mode, CUDA events around the op.
@@ -453,18 +448,22 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   c->z = (float*)work.take((size_t)B * 4);
   c->lossb = (float*)work.take((size_t)B * 4);
   c->dz = (float*)work.take((size_t)B * 4);
+  c->headw = work.take((size_t)d * es);
   (void)f_max;
 }
 
 // ------------------------------------------------------------------ GEMM helpers
 static double vbytes(const View& v, double n) { return v.ptr ? n * (v.dt == F32 ? 4 : 2) : 0; }
-// algorithmic traffic of a GEMM: each operand read once (shared operands once), C written (and read if +=)
+// Algorithmic traffic of a GEMM: each operand read once (shared operands once), C written, and C read only
+// when it is really read: `+=` (accumulate), or the DCN backward's red.global.add into the fp32 dX accumulator
+// (dcn_bwd without a residual; with one, the epilogue is dX's first writer and only stores C).
 static double gemm_bytes(const Gemm& g) {
   const double es = g.a.dt == F32 ? 4 : 2;
   const double mn = (double)g.M * g.N * g.batch;
+  const bool c_read = g.e.accumulate || (g.e.dcn_bwd && !g.e.resid.ptr);
   return (double)g.M * g.K * es * (g.a.bs0 || g.a.bs1 ? g.batch : 1) +
          (double)g.N * g.K * es * (g.b.bs0 || g.b.bs1 ? g.batch : 1) +
-         vbytes(g.c, mn) * (g.e.accumulate || g.e.dcn_bwd ? 2 : 1) + vbytes(g.e.resid, mn) + vbytes(g.e.mask, mn) +
+         vbytes(g.c, mn) * (c_read ? 2 : 1) + vbytes(g.e.resid, mn) + vbytes(g.e.mask, mn) +
          vbytes(g.e.cross, mn) + vbytes(g.e.aux, mn);
 }
 static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const char* tag, const Workspace* ws = nullptr) {
@@ -476,12 +475,14 @@ static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const 
 }
 // The DCN backward dT GEMM with the fused dA column sums (Epilogue::bsum) when its tcgen05 pass can take
 // them; otherwise the same GEMM without (and *rows = 0: the caller sums dA with colsum_add instead).
-static dhen_status G_dT(Gemm& g, dhen_ctx* c, cudaStream_t st, int* rows) {
+// `overlap` = bytes of an operand that lie inside another counted view (the dU slice of the dR residual:
+// read once), subtracted from the algorithmic bytes.
+static dhen_status G_dT(Gemm& g, dhen_ctx* c, cudaStream_t st, int* rows, double overlap) {
   *rows = 0;
   if (g.e.bsum) {
     cudaError_t e;
     {
-      ProfScope ps(c, "dcn.dT_fused", 2.0 * (double)g.M * g.N * g.K * g.batch, gemm_bytes(g), st);
+      ProfScope ps(c, "dcn.dT_fused", 2.0 * (double)g.M * g.N * g.K * g.batch, gemm_bytes(g) - overlap, st);
       e = gemm_run(g, c->ws, st);
       if (ps.rec >= 0) c->recs[ps.rec].tc = g_last_gemm_tc;
     }
@@ -490,7 +491,10 @@ static dhen_status G_dT(Gemm& g, dhen_ctx* c, cudaStream_t st, int* rows) {
     (void)cudaGetLastError();
     g.e.bsum = nullptr;
   }
-  return G_(g, c, st, "dcn.dT_fused");
+  ProfScope ps(c, "dcn.dT_fused", 2.0 * (double)g.M * g.N * g.K * g.batch, gemm_bytes(g) - overlap, st);
+  CK(gemm_run(g, c->ws, st));
+  if (ps.rec >= 0) c->recs[ps.rec].tc = g_last_gemm_tc;
+  return DHEN_OK;
 }
 // A GEMM with fused column sums of its stored output (Epilogue::csum) when its TMA-store pass can take
 // them; otherwise the same GEMM without (*ok = false: the caller sums the output itself).
@@ -570,8 +574,8 @@ static dhen_status prefetch(dhen_ctx* c, int gi) {
   if (c->gathered_owner[slot] == gi) return DHEN_OK;
   Group& g = c->G[gi];
   CK(cudaStreamWaitEvent(c->comm_st, c->ev_use[slot], 0));
-  NK(ncclAllGather(g.comp, c->gathered[slot], (size_t)g.shard, c->dt == F32 ? ncclFloat32 : ncclBfloat16, c->comm,
-                   c->comm_st));
+  if (c->comm->all_gather(g.comp, c->gathered[slot], (size_t)g.shard, c->dt, c->comm_st))
+    return fail(DHEN_E_NCCL, "all-gather of group %d (%s): %s", gi, c->comm->name(), c->comm->err.c_str());
   CK(cudaEventRecord(c->ev_ag[slot], c->comm_st));
   c->gathered_owner[slot] = gi;
   return DHEN_OK;
@@ -598,16 +602,19 @@ static dhen_status fence_params(dhen_ctx* c, cudaStream_t st) {
   return DHEN_OK;
 }
 
-static dhen_status reduce_grads(dhen_ctx* c, int gi, cudaStream_t st) {
+// (`also`: a second stream whose pending work also produces this group's gradients, e.g. trailing head sums)
+static dhen_status reduce_grads(dhen_ctx* c, int gi, cudaStream_t st, cudaStream_t also = nullptr) {
   if (c->dist.world == 1) return DHEN_OK;
   Group& g = c->G[gi];
   CK(cudaEventRecord(c->ev_grad, st));
   CK(cudaStreamWaitEvent(c->comm_st, c->ev_grad, 0));
-  if (c->dist.fsdp) {
-    NK(ncclReduceScatter(g.grad, g.gshard, (size_t)g.shard, ncclFloat32, ncclSum, c->comm, c->comm_st));
-  } else {
-    NK(ncclAllReduce(g.grad, g.gshard, (size_t)g.shard, ncclFloat32, ncclSum, c->comm, c->comm_st));
+  if (also && also != st) {
+    CK(cudaEventRecord(c->ev_grad2, also));
+    CK(cudaStreamWaitEvent(c->comm_st, c->ev_grad2, 0));
   }
+  const int r = c->dist.fsdp ? c->comm->reduce_scatter(g.grad, g.gshard, (size_t)g.shard, c->comm_st)
+                             : c->comm->all_reduce(g.grad, g.gshard, (size_t)g.shard, c->comm_st);
+  if (r) return fail(DHEN_E_NCCL, "gradient reduction of group %d (%s): %s", gi, c->comm->name(), c->comm->err.c_str());
   return DHEN_OK;
 }
 // the compute stream waits for every collective issued so far
@@ -622,7 +629,7 @@ static dhen_status join_comm(dhen_ctx* c, cudaStream_t st) {
 static bool layer_lnf(const dhen_ctx* c, int n, int B) {
   const Layer& Lr = c->L[n];
   const int d = c->d, mi = Lr.m_in, mo = Lr.m_out;
-  bool lnf = c->ln_fuse && c->dt == BF16 && Lr.Wn < 0 && mi == mo && (d == 128 || d == 256);
+  bool lnf = c->tune.ln_fuse && c->dt == BF16 && Lr.Wn < 0 && mi == mo && (d == 128 || d == 256);
   for (const Mod& m_ : Lr.mods) {
     if (!lnf) break;
     const int l_ = m_.s.l;
@@ -638,7 +645,7 @@ static bool layer_lnf(const dhen_ctx* c, int n, int B) {
 // Whether the DCN backward's token-map dgrad packs 128 / m samples per tile (block-diagonal W_u).
 static bool dcn_pack(const dhen_ctx* c, int mi, int l, int B) {
   const int spt = 128 / std::max(mi, 1);
-  return !c->tr_small_m && c->dt == BF16 && mi <= 64 && 128 % mi == 0 && l <= 64 && 64 % l == 0 &&
+  return c->dt == BF16 && mi <= 64 && 128 % mi == 0 && l <= 64 && 64 % l == 0 &&
          (spt * l) % 64 == 0 && B % spt == 0;
 }
 
@@ -663,7 +670,7 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
   // form U[(b, t)] = blockdiag(W_u^T, ..) x [T_b; T_b+1; ..] (rows = tokens of 128 / l samples per tile).
   const bool lnf = layer_lnf(c, n, B);
   const cudaStream_t st0 = st;
-  const bool use_side = c->overlap && !serial_prof(c) && Lr.mods.size() > 1;
+  const bool use_side = c->tune.overlap && !serial_prof(c) && Lr.mods.size() > 1;
   bool has_attn = false;
   for (const Mod& m_ : Lr.mods) has_attn |= m_.s.kind == DHEN_ATTN;
   if (use_side) { CK(cudaEventRecord(c->ev_sf, st0)); CK(cudaStreamWaitEvent(c->side_st, c->ev_sf, 0)); }
@@ -699,15 +706,10 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
     switch (md.s.kind) {
       case DHEN_DOT: {   // F1 + F2
         const int h = mi * (mi - 1) / 2;
-        // Gram X X^T per sample; the epilogue writes the strict upper triangle Z directly (F1, R7).  For
-        // m <= 64 (dividing 128) spt = 128 / m samples share one 128-row tile: the tile is the Gram of the
-        // stacked samples and only its diagonal blocks are stored (full MMA rows, one tile per spt samples).
-        const int spt = (c->gram_spt && dt == BF16 && mi <= 64 && 128 % mi == 0 && B % (128 / mi) == 0) ? 128 / mi : 1;
-        Gemm g = mk(spt * mi, spt * mi, d, B / spt, operand(X, dt, d, 1, (int64_t)spt * mi * d),
-                    operand(X, dt, d, 1, (int64_t)spt * mi * d), view(md.Z, dt, 0, 1, (int64_t)spt * h));
+        // Gram X X^T per sample; the epilogue writes the strict upper triangle Z directly (F1, R7)
+        Gemm g = mk(mi, mi, d, B, operand(X, dt, d, 1, (int64_t)mi * d), operand(X, dt, d, 1, (int64_t)mi * d),
+                    view(md.Z, dt, 0, 1, (int64_t)h));
         g.e.triu_m = mi;
-        g.e.triu_spt = spt;
-        g.e.triu_ld = h;
         RET(G_(g, c, st, "dot.gram"));
         if (lnf) {   // F2 + F12: the projection's rows are samples, its columns l tokens x d (LN per d segment)
           Gemm v = mk(B, l * d, h, 1, operand(md.Z, dt, h, 1), operand(p(md.Wm), dt, h, 1), view(Yo, dt, so, 1));
@@ -765,7 +767,7 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         }
         // F5: Z1 = LN1(X + O W_o^T + b_o) -- with whole rows per tile (bf16, d = 128 / 256) the LayerNorm runs
         // in the GEMM epilogue (R1 and the row statistics saved for B6), else GEMM into fp32 + LN kernel
-        const bool ln_fused = c->ln_fuse && dt == BF16 && (d == 128 || d == 256);
+        const bool ln_fused = c->tune.ln_fuse && dt == BF16 && (d == 128 || d == 256);
         if (ln_fused) {
           Gemm r1 = mk((int)rows, d, d, 1, operand(md.O, dt, d, 1), operand(p(md.Wo), dt, d, 1), view(md.Z1, dt, d, 1));
           r1.e.bias = p(md.bo); r1.e.bias_dt = dt; r1.e.resid = view((void*)X, dt, d, 1);
@@ -781,7 +783,8 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         }
         Gemm f1 = mk((int)rows, f, d, 1, operand(md.Z1, dt, d, 1), operand(p(md.W1), dt, d, 1), view(md.F, dt, f, 1));
         f1.e.bias = p(md.b1); f1.e.bias_dt = dt; f1.e.relu = 1;
-        const bool fbits = c->relu_bits && dt == BF16 && f % 64 == 0 && f >= 128;
+        // (the bitmask is written / read by the TMA-store epilogue only)
+        const bool fbits = c->tune.relu_bits && c->tune.tstore && dt == BF16 && f % 64 == 0 && f >= 128;
         if (fbits) { f1.e.bits = md.Fbits; f1.e.bits_mode = 1; f1.e.bits_ld = rows; }
         RET(G_(f1, c, st, "attn.ffn1"));
         // F6: T = LN2(Z1 + F W_2^T + b_2), fused the same way
@@ -865,22 +868,22 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
       const int rk = rank_of[Lr.mods[i].s.kind];
       if (rk < best_rank) { best_rank = rk; best = i; }
     }
-    if (best >= 0 && c->first_writer) order.push_back(&Lr.mods[best]);
+    if (best >= 0 && c->tune.first_writer) order.push_back(&Lr.mods[best]);
     for (int i = 0; i < (int)Lr.mods.size(); ++i)
-      if (!(c->first_writer && i == best)) order.push_back(&Lr.mods[i]);
+      if (!(c->tune.first_writer && i == best)) order.push_back(&Lr.mods[i]);
   }
   const int first_kind = order.empty() ? -1 : order[0]->s.kind;
-  const bool first_dR = c->first_writer && Lr.Wn < 0 && mi == mo &&
+  const bool first_dR = c->tune.first_writer && Lr.Wn < 0 && mi == mo &&
                         (first_kind == DHEN_DOT || first_kind == DHEN_DCN || first_kind == DHEN_LINEAR || first_kind == DHEN_MLP);
   // Weight gradients of a module run on the side stream `sd` (own split-K / reduction scratch) while its
   // data gradients run on `st`; `fork` hands the side stream everything enqueued on st so far, and st waits
   // for the side stream before it overwrites a shared buffer that pending side work reads (and at layer end).
   // (the profiled pass runs serialised so every op's event-timed duration is its own)
-  cudaStream_t sd = (c->overlap && !serial_prof(c)) ? c->side_st : st;
+  cudaStream_t sd = (c->tune.overlap && !serial_prof(c)) ? c->side_st : st;
   // the LN parameter sums trail on sd (own scratch red3; the modules' joins below order its reuse)
   KT("layer.ln_bwd", 0, (double)B * mo * d * (3 * es + (first_dR ? 0 : 4)), ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc, (Lr.Wn >= 0 || first_dR) ? 0 : 1,
-            gp(Lr.gamma), gp(Lr.beta), c->red3, c->red_bytes, st, c->trail ? sd : st, c->ev_red,
-            c->vdy_now ? c->dz : nullptr, c->vdy_now ? c->G[c->cfg.n_layers].comp : nullptr, mo));
+            gp(Lr.gamma), gp(Lr.beta), c->red3, c->red_bytes, st, c->tune.trail ? sd : st, c->ev_red,
+            c->vdy_now ? c->dz : nullptr, c->vdy_now ? (sharded(c) ? c->headw : c->G[c->cfg.n_layers].comp) : nullptr, mo));
   c->vdy_now = false;
   if (Lr.Wn >= 0)   // B3: dX = W_n dR ; dW_n += sum_b X_b dR_b^T
     RET(tokmix_bwd(c, X, mi, p(Lr.Wn), mo, c->dR, ldU, acc, F32, 0, gp(Lr.Wn), B, st));
@@ -917,15 +920,14 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
     side_pending = 0;
     return DHEN_OK;
   };
-  static int defer = [] { const char* e = getenv("DHEN_DEFER_JOIN"); return e ? atoi(e) : 1; }();
   auto join = [&]() -> dhen_status {   // end of a module: record what its side work still reads
     side_pending |= side_reads(cur_kind);
-    return defer ? DHEN_OK : real_join();
+    return c->tune.defer_join ? DHEN_OK : real_join();
   };
   // The last module's last dX-writing GEMM emits dX (layer dtype) = accumulator + its contribution: the fp32
   // accumulator is read once and never written back, and no cast kernel runs.
   const int last_kind = order.empty() ? -1 : order.back()->s.kind;
-  const bool last_dX = dX && c->first_writer &&
+  const bool last_dX = dX && c->tune.first_writer &&
                        (last_kind == DHEN_DOT || last_kind == DHEN_DCN || last_kind == DHEN_LINEAR || last_kind == DHEN_MLP);
   bool first_mod = true;
   for (Mod* mdp : order) {
@@ -947,13 +949,9 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         Gemm gz = mk(B, h, l * d, 1, operand(dU, dt, ldU, 1), operand(p(md.Wm), dt, 1, h), view(c->tA, dt, h, 1));
         RET(G_(gz, c, st, "dot.proj_dgrad"));
         KT("dot.sym", 0, (double)B * (h + mi * mi) * es, sym_from_triu(c->tA, c->tD, dt, B, mi, h, st));
-        // dX_b += S_b X_b.  m < 128: as its transpose dX_b^T += X_b^T S_b (M = d rows fill the 128-row MMA
-        // tile; S symmetric, K-major), C column-contiguous
-        Gemm gx = c->tr_small_m && mi < 128 && dt == BF16
-                      ? mk(d, mi, mi, B, operand(X, dt, 1, d, (int64_t)mi * d), operand(c->tD, dt, mi, 1, (int64_t)mi * mi),
-                           view(acc, F32, 1, d, (int64_t)mi * d))
-                      : mk(mi, d, mi, B, operand(c->tD, dt, mi, 1, (int64_t)mi * mi), operand(X, dt, 1, d, (int64_t)mi * d),
-                           view(acc, F32, d, 1, (int64_t)mi * d));
+        // dX_b += S_b X_b
+        Gemm gx = mk(mi, d, mi, B, operand(c->tD, dt, mi, 1, (int64_t)mi * mi), operand(X, dt, 1, d, (int64_t)mi * d),
+                     view(acc, F32, d, 1, (int64_t)mi * d));
         gx.e.accumulate = 1;
         if (take_dR) { gx.e.accumulate = 0; gx.e.resid = gx.c; gx.e.resid.ptr = c->dR; gx.e.resid.dt = dt; }
         if (emit_dX) {   // dX = (dR | acc) + S X
@@ -990,8 +988,9 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         const int spt = 128 / std::max(mi, 1);
         const bool pack = dcn_pack(c, mi, l, B);
         // the bias gradient's column sums of dA come out of the dT GEMM's epilogue (one partial row per CTA)
-        const bool fuse_db = c->fuse_db && dt == BF16 && d <= 256;
+        const bool fuse_db = c->tune.fuse_db && dt == BF16 && d <= 256;
         int bsum_rows = 0;
+        const double dU_in_dR = take_dR ? (double)B * l * d * es : 0.0;   // dU is a slice of the dR residual
         if (pack) {
           void* bdg = md.bdg_pre ? md.bdg : c->bdiag;
           if (!md.bdg_pre) KT("dcn.bdiag", 0, 2.0 * 128 * 128 * es, blockdiag(p(md.Wu), mi, l, spt, bdg, st));
@@ -1003,22 +1002,17 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
           gt.e.aux = view(dA, dt, d, 1, (int64_t)spt * mi * d);
           if (take_dR) gt.e.resid = view(c->dR, dt, d, 1, (int64_t)spt * mi * d);
           if (fuse_db) gt.e.bsum = c->bsum;
-          RET(G_dT(gt, c, st, &bsum_rows));
+            RET(G_dT(gt, c, st, &bsum_rows, dU_in_dR));
         } else {
-        // m < 128: as its transpose dT_b^T = dU_b^T W_u^T (M = d rows fill the MMA tile), C column-contiguous
-        const bool tr = c->tr_small_m && mi < 128 && dt == BF16;
-        Gemm gt = tr ? mk(d, mi, l, B, operand(dU, dt, 1, d, ldU), operand(p(md.Wu), dt, l, 1),
-                          view(acc, F32, 1, d, (int64_t)mi * d))
-                     : mk(mi, d, l, B, operand(p(md.Wu), dt, l, 1), operand(dU, dt, 1, d, ldU),
-                          view(acc, F32, d, 1, (int64_t)mi * d));
-        const int64_t vr = tr ? 1 : d, vc = tr ? d : 1;
-        gt.e.dcn_bwd = 1;
-        gt.e.cross = view((void*)X, dt, vr, vc, (int64_t)mi * d);
-        gt.e.mask = view(md.A, dt, vr, vc, (int64_t)mi * d);
-        gt.e.aux = view(dA, dt, vr, vc, (int64_t)mi * d);
-        if (take_dR) gt.e.resid = view(c->dR, dt, vr, vc, (int64_t)mi * d);
-        if (fuse_db && !tr) gt.e.bsum = c->bsum;
-        RET(G_dT(gt, c, st, &bsum_rows));
+          Gemm gt = mk(mi, d, l, B, operand(p(md.Wu), dt, l, 1), operand(dU, dt, 1, d, ldU),
+                       view(acc, F32, d, 1, (int64_t)mi * d));
+          gt.e.dcn_bwd = 1;
+          gt.e.cross = view((void*)X, dt, d, 1, (int64_t)mi * d);
+          gt.e.mask = view(md.A, dt, d, 1, (int64_t)mi * d);
+          gt.e.aux = view(dA, dt, d, 1, (int64_t)mi * d);
+          if (take_dR) gt.e.resid = view(c->dR, dt, d, 1, (int64_t)mi * d);
+          if (fuse_db) gt.e.bsum = c->bsum;
+        RET(G_dT(gt, c, st, &bsum_rows, dU_in_dR));
         }
         if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dA ready
         Gemm gx = mk((int)rows, d, d, 1, operand(dA, dt, d, 1), operand(p(md.W), dt, 1, d), view(acc, F32, d, 1));
@@ -1070,14 +1064,14 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         }
         void* dF = c->tC;
         Gemm a = mk((int)rows, f, d, 1, operand(dR2, dt, d, 1), operand(p(md.W2), dt, 1, f), view(dF, dt, f, 1));
-        if (c->relu_bits && dt == BF16 && f % 64 == 0 && f >= 128) {   // ReLU'(0) = 0 from the forward's bitmask
+        if (c->tune.relu_bits && c->tune.tstore && dt == BF16 && f % 64 == 0 && f >= 128) {   // ReLU'(0) = 0 from the bitmask
           a.e.bits = md.Fbits; a.e.bits_mode = 2; a.e.bits_ld = rows;
         } else {
           a.e.mask = view(md.F, dt, f, 1);
         }
         // db_1 = column sums of dF: 32-row partial sums folded in the dgrad's TMA-store epilogue
         bool db1_fused = false;
-        if (c->fuse_db && dt == BF16 && c->csum) a.e.csum = c->csum;
+        if (c->tune.fuse_db && dt == BF16 && c->csum) a.e.csum = c->csum;
         RET(G_csum(a, c, st, "attn.ffn2_dgrad", &db1_fused));
         RET(ready());   // dF
         {
@@ -1198,8 +1192,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
 // (forward packed token projection, DCN backward packed dT) are built up front in ONE launch instead of one
 // small launch per module and direction.  The flags are cleared when the step ends (SGD changes W_u).
 static dhen_status prebuild_bd(dhen_ctx* c, int B, cudaStream_t st) {
-  static int on = [] { const char* e = getenv("DHEN_BD_PRE"); return e ? atoi(e) : 1; }();
-  if (!on || c->dist.world != 1 || c->dt != BF16) return DHEN_OK;
+  if (!c->tune.bd_pre || c->dist.world != 1 || c->dt != BF16) return DHEN_OK;
   BdJobs jobs;
   jobs.n = 0;
   for (int n = 0; n < c->cfg.n_layers; ++n) {
@@ -1233,19 +1226,21 @@ static void clear_bd(dhen_ctx* c) {
 
 // ------------------------------------------------------------------ head
 static dhen_status head(dhen_ctx* c, const void* YN, int mN, const float* labels, int B, int Bg, void* dY, float* loss,
-                        int do_bwd, cudaStream_t st) {
+                        int do_bwd, bool keep_w, cudaStream_t st) {
   const int gi = c->cfg.n_layers;
   void* pbase;
   RET(comp_params(c, gi, st, &pbase));
   PP p{(char*)pbase, c->es};
   Group& G = c->G[gi];
-  // single GPU: the head's parameter / loss sums trail on the side stream (the first backward layer's
-  // module joins bring it back before anything reads them); with collectives they stay on st
-  cudaStream_t sr = (c->overlap && c->trail && !serial_prof(c) && c->dist.world == 1) ? c->side_st : st;
+  // the head's parameter / loss sums trail on the side stream (the first backward layer's module joins bring
+  // it back before anything reads them; with collectives the reduce-scatter also waits for it)
+  cudaStream_t sr = (c->tune.overlap && c->tune.trail && !serial_prof(c)) ? c->side_st : st;
   KT("head", 0, (double)B * mN * c->d * c->es * (do_bwd ? 2 : 1), head_fwd_bwd(YN, p(0), p(G.toff[1]), c->dt, labels, B, mN, c->d, Bg, dY, c->dt, c->pooled, c->z, c->lossb, c->dz, loss,
                   G.grad, G.grad + G.toff[1], do_bwd, st, sr, c->ev_red));
+  // FSDP: the gathered slot is reused by the next all-gather; the last layer's LN backward reads w_h from a copy
+  if (keep_w && sharded(c)) CK(cudaMemcpyAsync(c->headw, p(0), (size_t)c->d * c->es, cudaMemcpyDeviceToDevice, st));
   RET(release(c, gi, st));
-  if (do_bwd) RET(reduce_grads(c, gi, st));
+  if (do_bwd) RET(reduce_grads(c, gi, st, sr));
   return DHEN_OK;
 }
 
@@ -1265,12 +1260,8 @@ static dhen_status make_ctx(const dhen_config* cfg, const dhen_dist* dist, dhen_
   if (dist) dd = *dist; else { memset(&dd, 0, sizeof dd); dd.world = 1; dd.fsdp = 1; }
   if (dd.world < 1 || dd.rank < 0 || dd.rank >= dd.world)
     return fail(DHEN_E_CONFIG, "dhen: rank=%d world=%d", dd.rank, dd.world);
+  if (dd.backend != 0 && dd.backend != 1) return fail(DHEN_E_CONFIG, "dhen: collective backend=%d (0 NCCL, 1 loopback)", dd.backend);
   c->cfg = *cfg;
-  { const char* e = getenv("DHEN_GRAM_SPT"); c->gram_spt = e ? atoi(e) : 0; }
-  { const char* e = getenv("DHEN_TR_SMALL_M"); c->tr_small_m = e ? atoi(e) : 0; }
-  { const char* e = getenv("DHEN_LN_FUSE"); c->ln_fuse = e ? atoi(e) : 1; }
-  { const char* e = getenv("DHEN_RELU_BITS"); c->relu_bits = e ? atoi(e) : 1; }
-  { const char* e = getenv("DHEN_FIRST_WRITER"); c->first_writer = e ? atoi(e) : 1; }
   if (c->cfg.ln_eps <= 0.f) c->cfg.ln_eps = 1e-5f;
   c->mods_cfg.resize(cfg->n_layers);
   c->layers_cfg.resize(cfg->n_layers);
@@ -1309,6 +1300,14 @@ dhen_status dhen_group_numel(const dhen_config* cfg, const dhen_dist* dist, int 
   return DHEN_OK;
 }
 
+dhen_status dhen_loopback_id(unsigned char out[128]) {
+  if (!out) return fail(DHEN_E_ALIGN, "dhen_loopback_id: out is NULL");
+  loopback_new_id(out);
+  return DHEN_OK;
+}
+
+unsigned long long dhen_comm_bytes(const dhen_ctx* c) { return c && c->comm ? c->comm->bytes : 0ull; }
+
 dhen_status dhen_nccl_id(unsigned char out[128]) {
   ncclUniqueId id;
   NK(ncclGetUniqueId(&id));
@@ -1338,14 +1337,6 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
   }
   plan(c, s, w);
   {
-    const char* ev = getenv("DHEN_OVERLAP");
-    c->overlap = ev ? atoi(ev) : 1;
-    const char* et = getenv("DHEN_TRAIL");
-    c->trail = et ? atoi(et) : 1;
-    const char* ef = getenv("DHEN_FUSE_DB");
-    c->fuse_db = ef ? atoi(ef) : 1;
-    const char* ev2 = getenv("DHEN_VDY");
-    c->vdy = ev2 ? atoi(ev2) : 1;
     bool ok = cudaStreamCreateWithFlags(&c->side_st, cudaStreamNonBlocking) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_sf, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_sx, cudaEventDisableTiming) == cudaSuccess;
@@ -1354,10 +1345,9 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
     if (!ok) { dhen_destroy(c); return fail(DHEN_E_CUDA, "dhen_init: side stream creation failed"); }
   }
   if (c->dist.world > 1) {
-    ncclUniqueId id;
-    memcpy(id.internal, c->dist.nccl_id, 128);
-    ncclResult_t r = ncclCommInitRank(&c->comm, c->dist.world, id, c->dist.rank);
-    if (r != ncclSuccess) { delete c; return fail(DHEN_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)); }
+    std::string why;
+    c->comm = comm_create(c->dist.backend, c->dist.nccl_id, c->dist.world, c->dist.rank, &why);
+    if (!c->comm) { dhen_destroy(c); return fail(DHEN_E_NCCL, "dhen_init: collective backend %d: %s", c->dist.backend, why.c_str()); }
     bool ok = cudaStreamCreateWithFlags(&c->comm_st, cudaStreamNonBlocking) == cudaSuccess;
     for (int k = 0; k < 2; ++k) {
       ok = ok && cudaEventCreateWithFlags(&c->ev_ag[k], cudaEventDisableTiming) == cudaSuccess;
@@ -1365,6 +1355,8 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
     }
     ok = ok && cudaEventCreateWithFlags(&c->ev_grad, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_grad2, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_cfork, cudaEventDisableTiming) == cudaSuccess;
     if (!ok) { dhen_destroy(c); return fail(DHEN_E_CUDA, "dhen_init: stream/event creation failed"); }
   }
   // parameter init: every rank initialises its own slice of the canonical vector
@@ -1417,8 +1409,10 @@ void dhen_destroy(dhen_ctx* c) {
   if (c->side_st) cudaStreamDestroy(c->side_st);
   if (c->ev_grad) cudaEventDestroy(c->ev_grad);
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+  if (c->ev_grad2) cudaEventDestroy(c->ev_grad2);
+  if (c->ev_cfork) cudaEventDestroy(c->ev_cfork);
   if (c->comm_st) cudaStreamDestroy(c->comm_st);
-  if (c->comm) ncclCommDestroy(c->comm);
+  delete c->comm;
   delete c;
 }
 
@@ -1452,12 +1446,6 @@ dhen_status dhen_debug_gemm(const long long* q, const void* A, const void* Bp, v
 }
 
 int dhen_debug_last_gemm_tc(void) { return g_last_gemm_tc; }
-int dhen_debug_attn_fused(int mode) { return attn::set_mode(mode); }
-int dhen_debug_gemm_pair(int mode) {
-  const int old = dhen::g_gemm_pair;
-  dhen::g_gemm_pair = mode < 0 ? -1 : mode > 0 ? 1 : 0;
-  return old;
-}
 
 dhen_status dhen_debug_gemm_epi(const long long* q, const void* A, const void* Bp, void* Cp, int ab_dt, int c_dt,
                                 int path, void* ws, size_t ws_bytes, int mode, const void* E, const void* bias,
@@ -1501,9 +1489,51 @@ dhen_status dhen_debug_gemm_epi(const long long* q, const void* A, const void* B
 
 void dhen_debug_gemm_trace(void* dev_buf) { g_gemm_trace = (long long*)dev_buf; }
 
+dhen_status dhen_debug_profile_trace(dhen_ctx* c, const char* path) {
+  if (!c || !path) return fail(DHEN_E_STATE, "dhen_debug_profile_trace: ctx or path is NULL");
+  FILE* fp = fopen(path, "w");
+  if (!fp) return fail(DHEN_E_CONFIG, "dhen_debug_profile_trace: cannot open %s", path);
+  std::vector<cudaStream_t> sts;
+  for (auto& r : c->recs) {
+    CK(cudaEventSynchronize(c->events[r.e1]));
+    float t0 = 0.f, t1 = 0.f;
+    cudaEventElapsedTime(&t0, c->events[c->recs[0].e0], c->events[r.e0]);
+    cudaEventElapsedTime(&t1, c->events[c->recs[0].e0], c->events[r.e1]);
+    size_t si = 0;
+    for (; si < sts.size(); ++si) if (sts[si] == r.st) break;
+    if (si == sts.size()) sts.push_back(r.st);
+    fprintf(fp, "%s,%zu,%.4f,%.4f\n", r.tag, si, t0, t1);
+  }
+  fclose(fp);
+  return DHEN_OK;
+}
+
+void dhen_tuning_default(dhen_tuning* t) { if (t) *t = tuning_default(); }
+
+dhen_status dhen_set_tuning(dhen_ctx* c, const dhen_tuning* t) {
+  if (!c || !t) return fail(DHEN_E_STATE, "dhen_set_tuning: ctx or tuning is NULL");
+  const int bits[] = {t->overlap, t->defer_join, t->ln_fuse, t->first_writer, t->relu_bits, t->fuse_db, t->vdy,
+                      t->trail, t->bd_pre, t->tstore, t->attn_fused, t->pdl, t->gemm_simt};
+  for (int b : bits)
+    if (b != 0 && b != 1) return fail(DHEN_E_CONFIG, "dhen_set_tuning: a 0/1 switch is %d", b);
+  if (t->sym < -1 || t->sym > 2 || t->pair < -1 || t->pair > 1 || t->pair_k < 0)
+    return fail(DHEN_E_CONFIG, "dhen_set_tuning: sym=%d pair=%d pair_k=%d", t->sym, t->pair, t->pair_k);
+  c->tune = *t;
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }   // the captured step baked the old switches in
+  c->graph_off = false;
+  return DHEN_OK;
+}
+
+dhen_status dhen_get_tuning(const dhen_ctx* c, dhen_tuning* t) {
+  if (!c || !t) return fail(DHEN_E_STATE, "dhen_get_tuning: ctx or tuning is NULL");
+  *t = c->tune;
+  return DHEN_OK;
+}
+
 dhen_status dhen_profile(dhen_ctx* c, int enable) {
   if (!c) return fail(DHEN_E_STATE, "dhen_profile: ctx is NULL");
   c->prof = enable != 0;
+  c->prof_mode = enable == 2 ? 2 : 1;
   if (enable) { c->recs.clear(); c->next_event = 0; }
   return DHEN_OK;
 }
@@ -1531,22 +1561,6 @@ dhen_status dhen_profile_read(dhen_ctx* c, dhen_op_stat* out, int cap, int* n) {
   }
   *n = (int)agg.size();
   for (int k = 0; k < (int)agg.size() && k < cap; ++k) out[k] = agg[k];
-  // DHEN_PROF_TRACE=<file>: also dump every record (op, stream, start and end in ms from the first record)
-  if (const char* tf = getenv("DHEN_PROF_TRACE")) {
-    if (FILE* fp = fopen(tf, "w")) {
-      std::vector<cudaStream_t> sts;
-      for (auto& r : c->recs) {
-        float t0 = 0.f, t1 = 0.f;
-        cudaEventElapsedTime(&t0, c->events[c->recs[0].e0], c->events[r.e0]);
-        cudaEventElapsedTime(&t1, c->events[c->recs[0].e0], c->events[r.e1]);
-        size_t si = 0;
-        for (; si < sts.size(); ++si) if (sts[si] == r.st) break;
-        if (si == sts.size()) sts.push_back(r.st);
-        fprintf(fp, "%s,%zu,%.4f,%.4f\n", r.tag, si, t0, t1);
-      }
-      fclose(fp);
-    }
-  }
   return DHEN_OK;
 }
 
@@ -1561,6 +1575,7 @@ dhen_status dhen_zero_grad(dhen_ctx* c, void* stream) {
 
 dhen_status dhen_layer_fwd(dhen_ctx* c, int n, const void* x, void* y, int B, void* stream) {
   if (!c) return fail(DHEN_E_STATE, "dhen_layer_fwd: ctx is NULL");
+  TuneScope ts_(&c->tune);
   if (n < 0 || n >= c->cfg.n_layers) return fail(DHEN_E_SHAPE, "dhen_layer_fwd: layer=%d of %d", n, c->cfg.n_layers);
   if (B < 1 || B > c->Bmax) return fail(DHEN_E_SHAPE, "dhen_layer_fwd: B=%d not in [1, %d]", B, c->Bmax);
   if (!aligned16(x) || !aligned16(y)) return fail(DHEN_E_ALIGN, "dhen_layer_fwd: x=%p y=%p", x, y);
@@ -1573,6 +1588,7 @@ dhen_status dhen_layer_fwd(dhen_ctx* c, int n, const void* x, void* y, int B, vo
 
 dhen_status dhen_layer_bwd(dhen_ctx* c, int n, const void* dy, void* dx, int B, void* stream) {
   if (!c) return fail(DHEN_E_STATE, "dhen_layer_bwd: ctx is NULL");
+  TuneScope ts_(&c->tune);
   if (n < 0 || n >= c->cfg.n_layers) return fail(DHEN_E_SHAPE, "dhen_layer_bwd: layer=%d of %d", n, c->cfg.n_layers);
   if (c->L[n].B != B) return fail(DHEN_E_STATE, "dhen_layer_bwd: layer %d has no saved forward at B=%d (saved B=%d)", n, B, c->L[n].B);
   if (!aligned16(dy) || (dx && !aligned16(dx))) return fail(DHEN_E_ALIGN, "dhen_layer_bwd: dy=%p dx=%p", dy, dx);
@@ -1586,6 +1602,7 @@ dhen_status dhen_layer_bwd(dhen_ctx* c, int n, const void* dy, void* dx, int B, 
 
 dhen_status dhen_forward(dhen_ctx* c, const void* x0, int B, float* logits, void* stream) {
   if (!c) return fail(DHEN_E_STATE, "dhen_forward: ctx is NULL");
+  TuneScope ts_(&c->tune);
   if (B < 1 || B > c->Bmax) return fail(DHEN_E_SHAPE, "dhen_forward: B=%d not in [1, %d]", B, c->Bmax);
   if (!aligned16(x0) || !aligned16(logits)) return fail(DHEN_E_ALIGN, "dhen_forward: x0=%p logits=%p", x0, logits);
   cudaStream_t st = S(stream);
@@ -1597,7 +1614,7 @@ dhen_status dhen_forward(dhen_ctx* c, const void* x0, int B, float* logits, void
     RET(layer_fwd(c, n, X, c->L[n].Y, B, st));
     X = c->L[n].Y;
   }
-  RET(head(c, X, c->L.back().m_out, nullptr, B, B, nullptr, nullptr, 0, st));
+  RET(head(c, X, c->L.back().m_out, nullptr, B, B, nullptr, nullptr, 0, false, st));
   CK(cudaMemcpyAsync(logits, c->z, (size_t)B * 4, cudaMemcpyDeviceToDevice, st));
   CK(cudaGetLastError());
   return DHEN_OK;
@@ -1606,6 +1623,7 @@ dhen_status dhen_forward(dhen_ctx* c, const void* x0, int B, float* logits, void
 dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, int B, int Bg, float lr, float* loss,
                             void* dx0, void* stream) {
   if (!c) return fail(DHEN_E_STATE, "dhen_train_step: ctx is NULL");
+  TuneScope ts_(&c->tune);
   if (B < 1 || B > c->Bmax) return fail(DHEN_E_SHAPE, "dhen_train_step: B=%d not in [1, %d]", B, c->Bmax);
   if (Bg < B) return fail(DHEN_E_SHAPE, "dhen_train_step: B_global=%d < B=%d", Bg, B);
   if (!aligned16(x0) || !aligned16(labels) || (dx0 && !aligned16(dx0)) || (loss && ((uintptr_t)loss & 3)))
@@ -1614,6 +1632,14 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
   cudaStream_t st = S(stream);
   RET(dhen_zero_grad(c, stream));
   invalidate_gathered(c);
+  if (c->dist.world > 1) {
+    // the communication stream (and the slot-release events it waits on) start from this step's stream: the
+    // collectives are ordered after everything before the step, and a CUDA-graph capture of the step takes
+    // the communication stream in with it
+    CK(cudaEventRecord(c->ev_cfork, st));
+    CK(cudaStreamWaitEvent(c->comm_st, c->ev_cfork, 0));
+    for (int k = 0; k < 2; ++k) CK(cudaEventRecord(c->ev_use[k], st));
+  }
   const void* X = x0;
   clear_bd(c);
   RET(prebuild_bd(c, B, st));
@@ -1623,10 +1649,9 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
     RET(layer_fwd(c, n, X, c->L[n].Y, B, st));
     X = c->L[n].Y;
   }
-  // single GPU, bf16: the head writes only dz; the last layer's LN backward forms dY = dz w / m itself
-  const bool vdy = c->vdy && c->dist.world == 1 && c->dt == BF16 && c->d % 8 == 0 && c->d >= 32 && c->d <= 256 &&
-                   (c->d & (c->d - 1)) == 0;
-  RET(head(c, X, c->L.back().m_out, labels, B, Bg, vdy ? nullptr : c->dY[0], loss, 1, st));
+  // bf16: the head writes only dz; the last layer's LN backward forms dY = dz w / m itself
+  const bool vdy = c->tune.vdy && c->dt == BF16 && c->d % 8 == 0 && c->d >= 32 && c->d <= 256 && (c->d & (c->d - 1)) == 0;
+  RET(head(c, X, c->L.back().m_out, labels, B, Bg, vdy ? nullptr : c->dY[0], loss, 1, vdy, st));
   c->vdy_now = vdy;
   int cur = 0;
   for (int n = c->cfg.n_layers - 1; n >= 0; --n) {
@@ -1681,7 +1706,8 @@ static dhen_status gather_f32(dhen_ctx* c, Group& g, const float* shard_or_full,
                               cudaStream_t st) {
   pad.assign((size_t)g.npad, 0.f);
   if (c->dist.world > 1 && c->dist.fsdp) {
-    NK(ncclAllGather(shard_or_full, c->gtmp, (size_t)g.shard, ncclFloat32, c->comm, st));
+    if (c->comm->all_gather(shard_or_full, c->gtmp, (size_t)g.shard, F32, st))
+      return fail(DHEN_E_NCCL, "all-gather (fp32 host read) (%s): %s", c->comm->name(), c->comm->err.c_str());
     CK(cudaMemcpyAsync(pad.data(), c->gtmp, (size_t)g.npad * 4, cudaMemcpyDeviceToHost, st));
   } else {
     CK(cudaMemcpyAsync(pad.data(), shard_or_full, (size_t)g.n * 4, cudaMemcpyDeviceToHost, st));
@@ -1693,7 +1719,10 @@ static dhen_status gather_f32(dhen_ctx* c, Group& g, const float* shard_or_full,
 dhen_status dhen_train_step_graphed(dhen_ctx* c, const void* x0, const float* labels, int B, int Bg, float lr,
                                     float* loss, void* dx0, void* stream) {
   if (!c) return fail(DHEN_E_STATE, "dhen_train_step_graphed: ctx is NULL");
-  if (c->dist.world > 1 || c->prof) return dhen_train_step(c, x0, labels, B, Bg, lr, loss, dx0, stream);
+  TuneScope ts_(&c->tune);
+  // loopback collectives are host rendezvous between threads (not capturable); a profiled step records events
+  if (c->prof || (c->dist.world > 1 && (c->dist.backend != 0 || c->graph_off)))
+    return dhen_train_step(c, x0, labels, B, Bg, lr, loss, dx0, stream);
   cudaStream_t st = S(stream);
   const bool same = c->gexec && c->gkey[0] == x0 && c->gkey[1] == labels && c->gkey[2] == loss &&
                     c->gkey[3] == dx0 && c->gkey_B == B && c->gkey_Bg == Bg && c->gkey_lr == lr;
@@ -1713,8 +1742,16 @@ dhen_status dhen_train_step_graphed(dhen_ctx* c, const void* x0, const float* la
     dhen_status s0 = dhen_train_step(c, x0, labels, B, Bg, lr, loss, dx0, c->cap_st);
     c->graph_launches = g_launches - l0;
     cudaError_t e = cudaStreamEndCapture(c->cap_st, &graph);
-    if (s0 != DHEN_OK) { if (graph) cudaGraphDestroy(graph); return s0; }
-    CK(e);
+    if (s0 != DHEN_OK || e != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      if (c->dist.world > 1) {   // NCCL step not capturable here: every later step runs eagerly (same result)
+        (void)cudaGetLastError();
+        c->graph_off = true;
+        return DHEN_OK;          // this call's step already ran eagerly
+      }
+      if (s0 != DHEN_OK) return s0;
+      CK(e);
+    }
     e = cudaGraphInstantiate(&c->gexec, graph, 0);
     cudaGraphDestroy(graph);
     CK(e);
@@ -1729,6 +1766,7 @@ dhen_status dhen_train_step_graphed(dhen_ctx* c, const void* x0, const float* la
 
 dhen_status dhen_params_io(dhen_ctx* c, int gi, float* host, int set, void* stream) {
   if (!c) return fail(DHEN_E_STATE, "dhen_params_io: ctx is NULL");
+  TuneScope ts_(&c->tune);
   if (gi < 0 || gi > c->cfg.n_layers) return fail(DHEN_E_SHAPE, "dhen_params_io: group=%d", gi);
   if (!host) return fail(DHEN_E_ALIGN, "dhen_params_io: host is NULL");
   Group& g = c->G[gi];
@@ -1751,6 +1789,7 @@ dhen_status dhen_params_io(dhen_ctx* c, int gi, float* host, int set, void* stre
 
 dhen_status dhen_grads_get(dhen_ctx* c, int gi, float* host, void* stream) {
   if (!c) return fail(DHEN_E_STATE, "dhen_grads_get: ctx is NULL");
+  TuneScope ts_(&c->tune);
   if (gi < 0 || gi > c->cfg.n_layers) return fail(DHEN_E_SHAPE, "dhen_grads_get: group=%d", gi);
   if (!host) return fail(DHEN_E_ALIGN, "dhen_grads_get: host is NULL");
   Group& g = c->G[gi];

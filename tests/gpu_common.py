@@ -24,7 +24,7 @@ def t2np(t):
 class Case:
     """One seeded problem: params, X0, labels, for both sides."""
 
-    def __init__(self, net: O.NetSpec, B: int, dtype: str, seed: int):
+    def __init__(self, net: O.NetSpec, B: int, dtype: str, seed: int, tuning=None):
         import torch
         self.net, self.B, self.dtype = net, B, dtype
         self.flats = make_flat_params(net, seed)
@@ -35,6 +35,8 @@ class Case:
         self.y = synth.make_labels(seed, B).astype(np.float64)
         from paper_2203_11014_b200.binding import DHEN
         self.model = DHEN(to_binding(net, dtype, B))
+        if tuning:
+            self.model.set_tuning(**tuning)
         for g, f in enumerate(self.flats):
             self.model.set_params(g, f)
         tdt = torch.bfloat16 if dtype == "bf16" else torch.float32

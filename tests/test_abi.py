@@ -1,5 +1,5 @@
 """C ABI checks that need no GPU: the library loads, exports every symbol
-include/dhen.h declares, validates configs with the documented errors, and its
+include/dhen.h and include/dhen_debug.h declare, validates configs with the documented errors, and its
 parameter layout agrees with the oracle's canonical order (sizes per group)."""
 import os
 import re
@@ -20,18 +20,20 @@ def B():
     return binding
 
 
-def header_symbols():
-    src = open(os.path.join(ROOT, "include", "dhen.h")).read()
+def header_symbols(name="dhen.h"):
+    src = open(os.path.join(ROOT, "include", name)).read()
     return sorted(set(re.findall(r"\b(dhen_[a-z_]+)\s*\(", src)))
 
 
 def test_exports_every_header_symbol(B):
     lib = B.load()
     syms = header_symbols()
-    assert len(syms) >= 14
-    for s in syms:
+    dbg = header_symbols("dhen_debug.h")
+    assert len(syms) >= 14 and len(dbg) >= 4
+    assert not set(syms) & set(dbg)
+    for s in syms + dbg:
         assert hasattr(lib, s), s
-    assert set(syms) == set(B.EXPORTS)
+    assert set(syms) | set(dbg) == set(B.EXPORTS)
 
 
 def _cfg(B, net, dtype="bf16", bmax=8):

@@ -1,15 +1,20 @@
-"""A/B tests of the fusions and schedules that are switchable at context creation (env read by dhen_init):
-each variant must reproduce the reference schedule on the same inputs -- bit for bit where the arithmetic
-is the same, within bf16 rounding where a fusion changes where a value is rounded.
+"""A/B tests of a context's schedule / fusion switches (dhen_tuning, include/dhen_debug.h; per context, set
+through dhen_set_tuning -- nothing is read from the environment): each variant must reproduce the default
+schedule on the same inputs -- bit for bit where the arithmetic is the same, within bf16 rounding where a
+fusion changes where a value is rounded.
 
-DHEN_OVERLAP      weight gradients / module branches on a second stream        -> bitwise identical
-DHEN_LN_FUSE      LayerNorm in the producing GEMM epilogues (F5, F6, F12)      -> same storage points
-DHEN_FIRST_WRITER first / last dX writer (B3, B10) instead of LN-bwd init + cast -> same fp32 sums, other order
-DHEN_RELU_BITS    FFN ReLU derivative from a bitmask                            -> bitwise identical
-dhen_debug_gemm_pair CTA-pair GEMMs vs single-CTA tiles                       -> same sums up to split grouping
-DHEN_FUSE_DB      bias gradients from GEMM epilogue column sums (DCN db, FFN db_1) -> same values, other grouping
-DHEN_VDY          head dY formed inside the last LayerNorm backward (not stored) -> bitwise identical
-DHEN_SYM          dot backward symmetrisation through a dense shared image       -> bitwise identical
+overlap       weight gradients / module branches on a second stream           -> bitwise identical
+defer_join    side-stream joins deferred to buffer reuse                      -> bitwise identical
+trail         LayerNorm / head parameter sums trailing on the side stream     -> bitwise identical
+bd_pre        every layer's block-diagonal token maps in one launch per step  -> bitwise identical
+ln_fuse       LayerNorm in the producing GEMM epilogues (F5, F6, F12)         -> same storage points
+first_writer  first / last dX writer (B3, B10) instead of LN-bwd init + cast  -> same fp32 sums, other order
+relu_bits     FFN ReLU derivative from a bitmask                               -> bitwise identical
+pair          CTA-pair GEMMs vs single-CTA tiles                               -> same sums up to split grouping
+fuse_db       bias gradients from GEMM epilogue column sums (DCN db, FFN db_1) -> same values, other grouping
+vdy           head dY formed inside the last LayerNorm backward (not stored)   -> bitwise identical
+sym           dot backward symmetrisation through a dense shared image         -> bitwise identical
+tstore        TMA-store GEMM epilogue vs the register epilogue                 -> same values (db_1 grouping)
 """
 import numpy as np
 import pytest
@@ -21,14 +26,9 @@ from tests.helpers import config, norm_err
 pytestmark = pytest.mark.gpu
 
 
-def _step(net, B, seed, env, monkeypatch):
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    case = Case(net, B, "bf16", seed=seed)
-    out = case.gpu_step(lr=0.01)
-    for k in env:
-        monkeypatch.delenv(k, raising=False)
-    return out
+def _step(net, B, seed, tuning):
+    case = Case(net, B, "bf16", seed=seed, tuning=tuning)
+    return case.gpu_step(lr=0.01)
 
 
 def _cmp(a, b, net, tol):
@@ -53,75 +53,82 @@ def _net(name, layers):
 
 
 @pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2), ("C3", 32, 2), ("C5", 16, 2)])
-def test_side_streams_bitwise(name, B, layers, monkeypatch):
+def test_side_streams_bitwise(name, B, layers):
     net = _net(name, layers)
-    a = _step(net, B, 11, {"DHEN_OVERLAP": "0"}, monkeypatch)
-    b = _step(net, B, 11, {"DHEN_OVERLAP": "1"}, monkeypatch)
+    a = _step(net, B, 11, {"overlap": 0})
+    b = _step(net, B, 11, {"overlap": 1})
     _cmp(a, b, net, 0)
 
 
 @pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2), ("C5", 16, 2)])
-def test_fused_layernorm_matches_kernel(name, B, layers, monkeypatch):
+def test_fused_layernorm_matches_kernel(name, B, layers):
     net = _net(name, layers)
-    a = _step(net, B, 12, {"DHEN_LN_FUSE": "0"}, monkeypatch)
-    b = _step(net, B, 12, {"DHEN_LN_FUSE": "1"}, monkeypatch)
+    a = _step(net, B, 12, {"ln_fuse": 0})
+    b = _step(net, B, 12, {"ln_fuse": 1})
     _cmp(a, b, net, 1e-2)
 
 
 @pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2), ("C5", 16, 2), ("C3", 32, 2)])
-def test_first_last_dx_writer(name, B, layers, monkeypatch):
+def test_first_last_dx_writer(name, B, layers):
     net = _net(name, layers)
-    a = _step(net, B, 13, {"DHEN_FIRST_WRITER": "0"}, monkeypatch)
-    b = _step(net, B, 13, {"DHEN_FIRST_WRITER": "1"}, monkeypatch)
+    a = _step(net, B, 13, {"first_writer": 0})
+    b = _step(net, B, 13, {"first_writer": 1})
     _cmp(a, b, net, 1e-2)
 
 
 @pytest.mark.parametrize("name,B,layers", [("C2", 2048, 2), ("C4", 128, 2)])
-def test_cta_pairs_match_single_cta(name, B, layers, monkeypatch):
+def test_cta_pairs_match_single_cta(name, B, layers):
     """CTA-pair GEMMs (cta_group::2, deeper ring; LayerNorm epilogues included) against single-CTA tiles on
     the same step, at batch sizes where the size rule takes pairs (C2: the dot projection family at the
     bench's B = 2048; C4: FFN2 and the long-K weight gradients).  Same MMA chain per output row, so the
     results agree to rounding of the split-K reduction grouping."""
-    from paper_2203_11014_b200.binding import debug_gemm_pair
     net = _net(name, layers)
-    old = debug_gemm_pair(0)
-    try:
-        a = _step(net, B, 14, {}, monkeypatch)
-        debug_gemm_pair(-1)
-        b = _step(net, B, 14, {}, monkeypatch)
-    finally:
-        debug_gemm_pair(old)
+    a = _step(net, B, 14, {"pair": 0})
+    b = _step(net, B, 14, {"pair": -1})
     _cmp(a, b, net, 1e-2)
 
 
 @pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C5", 16, 2), ("C3", 32, 2), ("C4", 16, 2)])
-def test_fused_bias_grads(name, B, layers, monkeypatch):
+def test_fused_bias_grads(name, B, layers):
     """Bias gradients summed inside the producing GEMM epilogues against the separate column-sum kernel
     (same stored bf16 values, other grouping): B8 db = sum of dA (per-CTA partial rows from the DCN dT GEMM)
     and B6 db_1 = sum of dF (32-row partial rows from the FFN2 dgrad's TMA-store epilogue)."""
     net = _net(name, layers)
-    a = _step(net, B, 15, {"DHEN_FUSE_DB": "0"}, monkeypatch)
-    b = _step(net, B, 15, {"DHEN_FUSE_DB": "1"}, monkeypatch)
+    a = _step(net, B, 15, {"fuse_db": 0})
+    b = _step(net, B, 15, {"fuse_db": 1})
     _cmp(a, b, net, 1e-3)
 
 
 @pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2)])
-def test_head_gradient_formed_in_ln_backward(name, B, layers, monkeypatch):
+def test_head_gradient_formed_in_ln_backward(name, B, layers):
     """B1 -> B2: the head's dY = bf16(dz_b / m w) formed inside the last layer's LayerNorm backward (never
     stored) is bit-identical to the head kernel writing it and the LayerNorm backward reading it."""
     net = _net(name, layers)
-    a = _step(net, B, 16, {"DHEN_VDY": "0"}, monkeypatch)
-    b = _step(net, B, 16, {"DHEN_VDY": "1"}, monkeypatch)
+    a = _step(net, B, 16, {"vdy": 0})
+    b = _step(net, B, 16, {"vdy": 1})
     _cmp(a, b, net, 0)
 
 
 @pytest.mark.parametrize("mode", ["1", "2"])
 @pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2)])
-def test_dense_symmetrisation_bitwise(name, B, layers, mode, monkeypatch):
+def test_dense_symmetrisation_bitwise(name, B, layers, mode):
     """B-dot: S = sym(dZ) scattered through a dense bf16 m x (m+2) shared image (one warp per triangle row)
     is bit-identical to the staged-triangle kernel (both copy the stored bf16 values); mode 1 stages the
     triangle in shared memory first, mode 2 reads it from global memory."""
     net = _net(name, layers)
-    a = _step(net, B, 17, {"DHEN_SYM": "0"}, monkeypatch)
-    b = _step(net, B, 17, {"DHEN_SYM": mode}, monkeypatch)
+    a = _step(net, B, 17, {"sym": 0})
+    b = _step(net, B, 17, {"sym": int(mode)})
     _cmp(a, b, net, 0)
+
+
+@pytest.mark.parametrize("switch", ["defer_join", "trail", "bd_pre", "tstore"])
+@pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2), ("C3", 32, 2)])
+def test_schedule_switches_bitwise(name, B, layers, switch):
+    """Schedule-only switches (same kernels' arithmetic in another order of launch / store path): the
+    default and the switch turned off give bit-identical loss, dL/dX0 and gradients.  Without the TMA-store
+    epilogue the FFN db_1 column sums come from the separate column-sum kernel (other grouping; the ReLU
+    bitmask, a TMA-store feature, also falls back to the bf16 mask): 1e-3 there."""
+    net = _net(name, layers)
+    a = _step(net, B, 18, {switch: 0})
+    b = _step(net, B, 18, {})
+    _cmp(a, b, net, 1e-3 if switch == "tstore" else 0)

@@ -3,10 +3,15 @@ same seeded inputs (SURVEY §8(c) protocol).
 
 G1  fp32 mode, full train step:   loss / dX0 / new params elem <= 1e-5, grads norm <= 1e-5.
 G3  bf16 mode, full train step:   oracle emulates the bf16 storage points (DESIGN.md §4);
-                                  norm <= 2e-2 for Y-side outputs and grads (ReLU-gated grads
-                                  reported, gated at 5e-2: mask flips, SURVEY G3').
-G2  bf16 layer-local:             oracle fed the GPU's own bf16 layer input and dY.
-Sizes span several 64/128 tiles plus ragged tails (B*m not a tile multiple)."""
+                                  norm <= 2e-2 for Y-side outputs and grads; ReLU-gated grads
+                                  (a Linear feeding a ReLU) are report-only end to end (SURVEY G3':
+                                  mask flips of near-zero pre-activations), bounded by a relative
+                                  Frobenius error <= 0.5.
+G2  bf16 layer-local:             oracle fed the GPU's own bf16 layer input and dY; every grad
+                                  (ReLU-gated included) norm <= 2e-2.
+Sizes span several 64/128 tiles plus ragged tails (B*m not a tile multiple); the timed launch
+configurations (full per-GPU batch) are covered by sampled-sample parity (test_full_size_sampled).
+Every comparison prints its achieved errors (run with -s)."""
 import numpy as np
 import pytest
 
@@ -22,24 +27,40 @@ def _gated(name):
         (".mlp." in name and name.endswith(("W_1", "b_1", "W_2", "b_2")))
 
 
-def _compare(case, g, o, tol_elem, tol_norm, relu_tol=None):
+def _frob(a, o):
+    a, o = np.asarray(a, np.float64), np.asarray(o, np.float64)
+    den = np.linalg.norm(o)
+    return float(np.linalg.norm(a - o) / (den if den > 0 else 1.0))
+
+
+def _compare(case, g, o, tol_elem, tol_norm, gated_report_only=False, label=""):
+    """gated_report_only: ReLU-gated grads are reported (norm) and bounded by a relative Frobenius error
+    <= 0.5 instead of gated at tol_norm (SURVEY G3', end-to-end bf16 only)."""
     net = case.net
     report = {}
     report["loss"] = abs(g["loss"] - o["loss"]) / max(1.0, abs(o["loss"]))
     report["dX0"] = norm_err(g["dX0"], o["dX0"])
     og = case.flat_grads(o)
     op = case.flat_params(o)
-    worst = []
+    worst, gated = [], []
     for gi in range(len(og)):
         gt = per_tensor(net, gi, g["grads"][gi])
         ot = per_tensor(net, gi, og[gi])
         for k in ot:
             e = norm_err(gt[k], ot[k])
-            tol = relu_tol if (relu_tol is not None and _gated(k)) else tol_norm
-            worst.append((e, tol, f"g{gi}.{k}"))
+            if gated_report_only and _gated(k):
+                gated.append((e, _frob(gt[k], ot[k]), f"g{gi}.{k}"))
+            else:
+                worst.append((e, tol_norm, f"g{gi}.{k}"))
         report[f"params{gi}"] = elem_err(g["params"][gi], op[gi])
-    bad = [(e, t, k) for e, t, k in worst if not e <= t]
-    msg = f"{report} worst grads {sorted(worst, reverse=True)[:5]}"
+    bad = [(e, t, k) for e, t, k in worst if not e <= t] + [(f, 0.5, k) for _, f, k in gated if not f <= 0.5]
+    top = sorted(worst, reverse=True)[:3]
+    print(f"\nPARITY {label}: loss {report['loss']:.2e} dX0 {report['dX0']:.2e} "
+          f"params {max(v for k, v in report.items() if k.startswith('params')):.2e} "
+          f"worst grads " + ", ".join(f"{k} {e:.2e}" for e, _, k in top) +
+          ("; ReLU-gated (report only) " + ", ".join(f"{k} norm {e:.2e} frob {f:.2e}" for e, f, k in
+                                                     sorted(gated, reverse=True)[:4]) if gated else ""))
+    msg = f"{report} worst grads {sorted(worst, reverse=True)[:5]} gated {gated}"
     assert report["loss"] <= tol_elem, msg
     assert report["dX0"] <= tol_norm, msg
     for gi in range(len(og)):
@@ -55,7 +76,7 @@ def test_fp32_train_step_matches_oracle(name, B):
     case = Case(net, B, "fp32", seed=2203011014 + 1)
     g = case.gpu_step(lr=0.1)
     o = case.oracle_step(lr=0.1)
-    _compare(case, g, o, 1e-5, 1e-5)
+    _compare(case, g, o, 1e-5, 1e-5, label=f"G1 fp32 {name} B={B}")
 
 
 @pytest.mark.parametrize("name,B", [("C2", 37), ("C3", 21), ("C4", 19), ("C5", 29)])
@@ -65,13 +86,13 @@ def test_bf16_train_step_matches_oracle(name, B):
     case = Case(net, B, "bf16", seed=2203011014 + 2)
     g = case.gpu_step(lr=0.05)
     o = case.oracle_step(lr=0.05)
-    _compare(case, g, o, 2e-2, 2e-2, relu_tol=5e-2)
+    _compare(case, g, o, 2e-2, 2e-2, gated_report_only=True, label=f"G3 bf16 small {name} B={B}")
 
 
 def test_fp32_c1_full_config():
     """C1 exactly as BASELINE.json names it (1 layer {Dot 4, Linear 4}, 8 x 16, B = 32, fp32)."""
     case = Case(config("C1"), 32, "fp32", seed=2203011014 + 1)
-    _compare(case, case.gpu_step(0.1), case.oracle_step(0.1), 1e-5, 1e-5)
+    _compare(case, case.gpu_step(0.1), case.oracle_step(0.1), 1e-5, 1e-5, label="G1 C1 full")
 
 
 @pytest.mark.parametrize("kind", ["dot", "attn", "conv", "dcn", "linear", "mlp"])
@@ -95,12 +116,13 @@ def test_bf16_layer_local(kind):
     pr = case.prec()
     P = O.compute_params(case.params, pr)[0]
     Yo, cache = O.layer_fwd(net, 0, case.X0, P, pr)
-    assert elem_err(t2np(y), Yo) <= 2e-2
     dXo, go = O.layer_bwd(net, 0, cache, t2np(dy), P, pr)
-    assert norm_err(t2np(dx), dXo) <= 2e-2
     gg = per_tensor(net, 0, case.model.get_grads(0).astype(np.float64))
-    for k, v in go.items():
-        assert norm_err(gg[k], v) <= 2e-2, (k, norm_err(gg[k], v))
+    errs = {"Y": elem_err(t2np(y), Yo), "dX": norm_err(t2np(dx), dXo)}
+    errs.update({k: norm_err(gg[k], v) for k, v in go.items()})
+    print(f"\nPARITY G2 {kind}: " + " ".join(f"{k} {e:.2e}" for k, e in errs.items()))
+    bad = {k: e for k, e in errs.items() if e > 2e-2}
+    assert not bad, (bad, errs)
 
 
 def test_layer_bwd_accumulates_and_is_deterministic():
@@ -126,51 +148,62 @@ def test_layer_bwd_accumulates_and_is_deterministic():
     assert np.array_equal(case.model.get_grads(0), g1)
 
 
-def test_full_size_c2_sampled():
-    """C2 at BASELINE.json's full size (B = 2048), the launch configuration bench.py times:
-    logits and dX0 of sampled samples against the oracle run on those samples alone
-    (both depend on their own sample only; B_global = 2048 scales dX0)."""
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_full_size_sampled(name):
+    """Every bf16 config at its FULL per-GPU batch (C2 2048, C3 / C4 / C5 8192), i.e. the launch
+    configurations bench.py times (pair / split-K / packing rules keyed on B): the logits and dL/dX0 of
+    sampled samples against the oracle run on those samples alone (each depends on its own sample only;
+    B_global = B scales dX0).  Sample 0, the last sample (ragged tail of every tile walk) and two inner ones."""
     import torch
-    net = config("C2")
-    B = 2048
-    case = Case(net, B, "bf16", seed=2203011014 + 2)
+    from paper_2203_11014_b200 import configs
+    net = config(name)
+    B = configs.BATCH[name]
+    case = Case(net, B, "bf16", seed=2203011014 + 7)
+    logits = torch.empty(B, dtype=torch.float32, device="cuda")
+    case.model.forward(case.x0, logits)
     g = case.gpu_step(lr=0.01)
     assert np.isfinite(g["loss"]) and all(np.isfinite(x).all() for x in g["grads"])
-    logits = torch.empty(B, dtype=torch.float32, device="cuda")
-    # logits after the step use the updated params; recompute the pre-step logits instead
-    for gi, f in enumerate(case.flats):
-        case.model.set_params(gi, f)
-    case.model.forward(case.x0, logits)
-    torch.cuda.synchronize()
-    zl = logits.cpu().numpy()
-    idx = [0, 1, 777, 2047]
+    zl = logits.cpu().numpy().astype(np.float64)
+    idx = [0, 1, B // 2 + 3, B - 1]
     o = O.train_step(net, case.params, case.X0[idx], case.y[idx], 0.0, B_global=B, pr=case.prec())
-    assert np.abs(zl[idx] - o["logits"]).max() <= 2e-2 * max(1.0, np.abs(o["logits"]).max())
-    assert norm_err(g["dX0"][idx], o["dX0"]) <= 2e-2
+    e_z = np.abs(zl[idx] - o["logits"]).max() / max(1.0, np.abs(o["logits"]).max())
+    e_dx = norm_err(g["dX0"][idx], o["dX0"])
+    print(f"\nPARITY full-size {name} B={B} samples {idx}: logits {e_z:.2e} dX0 {e_dx:.2e}")
+    assert e_z <= 2e-2 and e_dx <= 2e-2, (e_z, e_dx)
 
 
-@pytest.mark.parametrize("name,B,layers", [("C2", 40, 2), ("C3", 32, 4), ("C4", 3, 2), ("C5", 8, 8)])
+def test_full_size_c2_all_grads():
+    """C2 at its full BASELINE batch (2048, the bench launch configuration): loss, dX0, every parameter
+    gradient and every updated parameter against the oracle run on the whole batch (G3; C2 has no ReLU)."""
+    net = config("C2")
+    case = Case(net, 2048, "bf16", seed=2203011014 + 2)
+    g = case.gpu_step(lr=0.01)
+    o = case.oracle_step(lr=0.01)
+    _compare(case, g, o, 2e-2, 2e-2, label="G3 full C2 B=2048")
+
+
+@pytest.mark.parametrize("name,B,layers", [("C2", 40, 2), ("C3", 32, 4), ("C4", 16, 2), ("C5", 8, 8)])
 def test_bf16_full_dims_train_step(name, B, layers):
-    """G3 at BASELINE.json's per-layer shapes (m, d, l_i, heads, FFN, MLP widths) and a small batch,
-    so the contractions take the tcgen05/TMA path exactly as in the timed step (C4 truncated to 2
-    of its 8 identical layers to bound the fp64 oracle's memory).  ReLU-gated grads are chaotic
-    end to end (mask flips of near-zero pre-activations, SURVEY G3') and are checked layer-locally
-    in test_bf16_full_dims_layer_local instead; here they only have to stay bounded."""
+    """G3 at BASELINE.json's per-layer shapes (m, d, l_i, heads, FFN, MLP widths) and a small batch
+    that takes the same fused paths as the timed step (B a multiple of every 128 / l_i: the LayerNorm-
+    fused packed token projections), so the contractions run on the tcgen05/TMA path exactly as in the
+    bench (C4 truncated to 2 of its 8 identical layers to bound the fp64 oracle's memory).  ReLU-gated
+    grads are chaotic end to end (mask flips of near-zero pre-activations, SURVEY G3'): reported and
+    bounded here, gated layer-locally in test_bf16_full_dims_layer_local."""
     net = config(name)
     net = O.NetSpec(net.m0, net.d, net.layers[:layers])
     case = Case(net, B, "bf16", seed=2203011014 + 5)
     g = case.gpu_step(lr=0.01)
     o = case.oracle_step(lr=0.01)
-    _compare(case, g, o, 2e-2, 2e-2, relu_tol=1.0)
+    _compare(case, g, o, 2e-2, 2e-2, gated_report_only=True, label=f"G3 full-dims {name} B={B}")
 
 
 @pytest.mark.parametrize("name,B,layers", [("C2", 24, 2), ("C3", 24, 4), ("C4", 16, 2), ("C5", 6, 8)])
 def test_bf16_full_dims_layer_local(name, B, layers):
     """G2 for every layer at full per-layer shapes: run the stack layer by layer through the C ABI;
     the oracle gets the GPU's own bf16 layer input X_n and upstream gradient dY_n (emulating the
-    same bf16 storage points) and must match Y_n, dX_n and every gradient of the layer at 2e-2.
-    ReLU-gated gradients (a Linear feeding a ReLU) get 5e-2: the ReLU decision is taken on fp32 (GPU)
-    vs fp64 (oracle) pre-activations, and the few that sit within rounding of 0 flip (R22)."""
+    same bf16 storage points) and must match Y_n, dX_n and every gradient of the layer at 2e-2
+    (ReLU-gated ones included)."""
     import torch
     net = config(name)
     net = O.NetSpec(net.m0, net.d, net.layers[:layers])
@@ -197,13 +230,15 @@ def test_bf16_full_dims_layer_local(name, B, layers):
     torch.cuda.synchronize()
     for n in range(len(dims)):
         Yo, cache = O.layer_fwd(net, n, t2np(xs[n]), P[n], pr)
-        assert elem_err(t2np(xs[n + 1]), Yo) <= 2e-2, (n, elem_err(t2np(xs[n + 1]), Yo))
         dXo, go = O.layer_bwd(net, n, cache, t2np(dys[n]), P[n], pr)
-        if n > 0:
-            assert norm_err(t2np(dys[n - 1]), dXo) <= 2e-2, (n, norm_err(t2np(dys[n - 1]), dXo))
         gg = per_tensor(net, n, case.model.get_grads(n).astype(np.float64))
-        errs = {k: norm_err(gg[k], v) for k, v in go.items()}
-        bad = {k: e for k, e in errs.items() if e > (5e-2 if _gated(k) else 2e-2)}
+        errs = {"Y": elem_err(t2np(xs[n + 1]), Yo)}
+        if n > 0:
+            errs["dX"] = norm_err(t2np(dys[n - 1]), dXo)
+        errs.update({k: norm_err(gg[k], v) for k, v in go.items()})
+        top = sorted(errs.items(), key=lambda kv: -kv[1])[:4]
+        print(f"\nPARITY G2 full-dims {name} layer {n}: " + " ".join(f"{k} {e:.2e}" for k, e in top))
+        bad = {k: e for k, e in errs.items() if e > 2e-2}
         assert not bad, (n, bad, errs)
 
 

@@ -1,5 +1,5 @@
-"""Print one step of a DHEN_PROF_TRACE dump (op, stream, start, end) as a timeline, ops sorted by start;
-gap_us = idle time of that op's stream before it.  With DHEN_PROF_OVERLAP=1 the side stream is kept.
+"""Print one step of a per-op trace (DHEN.profile_trace / dhen_debug_profile_trace: op, stream, start, end) as a
+timeline, ops sorted by start; gap_us = idle time of that op's stream before it (profile(keep_overlap=True) keeps the side stream).
 Usage: timeline.py trace.csv steps"""
 import sys
 
