@@ -212,6 +212,7 @@ def main():
     ap.add_argument("--watchdog", action="store_true",
                     help="debug: run the libdhen_wd.so build (bounded mbarrier waits that report and trap)")
     ap.add_argument("--lib", default="", help="debug: load this library build instead (A/B experiments)")
+    ap.add_argument("--tuning", default="", help="schedule switches for A/B runs, e.g. sym=1,pair=0 (dhen_tuning)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -250,6 +251,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     model = binding.DHEN(cfg, rank=rank, world=world, nccl_id=nid)
+    if args.tuning:
+        model.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in args.tuning.split(","))})
     tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
     X0 = synth.make_x0(synth.SEED_BASE + 100 + rank, B, cfg.m0, cfg.d, bf16=(cfg.dtype == "bf16"))
     y = synth.make_labels(synth.SEED_BASE + 100 + rank, B)
@@ -411,6 +414,7 @@ def main():
         "config": {"workload": f"{args.config}: {configs.DESCR[args.config]}", "global_batch": Bg, "batch_per_gpu": B,
                    "m0": cfg.m0, "d": cfg.d, "layers": len(cfg.layers),
                    "parallelism": f"fsdp{world}" if world > 1 else "single",
+                   **({"tuning": args.tuning} if args.tuning else {}),
                    "l2": "flushed (256 MiB write) before every timed step"},
         "mfu": {"train_flops_per_sample": tf, "vs_burst": value * tf / (world * pk["tc"] * 1e12),
                 "vs_sustained": value * tf / (world * pk["tc_sus"] * 1e12)},

@@ -90,6 +90,9 @@ typedef struct {
   float ln_eps;           /* LayerNorm epsilon (0 -> 1e-5)                  */
   int batch_max_local;    /* largest per-rank B any call will use          */
   unsigned long long seed;/* parameter init seed                            */
+  int optimizer;          /* 0: SGD theta -= lr g (R18, default); 1: Adam (P:158's optimizer, NEXT#3): fp32
+                             moments on the master shard, PyTorch semantics, no weight decay                */
+  float adam_beta1, adam_beta2, adam_eps;   /* Adam (0 -> 0.9, 0.999, 1e-8)                          */
 } dhen_config;
 
 typedef struct {
@@ -100,6 +103,8 @@ typedef struct {
                                    ranks in ONE process on one GPU, one host thread and ctx per rank, collectives
                                    = host rendezvous + stream/event-ordered copies and fixed-order sums (a test
                                    backend for the FSDP path on a one-GPU machine; no CUDA-graph capture) */
+  int grad_bf16;                /* 1: gradients reduce-scattered in bf16 (the paper's quantized collectives,
+                                   P:158 / P:277: cast, bf16 sum, widened into the fp32 gradient shard); 0: fp32 */
 } dhen_dist;
 
 /* Host-only, pure: validates a config (preconditions S:186, S:195, S:204,
@@ -148,7 +153,8 @@ dhen_status dhen_layer_bwd(dhen_ctx* ctx, int layer, const void* dy, void* dx, i
 /* One training step on the local batch x0 [B][m0][d], labels [B] (0/1 fp32):
  * zero grads, forward all layers, head z_b = w_h . mean_t Y_N[b,t] + b_h,
  * loss = sum_b BCEWithLogits(z_b, y_b) / B_global (R17, R21), backward,
- * reduce-scatter (world > 1), SGD theta -= lr * g on fp32 masters (R18).
+ * reduce-scatter (world > 1), then the optimizer on the fp32 masters: SGD theta -= lr * g (R18), or Adam
+ * (cfg->optimizer = 1; its step count lives on the device, so graph replays stay correct).
  * loss_dev (nullable, fp32 device scalar) receives the loss of this rank's
  * samples (sum over ranks = global loss).  dx0 (nullable) receives dL/dx0. */
 dhen_status dhen_train_step(dhen_ctx* ctx, const void* x0, const float* labels, int B, int B_global,

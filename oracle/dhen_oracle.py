@@ -596,6 +596,36 @@ def train_step(net: NetSpec, params: List[Dict[str, np.ndarray]], X0: np.ndarray
 
 
 # --------------------------------------------------------------------------
+# Adam (NEXT#3; P:158 names the paper's optimizer only as a "BF16 optimizer"): the method variant the
+# library offers beside SGD (R18).  Kingma & Ba's update with PyTorch's torch.optim.Adam conventions
+# (bias-corrected moments, eps added to sqrt(v_hat), no weight decay), written out per element.
+# Pin: tests/test_oracle_modules.py::test_adam_matches_torch (the library routine, several steps).
+# --------------------------------------------------------------------------
+
+
+def adam_init(params: List[Dict[str, np.ndarray]]):
+    return {"t": 0, "m": [{k: np.zeros_like(v) for k, v in g.items()} for g in params],
+            "v": [{k: np.zeros_like(v) for k, v in g.items()} for g in params]}
+
+
+def adam_update(params, grads, state, lr: float, b1: float = 0.9, b2: float = 0.999, eps: float = 1e-8):
+    """Step t = state.t + 1:  m = b1 m + (1 - b1) g;  v = b2 v + (1 - b2) g^2;
+    theta -= lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps).  Returns (new params, new state)."""
+    t = state["t"] + 1
+    c1, c2 = 1.0 - b1 ** t, 1.0 - b2 ** t
+    new_p, new_m, new_v = [], [], []
+    for gi, grp in enumerate(params):
+        P, M, V = {}, {}, {}
+        for k, th in grp.items():
+            g = grads[gi][k]
+            M[k] = b1 * state["m"][gi][k] + (1.0 - b1) * g
+            V[k] = b2 * state["v"][gi][k] + (1.0 - b2) * g * g
+            P[k] = th - lr * (M[k] / c1) / (np.sqrt(V[k] / c2) + eps)
+        new_p.append(P); new_m.append(M); new_v.append(V)
+    return new_p, {"t": t, "m": new_m, "v": new_v}
+
+
+# --------------------------------------------------------------------------
 # FLOP accounting (A18; SURVEY §8(d): 2·M·N·K per contraction, forward only)
 # --------------------------------------------------------------------------
 

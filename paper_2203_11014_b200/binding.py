@@ -42,12 +42,13 @@ class dhen_layer(C.Structure):
 class dhen_config(C.Structure):
     _fields_ = [("m0", C.c_int), ("d", C.c_int), ("n_layers", C.c_int), ("layers", C.POINTER(dhen_layer)),
                 ("dtype", C.c_int), ("ln_eps", C.c_float), ("batch_max_local", C.c_int),
-                ("seed", C.c_ulonglong)]
+                ("seed", C.c_ulonglong), ("optimizer", C.c_int), ("adam_beta1", C.c_float),
+                ("adam_beta2", C.c_float), ("adam_eps", C.c_float)]
 
 
 class dhen_dist(C.Structure):
     _fields_ = [("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.c_ubyte * 128), ("fsdp", C.c_int),
-                ("backend", C.c_int)]
+                ("backend", C.c_int), ("grad_bf16", C.c_int)]
 
 
 NCCL, LOOPBACK = 0, 1   # dhen_dist.backend
@@ -157,6 +158,8 @@ class Config:
     batch_max_local: int = 1
     ln_eps: float = 1e-5
     seed: int = 0
+    optimizer: str = "sgd"            # "sgd" (R18) | "adam"
+    adam: Sequence[float] = (0.9, 0.999, 1e-8)
     _keep: list = field(default_factory=list, repr=False)
 
     def to_c(self) -> dhen_config:
@@ -178,7 +181,8 @@ class Config:
             keep.append(mods)
         self._keep = keep
         return dhen_config(self.m0, self.d, len(self.layers), C.cast(layers, C.POINTER(dhen_layer)),
-                           BF16 if self.dtype == "bf16" else FP32, self.ln_eps, self.batch_max_local, self.seed)
+                           BF16 if self.dtype == "bf16" else FP32, self.ln_eps, self.batch_max_local, self.seed,
+                           {"sgd": 0, "adam": 1}[self.optimizer], *[float(x) for x in self.adam])
 
     def dims(self):
         out, m = [], self.m0
@@ -190,9 +194,9 @@ class Config:
 
 
 def make_dist(rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, fsdp: bool = True,
-              backend: int = NCCL) -> dhen_dist:
+              backend: int = NCCL, grad_bf16: bool = False) -> dhen_dist:
     d = dhen_dist()
-    d.rank, d.world, d.fsdp, d.backend = rank, world, int(fsdp), int(backend)
+    d.rank, d.world, d.fsdp, d.backend, d.grad_bf16 = rank, world, int(fsdp), int(backend), int(grad_bf16)
     if nccl_id is not None:
         for k in range(128):
             d.nccl_id[k] = nccl_id[k]
@@ -285,12 +289,12 @@ class DHEN:
     torch uint8 CUDA tensors handed to the library (which carves them)."""
 
     def __init__(self, cfg: Config, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
-                 fsdp: bool = True, stream=None, backend: int = NCCL):
+                 fsdp: bool = True, stream=None, backend: int = NCCL, grad_bf16: bool = False):
         import torch
         self.torch = torch
         self.cfg = cfg
         self.lib = load()
-        self.dist = make_dist(rank, world, nccl_id, fsdp, backend)
+        self.dist = make_dist(rank, world, nccl_id, fsdp, backend, grad_bf16)
         self._c = cfg.to_c()
         sb, wb = sizes(cfg, self.dist)
         dev = torch.device("cuda", torch.cuda.current_device())

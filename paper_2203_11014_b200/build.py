@@ -92,5 +92,35 @@ def build(force: bool = False, verbose: bool = False, watchdog: bool = False) ->
     return lib_out
 
 
+def build_probe(n: int) -> str:
+    """Race-probe test build libdhen_probe<n>.so (tests/test_gpu_attn.py): attn_tc.cu recompiled with bounded
+    mbarrier waits (2 s) and delay injection (DHEN_RACE_PROBE = n: 1 current protocol, 2 round 1's dh = 64
+    backward protocol), linked with the default build's other objects."""
+    build()
+    flags, nd = _flags()
+    pdir = BUILD + f"_probe{n}"
+    os.makedirs(pdir, exist_ok=True)
+    src = os.path.join(CSRC, "attn_tc.cu")
+    obj = os.path.join(pdir, "attn_tc.cu.o")
+    out = os.path.join(HERE, f"libdhen_probe{n}.so")
+    if _deps_newer(obj, src) or not os.path.exists(out):
+        cmd = [NVCC] + flags + ["-DDHEN_WATCHDOG=1", "-DDHEN_WATCHDOG_NS=2000000000ull", f"-DDHEN_RACE_PROBE={n}",
+                                "-c", src, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+        objs = [obj] + [os.path.join(BUILD, os.path.basename(x) + ".o") for x in sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+                        if os.path.basename(x) != "attn_tc.cu"]
+        lib = os.path.join(nd, "lib")
+        r = subprocess.run([NVCC] + ARCH + ["-shared", "-o", out] + objs +
+                           ["-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}", "-lcuda"], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
+    return out
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, watchdog="--watchdog" in sys.argv))
+    if "--probe" in sys.argv:
+        print(build_probe(int(sys.argv[sys.argv.index("--probe") + 1])))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True, watchdog="--watchdog" in sys.argv))

@@ -29,6 +29,12 @@
 #include "gemm_tc_kernel.cuh"
 #include "tuning.h"
 
+// DHEN_RACE_PROBE (test builds only, build.py --probe N): 1 = delay injection on the current protocol,
+// 2 = the same delays on round 1's dh = 64 backward protocol.  0 in every product build.
+#ifndef DHEN_RACE_PROBE
+#define DHEN_RACE_PROBE 0
+#endif
+
 namespace dhen {
 namespace attn {
 
@@ -306,7 +312,16 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
         if (it + 1 < n) issueS(it + 1);   // the next item's softmax input goes first
         tc_after();
         mma_chain(tg + C_DK, sP, true, sQ(s), true, id_t, ROWS / 16);  // dK = dS^T Q
-        if (DH == 128) mbar_wait(B_(10), ph);  // dV read out of TMEM (dQ overlays it)
+        // dV of this item read out of TMEM by the output group.  For dh = 128 dQ overlays dV; for every dh the
+        // wait also keeps barrier 11 (dQ / dK done) from completing for this item before the output group has
+        // observed its completion for the previous one: the output group arrives on barrier 10 for item `it`
+        // only after its wait on barrier 11 for item it - 1.  Without it (round 1's dh = 64 kernel) two
+        // completions of barrier 11 could land while an output warp still waited on the first -- the phase
+        // parity then reads "not yet" forever (the intermittent C3 hang, tests/test_gpu_attn.py).
+#if DHEN_RACE_PROBE == 2
+        if (DH == 128)   // probe build 2: round 1's protocol (reproduces the hang, tests/test_gpu_attn.py)
+#endif
+        mbar_wait(B_(10), ph);
         tc_after();
         mma_chain(tg + C_DQ, sP, false, sK(s), true, id_q, ROWS / 16); // dQ = dS K
         mma_commit(B_(11));
@@ -395,6 +410,11 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_ws(const __grid_constant__ CU
         bulk_wait_read<0>();
         mbar_arrive(B_(14));
       }
+#if DHEN_RACE_PROBE
+      // probe builds: warps 11-13 look at barrier 11 only 20 us late (the leader warp on time), the schedule
+      // under which round 1's protocol lets barrier 11 complete twice unobserved
+      if (warp != 10) for (int k = 0; k < 20; ++k) __nanosleep(1000);
+#endif
       mbar_wait(B_(11), ph);   // dQ, dK done (Q, K of this item are dead)
       tc_after();
       for (int c = 0; c < NCH; ++c) stage_chunk(tl + C_DQ + 64 * c, sQ(s) + c * CHUNK);

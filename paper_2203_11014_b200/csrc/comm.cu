@@ -34,13 +34,14 @@ struct NcclComm final : Comm {
     bytes += (unsigned long long)(world - 1) * count * (dt == F32 ? 4 : 2);
     return chk(ncclAllGather(send, recv, count, dt == F32 ? ncclFloat32 : ncclBfloat16, c, st), "ncclAllGather");
   }
-  int reduce_scatter(const float* send, float* recv, size_t count, cudaStream_t st) override {
-    bytes += (unsigned long long)(world - 1) * count * 4;
-    return chk(ncclReduceScatter(send, recv, count, ncclFloat32, ncclSum, c, st), "ncclReduceScatter");
+  int reduce_scatter(const void* send, void* recv, size_t count, int dt, cudaStream_t st) override {
+    bytes += (unsigned long long)(world - 1) * count * (dt == F32 ? 4 : 2);
+    return chk(ncclReduceScatter(send, recv, count, dt == F32 ? ncclFloat32 : ncclBfloat16, ncclSum, c, st),
+               "ncclReduceScatter");
   }
-  int all_reduce(const float* send, float* recv, size_t count, cudaStream_t st) override {
-    bytes += 2ull * (unsigned long long)(world - 1) * count * 4 / (unsigned long long)world;
-    return chk(ncclAllReduce(send, recv, count, ncclFloat32, ncclSum, c, st), "ncclAllReduce");
+  int all_reduce(const void* send, void* recv, size_t count, int dt, cudaStream_t st) override {
+    bytes += 2ull * (unsigned long long)(world - 1) * count * (dt == F32 ? 4 : 2) / (unsigned long long)world;
+    return chk(ncclAllReduce(send, recv, count, dt == F32 ? ncclFloat32 : ncclBfloat16, ncclSum, c, st), "ncclAllReduce");
   }
   const char* name() const override { return "nccl"; }
 };
@@ -50,15 +51,16 @@ constexpr int kMaxLoop = 16;
 constexpr int kAG = 0, kRS = 1, kAR = 2;
 
 struct SumSrc {
-  const float* p[kMaxLoop];
+  const void* p[kMaxLoop];
   int n;
 };
-// dst[i] = src_0[i] + src_1[i] + ... (rank order: deterministic)
-__global__ void loop_sum_k(SumSrc s, float* __restrict__ dst, size_t count) {
+// dst[i] = src_0[i] + src_1[i] + ... (rank order: deterministic), in fp32; bf16 operands rounded once at the end
+template <typename T>
+__global__ void loop_sum_k(SumSrc s, T* __restrict__ dst, size_t count) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
-    float a = s.p[0][i];
-    for (int k = 1; k < s.n; ++k) a += s.p[k][i];
-    dst[i] = a;
+    float a = tof<T>(static_cast<const T*>(s.p[0])[i]);
+    for (int k = 1; k < s.n; ++k) a += tof<T>(static_cast<const T*>(s.p[k])[i]);
+    dst[i] = fromf<T>(a);
   }
 }
 
@@ -123,13 +125,17 @@ struct LoopComm final : Comm {
             return 1;
           }
     } else {
+      const size_t es = s0.dt == F32 ? 4 : 2;
       for (int r = 0; r < world; ++r) {
         SumSrc src;
         src.n = world;
         for (int k = 0; k < world; ++k)
-          src.p[k] = (const float*)g->slot[k].send + (s0.kind == kRS ? (size_t)r * n : 0);
+          src.p[k] = (const char*)g->slot[k].send + (s0.kind == kRS ? (size_t)r * n * es : 0);
         const int grid = (int)std::min<size_t>((n + 255) / 256, 148 * 8);
-        if (n) loop_sum_k<<<grid > 0 ? grid : 1, 256, 0, st>>>(src, (float*)g->slot[r].recv, n);
+        if (n) {
+          if (s0.dt == F32) loop_sum_k<float><<<grid > 0 ? grid : 1, 256, 0, st>>>(src, (float*)g->slot[r].recv, n);
+          else loop_sum_k<__nv_bfloat16><<<grid > 0 ? grid : 1, 256, 0, st>>>(src, (__nv_bfloat16*)g->slot[r].recv, n);
+        }
         ++g_launches;
       }
       if (cudaGetLastError() != cudaSuccess) { err = "loopback: sum kernel launch"; return 1; }
@@ -168,13 +174,13 @@ struct LoopComm final : Comm {
     bytes += (unsigned long long)(world - 1) * count * (dt == F32 ? 4 : 2);
     return collective(kAG, send, recv, count, dt, st);
   }
-  int reduce_scatter(const float* send, float* recv, size_t count, cudaStream_t st) override {
-    bytes += (unsigned long long)(world - 1) * count * 4;
-    return collective(kRS, send, recv, count, F32, st);
+  int reduce_scatter(const void* send, void* recv, size_t count, int dt, cudaStream_t st) override {
+    bytes += (unsigned long long)(world - 1) * count * (dt == F32 ? 4 : 2);
+    return collective(kRS, send, recv, count, dt, st);
   }
-  int all_reduce(const float* send, float* recv, size_t count, cudaStream_t st) override {
-    bytes += 2ull * (unsigned long long)(world - 1) * count * 4 / (unsigned long long)world;
-    return collective(kAR, send, recv, count, F32, st);
+  int all_reduce(const void* send, void* recv, size_t count, int dt, cudaStream_t st) override {
+    bytes += 2ull * (unsigned long long)(world - 1) * count * (dt == F32 ? 4 : 2) / (unsigned long long)world;
+    return collective(kAR, send, recv, count, dt, st);
   }
   const char* name() const override { return "loopback"; }
 };

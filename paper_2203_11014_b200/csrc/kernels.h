@@ -86,6 +86,12 @@ struct SgdSegs {
   int64_t n4[32];
 };
 cudaError_t sgd_multi(const SgdSegs& segs, float lr, cudaStream_t st);
+// Adam (Kingma & Ba; PyTorch torch.optim.Adam semantics, no weight decay) on an fp32 master shard with fp32
+// moments m, v; the step number t is read from *step (device; the update of step t uses t = *step + 1) and
+// the compute copy (dt) refreshed.  adam_count(step) increments *step afterwards (graph-replay safe).
+cudaError_t adam_step(float* master, const float* grad, float* m, float* v, void* copy, int dt, int64_t n, float lr,
+                      float b1, float b2, float eps, const int* step, cudaStream_t st);
+cudaError_t adam_count(int* step, cudaStream_t st);
 // parameter init: uniform(-bound, bound) from a counter-based hash of (seed, index), or a constant.
 // element i gets the value of tensor index idx0 + i (sharded init gives the same tensor at any world size)
 cudaError_t init_uniform(float* p, int64_t n, float bound, unsigned long long seed, unsigned long long stream_id,

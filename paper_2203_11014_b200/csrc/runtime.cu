@@ -27,6 +27,7 @@
 #include "gemm.h"
 #include "kernels.h"
 #include "attn.h"
+#include "dot_bwd.h"
 #include "comm.h"
 #include "tuning.h"
 
@@ -87,6 +88,7 @@ struct Group {
   void* comp = nullptr;                 // dtype copy [shard] (full when world == 1 / DP)
   float* grad = nullptr;                // fp32 [npad] full gradient (accumulated in bwd)
   float* gshard = nullptr;              // fp32 [shard] reduced gradient shard (world > 1)
+  float *adam_m = nullptr, *adam_v = nullptr;   // Adam moments [shard] (cfg.optimizer == 1)
   std::vector<int64_t> toff, tn;        // tensors: internal offset (64-element aligned), numel
   std::vector<int64_t> tcanon;          // tensors: offset in the dense canonical order (params_io)
   int64_t ncanon = 0;                   // canonical (dense) numel
@@ -161,7 +163,11 @@ struct dhen_ctx {
   bool vdy_now = false;               // set by train_step for the last layer's backward
   float *pooled = nullptr, *z = nullptr, *lossb = nullptr, *dz = nullptr;
   void* headw = nullptr;    // FSDP: the gathered head weight w_h, kept for the last layer's in-LN dY (vdy)
+  int* adam_t = nullptr;    // Adam: completed optimizer steps (device; the next update is step *adam_t + 1)
   float* gtmp = nullptr;    // fp32 [max_npad]: all-gather target of params_io / grads_get (world > 1)
+  void* gbf[2] = {nullptr, nullptr};   // bf16 reduce-scatter: [max_npad] bf16 gradient send buffers (ping-pong)
+  void* gbf_shard = nullptr;           //                      [max shard] bf16 receive buffer
+  cudaEvent_t ev_rs[2] = {nullptr, nullptr};   // the reduce-scatter that read gbf[k] has finished
   Comm* comm = nullptr;                // collectives (world > 1): NCCL or the in-process loopback (comm.h)
   // CUDA graph of dhen_train_step (dhen_train_step_graphed), keyed by its arguments
   cudaGraphExec_t gexec = nullptr;
@@ -237,6 +243,7 @@ static dhen_status validate(const dhen_config* c) {
   if (c->d > 1024) return fail(DHEN_E_CONFIG, "dhen_validate: d=%d > 1024", c->d);
   if (c->dtype != DHEN_FP32 && c->dtype != DHEN_BF16) return fail(DHEN_E_CONFIG, "dhen_validate: dtype=%d", c->dtype);
   if (c->batch_max_local < 1) return fail(DHEN_E_CONFIG, "dhen_validate: batch_max_local=%d", c->batch_max_local);
+  if (c->optimizer != 0 && c->optimizer != 1) return fail(DHEN_E_CONFIG, "dhen_validate: optimizer=%d (0 SGD, 1 Adam)", c->optimizer);
   int m = c->m0;
   for (int n = 0; n < c->n_layers; ++n) {
     const dhen_layer& L = c->layers[n];
@@ -359,9 +366,19 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
     g.comp = state.take(g.shard * es);
     g.grad = (float*)state.take(g.npad * 4);
     g.gshard = world > 1 ? (float*)state.take(g.shard * 4) : nullptr;
+    if (c->cfg.optimizer == 1) {
+      g.adam_m = (float*)state.take(g.shard * 4);
+      g.adam_v = (float*)state.take(g.shard * 4);
+    }
   }
+  if (c->cfg.optimizer == 1) c->adam_t = (int*)state.take(256);
   if (shard) { c->gathered[0] = state.take(c->max_npad * es); c->gathered[1] = state.take(c->max_npad * es); }
   if (world > 1) c->gtmp = (float*)state.take(c->max_npad * 4);
+  if (world > 1 && c->dist.grad_bf16) {
+    c->gbf[0] = state.take(c->max_npad * 2);
+    c->gbf[1] = state.take(c->max_npad * 2);
+    c->gbf_shard = state.take(c->max_npad * 2);
+  }
   // saved activations (work)
   m = c->cfg.m0;
   for (int n = 0; n < c->cfg.n_layers; ++n) {
@@ -612,8 +629,26 @@ static dhen_status reduce_grads(dhen_ctx* c, int gi, cudaStream_t st, cudaStream
     CK(cudaEventRecord(c->ev_grad2, also));
     CK(cudaStreamWaitEvent(c->comm_st, c->ev_grad2, 0));
   }
-  const int r = c->dist.fsdp ? c->comm->reduce_scatter(g.grad, g.gshard, (size_t)g.shard, c->comm_st)
-                             : c->comm->all_reduce(g.grad, g.gshard, (size_t)g.shard, c->comm_st);
+  if (c->dist.grad_bf16) {
+    // quantized gradient collective: the compute stream casts the fp32 gradient into one of two
+    // bf16 buffers (after the reduction that last read it), the communication stream reduces in bf16 and
+    // widens its shard into the fp32 gradient shard
+    const int k = gi & 1;
+    if (also && also != st) CK(cudaStreamWaitEvent(st, c->ev_grad2, 0));   // (trailing gradient sums)
+    CK(cudaStreamWaitEvent(st, c->ev_rs[k], 0));
+    KT("comm.grad_cast", 0, (double)g.npad * 6, cast(g.grad, F32, c->gbf[k], BF16, g.npad, st));
+    CK(cudaEventRecord(c->ev_grad, st));
+    CK(cudaStreamWaitEvent(c->comm_st, c->ev_grad, 0));
+    const size_t n = c->dist.fsdp ? (size_t)g.shard : (size_t)g.npad;
+    const int r = c->dist.fsdp ? c->comm->reduce_scatter(c->gbf[k], c->gbf_shard, n, BF16, c->comm_st)
+                               : c->comm->all_reduce(c->gbf[k], c->gbf_shard, n, BF16, c->comm_st);
+    if (r) return fail(DHEN_E_NCCL, "gradient reduction of group %d (%s): %s", gi, c->comm->name(), c->comm->err.c_str());
+    CK(cudaEventRecord(c->ev_rs[k], c->comm_st));
+    CK(cast(c->gbf_shard, BF16, g.gshard, F32, (int64_t)n, c->comm_st));
+    return DHEN_OK;
+  }
+  const int r = c->dist.fsdp ? c->comm->reduce_scatter(g.grad, g.gshard, (size_t)g.shard, F32, c->comm_st)
+                             : c->comm->all_reduce(g.grad, g.gshard, (size_t)g.shard, F32, c->comm_st);
   if (r) return fail(DHEN_E_NCCL, "gradient reduction of group %d (%s): %s", gi, c->comm->name(), c->comm->err.c_str());
   return DHEN_OK;
 }
@@ -948,6 +983,21 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         RET(G_(gw, c, sd, "dot.proj_wgrad", ws2));
         Gemm gz = mk(B, h, l * d, 1, operand(dU, dt, ldU, 1), operand(p(md.Wm), dt, 1, h), view(c->tA, dt, h, 1));
         RET(G_(gz, c, st, "dot.proj_dgrad"));
+        // dX_b (+)= S_b X_b with S built on chip from the packed dZ (no dense S in HBM): one kernel
+        if (c->tune.sym < 0 && dt == BF16 && dotb::supported(B, mi, d, h)) {
+          const int mode = (take_dR ? 1 : 0) + (emit_dX ? 2 : 0);
+          const void* rin = take_dR ? (const void*)c->dR : emit_dX ? (const void*)acc : nullptr;
+          void* out = emit_dX ? dX : (void*)acc;
+          // algorithmic bytes: dZ + X in; dX out (fp32 +=: read + write; first writer: dR in + fp32 out; emit: fp32
+          // acc or dR in + bf16 out)
+          const double rows_d = (double)B * mi * d;
+          const double io = mode == 0 ? 8.0 * rows_d : mode == 1 ? 6.0 * rows_d : mode == 2 ? 6.0 * rows_d : 4.0 * rows_d;
+          ProfScope ps(c, "dot.gram_bwd", 2.0 * B * (double)mi * mi * d, (double)B * h * es + rows_d * es + io, st);
+          CK(dotb::gram_bwd(c->tA, h, X, B, mi, d, mode, rin, out, st));
+          if (ps.rec >= 0) c->recs[ps.rec].tc = 1;
+          RET(join());
+          break;
+        }
         KT("dot.sym", 0, (double)B * (h + mi * mi) * es, sym_from_triu(c->tA, c->tD, dt, B, mi, h, st));
         // dX_b += S_b X_b
         Gemm gx = mk(mi, d, mi, B, operand(c->tD, dt, mi, 1, (int64_t)mi * mi), operand(X, dt, 1, d, (int64_t)mi * d),
@@ -1263,6 +1313,9 @@ static dhen_status make_ctx(const dhen_config* cfg, const dhen_dist* dist, dhen_
   if (dd.backend != 0 && dd.backend != 1) return fail(DHEN_E_CONFIG, "dhen: collective backend=%d (0 NCCL, 1 loopback)", dd.backend);
   c->cfg = *cfg;
   if (c->cfg.ln_eps <= 0.f) c->cfg.ln_eps = 1e-5f;
+  if (c->cfg.adam_beta1 <= 0.f) c->cfg.adam_beta1 = 0.9f;
+  if (c->cfg.adam_beta2 <= 0.f) c->cfg.adam_beta2 = 0.999f;
+  if (c->cfg.adam_eps <= 0.f) c->cfg.adam_eps = 1e-8f;
   c->mods_cfg.resize(cfg->n_layers);
   c->layers_cfg.resize(cfg->n_layers);
   for (int n = 0; n < cfg->n_layers; ++n) {
@@ -1357,6 +1410,7 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
     ok = ok && cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_grad2, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_cfork, cudaEventDisableTiming) == cudaSuccess;
+    for (int k = 0; k < 2; ++k) ok = ok && cudaEventCreateWithFlags(&c->ev_rs[k], cudaEventDisableTiming) == cudaSuccess;
     if (!ok) { dhen_destroy(c); return fail(DHEN_E_CUDA, "dhen_init: stream/event creation failed"); }
   }
   // parameter init: every rank initialises its own slice of the canonical vector
@@ -1383,7 +1437,13 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
     cudaError_t e3 = sgd_cast(g.master, nullptr, 0.f, g.comp, c->dt, g.shard, st);
     if (e3 != cudaSuccess) { delete c; return fail(DHEN_E_CUDA, "dhen_init: %s", cudaGetErrorString(e3)); }
     e3 = cudaMemsetAsync(g.grad, 0, g.npad * 4, st);
+    if (e3 == cudaSuccess && g.adam_m) e3 = cudaMemsetAsync(g.adam_m, 0, g.shard * 4, st);
+    if (e3 == cudaSuccess && g.adam_v) e3 = cudaMemsetAsync(g.adam_v, 0, g.shard * 4, st);
     if (e3 != cudaSuccess) { delete c; return fail(DHEN_E_CUDA, "dhen_init: %s", cudaGetErrorString(e3)); }
+  }
+  if (c->adam_t && cudaMemsetAsync(c->adam_t, 0, sizeof(int), st) != cudaSuccess) {
+    delete c;
+    return fail(DHEN_E_CUDA, "dhen_init: adam step counter");
   }
   c->launches0 = launches_before;
   if (fence_params(c, st) != DHEN_OK) { dhen_destroy(c); return DHEN_E_CUDA; }
@@ -1411,6 +1471,7 @@ void dhen_destroy(dhen_ctx* c) {
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
   if (c->ev_grad2) cudaEventDestroy(c->ev_grad2);
   if (c->ev_cfork) cudaEventDestroy(c->ev_cfork);
+  for (int k = 0; k < 2; ++k) if (c->ev_rs[k]) cudaEventDestroy(c->ev_rs[k]);
   if (c->comm_st) cudaStreamDestroy(c->comm_st);
   delete c->comm;
   delete c;
@@ -1662,7 +1723,20 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
     cur ^= 1;
   }
   RET(join_comm(c, st));
-  // B12: SGD on the (local shard of the) fp32 masters, refresh the compute copy
+  // B12: the optimizer on the (local shard of the) fp32 masters, refresh the compute copy
+  if (c->cfg.optimizer == 1) {   // Adam (NEXT#3): per group, then the device step counter
+    for (auto& g : c->G) {
+      const float* gr = c->dist.world > 1 ? g.gshard : g.grad;
+      KT("adam", 0, (double)g.shard * (20 + c->es),
+         adam_step(g.master, gr, g.adam_m, g.adam_v, g.comp, c->dt, g.shard, lr, c->cfg.adam_beta1, c->cfg.adam_beta2,
+                   c->cfg.adam_eps, c->adam_t, st));
+    }
+    CK(adam_count(c->adam_t, st));
+    RET(fence_params(c, st));
+    clear_bd(c);
+    CK(cudaGetLastError());
+    return DHEN_OK;
+  }
   bool multi = c->dt == BF16 && c->G.size() <= 32;
   for (auto& g : c->G) multi = multi && g.shard % 4 == 0;
   if (multi) {   // every group in one launch

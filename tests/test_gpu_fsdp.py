@@ -154,3 +154,59 @@ def test_fsdp_matches_oracle_bf16():
     for g, grp in enumerate(O.param_groups(net)):
         e = norm_err(many["grads"][g], O.flatten(grp, o["grads"][g]))
         assert e <= 2e-2, (g, e)
+
+
+def test_bf16_reduce_scatter():
+    """The paper's quantized gradient collective (dhen_dist.grad_bf16): gradients cast to bf16,
+    reduce-scattered in bf16 and widened into the fp32 shard.  Against the fp32 reduce-scatter of the same step:
+    every reduced gradient within bf16 rounding (norm 1e-2), parameters within lr times that, and the reduce-scatter
+    moves half the bytes."""
+    import threading as th
+    from paper_2203_11014_b200 import binding
+    net = small("C4")
+    B, world, seed, lr = 64, 2, 3, 0.05
+    flats = make_flat_params(net, seed)
+    X0, y = _inputs(net, B, "bf16", seed)
+    cfg = to_binding(net, "bf16", B // world)
+    outs = {}
+    for q in (False, True):
+        nid = binding.loopback_id()
+        out = [None] * world
+
+        def work(r):
+            import torch
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                m = binding.DHEN(cfg, rank=r, world=world, nccl_id=nid, backend=binding.LOOPBACK, grad_bf16=q,
+                                 stream=s)
+                for gi, f in enumerate(flats):
+                    m.set_params(gi, f, stream=s)
+                Bl = B // world
+                x0 = torch.tensor(X0[r * Bl:(r + 1) * Bl], device="cuda").to(torch.bfloat16).contiguous()
+                lab = torch.tensor(y[r * Bl:(r + 1) * Bl], device="cuda")
+                s.synchronize()
+                b0 = m.comm_bytes()
+                m.train_step(x0, lab, lr, B_global=B, stream=s)
+                s.synchronize()
+                b1 = m.comm_bytes()
+                out[r] = {"grads": [m.get_grads(g, stream=s) for g in range(len(flats))],
+                          "params": [m.get_params(g, stream=s) for g in range(len(flats))], "bytes": b1 - b0, "m": m}
+
+        ts = [th.Thread(target=work, args=(r,)) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(timeout=600)
+        assert all(o is not None for o in out)
+        outs[q] = out
+    eg = max(norm_err(a, b) for a, b in zip(outs[True][0]["grads"], outs[False][0]["grads"]))
+    ep = max(elem_err(a, b) for a, b in zip(outs[True][0]["params"], outs[False][0]["params"]))
+    print(f"\nbf16 reduce-scatter vs fp32: grads {eg:.2e} params {ep:.2e}")
+    gmax = max(float(np.abs(g).max()) for g in outs[False][0]["grads"])
+    assert eg <= 1e-2 and ep <= lr * 1e-2 * max(1.0, gmax)
+    from paper_2203_11014_b200 import binding as bd
+    sh = [bd.group_numel(cfg, g, bd.make_dist(0, world))[1] for g in range(len(net.layers) + 1)]
+    ag = sum(sh) + sum(sh[:len(net.layers) - 1])
+    assert outs[True][0]["bytes"] == (world - 1) * (ag * 2 + sum(sh) * 2)
+    assert outs[False][0]["bytes"] == (world - 1) * (ag * 2 + sum(sh) * 4)

@@ -13,7 +13,7 @@ relu_bits     FFN ReLU derivative from a bitmask                               -
 pair          CTA-pair GEMMs vs single-CTA tiles                               -> same sums up to split grouping
 fuse_db       bias gradients from GEMM epilogue column sums (DCN db, FFN db_1) -> same values, other grouping
 vdy           head dY formed inside the last LayerNorm backward (not stored)   -> bitwise identical
-sym           dot backward symmetrisation through a dense shared image         -> bitwise identical
+sym           dot backward: S on chip (-1) / dense S via a shared image (1, 2) / staged (0) -> bitwise identical
 tstore        TMA-store GEMM epilogue vs the register epilogue                 -> same values (db_1 grouping)
 """
 import numpy as np
@@ -132,3 +132,14 @@ def test_schedule_switches_bitwise(name, B, layers, switch):
     a = _step(net, B, 18, {switch: 0})
     b = _step(net, B, 18, {})
     _cmp(a, b, net, 1e-3 if switch == "tstore" else 0)
+
+
+@pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2)])
+def test_gram_bwd_onchip_matches_dense_s(name, B, layers):
+    """B5: the Gram backward with S built on chip from the packed dZ (sym = -1, dot_bwd_tc.cu) against the dense-S
+    path (S scattered to HBM by the symmetrisation kernel, then a batched GEMM): the same MMA chain over the same
+    bf16 operands (C2's two stacked samples add exact zeros), so loss, dX0 and every gradient agree bit for bit."""
+    net = _net(name, layers)
+    a = _step(net, B, 19, {"sym": 1})
+    b = _step(net, B, 19, {})
+    _cmp(a, b, net, 0)

@@ -355,3 +355,24 @@ def test_flop_formula_vs_torch_counter():
                     outs.append(torch.matmul(pp["W_u"].t(), X * A + X))
             X = torch.cat(outs, 1)
     assert fc.get_total_flops() == O.forward_flops_per_sample(net)
+
+
+# ------------------------------------------------------------------- Adam (NEXT#3)
+def test_adam_matches_torch():
+    """oracle.adam_update against the library routine torch.optim.Adam (fp64, 4 steps, several tensors)."""
+    rng = np.random.default_rng(3)
+    params = [{"a": rng.standard_normal((5, 7)), "b": rng.standard_normal(3)}, {"c": rng.standard_normal(11)}]
+    tp = [torch.tensor(v, dtype=torch.float64, requires_grad=True) for g in params for v in g.values()]
+    opt = torch.optim.Adam(tp, lr=0.01, betas=(0.8, 0.95), eps=1e-6)
+    st = O.adam_init(params)
+    for _ in range(4):
+        grads = [{k: rng.standard_normal(v.shape) for k, v in g.items()} for g in params]
+        flat = [gr for g in grads for gr in g.values()]
+        for t_, gr in zip(tp, flat):
+            t_.grad = torch.tensor(gr)
+        opt.step()
+        params, st = O.adam_update(params, grads, st, 0.01, 0.8, 0.95, 1e-6)
+        got = [v for g in params for v in g.values()]
+        for a, b in zip(got, tp):
+            assert np.abs(a - b.detach().numpy()).max() <= 1e-12
+    assert st["t"] == 4
