@@ -76,9 +76,15 @@ typedef struct {
   int mlp_hidden[2]; /* MLP: hidden widths (0 -> 1024)              */
 } dhen_module;
 
+typedef enum { DHEN_CONCAT = 0, DHEN_SUM = 1, DHEN_WSUM = 2 } dhen_ensemble;
+
 typedef struct {
   int n_modules;
-  const dhen_module* modules; /* ensemble = concat along tokens in this order */
+  const dhen_module* modules; /* in this order: concat offsets, canonical parameter order           */
+  int ensemble;               /* a dhen_ensemble value -- P:91 "concatenation, sum, or weighted sum": CONCAT along
+                                 tokens (R5, default); SUM or WSUM (one learnable scalar per module, R27,
+                                 initialised to 1) of the modules' outputs, which then need equal l_i and
+                                 give m_out = l                                                          */
 } dhen_layer;
 
 typedef struct {

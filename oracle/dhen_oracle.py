@@ -52,6 +52,10 @@ class ModuleSpec:
 @dataclass
 class LayerSpec:
     modules: List[ModuleSpec]
+    # Ensemble of Eq.(1) ("it can be concatenation, sum, or weighted sum"): "concat" along tokens (R5,
+    # the configs' reading), "sum" of the modules' outputs, or "wsum" = sum with one learnable scalar weight
+    # per module (R27; initialised to 1, so a fresh wsum layer computes the sum).  sum / wsum need equal l_i.
+    ensemble: str = "concat"
 
 
 @dataclass
@@ -63,10 +67,10 @@ class NetSpec:
 
 
 def layer_dims(net: NetSpec) -> List[Tuple[int, int]]:
-    """(m_in, m_out) per layer; m_out = Σ l_i (concat ensemble, R5)."""
+    """(m_in, m_out) per layer; m_out = Σ l_i (concat ensemble, R5), or the common l_i (sum / wsum)."""
     dims, m = [], net.m0
     for L in net.layers:
-        mo = sum(s.l for s in L.modules)
+        mo = sum(s.l for s in L.modules) if L.ensemble == "concat" else L.modules[0].l
         dims.append((m, mo))
         m = mo
     return dims
@@ -79,6 +83,10 @@ def validate(net: NetSpec) -> None:
     for (m_in, _), L in zip(layer_dims(net), net.layers):
         if not L.modules:
             raise ValueError("empty layer")
+        if L.ensemble not in ("concat", "sum", "wsum"):
+            raise ValueError(f"unknown ensemble {L.ensemble}")
+        if L.ensemble != "concat" and len({s.l for s in L.modules}) != 1:
+            raise ValueError("sum / weighted-sum ensembles need equal module output counts l_i")
         for s in L.modules:
             if s.kind not in KINDS:
                 raise ValueError(f"unknown kind {s.kind}")
@@ -132,6 +140,8 @@ def param_groups(net: NetSpec) -> List[List[Tuple[str, Tuple[int, ...], int]]]:
         for i, s in enumerate(L.modules):
             for name, shp, fan in module_param_shapes(s, m_in, net.d):
                 g.append((f"{i}.{s.kind}.{name}", shp, fan))
+        if L.ensemble == "wsum":
+            g.append(("ens_w", (len(L.modules),), 0))         # R27, initialised to 1
         if m_in != m_out:
             g.append(("W_n", (m_in, m_out), m_in))      # Eq.(2), R4
         g.append(("gamma", (net.d,), 0))
@@ -167,6 +177,8 @@ STORAGE_POINTS = (
     "params",
     # layer level
     "Y", "R", "dR", "dX",
+    # weighted-sum ensemble: each module's dU = w_i dR (R27)
+    "ens.dU",
     # head
     "head.dY",
     # modules
@@ -498,10 +510,16 @@ def layer_fwd(net: NetSpec, n: int, X: np.ndarray, P: Dict[str, np.ndarray], pr:
                     "conv": conv_fwd, "mlp": mlp_fwd}[s.kind](X, p, s, pr)
         us.append(U)
         caches.append(c)
-    Ucat = np.concatenate(us, axis=1)
+    if L.ensemble == "concat":
+        Ucat = np.concatenate(us, axis=1)
+    elif L.ensemble == "sum":
+        Ucat = sum(us)
+    else:
+        Ucat = sum(w * u for w, u in zip(P["ens_w"], us))
     R = Ucat + (X if m_in == m_out else tokmix_fwd(X, P["W_n"]))
     Y, mu, rstd = ln_fwd(R, P["gamma"], P["beta"], net.ln_eps)
-    cache = {"X": X, "mods": caches, "R": pr.q("R", R), "mu": mu, "rstd": rstd}
+    cache = {"X": X, "mods": caches, "R": pr.q("R", R), "mu": mu, "rstd": rstd,
+             "us": us if L.ensemble == "wsum" else None}
     return pr.q("Y", Y), cache
 
 
@@ -518,10 +536,17 @@ def layer_bwd(net: NetSpec, n: int, cache, dY: np.ndarray, P, pr: Precision = FP
     else:
         dX, g["W_n"] = tokmix_bwd(X, P["W_n"], dR)
     off = 0
+    if L.ensemble == "wsum":   # d(sum_i w_i U_i)/dw_i = <U_i, dR>
+        g["ens_w"] = np.array([(u * dR).sum() for u in cache["us"]])
     for i, s in enumerate(L.modules):
         p = _module_params(P, i, s.kind)
-        dU = dR[:, off:off + s.l, :]
-        off += s.l
+        if L.ensemble == "concat":
+            dU = dR[:, off:off + s.l, :]
+            off += s.l
+        elif L.ensemble == "sum":
+            dU = dR
+        else:
+            dU = pr.q("ens.dU", P["ens_w"][i] * dR)
         fn = {"dot": dot_bwd, "linear": linear_bwd, "dcn": dcn_bwd, "conv": conv_bwd,
               "attn": attn_bwd, "mlp": mlp_bwd}[s.kind]
         dXi, gi = fn(X, p, s, cache["mods"][i], dU, pr)

@@ -36,7 +36,10 @@ class dhen_module(C.Structure):
 
 
 class dhen_layer(C.Structure):
-    _fields_ = [("n_modules", C.c_int), ("modules", C.POINTER(dhen_module))]
+    _fields_ = [("n_modules", C.c_int), ("modules", C.POINTER(dhen_module)), ("ensemble", C.c_int)]
+
+
+ENSEMBLES = {"concat": 0, "sum": 1, "wsum": 2}   # dhen_ensemble
 
 
 class dhen_config(C.Structure):
@@ -159,6 +162,7 @@ class Config:
     ln_eps: float = 1e-5
     seed: int = 0
     optimizer: str = "sgd"            # "sgd" (R18) | "adam"
+    ensembles: Optional[Sequence[str]] = None   # per layer: "concat" (default) | "sum" | "wsum"
     adam: Sequence[float] = (0.9, 0.999, 1e-8)
     _keep: list = field(default_factory=list, repr=False)
 
@@ -178,6 +182,7 @@ class Config:
                 mods[i].mlp_hidden[1] = s.mlp_hidden[1]
             layers[n].n_modules = len(L)
             layers[n].modules = C.cast(mods, C.POINTER(dhen_module))
+            layers[n].ensemble = ENSEMBLES[self.ensembles[n]] if self.ensembles else 0
             keep.append(mods)
         self._keep = keep
         return dhen_config(self.m0, self.d, len(self.layers), C.cast(layers, C.POINTER(dhen_layer)),
@@ -186,8 +191,8 @@ class Config:
 
     def dims(self):
         out, m = [], self.m0
-        for L in self.layers:
-            mo = sum(s.l for s in L)
+        for n, L in enumerate(self.layers):
+            mo = sum(s.l for s in L) if not self.ensembles or self.ensembles[n] == "concat" else L[0].l
             out.append((m, mo))
             m = mo
         return out

@@ -2043,6 +2043,99 @@ cudaError_t adam_count(int* step, cudaStream_t st) {
   ++g_launches;
   return cudaGetLastError();
 }
+// ------------------------------------------------------------------ sum / weighted-sum ensembles (R27)
+// one warp per row; lane holds columns lane, lane + 32, ... (d <= 1024)
+__global__ void __launch_bounds__(256) ens_ln_fwd_k(EnsU U, const void* w, int pdt, const float* base32, const void* basex,
+                                                    const void* gamma, const void* beta, float eps, int64_t rows, int d,
+                                                    void* Y, void* R, float* mu, float* rstd, int dt) {
+  pdl_entry();
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  float wk[16];
+  for (int i = 0; i < U.k; ++i) wk[i] = w ? ld_as_f32(w, i, pdt) : 1.f;
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
+    float v[32];
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int c = lane + 32 * q;
+      v[q] = 0.f;
+      if (c < d) {
+        const int64_t o = r * d + c;
+        float a = base32 ? base32[o] : ld_as_f32(basex, o, dt);
+        for (int i = 0; i < U.k; ++i) a += wk[i] * U.u[i][o];
+        v[q] = a;
+        s += a;
+      }
+    }
+    const float mean = warp_sum(s) / d;
+    float s2 = 0.f;
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (lane + 32 * q < d) { const float t = v[q] - mean; s2 += t * t; }
+    const float rs = rsqrtf(warp_sum(s2) / d + eps);
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int c = lane + 32 * q;
+      if (c < d) {
+        const int64_t o = r * d + c;
+        st_from_f32(R, o, dt, v[q]);
+        st_from_f32(Y, o, dt, (v[q] - mean) * rs * ld_as_f32(gamma, c, dt) + ld_as_f32(beta, c, dt));
+      }
+    }
+    if (lane == 0) { mu[r] = mean; rstd[r] = rs; }
+  }
+}
+cudaError_t ens_ln_fwd(const EnsU& U, const void* w, int pdt, const float* base32, const void* basex, const void* gamma,
+                       const void* beta, float eps, int64_t rows, int d, void* Y, void* R, float* mu, float* rstd, int dt,
+                       cudaStream_t st) {
+  if (d > 1024 || U.k < 1 || U.k > 16 || (!base32 && !basex)) return cudaErrorInvalidValue;
+  pdl_launch(ens_ln_fwd_k, nblocks(rows, 8, 148 * 64), 256, 0, st, U, w, pdt, base32, basex, gamma, beta, eps, rows, d, Y, R,
+             mu, rstd, dt);
+  ++g_launches;
+  return cudaGetLastError();
+}
+__global__ void ens_scale_k(const void* dR, const void* w, int i, int pdt, void* out, int64_t n, int dt) {
+  pdl_entry();
+  const float a = ld_as_f32(w, i, pdt);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    st_from_f32(out, t, dt, a * ld_as_f32(dR, t, dt));
+}
+cudaError_t ens_scale(const void* dR, const void* w, int i, int pdt, void* out, int64_t n, int dt, cudaStream_t st) {
+  pdl_launch(ens_scale_k, nblocks(n), 256, 0, st, dR, w, i, pdt, out, n, dt);
+  ++g_launches;
+  return cudaGetLastError();
+}
+constexpr int ENS_DOT_BLOCKS = 592;
+__global__ void __launch_bounds__(256) ens_dot_k(const float* U, const void* dR, int dt, int64_t n, float* part) {
+  pdl_entry();
+  float s = 0.f;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    s += U[t] * ld_as_f32(dR, t, dt);
+  __shared__ float red[8];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = 0.f;
+    for (int q = 0; q < 8; ++q) a += red[q];
+    part[blockIdx.x] = a;
+  }
+}
+__global__ void ens_dot_fin_k(const float* part, int np, float* acc) {
+  pdl_entry();
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    float a = 0.f;
+    for (int q = 0; q < np; ++q) a += part[q];
+    *acc += a;
+  }
+}
+cudaError_t ens_dot(const float* U, const void* dR, int dt, int64_t n, float* acc, float* scratch, cudaStream_t st) {
+  pdl_launch(ens_dot_k, ENS_DOT_BLOCKS, 256, 0, st, U, dR, dt, n, scratch);
+  pdl_launch(ens_dot_fin_k, 1, 32, 0, st, (const float*)scratch, ENS_DOT_BLOCKS, acc);
+  g_launches += 2;
+  return cudaGetLastError();
+}
 cudaError_t sgd_multi(const SgdSegs& segs, float lr, cudaStream_t st) {
   int64_t tot = 0;
   for (int s = 0; s < segs.n; ++s) {

@@ -92,6 +92,17 @@ cudaError_t sgd_multi(const SgdSegs& segs, float lr, cudaStream_t st);
 cudaError_t adam_step(float* master, const float* grad, float* m, float* v, void* copy, int dt, int64_t n, float lr,
                       float b1, float b2, float eps, const int* step, cudaStream_t st);
 cudaError_t adam_count(int* step, cudaStream_t st);
+// Sum / weighted-sum ensemble (R27).  ens_ln_fwd: R = sum_i w_i U_i + base (w nullable = all 1; base = the
+// fp32 W_n projection `base32`, or the identity shortcut `basex` in dt), then the layer LayerNorm (two-pass
+// statistics) -> Y (dt), R (dt, saved), mu, rstd.  U: k fp32 [rows][d] buffers.
+struct EnsU { const float* u[16]; int k; };
+cudaError_t ens_ln_fwd(const EnsU& U, const void* w, int pdt, const float* base32, const void* basex, const void* gamma,
+                       const void* beta, float eps, int64_t rows, int d, void* Y, void* R, float* mu, float* rstd, int dt,
+                       cudaStream_t st);
+// out (dt) = w[i] (pdt) * dR (dt), n elements
+cudaError_t ens_scale(const void* dR, const void* w, int i, int pdt, void* out, int64_t n, int dt, cudaStream_t st);
+// *acc += sum_j U[j] dR[j] (fixed-order two-pass reduction through `scratch` >= 4 KB)
+cudaError_t ens_dot(const float* U, const void* dR, int dt, int64_t n, float* acc, float* scratch, cudaStream_t st);
 // parameter init: uniform(-bound, bound) from a counter-based hash of (seed, index), or a constant.
 // element i gets the value of tensor index idx0 + i (sharded init gives the same tensor at any world size)
 cudaError_t init_uniform(float* p, int64_t n, float bound, unsigned long long seed, unsigned long long stream_id,

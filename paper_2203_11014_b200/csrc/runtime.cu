@@ -78,6 +78,8 @@ struct Mod {
   // backward scratch of its own (not the shared tA / tC), so the module's data gradients never wait for an
   // earlier module's side-stream weight gradients: MLP dh2 / dh1, Conv dT
   void *dh2 = nullptr, *dh1 = nullptr, *dT = nullptr;
+  float* Uo = nullptr;   // sum / weighted-sum ensembles: this module's output U_i (fp32 [B][m_out][d], saved)
+  void* dUs = nullptr;   // weighted sum: this module's dU_i = bf16(w_i dR)
   bool bdT_pre = false, bdg_pre = false;   // built for this step by prebuild_bd (train_step, one launch)
   uint32_t* Fbits = nullptr;   // attention FFN ReLU bitmask [f / 32][B m] (FFN2 data gradient reads it, not F)
 };
@@ -98,8 +100,9 @@ struct Group {
 
 struct Layer {
   int m_in = 0, m_out = 0;
+  int ens = 0;               // dhen_ensemble
   std::vector<Mod> mods;
-  int64_t Wn = -1, gamma = -1, beta = -1;
+  int64_t Wn = -1, gamma = -1, beta = -1, ensw = -1;
   void* Y = nullptr;
   void* R = nullptr;
   float *mu = nullptr, *rstd = nullptr;
@@ -249,8 +252,13 @@ static dhen_status validate(const dhen_config* c) {
     const dhen_layer& L = c->layers[n];
     if (L.n_modules < 1 || !L.modules) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d has no modules", n);
     int mo = 0;
+    if (L.ensemble < DHEN_CONCAT || L.ensemble > DHEN_WSUM)
+      return fail(DHEN_E_CONFIG, "dhen_validate: layer %d ensemble=%d (0 concat, 1 sum, 2 weighted sum)", n, L.ensemble);
     for (int i = 0; i < L.n_modules; ++i) {
       const dhen_module& s = L.modules[i];
+      if (L.ensemble != DHEN_CONCAT && s.l != L.modules[0].l)
+        return fail(DHEN_E_CONFIG, "dhen_validate: layer %d sum ensemble with l=%d and l=%d (P:91 needs equal l_i)", n,
+                    L.modules[0].l, s.l);
       if (s.kind < DHEN_DOT || s.kind > DHEN_MLP) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d module %d kind=%d", n, i, s.kind);
       if (s.l < 1) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d module %d l=%d < 1", n, i, s.l);
       if (s.kind == DHEN_DOT && m < 2) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d Dot needs m >= 2, m=%d (S:186)", n, m);
@@ -260,6 +268,7 @@ static dhen_status validate(const dhen_config* c) {
         return fail(DHEN_E_CONFIG, "dhen_validate: layer %d conv_k=%d must be odd and <= 7 (S:204)", n, mdef(s.conv_k, 3));
       mo += s.l;
     }
+    if (L.ensemble != DHEN_CONCAT) mo = L.modules[0].l;
     m = mo;
   }
   return DHEN_OK;
@@ -284,6 +293,8 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
     Lr.m_in = m;
     int mo = 0;
     for (int i = 0; i < lc.n_modules; ++i) mo += lc.modules[i].l;
+    Lr.ens = lc.ensemble;
+    if (Lr.ens != DHEN_CONCAT) mo = lc.modules[0].l;
     Lr.m_out = mo;
     int64_t off = 0;
     int64_t coff = 0;
@@ -310,7 +321,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
       md.s.conv_k = mdef(md.s.conv_k, 3);
       md.s.mlp_hidden[0] = mdef(md.s.mlp_hidden[0], 1024);
       md.s.mlp_hidden[1] = mdef(md.s.mlp_hidden[1], 1024);
-      md.off_tok = tok;
+      md.off_tok = Lr.ens == DHEN_CONCAT ? tok : 0;   // sum ensembles: every module covers all m_out tokens
       tok += md.s.l;
       const int l = md.s.l;
       switch (md.s.kind) {
@@ -338,6 +349,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
       }
       Lr.mods.push_back(md);
     }
+    if (Lr.ens == DHEN_WSUM) Lr.ensw = tensor(lc.n_modules, 1, 0);   // R27: initialised to 1
     if (m != mo) Lr.Wn = tensor((int64_t)m * mo, 0, m);
     Lr.gamma = tensor(d, 1, 0);
     Lr.beta = tensor(d, 2, 0);
@@ -430,6 +442,8 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
         default: break;
       }
       md.bdT = work.take((size_t)128 * 128 * 8 * 2);   // spt m <= 1024 columns
+      if (Lr.ens != DHEN_CONCAT) md.Uo = (float*)work.take((size_t)B * mo * d * 4);
+      if (Lr.ens == DHEN_WSUM) md.dUs = work.take((size_t)B * mo * d * es);
       if (md.s.kind == DHEN_DCN) md.bdg = work.take((size_t)128 * 128 * 2);
     }
   }
@@ -664,7 +678,7 @@ static dhen_status join_comm(dhen_ctx* c, cudaStream_t st) {
 static bool layer_lnf(const dhen_ctx* c, int n, int B) {
   const Layer& Lr = c->L[n];
   const int d = c->d, mi = Lr.m_in, mo = Lr.m_out;
-  bool lnf = c->tune.ln_fuse && c->dt == BF16 && Lr.Wn < 0 && mi == mo && (d == 128 || d == 256);
+  bool lnf = c->tune.ln_fuse && c->dt == BF16 && Lr.Wn < 0 && mi == mo && (d == 128 || d == 256) && Lr.ens == DHEN_CONCAT;
   for (const Mod& m_ : Lr.mods) {
     if (!lnf) break;
     const int l_ = m_.s.l;
@@ -712,7 +726,8 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
   int mod_idx = 0;
   for (Mod& md : Lr.mods) {
     const int l = md.s.l;
-    float* Us = U + (int64_t)md.off_tok * d;
+    // (sum / weighted-sum ensembles: each module writes its own fp32 output, combined with the LayerNorm below)
+    float* Us = Lr.ens != DHEN_CONCAT ? md.Uo : U + (int64_t)md.off_tok * d;
     const bool on_side = use_side && md.s.kind != DHEN_ATTN && (has_attn || (mod_idx & 1));
     ++mod_idx;
     cudaStream_t st = on_side ? c->side_st : st0;   // this module's stream (shadows the layer stream)
@@ -864,8 +879,15 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
   }
   if (use_side) { CK(cudaEventRecord(c->ev_sj, c->side_st)); CK(cudaStreamWaitEvent(st0, c->ev_sj, 0)); }
   // F11 shortcut (Eq.(2)) + F12 LayerNorm
-  if (Lr.Wn >= 0) RET(tokmix_fwd(c, X, mi, p(Lr.Wn), mo, U, ldU, B, 1, st));
-  if (!lnf)
+  if (Lr.Wn >= 0) RET(tokmix_fwd(c, X, mi, p(Lr.Wn), mo, U, ldU, B, Lr.ens == DHEN_CONCAT ? 1 : 0, st));
+  if (Lr.ens != DHEN_CONCAT) {   // R = sum_i (w_i) U_i + shortcut, then the layer LayerNorm (R27)
+    EnsU eu;
+    eu.k = (int)Lr.mods.size();
+    for (int i = 0; i < eu.k; ++i) eu.u[i] = Lr.mods[i].Uo;
+    KT("layer.ens_ln", 0, (double)B * mo * d * (4.0 * eu.k + 2 * es + es),
+       ens_ln_fwd(eu, Lr.ens == DHEN_WSUM ? p(Lr.ensw) : nullptr, dt, Lr.Wn >= 0 ? U : nullptr, Lr.Wn >= 0 ? nullptr : X,
+                  p(Lr.gamma), p(Lr.beta), c->cfg.ln_eps, (int64_t)B * mo, d, Y, Lr.R, Lr.mu, Lr.rstd, dt, st));
+  } else if (!lnf)
     KT("layer.ln", 0, (double)B * mo * d * (4 + 2 * es) + (Lr.Wn >= 0 ? 0.0 : (double)B * mo * d * es), ln_fwd(U, Lr.Wn >= 0 ? nullptr : X, p(Lr.gamma), p(Lr.beta), dt, c->cfg.ln_eps, (int64_t)B * mo, d, Y, Lr.R, Lr.mu,
               Lr.rstd, dt, st));
   Lr.X = X;
@@ -968,7 +990,15 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   for (Mod* mdp : order) {
     Mod& md = *mdp;
     const int l = md.s.l;
-    char* dU = (char*)c->dR + (int64_t)md.off_tok * d * es;
+    char* dU = (char*)c->dR + (int64_t)md.off_tok * d * es;   // (sum ensembles: off_tok = 0, dU_i = dR)
+    if (Lr.ens == DHEN_WSUM) {   // dU_i = w_i dR;  dw_i += <U_i, dR>  (R27)
+      const int mi_idx = (int)(mdp - Lr.mods.data());
+      KT("layer.ens_bwd", 0, (double)rows * d * (2.0 * es),
+         ens_scale(c->dR, p(Lr.ensw), mi_idx, dt, md.dUs, (int64_t)B * mo * d, dt, st));
+      KT("layer.ens_bwd", 0, (double)B * mo * d * (4.0 + es),
+         ens_dot(md.Uo, c->dR, dt, (int64_t)B * mo * d, gp(Lr.ensw) + mi_idx, c->red, st));
+      dU = (char*)md.dUs;
+    }
     const bool take_dR = first_dR && first_mod;   // this module's first dX write adds the shortcut's dR
     const bool emit_dX = last_dX && mdp == order.back();   // this module's last dX write emits dX
     first_mod = false;
@@ -1321,6 +1351,7 @@ static dhen_status make_ctx(const dhen_config* cfg, const dhen_dist* dist, dhen_
   for (int n = 0; n < cfg->n_layers; ++n) {
     c->mods_cfg[n].assign(cfg->layers[n].modules, cfg->layers[n].modules + cfg->layers[n].n_modules);
     c->layers_cfg[n].n_modules = cfg->layers[n].n_modules;
+    c->layers_cfg[n].ensemble = cfg->layers[n].ensemble;
     c->layers_cfg[n].modules = c->mods_cfg[n].data();
   }
   c->cfg.layers = c->layers_cfg.data();

@@ -13,7 +13,8 @@ def to_binding(net: O.NetSpec, dtype: str, B: int, seed: int = 0):
     from paper_2203_11014_b200.binding import Config, Module
     layers = [[Module(s.kind, s.l, s.heads, s.ffn_mult, s.conv_channels, s.conv_k, tuple(s.mlp_hidden))
                for s in L.modules] for L in net.layers]
-    return Config(net.m0, net.d, layers, dtype=dtype, batch_max_local=B, ln_eps=net.ln_eps, seed=seed)
+    return Config(net.m0, net.d, layers, dtype=dtype, batch_max_local=B, ln_eps=net.ln_eps, seed=seed,
+                  ensembles=[L.ensemble for L in net.layers])
 
 
 def t2np(t):

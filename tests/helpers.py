@@ -55,7 +55,7 @@ def init_entries(group):
     for name, shp, fan in group:
         size = int(np.prod(shp))
         base = name.split(".")[-1]
-        if base in ("gamma", "g1", "g2"):
+        if base in ("gamma", "g1", "g2", "ens_w"):
             ent.append((size, ("one",)))
         elif base in ("beta", "be1", "be2"):
             ent.append((size, ("zero",)))

@@ -80,3 +80,24 @@ def test_sizes_scale_with_batch(B):
     # saved activations at C4's per-GPU batch fit one B200 (180 GB)
     s, w = B.sizes(_cfg(B, config("C4"), bmax=8192))
     assert s + w < 170e9, (s, w)
+
+
+@pytest.mark.parametrize("ens", ["sum", "wsum"])
+def test_ensemble_group_sizes_match_oracle(B, ens):
+    """Sum / weighted-sum ensembles: the library's canonical group sizes (ensemble weights between the
+    modules and W_n) equal the oracle's, and the 6 -> 5 token count (m_out = l) brings W_n."""
+    mods = [O.ModuleSpec("dot", 5), O.ModuleSpec("dcn", 5), O.ModuleSpec("linear", 5)]
+    net = O.NetSpec(6, 8, [O.LayerSpec(mods, ensemble=ens), O.LayerSpec(mods, ensemble=ens)])
+    cfg = _cfg(B, net)
+    for gi, g in enumerate(O.param_groups(net)):
+        n, _ = B.group_numel(cfg, gi)
+        assert n == O.group_size(g)
+    assert O.layer_dims(net) == [(6, 5), (5, 5)]
+
+
+def test_ensemble_validation_errors(B):
+    mods = [O.ModuleSpec("dot", 5), O.ModuleSpec("dcn", 4)]
+    net = O.NetSpec(6, 8, [O.LayerSpec(mods, ensemble="sum")])
+    with pytest.raises(B.DhenError) as e:
+        B.validate(_cfg(B, net))
+    assert "equal l_i" in str(e.value) or "sum ensemble" in str(e.value)

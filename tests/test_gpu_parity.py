@@ -339,3 +339,24 @@ def test_adam_steps_match_oracle(name, dtype, B, tol):
         errs = [elem_err(model.get_params(gi), O.flatten(g, params[gi])) for gi, g in enumerate(groups)]
         print(f"\nPARITY Adam {name} {dtype} step {step + 1}: params {max(errs):.2e}")
         assert max(errs) <= tol, (step, errs)
+
+
+def _ens_net(ens, proj):
+    l = 5 if proj else 12
+    mods = [M("dot", l), M("dcn", l), M("attn", l, heads=2), M("conv", l), M("linear", l),
+            M("mlp", l, mlp_hidden=(24, 20))]
+    return O.NetSpec(12, 16, [O.LayerSpec(mods, ensemble=ens), O.LayerSpec([M("dcn", l), M("linear", l)], ensemble=ens)])
+
+
+@pytest.mark.parametrize("ens", ["sum", "wsum"])
+@pytest.mark.parametrize("proj", [False, True])
+@pytest.mark.parametrize("dtype,tol", [("fp32", 1e-5), ("bf16", 2e-2)])
+def test_ensemble_variants_match_oracle(ens, proj, dtype, tol):
+    """NEXT#3 method variant: sum / weighted-sum ensembles of Eq.(1), every module kind, with and without
+    the W_n shortcut, full train step against the oracle (G1 fp32 1e-5, G3 bf16 2e-2; the learnable ensemble
+    weights are gradients like any other)."""
+    net = _ens_net(ens, proj)
+    case = Case(net, 24, dtype, seed=2203011014 + 9)
+    g = case.gpu_step(lr=0.05)
+    o = case.oracle_step(lr=0.05)
+    _compare(case, g, o, tol, tol, gated_report_only=(dtype == "bf16"), label=f"ensemble {ens} proj={proj} {dtype}")

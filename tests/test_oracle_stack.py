@@ -147,3 +147,81 @@ def test_bf16_emulation_is_close_and_exercised():
     _, caches = O.forward(net, O.compute_params(params, O.Precision(bf16=True)), X0, O.Precision(bf16=True))
     R = caches[0]["R"]
     assert np.array_equal(O.round_bf16(R), R)
+
+
+# ------------------------------------------------------------------- ensemble variants (R27; NEXT#3)
+def _ens_net(ens, shortcut_proj=False):
+    m0 = 6
+    l = 5 if shortcut_proj else 6                     # 6 -> 5 exercises W_n with a sum ensemble
+    mods = [M("dot", l), M("dcn", l), M("attn", l, heads=2), M("mlp", l, mlp_hidden=(12, 10))]
+    return O.NetSpec(m0, 8, [O.LayerSpec(mods, ensemble=ens), O.LayerSpec([M("linear", l), M("conv", l)],
+                                                                            ensemble=ens)])
+
+
+@pytest.mark.parametrize("ens", ["sum", "wsum"])
+@pytest.mark.parametrize("proj", [False, True])
+def test_ensemble_gradients_vs_finite_differences(ens, proj):
+    """Sum / weighted-sum ensembles: every gradient (the ensemble weights included) and dX0 against
+    central finite differences of the loss."""
+    net = _ens_net(ens, proj)
+    O.validate(net)
+    B = 3
+    params = oracle_params(net, make_flat_params(net, 12))
+    X0 = RNG.standard_normal((B, net.m0, net.d))
+    y = (RNG.random(B) < 0.5).astype(np.float64)
+    out = O.train_step(net, params, X0, y, lr=0.0)
+    h = 1e-6
+    for gi, grp in enumerate(params):
+        for k, v in grp.items():
+            flat = v.reshape(-1)
+            idx = RNG.choice(flat.size, size=min(3, flat.size), replace=False)
+            for j in idx:
+                old = flat[j]
+                flat[j] = old + h
+                lp = _loss(net, params, X0, y)
+                flat[j] = old - h
+                lm = _loss(net, params, X0, y)
+                flat[j] = old
+                fd = (lp - lm) / (2 * h)
+                an = out["grads"][gi][k].reshape(-1)[j]
+                assert abs(fd - an) <= 1e-4 * max(1e-2, abs(fd)) + 1e-7, (ens, k, j, fd, an)
+    b, i, c = 1, 2, 3
+    old = X0[b, i, c]
+    X0[b, i, c] = old + h
+    lp = _loss(net, params, X0, y)
+    X0[b, i, c] = old - h
+    lm = _loss(net, params, X0, y)
+    X0[b, i, c] = old
+    assert abs((lp - lm) / (2 * h) - out["dX0"][b, i, c]) <= 1e-4 * max(1e-2, abs((lp - lm) / (2 * h))) + 1e-7
+
+
+def test_ensemble_reductions():
+    """A 1-module sum / weighted-sum (w = 1) layer is the 1-module concat layer; a weighted sum with all w = 1
+    is the sum (outputs and every shared gradient); scaling one module's weight to 0 removes that module."""
+    X = RNG.standard_normal((3, 6, 8))
+    one = [M("dcn", 6)]
+    outs = []
+    for ens in ("concat", "sum", "wsum"):
+        net = O.NetSpec(6, 8, [O.LayerSpec(one, ensemble=ens)])
+        P = oracle_params(net, make_flat_params(net, 5, perturb_ln=False))[0]
+        outs.append(O.layer_fwd(net, 0, X, P)[0])
+    assert np.array_equal(outs[0], outs[1]) and np.allclose(outs[1], outs[2], atol=0, rtol=0)
+    mods = [M("linear", 6), M("dcn", 6), M("conv", 6)]
+    ns, nw = (O.NetSpec(6, 8, [O.LayerSpec(mods, ensemble=e)]) for e in ("sum", "wsum"))
+    Ps = oracle_params(ns, make_flat_params(ns, 6, perturb_ln=False))[0]
+    Pw = dict(Ps, ens_w=np.ones(3))
+    Ys, cs = O.layer_fwd(ns, 0, X, Ps)
+    Yw, cw = O.layer_fwd(nw, 0, X, Pw)
+    assert np.allclose(Ys, Yw, rtol=0, atol=1e-13)
+    dY = RNG.standard_normal(Ys.shape)
+    dXs, gs = O.layer_bwd(ns, 0, cs, dY, Ps)
+    dXw, gw = O.layer_bwd(nw, 0, cw, dY, Pw)
+    assert np.allclose(dXs, dXw, rtol=0, atol=1e-12)
+    for k, v in gs.items():
+        assert np.allclose(v, gw[k], rtol=0, atol=1e-12), k
+    # w_1 = 0: the layer equals the sum of modules 0 and 2
+    P0 = dict(Pw, ens_w=np.array([1.0, 0.0, 1.0]))
+    n2 = O.NetSpec(6, 8, [O.LayerSpec([mods[0], mods[2]], ensemble="sum")])
+    P2 = {k: v for k, v in Ps.items() if not k.startswith("1.")}
+    P2 = {k.replace("2.conv", "1.conv"): v for k, v in P2.items()}
+    assert np.allclose(O.layer_fwd(nw, 0, X, P0)[0], O.layer_fwd(n2, 0, X, P2)[0], rtol=0, atol=1e-13)
