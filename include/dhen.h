@@ -99,6 +99,10 @@ typedef struct {
   int optimizer;          /* 0: SGD theta -= lr g (R18, default); 1: Adam (P:158's optimizer, NEXT#3): fp32
                              moments on the master shard, PyTorch semantics, no weight decay                */
   float adam_beta1, adam_beta2, adam_eps;   /* Adam (0 -> 0.9, 0.999, 1e-8)                          */
+  int recompute;          /* activation recompute ("activation checkpointing", NEXT#2), bit mask:
+                             1 = the attention FFN hidden F (and its ReLU bitmask) is not kept from forward
+                             to backward: one shared buffer, F recomputed by the backward (one FFN1 GEMM per
+                             layer; at C4 16 GB less work memory); results are bit-identical            */
 } dhen_config;
 
 typedef struct {

@@ -46,7 +46,7 @@ class dhen_config(C.Structure):
     _fields_ = [("m0", C.c_int), ("d", C.c_int), ("n_layers", C.c_int), ("layers", C.POINTER(dhen_layer)),
                 ("dtype", C.c_int), ("ln_eps", C.c_float), ("batch_max_local", C.c_int),
                 ("seed", C.c_ulonglong), ("optimizer", C.c_int), ("adam_beta1", C.c_float),
-                ("adam_beta2", C.c_float), ("adam_eps", C.c_float)]
+                ("adam_beta2", C.c_float), ("adam_eps", C.c_float), ("recompute", C.c_int)]
 
 
 class dhen_dist(C.Structure):
@@ -163,6 +163,7 @@ class Config:
     seed: int = 0
     optimizer: str = "sgd"            # "sgd" (R18) | "adam"
     ensembles: Optional[Sequence[str]] = None   # per layer: "concat" (default) | "sum" | "wsum"
+    recompute: int = 0                # bit 1: attention FFN hidden recomputed in the backward (NEXT#2)
     adam: Sequence[float] = (0.9, 0.999, 1e-8)
     _keep: list = field(default_factory=list, repr=False)
 
@@ -187,7 +188,7 @@ class Config:
         self._keep = keep
         return dhen_config(self.m0, self.d, len(self.layers), C.cast(layers, C.POINTER(dhen_layer)),
                            BF16 if self.dtype == "bf16" else FP32, self.ln_eps, self.batch_max_local, self.seed,
-                           {"sgd": 0, "adam": 1}[self.optimizer], *[float(x) for x in self.adam])
+                           {"sgd": 0, "adam": 1}[self.optimizer], *[float(x) for x in self.adam], int(self.recompute))
 
     def dims(self):
         out, m = [], self.m0

@@ -82,7 +82,7 @@ __device__ __forceinline__ void mma_sx(uint32_t d, uint32_t a, uint32_t b, uint3
 }
 
 template <int D>
-__global__ void __launch_bounds__(320, 1) gram_bwd_kernel(const __grid_constant__ CUtensorMap xmap,
+__global__ void __maxnreg__(200) gram_bwd_kernel(const __grid_constant__ CUtensorMap xmap,
                                                           const __grid_constant__ CUtensorMap omap,
                                                           const __grid_constant__ Params p) {
   pdl_release();
@@ -193,16 +193,15 @@ __global__ void __launch_bounds__(320, 1) gram_bwd_kernel(const __grid_constant_
     const int rbase = q4 * 32;
     if (n > 0) build(0);
     for (int it = 0; it < n; ++it) {
-      if (it + 1 < n) build(it + 1);
       const int item = blockIdx.x + it * gridDim.x, ab = it & 1;
       const bool rows_ok = rbase < R;
       const int64_t grow = (int64_t)item * R + rbase + lane;   // this lane's row of [B m][d]
       const bool out_bf16 = p.mode >= 2;
       constexpr int HC = D / 2;
-      const int cw = out_bf16 ? 64 : 32;
-      // the first 32 columns' dR / accumulator row segment is loaded before the accumulator is ready (its latency
-      // hides under the MMA); every later 32-column piece loads its own
-      float pre[32];
+      // the first NPRE columns' dR / accumulator row segment is loaded before the next item's S is built and
+      // the accumulator is ready (its latency hides under both); every later 32-column piece loads its own
+      constexpr int NPRE = D == 128 ? 64 : 32;
+      float pre[NPRE];
       auto load_rin = [&](int col, float* f) {   // 32 columns of this lane's row of rin, as fp32
         if (p.mode == 2) {
           const float4* src = reinterpret_cast<const float4*>((const float*)p.rin + grow * p.d + col);
@@ -217,46 +216,48 @@ __global__ void __launch_bounds__(320, 1) gram_bwd_kernel(const __grid_constant_
           for (int q = 0; q < 4; ++q) unpack_bf8(__ldg(src + q), f + 8 * q);
         }
       };
-      if (p.mode != 0 && rows_ok) load_rin(hh * HC, pre);
+      if (p.mode != 0 && rows_ok) {
+        load_rin(hh * HC, pre);
+        if (NPRE == 64) load_rin(hh * HC + 32, pre + 32);
+      }
+      if (it + 1 < n) build(it + 1);
       mbar_wait(B_(8 + ab), (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t tq = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * D + hh * (D / 2));
-      for (int pc = 0; pc < HC; pc += cw) {   // one 128-B box row per pass: 32 fp32 or 64 bf16 columns
-        uint32_t pk[32];                        // the pass's output row, packed (fp32 bits, or bf16 pairs)
+      uint32_t pk[32];   // the current box row, packed (32 fp32 values, or 64 bf16 as pairs)
 #pragma unroll
-        for (int sub = 0; sub < 2; ++sub) {
-          if (sub == 1 && !out_bf16) break;
-          const int col = hh * HC + pc + 32 * sub;
-          uint32_t v[32];
-          ld_tmem32(tq + pc + 32 * sub, v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (pc + cw >= HC && (sub == 1 || !out_bf16)) {   // accumulator read: hand it back
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) arrive(B_(10 + ab));
-          }
-          if (!rows_ok) continue;
-          float* a = reinterpret_cast<float*>(v);
-          if (p.mode != 0) {
-            float f[32];
-            if (pc == 0 && sub == 0) {
-#pragma unroll
-              for (int e = 0; e < 32; ++e) f[e] = pre[e];
-            } else {
-              load_rin(col, f);
-            }
-#pragma unroll
-            for (int e = 0; e < 32; ++e) a[e] += f[e];
-          }
-          if (out_bf16) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) pk[16 * sub + e] = pack_bf2(a[2 * e], a[2 * e + 1]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) pk[e] = v[e];
-          }
+      for (int q = 0; q < HC / 32; ++q) {   // 32-column chunks; a box row holds 1 (fp32) or 2 (bf16) chunks
+        const int col = hh * HC + 32 * q;
+        uint32_t v[32];
+        ld_tmem32(tq + 32 * q, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (q == HC / 32 - 1) {   // accumulator read: hand it back
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) arrive(B_(10 + ab));
         }
         if (!rows_ok) continue;
+        float* a = reinterpret_cast<float*>(v);
+        if (p.mode != 0) {
+          float f[32];
+          if (32 * q < NPRE) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) f[e] = pre[(32 * q) % NPRE + e];
+          } else {
+            load_rin(col, f);
+          }
+#pragma unroll
+          for (int e = 0; e < 32; ++e) a[e] += f[e];
+        }
+        if (out_bf16) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pk[16 * (q & 1) + e] = pack_bf2(a[2 * e], a[2 * e + 1]);
+          if ((q & 1) == 0) continue;   // the box row is complete after the odd chunk
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) pk[e] = v[e];
+        }
+        const int bcol = out_bf16 ? col - 32 : col;   // first column of this box
         const uint32_t box = boxes + (uint32_t)((tsel & 1) * 4096);
         ++tsel;
         if (lane == 0) bulk_wait_read<1>();   // the store that last read this box is done with it
@@ -269,8 +270,8 @@ __global__ void __launch_bounds__(320, 1) gram_bwd_kernel(const __grid_constant_
         __syncwarp();
         if (lane == 0) {
           const int row0 = item * R + rbase;
-          if (p.mode == 0) tma_radd2d(&omap, box, hh * HC + pc, row0);
-          else tma_store2d(&omap, box, hh * HC + pc, row0);
+          if (p.mode == 0) tma_radd2d(&omap, box, bcol, row0);
+          else tma_store2d(&omap, box, bcol, row0);
           bulk_commit();
         }
       }

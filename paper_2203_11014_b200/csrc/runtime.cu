@@ -280,7 +280,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   const int world = c->dist.world;
   const bool shard = world > 1 && c->dist.fsdp;
   int m = c->cfg.m0, m_max = m, H_mm_max = 0, f_max = d, m_out_max = 0;
-  int64_t tC_elems = 0, tA_elems = 0, csum_elems = 0;
+  int64_t tC_elems = 0, tA_elems = 0, csum_elems = 0, fsh_elems = 0, fbsh_words = 0;
   bool has_attn_any = false;
   for (int n = 0; n < c->cfg.n_layers; ++n)
     for (int i = 0; i < c->cfg.layers[n].n_modules; ++i) has_attn_any |= c->cfg.layers[n].modules[i].kind == DHEN_ATTN;
@@ -418,8 +418,13 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
           md.O = work.take(tok * es);
           md.R1 = work.take(tok * es);
           md.Z1 = work.take(tok * es);
-          md.F = work.take((size_t)B * mi * f * es);
-          md.Fbits = (uint32_t*)work.take((size_t)B * mi * ((f + 31) / 32) * 4);
+          if (c->cfg.recompute & 1) {   // shared across layers (assigned below); recomputed by the backward
+            fsh_elems = std::max<int64_t>(fsh_elems, (int64_t)B * mi * f);
+            fbsh_words = std::max<int64_t>(fbsh_words, (int64_t)B * mi * ((f + 31) / 32));
+          } else {
+            md.F = work.take((size_t)B * mi * f * es);
+            md.Fbits = (uint32_t*)work.take((size_t)B * mi * ((f + 31) / 32) * 4);
+          }
           md.R2 = work.take(tok * es);
           md.T = work.take(tok * es);
           md.mu1 = (float*)work.take((size_t)B * mi * 4); md.rs1 = (float*)work.take((size_t)B * mi * 4);
@@ -446,6 +451,13 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
       if (Lr.ens == DHEN_WSUM) md.dUs = work.take((size_t)B * mo * d * es);
       if (md.s.kind == DHEN_DCN) md.bdg = work.take((size_t)128 * 128 * 2);
     }
+  }
+  if (fsh_elems) {   // recompute: one F / bitmask buffer for every attention module
+    void* F = work.take((size_t)fsh_elems * es);
+    uint32_t* Fb = (uint32_t*)work.take((size_t)fbsh_words * 4);
+    for (Layer& Lr : c->L)
+      for (Mod& md : Lr.mods)
+        if (md.s.kind == DHEN_ATTN) { md.F = F; md.Fbits = Fb; }
   }
   // scratch
   const size_t rows_d = (size_t)B * m_max * d;
@@ -957,7 +969,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
     switch (k) {
       case DHEN_DOT: return 1u | 8u;      // dZ (tA), S (tD)
       case DHEN_DCN: return 2u | 16u;     // dA (tB), dA column sums (bsum)
-      case DHEN_ATTN: return 1u | 2u | 4u | 8u | 32u | 64u | 128u | 256u | 512u;
+      case DHEN_ATTN: return 1u | 2u | 4u | 8u | 32u | 64u | 128u | 256u | 512u | 1024u;   // (1024: F, when shared)
       case DHEN_CONV: case DHEN_MLP: case DHEN_LINEAR: return 0u;   // own scratch / the dX accumulator
       default: return ~0u;
     }
@@ -965,7 +977,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   auto side_reads = [](int k) -> uint32_t {
     switch (k) {
       case DHEN_DCN: return 2u | 16u;     // dA, its column sums
-      case DHEN_ATTN: return 1u | 2u | 4u | 64u | 512u;   // dR2 (tA), dR1 (tB), dF (tC), dQKV (tF), db1 partials
+      case DHEN_ATTN: return 1u | 2u | 4u | 64u | 512u | 1024u;   // dR2 (tA), dR1 (tB), dF (tC), dQKV (tF), db1, F
       case DHEN_DOT: case DHEN_CONV: case DHEN_MLP: case DHEN_LINEAR: return 0u;   // saved / own buffers
       default: return ~0u;
     }
@@ -1131,6 +1143,14 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
           return DHEN_OK;
         };
         RET(fork());
+        if (c->cfg.recompute & 1) {   // NEXT#2: F (and its ReLU bitmask) recomputed from the saved Z1, bit-identical
+          Gemm f1 = mk((int)rows, f, d, 1, operand(md.Z1, dt, d, 1), operand(p(md.W1), dt, d, 1), view(md.F, dt, f, 1));
+          f1.e.bias = p(md.b1); f1.e.bias_dt = dt; f1.e.relu = 1;
+          if (c->tune.relu_bits && c->tune.tstore && dt == BF16 && f % 64 == 0 && f >= 128) {
+            f1.e.bits = md.Fbits; f1.e.bits_mode = 1; f1.e.bits_ld = rows;
+          }
+          RET(G_(f1, c, st, "attn.ffn1_recompute"));
+        }
         RET(tokmix_bwd(c, md.T, mi, p(md.Wu), l, dU, ldU, dT, dt, 0, gp(md.Wu), B, st, sd, ws2));
         void* dR2 = c->tA;   // [rows, d]
         KT("attn.ln2_bwd", 0, (double)rows * d * 3 * es, ln_bwd(dT, dt, md.R2, md.mu2, md.rs2, p(md.g2), dt, rows, d, dR2, dt, nullptr, 0, gp(md.g2), gp(md.be2), c->red,

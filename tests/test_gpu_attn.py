@@ -123,29 +123,34 @@ def test_relu_bitmask_matches_bf16_mask(m, d, B):
     assert np.array_equal(out["0"][2], out["1"][2])
 
 
-@pytest.mark.parametrize("m,d,B", [(128, 128, 48), (100, 128, 40)])
-def test_layernorm_epilogue_large_offset(m, d, B):
-    """The fused LayerNorm epilogue's row statistics (chunked mean / M2, Chan-merged) on pre-norm rows with a large
-    common offset (X0 = 1000 + N(0, 1): |mean| >> std) against the fp64 oracle (G2 protocol, storage points
-    emulated), for both the fused (ln_fuse = 1) and the LayerNorm-kernel (ln_fuse = 0) paths: a one-pass
-    E[v^2] - mean^2 form loses the variance here."""
+@pytest.mark.parametrize("d", [128, 256])
+def test_layernorm_epilogue_large_offset(d):
+    """The fused LayerNorm epilogue's row statistics (chunked mean / M2, Chan-merged across the warp pair) on
+    pre-norm rows with a large common offset: a Linear layer (m = l = 128, identity shortcut, the packed token
+    projection with the layer LN in its epilogue) on X0 = 1000 + N(0, 1), so R = X + W^T X has |mean| ~ 1e3
+    and std ~ 1.  The layer output Y of the fused path (ln_fuse = 1) and of the two-pass LayerNorm kernel
+    (ln_fuse = 0) against the fp64 oracle (storage points emulated) -- a one-pass E[v^2] - mean^2 loses the
+    variance here.  (Forward only: the backward recomputes x-hat from the bf16-stored R, which
+    both sides emulate but which is ill-conditioned at |mean| >> std by design.)"""
     import torch
-    net = _net(m, d)
-    errs = {}
+    net = O.NetSpec(128, d, [O.LayerSpec([M("linear", 128)])])
+    B = 16
+    ys = {}
     for mode in (0, 1):
         case = Case(net, B, "bf16", seed=55, tuning={"ln_fuse": mode})
         case.x0 = (case.x0.float() + 1000.0).to(torch.bfloat16).contiguous()
         case.X0 = t2np(case.x0)
-        y, dy, dx, gg = _layer(case, net)
+        y = torch.empty(B, 128, d, dtype=torch.bfloat16, device="cuda")
+        case.model.layer_fwd(0, case.x0, y)
+        torch.cuda.synchronize()
         pr = case.prec()
         P = O.compute_params(case.params, pr)[0]
-        Yo, cache = O.layer_fwd(net, 0, case.X0, P, pr)
-        dXo, go = O.layer_bwd(net, 0, cache, t2np(dy), P, pr)
-        errs[mode] = (elem_err(t2np(y), Yo), norm_err(t2np(dx), dXo))
-    print(f"\nLN offset m={m}: ln_fuse=0 Y {errs[0][0]:.2e} dX {errs[0][1]:.2e}; ln_fuse=1 Y {errs[1][0]:.2e} "
-          f"dX {errs[1][1]:.2e}")
-    for mode in (0, 1):
-        assert errs[mode][0] <= 2e-2 and errs[mode][1] <= 2e-2, errs
+        Yo, _ = O.layer_fwd(net, 0, case.X0, P, pr)
+        ys[mode] = (t2np(y), Yo)
+    e0, e1 = elem_err(*ys[0]), elem_err(*ys[1])
+    e01 = elem_err(ys[1][0], ys[0][0])
+    print(f"\nLN offset d={d}: Y vs oracle: ln_fuse=0 {e0:.2e} ln_fuse=1 {e1:.2e}; fused vs kernel {e01:.2e}")
+    assert e0 <= 2e-2 and e1 <= 2e-2 and e01 <= 2e-2, (e0, e1, e01)
 
 
 def _probe_run(lib):

@@ -143,3 +143,24 @@ def test_gram_bwd_onchip_matches_dense_s(name, B, layers):
     a = _step(net, B, 19, {"sym": 1})
     b = _step(net, B, 19, {})
     _cmp(a, b, net, 0)
+
+
+@pytest.mark.parametrize("name,B,layers", [("C3", 32, 2), ("C4", 16, 2)])
+def test_ffn_recompute_bitwise(name, B, layers):
+    """NEXT#2 activation recompute (dhen_config.recompute = 1): the attention FFN hidden F is kept in one shared
+    buffer and recomputed by the backward from the saved Z1 -- the same GEMM on the same operands, so loss,
+    dX0 and every gradient are bit-identical, with less work memory."""
+    from paper_2203_11014_b200 import binding
+    from tests.gpu_common import to_binding
+    net = _net(name, layers)
+    a = _step(net, B, 20, {})
+    cfg = to_binding(net, "bf16", B)
+    cfg.recompute = 1
+    case = Case(net, B, "bf16", seed=20)
+    model = binding.DHEN(cfg)
+    for g, f in enumerate(case.flats):
+        model.set_params(g, f)
+    case.model = model
+    b = case.gpu_step(lr=0.01)
+    _cmp(a, b, net, 0)
+    assert binding.sizes(cfg)[1] < binding.sizes(to_binding(net, "bf16", B))[1]

@@ -43,11 +43,22 @@ def full(path):
             "sm__inst_executed_pipe_tensor.sum", "launch__registers_per_thread", "launch__grid_size",
             "launch__block_size", "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "lts__t_bytes.sum", "smsp__inst_executed.sum"]
+    want += ["lts__t_sector_hit_rate.pct", "lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum",
+             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg.per_second"]
     for r in rows[2:]:
         print("---")
+        stalls = []
         for h, u, v in zip(hdr, units, r):
-            if h in want or h.startswith("sm__pipe_tensor") and "pct" in h:
+            if h in want or (("pipe_tensor" in h or "tmem" in h or "pipe_uma" in h or "tcgen" in h) and "pct" in h):
                 print(f"{h} [{u}] = {v}")
+            elif h.startswith("smsp__average_warp_latency_issue_stalled_") or \
+                    (h.startswith("smsp__warp_issue_stalled_") and h.endswith("per_warp_active.pct")):
+                try:
+                    stalls.append((float(v.replace(",", "")), h, u))
+                except ValueError:
+                    pass
+        for val, h, u in sorted(stalls, reverse=True)[:8]:
+            print(f"stall {h} [{u}] = {val}")
 
 
 def traffic(path, cfg, op, summary):
