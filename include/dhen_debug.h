@@ -61,6 +61,9 @@ typedef struct {
   int attn_fused;    /* 1: fused tcgen05 attention core (m <= 128, dh 64 / 128); 0: 2 GEMMs + softmax  (1) */
   int pdl;           /* 1: programmatic dependent launch on every library launch                        (0) */
   int gemm_simt;     /* 1: every GEMM on the exact-fp32 SIMT path (never in bf16 production)           (0) */
+  int dcn_fused;     /* 1: DCN backward as one kernel (dT, dA, dA W, partial dX kept in TMEM; bit-identical);
+                        0: two GEMMs with an fp32 partial dX in HBM.  Measured slower (C5 11.3 vs 11.0
+                        ms/step: its lane-per-row epilogue is load/store-unit bound)      (0) */
 } dhen_tuning;
 
 void dhen_tuning_default(dhen_tuning* t);

@@ -35,7 +35,7 @@ import numpy as np
 # --------------------------------------------------------------------------
 # configuration (the oracle's own; the product has its own C structs)
 # --------------------------------------------------------------------------
-KINDS = ("dot", "attn", "conv", "dcn", "linear", "mlp")
+KINDS = ("dot", "attn", "conv", "dcn", "linear", "mlp", "dcn_lit")
 
 
 @dataclass
@@ -112,6 +112,8 @@ def module_param_shapes(s: ModuleSpec, m: int, d: int) -> List[Tuple[str, Tuple[
         return [("W_m", (l * d, h), h)]
     if s.kind == "linear":
         return [("W", (m, l), m)]
+    if s.kind == "dcn_lit":   # Eq.(7) literally (R31): W ∈ R^{d×l}, the bias of the l output embeddings [l, d]
+        return [("W", (d, l), d), ("b", (l, d), d)]
     if s.kind == "dcn":
         return [("W", (d, d), d), ("b", (d,), d), ("W_u", (m, l), m)]
     if s.kind == "conv":
@@ -179,6 +181,8 @@ STORAGE_POINTS = (
     "Y", "R", "dR", "dX",
     # weighted-sum ensemble: each module's dU = w_i dR (R27)
     "ens.dU",
+    # paper-literal DCN (R31): the per-sample d x d Gram and the symmetrised dG
+    "dcnl.G", "dcnl.S",
     # head
     "head.dY",
     # modules
@@ -325,6 +329,26 @@ def dcn_bwd(X, p, s, c, dU, pr):
     dW = dA.reshape(-1, dA.shape[-1]).T @ X.reshape(-1, X.shape[-1])
     db = dA.reshape(-1, dA.shape[-1]).sum(0)
     return dX, {"W": dW, "b": db, "W_u": dWu}
+
+
+def dcn_lit_fwd(X, p, s, pr):
+    """Eq.(7) read literally (NEXT#3; R31 after SPEC S:219-222 / S:235): per sample the d x d
+    Gram over tokens G = X_n X_nᵀ (X_n = Xᵀ is d x m, so G[c][k] = Σ_i X[i][c] X[i][k]), u = G W + b with
+    W ∈ R^{d×l}; the columns of u are the l output embeddings, U[t][c] = (G W)[c][t] + b[t][c]."""
+    G = pr.q("dcnl.G", np.einsum("bic,bik->bck", X, X))
+    U = np.einsum("bck,kt->btc", G, p["W"]) + p["b"]
+    return U, {"G": G}
+
+
+def dcn_lit_bwd(X, p, s, c, dU, pr):
+    """dW[k][t] = Σ_b Σ_c G[c][k] dU[t][c];  db = Σ_b dU;  dG[c][k] = Σ_t dU[t][c] W[k][t];
+    dX = X (dG + dGᵀ)  (G = XᵀX)."""
+    G = c["G"]
+    dW = np.einsum("bck,btc->kt", G, dU)
+    db = dU.sum(0)
+    dG = np.einsum("btc,kt->bck", dU, p["W"])
+    S = pr.q("dcnl.S", dG + dG.transpose(0, 2, 1))
+    return X @ S, {"W": dW, "b": db}
 
 
 def _corr2d_same(img, ker):
@@ -506,7 +530,7 @@ def layer_fwd(net: NetSpec, n: int, X: np.ndarray, P: Dict[str, np.ndarray], pr:
         if s.kind == "attn":
             U, c = attn_fwd(X, p, s, pr, net.ln_eps)
         else:
-            U, c = {"dot": dot_fwd, "linear": linear_fwd, "dcn": dcn_fwd,
+            U, c = {"dot": dot_fwd, "linear": linear_fwd, "dcn": dcn_fwd, "dcn_lit": dcn_lit_fwd,
                     "conv": conv_fwd, "mlp": mlp_fwd}[s.kind](X, p, s, pr)
         us.append(U)
         caches.append(c)
@@ -547,7 +571,7 @@ def layer_bwd(net: NetSpec, n: int, cache, dY: np.ndarray, P, pr: Precision = FP
             dU = dR
         else:
             dU = pr.q("ens.dU", P["ens_w"][i] * dR)
-        fn = {"dot": dot_bwd, "linear": linear_bwd, "dcn": dcn_bwd, "conv": conv_bwd,
+        fn = {"dot": dot_bwd, "linear": linear_bwd, "dcn": dcn_bwd, "dcn_lit": dcn_lit_bwd, "conv": conv_bwd,
               "attn": attn_bwd, "mlp": mlp_bwd}[s.kind]
         dXi, gi = fn(X, p, s, cache["mods"][i], dU, pr)
         dX = dX + dXi
@@ -665,6 +689,8 @@ def forward_flops_per_sample(net: NetSpec) -> int:
                 tot += 2 * m_in * m_in * d + 2 * h * l * d
             elif s.kind == "linear":
                 tot += 2 * m_in * l * d
+            elif s.kind == "dcn_lit":
+                tot += 2 * d * d * m_in + 2 * d * d * l
             elif s.kind == "dcn":
                 tot += 2 * m_in * d * d + 2 * m_in * l * d
             elif s.kind == "conv":

@@ -13,8 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdhen.so")
 WD_LIB_PATH = os.path.join(HERE, "libdhen_wd.so")   # debug build: bounded mbarrier waits (build.py --watchdog)
 
-DOT, ATTN, CONV, DCN, LINEAR, MLP = range(6)
-KIND_IDS = {"dot": DOT, "attn": ATTN, "conv": CONV, "dcn": DCN, "linear": LINEAR, "mlp": MLP}
+DOT, ATTN, CONV, DCN, LINEAR, MLP, DCN_LIT = range(7)
+KIND_IDS = {"dot": DOT, "attn": ATTN, "conv": CONV, "dcn": DCN, "linear": LINEAR, "mlp": MLP, "dcn_lit": DCN_LIT}
 FP32, BF16 = 0, 1
 
 STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_SHAPE", 3: "E_ALIGN", 4: "E_STATE", 5: "E_CUDA", 6: "E_NCCL",
@@ -66,7 +66,7 @@ class dhen_tuning(C.Structure):
     """Schedule / fusion switches of one context (include/dhen_debug.h); defaults = measured best."""
     _fields_ = [(n, C.c_int) for n in ("overlap", "defer_join", "ln_fuse", "first_writer", "relu_bits", "fuse_db",
                                          "vdy", "trail", "bd_pre", "sym", "tstore", "pair", "pair_k", "attn_fused",
-                                         "pdl", "gemm_simt")]
+                                         "pdl", "gemm_simt", "dcn_fused")]
 
 
 class DhenError(RuntimeError):

@@ -82,7 +82,7 @@ __device__ __forceinline__ void mma_sx(uint32_t d, uint32_t a, uint32_t b, uint3
 }
 
 template <int D>
-__global__ void __maxnreg__(200) gram_bwd_kernel(const __grid_constant__ CUtensorMap xmap,
+__global__ void __launch_bounds__(320, 1) gram_bwd_kernel(const __grid_constant__ CUtensorMap xmap,
                                                           const __grid_constant__ CUtensorMap omap,
                                                           const __grid_constant__ Params p) {
   pdl_release();

@@ -2136,6 +2136,25 @@ cudaError_t ens_dot(const float* U, const void* dR, int dt, int64_t n, float* ac
   g_launches += 2;
   return cudaGetLastError();
 }
+// S = dG + dG^T per sample (32 x 32 tiles through shared memory: both reads coalesced)
+__global__ void sym_add_k(const float* __restrict__ dG, void* S, int dt, int d) {
+  pdl_entry();
+  __shared__ float tl[32][33];
+  const int64_t base = (int64_t)blockIdx.z * d * d;
+  const int c0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y)   // tile (k0.., c0..) transposed into tl[c][k]
+    if (k0 + r < d && c0 + threadIdx.x < d) tl[threadIdx.x][r] = dG[base + (int64_t)(k0 + r) * d + c0 + threadIdx.x];
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int c = c0 + r, k = k0 + threadIdx.x;
+    if (c < d && k < d) st_from_f32(S, base + (int64_t)c * d + k, dt, dG[base + (int64_t)c * d + k] + tl[r][threadIdx.x]);
+  }
+}
+cudaError_t sym_add(const float* dG, void* S, int dt, int B, int d, cudaStream_t st) {
+  pdl_launch(sym_add_k, dim3((d + 31) / 32, (d + 31) / 32, B), dim3(32, 8), 0, st, dG, S, dt, d);
+  ++g_launches;
+  return cudaGetLastError();
+}
 cudaError_t sgd_multi(const SgdSegs& segs, float lr, cudaStream_t st) {
   int64_t tot = 0;
   for (int s = 0; s < segs.n; ++s) {

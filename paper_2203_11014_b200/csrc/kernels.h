@@ -99,6 +99,8 @@ struct EnsU { const float* u[16]; int k; };
 cudaError_t ens_ln_fwd(const EnsU& U, const void* w, int pdt, const float* base32, const void* basex, const void* gamma,
                        const void* beta, float eps, int64_t rows, int d, void* Y, void* R, float* mu, float* rstd, int dt,
                        cudaStream_t st);
+// paper-literal DCN backward (R31): S[b][c][k] = dG[b][c][k] + dG[b][k][c] (fp32 in, dt out), d x d per sample
+cudaError_t sym_add(const float* dG, void* S, int dt, int B, int d, cudaStream_t st);
 // out (dt) = w[i] (pdt) * dR (dt), n elements
 cudaError_t ens_scale(const void* dR, const void* w, int i, int pdt, void* out, int64_t n, int dt, cudaStream_t st);
 // *acc += sum_j U[j] dR[j] (fixed-order two-pass reduction through `scratch` >= 4 KB)

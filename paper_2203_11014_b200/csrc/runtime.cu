@@ -28,6 +28,7 @@
 #include "kernels.h"
 #include "attn.h"
 #include "dot_bwd.h"
+#include "dcn_bwd.h"
 #include "comm.h"
 #include "tuning.h"
 
@@ -78,6 +79,8 @@ struct Mod {
   // backward scratch of its own (not the shared tA / tC), so the module's data gradients never wait for an
   // earlier module's side-stream weight gradients: MLP dh2 / dh1, Conv dT
   void *dh2 = nullptr, *dh1 = nullptr, *dT = nullptr;
+  void *G = nullptr, *S = nullptr;   // paper-literal DCN: saved d x d Gram per sample (dt), symmetrised dG (dt)
+  float* dGf = nullptr;              //                    dG (fp32 scratch)
   float* Uo = nullptr;   // sum / weighted-sum ensembles: this module's output U_i (fp32 [B][m_out][d], saved)
   void* dUs = nullptr;   // weighted sum: this module's dU_i = bf16(w_i dR)
   bool bdT_pre = false, bdg_pre = false;   // built for this step by prebuild_bd (train_step, one launch)
@@ -259,7 +262,7 @@ static dhen_status validate(const dhen_config* c) {
       if (L.ensemble != DHEN_CONCAT && s.l != L.modules[0].l)
         return fail(DHEN_E_CONFIG, "dhen_validate: layer %d sum ensemble with l=%d and l=%d (P:91 needs equal l_i)", n,
                     L.modules[0].l, s.l);
-      if (s.kind < DHEN_DOT || s.kind > DHEN_MLP) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d module %d kind=%d", n, i, s.kind);
+      if (s.kind < DHEN_DOT || s.kind > DHEN_DCN_LIT) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d module %d kind=%d", n, i, s.kind);
       if (s.l < 1) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d module %d l=%d < 1", n, i, s.l);
       if (s.kind == DHEN_DOT && m < 2) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d Dot needs m >= 2, m=%d (S:186)", n, m);
       if (s.kind == DHEN_ATTN && c->d % mdef(s.heads, 2) != 0)
@@ -339,6 +342,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
           md.Wu = tensor((int64_t)m * l, 0, m);
           break;
         }
+        case DHEN_DCN_LIT: md.W = tensor((int64_t)d * l, 0, d); md.b = tensor((int64_t)l * d, 0, d); break;
         case DHEN_MLP: {
           int h1 = md.s.mlp_hidden[0], h2 = md.s.mlp_hidden[1];
           md.W1 = tensor((int64_t)h1 * m * d, 0, m * d); md.b1 = tensor(h1, 0, m * d);
@@ -409,6 +413,11 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
           tA_elems = std::max<int64_t>(tA_elems, (int64_t)B * (mi * (mi - 1) / 2));
           break;
         case DHEN_DCN: md.A = work.take(tok * es); md.T = work.take(tok * es); break;
+        case DHEN_DCN_LIT:
+          md.G = work.take((size_t)B * d * d * es);
+          md.S = work.take((size_t)B * d * d * es);
+          md.dGf = (float*)work.take((size_t)B * d * d * 4);
+          break;
         case DHEN_CONV: md.T = work.take(tok * es); md.dT = work.take(tok * es); break;
         case DHEN_ATTN: {
           int H = md.s.heads, f = md.s.ffn_mult * d;
@@ -485,7 +494,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   c->ws2.ptr = (float*)work.take(c->ws2.bytes);
   c->red2 = (float*)work.take(c->red_bytes);
   c->red3 = (float*)work.take(c->red_bytes);
-  c->bsum = (float*)work.take((size_t)2 * 148 * 256 * 4);   // DCN bias partial rows [<= 296 CTAs][d <= 256]
+  c->bsum = (float*)work.take((size_t)4 * 148 * 256 * 4);   // DCN bias partial rows [<= 592][d <= 256]
   if (csum_elems) c->csum = (float*)work.take((size_t)csum_elems * 4);   // attention db_1 partial rows
   c->pooled = (float*)work.take(((size_t)B * d + (size_t)B * (d + 2)) * 4);   // + head partials [B][d + 2]
   c->z = (float*)work.take((size_t)B * 4);
@@ -691,6 +700,7 @@ static bool layer_lnf(const dhen_ctx* c, int n, int B) {
   const Layer& Lr = c->L[n];
   const int d = c->d, mi = Lr.m_in, mo = Lr.m_out;
   bool lnf = c->tune.ln_fuse && c->dt == BF16 && Lr.Wn < 0 && mi == mo && (d == 128 || d == 256) && Lr.ens == DHEN_CONCAT;
+  for (const Mod& m_ : Lr.mods) lnf = lnf && m_.s.kind != DHEN_DCN_LIT;   // (its output goes through the fp32 concat)
   for (const Mod& m_ : Lr.mods) {
     if (!lnf) break;
     const int l_ = m_.s.l;
@@ -866,6 +876,16 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
         RET(emit_tm(md.T, p(md.Wu)));
         break;
       }
+      case DHEN_DCN_LIT: {   // Eq.(7) literally (R31): G_b = X_b^T X_b (d x d), U_b = W^T G_b + b
+        Gemm g = mk(d, d, mi, B, operand(X, dt, 1, d, (int64_t)mi * d), operand(X, dt, 1, d, (int64_t)mi * d),
+                    view(md.G, dt, d, 1, (int64_t)d * d));
+        RET(G_(g, c, st, "dcnl.gram"));
+        Gemm u = mk(l, d, d, B, operand(p(md.W), dt, 1, l), operand(md.G, dt, 1, d, (int64_t)d * d),
+                    view(Us, F32, d, 1, ldU));
+        u.e.resid = view(p(md.b), dt, d, 1, 0);   // the [l][d] bias, the same for every sample
+        RET(G_(u, c, st, "dcnl.proj"));
+        break;
+      }
       case DHEN_MLP: {   // F9
         const int h1 = md.s.mlp_hidden[0], h2 = md.s.mlp_hidden[1];
         const int K1 = mi * d;
@@ -932,7 +952,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   std::vector<Mod*> order;
   {
     int best = -1, best_rank = 99;
-    const int rank_of[6] = {3 /*DOT*/, 99 /*ATTN*/, 99 /*CONV*/, 0 /*DCN*/, 1 /*LINEAR*/, 2 /*MLP*/};
+    const int rank_of[7] = {3 /*DOT*/, 99 /*ATTN*/, 99 /*CONV*/, 0 /*DCN*/, 1 /*LINEAR*/, 2 /*MLP*/, 99 /*DCN_LIT*/};
     for (int i = 0; i < (int)Lr.mods.size(); ++i) {
       const int rk = rank_of[Lr.mods[i].s.kind];
       if (rk < best_rank) { best_rank = rk; best = i; }
@@ -970,7 +990,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
       case DHEN_DOT: return 1u | 8u;      // dZ (tA), S (tD)
       case DHEN_DCN: return 2u | 16u;     // dA (tB), dA column sums (bsum)
       case DHEN_ATTN: return 1u | 2u | 4u | 8u | 32u | 64u | 128u | 256u | 512u | 1024u;   // (1024: F, when shared)
-      case DHEN_CONV: case DHEN_MLP: case DHEN_LINEAR: return 0u;   // own scratch / the dX accumulator
+      case DHEN_CONV: case DHEN_MLP: case DHEN_LINEAR: case DHEN_DCN_LIT: return 0u;   // own scratch / the dX accumulator
       default: return ~0u;
     }
   };
@@ -978,7 +998,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
     switch (k) {
       case DHEN_DCN: return 2u | 16u;     // dA, its column sums
       case DHEN_ATTN: return 1u | 2u | 4u | 64u | 512u | 1024u;   // dR2 (tA), dR1 (tB), dF (tC), dQKV (tF), db1, F
-      case DHEN_DOT: case DHEN_CONV: case DHEN_MLP: case DHEN_LINEAR: return 0u;   // saved / own buffers
+      case DHEN_DOT: case DHEN_CONV: case DHEN_MLP: case DHEN_LINEAR: case DHEN_DCN_LIT: return 0u;   // saved / own buffers
       default: return ~0u;
     }
   };
@@ -1083,7 +1103,24 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         const bool fuse_db = c->tune.fuse_db && dt == BF16 && d <= 256;
         int bsum_rows = 0;
         const double dU_in_dR = take_dR ? (double)B * l * d * es : 0.0;   // dU is a slice of the dR residual
-        if (pack) {
+        if (c->tune.dcn_fused && dt == BF16 && dcnb::supported(B, mi, l, d, ldU) && (mi == 128 || pack)) {
+          // one kernel: dT = W_u dU, dA = dT (.) X, dX = base + dT (.) A + dT + dA W (partial dX in TMEM)
+          const void* wu = p(md.Wu);
+          if (mi < 128) {   // several samples per tile: the block-diagonal token map
+            void* bdg = md.bdg_pre ? md.bdg : c->bdiag;
+            if (!md.bdg_pre) KT("dcn.bdiag", 0, 2.0 * 128 * 128 * es, blockdiag(p(md.Wu), mi, l, spt, bdg, st));
+            wu = bdg;
+          }
+          const double rd = (double)rows * d;
+          // algorithmic bytes: dU + X + A + base in, dA + dX out (W, W_u once)
+          const double bytes = (double)B * l * d * es + rd * (es + es + (take_dR ? es : 4) + es + (emit_dX ? es : 4)) +
+                               (double)d * d * es - dU_in_dR;
+          ProfScope ps(c, "dcn.bwd_fused", 2.0 * rows * l * d + 2.0 * rd * d, bytes, st);
+          CK(dcnb::bwd(wu, dU, ldU, p(md.W), X, md.A, take_dR ? (const void*)c->dR : (const void*)acc, take_dR ? 0 : 1,
+                       emit_dX ? dX : (void*)acc, emit_dX ? 0 : 1, dA, fuse_db ? c->bsum : nullptr, B, mi, l, d, st,
+                       &bsum_rows));
+          if (ps.rec >= 0) c->recs[ps.rec].tc = 1;
+        } else if (pack) {
           void* bdg = md.bdg_pre ? md.bdg : c->bdiag;
           if (!md.bdg_pre) KT("dcn.bdiag", 0, 2.0 * 128 * 128 * es, blockdiag(p(md.Wu), mi, l, spt, bdg, st));
           Gemm gt = mk(spt * mi, d, spt * l, B / spt, operand(bdg, dt, spt * l, 1),
@@ -1106,11 +1143,14 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
           if (fuse_db) gt.e.bsum = c->bsum;
         RET(G_dT(gt, c, st, &bsum_rows, dU_in_dR));
         }
+        const bool fused_bwd = c->tune.dcn_fused && dt == BF16 && dcnb::supported(B, mi, l, d, ldU) && (mi == 128 || pack);
         if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dA ready
-        Gemm gx = mk((int)rows, d, d, 1, operand(dA, dt, d, 1), operand(p(md.W), dt, 1, d), view(acc, F32, d, 1));
-        gx.e.accumulate = 1;
-        if (emit_dX) { gx.e.accumulate = 0; gx.e.resid = view(acc, F32, d, 1); gx.c = view(dX, dt, d, 1); }   // dX = acc + dA W
-        RET(G_(gx, c, st, "dcn.dgrad"));
+        if (!fused_bwd) {
+          Gemm gx = mk((int)rows, d, d, 1, operand(dA, dt, d, 1), operand(p(md.W), dt, 1, d), view(acc, F32, d, 1));
+          gx.e.accumulate = 1;
+          if (emit_dX) { gx.e.accumulate = 0; gx.e.resid = view(acc, F32, d, 1); gx.c = view(dX, dt, d, 1); }   // dX = acc + dA W
+          RET(G_(gx, c, st, "dcn.dgrad"));
+        }
         Gemm gw = mk(d, d, (int)rows, 1, operand(dA, dt, 1, d), operand(X, dt, 1, d), view(gp(md.W), F32, d, 1));
         gw.e.accumulate = 1;
         RET(G_(gw, c, sd, "dcn.wgrad", ws2));
@@ -1238,6 +1278,23 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         Gemm gx = mk((int)rows, d, 3 * d, 1, operand(dQKV, dt, s3, 1), operand(p(md.Wq), dt, 1, d), view(acc, F32, d, 1));
         gx.e.accumulate = 1;
         RET(G_(gx, c, st, "attn.qkv_dgrad"));
+        RET(join());
+        break;
+      }
+      case DHEN_DCN_LIT: {   // R31: dW = sum_b G_b dU_b^T, db = sum_b dU_b (side); dG_b = dU_b^T W^T, dX += X (dG + dG^T)
+        RET(fork());
+        Gemm gw = mk(d, l, B * d, 1, operand(md.G, dt, d, 1, 0, 0, 1, d, (int64_t)d * d),
+                     operand(dU, dt, d, 1, 0, 0, 1, d, ldU), view(gp(md.W), F32, l, 1));
+        gw.e.accumulate = 1;
+        RET(G_(gw, c, sd, "dcnl.wgrad", ws2));
+        KTS(sd, "dcnl.bias_grad", 0, (double)B * l * d * es, colsum_add(dU, dt, B, l * d, ldU, gp(md.b), red2, c->red_bytes, sd));
+        Gemm gg = mk(d, d, l, B, operand(dU, dt, 1, d, ldU), operand(p(md.W), dt, l, 1), view(md.dGf, F32, d, 1, (int64_t)d * d));
+        RET(G_(gg, c, st, "dcnl.dG"));
+        KT("dcnl.sym", 0, (double)B * d * d * (4 + es), sym_add(md.dGf, md.S, dt, B, d, st));
+        Gemm gx = mk(mi, d, d, B, operand(X, dt, d, 1, (int64_t)mi * d), operand(md.S, dt, 1, d, (int64_t)d * d),
+                     view(acc, F32, d, 1, (int64_t)mi * d));
+        gx.e.accumulate = 1;
+        RET(G_(gx, c, st, "dcnl.dgrad"));
         RET(join());
         break;
       }
@@ -1625,7 +1682,7 @@ void dhen_tuning_default(dhen_tuning* t) { if (t) *t = tuning_default(); }
 dhen_status dhen_set_tuning(dhen_ctx* c, const dhen_tuning* t) {
   if (!c || !t) return fail(DHEN_E_STATE, "dhen_set_tuning: ctx or tuning is NULL");
   const int bits[] = {t->overlap, t->defer_join, t->ln_fuse, t->first_writer, t->relu_bits, t->fuse_db, t->vdy,
-                      t->trail, t->bd_pre, t->tstore, t->attn_fused, t->pdl, t->gemm_simt};
+                      t->trail, t->bd_pre, t->tstore, t->attn_fused, t->pdl, t->gemm_simt, t->dcn_fused};
   for (int b : bits)
     if (b != 0 && b != 1) return fail(DHEN_E_CONFIG, "dhen_set_tuning: a 0/1 switch is %d", b);
   if (t->sym < -1 || t->sym > 2 || t->pair < -1 || t->pair > 1 || t->pair_k < 0)

@@ -19,6 +19,8 @@ def forward_flops_per_sample(cfg) -> int:
                 tot += 2 * mi * mi * d + 2 * h * l * d
             elif s.kind == "linear":
                 tot += tok
+            elif s.kind == "dcn_lit":
+                tot += 2 * d * d * mi + 2 * d * d * l     # per-sample d x d Gram + projection (Eq.(7) literal)
             elif s.kind == "dcn":
                 tot += 2 * mi * d * d + tok
             elif s.kind == "conv":

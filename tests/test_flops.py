@@ -53,6 +53,9 @@ def _module_forward(kind, s, m, d):
         from torch.nn.attention import SDPBackend, sdpa_kernel
         with sdpa_kernel(SDPBackend.MATH):
             return torch.matmul(Wu.t(), enc(X))
+    if kind == "dcn_lit":
+        Xn = X.transpose(1, 2)
+        return (torch.matmul(torch.bmm(Xn, Xn.transpose(1, 2)), torch.randn(d, l)).transpose(1, 2) + torch.randn(l, d))
     if kind == "mlp":
         h1, h2 = s.mlp_hidden
         a = F.relu(F.linear(X.reshape(1, m * d), torch.randn(h1, m * d), torch.randn(h1)))
@@ -84,7 +87,7 @@ def _binding_cfg(net):
                                           tuple(s.mlp_hidden)) for s in L.modules] for L in net.layers])
 
 
-@pytest.mark.parametrize("kind", ["dot", "linear", "dcn", "conv", "attn", "mlp"])
+@pytest.mark.parametrize("kind", ["dot", "linear", "dcn", "conv", "attn", "mlp", "dcn_lit"])
 def test_module_flops_vs_torch_counter(kind):
     from paper_2203_11014_b200 import flops
     m, d = 12, 32

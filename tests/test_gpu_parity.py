@@ -360,3 +360,15 @@ def test_ensemble_variants_match_oracle(ens, proj, dtype, tol):
     g = case.gpu_step(lr=0.05)
     o = case.oracle_step(lr=0.05)
     _compare(case, g, o, tol, tol, gated_report_only=(dtype == "bf16"), label=f"ensemble {ens} proj={proj} {dtype}")
+
+
+@pytest.mark.parametrize("dtype,tol,m,d,l,B", [("fp32", 1e-5, 12, 16, 6, 19), ("bf16", 2e-2, 12, 16, 6, 19),
+                                               ("bf16", 2e-2, 64, 128, 32, 24)])
+def test_dcn_literal_matches_oracle(dtype, tol, m, d, l, B):
+    """NEXT#3 method variant: Eq.(7) read literally (R31: per-sample d x d Gram over tokens, u = G W + b) as a
+    module next to the others, two layers, full train step against the oracle (G1 / G3)."""
+    net = O.NetSpec(m, d, [O.LayerSpec([M("dcn_lit", l), M("dcn", m - l)]), O.LayerSpec([M("dcn_lit", l), M("linear", m - l)])])
+    case = Case(net, B, dtype, seed=2203011014 + 11)
+    g = case.gpu_step(lr=0.05)
+    o = case.oracle_step(lr=0.05)
+    _compare(case, g, o, tol, tol, label=f"paper-literal DCN {dtype} m={m} d={d}")

@@ -376,3 +376,47 @@ def test_adam_matches_torch():
         for a, b in zip(got, tp):
             assert np.abs(a - b.detach().numpy()).max() <= 1e-12
     assert st["t"] == 4
+
+
+# ------------------------------------------------------------------- paper-literal DCN, Eq.(7) (R31; NEXT#3)
+def _dcnl(X, W, b):
+    net = O.NetSpec(X.shape[1], X.shape[2], [O.LayerSpec([O.ModuleSpec("dcn_lit", W.shape[1])])])
+    return O.dcn_lit_fwd(X, {"W": W, "b": b}, net.layers[0].modules[0], O.FP64)
+
+
+def test_dcn_lit_spec_examples():
+    """identity tokens -> G = I, u = W + b; all-zero X -> u = b (columns of u = the l embeddings)."""
+    W = RNG.standard_normal((2, 3))
+    b = RNG.standard_normal((3, 2))
+    U, _ = _dcnl(np.eye(2)[None], W, b)
+    assert np.allclose(U[0], W.T + b, atol=1e-14)
+    U0, _ = _dcnl(np.zeros((1, 4, 2)), W, b)
+    assert np.array_equal(U0[0], b)
+
+
+def test_dcn_lit_vs_torch_autograd():
+    """u = (X_nX_nᵀ) W + b in torch fp64 (bmm + matmul), outputs and every gradient by autograd."""
+    B, m, d, l = 3, 5, 4, 6
+    X = RNG.standard_normal((B, m, d))
+    W = RNG.standard_normal((d, l))
+    b = RNG.standard_normal((l, d))
+    U, cache = _dcnl(X, W, b)
+    Xt, Wt, bt = (torch.tensor(a, requires_grad=True) for a in (X, W, b))
+    Xn = Xt.transpose(1, 2)                                     # X_n = d x m (P:67)
+    u = torch.matmul(torch.bmm(Xn, Xn.transpose(1, 2)), Wt)     # [B][d][l]
+    Ut = u.transpose(1, 2) + bt
+    assert np.abs(Ut.detach().numpy() - U).max() <= 1e-12
+    dU = RNG.standard_normal(U.shape)
+    Ut.backward(torch.tensor(dU))
+    net = O.NetSpec(m, d, [O.LayerSpec([O.ModuleSpec("dcn_lit", l)])])
+    dX, g = O.dcn_lit_bwd(X, {"W": W, "b": b}, net.layers[0].modules[0], cache, dU, O.FP64)
+    assert np.abs(dX - Xt.grad.numpy()).max() <= 1e-11
+    assert np.abs(g["W"] - Wt.grad.numpy()).max() <= 1e-11
+    assert np.abs(g["b"] - bt.grad.numpy()).max() <= 1e-12
+
+
+def test_dcn_lit_flops_spec_example():
+    """cross-net d = 8, m = 6, l = 4 -> Gram 2·8·8·6 = 768 + projection 2·8·8·4 = 512 = 1280 (plus the
+    concat layer's nothing else: one module, m_in != m_out brings W_n: 2·6·4·8)."""
+    net = O.NetSpec(6, 8, [O.LayerSpec([O.ModuleSpec("dcn_lit", 4)])])
+    assert O.forward_flops_per_sample(net) == 1280 + 2 * 6 * 4 * 8

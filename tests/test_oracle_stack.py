@@ -153,7 +153,7 @@ def test_bf16_emulation_is_close_and_exercised():
 def _ens_net(ens, shortcut_proj=False):
     m0 = 6
     l = 5 if shortcut_proj else 6                     # 6 -> 5 exercises W_n with a sum ensemble
-    mods = [M("dot", l), M("dcn", l), M("attn", l, heads=2), M("mlp", l, mlp_hidden=(12, 10))]
+    mods = [M("dot", l), M("dcn", l), M("attn", l, heads=2), M("mlp", l, mlp_hidden=(12, 10)), M("dcn_lit", l)]
     return O.NetSpec(m0, 8, [O.LayerSpec(mods, ensemble=ens), O.LayerSpec([M("linear", l), M("conv", l)],
                                                                             ensemble=ens)])
 
