@@ -407,6 +407,8 @@ def main():
             dist.destroy_process_group()
         return
     tf = flops.train_flops_per_sample(cfg)
+    es = 2 if cfg.dtype == "bf16" else 4
+    step_bytes = sum((3 * mi + 2 * mo) * cfg.d * es for mi, mo in cfg.dims())
     out = {
         "metric": "DHEN train samples/sec (fwd+bwd)", "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
@@ -418,6 +420,10 @@ def main():
                    "l2": "flushed (256 MiB write) before every timed step"},
         "mfu": {"train_flops_per_sample": tf, "vs_burst": value * tf / (world * pk["tc"] * 1e12),
                 "vs_sustained": value * tf / (world * pk["tc_sus"] * 1e12)},
+        # whole-step rooflines: MFU above; HBM = the step's algorithmic bytes -- per layer X_n read
+        # and Y written (forward), X_n and dY read and dX_n written (backward): (3 m_in + 2 m_out) d elements / sample
+        "step_hbm": {"alg_bytes_per_sample": step_bytes,
+                     "frac": value * step_bytes / (world * pk["hbm"] * 1e9), "peak_gbs": pk["hbm"]},
         "loss": loss_val,
         "e2e": e2e,
         "gpu_launches": int(launches),

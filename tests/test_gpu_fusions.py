@@ -134,7 +134,7 @@ def test_schedule_switches_bitwise(name, B, layers, switch):
     _cmp(a, b, net, 1e-3 if switch == "tstore" else 0)
 
 
-@pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2)])
+@pytest.mark.parametrize("name,B,layers", [("C4", 16, 2)])
 def test_gram_bwd_onchip_matches_dense_s(name, B, layers):
     """B5: the Gram backward with S built on chip from the packed dZ (sym = -1, dot_bwd_tc.cu) against the dense-S
     path (S scattered to HBM by the symmetrisation kernel, then a batched GEMM): the same MMA chain over the same

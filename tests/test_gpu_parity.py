@@ -270,10 +270,10 @@ def test_graphed_step_matches_eager_bitwise():
 
 
 @pytest.mark.parametrize("mods,m,d,B", [
-    ([("dot", 64)], 64, 128, 32),                      # Dot alone: first AND last dX writer (dR in, bf16 dX out)
-    ([("dot", 32), ("conv", 32)], 64, 128, 32),        # Dot first writer (dR in, fp32 accumulator out)
-    ([("dcn", 32), ("dot", 32)], 64, 128, 32),         # Dot last writer (fp32 accumulator in, bf16 dX out)
-    ([("dcn", 64), ("dot", 32), ("linear", 32)], 128, 256, 8),   # Dot in between (fp32 +=), C4 shape
+    ([("dot", 128)], 128, 128, 6),                     # Dot alone: first AND last dX writer (dR in, bf16 dX out)
+    ([("dot", 64), ("conv", 64)], 128, 128, 6),        # Dot first writer (dR in, fp32 accumulator out)
+    ([("dcn", 64), ("dot", 64)], 128, 128, 6),         # Dot last writer (fp32 accumulator in, bf16 dX out)
+    ([("dcn", 64), ("dot", 32), ("linear", 32)], 128, 256, 6),   # Dot in between (fp32 +=), C4 shape
 ])
 def test_dot_gram_bwd_onchip_modes(mods, m, d, B):
     """B5's Gram backward with S built on chip (dot_bwd_tc.cu) in each of its four dX-writer forms, layer-local

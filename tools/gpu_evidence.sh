@@ -23,6 +23,13 @@ ECMD="python bench.py --config C4 --steps 2 --warmup 3 --no-cpu-baseline --eager
 timeout 600 $ECMD > gpurun_out/ev_plain_eager.log 2>&1 || { echo "eager plain run failed"; exit 1; }
 for op in ${OPS:-dot.proj_ln dot.proj_dgrad dot.proj_wgrad attn.qkv attn.ffn1 attn.ffn2_ln2 attn.ffn2_dgrad attn.ffn1_wgrad attn.core attn.core_bwd dcn.dT_fused dot.gram_bwd}; do
   timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "$op/" -s 2 -c 1 \
-    -o gpurun_out/ev_ncu_C4_$op -f $ECMD > gpurun_out/ev_ncu_C4_$op.log 2>&1
+    -o /tmp/ev_ncu_C4_$op -f $ECMD > gpurun_out/ev_ncu_C4_$op.log 2>&1
   echo "ncu C4 $op rc=$?"
+  # keep the raw metrics (small) and a source-level stall table; the report itself stays on the box
+  ncu -i /tmp/ev_ncu_C4_$op.ncu-rep --page raw --csv > gpurun_out/ev_raw_C4_$op.csv 2>/dev/null
+  ncu -i /tmp/ev_ncu_C4_$op.ncu-rep --page source --csv --print-source cuda > /tmp/src_$op.csv 2>/dev/null && \
+    python tools/ncu_summary.py source /tmp/src_$op.csv > gpurun_out/ev_src_C4_$op.txt 2>&1
+  rm -f /tmp/ev_ncu_C4_$op.ncu-rep /tmp/src_$op.csv
 done
+gzip -f gpurun_out/ev_launches_C4.csv 2>/dev/null
+du -sh gpurun_out

@@ -32,8 +32,15 @@ def launches(path):
         print(f"{k[:60]:60s} {n:8d} {t/1e3:10.1f} {100*t/tot:6.1f}%")
 
 
+def _raw(path):
+    """The raw-page CSV of a report (.ncu-rep), or a saved raw CSV (.csv)."""
+    if path.endswith(".csv"):
+        return open(path).read()
+    return subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+
+
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    out = _raw(path)
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -62,7 +69,7 @@ def full(path):
 
 
 def traffic(path, cfg, op, summary):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    out = _raw(path)
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     r = rows[2]
@@ -84,8 +91,34 @@ def traffic(path, cfg, op, summary):
     print(f"{cfg} {op}: {nbytes / 1e6:.1f} MB per launch, {dur_us:.1f} us under ncu")
 
 
+def source(path, top=15):
+    """Top source lines by warp-stall samples from `ncu -i rep --page source --csv --print-source cuda`."""
+    rows = [r for r in csv.reader(open(path)) if r]
+    hi = next((i for i, r in enumerate(rows) if any("Stall" in c or "Sampl" in c for c in r)), None)
+    if hi is None:
+        print("(no stall-sampling columns found; header:", rows[0][:12] if rows else [], ")")
+        return
+    hdr = rows[hi]
+    samp = [i for i, c in enumerate(hdr) if "Sampl" in c and "All" in c] or \
+           [i for i, c in enumerate(hdr) if "Stall" in c or "Sampl" in c]
+    src = next((i for i, c in enumerate(hdr) if c.strip().lower() in ("source", "cuda source")), None)
+    line = next((i for i, c in enumerate(hdr) if c.strip() in ("#", "Line", "Line Number")), None)
+    k = samp[0]
+    recs = []
+    for r in rows[hi + 1:]:
+        try:
+            v = float(r[k].replace(",", ""))
+        except (ValueError, IndexError):
+            continue
+        recs.append((v, r[line] if line is not None else "", (r[src] if src is not None else "").strip()[:110]))
+    tot = sum(v for v, _, _ in recs) or 1.0
+    print(f"column '{hdr[k]}', {int(tot)} samples")
+    for v, ln, tx in sorted(recs, reverse=True)[:top]:
+        print(f"{100 * v / tot:5.1f}%  line {ln:>5}  {tx}")
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "traffic":
         traffic(*sys.argv[2:6])
     else:
-        {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+        {"launches": launches, "full": full, "source": source}[sys.argv[1]](sys.argv[2])
