@@ -64,6 +64,8 @@ typedef struct {
   int dcn_fused;     /* 1: DCN backward as one kernel (dT, dA, dA W, partial dX kept in TMEM; bit-identical);
                         0: two GEMMs with an fp32 partial dX in HBM.  Measured slower (C5 11.3 vs 11.0
                         ms/step: its lane-per-row epilogue is load/store-unit bound)      (0) */
+  int dcn_tma;       /* 1: the DCN-backward dT GEMM's epilogue takes X, A, dR through TMA-loaded shared boxes
+                        and stores dA, dX by TMA; 0: per-lane global loads (round 1)                    (1) */
 } dhen_tuning;
 
 void dhen_tuning_default(dhen_tuning* t);

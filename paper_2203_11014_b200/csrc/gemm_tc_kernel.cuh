@@ -71,6 +71,9 @@ struct Lean {
 struct OutMaps {
   CUtensorMap c;
   CUtensorMap d;
+  // DCN-backward operand epilogue (Params::dcnt): X, A, dR loaded and dA stored as 32 x 32 bf16 boxes (64-B
+  // swizzle); dX (c) leaves as 32 x 32 fp32 boxes (128-B swizzle) through `c`
+  CUtensorMap x, m, r, a;
 };
 
 struct Params {
@@ -93,6 +96,7 @@ struct Params {
   int tstore;         // 1: TMA-store epilogue (row-major C, flags within TS_FLAGS; fp32 += is a TMA reduce-add)
   int lnst;           // LayerNorm epilogue: 1 = Y and R leave through TMA stores (tma_o.c / tma_o.d)
   int ln_rdiv;        // 0: 3-D maps {N, M, batch}; l > 0: 4-D maps {N, l, M / l, batch} (two-level rows)
+  int dcnt;           // DCN backward (EF_DCNB): operands staged by TMA into per-warp shared boxes, outputs TMA-stored
 };
 // epilogue flags the TMA-store path implements (any subset; EF_ACC only with fp32 C, as cp.reduce .add)
 constexpr int TS_FLAGS = EF_BIAS | EF_RELU | EF_ACC | EF_BITS | EF_BMASK;
@@ -192,6 +196,12 @@ __device__ __forceinline__ void tma_store4(const CUtensorMap* map, uint32_t src,
   asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(map), "r"(c0),
                "r"(c1), "r"(c2), "r"(c3), "r"(src)
                : "memory");
+}
+__device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
+      : "memory");
 }
 __device__ __forceinline__ void tma_reduce_add3(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
   asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map),
@@ -781,6 +791,15 @@ template <int BN> struct EpiSmem {
   static constexpr int SBIAS = 2 * BN > 512 ? 2 * BN : 512;   // floats: [2][BN] bias, or the LN (mean, M2) exchange
 };
 
+// DCN-backward operand epilogue (Params::dcnt): per epilogue warp two 6-KB operand slots (X | A | dR boxes of
+// 32 rows x 32 bf16) and one 4-KB fp32 dX box, in place of the fp32 staging area
+constexpr int DCNT_WARP_BYTES = 16384;
+template <int BN, int VAR>
+constexpr int epi_bytes() {
+  return ((VarF<VAR>::F & EF_DCNB) != 0 && EpiSmem<BN>::BYTES < 8 * DCNT_WARP_BYTES) ? 8 * DCNT_WARP_BYTES
+                                                                                     : EpiSmem<BN>::BYTES;
+}
+
 template <int BN, int STAGES, bool PAIR>
 constexpr int ring_stages() {
   return PAIR ? (STAGES * (BM * BK * 2 + BN * BK * 2)) / (BM * BK * 2 + BN * BK) : STAGES;
@@ -803,7 +822,7 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + NST * A_BYTES;
   float* stage_all = (float*)(sB + NST * B_BYTES);   // fp32 staging, or the TMA-store boxes (1024-B aligned)
-  float* sbias = (float*)((uint8_t*)stage_all + EpiSmem<BN>::BYTES);   // [2][BN] bias of the current tiles
+  float* sbias = (float*)((uint8_t*)stage_all + epi_bytes<BN, VAR>());   // [2][BN] bias of the current tiles
   uint64_t* bars = (uint64_t*)(sbias + EpiSmem<BN>::SBIAS);   // full[S], empty[S], tfull[2], tempty[2]
   uint64_t* full = bars;
   uint64_t* empty = bars + NST;
@@ -813,6 +832,7 @@ __global__ void __launch_bounds__(320, 1)
   // DCN-backward variants: [8 epilogue warps][256 columns] fp32 column sums of dA (Lean::bsum)
   constexpr bool BSV = VAR > 0 && (VarF<VAR>::F & EF_DCNB) != 0;
   float* csum = (float*)(bars + 2 * NST + 6);
+  uint64_t* opbar = (uint64_t*)(csum + 8 * 256);   // BSV: [8 epilogue warps][2 operand slots] TMA-arrival barriers
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = p.tiles_m * p.tiles_n;
   const int total = ntiles * p.nz * p.splits;
@@ -828,6 +848,8 @@ __global__ void __launch_bounds__(320, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
     for (int s = 0; s < 2 * NST + 2; ++s) mbar_init(smem_u32(bars + s), 1);
     for (int s = 0; s < 2; ++s) mbar_init(smem_u32(tempty + s), pair ? 16 : 8);   // epilogue warps of both CTAs
+    if constexpr (BSV)
+      for (int s = 0; s < 16; ++s) mbar_init(smem_u32(opbar + s), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -949,11 +971,113 @@ __global__ void __launch_bounds__(320, 1)
     const Lean& e = p.ep;
     uint32_t tsel = 0;   // TMA-store box parity of this warp (running over all passes of all tiles)
     int li = 0;
+    // DCN-backward operand epilogue (BSV && p.dcnt).  Per warp and 32-column pass: X, A (and the first writer's
+    // dR) arrive as 32 x 32 bf16 boxes by TMA into one of two operand slots -- the next pass's boxes are in
+    // flight while this pass is combined, with no registers held for them -- lane = row combines them with the
+    // accumulator row from TMEM, dA = bf16(dT X) overwrites X in its box, dX = dT A + dT (+ dR) goes to an fp32
+    // box, and both leave by TMA store (dX +=: TMA reduce-add).  The dA column sums are read down the stored box.
+    constexpr int NPD = BSV ? HC / 32 : 1;   // 32-column passes per warp and tile
+    uint32_t gpass = 0;                      // running pass count of this warp: operand slot gpass & 1
+    float dsum_t[NPD];
+#pragma unroll
+    for (int j = 0; j < NPD; ++j) dsum_t[j] = 0.f;
+    const uint32_t opw = smem_u32(stage_all) + (uint32_t)((warp - 2) * DCNT_WARP_BYTES);
+    const uint32_t obar = smem_u32(opbar) + (uint32_t)((warp - 2) * 16);
+    auto op_issue = [&](int item_, int j_, uint32_t slot_) {   // lane 0: the operand boxes of (item_, pass j_)
+      int m0_, n0_, z_, sp_, kb0_, nk_;
+      decode(item_, m0_, n0_, z_, sp_, kb0_, nk_);
+      const int r_ = m0_ + q4 * 32, c_ = n0_ + hh * HC + 32 * j_;
+      const uint32_t dst = opw + slot_ * 6144u, b = obar + slot_ * 8u;
+      constexpr bool FR = (VarF<VAR>::F & EF_RESID) != 0;
+      mbar_expect_tx(b, FR ? 3 * 2048 : 2 * 2048);
+      tma_load3(dst, &tma_o.x, c_, r_, z_, b);
+      tma_load3(dst + 2048, &tma_o.m, c_, r_, z_, b);
+      if (FR) tma_load3(dst + 4096, &tma_o.r, c_, r_, z_, b);
+    };
+    if (BSV && p.dcnt && lane == 0 && wid < total) op_issue(wid, 0, 0u);
     for (int item = wid; item < total; item += nwk, ++li) {
       int m0, n0, z, sp, kb0, nk;
       decode(item, m0, n0, z, sp, kb0, nk);
       const int ab = li & 1;
       const uint32_t aph = (li >> 1) & 1;
+      if constexpr (BSV) {
+        if (p.dcnt) {
+          constexpr bool FIRST = (VarF<VAR>::F & EF_RESID) != 0;
+          const int rbase = m0 + q4 * 32;
+          const float alpha = e.alpha;
+          const bool alpha1 = alpha == 1.f;
+          mbar_wait(smem_u32(tfull + ab), aph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+          for (int j = 0; j < NPD; ++j, ++gpass) {
+            const uint32_t slot = gpass & 1u, oph = (gpass >> 1) & 1u;
+            // the previous pass's stores have read their boxes (dA in the other slot, the dX box): refill the
+            // other slot with the next pass's operands (this tile's pass j + 1, else the next tile's pass 0)
+            if (lane == 0) {
+              bulk_wait_read<0>();
+              if (j + 1 < NPD) op_issue(item, j + 1, slot ^ 1u);
+              else if (item + nwk < total) op_issue(item + nwk, 0, slot ^ 1u);
+            }
+            __syncwarp();
+            uint32_t v[32];
+            ld_tmem32(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC + 32 * j), v);
+            mbar_wait(obar + slot * 8u, oph);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (j + 1 == NPD) {   // accumulator fully read: hand it back to the MMA warp
+              asm volatile("tcgen05.fence::before_thread_sync;");
+              __syncwarp();
+              if (lane == 0) tempty_arrive(smem_u32(tempty + ab), pair);
+            }
+            const uint32_t xb = opw + slot * 6144u;
+            const uint32_t rowx = xb + (uint32_t)(lane * 64), rowd = opw + 12288u + (uint32_t)(lane * 128);
+            const uint32_t swx = (uint32_t)((lane >> 1) & 3), swd = (uint32_t)(lane & 7);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {   // 16-B granule c of the 64-B bf16 row (64-B swizzle: c ^ ((row >> 1) & 3))
+              const uint32_t off = ((uint32_t)c ^ swx) << 4;
+              float xv[8], av[8], rv[8], da[8], dx[8];
+              unpack_bf8(lds16_(rowx + off), xv);
+              unpack_bf8(lds16_(rowx + 2048u + off), av);
+              if (FIRST) unpack_bf8(lds16_(rowx + 4096u + off), rv);
+#pragma unroll
+              for (int t = 0; t < 8; ++t) {
+                const float tv = alpha1 ? __uint_as_float(v[8 * c + t]) : __uint_as_float(v[8 * c + t]) * alpha;
+                da[t] = tv * xv[t];
+                dx[t] = tv * av[t] + tv;
+                if (FIRST) dx[t] += rv[t];
+              }
+              sts4u(rowx + off, pack_bf2(da[0], da[1]), pack_bf2(da[2], da[3]), pack_bf2(da[4], da[5]),
+                    pack_bf2(da[6], da[7]));
+              sts4(rowd + ((((uint32_t)(2 * c)) ^ swd) << 4), dx[0], dx[1], dx[2], dx[3]);
+              sts4(rowd + ((((uint32_t)(2 * c + 1)) ^ swd) << 4), dx[4], dx[5], dx[6], dx[7]);
+            }
+            __syncwarp();
+            if (e.bsum) {   // column sums of the stored dA: lane = column, rows in order
+              float s_ = 0.f;
+#pragma unroll 8
+              for (int r = 0; r < 32; ++r) {
+                unsigned short h_;
+                asm volatile("ld.shared.u16 %0, [%1];"
+                             : "=h"(h_)
+                             : "r"(xb + (uint32_t)(r * 64) + (((uint32_t)(lane >> 3) ^ (uint32_t)((r >> 1) & 3)) << 4) +
+                                   (uint32_t)((lane & 7) * 2))
+                             : "memory");
+                s_ += __uint_as_float((uint32_t)h_ << 16);
+              }
+              dsum_t[j] += s_;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              const int col = n0 + hh * HC + 32 * j;
+              tma_store3(&tma_o.a, xb, col, rbase, z);
+              if (FIRST) tma_store3(&tma_o.c, opw + 12288u, col, rbase, z);
+              else tma_reduce_add3(&tma_o.c, opw + 12288u, col, rbase, z);
+              bulk_commit();
+            }
+          }
+          continue;
+        }
+      }
       // LayerNorm epilogue: the warp's residual block (32 rows x HC bf16) is loaded BEFORE the accumulator is
       // ready -- with lanes along columns (coalesced 16-B loads) into the warp's staging area, where pass 1
       // reads its row back and overwrites it with R -- so its latency hides under the tile's MMAs
@@ -1420,8 +1544,17 @@ __global__ void __launch_bounds__(320, 1)
       }
       if (p.trace && blockIdx.x == 0 && li < 64 && warp == 2 && lane == 0) p.trace[320 + li] = clock64();
     }
+    if constexpr (BSV) {
+      if (p.dcnt && p.ep.bsum) {   // this warp's dA column sums into its row of the CTA's partial sums
+#pragma unroll
+        for (int j = 0; j < NPD; ++j) {
+          const int col = hh * HC + 32 * j + lane;
+          if (col < p.g.N) csum[(warp - 2) * 256 + col] += dsum_t[j];
+        }
+      }
+    }
   }
-  if ((p.tstore || p.lnst) && warp >= 2 && lane == 0) bulk_wait_all();   // TMA stores done reading smem and written
+  if ((p.tstore || p.lnst || p.dcnt) && warp >= 2 && lane == 0) bulk_wait_all();   // TMA stores done reading smem and written
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if constexpr (BSV) {   // this CTA's partial row of the dA column sums: warps summed in a fixed order
@@ -1446,9 +1579,9 @@ __global__ void __launch_bounds__(320, 1)
 template <int BN, int STAGES, int VAR>
 static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                           cudaStream_t st) {
-  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + EpiSmem<BN>::BYTES + EpiSmem<BN>::SBIAS * 4 +
+  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + epi_bytes<BN, VAR>() + EpiSmem<BN>::SBIAS * 4 +
                        (2 * ring_stages<BN, STAGES, true>() + 4) * 8 + 16 + 1024 +
-                       ((VarF<VAR>::F & EF_DCNB) != 0 ? 8 * 256 * 4 : 0);
+                       ((VarF<VAR>::F & EF_DCNB) != 0 ? 8 * 256 * 4 + 16 * 8 : 0);
   static_assert(SMEM <= 227 * 1024, "smem");
   static bool attr = false;
   if (!attr) {
@@ -1506,7 +1639,7 @@ cudaError_t launch_var(const Params& p, const CUtensorMap& ma, const CUtensorMap
                        cudaStream_t st, int var) {
   switch (var) {
 #define LV_L(i, f, c) \
-  case i: return launch<BN, STAGES, i>(p, ma, mb, mc, st);
+  case i: return launch<BN, ((f) & EF_DCNB) ? 1 : STAGES, i>(p, ma, mb, mc, st);
     LEAN_VARIANTS(LV_L)
 #undef LV_L
     default: return launch<BN, STAGES, 0>(p, ma, mb, mc, st);

@@ -167,6 +167,31 @@ def test_ffn_recompute_bitwise(name, B, layers):
 
 
 @pytest.mark.parametrize("case_", ["C2", "C4", "C5", "wn"])
+def test_dcn_tma_epilogue_matches_lane_epilogue(case_):
+    """The dT GEMM's DCN-backward epilogue with TMA-staged operand boxes (dhen_tuning.dcn_tma = 1) against the
+    per-lane global-load epilogue: the same per-element arithmetic (dA = bf16(dT X), dX = dT A + dT (+ dR), the
+    non-first writer's fp32 add now a TMA reduce-add), so everything is bit-identical except the DCN bias
+    gradient, whose column sums of the stored dA are grouped differently (fp32 rounding only)."""
+    if case_ == "wn":
+        net = O.NetSpec(128, 128, [O.LayerSpec([O.ModuleSpec("dcn", 64)]), O.LayerSpec([O.ModuleSpec("dcn", 64)])])
+        B = 32
+    else:
+        B, layers = {"C2": (64, 2), "C4": (16, 2), "C5": (16, 2)}[case_]
+        net = _net(case_, layers)
+    a = _step(net, B, 22, {"dcn_tma": 0})
+    b = _step(net, B, 22, {"dcn_tma": 1})
+    assert a["loss"] == b["loss"]
+    assert np.array_equal(a["dX0"], b["dX0"])
+    for gi, (ga, gb) in enumerate(zip(a["grads"], b["grads"])):
+        ta, tb = per_tensor(net, gi, ga), per_tensor(net, gi, gb)
+        for k in tb:
+            if k.endswith("dcn.b"):
+                assert norm_err(ta[k], tb[k]) <= 1e-5, (gi, k)
+            else:
+                assert np.array_equal(ta[k], tb[k]), (gi, k, norm_err(ta[k], tb[k]))
+
+
+@pytest.mark.parametrize("case_", ["C2", "C4", "C5", "wn"])
 def test_dcn_fused_backward_matches_two_gemms(case_):
     """B8 as one kernel (dcn_bwd_tc.cu: dT, dA, dA W with the partial dX kept in TMEM) against round 1's two
     GEMMs with the fp32 partial dX in HBM, on the same step: the same arithmetic in the same order, so loss,
