@@ -66,6 +66,8 @@ typedef struct {
                         ms/step: its lane-per-row epilogue is load/store-unit bound)      (0) */
   int dcn_tma;       /* 1: the DCN-backward dT GEMM's epilogue takes X, A, dR through TMA-loaded shared boxes
                         and stores dA, dX by TMA; 0: per-lane global loads (round 1)                    (1) */
+  int ln_tma;        /* 1: LayerNorm GEMM epilogues take the residual by TMA and store R, Y by TMA; 0: register
+                        prefetch and staged coalesced stores                                            (1) */
 } dhen_tuning;
 
 void dhen_tuning_default(dhen_tuning* t);

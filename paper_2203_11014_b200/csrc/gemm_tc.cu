@@ -293,12 +293,38 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
         map3(&mc.c, g.c, true) && (!first || map3(&mc.r, g.e.resid, false)))
       p.dcnt = 1;
   }
-  p.lnst = 0;   // (TMA-store outputs for the LayerNorm epilogue were measured 2-3 % slower than direct stores)
+  p.lnst = 0;
   p.ln_rdiv = 0;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a.mn_major << 15) | ((uint32_t)p.b.mn_major << 16) |
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((p.pair ? 2 * BM : BM) >> 4) << 24);
   const int var = (p.lean_id > 0 && (p.fast8 || p.lanes_rows)) ? p.lean_id : 0;
   if (p.tstore && var != p.lean_id) p.tstore = 0;
+  // LayerNorm epilogue with TMA: residual boxes in, R and Y boxes out over 4-D maps {N, L, M / L, batch}
+  // (L = rows per group of a two-level row view, else M), 32-row warp boxes inside one group or whole groups
+  if (tune().ln_tma && p.lean && (p.ep.flags & EF_LN) && var == p.lean_id && var > 0 && !p.lanes_rows && splits == 1 && !p.pair &&
+      g.M % 32 == 0) {
+    EncodeFn fn = encode_fn();
+    const int L = g.c.rdiv ? g.c.rdiv : g.M;
+    const bool geo = fn && g.M % L == 0 && (L % 32 == 0 || 32 % L == 0) && g.c.cs == 1 && (g.c.zdiv == 1 || g.c.bs1 == 0);
+    auto map4 = [&](CUtensorMap* m, const View& v) -> bool {
+      if (!v.ptr || v.dt != BF16 || ((uintptr_t)v.ptr % 16)) return false;
+      const int64_t rs_o = g.c.rdiv ? v.rs_o : (int64_t)v.rs * L;
+      const int64_t groups = g.M / L;
+      const int64_t bstride = (g.batch > 1 && v.bs0) ? v.bs0 : rs_o * groups;
+      cuuint64_t dims[4] = {(cuuint64_t)g.N, (cuuint64_t)L, (cuuint64_t)groups, (cuuint64_t)g.batch};
+      cuuint64_t strides[3] = {(cuuint64_t)(v.rs * 2), (cuuint64_t)(rs_o * 2), (cuuint64_t)(bstride * 2)};
+      for (int i = 0; i < 3; ++i)
+        if (strides[i] % 16 || strides[i] == 0) return false;
+      cuuint32_t box[4] = {64, (cuuint32_t)std::min(L, 32), (cuuint32_t)(L < 32 ? 32 / L : 1), 1}, estr[4] = {1, 1, 1, 1};
+      return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+             CUDA_SUCCESS;
+    };
+    if (geo && map4(&mc.c, g.c) && map4(&mc.d, g.e.aux) && map4(&mc.r, g.e.resid)) {
+      p.lnst = 1;
+      p.ln_rdiv = L;
+    }
+  }
   if (g.e.ln_gamma && (!p.lean || var != p.lean_id || (p.ep.flags & EF_LN) == 0 || p.lanes_rows)) return cudaErrorNotSupported;
   if (g.e.bits_mode && !p.tstore) return cudaErrorNotSupported;   // bitmask epilogues exist on the TMA-store path
   // column sums of the stored C exist on the bf16 TMA-store path only (rows = M / 32 blocks per batch item)

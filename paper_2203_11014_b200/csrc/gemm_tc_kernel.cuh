@@ -94,8 +94,8 @@ struct Params {
   int pair;           // 1: CTA pairs (cluster of 2) compute 256-row tiles with cta_group::2 MMAs
   long long* trace;   // debug: CTA 0 records clock64 timestamps (nullptr = off)
   int tstore;         // 1: TMA-store epilogue (row-major C, flags within TS_FLAGS; fp32 += is a TMA reduce-add)
-  int lnst;           // LayerNorm epilogue: 1 = Y and R leave through TMA stores (tma_o.c / tma_o.d)
-  int ln_rdiv;        // 0: 3-D maps {N, M, batch}; l > 0: 4-D maps {N, l, M / l, batch} (two-level rows)
+  int lnst;           // LayerNorm epilogue with TMA: residual boxes in (tma_o.r), R (tma_o.d) and Y (tma_o.c) out
+  int ln_rdiv;        // lnst: rows per group L of the 4-D maps {N, L, M / L, batch}
   int dcnt;           // DCN backward (EF_DCNB): operands staged by TMA into per-warp shared boxes, outputs TMA-stored
 };
 // epilogue flags the TMA-store path implements (any subset; EF_ACC only with fp32 C, as cp.reduce .add)
@@ -201,6 +201,14 @@ __device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, 
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load4(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                          uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+          dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar)
       : "memory");
 }
 __device__ __forceinline__ void tma_reduce_add3(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
@@ -794,11 +802,25 @@ template <int BN> struct EpiSmem {
 // DCN-backward operand epilogue (Params::dcnt): per epilogue warp two 6-KB operand slots (X | A | dR boxes of
 // 32 rows x 32 bf16) and one 4-KB fp32 dX box, in place of the fp32 staging area
 constexpr int DCNT_WARP_BYTES = 16384;
-template <int BN, int VAR>
+// LayerNorm epilogue with TMA (Params::lnst): per warp the residual / R boxes (HC / 64 boxes of 32 rows x 64
+// bf16, 128-B swizzle) and one Y box
+template <int BN> constexpr int lnt_warp_bytes() { return (BN / 2) * 64 + 4096; }
+// (the TMA LayerNorm epilogue runs in single-CTA kernels: a CTA pair's deeper operand ring leaves no room)
+template <int BN, int VAR, bool PAIR>
 constexpr int epi_bytes() {
   return ((VarF<VAR>::F & EF_DCNB) != 0 && EpiSmem<BN>::BYTES < 8 * DCNT_WARP_BYTES) ? 8 * DCNT_WARP_BYTES
-                                                                                     : EpiSmem<BN>::BYTES;
+         : ((VarF<VAR>::F & EF_LN) != 0 && !PAIR && EpiSmem<BN>::BYTES < 8 * lnt_warp_bytes<BN>())
+             ? 8 * lnt_warp_bytes<BN>()
+             : EpiSmem<BN>::BYTES;
 }
+// operand-ring depth of an instantiation: the DCN-backward dT GEMM (K = l, one k-block) takes one slot, the
+// single-CTA LayerNorm GEMMs at BN = 256 two (their epilogue boxes need the rest of shared memory)
+template <int BN, int STAGES, int VAR, bool PAIR>
+constexpr int eff_stages() {
+  return (VarF<VAR>::F & EF_DCNB) != 0 ? 1 : ((VarF<VAR>::F & EF_LN) != 0 && BN == 256 && !PAIR) ? 2 : STAGES;
+}
+// per-warp TMA-arrival barriers of the operand epilogues (DCN backward: 2 slots; LayerNorm: 1)
+template <int VAR> constexpr bool has_opbar() { return (VarF<VAR>::F & (EF_DCNB | EF_LN)) != 0; }
 
 template <int BN, int STAGES, bool PAIR>
 constexpr int ring_stages() {
@@ -822,7 +844,7 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + NST * A_BYTES;
   float* stage_all = (float*)(sB + NST * B_BYTES);   // fp32 staging, or the TMA-store boxes (1024-B aligned)
-  float* sbias = (float*)((uint8_t*)stage_all + epi_bytes<BN, VAR>());   // [2][BN] bias of the current tiles
+  float* sbias = (float*)((uint8_t*)stage_all + epi_bytes<BN, VAR, PAIR>());   // [2][BN] bias of the current tiles
   uint64_t* bars = (uint64_t*)(sbias + EpiSmem<BN>::SBIAS);   // full[S], empty[S], tfull[2], tempty[2]
   uint64_t* full = bars;
   uint64_t* empty = bars + NST;
@@ -832,7 +854,8 @@ __global__ void __launch_bounds__(320, 1)
   // DCN-backward variants: [8 epilogue warps][256 columns] fp32 column sums of dA (Lean::bsum)
   constexpr bool BSV = VAR > 0 && (VarF<VAR>::F & EF_DCNB) != 0;
   float* csum = (float*)(bars + 2 * NST + 6);
-  uint64_t* opbar = (uint64_t*)(csum + 8 * 256);   // BSV: [8 epilogue warps][2 operand slots] TMA-arrival barriers
+  // [8 epilogue warps][2 slots] TMA-arrival barriers of the operand epilogues (after the DCN column sums)
+  uint64_t* opbar = (uint64_t*)(csum + (BSV ? 8 * 256 : 0));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = p.tiles_m * p.tiles_n;
   const int total = ntiles * p.nz * p.splits;
@@ -848,7 +871,7 @@ __global__ void __launch_bounds__(320, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
     for (int s = 0; s < 2 * NST + 2; ++s) mbar_init(smem_u32(bars + s), 1);
     for (int s = 0; s < 2; ++s) mbar_init(smem_u32(tempty + s), pair ? 16 : 8);   // epilogue warps of both CTAs
-    if constexpr (BSV)
+    if constexpr (VAR > 0 && has_opbar<VAR>())
       for (int s = 0; s < 16; ++s) mbar_init(smem_u32(opbar + s), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -995,6 +1018,22 @@ __global__ void __launch_bounds__(320, 1)
       if (FR) tma_load3(dst + 4096, &tma_o.r, c_, r_, z_, b);
     };
     if (BSV && p.dcnt && lane == 0 && wid < total) op_issue(wid, 0, 0u);
+    // LayerNorm epilogue with TMA (LNV && p.lnst): the warp's 32 x HC residual block arrives by TMA into its
+    // boxes (the next tile's as soon as this tile's R stores have read them), R = acc + bias + resid overwrites
+    // it in place and leaves by TMA store, Y goes through one 64-column box
+    constexpr bool LNT = VAR > 0 && (VarF<VAR>::F & EF_LN) != 0 && !PAIR;
+    const uint32_t lnw = smem_u32(stage_all) + (uint32_t)((warp - 2) * lnt_warp_bytes<BN>());
+    uint32_t lph = 0;
+    auto ln_issue = [&](int item_) {   // lane 0: the residual boxes of item_'s 32 x HC block
+      int m0_, n0_, z_, sp_, kb0_, nk_;
+      decode(item_, m0_, n0_, z_, sp_, kb0_, nk_);
+      const int r_ = m0_ + (int)crank * BM + q4 * 32, c_ = n0_ + hh * HC;
+      mbar_expect_tx(obar, (uint32_t)(HC * 64));
+#pragma unroll
+      for (int j = 0; j < HC / 64; ++j)
+        tma_load4(lnw + (uint32_t)(j * 4096), &tma_o.r, c_ + 64 * j, r_ % p.ln_rdiv, r_ / p.ln_rdiv, z_, obar);
+    };
+    if (LNT && p.lnst && lane == 0 && wid < total) ln_issue(wid);
     for (int item = wid; item < total; item += nwk, ++li) {
       int m0, n0, z, sp, kb0, nk;
       decode(item, m0, n0, z, sp, kb0, nk);
@@ -1078,15 +1117,156 @@ __global__ void __launch_bounds__(320, 1)
           continue;
         }
       }
+      if constexpr (LNT) {
+        if (p.lnst) {
+          constexpr int F = VarF<VAR>::F;
+          const int rbase = m0 + (int)crank * BM + q4 * 32;
+          const int row = rbase + lane;
+          const bool rok = row < g.M;
+          const int64_t ro = rok ? lean_row(e, z, row) : 0;
+          const uint32_t tq = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC);
+          const bool xch_mode = e.ln_d != HC;
+          float* xch = sbias + q4 * 128;
+          const int cb0 = n0 + hh * HC;
+          const int seg0 = xch_mode ? n0 : cb0;
+          const int gofs = cb0 - seg0;
+          const float inv_d = 1.f / (float)e.ln_d;
+          const uint32_t bar_id = 2 + q4;
+          const int gr = rbase % p.ln_rdiv, gq = rbase / p.ln_rdiv;   // the boxes' row coordinates
+          const uint32_t ybox = lnw + (uint32_t)(HC * 64);
+          const uint32_t sw = (uint32_t)(lane & 7);
+          mbar_wait(smem_u32(tfull + ab), aph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          mbar_wait(obar, lph);
+          lph ^= 1u;
+          // pass 1: v = alpha acc (+ bias) + resid -> TMEM and R (in place of the residual), chunked mean / M2
+          float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+          for (int c = 0; c < HC; c += 32) {
+            uint32_t v[32];
+            ld_tmem32(tq + c, v);
+            float bv[32], rv[32];
+            if constexpr ((F & EF_BIAS) != 0) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) ldg_bf8(e.bias, cb0 + c + 8 * q, bv + 8 * q);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 32; ++q) bv[q] = 0.f;
+            }
+            const uint32_t rrow = lnw + (uint32_t)((c >> 6) * 4096 + lane * 128);
+            const uint32_t g0 = (uint32_t)((c & 63) >> 3);   // first 16-B granule of these 32 columns
+#pragma unroll
+            for (int q = 0; q < 4; ++q) unpack_bf8(lds16_(rrow + (((g0 + q) ^ sw) << 4)), rv + 8 * q);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            float f[32];
+            float cs_ = 0.f;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) { f[q] = __uint_as_float(v[q]) * e.alpha + bv[q] + rv[q]; cs_ += f[q]; }
+            const float cm = cs_ * (1.f / 32.f);
+            float cm2 = 0.f;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) { const float t_ = f[q] - cm; cm2 = fmaf(t_, t_, cm2); }
+            if (c == 0) {
+              s1 = cm; s2 = cm2;
+            } else {
+              const float w_ = 32.f / (float)(c + 32), dl = cm - s1;
+              s1 = fmaf(dl, w_, s1);
+              s2 += cm2 + dl * dl * ((float)c * w_);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              sts4u(rrow + (((g0 + q) ^ sw) << 4), pack_bf2(f[8 * q], f[8 * q + 1]), pack_bf2(f[8 * q + 2], f[8 * q + 3]),
+                    pack_bf2(f[8 * q + 4], f[8 * q + 5]), pack_bf2(f[8 * q + 6], f[8 * q + 7]));
+            tmem_st32f(tq + c, f);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < HC / 64; ++j) tma_store4(&tma_o.d, lnw + (uint32_t)(j * 4096), cb0 + 64 * j, gr, gq, z);
+            bulk_commit();
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          if (xch_mode) {   // [quadrant][hh][32 lanes] of (mean, M2) pairs through the bias scratch
+            const uint32_t xa = smem_u32(xch);
+            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(xa + (uint32_t)((hh * 32 + lane) * 8)), "f"(s1), "f"(s2)
+                         : "memory");
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+            float a1, a2, b1, b2;
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a1), "=f"(a2) : "r"(xa + (uint32_t)(lane * 8)) : "memory");
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(b1), "=f"(b2) : "r"(xa + (uint32_t)((32 + lane) * 8))
+                         : "memory");
+            const float dl = b1 - a1;
+            s1 = 0.5f * (a1 + b1);
+            s2 = (a2 + b2) + dl * dl * (0.5f * (float)HC);
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+          }
+          const float mean = s1;
+          const float rs = rsqrtf(s2 * inv_d + e.ln_eps);
+          if (rok && (!xch_mode || hh == 0)) {
+            const int64_t tok = (ro + seg0) / e.ln_d;
+            e.ln_mu[tok] = mean;
+            e.ln_rstd[tok] = rs;
+          }
+          // the residual boxes are free once the R stores have read them: the next tile's residual flies
+          // during pass 2 (this wait also covers the previous tile's last Y store)
+          if (lane == 0) {
+            bulk_wait_read<0>();
+            if (item + nwk < total) ln_issue(item + nwk);
+          }
+          __syncwarp();
+          // pass 2: Y = gamma (v - mu) rstd + beta through the Y box, one 64-column box store at a time
+          const uint32_t yrow = ybox + (uint32_t)(lane * 128);
+#pragma unroll 1
+          for (int c = 0; c < HC; c += 32) {
+            uint32_t v[32];
+            ld_tmem32(tq + c, v);
+            float gv[32], be[32];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              ldg_bf8(e.ln_gamma, gofs + c + 8 * q, gv + 8 * q);
+              ldg_bf8(e.ln_beta, gofs + c + 8 * q, be + 8 * q);
+            }
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (c + 32 >= HC) {   // accumulator fully read: hand it back to the MMA warp
+              asm volatile("tcgen05.fence::before_thread_sync;");
+              __syncwarp();
+              if (lane == 0) tempty_arrive(smem_u32(tempty + ab), pair);
+            }
+            if ((c & 63) == 0 && c > 0) {   // the Y box's previous store has read it
+              if (lane == 0) bulk_wait_read<0>();
+              __syncwarp();
+            }
+            const uint32_t g0 = (uint32_t)((c & 63) >> 3);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float y[8];
+#pragma unroll
+              for (int t = 0; t < 8; ++t) y[t] = (__uint_as_float(v[8 * q + t]) - mean) * rs * gv[8 * q + t] + be[8 * q + t];
+              sts4u(yrow + (((g0 + q) ^ sw) << 4), pack_bf2(y[0], y[1]), pack_bf2(y[2], y[3]), pack_bf2(y[4], y[5]),
+                    pack_bf2(y[6], y[7]));
+            }
+            if ((c & 63) == 32 || c + 32 >= HC) {   // the 64-column box is complete
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) {
+                tma_store4(&tma_o.c, ybox, cb0 + (c & ~63), gr, gq, z);
+                bulk_commit();
+              }
+            }
+          }
+          continue;
+        }
+      }
       // LayerNorm epilogue: the warp's residual block (32 rows x HC bf16) is loaded BEFORE the accumulator is
       // ready -- with lanes along columns (coalesced 16-B loads) into the warp's staging area, where pass 1
       // reads its row back and overwrites it with R -- so its latency hides under the tile's MMAs
       constexpr bool LNV = VAR > 0 && (VarF<VAR>::F & EF_LN) != 0;
       // (measured: the coalesced staging pre-load wins when a warp half is a whole LN segment, ln_d == HC;
       // with the warp-pair exchange, ln_d == BN, a per-row register prefetch is faster)
-      const bool ln_stage_x = LNV && e.ln_d == HC;
+      const bool ln_stage_x = LNV && e.ln_d == HC && !p.lnst;
       uint4 rpre[LNV ? HC / 8 : 1];
-      if (LNV && !ln_stage_x) {
+      if (LNV && !ln_stage_x && !p.lnst) {
         const int row_ = m0 + (int)crank * BM + q4 * 32 + lane;
         if (row_ < g.M) {
           const __nv_bfloat16* rp = (const __nv_bfloat16*)e.resid + lean_row(e, z, row_) + n0 + hh * HC;
@@ -1576,18 +1756,25 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+template <int BN, int STAGES, int VAR, bool PAIR>
+constexpr int smem_bytes() {
+  constexpr int S = eff_stages<BN, STAGES, VAR, PAIR>();
+  return ring_stages<BN, S, PAIR>() * (BM * BK * 2 + (PAIR ? BN * BK : BN * BK * 2)) + epi_bytes<BN, VAR, PAIR>() +
+         EpiSmem<BN>::SBIAS * 4 + (2 * ring_stages<BN, S, PAIR>() + 4) * 8 + 16 + 1024 +
+         ((VarF<VAR>::F & EF_DCNB) != 0 ? 8 * 256 * 4 : 0) + (has_opbar<VAR>() ? 16 * 8 : 0);
+}
+
 template <int BN, int STAGES, int VAR>
 static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtensorMap& mb, const OutMaps& mc,
                           cudaStream_t st) {
-  constexpr int SMEM = STAGES * (BM * BK * 2 + BN * BK * 2) + epi_bytes<BN, VAR>() + EpiSmem<BN>::SBIAS * 4 +
-                       (2 * ring_stages<BN, STAGES, true>() + 4) * 8 + 16 + 1024 +
-                       ((VarF<VAR>::F & EF_DCNB) != 0 ? 8 * 256 * 4 + 16 * 8 : 0);
-  static_assert(SMEM <= 227 * 1024, "smem");
+  constexpr int S0 = eff_stages<BN, STAGES, VAR, false>(), S1 = eff_stages<BN, STAGES, VAR, true>();
+  constexpr int SMEM = smem_bytes<BN, STAGES, VAR, false>(), SMEM_P = smem_bytes<BN, STAGES, VAR, true>();
+  static_assert(SMEM <= 227 * 1024 && SMEM_P <= 227 * 1024, "smem");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, VAR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, S0, VAR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if constexpr (BN >= 128)
-      cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, VAR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+      cudaFuncSetAttribute(gemm_tc_kernel<BN, S1, VAR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_P);
     attr = true;
   }
   const int ntiles = p0.tiles_m * p0.tiles_n;
@@ -1605,11 +1792,11 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
       at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
       at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[1].val.programmaticStreamSerializationAllowed = 1;
-      cfg.blockDim = dim3(320); cfg.dynamicSmemBytes = SMEM; cfg.stream = st; cfg.attrs = at;
+      cfg.blockDim = dim3(320); cfg.dynamicSmemBytes = SMEM_P; cfg.stream = st; cfg.attrs = at;
       cfg.numAttrs = pdl_enabled() ? 2 : 1;
       if (!max_clusters) {   // SM pairs the GPC layout can co-schedule (<= 74 on 148 SMs)
         cfg.gridDim = dim3(148);
-        if (cudaOccupancyMaxActiveClusters(&max_clusters, gemm_tc_kernel<BN, STAGES, VAR, true>, &cfg) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveClusters(&max_clusters, gemm_tc_kernel<BN, S1, VAR, true>, &cfg) != cudaSuccess ||
             max_clusters <= 0) {
           (void)cudaGetLastError();
           max_clusters = 64;
@@ -1617,7 +1804,7 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
       }
       cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(items, max_clusters)));
       g_last_gemm_grid = (int)cfg.gridDim.x;
-      cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, VAR, true>, ma, mb, mc, p);
+      cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, S1, VAR, true>, ma, mb, mc, p);
       if (e != cudaSuccess) return e;
       ++g_launches;
       continue;
@@ -1625,7 +1812,7 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
     {
       const int grid = (int)std::min<int64_t>(items, 148);
       g_last_gemm_grid = grid;
-      cudaError_t e = pdl_launch(gemm_tc_kernel<BN, STAGES, VAR, false>, grid, 320, SMEM, st, ma, mb, mc, p);
+      cudaError_t e = pdl_launch(gemm_tc_kernel<BN, S0, VAR, false>, grid, 320, SMEM, st, ma, mb, mc, p);
       if (e != cudaSuccess) return e;
     }
     ++g_launches;
@@ -1639,7 +1826,7 @@ cudaError_t launch_var(const Params& p, const CUtensorMap& ma, const CUtensorMap
                        cudaStream_t st, int var) {
   switch (var) {
 #define LV_L(i, f, c) \
-  case i: return launch<BN, ((f) & EF_DCNB) ? 1 : STAGES, i>(p, ma, mb, mc, st);
+  case i: return launch<BN, STAGES, i>(p, ma, mb, mc, st);
     LEAN_VARIANTS(LV_L)
 #undef LV_L
     default: return launch<BN, STAGES, 0>(p, ma, mb, mc, st);

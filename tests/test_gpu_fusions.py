@@ -15,6 +15,8 @@ fuse_db       bias gradients from GEMM epilogue column sums (DCN db, FFN db_1) -
 vdy           head dY formed inside the last LayerNorm backward (not stored)   -> bitwise identical
 sym           dot backward: S on chip (-1) / dense S via a shared image (1, 2) / staged (0) -> bitwise identical
 tstore        TMA-store GEMM epilogue vs the register epilogue                 -> same values (db_1 grouping)
+ln_tma        LayerNorm epilogue: residual by TMA, R / Y by TMA store          -> bitwise identical
+dcn_tma       DCN-backward epilogue: X / A / dR by TMA, dA / dX by TMA store   -> bitwise (db grouping)
 """
 import numpy as np
 import pytest
@@ -121,7 +123,7 @@ def test_dense_symmetrisation_bitwise(name, B, layers, mode):
     _cmp(a, b, net, 0)
 
 
-@pytest.mark.parametrize("switch", ["defer_join", "trail", "bd_pre", "tstore"])
+@pytest.mark.parametrize("switch", ["defer_join", "trail", "bd_pre", "tstore", "ln_tma"])
 @pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2), ("C3", 32, 2)])
 def test_schedule_switches_bitwise(name, B, layers, switch):
     """Schedule-only switches (same kernels' arithmetic in another order of launch / store path): the
@@ -132,6 +134,17 @@ def test_schedule_switches_bitwise(name, B, layers, switch):
     a = _step(net, B, 18, {switch: 0})
     b = _step(net, B, 18, {})
     _cmp(a, b, net, 1e-3 if switch == "tstore" else 0)
+
+
+def test_ln_tma_small_token_groups():
+    """The TMA LayerNorm epilogue over two-level rows: a 16-token Linear module's packed token projection
+    (8 samples per 128-row tile, 4-D boxes of 16 tokens x 2 samples) and a 48-token one (groups of 48 rows:
+    not expressible as 32-row boxes, so the register epilogue runs) -- bit-identical to ln_tma = 0."""
+    net = O.NetSpec(64, 128, [O.LayerSpec([O.ModuleSpec("linear", 16), O.ModuleSpec("dot", 48)]),
+                              O.LayerSpec([O.ModuleSpec("linear", 64)])])
+    a = _step(net, 32, 19, {"ln_tma": 0})
+    b = _step(net, 32, 19, {})
+    _cmp(a, b, net, 0)
 
 
 @pytest.mark.parametrize("name,B,layers", [("C4", 16, 2)])
