@@ -219,6 +219,56 @@ unsigned long long dhen_launch_count(const dhen_ctx* ctx);
 const char* dhen_last_error(void);
 void dhen_destroy(dhen_ctx* ctx);
 
+/* ---------------------------------------------------------------------------------------------------------
+ * Feature processing layer (NEXT#4; "we use the same feature processing layer in DLRM"; readings
+ * R32-R34): the step in front of the stack that produces X0 [B][m0][d], m0 = n_dtok + n_sparse:
+ *   X0[b][0 .. n_dtok)        = the bottom MLP of the numerical features, H_k = relu(H_{k-1} W_k^T + b_k),
+ *                               H_0 = dense[b], output width n_dtok * d read as n_dtok tokens (R32);
+ *   X0[b][n_dtok + t]         = sum of the rows of table t (R_t x d) listed in bag (b, t)  (sum pooling).
+ * Tables are fp32 (lookups and sums in fp32, X0 stored in `dtype`); W_k [out][in] / b_k have fp32 masters
+ * and `dtype` compute copies.  One object owns its device memory (cudaMalloc at init, freed by destroy).
+ * --------------------------------------------------------------------------------------------------------- */
+typedef struct {
+  int n_sparse;             /* sparse features = tables, one pooled token each (>= 0)                      */
+  const long long* rows;    /* [n_sparse] table rows R_t (host)                                             */
+  int n_dense;              /* numerical features per sample                                               */
+  int n_hidden;             /* bottom-MLP hidden layers                                                     */
+  const int* hidden;        /* [n_hidden] hidden widths (host)                                              */
+  int n_dtok;               /* dense tokens (0: no bottom MLP)                                              */
+  int d;                    /* token dimension: 4 | d, d <= 512                                             */
+  int dtype;                /* dhen_dtype of dense, X0 and dX0                                              */
+  int max_batch;            /* largest B of a forward                                                       */
+  long long max_nnz;        /* largest total number of ids of a forward                                     */
+  unsigned long long seed;  /* init: tables U(+-sqrt(1/R_t)), W_k / b_k U(+-1/sqrt(fan_in))                 */
+} dhen_fp_config;
+typedef struct dhen_fp dhen_fp;
+
+/* Allocate and initialise (synchronises `stream`).  DHEN_E_CONFIG on an invalid config, DHEN_E_NOMEM when
+ * the device allocation fails. */
+dhen_status dhen_fp_init(const dhen_fp_config* cfg, void* stream, dhen_fp** out);
+
+/* Forward of B samples (device pointers): ids int32 [nnz] (each relative to its table), offsets int32
+ * [B n_sparse + 1] with bag (b, t) = ids[offsets[b n_sparse + t] .. offsets[b n_sparse + t + 1]) (empty bags
+ * pool to 0), dense [B][n_dense] in dtype (16-B aligned; ignored when n_dtok = 0), x0 [B][m0][d] out (16-B
+ * aligned).  ids outside [0, R_t) are skipped and counted (dhen_fp_bad_ids).  ids, offsets, dense and x0 are
+ * referenced by the following dhen_fp_backward_sgd: keep them unchanged until it returns. */
+dhen_status dhen_fp_forward(dhen_fp* fp, const int* ids, const int* offsets, long long nnz, const void* dense, int B,
+                            void* x0, void* stream);
+
+/* Backward of the last forward given dx0 [B][m0][d] (dtype; e.g. dhen_train_step's dx0), fused with SGD:
+ * E_t[r] -= lr * sum over r's occurrences of dx0[b][n_dtok + t] (rows summed in sample order, deterministic;
+ * untouched rows unchanged, R34), then W_k, b_k -= lr * their gradients (fp32 masters, copies refreshed). */
+dhen_status dhen_fp_backward_sgd(dhen_fp* fp, const void* dx0, float lr, void* stream);
+
+/* Parameter `which` as fp32 on the host: 0 .. n_sparse-1 table t [R_t][d]; then W_1, b_1, W_2, b_2, ...
+ * (W_k [out][in]).  set = 1 writes (and refreshes the compute copy), 0 reads.  Synchronises `stream`. */
+dhen_status dhen_fp_params_io(dhen_fp* fp, int which, float* host, int set, void* stream);
+/* Elements of parameter `which` (-1 on an invalid config / index). */
+long long dhen_fp_param_numel(const dhen_fp_config* cfg, int which);
+/* ids skipped as out of range since init (synchronous read). */
+long long dhen_fp_bad_ids(dhen_fp* fp);
+void dhen_fp_destroy(dhen_fp* fp);
+
 #ifdef __cplusplus
 }
 #endif

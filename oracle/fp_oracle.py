@@ -15,7 +15,7 @@ MLP's parameters take plain SGD like the stack's.
 
 Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s baseline legs may import this module; it imports
 nothing from the product.  bf16 storage points (R33, mirrored from the CUDA path): the dense input, the MLP
-weights' compute copies, the hidden activations H_k, X0, and the MLP backward's dZ_k; the tables and every
+parameters' compute copies (W_k and b_k), the hidden activations H_k, X0, and the MLP backward's dZ_k; the tables and every
 sum stay fp32 / fp64.  Pins: tests/test_oracle_fp.py (torch embedding_bag / autograd / SGD, brute force).
 """
 from __future__ import annotations
@@ -85,7 +85,7 @@ def fp_fwd(spec: FPSpec, P, indices: np.ndarray, offsets: np.ndarray, dense: np.
     h = prec.q("fp.dense", dense.astype(np.float64))
     Hs, Zs = [h], []
     for k, (W, b) in enumerate(zip(P["W"], P["b"])):
-        z = h @ prec.q("fp.W", W).T + b
+        z = h @ prec.q("fp.W", W).T + prec.q("fp.W", b)   # the compute copies of W_k and b_k (R33)
         a = np.maximum(z, 0.0)                     # ReLU after every bottom-MLP layer (R32)
         Zs.append(z)
         last = k == len(P["W"]) - 1

@@ -27,7 +27,8 @@ EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "d
            "dhen_grads_get", "dhen_launch_count", "dhen_last_error", "dhen_destroy", "dhen_profile",
            "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_gemm_epi", "dhen_debug_last_gemm_tc",
            "dhen_debug_gemm_trace", "dhen_tuning_default", "dhen_set_tuning", "dhen_get_tuning",
-           "dhen_debug_profile_trace")
+           "dhen_debug_profile_trace", "dhen_fp_init", "dhen_fp_forward", "dhen_fp_backward_sgd", "dhen_fp_params_io",
+           "dhen_fp_param_numel", "dhen_fp_bad_ids", "dhen_fp_destroy")
 
 
 class dhen_module(C.Structure):
@@ -67,6 +68,13 @@ class dhen_tuning(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("overlap", "defer_join", "ln_fuse", "first_writer", "relu_bits", "fuse_db",
                                          "vdy", "trail", "bd_pre", "sym", "tstore", "pair", "pair_k", "attn_fused",
                                          "pdl", "gemm_simt", "dcn_fused", "dcn_tma", "ln_tma")]
+
+
+class dhen_fp_config(C.Structure):
+    """Feature processing layer (include/dhen.h, NEXT#4)."""
+    _fields_ = [("n_sparse", C.c_int), ("rows", C.POINTER(C.c_longlong)), ("n_dense", C.c_int),
+                ("n_hidden", C.c_int), ("hidden", C.POINTER(C.c_int)), ("n_dtok", C.c_int), ("d", C.c_int),
+                ("dtype", C.c_int), ("max_batch", C.c_int), ("max_nnz", C.c_longlong), ("seed", C.c_ulonglong)]
 
 
 class DhenError(RuntimeError):
@@ -109,6 +117,10 @@ def load(path: str = LIB_PATH):
         "dhen_set_tuning": [vp, C.POINTER(dhen_tuning)],
         "dhen_get_tuning": [vp, C.POINTER(dhen_tuning)],
         "dhen_debug_profile_trace": [vp, C.c_char_p],
+        "dhen_fp_init": [C.POINTER(dhen_fp_config), vp, C.POINTER(vp)],
+        "dhen_fp_forward": [vp, vp, vp, C.c_longlong, vp, i, vp, vp],
+        "dhen_fp_backward_sgd": [vp, vp, C.c_float, vp],
+        "dhen_fp_params_io": [vp, i, vp, i, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name, None)
@@ -132,6 +144,13 @@ def load(path: str = LIB_PATH):
         lib.dhen_tuning_default.argtypes = [C.POINTER(dhen_tuning)]
     lib.dhen_destroy.restype = None
     lib.dhen_destroy.argtypes = [vp]
+    if hasattr(lib, "dhen_fp_init"):
+        lib.dhen_fp_param_numel.restype = C.c_longlong
+        lib.dhen_fp_param_numel.argtypes = [C.POINTER(dhen_fp_config), i]
+        lib.dhen_fp_bad_ids.restype = C.c_longlong
+        lib.dhen_fp_bad_ids.argtypes = [vp]
+        lib.dhen_fp_destroy.restype = None
+        lib.dhen_fp_destroy.argtypes = [vp]
     _lib = lib
     return lib
 
@@ -419,3 +438,69 @@ class DHEN:
     def forward(self, x0, logits, stream=None):
         _check("dhen_forward", self.lib.dhen_forward(self.ctx, _ptr(x0), x0.shape[0], _ptr(logits),
                                                      self._stream(stream)))
+
+
+class FeatureProcessing:
+    """The feature processing layer in front of the stack (NEXT#4, include/dhen.h dhen_fp_*): sum-pooled
+    embedding bags + bottom MLP -> X0 [B][n_dtok + n_sparse][d].  Argument marshalling only."""
+
+    def __init__(self, rows, n_dense, hidden, n_dtok, d, dtype="bf16", max_batch=1, max_nnz=0, seed=0, stream=None):
+        import torch
+        self.torch = torch
+        self.lib = load()
+        self.rows, self.n_dense, self.hidden, self.n_dtok, self.d = list(rows), n_dense, list(hidden), n_dtok, d
+        self.dtype = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self._rows = (C.c_longlong * max(1, len(self.rows)))(*self.rows)
+        self._hidden = (C.c_int * max(1, len(self.hidden)))(*self.hidden)
+        self._c = dhen_fp_config(len(self.rows), self._rows, n_dense, len(self.hidden), self._hidden, n_dtok, d,
+                                 BF16 if dtype == "bf16" else FP32, max_batch, max_nnz, seed)
+        h = C.c_void_p()
+        _check("dhen_fp_init", self.lib.dhen_fp_init(C.byref(self._c), self._stream(stream), C.byref(h)))
+        self.h = h
+        self.m0 = n_dtok + len(self.rows)
+        self.n_params = len(self.rows) + 2 * ((len(self.hidden) + 1) if n_dtok > 0 else 0)
+
+    def _stream(self, stream=None):
+        s = stream if stream is not None else self.torch.cuda.current_stream()
+        return C.c_void_p(s.cuda_stream)
+
+    def numel(self, which):
+        return self.lib.dhen_fp_param_numel(C.byref(self._c), which)
+
+    def forward(self, ids, offsets, dense, x0, stream=None):
+        """ids / offsets int32 CUDA tensors (CSR bags, sample-major), dense [B][n_dense], x0 [B][m0][d] out."""
+        B = x0.shape[0]
+        _check("dhen_fp_forward", self.lib.dhen_fp_forward(self.h, _ptr(ids), _ptr(offsets), int(ids.numel()),
+                                                           _ptr(dense), B, _ptr(x0), self._stream(stream)))
+
+    def backward_sgd(self, dx0, lr, stream=None):
+        _check("dhen_fp_backward_sgd", self.lib.dhen_fp_backward_sgd(self.h, _ptr(dx0), C.c_float(lr),
+                                                                     self._stream(stream)))
+
+    def get(self, which):
+        import numpy as np
+        out = np.empty(self.numel(which), np.float32)
+        _check("dhen_fp_params_io", self.lib.dhen_fp_params_io(self.h, which, out.ctypes.data_as(C.c_void_p), 0,
+                                                               self._stream()))
+        return out
+
+    def set(self, which, values):
+        import numpy as np
+        a = np.ascontiguousarray(values, np.float32).reshape(-1)
+        assert a.size == self.numel(which)
+        _check("dhen_fp_params_io", self.lib.dhen_fp_params_io(self.h, which, a.ctypes.data_as(C.c_void_p), 1,
+                                                               self._stream()))
+
+    def bad_ids(self):
+        return self.lib.dhen_fp_bad_ids(self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.dhen_fp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

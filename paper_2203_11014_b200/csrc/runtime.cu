@@ -45,6 +45,12 @@ static dhen_status fail(dhen_status s, const char* fmt, ...) {
   t_err = buf;
   return s;
 }
+namespace dhen {
+dhen_status fail_msg(dhen_status s, const char* msg) {   // the error of a call outside this file (fp.cu)
+  t_err = msg;
+  return s;
+}
+}  // namespace dhen
 #define CK(call)                                                                               \
   do {                                                                                         \
     cudaError_t e_ = (call);                                                                   \

@@ -63,3 +63,26 @@ def make_params(seed: int, entries, perturb_ln: bool = True) -> np.ndarray:
         else:
             raise ValueError(init)
     return np.concatenate(out).astype(np.float32) if out else np.zeros(0, np.float32)
+
+
+def make_fp_batch(seed: int, B: int, rows, n_dense: int, mean_bag: float, alpha: float = 3.0,
+                  bf16: bool = True, empty_frac: float = 0.0):
+    """Feature-processing inputs (NEXT#4): per (sample, table) a bag of
+    1 + Poisson(mean_bag - 1) ids (a fraction `empty_frac` of bags empty), ids skewed towards the head of
+    each table (floor(R u^alpha), u ~ U(0, 1): power-law-like row popularity, as in click logs), CSR in
+    sample-major order (int32 ids relative to their table, int32 offsets); dense features ~ N(0, 1)
+    (bf16-rounded for bf16 runs).  Returns (ids, offsets, dense)."""
+    rng = _rng(seed + 15485863)
+    ns = len(rows)
+    lens = 1 + rng.poisson(max(mean_bag - 1.0, 0.0), B * ns)
+    if empty_frac > 0:
+        lens[rng.random(B * ns) < empty_frac] = 0
+    offsets = np.zeros(B * ns + 1, np.int64)
+    offsets[1:] = np.cumsum(lens)
+    R = np.tile(np.asarray(rows, np.int64), B)
+    ids = np.floor(np.repeat(R, lens) * rng.random(int(offsets[-1])) ** alpha).astype(np.int64)
+    ids = np.minimum(ids, np.repeat(R, lens) - 1)
+    dense = rng.standard_normal((B, n_dense), dtype=np.float32)
+    if bf16:
+        dense = to_bf16_f32(dense)
+    return ids.astype(np.int32), offsets.astype(np.int32), dense
