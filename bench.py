@@ -213,6 +213,9 @@ def main():
                     help="debug: run the libdhen_wd.so build (bounded mbarrier waits that report and trap)")
     ap.add_argument("--lib", default="", help="debug: load this library build instead (A/B experiments)")
     ap.add_argument("--tuning", default="", help="schedule switches for A/B runs, e.g. sym=1,pair=0 (dhen_tuning)")
+    ap.add_argument("--fp", action="store_true",
+                    help="NEXT#4 workload: the feature processing layer (configs.FP) in front of the stack, X0 from "
+                         "sparse ids and dense features, its backward + sparse SGD after the stack's step")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -258,6 +261,17 @@ def main():
     y = synth.make_labels(synth.SEED_BASE + 100 + rank, B)
     x0 = torch.tensor(X0, device="cuda").to(tdt).contiguous()
     lab = torch.tensor(y, device="cuda")
+    fp = None
+    if args.fp:   # X0 comes from the feature processing layer; its dX0 drives the sparse SGD
+        ntab, R, ndense, hidden, ndtok, mbag = configs.FP[args.config]
+        assert ntab + ndtok == cfg.m0
+        ids, offs, dense = synth.make_fp_batch(synth.SEED_BASE + 200 + rank, B, [R] * ntab, ndense, mbag,
+                                               bf16=(cfg.dtype == "bf16"))
+        fp = binding.FeatureProcessing([R] * ntab, ndense, hidden, ndtok, cfg.d, dtype=cfg.dtype, max_batch=B,
+                                       max_nnz=len(ids), seed=synth.SEED_BASE + 300)
+        t_ids, t_offs = torch.tensor(ids, device="cuda"), torch.tensor(offs, device="cuda")
+        t_dense = torch.tensor(dense, device="cuda").to(tdt).contiguous()
+        dx0_buf = torch.empty_like(x0)
     loss = torch.zeros(1, device="cuda")
     Bg = B * world
     lr = 0.01
@@ -266,8 +280,18 @@ def main():
 
     graphed = not args.eager
 
-    def step():
+    def step_fp(ids_, offs_, dense_, lab_):
+        fp.forward(ids_, offs_, dense_, x0)
         if graphed:
+            model.train_step_graphed(x0, lab_, lr, B_global=Bg, loss=loss, dx0=dx0_buf)
+        else:
+            model.train_step(x0, lab_, lr, B_global=Bg, loss=loss, dx0=dx0_buf)
+        fp.backward_sgd(dx0_buf, lr)
+
+    def step():
+        if fp is not None:
+            step_fp(t_ids, t_offs, t_dense, lab)
+        elif graphed:
             model.train_step_graphed(x0, lab, lr, B_global=Bg, loss=loss)
         else:
             model.train_step(x0, lab, lr, B_global=Bg, loss=loss)
@@ -304,12 +328,20 @@ def main():
     # copies its inputs host->device (pinned, on a copy stream, double-buffered: step k+1's upload overlaps
     # step k's compute, as a training input pipeline does), moves them into the step's input buffers and
     # reads the loss back to the host.  The first upload is inside the timed region too.
+    if fp is not None:   # the step's host inputs are the ids, offsets and dense features (X0 is computed)
+        X0 = dense
     hx = [torch.tensor(X0).to(tdt).pin_memory() for _ in range(2)]
+    if fp is not None:
+        hids = [torch.tensor(ids).pin_memory() for _ in range(2)]
+        hoffs = [torch.tensor(offs).pin_memory() for _ in range(2)]
+        stage_i = [torch.empty_like(t_ids) for _ in range(2)]
+        stage_o = [torch.empty_like(t_offs) for _ in range(2)]
+        di, do = torch.empty_like(t_ids), torch.empty_like(t_offs)
     hy = [torch.tensor(y).pin_memory() for _ in range(2)]
     hl = torch.zeros(1).pin_memory()
-    stage_x = [torch.empty_like(x0) for _ in range(2)]
+    stage_x = [torch.empty_like(t_dense if fp is not None else x0) for _ in range(2)]
     stage_y = [torch.empty_like(lab) for _ in range(2)]
-    dx = torch.empty_like(x0)
+    dx = torch.empty_like(t_dense if fp is not None else x0)
     dy = torch.empty_like(lab)
     cp = torch.cuda.Stream()
     up_done = [torch.cuda.Event() for _ in range(2)]
@@ -317,9 +349,20 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dx.copy_(hx[0])
     dy.copy_(hy[0])
+    if fp is not None:
+        di.copy_(hids[0])
+        do.copy_(hoffs[0])
+
+    def e2e_step():
+        if fp is not None:
+            step_fp(di, do, dx, dy)
+        elif graphed:
+            model.train_step_graphed(dx, dy, lr, B_global=Bg, loss=loss)
+        else:
+            model.train_step(dx, dy, lr, B_global=Bg, loss=loss)
+
     for _ in range(2):   # capture the graph for these buffers outside the timed region
-        step_e2e_warm = model.train_step_graphed if graphed else model.train_step
-        step_e2e_warm(dx, dy, lr, B_global=Bg, loss=loss)
+        e2e_step()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -331,6 +374,9 @@ def main():
                 cp.wait_event(used[s])   # the step that read this staging buffer has moved it on
             stage_x[s].copy_(hx[s], non_blocking=True)
             stage_y[s].copy_(hy[s], non_blocking=True)
+            if fp is not None:
+                stage_i[s].copy_(hids[s], non_blocking=True)
+                stage_o[s].copy_(hoffs[s], non_blocking=True)
             up_done[s].record(cp)
 
     e0.record(st)
@@ -343,11 +389,11 @@ def main():
         st.wait_event(up_done[s])
         dx.copy_(stage_x[s], non_blocking=True)
         dy.copy_(stage_y[s], non_blocking=True)
+        if fp is not None:
+            di.copy_(stage_i[s], non_blocking=True)
+            do.copy_(stage_o[s], non_blocking=True)
         used[s].record(st)
-        if graphed:
-            model.train_step_graphed(dx, dy, lr, B_global=Bg, loss=loss)
-        else:
-            model.train_step(dx, dy, lr, B_global=Bg, loss=loss)
+        e2e_step()
         hl.copy_(loss, non_blocking=True)
     e1.record(st)
     torch.cuda.synchronize()
@@ -357,8 +403,41 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
     e2e = {"value": Bg * args.steps / (e2e_ms / 1e3), "unit": "samples/s",
-           "h2d_bytes_per_step": int(hx[0].numel() * hx[0].element_size() + hy[0].numel() * 4), "d2h_bytes_per_step": 4,
+           "h2d_bytes_per_step": int(hx[0].numel() * hx[0].element_size() + hy[0].numel() * 4 +
+                                     (hids[0].numel() * 4 + hoffs[0].numel() * 4 if fp is not None else 0)),
+           "d2h_bytes_per_step": 4,
            "pipeline": "pinned H2D of step k+1 on a copy stream overlaps step k; D2D into the step buffers; loss D2H"}
+
+    # ---------------- feature processing: device time of its forward and backward + SGD alone (CUDA events)
+    fp_info = None
+    if fp is not None:
+        ef = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        f_ms = b_ms = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            ef[0].record(st)
+            fp.forward(t_ids, t_offs, t_dense, x0)
+            ef[1].record(st)
+            flush.zero_()
+            ef[2].record(st)
+            fp.backward_sgd(dx0_buf, 0.0)
+            ef[3].record(st)
+            torch.cuda.synchronize()
+            f_ms += ef[0].elapsed_time(ef[1])
+            b_ms += ef[2].elapsed_time(ef[3])
+        f_ms /= args.steps
+        b_ms /= args.steps
+        nnz = len(ids)
+        es_ = 2 if cfg.dtype == "bf16" else 4
+        gather = nnz * cfg.d * 4 + B * ntab * cfg.d * es_ + nnz * 4 + (B * ntab + 1) * 4   # rows, pooled tokens, ids, offsets
+        fp_info = {"tables": ntab, "rows_per_table": R, "dense_features": ndense, "hidden": list(hidden),
+                   "dense_tokens": ndtok, "mean_bag": mbag, "ids_per_step": nnz,
+                   "table_bytes": ntab * R * cfg.d * 4, "fwd_ms": f_ms, "bwd_sgd_ms": b_ms,
+                   "share_of_step": (f_ms + b_ms) / (dev_ms / args.steps),
+                   "gather_roofline": {"bound": "hbm", "algorithmic_bytes": gather,
+                                       "note": "forward incl. the bottom MLP; bytes = looked-up fp32 rows + pooled "
+                                               "tokens + ids + offsets",
+                                       "achieved_gbs": gather / f_ms / 1e6}}
 
     # ---------------- profiled pass: per-op device time (roofline of the dominant op)
     model.profile(True)
@@ -413,7 +492,9 @@ def main():
         "metric": "DHEN train samples/sec (fwd+bwd)", "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
-        "config": {"workload": f"{args.config}: {configs.DESCR[args.config]}", "global_batch": Bg, "batch_per_gpu": B,
+        "config": {"workload": f"{args.config}{'+FP' if fp is not None else ''}: {configs.DESCR[args.config]}"
+                               f"{' behind the feature processing layer (NEXT#4)' if fp is not None else ''}",
+                   "global_batch": Bg, "batch_per_gpu": B,
                    "m0": cfg.m0, "d": cfg.d, "layers": len(cfg.layers),
                    "parallelism": f"fsdp{world}" if world > 1 else "single",
                    **({"tuning": args.tuning} if args.tuning else {}),
@@ -431,6 +512,7 @@ def main():
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk.summary(),
         "roofline": roof,
+        **({"fp": fp_info} if fp_info else {}),
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.config)

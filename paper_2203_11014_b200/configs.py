@@ -31,3 +31,15 @@ def make(name: str, batch: int | None = None, seed: int = 2203011014) -> Config:
         return Config(128, 256, [[Module("dcn", 128)] for _ in range(8)], dtype="bf16", batch_max_local=B,
                       seed=seed + 5)
     raise KeyError(name)
+
+
+# Feature processing fronts (NEXT#4, `bench.py --fp`): (tables, rows per table, dense features, bottom-MLP
+# hidden widths, dense tokens, mean ids per bag).  Tables + dense tokens = the config's m0; ids per bag
+# 1 + Poisson(mean - 1), power-law row popularity (synth.make_fp_batch).
+FP = {
+    "C1": (6, 1_000, 8, (), 2, 4.0),
+    "C2": (56, 100_000, 64, (512,), 8, 20.0),
+    "C3": (92, 100_000, 64, (512,), 8, 20.0),
+    "C4": (120, 100_000, 64, (512,), 8, 20.0),
+    "C5": (120, 100_000, 64, (512,), 8, 20.0),
+}

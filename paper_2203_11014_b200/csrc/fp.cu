@@ -8,8 +8,9 @@
 // B200 layout: every table lives in one fp32 buffer [sum_t R_t][d] (row r of table t at row_base[t] + r);
 // the forward is a gather (one warp per bag, 16-B lanes across the row, four rows in flight per warp), the
 // backward sorts the (row, bag) occurrence pairs once (CUB radix sort: stable, so equal rows keep their
-// sample order) and one warp per distinct row sums its occurrences in that order and applies the SGD update
-// in place -- deterministic, no atomics, no dense gradient table.  The bottom MLP runs on the library's
+// sample order), compacts the run heads (CUB select), and a persistent kernel gives each run of equal rows
+// to one warp, which sums its dX0 tokens in that order (eight rows in flight) and applies the SGD update in
+// place -- deterministic, no atomics, no dense gradient table.  The bottom MLP runs on the library's
 // tcgen05 GEMM engine with bias + ReLU epilogues (last layer written straight into X0's dense tokens) and
 // ReLU-mask epilogues in the backward.
 #include <cub/cub.cuh>
@@ -132,43 +133,70 @@ __global__ void __launch_bounds__(256) emb_keys_k(const long long* __restrict__ 
   }
 }
 
-// Backward, step 3: warp = sorted position i; the head of each run of equal rows sums the run's dX0 tokens in
-// the sorted (= sample) order and applies E[row] -= lr * sum.
-template <typename GT>
-__global__ void __launch_bounds__(256) emb_sgd_k(const unsigned long long* __restrict__ keys, const int* __restrict__ bags,
-                                                 long long nnz, unsigned long long total, const GT* __restrict__ dx0,
-                                                 int ns, int nd, int d, int m0, float lr, float* tab) {
+// Backward, step 3: run heads of the sorted keys (position 0 or a key change), compacted by CUB select.
+__global__ void __launch_bounds__(256) emb_heads_k(const unsigned long long* __restrict__ keys, long long nnz,
+                                                   unsigned char* head) {
   pdl_entry();
-  const long long i = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += (long long)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+// Backward, step 4 (persistent, warp = run of equal rows, grid-strided over the *nruns runs): the run's dX0
+// tokens summed in the sorted (= sample) order, FP_U rows in flight, then E[row] -= lr * sum.  The table row
+// is fetched with the run's first rows, so a run of one occurrence costs one round of loads; 64 registers a
+// thread keep 32 warps an SM resident (the kernel is latency-bound on short runs).
+constexpr int FP_U = 4;
+template <typename GT>
+__global__ void __launch_bounds__(256, 4) emb_runs_k(const unsigned long long* __restrict__ keys, const int* __restrict__ bags,
+                                                     const int* __restrict__ heads, const int* __restrict__ nruns,
+                                                     long long nnz, unsigned long long total, const GT* __restrict__ dx0,
+                                                     int ns, int nd, int d, int m0, float lr, float* tab) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
-  if (i >= nnz) return;
-  const unsigned long long key = keys[i];
-  if (key >= total || (i > 0 && keys[i - 1] == key)) return;
+  const int nr = *nruns;
   const int nc = (d + 127) >> 7;
-  float4 acc[4];
+  for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < nr; r += gridDim.x * 8) {
+    const long long lo = heads[r], hi = r + 1 < nr ? heads[r + 1] : nnz;
+    const unsigned long long K = keys[lo];
+    if (K >= total) continue;   // the sentinel run of skipped ids
+    float* row = tab + (long long)K * d;
+    for (int q0 = 0; q0 < nc; q0 += 2) {   // 256 columns per round (d <= 512: at most two rounds)
+      float4 w[2], acc[2];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (long long j = i; j < nnz && keys[j] == key; ++j) {
-    const int bag = bags[j];
-    const int b = bag / ns, t = bag - b * ns;
-    const GT* g = dx0 + ((long long)b * m0 + nd + t) * d;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int col = 128 * c + 4 * lane;
-      if (c < nc && col < d) {
-        const float4 v = ld4<GT>(g + col);
-        acc[c].x += v.x; acc[c].y += v.y; acc[c].z += v.z; acc[c].w += v.w;
+      for (int q = 0; q < 2; ++q) {
+        const int col = 128 * (q0 + q) + 4 * lane;
+        w[q] = (q0 + q < nc && col < d) ? *reinterpret_cast<const float4*>(row + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+        acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
-    }
-  }
-  float* row = tab + (long long)key * d;
+      for (long long p0 = lo; p0 < hi; p0 += FP_U) {
+        float4 v[FP_U][2];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int col = 128 * c + 4 * lane;
-    if (c < nc && col < d) {
-      float4 w = *reinterpret_cast<float4*>(row + col);
-      w.x -= lr * acc[c].x; w.y -= lr * acc[c].y; w.z -= lr * acc[c].z; w.w -= lr * acc[c].w;
-      *reinterpret_cast<float4*>(row + col) = w;
+        for (int u = 0; u < FP_U; ++u) {
+          const bool ok = p0 + u < hi;
+          const int bag = ok ? bags[p0 + u] : 0;
+          const int b = bag / ns, t = bag - b * ns;
+          const GT* g = dx0 + ((long long)b * m0 + nd + t) * d;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int col = 128 * (q0 + q) + 4 * lane;
+            v[u][q] = (ok && q0 + q < nc && col < d) ? ld4<GT>(g + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < FP_U; ++u)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            acc[q].x += v[u][q].x; acc[q].y += v[u][q].y; acc[q].z += v[u][q].z; acc[q].w += v[u][q].w;
+          }
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int col = 128 * (q0 + q) + 4 * lane;
+        if (q0 + q < nc && col < d) {
+          w[q].x -= lr * acc[q].x; w[q].y -= lr * acc[q].y; w[q].z -= lr * acc[q].z; w[q].w -= lr * acc[q].w;
+          *reinterpret_cast<float4*>(row + col) = w[q];
+        }
+      }
     }
   }
 }
@@ -203,6 +231,11 @@ struct dhen_fp {
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   int key_bits = 1;
+  unsigned char* head = nullptr;   // run-head flags of the sorted keys [nnz]
+  int* heads = nullptr;            // compacted run-head positions [nnz]
+  int* nruns = nullptr;
+  void* sel_tmp = nullptr;
+  size_t sel_bytes = 0;
   float* scratch = nullptr;
   size_t scratch_bytes = 0;
   Workspace ws;
@@ -343,6 +376,10 @@ dhen_status dhen_fp_init(const dhen_fp_config* c, void* stream, dhen_fp** out) {
     FA(cub::DeviceRadixSort::SortPairs(nullptr, f->cub_bytes, f->keys_in, f->keys_out, f->bags_in, f->bags_out,
                                        (int64_t)n, 0, f->key_bits, st));
     FA(falloc(f, &f->cub_tmp, f->cub_bytes));
+    FA(falloc(f, &f->head, n)); FA(falloc(f, &f->heads, n * 4)); FA(falloc(f, &f->nruns, 4));
+    FA(cub::DeviceSelect::Flagged(nullptr, f->sel_bytes, cub::CountingInputIterator<int>(0), f->head, f->heads, f->nruns,
+                                  (int64_t)n, st));
+    FA(falloc(f, &f->sel_tmp, f->sel_bytes));
   }
   FA(cudaStreamSynchronize(st));
 #undef FA
@@ -441,14 +478,17 @@ dhen_status dhen_fp_backward_sgd(dhen_fp* f, const void* dx0, float lr, void* st
     size_t tb = f->cub_bytes;
     FCK(cub::DeviceRadixSort::SortPairs(f->cub_tmp, tb, f->keys_in, f->keys_out, f->bags_in, f->bags_out, (int64_t)f->nnz,
                                         0, f->key_bits, st));
-    const unsigned grid = (unsigned)((f->nnz + 7) / 8);
+    FCK(pdl_launch(emb_heads_k, 148 * 8, 256, 0, st, f->keys_out, f->nnz, f->head));
+    size_t sb = f->sel_bytes;
+    FCK(cub::DeviceSelect::Flagged(f->sel_tmp, sb, cub::CountingInputIterator<int>(0), f->head, f->heads, f->nruns,
+                                   (int64_t)f->nnz, st));
     if (f->dt == DHEN_BF16)
-      FCK(pdl_launch(emb_sgd_k<__nv_bfloat16>, grid, 256, 0, st, f->keys_out, f->bags_out, f->nnz, total,
-                     (const __nv_bfloat16*)dx0, f->ns, f->nd, d, m0, lr, f->tables));
+      FCK(pdl_launch(emb_runs_k<__nv_bfloat16>, 148 * 4, 256, 0, st, f->keys_out, f->bags_out, f->heads, f->nruns, f->nnz,
+                     total, (const __nv_bfloat16*)dx0, f->ns, f->nd, d, m0, lr, f->tables));
     else
-      FCK(pdl_launch(emb_sgd_k<float>, grid, 256, 0, st, f->keys_out, f->bags_out, f->nnz, total, (const float*)dx0, f->ns,
-                     f->nd, d, m0, lr, f->tables));
-    g_launches += 3;
+      FCK(pdl_launch(emb_runs_k<float>, 148 * 4, 256, 0, st, f->keys_out, f->bags_out, f->heads, f->nruns, f->nnz, total,
+                     (const float*)dx0, f->ns, f->nd, d, m0, lr, f->tables));
+    g_launches += 5;
   }
   (void)es;
   f->fwd_done = false;

@@ -101,3 +101,20 @@ def test_ensemble_validation_errors(B):
     with pytest.raises(B.DhenError) as e:
         B.validate(_cfg(B, net))
     assert "equal l_i" in str(e.value) or "sum ensemble" in str(e.value)
+
+
+def test_fp_param_numel_and_validation(B):
+    """Feature processing layer (NEXT#4) host-side layout: tables then (W_k, b_k) pairs; invalid configs
+    are rejected without touching a device."""
+    import ctypes as C
+    lib = B.load()
+    rows = (C.c_longlong * 2)(10, 20)
+    hid = (C.c_int * 1)(32)
+    cfg = B.dhen_fp_config(2, rows, 13, 1, hid, 2, 128, B.BF16, 64, 1000, 0)
+    assert [lib.dhen_fp_param_numel(C.byref(cfg), w) for w in range(6)] == [1280, 2560, 32 * 13, 32, 256 * 32, 256]
+    assert lib.dhen_fp_param_numel(C.byref(cfg), 6) == -1
+    bad = B.dhen_fp_config(2, rows, 13, 1, hid, 2, 130, B.BF16, 64, 1000, 0)    # 4 does not divide d
+    assert lib.dhen_fp_param_numel(C.byref(bad), 0) == -1
+    h = C.c_void_p()
+    assert lib.dhen_fp_init(C.byref(bad), None, C.byref(h)) == 1 and not h.value
+    assert b"d = 130" in lib.dhen_last_error()

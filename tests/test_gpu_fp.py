@@ -4,7 +4,7 @@ SGD every table and bottom-MLP parameter.
 
 Tolerances: fp32 runs -- the lookups, sums and GEMMs are fp32 (SIMT GEMMs, exact fp32): 1e-5 normwise;
 bf16 runs -- the oracle emulates the same storage points (dense input, W copies, hidden activations, X0, dZ):
-X0 element error <= 1 bf16 ulp of the element (|x| 2^-8) + 1e-6 (an fp32 vs fp64 sum can round to the
+X0 element error <= 1 bf16 ulp of the element (<= |x| 2^-7) + 1e-6 (an fp32 vs fp64 sum can round to the
 neighbouring bf16 value), MLP parameter steps 2e-2 normwise (BASELINE G3), table steps 1e-5 (the dX0 rows
 are exact bf16 values summed in fp32)."""
 import numpy as np
@@ -66,7 +66,7 @@ def _run(rows, n_dense, hidden, n_dtok, d, B, dtype, seed=1, mean_bag=3.0, lr=0.
 def _check(got, X0, P, newP, bf, nd):
     if bf:   # pooled tokens: within one bf16 ulp; dense tokens (two bf16 GEMM layers deep): G3-style normwise
         err = np.abs(got["X0"][:, nd:] - X0[:, nd:])
-        assert np.all(err <= np.abs(X0[:, nd:]) * 2.0 ** -8 + 1e-6), err.max()
+        assert np.all(err <= np.abs(X0[:, nd:]) * 2.0 ** -7 + 1e-6), err.max()
         if nd:
             assert norm_err(got["X0"][:, :nd], X0[:, :nd]) <= 1e-2
     else:
@@ -106,11 +106,13 @@ def test_fp_out_of_range_ids_skipped():
     assert got["bad"] == 3
 
 
-def test_fp_hot_rows_deterministic():
-    """Power-law ids with long bags (a few rows hit hundreds of times per batch): the sorted-run SGD is
-    deterministic -- two runs give bit-identical tables -- and matches the oracle."""
-    a = _run((64,), 8, (16,), 1, 256, 64, "bf16", seed=3, mean_bag=20.0, empty_frac=0.0)
-    b = _run((64,), 8, (16,), 1, 256, 64, "bf16", seed=3, mean_bag=20.0, empty_frac=0.0)
+@pytest.mark.parametrize("rows,B,mean_bag", [((64,), 64, 20.0), ((3, 5), 256, 8.0)])
+def test_fp_hot_rows_deterministic(rows, B, mean_bag):
+    """Power-law ids with long bags (a few rows hit hundreds of times per batch; with 3- and 5-row tables every
+    run is hundreds of occurrences long): the sorted-run SGD is deterministic -- two runs give bit-identical
+    tables -- and matches the oracle."""
+    a = _run(rows, 8, (16,), 1, 256, B, "bf16", seed=3, mean_bag=mean_bag, empty_frac=0.0)
+    b = _run(rows, 8, (16,), 1, 256, B, "bf16", seed=3, mean_bag=mean_bag, empty_frac=0.0)
     _check(*a, True, 1)
     for x, y in zip(a[0]["tables"], b[0]["tables"]):
         assert np.array_equal(x, y)
@@ -135,4 +137,4 @@ def test_fp_timed_size_sampled():
         for b in (0, 1, 128, 255):
             lo, hi = off[b * ns + t], off[b * ns + t + 1]
             ref = FO.round_bf16(FO.embedding_bag_sum(T, ids[lo:hi]))
-            assert np.all(np.abs(X[b, n_dtok + t] - ref) <= np.abs(ref) * 2.0 ** -8 + 1e-6)
+            assert np.all(np.abs(X[b, n_dtok + t] - ref) <= np.abs(ref) * 2.0 ** -7 + 1e-6)
