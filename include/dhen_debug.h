@@ -61,13 +61,15 @@ typedef struct {
   int attn_fused;    /* 1: fused tcgen05 attention core (m <= 128, dh 64 / 128); 0: 2 GEMMs + softmax  (1) */
   int pdl;           /* 1: programmatic dependent launch on every library launch                        (0) */
   int gemm_simt;     /* 1: every GEMM on the exact-fp32 SIMT path (never in bf16 production)           (0) */
-  int dcn_fused;     /* 1: DCN backward as one kernel (dT, dA, dA W, partial dX kept in TMEM; bit-identical);
-                        0: two GEMMs with an fp32 partial dX in HBM.  Measured slower (C5 11.3 vs 11.0
-                        ms/step: its lane-per-row epilogue is load/store-unit bound)      (0) */
+  int dcn_fused;     /* 1: DCN backward as one kernel where the shape allows (dT, dA, dA W; the partial dX
+                        kept in TMEM, W streamed, operands / outputs as TMA boxes; bit-identical);
+                        0: two GEMMs with an fp32 partial dX in HBM.  C5 +20 %, C2 +9 %, C4 +2 %        (1) */
   int dcn_tma;       /* 1: the DCN-backward dT GEMM's epilogue takes X, A, dR through TMA-loaded shared boxes
                         and stores dA, dX by TMA; 0: per-lane global loads (round 1)                    (1) */
   int ln_tma;        /* 1: LayerNorm GEMM epilogues take the residual by TMA and store R, Y by TMA; 0: register
                         prefetch and staged coalesced stores                                            (1) */
+  int bn_max;        /* widest GEMM tile N (64 / 128 / 256); smaller tiles trade per-tile efficiency for
+                        more tiles (wave quantization of short grids)                                 (256) */
 } dhen_tuning;
 
 void dhen_tuning_default(dhen_tuning* t);

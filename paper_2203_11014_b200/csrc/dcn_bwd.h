@@ -3,14 +3,15 @@
 //   (sample stride ldu); W: bf16 [d][d]; X, A: bf16 [B m][d]; rin: bf16 dR (first writer) or fp32 accumulator;
 //   out: fp32 accumulator or bf16 dX; dA: bf16 [B m][d] out; bsum (nullable): fp32 [rows][d] partial column sums
 //   of dA (*rows_out rows, to be added in order).  cudaErrorNotSupported (nothing launched) outside d in
-//   {128, 256}, m dividing 128, 16 | spt l <= 128, B a multiple of spt.
+//   {128, 256}, m dividing 128, B a multiple of spt, 16 | K1 = spt l with K1 d 2 <= 16 KB, or K1 <= 128 with a bf16
+//   base and bf16 dX (the shared-tile form).
 #pragma once
 #include "common.cuh"
 
 namespace dhen {
 extern unsigned long long g_launches;
 namespace dcnb {
-bool supported(int B, int m, int l, int d, int64_t ldu);
+bool supported(int B, int m, int l, int d, int64_t ldu, int rin_f32, int out_f32);
 cudaError_t bwd(const void* Wu, const void* dU, int64_t ldu, const void* W, const void* X, const void* A, const void* rin,
                 int rin_f32, void* out, int out_f32, void* dA, float* bsum, int B, int m, int l, int d, cudaStream_t st,
                 int* rows_out);

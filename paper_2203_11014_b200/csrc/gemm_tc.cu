@@ -179,7 +179,10 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   using namespace tc;
   if (g.a.dt != BF16 || g.b.dt != BF16 || g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return cudaErrorNotSupported;
   if (g.N < 16) return cudaErrorNotSupported;
-  const int BN = g.N <= 64 ? 64 : g.N <= 128 ? 128 : 256;
+  const int BN0 = g.N <= 64 ? 64 : g.N <= 128 ? 128 : 256;
+  // dhen_tuning.bn_max caps the tile width, except where a LayerNorm segment needs the wider tile
+  const int BN = (g.e.ln_gamma && (g.e.ln_d ? g.e.ln_d : g.N) > std::min(tune().bn_max, BN0)) ? BN0
+                                                                                            : std::min(tune().bn_max, BN0);
   if (g.e.ln_gamma) {   // LN segments must be whole warp halves or whole tiles, and tiles must be full
     const int ld_ = g.e.ln_d ? g.e.ln_d : g.N;
     if (BN < 128 || g.N % BN != 0 || (ld_ != BN && ld_ != BN / 2)) return cudaErrorNotSupported;

@@ -1110,7 +1110,9 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         const bool fuse_db = c->tune.fuse_db && dt == BF16 && d <= 256;
         int bsum_rows = 0;
         const double dU_in_dR = take_dR ? (double)B * l * d * es : 0.0;   // dU is a slice of the dR residual
-        if (c->tune.dcn_fused && dt == BF16 && dcnb::supported(B, mi, l, d, ldU) && (mi == 128 || pack)) {
+        const bool fused_bwd = c->tune.dcn_fused && dt == BF16 && (mi == 128 || pack) &&
+                               dcnb::supported(B, mi, l, d, ldU, take_dR ? 0 : 1, emit_dX ? 0 : 1);
+        if (fused_bwd) {
           // one kernel: dT = W_u dU, dA = dT (.) X, dX = base + dT (.) A + dT + dA W (partial dX in TMEM)
           const void* wu = p(md.Wu);
           if (mi < 128) {   // several samples per tile: the block-diagonal token map
@@ -1150,7 +1152,6 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
           if (fuse_db) gt.e.bsum = c->bsum;
         RET(G_dT(gt, c, st, &bsum_rows, dU_in_dR));
         }
-        const bool fused_bwd = c->tune.dcn_fused && dt == BF16 && dcnb::supported(B, mi, l, d, ldU) && (mi == 128 || pack);
         if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dA ready
         if (!fused_bwd) {
           Gemm gx = mk((int)rows, d, d, 1, operand(dA, dt, d, 1), operand(p(md.W), dt, 1, d), view(acc, F32, d, 1));
@@ -1692,6 +1693,8 @@ dhen_status dhen_set_tuning(dhen_ctx* c, const dhen_tuning* t) {
                       t->trail, t->bd_pre, t->tstore, t->attn_fused, t->pdl, t->gemm_simt, t->dcn_fused, t->dcn_tma, t->ln_tma};
   for (int b : bits)
     if (b != 0 && b != 1) return fail(DHEN_E_CONFIG, "dhen_set_tuning: a 0/1 switch is %d", b);
+  if (t->bn_max != 64 && t->bn_max != 128 && t->bn_max != 256)
+    return fail(DHEN_E_CONFIG, "dhen_set_tuning: bn_max=%d (64, 128 or 256)", t->bn_max);
   if (t->sym < -1 || t->sym > 2 || t->pair < -1 || t->pair > 1 || t->pair_k < 0)
     return fail(DHEN_E_CONFIG, "dhen_set_tuning: sym=%d pair=%d pair_k=%d", t->sym, t->pair, t->pair_k);
   c->tune = *t;

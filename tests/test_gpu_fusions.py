@@ -17,6 +17,7 @@ sym           dot backward: S on chip (-1) / dense S via a shared image (1, 2) /
 tstore        TMA-store GEMM epilogue vs the register epilogue                 -> same values (db_1 grouping)
 ln_tma        LayerNorm epilogue: residual by TMA, R / Y by TMA store          -> bitwise identical
 dcn_tma       DCN-backward epilogue: X / A / dR by TMA, dA / dX by TMA store   -> bitwise (db grouping)
+dcn_fused     DCN backward as one kernel vs dT GEMM + dA W GEMM               -> bitwise (db grouping)
 """
 import numpy as np
 import pytest
@@ -191,8 +192,8 @@ def test_dcn_tma_epilogue_matches_lane_epilogue(case_):
     else:
         B, layers = {"C2": (64, 2), "C4": (16, 2), "C5": (16, 2)}[case_]
         net = _net(case_, layers)
-    a = _step(net, B, 22, {"dcn_tma": 0})
-    b = _step(net, B, 22, {"dcn_tma": 1})
+    a = _step(net, B, 22, {"dcn_tma": 0, "dcn_fused": 0})   # (the two-GEMM path, where the dT epilogue runs)
+    b = _step(net, B, 22, {"dcn_tma": 1, "dcn_fused": 0})
     assert a["loss"] == b["loss"]
     assert np.array_equal(a["dX0"], b["dX0"])
     for gi, (ga, gb) in enumerate(zip(a["grads"], b["grads"])):
@@ -206,11 +207,12 @@ def test_dcn_tma_epilogue_matches_lane_epilogue(case_):
 
 @pytest.mark.parametrize("case_", ["C2", "C4", "C5", "wn"])
 def test_dcn_fused_backward_matches_two_gemms(case_):
-    """B8 as one kernel (dcn_bwd_tc.cu: dT, dA, dA W with the partial dX kept in TMEM) against round 1's two
-    GEMMs with the fp32 partial dX in HBM, on the same step: the same arithmetic in the same order, so loss,
-    dX0 and every gradient are bit-identical -- except the DCN bias gradient, whose column sums of the stored
-    dA are grouped differently (fp32 rounding only).  'wn': a 128 -> 64 token DCN layer (the W_n shortcut
-    initialises the accumulator, so the kernel adds to it) followed by a two-samples-per-tile 64 -> 64 one."""
+    """B8 as one kernel (dcn_bwd_tc.cu, the default: dT, dA, dA W with the partial dX kept in TMEM, W streamed, the
+    operands and outputs as TMA boxes) against the two-GEMM path with the fp32 partial dX in HBM, on the same step:
+    the same arithmetic in the same order, so loss, dX0 and every gradient are bit-identical -- except the DCN bias
+    gradient, whose column sums of the stored dA are grouped differently (fp32 rounding only).  C2: two samples per
+    tile; C4: separate dU / dA tiles (K1 = 32); C5: the shared-tile form (K1 = 128); 'wn': a 128 -> 64 token DCN
+    layer (the W_n shortcut initialises the accumulator: fp32 base) followed by a two-samples-per-tile 64 -> 64 one."""
     if case_ == "wn":
         net = O.NetSpec(128, 128, [O.LayerSpec([O.ModuleSpec("dcn", 64)]), O.LayerSpec([O.ModuleSpec("dcn", 64)])])
         B = 32
