@@ -1,6 +1,7 @@
 """Summarise ncu outputs for profiles/.
     python tools/ncu_summary.py launches <launches.csv>      -> per-kernel share of device time
     python tools/ncu_summary.py full <report.ncu-rep>        -> key metrics of a --set full capture
+    python tools/ncu_summary.py sass <sass-page.csv>         -> warp-stall samples per SASS instruction / region
     python tools/ncu_summary.py traffic <report.ncu-rep> <config> <op> <summary.txt>
         -> add {config: {op: dram bytes per launch, ncu duration}} to profiles/ncu_traffic.json (read by bench.py
            to fill roofline.traffic for that op)"""
@@ -117,8 +118,40 @@ def source(path, top=15):
         print(f"{100 * v / tot:5.1f}%  line {ln:>5}  {tx}")
 
 
+def sass(path, top=25, bucket=100):
+    """Stall sampling per SASS instruction from `ncu -i rep --page source --csv --print-source sass`: the top
+    instructions (with their neighbours' opcodes) and a histogram over 100-instruction regions."""
+    rows = [r for r in csv.reader(open(path)) if r]
+    hi = next((i for i, r in enumerate(rows) if "Warp Stall Sampling (All Samples)" in r), None)
+    if hi is None:
+        print("(no SASS stall-sampling table)")
+        return
+    hdr = rows[hi]
+    iS, iE, iT = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed"), hdr.index("Source")
+    data = rows[hi + 1:]
+    val = lambda r: float((r[iS] or "0").replace(",", ""))
+    tot = sum(val(r) for r in data) or 1.0
+    print(f"{int(tot)} warp-stall samples over {len(data)} SASS instructions"
+          f"{' (kernel: ' + rows[0][1][:90] + ')' if rows[0] and rows[0][0] == 'Kernel Name' else ''}")
+    print("-- top instructions (share of samples, times executed, instruction)")
+    for i in sorted(sorted(range(len(data)), key=lambda i: -val(data[i]))[:top]):
+        print(f"{i:5d} {100 * val(data[i]) / tot:5.1f}% {data[i][iE]:>10s}  {data[i][iT].strip()[:80]}")
+    print(f"-- regions of {bucket} instructions with >= 2 % of the samples")
+    for b in range(0, len(data), bucket):
+        sh = sum(val(r) for r in data[b:b + bucket]) / tot
+        if sh >= 0.02:
+            ops = defaultdict(int)
+            for r in data[b:b + bucket]:
+                t = r[iT].strip().split()
+                if t:
+                    op = t[1] if t[0].startswith("@") and len(t) > 1 else t[0]
+                    ops[op.split(".")[0]] += 1
+            top_ops = ",".join(f"{k}:{v}" for k, v in sorted(ops.items(), key=lambda kv: -kv[1])[:6])
+            print(f"{b:5d}-{b + bucket:<5d} {100 * sh:5.1f}%  {top_ops}")
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "traffic":
         traffic(*sys.argv[2:6])
     else:
-        {"launches": launches, "full": full, "source": source}[sys.argv[1]](sys.argv[2])
+        {"launches": launches, "full": full, "source": source, "sass": sass}[sys.argv[1]](sys.argv[2])
