@@ -271,30 +271,37 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
         p.tstore = 1;
     }
   }
-  // DCN-backward operand epilogue: X, A, dR in and dA, dX out as 32 x 32 boxes by TMA (whole 128-row tiles,
-  // 32-column multiples, single-level rows with one batch stride per view)
+  // 3-D maps {N, M, batch} of a row-major view with 32 x 32 boxes (bf16: 64-B swizzle, fp32: 128-B) for the
+  // operand epilogues below
+  EncodeFn fn3 = encode_fn();
+  auto map3 = [&](CUtensorMap* m, const View& v, bool f32) -> bool {
+    const int es = f32 ? 4 : 2;
+    if (!fn3 || !v.ptr || v.cs != 1 || v.rdiv || !(v.zdiv == 1 || v.bs1 == 0) || ((uintptr_t)v.ptr % 16) ||
+        (v.rs * es) % 16 || v.rs < g.N)
+      return false;
+    const int64_t bstride = (g.batch > 1 && v.bs0) ? v.bs0 : (int64_t)v.rs * g.M;
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)g.batch};
+    cuuint64_t strides[2] = {(cuuint64_t)(v.rs * es), (cuuint64_t)(bstride * es)};
+    cuuint32_t box[3] = {32, 32, 1}, estr[3] = {1, 1, 1};
+    return strides[1] % 16 == 0 &&
+           fn3(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, v.ptr, dims, strides, box,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  const bool opnd_ok = p.lean && p.fast8 && !p.lanes_rows && !p.pair && splits == 1 && g.M % 32 == 0 && g.N % 32 == 0;
+  // DCN-backward operand epilogue: X, A, dR in and dA, dX out as 32 x 32 boxes by TMA
   p.dcnt = 0;
-  if (tune().dcn_tma && p.lean && (p.ep.flags & EF_DCNB) && p.fast8 && !p.lanes_rows && !p.pair && splits == 1 &&
-      g.M % BM == 0 && g.N % 32 == 0 && g.c.dt == F32) {
-    EncodeFn fn = encode_fn();
-    auto map3 = [&](CUtensorMap* m, const View& v, bool f32) -> bool {
-      const int es = f32 ? 4 : 2;
-      if (!v.ptr || v.cs != 1 || v.rdiv || !(v.zdiv == 1 || v.bs1 == 0) || ((uintptr_t)v.ptr % 16) ||
-          (v.rs * es) % 16 || v.rs < g.N)
-        return false;
-      const int64_t bstride = (g.batch > 1 && v.bs0) ? v.bs0 : (int64_t)v.rs * g.M;
-      cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)g.batch};
-      cuuint64_t strides[2] = {(cuuint64_t)(v.rs * es), (cuuint64_t)(bstride * es)};
-      cuuint32_t box[3] = {32, 32, 1}, estr[3] = {1, 1, 1};
-      return strides[1] % 16 == 0 &&
-             fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, v.ptr, dims, strides, box,
-                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-    };
+  if (tune().dcn_tma && opnd_ok && (p.ep.flags & EF_DCNB) && g.M % BM == 0 && g.c.dt == F32) {
     const bool first = (p.ep.flags & EF_RESID) != 0;
-    if (fn && map3(&mc.x, g.e.cross, false) && map3(&mc.m, g.e.mask, false) && map3(&mc.a, g.e.aux, false) &&
+    if (map3(&mc.x, g.e.cross, false) && map3(&mc.m, g.e.mask, false) && map3(&mc.a, g.e.aux, false) &&
         map3(&mc.c, g.c, true) && (!first || map3(&mc.r, g.e.resid, false)))
       p.dcnt = 1;
+  }
+  // DCN cross forward: X in, A (aux) and T (C) out as 32 x 32 bf16 boxes by TMA
+  p.crosst = 0;
+  if (tune().dcn_tma && opnd_ok && BN >= 128 && p.ep.flags == (EF_BIAS | EF_CROSS | EF_AUX) && g.c.dt == BF16 && !g.e.bias_gap_hi &&
+      g.e.bias_dt == BF16 && p.lean_id > 0) {
+    if (map3(&mc.x, g.e.cross, false) && map3(&mc.a, g.e.aux, false) && map3(&mc.c, g.c, false)) p.crosst = 1;
   }
   p.lnst = 0;
   p.ln_rdiv = 0;

@@ -97,6 +97,7 @@ struct Params {
   int lnst;           // LayerNorm epilogue with TMA: residual boxes in (tma_o.r), R (tma_o.d) and Y (tma_o.c) out
   int ln_rdiv;        // lnst: rows per group L of the 4-D maps {N, L, M / L, batch}
   int dcnt;           // DCN backward (EF_DCNB): operands staged by TMA into per-warp shared boxes, outputs TMA-stored
+  int crosst;         // DCN cross forward (bias + cross + aux, bf16): X by TMA boxes, A and T TMA-stored
 };
 // epilogue flags the TMA-store path implements (any subset; EF_ACC only with fp32 C, as cp.reduce .add)
 constexpr int TS_FLAGS = EF_BIAS | EF_RELU | EF_ACC | EF_BITS | EF_BMASK;
@@ -806,6 +807,7 @@ constexpr int DCNT_WARP_BYTES = 16384;
 // bf16, 128-B swizzle) and one Y box
 template <int BN> constexpr int lnt_warp_bytes() { return (BN / 2) * 64 + 4096; }
 // (the TMA LayerNorm epilogue runs in single-CTA kernels: a CTA pair's deeper operand ring leaves no room)
+static_assert(EpiSmem<128>::BYTES >= 8 * 8192, "the cross epilogue's per-warp boxes fit the staging area (BN >= 128)");
 template <int BN, int VAR, bool PAIR>
 constexpr int epi_bytes() {
   return ((VarF<VAR>::F & EF_DCNB) != 0 && EpiSmem<BN>::BYTES < 8 * DCNT_WARP_BYTES) ? 8 * DCNT_WARP_BYTES
@@ -820,7 +822,7 @@ constexpr int eff_stages() {
   return (VarF<VAR>::F & EF_DCNB) != 0 ? 1 : ((VarF<VAR>::F & EF_LN) != 0 && BN == 256 && !PAIR) ? 2 : STAGES;
 }
 // per-warp TMA-arrival barriers of the operand epilogues (DCN backward: 2 slots; LayerNorm: 1)
-template <int VAR> constexpr bool has_opbar() { return (VarF<VAR>::F & (EF_DCNB | EF_LN)) != 0; }
+template <int VAR> constexpr bool has_opbar() { return (VarF<VAR>::F & (EF_DCNB | EF_LN | EF_CROSS)) != 0; }
 
 template <int BN, int STAGES, bool PAIR>
 constexpr int ring_stages() {
@@ -1004,7 +1006,8 @@ __global__ void __launch_bounds__(320, 1)
     float dsum_t[NPD];
 #pragma unroll
     for (int j = 0; j < NPD; ++j) dsum_t[j] = 0.f;
-    const uint32_t opw = smem_u32(stage_all) + (uint32_t)((warp - 2) * DCNT_WARP_BYTES);
+    // per-warp operand boxes: 16 KB (DCN backward: two 6-KB slots + the dX box) or 8 KB (cross: two 4-KB slots)
+    const uint32_t opw = smem_u32(stage_all) + (uint32_t)((warp - 2) * (BSV ? DCNT_WARP_BYTES : 8192));
     const uint32_t obar = smem_u32(opbar) + (uint32_t)((warp - 2) * 16);
     auto op_issue = [&](int item_, int j_, uint32_t slot_) {   // lane 0: the operand boxes of (item_, pass j_)
       int m0_, n0_, z_, sp_, kb0_, nk_;
@@ -1018,6 +1021,18 @@ __global__ void __launch_bounds__(320, 1)
       if (FR) tma_load3(dst + 4096, &tma_o.r, c_, r_, z_, b);
     };
     if (BSV && p.dcnt && lane == 0 && wid < total) op_issue(wid, 0, 0u);
+    // DCN cross forward with TMA (XTV && p.crosst): per warp and 32-column pass the X box (32 x 32 bf16) arrives
+    // into one of two 4-KB slots -- the next pass's flies while this one is combined -- A = alpha acc + b goes to
+    // the slot's second box, T = X (.) A + X overwrites X in place, and both leave by TMA store
+    constexpr bool XTV = VAR > 0 && VarF<VAR>::F == (EF_BIAS | EF_CROSS | EF_AUX) && !VarF<VAR>::C;
+    auto xt_issue = [&](int item_, int j_, uint32_t slot_) {   // lane 0: the X box of (item_, pass j_)
+      int m0_, n0_, z_, sp_, kb0_, nk_;
+      decode(item_, m0_, n0_, z_, sp_, kb0_, nk_);
+      const uint32_t b = obar + slot_ * 8u;
+      mbar_expect_tx(b, 2048u);
+      tma_load3(opw + slot_ * 4096u, &tma_o.x, n0_ + hh * HC + 32 * j_, m0_ + q4 * 32, z_, b);
+    };
+    if (XTV && p.crosst && lane == 0 && wid < total) xt_issue(wid, 0, 0u);
     // LayerNorm epilogue with TMA (LNV && p.lnst): the warp's 32 x HC residual block arrives by TMA into its
     // boxes (the next tile's as soon as this tile's R stores have read them), R = acc + bias + resid overwrites
     // it in place and leaves by TMA store, Y goes through one 64-column box
@@ -1111,6 +1126,60 @@ __global__ void __launch_bounds__(320, 1)
               tma_store3(&tma_o.a, xb, col, rbase, z);
               if (FIRST) tma_store3(&tma_o.c, opw + 12288u, col, rbase, z);
               else tma_reduce_add3(&tma_o.c, opw + 12288u, col, rbase, z);
+              bulk_commit();
+            }
+          }
+          continue;
+        }
+      }
+      if constexpr (XTV) {
+        if (p.crosst) {
+          const int rbase = m0 + q4 * 32;
+          const float alpha = e.alpha;
+          mbar_wait(smem_u32(tfull + ab), aph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+          for (int j = 0; j < HC / 32; ++j, ++gpass) {
+            const uint32_t slot = gpass & 1u, oph = (gpass >> 1) & 1u;
+            if (lane == 0) {   // the previous pass's stores have read the other slot: refill it
+              bulk_wait_read<0>();
+              if (j + 1 < HC / 32) xt_issue(item, j + 1, slot ^ 1u);
+              else if (item + nwk < total) xt_issue(item + nwk, 0, slot ^ 1u);
+            }
+            __syncwarp();
+            uint32_t v[32];
+            ld_tmem32(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC + 32 * j), v);
+            const int col = n0 + hh * HC + 32 * j;
+            float bv[32];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ldg_bf8(e.bias, col + 8 * q, bv + 8 * q);
+            mbar_wait(obar + slot * 8u, oph);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (j + 1 == HC / 32) {   // accumulator fully read: hand it back to the MMA warp
+              asm volatile("tcgen05.fence::before_thread_sync;");
+              __syncwarp();
+              if (lane == 0) tempty_arrive(smem_u32(tempty + ab), pair);
+            }
+            const uint32_t xrow = opw + slot * 4096u + (uint32_t)(lane * 64), arow = xrow + 2048u;
+            const uint32_t swx = (uint32_t)((lane >> 1) & 3);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const uint32_t off = ((uint32_t)c ^ swx) << 4;
+              float xv[8], a8[8], t8[8];
+              unpack_bf8(lds16_(xrow + off), xv);
+#pragma unroll
+              for (int t = 0; t < 8; ++t) {
+                a8[t] = __uint_as_float(v[8 * c + t]) * alpha + bv[8 * c + t];
+                t8[t] = xv[t] * a8[t] + xv[t];
+              }
+              sts4u(arow + off, pack_bf2(a8[0], a8[1]), pack_bf2(a8[2], a8[3]), pack_bf2(a8[4], a8[5]), pack_bf2(a8[6], a8[7]));
+              sts4u(xrow + off, pack_bf2(t8[0], t8[1]), pack_bf2(t8[2], t8[3]), pack_bf2(t8[4], t8[5]), pack_bf2(t8[6], t8[7]));
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store3(&tma_o.a, opw + slot * 4096u + 2048u, col, rbase, z);
+              tma_store3(&tma_o.c, opw + slot * 4096u, col, rbase, z);
               bulk_commit();
             }
           }
@@ -1734,7 +1803,7 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   }
-  if ((p.tstore || p.lnst || p.dcnt) && warp >= 2 && lane == 0) bulk_wait_all();   // TMA stores done reading smem and written
+  if ((p.tstore || p.lnst || p.dcnt || p.crosst) && warp >= 2 && lane == 0) bulk_wait_all();   // TMA stores done reading smem and written
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if constexpr (BSV) {   // this CTA's partial row of the dA column sums: warps summed in a fixed order

@@ -522,7 +522,8 @@ static double gemm_bytes(const Gemm& g) {
   return (double)g.M * g.K * es * (g.a.bs0 || g.a.bs1 ? g.batch : 1) +
          (double)g.N * g.K * es * (g.b.bs0 || g.b.bs1 ? g.batch : 1) +
          vbytes(g.c, mn) * (c_read ? 2 : 1) + vbytes(g.e.resid, mn) + vbytes(g.e.mask, mn) +
-         vbytes(g.e.cross, mn) + vbytes(g.e.aux, mn);
+         (g.e.cross.ptr == g.a.ptr ? 0.0 : vbytes(g.e.cross, mn)) + vbytes(g.e.aux, mn);   // (the DCN cross reads X
+                                                                                              //  as A and as cross: once)
 }
 static inline dhen_status G_(const Gemm& g, dhen_ctx* c, cudaStream_t st, const char* tag, const Workspace* ws = nullptr) {
   const double bytes = gemm_bytes(g);
