@@ -99,7 +99,9 @@ typedef struct {
   int batch_max_local;    /* largest per-rank B any call will use          */
   unsigned long long seed;/* parameter init seed                            */
   int optimizer;          /* 0: SGD theta -= lr g (R18, default); 1: Adam (P:158's optimizer, NEXT#3): fp32
-                             moments on the master shard, PyTorch semantics, no weight decay                */
+                             moments on the master shard, PyTorch semantics, no weight decay; 2: the same
+                             Adam with its moments stored in bf16 ("BF16 optimizer", R35: fp32 math,
+                             RNE storage, half the optimizer-state memory)                                  */
   float adam_beta1, adam_beta2, adam_eps;   /* Adam (0 -> 0.9, 0.999, 1e-8)                          */
   int recompute;          /* activation recompute ("activation checkpointing", NEXT#2), bit mask:
                              1 = the attention FFN hidden F (and its ReLU bitmask) is not kept from forward

@@ -657,9 +657,12 @@ def adam_init(params: List[Dict[str, np.ndarray]]):
             "v": [{k: np.zeros_like(v) for k, v in g.items()} for g in params]}
 
 
-def adam_update(params, grads, state, lr: float, b1: float = 0.9, b2: float = 0.999, eps: float = 1e-8):
+def adam_update(params, grads, state, lr: float, b1: float = 0.9, b2: float = 0.999, eps: float = 1e-8,
+                bf16_state: bool = False):
     """Step t = state.t + 1:  m = b1 m + (1 - b1) g;  v = b2 v + (1 - b2) g^2;
-    theta -= lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps).  Returns (new params, new state)."""
+    theta -= lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps).  Returns (new params, new state).
+    bf16_state (the "BF16 optimizer", P:158, R35): the moments are STORED rounded to bf16 (RNE) after each step;
+    this step's update uses the unrounded m, v."""
     t = state["t"] + 1
     c1, c2 = 1.0 - b1 ** t, 1.0 - b2 ** t
     new_p, new_m, new_v = [], [], []
@@ -670,6 +673,8 @@ def adam_update(params, grads, state, lr: float, b1: float = 0.9, b2: float = 0.
             M[k] = b1 * state["m"][gi][k] + (1.0 - b1) * g
             V[k] = b2 * state["v"][gi][k] + (1.0 - b2) * g * g
             P[k] = th - lr * (M[k] / c1) / (np.sqrt(V[k] / c2) + eps)
+            if bf16_state:
+                M[k], V[k] = round_bf16(M[k]), round_bf16(V[k])
         new_p.append(P); new_m.append(M); new_v.append(V)
     return new_p, {"t": t, "m": new_m, "v": new_v}
 

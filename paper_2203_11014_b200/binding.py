@@ -180,7 +180,7 @@ class Config:
     batch_max_local: int = 1
     ln_eps: float = 1e-5
     seed: int = 0
-    optimizer: str = "sgd"            # "sgd" (R18) | "adam"
+    optimizer: str = "sgd"            # "sgd" (R18) | "adam" | "adam_bf16" (bf16 moments, R35)
     ensembles: Optional[Sequence[str]] = None   # per layer: "concat" (default) | "sum" | "wsum"
     recompute: int = 0                # bit 1: attention FFN hidden recomputed in the backward (NEXT#2)
     adam: Sequence[float] = (0.9, 0.999, 1e-8)
@@ -207,7 +207,7 @@ class Config:
         self._keep = keep
         return dhen_config(self.m0, self.d, len(self.layers), C.cast(layers, C.POINTER(dhen_layer)),
                            BF16 if self.dtype == "bf16" else FP32, self.ln_eps, self.batch_max_local, self.seed,
-                           {"sgd": 0, "adam": 1}[self.optimizer], *[float(x) for x in self.adam], int(self.recompute))
+                           {"sgd": 0, "adam": 1, "adam_bf16": 2}[self.optimizer], *[float(x) for x in self.adam], int(self.recompute))
 
     def dims(self):
         out, m = [], self.m0

@@ -2010,18 +2010,21 @@ __global__ void __launch_bounds__(256) sgd_multi_k(SgdSegs segs, float lr) {
     reinterpret_cast<uint2*>(segs.copy[s])[u] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
   }
 }
+// Adam on the fp32 master shard; the moments are stored in MT (fp32, or bf16 for the BF16 optimizer of R35:
+// each step computes in fp32 from the stored moments, updates theta with the fp32 values and stores them RNE)
+template <typename MT>
 __global__ void __launch_bounds__(256) adam_k(float* __restrict__ master, const float* __restrict__ grad,
-                                             float* __restrict__ m, float* __restrict__ v, void* copy, int dt, int64_t n,
+                                             MT* __restrict__ m, MT* __restrict__ v, void* copy, int dt, int64_t n,
                                              float lr, float b1, float b2, float eps, const int* __restrict__ step) {
   pdl_entry();
   const float t = (float)(*step + 1);
   const float c1 = 1.f - powf(b1, t), c2 = 1.f - powf(b2, t);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float g = grad[i];
-    const float mi = b1 * m[i] + (1.f - b1) * g;
-    const float vi = b2 * v[i] + (1.f - b2) * g * g;
-    m[i] = mi;
-    v[i] = vi;
+    const float mi = b1 * (float)m[i] + (1.f - b1) * g;
+    const float vi = b2 * (float)v[i] + (1.f - b2) * g * g;
+    m[i] = (MT)mi;
+    v[i] = (MT)vi;
     const float p = master[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
     master[i] = p;
     st_from_f32(copy, i, dt, p);
@@ -2031,10 +2034,15 @@ __global__ void adam_count_k(int* step) {
   pdl_entry();
   if (threadIdx.x == 0 && blockIdx.x == 0) *step += 1;
 }
-cudaError_t adam_step(float* master, const float* grad, float* m, float* v, void* copy, int dt, int64_t n, float lr,
+cudaError_t adam_step(float* master, const float* grad, void* m, void* v, int mdt, void* copy, int dt, int64_t n, float lr,
                       float b1, float b2, float eps, const int* step, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  pdl_launch(adam_k, nblocks(n, 256, 148 * 16), 256, 0, st, master, grad, m, v, copy, dt, n, lr, b1, b2, eps, step);
+  if (mdt == BF16)
+    pdl_launch(adam_k<__nv_bfloat16>, nblocks(n, 256, 148 * 16), 256, 0, st, master, grad, (__nv_bfloat16*)m,
+               (__nv_bfloat16*)v, copy, dt, n, lr, b1, b2, eps, step);
+  else
+    pdl_launch(adam_k<float>, nblocks(n, 256, 148 * 16), 256, 0, st, master, grad, (float*)m, (float*)v, copy, dt, n, lr,
+               b1, b2, eps, step);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -89,7 +89,7 @@ cudaError_t sgd_multi(const SgdSegs& segs, float lr, cudaStream_t st);
 // Adam (Kingma & Ba; PyTorch torch.optim.Adam semantics, no weight decay) on an fp32 master shard with fp32
 // moments m, v; the step number t is read from *step (device; the update of step t uses t = *step + 1) and
 // the compute copy (dt) refreshed.  adam_count(step) increments *step afterwards (graph-replay safe).
-cudaError_t adam_step(float* master, const float* grad, float* m, float* v, void* copy, int dt, int64_t n, float lr,
+cudaError_t adam_step(float* master, const float* grad, void* m, void* v, int mdt, void* copy, int dt, int64_t n, float lr,
                       float b1, float b2, float eps, const int* step, cudaStream_t st);
 cudaError_t adam_count(int* step, cudaStream_t st);
 // Sum / weighted-sum ensemble (R27).  ens_ln_fwd: R = sum_i w_i U_i + base (w nullable = all 1; base = the

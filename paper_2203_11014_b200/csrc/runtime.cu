@@ -99,7 +99,7 @@ struct Group {
   void* comp = nullptr;                 // dtype copy [shard] (full when world == 1 / DP)
   float* grad = nullptr;                // fp32 [npad] full gradient (accumulated in bwd)
   float* gshard = nullptr;              // fp32 [shard] reduced gradient shard (world > 1)
-  float *adam_m = nullptr, *adam_v = nullptr;   // Adam moments [shard] (cfg.optimizer == 1)
+  float *adam_m = nullptr, *adam_v = nullptr;   // Adam moments [shard] (cfg.optimizer 1: fp32; 2: bf16 storage)
   std::vector<int64_t> toff, tn;        // tensors: internal offset (64-element aligned), numel
   std::vector<int64_t> tcanon;          // tensors: offset in the dense canonical order (params_io)
   int64_t ncanon = 0;                   // canonical (dense) numel
@@ -255,7 +255,8 @@ static dhen_status validate(const dhen_config* c) {
   if (c->d > 1024) return fail(DHEN_E_CONFIG, "dhen_validate: d=%d > 1024", c->d);
   if (c->dtype != DHEN_FP32 && c->dtype != DHEN_BF16) return fail(DHEN_E_CONFIG, "dhen_validate: dtype=%d", c->dtype);
   if (c->batch_max_local < 1) return fail(DHEN_E_CONFIG, "dhen_validate: batch_max_local=%d", c->batch_max_local);
-  if (c->optimizer != 0 && c->optimizer != 1) return fail(DHEN_E_CONFIG, "dhen_validate: optimizer=%d (0 SGD, 1 Adam)", c->optimizer);
+  if (c->optimizer < 0 || c->optimizer > 2)
+    return fail(DHEN_E_CONFIG, "dhen_validate: optimizer=%d (0 SGD, 1 Adam, 2 Adam with bf16 moments)", c->optimizer);
   int m = c->m0;
   for (int n = 0; n < c->n_layers; ++n) {
     const dhen_layer& L = c->layers[n];
@@ -388,12 +389,12 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
     g.comp = state.take(g.shard * es);
     g.grad = (float*)state.take(g.npad * 4);
     g.gshard = world > 1 ? (float*)state.take(g.shard * 4) : nullptr;
-    if (c->cfg.optimizer == 1) {
-      g.adam_m = (float*)state.take(g.shard * 4);
-      g.adam_v = (float*)state.take(g.shard * 4);
+    if (c->cfg.optimizer >= 1) {   // Adam moments: fp32 (1) or bf16 (2, the BF16 optimizer of R35)
+      g.adam_m = (float*)state.take(g.shard * (c->cfg.optimizer == 2 ? 2 : 4));
+      g.adam_v = (float*)state.take(g.shard * (c->cfg.optimizer == 2 ? 2 : 4));
     }
   }
-  if (c->cfg.optimizer == 1) c->adam_t = (int*)state.take(256);
+  if (c->cfg.optimizer >= 1) c->adam_t = (int*)state.take(256);
   if (shard) { c->gathered[0] = state.take(c->max_npad * es); c->gathered[1] = state.take(c->max_npad * es); }
   if (world > 1) c->gtmp = (float*)state.take(c->max_npad * 4);
   if (world > 1 && c->dist.grad_bf16) {
@@ -1554,8 +1555,8 @@ dhen_status dhen_init(const dhen_config* cfg, const dhen_dist* dist, void* state
     cudaError_t e3 = sgd_cast(g.master, nullptr, 0.f, g.comp, c->dt, g.shard, st);
     if (e3 != cudaSuccess) { delete c; return fail(DHEN_E_CUDA, "dhen_init: %s", cudaGetErrorString(e3)); }
     e3 = cudaMemsetAsync(g.grad, 0, g.npad * 4, st);
-    if (e3 == cudaSuccess && g.adam_m) e3 = cudaMemsetAsync(g.adam_m, 0, g.shard * 4, st);
-    if (e3 == cudaSuccess && g.adam_v) e3 = cudaMemsetAsync(g.adam_v, 0, g.shard * 4, st);
+    if (e3 == cudaSuccess && g.adam_m) e3 = cudaMemsetAsync(g.adam_m, 0, g.shard * (c->cfg.optimizer == 2 ? 2 : 4), st);
+    if (e3 == cudaSuccess && g.adam_v) e3 = cudaMemsetAsync(g.adam_v, 0, g.shard * (c->cfg.optimizer == 2 ? 2 : 4), st);
     if (e3 != cudaSuccess) { delete c; return fail(DHEN_E_CUDA, "dhen_init: %s", cudaGetErrorString(e3)); }
   }
   if (c->adam_t && cudaMemsetAsync(c->adam_t, 0, sizeof(int), st) != cudaSuccess) {
@@ -1843,12 +1844,13 @@ dhen_status dhen_train_step(dhen_ctx* c, const void* x0, const float* labels, in
   }
   RET(join_comm(c, st));
   // B12: the optimizer on the (local shard of the) fp32 masters, refresh the compute copy
-  if (c->cfg.optimizer == 1) {   // Adam (NEXT#3): per group, then the device step counter
+  if (c->cfg.optimizer >= 1) {   // Adam (NEXT#3): per group, then the device step counter
+    const int mdt = c->cfg.optimizer == 2 ? BF16 : F32;
     for (auto& g : c->G) {
       const float* gr = c->dist.world > 1 ? g.gshard : g.grad;
-      KT("adam", 0, (double)g.shard * (20 + c->es),
-         adam_step(g.master, gr, g.adam_m, g.adam_v, g.comp, c->dt, g.shard, lr, c->cfg.adam_beta1, c->cfg.adam_beta2,
-                   c->cfg.adam_eps, c->adam_t, st));
+      KT("adam", 0, (double)g.shard * (12 + 4 * (mdt == BF16 ? 2 : 4) + c->es),
+         adam_step(g.master, gr, g.adam_m, g.adam_v, mdt, g.comp, c->dt, g.shard, lr, c->cfg.adam_beta1,
+                   c->cfg.adam_beta2, c->cfg.adam_eps, c->adam_t, st));
     }
     CK(adam_count(c->adam_t, st));
     RET(fence_params(c, st));

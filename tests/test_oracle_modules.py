@@ -378,6 +378,31 @@ def test_adam_matches_torch():
     assert st["t"] == 4
 
 
+def test_adam_bf16_state_matches_torch_bf16_loop():
+    """The BF16 optimizer (R35): Adam whose moments live in torch.bfloat16 tensors (torch's own RNE conversion),
+    fp32-free fp64 math for the update -- the oracle's bf16_state rounding must give the same parameters and
+    bf16-representable moments; with the moments left unrounded it differs (the rounding is live)."""
+    rng = np.random.default_rng(4)
+    params = [{"a": rng.standard_normal((6, 5))}]
+    th = torch.tensor(params[0]["a"])
+    m = torch.zeros(6, 5, dtype=torch.bfloat16)
+    v = torch.zeros(6, 5, dtype=torch.bfloat16)
+    st, st32 = O.adam_init(params), O.adam_init(params)
+    p32 = params
+    b1, b2, eps, lr = 0.9, 0.99, 1e-3, 0.01
+    for t in range(1, 5):
+        g = rng.standard_normal((6, 5))
+        mt = b1 * m.double() + (1 - b1) * torch.tensor(g)
+        vt = b2 * v.double() + (1 - b2) * torch.tensor(g) ** 2
+        th = th - lr * (mt / (1 - b1 ** t)) / ((vt / (1 - b2 ** t)).sqrt() + eps)
+        m, v = mt.to(torch.bfloat16), vt.to(torch.bfloat16)
+        params, st = O.adam_update(params, [{"a": g}], st, lr, b1, b2, eps, bf16_state=True)
+        p32, st32 = O.adam_update(p32, [{"a": g}], st32, lr, b1, b2, eps)
+        assert np.abs(params[0]["a"] - th.numpy()).max() <= 1e-12
+        assert np.array_equal(st["m"][0]["a"], m.double().numpy()) and np.array_equal(st["v"][0]["a"], v.double().numpy())
+    assert np.abs(p32[0]["a"] - params[0]["a"]).max() > 1e-9
+
+
 # ------------------------------------------------------------------- paper-literal DCN, Eq.(7) (R31; NEXT#3)
 def _dcnl(X, W, b):
     net = O.NetSpec(X.shape[1], X.shape[2], [O.LayerSpec([O.ModuleSpec("dcn_lit", W.shape[1])])])
