@@ -249,6 +249,25 @@ typedef struct dhen_fp dhen_fp;
  * the device allocation fails. */
 dhen_status dhen_fp_init(const dhen_fp_config* cfg, void* stream, dhen_fp** out);
 
+/* Sharded feature processing (NEXT#4, reading R36): `dist->world` ranks train data-parallel on B samples
+ * each (global sample k B + b = rank k's sample b).  Every table is cut into S_t equal column shards and the shards
+ * are placed on ranks by LPT (dhen_fp_shard_plan; the same plan on every rank); a rank stores only its shards and
+ * the whole bottom MLP (data parallel).  Collective over the ranks (dist->backend: NCCL or loopback, as for the
+ * stack).  Forward: `ids` / `offsets` / `nnz` describe the GLOBAL batch's bags of the tables this rank owns a shard
+ * of (dhen_fp_owned_tables, ascending; bag (k B + b, j) = ids[offsets[(k B + b) n_owned + j] ..]) -- the input
+ * pipeline routes the sparse features, as DLRM data loaders do -- and `dense` this rank's B samples; the rank pools
+ * its shards for all world x B samples, one pooled all-to-all moves every block to its samples' rank, and X0
+ * [B][m0][d] is assembled there.  Backward: the reverse all-to-all gives every shard owner dX0's columns of its
+ * shards, its rows take the sorted-run SGD, and the bottom MLP's gradients are all-reduced (sum, rank order).
+ * world = 1 (or dist = NULL) is dhen_fp_init. */
+dhen_status dhen_fp_init_dist(const dhen_fp_config* cfg, const dhen_dist* dist, void* stream, dhen_fp** out);
+/* The tables this rank owns a shard of (ascending) -> tables[] (nullable: count only); returns their count. */
+int dhen_fp_owned_tables(const dhen_fp* fp, int* tables);
+/* The column-shard plan for `world` ranks: shards[t] = S_t (a power of two: a shard's elements at most half of one
+ * rank's share of all table elements, >= 32 columns each); owner[] = the rank of each shard, tables in order and
+ * shards of a table in column order (sum_t S_t entries).  LPT: largest R_t d / S_t first onto the least-loaded rank. */
+dhen_status dhen_fp_shard_plan(const dhen_fp_config* cfg, int world, int* shards, int* owner);
+
 /* Forward of B samples (device pointers): ids int32 [nnz] (each relative to its table), offsets int32
  * [B n_sparse + 1] with bag (b, t) = ids[offsets[b n_sparse + t] .. offsets[b n_sparse + t + 1]) (empty bags
  * pool to 0), dense [B][n_dense] in dtype (16-B aligned; ignored when n_dtok = 0), x0 [B][m0][d] out (16-B
@@ -262,7 +281,8 @@ dhen_status dhen_fp_forward(dhen_fp* fp, const int* ids, const int* offsets, lon
  * untouched rows unchanged, R34), then W_k, b_k -= lr * their gradients (fp32 masters, copies refreshed). */
 dhen_status dhen_fp_backward_sgd(dhen_fp* fp, const void* dx0, float lr, void* stream);
 
-/* Parameter `which` as fp32 on the host: 0 .. n_sparse-1 table t [R_t][d]; then W_1, b_1, W_2, b_2, ...
+/* Parameter `which` as fp32 on the host: 0 .. n_sparse-1 table t [R_t][d] (sharded: only this rank's column
+ * shards of it are read / written; other columns of `host` are left as they are); then W_1, b_1, W_2, b_2, ...
  * (W_k [out][in]).  set = 1 writes (and refreshes the compute copy), 0 reads.  Synchronises `stream`. */
 dhen_status dhen_fp_params_io(dhen_fp* fp, int which, float* host, int set, void* stream);
 /* Elements of parameter `which` (-1 on an invalid config / index). */

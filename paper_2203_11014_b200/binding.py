@@ -28,7 +28,8 @@ EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "d
            "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_gemm_epi", "dhen_debug_last_gemm_tc",
            "dhen_debug_gemm_trace", "dhen_tuning_default", "dhen_set_tuning", "dhen_get_tuning",
            "dhen_debug_profile_trace", "dhen_fp_init", "dhen_fp_forward", "dhen_fp_backward_sgd", "dhen_fp_params_io",
-           "dhen_fp_param_numel", "dhen_fp_bad_ids", "dhen_fp_destroy")
+           "dhen_fp_param_numel", "dhen_fp_bad_ids", "dhen_fp_destroy", "dhen_fp_init_dist", "dhen_fp_owned_tables",
+           "dhen_fp_shard_plan")
 
 
 class dhen_module(C.Structure):
@@ -121,6 +122,8 @@ def load(path: str = LIB_PATH):
         "dhen_fp_forward": [vp, vp, vp, C.c_longlong, vp, i, vp, vp],
         "dhen_fp_backward_sgd": [vp, vp, C.c_float, vp],
         "dhen_fp_params_io": [vp, i, vp, i, vp],
+        "dhen_fp_init_dist": [C.POINTER(dhen_fp_config), C.POINTER(dhen_dist), vp, C.POINTER(vp)],
+        "dhen_fp_shard_plan": [C.POINTER(dhen_fp_config), i, C.POINTER(i), C.POINTER(i)],
     }
     for name, args in sig.items():
         f = getattr(lib, name, None)
@@ -151,6 +154,8 @@ def load(path: str = LIB_PATH):
         lib.dhen_fp_bad_ids.argtypes = [vp]
         lib.dhen_fp_destroy.restype = None
         lib.dhen_fp_destroy.argtypes = [vp]
+        lib.dhen_fp_owned_tables.restype = C.c_int
+        lib.dhen_fp_owned_tables.argtypes = [vp, C.POINTER(C.c_int)]
     _lib = lib
     return lib
 
@@ -444,7 +449,8 @@ class FeatureProcessing:
     """The feature processing layer in front of the stack (NEXT#4, include/dhen.h dhen_fp_*): sum-pooled
     embedding bags + bottom MLP -> X0 [B][n_dtok + n_sparse][d].  Argument marshalling only."""
 
-    def __init__(self, rows, n_dense, hidden, n_dtok, d, dtype="bf16", max_batch=1, max_nnz=0, seed=0, stream=None):
+    def __init__(self, rows, n_dense, hidden, n_dtok, d, dtype="bf16", max_batch=1, max_nnz=0, seed=0, stream=None,
+                 rank=0, world=1, comm_id=None, backend=NCCL):
         import torch
         self.torch = torch
         self.lib = load()
@@ -455,7 +461,13 @@ class FeatureProcessing:
         self._c = dhen_fp_config(len(self.rows), self._rows, n_dense, len(self.hidden), self._hidden, n_dtok, d,
                                  BF16 if dtype == "bf16" else FP32, max_batch, max_nnz, seed)
         h = C.c_void_p()
-        _check("dhen_fp_init", self.lib.dhen_fp_init(C.byref(self._c), self._stream(stream), C.byref(h)))
+        self.world, self.rank = world, rank
+        if world > 1:   # column-sharded tables over `world` ranks (R36); comm_id from nccl_id() / loopback_id()
+            self._dist = make_dist(rank, world, comm_id, True, backend)
+            _check("dhen_fp_init_dist", self.lib.dhen_fp_init_dist(C.byref(self._c), C.byref(self._dist),
+                                                                   self._stream(stream), C.byref(h)))
+        else:
+            _check("dhen_fp_init", self.lib.dhen_fp_init(C.byref(self._c), self._stream(stream), C.byref(h)))
         self.h = h
         self.m0 = n_dtok + len(self.rows)
         self.n_params = len(self.rows) + 2 * ((len(self.hidden) + 1) if n_dtok > 0 else 0)
@@ -467,19 +479,35 @@ class FeatureProcessing:
     def numel(self, which):
         return self.lib.dhen_fp_param_numel(C.byref(self._c), which)
 
+    def owned_tables(self):
+        n = self.lib.dhen_fp_owned_tables(self.h, None)
+        out = (C.c_int * max(1, n))()
+        self.lib.dhen_fp_owned_tables(self.h, out)
+        return list(out)[:n]
+
+    def plan(self, world):
+        """(shards per table, owner rank of each shard) of the column-shard plan for `world` ranks."""
+        S = (C.c_int * max(1, len(self.rows)))()
+        own = (C.c_int * max(1, len(self.rows) * (self.d // 4)))()
+        _check("dhen_fp_shard_plan", self.lib.dhen_fp_shard_plan(C.byref(self._c), world, S, own))
+        S = list(S)[:len(self.rows)]
+        return S, list(own)[:sum(S)]
+
     def forward(self, ids, offsets, dense, x0, stream=None):
         """ids / offsets int32 CUDA tensors (CSR bags, sample-major), dense [B][n_dense], x0 [B][m0][d] out."""
         B = x0.shape[0]
         _check("dhen_fp_forward", self.lib.dhen_fp_forward(self.h, _ptr(ids), _ptr(offsets), int(ids.numel()),
                                                            _ptr(dense), B, _ptr(x0), self._stream(stream)))
+        self._fwd_refs = (ids, offsets, dense, x0)   # the library reads them again in backward_sgd
 
     def backward_sgd(self, dx0, lr, stream=None):
         _check("dhen_fp_backward_sgd", self.lib.dhen_fp_backward_sgd(self.h, _ptr(dx0), C.c_float(lr),
                                                                      self._stream(stream)))
+        self._bwd_refs, self._fwd_refs = (dx0, getattr(self, "_fwd_refs", None)), None   # (until the next call)
 
     def get(self, which):
         import numpy as np
-        out = np.empty(self.numel(which), np.float32)
+        out = np.zeros(self.numel(which), np.float32)   # (sharded tables: this rank's columns, zeros elsewhere)
         _check("dhen_fp_params_io", self.lib.dhen_fp_params_io(self.h, which, out.ctypes.data_as(C.c_void_p), 0,
                                                                self._stream()))
         return out

@@ -43,12 +43,23 @@ struct NcclComm final : Comm {
     bytes += 2ull * (unsigned long long)(world - 1) * count * (dt == F32 ? 4 : 2) / (unsigned long long)world;
     return chk(ncclAllReduce(send, recv, count, dt == F32 ? ncclFloat32 : ncclBfloat16, ncclSum, c, st), "ncclAllReduce");
   }
+  int all_to_all(const void* send, void* recv, size_t count, int dt, cudaStream_t st) override {
+    const size_t es = dt == F32 ? 4 : 2;
+    bytes += (unsigned long long)(world - 1) * count * es;
+    const ncclDataType_t t = dt == F32 ? ncclFloat32 : ncclBfloat16;
+    if (chk(ncclGroupStart(), "ncclGroupStart")) return 1;
+    for (int k = 0; k < world; ++k) {
+      if (chk(ncclSend((const char*)send + k * count * es, count, t, k, c, st), "ncclSend")) return 1;
+      if (chk(ncclRecv((char*)recv + k * count * es, count, t, k, c, st), "ncclRecv")) return 1;
+    }
+    return chk(ncclGroupEnd(), "ncclGroupEnd");
+  }
   const char* name() const override { return "nccl"; }
 };
 
 // ------------------------------------------------------------------ loopback (virtual ranks, one process)
 constexpr int kMaxLoop = 16;
-constexpr int kAG = 0, kRS = 1, kAR = 2;
+constexpr int kAG = 0, kRS = 1, kAR = 2, kA2A = 3;
 
 struct SumSrc {
   const void* p[kMaxLoop];
@@ -115,7 +126,16 @@ struct LoopComm final : Comm {
       if (cudaStreamWaitEvent(st, sk.ready, 0) != cudaSuccess) { err = "loopback: cudaStreamWaitEvent"; return 1; }
     }
     const size_t n = s0.count;
-    if (s0.kind == kAG) {
+    if (s0.kind == kA2A) {
+      const size_t es = s0.dt == F32 ? 4 : 2;
+      for (int r = 0; r < world; ++r)
+        for (int k = 0; k < world; ++k)
+          if (n && cudaMemcpyAsync((char*)g->slot[r].recv + k * n * es, (const char*)g->slot[k].send + r * n * es, n * es,
+                                   cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+            err = "loopback: all-to-all copy";
+            return 1;
+          }
+    } else if (s0.kind == kAG) {
       const size_t es = s0.dt == F32 ? 4 : 2;
       for (int r = 0; r < world; ++r)
         for (int k = 0; k < world; ++k)
@@ -181,6 +201,10 @@ struct LoopComm final : Comm {
   int all_reduce(const void* send, void* recv, size_t count, int dt, cudaStream_t st) override {
     bytes += 2ull * (unsigned long long)(world - 1) * count * (dt == F32 ? 4 : 2) / (unsigned long long)world;
     return collective(kAR, send, recv, count, dt, st);
+  }
+  int all_to_all(const void* send, void* recv, size_t count, int dt, cudaStream_t st) override {
+    bytes += (unsigned long long)(world - 1) * count * (dt == F32 ? 4 : 2);
+    return collective(kA2A, send, recv, count, dt, st);
   }
   const char* name() const override { return "loopback"; }
 };

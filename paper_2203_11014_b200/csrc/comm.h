@@ -13,7 +13,8 @@
 //     one-GPU machine (tests/test_gpu_fsdp.py).
 // Both count the bytes each rank moves with the ring-collective convention: an all-gather of `count`
 // elements per rank receives (G - 1) count elements, a reduce-scatter to `count` per rank sends
-// (G - 1) count, an all-reduce of n elements moves 2 (G - 1) / G n.  The reductions take fp32 or bf16
+// (G - 1) count, an all-reduce of n elements moves 2 (G - 1) / G n, an all-to-all of `count` per peer sends
+// (G - 1) count.  The reductions take fp32 or bf16
 // operands (bf16: the paper's quantized collectives, P:158 / P:277; the loopback sums in fp32 in rank order
 // and rounds once, NCCL rounds per ring hop).
 #pragma once
@@ -34,6 +35,9 @@ struct Comm {
   virtual int reduce_scatter(const void* send, void* recv, size_t count, int dt, cudaStream_t st) = 0;
   // recv[i] = sum over ranks k (in rank order) of send_k[i]
   virtual int all_reduce(const void* send, void* recv, size_t count, int dt, cudaStream_t st) = 0;
+  // recv[k * count + i] = send of rank k [rank * count + i] (equal blocks; the feature-processing layer's pooled
+  // embedding exchange)
+  virtual int all_to_all(const void* send, void* recv, size_t count, int dt, cudaStream_t st) = 0;
   virtual const char* name() const = 0;
 };
 

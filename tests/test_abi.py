@@ -118,3 +118,38 @@ def test_fp_param_numel_and_validation(B):
     h = C.c_void_p()
     assert lib.dhen_fp_init(C.byref(bad), None, C.byref(h)) == 1 and not h.value
     assert b"d = 130" in lib.dhen_last_error()
+
+
+def test_fp_shard_plan_lpt(B):
+    """The column-shard plan (R36), host only: a table larger than half of a rank's share is cut into
+    power-of-two column shards of >= 32 columns, every shard has one owner, and LPT keeps every rank's load
+    within one largest shard of the average (the greedy bound); one rank keeps every table whole."""
+    import ctypes as C
+    lib = B.load()
+    rows = [1_000_000, 200_000, 50_000, 50_000, 3_000, 10, 900_000, 120_000]
+    d = 256
+    r = (C.c_longlong * len(rows))(*rows)
+    cfg = B.dhen_fp_config(len(rows), r, 8, 0, None, 1, d, B.BF16, 64, 1000, 0)
+    for world in (1, 2, 4, 8):
+        S = (C.c_int * len(rows))()
+        own = (C.c_int * (len(rows) * d // 32))()
+        assert lib.dhen_fp_shard_plan(C.byref(cfg), world, S, own) == 0
+        S = list(S)
+        assert all(s & (s - 1) == 0 and d // s >= 32 for s in S)
+        owners = list(own)[:sum(S)]
+        assert all(0 <= o < world for o in owners)
+        if world == 1:
+            assert S == [1] * len(rows) and owners == [0] * len(rows)
+            continue
+        share = sum(rows) * d / world
+        cost, load = [], [0.0] * world
+        k = 0
+        for t, s in enumerate(S):
+            if rows[t] * d / s > share / 2:
+                assert d // (2 * s) < 32   # only when a further cut would drop below 32 columns
+            for _ in range(s):
+                c = rows[t] * d / s
+                cost.append(c)
+                load[owners[k]] += c
+                k += 1
+        assert max(load) <= share + max(cost) + 1e-6

@@ -138,3 +138,88 @@ def test_fp_timed_size_sampled():
             lo, hi = off[b * ns + t], off[b * ns + t + 1]
             ref = FO.round_bf16(FO.embedding_bag_sum(T, ids[lo:hi]))
             assert np.all(np.abs(X[b, n_dtok + t] - ref) <= np.abs(ref) * 2.0 ** -7 + 1e-6)
+
+
+def _sharded(rows, n_dense, hidden, n_dtok, d, B, world, dtype="bf16", seed=5, lr=0.5):
+    """One forward + backward/SGD of the column-sharded layer at `world` loopback ranks (B samples each) and the
+    same global batch on one unsharded object."""
+    import threading
+    import torch
+    from paper_2203_11014_b200 import binding
+    from paper_2203_11014_b200.binding import FeatureProcessing
+    bf = dtype == "bf16"
+    tdt = torch.bfloat16 if bf else torch.float32
+    Bg, ns = world * B, len(rows)
+    ids, off, dense = synth.make_fp_batch(seed, Bg, rows, n_dense, 6.0, bf16=bf, empty_frac=0.1)
+    G = synth.make_x0(seed + 5, Bg, n_dtok + ns, d, bf16=bf) * 0.1
+    G = FO.round_bf16(G.astype(np.float64)) if bf else G
+    # world 1 on the whole global batch
+    ref = FeatureProcessing(rows, n_dense, hidden, n_dtok, d, dtype=dtype, max_batch=Bg, max_nnz=len(ids), seed=seed)
+    x_ref = torch.empty(Bg, n_dtok + ns, d, device="cuda", dtype=tdt)
+    ref.forward(torch.tensor(ids, device="cuda"), torch.tensor(off, device="cuda"),
+                torch.tensor(dense, device="cuda").to(tdt).contiguous(), x_ref)
+    ref.backward_sgd(torch.tensor(G, dtype=torch.float32, device="cuda").to(tdt), lr)
+    torch.cuda.synchronize()
+    nP = ns + 2 * (len(hidden) + 1)
+    P_ref = [ref.get(w) for w in range(nP)]
+    X_ref = x_ref.float().cpu().numpy()
+    nid = binding.loopback_id()
+    out, errs = [None] * world, []
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                probe = FeatureProcessing(rows, n_dense, hidden, n_dtok, d, dtype=dtype, max_batch=B, max_nnz=1, seed=seed)
+                S, own = probe.plan(world)
+                probe.close()
+                owned = sorted({t for t in range(ns) for k in range(S[t]) if own[sum(S[:t]) + k] == r})
+                rid, roff = [], [0]   # the global batch's bags of the owned tables, (sample, owned table) order
+                for b in range(Bg):
+                    for t in owned:
+                        seg = ids[off[b * ns + t]:off[b * ns + t + 1]]
+                        rid.extend(seg.tolist())
+                        roff.append(roff[-1] + len(seg))
+                fp = FeatureProcessing(rows, n_dense, hidden, n_dtok, d, dtype=dtype, max_batch=B,
+                                       max_nnz=max(1, len(rid)), seed=seed, rank=r, world=world, comm_id=nid,
+                                       backend=binding.LOOPBACK)
+                assert fp.owned_tables() == owned
+                x0 = torch.empty(B, n_dtok + ns, d, device="cuda", dtype=tdt)
+                fp.forward(torch.tensor(np.array(rid, np.int32), device="cuda"),
+                           torch.tensor(np.array(roff, np.int32), device="cuda"),
+                           torch.tensor(dense[r * B:(r + 1) * B], device="cuda").to(tdt).contiguous(), x0)
+                fp.backward_sgd(torch.tensor(G[r * B:(r + 1) * B], dtype=torch.float32, device="cuda").to(tdt), lr)
+                s.synchronize()
+                out[r] = {"X0": x0.float().cpu().numpy(), "P": [fp.get(w) for w in range(nP)], "owned": owned, "fp": fp}
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append((r, repr(e)))
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    return X_ref, P_ref, out, ns
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fp_sharded_matches_single(world):
+    """Column-sharded tables over `world` loopback ranks (LPT plan, pooled all-to-all forward and backward,
+    data-parallel bottom MLP with an all-reduce) against one object holding every table, on the same global
+    batch: X0 of every rank's samples and every table after the sparse SGD are bit-identical (the same sums in
+    the same order), the bottom MLP within fp32 rounding of the split batch (rank-order all-reduce)."""
+    rows, d = (300, 40, 1000, 7, 64), 128      # a large table is cut into column shards, small ones stay whole
+    X_ref, P_ref, out, ns = _sharded(rows, 16, (32,), 2, d, 12, world)
+    B = 12
+    for r, o in enumerate(out):
+        assert np.array_equal(o["X0"], X_ref[r * B:(r + 1) * B]), r
+    for t in range(ns):   # each rank fills the columns of its shards; together they cover the table once
+        merged = np.zeros_like(P_ref[t])
+        for o in out:
+            merged += o["P"][t]
+        assert np.array_equal(merged, P_ref[t]), t
+    for w in range(ns, len(P_ref)):
+        for o in out:
+            assert norm_err(o["P"][w].astype(np.float64), P_ref[w].astype(np.float64)) <= 1e-5, w
