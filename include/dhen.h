@@ -62,6 +62,8 @@ typedef enum {
   DHEN_DCN = 3,    /* Eq.(7) north star: T = X (.) (X W^T + b) + X per token, U = W_u^T T          */
   DHEN_LINEAR = 4, /* Eq.(6): U = W^T X on the token axis                                          */
   DHEN_MLP = 5,    /* U = reshape(W_m relu(W_2 relu(W_1 vec(X) + b_1) + b_2), l, d)           */
+  DHEN_DCN_FULL = 7,/* flattened full-rank DCN-v2 (NEXT#3, R37): x = vec(X) in R^{m d}, A = x W^T + b with W in
+                      R^{md x md}, T = x (.) A + x, U = W_u^T T (tokens)                                   */
   DHEN_DCN_LIT = 6 /* Eq.(7) read literally (NEXT#3, R31): per sample G = X_n X_n^T (d x d Gram over
                       tokens), u = G W + b, W in R^{d x l}, b in R^{l x d}; U[t][c] = (G W)[c][t] + b[t][c]  */
 } dhen_kind;

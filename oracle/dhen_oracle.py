@@ -35,7 +35,7 @@ import numpy as np
 # --------------------------------------------------------------------------
 # configuration (the oracle's own; the product has its own C structs)
 # --------------------------------------------------------------------------
-KINDS = ("dot", "attn", "conv", "dcn", "linear", "mlp", "dcn_lit")
+KINDS = ("dot", "attn", "conv", "dcn", "linear", "mlp", "dcn_lit", "dcn_full")
 
 
 @dataclass
@@ -116,6 +116,8 @@ def module_param_shapes(s: ModuleSpec, m: int, d: int) -> List[Tuple[str, Tuple[
         return [("W", (d, l), d), ("b", (l, d), d)]
     if s.kind == "dcn":
         return [("W", (d, d), d), ("b", (d,), d), ("W_u", (m, l), m)]
+    if s.kind == "dcn_full":   # the flattened full-rank DCN-v2 (R37): W ∈ R^{md×md} on vec(X)
+        return [("W", (m * d, m * d), m * d), ("b", (m * d,), m * d), ("W_u", (m, l), m)]
     if s.kind == "conv":
         k = s.conv_k
         return [("K", (s.conv_channels, k, k), k * k), ("W_u", (m, l), m)]
@@ -331,6 +333,25 @@ def dcn_bwd(X, p, s, c, dU, pr):
     return dX, {"W": dW, "b": db, "W_u": dWu}
 
 
+def dcn_full_fwd(X, p, s, pr):
+    """Flattened full-rank DCN-v2 (NEXT#3, SURVEY ledger 13, R37): the sample x = vec(X) ∈ R^{m·d} (token rows in
+    order), A = x Wᵀ + b with W ∈ R^{md×md}, T = x ⊙ A + x, read back as m tokens; then the unify map W_u."""
+    B, m, d = X.shape
+    A = (X.reshape(B, m * d) @ p["W"].T + p["b"]).reshape(B, m, d)
+    T = pr.q("dcn.T", X * A + X)
+    A = pr.q("dcn.A", A)
+    return tokmix_fwd(T, p["W_u"]), {"A": A, "T": T}
+
+
+def dcn_full_bwd(X, p, s, c, dU, pr):
+    B, m, d = X.shape
+    dT, dWu = tokmix_bwd(c["T"], p["W_u"], dU)
+    dA = pr.q("dcn.dA", dT * X)
+    dAf, Xf = dA.reshape(B, m * d), X.reshape(B, m * d)
+    dX = dT * c["A"] + dT + (dAf @ p["W"]).reshape(B, m, d)
+    return dX, {"W": dAf.T @ Xf, "b": dAf.sum(0), "W_u": dWu}
+
+
 def dcn_lit_fwd(X, p, s, pr):
     """Eq.(7) read literally (NEXT#3; R31 after SPEC S:219-222 / S:235): per sample the d x d
     Gram over tokens G = X_n X_nᵀ (X_n = Xᵀ is d x m, so G[c][k] = Σ_i X[i][c] X[i][k]), u = G W + b with
@@ -530,7 +551,7 @@ def layer_fwd(net: NetSpec, n: int, X: np.ndarray, P: Dict[str, np.ndarray], pr:
         if s.kind == "attn":
             U, c = attn_fwd(X, p, s, pr, net.ln_eps)
         else:
-            U, c = {"dot": dot_fwd, "linear": linear_fwd, "dcn": dcn_fwd, "dcn_lit": dcn_lit_fwd,
+            U, c = {"dot": dot_fwd, "linear": linear_fwd, "dcn": dcn_fwd, "dcn_lit": dcn_lit_fwd, "dcn_full": dcn_full_fwd,
                     "conv": conv_fwd, "mlp": mlp_fwd}[s.kind](X, p, s, pr)
         us.append(U)
         caches.append(c)
@@ -571,7 +592,8 @@ def layer_bwd(net: NetSpec, n: int, cache, dY: np.ndarray, P, pr: Precision = FP
             dU = dR
         else:
             dU = pr.q("ens.dU", P["ens_w"][i] * dR)
-        fn = {"dot": dot_bwd, "linear": linear_bwd, "dcn": dcn_bwd, "dcn_lit": dcn_lit_bwd, "conv": conv_bwd,
+        fn = {"dot": dot_bwd, "linear": linear_bwd, "dcn": dcn_bwd, "dcn_lit": dcn_lit_bwd, "dcn_full": dcn_full_bwd,
+              "conv": conv_bwd,
               "attn": attn_bwd, "mlp": mlp_bwd}[s.kind]
         dXi, gi = fn(X, p, s, cache["mods"][i], dU, pr)
         dX = dX + dXi
@@ -698,6 +720,8 @@ def forward_flops_per_sample(net: NetSpec) -> int:
                 tot += 2 * d * d * m_in + 2 * d * d * l
             elif s.kind == "dcn":
                 tot += 2 * m_in * d * d + 2 * m_in * l * d
+            elif s.kind == "dcn_full":
+                tot += 2 * (m_in * d) ** 2 + 2 * m_in * l * d
             elif s.kind == "conv":
                 tot += 2 * m_in * d * s.conv_k * s.conv_k + 2 * m_in * l * d
             elif s.kind == "attn":

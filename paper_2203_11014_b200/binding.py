@@ -13,8 +13,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdhen.so")
 WD_LIB_PATH = os.path.join(HERE, "libdhen_wd.so")   # debug build: bounded mbarrier waits (build.py --watchdog)
 
-DOT, ATTN, CONV, DCN, LINEAR, MLP, DCN_LIT = range(7)
-KIND_IDS = {"dot": DOT, "attn": ATTN, "conv": CONV, "dcn": DCN, "linear": LINEAR, "mlp": MLP, "dcn_lit": DCN_LIT}
+DOT, ATTN, CONV, DCN, LINEAR, MLP, DCN_LIT, DCN_FULL = range(8)
+KIND_IDS = {"dot": DOT, "attn": ATTN, "conv": CONV, "dcn": DCN, "linear": LINEAR, "mlp": MLP, "dcn_lit": DCN_LIT,
+            "dcn_full": DCN_FULL}
 FP32, BF16 = 0, 1
 
 STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_SHAPE", 3: "E_ALIGN", 4: "E_STATE", 5: "E_CUDA", 6: "E_NCCL",

@@ -269,7 +269,7 @@ static dhen_status validate(const dhen_config* c) {
       if (L.ensemble != DHEN_CONCAT && s.l != L.modules[0].l)
         return fail(DHEN_E_CONFIG, "dhen_validate: layer %d sum ensemble with l=%d and l=%d (P:91 needs equal l_i)", n,
                     L.modules[0].l, s.l);
-      if (s.kind < DHEN_DOT || s.kind > DHEN_DCN_LIT) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d module %d kind=%d", n, i, s.kind);
+      if (s.kind < DHEN_DOT || s.kind > DHEN_DCN_FULL) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d module %d kind=%d", n, i, s.kind);
       if (s.l < 1) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d module %d l=%d < 1", n, i, s.l);
       if (s.kind == DHEN_DOT && m < 2) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d Dot needs m >= 2, m=%d (S:186)", n, m);
       if (s.kind == DHEN_ATTN && c->d % mdef(s.heads, 2) != 0)
@@ -338,6 +338,11 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
         case DHEN_DOT: { int h = m * (m - 1) / 2; md.Wm = tensor((int64_t)l * d * h, 0, h); break; }
         case DHEN_LINEAR: md.W = tensor((int64_t)m * l, 0, m); break;
         case DHEN_DCN: md.W = tensor((int64_t)d * d, 0, d); md.b = tensor(d, 0, d); md.Wu = tensor((int64_t)m * l, 0, m); break;
+        case DHEN_DCN_FULL: {   // R37: the cross over the flattened sample, W [m d][m d]
+          const int64_t f = (int64_t)m * d;
+          md.W = tensor(f * f, 0, (int)f); md.b = tensor(f, 0, (int)f); md.Wu = tensor((int64_t)m * l, 0, m);
+          break;
+        }
         case DHEN_CONV: { int k = md.s.conv_k; md.K = tensor((int64_t)md.s.conv_channels * k * k, 0, k * k); md.Wu = tensor((int64_t)m * l, 0, m); break; }
         case DHEN_ATTN: {
           int f = md.s.ffn_mult * d;
@@ -419,7 +424,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
           H_mm_max = std::max(H_mm_max, mi * mi);
           tA_elems = std::max<int64_t>(tA_elems, (int64_t)B * (mi * (mi - 1) / 2));
           break;
-        case DHEN_DCN: md.A = work.take(tok * es); md.T = work.take(tok * es); break;
+        case DHEN_DCN: case DHEN_DCN_FULL: md.A = work.take(tok * es); md.T = work.take(tok * es); break;
         case DHEN_DCN_LIT:
           md.G = work.take((size_t)B * d * d * es);
           md.S = work.take((size_t)B * d * d * es);
@@ -465,7 +470,7 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
       md.bdT = work.take((size_t)128 * 128 * 8 * 2);   // spt m <= 1024 columns
       if (Lr.ens != DHEN_CONCAT) md.Uo = (float*)work.take((size_t)B * mo * d * 4);
       if (Lr.ens == DHEN_WSUM) md.dUs = work.take((size_t)B * mo * d * es);
-      if (md.s.kind == DHEN_DCN) md.bdg = work.take((size_t)128 * 128 * 2);
+      if (md.s.kind == DHEN_DCN || md.s.kind == DHEN_DCN_FULL) md.bdg = work.take((size_t)128 * 128 * 2);
     }
   }
   if (fsh_elems) {   // recompute: one F / bitmask buffer for every attention module
@@ -806,11 +811,13 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
       case DHEN_LINEAR:  // F10 with T = X
         RET(emit_tm(X, p(md.W)));
         break;
-      case DHEN_DCN: {   // F8: A = X W^T + b ; T = X * A + X
-        Gemm g = mk((int)rows, d, d, 1, operand(X, dt, d, 1), operand(p(md.W), dt, d, 1), view(md.T, dt, d, 1));
+      case DHEN_DCN: case DHEN_DCN_FULL: {   // F8: A = X W^T + b ; T = X * A + X (per token, or R37 per sample)
+        const bool flat = md.s.kind == DHEN_DCN_FULL;
+        const int w = flat ? mi * d : d;
+        Gemm g = mk(flat ? B : (int)rows, w, w, 1, operand(X, dt, w, 1), operand(p(md.W), dt, w, 1), view(md.T, dt, w, 1));
         g.e.bias = p(md.b); g.e.bias_dt = dt;
-        g.e.cross = view((void*)X, dt, d, 1);
-        g.e.aux = view(md.A, dt, d, 1);
+        g.e.cross = view((void*)X, dt, w, 1);
+        g.e.aux = view(md.A, dt, w, 1);
         RET(G_(g, c, st, "dcn.cross"));
         RET(emit_tm(md.T, p(md.Wu)));
         break;
@@ -960,7 +967,8 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   std::vector<Mod*> order;
   {
     int best = -1, best_rank = 99;
-    const int rank_of[7] = {3 /*DOT*/, 99 /*ATTN*/, 99 /*CONV*/, 0 /*DCN*/, 1 /*LINEAR*/, 2 /*MLP*/, 99 /*DCN_LIT*/};
+    const int rank_of[8] = {3 /*DOT*/, 99 /*ATTN*/, 99 /*CONV*/, 0 /*DCN*/, 1 /*LINEAR*/, 2 /*MLP*/, 99 /*DCN_LIT*/,
+                            0 /*DCN_FULL*/};
     for (int i = 0; i < (int)Lr.mods.size(); ++i) {
       const int rk = rank_of[Lr.mods[i].s.kind];
       if (rk < best_rank) { best_rank = rk; best = i; }
@@ -971,7 +979,8 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   }
   const int first_kind = order.empty() ? -1 : order[0]->s.kind;
   const bool first_dR = c->tune.first_writer && Lr.Wn < 0 && mi == mo &&
-                        (first_kind == DHEN_DOT || first_kind == DHEN_DCN || first_kind == DHEN_LINEAR || first_kind == DHEN_MLP);
+                        (first_kind == DHEN_DOT || first_kind == DHEN_DCN || first_kind == DHEN_DCN_FULL ||
+                         first_kind == DHEN_LINEAR || first_kind == DHEN_MLP);
   // Weight gradients of a module run on the side stream `sd` (own split-K / reduction scratch) while its
   // data gradients run on `st`; `fork` hands the side stream everything enqueued on st so far, and st waits
   // for the side stream before it overwrites a shared buffer that pending side work reads (and at layer end).
@@ -996,7 +1005,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   auto st_writes = [](int k) -> uint32_t {
     switch (k) {
       case DHEN_DOT: return 1u | 8u;      // dZ (tA), S (tD)
-      case DHEN_DCN: return 2u | 16u;     // dA (tB), dA column sums (bsum)
+      case DHEN_DCN: case DHEN_DCN_FULL: return 2u | 16u;     // dA (tB), dA column sums (bsum)
       case DHEN_ATTN: return 1u | 2u | 4u | 8u | 32u | 64u | 128u | 256u | 512u | 1024u;   // (1024: F, when shared)
       case DHEN_CONV: case DHEN_MLP: case DHEN_LINEAR: case DHEN_DCN_LIT: return 0u;   // own scratch / the dX accumulator
       default: return ~0u;
@@ -1004,7 +1013,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   };
   auto side_reads = [](int k) -> uint32_t {
     switch (k) {
-      case DHEN_DCN: return 2u | 16u;     // dA, its column sums
+      case DHEN_DCN: case DHEN_DCN_FULL: return 2u | 16u;     // dA, its column sums
       case DHEN_ATTN: return 1u | 2u | 4u | 64u | 512u | 1024u;   // dR2 (tA), dR1 (tB), dF (tC), dQKV (tF), db1, F
       case DHEN_DOT: case DHEN_CONV: case DHEN_MLP: case DHEN_LINEAR: case DHEN_DCN_LIT: return 0u;   // saved / own buffers
       default: return ~0u;
@@ -1025,7 +1034,8 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   // accumulator is read once and never written back, and no cast kernel runs.
   const int last_kind = order.empty() ? -1 : order.back()->s.kind;
   const bool last_dX = dX && c->tune.first_writer &&
-                       (last_kind == DHEN_DOT || last_kind == DHEN_DCN || last_kind == DHEN_LINEAR || last_kind == DHEN_MLP);
+                       (last_kind == DHEN_DOT || last_kind == DHEN_DCN || last_kind == DHEN_DCN_FULL ||
+                        last_kind == DHEN_LINEAR || last_kind == DHEN_MLP);
   bool first_mod = true;
   for (Mod* mdp : order) {
     Mod& md = *mdp;
@@ -1093,7 +1103,10 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
           RET(tokmix_bwd(c, X, mi, p(md.W), l, dU, ldU, acc, F32, 1, gp(md.W), B, st, sd, ws2, take_dR ? c->dR : nullptr));
         RET(join());
         break;
-      case DHEN_DCN: {   // B8
+      case DHEN_DCN: case DHEN_DCN_FULL: {   // B8 (R37: the dA W and dW contractions over the flattened sample)
+        const bool flat = md.s.kind == DHEN_DCN_FULL;
+        const int wf = flat ? mi * d : d;            // width of the cross contraction
+        const int64_t rf = flat ? B : rows;          // its rows
         void* dA = c->tB;
         RET(fork());
         {   // dW_u += sum T dU (side stream; needs only saved T and dU)
@@ -1109,10 +1122,10 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         const int spt = 128 / std::max(mi, 1);
         const bool pack = dcn_pack(c, mi, l, B);
         // the bias gradient's column sums of dA come out of the dT GEMM's epilogue (one partial row per CTA)
-        const bool fuse_db = c->tune.fuse_db && dt == BF16 && d <= 256;
+        const bool fuse_db = c->tune.fuse_db && dt == BF16 && d <= 256 && !flat;   // (flat: db has m d entries)
         int bsum_rows = 0;
         const double dU_in_dR = take_dR ? (double)B * l * d * es : 0.0;   // dU is a slice of the dR residual
-        const bool fused_bwd = c->tune.dcn_fused && dt == BF16 && (mi == 128 || pack) &&
+        const bool fused_bwd = !flat && c->tune.dcn_fused && dt == BF16 && (mi == 128 || pack) &&
                                dcnb::supported(B, mi, l, d, ldU, take_dR ? 0 : 1, emit_dX ? 0 : 1);
         if (fused_bwd) {
           // one kernel: dT = W_u dU, dA = dT (.) X, dX = base + dT (.) A + dT + dA W (partial dX in TMEM)
@@ -1156,18 +1169,18 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
         }
         if (sd != st) { CK(cudaEventRecord(c->ev_sx, st)); CK(cudaStreamWaitEvent(sd, c->ev_sx, 0)); }   // dA ready
         if (!fused_bwd) {
-          Gemm gx = mk((int)rows, d, d, 1, operand(dA, dt, d, 1), operand(p(md.W), dt, 1, d), view(acc, F32, d, 1));
+          Gemm gx = mk((int)rf, wf, wf, 1, operand(dA, dt, wf, 1), operand(p(md.W), dt, 1, wf), view(acc, F32, wf, 1));
           gx.e.accumulate = 1;
-          if (emit_dX) { gx.e.accumulate = 0; gx.e.resid = view(acc, F32, d, 1); gx.c = view(dX, dt, d, 1); }   // dX = acc + dA W
+          if (emit_dX) { gx.e.accumulate = 0; gx.e.resid = view(acc, F32, wf, 1); gx.c = view(dX, dt, wf, 1); }   // dX = acc + dA W
           RET(G_(gx, c, st, "dcn.dgrad"));
         }
-        Gemm gw = mk(d, d, (int)rows, 1, operand(dA, dt, 1, d), operand(X, dt, 1, d), view(gp(md.W), F32, d, 1));
+        Gemm gw = mk(wf, wf, (int)rf, 1, operand(dA, dt, 1, wf), operand(X, dt, 1, wf), view(gp(md.W), F32, wf, 1));
         gw.e.accumulate = 1;
         RET(G_(gw, c, sd, "dcn.wgrad", ws2));
         if (bsum_rows > 0)
           KTS(sd, "dcn.bias_grad", 0, (double)bsum_rows * d * 4, rows_sum_add(c->bsum, bsum_rows, d, gp(md.b), sd));
         else
-          KTS(sd, "dcn.bias_grad", 0, (double)rows * d * es, colsum_add(dA, dt, rows, d, d, gp(md.b), red2, c->red_bytes, sd));
+          KTS(sd, "dcn.bias_grad", 0, (double)rows * d * es, colsum_add(dA, dt, rf, wf, wf, gp(md.b), red2, c->red_bytes, sd));
         RET(join());
         break;
       }
@@ -1372,12 +1385,13 @@ static dhen_status prebuild_bd(dhen_ctx* c, int B, cudaStream_t st) {
     for (Mod& md : Lr.mods) {
       const int l = md.s.l;
       const int64_t wu = md.s.kind == DHEN_LINEAR ? md.W : md.Wu;
-      const bool tm = md.s.kind == DHEN_LINEAR || md.s.kind == DHEN_DCN || md.s.kind == DHEN_CONV || md.s.kind == DHEN_ATTN;
+      const bool tm = md.s.kind == DHEN_LINEAR || md.s.kind == DHEN_DCN || md.s.kind == DHEN_DCN_FULL ||
+                      md.s.kind == DHEN_CONV || md.s.kind == DHEN_ATTN;
       if (tm && lnf && md.bdT && jobs.n < 32) {
         jobs.job[jobs.n++] = {(const __nv_bfloat16*)p(wu), (__nv_bfloat16*)md.bdT, mi, l, 128 / l, 1};
         md.bdT_pre = true;
       }
-      if (md.s.kind == DHEN_DCN && md.bdg && dcn_pack(c, mi, l, B) && jobs.n < 32) {
+      if ((md.s.kind == DHEN_DCN || md.s.kind == DHEN_DCN_FULL) && md.bdg && dcn_pack(c, mi, l, B) && jobs.n < 32) {
         jobs.job[jobs.n++] = {(const __nv_bfloat16*)p(md.Wu), (__nv_bfloat16*)md.bdg, mi, l, 128 / std::max(mi, 1), 0};
         md.bdg_pre = true;
       }

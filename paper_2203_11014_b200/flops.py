@@ -23,6 +23,8 @@ def forward_flops_per_sample(cfg) -> int:
                 tot += 2 * d * d * mi + 2 * d * d * l     # per-sample d x d Gram + projection (Eq.(7) literal)
             elif s.kind == "dcn":
                 tot += 2 * mi * d * d + tok
+            elif s.kind == "dcn_full":
+                tot += 2 * (mi * d) ** 2 + tok          # the cross over the flattened sample (R37)
             elif s.kind == "conv":
                 tot += 2 * mi * d * s.conv_k ** 2 + tok
             elif s.kind == "attn":

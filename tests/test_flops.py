@@ -53,6 +53,10 @@ def _module_forward(kind, s, m, d):
         from torch.nn.attention import SDPBackend, sdpa_kernel
         with sdpa_kernel(SDPBackend.MATH):
             return torch.matmul(Wu.t(), enc(X))
+    if kind == "dcn_full":   # R37: the cross on the flattened sample
+        x = X.reshape(1, m * d)
+        A = F.linear(x, torch.randn(m * d, m * d), torch.randn(m * d))
+        return torch.matmul(Wu.t(), (x * A + x).reshape(1, m, d))
     if kind == "dcn_lit":
         Xn = X.transpose(1, 2)
         return (torch.matmul(torch.bmm(Xn, Xn.transpose(1, 2)), torch.randn(d, l)).transpose(1, 2) + torch.randn(l, d))
@@ -87,7 +91,7 @@ def _binding_cfg(net):
                                           tuple(s.mlp_hidden)) for s in L.modules] for L in net.layers])
 
 
-@pytest.mark.parametrize("kind", ["dot", "linear", "dcn", "conv", "attn", "mlp", "dcn_lit"])
+@pytest.mark.parametrize("kind", ["dot", "linear", "dcn", "conv", "attn", "mlp", "dcn_lit", "dcn_full"])
 def test_module_flops_vs_torch_counter(kind):
     from paper_2203_11014_b200 import flops
     m, d = 12, 32

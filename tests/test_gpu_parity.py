@@ -376,3 +376,16 @@ def test_dcn_literal_matches_oracle(dtype, tol, m, d, l, B):
     g = case.gpu_step(lr=0.05)
     o = case.oracle_step(lr=0.05)
     _compare(case, g, o, tol, tol, label=f"paper-literal DCN {dtype} m={m} d={d}")
+
+
+@pytest.mark.parametrize("dtype,tol,m,d,l,B", [("fp32", 1e-5, 8, 16, 4, 19), ("bf16", 2e-2, 8, 16, 4, 19),
+                                               ("bf16", 2e-2, 16, 32, 8, 40)])
+def test_dcn_full_matches_oracle(dtype, tol, m, d, l, B):
+    """NEXT#3 method variant: the flattened full-rank DCN-v2 (R37: the cross on vec(X) with W in R^{md x md}) as a
+    module next to the others, two layers (the second its dX's first and last writer), full train step against
+    the oracle (G1 / G3)."""
+    net = O.NetSpec(m, d, [O.LayerSpec([M("dcn_full", l), M("linear", m - l)]), O.LayerSpec([M("dcn_full", m)])])
+    case = Case(net, B, dtype, seed=2203011014 + 12)
+    g = case.gpu_step(lr=0.05)
+    o = case.oracle_step(lr=0.05)
+    _compare(case, g, o, tol, tol, label=f"flattened DCN {dtype} m={m} d={d}")

@@ -403,6 +403,43 @@ def test_adam_bf16_state_matches_torch_bf16_loop():
     assert np.abs(p32[0]["a"] - params[0]["a"]).max() > 1e-9
 
 
+# ------------------------------------------------------------------- flattened full-rank DCN-v2 (R37; NEXT#3)
+def test_dcn_full_vs_torch_autograd():
+    B, m, d, l = 3, 4, 5, 3
+    s = O.ModuleSpec("dcn_full", l)
+    X, W, b, Wu = rnd(B, m, d), rnd(m * d, m * d, scale=0.2), rnd(m * d), rnd(m, l)
+    p = {"W": W, "b": b, "W_u": Wu}
+    U, cache = O.dcn_full_fwd(X, p, s, O.FP64)
+    dU = rnd(B, l, d)
+    dX, g = O.dcn_full_bwd(X, p, s, cache, dU, O.FP64)
+    Xt, Wt, bt, Wut = t(X, True), t(W, True), t(b, True), t(Wu, True)
+    x = Xt.reshape(B, m * d)
+    A = F.linear(x, Wt, bt)
+    Ut = torch.matmul(Wut.t(), (x * A + x).reshape(B, m, d))
+    assert np.abs(U - Ut.detach().numpy()).max() < 1e-12
+    (Ut * t(dU)).sum().backward()
+    for a, ref in ((dX, Xt), (g["W"], Wt), (g["b"], bt), (g["W_u"], Wut)):
+        assert np.abs(a - ref.grad.numpy()).max() < 1e-10
+
+
+def test_dcn_full_reduces_to_per_token_dcn():
+    """A block-diagonal W = I_m (x) W_tok and b = (b_tok, .., b_tok) make the flattened cross the per-token
+    north-star DCN (R13): same output, same dX, and the diagonal blocks of dW sum to the per-token dW."""
+    B, m, d, l = 2, 3, 4, 2
+    Wt, bt, Wu = rnd(d, d, scale=0.3), rnd(d), rnd(m, l)
+    X, dU = rnd(B, m, d), rnd(B, l, d)
+    pf = {"W": np.kron(np.eye(m), Wt), "b": np.tile(bt, m), "W_u": Wu}
+    pt = {"W": Wt, "b": bt, "W_u": Wu}
+    Uf, cf = O.dcn_full_fwd(X, pf, O.ModuleSpec("dcn_full", l), O.FP64)
+    Ut, ct = O.dcn_fwd(X, pt, O.ModuleSpec("dcn", l), O.FP64)
+    assert np.abs(Uf - Ut).max() < 1e-12
+    dXf, gf = O.dcn_full_bwd(X, pf, O.ModuleSpec("dcn_full", l), cf, dU, O.FP64)
+    dXt, gt = O.dcn_bwd(X, pt, O.ModuleSpec("dcn", l), ct, dU, O.FP64)
+    assert np.abs(dXf - dXt).max() < 1e-12
+    assert np.abs(sum(gf["W"][i * d:(i + 1) * d, i * d:(i + 1) * d] for i in range(m)) - gt["W"]).max() < 1e-12
+    assert np.abs(gf["b"].reshape(m, d).sum(0) - gt["b"]).max() < 1e-12
+
+
 # ------------------------------------------------------------------- paper-literal DCN, Eq.(7) (R31; NEXT#3)
 def _dcnl(X, W, b):
     net = O.NetSpec(X.shape[1], X.shape[2], [O.LayerSpec([O.ModuleSpec("dcn_lit", W.shape[1])])])
