@@ -61,7 +61,8 @@ __device__ __forceinline__ void arrive(uint32_t a) {
 }
 
 // barrier indices
-enum { BC = 0, BUF = 1, BUE = 2, BD1 = 3, BDA = 4, BD2 = 5, BTF = 6, BWF = 7, BWE = 9, BOP = 11, BSR = 19, NBAR = 20 };
+// (BDA + c: 64-column chunk c of dA is in shared memory -- MMA 2's k-block c may start)
+enum { BC = 0, BUF = 1, BUE = 2, BD1 = 3, BD2 = 4, BTF = 5, BWF = 6, BWE = 8, BOP = 10, BSR = 18, BDA = 19, NBAR = 23 };
 
 // SH (the shared-tile form, K1 up to 128): the dU tile and the dA tile share one 128 x D buffer (dU is consumed by
 // MMA 1 before dA is written; the next dU lands once MMA 2 and the dA stores have read it), W_u' takes two chunks,
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(320, 1) dcn_bwd_kernel(const __grid_constant__
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mp.wu) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mp.du) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mp.w) : "memory");
-    for (int i = 0; i < NBAR; ++i) mbar_init(B_(i), (i == BDA || i == BTF || i == BSR) ? 8 : 1);
+    for (int i = 0; i < NBAR; ++i) mbar_init(B_(i), (i >= BDA || i == BTF || i == BSR) ? 8 : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -157,10 +158,10 @@ __global__ void __launch_bounds__(320, 1) dcn_bwd_kernel(const __grid_constant__
         }
         mma_commit(B_(BUE));
         mma_commit(B_(BD1));
-        mbar_wait(B_(BDA), ph);                              // dA in shared memory, P back in TMEM
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int kb = 0; kb < NCH; ++kb, ++wc) {
+        for (int kb = 0; kb < NCH; ++kb, ++wc) {   // k-block kb as soon as dA chunk kb is written (K in order)
           const int s = wc & 1;
+          mbar_wait(B_(BDA + kb), ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           mbar_wait(B_(BWF + s), (wc >> 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
@@ -175,21 +176,26 @@ __global__ void __launch_bounds__(320, 1) dcn_bwd_kernel(const __grid_constant__
       }
     }
   } else {   // ---------------- epilogue warps 2-9
+    // warp (q4, hh) owns rows 32 q4 .. and, in pass j, columns 64 j + 32 hh .. (chunk j's half hh): after pass j of
+    // all eight warps dA chunk j is complete and MMA 2 runs its k-block j while the next passes are combined.  The
+    // two warps of a quadrant share its 32-row slices of the dA tile (named barrier 1 + q4 before a slice is stored).
     const int q4 = warp & 3, hh = (warp - 2) >> 2;
-    const uint32_t tq = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(hh * HC);
+    const uint32_t tq = tmem + ((uint32_t)(q4 * 32) << 16);
+    auto colj = [&](int j) { return 64 * j + 32 * hh; };
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory"); };
     const uint32_t op = sOP + (uint32_t)((warp - 2) * S::OPW), opb = B_(BOP + warp - 2);
     const uint32_t swx = (uint32_t)((lane >> 1) & 3), sw8 = (uint32_t)(lane & 7);
     // the warp's slice of the dA tile for its 64-column chunk c: rows 32 q4.., a 32 x 64 bf16 box (128-B swizzle)
     auto slice = [&](int c) { return sA + (uint32_t)(c * 16384 + q4 * 4096); };
     const uint32_t base_bytes = p.rin_f32 ? 4096u : 2048u;
     auto issue = [&](int item, int j) {   // lane 0: operand boxes of (item, pass j)
-      const int row0 = item * 128 + q4 * 32, col = hh * HC + 32 * j;
+      const int row0 = item * 128 + q4 * 32, col = colj(j);
       mbar_expect_tx(opb, 4096u + base_bytes);
       tma_load2d(op, &mp.x, col, row0, opb);
       tma_load2d(op + 2048u, &mp.a, col, row0, opb);
       tma_load2d(op + 4096u, &mp.rin, col, row0, opb);
     };
-    float bs[NP];   // running column sums of dA: lane = column 32 j + lane of this warp's half
+    float bs[NP];   // running column sums of dA: lane = column colj(j) + lane
 #pragma unroll
     for (int j = 0; j < NP; ++j) bs[j] = 0.f;
     uint32_t oph = 0;
@@ -199,18 +205,19 @@ __global__ void __launch_bounds__(320, 1) dcn_bwd_kernel(const __grid_constant__
       const uint32_t ph = it & 1;
       mbar_wait(B_(BD1), ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (lane == 0) bulk_wait_read<0>();   // the previous item's dX stores have read this warp's dA slices
+      if (lane == 0) bulk_wait_read<0>();   // the previous item's dX stores have read the quadrant's dA slices
       __syncwarp();
+      pair_sync();
       // ---- phase 1: dA = dT (.) X -> the dA tile; P = base + dT (.) A + dT -> MMA 1's TMEM columns
 #pragma unroll 1
       for (int j = 0; j < NP; ++j) {
         uint32_t v[32];
-        ld_tmem32(tq + 32 * j, v);
+        ld_tmem32(tq + colj(j), v);
         mbar_wait(opb, oph);
         oph ^= 1u;
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         float pv[32];
-        const int col = hh * HC + 32 * j;
+        const int col = colj(j);
         const uint32_t drow = slice(col >> 6) + (uint32_t)(lane * 128);
 #pragma unroll
         for (int g = 0; g < 4; ++g) {   // 8 columns at a time
@@ -238,19 +245,21 @@ __global__ void __launch_bounds__(320, 1) dcn_bwd_kernel(const __grid_constant__
           const uint32_t gg = (uint32_t)(((col & 63) >> 3) + g);   // 16-B granule within the 64-column chunk
           sts4u(drow + ((gg ^ sw8) << 4), da[0], da[1], da[2], da[3]);
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // dA chunk j visible to MMA 2
         __syncwarp();   // every lane has read the operand slot: refill it (next pass, or the next item's first)
         if (lane == 0) {
+          arrive(B_(BDA + j));
           if (j + 1 < NP) issue(item, j + 1);
           else if (it + 1 < n) issue(item + gridDim.x, 0);
         }
-        tmem_st32f(tq + 32 * j, pv);   // P replaces dT in MMA 1's columns
+        tmem_st32f(tq + colj(j), pv);   // P replaces dT in MMA 1's columns
       }
       __syncwarp();
       // the bias gradient: column sums of the STORED dA over this warp's rows (lane = column, rows in order)
       if (p.bsum) {
 #pragma unroll
         for (int j = 0; j < NP; ++j) {
-          const int col = hh * HC + 32 * j + lane;
+          const int col = colj(j) + lane;
           const uint32_t sl = slice(col >> 6);
           const uint32_t cb = (uint32_t)((col & 63) >> 3), ce = (uint32_t)((col & 7) * 2);
           float s_ = 0.f;
@@ -265,13 +274,10 @@ __global__ void __launch_bounds__(320, 1) dcn_bwd_kernel(const __grid_constant__
         }
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // dA visible to MMA 2 and the TMA store
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-        arrive(B_(BDA));
+      pair_sync();   // both halves of every slice of the quadrant are written: the hh = 0 warp stores them
+      if (hh == 0 && lane == 0) {
 #pragma unroll
-        for (int c = 0; c < HC / 64; ++c) tma_store2d(&mp.da, slice(hh * (HC / 64) + c), hh * HC + 64 * c, item * 128 + q4 * 32);
+        for (int c = 0; c < NCH; ++c) tma_store2d(&mp.da, slice(c), 64 * c, item * 128 + q4 * 32);
         bulk_commit();
       }
       // ---- phase 2: out = P + dA W, through the warp's dA slices (free once MMA 2 is done and dA is stored)
@@ -282,11 +288,12 @@ __global__ void __launch_bounds__(320, 1) dcn_bwd_kernel(const __grid_constant__
         if (SH) arrive(B_(BSR));          // (SH: the next dU may land in it)
       }
       __syncwarp();
+      pair_sync();
 #pragma unroll 1
       for (int j = 0; j < NP; ++j) {
         uint32_t pv[32], w2[32];
-        ld_tmem32(tq + 32 * j, pv);
-        ld_tmem32(tq + (uint32_t)D + 32 * j, w2);
+        ld_tmem32(tq + colj(j), pv);
+        ld_tmem32(tq + (uint32_t)D + colj(j), w2);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (j + 1 == NP) {   // both accumulators read: MMA 1 of the next item may start
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -296,7 +303,7 @@ __global__ void __launch_bounds__(320, 1) dcn_bwd_kernel(const __grid_constant__
         float o[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) o[e] = __uint_as_float(pv[e]) + __uint_as_float(w2[e]);
-        const int col = hh * HC + 32 * j;
+        const int col = colj(j);
         if (SH) {          // bf16, one 32 x 32 box per pass in the operand slot's spare 2 KB
           const uint32_t ob = op + 6144u;
           if (j > 0) {
@@ -313,9 +320,9 @@ __global__ void __launch_bounds__(320, 1) dcn_bwd_kernel(const __grid_constant__
             tma_store2d(&mp.out, ob, col, item * 128 + q4 * 32);
             bulk_commit();
           }
-        } else if (p.out_f32) {   // one 32 x 32 fp32 box per pass, cycling through the warp's HC / 64 slices
-          constexpr int NSL = HC / 64;
-          const uint32_t box = slice(hh * NSL + (j % NSL)) + (uint32_t)(lane * 128);
+        } else if (p.out_f32) {   // one 32 x 32 fp32 box per pass, cycling through the warp's slices (chunks = hh mod 2)
+          constexpr int NSL = NCH / 2;
+          const uint32_t box = slice(2 * (j % NSL) + hh) + (uint32_t)(lane * 128);
           if (j >= NSL) {   // the store that last read this slice is done with it
             if (lane == 0) bulk_wait_read<NSL - 1>();
             __syncwarp();
@@ -325,10 +332,10 @@ __global__ void __launch_bounds__(320, 1) dcn_bwd_kernel(const __grid_constant__
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            tma_store2d(&mp.out, slice(hh * NSL + (j % NSL)), col, item * 128 + q4 * 32);
+            tma_store2d(&mp.out, slice(2 * (j % NSL) + hh), col, item * 128 + q4 * 32);
             bulk_commit();
           }
-        } else {           // bf16: two passes fill one 32 x 64 box (the slice of that chunk)
+        } else {           // bf16: the quadrant's two warps fill chunk j's 32 x 64 slice, the hh = 0 warp stores it
           const uint32_t rowb = slice(col >> 6) + (uint32_t)(lane * 128);
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
@@ -336,21 +343,19 @@ __global__ void __launch_bounds__(320, 1) dcn_bwd_kernel(const __grid_constant__
             sts4u(rowb + ((gg ^ sw8) << 4), pack_bf2(o[8 * g], o[8 * g + 1]), pack_bf2(o[8 * g + 2], o[8 * g + 3]),
                   pack_bf2(o[8 * g + 4], o[8 * g + 5]), pack_bf2(o[8 * g + 6], o[8 * g + 7]));
           }
-          if (col & 32) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-              tma_store2d(&mp.out, slice(col >> 6), col & ~63, item * 128 + q4 * 32);
-              bulk_commit();
-            }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          pair_sync();
+          if (hh == 0 && lane == 0) {
+            tma_store2d(&mp.out, slice(j), 64 * j, item * 128 + q4 * 32);
+            bulk_commit();
           }
         }
       }
     }
     if (lane == 0) bulk_wait_all();
-    if (p.bsum) {   // this warp's partial column sums -> row (blockIdx * 4 + q4), columns hh HC + 32 j + lane
+    if (p.bsum) {   // this warp's partial column sums -> row (blockIdx * 4 + q4), columns colj(j) + lane
 #pragma unroll
-      for (int j = 0; j < NP; ++j) p.bsum[((int64_t)blockIdx.x * 4 + q4) * p.d + hh * HC + 32 * j + lane] = bs[j];
+      for (int j = 0; j < NP; ++j) p.bsum[((int64_t)blockIdx.x * 4 + q4) * p.d + colj(j) + lane] = bs[j];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
