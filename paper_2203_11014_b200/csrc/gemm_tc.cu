@@ -311,7 +311,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   if (p.tstore && var != p.lean_id) p.tstore = 0;
   // LayerNorm epilogue with TMA: residual boxes in, R and Y boxes out over 4-D maps {N, L, M / L, batch}
   // (L = rows per group of a two-level row view, else M), 32-row warp boxes inside one group or whole groups
-  if (tune().ln_tma && p.lean && (p.ep.flags & EF_LN) && var == p.lean_id && var > 0 && !p.lanes_rows && splits == 1 && !p.pair &&
+  if (tune().ln_tma && p.lean && (p.ep.flags & EF_LN) && var == p.lean_id && var > 0 && !p.lanes_rows && splits == 1 &&
       g.M % 32 == 0) {
     EncodeFn fn = encode_fn();
     const int L = g.c.rdiv ? g.c.rdiv : g.M;

@@ -805,8 +805,7 @@ template <int BN> struct EpiSmem {
 constexpr int DCNT_WARP_BYTES = 16384;
 // LayerNorm epilogue with TMA (Params::lnst): per warp the residual / R boxes (HC / 64 boxes of 32 rows x 64
 // bf16, 128-B swizzle) and one Y box
-template <int BN> constexpr int lnt_warp_bytes() { return (BN / 2) * 64 + 4096; }
-// (the TMA LayerNorm epilogue runs in single-CTA kernels: a CTA pair's deeper operand ring leaves no room)
+template <int BN> constexpr int lnt_warp_bytes() { return (BN / 2) * 64; }   // (Y overwrites R in the same boxes)
 static_assert(EpiSmem<128>::BYTES >= 8 * 8192, "the cross epilogue's per-warp boxes fit the staging area (BN >= 128)");
 template <int BN, int VAR, bool PAIR>
 constexpr int epi_bytes() {
@@ -819,7 +818,7 @@ constexpr int epi_bytes() {
 // single-CTA LayerNorm GEMMs at BN = 256 two (their epilogue boxes need the rest of shared memory)
 template <int BN, int STAGES, int VAR, bool PAIR>
 constexpr int eff_stages() {
-  return (VarF<VAR>::F & EF_DCNB) != 0 ? 1 : ((VarF<VAR>::F & EF_LN) != 0 && BN == 256 && !PAIR) ? 2 : STAGES;
+  return (VarF<VAR>::F & EF_DCNB) != 0 ? 1 : STAGES;
 }
 // per-warp TMA-arrival barriers of the operand epilogues (DCN backward: 2 slots; LayerNorm: 1)
 template <int VAR> constexpr bool has_opbar() { return (VarF<VAR>::F & (EF_DCNB | EF_LN | EF_CROSS)) != 0; }
@@ -1034,9 +1033,11 @@ __global__ void __launch_bounds__(320, 1)
     };
     if (XTV && p.crosst && lane == 0 && wid < total) xt_issue(wid, 0, 0u);
     // LayerNorm epilogue with TMA (LNV && p.lnst): the warp's 32 x HC residual block arrives by TMA into its
-    // boxes (the next tile's as soon as this tile's R stores have read them), R = acc + bias + resid overwrites
-    // it in place and leaves by TMA store, Y goes through one 64-column box
-    constexpr bool LNT = VAR > 0 && (VarF<VAR>::F & EF_LN) != 0 && !PAIR;
+    // boxes, R = acc + bias + resid overwrites it in place and leaves by TMA store, then Y overwrites R (once the R
+    // stores have read it) and leaves the same way; the next tile's residual is requested as soon as the Y stores
+    // have read the boxes, so it lands while the warp waits for the next accumulator.  8 KB a warp fit the staging
+    // area, so the operand ring keeps its depth and CTA pairs take it too.
+    constexpr bool LNT = VAR > 0 && (VarF<VAR>::F & EF_LN) != 0;
     const uint32_t lnw = smem_u32(stage_all) + (uint32_t)((warp - 2) * lnt_warp_bytes<BN>());
     uint32_t lph = 0;
     auto ln_issue = [&](int item_) {   // lane 0: the residual boxes of item_'s 32 x HC block
@@ -1202,7 +1203,6 @@ __global__ void __launch_bounds__(320, 1)
           const float inv_d = 1.f / (float)e.ln_d;
           const uint32_t bar_id = 2 + q4;
           const int gr = rbase % p.ln_rdiv, gq = rbase / p.ln_rdiv;   // the boxes' row coordinates
-          const uint32_t ybox = lnw + (uint32_t)(HC * 64);
           const uint32_t sw = (uint32_t)(lane & 7);
           mbar_wait(smem_u32(tfull + ab), aph);
           asm volatile("tcgen05.fence::after_thread_sync;");
@@ -1277,15 +1277,10 @@ __global__ void __launch_bounds__(320, 1)
             e.ln_mu[tok] = mean;
             e.ln_rstd[tok] = rs;
           }
-          // the residual boxes are free once the R stores have read them: the next tile's residual flies
-          // during pass 2 (this wait also covers the previous tile's last Y store)
-          if (lane == 0) {
-            bulk_wait_read<0>();
-            if (item + nwk < total) ln_issue(item + nwk);
-          }
+          // Y overwrites R in the same boxes once the R stores have read them
+          if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
-          // pass 2: Y = gamma (v - mu) rstd + beta through the Y box, one 64-column box store at a time
-          const uint32_t yrow = ybox + (uint32_t)(lane * 128);
+          // pass 2: Y = gamma (v - mu) rstd + beta, one 64-column box store at a time
 #pragma unroll 1
           for (int c = 0; c < HC; c += 32) {
             uint32_t v[32];
@@ -1302,11 +1297,8 @@ __global__ void __launch_bounds__(320, 1)
               __syncwarp();
               if (lane == 0) tempty_arrive(smem_u32(tempty + ab), pair);
             }
-            if ((c & 63) == 0 && c > 0) {   // the Y box's previous store has read it
-              if (lane == 0) bulk_wait_read<0>();
-              __syncwarp();
-            }
             const uint32_t g0 = (uint32_t)((c & 63) >> 3);
+            const uint32_t yrow = lnw + (uint32_t)((c >> 6) * 4096 + lane * 128);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               float y[8];
@@ -1319,10 +1311,16 @@ __global__ void __launch_bounds__(320, 1)
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               __syncwarp();
               if (lane == 0) {
-                tma_store4(&tma_o.c, ybox, cb0 + (c & ~63), gr, gq, z);
+                tma_store4(&tma_o.c, lnw + (uint32_t)((c >> 6) * 4096), cb0 + (c & ~63), gr, gq, z);
                 bulk_commit();
               }
             }
+          }
+          // the boxes are free once the Y stores have read them: the next tile's residual can land (its latency
+          // overlaps the wait for the next accumulator)
+          if (lane == 0) {
+            bulk_wait_read<0>();
+            if (item + nwk < total) ln_issue(item + nwk);
           }
           continue;
         }

@@ -137,6 +137,16 @@ def test_schedule_switches_bitwise(name, B, layers, switch):
     _cmp(a, b, net, 1e-3 if switch == "tstore" else 0)
 
 
+@pytest.mark.parametrize("name,B,layers", [("C4", 16, 2), ("C2", 64, 2)])
+def test_ln_tma_cta_pairs_bitwise(name, B, layers):
+    """The TMA LayerNorm epilogue in CTA-pair GEMMs (pair = 1 forces cta_group::2 tiles wherever expressible:
+    the dot projection with its LayerNorm) against the register epilogue on the same pair tiles: bit-identical."""
+    net = _net(name, layers)
+    a = _step(net, B, 23, {"ln_tma": 0, "pair": 1})
+    b = _step(net, B, 23, {"pair": 1})
+    _cmp(a, b, net, 0)
+
+
 def test_ln_tma_small_token_groups():
     """The TMA LayerNorm epilogue over two-level rows: a 16-token Linear module's packed token projection
     (8 samples per 128-row tile, 4-D boxes of 16 tokens x 2 samples) and a 48-token one (groups of 48 rows:
