@@ -5,6 +5,7 @@ for c in C1 C2 C3 C4 C5 C4fp; do
   [ -f gpurun_out/ev_bench_$c.json ] || continue
   tail -1 gpurun_out/ev_bench_$c.json > profiles/${T}_bench_$c.json
   [ -f gpurun_out/ev_prof_$c.json ] && python tools/prof_table.py gpurun_out/ev_prof_$c.json > profiles/${T}_ops_$c.txt
+  [ -f gpurun_out/ev_prof_$c.json ] && python tools/gap_table.py gpurun_out/ev_prof_$c.json 40 > profiles/${T}_roofline_gap_$c.txt
 done
 [ -f gpurun_out/ev_ref_C4.json ] && tail -1 gpurun_out/ev_ref_C4.json > profiles/${T}_bench_C4_reference.json
 if [ -f gpurun_out/ev_launches_C4.csv.gz ]; then
