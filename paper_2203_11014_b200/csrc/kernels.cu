@@ -1464,12 +1464,22 @@ __global__ void __launch_bounds__(512, 1) conv_db_k(const __nv_bfloat16* __restr
       load_row(i0, w[1]);
       load_row(i0 + 1, w[2]);
       const int64_t base = (int64_t)b * m * d + c0;
+      // wgrad: the dT rows of the next group of 8 are loaded while this group is combined (two groups in flight)
+      uint2 gnext[MODE == 2 ? 8 : 1];
+      if (MODE == 2) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          gnext[u] = (i0 + u < i1) ? __ldcs(reinterpret_cast<const uint2*>(other + base + (int64_t)(i0 + u) * d)) : make_uint2(0u, 0u);
+      }
       for (int i = i0; i < i1; i += 8) {
         uint2 g8[8];
         if (MODE == 2) {
 #pragma unroll
+          for (int u = 0; u < 8; ++u) g8[u] = gnext[u];
+#pragma unroll
           for (int u = 0; u < 8; ++u)
-            g8[u] = (i + u < i1) ? __ldcs(reinterpret_cast<const uint2*>(other + base + (int64_t)(i + u) * d)) : make_uint2(0u, 0u);
+            gnext[u] = (i + 8 + u < i1) ? __ldcs(reinterpret_cast<const uint2*>(other + base + (int64_t)(i + 8 + u) * d))
+                                        : make_uint2(0u, 0u);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
