@@ -56,6 +56,11 @@ class LayerSpec:
     # the configs' reading), "sum" of the modules' outputs, or "wsum" = sum with one learnable scalar weight
     # per module (R27; initialised to 1, so a fresh wsum layer computes the sum).  sum / wsum need equal l_i.
     ensemble: str = "concat"
+    # Dense-token injection ("the raw numerical (dense) features can be part of the input to any modules for
+    # ensembling in every layer", NEXT#3, R38): every module of the layer reads [X_n ; D] (m_in + n_dense tokens),
+    # D = the first NetSpec.dense_tokens tokens of X0 (the feature processing layer's dense tokens, R32); the
+    # shortcut and the LayerNorm still see X_n.
+    dense_in: bool = False
 
 
 @dataclass
@@ -64,6 +69,12 @@ class NetSpec:
     d: int
     layers: List[LayerSpec]
     ln_eps: float = 1e-5
+    dense_tokens: int = 0       # R38: X0[:, :dense_tokens] are the dense tokens D injected into dense_in layers
+
+
+def module_in(net: NetSpec, n: int) -> int:
+    """Tokens every module of layer n reads: m_in, plus the dense tokens when the layer injects them (R38)."""
+    return layer_dims(net)[n][0] + (net.dense_tokens if net.layers[n].dense_in else 0)
 
 
 def layer_dims(net: NetSpec) -> List[Tuple[int, int]]:
@@ -80,6 +91,8 @@ def validate(net: NetSpec) -> None:
     """Preconditions of SURVEY §8(b)."""
     if net.m0 < 1 or net.d < 1 or not net.layers:
         raise ValueError("bad net dims")
+    if not 0 <= net.dense_tokens <= net.m0 or (any(L.dense_in for L in net.layers) and net.dense_tokens == 0):
+        raise ValueError("dense injection needs 1 <= dense_tokens <= m0 (R38)")
     for (m_in, _), L in zip(layer_dims(net), net.layers):
         if not L.modules:
             raise ValueError("empty layer")
@@ -139,10 +152,10 @@ def module_param_shapes(s: ModuleSpec, m: int, d: int) -> List[Tuple[str, Tuple[
 def param_groups(net: NetSpec) -> List[List[Tuple[str, Tuple[int, ...], int]]]:
     """Groups 0..N-1 = layers, group N = head.  Names are '<i>.<kind>.<p>'."""
     groups = []
-    for (m_in, m_out), L in zip(layer_dims(net), net.layers):
+    for n, ((m_in, m_out), L) in enumerate(zip(layer_dims(net), net.layers)):
         g = []
         for i, s in enumerate(L.modules):
-            for name, shp, fan in module_param_shapes(s, m_in, net.d):
+            for name, shp, fan in module_param_shapes(s, module_in(net, n), net.d):
                 g.append((f"{i}.{s.kind}.{name}", shp, fan))
         if L.ensemble == "wsum":
             g.append(("ens_w", (len(L.modules),), 0))         # R27, initialised to 1
@@ -538,21 +551,22 @@ def _module_params(P: Dict[str, np.ndarray], i: int, kind: str):
     return {k[len(pre):]: v for k, v in P.items() if k.startswith(pre)}
 
 
-def layer_fwd(net: NetSpec, n: int, X: np.ndarray, P: Dict[str, np.ndarray], pr: Precision = FP64):
+def layer_fwd(net: NetSpec, n: int, X: np.ndarray, P: Dict[str, np.ndarray], pr: Precision = FP64, D=None):
     """Y = Norm(Concat_i Interaction_i(X_n) + ShortCut(X_n)) (Eq.(1)); ShortCut
     = X_n if len(X_n) == len(Y) else W_nᵀ X_n on the token axis (Eq.(2), R2-R4).
-    Returns (Y, cache)."""
+    With dense injection (R38) the modules read [X_n ; D].  Returns (Y, cache)."""
     L = net.layers[n]
     m_in, m_out = layer_dims(net)[n]
     assert X.shape[1] == m_in
+    Xm = np.concatenate([X, D], axis=1) if L.dense_in else X
     us, caches = [], []
     for i, s in enumerate(L.modules):
         p = _module_params(P, i, s.kind)
         if s.kind == "attn":
-            U, c = attn_fwd(X, p, s, pr, net.ln_eps)
+            U, c = attn_fwd(Xm, p, s, pr, net.ln_eps)
         else:
             U, c = {"dot": dot_fwd, "linear": linear_fwd, "dcn": dcn_fwd, "dcn_lit": dcn_lit_fwd, "dcn_full": dcn_full_fwd,
-                    "conv": conv_fwd, "mlp": mlp_fwd}[s.kind](X, p, s, pr)
+                    "conv": conv_fwd, "mlp": mlp_fwd}[s.kind](Xm, p, s, pr)
         us.append(U)
         caches.append(c)
     if L.ensemble == "concat":
@@ -563,16 +577,19 @@ def layer_fwd(net: NetSpec, n: int, X: np.ndarray, P: Dict[str, np.ndarray], pr:
         Ucat = sum(w * u for w, u in zip(P["ens_w"], us))
     R = Ucat + (X if m_in == m_out else tokmix_fwd(X, P["W_n"]))
     Y, mu, rstd = ln_fwd(R, P["gamma"], P["beta"], net.ln_eps)
-    cache = {"X": X, "mods": caches, "R": pr.q("R", R), "mu": mu, "rstd": rstd,
+    cache = {"X": X, "Xm": Xm, "mods": caches, "R": pr.q("R", R), "mu": mu, "rstd": rstd,
              "us": us if L.ensemble == "wsum" else None}
     return pr.q("Y", Y), cache
 
 
-def layer_bwd(net: NetSpec, n: int, cache, dY: np.ndarray, P, pr: Precision = FP64):
-    """Backward of layer_fwd.  Returns (dX, grads dict in canonical names)."""
+def layer_bwd(net: NetSpec, n: int, cache, dY: np.ndarray, P, pr: Precision = FP64, add=None, with_dD: bool = False):
+    """Backward of layer_fwd.  Returns (dX, grads dict in canonical names).  Dense injection (R38): the modules'
+    gradient w.r.t. the injected tokens D is returned as a third value when with_dD; `add` (fp64, the layer input's
+    shape) is added before dX is rounded (the stack adds every layer's dD to dX0's dense tokens that way)."""
     L = net.layers[n]
     m_in, m_out = layer_dims(net)[n]
     X = cache["X"]
+    Xm = cache["Xm"]
     g = {}
     dR, g["gamma"], g["beta"] = ln_bwd(dY, cache["R"], cache["mu"], cache["rstd"], P["gamma"])
     dR = pr.q("dR", dR)
@@ -581,6 +598,7 @@ def layer_bwd(net: NetSpec, n: int, cache, dY: np.ndarray, P, pr: Precision = FP
     else:
         dX, g["W_n"] = tokmix_bwd(X, P["W_n"], dR)
     off = 0
+    dD = None
     if L.ensemble == "wsum":   # d(sum_i w_i U_i)/dw_i = <U_i, dR>
         g["ens_w"] = np.array([(u * dR).sum() for u in cache["us"]])
     for i, s in enumerate(L.modules):
@@ -595,11 +613,15 @@ def layer_bwd(net: NetSpec, n: int, cache, dY: np.ndarray, P, pr: Precision = FP
         fn = {"dot": dot_bwd, "linear": linear_bwd, "dcn": dcn_bwd, "dcn_lit": dcn_lit_bwd, "dcn_full": dcn_full_bwd,
               "conv": conv_bwd,
               "attn": attn_bwd, "mlp": mlp_bwd}[s.kind]
-        dXi, gi = fn(X, p, s, cache["mods"][i], dU, pr)
-        dX = dX + dXi
+        dXi, gi = fn(Xm, p, s, cache["mods"][i], dU, pr)
+        dX = dX + dXi[:, :m_in]
+        if L.dense_in:
+            dD = dXi[:, m_in:] if dD is None else dD + dXi[:, m_in:]
         for k, v in gi.items():
             g[f"{i}.{s.kind}.{k}"] = v
-    return pr.q("dX", dX), g
+    if add is not None:
+        dX = dX + add
+    return (pr.q("dX", dX), g, dD) if with_dD else (pr.q("dX", dX), g)
 
 
 # --------------------------------------------------------------------------
@@ -638,9 +660,10 @@ def compute_params(params: List[Dict[str, np.ndarray]], pr: Precision = FP64):
 def forward(net: NetSpec, params: List[Dict[str, np.ndarray]], X0: np.ndarray, pr: Precision = FP64):
     """Forward of the stack; `params` are the compute values (see compute_params)."""
     X = X0
+    D = X0[:, :net.dense_tokens]   # R38: the dense tokens injected into dense_in layers
     caches = []
     for n in range(len(net.layers)):
-        X, c = layer_fwd(net, n, X, params[n], pr)
+        X, c = layer_fwd(net, n, X, params[n], pr, D)
         caches.append(c)
     return X, caches
 
@@ -659,8 +682,21 @@ def train_step(net: NetSpec, params: List[Dict[str, np.ndarray]], X0: np.ndarray
     dY, gh = head_bwd(YN, pooled, z, y, ph, Bg, pr)
     grads: List[Dict[str, np.ndarray]] = [None] * len(params)
     grads[-1] = gh
-    for n in reversed(range(len(net.layers))):
-        dY, grads[n] = layer_bwd(net, n, caches[n], dY, cparams[n], pr)
+    dD = np.zeros(X0[:, :net.dense_tokens].shape)   # R38: the injected tokens' gradient, summed over layers
+    for n in reversed(range(1, len(net.layers))):
+        dY, grads[n], dDn = layer_bwd(net, n, caches[n], dY, cparams[n], pr, with_dD=True)
+        if dDn is not None:
+            dD = dD + dDn
+    if net.layers:
+        # layer 0: dX0's dense tokens (X0[:, :dense_tokens]) also take dD -- every layer's, layer 0's own included --
+        # added before dX0 is rounded (the GPU adds it in the same fp32 step)
+        if net.layers[0].dense_in:
+            dD = dD + layer_bwd(net, 0, caches[0], dY, cparams[0], pr, with_dD=True)[2]
+        add = None
+        if net.dense_tokens:
+            add = np.zeros(caches[0]["X"].shape)
+            add[:, :net.dense_tokens] = dD
+        dY, grads[0] = layer_bwd(net, 0, caches[0], dY, cparams[0], pr, add)
     new = [{k: v - lr * grads[gi][k] for k, v in grp.items()} for gi, grp in enumerate(params)]
     return {"loss": loss_sum / Bg, "loss_sum": loss_sum, "logits": z, "Y_N": YN, "dX0": dY,
             "grads": grads, "params": new}

@@ -225,3 +225,63 @@ def test_ensemble_reductions():
     P2 = {k: v for k, v in Ps.items() if not k.startswith("1.")}
     P2 = {k.replace("2.conv", "1.conv"): v for k, v in P2.items()}
     assert np.allclose(O.layer_fwd(nw, 0, X, P0)[0], O.layer_fwd(n2, 0, X, P2)[0], rtol=0, atol=1e-13)
+
+
+def _inj_net():
+    """Dense-token injection (R38): 2 dense tokens of X0 fed to every module of layers 0 and 2 (several kinds),
+    layer 1 without; layer 2 maps 9 -> 7 tokens (W_n)."""
+    l0 = O.LayerSpec([M("dot", 4), M("dcn", 2), M("attn", 3, heads=2)], dense_in=True)
+    l1 = O.LayerSpec([M("linear", 5), M("conv", 4)])
+    l2 = O.LayerSpec([M("mlp", 3, mlp_hidden=(12, 10)), M("dcn_full", 4)], dense_in=True)
+    return O.NetSpec(9, 8, [l0, l1, l2], dense_tokens=2)
+
+
+def test_dense_injection_gradients_vs_finite_differences():
+    """Every sampled gradient and dX0 -- the injected dense tokens (X0[:, :2]: their gradient comes through the
+    layer-0 input path and both injected layers) and ordinary tokens -- against central finite differences."""
+    net = _inj_net()
+    O.validate(net)
+    B = 3
+    params = oracle_params(net, make_flat_params(net, 13))
+    X0 = RNG.standard_normal((B, net.m0, net.d))
+    y = (RNG.random(B) < 0.5).astype(np.float64)
+    out = O.train_step(net, params, X0, y, lr=0.0)
+    h = 1e-6
+    for gi, grp in enumerate(params):
+        for k, v in grp.items():
+            flat = v.reshape(-1)
+            for j in RNG.choice(flat.size, size=min(2, flat.size), replace=False):
+                old = flat[j]
+                flat[j] = old + h
+                lp = _loss(net, params, X0, y)
+                flat[j] = old - h
+                lm = _loss(net, params, X0, y)
+                flat[j] = old
+                fd = (lp - lm) / (2 * h)
+                an = out["grads"][gi][k].reshape(-1)[j]
+                assert abs(fd - an) <= 1e-4 * max(1e-2, abs(fd)) + 1e-7, (gi, k, j, fd, an)
+    for (b, i, c) in [(0, 0, 1), (1, 1, 5), (2, 4, 3), (1, 8, 7)]:   # dense tokens 0, 1 and two ordinary ones
+        old = X0[b, i, c]
+        X0[b, i, c] = old + h
+        lp = _loss(net, params, X0, y)
+        X0[b, i, c] = old - h
+        lm = _loss(net, params, X0, y)
+        X0[b, i, c] = old
+        fd = (lp - lm) / (2 * h)
+        assert abs(fd - out["dX0"][b, i, c]) <= 1e-4 * max(1e-2, abs(fd)) + 1e-7, (b, i, c)
+
+
+def test_dense_injection_reduces_to_explicit_concat():
+    """A one-layer net with injection equals the same modules on the explicitly widened input [X ; D] whose
+    extra tokens are dropped from the shortcut: with a 1-module concat layer that is the module on [X ; D] plus X,
+    and the module's gradient w.r.t. D is what the injected net adds to dX0's dense tokens."""
+    d, m, nD, l = 6, 5, 2, 5
+    X0 = RNG.standard_normal((2, m, d))
+    s = M("linear", l)
+    net = O.NetSpec(m, d, [O.LayerSpec([s], dense_in=True)], dense_tokens=nD)
+    p = oracle_params(net, make_flat_params(net, 14))
+    Y, cache = O.layer_fwd(net, 0, X0, p[0], O.FP64, X0[:, :nD])
+    U, _ = O.linear_fwd(np.concatenate([X0, X0[:, :nD]], 1), {"W": p[0]["0.linear.W"]}, s, O.FP64)
+    ref, _, _ = O.ln_fwd(U + X0, p[0]["gamma"], p[0]["beta"], net.ln_eps)
+    assert np.abs(Y - ref).max() < 1e-12
+    assert p[0]["0.linear.W"].shape == (m + nD, l)
