@@ -89,6 +89,10 @@ typedef struct {
                                  tokens (R5, default); SUM or WSUM (one learnable scalar per module, R27,
                                  initialised to 1) of the modules' outputs, which then need equal l_i and
                                  give m_out = l                                                          */
+  int dense_in;               /* 1: every module reads [X_n ; D] (m_in + dense_tokens tokens), D = the first
+                                 dhen_config.dense_tokens tokens of X_0 -- P:64 "the raw numerical (dense)
+                                 features can be part of the input to any modules ... in every layer" (NEXT#3,
+                                 R38); the shortcut and the LayerNorm still see X_n                         */
 } dhen_layer;
 
 typedef struct {
@@ -105,6 +109,8 @@ typedef struct {
                              Adam with its moments stored in bf16 ("BF16 optimizer", R35: fp32 math,
                              RNE storage, half the optimizer-state memory)                                  */
   float adam_beta1, adam_beta2, adam_eps;   /* Adam (0 -> 0.9, 0.999, 1e-8)                          */
+  int dense_tokens;       /* R38: X_0[:, :dense_tokens] are the dense tokens D injected into dense_in layers
+                             (0: none); dL/dX_0 of those tokens adds every injected layer's dD             */
   int recompute;          /* activation recompute ("activation checkpointing", NEXT#2), bit mask:
                              1 = the attention FFN hidden F (and its ReLU bitmask) is not kept from forward
                              to backward: one shared buffer, F recomputed by the backward (one FFN1 GEMM per

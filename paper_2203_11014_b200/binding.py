@@ -39,7 +39,8 @@ class dhen_module(C.Structure):
 
 
 class dhen_layer(C.Structure):
-    _fields_ = [("n_modules", C.c_int), ("modules", C.POINTER(dhen_module)), ("ensemble", C.c_int)]
+    _fields_ = [("n_modules", C.c_int), ("modules", C.POINTER(dhen_module)), ("ensemble", C.c_int),
+                ("dense_in", C.c_int)]
 
 
 ENSEMBLES = {"concat": 0, "sum": 1, "wsum": 2}   # dhen_ensemble
@@ -49,7 +50,7 @@ class dhen_config(C.Structure):
     _fields_ = [("m0", C.c_int), ("d", C.c_int), ("n_layers", C.c_int), ("layers", C.POINTER(dhen_layer)),
                 ("dtype", C.c_int), ("ln_eps", C.c_float), ("batch_max_local", C.c_int),
                 ("seed", C.c_ulonglong), ("optimizer", C.c_int), ("adam_beta1", C.c_float),
-                ("adam_beta2", C.c_float), ("adam_eps", C.c_float), ("recompute", C.c_int)]
+                ("adam_beta2", C.c_float), ("adam_eps", C.c_float), ("dense_tokens", C.c_int), ("recompute", C.c_int)]
 
 
 class dhen_dist(C.Structure):
@@ -189,6 +190,8 @@ class Config:
     optimizer: str = "sgd"            # "sgd" (R18) | "adam" | "adam_bf16" (bf16 moments, R35)
     ensembles: Optional[Sequence[str]] = None   # per layer: "concat" (default) | "sum" | "wsum"
     recompute: int = 0                # bit 1: attention FFN hidden recomputed in the backward (NEXT#2)
+    dense_tokens: int = 0             # R38: X0[:, :dense_tokens] injected into the dense_in layers
+    dense_in: Optional[Sequence[bool]] = None   # per layer (NEXT#3)
     adam: Sequence[float] = (0.9, 0.999, 1e-8)
     _keep: list = field(default_factory=list, repr=False)
 
@@ -209,11 +212,13 @@ class Config:
             layers[n].n_modules = len(L)
             layers[n].modules = C.cast(mods, C.POINTER(dhen_module))
             layers[n].ensemble = ENSEMBLES[self.ensembles[n]] if self.ensembles else 0
+            layers[n].dense_in = int(bool(self.dense_in[n])) if self.dense_in else 0
             keep.append(mods)
         self._keep = keep
         return dhen_config(self.m0, self.d, len(self.layers), C.cast(layers, C.POINTER(dhen_layer)),
                            BF16 if self.dtype == "bf16" else FP32, self.ln_eps, self.batch_max_local, self.seed,
-                           {"sgd": 0, "adam": 1, "adam_bf16": 2}[self.optimizer], *[float(x) for x in self.adam], int(self.recompute))
+                           {"sgd": 0, "adam": 1, "adam_bf16": 2}[self.optimizer], *[float(x) for x in self.adam],
+                           int(self.dense_tokens), int(self.recompute))
 
     def dims(self):
         out, m = [], self.m0

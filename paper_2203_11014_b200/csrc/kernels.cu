@@ -2244,3 +2244,78 @@ cudaError_t fill(float* p, int64_t n, float v, cudaStream_t st) {
 }
 
 }  // namespace dhen
+
+// ------------------------------------------------------------------ dense-token injection (R38, NEXT#3)
+namespace dhen {
+namespace {
+template <typename T>
+__global__ void inject_copy_k(const T* __restrict__ X, const T* __restrict__ X0, int64_t B, int mi, int nD, int m0,
+                              int d4, T* __restrict__ Xin) {
+  pdl_entry();
+  const int mm = mi + nD;
+  const int64_t n = B * mm * d4;   // 4-element groups
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / ((int64_t)mm * d4);
+    const int64_t r = i - b * mm * d4;
+    const int t = (int)(r / d4), c = (int)(r - (int64_t)t * d4);
+    const T* src = t < mi ? X + ((b * mi + t) * d4 + c) * 4 : X0 + ((b * m0 + (t - mi)) * d4 + c) * 4;
+    T* dst = Xin + i * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[k] = src[k];
+  }
+}
+__global__ void inject_dD_k(const float* __restrict__ accm, int64_t B, int mi, int nD, int d, float* __restrict__ dD) {
+  pdl_entry();
+  const int64_t n = B * nD * d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / ((int64_t)nD * d);
+    const int64_t r = i - b * nD * d;
+    dD[i] += accm[(b * (mi + nD)) * d + (int64_t)mi * d + r];
+  }
+}
+template <typename T>
+__global__ void inject_final_k(const float* __restrict__ acc_sc, const float* __restrict__ accm, int m_mod,
+                               const float* __restrict__ dD, int nDadd, int64_t B, int mi, int d, T* __restrict__ dX) {
+  pdl_entry();
+  const int64_t n = B * mi * d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / ((int64_t)mi * d);
+    const int64_t r = i - b * mi * d;
+    const int t = (int)(r / d);
+    float v = acc_sc[i] + accm[b * (int64_t)m_mod * d + r];
+    if (t < nDadd) v += dD[(b * nDadd + t) * d + (r - (int64_t)t * d)];
+    dX[i] = fromf<T>(v);
+  }
+}
+}  // namespace
+
+cudaError_t inject_copy(const void* X, const void* X0, int dt, int64_t B, int mi, int nD, int m0, int d, void* Xin,
+                        cudaStream_t st) {
+  const int64_t n = B * (mi + nD) * (d / 4);
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (dt == BF16)
+    pdl_launch(inject_copy_k<__nv_bfloat16>, grid, 256, 0, st, (const __nv_bfloat16*)X, (const __nv_bfloat16*)X0, B, mi, nD,
+               m0, d / 4, (__nv_bfloat16*)Xin);
+  else
+    pdl_launch(inject_copy_k<float>, grid, 256, 0, st, (const float*)X, (const float*)X0, B, mi, nD, m0, d / 4, (float*)Xin);
+  ++g_launches;
+  return cudaGetLastError();
+}
+cudaError_t inject_dD(const float* accm, int64_t B, int mi, int nD, int d, float* dD, cudaStream_t st) {
+  const int64_t n = B * nD * d;
+  pdl_launch(inject_dD_k, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st, accm, B, mi, nD, d, dD);
+  ++g_launches;
+  return cudaGetLastError();
+}
+cudaError_t inject_final(const float* acc_sc, const float* accm, int m_mod, const float* dD, int nDadd, int64_t B, int mi,
+                         int d, void* dX, int dt, cudaStream_t st) {
+  const int64_t n = B * mi * d;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (dt == BF16)
+    pdl_launch(inject_final_k<__nv_bfloat16>, grid, 256, 0, st, acc_sc, accm, m_mod, dD, nDadd, B, mi, d, (__nv_bfloat16*)dX);
+  else
+    pdl_launch(inject_final_k<float>, grid, 256, 0, st, acc_sc, accm, m_mod, dD, nDadd, B, mi, d, (float*)dX);
+  ++g_launches;
+  return cudaGetLastError();
+}
+}  // namespace dhen

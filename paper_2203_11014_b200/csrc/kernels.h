@@ -110,5 +110,12 @@ cudaError_t ens_dot(const float* U, const void* dR, int dt, int64_t n, float* ac
 cudaError_t init_uniform(float* p, int64_t n, float bound, unsigned long long seed, unsigned long long stream_id,
                          int64_t idx0, cudaStream_t st);
 cudaError_t fill(float* p, int64_t n, float v, cudaStream_t st);
+// Dense-token injection (R38): Xin[b] = [X[b] (mi rows) ; X0[b][0 .. nD)]; backward: dD[b] += accm[b][mi ..];
+// dX[b][t] = dt(acc_sc[b][t] + accm[b][t] (+ dD[b][t] for t < nDadd)), accm rows of pitch m_mod.
+cudaError_t inject_copy(const void* X, const void* X0, int dt, int64_t B, int mi, int nD, int m0, int d, void* Xin,
+                        cudaStream_t st);
+cudaError_t inject_dD(const float* accm, int64_t B, int mi, int nD, int d, float* dD, cudaStream_t st);
+cudaError_t inject_final(const float* acc_sc, const float* accm, int m_mod, const float* dD, int nDadd, int64_t B, int mi,
+                         int d, void* dX, int dt, cudaStream_t st);
 
 }  // namespace dhen

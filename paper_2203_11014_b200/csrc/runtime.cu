@@ -109,6 +109,10 @@ struct Group {
 
 struct Layer {
   int m_in = 0, m_out = 0;
+  int m_mod = 0;             // tokens the modules read: m_in, + dense_tokens with dense injection (R38)
+  bool inj = false;          // dense_in: modules read [X_n ; D]
+  void* Xin = nullptr;       // inj: the widened module input [B][m_mod][d] (work)
+  const void* Xs = nullptr;  // forward input X_n (the shortcut's; Xs == X without injection)
   int ens = 0;               // dhen_ensemble
   std::vector<Mod> mods;
   int64_t Wn = -1, gamma = -1, beta = -1, ensw = -1;
@@ -149,6 +153,10 @@ struct dhen_ctx {
   // scratch
   float* Ucat = nullptr;
   float* dXacc = nullptr;
+  float* dXacc2 = nullptr;        // R38: the modules' dX accumulator of injected layers [B][m_mod][d] (fp32)
+  float* dD = nullptr;            // R38: the injected dense tokens' gradient, summed over layers [B][nD][d]
+  bool dense_active = false;      // some layer injects dense tokens
+  const void* x0_cur = nullptr;   // X0 of the current step (layer 0's forward input): the injected tokens' source
   void* dR = nullptr;
   void* dY[2] = {nullptr, nullptr};
   dhen_tuning tune = tuning_default();   // schedule / fusion switches of this context (dhen_debug.h)
@@ -258,9 +266,15 @@ static dhen_status validate(const dhen_config* c) {
   if (c->optimizer < 0 || c->optimizer > 2)
     return fail(DHEN_E_CONFIG, "dhen_validate: optimizer=%d (0 SGD, 1 Adam, 2 Adam with bf16 moments)", c->optimizer);
   int m = c->m0;
+  if (c->dense_tokens < 0 || c->dense_tokens > c->m0)
+    return fail(DHEN_E_CONFIG, "dhen_validate: dense_tokens=%d (0 .. m0=%d)", c->dense_tokens, c->m0);
   for (int n = 0; n < c->n_layers; ++n) {
     const dhen_layer& L = c->layers[n];
     if (L.n_modules < 1 || !L.modules) return fail(DHEN_E_CONFIG, "dhen_validate: layer %d has no modules", n);
+    if (L.dense_in && c->dense_tokens < 1)
+      return fail(DHEN_E_CONFIG, "dhen_validate: layer %d injects dense tokens but dense_tokens=0 (R38)", n);
+    const int m_layer = m;
+    if (L.dense_in) m += c->dense_tokens;   // the modules read m_in + dense_tokens tokens
     int mo = 0;
     if (L.ensemble < DHEN_CONCAT || L.ensemble > DHEN_WSUM)
       return fail(DHEN_E_CONFIG, "dhen_validate: layer %d ensemble=%d (0 concat, 1 sum, 2 weighted sum)", n, L.ensemble);
@@ -279,6 +293,7 @@ static dhen_status validate(const dhen_config* c) {
       mo += s.l;
     }
     if (L.ensemble != DHEN_CONCAT) mo = L.modules[0].l;
+    (void)m_layer;
     m = mo;
   }
   return DHEN_OK;
@@ -301,6 +316,8 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
     Group& g = c->G[n];
     const dhen_layer& lc = c->cfg.layers[n];
     Lr.m_in = m;
+    Lr.inj = lc.dense_in != 0;
+    Lr.m_mod = m + (Lr.inj ? c->cfg.dense_tokens : 0);
     int mo = 0;
     for (int i = 0; i < lc.n_modules; ++i) mo += lc.modules[i].l;
     Lr.ens = lc.ensemble;
@@ -322,6 +339,8 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
     };
     Lr.mods.clear();
     int tok = 0;
+    const int m_layer = m;
+    m = Lr.m_mod;   // module parameters are shaped by the tokens the modules read (R38)
     for (int i = 0; i < lc.n_modules; ++i) {
       Mod md;
       md.s = lc.modules[i];
@@ -365,6 +384,8 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
       }
       Lr.mods.push_back(md);
     }
+    m = m_layer;
+    m_max = std::max(m_max, Lr.m_mod);
     if (Lr.ens == DHEN_WSUM) Lr.ensw = tensor(lc.n_modules, 1, 0);   // R27: initialised to 1
     if (m != mo) Lr.Wn = tensor((int64_t)m * mo, 0, m);
     Lr.gamma = tensor(d, 1, 0);
@@ -411,7 +432,8 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   m = c->cfg.m0;
   for (int n = 0; n < c->cfg.n_layers; ++n) {
     Layer& Lr = c->L[n];
-    const int mi = Lr.m_in, mo = Lr.m_out;
+    const int mi = Lr.m_mod, mo = Lr.m_out;   // (module buffers: the tokens the modules read)
+    if (Lr.inj) Lr.Xin = work.take((size_t)B * mi * d * es);
     Lr.Y = work.take((size_t)B * mo * d * es);
     Lr.R = work.take((size_t)B * mo * d * es);
     Lr.mu = (float*)work.take((size_t)B * mo * 4);
@@ -484,6 +506,12 @@ static void plan(dhen_ctx* c, Carver& state, Carver& work) {
   const size_t rows_d = (size_t)B * m_max * d;
   c->Ucat = (float*)work.take((size_t)B * m_out_max * d * 4);
   c->dXacc = (float*)work.take(rows_d * 4);
+  c->dense_active = false;
+  for (const Layer& Lr : c->L) c->dense_active = c->dense_active || Lr.inj;
+  if (c->dense_active) {
+    c->dXacc2 = (float*)work.take(rows_d * 4);
+    c->dD = (float*)work.take((size_t)B * c->cfg.dense_tokens * d * 4);
+  }
   c->dR = work.take(rows_d * es);
   c->dY[0] = work.take(rows_d * es);
   c->dY[1] = work.take(rows_d * es);
@@ -712,7 +740,8 @@ static dhen_status join_comm(dhen_ctx* c, cudaStream_t st) {
 static bool layer_lnf(const dhen_ctx* c, int n, int B) {
   const Layer& Lr = c->L[n];
   const int d = c->d, mi = Lr.m_in, mo = Lr.m_out;
-  bool lnf = c->tune.ln_fuse && c->dt == BF16 && Lr.Wn < 0 && mi == mo && (d == 128 || d == 256) && Lr.ens == DHEN_CONCAT;
+  bool lnf = c->tune.ln_fuse && c->dt == BF16 && Lr.Wn < 0 && mi == mo && (d == 128 || d == 256) && Lr.ens == DHEN_CONCAT &&
+             !Lr.inj;   // (injection: the modules read the widened input, the LayerNorm the layer's own)
   for (const Mod& m_ : Lr.mods) lnf = lnf && m_.s.kind != DHEN_DCN_LIT;   // (its output goes through the fp32 concat)
   for (const Mod& m_ : Lr.mods) {
     if (!lnf) break;
@@ -737,9 +766,17 @@ static bool dcn_pack(const dhen_ctx* c, int mi, int l, int B) {
 static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, cudaStream_t st) {
   Layer& Lr = c->L[n];
   const int d = c->d, dt = c->dt, es = c->es;
-  const int mi = Lr.m_in, mo = Lr.m_out;
+  const int mi = Lr.m_mod, mo = Lr.m_out;   // (mi: the tokens the modules read; the shortcut reads Lr.m_in)
   void* pbase;
   RET(comp_params(c, n, st, &pbase));
+  if (n == 0) c->x0_cur = X;
+  const void* Xs = X;   // the shortcut's input X_n
+  if (Lr.inj) {         // R38: the modules read [X_n ; D], D = X0's first dense_tokens tokens
+    if (!c->x0_cur) return fail(DHEN_E_STATE, "layer %d injects dense tokens: layer 0's forward has not run", n);
+    KT("layer.inject", 0, (double)B * (Lr.m_in + 2.0 * c->cfg.dense_tokens + mi) * d * es,
+       inject_copy(Xs, c->x0_cur, dt, B, Lr.m_in, c->cfg.dense_tokens, c->cfg.m0, d, Lr.Xin, st));
+    X = Lr.Xin;
+  }
   PP p{(char*)pbase, es};
   float* U = c->Ucat;
   const int64_t ldU = (int64_t)mo * d;
@@ -926,18 +963,19 @@ static dhen_status layer_fwd(dhen_ctx* c, int n, const void* X, void* Y, int B, 
   }
   if (use_side) { CK(cudaEventRecord(c->ev_sj, c->side_st)); CK(cudaStreamWaitEvent(st0, c->ev_sj, 0)); }
   // F11 shortcut (Eq.(2)) + F12 LayerNorm
-  if (Lr.Wn >= 0) RET(tokmix_fwd(c, X, mi, p(Lr.Wn), mo, U, ldU, B, Lr.ens == DHEN_CONCAT ? 1 : 0, st));
+  if (Lr.Wn >= 0) RET(tokmix_fwd(c, Xs, Lr.m_in, p(Lr.Wn), mo, U, ldU, B, Lr.ens == DHEN_CONCAT ? 1 : 0, st));
   if (Lr.ens != DHEN_CONCAT) {   // R = sum_i (w_i) U_i + shortcut, then the layer LayerNorm (R27)
     EnsU eu;
     eu.k = (int)Lr.mods.size();
     for (int i = 0; i < eu.k; ++i) eu.u[i] = Lr.mods[i].Uo;
     KT("layer.ens_ln", 0, (double)B * mo * d * (4.0 * eu.k + 2 * es + es),
-       ens_ln_fwd(eu, Lr.ens == DHEN_WSUM ? p(Lr.ensw) : nullptr, dt, Lr.Wn >= 0 ? U : nullptr, Lr.Wn >= 0 ? nullptr : X,
+       ens_ln_fwd(eu, Lr.ens == DHEN_WSUM ? p(Lr.ensw) : nullptr, dt, Lr.Wn >= 0 ? U : nullptr, Lr.Wn >= 0 ? nullptr : Xs,
                   p(Lr.gamma), p(Lr.beta), c->cfg.ln_eps, (int64_t)B * mo, d, Y, Lr.R, Lr.mu, Lr.rstd, dt, st));
   } else if (!lnf)
-    KT("layer.ln", 0, (double)B * mo * d * (4 + 2 * es) + (Lr.Wn >= 0 ? 0.0 : (double)B * mo * d * es), ln_fwd(U, Lr.Wn >= 0 ? nullptr : X, p(Lr.gamma), p(Lr.beta), dt, c->cfg.ln_eps, (int64_t)B * mo, d, Y, Lr.R, Lr.mu,
+    KT("layer.ln", 0, (double)B * mo * d * (4 + 2 * es) + (Lr.Wn >= 0 ? 0.0 : (double)B * mo * d * es), ln_fwd(U, Lr.Wn >= 0 ? nullptr : Xs, p(Lr.gamma), p(Lr.beta), dt, c->cfg.ln_eps, (int64_t)B * mo, d, Y, Lr.R, Lr.mu,
               Lr.rstd, dt, st));
-  Lr.X = X;
+  Lr.X = X;     // the modules' input
+  Lr.Xs = Xs;   // the shortcut's
   Lr.B = B;
   RET(release(c, n, st));
   return DHEN_OK;
@@ -948,7 +986,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   Layer& Lr = c->L[n];
   Group& G = c->G[n];
   const int d = c->d, dt = c->dt, es = c->es;
-  const int mi = Lr.m_in, mo = Lr.m_out;
+  const int mi = Lr.m_mod, mo = Lr.m_out;   // (mi: the tokens the modules read, R38)
   const void* X = Lr.X;
   void* pbase;
   RET(comp_params(c, n, st, &pbase));
@@ -957,7 +995,14 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   auto gp = [&](int64_t off) { return g + off; };
   const int64_t ldU = (int64_t)mo * d;
   const int64_t rows = (int64_t)B * mi;
-  float* acc = c->dXacc;
+  // R38 route (an injected layer, or layer 0 when any layer injects): the modules accumulate into their own
+  // [B][m_mod][d] buffer; the shortcut's part stays in dXacc; a final kernel forms dX (+ dD at layer 0)
+  const bool route = Lr.inj || (n == 0 && c->dense_active);
+  if (c->dense_active && n == c->cfg.n_layers - 1)   // the first backward layer of the step: dD starts at 0
+    CK(cudaMemsetAsync(c->dD, 0, (size_t)B * c->cfg.dense_tokens * d * 4, st));
+  float* acc_sc = c->dXacc;
+  float* acc = route ? c->dXacc2 : acc_sc;
+  if (route) CK(cudaMemsetAsync(acc, 0, (size_t)B * mi * d * 4, st));
   // B2: LN backward; identity shortcut (B3) initialises the dX accumulator
   // B3 identity shortcut: dX starts as dR.  When the first module's first dX-writing GEMM can add dR in its
   // epilogue (Dot: Gram backward, DCN: dT, Linear: token dgrad, MLP: fc1 dgrad) it initialises the fp32
@@ -978,7 +1023,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
       if (!(c->tune.first_writer && i == best)) order.push_back(&Lr.mods[i]);
   }
   const int first_kind = order.empty() ? -1 : order[0]->s.kind;
-  const bool first_dR = c->tune.first_writer && Lr.Wn < 0 && mi == mo &&
+  const bool first_dR = c->tune.first_writer && !route && Lr.Wn < 0 && mi == mo &&
                         (first_kind == DHEN_DOT || first_kind == DHEN_DCN || first_kind == DHEN_DCN_FULL ||
                          first_kind == DHEN_LINEAR || first_kind == DHEN_MLP);
   // Weight gradients of a module run on the side stream `sd` (own split-K / reduction scratch) while its
@@ -987,12 +1032,12 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   // (the profiled pass runs serialised so every op's event-timed duration is its own)
   cudaStream_t sd = (c->tune.overlap && !serial_prof(c)) ? c->side_st : st;
   // the LN parameter sums trail on sd (own scratch red3; the modules' joins below order its reuse)
-  KT("layer.ln_bwd", 0, (double)B * mo * d * (3 * es + (first_dR ? 0 : 4)), ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc, (Lr.Wn >= 0 || first_dR) ? 0 : 1,
+  KT("layer.ln_bwd", 0, (double)B * mo * d * (3 * es + (first_dR ? 0 : 4)), ln_bwd(dY, dt, Lr.R, Lr.mu, Lr.rstd, p(Lr.gamma), dt, (int64_t)B * mo, d, c->dR, dt, acc_sc, (Lr.Wn >= 0 || first_dR) ? 0 : 1,
             gp(Lr.gamma), gp(Lr.beta), c->red3, c->red_bytes, st, c->tune.trail ? sd : st, c->ev_red,
             c->vdy_now ? c->dz : nullptr, c->vdy_now ? (sharded(c) ? c->headw : c->G[c->cfg.n_layers].comp) : nullptr, mo));
   c->vdy_now = false;
   if (Lr.Wn >= 0)   // B3: dX = W_n dR ; dW_n += sum_b X_b dR_b^T
-    RET(tokmix_bwd(c, X, mi, p(Lr.Wn), mo, c->dR, ldU, acc, F32, 0, gp(Lr.Wn), B, st));
+    RET(tokmix_bwd(c, Lr.Xs, Lr.m_in, p(Lr.Wn), mo, c->dR, ldU, acc_sc, F32, 0, gp(Lr.Wn), B, st));
   const Workspace* ws2 = &c->ws2;
   float* red2 = c->red2;
   auto fork = [&]() -> dhen_status {
@@ -1033,7 +1078,7 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
   // The last module's last dX-writing GEMM emits dX (layer dtype) = accumulator + its contribution: the fp32
   // accumulator is read once and never written back, and no cast kernel runs.
   const int last_kind = order.empty() ? -1 : order.back()->s.kind;
-  const bool last_dX = dX && c->tune.first_writer &&
+  const bool last_dX = dX && c->tune.first_writer && !route &&
                        (last_kind == DHEN_DOT || last_kind == DHEN_DCN || last_kind == DHEN_DCN_FULL ||
                         last_kind == DHEN_LINEAR || last_kind == DHEN_MLP);
   bool first_mod = true;
@@ -1361,7 +1406,15 @@ static dhen_status layer_bwd(dhen_ctx* c, int n, const void* dY, void* dX, int B
     }
   }
   RET(real_join());   // the layer's side-stream work is done before anything after the layer
-  if (dX && !last_dX) KT("layer.dx_cast", 0, (double)rows * d * (4 + es), cast(acc, F32, dX, dt, rows * d, st));
+  if (route) {   // R38: the injected tokens' gradient, then dX = shortcut part + the modules' first m_in tokens (+ dD)
+    const int nD = c->cfg.dense_tokens, m_l = Lr.m_in;
+    if (Lr.inj) KT("layer.inject_bwd", 0, (double)B * nD * d * 12, inject_dD(acc, B, m_l, nD, d, c->dD, st));
+    if (dX)
+      KT("layer.dx_cast", 0, (double)B * m_l * d * (8 + es),
+         inject_final(acc_sc, acc, mi, n == 0 ? c->dD : nullptr, n == 0 ? nD : 0, B, m_l, d, dX, dt, st));
+  } else if (dX && !last_dX) {
+    KT("layer.dx_cast", 0, (double)rows * d * (4 + es), cast(acc, F32, dX, dt, rows * d, st));
+  }
   RET(release(c, n, st));
   RET(reduce_grads(c, n, st));
   return DHEN_OK;
@@ -1453,6 +1506,7 @@ static dhen_status make_ctx(const dhen_config* cfg, const dhen_dist* dist, dhen_
     c->mods_cfg[n].assign(cfg->layers[n].modules, cfg->layers[n].modules + cfg->layers[n].n_modules);
     c->layers_cfg[n].n_modules = cfg->layers[n].n_modules;
     c->layers_cfg[n].ensemble = cfg->layers[n].ensemble;
+    c->layers_cfg[n].dense_in = cfg->layers[n].dense_in;
     c->layers_cfg[n].modules = c->mods_cfg[n].data();
   }
   c->cfg.layers = c->layers_cfg.data();

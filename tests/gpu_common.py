@@ -14,7 +14,8 @@ def to_binding(net: O.NetSpec, dtype: str, B: int, seed: int = 0):
     layers = [[Module(s.kind, s.l, s.heads, s.ffn_mult, s.conv_channels, s.conv_k, tuple(s.mlp_hidden))
                for s in L.modules] for L in net.layers]
     return Config(net.m0, net.d, layers, dtype=dtype, batch_max_local=B, ln_eps=net.ln_eps, seed=seed,
-                  ensembles=[L.ensemble for L in net.layers])
+                  ensembles=[L.ensemble for L in net.layers], dense_tokens=net.dense_tokens,
+                  dense_in=[L.dense_in for L in net.layers])
 
 
 def t2np(t):

@@ -95,6 +95,24 @@ def test_ensemble_group_sizes_match_oracle(B, ens):
     assert O.layer_dims(net) == [(6, 5), (5, 5)]
 
 
+def test_dense_injection_group_sizes_match_oracle(B):
+    """Dense-token injection (R38): module parameters are shaped by m_in + dense_tokens in the injected layers
+    (token maps, the Dot pairs, the MLP input, the flattened DCN) -- the library's group sizes equal the oracle's;
+    a layer that injects with dense_tokens = 0 is rejected."""
+    import sys
+    sys.path.insert(0, "tests")
+    from test_oracle_stack import _inj_net
+    net = _inj_net()
+    cfg = _cfg(B, net)
+    for gi, g in enumerate(O.param_groups(net)):
+        n, _ = B.group_numel(cfg, gi)
+        assert n == O.group_size(g), gi
+    bad = O.NetSpec(6, 8, [O.LayerSpec([O.ModuleSpec("dcn", 6)], dense_in=True)])
+    with pytest.raises(B.DhenError) as e:
+        B.validate(_cfg(B, bad))
+    assert "dense_tokens" in str(e.value)
+
+
 def test_ensemble_validation_errors(B):
     mods = [O.ModuleSpec("dot", 5), O.ModuleSpec("dcn", 4)]
     net = O.NetSpec(6, 8, [O.LayerSpec(mods, ensemble="sum")])

@@ -389,3 +389,24 @@ def test_dcn_full_matches_oracle(dtype, tol, m, d, l, B):
     g = case.gpu_step(lr=0.05)
     o = case.oracle_step(lr=0.05)
     _compare(case, g, o, tol, tol, label=f"flattened DCN {dtype} m={m} d={d}")
+
+
+@pytest.mark.parametrize("dtype,tol,big", [("fp32", 1e-5, False), ("bf16", 2e-2, False), ("bf16", 2e-2, True)])
+def test_dense_injection_matches_oracle(dtype, tol, big):
+    """NEXT#3 method variant (R38): X0's first dense_tokens tokens injected into every module of the
+    dense_in layers (the modules read [X_n ; D]; the shortcut and the LayerNorm X_n), dD summed over the layers into
+    dX0's dense tokens -- full train step against the oracle (G1 / G3)."""
+    if big:
+        net = O.NetSpec(64, 128, [O.LayerSpec([M("dot", 32), M("dcn", 16), M("linear", 16)], dense_in=True),
+                                  O.LayerSpec([M("attn", 32), M("mlp", 32, mlp_hidden=(256, 128))]),
+                                  O.LayerSpec([M("dcn", 40), M("conv", 24)], dense_in=True)], dense_tokens=8)
+        B = 32
+    else:
+        import sys
+        sys.path.insert(0, "tests")
+        from test_oracle_stack import _inj_net
+        net, B = _inj_net(), 7
+    case = Case(net, B, dtype, seed=2203011014 + 13)
+    g = case.gpu_step(lr=0.05)
+    o = case.oracle_step(lr=0.05)
+    _compare(case, g, o, tol, tol, gated_report_only=(dtype == "bf16"), label=f"dense injection {dtype} big={big}")
