@@ -248,7 +248,7 @@ typedef struct {
   int d;                    /* token dimension: 4 | d, d <= 512                                             */
   int dtype;                /* dhen_dtype of dense, X0 and dX0                                              */
   int max_batch;            /* largest B of a forward                                                       */
-  long long max_nnz;        /* largest total number of ids of a forward                                     */
+  long long max_nnz;        /* largest total number of ids of a forward (<= 2^31 - 1)                        */
   unsigned long long seed;  /* init: tables U(+-sqrt(1/R_t)), W_k / b_k U(+-1/sqrt(fan_in))                 */
 } dhen_fp_config;
 typedef struct dhen_fp dhen_fp;

@@ -155,10 +155,10 @@ __global__ void __launch_bounds__(256) fp_route_k(const Shard* __restrict__ gsh,
 }
 
 // Backward, step 1: the occurrence keys (owned table jt << 40 | row; skipped ids -> all ones, sorted last) and their
-// bag ids (b * ntab + jt), in list order.
+// samples b (the bag is b * ntab + jt), in list order.
 __global__ void __launch_bounds__(256) emb_keys_k(const long long* __restrict__ trows, const int* __restrict__ ids,
                                                   const int* __restrict__ off, int ntab, int nb, unsigned long long* keys,
-                                                  int* bags) {
+                                                  int* samp) {
   pdl_entry();
   const int bag = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (bag >= nb * ntab) return;
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(256) emb_keys_k(const long long* __restrict__ 
   for (int e = lo + lane; e < hi; e += 32) {
     const long long r = ids[e];
     keys[e] = (r >= 0 && r < R) ? (((unsigned long long)jt << 40) | (unsigned long long)r) : ~0ull;
-    bags[e] = bag;
+    samp[e] = bag / ntab;
   }
 }
 
@@ -182,66 +182,59 @@ __global__ void __launch_bounds__(256) emb_heads_k(const unsigned long long* __r
 
 // Backward, step 3 (persistent, warp = run of equal rows, grid-strided over the *nruns runs): for each of this
 // rank's shards of the run's table, the run's gradient rows (grad[b * pitch + shard.out ..]) summed in the sorted
-// (= sample) order, four rows in flight, then E[row] -= lr * sum.  The table row is fetched with the run's first
-// rows, so a run of one occurrence costs one round of loads; 64 registers a thread keep 32 warps an SM resident
-// (the kernel is latency-bound on short runs).
-constexpr int FP_U = 4;
+// (= sample) order, two rows in flight, then E[row] -= lr * sum.  The table row is fetched with the run's first
+// rows, so a run of one occurrence costs one round of loads.  The kernel is latency-bound on short runs (three
+// occurrences a run on average at the bench shape), so resident warps are what count: 40 registers a thread keep
+// 48 warps an SM (measured, C4 bench shape: 11.7 ms at 4 rows in flight x 32 warps, 7.8 ms here; batching 32
+// runs' metadata per warp clumps the hot rows of a table onto one warp and was slower).
+constexpr int FP_U = 2;
 template <typename GT>
-__global__ void __launch_bounds__(256, 4) emb_runs_k(const unsigned long long* __restrict__ keys, const int* __restrict__ bags,
+__global__ void __launch_bounds__(256, 6) emb_runs_k(const unsigned long long* __restrict__ keys, const int* __restrict__ samp,
                                                      const int* __restrict__ heads, const int* __restrict__ nruns,
-                                                     long long n, const Shard* __restrict__ sh, const int2* __restrict__ trange,
+                                                     int n, const Shard* __restrict__ sh, const int2* __restrict__ trange,
                                                      int ntab, const GT* __restrict__ grad, long long pitch, float lr,
                                                      float* tab) {
   pdl_entry();
   const int lane = threadIdx.x & 31;
   const int nr = *nruns;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < nr; r += gridDim.x * 8) {
-    const long long lo = heads[r], hi = r + 1 < nr ? heads[r + 1] : n;
+    const int lo = heads[r], hi = r + 1 < nr ? heads[r + 1] : n;
     const unsigned long long K = keys[lo];
     const int jt = (int)(K >> 40);
     if (jt >= ntab) continue;   // the run of skipped ids
     const long long row_i = (long long)(K & ((1ull << 40) - 1));
     const int2 tr = trange[jt];   // this rank's shards of the table: [tr.x, tr.x + tr.y)
     for (int j = tr.x; j < tr.x + tr.y; ++j) {
-      const Shard s = sh[j];
-      const int w = s.width, nc = (w + 127) >> 7;
-      float* row = tab + s.base + row_i * w;
-      for (int q0 = 0; q0 < nc; q0 += 2) {   // 256 columns per round (w <= 512: at most two rounds)
-        float4 wv[2], acc[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int col = 128 * (q0 + q) + 4 * lane;
-          wv[q] = (q0 + q < nc && col < w) ? *reinterpret_cast<const float4*>(row + col) : make_float4(0.f, 0.f, 0.f, 0.f);
-          acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        for (long long p0 = lo; p0 < hi; p0 += FP_U) {
+      const int w = sh[j].width;
+      float* row = tab + sh[j].base + row_i * w + 4 * lane;
+      const GT* gcol = grad + sh[j].out + 4 * lane;
+      for (int c0 = 0; c0 < w; c0 += 256) {   // 256 columns per round (w <= 512: at most two rounds)
+        const bool ok0 = c0 + 4 * lane < w, ok1 = c0 + 128 + 4 * lane < w;
+        const float4 wv0 = ok0 ? *reinterpret_cast<const float4*>(row + c0) : z4;
+        const float4 wv1 = ok1 ? *reinterpret_cast<const float4*>(row + c0 + 128) : z4;
+        float4 acc0 = z4, acc1 = z4;
+        for (int p0 = lo; p0 < hi; p0 += FP_U) {
           float4 v[FP_U][2];
 #pragma unroll
           for (int u = 0; u < FP_U; ++u) {
             const bool ok = p0 + u < hi;
-            const int bag = ok ? bags[p0 + u] : 0;
-            const GT* g = grad + (long long)(bag / ntab) * pitch + s.out;
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int col = 128 * (q0 + q) + 4 * lane;
-              v[u][q] = (ok && q0 + q < nc && col < w) ? ld4<GT>(g + col) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
+            const GT* g = gcol + (long long)(ok ? samp[p0 + u] : 0) * pitch + c0;
+            v[u][0] = (ok && ok0) ? ld4<GT>(g) : z4;
+            v[u][1] = (ok && ok1) ? ld4<GT>(g + 128) : z4;
           }
 #pragma unroll
-          for (int u = 0; u < FP_U; ++u)
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              acc[q].x += v[u][q].x; acc[q].y += v[u][q].y; acc[q].z += v[u][q].z; acc[q].w += v[u][q].w;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int col = 128 * (q0 + q) + 4 * lane;
-          if (q0 + q < nc && col < w) {
-            wv[q].x -= lr * acc[q].x; wv[q].y -= lr * acc[q].y; wv[q].z -= lr * acc[q].z; wv[q].w -= lr * acc[q].w;
-            *reinterpret_cast<float4*>(row + col) = wv[q];
+          for (int u = 0; u < FP_U; ++u) {
+            acc0.x += v[u][0].x; acc0.y += v[u][0].y; acc0.z += v[u][0].z; acc0.w += v[u][0].w;
+            acc1.x += v[u][1].x; acc1.y += v[u][1].y; acc1.z += v[u][1].z; acc1.w += v[u][1].w;
           }
         }
+        if (ok0)
+          *reinterpret_cast<float4*>(row + c0) =
+              make_float4(wv0.x - lr * acc0.x, wv0.y - lr * acc0.y, wv0.z - lr * acc0.z, wv0.w - lr * acc0.w);
+        if (ok1)
+          *reinterpret_cast<float4*>(row + c0 + 128) =
+              make_float4(wv1.x - lr * acc1.x, wv1.y - lr * acc1.y, wv1.z - lr * acc1.z, wv1.w - lr * acc1.w);
       }
     }
   }
@@ -356,7 +349,8 @@ dhen_status validate(const dhen_fp_config* c) {
   if (c->n_dtok > 0 && c->n_dense <= 0) return ffail(DHEN_E_CONFIG, "dhen_fp: dense tokens need n_dense > 0");
   if (c->d <= 0 || c->d % 4 || c->d > 512) return ffail(DHEN_E_CONFIG, "dhen_fp: d = %d (4 | d, d <= 512)", c->d);
   if (c->dtype != DHEN_FP32 && c->dtype != DHEN_BF16) return ffail(DHEN_E_CONFIG, "dhen_fp: dtype %d", c->dtype);
-  if (c->max_batch <= 0 || c->max_nnz < 0) return ffail(DHEN_E_CONFIG, "dhen_fp: max_batch %d max_nnz %lld", c->max_batch, c->max_nnz);
+  if (c->max_batch <= 0 || c->max_nnz < 0 || c->max_nnz > 2147483647LL)   // int32 offsets / run heads
+    return ffail(DHEN_E_CONFIG, "dhen_fp: max_batch %d max_nnz %lld", c->max_batch, c->max_nnz);
   if (c->n_hidden < 0 || (c->n_hidden > 0 && !c->hidden) || (c->n_sparse > 0 && !c->rows))
     return ffail(DHEN_E_CONFIG, "dhen_fp: hidden / rows arrays missing");
   for (int i = 0; i < c->n_hidden; ++i)
@@ -664,10 +658,10 @@ dhen_status dhen_fp_backward_sgd(dhen_fp* f, const void* dx0, float lr, void* st
     FCK(cub::DeviceSelect::Flagged(f->sel_tmp, sb, cub::CountingInputIterator<int>(0), f->head, f->heads, f->nruns,
                                    (int64_t)n, st));
     if (bf)
-      FCK(pdl_launch(emb_runs_k<__nv_bfloat16>, 148 * 4, 256, 0, st, f->keys_out, f->bags_out, f->heads, f->nruns, n,
+      FCK(pdl_launch(emb_runs_k<__nv_bfloat16>, 148 * 6, 256, 0, st, f->keys_out, f->bags_out, f->heads, f->nruns, (int)n,
                      f->d_lsh, f->d_trange, nt, (const __nv_bfloat16*)grad, pitch, lr, f->tables));
     else
-      FCK(pdl_launch(emb_runs_k<float>, 148 * 4, 256, 0, st, f->keys_out, f->bags_out, f->heads, f->nruns, n, f->d_lsh,
+      FCK(pdl_launch(emb_runs_k<float>, 148 * 6, 256, 0, st, f->keys_out, f->bags_out, f->heads, f->nruns, (int)n, f->d_lsh,
                      f->d_trange, nt, (const float*)grad, pitch, lr, f->tables));
     g_launches += 5;
   }

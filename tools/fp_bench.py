@@ -15,7 +15,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--batch", type=int, default=0)
+ap.add_argument("--lib", default="", help="load this libdhen build instead of the default (A/B runs)")
 a = ap.parse_args()
+if a.lib:
+    binding.load(a.lib)
 cfg = configs.make(a.config, a.batch or None)
 B = cfg.batch_max_local
 ntab, R, nden, hid, ndtok, mbag = configs.FP[a.config]
