@@ -70,6 +70,8 @@ typedef struct {
                         prefetch and staged coalesced stores                                            (1) */
   int bn_max;        /* widest GEMM tile N (64 / 128 / 256); smaller tiles trade per-tile efficiency for
                         more tiles (wave quantization of short grids)                                 (256) */
+  int l2_prefetch;   /* short-K GEMMs (K <= 512): the TMA producer prefetches the operand tiles of the CTA's
+                        item this many items ahead into L2 (cp.async.bulk.prefetch.tensor); 0 off, <= 4 */
 } dhen_tuning;
 
 void dhen_tuning_default(dhen_tuning* t);

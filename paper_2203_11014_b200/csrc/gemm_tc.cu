@@ -222,6 +222,7 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   p.splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;   // no empty splits
   p.ws = ws.ptr;
   p.trace = g_gemm_trace;
+  p.pf_dist = tune().l2_prefetch;
   p.zbase = 0;
   p.nz = g.batch;
   p.lanes_rows = (g.c.cs != 1 && g.c.rs == 1 && splits == 1) ? 1 : 0;

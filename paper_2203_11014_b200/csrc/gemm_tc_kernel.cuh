@@ -98,6 +98,7 @@ struct Params {
   int ln_rdiv;        // lnst: rows per group L of the 4-D maps {N, L, M / L, batch}
   int dcnt;           // DCN backward (EF_DCNB): operands staged by TMA into per-warp shared boxes, outputs TMA-stored
   int crosst;         // DCN cross forward (bias + cross + aux, bf16): X by TMA boxes, A and T TMA-stored
+  int pf_dist;        // > 0: the producer prefetches the operand tiles of the item pf_dist items ahead into L2
 };
 // epilogue flags the TMA-store path implements (any subset; EF_ACC only with fp32 C, as cp.reduce .add)
 constexpr int TS_FLAGS = EF_BIAS | EF_RELU | EF_ACC | EF_BITS | EF_BMASK;
@@ -787,6 +788,20 @@ __device__ __forceinline__ void load_tile(const CUtensorMap* map, bool mn_major,
   }
 }
 
+// L2 prefetch of one operand's k-block tile (the same boxes load_tile fetches; no shared memory, no barrier)
+__device__ __forceinline__ void prefetch_tile(const CUtensorMap* map, bool mn_major, const OpCoords& q, int kin, int ko,
+                                              int chunks) {
+  int c[5];
+  c[2] = q.c2 + ko; c[3] = q.c3; c[4] = q.c4;
+  for (int j = 0; j < (mn_major ? chunks : 1); ++j) {
+    if (!mn_major) { c[0] = kin; c[1] = q.mn; }
+    else { c[0] = q.mn + 64 * j; c[1] = kin; }
+    asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(map), "r"(c[0]),
+                 "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4])
+                 : "memory");
+  }
+}
+
 // Persistent, warp-specialised kernel: warp 0 = TMA producer, warp 1 = MMA issuer,
 // warps 2-9 = epilogue.  Work items (tile, batch index, K split) are strided over
 // the grid.  The TMEM accumulator is double-buffered (2 x BN columns) so the
@@ -917,7 +932,28 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       // ---------------- TMA producer
       int it = 0;
+      // short K: the operand tiles of the item pf_dist items ahead are requested into L2 now, so the ring's loads
+      // of that item hit L2 instead of waiting out a DRAM round trip with only NST k-blocks in flight
+      auto l2_prefetch = [&](int pitem) {
+        int m0, n0, z, sp, kb0, nk;
+        decode(pitem, m0, n0, z, sp, kb0, nk);
+        const OpCoords qa = op_coords(p.a, m0 + (int)crank * BM, z), qb = op_coords(p.b, n0 + (int)crank * (BN / 2), z);
+        int ka = p.a.has_ko ? (kb0 * BK) % p.a.kdiv : kb0 * BK, koa = p.a.has_ko ? (kb0 * BK) / p.a.kdiv : 0;
+        int kbk = p.b.has_ko ? (kb0 * BK) % p.b.kdiv : kb0 * BK, kob = p.b.has_ko ? (kb0 * BK) / p.b.kdiv : 0;
+        const int kda = p.a.has_ko ? p.a.kdiv : 0x7fffffff, kdb = p.b.has_ko ? p.b.kdiv : 0x7fffffff;
+        for (int i = 0; i < nk; ++i) {
+          prefetch_tile(&tma_a, p.a.mn_major != 0, qa, ka, koa, BM / 64);
+          prefetch_tile(&tma_b, p.b.mn_major != 0, qb, kbk, kob, pair ? BN / 128 : BN / 64);
+          ka += BK; while (ka >= kda) { ka -= kda; ++koa; }
+          kbk += BK; while (kbk >= kdb) { kbk -= kdb; ++kob; }
+        }
+      };
+      const bool pf = p.pf_dist > 0 && p.kb_per_split <= 8;
+      if (pf)
+        for (int d = 1; d < p.pf_dist; ++d)
+          if (wid + d * nwk < total) l2_prefetch(wid + d * nwk);
       for (int item = wid; item < total; item += nwk) {
+        if (pf && item + p.pf_dist * nwk < total) l2_prefetch(item + p.pf_dist * nwk);
         int m0, n0, z, sp, kb0, nk;
         decode(item, m0, n0, z, sp, kb0, nk);
         const OpCoords qa = op_coords(p.a, m0 + (int)crank * BM, z), qb = op_coords(p.b, n0 + (int)crank * (BN / 2), z);

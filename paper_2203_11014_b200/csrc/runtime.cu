@@ -1765,6 +1765,8 @@ dhen_status dhen_set_tuning(dhen_ctx* c, const dhen_tuning* t) {
     if (b != 0 && b != 1) return fail(DHEN_E_CONFIG, "dhen_set_tuning: a 0/1 switch is %d", b);
   if (t->bn_max != 64 && t->bn_max != 128 && t->bn_max != 256)
     return fail(DHEN_E_CONFIG, "dhen_set_tuning: bn_max=%d (64, 128 or 256)", t->bn_max);
+  if (t->l2_prefetch < 0 || t->l2_prefetch > 4)
+    return fail(DHEN_E_CONFIG, "dhen_set_tuning: l2_prefetch=%d (0..4)", t->l2_prefetch);
   if (t->sym < -1 || t->sym > 2 || t->pair < -1 || t->pair > 1 || t->pair_k < 0)
     return fail(DHEN_E_CONFIG, "dhen_set_tuning: sym=%d pair=%d pair_k=%d", t->sym, t->pair, t->pair_k);
   c->tune = *t;

@@ -18,6 +18,7 @@ tstore        TMA-store GEMM epilogue vs the register epilogue                 -
 ln_tma        LayerNorm epilogue: residual by TMA, R / Y by TMA store          -> bitwise identical
 dcn_tma       DCN-backward epilogue: X / A / dR by TMA, dA / dX by TMA store   -> bitwise (db grouping)
 dcn_fused     DCN backward as one kernel vs dT GEMM + dA W GEMM               -> bitwise (db grouping)
+l2_prefetch   short-K GEMM operands prefetched into L2 items ahead (off)      -> bitwise identical
 """
 import numpy as np
 import pytest
@@ -135,6 +136,17 @@ def test_schedule_switches_bitwise(name, B, layers, switch):
     a = _step(net, B, 18, {switch: 0})
     b = _step(net, B, 18, {})
     _cmp(a, b, net, 1e-3 if switch == "tstore" else 0)
+
+
+@pytest.mark.parametrize("name,B,layers", [("C4", 256, 1), ("C5", 1024, 1)])
+def test_l2_prefetch_bitwise(name, B, layers):
+    """The producer's L2 prefetch of later items' operand tiles (dhen_tuning.l2_prefetch, off by default:
+    measured slower) only moves data into L2: bit-identical steps.  Batches large enough that the
+    short-K GEMMs have more than 2 x 148 items, so the prefetch is issued."""
+    net = _net(name, layers)
+    a = _step(net, B, 24, {"l2_prefetch": 2})
+    b = _step(net, B, 24, {})
+    _cmp(a, b, net, 0)
 
 
 @pytest.mark.parametrize("name,B,layers", [("C4", 16, 2), ("C2", 64, 2)])
