@@ -72,6 +72,8 @@ typedef struct {
                         more tiles (wave quantization of short grids)                                 (256) */
   int l2_prefetch;   /* short-K GEMMs (K <= 512): the TMA producer prefetches the operand tiles of the CTA's
                         item this many items ahead into L2 (cp.async.bulk.prefetch.tensor); 0 off, <= 4 */
+  int wres;          /* 1: short-K TMA-store GEMMs (K <= 256, BN = 256, bf16 C) keep the CTA's weight tile resident
+                        in shared memory and stream only A (a third of the L2 reads)                    (1) */
 } dhen_tuning;
 
 void dhen_tuning_default(dhen_tuning* t);

@@ -336,6 +336,10 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
       p.ln_rdiv = L;
     }
   }
+  // W-resident short-K GEMMs (Params::wr): the CTA's K x 256 weight tile stays in shared memory, the ring streams A
+  const int fl_ = p.ep.flags;
+  p.wr = (tune().wres && p.tstore && var > 0 && BN == 256 && !p.pair && splits == 1 && g.batch == 1 && p.kblocks <= 4 &&
+          p.n_fast && (fl_ & ~TS_FLAGS) == 0 && !(fl_ & EF_ACC) && g.c.dt == BF16) ? 1 : 0;
   if (g.e.ln_gamma && (!p.lean || var != p.lean_id || (p.ep.flags & EF_LN) == 0 || p.lanes_rows)) return cudaErrorNotSupported;
   if (g.e.bits_mode && !p.tstore) return cudaErrorNotSupported;   // bitmask epilogues exist on the TMA-store path
   // column sums of the stored C exist on the bf16 TMA-store path only (rows = M / 32 blocks per batch item)

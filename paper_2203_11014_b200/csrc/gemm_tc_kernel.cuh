@@ -99,6 +99,7 @@ struct Params {
   int dcnt;           // DCN backward (EF_DCNB): operands staged by TMA into per-warp shared boxes, outputs TMA-stored
   int crosst;         // DCN cross forward (bias + cross + aux, bf16): X by TMA boxes, A and T TMA-stored
   int pf_dist;        // > 0: the producer prefetches the operand tiles of the item pf_dist items ahead into L2
+  int wr;             // W-resident instantiation (gemm_tc_kernel<.., WR = true>): the CTA's B tile stays in shared memory
 };
 // epilogue flags the TMA-store path implements (any subset; EF_ACC only with fp32 C, as cp.reduce .add)
 constexpr int TS_FLAGS = EF_BIAS | EF_RELU | EF_ACC | EF_BITS | EF_BMASK;
@@ -838,12 +839,26 @@ constexpr int eff_stages() {
 // per-warp TMA-arrival barriers of the operand epilogues (DCN backward: 2 slots; LayerNorm: 1)
 template <int VAR> constexpr bool has_opbar() { return (VarF<VAR>::F & (EF_DCNB | EF_LN | EF_CROSS)) != 0; }
 
+// W-resident short-K GEMMs (Params::wr): a CTA keeps the whole K x BN tile of B (the weight, K <= 256) in shared
+// memory for all its items -- with N tiles fastest and a grid that is a multiple of tiles_n, every item of a CTA
+// has the same N tile -- and the ring streams only A.  Per 128 x 256 tile the CTA then reads 64 KB instead of
+// 192 KB through L2 (these GEMMs sit at the L2 throughput cap).  TMA-store epilogues only, with one
+// store box per warp (the resident tile takes the second box's shared memory), and the bias row of the CTA's one N
+// tile staged once.
+constexpr int WR_NA = 4, WR_KB = 4;   // A-ring slots; resident B k-blocks (K <= 4 BK = 256)
+template <int BN, int VAR> constexpr bool wr_ok() {
+  return BN == 256 && VAR > 0 && (VarF<VAR>::F & ~TS_FLAGS) == 0 && !VarF<VAR>::C && (VarF<VAR>::F & EF_ACC) == 0;
+}
+template <int BN> constexpr int wr_smem() {
+  return WR_NA * BM * BK * 2 + WR_KB * BN * BK * 2 + 8 * 4096 + BN * 4 + (2 * WR_NA + 6) * 8 + 16 + 1024;   // bias: 1 tile
+}
+
 template <int BN, int STAGES, bool PAIR>
 constexpr int ring_stages() {
   return PAIR ? (STAGES * (BM * BK * 2 + BN * BK * 2)) / (BM * BK * 2 + BN * BK) : STAGES;
 }
 
-template <int BN, int STAGES, int VAR, bool PAIR>
+template <int BN, int STAGES, int VAR, bool PAIR, bool WR = false>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    const __grid_constant__ OutMaps tma_o, const __grid_constant__ Params p) {
@@ -852,21 +867,23 @@ __global__ void __launch_bounds__(320, 1)
   // B bytes per ring slot in this CTA (a pair CTA loads BN / 2 rows), and the ring depth the same shared
   // memory holds: a pair kernel gets the deeper ring (BN = 256: 4 slots instead of 3)
   constexpr int B_BYTES = PAIR ? BN * BK : BN * BK * 2;
-  constexpr int NST = ring_stages<BN, STAGES, PAIR>();
+  constexpr int NST = WR ? WR_NA : ring_stages<BN, STAGES, PAIR>();
+  static_assert(!WR || (!PAIR && wr_ok<BN, VAR>()), "W-resident: single-CTA TMA-store variants");
   constexpr int SC = EpiSmem<BN>::SC;
   constexpr int SROW = EpiSmem<BN>::SROW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + NST * A_BYTES;
-  float* stage_all = (float*)(sB + NST * B_BYTES);   // fp32 staging, or the TMA-store boxes (1024-B aligned)
-  float* sbias = (float*)((uint8_t*)stage_all + epi_bytes<BN, VAR, PAIR>());   // [2][BN] bias of the current tiles
-  uint64_t* bars = (uint64_t*)(sbias + EpiSmem<BN>::SBIAS);   // full[S], empty[S], tfull[2], tempty[2]
+  uint8_t* sB = smem + NST * A_BYTES;   // WR: the resident B tile (WR_KB k-blocks), else the ring's B slots
+  float* stage_all = (float*)(sB + (WR ? WR_KB : NST) * B_BYTES);   // fp32 staging, or the TMA-store boxes (1024-B aligned)
+  float* sbias = (float*)((uint8_t*)stage_all + (WR ? 8 * 4096 : epi_bytes<BN, VAR, PAIR>()));   // [2][BN] bias of the current tiles
+  uint64_t* bars = (uint64_t*)(sbias + (WR ? BN : EpiSmem<BN>::SBIAS));   // full[S], empty[S], tfull[2], tempty[2]
   uint64_t* full = bars;
   uint64_t* empty = bars + NST;
   uint64_t* tfull = bars + 2 * NST;
   uint64_t* tempty = bars + 2 * NST + 2;
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * NST + 4);
+  uint64_t* wfull = bars + 2 * NST + 5;   // WR: the resident B tile has landed
   // DCN-backward variants: [8 epilogue warps][256 columns] fp32 column sums of dA (Lean::bsum)
   constexpr bool BSV = VAR > 0 && (VarF<VAR>::F & EF_DCNB) != 0;
   float* csum = (float*)(bars + 2 * NST + 6);
@@ -887,6 +904,7 @@ __global__ void __launch_bounds__(320, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
     for (int s = 0; s < 2 * NST + 2; ++s) mbar_init(smem_u32(bars + s), 1);
     for (int s = 0; s < 2; ++s) mbar_init(smem_u32(tempty + s), pair ? 16 : 8);   // epilogue warps of both CTAs
+    if constexpr (WR) mbar_init(smem_u32(wfull), 1);
     if constexpr (VAR > 0 && has_opbar<VAR>())
       for (int s = 0; s < 16; ++s) mbar_init(smem_u32(opbar + s), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -943,11 +961,25 @@ __global__ void __launch_bounds__(320, 1)
         const int kda = p.a.has_ko ? p.a.kdiv : 0x7fffffff, kdb = p.b.has_ko ? p.b.kdiv : 0x7fffffff;
         for (int i = 0; i < nk; ++i) {
           prefetch_tile(&tma_a, p.a.mn_major != 0, qa, ka, koa, BM / 64);
-          prefetch_tile(&tma_b, p.b.mn_major != 0, qb, kbk, kob, pair ? BN / 128 : BN / 64);
+          if (!WR) prefetch_tile(&tma_b, p.b.mn_major != 0, qb, kbk, kob, pair ? BN / 128 : BN / 64);   // (WR: resident)
           ka += BK; while (ka >= kda) { ka -= kda; ++koa; }
           kbk += BK; while (kbk >= kdb) { kbk -= kdb; ++kob; }
         }
       };
+      if constexpr (WR) {   // the CTA's B tile, once (every item of this CTA has the same N tile and all of K)
+        if (wid < total) {
+          int m0, n0, z, sp, kb0, nk;
+          decode(wid, m0, n0, z, sp, kb0, nk);
+          const OpCoords qb = op_coords(p.b, n0, z);
+          int kbk = p.b.has_ko ? (kb0 * BK) % p.b.kdiv : kb0 * BK, kob = p.b.has_ko ? (kb0 * BK) / p.b.kdiv : 0;
+          const int kdb = p.b.has_ko ? p.b.kdiv : 0x7fffffff;
+          mbar_expect_tx(smem_u32(wfull), (uint32_t)(nk * B_BYTES));
+          for (int i = 0; i < nk; ++i) {
+            load_tile(&tma_b, p.b.mn_major != 0, qb, kbk, kob, smem_u32(sB) + i * B_BYTES, smem_u32(wfull), BN / 64, false);
+            kbk += BK; while (kbk >= kdb) { kbk -= kdb; ++kob; }
+          }
+        }
+      }
       const bool pf = p.pf_dist > 0 && p.kb_per_split <= 8;
       if (pf)
         for (int d = 1; d < p.pf_dist; ++d)
@@ -968,14 +1000,16 @@ __global__ void __launch_bounds__(320, 1)
           mbar_wait(smem_u32(empty + s), ph ^ 1);
           if (p.trace && blockIdx.x == 0 && it < 64) p.trace[it] = clock64();
           uint32_t fb = smem_u32(full + s);
-          if (!pair) {
+          if (WR) {
+            mbar_expect_tx(fb, A_BYTES);
+          } else if (!pair) {
             mbar_expect_tx(fb, A_BYTES + B_BYTES);
           } else {
             if (crank == 0) mbar_expect_tx(fb, 2 * (A_BYTES + B_BYTES));   // both CTAs' halves land on rank 0's barrier
             fb = mapa_u32(fb, 0);
           }
           load_tile(&tma_a, amn, qa, ka, koa, smem_u32(sA) + s * A_BYTES, fb, BM / 64, pair);
-          load_tile(&tma_b, bmn, qb, kbk, kob, smem_u32(sB) + s * B_BYTES, fb, pair ? BN / 128 : BN / 64, pair);
+          if (!WR) load_tile(&tma_b, bmn, qb, kbk, kob, smem_u32(sB) + s * B_BYTES, fb, pair ? BN / 128 : BN / 64, pair);
           ka += BK; while (ka >= kda) { ka -= kda; ++koa; }     // kdiv < BK: several outer indices per k-block
           kbk += BK; while (kbk >= kdb) { kbk -= kdb; ++kob; }
           if (++s == NST) { s = 0; ph ^= 1; }
@@ -989,6 +1023,10 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t b_step = p.b.mn_major ? 16 * 128 : 32;
       const uint32_t a_lbo = p.a.mn_major ? 64 * BK * 2 : 16, b_lbo = p.b.mn_major ? 64 * BK * 2 : 16;
       int it = 0, li = 0;
+      if constexpr (WR) {
+        mbar_wait(smem_u32(wfull), 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+      }
       for (int item = wid; item < total; item += nwk, ++li) {
         int m0, n0, z, sp, kb0, nk;
         decode(item, m0, n0, z, sp, kb0, nk);
@@ -1005,7 +1043,7 @@ __global__ void __launch_bounds__(320, 1)
           mbar_wait(smem_u32(full + s), ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (p.trace && blockIdx.x == 0 && it < 64) p.trace[128 + it] = clock64();
-          const uint32_t ab_ = smem_u32(sA + s * A_BYTES), bb_ = smem_u32(sB + s * B_BYTES);
+          const uint32_t ab_ = smem_u32(sA + s * A_BYTES), bb_ = smem_u32(sB + (WR ? i : s) * B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = sdesc(ab_ + kk * a_step, a_lbo, 1024);
@@ -1549,14 +1587,16 @@ __global__ void __launch_bounds__(320, 1)
           constexpr int F = VarF<VAR>::F;
           constexpr bool CF = VarF<VAR>::C;
           constexpr int CW = CF ? 32 : 64;
-          float* sb = sbias + ab * BN;
+          float* sb = WR ? sbias : sbias + ab * BN;
           if constexpr ((F & EF_BIAS) != 0) {
-            asm volatile("bar.sync 1, 256;" ::: "memory");   // every epilogue warp finished the tile that used sb
-            const int t = threadIdx.x - 64;
-            for (int j = t; j < BN; j += 256) sb[j] = (n0 + j < g.N) ? lean_bias(e, n0 + j) : 0.f;
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (!WR || li == 0) {   // WR: every item of the CTA has the same N tile, so the same bias row
+              asm volatile("bar.sync 1, 256;" ::: "memory");   // every epilogue warp finished the tile that used sb
+              const int t = threadIdx.x - 64;
+              for (int j = t; j < BN; j += 256) sb[j] = (n0 + j < g.N) ? lean_bias(e, n0 + j) : 0.f;
+              asm volatile("bar.sync 1, 256;" ::: "memory");
+            }
           }
-          const uint32_t boxes = smem_u32(stage_all) + (uint32_t)((warp - 2) * 2 * 4096);
+          const uint32_t boxes = smem_u32(stage_all) + (uint32_t)((warp - 2) * (WR ? 1 : 2) * 4096);
           const float alpha = e.alpha;
 #pragma unroll 1
           for (int pc = 0; pc < HC; pc += CW) {
@@ -1617,9 +1657,11 @@ __global__ void __launch_bounds__(320, 1)
                 for (int q = 0; q < CW / 32; ++q) bp[(int64_t)q * e.bits_ld] = mw[q];
               }
             }
-            const uint32_t box = boxes + (uint32_t)((tsel & 1) * 4096);   // alternate across passes AND tiles
+            const uint32_t box = boxes + (uint32_t)(WR ? 0 : (tsel & 1) * 4096);   // alternate across passes AND tiles
             ++tsel;
-            if (lane == 0) bulk_wait_read<1>();   // the store that last read this box is done with it
+            if (lane == 0) {   // the store that last read this box is done with it
+              if constexpr (WR) bulk_wait_read<0>(); else bulk_wait_read<1>();
+            }
             __syncwarp();
             const uint32_t rowa = box + (uint32_t)(lane * 128);
 #pragma unroll
@@ -1881,6 +1923,22 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
     attr = true;
   }
   const int ntiles = p0.tiles_m * p0.tiles_n;
+  if constexpr (wr_ok<BN, VAR>()) if (p0.wr) {   // W-resident (host: batch 1, one split, N tiles fastest, K <= 256)
+    constexpr int SMEM_W = wr_smem<BN>();
+    static_assert(SMEM_W <= 227 * 1024, "smem");
+    static bool wattr = false;
+    if (!wattr) {
+      cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, VAR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_W);
+      wattr = true;
+    }
+    // a multiple of tiles_n CTAs: with N tiles fastest, CTA c only ever sees N tile c % tiles_n
+    const int grid = (int)std::min<int64_t>(ntiles, (148 / p0.tiles_n) * p0.tiles_n);
+    g_last_gemm_grid = grid;
+    cudaError_t e = pdl_launch(gemm_tc_kernel<BN, STAGES, VAR, false, true>, grid, 320, SMEM_W, st, ma, mb, mc, p0);
+    if (e != cudaSuccess) return e;
+    ++g_launches;
+    return cudaGetLastError();
+  }
   const int zmax = std::max(1, (int)std::min<int64_t>(p0.g.batch, (int64_t)(1 << 30) / ((int64_t)ntiles * p0.splits)));
   for (int zb = 0; zb < p0.g.batch; zb += zmax) {
     Params p = p0;

@@ -19,6 +19,7 @@ ln_tma        LayerNorm epilogue: residual by TMA, R / Y by TMA store          -
 dcn_tma       DCN-backward epilogue: X / A / dR by TMA, dA / dX by TMA store   -> bitwise (db grouping)
 dcn_fused     DCN backward as one kernel vs dT GEMM + dA W GEMM               -> bitwise (db grouping)
 l2_prefetch   short-K GEMM operands prefetched into L2 items ahead (off)      -> bitwise identical
+wres          short-K GEMMs with the weight tile resident in shared memory    -> bitwise identical
 """
 import numpy as np
 import pytest
@@ -125,7 +126,7 @@ def test_dense_symmetrisation_bitwise(name, B, layers, mode):
     _cmp(a, b, net, 0)
 
 
-@pytest.mark.parametrize("switch", ["defer_join", "trail", "bd_pre", "tstore", "ln_tma"])
+@pytest.mark.parametrize("switch", ["defer_join", "trail", "bd_pre", "tstore", "ln_tma", "wres"])
 @pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2), ("C3", 32, 2)])
 def test_schedule_switches_bitwise(name, B, layers, switch):
     """Schedule-only switches (same kernels' arithmetic in another order of launch / store path): the
@@ -136,6 +137,16 @@ def test_schedule_switches_bitwise(name, B, layers, switch):
     a = _step(net, B, 18, {switch: 0})
     b = _step(net, B, 18, {})
     _cmp(a, b, net, 1e-3 if switch == "tstore" else 0)
+
+
+@pytest.mark.parametrize("name,B,layers", [("C4", 256, 1), ("C3", 512, 1)])
+def test_wres_many_items_bitwise(name, B, layers):
+    """W-resident GEMMs over many items a CTA (FFN1 / FFN2 dgrad / QKV at C4, the MLP GEMMs at C3): bit-identical
+    to the streamed-B kernel."""
+    net = _net(name, layers)
+    a = _step(net, B, 25, {"wres": 0})
+    b = _step(net, B, 25, {})
+    _cmp(a, b, net, 0)
 
 
 @pytest.mark.parametrize("name,B,layers", [("C4", 256, 1), ("C5", 1024, 1)])

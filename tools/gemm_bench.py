@@ -82,8 +82,12 @@ def main():
     ap.add_argument("--path", type=int, default=0)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--flush", default="write", choices=["write", "read", "none"])
+    ap.add_argument("--lib", default="", help="load this libdhen build instead of the default (A/B runs)")
     ap.add_argument("--epi", type=int, default=0, help="fused epilogue mode (1 mask, 2 resid, 3 cross, 4 relu, 5 relu+bits out, 6 bits in)")
     args = ap.parse_args()
+    if args.lib:
+        from paper_2203_11014_b200 import binding
+        binding.load(args.lib)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for (name, M, N, K, Z, a, b, c, acc, a2, b2, c2, cdt) in shapes(args.cfg):
