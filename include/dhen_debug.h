@@ -74,6 +74,8 @@ typedef struct {
                         item this many items ahead into L2 (cp.async.bulk.prefetch.tensor); 0 off, <= 4 */
   int wres;          /* 1: short-K TMA-store GEMMs (K <= 256, BN = 256, bf16 C) keep the CTA's weight tile resident
                         in shared memory and stream only A (a third of the L2 reads)                    (1) */
+  int resid_tma;     /* 1: the fp32-residual GEMM epilogue (token-map dgrad first writer) takes dR through TMA
+                        boxes and stores C by TMA; 0: register prefetch and staged stores               (1) */
 } dhen_tuning;
 
 void dhen_tuning_default(dhen_tuning* t);

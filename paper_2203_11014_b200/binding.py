@@ -71,7 +71,7 @@ class dhen_tuning(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("overlap", "defer_join", "ln_fuse", "first_writer", "relu_bits", "fuse_db",
                                          "vdy", "trail", "bd_pre", "sym", "tstore", "pair", "pair_k", "attn_fused",
                                          "pdl", "gemm_simt", "dcn_fused", "dcn_tma", "ln_tma", "bn_max",
-                                         "l2_prefetch", "wres")]
+                                         "l2_prefetch", "wres", "resid_tma")]
 
 
 class dhen_fp_config(C.Structure):

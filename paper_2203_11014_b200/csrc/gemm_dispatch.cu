@@ -13,7 +13,7 @@ dhen_tuning tuning_default() {
   dhen_tuning t;
   t.overlap = 1; t.defer_join = 1; t.ln_fuse = 1; t.first_writer = 1; t.relu_bits = 1; t.fuse_db = 1; t.vdy = 1;
   t.trail = 1; t.bd_pre = 1; t.sym = -1; t.tstore = 1; t.pair = -1; t.pair_k = 1024; t.attn_fused = 1; t.pdl = 0;
-  t.gemm_simt = 0; t.dcn_fused = 1; t.dcn_tma = 1; t.ln_tma = 1; t.bn_max = 256; t.l2_prefetch = 0; t.wres = 1;
+  t.gemm_simt = 0; t.dcn_fused = 1; t.dcn_tma = 1; t.ln_tma = 1; t.bn_max = 256; t.l2_prefetch = 0; t.wres = 1; t.resid_tma = 1;
   return t;
 }
 static thread_local const dhen_tuning* t_tune = nullptr;

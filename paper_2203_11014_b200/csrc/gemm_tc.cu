@@ -304,6 +304,12 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
       g.e.bias_dt == BF16 && p.lean_id > 0) {
     if (map3(&mc.x, g.e.cross, false) && map3(&mc.a, g.e.aux, false) && map3(&mc.c, g.c, false)) p.crosst = 1;
   }
+  // fp32-residual epilogue (the token-map dgrad's first writer): dR in, C out as 32 x 32 boxes by TMA
+  p.rst = 0;
+  if (tune().resid_tma && opnd_ok && BN >= 128 && p.ep.flags == (EF_RESID | EF_R32) && g.c.dt == BF16 && p.lean_id > 0 &&
+      g.e.resid.dt == F32) {
+    if (map3(&mc.r, g.e.resid, true) && map3(&mc.c, g.c, false)) p.rst = 1;
+  }
   p.lnst = 0;
   p.ln_rdiv = 0;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a.mn_major << 15) | ((uint32_t)p.b.mn_major << 16) |

@@ -98,6 +98,7 @@ struct Params {
   int ln_rdiv;        // lnst: rows per group L of the 4-D maps {N, L, M / L, batch}
   int dcnt;           // DCN backward (EF_DCNB): operands staged by TMA into per-warp shared boxes, outputs TMA-stored
   int crosst;         // DCN cross forward (bias + cross + aux, bf16): X by TMA boxes, A and T TMA-stored
+  int rst;            // fp32-residual epilogue (EF_RESID | EF_R32, bf16 C): residual by TMA boxes, C TMA-stored
   int pf_dist;        // > 0: the producer prefetches the operand tiles of the item pf_dist items ahead into L2
   int wr;             // W-resident instantiation (gemm_tc_kernel<.., WR = true>): the CTA's B tile stays in shared memory
 };
@@ -837,7 +838,9 @@ constexpr int eff_stages() {
   return (VarF<VAR>::F & EF_DCNB) != 0 ? 1 : STAGES;
 }
 // per-warp TMA-arrival barriers of the operand epilogues (DCN backward: 2 slots; LayerNorm: 1)
-template <int VAR> constexpr bool has_opbar() { return (VarF<VAR>::F & (EF_DCNB | EF_LN | EF_CROSS)) != 0; }
+template <int VAR> constexpr bool has_opbar() {
+  return (VarF<VAR>::F & (EF_DCNB | EF_LN | EF_CROSS)) != 0 || (VarF<VAR>::F == (EF_RESID | EF_R32) && !VarF<VAR>::C);
+}
 
 // W-resident short-K GEMMs (Params::wr): a CTA keeps the whole K x BN tile of B (the weight, K <= 256) in shared
 // memory for all its items -- with N tiles fastest and a grid that is a multiple of tiles_n, every item of a CTA
@@ -1106,6 +1109,19 @@ __global__ void __launch_bounds__(320, 1)
       tma_load3(opw + slot_ * 4096u, &tma_o.x, n0_ + hh * HC + 32 * j_, m0_ + q4 * 32, z_, b);
     };
     if (XTV && p.crosst && lane == 0 && wid < total) xt_issue(wid, 0, 0u);
+    // fp32-residual epilogue with TMA (RTV && p.rst; the first writer of a token-map dgrad, C = alpha acc + dR):
+    // per warp and 32-column pass the fp32 residual box (32 rows x 128 B) arrives into one of two 4-KB slots --
+    // the next pass's flies while this one is combined -- lane = row reads its 32 values, then writes the bf16
+    // result into the slot's first 2 KB as a 64-B-swizzled 32 x 32 box, which leaves by TMA store
+    constexpr bool RTV = VAR > 0 && VarF<VAR>::F == (EF_RESID | EF_R32) && !VarF<VAR>::C;
+    auto rt_issue = [&](int item_, int j_, uint32_t slot_) {   // lane 0: the residual box of (item_, pass j_)
+      int m0_, n0_, z_, sp_, kb0_, nk_;
+      decode(item_, m0_, n0_, z_, sp_, kb0_, nk_);
+      const uint32_t b = obar + slot_ * 8u;
+      mbar_expect_tx(b, 4096u);
+      tma_load3(opw + slot_ * 4096u, &tma_o.r, n0_ + hh * HC + 32 * j_, m0_ + q4 * 32, z_, b);
+    };
+    if (RTV && p.rst && lane == 0 && wid < total) rt_issue(wid, 0, 0u);
     // LayerNorm epilogue with TMA (LNV && p.lnst): the warp's 32 x HC residual block arrives by TMA into its
     // boxes, R = acc + bias + resid overwrites it in place and leaves by TMA store, then Y overwrites R (once the R
     // stores have read it) and leaves the same way; the next tile's residual is requested as soon as the Y stores
@@ -1201,6 +1217,57 @@ __global__ void __launch_bounds__(320, 1)
               tma_store3(&tma_o.a, xb, col, rbase, z);
               if (FIRST) tma_store3(&tma_o.c, opw + 12288u, col, rbase, z);
               else tma_reduce_add3(&tma_o.c, opw + 12288u, col, rbase, z);
+              bulk_commit();
+            }
+          }
+          continue;
+        }
+      }
+      if constexpr (RTV) {
+        if (p.rst) {
+          const int rbase = m0 + q4 * 32;
+          const float alpha = e.alpha;
+          mbar_wait(smem_u32(tfull + ab), aph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+          for (int j = 0; j < HC / 32; ++j, ++gpass) {
+            const uint32_t slot = gpass & 1u, oph = (gpass >> 1) & 1u;
+            if (lane == 0) {   // the previous pass's store has read the other slot: refill it
+              bulk_wait_read<0>();
+              if (j + 1 < HC / 32) rt_issue(item, j + 1, slot ^ 1u);
+              else if (item + nwk < total) rt_issue(item + nwk, 0, slot ^ 1u);
+            }
+            __syncwarp();
+            uint32_t v[32];
+            ld_tmem32(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * BN + hh * HC + 32 * j), v);
+            mbar_wait(obar + slot * 8u, oph);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (j + 1 == HC / 32) {   // accumulator fully read: hand it back to the MMA warp
+              asm volatile("tcgen05.fence::before_thread_sync;");
+              __syncwarp();
+              if (lane == 0) tempty_arrive(smem_u32(tempty + ab), pair);
+            }
+            const uint32_t sl = opw + slot * 4096u;
+            const uint32_t rrow = sl + (uint32_t)(lane * 128), swr = (uint32_t)(lane & 7);
+            float a[32];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {   // 16-B granule c of the 128-B fp32 row (128-B swizzle: c ^ (row & 7))
+              const float4 r4 = lds4(rrow + ((((uint32_t)c) ^ swr) << 4));
+              a[4 * c] = __uint_as_float(v[4 * c]) * alpha + 0.f + r4.x;
+              a[4 * c + 1] = __uint_as_float(v[4 * c + 1]) * alpha + 0.f + r4.y;
+              a[4 * c + 2] = __uint_as_float(v[4 * c + 2]) * alpha + 0.f + r4.z;
+              a[4 * c + 3] = __uint_as_float(v[4 * c + 3]) * alpha + 0.f + r4.w;
+            }
+            __syncwarp();   // every lane has read its residual row before the bf16 rows overwrite the slot
+            const uint32_t orow = sl + (uint32_t)(lane * 64), swo = (uint32_t)((lane >> 1) & 3);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)   // 16-B granule c of the 64-B bf16 row (64-B swizzle: c ^ ((row >> 1) & 3))
+              sts4u(orow + ((((uint32_t)c) ^ swo) << 4), pack_bf2(a[8 * c], a[8 * c + 1]), pack_bf2(a[8 * c + 2], a[8 * c + 3]),
+                    pack_bf2(a[8 * c + 4], a[8 * c + 5]), pack_bf2(a[8 * c + 6], a[8 * c + 7]));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store3(&tma_o.c, sl, n0 + hh * HC + 32 * j, rbase, z);
               bulk_commit();
             }
           }
@@ -1879,7 +1946,7 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   }
-  if ((p.tstore || p.lnst || p.dcnt || p.crosst) && warp >= 2 && lane == 0) bulk_wait_all();   // TMA stores done reading smem and written
+  if ((p.tstore || p.lnst || p.dcnt || p.crosst || p.rst) && warp >= 2 && lane == 0) bulk_wait_all();   // TMA stores done reading smem and written
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if constexpr (BSV) {   // this CTA's partial row of the dA column sums: warps summed in a fixed order

@@ -1760,7 +1760,7 @@ void dhen_tuning_default(dhen_tuning* t) { if (t) *t = tuning_default(); }
 dhen_status dhen_set_tuning(dhen_ctx* c, const dhen_tuning* t) {
   if (!c || !t) return fail(DHEN_E_STATE, "dhen_set_tuning: ctx or tuning is NULL");
   const int bits[] = {t->overlap, t->defer_join, t->ln_fuse, t->first_writer, t->relu_bits, t->fuse_db, t->vdy,
-                      t->trail, t->bd_pre, t->tstore, t->attn_fused, t->pdl, t->gemm_simt, t->dcn_fused, t->dcn_tma, t->ln_tma, t->wres};
+                      t->trail, t->bd_pre, t->tstore, t->attn_fused, t->pdl, t->gemm_simt, t->dcn_fused, t->dcn_tma, t->ln_tma, t->wres, t->resid_tma};
   for (int b : bits)
     if (b != 0 && b != 1) return fail(DHEN_E_CONFIG, "dhen_set_tuning: a 0/1 switch is %d", b);
   if (t->bn_max != 64 && t->bn_max != 128 && t->bn_max != 256)

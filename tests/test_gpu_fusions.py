@@ -20,6 +20,7 @@ dcn_tma       DCN-backward epilogue: X / A / dR by TMA, dA / dX by TMA store   -
 dcn_fused     DCN backward as one kernel vs dT GEMM + dA W GEMM               -> bitwise (db grouping)
 l2_prefetch   short-K GEMM operands prefetched into L2 items ahead (off)      -> bitwise identical
 wres          short-K GEMMs with the weight tile resident in shared memory    -> bitwise identical
+resid_tma     fp32-residual epilogue: dR by TMA boxes, C by TMA store         -> bitwise identical
 """
 import numpy as np
 import pytest
@@ -126,7 +127,7 @@ def test_dense_symmetrisation_bitwise(name, B, layers, mode):
     _cmp(a, b, net, 0)
 
 
-@pytest.mark.parametrize("switch", ["defer_join", "trail", "bd_pre", "tstore", "ln_tma", "wres"])
+@pytest.mark.parametrize("switch", ["defer_join", "trail", "bd_pre", "tstore", "ln_tma", "wres", "resid_tma"])
 @pytest.mark.parametrize("name,B,layers", [("C2", 64, 2), ("C4", 16, 2), ("C3", 32, 2)])
 def test_schedule_switches_bitwise(name, B, layers, switch):
     """Schedule-only switches (same kernels' arithmetic in another order of launch / store path): the
