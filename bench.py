@@ -14,9 +14,10 @@ itself through torch.distributed.run with N local ranks.
 value:   device time (CUDA events on the launch stream) of K steps, inputs
          resident in HBM, L2 flushed (256 MiB write) before every timed step,
          max over ranks;  samples/s = N * B_local * K / time.
-e2e:     the same through the public API with pinned HOST buffers: every step
-         copies X0 + labels host->device and the loss device->host inside the
-         timed region.
+e2e:     the same through the C ABI's host-buffer entry (dhen_train_step_host)
+         with pinned HOST buffers: every step copies X0 + labels host->device
+         and the loss device->host inside the timed region (--fp: torch copies
+         of ids / offsets / dense features around the device-pointer calls).
 roofline: the op with the largest device time in a separate profiled pass of K
          steps (per-op CUDA events from dhen_profile), algorithmic FLOPs or bytes
          per launch / its mean launch time, against MEASURED_PEAKS.json.
@@ -379,24 +380,39 @@ def main():
                 stage_o[s].copy_(hoffs[s], non_blocking=True)
             up_done[s].record(cp)
 
-    e0.record(st)
-    cp.wait_event(e0)
-    upload(0)
-    for k in range(args.steps):
-        s = k % 2
-        if k + 1 < args.steps:
-            upload(k + 1)
-        st.wait_event(up_done[s])
-        dx.copy_(stage_x[s], non_blocking=True)
-        dy.copy_(stage_y[s], non_blocking=True)
-        if fp is not None:
+    if fp is None:
+        # the C ABI's host-buffer entry (dhen_train_step_host): the library uploads each step's pinned host
+        # inputs on its own copy stream (two staging slots: step k+1's upload overlaps step k), moves them into
+        # the step's input buffers, replays the step graph and copies the loss to a pinned host scalar
+        hls = [torch.zeros(1).pin_memory() for _ in range(2)]
+        for k in range(2):   # first calls: device buffers and the step graph on them, outside the timed region
+            model.train_step_host(hx[k], hy[k], lr, B_global=Bg, loss_host=hls[k], sync=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for k in range(args.steps):
+            model.train_step_host(hx[k % 2], hy[k % 2], lr, B_global=Bg, loss_host=hls[k % 2], sync=False)
+        e1.record(st)
+        torch.cuda.synchronize()
+    else:
+        e0.record(st)
+        cp.wait_event(e0)
+        upload(0)
+        for k in range(args.steps):
+            s = k % 2
+            if k + 1 < args.steps:
+                upload(k + 1)
+            st.wait_event(up_done[s])
+            dx.copy_(stage_x[s], non_blocking=True)
+            dy.copy_(stage_y[s], non_blocking=True)
             di.copy_(stage_i[s], non_blocking=True)
             do.copy_(stage_o[s], non_blocking=True)
-        used[s].record(st)
-        e2e_step()
-        hl.copy_(loss, non_blocking=True)
-    e1.record(st)
-    torch.cuda.synchronize()
+            used[s].record(st)
+            e2e_step()
+            hl.copy_(loss, non_blocking=True)
+        e1.record(st)
+        torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
     if world > 1:
@@ -406,7 +422,8 @@ def main():
            "h2d_bytes_per_step": int(hx[0].numel() * hx[0].element_size() + hy[0].numel() * 4 +
                                      (hids[0].numel() * 4 + hoffs[0].numel() * 4 if fp is not None else 0)),
            "d2h_bytes_per_step": 4,
-           "pipeline": "pinned H2D of step k+1 on a copy stream overlaps step k; D2D into the step buffers; loss D2H"}
+           "pipeline": ("C ABI dhen_train_step_host: " if fp is None else "torch copies around the device-pointer calls: ") +
+                       "pinned H2D of step k+1 on a copy stream overlaps step k; D2D into the step buffers; loss D2H"}
 
     # ---------------- feature processing: device time of its forward and backward + SGD alone (CUDA events)
     fp_info = None

@@ -189,6 +189,17 @@ dhen_status dhen_train_step(dhen_ctx* ctx, const void* x0, const float* labels, 
 dhen_status dhen_train_step_graphed(dhen_ctx* ctx, const void* x0, const float* labels, int B, int B_global,
                                     float lr, float* loss_dev, void* dx0, void* stream);
 
+/* One training step from HOST buffers (the end-to-end path a data loader drives): x0_host [B][m0][d] (dtype) and
+ * labels_host [B] fp32 (page-locked memory, e.g. cudaHostAlloc, for asynchronous copies) are copied host -> device
+ * on the context's copy stream into one of two staging slots (call k uses slot k % 2; its upload waits only for
+ * call k - 2's step to have consumed that slot, so an upload overlaps the previous step), moved into the step's
+ * input buffers on `stream`, the step runs (dhen_train_step_graphed semantics), and this rank's loss is copied
+ * device -> host into *loss_host.  sync = 1: `stream` is synchronised before returning (*loss_host valid); sync = 0:
+ * *loss_host becomes valid, and x0_host / labels_host may be reused, once `stream` has been synchronised.
+ * Device buffers are allocated on the first call (2 x B_max staging + inputs). */
+dhen_status dhen_train_step_host(dhen_ctx* ctx, const void* x0_host, const float* labels_host, int B, int B_global,
+                                 float lr, float* loss_host, int sync, void* stream);
+
 /* Forward of the whole stack + head without backward: logits_dev [B] fp32. */
 dhen_status dhen_forward(dhen_ctx* ctx, const void* x0, int B, float* logits_dev, void* stream);
 

@@ -24,7 +24,7 @@ STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_SHAPE", 3: "E_ALIGN", 4: "E_STATE", 5: "
 # every symbol include/dhen.h and include/dhen_debug.h declare
 EXPORTS = ("dhen_validate", "dhen_sizes", "dhen_group_numel", "dhen_nccl_id", "dhen_loopback_id", "dhen_comm_bytes",
            "dhen_init", "dhen_layer_fwd",
-           "dhen_layer_bwd", "dhen_train_step", "dhen_train_step_graphed", "dhen_forward", "dhen_zero_grad", "dhen_params_io",
+           "dhen_layer_bwd", "dhen_train_step", "dhen_train_step_graphed", "dhen_train_step_host", "dhen_forward", "dhen_zero_grad", "dhen_params_io",
            "dhen_grads_get", "dhen_launch_count", "dhen_last_error", "dhen_destroy", "dhen_profile",
            "dhen_profile_read", "dhen_debug_gemm", "dhen_debug_gemm_epi", "dhen_debug_last_gemm_tc",
            "dhen_debug_gemm_trace", "dhen_tuning_default", "dhen_set_tuning", "dhen_get_tuning",
@@ -110,6 +110,7 @@ def load(path: str = LIB_PATH):
         "dhen_layer_bwd": [vp, i, vp, vp, i, vp],
         "dhen_train_step": [vp, vp, vp, i, i, C.c_float, vp, vp, vp],
         "dhen_train_step_graphed": [vp, vp, vp, i, i, C.c_float, vp, vp, vp],
+        "dhen_train_step_host": [vp, vp, vp, i, i, C.c_float, vp, i, vp],
         "dhen_forward": [vp, vp, i, vp, vp],
         "dhen_zero_grad": [vp, vp],
         "dhen_params_io": [vp, i, vp, i, vp],
@@ -446,6 +447,14 @@ class DHEN:
         _check("dhen_train_step_graphed", self.lib.dhen_train_step_graphed(
             self.ctx, _ptr(x0), _ptr(labels), B, B_global or B, float(lr), _ptr(loss), _ptr(dx0),
             self._stream(stream)))
+
+    def train_step_host(self, x0_host, labels_host, lr, B_global=None, loss_host=None, sync=True, stream=None):
+        """One step from (pinned) host tensors through the C ABI's host-buffer entry: the library uploads them,
+        runs the step and writes this rank's loss into loss_host (a 1-element host fp32 tensor)."""
+        B = x0_host.shape[0]
+        _check("dhen_train_step_host", self.lib.dhen_train_step_host(
+            self.ctx, _ptr(x0_host), _ptr(labels_host), B, B_global or B, float(lr), _ptr(loss_host),
+            1 if sync else 0, self._stream(stream)))
 
     def forward(self, x0, logits, stream=None):
         _check("dhen_forward", self.lib.dhen_forward(self.ctx, _ptr(x0), x0.shape[0], _ptr(logits),

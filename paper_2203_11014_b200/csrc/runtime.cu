@@ -197,6 +197,15 @@ struct dhen_ctx {
   int gkey_B = 0, gkey_Bg = 0;
   float gkey_lr = 0.f;
   unsigned long long graph_launches = 0;   // kernels inside the captured step
+  // dhen_train_step_host: two host->device staging slots (copy stream), the step's input buffers, the loss
+  void* hx[2] = {nullptr, nullptr};
+  float* hy[2] = {nullptr, nullptr};
+  void* hxin = nullptr;
+  float* hyin = nullptr;
+  float* hloss = nullptr;
+  cudaStream_t hcp = nullptr;
+  cudaEvent_t hev_up[2] = {nullptr, nullptr}, hev_free[2] = {nullptr, nullptr};
+  unsigned long long hcalls = 0;
   cudaStream_t comm_st = nullptr;     // collectives (world > 1)
   cudaEvent_t ev_ag[2] = {nullptr, nullptr}, ev_use[2] = {nullptr, nullptr}, ev_grad = nullptr, ev_comm = nullptr;
   cudaEvent_t ev_grad2 = nullptr, ev_cfork = nullptr;
@@ -1659,6 +1668,16 @@ void dhen_destroy(dhen_ctx* c) {
   if (c->ev_cfork) cudaEventDestroy(c->ev_cfork);
   for (int k = 0; k < 2; ++k) if (c->ev_rs[k]) cudaEventDestroy(c->ev_rs[k]);
   if (c->comm_st) cudaStreamDestroy(c->comm_st);
+  for (int k = 0; k < 2; ++k) {
+    if (c->hx[k]) cudaFree(c->hx[k]);
+    if (c->hy[k]) cudaFree(c->hy[k]);
+    if (c->hev_up[k]) cudaEventDestroy(c->hev_up[k]);
+    if (c->hev_free[k]) cudaEventDestroy(c->hev_free[k]);
+  }
+  if (c->hxin) cudaFree(c->hxin);
+  if (c->hyin) cudaFree(c->hyin);
+  if (c->hloss) cudaFree(c->hloss);
+  if (c->hcp) cudaStreamDestroy(c->hcp);
   delete c->comm;
   delete c;
 }
@@ -1978,6 +1997,46 @@ static dhen_status gather_f32(dhen_ctx* c, Group& g, const float* shard_or_full,
     CK(cudaMemcpyAsync(pad.data(), shard_or_full, (size_t)g.n * 4, cudaMemcpyDeviceToHost, st));
   }
   CK(cudaStreamSynchronize(st));
+  return DHEN_OK;
+}
+
+dhen_status dhen_train_step_host(dhen_ctx* c, const void* x0_host, const float* labels_host, int B, int Bg, float lr,
+                                 float* loss_host, int sync, void* stream) {
+  if (!c) return fail(DHEN_E_STATE, "dhen_train_step_host: ctx is NULL");
+  if (!x0_host || !labels_host || !loss_host)
+    return fail(DHEN_E_ALIGN, "dhen_train_step_host: x0_host=%p labels_host=%p loss_host=%p", x0_host,
+                (const void*)labels_host, (void*)loss_host);
+  if (B < 1 || B > c->Bmax) return fail(DHEN_E_SHAPE, "dhen_train_step_host: B=%d not in [1, %d]", B, c->Bmax);
+  cudaStream_t st = S(stream);
+  const size_t xrow = (size_t)c->cfg.m0 * c->d * (c->dt == BF16 ? 2 : 4);
+  if (!c->hxin) {   // first call: staging slots, input buffers, copy stream, slot events (slots start free)
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaMalloc(&c->hx[k], xrow * c->Bmax));
+      CK(cudaMalloc((void**)&c->hy[k], sizeof(float) * c->Bmax));
+      CK(cudaEventCreateWithFlags(&c->hev_up[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->hev_free[k], cudaEventDisableTiming));
+      CK(cudaEventRecord(c->hev_free[k], st));
+    }
+    CK(cudaMalloc(&c->hxin, xrow * c->Bmax));
+    CK(cudaMalloc((void**)&c->hyin, sizeof(float) * c->Bmax));
+    CK(cudaMalloc((void**)&c->hloss, sizeof(float)));
+    CK(cudaStreamCreateWithFlags(&c->hcp, cudaStreamNonBlocking));
+  }
+  const int s = (int)(c->hcalls & 1);
+  // upload into slot s once the step that last moved it out is done with it
+  CK(cudaStreamWaitEvent(c->hcp, c->hev_free[s], 0));
+  CK(cudaMemcpyAsync(c->hx[s], x0_host, xrow * B, cudaMemcpyHostToDevice, c->hcp));
+  CK(cudaMemcpyAsync(c->hy[s], labels_host, sizeof(float) * B, cudaMemcpyHostToDevice, c->hcp));
+  CK(cudaEventRecord(c->hev_up[s], c->hcp));
+  // into the step's (fixed) input buffers, so the captured step graph is replayed, not re-captured
+  CK(cudaStreamWaitEvent(st, c->hev_up[s], 0));
+  CK(cudaMemcpyAsync(c->hxin, c->hx[s], xrow * B, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(c->hyin, c->hy[s], sizeof(float) * B, cudaMemcpyDeviceToDevice, st));
+  CK(cudaEventRecord(c->hev_free[s], st));
+  ++c->hcalls;
+  RET(dhen_train_step_graphed(c, c->hxin, c->hyin, B, Bg, lr, c->hloss, nullptr, stream));
+  CK(cudaMemcpyAsync(loss_host, c->hloss, sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (sync) CK(cudaStreamSynchronize(st));
   return DHEN_OK;
 }
 

@@ -269,6 +269,41 @@ def test_graphed_step_matches_eager_bitwise():
         assert np.array_equal(a, b)
 
 
+def test_host_buffer_step_matches_device_step_bitwise():
+    """dhen_train_step_host (pinned host inputs uploaded by the library on its copy stream, two staging slots,
+    loss copied back to the host) == dhen_train_step on the same inputs, bit for bit, over 4 steps whose
+    inputs alternate between two host batches -- with sync = 0 for the middle steps, so an upload overlaps the
+    previous step."""
+    import torch
+    net = small("C4")
+    B = 13
+    outs = []
+    for host in (False, True):
+        case = Case(net, B, "bf16", seed=98)
+        other = Case(net, B, "bf16", seed=97)   # a second batch (its model is not used)
+        xs = [case.x0, other.x0]
+        ys = [case.labels, other.labels]
+        loss = torch.zeros(1, device="cuda")
+        hx = [x.cpu().pin_memory() for x in xs]
+        hy = [y.cpu().pin_memory() for y in ys]
+        hl = [torch.zeros(1).pin_memory() for _ in range(4)]
+        losses = []
+        for k in range(4):
+            if host:
+                case.model.train_step_host(hx[k % 2], hy[k % 2], 0.05, loss_host=hl[k], sync=(k in (0, 3)))
+            else:
+                case.model.train_step(xs[k % 2], ys[k % 2], 0.05, loss=loss)
+                torch.cuda.synchronize()
+                losses.append(loss.item())
+        torch.cuda.synchronize()
+        if host:
+            losses = [float(h.item()) for h in hl]
+        outs.append((losses, [case.model.get_params(g) for g in range(len(case.flats))]))
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("mods,m,d,B", [
     ([("dot", 128)], 128, 128, 6),                     # Dot alone: first AND last dX writer (dR in, bf16 dX out)
     ([("dot", 64), ("conv", 64)], 128, 128, 6),        # Dot first writer (dR in, fp32 accumulator out)
