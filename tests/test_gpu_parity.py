@@ -130,6 +130,28 @@ def test_bf16_layer_local(kind):
     assert not bad, (bad, errs)
 
 
+@pytest.mark.parametrize("dtype,m,d,k,path", [
+    ("bf16", 16, 64, 3, "double-buffered whole-sample stencil (conv_db_k)"),
+    ("bf16", 16, 24, 3, "whole-sample stencil (conv_sample_k, bf16: 2048 % d != 0)"),
+    ("fp32", 16, 64, 3, "whole-sample stencil (conv_sample_k, fp32)"),
+    ("bf16", 16, 64, 5, "row bands (conv_band_k / conv_wgrad_band_k, k = 5)"),
+    ("fp32", 12, 24, 5, "row bands, fp32 (k = 5)"),
+    ("fp32", 10, 16, 7, "generic per-element kernels (k = 7)"),
+    ("bf16", 9, 16, 7, "generic per-element kernels, bf16 (k = 7)"),
+])
+def test_conv_kernel_family_matches_oracle(dtype, m, d, k, path):
+    """Every conv kernel generation the dispatcher can pick (F7 / B7, Eq.(5)) against the oracle on one train step of
+    a conv-only layer (+ a linear module so the conv is not the only dX writer): G1 fp32 1e-5, G3 bf16 2e-2."""
+    net = O.NetSpec(m, d, [O.LayerSpec([M("conv", m // 2, conv_k=k, conv_channels=3), M("linear", m - m // 2)])])
+    B = 11
+    case = Case(net, B, dtype, seed=4242 + k)
+    lr = 0.1 if dtype == "fp32" else 0.05
+    g = case.gpu_step(lr)
+    o = case.oracle_step(lr)
+    tol = 1e-5 if dtype == "fp32" else 2e-2
+    _compare(case, g, o, tol, tol, label=f"conv {dtype} m={m} d={d} k={k}: {path}")
+
+
 def test_layer_bwd_accumulates_and_is_deterministic():
     """backward twice == 2 x backward once; bitwise repeatable."""
     import torch
