@@ -72,8 +72,9 @@ typedef struct {
                         more tiles (wave quantization of short grids)                                 (256) */
   int l2_prefetch;   /* short-K GEMMs (K <= 512): the TMA producer prefetches the operand tiles of the CTA's
                         item this many items ahead into L2 (cp.async.bulk.prefetch.tensor); 0 off, <= 4 */
-  int wres;          /* 1: short-K TMA-store GEMMs (K <= 256, BN = 256, bf16 C) keep the CTA's weight tile resident
-                        in shared memory and stream only A (a third of the L2 reads)                    (1) */
+  int wres;          /* short-K TMA-store GEMMs (K <= 256, BN = 256, bf16 C) keep the weight tile resident in shared
+                        memory and stream only A (a third of the L2 reads): 1 one CTA a tile, 2 CTA pairs (each
+                        CTA half the tile, an A ring twice as deep), 0 off                              (1) */
   int resid_tma;     /* 1: the fp32-residual GEMM epilogue (token-map dgrad first writer) takes dR through TMA
                         boxes and stores C by TMA; 0: register prefetch and staged stores               (1) */
 } dhen_tuning;

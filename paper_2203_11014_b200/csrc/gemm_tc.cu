@@ -346,6 +346,22 @@ cudaError_t gemm_tc(const Gemm& g, const Workspace& ws, cudaStream_t st) {
   const int fl_ = p.ep.flags;
   p.wr = (tune().wres && p.tstore && var > 0 && BN == 256 && !p.pair && splits == 1 && g.batch == 1 && p.kblocks <= 4 &&
           p.n_fast && (fl_ & ~TS_FLAGS) == 0 && !(fl_ & EF_ACC) && g.c.dt == BF16) ? 1 : 0;
+  if (p.wr && tune().wres == 2 && g.M >= 4 * BM) {
+    // the CTA-pair form: each CTA keeps half of the B tile, so the A ring is twice as deep (256-row pair tiles)
+    Params q = p;
+    q.pair = 1;
+    if (make_map(&mb, &q.b, g.b, g.N, g.K, g.batch, BN / 2)) {
+      p = q;
+      p.tiles_m = (g.M + 2 * BM - 1) / (2 * BM);
+      p.n_fast = (p.tiles_n <= 16 && p.tiles_m >= p.tiles_n) ? 1 : 0;
+      if (!p.n_fast) p.wr = 0;
+      p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.a.mn_major << 15) | ((uint32_t)p.b.mn_major << 16) |
+                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
+      g_last_gemm_pair = 1;
+    } else {
+      (void)make_map(&mb, &p.b, g.b, g.N, g.K, g.batch, BN);
+    }
+  }
   if (g.e.ln_gamma && (!p.lean || var != p.lean_id || (p.ep.flags & EF_LN) == 0 || p.lanes_rows)) return cudaErrorNotSupported;
   if (g.e.bits_mode && !p.tstore) return cudaErrorNotSupported;   // bitmask epilogues exist on the TMA-store path
   // column sums of the stored C exist on the bf16 TMA-store path only (rows = M / 32 blocks per batch item)

@@ -848,12 +848,15 @@ template <int VAR> constexpr bool has_opbar() {
 // 192 KB through L2 (these GEMMs sit at the L2 throughput cap).  TMA-store epilogues only, with one
 // store box per warp (the resident tile takes the second box's shared memory), and the bias row of the CTA's one N
 // tile staged once.
-constexpr int WR_NA = 4, WR_KB = 4;   // A-ring slots; resident B k-blocks (K <= 4 BK = 256)
+constexpr int WR_KB = 4;   // resident B k-blocks (K <= 4 BK = 256)
+// A-ring slots: single CTA 4; a CTA pair holds half the B tile each, so 8 (128 KB of A in flight a CTA)
+template <bool PAIR> constexpr int wr_na() { return PAIR ? 8 : 4; }
 template <int BN, int VAR> constexpr bool wr_ok() {
   return BN == 256 && VAR > 0 && (VarF<VAR>::F & ~TS_FLAGS) == 0 && !VarF<VAR>::C && (VarF<VAR>::F & EF_ACC) == 0;
 }
-template <int BN> constexpr int wr_smem() {
-  return WR_NA * BM * BK * 2 + WR_KB * BN * BK * 2 + 8 * 4096 + BN * 4 + (2 * WR_NA + 6) * 8 + 16 + 1024;   // bias: 1 tile
+template <int BN, bool PAIR> constexpr int wr_smem() {
+  return wr_na<PAIR>() * BM * BK * 2 + WR_KB * (PAIR ? BN * BK : BN * BK * 2) + 8 * 4096 + BN * 4 +
+         (2 * wr_na<PAIR>() + 6) * 8 + 16 + 1024;   // bias: 1 tile
 }
 
 template <int BN, int STAGES, bool PAIR>
@@ -870,8 +873,8 @@ __global__ void __launch_bounds__(320, 1)
   // B bytes per ring slot in this CTA (a pair CTA loads BN / 2 rows), and the ring depth the same shared
   // memory holds: a pair kernel gets the deeper ring (BN = 256: 4 slots instead of 3)
   constexpr int B_BYTES = PAIR ? BN * BK : BN * BK * 2;
-  constexpr int NST = WR ? WR_NA : ring_stages<BN, STAGES, PAIR>();
-  static_assert(!WR || (!PAIR && wr_ok<BN, VAR>()), "W-resident: single-CTA TMA-store variants");
+  constexpr int NST = WR ? wr_na<PAIR>() : ring_stages<BN, STAGES, PAIR>();
+  static_assert(!WR || wr_ok<BN, VAR>(), "W-resident: TMA-store variants");
   constexpr int SC = EpiSmem<BN>::SC;
   constexpr int SROW = EpiSmem<BN>::SROW;
   extern __shared__ uint8_t smem_raw[];
@@ -973,12 +976,18 @@ __global__ void __launch_bounds__(320, 1)
         if (wid < total) {
           int m0, n0, z, sp, kb0, nk;
           decode(wid, m0, n0, z, sp, kb0, nk);
-          const OpCoords qb = op_coords(p.b, n0, z);
+          const OpCoords qb = op_coords(p.b, n0 + (int)crank * (BN / 2), z);   // (a pair CTA: its half of B)
           int kbk = p.b.has_ko ? (kb0 * BK) % p.b.kdiv : kb0 * BK, kob = p.b.has_ko ? (kb0 * BK) / p.b.kdiv : 0;
           const int kdb = p.b.has_ko ? p.b.kdiv : 0x7fffffff;
-          mbar_expect_tx(smem_u32(wfull), (uint32_t)(nk * B_BYTES));
+          uint32_t wb = smem_u32(wfull);
+          if (!pair) {
+            mbar_expect_tx(wb, (uint32_t)(nk * B_BYTES));
+          } else {   // both CTAs' halves land on rank 0's barrier
+            if (crank == 0) mbar_expect_tx(wb, (uint32_t)(2 * nk * B_BYTES));
+            wb = mapa_u32(wb, 0);
+          }
           for (int i = 0; i < nk; ++i) {
-            load_tile(&tma_b, p.b.mn_major != 0, qb, kbk, kob, smem_u32(sB) + i * B_BYTES, smem_u32(wfull), BN / 64, false);
+            load_tile(&tma_b, p.b.mn_major != 0, qb, kbk, kob, smem_u32(sB) + i * B_BYTES, wb, pair ? BN / 128 : BN / 64, pair);
             kbk += BK; while (kbk >= kdb) { kbk -= kdb; ++kob; }
           }
         }
@@ -1003,8 +1012,11 @@ __global__ void __launch_bounds__(320, 1)
           mbar_wait(smem_u32(empty + s), ph ^ 1);
           if (p.trace && blockIdx.x == 0 && it < 64) p.trace[it] = clock64();
           uint32_t fb = smem_u32(full + s);
-          if (WR) {
+          if (WR && !pair) {
             mbar_expect_tx(fb, A_BYTES);
+          } else if (WR) {
+            if (crank == 0) mbar_expect_tx(fb, 2 * A_BYTES);
+            fb = mapa_u32(fb, 0);
           } else if (!pair) {
             mbar_expect_tx(fb, A_BYTES + B_BYTES);
           } else {
@@ -1991,12 +2003,39 @@ static cudaError_t launch(const Params& p0, const CUtensorMap& ma, const CUtenso
   }
   const int ntiles = p0.tiles_m * p0.tiles_n;
   if constexpr (wr_ok<BN, VAR>()) if (p0.wr) {   // W-resident (host: batch 1, one split, N tiles fastest, K <= 256)
-    constexpr int SMEM_W = wr_smem<BN>();
-    static_assert(SMEM_W <= 227 * 1024, "smem");
+    constexpr int SMEM_W = wr_smem<BN, false>(), SMEM_WP = wr_smem<BN, true>();
+    static_assert(SMEM_W <= 227 * 1024 && SMEM_WP <= 227 * 1024, "smem");
     static bool wattr = false;
     if (!wattr) {
       cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, VAR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_W);
+      cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, VAR, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_WP);
       wattr = true;
+    }
+    if (p0.pair) {   // CTA pairs: a multiple of tiles_n clusters, so every cluster keeps one N tile
+      static int max_cl = 0;
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.blockDim = dim3(320); cfg.dynamicSmemBytes = SMEM_WP; cfg.stream = st; cfg.attrs = at;
+      cfg.numAttrs = pdl_enabled() ? 2 : 1;
+      if (!max_cl) {
+        cfg.gridDim = dim3(148);
+        if (cudaOccupancyMaxActiveClusters(&max_cl, gemm_tc_kernel<BN, STAGES, VAR, true, true>, &cfg) != cudaSuccess ||
+            max_cl <= 0) {
+          (void)cudaGetLastError();
+          max_cl = 64;
+        }
+      }
+      const int cl = (int)std::min<int64_t>(ntiles, std::max(1, max_cl / p0.tiles_n) * p0.tiles_n);
+      cfg.gridDim = dim3((unsigned)(2 * cl));
+      g_last_gemm_grid = (int)cfg.gridDim.x;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, VAR, true, true>, ma, mb, mc, p0);
+      if (e != cudaSuccess) return e;
+      ++g_launches;
+      return cudaGetLastError();
     }
     // a multiple of tiles_n CTAs: with N tiles fastest, CTA c only ever sees N tile c % tiles_n
     const int grid = (int)std::min<int64_t>(ntiles, (148 / p0.tiles_n) * p0.tiles_n);

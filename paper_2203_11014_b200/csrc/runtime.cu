@@ -1779,11 +1779,12 @@ void dhen_tuning_default(dhen_tuning* t) { if (t) *t = tuning_default(); }
 dhen_status dhen_set_tuning(dhen_ctx* c, const dhen_tuning* t) {
   if (!c || !t) return fail(DHEN_E_STATE, "dhen_set_tuning: ctx or tuning is NULL");
   const int bits[] = {t->overlap, t->defer_join, t->ln_fuse, t->first_writer, t->relu_bits, t->fuse_db, t->vdy,
-                      t->trail, t->bd_pre, t->tstore, t->attn_fused, t->pdl, t->gemm_simt, t->dcn_fused, t->dcn_tma, t->ln_tma, t->wres, t->resid_tma};
+                      t->trail, t->bd_pre, t->tstore, t->attn_fused, t->pdl, t->gemm_simt, t->dcn_fused, t->dcn_tma, t->ln_tma, t->resid_tma};
   for (int b : bits)
     if (b != 0 && b != 1) return fail(DHEN_E_CONFIG, "dhen_set_tuning: a 0/1 switch is %d", b);
   if (t->bn_max != 64 && t->bn_max != 128 && t->bn_max != 256)
     return fail(DHEN_E_CONFIG, "dhen_set_tuning: bn_max=%d (64, 128 or 256)", t->bn_max);
+  if (t->wres < 0 || t->wres > 2) return fail(DHEN_E_CONFIG, "dhen_set_tuning: wres=%d (0, 1 or 2)", t->wres);
   if (t->l2_prefetch < 0 || t->l2_prefetch > 4)
     return fail(DHEN_E_CONFIG, "dhen_set_tuning: l2_prefetch=%d (0..4)", t->l2_prefetch);
   if (t->sym < -1 || t->sym > 2 || t->pair < -1 || t->pair > 1 || t->pair_k < 0)

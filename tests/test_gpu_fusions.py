@@ -140,13 +140,14 @@ def test_schedule_switches_bitwise(name, B, layers, switch):
     _cmp(a, b, net, 1e-3 if switch == "tstore" else 0)
 
 
+@pytest.mark.parametrize("wres", [1, 2])
 @pytest.mark.parametrize("name,B,layers", [("C4", 256, 1), ("C3", 512, 1)])
-def test_wres_many_items_bitwise(name, B, layers):
-    """W-resident GEMMs over many items a CTA (FFN1 / FFN2 dgrad / QKV at C4, the MLP GEMMs at C3): bit-identical
-    to the streamed-B kernel."""
+def test_wres_many_items_bitwise(name, B, layers, wres):
+    """W-resident GEMMs over many items a CTA (FFN1 / FFN2 dgrad / QKV at C4, the MLP GEMMs at C3), one CTA or a
+    CTA pair a tile: bit-identical to the streamed-B kernel."""
     net = _net(name, layers)
     a = _step(net, B, 25, {"wres": 0})
-    b = _step(net, B, 25, {})
+    b = _step(net, B, 25, {"wres": wres})
     _cmp(a, b, net, 0)
 
 
