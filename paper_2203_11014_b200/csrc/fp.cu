@@ -84,11 +84,13 @@ template <> __device__ __forceinline__ float4 ld4<__nv_bfloat16>(const __nv_bflo
                      __uint_as_float(u.y & 0xffff0000u));
 }
 
-// Forward gather: warp = bag (b, shard j) of nb samples; lane owns columns 4 lane + 128 c of the shard; four rows
-// in flight, summed in list order; the pooled row -> out[b * pitch + shard.out ..].  Ids outside [0, R_t) are
-// skipped and counted in *bad (once per table: at its first column shard).
-template <typename OT>
-__global__ void __launch_bounds__(256) emb_fwd_k(const float* __restrict__ tab, const Shard* __restrict__ sh, int nsh,
+// Forward gather: warp = bag (b, shard j) of nb samples; lane owns columns 4 lane + 128 c (c < NC) of the shard;
+// four rows in flight, summed in list order; the pooled row -> out[b * pitch + shard.out ..].  Ids outside
+// [0, R_t) are skipped and counted in *bad (once per table: at its first column shard).  NC = 2 when every shard
+// is at most 256 columns wide (half the registers: 32 warps an SM in flight; C4 bench shape 3.83 -> 2.83 ms,
+// same-box A/B; 48 or 64 warps measured slower), else 4.
+template <typename OT, int NC>
+__global__ void __launch_bounds__(256, NC == 2 ? 4 : 1) emb_fwd_k(const float* __restrict__ tab, const Shard* __restrict__ sh, int nsh,
                                                  const int* __restrict__ ids, const int* __restrict__ off, int ntab, int nb,
                                                  OT* __restrict__ out, long long pitch, int* bad) {
   pdl_entry();
@@ -99,9 +101,9 @@ __global__ void __launch_bounds__(256) emb_fwd_k(const float* __restrict__ tab, 
   const int lo = off[b * ntab + s.jt], hi = off[b * ntab + s.jt + 1];
   const float* T = tab + s.base;
   const int w = s.width, nc = (w + 127) >> 7;
-  float4 acc[4];
+  float4 acc[NC];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c = 0; c < NC; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int e = lo; e < hi; e += 4) {
     long long r[4];
 #pragma unroll
@@ -112,11 +114,11 @@ __global__ void __launch_bounds__(256) emb_fwd_k(const float* __restrict__ tab, 
         r[u] = -1;
       }
     }
-    float4 v[4][4];
+    float4 v[4][NC];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < NC; ++c) {
         const int col = 128 * c + 4 * lane;
         v[u][c] = (r[u] >= 0 && c < nc && col < w) ? __ldg(reinterpret_cast<const float4*>(T + r[u] * w + col))
                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -124,13 +126,13 @@ __global__ void __launch_bounds__(256) emb_fwd_k(const float* __restrict__ tab, 
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < NC; ++c) {
         acc[c].x += v[u][c].x; acc[c].y += v[u][c].y; acc[c].z += v[u][c].z; acc[c].w += v[u][c].w;
       }
   }
   OT* dst = out + (long long)b * pitch + s.out;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < NC; ++c) {
     const int col = 128 * c + 4 * lane;
     if (c < nc && col < w) st4<OT>(dst + col, acc[c]);
   }
@@ -593,12 +595,20 @@ dhen_status dhen_fp_forward(dhen_fp* f, const int* ids, const int* offsets, long
     const unsigned grid = (unsigned)(((long long)nb * nl + 7) / 8);
     void* dst = f->world == 1 ? x0 : f->send;
     const long long pitch = f->world == 1 ? (long long)m0 * d : f->cmax;
-    if (bf)
-      FCK(pdl_launch(emb_fwd_k<__nv_bfloat16>, grid, 256, 0, st, f->tables, f->d_lsh, nl, ids, offsets, nt, nb,
+    int wmax = 0;
+    for (const Shard& sh_ : f->lsh) wmax = std::max(wmax, sh_.width);
+    if (bf && wmax <= 256)
+      FCK(pdl_launch(emb_fwd_k<__nv_bfloat16, 2>, grid, 256, 0, st, f->tables, f->d_lsh, nl, ids, offsets, nt, nb,
                      (__nv_bfloat16*)dst, pitch, f->bad));
+    else if (bf)
+      FCK(pdl_launch(emb_fwd_k<__nv_bfloat16, 4>, grid, 256, 0, st, f->tables, f->d_lsh, nl, ids, offsets, nt, nb,
+                     (__nv_bfloat16*)dst, pitch, f->bad));
+    else if (wmax <= 256)
+      FCK(pdl_launch(emb_fwd_k<float, 2>, grid, 256, 0, st, f->tables, f->d_lsh, nl, ids, offsets, nt, nb, (float*)dst,
+                     pitch, f->bad));
     else
-      FCK(pdl_launch(emb_fwd_k<float>, grid, 256, 0, st, f->tables, f->d_lsh, nl, ids, offsets, nt, nb, (float*)dst, pitch,
-                     f->bad));
+      FCK(pdl_launch(emb_fwd_k<float, 4>, grid, 256, 0, st, f->tables, f->d_lsh, nl, ids, offsets, nt, nb, (float*)dst,
+                     pitch, f->bad));
     ++g_launches;
   }
   if (f->world > 1 && f->ns) {
