@@ -764,7 +764,8 @@ static int resident_blocks(K kern, int threads, size_t smem) {
   return sms * per;
 }
 #ifndef LNB_UR
-#define LNB_UR 2   // rows per lane segment per iteration of the LayerNorm backward (loads in flight)
+#define LNB_UR 1   // rows per lane segment per iteration of the LayerNorm backward (loads in flight); 1 measured
+                   // best on the same box: C5 +3.8 %, C2 +1.3 %, C3 +1 %, C4 +0.9 % over 2 (fewer registers)
 #endif
 static int ln_bwd_grid(int lpr, int dydt) {
   static int cache[2][6] = {{0}};
