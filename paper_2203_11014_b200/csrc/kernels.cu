@@ -594,6 +594,10 @@ __global__ void __launch_bounds__(256) ln_fwd_r(const float* __restrict__ U, con
   }
 }
 
+#ifndef LNB_NB
+#define LNB_NB 4   // operand buffers of the LayerNorm backward: 3 iterations of loads in flight ahead of the one
+                   // computed (same box: C5 +2.6 %, C4 +0.7 % over 1 ahead; 128 registers keep 2 blocks an SM)
+#endif
 template <int LPR, int UR, typename TD>
 __global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const __nv_bfloat16* __restrict__ Rsave,
                                                 const float* __restrict__ mu, const float* __restrict__ rstd,
@@ -618,8 +622,9 @@ __global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const
   // one is computed (software pipelining: two iterations of loads in flight per warp)
   constexpr bool RAWP = true;   // bf16 dY: one 16-B word; fp32 dY: two (ry, ry2)
   constexpr bool F32DY = std::is_same<TD, float>::value;
-  uint4 ry[2][UR], rx[2][UR], ry2[2][F32DY ? UR : 1];
-  float rm[2][UR], rq[2][UR];
+  constexpr int NB = LNB_NB;   // iterations of loads in flight (ring of operand buffers)
+  uint4 ry[NB][UR], rx[NB][UR], ry2[NB][F32DY ? UR : 1];
+  float rm[NB][UR], rq[NB][UR];
   auto fetch = [&](int64_t r0_, int bsl) {
 #pragma unroll
     for (int u = 0; u < UR; ++u) {
@@ -654,7 +659,7 @@ __global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const
   };
   auto body = [&](int64_t r0, auto BSC) {
     constexpr int BS = decltype(BSC)::value;
-    if (r0 + 8 * RPI < rb1) fetch(r0 + 8 * RPI, BS ^ 1);   // next iteration's operands in flight
+    if (r0 + (NB - 1) * 8 * RPI < rb1) fetch(r0 + (NB - 1) * 8 * RPI, (BS + NB - 1) % NB);   // later iterations' operands in flight
     float dy[UR][8], x[UR][8], mr[UR], rr[UR];
 #pragma unroll
     for (int u = 0; u < UR; ++u) {
@@ -724,10 +729,14 @@ __global__ void __launch_bounds__(256) ln_bwd_r(const TD* __restrict__ dY, const
     }
     };
   const int64_t rs0 = rb0 + (int64_t)w * RPI;
-  if (rs0 < rb1) fetch(rs0, 0);
-  for (int64_t r0 = rs0; r0 < rb1; r0 += 16 * RPI) {   // two iterations per trip: buffer indices compile-time
+#pragma unroll
+  for (int k = 0; k < NB - 1; ++k)
+    if (rs0 + k * 8 * RPI < rb1) fetch(rs0 + k * 8 * RPI, k);
+  for (int64_t r0 = rs0; r0 < rb1; r0 += NB * 8 * RPI) {   // NB iterations per trip: buffer indices compile-time
     body(r0, std::integral_constant<int, 0>{});
     if (r0 + 8 * RPI < rb1) body(r0 + 8 * RPI, std::integral_constant<int, 1>{});
+    if constexpr (NB > 2) { if (r0 + 16 * RPI < rb1) body(r0 + 16 * RPI, std::integral_constant<int, 2 % NB>{}); }
+    if constexpr (NB > 3) { if (r0 + 24 * RPI < rb1) body(r0 + 24 * RPI, std::integral_constant<int, 3 % NB>{}); }
   }
   // dgamma / dbeta: lanes with equal columns (xor offsets >= LPR), then the 8 warps in order
 #pragma unroll
