@@ -1,4 +1,6 @@
-"""HBM bandwidth probes (CUDA events): write-only fill, read-only reduction, copy.  Usage: python tools/membw.py"""
+"""HBM bandwidth probes (CUDA events): write-only fill, read-only reduction, copy.  Usage: python tools/membw.py
+Note: torch's fill_ / zero_ of a uint8 tensor measure torch's byte-fill kernel (3.9 TB/s here), not the HBM write
+ceiling; tools/micro/write_bw.cu measures plain, streaming and TMA bulk stores (6.2-7.4 TB/s)."""
 import torch
 
 
